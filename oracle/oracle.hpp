@@ -1,0 +1,936 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// CPU restatement of the reference `adipc` hot path (StiffGIPC, arXiv
+// 2411.06224): Hessian assembly (sort + hash/segment reduction + two-level
+// affine-body reduction), MAS preconditioner construction/apply, block Jacobi
+// and PCG. Every function cites the reference file:line it follows; paths are
+// relative to /root/reference/proj/include/adipc/.
+//
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+// --impl reference leg may load this code, and only as the checker or as the
+// timed CPU baseline. The product path (paper_2411_06224_b200/) never links
+// or calls it.
+//
+// The reference cannot be compiled here (Eigen 3.4, Catch2 and CLI11 are
+// absent), so the arithmetic Eigen performs (3x3 products, LLT, dots) is
+// restated with plain loops. Results Eigen produces are pinned by the
+// reference's tests to tolerance only; everything integer (keys, sort order,
+// partitions, hierarchies) and the deterministic reductions are bit-exact.
+// Compiled like the reference: -O2 -fopenmp, no FMA contraction.
+#pragma once
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <stdexcept>
+#include <thread>
+#include <utility>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace oracle {
+
+using Real = double;  // core/types.hpp:9
+using Index = std::int32_t;  // core/types.hpp:10
+constexpr Index kInvalid = -1;  // core/types.hpp:31
+
+// Eigen::Matrix3d / Vector3d stand-ins, column-major storage like Eigen
+// (Mat3::data()[k] walks columns).
+struct Vec3 {
+    Real v[3] = {0, 0, 0};
+    Real& operator[](int i) { return v[i]; }
+    Real operator[](int i) const { return v[i]; }
+    Vec3& operator+=(const Vec3& o) {
+        for (int i = 0; i < 3; ++i) v[i] += o.v[i];
+        return *this;
+    }
+    bool operator==(const Vec3& o) const {
+        return v[0] == o.v[0] && v[1] == o.v[1] && v[2] == o.v[2];
+    }
+};
+
+struct Mat3 {
+    Real m[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // column-major
+    Real& operator()(int r, int c) { return m[3 * c + r]; }
+    Real operator()(int r, int c) const { return m[3 * c + r]; }
+    Real* data() { return m; }
+    const Real* data() const { return m; }
+    static Mat3 identity() {
+        Mat3 a;
+        a.m[0] = a.m[4] = a.m[8] = 1;
+        return a;
+    }
+    Mat3 transpose() const {
+        Mat3 t;
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) t(r, c) = (*this)(c, r);
+        return t;
+    }
+    Mat3& operator+=(const Mat3& o) {
+        for (int k = 0; k < 9; ++k) m[k] += o.m[k];
+        return *this;
+    }
+    bool operator==(const Mat3& o) const {
+        for (int k = 0; k < 9; ++k)
+            if (m[k] != o.m[k]) return false;
+        return true;
+    }
+    // Eigen's lazy fixed-size product: ((a0 b0 + a1 b1) + a2 b2).
+    Vec3 operator*(const Vec3& x) const {
+        Vec3 y;
+        for (int r = 0; r < 3; ++r)
+            y[r] = (*this)(r, 0) * x[0] + (*this)(r, 1) * x[1] + (*this)(r, 2) * x[2];
+        return y;
+    }
+    // Mat3::inverse via the adjugate (block_jacobi.hpp:13 uses Eigen's
+    // closed-form cofactor inverse for 3x3).
+    Mat3 inverse() const {
+        const Mat3& a = *this;
+        Mat3 cof;
+        cof(0, 0) = a(1, 1) * a(2, 2) - a(1, 2) * a(2, 1);
+        cof(1, 0) = a(1, 2) * a(2, 0) - a(1, 0) * a(2, 2);
+        cof(2, 0) = a(1, 0) * a(2, 1) - a(1, 1) * a(2, 0);
+        const Real det = a(0, 0) * cof(0, 0) + a(0, 1) * cof(1, 0) + a(0, 2) * cof(2, 0);
+        cof(0, 1) = a(0, 2) * a(2, 1) - a(0, 1) * a(2, 2);
+        cof(1, 1) = a(0, 0) * a(2, 2) - a(0, 2) * a(2, 0);
+        cof(2, 1) = a(0, 1) * a(2, 0) - a(0, 0) * a(2, 1);
+        cof(0, 2) = a(0, 1) * a(1, 2) - a(0, 2) * a(1, 1);
+        cof(1, 2) = a(0, 2) * a(1, 0) - a(0, 0) * a(1, 2);
+        cof(2, 2) = a(0, 0) * a(1, 1) - a(0, 1) * a(1, 0);
+        Mat3 inv;
+        for (int k = 0; k < 9; ++k) inv.m[k] = cof.m[k] / det;
+        return inv;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// core/parallel.hpp:18-70
+struct ExecPolicy {
+    bool deterministic = false;
+    int threads = 0;
+    int lane_width = 32;
+};
+
+inline int& process_thread_default() {  // parallel.hpp:24-34
+    static int n = [] {
+        if (const char* env = std::getenv("ADIPC_THREADS")) {
+            int v = std::atoi(env);
+            if (v > 0) return v;
+        }
+        unsigned hw = std::thread::hardware_concurrency();
+        return hw > 0 ? static_cast<int>(hw) : 1;
+    }();
+    return n;
+}
+
+inline int effective_threads(const ExecPolicy& pol) {  // parallel.hpp:40-43
+    if (pol.deterministic) return 1;
+    return pol.threads > 0 ? pol.threads : process_thread_default();
+}
+
+template <class F>
+void parallel_for(std::int64_t n, const ExecPolicy& pol, F&& fn) {  // parallel.hpp:46-58
+    const int nt = effective_threads(pol);
+    if (nt <= 1 || n < 2) {
+        for (std::int64_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(nt)
+    for (std::int64_t i = 0; i < n; ++i) fn(i);
+#else
+    for (std::int64_t i = 0; i < n; ++i) fn(i);
+#endif
+}
+
+inline void atomic_add(Real& slot, Real v) {  // parallel.hpp:60-62
+    std::atomic_ref<Real>(slot).fetch_add(v, std::memory_order_relaxed);
+}
+inline void atomic_add(Vec3& slot, const Vec3& v) {
+    for (int k = 0; k < 3; ++k) atomic_add(slot.v[k], v.v[k]);
+}
+inline void atomic_add(Mat3& slot, const Mat3& v) {
+    for (int k = 0; k < 9; ++k) atomic_add(slot.m[k], v.m[k]);
+}
+
+// ---------------------------------------------------------------------------
+// sparse/block_coo.hpp:13-21
+inline std::uint64_t make_block_key(std::uint32_t row, std::uint32_t col) {
+    return (static_cast<std::uint64_t>(row) << 32) | col;
+}
+inline std::uint32_t block_key_row(std::uint64_t k) { return static_cast<std::uint32_t>(k >> 32); }
+inline std::uint32_t block_key_col(std::uint64_t k) {
+    return static_cast<std::uint32_t>(k & 0xFFFFFFFFu);
+}
+
+// sparse/block_coo.hpp:25-51
+struct BlockTripletStream {
+    std::vector<std::uint64_t> keys;
+    std::vector<Mat3> values;
+    std::size_t size() const { return keys.size(); }
+    void emit(Index r, Index c, const Mat3& m) {
+        if (r <= c) {
+            keys.push_back(make_block_key(r, c));
+            values.push_back(m);
+        } else {
+            keys.push_back(make_block_key(c, r));
+            values.push_back(m.transpose());
+        }
+    }
+    void append(const BlockTripletStream& o) {
+        keys.insert(keys.end(), o.keys.begin(), o.keys.end());
+        values.insert(values.end(), o.values.begin(), o.values.end());
+    }
+};
+
+// sparse/block_coo.hpp:54-61
+struct SortedSymBlockCoo {
+    Index n_block_rows = 0;
+    std::vector<std::uint32_t> rows, cols;
+    std::vector<Mat3> blocks;
+    std::size_t size() const { return blocks.size(); }
+};
+
+// sparse/block_coo.hpp:67-101 — serial stable LSD radix sort, 4 x 16 bits,
+// always four passes (the "skip" comment at :82 is not implemented).
+inline void radix_sort_keys(std::vector<std::uint64_t>& keys, std::vector<std::uint32_t>& perm) {
+    const std::size_t n = keys.size();
+    perm.resize(n);
+    for (std::size_t i = 0; i < n; ++i) perm[i] = static_cast<std::uint32_t>(i);
+    if (n < 2) return;
+    std::vector<std::uint64_t> kbuf(n);
+    std::vector<std::uint32_t> pbuf(n);
+    constexpr int kBits = 16;
+    constexpr std::size_t kBuckets = std::size_t(1) << kBits;
+    std::vector<std::size_t> count(kBuckets);
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = pass * kBits;
+        std::fill(count.begin(), count.end(), 0);
+        for (std::size_t i = 0; i < n; ++i) ++count[(keys[i] >> shift) & (kBuckets - 1)];
+        std::size_t sum = 0;
+        for (std::size_t b = 0; b < kBuckets; ++b) {
+            std::size_t c = count[b];
+            count[b] = sum;
+            sum += c;
+        }
+        for (std::size_t i = 0; i < n; ++i) {
+            const std::size_t b = (keys[i] >> shift) & (kBuckets - 1);
+            kbuf[count[b]] = keys[i];
+            pbuf[count[b]] = perm[i];
+            ++count[b];
+        }
+        keys.swap(kbuf);
+        perm.swap(pbuf);
+    }
+}
+
+// sparse/block_coo.hpp:106-113
+inline void sort_stream(BlockTripletStream& s, const ExecPolicy& pol) {
+    std::vector<std::uint32_t> perm;
+    radix_sort_keys(s.keys, perm);
+    std::vector<Mat3> sorted(s.values.size());
+    parallel_for(static_cast<std::int64_t>(perm.size()), pol,
+                 [&](std::int64_t i) { sorted[i] = s.values[perm[i]]; });
+    s.values.swap(sorted);
+}
+
+// ---------------------------------------------------------------------------
+// sparse/reduction.hpp:30-79. V is Real, Vec3 or Mat3 (tests use all three).
+inline void zero_value(Real& v) { v = 0; }
+inline void zero_value(Vec3& v) { v = Vec3(); }
+inline void zero_value(Mat3& v) { v = Mat3(); }
+
+template <class V>
+std::vector<V> fast_segment_reduction(const std::vector<Index>& O, const std::vector<V>& values,
+                                      Index n_segments, const ExecPolicy& pol) {
+    const std::size_t n = values.size();
+    if (O.size() != n) throw std::invalid_argument("segment map size mismatch");
+    std::vector<V> R(n_segments);
+    for (auto& r : R) zero_value(r);
+    if (n == 0) return R;
+    if (pol.deterministic) {  // reduction.hpp:39-53
+        Index seg = O[0];
+        V sum = values[0];
+        for (std::size_t i = 1; i < n; ++i) {
+            if (O[i] == seg) {
+                sum += values[i];
+            } else {
+                R[seg] = sum;
+                seg = O[i];
+                sum = values[i];
+            }
+        }
+        R[seg] = sum;
+        return R;
+    }
+    const std::size_t w = static_cast<std::size_t>(pol.lane_width);  // reduction.hpp:55-77
+    const std::int64_t n_groups = static_cast<std::int64_t>((n + w - 1) / w);
+    parallel_for(n_groups, pol, [&](std::int64_t gi) {
+        const std::size_t begin = static_cast<std::size_t>(gi) * w;
+        const std::size_t end = std::min(begin + w, n);
+        std::size_t i = begin;
+        while (i < end) {
+            const Index seg = O[i];
+            V sum = values[i];
+            std::size_t j = i + 1;
+            while (j < end && O[j] == seg) {
+                sum += values[j];
+                ++j;
+            }
+            const bool cl = (i == begin && begin > 0 && O[begin - 1] == seg);
+            const bool cr = (j == end && end < n && O[end] == seg);
+            if (cl || cr)
+                atomic_add(R[seg], sum);
+            else
+                R[seg] = sum;
+            i = j;
+        }
+    });
+    return R;
+}
+
+// sparse/reduction.hpp:83-107 (serial O scan + head rows/cols)
+inline SortedSymBlockCoo fast_hash_reduction(const BlockTripletStream& sorted, Index n_block_rows,
+                                             const ExecPolicy& pol) {
+    SortedSymBlockCoo out;
+    out.n_block_rows = n_block_rows;
+    const std::size_t n = sorted.size();
+    if (n == 0) return out;
+    std::vector<Index> O(n);
+    O[0] = 0;
+    for (std::size_t i = 1; i < n; ++i)
+        O[i] = O[i - 1] + (sorted.keys[i - 1] != sorted.keys[i] ? 1 : 0);
+    const Index n_unique = O[n - 1] + 1;
+    out.rows.resize(n_unique);
+    out.cols.resize(n_unique);
+    for (std::size_t i = 0; i < n; ++i)
+        if (i == 0 || O[i] != O[i - 1]) {
+            out.rows[O[i]] = block_key_row(sorted.keys[i]);
+            out.cols[O[i]] = block_key_col(sorted.keys[i]);
+        }
+    out.blocks = fast_segment_reduction(O, sorted.values, n_unique, pol);
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// sparse/srbk_spmv.hpp:13-49
+inline std::vector<Vec3> srbk_spmv(const SortedSymBlockCoo& A, const std::vector<Vec3>& x,
+                                   const ExecPolicy& pol) {
+    std::vector<Vec3> y(x.size());
+    const std::size_t n = A.size();
+    if (n == 0) return y;
+    if (effective_threads(pol) <= 1) {
+        for (std::size_t e = 0; e < n; ++e) {
+            const Index r = A.rows[e], c = A.cols[e];
+            y[r] += A.blocks[e] * x[c];
+            if (r != c) y[c] += A.blocks[e].transpose() * x[r];
+        }
+        return y;
+    }
+    const std::size_t w = static_cast<std::size_t>(pol.lane_width);
+    const std::int64_t n_groups = static_cast<std::int64_t>((n + w - 1) / w);
+    parallel_for(n_groups, pol, [&](std::int64_t gi) {
+        const std::size_t begin = static_cast<std::size_t>(gi) * w;
+        const std::size_t end = std::min(begin + w, n);
+        std::size_t i = begin;
+        while (i < end) {
+            const std::uint32_t row = A.rows[i];
+            Vec3 run;
+            std::size_t j = i;
+            for (; j < end && A.rows[j] == row; ++j) {
+                run += A.blocks[j] * x[A.cols[j]];
+                if (A.cols[j] != row) atomic_add(y[A.cols[j]], A.blocks[j].transpose() * x[row]);
+            }
+            atomic_add(y[row], run);
+            i = j;
+        }
+    });
+    return y;
+}
+
+// ---------------------------------------------------------------------------
+// sparse/block_split.hpp:10-33. Large blocks are dense column-major arrays.
+struct MatRC {  // small dense column-major matrix (Mat12, Mat12x3, Mat3x12)
+    int rows = 0, cols = 0;
+    std::vector<Real> a;
+    MatRC() = default;
+    MatRC(int r, int c) : rows(r), cols(c), a(static_cast<std::size_t>(r) * c, 0.0) {}
+    Real& operator()(int r, int c) { return a[static_cast<std::size_t>(c) * rows + r]; }
+    Real operator()(int r, int c) const { return a[static_cast<std::size_t>(c) * rows + r]; }
+    Mat3 block3(int r0, int c0) const {
+        Mat3 b;
+        for (int c = 0; c < 3; ++c)
+            for (int r = 0; r < 3; ++r) b(r, c) = (*this)(r0 + r, c0 + c);
+        return b;
+    }
+    MatRC transpose() const {
+        MatRC t(cols, rows);
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c) t(c, r) = (*this)(r, c);
+        return t;
+    }
+};
+
+// Eigen's dynamic-free product for small fixed matrices: inner-product order k=0..K-1.
+inline MatRC matmul(const MatRC& A, const MatRC& B) {
+    MatRC C(A.rows, B.cols);
+    for (int c = 0; c < B.cols; ++c)
+        for (int r = 0; r < A.rows; ++r) {
+            Real s = A(r, 0) * B(0, c);
+            for (int k = 1; k < A.cols; ++k) s += A(r, k) * B(k, c);
+            C(r, c) = s;
+        }
+    return C;
+}
+
+inline MatRC from_mat3(const Mat3& m) {
+    MatRC a(3, 3);
+    for (int k = 0; k < 9; ++k) a.a[k] = m.m[k];
+    return a;
+}
+
+inline void split_12x12(Index row_base, Index col_base, const MatRC& H, BlockTripletStream& out) {
+    for (int ti = 0; ti < 4; ++ti)
+        for (int tj = 0; tj < 4; ++tj) out.emit(row_base + ti, col_base + tj, H.block3(3 * ti, 3 * tj));
+}
+inline void split_sym_12x12(Index base, const MatRC& H, BlockTripletStream& out) {
+    for (int ti = 0; ti < 4; ++ti)
+        for (int tj = ti; tj < 4; ++tj) out.emit(base + ti, base + tj, H.block3(3 * ti, 3 * tj));
+}
+inline void split_12x3(Index row_base, Index col, const MatRC& H, BlockTripletStream& out) {
+    for (int t = 0; t < 4; ++t) out.emit(row_base + t, col, H.block3(3 * t, 0));
+}
+inline void split_3x12(Index row, Index col_base, const MatRC& H, BlockTripletStream& out) {
+    for (int t = 0; t < 4; ++t) out.emit(row, col_base + t, H.block3(0, 3 * t));
+}
+
+// sparse/abd_reduce.hpp:11-27
+struct DofMap {
+    Index n_fem_nodes = 0;
+    Index n_bodies = 0;
+    std::vector<Index> abd_node_body;
+    std::vector<MatRC> abd_node_jacobian;  // 3x12 each
+    Index n_nodes() const { return n_fem_nodes + static_cast<Index>(abd_node_body.size()); }
+    Index n_blocks() const { return n_fem_nodes + 4 * n_bodies; }
+    bool is_fem(Index node) const { return node < n_fem_nodes; }
+    Index body_of(Index node) const { return abd_node_body[node - n_fem_nodes]; }
+    Index body_block_base(Index body) const { return n_fem_nodes + 4 * body; }
+    const MatRC& jacobian(Index node) const { return abd_node_jacobian[node - n_fem_nodes]; }
+};
+
+// sparse/abd_reduce.hpp:32-74
+inline BlockTripletStream two_level_abd_reduce(const BlockTripletStream& node_pairs, const DofMap& map,
+                                               const ExecPolicy& pol) {
+    BlockTripletStream sorted = node_pairs;
+    sort_stream(sorted, pol);
+    SortedSymBlockCoo merged = fast_hash_reduction(sorted, map.n_nodes(), pol);
+    BlockTripletStream out;
+    for (std::size_t e = 0; e < merged.size(); ++e) {
+        const Index i = static_cast<Index>(merged.rows[e]);
+        const Index j = static_cast<Index>(merged.cols[e]);
+        const MatRC C = from_mat3(merged.blocks[e]);
+        const bool fi = map.is_fem(i), fj = map.is_fem(j);
+        if (fi && fj) {
+            out.emit(i, j, merged.blocks[e]);
+        } else if (fi && !fj) {
+            split_3x12(i, map.body_block_base(map.body_of(j)), matmul(C, map.jacobian(j)), out);
+        } else if (!fi && fj) {  // unreachable for canonical keys (abd_reduce.hpp:52-54)
+            split_12x3(map.body_block_base(map.body_of(i)), j, matmul(map.jacobian(i).transpose(), C),
+                       out);
+        } else {
+            const Index bi = map.body_of(i), bj = map.body_of(j);
+            const MatRC JiT = map.jacobian(i).transpose();
+            if (bi != bj) {
+                split_12x12(map.body_block_base(bi), map.body_block_base(bj),
+                            matmul(matmul(JiT, C), map.jacobian(j)), out);
+            } else if (i == j) {
+                split_sym_12x12(map.body_block_base(bi), matmul(matmul(JiT, C), map.jacobian(i)), out);
+            } else {
+                const MatRC K = matmul(matmul(JiT, C), map.jacobian(j));
+                MatRC S(12, 12);
+                for (int r = 0; r < 12; ++r)
+                    for (int c = 0; c < 12; ++c) S(r, c) = K(r, c) + K(c, r);
+                split_sym_12x12(map.body_block_base(bi), S, out);
+            }
+        }
+    }
+    return out;
+}
+
+// solver/incremental_potential.hpp:410-425
+inline void filter_pinned(BlockTripletStream& s, const std::vector<char>& slot_pinned) {
+    std::size_t w = 0;
+    for (std::size_t i = 0; i < s.size(); ++i) {
+        const Index r = block_key_row(s.keys[i]);
+        const Index c = block_key_col(s.keys[i]);
+        if (slot_pinned[r] || slot_pinned[c]) continue;
+        s.keys[w] = s.keys[i];
+        s.values[w] = s.values[i];
+        ++w;
+    }
+    s.keys.resize(w);
+    s.values.resize(w);
+    for (Index slot = 0; slot < static_cast<Index>(slot_pinned.size()); ++slot)
+        if (slot_pinned[slot]) s.emit(slot, slot, Mat3::identity());
+}
+
+// ---------------------------------------------------------------------------
+// precond/partition.hpp:12-32
+inline Index subdomain_count(Index v, Index n, Index n_o) {
+    const Index eff = n - n_o;
+    return (v + eff - 1) / eff;
+}
+
+struct Partition {
+    std::vector<Index> part_of;
+    Index n_parts = 0;
+    Index capacity = 0;
+};
+
+inline Partition chunk_partition(Index v, Index capacity) {
+    Partition p;
+    p.capacity = capacity;
+    p.part_of.resize(v);
+    for (Index i = 0; i < v; ++i) p.part_of[i] = i / capacity;
+    p.n_parts = v == 0 ? 0 : (v - 1) / capacity + 1;
+    return p;
+}
+
+using Edge = std::pair<Index, Index>;
+
+// partition.hpp:37-50
+inline std::vector<std::vector<Index>> adjacency_lists(Index v, const std::vector<Edge>& edges) {
+    std::vector<std::vector<Index>> adj(v);
+    for (const auto& [a, b] : edges) {
+        if (a == b) continue;
+        adj[a].push_back(b);
+        adj[b].push_back(a);
+    }
+    for (auto& n : adj) {
+        std::sort(n.begin(), n.end());
+        n.erase(std::unique(n.begin(), n.end()), n.end());
+    }
+    return adj;
+}
+
+// partition.hpp:54-77
+inline std::vector<std::vector<Index>> connected_components(const std::vector<std::vector<Index>>& adj) {
+    const Index v = static_cast<Index>(adj.size());
+    std::vector<std::vector<Index>> comps;
+    std::vector<char> seen(v, 0);
+    std::vector<Index> queue;
+    for (Index start = 0; start < v; ++start) {
+        if (seen[start]) continue;
+        comps.emplace_back();
+        auto& comp = comps.back();
+        seen[start] = 1;
+        queue.assign(1, start);
+        for (std::size_t head = 0; head < queue.size(); ++head) {
+            const Index cur = queue[head];
+            comp.push_back(cur);
+            for (Index nb : adj[cur])
+                if (!seen[nb]) {
+                    seen[nb] = 1;
+                    queue.push_back(nb);
+                }
+        }
+    }
+    return comps;
+}
+
+// partition.hpp:88-159 — next-fit packing (only the single open part is
+// tried, :106-111) + greedy max-connectivity cluster growth.
+inline Partition partition_block_graph(Index v, const std::vector<Edge>& edges, Index capacity) {
+    Partition p;
+    p.capacity = capacity;
+    p.part_of.assign(v, 0);
+    const auto adj = adjacency_lists(v, edges);
+    const auto comps = connected_components(adj);
+    std::vector<char> assigned(v, 0);
+    std::vector<Index> conn(v, 0);
+    std::vector<Index> cand, touched;
+    Index next_part = 0;
+    Index open_part = kInvalid;
+    Index open_fill = 0;
+    for (const auto& comp : comps) {
+        const Index size = static_cast<Index>(comp.size());
+        if (size <= capacity) {
+            if (open_part == kInvalid || open_fill + size > capacity) {
+                open_part = next_part++;
+                open_fill = 0;
+            }
+            for (Index slot : comp) p.part_of[slot] = open_part;
+            open_fill += size;
+            continue;
+        }
+        const Index chunks = subdomain_count(size, capacity, 0);
+        const Index base = size / chunks, extra = size % chunks;
+        std::size_t seed_at = 0;
+        Index chunk = 0, left = size;
+        while (left > 0) {
+            const Index target = chunk < chunks ? base + (chunk < extra ? 1 : 0) : capacity;
+            ++chunk;
+            while (assigned[comp[seed_at]]) ++seed_at;
+            Index pick = comp[seed_at];
+            const Index part = next_part++;
+            cand.clear();
+            touched.clear();
+            for (Index fill = 0; pick != kInvalid;) {
+                p.part_of[pick] = part;
+                assigned[pick] = 1;
+                ++fill;
+                --left;
+                if (fill == target || left == 0) break;
+                for (Index nb : adj[pick])
+                    if (!assigned[nb]) {
+                        if (conn[nb] == 0) {
+                            cand.push_back(nb);
+                            touched.push_back(nb);
+                        }
+                        ++conn[nb];
+                    }
+                pick = kInvalid;
+                Index best = 0;
+                for (Index c : cand)
+                    if (!assigned[c] && (pick == kInvalid || conn[c] > best || (conn[c] == best && c < pick))) {
+                        pick = c;
+                        best = conn[c];
+                    }
+            }
+            for (Index t : touched) conn[t] = 0;
+        }
+    }
+    p.n_parts = next_part;
+    return p;
+}
+
+// ---------------------------------------------------------------------------
+// precond/hierarchy.hpp:15-28
+struct MasHierarchy {
+    Index capacity = 0;
+    Index n_slots = 0;
+    struct Level {
+        Index n_nodes = 0;
+        Index n_parts = 0;
+        std::vector<Index> part_of;
+        std::vector<Index> agg;
+    };
+    std::vector<Level> levels;
+    int n_levels() const { return static_cast<int>(levels.size()); }
+};
+
+// hierarchy.hpp:30-100
+inline MasHierarchy build_hierarchy(const Partition& l0, const std::vector<Edge>& edges, int max_levels) {
+    MasHierarchy h;
+    h.capacity = l0.capacity;
+    h.n_slots = static_cast<Index>(l0.part_of.size());
+    MasHierarchy::Level base;
+    base.n_nodes = h.n_slots;
+    base.n_parts = l0.n_parts;
+    base.part_of = l0.part_of;
+    base.agg.resize(h.n_slots);
+    for (Index i = 0; i < h.n_slots; ++i) base.agg[i] = i;
+    h.levels.push_back(std::move(base));
+    std::vector<Edge> cur_edges = edges;
+    while (h.n_levels() < max_levels) {
+        const MasHierarchy::Level& cur = h.levels.back();
+        if (cur.n_parts <= 1) break;
+        auto adj = adjacency_lists(cur.n_nodes, cur_edges);
+        std::vector<std::vector<Index>> members(cur.n_parts);
+        for (Index i = 0; i < cur.n_nodes; ++i) members[cur.part_of[i]].push_back(i);
+        std::vector<Index> up(cur.n_nodes, kInvalid);
+        Index n_next = 0;
+        std::vector<Index> queue;
+        for (Index s = 0; s < cur.n_parts; ++s)
+            for (Index seed : members[s]) {
+                if (up[seed] != kInvalid) continue;
+                const Index super = n_next++;
+                up[seed] = super;
+                queue.assign(1, seed);
+                for (std::size_t head = 0; head < queue.size(); ++head)
+                    for (Index nb : adj[queue[head]])
+                        if (cur.part_of[nb] == s && up[nb] == kInvalid) {
+                            up[nb] = super;
+                            queue.push_back(nb);
+                        }
+            }
+        if (n_next == cur.n_nodes) break;
+        std::vector<Edge> next_edges;
+        next_edges.reserve(cur_edges.size());
+        for (const auto& [a, b] : cur_edges) {
+            Index ua = up[a], ub = up[b];
+            if (ua == ub) continue;
+            if (ua > ub) std::swap(ua, ub);
+            next_edges.emplace_back(ua, ub);
+        }
+        std::sort(next_edges.begin(), next_edges.end());
+        next_edges.erase(std::unique(next_edges.begin(), next_edges.end()), next_edges.end());
+        MasHierarchy::Level next;
+        next.n_nodes = n_next;
+        Partition grouped = partition_block_graph(n_next, next_edges, h.capacity);
+        next.n_parts = grouped.n_parts;
+        next.part_of = std::move(grouped.part_of);
+        next.agg.resize(h.n_slots);
+        for (Index slot = 0; slot < h.n_slots; ++slot) next.agg[slot] = up[cur.agg[slot]];
+        h.levels.push_back(std::move(next));
+        cur_edges = std::move(next_edges);
+    }
+    return h;
+}
+
+// ---------------------------------------------------------------------------
+// precond/mas.hpp:19-25
+inline std::vector<Edge> block_edges(const SortedSymBlockCoo& A) {
+    std::vector<Edge> e;
+    e.reserve(A.rows.size());
+    for (std::size_t i = 0; i < A.rows.size(); ++i)
+        if (A.rows[i] != A.cols[i]) e.emplace_back(A.rows[i], A.cols[i]);
+    return e;
+}
+
+// Dense column-major square matrix + Eigen::LLT restatement (unblocked,
+// lower, right-looking like Eigen's llt_inplace::unblocked: fail iff a pivot
+// x <= 0; a NaN pivot does not fail, as in Eigen).
+struct DenseLLT {
+    int n = 0;
+    std::vector<Real> L;  // column-major lower factor
+    bool ok = false;
+    bool compute(const std::vector<Real>& A, int dim) {
+        n = dim;
+        L = A;
+        auto at = [&](int r, int c) -> Real& { return L[static_cast<std::size_t>(c) * n + r]; };
+        for (int k = 0; k < n; ++k) {
+            Real x = at(k, k);
+            for (int j = 0; j < k; ++j) x -= at(k, j) * at(k, j);
+            if (x <= 0) {
+                ok = false;
+                return false;
+            }
+            x = std::sqrt(x);
+            at(k, k) = x;
+            for (int i = k + 1; i < n; ++i) {
+                Real s = at(i, k);
+                for (int j = 0; j < k; ++j) s -= at(i, j) * at(k, j);
+                at(i, k) = s / x;
+            }
+        }
+        for (int c = 0; c < n; ++c)
+            for (int r = 0; r < c; ++r) at(r, c) = 0;
+        ok = true;
+        return true;
+    }
+    std::vector<Real> solve(const std::vector<Real>& b) const {
+        std::vector<Real> y = b;
+        auto at = [&](int r, int c) { return L[static_cast<std::size_t>(c) * n + r]; };
+        for (int i = 0; i < n; ++i) {
+            Real s = y[i];
+            for (int j = 0; j < i; ++j) s -= at(i, j) * y[j];
+            y[i] = s / at(i, i);
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            Real s = y[i];
+            for (int j = i + 1; j < n; ++j) s -= at(j, i) * y[j];
+            y[i] = s / at(i, i);
+        }
+        return y;
+    }
+};
+
+struct Preconditioner {  // mas.hpp:12-15
+    virtual ~Preconditioner() = default;
+    virtual void apply(const std::vector<Real>& r, std::vector<Real>& z) const = 0;
+};
+
+class MasPreconditioner : public Preconditioner {  // mas.hpp:32-115
+public:
+    struct LevelData {
+        std::vector<Index> agg, part_of, pos_of;
+        std::vector<std::vector<std::pair<Index, Index>>> sub_slots;
+        std::vector<std::vector<Real>> dense;  // column-major 3f x 3f
+        std::vector<int> dim;
+        std::vector<DenseLLT> factor;
+    };
+    std::vector<LevelData> levels_;
+    // counts regularisation shifts applied, for parity checks of the retry rule
+    long shifts_applied = 0;
+
+    // mas.hpp:34-83
+    void build(const SortedSymBlockCoo& A, const MasHierarchy& h) {
+        levels_.assign(h.n_levels(), LevelData{});
+        shifts_applied = 0;
+        const Index n_slots = h.n_slots;
+        for (int l = 0; l < h.n_levels(); ++l) {
+            const auto& hl = h.levels[l];
+            LevelData& ld = levels_[l];
+            ld.agg = hl.agg;
+            ld.part_of = hl.part_of;
+            ld.pos_of.assign(hl.n_nodes, 0);
+            std::vector<Index> fill(hl.n_parts, 0);
+            for (Index node = 0; node < hl.n_nodes; ++node) ld.pos_of[node] = fill[hl.part_of[node]]++;
+            ld.dense.resize(hl.n_parts);
+            ld.dim.resize(hl.n_parts);
+            for (Index s = 0; s < hl.n_parts; ++s) {
+                ld.dim[s] = 3 * fill[s];
+                ld.dense[s].assign(static_cast<std::size_t>(ld.dim[s]) * ld.dim[s], 0.0);
+            }
+            ld.sub_slots.assign(hl.n_parts, {});
+            for (Index slot = 0; slot < n_slots; ++slot) {
+                const Index node = ld.agg[slot];
+                ld.sub_slots[ld.part_of[node]].emplace_back(slot, ld.pos_of[node]);
+            }
+            for (std::size_t i = 0; i < A.rows.size(); ++i) {  // mas.hpp:56-64
+                const Index r = A.rows[i], c = A.cols[i];
+                const Index nr = ld.agg[r], nc = ld.agg[c];
+                if (ld.part_of[nr] != ld.part_of[nc]) continue;
+                const Index s = ld.part_of[nr];
+                auto& D = ld.dense[s];
+                const int d = ld.dim[s];
+                const Index pr = ld.pos_of[nr], pc = ld.pos_of[nc];
+                for (int cc = 0; cc < 3; ++cc)
+                    for (int rr = 0; rr < 3; ++rr) {
+                        D[static_cast<std::size_t>(3 * pc + cc) * d + 3 * pr + rr] += A.blocks[i](rr, cc);
+                    }
+                if (r != c)
+                    for (int cc = 0; cc < 3; ++cc)
+                        for (int rr = 0; rr < 3; ++rr)
+                            D[static_cast<std::size_t>(3 * pr + cc) * d + 3 * pc + rr] += A.blocks[i](cc, rr);
+            }
+            ld.factor.resize(hl.n_parts);
+            for (Index s = 0; s < hl.n_parts; ++s) {  // mas.hpp:66-81
+                std::vector<Real> D = ld.dense[s];
+                const int d = ld.dim[s];
+                Real tr = 0;
+                for (int k = 0; k < d; ++k) tr += D[static_cast<std::size_t>(k) * d + k];
+                Real eps = 1e-8 * tr / d;
+                if (!(eps > 0)) eps = 1e-12;
+                for (int attempt = 0;; ++attempt) {
+                    if (ld.factor[s].compute(D, d)) break;
+                    if (attempt >= 3)
+                        throw std::runtime_error("subdomain matrix stayed indefinite after regularization");
+                    for (int k = 0; k < d; ++k) D[static_cast<std::size_t>(k) * d + k] += eps;
+                    eps *= 100;
+                    ++shifts_applied;
+                }
+            }
+        }
+    }
+
+    // mas.hpp:85-99
+    void apply(const std::vector<Real>& r, std::vector<Real>& z) const override {
+        z.assign(r.size(), 0.0);
+        ExecPolicy pol;
+        for (const LevelData& ld : levels_) {
+            parallel_for(static_cast<Index>(ld.sub_slots.size()), pol, [&](std::int64_t s) {
+                const auto& slots = ld.sub_slots[s];
+                std::vector<Real> b(ld.dim[s], 0.0);
+                for (const auto& [slot, pos] : slots)
+                    for (int k = 0; k < 3; ++k) b[3 * pos + k] += r[3 * slot + k];
+                const std::vector<Real> y = ld.factor[s].solve(b);
+                for (const auto& [slot, pos] : slots)
+                    for (int k = 0; k < 3; ++k) z[3 * slot + k] += y[3 * pos + k];
+            });
+        }
+    }
+};
+
+// precond/block_jacobi.hpp:8-26
+class BlockJacobiPreconditioner : public Preconditioner {
+public:
+    std::vector<Mat3> inv_;
+    void build(const SortedSymBlockCoo& A) {
+        inv_.assign(A.n_block_rows, Mat3::identity());
+        for (std::size_t i = 0; i < A.rows.size(); ++i)
+            if (A.rows[i] == A.cols[i]) inv_[A.rows[i]] = A.blocks[i].inverse();
+    }
+    void apply(const std::vector<Real>& r, std::vector<Real>& z) const override {
+        z.resize(r.size());
+        ExecPolicy pol;
+        parallel_for(static_cast<Index>(inv_.size()), pol, [&](std::int64_t i) {
+            Vec3 ri;
+            for (int k = 0; k < 3; ++k) ri[k] = r[3 * i + k];
+            const Vec3 zi = inv_[i] * ri;
+            for (int k = 0; k < 3; ++k) z[3 * i + k] = zi[k];
+        });
+    }
+};
+
+// ---------------------------------------------------------------------------
+// solver/pcg.hpp:10-88. Dot products and axpys are single-threaded loops
+// (Eigen VecX ops in the reference run on one thread).
+struct PcgResult {
+    int iters = 0;
+    Real rel_residual = 0;
+    bool converged = false;
+};
+
+inline Real dot(const std::vector<Real>& a, const std::vector<Real>& b) {
+    Real s = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+    return s;
+}
+
+inline PcgResult pcg_solve(const SortedSymBlockCoo& A, const std::vector<Real>& b, const Preconditioner& M,
+                           Real rel_tol, int restart, int max_iters, const ExecPolicy& pol,
+                           std::vector<Real>& x) {
+    PcgResult out;
+    const std::size_t n = b.size();
+    x.assign(n, 0.0);
+    if (dot(b, b) == 0) {
+        out.converged = true;
+        return out;
+    }
+    std::vector<Vec3> sin, sout;
+    auto apply_a = [&](const std::vector<Real>& v, std::vector<Real>& av) {  // pcg.hpp:45-49
+        sin.resize(n / 3);
+        for (std::size_t i = 0; i < sin.size(); ++i)
+            for (int k = 0; k < 3; ++k) sin[i][k] = v[3 * i + k];
+        sout = srbk_spmv(A, sin, pol);
+        av.resize(3 * sout.size());
+        for (std::size_t i = 0; i < sout.size(); ++i)
+            for (int k = 0; k < 3; ++k) av[3 * i + k] = sout[i][k];
+    };
+    std::vector<Real> r = b, z, p, ap;
+    M.apply(r, z);
+    p = z;
+    Real rho = dot(r, z);
+    const Real rho0 = rho;
+    if (!(rho0 > 0)) return out;
+    const Real stop = rel_tol * rel_tol * rho0;
+    for (int k = 1; k <= max_iters; ++k) {
+        apply_a(p, ap);
+        const Real p_ap = dot(p, ap);
+        if (!(p_ap > 0)) {
+            out.iters = k - 1;
+            out.rel_residual = std::sqrt(std::abs(rho) / rho0);
+            return out;
+        }
+        const Real alpha = rho / p_ap;
+        for (std::size_t i = 0; i < n; ++i) x[i] += alpha * p[i];
+        if (restart > 0 && k % restart == 0) {
+            apply_a(x, ap);
+            for (std::size_t i = 0; i < n; ++i) r[i] = b[i] - ap[i];
+        } else {
+            for (std::size_t i = 0; i < n; ++i) r[i] -= alpha * ap[i];
+        }
+        M.apply(r, z);
+        const Real rho_next = dot(r, z);
+        out.iters = k;
+        if (rho_next <= stop) {
+            out.rel_residual = std::sqrt(std::abs(rho_next) / rho0);
+            out.converged = true;
+            return out;
+        }
+        const Real beta = rho_next / rho;
+        for (std::size_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+        rho = rho_next;
+    }
+    out.rel_residual = std::sqrt(std::abs(rho) / rho0);
+    return out;
+}
+
+}  // namespace oracle

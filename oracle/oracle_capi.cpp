@@ -1,0 +1,399 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.hpp header).
+//
+// extern "C" surface over the restated reference so pytest (ctypes) and the
+// bench's CPU-baseline leg can drive it with plain pointers. Layout
+// conventions match the product C-ABI (include/adipc_gpu.h): keys u64[T],
+// blocks 9 doubles column-major (Eigen Mat3 storage), vectors flat 3n doubles.
+// Also exposes the reference tests' std::mt19937 draws so the Python ports of
+// the reference tests consume the identical random sequences.
+#include <cstring>
+#include <random>
+#include <string>
+
+#include "oracle.hpp"
+
+using namespace oracle;
+
+namespace {
+
+thread_local std::string g_err;
+
+ExecPolicy make_pol(int det, int threads, int lane_width) {
+    ExecPolicy p;
+    p.deterministic = det != 0;
+    p.threads = threads;
+    p.lane_width = lane_width > 0 ? lane_width : 32;
+    return p;
+}
+
+BlockTripletStream load_stream(const std::uint64_t* keys, const double* vals, std::size_t T) {
+    BlockTripletStream s;
+    s.keys.assign(keys, keys + T);
+    s.values.resize(T);
+    if (T) std::memcpy(s.values.data(), vals, T * 9 * sizeof(double));
+    return s;
+}
+
+void store_stream(const BlockTripletStream& s, std::uint64_t* keys, double* vals) {
+    if (s.size() == 0) return;
+    std::memcpy(keys, s.keys.data(), s.size() * sizeof(std::uint64_t));
+    std::memcpy(vals, s.values.data(), s.size() * 9 * sizeof(double));
+}
+
+SortedSymBlockCoo load_matrix(std::int32_t n_block_rows, std::size_t U, const std::uint32_t* rows,
+                              const std::uint32_t* cols, const double* blocks) {
+    SortedSymBlockCoo A;
+    A.n_block_rows = n_block_rows;
+    A.rows.assign(rows, rows + U);
+    A.cols.assign(cols, cols + U);
+    A.blocks.resize(U);
+    if (U) std::memcpy(A.blocks.data(), blocks, U * 9 * sizeof(double));
+    return A;
+}
+
+std::vector<Edge> load_edges(const std::int32_t* pairs, std::size_t n) {
+    std::vector<Edge> e(n);
+    for (std::size_t i = 0; i < n; ++i) e[i] = {pairs[2 * i], pairs[2 * i + 1]};
+    return e;
+}
+
+DofMap load_map(std::int32_t n_fem, std::int32_t n_bodies, std::size_t n_abd, const std::int32_t* body,
+                const double* jac36) {
+    DofMap m;
+    m.n_fem_nodes = n_fem;
+    m.n_bodies = n_bodies;
+    m.abd_node_body.assign(body, body + n_abd);
+    m.abd_node_jacobian.resize(n_abd, MatRC(3, 12));
+    for (std::size_t i = 0; i < n_abd; ++i)
+        std::memcpy(m.abd_node_jacobian[i].a.data(), jac36 + 36 * i, 36 * sizeof(double));
+    return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* oracle_last_error() { return g_err.c_str(); }
+
+int oracle_max_threads() { return process_thread_default(); }
+
+void oracle_set_default_threads(int n) {  // parallel.hpp:36-38
+    if (n > 0) process_thread_default() = n;
+}
+
+// ---- keys -----------------------------------------------------------------
+std::uint64_t oracle_make_block_key(std::uint32_t r, std::uint32_t c) { return make_block_key(r, c); }
+
+// emit(): canonicalise one block into (key, value); returns the key.
+std::uint64_t oracle_emit(std::int32_t r, std::int32_t c, const double* m9, double* out9) {
+    BlockTripletStream s;
+    Mat3 m;
+    std::memcpy(m.m, m9, sizeof(m.m));
+    s.emit(r, c, m);
+    std::memcpy(out9, s.values[0].m, sizeof(m.m));
+    return s.keys[0];
+}
+
+// ---- sort / reduce ----------------------------------------------------------
+void oracle_radix_sort_keys(std::uint64_t* keys, std::uint32_t* perm, std::size_t T) {
+    std::vector<std::uint64_t> k(keys, keys + T);
+    std::vector<std::uint32_t> p;
+    radix_sort_keys(k, p);
+    if (T) {
+        std::memcpy(keys, k.data(), T * sizeof(std::uint64_t));
+        std::memcpy(perm, p.data(), T * sizeof(std::uint32_t));
+    }
+}
+
+void oracle_sort_stream(std::uint64_t* keys, double* vals, std::size_t T, int det, int threads, int lw) {
+    BlockTripletStream s = load_stream(keys, vals, T);
+    sort_stream(s, make_pol(det, threads, lw));
+    store_stream(s, keys, vals);
+}
+
+// Sorted stream -> SortedSymBlockCoo. Output buffers sized >= T. Returns U.
+std::int64_t oracle_fast_hash_reduction(const std::uint64_t* keys, const double* vals, std::size_t T,
+                                        std::int32_t n_block_rows, int det, int threads, int lw,
+                                        std::uint32_t* rows, std::uint32_t* cols, double* blocks) {
+    const BlockTripletStream s = load_stream(keys, vals, T);
+    const SortedSymBlockCoo A = fast_hash_reduction(s, n_block_rows, make_pol(det, threads, lw));
+    const std::size_t U = A.size();
+    if (U) {
+        std::memcpy(rows, A.rows.data(), U * 4);
+        std::memcpy(cols, A.cols.data(), U * 4);
+        std::memcpy(blocks, A.blocks.data(), U * 72);
+    }
+    return static_cast<std::int64_t>(U);
+}
+
+// width: 1 (Real), 3 (Vec3) or 9 (Mat3). Returns 0, or 1 on size mismatch
+// (std::invalid_argument in reduction.hpp:34).
+int oracle_segment_reduce(const std::int32_t* O, std::size_t nO, const double* V, std::size_t nV, int width,
+                          std::int32_t n_segments, int det, int threads, int lw, double* R) {
+    const ExecPolicy pol = make_pol(det, threads, lw);
+    const std::vector<Index> o(O, O + nO);
+    try {
+        if (width == 1) {
+            std::vector<Real> v(V, V + nV);
+            auto r = fast_segment_reduction(o, v, n_segments, pol);
+            std::memcpy(R, r.data(), r.size() * sizeof(Real));
+        } else if (width == 3) {
+            std::vector<Vec3> v(nV);
+            if (nV) std::memcpy(v.data(), V, nV * 24);
+            auto r = fast_segment_reduction(o, v, n_segments, pol);
+            if (!r.empty()) std::memcpy(R, r.data(), r.size() * 24);
+        } else if (width == 9) {
+            std::vector<Mat3> v(nV);
+            if (nV) std::memcpy(v.data(), V, nV * 72);
+            auto r = fast_segment_reduction(o, v, n_segments, pol);
+            if (!r.empty()) std::memcpy(R, r.data(), r.size() * 72);
+        } else {
+            g_err = "width must be 1, 3 or 9";
+            return 1;
+        }
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    }
+    return 0;
+}
+
+// ---- spmv ---------------------------------------------------------------
+void oracle_srbk_spmv(std::int32_t n_block_rows, std::size_t U, const std::uint32_t* rows,
+                      const std::uint32_t* cols, const double* blocks, const double* x, std::size_t nx,
+                      int det, int threads, int lw, double* y) {
+    const SortedSymBlockCoo A = load_matrix(n_block_rows, U, rows, cols, blocks);
+    std::vector<Vec3> xv(nx);
+    if (nx) std::memcpy(xv.data(), x, nx * 24);
+    auto yv = srbk_spmv(A, xv, make_pol(det, threads, lw));
+    if (nx) std::memcpy(y, yv.data(), nx * 24);
+}
+
+// ---- tiling / two-level ------------------------------------------------------
+// kind: 0 split_12x12(rb, cb), 1 split_sym_12x12(rb), 2 split_12x3(rb, cb),
+// 3 split_3x12(rb, cb). H column-major with its natural shape. Returns count.
+int oracle_split(int kind, std::int32_t rb, std::int32_t cb, const double* H, std::uint64_t* keys,
+                 double* vals) {
+    BlockTripletStream out;
+    if (kind == 0 || kind == 1) {
+        MatRC m(12, 12);
+        std::memcpy(m.a.data(), H, 144 * 8);
+        if (kind == 0)
+            split_12x12(rb, cb, m, out);
+        else
+            split_sym_12x12(rb, m, out);
+    } else if (kind == 2) {
+        MatRC m(12, 3);
+        std::memcpy(m.a.data(), H, 36 * 8);
+        split_12x3(rb, cb, m, out);
+    } else {
+        MatRC m(3, 12);
+        std::memcpy(m.a.data(), H, 36 * 8);
+        split_3x12(rb, cb, m, out);
+    }
+    store_stream(out, keys, vals);
+    return static_cast<int>(out.size());
+}
+
+// Output capacity must be >= 16 * Tn. Returns the tile count.
+std::int64_t oracle_two_level_abd_reduce(const std::uint64_t* keys, const double* vals, std::size_t Tn,
+                                         std::int32_t n_fem, std::int32_t n_bodies, std::size_t n_abd,
+                                         const std::int32_t* abd_node_body, const double* jac36, int det,
+                                         int threads, int lw, std::uint64_t* out_keys, double* out_vals) {
+    const BlockTripletStream s = load_stream(keys, vals, Tn);
+    const DofMap m = load_map(n_fem, n_bodies, n_abd, abd_node_body, jac36);
+    const BlockTripletStream t = two_level_abd_reduce(s, m, make_pol(det, threads, lw));
+    store_stream(t, out_keys, out_vals);
+    return static_cast<std::int64_t>(t.size());
+}
+
+// filter_pinned: output capacity >= T + n_slots. Returns new size.
+std::int64_t oracle_filter_pinned(const std::uint64_t* keys, const double* vals, std::size_t T,
+                                  const std::uint8_t* pinned, std::int32_t n_slots, std::uint64_t* out_keys,
+                                  double* out_vals) {
+    BlockTripletStream s = load_stream(keys, vals, T);
+    std::vector<char> p(pinned, pinned + n_slots);
+    filter_pinned(s, p);
+    store_stream(s, out_keys, out_vals);
+    return static_cast<std::int64_t>(s.size());
+}
+
+// ---- partition / hierarchy ----------------------------------------------------
+std::int32_t oracle_subdomain_count(std::int32_t v, std::int32_t n, std::int32_t n_o) {
+    return subdomain_count(v, n, n_o);
+}
+
+std::int32_t oracle_chunk_partition(std::int32_t v, std::int32_t cap, std::int32_t* part_of) {
+    const Partition p = chunk_partition(v, cap);
+    if (v) std::memcpy(part_of, p.part_of.data(), v * 4);
+    return p.n_parts;
+}
+
+std::int32_t oracle_partition_block_graph(std::int32_t v, const std::int32_t* pairs, std::size_t n_edges,
+                                          std::int32_t cap, std::int32_t* part_of) {
+    const Partition p = partition_block_graph(v, load_edges(pairs, n_edges), cap);
+    if (v) std::memcpy(part_of, p.part_of.data(), v * 4);
+    return p.n_parts;
+}
+
+std::int64_t oracle_block_edges(std::size_t U, const std::uint32_t* rows, const std::uint32_t* cols,
+                                std::int32_t* pairs) {
+    std::int64_t w = 0;
+    for (std::size_t i = 0; i < U; ++i)
+        if (rows[i] != cols[i]) {
+            pairs[2 * w] = static_cast<std::int32_t>(rows[i]);
+            pairs[2 * w + 1] = static_cast<std::int32_t>(cols[i]);
+            ++w;
+        }
+    return w;
+}
+
+void* oracle_build_hierarchy(const std::int32_t* part_of, std::int32_t n_slots, std::int32_t n_parts,
+                             std::int32_t capacity, const std::int32_t* pairs, std::size_t n_edges,
+                             int max_levels) {
+    Partition l0;
+    l0.part_of.assign(part_of, part_of + n_slots);
+    l0.n_parts = n_parts;
+    l0.capacity = capacity;
+    return new MasHierarchy(build_hierarchy(l0, load_edges(pairs, n_edges), max_levels));
+}
+void oracle_hierarchy_free(void* h) { delete static_cast<MasHierarchy*>(h); }
+int oracle_hierarchy_n_levels(void* h) { return static_cast<MasHierarchy*>(h)->n_levels(); }
+void oracle_hierarchy_level(void* hp, int l, std::int32_t* n_nodes, std::int32_t* n_parts,
+                            std::int32_t* part_of, std::int32_t* agg) {
+    const auto& L = static_cast<MasHierarchy*>(hp)->levels[l];
+    *n_nodes = L.n_nodes;
+    *n_parts = L.n_parts;
+    if (part_of && L.n_nodes) std::memcpy(part_of, L.part_of.data(), L.n_nodes * 4);
+    if (agg && !L.agg.empty()) std::memcpy(agg, L.agg.data(), L.agg.size() * 4);
+}
+
+// ---- preconditioners ------------------------------------------------------------
+struct OracleMatrix {
+    SortedSymBlockCoo A;
+};
+
+void* oracle_matrix_new(std::int32_t n_block_rows, std::size_t U, const std::uint32_t* rows,
+                        const std::uint32_t* cols, const double* blocks) {
+    return new OracleMatrix{load_matrix(n_block_rows, U, rows, cols, blocks)};
+}
+void oracle_matrix_free(void* m) { delete static_cast<OracleMatrix*>(m); }
+
+// Returns a MasPreconditioner*, or null with oracle_last_error() set
+// (std::runtime_error of mas.hpp:74-77).
+void* oracle_mas_build(void* mat, void* hier) {
+    auto* M = new MasPreconditioner();
+    try {
+        M->build(static_cast<OracleMatrix*>(mat)->A, *static_cast<MasHierarchy*>(hier));
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        delete M;
+        return nullptr;
+    }
+    return M;
+}
+void oracle_precond_free(void* p) { delete static_cast<Preconditioner*>(p); }
+long oracle_mas_shifts(void* p) { return static_cast<MasPreconditioner*>(p)->shifts_applied; }
+int oracle_mas_n_levels(void* p) { return static_cast<int>(static_cast<MasPreconditioner*>(p)->levels_.size()); }
+// dim of subdomain s at level l; copies the dense restricted matrix if out != null
+int oracle_mas_level_matrix(void* p, int l, std::int32_t s, double* out) {
+    const auto& ld = static_cast<MasPreconditioner*>(p)->levels_[l];
+    if (out) std::memcpy(out, ld.dense[s].data(), ld.dense[s].size() * 8);
+    return ld.dim[s];
+}
+
+void* oracle_jacobi_build(void* mat) {
+    auto* J = new BlockJacobiPreconditioner();
+    J->build(static_cast<OracleMatrix*>(mat)->A);
+    return J;
+}
+
+void oracle_precond_apply(void* p, const double* r, std::size_t n, double* z) {
+    std::vector<Real> rv(r, r + n), zv;
+    static_cast<Preconditioner*>(p)->apply(rv, zv);
+    std::memcpy(z, zv.data(), n * 8);
+}
+
+int oracle_pcg_solve(void* mat, const double* b, std::size_t n, void* precond, double rel_tol, int restart,
+                     int max_iters, int det, int threads, int lw, double* x, int* iters, double* rel_residual,
+                     int* converged) {
+    std::vector<Real> bv(b, b + n), xv;
+    const PcgResult r = pcg_solve(static_cast<OracleMatrix*>(mat)->A, bv, *static_cast<Preconditioner*>(precond),
+                                  rel_tol, restart, max_iters, make_pol(det, threads, lw), xv);
+    std::memcpy(x, xv.data(), n * 8);
+    *iters = r.iters;
+    *rel_residual = r.rel_residual;
+    *converged = r.converged ? 1 : 0;
+    return 0;
+}
+
+// ---- the reference tests' random draws (libstdc++ std::mt19937) -------------------
+void* oracle_rng_new(std::uint32_t seed) { return new std::mt19937(seed); }
+void oracle_rng_free(void* g) { delete static_cast<std::mt19937*>(g); }
+
+struct Dist {
+    int kind;  // 0 uniform_int, 1 normal, 2 uniform_real
+    std::uniform_int_distribution<long> ui;
+    std::normal_distribution<double> nd;
+    std::uniform_real_distribution<double> ur;
+};
+void* oracle_dist_uniform_int(long a, long b) { return new Dist{0, std::uniform_int_distribution<long>(a, b), {}, {}}; }
+void* oracle_dist_normal(double m, double s) { return new Dist{1, {}, std::normal_distribution<double>(m, s), {}}; }
+void* oracle_dist_uniform_real(double a, double b) {
+    return new Dist{2, {}, {}, std::uniform_real_distribution<double>(a, b)};
+}
+void oracle_dist_free(void* d) { delete static_cast<Dist*>(d); }
+// std::uniform_int_distribution<int> and <long> draw identically for these
+// ranges in libstdc++ (both downscale one 32-bit mt19937 output).
+double oracle_dist_draw(void* dp, void* gp) {
+    auto* d = static_cast<Dist*>(dp);
+    auto& g = *static_cast<std::mt19937*>(gp);
+    if (d->kind == 0) return static_cast<double>(d->ui(g));
+    if (d->kind == 1) return d->nd(g);
+    return d->ur(g);
+}
+void oracle_dist_fill(void* dp, void* gp, double* out, std::size_t n) {
+    for (std::size_t i = 0; i < n; ++i) out[i] = oracle_dist_draw(dp, gp);
+}
+
+// test_block_sparse.cpp:40-52 / verify_suites.hpp:106-119 random_stream:
+// fresh distributions per call, B.data()[k] column-major, symmetrised
+// diagonal blocks, canonicalising emit. Buffers sized >= n_entries.
+void oracle_random_stream(void* gp, int n_blocks, int n_entries, std::uint64_t* keys, double* vals) {
+    auto& rng = *static_cast<std::mt19937*>(gp);
+    std::uniform_int_distribution<int> pick(0, n_blocks - 1);
+    std::normal_distribution<Real> val(0.0, 1.0);
+    BlockTripletStream s;
+    for (int i = 0; i < n_entries; ++i) {
+        Mat3 B;
+        for (int k = 0; k < 9; ++k) B.data()[k] = val(rng);
+        const Index r = pick(rng), c = pick(rng);
+        if (r == c) {
+            const Mat3 t = B.transpose();
+            Mat3 sym;
+            for (int k = 0; k < 9; ++k) sym.m[k] = B.m[k] + t.m[k];
+            B = sym;
+        }
+        s.emit(r, c, B);
+    }
+    store_stream(s, keys, vals);
+}
+
+// test_precond.cpp:17-23 / test_solver.cpp:15-21 random_spd3 with a fresh
+// uniform(-1,1) per call: g g^T + shift I (Eigen lazy product order).
+void oracle_random_spd3(void* gp, double shift, double* out9) {
+    auto& rng = *static_cast<std::mt19937*>(gp);
+    std::uniform_real_distribution<Real> u(-1, 1);
+    Mat3 g;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) g(r, c) = u(rng);
+    Mat3 m;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            m(r, c) = g(r, 0) * g(c, 0) + g(r, 1) * g(c, 1) + g(r, 2) * g(c, 2);
+            if (r == c) m(r, c) += shift;
+        }
+    std::memcpy(out9, m.m, 72);
+}
+
+}  // extern "C"

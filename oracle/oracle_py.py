@@ -1,0 +1,397 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+ctypes wrappers over ``oracle/build/liboracle.so`` (the C++ restatement of
+the reference hot path, see ``oracle/oracle.hpp``). Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline / reference legs
+may import this module; the product package never does.
+
+Array conventions (shared with the product C-ABI, include/adipc_gpu.h):
+keys uint64[T]; blocks float64[T, 9] column-major (Eigen ``Mat3::data()``
+order); vectors float64[3n]; edges int32[E, 2].
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "build", "liboracle.so")
+
+u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+vp = C.c_void_p
+sz = C.c_size_t
+i32 = C.c_int32
+i64 = C.c_int64
+ci = C.c_int
+cd = C.c_double
+
+
+def build() -> None:
+    """Compile the oracle with its Makefile (g++ -O2 -fopenmp)."""
+    subprocess.check_call(["make", "-s", "-C", _HERE])
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        build()
+    L = C.CDLL(_LIB_PATH)
+    sig = {
+        "oracle_last_error": (C.c_char_p, []),
+        "oracle_max_threads": (ci, []),
+        "oracle_set_default_threads": (None, [ci]),
+        "oracle_make_block_key": (C.c_uint64, [C.c_uint32, C.c_uint32]),
+        "oracle_emit": (C.c_uint64, [i32, i32, f64p, f64p]),
+        "oracle_radix_sort_keys": (None, [u64p, u32p, sz]),
+        "oracle_sort_stream": (None, [u64p, f64p, sz, ci, ci, ci]),
+        "oracle_fast_hash_reduction": (i64, [u64p, f64p, sz, i32, ci, ci, ci, u32p, u32p, f64p]),
+        "oracle_segment_reduce": (ci, [i32p, sz, f64p, sz, ci, i32, ci, ci, ci, f64p]),
+        "oracle_srbk_spmv": (None, [i32, sz, u32p, u32p, f64p, f64p, sz, ci, ci, ci, f64p]),
+        "oracle_split": (ci, [ci, i32, i32, f64p, u64p, f64p]),
+        "oracle_two_level_abd_reduce": (i64, [u64p, f64p, sz, i32, i32, sz, i32p, f64p, ci, ci, ci, u64p, f64p]),
+        "oracle_filter_pinned": (i64, [u64p, f64p, sz, u8p, i32, u64p, f64p]),
+        "oracle_subdomain_count": (i32, [i32, i32, i32]),
+        "oracle_chunk_partition": (i32, [i32, i32, i32p]),
+        "oracle_partition_block_graph": (i32, [i32, i32p, sz, i32, i32p]),
+        "oracle_block_edges": (i64, [sz, u32p, u32p, i32p]),
+        "oracle_build_hierarchy": (vp, [i32p, i32, i32, i32, i32p, sz, ci]),
+        "oracle_hierarchy_free": (None, [vp]),
+        "oracle_hierarchy_n_levels": (ci, [vp]),
+        "oracle_hierarchy_level": (None, [vp, ci, C.POINTER(i32), C.POINTER(i32), vp, vp]),
+        "oracle_matrix_new": (vp, [i32, sz, u32p, u32p, f64p]),
+        "oracle_matrix_free": (None, [vp]),
+        "oracle_mas_build": (vp, [vp, vp]),
+        "oracle_precond_free": (None, [vp]),
+        "oracle_mas_shifts": (C.c_long, [vp]),
+        "oracle_mas_n_levels": (ci, [vp]),
+        "oracle_mas_level_matrix": (ci, [vp, ci, i32, vp]),
+        "oracle_jacobi_build": (vp, [vp]),
+        "oracle_precond_apply": (None, [vp, f64p, sz, f64p]),
+        "oracle_pcg_solve": (ci, [vp, f64p, sz, vp, cd, ci, ci, ci, ci, ci, f64p,
+                                  C.POINTER(ci), C.POINTER(cd), C.POINTER(ci)]),
+        "oracle_rng_new": (vp, [C.c_uint32]),
+        "oracle_rng_free": (None, [vp]),
+        "oracle_dist_uniform_int": (vp, [C.c_long, C.c_long]),
+        "oracle_dist_normal": (vp, [cd, cd]),
+        "oracle_dist_uniform_real": (vp, [cd, cd]),
+        "oracle_dist_free": (None, [vp]),
+        "oracle_dist_draw": (cd, [vp, vp]),
+        "oracle_dist_fill": (None, [vp, vp, f64p, sz]),
+        "oracle_random_stream": (None, [vp, ci, ci, u64p, f64p]),
+        "oracle_random_spd3": (None, [vp, cd, f64p]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _pol(policy):
+    if policy is None:
+        return 0, 0, 32
+    return int(bool(policy.deterministic)), int(policy.threads), int(policy.lane_width)
+
+
+class ExecPolicy:
+    """core/parallel.hpp:18-22."""
+
+    def __init__(self, deterministic=False, threads=0, lane_width=32):
+        self.deterministic = deterministic
+        self.threads = threads
+        self.lane_width = lane_width
+
+
+# ---------------------------------------------------------------- RNG ------
+class Rng:
+    """std::mt19937 of the reference tests (libstdc++ draws)."""
+
+    def __init__(self, seed: int):
+        self.h = lib().oracle_rng_new(seed)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().oracle_rng_free(self.h)
+            self.h = None
+
+
+class _Dist:
+    def __init__(self, h):
+        self.h = h
+
+    def __call__(self, rng: Rng):
+        return lib().oracle_dist_draw(self.h, rng.h)
+
+    def fill(self, rng: Rng, n: int) -> np.ndarray:
+        out = np.empty(n, np.float64)
+        lib().oracle_dist_fill(self.h, rng.h, out, n)
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().oracle_dist_free(self.h)
+            self.h = None
+
+
+class UniformInt(_Dist):
+    def __init__(self, a, b):
+        super().__init__(lib().oracle_dist_uniform_int(a, b))
+
+    def __call__(self, rng):
+        return int(super().__call__(rng))
+
+
+class Normal(_Dist):
+    def __init__(self, m=0.0, s=1.0):
+        super().__init__(lib().oracle_dist_normal(m, s))
+
+
+class UniformReal(_Dist):
+    def __init__(self, a, b):
+        super().__init__(lib().oracle_dist_uniform_real(a, b))
+
+
+def random_stream(rng: Rng, n_blocks: int, n_entries: int):
+    keys = np.empty(n_entries, np.uint64)
+    vals = np.empty((n_entries, 9), np.float64)
+    lib().oracle_random_stream(rng.h, n_blocks, n_entries, keys, vals)
+    return keys, vals
+
+
+def random_spd3(rng: Rng, shift: float = 1.0) -> np.ndarray:
+    out = np.empty(9, np.float64)
+    lib().oracle_random_spd3(rng.h, shift, out)
+    return out
+
+
+# --------------------------------------------------------------- sparse ----
+def make_block_key(r, c):
+    return lib().oracle_make_block_key(r, c)
+
+
+def emit(r, c, m9):
+    out = np.empty(9, np.float64)
+    k = lib().oracle_emit(r, c, np.ascontiguousarray(m9, np.float64), out)
+    return k, out
+
+
+def radix_sort_keys(keys):
+    k = np.array(keys, np.uint64)
+    perm = np.empty(len(k), np.uint32)
+    lib().oracle_radix_sort_keys(k, perm, len(k))
+    return k, perm
+
+
+def sort_stream(keys, vals, policy=None):
+    k = np.array(keys, np.uint64)
+    v = np.array(vals, np.float64).reshape(-1, 9).copy()
+    lib().oracle_sort_stream(k, v, len(k), *_pol(policy))
+    return k, v
+
+
+def fast_hash_reduction(keys, vals, n_block_rows, policy=None):
+    k = np.ascontiguousarray(keys, np.uint64)
+    v = np.ascontiguousarray(vals, np.float64).reshape(-1, 9)
+    T = len(k)
+    rows = np.empty(max(T, 1), np.uint32)
+    cols = np.empty(max(T, 1), np.uint32)
+    blocks = np.empty((max(T, 1), 9), np.float64)
+    U = lib().oracle_fast_hash_reduction(k, v, T, n_block_rows, *_pol(policy), rows, cols, blocks)
+    return rows[:U].copy(), cols[:U].copy(), blocks[:U].copy()
+
+
+def fast_segment_reduction(O, V, n_segments, policy=None):
+    O = np.ascontiguousarray(O, np.int32)
+    V = np.ascontiguousarray(V, np.float64)
+    width = 1 if V.ndim == 1 else V.shape[1]
+    nV = V.shape[0]
+    R = np.empty((max(n_segments, 1), width), np.float64)
+    rc = lib().oracle_segment_reduce(O, len(O), V.reshape(-1) if nV else np.zeros(1), nV, width,
+                                     n_segments, *_pol(policy), R)
+    if rc != 0:
+        raise ValueError(lib().oracle_last_error().decode())
+    R = R[:n_segments]
+    return R[:, 0].copy() if width == 1 else R.copy()
+
+
+def srbk_spmv(n_block_rows, rows, cols, blocks, x, policy=None):
+    x = np.ascontiguousarray(x, np.float64).reshape(-1)
+    nx = len(x) // 3
+    y = np.empty(max(3 * nx, 1), np.float64)
+    U = len(rows)
+    lib().oracle_srbk_spmv(n_block_rows, U, np.ascontiguousarray(rows, np.uint32) if U else np.zeros(1, np.uint32),
+                           np.ascontiguousarray(cols, np.uint32) if U else np.zeros(1, np.uint32),
+                           np.ascontiguousarray(blocks, np.float64).reshape(-1) if U else np.zeros(9),
+                           x if nx else np.zeros(3), nx, *_pol(policy), y)
+    return y[: 3 * nx].copy()
+
+
+SPLIT_12x12, SPLIT_SYM_12x12, SPLIT_12x3, SPLIT_3x12 = 0, 1, 2, 3
+
+
+def split(kind, rb, cb, H):
+    """H given as a 2-D numpy array in natural shape (row, col)."""
+    Hc = np.ascontiguousarray(np.asarray(H, np.float64).T).reshape(-1)  # column-major
+    keys = np.empty(16, np.uint64)
+    vals = np.empty((16, 9), np.float64)
+    n = lib().oracle_split(kind, rb, cb, Hc, keys, vals)
+    return keys[:n].copy(), vals[:n].copy()
+
+
+def two_level_abd_reduce(keys, vals, n_fem, n_bodies, abd_node_body, jac36, policy=None):
+    k = np.ascontiguousarray(keys, np.uint64)
+    v = np.ascontiguousarray(vals, np.float64).reshape(-1, 9)
+    body = np.ascontiguousarray(abd_node_body, np.int32)
+    jac = np.ascontiguousarray(jac36, np.float64).reshape(-1)
+    cap = max(16 * len(k), 1)
+    ok = np.empty(cap, np.uint64)
+    ov = np.empty((cap, 9), np.float64)
+    n = lib().oracle_two_level_abd_reduce(k, v, len(k), n_fem, n_bodies, len(body),
+                                          body if len(body) else np.zeros(1, np.int32),
+                                          jac if len(jac) else np.zeros(1), *_pol(policy), ok, ov)
+    return ok[:n].copy(), ov[:n].copy()
+
+
+def filter_pinned(keys, vals, pinned):
+    k = np.ascontiguousarray(keys, np.uint64)
+    v = np.ascontiguousarray(vals, np.float64).reshape(-1, 9)
+    p = np.ascontiguousarray(pinned, np.uint8)
+    cap = len(k) + len(p) + 1
+    ok = np.empty(cap, np.uint64)
+    ov = np.empty((cap, 9), np.float64)
+    n = lib().oracle_filter_pinned(k, v, len(k), p, len(p), ok, ov)
+    return ok[:n].copy(), ov[:n].copy()
+
+
+# -------------------------------------------------------------- precond ----
+def subdomain_count(v, n, n_o):
+    return lib().oracle_subdomain_count(v, n, n_o)
+
+
+def _edges(edges):
+    e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
+    return (e if len(e) else np.zeros((1, 2), np.int32)), len(e)
+
+
+def chunk_partition(v, cap):
+    part = np.empty(max(v, 1), np.int32)
+    n = lib().oracle_chunk_partition(v, cap, part)
+    return part[:v].copy(), n
+
+
+def partition_block_graph(v, edges, cap):
+    e, ne = _edges(edges)
+    part = np.empty(max(v, 1), np.int32)
+    n = lib().oracle_partition_block_graph(v, e, ne, cap, part)
+    return part[:v].copy(), n
+
+
+def block_edges(rows, cols):
+    U = len(rows)
+    out = np.empty((max(U, 1), 2), np.int32)
+    n = lib().oracle_block_edges(U, np.ascontiguousarray(rows, np.uint32), np.ascontiguousarray(cols, np.uint32), out)
+    return out[:n].copy()
+
+
+class Hierarchy:
+    """MasHierarchy (hierarchy.hpp:15-28) restated."""
+
+    def __init__(self, part_of, n_parts, capacity, edges, max_levels):
+        part_of = np.ascontiguousarray(part_of, np.int32)
+        e, ne = _edges(edges)
+        self.n_slots = len(part_of)
+        self.capacity = capacity
+        self.h = lib().oracle_build_hierarchy(part_of if len(part_of) else np.zeros(1, np.int32),
+                                              self.n_slots, n_parts, capacity, e, ne, max_levels)
+        self.levels = []
+        for l in range(lib().oracle_hierarchy_n_levels(self.h)):
+            nn, npart = i32(), i32()
+            lib().oracle_hierarchy_level(self.h, l, C.byref(nn), C.byref(npart), None, None)
+            part = np.empty(max(nn.value, 1), np.int32)
+            agg = np.empty(max(self.n_slots, 1), np.int32)
+            lib().oracle_hierarchy_level(self.h, l, C.byref(nn), C.byref(npart),
+                                         part.ctypes.data_as(vp), agg.ctypes.data_as(vp))
+            self.levels.append(dict(n_nodes=nn.value, n_parts=npart.value,
+                                    part_of=part[: nn.value].copy(), agg=agg[: self.n_slots].copy()))
+
+    def n_levels(self):
+        return len(self.levels)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().oracle_hierarchy_free(self.h)
+            self.h = None
+
+
+class Matrix:
+    def __init__(self, n_block_rows, rows, cols, blocks):
+        self.n_block_rows = n_block_rows
+        U = len(rows)
+        self.h = lib().oracle_matrix_new(n_block_rows, U,
+                                         np.ascontiguousarray(rows, np.uint32) if U else np.zeros(1, np.uint32),
+                                         np.ascontiguousarray(cols, np.uint32) if U else np.zeros(1, np.uint32),
+                                         np.ascontiguousarray(blocks, np.float64).reshape(-1) if U else np.zeros(9))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().oracle_matrix_free(self.h)
+            self.h = None
+
+
+class _Precond:
+    def apply(self, r):
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty_like(r)
+        lib().oracle_precond_apply(self.h, r, len(r), z)
+        return z
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().oracle_precond_free(self.h)
+            self.h = None
+
+
+class MasPreconditioner(_Precond):
+    def __init__(self, mat: Matrix, hier: Hierarchy):
+        self.h = lib().oracle_mas_build(mat.h, hier.h)
+        if not self.h:
+            raise RuntimeError(lib().oracle_last_error().decode())
+
+    def n_levels(self):
+        return lib().oracle_mas_n_levels(self.h)
+
+    def shifts(self):
+        return lib().oracle_mas_shifts(self.h)
+
+    def level_matrix(self, l, s):
+        d = lib().oracle_mas_level_matrix(self.h, l, s, None)
+        out = np.empty(d * d, np.float64)
+        lib().oracle_mas_level_matrix(self.h, l, s, out.ctypes.data_as(vp))
+        return out.reshape(d, d).T.copy()  # column-major -> natural
+
+
+class BlockJacobiPreconditioner(_Precond):
+    def __init__(self, mat: Matrix):
+        self.h = lib().oracle_jacobi_build(mat.h)
+
+
+def pcg_solve(mat: Matrix, b, M: _Precond, rel_tol, restart, max_iters, policy=None):
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.empty_like(b)
+    it, rr, cv = ci(), cd(), ci()
+    lib().oracle_pcg_solve(mat.h, b, len(b), M.h, rel_tol, restart, max_iters, *_pol(policy), x,
+                           C.byref(it), C.byref(rr), C.byref(cv))
+    return x, dict(iters=it.value, rel_residual=rr.value, converged=bool(cv.value))

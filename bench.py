@@ -1,0 +1,441 @@
+"""Benchmark of the per-Newton linear-solve hot path on B200 (driver contract).
+
+Workload (BASELINE.json config 5): stiff FEM box make_box_tets(68,68,68),
+985,527 DOF, E = 1e8, x = 0 face pinned, first-Newton stable Neo-Hookean
+matrix; right-hand side b = A x*, x* ~ N(0,1) (seed 5 + rank). One *step* is
+one Newton linear solve through the C-ABI with the triplet stream resident in
+HBM: filter_pinned -> assembly (sort + reduce) -> MAS build (block_edges +
+hierarchy + restriction + batched inversion) -> PCG to rel_tol 1e-4
+(restart 250). Multi-GPU: one independent scene per rank (the cfg5 batch,
+weak scaling), no data-path collective; NCCL only gathers per-scene stats and
+the max-over-ranks timing.
+
+  value        PCG iterations / s over the PCG loops (metric's first half)
+  ms_per_step  one full Newton solve (assembly + MAS build + PCG)
+  e2e          the same metric through the host-pointer C-ABI calls
+               (adipc_gpu_assemble / build_preconditioner / adipc_gpu_pcg with
+               pinned host buffers; H2D of the stream and b, D2H of x inside)
+  roofline     dominant PCG kernel, algorithmic bytes / CUDA-event time
+  cpu_baseline the oracle restatement of the reference (kind "port"; the
+               reference itself cannot be built: no Eigen) on the host cores
+
+`--impl reference` times that CPU port alone, same metric/config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+REL_TOL, RESTART, MAX_ITERS, CAPACITY, MAX_LEVELS = 1e-4, 250, 100000, 16, 4
+METRIC = "PCG iterations/sec + ms per Newton solve; HBM GB/s vs roofline; speedup vs host CPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg5_stiff_box")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=10, help="PCG iterations per CPU sample step")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(MEASURED) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------- clocks ---
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                f = [x.strip() for x in out.stdout.strip().split(",")]
+                if len(f) >= 6:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- byte model ---
+def byte_model(n, U, levels):
+    """Algorithmic (compulsory) bytes per PCG iteration by kernel class
+    (DESIGN.md 'byte model'): fp64 values, u32/i32 indices,
+    explicit dense inverses as stored (full (3f)^2)."""
+    inv = []
+    for L in levels:
+        fill = np.bincount(L["part_of"], minlength=L["n_parts"]).astype(np.int64)
+        inv.append(int(np.sum((3 * fill) ** 2) * 8))
+    nc = len(levels) - 1
+    vec = 24 * n
+    spmv = 80 * U + vec + vec                      # A + p read + Ap written
+    l0 = inv[0] + 4 * n + 7 * vec                  # D0^-1, slots, x r/w, p, r r/w, Ap, z write
+    coarse = sum(inv[1:]) + nc * (4 * n + vec)     # D_l^-1, node_slots, r gathered per level
+    final = 3 * vec + nc * (4 * n) + vec           # z, p r/w, agg maps, Ap cleared
+    return {"spmv": spmv, "l0": l0, "coarse": coarse, "final": final,
+            "total": spmv + l0 + coarse + final, "inv_bytes": inv}
+
+
+# --------------------------------------------------------------- scenes ---
+def make_problem(config, seed):
+    from paper_2411_06224_b200 import scenes
+
+    sc = scenes.CONFIGS[config]()
+    return sc
+
+
+def cpu_reference(sc, rank_seed, cpu_iters, steps, warmup, sample_note=True):
+    """The oracle restatement (reference algorithm, -O2 -fopenmp, all host
+    threads): one-time assembly + MAS build, then timed steps of `cpu_iters`
+    PCG iterations each (the bounded sample)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O
+
+    cores = O.lib().oracle_max_threads()
+    par = O.ExecPolicy(deterministic=False, threads=cores)
+    t0 = time.perf_counter()
+    fk, fv = O.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    sk, sv = O.sort_stream(fk, fv, par)
+    rows, cols, blocks = O.fast_hash_reduction(sk, sv, sc.n_blocks, par)
+    t_asm = time.perf_counter() - t0
+    from paper_2411_06224_b200 import api as P  # host-only partition (no GPU call)
+
+    l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, CAPACITY)
+    t0 = time.perf_counter()
+    A = O.Matrix(sc.n_blocks, rows, cols, blocks)
+    H = O.Hierarchy(l0.part_of, l0.n_parts, CAPACITY, O.block_edges(rows, cols), MAX_LEVELS)
+    M = O.MasPreconditioner(A, H)
+    t_build = time.perf_counter() - t0
+    xs = np.random.default_rng(rank_seed).standard_normal(3 * sc.n_blocks)
+    b = O.srbk_spmv(sc.n_blocks, rows, cols, blocks, xs, par)
+    times = []
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        _, r = O.pcg_solve(A, b, M, 1e-30, RESTART, cpu_iters, par)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            times.append(dt)
+    it_s = cpu_iters / float(np.mean(times))
+    return {"value": it_s, "unit": "PCG iterations/s", "cores": cores, "kind": "port",
+            "sample": f"{steps} steps x {cpu_iters} PCG iterations (MAS-preconditioned, cfg5 matrix) after a "
+                      f"one-time assembly ({t_asm:.2f} s) and MAS build ({t_build:.2f} s); the reference's "
+                      f"serial stages (radix sort, O scan, restriction, LLT, hierarchy, PCG vector ops) stay serial",
+            "assembly_s": t_asm, "mas_build_s": t_build,
+            "ms_per_newton_solve_est": None}
+
+
+# -------------------------------------------------------------- main arm ---
+def run_ours(args, rank, world, local_rank, dist):
+    import torch
+
+    from paper_2411_06224_b200 import _lib
+    from paper_2411_06224_b200 import api as P
+    from paper_2411_06224_b200.context import Context
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    sc = make_problem(args.config, 5 + rank)
+    stream = torch.cuda.Stream(dev)
+    ctx = Context(local_rank, stream=stream)
+    ctx.set_option(_lib.OPT_PROFILE, 1)
+    l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, CAPACITY)
+    ctx.set_level0_partition(l0.part_of, l0.n_parts, CAPACITY, MAX_LEVELS)
+
+    with torch.cuda.stream(stream):
+        d_keys = torch.from_numpy(sc.keys.view(np.int64)).to(dev)
+        d_vals = torch.from_numpy(sc.vals).to(dev)
+        d_pin = torch.from_numpy(sc.pinned).to(dev)
+        T = len(sc.keys)
+        d_fk = torch.empty(T + sc.n_blocks, dtype=torch.int64, device=dev)
+        d_fv = torch.empty((T + sc.n_blocks, 9), dtype=torch.float64, device=dev)
+    stream.synchronize()
+    # filtered stream on device (filter_pinned, incremental_potential.hpp:410-425)
+    import ctypes as C
+
+    L = _lib.gpu()
+    nf = C.c_int64()
+
+    def filter_dev():
+        # device filter through the same kernels the host-pointer API uses
+        ctx._check(L.adipc_gpu_filter_pinned_device(ctx.h, d_keys.data_ptr(), d_vals.data_ptr(), T,
+                                                    d_pin.data_ptr(), sc.n_blocks, d_fk.data_ptr(), d_fv.data_ptr(),
+                                                    C.byref(nf)))
+        return nf.value
+
+    Tf = filter_dev()
+    ctx.assemble(d_fk[:Tf], d_fv[:Tf], sc.n_blocks)
+    n, U = ctx.matrix_info()
+    # b = A x*
+    xs = torch.from_numpy(np.random.default_rng(5 + rank).standard_normal(3 * n)).to(dev)
+    d_b = torch.empty(3 * n, dtype=torch.float64, device=dev)
+    d_x = torch.empty(3 * n, dtype=torch.float64, device=dev)
+    with torch.cuda.stream(stream):
+        ctx.spmv(xs, d_b)
+    stream.synchronize()
+
+    def step():
+        Tf = filter_dev()
+        ctx.assemble(d_fk[:Tf], d_fv[:Tf], sc.n_blocks)
+        ctx.build_preconditioner(_lib.PRECOND_MAS)
+        _, res = ctx.pcg(d_b, REL_TOL, RESTART, MAX_ITERS, x=d_x)
+        t = ctx.timings()
+        prof = ctx.pcg_profile()
+        return res, t, prof
+
+    for _ in range(args.warmup):
+        step()
+    levels = ctx.precond_levels()
+    bm = byte_model(n, U, levels)
+
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = Context.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    recs = []
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            recs.append(step())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = Context.kernel_launches() - launches0
+    total_ms = ev0.elapsed_time(ev1)
+    iters = sum(r.iters for r, _, _ in recs)
+    pcg_ms = sum(t["pcg_ms"] for _, t, _ in recs)
+    asm_ms = sum(t["assemble_ms"] for _, t, _ in recs)
+    build_ms = sum(t["build_ms"] for _, t, _ in recs)
+    prof = {k: sum(p[k] for _, _, p in recs) for k in ("spmv_ms", "l0_ms", "coarse_ms", "final_ms", "iters")}
+    res_last = recs[-1][0]
+    # solution check against x* (size-independent property at full size)
+    xerr = float(torch.linalg.norm(d_x - xs) / torch.linalg.norm(xs))
+
+    stats = dict(total_ms=total_ms, pcg_ms=pcg_ms, iters=iters, asm_ms=asm_ms, build_ms=build_ms,
+                 launches=launches, conv=bool(res_last.converged), rel=float(res_last.rel_residual), xerr=xerr)
+    if dist:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, stats)  # the only collective: per-scene stats
+    else:
+        gathered = [stats]
+    max_total = max(g["total_ms"] for g in gathered)
+    max_pcg = max(g["pcg_ms"] for g in gathered)
+    all_iters = sum(g["iters"] for g in gathered)
+
+    out = None
+    if rank == 0:
+        hbm, peak_src = peaks()
+        kernels = {}
+        for key, bkey in (("spmv", "spmv"), ("l0", "l0"), ("coarse", "coarse"), ("final", "final")):
+            ms = prof[key + "_ms"]
+            it = max(prof["iters"], 1)
+            avg_s = ms / it / 1000.0
+            kernels[key] = {"bytes_per_launch": bm[bkey], "avg_ms": ms / it,
+                            "achieved_gbs": bm[bkey] / avg_s / 1e9 if avg_s > 0 else None}
+        dom = max(kernels, key=lambda k: kernels[k]["avg_ms"])
+        dk = kernels[dom]
+        iter_s = (prof["spmv_ms"] + prof["l0_ms"] + prof["coarse_ms"] + prof["final_ms"]) / max(prof["iters"], 1) / 1e3
+        out = {
+            "metric": METRIC,
+            "value": all_iters / (max_pcg / 1000.0),
+            "unit": "PCG iterations/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": max_total / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (reference generators: make_box_tets + stable Neo-Hookean first-Newton matrix; "
+                    "b = A x*, x* ~ N(0,1) seed 5+rank)",
+            "config": {"workload": "cfg5: stiff FEM box 68^3 cells, 985,527 DOF, E=1e8, PCG-only Newton solve, "
+                                   "MAS cemas16 (4 levels), rel_tol 1e-4, restart 250; one scene per GPU",
+                       "n_block_rows": n, "n_blocks": U, "triplets": int(len(sc.keys)),
+                       "l2": "inputs larger than L2 (A 206 MB + MAS inverses 402 MB per scene)",
+                       "parallelism": f"{world} independent scenes (replicas of the single-GPU solve)"},
+            "ms_per_newton_solve": (sum(g["build_ms"] + g["pcg_ms"] for g in gathered[:1]) / args.steps),
+            "assembly_ms": asm_ms / args.steps,
+            "mas_build_ms": build_ms / args.steps,
+            "pcg_ms": pcg_ms / args.steps,
+            "pcg_iters_per_solve": iters / args.steps,
+            "converged": all(g["conv"] for g in gathered),
+            "rel_residual": res_last.rel_residual,
+            "solution_rel_err_vs_xstar": xerr,
+            "per_rank": gathered,
+            "gpu_launches": launches,
+            "kernels": kernels,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_gbs"], "peak": hbm,
+                         "peak_source": peak_src, "unit": "GB/s",
+                         "frac": (dk["achieved_gbs"] / hbm) if dk["achieved_gbs"] else None,
+                         "algorithmic_bytes_per_launch": dk["bytes_per_launch"], "traffic": None},
+            "roofline_pcg_iteration": {"bound": "hbm", "bytes_per_iter": bm["total"],
+                                       "achieved": bm["total"] / iter_s / 1e9, "peak": hbm, "unit": "GB/s",
+                                       "frac": bm["total"] / iter_s / 1e9 / hbm},
+            "clocks": clk.summary(),
+        }
+    # e2e through the host-pointer C-ABI (pinned host buffers)
+    if not args.no_e2e:
+        e2e = run_e2e(args, ctx, sc, d_b, stream, dev)
+        if dist:
+            g = [None] * world
+            dist.all_gather_object(g, e2e)
+        else:
+            g = [e2e]
+        if rank == 0:
+            tot = max(x["ms"] for x in g)
+            out["e2e"] = {"value": sum(x["iters"] for x in g) / (tot / 1000.0), "unit": "PCG iterations/s",
+                          "h2d_bytes_per_step": g[0]["h2d"], "d2h_bytes_per_step": g[0]["d2h"],
+                          "ms_per_step": tot / args.steps,
+                          "path": "adipc_gpu_filter_pinned + adipc_gpu_assemble + adipc_gpu_build_preconditioner "
+                                  "+ adipc_gpu_pcg (host pointers, pinned)"}
+    ctx.close()
+    return out, sc
+
+
+def run_e2e(args, ctx, sc, d_b, stream, dev):
+    import torch
+
+    from paper_2411_06224_b200 import _lib
+
+    L = _lib.gpu()
+    import ctypes as C
+
+    T = len(sc.keys)
+    h_keys = torch.from_numpy(sc.keys.view(np.int64)).pin_memory()
+    h_vals = torch.from_numpy(sc.vals).pin_memory()
+    h_pin = torch.from_numpy(sc.pinned).pin_memory()
+    h_fk = torch.empty(T + sc.n_blocks, dtype=torch.int64).pin_memory()
+    h_fv = torch.empty((T + sc.n_blocks, 9), dtype=torch.float64).pin_memory()
+    h_b = d_b.cpu().pin_memory()
+    h_x = torch.empty_like(h_b).pin_memory()
+    nf, U = C.c_int64(), C.c_int64()
+    it, rr, cv = C.c_int(), C.c_double(), C.c_int()
+
+    def step():
+        ctx._check(L.adipc_gpu_filter_pinned(ctx.h, h_keys.data_ptr(), h_vals.data_ptr(), T, h_pin.data_ptr(),
+                                             sc.n_blocks, h_fk.data_ptr(), h_fv.data_ptr(), C.byref(nf)))
+        ctx._check(L.adipc_gpu_assemble(ctx.h, h_fk.data_ptr(), h_fv.data_ptr(), nf.value, sc.n_blocks, 1,
+                                        C.byref(U)))
+        ctx._check(L.adipc_gpu_build_preconditioner(ctx.h, _lib.PRECOND_MAS))
+        ctx._check(L.adipc_gpu_pcg(ctx.h, h_b.data_ptr(), REL_TOL, RESTART, MAX_ITERS, h_x.data_ptr(), C.byref(it),
+                                   C.byref(rr), C.byref(cv)))
+        return it.value
+
+    for _ in range(max(1, args.warmup // 2)):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    iters = 0
+    for _ in range(args.steps):
+        iters += step()
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1000.0
+    n3 = 3 * sc.n_blocks
+    h2d = T * 80 + sc.n_blocks + nf.value * 80 + n3 * 8  # raw stream + pins, filtered stream, b
+    d2h = nf.value * 80 + n3 * 8                           # filtered stream back, x
+    return {"ms": ms, "iters": iters, "h2d": int(h2d), "d2h": int(d2h)}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from paper_2411_06224_b200 import scenes
+
+        sc = scenes.CONFIGS[args.config]()
+        cb = cpu_reference(sc, 5, args.cpu_iters, args.steps, args.warmup)
+        line = {"metric": METRIC, "value": cb["value"], "unit": "PCG iterations/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * args.cpu_iters / cb["value"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (same generator and seed as the GPU arm)",
+                "config": {"workload": "cfg5: stiff FEM box 68^3 cells, 985,527 DOF, E=1e8, MAS cemas16"},
+                "impl": "reference",
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "assembly_s": cb["assembly_s"], "mas_build_s": cb["mas_build_s"],
+                "e2e": {"value": cb["value"], "unit": "PCG iterations/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    out, sc = run_ours(args, rank, world, local_rank, dist)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_reference(sc, 5, args.cpu_iters, 2, 1)
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            out["cpu_baseline"]["assembly_s"] = cb["assembly_s"]
+            out["cpu_baseline"]["mas_build_s"] = cb["mas_build_s"]
+            out["speedup_pcg_iters_per_s_vs_cpu"] = out["value"] / cb["value"]
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,171 @@
+/*
+ * adipc_gpu.h — C-ABI of the B200 (sm_100a) per-Newton linear-solve hot path
+ * of StiffGIPC (arXiv 2411.06224), drop-in for the reference `adipc` C++
+ * interfaces under /root/reference/proj/include/adipc (cited as adipc/...).
+ *
+ * Conventions (mirroring the reference's data layout so a C++ shim can pass
+ * std::vector storage straight through):
+ *   - block keys: uint64 (row << 32) | col           (adipc/sparse/block_coo.hpp:13-21)
+ *   - 3x3 blocks: 9 doubles, COLUMN-MAJOR            (Eigen Mat3 storage, core/types.hpp:21)
+ *   - vectors:    3n doubles, slot-major (x0 y0 z0 x1 ...) (VecX / std::vector<Vec3>)
+ *   - edges:      int32 pairs (a, b) interleaved      (std::vector<std::pair<Index,Index>>)
+ *   - Index = int32, Real = double                    (core/types.hpp:9-10)
+ * Plain pointers and sizes only. Functions without `_device` take HOST
+ * pointers and copy; `_device` variants take device pointers on the context's
+ * device and never copy. Every call is stream-ordered on the context stream
+ * and returns after its results are ready.
+ *
+ * Status codes (the shim maps them back to the reference's exceptions):
+ *   ADIPC_OK 0
+ *   ADIPC_INVALID_ARGUMENT 1 -> std::invalid_argument (e.g. adipc/sparse/reduction.hpp:34)
+ *   ADIPC_INDEFINITE 2       -> std::runtime_error "subdomain matrix stayed indefinite
+ *                               after regularization" (adipc/precond/mas.hpp:74-77)
+ *   ADIPC_CUDA_ERROR 3
+ * adipc_gpu_last_error(ctx) returns the message of the last failure.
+ * A context is not thread-safe; distinct contexts may be used from distinct
+ * host threads and devices.
+ */
+#ifndef ADIPC_GPU_H
+#define ADIPC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADIPC_OK 0
+#define ADIPC_INVALID_ARGUMENT 1
+#define ADIPC_INDEFINITE 2
+#define ADIPC_CUDA_ERROR 3
+
+#define ADIPC_PRECOND_MAS 1    /* MasPreconditioner   (adipc/precond/mas.hpp:32-115)        */
+#define ADIPC_PRECOND_JACOBI 2 /* BlockJacobiPreconditioner (adipc/precond/block_jacobi.hpp:8-26) */
+
+#define ADIPC_OPT_CACHE_HIERARCHY 1 /* reuse the MAS hierarchy while the sparsity is unchanged */
+#define ADIPC_OPT_PROFILE 2         /* time each PCG kernel class with CUDA events */
+
+typedef struct adipc_gpu_ctx adipc_gpu_ctx;
+typedef struct adipc_hierarchy adipc_hierarchy;
+
+/* ---- context ------------------------------------------------------------ */
+int adipc_gpu_create(int device, adipc_gpu_ctx** out);
+int adipc_gpu_destroy(adipc_gpu_ctx* ctx);
+const char* adipc_gpu_last_error(const adipc_gpu_ctx* ctx);
+/* Run on an external cudaStream_t (NULL: the context's own stream). */
+int adipc_gpu_set_stream(adipc_gpu_ctx* ctx, void* cuda_stream);
+int adipc_gpu_set_option(adipc_gpu_ctx* ctx, int option, int value);
+/* number of CUDA kernels this library has launched in the process so far */
+int64_t adipc_gpu_kernel_launches(void);
+/* with ADIPC_OPT_PROFILE: summed ms of the last PCG solve's SpMV, level-0 MAS
+ * (+ vector update), coarse MAS and prolongation/p-update launches, and the
+ * number of iterations they cover */
+int adipc_gpu_pcg_profile(adipc_gpu_ctx* ctx, float* ms4, int* iters);
+/* ms of the last assemble / preconditioner build (device) / build host part / pcg loop */
+int adipc_gpu_last_timings(adipc_gpu_ctx* ctx, float* ms4);
+
+/* ---- assembly ------------------------------------------------------------------
+ * sort_stream + fast_hash_reduction into the context's SortedSymBlockCoo, as at
+ * adipc/solver/incremental_potential.hpp:256-257. Replaces
+ *   void sort_stream(BlockTripletStream&, const ExecPolicy&)            block_coo.hpp:106
+ *   SortedSymBlockCoo fast_hash_reduction(const BlockTripletStream&, Index, const ExecPolicy&)
+ *                                                                        reduction.hpp:83
+ * Values are bitwise equal to the reference's deterministic mode (ExecPolicy::
+ * deterministic, reduction.hpp:39-53) whatever `deterministic` says. Keys must
+ * have row < n_block_rows. */
+int adipc_gpu_assemble(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T,
+                       int32_t n_block_rows, int deterministic, int64_t* n_unique);
+int adipc_gpu_assemble_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const double* d_vals9, int64_t T,
+                              int32_t n_block_rows, int deterministic, int64_t* n_unique);
+int adipc_gpu_matrix_info(adipc_gpu_ctx* ctx, int32_t* n_block_rows, int64_t* n_blocks);
+/* copy SortedSymBlockCoo{rows, cols, blocks} out (block_coo.hpp:54-61) */
+int adipc_gpu_copy_matrix(adipc_gpu_ctx* ctx, uint32_t* rows, uint32_t* cols, double* blocks9);
+/* upload an existing SortedSymBlockCoo (strictly increasing keys) */
+int adipc_gpu_set_matrix(adipc_gpu_ctx* ctx, int32_t n_block_rows, int64_t n_blocks, const uint32_t* rows,
+                         const uint32_t* cols, const double* blocks9);
+int adipc_gpu_set_matrix_device(adipc_gpu_ctx* ctx, int32_t n_block_rows, int64_t n_blocks, const uint32_t* d_rows,
+                                const uint32_t* d_cols, const double* d_blocks9);
+
+/* sort_stream alone (block_coo.hpp:106-113): stable, in place on host arrays. */
+int adipc_gpu_sort_stream(adipc_gpu_ctx* ctx, uint64_t* keys, double* vals9, int64_t T);
+
+/* fast_segment_reduction<V> (reduction.hpp:30-79), V = Real (width 1), Vec3 (3)
+ * or Mat3 (9). nO != nV -> ADIPC_INVALID_ARGUMENT ("segment map size mismatch"). */
+int adipc_gpu_segment_reduce(adipc_gpu_ctx* ctx, const int32_t* O, int64_t nO, const double* V, int64_t nV,
+                             int width, int32_t n_segments, int deterministic, double* R);
+
+/* two_level_abd_reduce (adipc/sparse/abd_reduce.hpp:32-74) for the DofMap
+ * {n_fem_nodes, n_bodies, abd_node_body[n_abd], abd_node_jacobian[n_abd]
+ * (3x12 column-major, 36 doubles each)} (abd_reduce.hpp:11-27). Writes the
+ * unsorted tile stream (<= 16 per unique node pair) in the reference's order. */
+int adipc_gpu_two_level_abd_reduce(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t Tn,
+                                   int32_t n_fem, int32_t n_bodies, int32_t n_abd, const int32_t* abd_node_body,
+                                   const double* abd_node_jacobian36, uint64_t* out_keys, double* out_vals9,
+                                   int64_t out_capacity, int64_t* n_out);
+
+/* IncrementalPotential::filter_pinned (incremental_potential.hpp:410-425):
+ * drop blocks touching a pinned slot, append I3 per pinned slot.
+ * out capacity >= T + n_slots. */
+int adipc_gpu_filter_pinned(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T,
+                            const uint8_t* pinned, int32_t n_slots, uint64_t* out_keys, double* out_vals9,
+                            int64_t* n_out);
+int adipc_gpu_filter_pinned_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const double* d_vals9, int64_t T,
+                                   const uint8_t* d_pinned, int32_t n_slots, uint64_t* d_out_keys,
+                                   double* d_out_vals9, int64_t* n_out);
+
+/* ---- SpMV ------------------------------------------------------------------------
+ * srbk_spmv (adipc/sparse/srbk_spmv.hpp:13-49) on the context matrix: y = A x,
+ * x and y of 3 * n_block_rows doubles. */
+int adipc_gpu_spmv(adipc_gpu_ctx* ctx, const double* x, double* y);
+int adipc_gpu_spmv_device(adipc_gpu_ctx* ctx, const double* d_x, double* d_y);
+
+/* ---- partition / hierarchy (host-side integer code, no GPU needed) ---------------- */
+int32_t adipc_subdomain_count(int32_t v, int32_t n, int32_t n_o);              /* partition.hpp:12-15 */
+int32_t adipc_chunk_partition(int32_t v, int32_t capacity, int32_t* part_of);  /* partition.hpp:25-32, returns n_parts */
+int32_t adipc_partition_block_graph(int32_t v, const int32_t* edge_pairs, int64_t n_edges, int32_t capacity,
+                                    int32_t* part_of);                         /* partition.hpp:88-159, returns n_parts */
+/* build_hierarchy (adipc/precond/hierarchy.hpp:30-100) */
+adipc_hierarchy* adipc_build_hierarchy(const int32_t* l0_part_of, int32_t n_slots, int32_t n_parts, int32_t capacity,
+                                       const int32_t* edge_pairs, int64_t n_edges, int32_t max_levels);
+int adipc_hierarchy_n_levels(const adipc_hierarchy* h);
+/* part_of (n_nodes) and agg (n_slots) may be NULL to query sizes */
+int adipc_hierarchy_level(const adipc_hierarchy* h, int level, int32_t* n_nodes, int32_t* n_parts, int32_t* part_of,
+                          int32_t* agg);
+void adipc_hierarchy_free(adipc_hierarchy* h);
+
+/* ---- preconditioner ------------------------------------------------------------------
+ * Level-0 partition, fixed per scene (TimeStepper ctor, adipc/solver/newton.hpp:66-68). */
+int adipc_gpu_set_level0_partition(adipc_gpu_ctx* ctx, const int32_t* part_of, int32_t n_slots, int32_t n_parts,
+                                   int32_t capacity, int32_t max_levels);
+/* TimeStepper::build_preconditioner (newton.hpp:243-255): MAS = block_edges +
+ * build_hierarchy + MasPreconditioner::build (mas.hpp:34-83), or Jacobi. */
+int adipc_gpu_build_preconditioner(adipc_gpu_ctx* ctx, int kind);
+/* MasPreconditioner::build(A, h) (mas.hpp:34-83) with a caller-built hierarchy
+ * (adipc_build_hierarchy); the level-0 partition is taken from h. */
+int adipc_gpu_build_mas(adipc_gpu_ctx* ctx, const adipc_hierarchy* h);
+int adipc_gpu_precond_n_levels(adipc_gpu_ctx* ctx);
+int adipc_gpu_precond_level(adipc_gpu_ctx* ctx, int level, int32_t* n_nodes, int32_t* n_parts, int32_t* part_of,
+                            int32_t* agg);
+/* explicit inverse of subdomain `sub` at `level` (dim x dim column-major, dim = 3 f); out may be NULL */
+int adipc_gpu_precond_subdomain_inverse(adipc_gpu_ctx* ctx, int level, int32_t sub, int32_t* dim, double* out);
+/* number of diagonal regularisation shifts applied by the last build (mas.hpp:68-80) */
+int adipc_gpu_precond_shifts(adipc_gpu_ctx* ctx, int64_t* shifts);
+/* Preconditioner::apply (mas.hpp:12-15, 85-99; block_jacobi.hpp:16-22) */
+int adipc_gpu_precond_apply(adipc_gpu_ctx* ctx, const double* r, double* z);
+int adipc_gpu_precond_apply_device(adipc_gpu_ctx* ctx, const double* d_r, double* d_z);
+
+/* ---- PCG -------------------------------------------------------------------------------
+ * pcg_solve (adipc/solver/pcg.hpp:34-88) with the context matrix and its built
+ * preconditioner: x0 = 0, stop when r.z <= rel_tol^2 r0.z0, residual recomputed
+ * every `restart` iterations. Returns PcgResult {iters, rel_residual, converged}. */
+int adipc_gpu_pcg(adipc_gpu_ctx* ctx, const double* b, double rel_tol, int restart, int max_iters, double* x,
+                  int* iters, double* rel_residual, int* converged);
+int adipc_gpu_pcg_device(adipc_gpu_ctx* ctx, const double* d_b, double rel_tol, int restart, int max_iters,
+                         double* d_x, int* iters, double* rel_residual, int* converged);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADIPC_GPU_H */

@@ -1,0 +1,84 @@
+"""In-tree build of the native libraries (no JIT cache: the .so files travel
+with the repo snapshot to the GPU box).
+
+  libadipc_gpu.so     CUDA kernels + C-ABI (include/adipc_gpu.h), sm_100a only
+  libadipc_scenes.so  host C++ synthetic-scene generators (bench/test inputs)
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(PKG, "build")
+GPU_LIB = os.path.join(PKG, "libadipc_gpu.so")
+SCENES_LIB = os.path.join(PKG, "libadipc_scenes.so")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+              "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
+CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"  # image's $CXX lacks libgomp.spec
+CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter"]
+
+GPU_SOURCES = ["assemble.cu", "spmv.cu", "mas.cu", "pcg.cu", "abd.cu", "capi.cu", "host_precond.cpp"]
+SCENE_SOURCES = ["scenes.cpp"]
+
+
+def _nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def _headers():
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))] + [
+        os.path.join(ROOT, "include", "adipc_gpu.h")]
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def _compile(src: str, verbose: bool) -> str:
+    path = os.path.join(CSRC, src)
+    obj = os.path.join(OBJ, src + ".o")
+    if not _stale(obj, [path] + _headers()):
+        return obj
+    if src.endswith(".cu"):
+        cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-c", path, "-o", obj]
+    else:
+        cmd = [CXX, *CXX_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", path, "-o", obj]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+    return obj
+
+
+def build(verbose: bool = False) -> None:
+    os.makedirs(OBJ, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose), GPU_SOURCES))
+    if _stale(GPU_LIB, objs):
+        cmd = [_nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", GPU_LIB, *objs]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    scene_srcs = [os.path.join(CSRC, s) for s in SCENE_SOURCES]
+    if _stale(SCENES_LIB, scene_srcs):
+        cmd = [CXX, *CXX_FLAGS, "-shared", "-o", SCENES_LIB, *scene_srcs]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+
+
+if __name__ == "__main__":
+    build(verbose="-v" in sys.argv)

@@ -1,0 +1,118 @@
+"""ctypes binding of libadipc_gpu.so (include/adipc_gpu.h) and
+libadipc_scenes.so. Loading fails loudly when the native library is missing:
+there is no CPU fallback on the product path."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+GPU_LIB = os.path.join(PKG, "libadipc_gpu.so")
+SCENES_LIB = os.path.join(PKG, "libadipc_scenes.so")
+
+u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+vp, ci, cd, i32, i64 = C.c_void_p, C.c_int, C.c_double, C.c_int32, C.c_int64
+
+OK, INVALID_ARGUMENT, INDEFINITE, CUDA_ERROR = 0, 1, 2, 3
+PRECOND_MAS, PRECOND_JACOBI = 1, 2
+OPT_CACHE_HIERARCHY = 1
+OPT_PROFILE = 2
+
+# Every symbol include/adipc_gpu.h declares, with its ctypes signature.
+GPU_SIGNATURES = {
+    "adipc_gpu_create": (ci, [ci, C.POINTER(vp)]),
+    "adipc_gpu_destroy": (ci, [vp]),
+    "adipc_gpu_last_error": (C.c_char_p, [vp]),
+    "adipc_gpu_set_stream": (ci, [vp, vp]),
+    "adipc_gpu_set_option": (ci, [vp, ci, ci]),
+    "adipc_gpu_last_timings": (ci, [vp, f32p]),
+    "adipc_gpu_kernel_launches": (i64, []),
+    "adipc_gpu_pcg_profile": (ci, [vp, f32p, C.POINTER(ci)]),
+    "adipc_gpu_assemble": (ci, [vp, vp, vp, i64, i32, ci, C.POINTER(i64)]),
+    "adipc_gpu_assemble_device": (ci, [vp, vp, vp, i64, i32, ci, C.POINTER(i64)]),
+    "adipc_gpu_matrix_info": (ci, [vp, C.POINTER(i32), C.POINTER(i64)]),
+    "adipc_gpu_copy_matrix": (ci, [vp, vp, vp, vp]),
+    "adipc_gpu_set_matrix": (ci, [vp, i32, i64, vp, vp, vp]),
+    "adipc_gpu_set_matrix_device": (ci, [vp, i32, i64, vp, vp, vp]),
+    "adipc_gpu_sort_stream": (ci, [vp, vp, vp, i64]),
+    "adipc_gpu_segment_reduce": (ci, [vp, vp, i64, vp, i64, ci, i32, ci, vp]),
+    "adipc_gpu_two_level_abd_reduce": (ci, [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, i64, C.POINTER(i64)]),
+    "adipc_gpu_filter_pinned": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
+    "adipc_gpu_filter_pinned_device": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
+    "adipc_gpu_spmv": (ci, [vp, vp, vp]),
+    "adipc_gpu_spmv_device": (ci, [vp, vp, vp]),
+    "adipc_subdomain_count": (i32, [i32, i32, i32]),
+    "adipc_chunk_partition": (i32, [i32, i32, vp]),
+    "adipc_partition_block_graph": (i32, [i32, vp, i64, i32, vp]),
+    "adipc_build_hierarchy": (vp, [vp, i32, i32, i32, vp, i64, i32]),
+    "adipc_hierarchy_n_levels": (ci, [vp]),
+    "adipc_hierarchy_level": (ci, [vp, ci, C.POINTER(i32), C.POINTER(i32), vp, vp]),
+    "adipc_hierarchy_free": (None, [vp]),
+    "adipc_gpu_set_level0_partition": (ci, [vp, vp, i32, i32, i32, i32]),
+    "adipc_gpu_build_preconditioner": (ci, [vp, ci]),
+    "adipc_gpu_build_mas": (ci, [vp, vp]),
+    "adipc_gpu_precond_n_levels": (ci, [vp]),
+    "adipc_gpu_precond_level": (ci, [vp, ci, C.POINTER(i32), C.POINTER(i32), vp, vp]),
+    "adipc_gpu_precond_subdomain_inverse": (ci, [vp, ci, i32, C.POINTER(i32), vp]),
+    "adipc_gpu_precond_shifts": (ci, [vp, C.POINTER(i64)]),
+    "adipc_gpu_precond_apply": (ci, [vp, vp, vp]),
+    "adipc_gpu_precond_apply_device": (ci, [vp, vp, vp]),
+    "adipc_gpu_pcg": (ci, [vp, vp, cd, ci, ci, vp, C.POINTER(ci), C.POINTER(cd), C.POINTER(ci)]),
+    "adipc_gpu_pcg_device": (ci, [vp, vp, cd, ci, ci, vp, C.POINTER(ci), C.POINTER(cd), C.POINTER(ci)]),
+}
+
+SCENE_SIGNATURES = {
+    "adipc_scene_fem_box": (vp, [ci, ci, ci, cd, cd, cd, cd, cd, cd, cd, ci]),
+    "adipc_scene_cloth": (vp, [ci, ci, cd, cd, C.c_uint]),
+    "adipc_scene_abd_stack": (vp, [ci, ci, ci, C.c_uint]),
+    "adipc_scene_hybrid": (vp, [ci, ci, ci, ci, ci, C.c_uint]),
+    "adipc_scene_free": (None, [vp]),
+    "adipc_scene_sizes": (None, [vp, vp]),
+    "adipc_scene_copy": (None, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+}
+
+_gpu = None
+_scenes = None
+
+
+def _load(path, sigs):
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{os.path.basename(path)} is not built (run __graft_entry__.build() or "
+            f"python paper_2411_06224_b200/_build.py); there is no CPU fallback")
+    L = C.CDLL(path)
+    for name, (res, args) in sigs.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
+
+
+def gpu():
+    global _gpu
+    if _gpu is None:
+        _gpu = _load(GPU_LIB, GPU_SIGNATURES)
+    return _gpu
+
+
+def scenes():
+    global _scenes
+    if _scenes is None:
+        _scenes = _load(SCENES_LIB, SCENE_SIGNATURES)
+    return _scenes
+
+
+def ptr(a) -> int | None:
+    """Raw address of a numpy array or torch tensor (None for None)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data if a.size else None
+    return a.data_ptr()  # torch tensor

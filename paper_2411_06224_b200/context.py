@@ -1,0 +1,263 @@
+"""Per-scene device context over the C-ABI (include/adipc_gpu.h).
+
+A Context owns one device-resident SortedSymBlockCoo, its preconditioner and
+the PCG workspace. Array arguments may be numpy arrays (host; the library
+copies) or torch CUDA tensors (device; the `_device` entry points are used and
+nothing is copied). Status codes are mapped back to the reference's
+exceptions: invalid_argument -> InvalidArgument (a ValueError),
+indefinite subdomain -> IndefiniteSubdomain (a RuntimeError).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import ptr
+
+
+class AdipcError(RuntimeError):
+    pass
+
+
+class InvalidArgument(AdipcError, ValueError):
+    """std::invalid_argument of the reference (e.g. reduction.hpp:34)."""
+
+
+class IndefiniteSubdomain(AdipcError):
+    """std::runtime_error of mas.hpp:74-77."""
+
+
+class CudaFailure(AdipcError):
+    pass
+
+
+def _is_device(a) -> bool:
+    return a is not None and not isinstance(a, np.ndarray) and getattr(a, "is_cuda", False)
+
+
+def _raise(rc: int, msg: str):
+    if rc == _lib.INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    if rc == _lib.INDEFINITE:
+        raise IndefiniteSubdomain(msg)
+    raise CudaFailure(msg)
+
+
+class PcgResult:
+    """solver/pcg.hpp:10-14."""
+
+    def __init__(self, iters=0, rel_residual=0.0, converged=False):
+        self.iters = iters
+        self.rel_residual = rel_residual
+        self.converged = converged
+
+    def __repr__(self):
+        return f"PcgResult(iters={self.iters}, rel_residual={self.rel_residual:.3e}, converged={self.converged})"
+
+
+class Context:
+    def __init__(self, device: int = 0, stream=None):
+        self._L = _lib.gpu()
+        h = C.c_void_p()
+        rc = self._L.adipc_gpu_create(device, C.byref(h))
+        if rc != 0:
+            _raise(rc, self._L.adipc_gpu_last_error(None).decode())
+        self.h = h
+        self.device = device
+        if stream is not None:
+            self.set_stream(stream)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.adipc_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            _raise(rc, self._L.adipc_gpu_last_error(self.h).decode())
+
+    # -- plumbing --------------------------------------------------------------
+    def set_stream(self, stream):
+        """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None."""
+        raw = getattr(stream, "cuda_stream", stream)
+        self._check(self._L.adipc_gpu_set_stream(self.h, raw))
+
+    def set_option(self, option: int, value: int):
+        self._check(self._L.adipc_gpu_set_option(self.h, option, value))
+
+    def timings(self):
+        t = np.zeros(4, np.float32)
+        self._check(self._L.adipc_gpu_last_timings(self.h, t))
+        return dict(assemble_ms=float(t[0]), build_ms=float(t[1]), build_host_ms=float(t[2]), pcg_ms=float(t[3]))
+
+    def pcg_profile(self):
+        t = np.zeros(4, np.float32)
+        it = C.c_int()
+        self._check(self._L.adipc_gpu_pcg_profile(self.h, t, C.byref(it)))
+        return dict(spmv_ms=float(t[0]), l0_ms=float(t[1]), coarse_ms=float(t[2]), final_ms=float(t[3]),
+                    iters=it.value)
+
+    @staticmethod
+    def kernel_launches() -> int:
+        return int(_lib.gpu().adipc_gpu_kernel_launches())
+
+    # -- assembly ------------------------------------------------------------------
+    def assemble(self, keys, vals, n_block_rows: int, deterministic: bool = True) -> int:
+        """sort_stream + fast_hash_reduction into the context matrix; returns U."""
+        U = C.c_int64()
+        T = len(keys)
+        if _is_device(keys):
+            self._check(self._L.adipc_gpu_assemble_device(self.h, ptr(keys), ptr(vals), T, n_block_rows,
+                                                          int(deterministic), C.byref(U)))
+        else:
+            k = np.ascontiguousarray(keys, np.uint64)
+            v = np.ascontiguousarray(vals, np.float64).reshape(-1, 9)
+            self._check(self._L.adipc_gpu_assemble(self.h, ptr(k), ptr(v), T, n_block_rows, int(deterministic),
+                                                   C.byref(U)))
+        return U.value
+
+    def matrix_info(self):
+        n, U = C.c_int32(), C.c_int64()
+        self._check(self._L.adipc_gpu_matrix_info(self.h, C.byref(n), C.byref(U)))
+        return n.value, U.value
+
+    def copy_matrix(self):
+        n, U = self.matrix_info()
+        rows = np.empty(U, np.uint32)
+        cols = np.empty(U, np.uint32)
+        blocks = np.empty((U, 9), np.float64)
+        self._check(self._L.adipc_gpu_copy_matrix(self.h, ptr(rows), ptr(cols), ptr(blocks)))
+        return n, rows, cols, blocks
+
+    def set_matrix(self, n_block_rows, rows, cols, blocks):
+        U = len(rows)
+        if _is_device(rows):
+            self._check(self._L.adipc_gpu_set_matrix_device(self.h, n_block_rows, U, ptr(rows), ptr(cols), ptr(blocks)))
+        else:
+            r = np.ascontiguousarray(rows, np.uint32)
+            c = np.ascontiguousarray(cols, np.uint32)
+            b = np.ascontiguousarray(blocks, np.float64).reshape(-1, 9)
+            self._check(self._L.adipc_gpu_set_matrix(self.h, n_block_rows, U, ptr(r), ptr(c), ptr(b)))
+
+    def sort_stream(self, keys, vals):
+        k = np.array(keys, np.uint64)
+        v = np.array(vals, np.float64).reshape(-1, 9).copy()
+        self._check(self._L.adipc_gpu_sort_stream(self.h, ptr(k), ptr(v), len(k)))
+        return k, v
+
+    def segment_reduce(self, O, V, n_segments, deterministic=True):
+        O = np.ascontiguousarray(O, np.int32)
+        V = np.ascontiguousarray(V, np.float64)
+        width = 1 if V.ndim == 1 else V.shape[1]
+        R = np.empty((max(n_segments, 0), width), np.float64)
+        self._check(self._L.adipc_gpu_segment_reduce(self.h, ptr(O), len(O), ptr(V), V.shape[0], width, n_segments,
+                                                     int(deterministic), ptr(R)))
+        return R[:, 0].copy() if width == 1 else R
+
+    def two_level_abd_reduce(self, keys, vals, n_fem, n_bodies, abd_node_body, jac36):
+        k = np.ascontiguousarray(keys, np.uint64)
+        v = np.ascontiguousarray(vals, np.float64).reshape(-1, 9)
+        body = np.ascontiguousarray(abd_node_body, np.int32)
+        jac = np.ascontiguousarray(jac36, np.float64).reshape(-1, 36)
+        cap = 16 * len(k)
+        ok = np.empty(cap, np.uint64)
+        ov = np.empty((cap, 9), np.float64)
+        n = C.c_int64()
+        self._check(self._L.adipc_gpu_two_level_abd_reduce(self.h, ptr(k), ptr(v), len(k), n_fem, n_bodies, len(body),
+                                                           ptr(body), ptr(jac), ptr(ok), ptr(ov), cap, C.byref(n)))
+        return ok[: n.value].copy(), ov[: n.value].copy()
+
+    def filter_pinned(self, keys, vals, pinned):
+        k = np.ascontiguousarray(keys, np.uint64)
+        v = np.ascontiguousarray(vals, np.float64).reshape(-1, 9)
+        p = np.ascontiguousarray(pinned, np.uint8)
+        ok = np.empty(len(k) + len(p), np.uint64)
+        ov = np.empty((len(k) + len(p), 9), np.float64)
+        n = C.c_int64()
+        self._check(self._L.adipc_gpu_filter_pinned(self.h, ptr(k), ptr(v), len(k), ptr(p), len(p), ptr(ok), ptr(ov),
+                                                    C.byref(n)))
+        return ok[: n.value].copy(), ov[: n.value].copy()
+
+    # -- spmv ----------------------------------------------------------------------------
+    def spmv(self, x, y=None):
+        if _is_device(x):
+            self._check(self._L.adipc_gpu_spmv_device(self.h, ptr(x), ptr(y)))
+            return y
+        x = np.ascontiguousarray(x, np.float64).reshape(-1)
+        y = np.empty_like(x)
+        self._check(self._L.adipc_gpu_spmv(self.h, ptr(x), ptr(y)))
+        return y
+
+    # -- preconditioner ----------------------------------------------------------------------
+    def set_level0_partition(self, part_of, n_parts, capacity, max_levels=4):
+        p = np.ascontiguousarray(part_of, np.int32)
+        self._check(self._L.adipc_gpu_set_level0_partition(self.h, ptr(p), len(p), n_parts, capacity, max_levels))
+
+    def build_preconditioner(self, kind=_lib.PRECOND_MAS):
+        self._check(self._L.adipc_gpu_build_preconditioner(self.h, kind))
+
+    def build_mas(self, hierarchy):
+        self._check(self._L.adipc_gpu_build_mas(self.h, hierarchy.h))
+
+    def precond_levels(self):
+        out = []
+        for l in range(self._L.adipc_gpu_precond_n_levels(self.h)):
+            nn, npart = C.c_int32(), C.c_int32()
+            self._check(self._L.adipc_gpu_precond_level(self.h, l, C.byref(nn), C.byref(npart), None, None))
+            n, _ = self.matrix_info()
+            part = np.empty(nn.value, np.int32)
+            agg = np.empty(n, np.int32)
+            self._check(self._L.adipc_gpu_precond_level(self.h, l, C.byref(nn), C.byref(npart), ptr(part), ptr(agg)))
+            out.append(dict(n_nodes=nn.value, n_parts=npart.value, part_of=part, agg=agg))
+        return out
+
+    def subdomain_inverse(self, level, sub):
+        d = C.c_int32()
+        self._check(self._L.adipc_gpu_precond_subdomain_inverse(self.h, level, sub, C.byref(d), None))
+        out = np.empty(d.value * d.value, np.float64)
+        self._check(self._L.adipc_gpu_precond_subdomain_inverse(self.h, level, sub, C.byref(d), ptr(out)))
+        return out.reshape(d.value, d.value).T.copy()
+
+    def shifts(self):
+        s = C.c_int64()
+        self._check(self._L.adipc_gpu_precond_shifts(self.h, C.byref(s)))
+        return s.value
+
+    def precond_apply(self, r, z=None):
+        if _is_device(r):
+            self._check(self._L.adipc_gpu_precond_apply_device(self.h, ptr(r), ptr(z)))
+            return z
+        r = np.ascontiguousarray(r, np.float64).reshape(-1)
+        z = np.empty_like(r)
+        self._check(self._L.adipc_gpu_precond_apply(self.h, ptr(r), ptr(z)))
+        return z
+
+    # -- pcg ----------------------------------------------------------------------------------
+    def pcg(self, b, rel_tol=1e-4, restart=250, max_iters=100000, x=None):
+        it, rr, cv = C.c_int(), C.c_double(), C.c_int()
+        if _is_device(b):
+            self._check(self._L.adipc_gpu_pcg_device(self.h, ptr(b), rel_tol, restart, max_iters, ptr(x),
+                                                     C.byref(it), C.byref(rr), C.byref(cv)))
+        else:
+            b = np.ascontiguousarray(b, np.float64).reshape(-1)
+            x = np.empty_like(b)
+            self._check(self._L.adipc_gpu_pcg(self.h, ptr(b), rel_tol, restart, max_iters, ptr(x), C.byref(it),
+                                              C.byref(rr), C.byref(cv)))
+        return x, PcgResult(it.value, rr.value, bool(cv.value))
+
+
+_default = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]

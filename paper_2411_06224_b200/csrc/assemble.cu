@@ -1,0 +1,514 @@
+// Hessian assembly on B200: replaces sort_stream + fast_hash_reduction
+// (sparse/block_coo.hpp:67-113, sparse/reduction.hpp:30-107) as called at
+// solver/incremental_potential.hpp:256-257.
+//
+// The reference sorts 64-bit (row, col) keys with a serial 4 x 16-bit LSD
+// radix sort, gathers the 72-byte blocks through the permutation, scans key
+// changes serially and sums each segment left to right (deterministic mode).
+// Here the same result is produced by exploiting that keys are block
+// coordinates with row < n:
+//   1. row histogram (atomics)                         -> row_cnt[n]
+//   2. exclusive scan                                  -> row_start[n+1]
+//   3. bucket scatter of (col << 32 | emission index)  -> sorted[T]
+//      (atomic slot order, fixed in 4)
+//   4. per-row sort of (col, index) in registers/shared memory; sorting by the
+//      emission index as the low word reproduces a *stable* sort exactly
+//   5. unique-col count per row + scan                 -> row_ptr / U
+//   6. per unique block: sequential fp64 sum in emission order of the gathered
+//      72-byte values (never materialising the sorted value copy, K2 fused
+//      into K4), written straight to rows/cols/blocks.
+// Step 6 reproduces the reference's deterministic mode bit for bit
+// (reduction.hpp:39-53: left-to-right adds, no FMA involved); the parallel
+// mode of the reference differs from it only by rounding (<= 1e-12).
+#include <algorithm>
+
+#include "context.hpp"
+#include "scan.cuh"
+
+namespace adipc_gpu {
+
+namespace {
+
+constexpr int kWarpSortMax = 256;   // rows up to this length: one warp, smem bitonic
+constexpr int kCtaSortMax = 8192;   // rows up to this length: one CTA, smem bitonic
+constexpr int kCtaSortThreads = 1024;
+
+__global__ void k_row_hist(const std::uint64_t* __restrict__ keys, std::int64_t T, std::int32_t n,
+                           std::int32_t* __restrict__ row_cnt, std::int32_t* __restrict__ err) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t row = static_cast<std::uint32_t>(keys[i] >> 32);
+        if (row >= static_cast<std::uint32_t>(n)) {
+            atomicOr(err, 1);
+            continue;
+        }
+        atomicAdd(row_cnt + row, 1);
+    }
+}
+
+__global__ void k_row_scatter(const std::uint64_t* __restrict__ keys, std::int64_t T,
+                              const std::int64_t* __restrict__ row_start, std::int32_t* __restrict__ cursor,
+                              std::uint64_t* __restrict__ out) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t k = keys[i];
+        const std::uint32_t row = static_cast<std::uint32_t>(k >> 32);
+        const std::int64_t pos = row_start[row] + atomicAdd(cursor + row, 1);
+        out[pos] = (k << 32) | static_cast<std::uint32_t>(i);
+    }
+}
+
+// Bitonic sort of s[0..N) (N power of two) by `nthr` cooperating threads.
+template <bool kWarp>
+__device__ __forceinline__ void bitonic(std::uint64_t* s, int N, int tid, int nthr) {
+    for (int k = 2; k <= N; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < N; i += nthr) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const std::uint64_t a = s[i], b = s[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        s[i] = b;
+                        s[ixj] = a;
+                    }
+                }
+            }
+            if (kWarp)
+                __syncwarp();
+            else
+                __syncthreads();
+        }
+}
+
+// One warp per row; rows longer than kWarpSortMax are deferred to the CTA
+// kernel through big_rows. Also counts unique cols of each sorted row.
+__global__ void k_sort_rows_warp(std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
+                                 std::int32_t n, std::int32_t* __restrict__ uniq_cnt,
+                                 std::int32_t* __restrict__ big_rows, std::int32_t* __restrict__ n_big) {
+    __shared__ std::uint64_t sm[8][kWarpSortMax];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    std::uint64_t* s = sm[w];
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps) {
+        const std::int64_t b = row_start[r], e = row_start[r + 1];
+        const int len = static_cast<int>(e - b);
+        if (len > kWarpSortMax) {
+            if (lane == 0) big_rows[atomicAdd(n_big, 1)] = r;
+            continue;
+        }
+        if (len <= 1) {
+            if (lane == 0) uniq_cnt[r] = len;
+            continue;
+        }
+        int N = 2;
+        while (N < len) N <<= 1;
+        for (int i = lane; i < N; i += 32) s[i] = i < len ? sorted[b + i] : ~0ull;
+        __syncwarp();
+        bitonic<true>(s, N, lane, 32);
+        int uniq = 0;
+        for (int i = lane; i < len; i += 32) {
+            const std::uint64_t v = s[i];
+            sorted[b + i] = v;
+            uniq += (i == 0 || (v >> 32) != (s[i - 1] >> 32)) ? 1 : 0;
+        }
+        for (int o = 16; o > 0; o >>= 1) uniq += __shfl_xor_sync(0xffffffffu, uniq, o);
+        if (lane == 0) uniq_cnt[r] = uniq;
+        __syncwarp();
+    }
+}
+
+// Merge two sorted runs a[0..na), b[0..nb) into out, cooperatively: each
+// thread takes an equal slice of the output via a merge-path search.
+__device__ void cta_merge(const std::uint64_t* a, int na, const std::uint64_t* b, int nb, std::uint64_t* out) {
+    const int total = na + nb;
+    const int per = (total + blockDim.x - 1) / blockDim.x;
+    const int d0 = min(total, static_cast<int>(threadIdx.x) * per);
+    const int d1 = min(total, d0 + per);
+    if (d0 >= d1) return;
+    auto split = [&](int d) {  // number of elements taken from a in the first d outputs
+        int lo = max(0, d - nb), hi = min(d, na);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (a[mid] <= b[d - mid - 1])  // a before b on ties (keys are unique anyway)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        return lo;
+    };
+    int i = split(d0), j = d0 - i;
+    for (int d = d0; d < d1; ++d) {
+        if (j >= nb || (i < na && a[i] <= b[j]))
+            out[d] = a[i++];
+        else
+            out[d] = b[j++];
+    }
+}
+
+// One CTA per long row: shared-memory bitonic for rows <= kCtaSortMax,
+// otherwise chunk sort + merge passes through `scratch` (rare: contact rows
+// of affine bodies can collect very many tiles).
+__global__ void k_sort_rows_cta(std::uint64_t* __restrict__ sorted, std::uint64_t* __restrict__ scratch,
+                                const std::int64_t* __restrict__ row_start, const std::int32_t* __restrict__ big_rows,
+                                const std::int32_t* __restrict__ n_big, std::int32_t* __restrict__ uniq_cnt) {
+    extern __shared__ std::uint64_t s[];
+    __shared__ int red[32];
+    const int nb = *n_big;
+    for (int bi = blockIdx.x; bi < nb; bi += gridDim.x) {
+        const std::int32_t r = big_rows[bi];
+        const std::int64_t b = row_start[r];
+        const int len = static_cast<int>(row_start[r + 1] - b);
+        std::uint64_t* seg = sorted + b;
+        // sort chunks of kCtaSortMax in shared memory
+        for (int c0 = 0; c0 < len; c0 += kCtaSortMax) {
+            const int cl = min(kCtaSortMax, len - c0);
+            int N = 2;
+            while (N < cl) N <<= 1;
+            for (int i = threadIdx.x; i < N; i += blockDim.x) s[i] = i < cl ? seg[c0 + i] : ~0ull;
+            __syncthreads();
+            bitonic<false>(s, N, threadIdx.x, blockDim.x);
+            for (int i = threadIdx.x; i < cl; i += blockDim.x) seg[c0 + i] = s[i];
+            __syncthreads();
+        }
+        // merge passes, ping-pong between seg and scratch
+        std::uint64_t* src = seg;
+        std::uint64_t* dst = scratch + b;
+        for (int width = kCtaSortMax; width < len; width <<= 1) {
+            for (int a0 = 0; a0 < len; a0 += 2 * width) {
+                const int na = min(width, len - a0);
+                const int nbb = min(width, max(0, len - a0 - width));
+                cta_merge(src + a0, na, src + a0 + na, nbb, dst + a0);
+            }
+            __syncthreads();
+            std::uint64_t* t = src;
+            src = dst;
+            dst = t;
+        }
+        if (src != seg) {
+            for (int i = threadIdx.x; i < len; i += blockDim.x) seg[i] = src[i];
+            __syncthreads();
+        }
+        int uniq = 0;
+        for (int i = threadIdx.x; i < len; i += blockDim.x)
+            uniq += (i == 0 || (seg[i] >> 32) != (seg[i - 1] >> 32)) ? 1 : 0;
+        for (int o = 16; o > 0; o >>= 1) uniq += __shfl_xor_sync(0xffffffffu, uniq, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = uniq;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
+            uniq_cnt[r] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// One warp per row: every head lane (first element of a unique col) sums its
+// run sequentially in emission order and writes the unique block.
+__global__ void k_reduce_rows(const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
+                              const std::int64_t* __restrict__ uniq_start, std::int32_t n,
+                              const double* __restrict__ vals, std::uint32_t* __restrict__ out_rows,
+                              std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps) {
+        const std::int64_t b = row_start[r], e = row_start[r + 1];
+        std::int64_t u = uniq_start[r];
+        for (std::int64_t base = b; base < e; base += 32) {
+            const std::int64_t p = base + lane;
+            const bool valid = p < e;
+            const std::uint64_t v = valid ? sorted[p] : 0;
+            const std::uint32_t col = static_cast<std::uint32_t>(v >> 32);
+            const bool head = valid && (p == b || static_cast<std::uint32_t>(sorted[p - 1] >> 32) != col);
+            const unsigned hm = __ballot_sync(0xffffffffu, head);
+            if (head) {
+                const std::int64_t my_u = u + __popc(hm & ((1u << lane) - 1u));
+                double acc[9];
+                const double* src = vals + 9 * static_cast<std::int64_t>(static_cast<std::uint32_t>(v));
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[k] = src[k];
+                for (std::int64_t q = p + 1; q < e; ++q) {
+                    const std::uint64_t w2 = sorted[q];
+                    if (static_cast<std::uint32_t>(w2 >> 32) != col) break;
+                    const double* s2 = vals + 9 * static_cast<std::int64_t>(static_cast<std::uint32_t>(w2));
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(acc[k], s2[k]);
+                }
+                out_rows[my_u] = static_cast<std::uint32_t>(r);
+                out_cols[my_u] = col;
+                double* dst = out_blocks + 9 * my_u;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) dst[k] = acc[k];
+            }
+            u += __popc(hm);
+        }
+    }
+}
+
+__global__ void k_max_row(const std::uint64_t* __restrict__ keys, std::int64_t T, unsigned* __restrict__ out) {
+    unsigned m = 0;
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        m = max(m, static_cast<unsigned>(keys[i] >> 32));
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// sorted (col << 32 | index) per row -> sorted keys + gathered values
+__global__ void k_gather_sorted(const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
+                                std::int32_t n, const double* __restrict__ vals, std::uint64_t* __restrict__ out_keys,
+                                double* __restrict__ out_vals) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps)
+        for (std::int64_t p = row_start[r] + lane; p < row_start[r + 1]; p += 32) {
+            const std::uint64_t v = sorted[p];
+            out_keys[p] = (static_cast<std::uint64_t>(r) << 32) | (v >> 32);
+            const double* src = vals + 9 * static_cast<std::int64_t>(static_cast<std::uint32_t>(v));
+            for (int k = 0; k < 9; ++k) out_vals[9 * p + k] = src[k];
+        }
+}
+
+__global__ void k_count_rows(const std::uint32_t* __restrict__ rows, std::int64_t U, std::int32_t n,
+                             std::int32_t* __restrict__ cnt) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < U;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t r = rows[i];
+        if (r < static_cast<std::uint32_t>(n)) atomicAdd(cnt + r, 1);
+    }
+}
+
+// fast_segment_reduction (reduction.hpp:30-79): one thread per run head sums
+// its run left to right (deterministic-mode order) and stores the segment.
+__global__ void k_segment_reduce(const std::int32_t* __restrict__ O, std::int64_t n, const double* __restrict__ V,
+                                 int width, std::int32_t n_seg, double* __restrict__ R) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int32_t seg = O[i];
+        if (i > 0 && O[i - 1] == seg) continue;
+        if (seg < 0 || seg >= n_seg) continue;
+        double acc[9];
+        for (int k = 0; k < width; ++k) acc[k] = V[i * width + k];
+        for (std::int64_t j = i + 1; j < n && O[j] == seg; ++j)
+            for (int k = 0; k < width; ++k) acc[k] = __dadd_rn(acc[k], V[j * width + k]);
+        for (int k = 0; k < width; ++k) R[static_cast<std::int64_t>(seg) * width + k] = acc[k];
+    }
+}
+
+// filter_pinned (incremental_potential.hpp:410-425), step 1: keep flags.
+__global__ void k_pin_keep(const std::uint64_t* __restrict__ keys, std::int64_t T, const std::uint8_t* __restrict__ pinned,
+                           std::int32_t* __restrict__ keep) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t r = static_cast<std::uint32_t>(keys[i] >> 32);
+        const std::uint32_t c = static_cast<std::uint32_t>(keys[i]);
+        keep[i] = (pinned[r] || pinned[c]) ? 0 : 1;
+    }
+}
+
+__global__ void k_pin_compact(const std::uint64_t* __restrict__ keys, const double* __restrict__ vals, std::int64_t T,
+                              const std::int32_t* __restrict__ keep, const std::int64_t* __restrict__ pos,
+                              std::uint64_t* __restrict__ ok, double* __restrict__ ov) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        if (!keep[i]) continue;
+        const std::int64_t p = pos[i];
+        ok[p] = keys[i];
+        for (int k = 0; k < 9; ++k) ov[9 * p + k] = vals[9 * i + k];
+    }
+}
+
+__global__ void k_pin_identity(const std::uint8_t* __restrict__ pinned, std::int32_t n_slots,
+                               const std::int64_t* __restrict__ pos, std::int64_t base, std::uint64_t* __restrict__ ok,
+                               double* __restrict__ ov) {
+    for (std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; s < n_slots;
+         s += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        if (!pinned[s]) continue;
+        const std::int64_t p = base + pos[s];
+        ok[p] = (static_cast<std::uint64_t>(s) << 32) | static_cast<std::uint64_t>(s);
+        for (int k = 0; k < 9; ++k) ov[9 * p + k] = (k % 4 == 0) ? 1.0 : 0.0;
+    }
+}
+
+__global__ void k_u8_to_i32(const std::uint8_t* __restrict__ a, std::int64_t n, std::int32_t* __restrict__ b) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        b[i] = a[i] ? 1 : 0;
+}
+
+}  // namespace
+
+// Steps 1-5: bucket by row, sort each row by (col, emission index), count
+// unique cols. Leaves c.sorted / c.row_start / c.uniq_cnt filled. Throws
+// kInvalidArgument if a key's row is >= n.
+void bucket_sort(Ctx& c, const std::uint64_t* d_keys, std::int64_t T, std::int32_t n) {
+    cudaStream_t st = c.stream;
+    if (T >= (std::int64_t(1) << 32)) throw StatusError(kInvalidArgument, "triplet stream longer than 2^32");
+    c.row_cnt.reserve(static_cast<std::size_t>(n) + 1);
+    c.row_cursor.reserve(static_cast<std::size_t>(n) + 1);
+    c.uniq_cnt.reserve(static_cast<std::size_t>(n) + 1);
+    c.big_rows.reserve(static_cast<std::size_t>(n) + 1);
+    c.row_start.reserve(static_cast<std::size_t>(n) + 1);
+    c.counters.reserve(4);
+    c.sorted.reserve(static_cast<std::size_t>(T));
+    ADIPC_CUDA(cudaMemsetAsync(c.row_cnt.p, 0, sizeof(std::int32_t) * (n + 1), st));
+    ADIPC_CUDA(cudaMemsetAsync(c.row_cursor.p, 0, sizeof(std::int32_t) * (n + 1), st));
+    ADIPC_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(std::int32_t) * 4, st));
+    if (T > 0) {
+        k_row_hist<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, n, c.row_cnt.p, c.counters.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    exclusive_scan(c.row_cnt.p, n, c.row_start.p, c.scan_scratch, st);
+    if (T > 0) {
+        k_row_scatter<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, c.row_start.p, c.row_cursor.p, c.sorted.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    if (n > 0) {
+        k_sort_rows_warp<<<grid_for(n, 8, 8), 256, 0, st>>>(c.sorted.p, c.row_start.p, n, c.uniq_cnt.p, c.big_rows.p,
+                                                            c.counters.p + 1);
+        ADIPC_LAUNCH_CHECK();
+    }
+    int h_counters[2] = {0, 0};
+    ADIPC_CUDA(cudaMemcpyAsync(h_counters, c.counters.p, sizeof(h_counters), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    if (h_counters[0]) throw StatusError(kInvalidArgument, "block row index >= n_block_rows in triplet stream");
+    if (h_counters[1] > 0) {
+        const int nb = h_counters[1];
+        c.merge_scratch.reserve(static_cast<std::size_t>(T));
+        const int smem = kCtaSortMax * sizeof(std::uint64_t);
+        ADIPC_CUDA(cudaFuncSetAttribute(k_sort_rows_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        k_sort_rows_cta<<<std::min(nb, kSMs * 2), kCtaSortThreads, smem, st>>>(
+            c.sorted.p, c.merge_scratch.p, c.row_start.p, c.big_rows.p, c.counters.p + 1, c.uniq_cnt.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+}
+
+// Sort + reduce of a device-resident triplet stream into `out` (CSR row_ptr
+// included). Shared by the global assembly and the two-level ABD reduction.
+void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
+                 DeviceMatrix& out) {
+    cudaStream_t st = c.stream;
+    bucket_sort(c, d_keys, T, n);
+    out.n = n;
+    out.row_ptr.reserve(static_cast<std::size_t>(n) + 1);
+    exclusive_scan(c.uniq_cnt.p, n, out.row_ptr.p, c.scan_scratch, st);
+    std::int64_t U = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&U, out.row_ptr.p + n, sizeof(U), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    out.U = U;
+    out.rows.reserve(static_cast<std::size_t>(U));
+    out.cols.reserve(static_cast<std::size_t>(U));
+    out.blocks.reserve(static_cast<std::size_t>(U) * 9);
+    if (n > 0 && U > 0) {
+        k_reduce_rows<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, out.row_ptr.p, n, d_vals,
+                                                          out.rows.p, out.cols.p, out.blocks.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    ++out.version;
+}
+
+// sort_stream drop-in (block_coo.hpp:106-113): stable sort of the stream by
+// key, values following. Rows must be < 2^30 (block coordinates).
+void sort_stream(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::uint64_t* d_out_keys,
+                 double* d_out_vals) {
+    cudaStream_t st = c.stream;
+    if (T == 0) return;
+    c.counters.reserve(4);
+    ADIPC_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(std::int32_t) * 4, st));
+    k_max_row<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, reinterpret_cast<unsigned*>(c.counters.p + 2));
+    ADIPC_LAUNCH_CHECK();
+    unsigned max_row = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&max_row, c.counters.p + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    if (max_row >= (1u << 30)) throw StatusError(kInvalidArgument, "sort_stream: block row index >= 2^30");
+    const std::int32_t n = static_cast<std::int32_t>(max_row) + 1;
+    bucket_sort(c, d_keys, T, n);
+    k_gather_sorted<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, n, d_vals, d_out_keys, d_out_vals);
+    ADIPC_LAUNCH_CHECK();
+}
+
+void assemble(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
+              int /*deterministic: the device path is always the bitwise-deterministic order*/) {
+    sort_reduce(c, d_keys, d_vals, T, n, c.A);
+}
+
+void upload_matrix(Ctx& c, std::int32_t n, std::int64_t U, const std::uint32_t* rows, const std::uint32_t* cols,
+                   const double* blocks, bool host_ptrs) {
+    DeviceMatrix& A = c.A;
+    A.n = n;
+    A.U = U;
+    A.rows.reserve(U);
+    A.cols.reserve(U);
+    A.blocks.reserve(9 * U);
+    A.row_ptr.reserve(static_cast<std::size_t>(n) + 1);
+    const cudaMemcpyKind kind = host_ptrs ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    if (U > 0) {
+        ADIPC_CUDA(cudaMemcpyAsync(A.rows.p, rows, 4 * U, kind, c.stream));
+        ADIPC_CUDA(cudaMemcpyAsync(A.cols.p, cols, 4 * U, kind, c.stream));
+        ADIPC_CUDA(cudaMemcpyAsync(A.blocks.p, blocks, 72 * U, kind, c.stream));
+    }
+    // row_ptr from the sorted rows: histogram + scan
+    c.row_cnt.reserve(static_cast<std::size_t>(n) + 1);
+    ADIPC_CUDA(cudaMemsetAsync(c.row_cnt.p, 0, 4 * (static_cast<std::size_t>(n) + 1), c.stream));
+    if (U > 0) {
+        k_count_rows<<<grid_for(U, 256, 16), 256, 0, c.stream>>>(A.rows.p, U, n, c.row_cnt.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    exclusive_scan(c.row_cnt.p, n, A.row_ptr.p, c.scan_scratch, c.stream);
+    ++A.version;
+}
+
+}  // namespace adipc_gpu
+
+namespace adipc_gpu {
+
+void segment_reduce(Ctx& c, const std::int32_t* d_O, std::int64_t n, const double* d_V, int width,
+                    std::int32_t n_segments, double* d_R) {
+    if (width != 1 && width != 3 && width != 9) throw StatusError(kInvalidArgument, "width must be 1, 3 or 9");
+    if (n_segments > 0)
+        ADIPC_CUDA(cudaMemsetAsync(d_R, 0, sizeof(double) * width * static_cast<std::size_t>(n_segments), c.stream));
+    if (n > 0) {
+        k_segment_reduce<<<grid_for(n, 256, 16), 256, 0, c.stream>>>(d_O, n, d_V, width, n_segments, d_R);
+        ADIPC_LAUNCH_CHECK();
+    }
+}
+
+std::int64_t filter_pinned(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T,
+                           const std::uint8_t* d_pinned, std::int32_t n_slots, std::uint64_t* d_out_keys,
+                           double* d_out_vals) {
+    cudaStream_t st = c.stream;
+    DBuf<std::int32_t>& keep = c.pin_keep;
+    DBuf<std::int64_t>& pos = c.pin_pos;
+    DBuf<std::int64_t>& spos = c.pin_spos;
+    keep.reserve(static_cast<std::size_t>(std::max<std::int64_t>(T, n_slots)) + 1);
+    pos.reserve(static_cast<std::size_t>(T) + 1);
+    spos.reserve(static_cast<std::size_t>(n_slots) + 1);
+    std::int64_t kept = 0, npin = 0;
+    if (T > 0) {
+        k_pin_keep<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, d_pinned, keep.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    exclusive_scan(keep.p, T, pos.p, c.scan_scratch, st);
+    if (T > 0) {
+        k_pin_compact<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, d_vals, T, keep.p, pos.p, d_out_keys, d_out_vals);
+        ADIPC_LAUNCH_CHECK();
+    }
+    ADIPC_CUDA(cudaMemcpyAsync(&kept, pos.p + T, sizeof(kept), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    if (n_slots > 0) {
+        k_u8_to_i32<<<grid_for(n_slots, 256, 16), 256, 0, st>>>(d_pinned, n_slots, keep.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    exclusive_scan(keep.p, n_slots, spos.p, c.scan_scratch, st);
+    if (n_slots > 0) {
+        k_pin_identity<<<grid_for(n_slots, 256, 16), 256, 0, st>>>(d_pinned, n_slots, spos.p, kept, d_out_keys,
+                                                                 d_out_vals);
+        ADIPC_LAUNCH_CHECK();
+    }
+    ADIPC_CUDA(cudaMemcpyAsync(&npin, spos.p + n_slots, sizeof(npin), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    return kept + npin;
+}
+
+}  // namespace adipc_gpu

@@ -1,0 +1,581 @@
+// extern "C" entry points of include/adipc_gpu.h. Each wraps the C++
+// implementation in a try/catch that maps exceptions to status codes and
+// records the message on the context.
+#include <cstring>
+#include <vector>
+
+#include "../../include/adipc_gpu.h"
+#include "context.hpp"
+
+struct adipc_gpu_ctx {
+    adipc_gpu::Ctx c;
+};
+struct adipc_hierarchy {
+    adipc_gpu::host::MasHierarchy h;
+};
+
+namespace adipc_gpu {
+Ctx* unwrap(adipc_gpu_ctx* c) { return &c->c; }
+long long& launch_counter() {
+    static long long n = 0;
+    return n;
+}
+}  // namespace adipc_gpu
+
+using namespace adipc_gpu;
+
+namespace {
+
+thread_local std::string g_global_err;
+
+template <class F>
+int guarded(adipc_gpu_ctx* ctx, F&& f) {
+    try {
+        if (ctx) ADIPC_CUDA(cudaSetDevice(ctx->c.device));
+        f();
+        return ADIPC_OK;
+    } catch (const StatusError& e) {
+        (ctx ? ctx->c.err : g_global_err) = e.what();
+        return e.code;
+    } catch (const CudaError& e) {
+        (ctx ? ctx->c.err : g_global_err) = e.what();
+        return ADIPC_CUDA_ERROR;
+    } catch (const std::bad_alloc& e) {
+        (ctx ? ctx->c.err : g_global_err) = "host allocation failed";
+        return ADIPC_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        (ctx ? ctx->c.err : g_global_err) = e.what();
+        return ADIPC_INVALID_ARGUMENT;
+    }
+}
+
+template <class T>
+void h2d(DBuf<T>& d, const T* h, std::size_t n, cudaStream_t st) {
+    d.reserve(n);
+    if (n) ADIPC_CUDA(cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+void sync(Ctx& c) { ADIPC_CUDA(cudaStreamSynchronize(c.stream)); }
+
+}  // namespace
+
+extern "C" {
+
+int adipc_gpu_create(int device, adipc_gpu_ctx** out) {
+    if (!out) return ADIPC_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto* ctx = new adipc_gpu_ctx();
+    ctx->c.device = device;
+    const int rc = guarded(ctx, [&] {
+        int n = 0;
+        ADIPC_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) throw StatusError(kInvalidArgument, "no such CUDA device");
+        ADIPC_CUDA(cudaSetDevice(device));
+        ADIPC_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+        ctx->c.own_stream = true;
+    });
+    if (rc != ADIPC_OK) {
+        g_global_err = ctx->c.err;
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return ADIPC_OK;
+}
+
+int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
+    if (!ctx) return ADIPC_OK;
+    cudaSetDevice(ctx->c.device);
+    Ctx& c = ctx->c;
+    cudaStreamSynchronize(c.stream);
+    c.A.rows.free();
+    c.A.cols.free();
+    c.A.blocks.free();
+    c.A.row_ptr.free();
+    c.keys.free();
+    c.sorted.free();
+    c.merge_scratch.free();
+    c.vals.free();
+    c.row_cnt.free();
+    c.row_cursor.free();
+    c.uniq_cnt.free();
+    c.big_rows.free();
+    c.row_start.free();
+    c.uniq_start.free();
+    c.scan_scratch.free();
+    c.counters.free();
+    c.pinned.free();
+    for (auto& L : c.levels) {
+        L->agg.free();
+        L->part_of.free();
+        L->pos_of.free();
+        L->sub_ptr.free();
+        L->sub_nodes.free();
+        L->node_ptr.free();
+        L->node_slots.free();
+        L->inv_off.free();
+        L->inv.free();
+        L->y.free();
+    }
+    c.levels.clear();
+    c.jinv.free();
+    c.build_status.free();
+    for (auto* b : {&c.w.x, &c.w.r, &c.w.p, &c.w.ap, &c.w.z, &c.w.b, &c.w.tmp, &c.w.partials, &c.w.scal}) b->free();
+    c.w.tickets.free();
+    c.w.flags.free();
+    for (auto e : c.prof_events) cudaEventDestroy(e);
+    if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
+    delete ctx;
+    return ADIPC_OK;
+}
+
+const char* adipc_gpu_last_error(const adipc_gpu_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_global_err.c_str(); }
+
+int adipc_gpu_set_stream(adipc_gpu_ctx* ctx, void* stream) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        ADIPC_CUDA(cudaStreamSynchronize(c.stream));
+        if (stream) {
+            if (c.own_stream && c.stream) ADIPC_CUDA(cudaStreamDestroy(c.stream));
+            c.stream = static_cast<cudaStream_t>(stream);
+            c.own_stream = false;
+        } else if (!c.own_stream) {
+            ADIPC_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+            c.own_stream = true;
+        }
+    });
+}
+
+int adipc_gpu_set_option(adipc_gpu_ctx* ctx, int option, int value) {
+    return guarded(ctx, [&] {
+        if (option == ADIPC_OPT_CACHE_HIERARCHY)
+            ctx->c.cache_hierarchy = value != 0;
+        else if (option == ADIPC_OPT_PROFILE)
+            ctx->c.profile = value != 0;
+        else
+            throw StatusError(kInvalidArgument, "unknown option");
+    });
+}
+
+int64_t adipc_gpu_kernel_launches(void) { return launch_counter(); }
+
+int adipc_gpu_pcg_profile(adipc_gpu_ctx* ctx, float* ms4, int* iters) {
+    if (!ctx || !ms4) return ADIPC_INVALID_ARGUMENT;
+    for (int q = 0; q < 4; ++q) ms4[q] = ctx->c.prof_ms[q];
+    if (iters) *iters = ctx->c.prof_iters;
+    return ADIPC_OK;
+}
+
+int adipc_gpu_last_timings(adipc_gpu_ctx* ctx, float* ms4) {
+    if (!ctx || !ms4) return ADIPC_INVALID_ARGUMENT;
+    ms4[0] = ctx->c.ms_assemble;
+    ms4[1] = ctx->c.ms_build;
+    ms4[2] = ctx->c.ms_build_host;
+    ms4[3] = ctx->c.ms_pcg;
+    return ADIPC_OK;
+}
+
+// ---- assembly -----------------------------------------------------------------
+static void timed_assemble(Ctx& c, const std::uint64_t* k, const double* v, std::int64_t T, std::int32_t n, int det) {
+    cudaEvent_t e0, e1;
+    ADIPC_CUDA(cudaEventCreate(&e0));
+    ADIPC_CUDA(cudaEventCreate(&e1));
+    ADIPC_CUDA(cudaEventRecord(e0, c.stream));
+    assemble(c, k, v, T, n, det);
+    ADIPC_CUDA(cudaEventRecord(e1, c.stream));
+    ADIPC_CUDA(cudaEventSynchronize(e1));
+    ADIPC_CUDA(cudaEventElapsedTime(&c.ms_assemble, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+}
+
+int adipc_gpu_assemble(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T, int32_t n,
+                       int det, int64_t* n_unique) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (T < 0 || n < 0) throw StatusError(kInvalidArgument, "negative size");
+        h2d(c.keys, keys, static_cast<std::size_t>(T), c.stream);
+        h2d(c.vals, vals9, 9 * static_cast<std::size_t>(T), c.stream);
+        timed_assemble(c, c.keys.p, c.vals.p, T, n, det);
+        if (n_unique) *n_unique = c.A.U;
+    });
+}
+
+int adipc_gpu_assemble_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const double* d_vals9, int64_t T, int32_t n,
+                              int det, int64_t* n_unique) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (T < 0 || n < 0) throw StatusError(kInvalidArgument, "negative size");
+        timed_assemble(c, d_keys, d_vals9, T, n, det);
+        if (n_unique) *n_unique = c.A.U;
+    });
+}
+
+int adipc_gpu_matrix_info(adipc_gpu_ctx* ctx, int32_t* n, int64_t* U) {
+    return guarded(ctx, [&] {
+        if (n) *n = ctx->c.A.n;
+        if (U) *U = ctx->c.A.U;
+    });
+}
+
+int adipc_gpu_copy_matrix(adipc_gpu_ctx* ctx, uint32_t* rows, uint32_t* cols, double* blocks9) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const std::int64_t U = c.A.U;
+        if (U == 0) return;
+        if (rows) ADIPC_CUDA(cudaMemcpyAsync(rows, c.A.rows.p, 4 * U, cudaMemcpyDeviceToHost, c.stream));
+        if (cols) ADIPC_CUDA(cudaMemcpyAsync(cols, c.A.cols.p, 4 * U, cudaMemcpyDeviceToHost, c.stream));
+        if (blocks9) ADIPC_CUDA(cudaMemcpyAsync(blocks9, c.A.blocks.p, 72 * U, cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+    });
+}
+
+int adipc_gpu_set_matrix(adipc_gpu_ctx* ctx, int32_t n, int64_t U, const uint32_t* rows, const uint32_t* cols,
+                         const double* blocks9) {
+    return guarded(ctx, [&] {
+        if (n < 0 || U < 0) throw StatusError(kInvalidArgument, "negative size");
+        upload_matrix(ctx->c, n, U, rows, cols, blocks9, true);
+        sync(ctx->c);
+    });
+}
+
+int adipc_gpu_set_matrix_device(adipc_gpu_ctx* ctx, int32_t n, int64_t U, const uint32_t* rows, const uint32_t* cols,
+                                const double* blocks9) {
+    return guarded(ctx, [&] {
+        if (n < 0 || U < 0) throw StatusError(kInvalidArgument, "negative size");
+        upload_matrix(ctx->c, n, U, rows, cols, blocks9, false);
+        sync(ctx->c);
+    });
+}
+
+int adipc_gpu_sort_stream(adipc_gpu_ctx* ctx, uint64_t* keys, double* vals9, int64_t T) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (T <= 0) return;
+        h2d(c.keys, keys, static_cast<std::size_t>(T), c.stream);
+        h2d(c.vals, vals9, 9 * static_cast<std::size_t>(T), c.stream);
+        DBuf<std::uint64_t> ok;
+        DBuf<double> ov;
+        ok.reserve(T);
+        ov.reserve(9 * T);
+        sort_stream(c, c.keys.p, c.vals.p, T, ok.p, ov.p);
+        ADIPC_CUDA(cudaMemcpyAsync(keys, ok.p, 8 * T, cudaMemcpyDeviceToHost, c.stream));
+        ADIPC_CUDA(cudaMemcpyAsync(vals9, ov.p, 72 * T, cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+        ok.free();
+        ov.free();
+    });
+}
+
+int adipc_gpu_segment_reduce(adipc_gpu_ctx* ctx, const int32_t* O, int64_t nO, const double* V, int64_t nV, int width,
+                             int32_t n_segments, int /*deterministic*/, double* R) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (nO != nV) throw StatusError(kInvalidArgument, "segment map size mismatch");
+        if (n_segments < 0) throw StatusError(kInvalidArgument, "negative segment count");
+        DBuf<std::int32_t> dO;
+        DBuf<double> dV, dR;
+        h2d(dO, O, static_cast<std::size_t>(nO), c.stream);
+        h2d(dV, V, static_cast<std::size_t>(nV) * width, c.stream);
+        dR.reserve(static_cast<std::size_t>(n_segments) * width);
+        segment_reduce(c, dO.p, nO, dV.p, width, n_segments, dR.p);
+        if (n_segments)
+            ADIPC_CUDA(cudaMemcpyAsync(R, dR.p, sizeof(double) * width * n_segments, cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+        dO.free();
+        dV.free();
+        dR.free();
+    });
+}
+
+int adipc_gpu_two_level_abd_reduce(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t Tn,
+                                   int32_t n_fem, int32_t n_bodies, int32_t n_abd, const int32_t* body,
+                                   const double* jac36, uint64_t* out_keys, double* out_vals9, int64_t out_cap,
+                                   int64_t* n_out) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (Tn < 0 || n_fem < 0 || n_bodies < 0 || n_abd < 0) throw StatusError(kInvalidArgument, "negative size");
+        DBuf<std::uint64_t> dk, ok;
+        DBuf<double> dv, ov, dj;
+        DBuf<std::int32_t> db;
+        h2d(dk, keys, static_cast<std::size_t>(Tn), c.stream);
+        h2d(dv, vals9, 9 * static_cast<std::size_t>(Tn), c.stream);
+        h2d(db, body, static_cast<std::size_t>(n_abd), c.stream);
+        h2d(dj, jac36, 36 * static_cast<std::size_t>(n_abd), c.stream);
+        ok.reserve(static_cast<std::size_t>(out_cap));
+        ov.reserve(9 * static_cast<std::size_t>(out_cap));
+        const std::int64_t n = two_level_abd_reduce(c, dk.p, dv.p, Tn, n_fem, n_bodies, n_abd, db.p, dj.p, ok.p, ov.p,
+                                                    out_cap);
+        if (n) {
+            ADIPC_CUDA(cudaMemcpyAsync(out_keys, ok.p, 8 * n, cudaMemcpyDeviceToHost, c.stream));
+            ADIPC_CUDA(cudaMemcpyAsync(out_vals9, ov.p, 72 * n, cudaMemcpyDeviceToHost, c.stream));
+        }
+        sync(c);
+        if (n_out) *n_out = n;
+        for (auto* b : {&dk, &ok}) b->free();
+        for (auto* b : {&dv, &ov, &dj}) b->free();
+        db.free();
+    });
+}
+
+int adipc_gpu_filter_pinned(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T,
+                            const uint8_t* pinned, int32_t n_slots, uint64_t* out_keys, double* out_vals9,
+                            int64_t* n_out) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        DBuf<std::uint64_t> dk, ok;
+        DBuf<double> dv, ov;
+        DBuf<std::uint8_t> dp;
+        h2d(dk, keys, static_cast<std::size_t>(T), c.stream);
+        h2d(dv, vals9, 9 * static_cast<std::size_t>(T), c.stream);
+        h2d(dp, pinned, static_cast<std::size_t>(n_slots), c.stream);
+        ok.reserve(static_cast<std::size_t>(T + n_slots));
+        ov.reserve(9 * static_cast<std::size_t>(T + n_slots));
+        const std::int64_t n = filter_pinned(c, dk.p, dv.p, T, dp.p, n_slots, ok.p, ov.p);
+        if (n) {
+            ADIPC_CUDA(cudaMemcpyAsync(out_keys, ok.p, 8 * n, cudaMemcpyDeviceToHost, c.stream));
+            ADIPC_CUDA(cudaMemcpyAsync(out_vals9, ov.p, 72 * n, cudaMemcpyDeviceToHost, c.stream));
+        }
+        sync(c);
+        if (n_out) *n_out = n;
+        for (auto* b : {&dk, &ok}) b->free();
+        for (auto* b : {&dv, &ov}) b->free();
+        dp.free();
+    });
+}
+
+int adipc_gpu_filter_pinned_device(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T,
+                                   const uint8_t* pinned, int32_t n_slots, uint64_t* out_keys, double* out_vals9,
+                                   int64_t* n_out) {
+    return guarded(ctx, [&] {
+        const std::int64_t n = filter_pinned(ctx->c, keys, vals9, T, pinned, n_slots, out_keys, out_vals9);
+        if (n_out) *n_out = n;
+    });
+}
+
+// ---- SpMV ---------------------------------------------------------------------------
+int adipc_gpu_spmv(adipc_gpu_ctx* ctx, const double* x, double* y) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const std::size_t n3 = 3 * static_cast<std::size_t>(c.A.n);
+        DBuf<double> dx, dy;
+        h2d(dx, x, n3, c.stream);
+        dy.reserve(n3);
+        spmv(c, dx.p, dy.p, nullptr, 0);
+        if (n3) ADIPC_CUDA(cudaMemcpyAsync(y, dy.p, 8 * n3, cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+        dx.free();
+        dy.free();
+    });
+}
+
+int adipc_gpu_spmv_device(adipc_gpu_ctx* ctx, const double* d_x, double* d_y) {
+    return guarded(ctx, [&] {
+        spmv(ctx->c, d_x, d_y, nullptr, 0);
+        sync(ctx->c);
+    });
+}
+
+// ---- partition / hierarchy ---------------------------------------------------------------
+int32_t adipc_subdomain_count(int32_t v, int32_t n, int32_t n_o) { return host::subdomain_count(v, n, n_o); }
+
+int32_t adipc_chunk_partition(int32_t v, int32_t capacity, int32_t* part_of) {
+    const host::Partition p = host::chunk_partition(v, capacity);
+    if (v > 0) std::memcpy(part_of, p.part_of.data(), 4 * static_cast<std::size_t>(v));
+    return p.n_parts;
+}
+
+int32_t adipc_partition_block_graph(int32_t v, const int32_t* pairs, int64_t n_edges, int32_t capacity,
+                                    int32_t* part_of) {
+    const host::Partition p = host::partition_block_graph(v, pairs, static_cast<std::size_t>(n_edges), capacity);
+    if (v > 0) std::memcpy(part_of, p.part_of.data(), 4 * static_cast<std::size_t>(v));
+    return p.n_parts;
+}
+
+adipc_hierarchy* adipc_build_hierarchy(const int32_t* part_of, int32_t n_slots, int32_t n_parts, int32_t capacity,
+                                       const int32_t* pairs, int64_t n_edges, int32_t max_levels) {
+    host::Partition l0;
+    l0.part_of.assign(part_of, part_of + n_slots);
+    l0.n_parts = n_parts;
+    l0.capacity = capacity;
+    auto* h = new adipc_hierarchy();
+    h->h = host::build_hierarchy(l0, pairs, static_cast<std::size_t>(n_edges), max_levels);
+    return h;
+}
+
+int adipc_hierarchy_n_levels(const adipc_hierarchy* h) { return h ? h->h.n_levels() : 0; }
+
+static int level_out(const host::MasHierarchy& h, int level, int32_t* n_nodes, int32_t* n_parts, int32_t* part_of,
+                     int32_t* agg) {
+    if (level < 0 || level >= h.n_levels()) return ADIPC_INVALID_ARGUMENT;
+    const host::Level& L = h.levels[level];
+    if (n_nodes) *n_nodes = L.n_nodes;
+    if (n_parts) *n_parts = L.n_parts;
+    if (part_of && L.n_nodes) std::memcpy(part_of, L.part_of.data(), 4 * static_cast<std::size_t>(L.n_nodes));
+    if (agg && !L.agg.empty()) std::memcpy(agg, L.agg.data(), 4 * L.agg.size());
+    return ADIPC_OK;
+}
+
+int adipc_hierarchy_level(const adipc_hierarchy* h, int level, int32_t* n_nodes, int32_t* n_parts, int32_t* part_of,
+                          int32_t* agg) {
+    if (!h) return ADIPC_INVALID_ARGUMENT;
+    return level_out(h->h, level, n_nodes, n_parts, part_of, agg);
+}
+
+void adipc_hierarchy_free(adipc_hierarchy* h) { delete h; }
+
+// ---- preconditioner -----------------------------------------------------------------------
+int adipc_gpu_set_level0_partition(adipc_gpu_ctx* ctx, const int32_t* part_of, int32_t n_slots, int32_t n_parts,
+                                   int32_t capacity, int32_t max_levels) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (n_slots < 0 || n_parts < 0 || capacity <= 0) throw StatusError(kInvalidArgument, "bad partition sizes");
+        for (int32_t i = 0; i < n_slots; ++i)
+            if (part_of[i] < 0 || part_of[i] >= n_parts) throw StatusError(kInvalidArgument, "part_of out of range");
+        c.l0.part_of.assign(part_of, part_of + n_slots);
+        c.l0.n_parts = n_parts;
+        c.l0.capacity = capacity;
+        c.max_levels = max_levels;
+        c.have_l0 = true;
+        c.hier_version = ~0ull;
+        c.levels.clear();
+    });
+}
+
+int adipc_gpu_build_preconditioner(adipc_gpu_ctx* ctx, int kind) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (kind != ADIPC_PRECOND_MAS && kind != ADIPC_PRECOND_JACOBI)
+            throw StatusError(kInvalidArgument, "unknown preconditioner kind");
+        cudaEvent_t e0, e1;
+        ADIPC_CUDA(cudaEventCreate(&e0));
+        ADIPC_CUDA(cudaEventCreate(&e1));
+        ADIPC_CUDA(cudaEventRecord(e0, c.stream));
+        try {
+            build_preconditioner(c, kind == ADIPC_PRECOND_MAS ? kMas : kJacobi);
+        } catch (...) {
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            throw;
+        }
+        ADIPC_CUDA(cudaEventRecord(e1, c.stream));
+        ADIPC_CUDA(cudaEventSynchronize(e1));
+        ADIPC_CUDA(cudaEventElapsedTime(&c.ms_build, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}
+
+int adipc_gpu_build_mas(adipc_gpu_ctx* ctx, const adipc_hierarchy* h) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (!h) throw StatusError(kInvalidArgument, "null hierarchy");
+        if (h->h.n_slots != c.A.n) throw StatusError(kInvalidArgument, "hierarchy slot count differs from n_block_rows");
+        cudaEvent_t e0, e1;
+        ADIPC_CUDA(cudaEventCreate(&e0));
+        ADIPC_CUDA(cudaEventCreate(&e1));
+        ADIPC_CUDA(cudaEventRecord(e0, c.stream));
+        try {
+            build_mas_from_hierarchy(c, h->h);
+        } catch (...) {
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            throw;
+        }
+        ADIPC_CUDA(cudaEventRecord(e1, c.stream));
+        ADIPC_CUDA(cudaEventSynchronize(e1));
+        ADIPC_CUDA(cudaEventElapsedTime(&c.ms_build, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}
+
+int adipc_gpu_precond_n_levels(adipc_gpu_ctx* ctx) {
+    if (!ctx) return 0;
+    return ctx->c.pkind == kMas ? ctx->c.hier.n_levels() : (ctx->c.pkind == kJacobi ? 1 : 0);
+}
+
+int adipc_gpu_precond_level(adipc_gpu_ctx* ctx, int level, int32_t* n_nodes, int32_t* n_parts, int32_t* part_of,
+                            int32_t* agg) {
+    if (!ctx || ctx->c.pkind != kMas) return ADIPC_INVALID_ARGUMENT;
+    return level_out(ctx->c.hier, level, n_nodes, n_parts, part_of, agg);
+}
+
+int adipc_gpu_precond_subdomain_inverse(adipc_gpu_ctx* ctx, int level, int32_t sub, int32_t* dim, double* out) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (c.pkind != kMas || level < 0 || level >= static_cast<int>(c.levels.size()))
+            throw StatusError(kInvalidArgument, "no such level");
+        DeviceLevel& L = *c.levels[level];
+        if (sub < 0 || sub >= L.n_parts) throw StatusError(kInvalidArgument, "no such subdomain");
+        std::int32_t sp[2];
+        std::int64_t off = 0;
+        ADIPC_CUDA(cudaMemcpyAsync(sp, L.sub_ptr.p + sub, 8, cudaMemcpyDeviceToHost, c.stream));
+        ADIPC_CUDA(cudaMemcpyAsync(&off, L.inv_off.p + sub, 8, cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+        const int d = 3 * (sp[1] - sp[0]);
+        if (dim) *dim = d;
+        if (out && d) {
+            ADIPC_CUDA(cudaMemcpyAsync(out, L.inv.p + off, 8 * static_cast<std::size_t>(d) * d, cudaMemcpyDeviceToHost,
+                                       c.stream));
+            sync(c);
+        }
+    });
+}
+
+int adipc_gpu_precond_shifts(adipc_gpu_ctx* ctx, int64_t* shifts) {
+    if (!ctx || !shifts) return ADIPC_INVALID_ARGUMENT;
+    *shifts = ctx->c.shifts_applied;
+    return ADIPC_OK;
+}
+
+int adipc_gpu_precond_apply(adipc_gpu_ctx* ctx, const double* r, double* z) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const std::size_t n3 = 3 * static_cast<std::size_t>(c.A.n);
+        DBuf<double> dr, dz;
+        h2d(dr, r, n3, c.stream);
+        dz.reserve(n3);
+        precond_apply(c, dr.p, dz.p);
+        if (n3) ADIPC_CUDA(cudaMemcpyAsync(z, dz.p, 8 * n3, cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+        dr.free();
+        dz.free();
+    });
+}
+
+int adipc_gpu_precond_apply_device(adipc_gpu_ctx* ctx, const double* d_r, double* d_z) {
+    return guarded(ctx, [&] {
+        precond_apply(ctx->c, d_r, d_z);
+        sync(ctx->c);
+    });
+}
+
+// ---- PCG --------------------------------------------------------------------------------------
+int adipc_gpu_pcg(adipc_gpu_ctx* ctx, const double* b, double rel_tol, int restart, int max_iters, double* x,
+                  int* iters, double* rel_residual, int* converged) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const std::size_t n3 = 3 * static_cast<std::size_t>(c.A.n);
+        h2d(c.w.b, b, n3, c.stream);
+        c.w.x.reserve(n3);
+        const PcgOut o = pcg(c, c.w.b.p, rel_tol, restart, max_iters, c.w.x.p);
+        if (n3) ADIPC_CUDA(cudaMemcpyAsync(x, c.w.x.p, 8 * n3, cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+        if (iters) *iters = o.iters;
+        if (rel_residual) *rel_residual = o.rel_residual;
+        if (converged) *converged = o.converged;
+    });
+}
+
+int adipc_gpu_pcg_device(adipc_gpu_ctx* ctx, const double* d_b, double rel_tol, int restart, int max_iters, double* d_x,
+                         int* iters, double* rel_residual, int* converged) {
+    return guarded(ctx, [&] {
+        const PcgOut o = pcg(ctx->c, d_b, rel_tol, restart, max_iters, d_x);
+        if (iters) *iters = o.iters;
+        if (rel_residual) *rel_residual = o.rel_residual;
+        if (converged) *converged = o.converged;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// Shared device helpers for the adipc B200 path (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace adipc_gpu {
+
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define ADIPC_CUDA(expr)                                                                  \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            throw ::adipc_gpu::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e) + \
+                                         " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
+    } while (0)
+
+// Every kernel launch of the library is followed by ADIPC_LAUNCH_CHECK, which
+// also counts it (adipc_gpu_kernel_launches(), the bench's gpu_launches).
+long long& launch_counter();
+#define ADIPC_LAUNCH_CHECK()                \
+    do {                                    \
+        ++::adipc_gpu::launch_counter();    \
+        ADIPC_CUDA(cudaGetLastError());     \
+    } while (0)
+
+__host__ __device__ inline std::int64_t ceil_div(std::int64_t a, std::int64_t b) { return (a + b - 1) / b; }
+
+// Grid size for grid-stride kernels: enough CTAs for every SM several times
+// over, never more than the work needs.
+inline int grid_for(std::int64_t work_items, int items_per_cta, int per_sm = 8) {
+    std::int64_t g = ceil_div(work_items, items_per_cta);
+    const std::int64_t cap = static_cast<std::int64_t>(kSMs) * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+
+// Growable device buffer (capacity only grows; contents not preserved).
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    std::size_t cap = 0;
+    std::size_t n = 0;
+    void reserve(std::size_t count) {
+        if (count <= cap) {
+            n = count;
+            return;
+        }
+        if (p) cudaFree(p);
+        p = nullptr;
+        std::size_t c = count < 1 ? 1 : count;
+        ADIPC_CUDA(cudaMalloc(&p, c * sizeof(T)));
+        cap = c;
+        n = count;
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = n = 0;
+    }
+    std::size_t bytes() const { return n * sizeof(T); }
+};
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Block-wide sum of a double; result valid in thread 0. blockDim <= 1024.
+__device__ __forceinline__ double block_sum(double v, double* smem32) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) smem32[w] = v;
+    __syncthreads();
+    double s = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < nw; ++i) s += smem32[i];  // fixed order: deterministic
+    return s;
+}
+
+}  // namespace adipc_gpu
+
+namespace adipc_gpu {
+
+// Grid-wide deterministic reduction of one double per CTA: every CTA stores
+// its partial, the last CTA to arrive (ticket) sums all partials in a fixed
+// order and writes *out, then re-arms the ticket. Must be called by all
+// threads of every CTA; `v` is this thread's contribution.
+__device__ __forceinline__ void grid_sum_last_block(double v, double* partials, unsigned* ticket, double* out) {
+    __shared__ double red[32];
+    __shared__ bool last;
+    const double bs = block_sum(v, red);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = bs;
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double s = 0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) s += __ldcg(partials + i);
+    const double tot = block_sum(s, red);
+    if (threadIdx.x == 0) {
+        *out = tot;
+        *ticket = 0;
+    }
+}
+
+}  // namespace adipc_gpu

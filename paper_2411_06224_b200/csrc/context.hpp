@@ -1,0 +1,151 @@
+// Per-scene device context behind the C-ABI (include/adipc_gpu.h). One
+// context = one assembled system + its preconditioner + PCG workspace, all
+// resident in HBM. Not thread-safe per context; distinct contexts may live on
+// distinct host threads and devices (SURVEY.md §8b conventions).
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "host_precond.hpp"
+
+struct adipc_gpu_ctx;
+
+namespace adipc_gpu {
+
+// Status codes of the C-ABI (adipc_gpu.h).
+enum Status : int { kOk = 0, kInvalidArgument = 1, kIndefinite = 2, kCudaError = 3 };
+
+struct StatusError : std::runtime_error {
+    int code;
+    StatusError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// Assembled SortedSymBlockCoo (block_coo.hpp:54-61) in HBM.
+//   rows/cols u32[U], blocks f64[9U] (each block column-major, 72 B, exactly
+//   the reference's std::vector<Mat3> storage), row_ptr i64[n+1] (CSR offsets
+//   of the sorted rows, derived).
+struct DeviceMatrix {
+    std::int32_t n = 0;
+    std::int64_t U = 0;
+    DBuf<std::uint32_t> rows, cols;
+    DBuf<double> blocks;
+    DBuf<std::int64_t> row_ptr;
+    std::uint64_t version = 0;  // bumps on every (re)assembly / upload
+};
+
+// One MAS level in HBM (mas.hpp:106-113 LevelData, re-laid out for the GPU).
+struct DeviceLevel {
+    std::int32_t n_nodes = 0, n_parts = 0;
+    DBuf<std::int32_t> agg;        // slot -> node (level 0: identity, not stored)
+    DBuf<std::int32_t> part_of;    // node -> subdomain
+    DBuf<std::int32_t> pos_of;     // node -> position inside its subdomain
+    DBuf<std::int32_t> sub_ptr;    // subdomain -> first member node (CSR over sub_nodes)
+    DBuf<std::int32_t> sub_nodes;  // members of each subdomain, ascending node id (= pos order)
+    DBuf<std::int32_t> node_ptr;   // node -> first member slot (CSR over node_slots); levels >= 1
+    DBuf<std::int32_t> node_slots; // member slots of each node, ascending
+    DBuf<std::int64_t> inv_off;    // subdomain -> offset of its dense (3f)^2 inverse
+    DBuf<double> inv;              // explicit dense inverses, column-major (symmetric)
+    DBuf<double> y;                // level >= 1: per-node solution (3 per node)
+    std::int64_t inv_doubles = 0;
+    int max_fill = 0;
+};
+
+enum PrecondKind : int { kNone = 0, kMas = 1, kJacobi = 2 };
+
+struct PcgWork {
+    DBuf<double> x, r, p, ap, z, b, tmp;
+    DBuf<double> partials;       // per-CTA partial dots
+    DBuf<unsigned> tickets;      // last-block-done counters
+    DBuf<double> scal;           // device scalars (see pcg.cu)
+    DBuf<int> flags;             // device flags (see pcg.cu)
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+
+    DeviceMatrix A;
+
+    // assembly scratch
+    DBuf<std::uint64_t> keys, sorted, merge_scratch;
+    DBuf<double> vals;
+    DBuf<std::int32_t> row_cnt, row_cursor, uniq_cnt, big_rows;
+    DBuf<std::int64_t> row_start, uniq_start, scan_scratch;
+    DBuf<std::int32_t> counters;
+    DBuf<std::uint8_t> pinned;
+    DBuf<std::int32_t> pin_keep;
+    DBuf<std::int64_t> pin_pos, pin_spos;
+
+    // preconditioner
+    PrecondKind pkind = kNone;
+    host::Partition l0;             // level-0 partition (set once per scene)
+    int max_levels = 4;
+    bool have_l0 = false;
+    host::MasHierarchy hier;        // last built hierarchy (host copy)
+    std::uint64_t hier_version = ~0ull;
+    std::vector<std::unique_ptr<DeviceLevel>> levels;
+    DBuf<double> jinv;              // block-Jacobi 3x3 inverses, column-major
+    DBuf<double> invert_scratch;    // global work arrays for subdomains too large for smem
+    DBuf<int> build_status;
+    long shifts_applied = 0;
+    bool cache_hierarchy = false;   // reuse the hierarchy while the pattern is unchanged
+
+    PcgWork w;
+
+    // per-kernel-class PCG timing (ADIPC_OPT_PROFILE): spmv, level 0, coarse, final
+    bool profile = false;
+    std::vector<cudaEvent_t> prof_events;
+    float prof_ms[4] = {0, 0, 0, 0};
+    int prof_iters = 0;
+
+    // timings of the last calls, ms (CUDA events on `stream`)
+    float ms_assemble = 0, ms_build = 0, ms_build_host = 0, ms_pcg = 0;
+    int last_iters = 0;
+};
+
+Ctx* unwrap(adipc_gpu_ctx* c);
+
+// assemble.cu
+void assemble(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n_block_rows,
+              int deterministic);
+void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
+                 DeviceMatrix& out);
+void sort_stream(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::uint64_t* d_out_keys,
+                 double* d_out_vals);
+void upload_matrix(Ctx& c, std::int32_t n, std::int64_t U, const std::uint32_t* rows, const std::uint32_t* cols,
+                   const double* blocks, bool host_ptrs);
+void segment_reduce(Ctx& c, const std::int32_t* d_O, std::int64_t n, const double* d_V, int width,
+                    std::int32_t n_segments, double* d_R);
+std::int64_t filter_pinned(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T,
+                           const std::uint8_t* d_pinned, std::int32_t n_slots, std::uint64_t* d_out_keys,
+                           double* d_out_vals);
+
+// abd.cu
+std::int64_t two_level_abd_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t Tn,
+                                  std::int32_t n_fem, std::int32_t n_bodies, std::int32_t n_abd,
+                                  const std::int32_t* d_body, const double* d_jac36, std::uint64_t* d_out_keys,
+                                  double* d_out_vals, std::int64_t out_cap);
+
+// spmv.cu
+void spmv(Ctx& c, const double* d_x, double* d_y, double* d_pdot_partials, int n_partials);
+int spmv_grid(const Ctx& c);
+
+// mas.cu
+void build_preconditioner(Ctx& c, PrecondKind kind);
+void build_mas_from_hierarchy(Ctx& c, const host::MasHierarchy& h);
+void precond_apply(Ctx& c, const double* d_r, double* d_z);
+
+// pcg.cu
+struct PcgOut {
+    int iters = 0;
+    double rel_residual = 0;
+    int converged = 0;
+};
+PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters, double* d_x);
+
+}  // namespace adipc_gpu

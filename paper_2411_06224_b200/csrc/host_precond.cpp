@@ -1,0 +1,243 @@
+// See host_precond.hpp. Integer-exact with the reference; the parity tests
+// compare every output array against the oracle restatement.
+#include "host_precond.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace adipc_gpu::host {
+
+Index subdomain_count(Index v, Index n, Index n_o) {  // partition.hpp:12-15
+    const Index eff = n - n_o;
+    return (v + eff - 1) / eff;
+}
+
+Partition chunk_partition(Index v, Index capacity) {  // partition.hpp:25-32
+    Partition p;
+    p.capacity = capacity;
+    p.part_of.resize(v);
+    for (Index i = 0; i < v; ++i) p.part_of[i] = i / capacity;
+    p.n_parts = v == 0 ? 0 : (v - 1) / capacity + 1;
+    return p;
+}
+
+Graph build_graph(Index v, const Index* pairs, std::size_t n_edges) {  // partition.hpp:37-50
+    Graph g;
+    g.ptr.assign(static_cast<std::size_t>(v) + 1, 0);
+    for (std::size_t e = 0; e < n_edges; ++e) {
+        const Index a = pairs[2 * e], b = pairs[2 * e + 1];
+        if (a == b) continue;
+        ++g.ptr[a + 1];
+        ++g.ptr[b + 1];
+    }
+    for (Index i = 0; i < v; ++i) g.ptr[i + 1] += g.ptr[i];
+    g.adj.resize(g.ptr[v]);
+    std::vector<std::int64_t> cur(g.ptr.begin(), g.ptr.end() - 1);
+    for (std::size_t e = 0; e < n_edges; ++e) {
+        const Index a = pairs[2 * e], b = pairs[2 * e + 1];
+        if (a == b) continue;
+        g.adj[cur[a]++] = b;
+        g.adj[cur[b]++] = a;
+    }
+    // sort + unique each list, compacting in place
+    std::int64_t w = 0;
+    for (Index i = 0; i < v; ++i) {
+        Index* beg = g.adj.data() + g.ptr[i];
+        Index* end = g.adj.data() + g.ptr[i + 1];
+        if (!std::is_sorted(beg, end)) std::sort(beg, end);
+        const std::int64_t start = w;
+        Index last = kInvalid;
+        for (Index* it = beg; it != end; ++it)
+            if (it == beg || *it != last) {
+                last = *it;
+                g.adj[w++] = *it;
+            }
+        g.ptr[i] = start;
+    }
+    g.ptr[v] = w;
+    g.adj.resize(w);
+    return g;
+}
+
+// partition.hpp:54-77 BFS components + partition.hpp:88-159 packing/carving.
+Partition partition_block_graph(Index v, const Graph& g, Index capacity) {
+    Partition p;
+    p.capacity = capacity;
+    p.part_of.assign(v, 0);
+    // components in discovery order, flattened
+    std::vector<Index> order;
+    order.reserve(v);
+    std::vector<std::int64_t> comp_ptr;
+    comp_ptr.reserve(64);
+    {
+        std::vector<char> seen(v, 0);
+        for (Index start = 0; start < v; ++start) {
+            if (seen[start]) continue;
+            comp_ptr.push_back(static_cast<std::int64_t>(order.size()));
+            seen[start] = 1;
+            std::size_t head = order.size();
+            order.push_back(start);
+            for (; head < order.size(); ++head) {
+                const Index cur = order[head];
+                for (std::int64_t k = g.ptr[cur]; k < g.ptr[cur + 1]; ++k) {
+                    const Index nb = g.adj[k];
+                    if (!seen[nb]) {
+                        seen[nb] = 1;
+                        order.push_back(nb);
+                    }
+                }
+            }
+        }
+        comp_ptr.push_back(static_cast<std::int64_t>(order.size()));
+    }
+    std::vector<char> assigned(v, 0);
+    std::vector<Index> conn(v, 0);
+    std::vector<Index> cand, touched;
+    Index next_part = 0, open_part = kInvalid, open_fill = 0;
+    const std::size_t n_comps = comp_ptr.size() - 1;
+    for (std::size_t ci = 0; ci < n_comps; ++ci) {
+        const Index* comp = order.data() + comp_ptr[ci];
+        const Index size = static_cast<Index>(comp_ptr[ci + 1] - comp_ptr[ci]);
+        if (size <= capacity) {  // next fit (partition.hpp:105-112)
+            if (open_part == kInvalid || open_fill + size > capacity) {
+                open_part = next_part++;
+                open_fill = 0;
+            }
+            for (Index k = 0; k < size; ++k) p.part_of[comp[k]] = open_part;
+            open_fill += size;
+            continue;
+        }
+        const Index chunks = subdomain_count(size, capacity, 0);
+        const Index base = size / chunks, extra = size % chunks;
+        Index seed_at = 0, chunk = 0, left = size;
+        while (left > 0) {
+            const Index target = chunk < chunks ? base + (chunk < extra ? 1 : 0) : capacity;
+            ++chunk;
+            while (assigned[comp[seed_at]]) ++seed_at;
+            Index pick = comp[seed_at];
+            const Index part = next_part++;
+            cand.clear();
+            touched.clear();
+            for (Index fill = 0; pick != kInvalid;) {
+                p.part_of[pick] = part;
+                assigned[pick] = 1;
+                ++fill;
+                --left;
+                if (fill == target || left == 0) break;
+                for (std::int64_t k = g.ptr[pick]; k < g.ptr[pick + 1]; ++k) {
+                    const Index nb = g.adj[k];
+                    if (!assigned[nb]) {
+                        if (conn[nb] == 0) {
+                            cand.push_back(nb);
+                            touched.push_back(nb);
+                        }
+                        ++conn[nb];
+                    }
+                }
+                // argmax conn, ties -> lowest id (order independent), so
+                // assigned candidates can be compacted away as we scan.
+                pick = kInvalid;
+                Index best = 0;
+                std::size_t w = 0;
+                for (std::size_t k = 0; k < cand.size(); ++k) {
+                    const Index c = cand[k];
+                    if (assigned[c]) continue;
+                    cand[w++] = c;
+                    if (pick == kInvalid || conn[c] > best || (conn[c] == best && c < pick)) {
+                        pick = c;
+                        best = conn[c];
+                    }
+                }
+                cand.resize(w);
+            }
+            for (Index t : touched) conn[t] = 0;
+        }
+    }
+    p.n_parts = next_part;
+    return p;
+}
+
+Partition partition_block_graph(Index v, const Index* pairs, std::size_t n_edges, Index capacity) {
+    return partition_block_graph(v, build_graph(v, pairs, n_edges), capacity);
+}
+
+// hierarchy.hpp:30-100
+MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_t n_edges, int max_levels) {
+    MasHierarchy h;
+    h.capacity = l0.capacity;
+    h.n_slots = static_cast<Index>(l0.part_of.size());
+    Level base;
+    base.n_nodes = h.n_slots;
+    base.n_parts = l0.n_parts;
+    base.part_of = l0.part_of;
+    base.agg.resize(h.n_slots);
+    for (Index i = 0; i < h.n_slots; ++i) base.agg[i] = i;
+    h.levels.push_back(std::move(base));
+
+    std::vector<Index> cur_edges(pairs, pairs + 2 * n_edges);
+    std::vector<Index> up, queue, members, mem_ptr;
+    std::vector<std::uint64_t> packed;
+    while (h.n_levels() < max_levels) {
+        const Level& cur = h.levels.back();
+        if (cur.n_parts <= 1) break;
+        const Graph g = build_graph(cur.n_nodes, cur_edges.data(), cur_edges.size() / 2);
+        // members of each subdomain in ascending node order (counting sort)
+        mem_ptr.assign(static_cast<std::size_t>(cur.n_parts) + 1, 0);
+        for (Index i = 0; i < cur.n_nodes; ++i) ++mem_ptr[cur.part_of[i] + 1];
+        for (Index s = 0; s < cur.n_parts; ++s) mem_ptr[s + 1] += mem_ptr[s];
+        members.resize(cur.n_nodes);
+        {
+            std::vector<Index> fill(mem_ptr.begin(), mem_ptr.end() - 1);
+            for (Index i = 0; i < cur.n_nodes; ++i) members[fill[cur.part_of[i]]++] = i;
+        }
+        up.assign(cur.n_nodes, kInvalid);
+        Index n_next = 0;
+        for (Index s = 0; s < cur.n_parts; ++s)
+            for (Index k = mem_ptr[s]; k < mem_ptr[s + 1]; ++k) {
+                const Index seed = members[k];
+                if (up[seed] != kInvalid) continue;
+                const Index super = n_next++;
+                up[seed] = super;
+                queue.assign(1, seed);
+                for (std::size_t head = 0; head < queue.size(); ++head) {
+                    const Index q = queue[head];
+                    for (std::int64_t e = g.ptr[q]; e < g.ptr[q + 1]; ++e) {
+                        const Index nb = g.adj[e];
+                        if (cur.part_of[nb] == s && up[nb] == kInvalid) {
+                            up[nb] = super;
+                            queue.push_back(nb);
+                        }
+                    }
+                }
+            }
+        if (n_next == cur.n_nodes) break;
+        packed.clear();
+        packed.reserve(cur_edges.size() / 2);
+        for (std::size_t e = 0; e + 1 < cur_edges.size(); e += 2) {
+            Index ua = up[cur_edges[e]], ub = up[cur_edges[e + 1]];
+            if (ua == ub) continue;
+            if (ua > ub) std::swap(ua, ub);
+            packed.push_back((static_cast<std::uint64_t>(static_cast<std::uint32_t>(ua)) << 32) |
+                             static_cast<std::uint32_t>(ub));
+        }
+        std::sort(packed.begin(), packed.end());
+        packed.erase(std::unique(packed.begin(), packed.end()), packed.end());
+        std::vector<Index> next_edges(2 * packed.size());
+        for (std::size_t e = 0; e < packed.size(); ++e) {
+            next_edges[2 * e] = static_cast<Index>(packed[e] >> 32);
+            next_edges[2 * e + 1] = static_cast<Index>(packed[e] & 0xFFFFFFFFu);
+        }
+        Level next;
+        next.n_nodes = n_next;
+        Partition grouped = partition_block_graph(n_next, next_edges.data(), packed.size(), h.capacity);
+        next.n_parts = grouped.n_parts;
+        next.part_of = std::move(grouped.part_of);
+        next.agg.resize(h.n_slots);
+        for (Index slot = 0; slot < h.n_slots; ++slot) next.agg[slot] = up[cur.agg[slot]];
+        h.levels.push_back(std::move(next));
+        cur_edges = std::move(next_edges);
+    }
+    return h;
+}
+
+}  // namespace adipc_gpu::host

@@ -1,0 +1,56 @@
+// Host-side (C++) partition and aggregation-hierarchy construction of the MAS
+// preconditioner: integer-exact re-implementations of
+//   precond/partition.hpp:12-159  (subdomain_count, chunk_partition,
+//                                  partition_block_graph)
+//   precond/hierarchy.hpp:30-100  (build_hierarchy)
+// over CSR adjacency instead of vector<vector>. These are sequential greedy
+// algorithms on graphs that are small after level 0, so they stay on the host;
+// their outputs (part_of / agg per level) feed the device restriction and
+// inversion kernels in mas.cu.
+#pragma once
+
+#include <cstdint>
+#include <utility>
+#include <vector>
+
+namespace adipc_gpu::host {
+
+using Index = std::int32_t;
+constexpr Index kInvalid = -1;
+
+struct Partition {
+    std::vector<Index> part_of;
+    Index n_parts = 0;
+    Index capacity = 0;
+};
+
+struct Level {
+    Index n_nodes = 0;
+    Index n_parts = 0;
+    std::vector<Index> part_of;  // node -> subdomain
+    std::vector<Index> agg;      // slot -> node
+};
+
+struct MasHierarchy {
+    Index capacity = 0;
+    Index n_slots = 0;
+    std::vector<Level> levels;
+    int n_levels() const { return static_cast<int>(levels.size()); }
+};
+
+// Undirected simple graph in CSR form: neighbours sorted ascending, unique,
+// self loops dropped (partition.hpp:37-50 semantics).
+struct Graph {
+    std::vector<std::int64_t> ptr;
+    std::vector<Index> adj;
+    Index n() const { return static_cast<Index>(ptr.size()) - 1; }
+};
+
+Index subdomain_count(Index v, Index n, Index n_o);
+Partition chunk_partition(Index v, Index capacity);
+Graph build_graph(Index v, const Index* pairs, std::size_t n_edges);  // pairs: (a,b) interleaved
+Partition partition_block_graph(Index v, const Graph& g, Index capacity);
+Partition partition_block_graph(Index v, const Index* pairs, std::size_t n_edges, Index capacity);
+MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_t n_edges, int max_levels);
+
+}  // namespace adipc_gpu::host

@@ -1,0 +1,484 @@
+// MAS preconditioner construction on B200 (replaces
+// TimeStepper::build_preconditioner, solver/newton.hpp:243-255:
+// block_edges + build_hierarchy + MasPreconditioner::build, and
+// BlockJacobiPreconditioner::build):
+//   host:   block_edges (D2H of the pattern) -> build_hierarchy (host_precond)
+//           -> per-level CSR metadata (sub_nodes, pos_of, node_slots)
+//   device: K9 Galerkin restriction of A onto every level in ONE pass over A
+//           (mas.hpp:56-64; level 0 is conflict-free and written directly,
+//           coarser levels use fp64 atomics), then
+//           K10 batched in-shared-memory Cholesky with the reference's
+//           regularisation retry (mas.hpp:66-81: eps = 1e-8 tr/dim, shifts
+//           eps, 100 eps, 1e4 eps cumulatively, failure after the 4th attempt)
+//           and explicit inverse D^-1 = L^-T L^-1 (paper Alg. 1), one CTA per
+//           subdomain.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "mas_kernels.cuh"
+
+
+namespace adipc_gpu {
+
+namespace {
+
+struct RestrictLevel {
+    const std::int32_t* agg;      // null at level 0 (identity)
+    const std::int32_t* part_of;
+    const std::int32_t* pos_of;
+    const std::int64_t* inv_off;
+    const std::int32_t* sub_ptr;
+    double* dense;
+};
+struct RestrictArgs {
+    int n_levels;
+    RestrictLevel lv[kMaxCoarse + 1];
+};
+
+__device__ __forceinline__ void add_tile(double* D, int dim, int pr, int pc, const double* h, bool transpose,
+                                         bool atomic) {
+    // D column-major: D(3pr+i, 3pc+j) at [(3pc+j)*dim + 3pr+i]; h column-major H(i,j)=h[3j+i]
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double v = transpose ? h[3 * i + j] : h[3 * j + i];
+            double* dst = D + static_cast<std::int64_t>(3 * pc + j) * dim + 3 * pr + i;
+            if (atomic)
+                atomicAdd(dst, v);
+            else
+                *dst += v;
+        }
+}
+
+__global__ void k_restrict(const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,
+                           const double* __restrict__ blocks, std::int64_t U, RestrictArgs ra) {
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < U;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int32_t r = rows[e], c = cols[e];
+        double h[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) h[k] = blocks[9 * e + k];
+        for (int l = 0; l < ra.n_levels; ++l) {
+            const RestrictLevel& L = ra.lv[l];
+            const std::int32_t nr = L.agg ? L.agg[r] : r;
+            const std::int32_t nc = L.agg ? L.agg[c] : c;
+            const std::int32_t s = L.part_of[nr];
+            if (s != L.part_of[nc]) continue;
+            const int dim = 3 * (L.sub_ptr[s + 1] - L.sub_ptr[s]);
+            double* D = L.dense + L.inv_off[s];
+            const int pr = L.pos_of[nr], pc = L.pos_of[nc];
+            const bool atomic = l > 0;
+            add_tile(D, dim, pr, pc, h, false, atomic);
+            if (r != c) add_tile(D, dim, pc, pr, h, true, atomic);
+        }
+    }
+}
+
+// One CTA per subdomain: Cholesky with retry, then explicit inverse.
+// Work arrays S (dim x dim, column-major) + X (dim x dim) live in shared
+// memory, or — for subdomains too large for it (capacity > 32) — in a global
+// scratch slice per CTA (`gscratch`, 2 * max_dim^2 doubles per CTA).
+__global__ void k_invert(std::int32_t n_parts, const std::int32_t* __restrict__ sub_ptr,
+                         const std::int64_t* __restrict__ inv_off, double* __restrict__ dense,
+                         int* __restrict__ status, int* __restrict__ shifts, double* __restrict__ gscratch,
+                         int max_dim) {
+    extern __shared__ double sm[];
+    __shared__ int fail;
+    __shared__ double eps0;
+    double* work = gscratch ? gscratch + 2 * static_cast<std::int64_t>(max_dim) * max_dim * blockIdx.x : sm;
+    for (std::int32_t s = blockIdx.x; s < n_parts; s += gridDim.x) {
+        const int dim = 3 * (sub_ptr[s + 1] - sub_ptr[s]);
+        if (dim == 0) continue;
+        double* S = work;
+        double* X = work + dim * dim;
+        double* D = dense + inv_off[s];
+        const int nn = dim * dim;
+        if (threadIdx.x == 0) {
+            double tr = 0;
+            for (int k = 0; k < dim; ++k) tr += D[k * dim + k];
+            double e = 1e-8 * tr / dim;
+            if (!(e > 0)) e = 1e-12;
+            eps0 = e;
+        }
+        __syncthreads();
+        int attempt = 0;
+        for (;; ++attempt) {
+            for (int i = threadIdx.x; i < nn; i += blockDim.x) S[i] = D[i];
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                fail = 0;
+                // cumulative shifts D += eps, D += 100 eps, ... (mas.hpp:78-79)
+                double e = eps0;
+                for (int a = 0; a < attempt; ++a) {
+                    for (int k = 0; k < dim; ++k) S[k * dim + k] += e;
+                    e *= 100;
+                }
+            }
+            __syncthreads();
+            // right-looking Cholesky on the lower triangle
+            for (int k = 0; k < dim; ++k) {
+                if (threadIdx.x == 0) {
+                    const double x = S[k * dim + k];
+                    if (x <= 0)  // Eigen LLT: non-positive pivot fails; NaN does not
+                        fail = 1;
+                    else
+                        S[k * dim + k] = sqrt(x);
+                }
+                __syncthreads();
+                if (fail) break;
+                const double piv = S[k * dim + k];
+                for (int i = k + 1 + threadIdx.x; i < dim; i += blockDim.x) S[k * dim + i] /= piv;
+                __syncthreads();
+                const int m = dim - k - 1;
+                for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+                    const int i = k + 1 + t % m, j = k + 1 + t / m;
+                    if (j <= i) S[j * dim + i] -= S[k * dim + i] * S[k * dim + j];
+                }
+                __syncthreads();
+            }
+            if (!fail) break;
+            __syncthreads();
+            if (attempt >= 3) break;
+        }
+        if (fail) {
+            if (threadIdx.x == 0) atomicOr(status, 1);
+            __syncthreads();
+            continue;
+        }
+        if (threadIdx.x == 0 && attempt > 0) atomicAdd(shifts, attempt);
+        // X = L^-1 (lower), column j by thread j: forward substitution
+        for (int j = threadIdx.x; j < dim; j += blockDim.x) {
+            for (int i = 0; i < dim; ++i) {
+                if (i < j) {
+                    X[j * dim + i] = 0;
+                    continue;
+                }
+                double v = (i == j) ? 1.0 : 0.0;
+                for (int k = j; k < i; ++k) v -= S[k * dim + i] * X[j * dim + k];
+                X[j * dim + i] = v / S[i * dim + i];
+            }
+        }
+        __syncthreads();
+        // D^-1 = X^T X, symmetric: compute lower, mirror
+        for (int t = threadIdx.x; t < nn; t += blockDim.x) {
+            const int i = t % dim, j = t / dim;
+            if (j > i) continue;
+            double v = 0;
+            for (int k = i; k < dim; ++k) v += X[i * dim + k] * X[j * dim + k];
+            D[j * dim + i] = v;
+            D[i * dim + j] = v;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_jacobi_build(std::int32_t n, const std::uint32_t* __restrict__ cols, const double* __restrict__ blocks,
+                               const std::int64_t* __restrict__ row_ptr, double* __restrict__ jinv) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        double a[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+        for (std::int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
+            if (cols[e] == static_cast<std::uint32_t>(i)) {
+                for (int k = 0; k < 9; ++k) a[k] = blocks[9 * e + k];
+                // adjugate inverse (Mat3::inverse), a column-major: A(r,c) = a[3c+r]
+                auto A = [&](int r, int c) { return a[3 * c + r]; };
+                double cof[9];
+                auto C = [&](int r, int c) -> double& { return cof[3 * c + r]; };
+                C(0, 0) = A(1, 1) * A(2, 2) - A(1, 2) * A(2, 1);
+                C(1, 0) = A(1, 2) * A(2, 0) - A(1, 0) * A(2, 2);
+                C(2, 0) = A(1, 0) * A(2, 1) - A(1, 1) * A(2, 0);
+                const double det = A(0, 0) * C(0, 0) + A(0, 1) * C(1, 0) + A(0, 2) * C(2, 0);
+                C(0, 1) = A(0, 2) * A(2, 1) - A(0, 1) * A(2, 2);
+                C(1, 1) = A(0, 0) * A(2, 2) - A(0, 2) * A(2, 0);
+                C(2, 1) = A(0, 1) * A(2, 0) - A(0, 0) * A(2, 1);
+                C(0, 2) = A(0, 1) * A(1, 2) - A(0, 2) * A(1, 1);
+                C(1, 2) = A(0, 2) * A(1, 0) - A(0, 0) * A(1, 2);
+                C(2, 2) = A(0, 0) * A(1, 1) - A(0, 1) * A(1, 0);
+                for (int k = 0; k < 9; ++k) a[k] = cof[k] / det;
+                break;
+            }
+        for (int k = 0; k < 9; ++k) jinv[9 * i + k] = a[k];
+    }
+}
+
+template <class T>
+void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
+    d.reserve(h.size());
+    if (!h.empty()) ADIPC_CUDA(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+// Per-level CSR metadata from a hierarchy level (mas.hpp:42-54 semantics:
+// pos_of = rank of the node among its subdomain's nodes in ascending id).
+void build_level(Ctx& c, DeviceLevel& L, const host::Level& hl, int level, std::int32_t n_slots) {
+    cudaStream_t st = c.stream;
+    L.n_nodes = hl.n_nodes;
+    L.n_parts = hl.n_parts;
+    std::vector<std::int32_t> sub_ptr(hl.n_parts + 1, 0), pos_of(hl.n_nodes), sub_nodes(hl.n_nodes);
+    for (std::int32_t v = 0; v < hl.n_nodes; ++v) pos_of[v] = sub_ptr[hl.part_of[v] + 1]++;
+    int max_fill = 0;
+    for (std::int32_t s = 0; s < hl.n_parts; ++s) max_fill = std::max(max_fill, sub_ptr[s + 1]);
+    for (std::int32_t s = 0; s < hl.n_parts; ++s) sub_ptr[s + 1] += sub_ptr[s];
+    for (std::int32_t v = 0; v < hl.n_nodes; ++v) sub_nodes[sub_ptr[hl.part_of[v]] + pos_of[v]] = v;
+    std::vector<std::int64_t> inv_off(hl.n_parts + 1, 0);
+    for (std::int32_t s = 0; s < hl.n_parts; ++s) {
+        const std::int64_t d = 3 * static_cast<std::int64_t>(sub_ptr[s + 1] - sub_ptr[s]);
+        inv_off[s + 1] = inv_off[s] + d * d;
+    }
+    L.max_fill = max_fill;
+    L.inv_doubles = inv_off[hl.n_parts];
+    upload(L.part_of, hl.part_of, st);
+    upload(L.pos_of, pos_of, st);
+    upload(L.sub_ptr, sub_ptr, st);
+    upload(L.sub_nodes, sub_nodes, st);
+    upload(L.inv_off, inv_off, st);
+    if (level > 0) {
+        upload(L.agg, hl.agg, st);
+        std::vector<std::int32_t> node_ptr(hl.n_nodes + 1, 0), node_slots(n_slots);
+        for (std::int32_t s = 0; s < n_slots; ++s) ++node_ptr[hl.agg[s] + 1];
+        for (std::int32_t v = 0; v < hl.n_nodes; ++v) node_ptr[v + 1] += node_ptr[v];
+        std::vector<std::int32_t> fill(node_ptr.begin(), node_ptr.end() - 1);
+        for (std::int32_t s = 0; s < n_slots; ++s) node_slots[fill[hl.agg[s]]++] = s;  // ascending slots
+        upload(L.node_ptr, node_ptr, st);
+        upload(L.node_slots, node_slots, st);
+        L.y.reserve(3 * static_cast<std::size_t>(hl.n_nodes));
+    }
+    L.inv.reserve(static_cast<std::size_t>(L.inv_doubles));
+    ADIPC_CUDA(cudaMemsetAsync(L.inv.p, 0, sizeof(double) * std::max<std::int64_t>(L.inv_doubles, 1), st));
+}
+
+}  // namespace
+
+// K9 restriction + K10 batched factorisation/inversion for the current levels.
+void factorize(Ctx& c) {
+    cudaStream_t st = c.stream;
+    const DeviceMatrix& A = c.A;
+    RestrictArgs ra{};
+    ra.n_levels = static_cast<int>(c.levels.size());
+    for (int l = 0; l < ra.n_levels; ++l) {
+        DeviceLevel& L = *c.levels[l];
+        ra.lv[l] = RestrictLevel{l > 0 ? L.agg.p : nullptr, L.part_of.p, L.pos_of.p, L.inv_off.p, L.sub_ptr.p, L.inv.p};
+    }
+    if (A.U > 0) {
+        k_restrict<<<grid_for(A.U, 256, 16), 256, 0, st>>>(A.rows.p, A.cols.p, A.blocks.p, A.U, ra);
+        ADIPC_LAUNCH_CHECK();
+    }
+    c.build_status.reserve(2);
+    ADIPC_CUDA(cudaMemsetAsync(c.build_status.p, 0, 2 * sizeof(int), st));
+    for (auto& Lp : c.levels) {
+        DeviceLevel& L = *Lp;
+        if (L.n_parts == 0) continue;
+        const int dim = 3 * L.max_fill;
+        const std::size_t need = 2 * sizeof(double) * dim * dim;
+        const bool in_smem = need <= 200 * 1024;
+        const int threads = dim <= 48 ? 128 : 256;
+        const int grid = static_cast<int>(std::min<std::int64_t>(L.n_parts, in_smem ? kSMs * 16 : kSMs * 2));
+        if (!in_smem) c.invert_scratch.reserve(need / sizeof(double) * grid);
+        const std::size_t smem = in_smem ? need : 0;
+        ADIPC_CUDA(cudaFuncSetAttribute(k_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        k_invert<<<grid, threads, smem, st>>>(L.n_parts, L.sub_ptr.p, L.inv_off.p, L.inv.p, c.build_status.p,
+                                              c.build_status.p + 1, in_smem ? nullptr : c.invert_scratch.p, dim);
+        ADIPC_LAUNCH_CHECK();
+    }
+    int h_status[2] = {0, 0};
+    ADIPC_CUDA(cudaMemcpyAsync(h_status, c.build_status.p, sizeof(h_status), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    c.shifts_applied = h_status[1];
+    if (h_status[0]) {
+        c.pkind = kNone;
+        throw StatusError(kIndefinite, "subdomain matrix stayed indefinite after regularization");
+    }
+    c.pkind = kMas;
+}
+
+
+void build_preconditioner(Ctx& c, PrecondKind kind) {
+    cudaStream_t st = c.stream;
+    const DeviceMatrix& A = c.A;
+    if (kind == kJacobi) {
+        c.jinv.reserve(9 * static_cast<std::size_t>(A.n));
+        if (A.n > 0) {
+            k_jacobi_build<<<grid_for(A.n, 256, 16), 256, 0, st>>>(A.n, A.cols.p, A.blocks.p, A.row_ptr.p, c.jinv.p);
+            ADIPC_LAUNCH_CHECK();
+        }
+        c.pkind = kJacobi;
+        return;
+    }
+    if (!c.have_l0) throw StatusError(kInvalidArgument, "level-0 partition not set (adipc_gpu_set_level0_partition)");
+    if (static_cast<std::int32_t>(c.l0.part_of.size()) != A.n)
+        throw StatusError(kInvalidArgument, "level-0 partition size differs from n_block_rows");
+    const auto t0 = std::chrono::steady_clock::now();
+    // block_edges(A) (mas.hpp:19-25): off-diagonal (row, col) pairs, in order
+    const bool reuse = c.cache_hierarchy && c.hier_version == A.version && !c.levels.empty();
+    if (!reuse) {
+        std::vector<std::uint32_t> rows(A.U), cols(A.U);
+        if (A.U) {
+            ADIPC_CUDA(cudaMemcpyAsync(rows.data(), A.rows.p, 4 * A.U, cudaMemcpyDeviceToHost, st));
+            ADIPC_CUDA(cudaMemcpyAsync(cols.data(), A.cols.p, 4 * A.U, cudaMemcpyDeviceToHost, st));
+            ADIPC_CUDA(cudaStreamSynchronize(st));
+        }
+        std::vector<std::int32_t> pairs;
+        pairs.reserve(2 * A.U);
+        for (std::int64_t i = 0; i < A.U; ++i)
+            if (rows[i] != cols[i]) {
+                pairs.push_back(static_cast<std::int32_t>(rows[i]));
+                pairs.push_back(static_cast<std::int32_t>(cols[i]));
+            }
+        c.hier = host::build_hierarchy(c.l0, pairs.data(), pairs.size() / 2, c.max_levels);
+        if (c.hier.n_levels() > kMaxCoarse + 1) throw StatusError(kInvalidArgument, "too many MAS levels");
+        c.levels.clear();
+        for (int l = 0; l < c.hier.n_levels(); ++l) {
+            c.levels.emplace_back(new DeviceLevel());
+            build_level(c, *c.levels.back(), c.hier.levels[l], l, A.n);
+        }
+        c.hier_version = A.version;
+    } else {
+        for (auto& L : c.levels)
+            ADIPC_CUDA(cudaMemsetAsync(L->inv.p, 0, sizeof(double) * std::max<std::int64_t>(L->inv_doubles, 1), st));
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    c.ms_build_host = std::chrono::duration<float, std::milli>(t1 - t0).count();
+    factorize(c);
+}
+
+void build_mas_from_hierarchy(Ctx& c, const host::MasHierarchy& h) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (h.n_levels() > kMaxCoarse + 1) throw StatusError(kInvalidArgument, "too many MAS levels");
+    c.hier = h;
+    c.levels.clear();
+    for (int l = 0; l < c.hier.n_levels(); ++l) {
+        c.levels.emplace_back(new DeviceLevel());
+        build_level(c, *c.levels.back(), c.hier.levels[l], l, c.A.n);
+    }
+    c.hier_version = ~0ull;  // explicit hierarchies are never reused by the cache
+    c.ms_build_host = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    factorize(c);
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers shared with pcg.cu
+int l0_grid(const Ctx& c) { return grid_for(c.levels[0]->n_parts, 8, 8); }
+int coarse_grid(const Ctx& c) {
+    std::int64_t tot = 0;
+    for (std::size_t l = 1; l < c.levels.size(); ++l) tot += c.levels[l]->n_parts;
+    return grid_for(std::max<std::int64_t>(tot, 1), 8, 8);
+}
+int slot_grid(const Ctx& c) { return grid_for(3 * static_cast<std::int64_t>(c.A.n), 256, 8); }
+int jacobi_grid(const Ctx& c) { return grid_for(c.A.n, 256, 8); }
+
+// lanes hold dims j = lane + 32 t, t < regs; fills above 32 use the CTA kernels
+static int dim_regs(int max_fill) { return max_fill <= 10 ? 1 : (max_fill <= 21 ? 2 : (max_fill <= 32 ? 3 : 0)); }
+
+template <int kMode>
+void launch_l0(Ctx& c, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
+               double* dot_out) {
+    const DeviceLevel& L = *c.levels[0];
+    const int regs = dim_regs(L.max_fill);
+    const int grid = l0_grid(c);
+    if (regs == 0) {
+        const std::size_t smem = sizeof(double) * 3 * L.max_fill;
+        ADIPC_CUDA(cudaFuncSetAttribute(k_mas_l0_big<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+        k_mas_l0_big<kMode><<<grid_for(L.n_parts, 1, 8), 128, smem, c.stream>>>(
+            L.n_parts, L.sub_ptr.p, L.sub_nodes.p, L.inv_off.p, L.inv.p, r_in, z, a, partials, ticket, dot_out);
+        ADIPC_LAUNCH_CHECK();
+        return;
+    }
+#define ADIPC_L0(R)                                                                                              \
+    k_mas_l0<kMode, R><<<grid, 256, 0, c.stream>>>(L.n_parts, L.sub_ptr.p, L.sub_nodes.p, L.inv_off.p, L.inv.p, \
+                                                   r_in, z, a, partials, ticket, dot_out)
+    if (regs == 1)
+        ADIPC_L0(1);
+    else if (regs == 2)
+        ADIPC_L0(2);
+    else
+        ADIPC_L0(3);
+#undef ADIPC_L0
+    ADIPC_LAUNCH_CHECK();
+}
+template void launch_l0<M_APPLY>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+template void launch_l0<M_INIT>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+template void launch_l0<M_UPDATE>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+template void launch_l0<M_RESTART>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+
+void launch_coarse(Ctx& c, const double* r, const int* flags, double* partials, unsigned* ticket, double* dot_out) {
+    const int nl = static_cast<int>(c.levels.size()) - 1;
+    if (nl <= 0) {
+        if (dot_out) ADIPC_CUDA(cudaMemsetAsync(dot_out, 0, sizeof(double), c.stream));
+        return;
+    }
+    CoarseArgs ca{};
+    ca.n_levels = nl;
+    ca.part_begin[0] = 0;
+    int max_fill = 0;
+    for (int l = 0; l < nl; ++l) {
+        DeviceLevel& L = *c.levels[l + 1];
+        ca.lv[l] = CoarseLevelArgs{L.n_parts, L.sub_ptr.p, L.sub_nodes.p, L.node_ptr.p, L.node_slots.p,
+                                   L.inv_off.p, L.inv.p, L.y.p};
+        ca.part_begin[l + 1] = ca.part_begin[l] + L.n_parts;
+        max_fill = std::max(max_fill, L.max_fill);
+    }
+    const int regs = dim_regs(max_fill);
+    const int grid = coarse_grid(c);
+    if (regs == 0) {
+        const std::size_t smem = sizeof(double) * 3 * max_fill;
+        ADIPC_CUDA(cudaFuncSetAttribute(k_mas_coarse_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+        k_mas_coarse_big<<<grid_for(ca.part_begin[nl], 1, 8), 128, smem, c.stream>>>(ca, r, flags, partials, ticket,
+                                                                                     dot_out);
+    } else if (regs == 1)
+        k_mas_coarse<1><<<grid, 256, 0, c.stream>>>(ca, r, flags, partials, ticket, dot_out);
+    else if (regs == 2)
+        k_mas_coarse<2><<<grid, 256, 0, c.stream>>>(ca, r, flags, partials, ticket, dot_out);
+    else
+        k_mas_coarse<3><<<grid, 256, 0, c.stream>>>(ca, r, flags, partials, ticket, dot_out);
+    ADIPC_LAUNCH_CHECK();
+}
+
+ProlongArgs prolong_args(const Ctx& c) {
+    ProlongArgs pa{};
+    pa.n_levels = c.pkind == kMas ? static_cast<int>(c.levels.size()) - 1 : 0;
+    for (int l = 0; l < pa.n_levels; ++l) {
+        pa.agg[l] = c.levels[l + 1]->agg.p;
+        pa.y[l] = c.levels[l + 1]->y.p;
+    }
+    return pa;
+}
+
+template <int kFinal>
+void launch_final(Ctx& c, double* z, double* p, const PcgArgs& a) {
+    k_mas_final<kFinal><<<slot_grid(c), 256, 0, c.stream>>>(c.A.n, prolong_args(c), z, p, a);
+    ADIPC_LAUNCH_CHECK();
+}
+template void launch_final<F_APPLY>(Ctx&, double*, double*, const PcgArgs&);
+template void launch_final<F_PCG_INIT>(Ctx&, double*, double*, const PcgArgs&);
+template void launch_final<F_PCG_STEP>(Ctx&, double*, double*, const PcgArgs&);
+
+template <int kMode>
+void launch_jacobi(Ctx& c, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
+                   double* dot_out) {
+    k_jacobi<kMode><<<jacobi_grid(c), 256, 0, c.stream>>>(c.A.n, c.jinv.p, r_in, z, a, partials, ticket, dot_out);
+    ADIPC_LAUNCH_CHECK();
+}
+template void launch_jacobi<M_APPLY>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+template void launch_jacobi<M_INIT>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+template void launch_jacobi<M_UPDATE>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+template void launch_jacobi<M_RESTART>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+
+// z = M r (MasPreconditioner::apply / BlockJacobiPreconditioner::apply).
+void precond_apply(Ctx& c, const double* d_r, double* d_z) {
+    PcgArgs a{};
+    if (c.A.n == 0) return;
+    if (c.pkind == kJacobi) {
+        launch_jacobi<M_APPLY>(c, d_r, d_z, a, nullptr, nullptr, nullptr);
+    } else if (c.pkind == kMas) {
+        launch_l0<M_APPLY>(c, d_r, d_z, a, nullptr, nullptr, nullptr);
+        launch_coarse(c, d_r, nullptr, nullptr, nullptr, nullptr);
+        launch_final<F_APPLY>(c, d_z, nullptr, a);
+    } else {
+        throw StatusError(kInvalidArgument, "no preconditioner built");
+    }
+}
+
+}  // namespace adipc_gpu

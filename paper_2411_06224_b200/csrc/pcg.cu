@@ -1,0 +1,241 @@
+// Fused PCG (replaces pcg_solve, solver/pcg.hpp:34-88) over the device
+// matrix and preconditioner of a context. One iteration is four launches,
+// each of which is also a grid-wide dependency point of the algorithm:
+//   1. SRBK SpMV  Ap = A p  with p.Ap fused (last CTA finishes the dot)
+//   2. level-0 MAS (or Jacobi): alpha = rho / p.Ap, x += alpha p,
+//      r -= alpha Ap, z0 = D0^-1 r per subdomain, partial r.z0
+//   3. all coarse MAS levels in one launch (restriction from r, dense solve,
+//      partial r.z_l)
+//   4. prolongation z = z0 + sum_l P_l y_l, rho' = r.z, convergence test,
+//      p = z + (rho'/rho) p, and Ap cleared for the next SpMV.
+// Scalars (alpha, beta, dots, stop test) never leave the device; the host
+// polls the done flag once per chunk of iterations. Every kernel returns
+// immediately once the done flag is set, so over-issued iterations are
+// near-free. Termination semantics follow pcg.hpp exactly: x0 = 0, zero rhs
+// -> 0 iterations, !(rho0 > 0) -> not converged, !(pAp > 0) -> iters = k-1,
+// residual recomputed as b - A x every `restart` iterations, stop when
+// r.z <= tol^2 r0.z0.
+#include <algorithm>
+#include <cmath>
+
+#include "mas_kernels.cuh"
+
+namespace adipc_gpu {
+
+void spmv_launch(Ctx& c, const double* d_x, double* d_y, bool zero_y, const int* flags, double* partials,
+                 unsigned* ticket, double* dot_out);
+int spmv_grid(const Ctx& c);
+int l0_grid(const Ctx& c);
+int coarse_grid(const Ctx& c);
+int slot_grid(const Ctx& c);
+int jacobi_grid(const Ctx& c);
+template <int kMode>
+void launch_l0(Ctx& c, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
+               double* dot_out);
+void launch_coarse(Ctx& c, const double* r, const int* flags, double* partials, unsigned* ticket, double* dot_out);
+template <int kFinal>
+void launch_final(Ctx& c, double* z, double* p, const PcgArgs& a);
+template <int kMode>
+void launch_jacobi(Ctx& c, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
+                   double* dot_out);
+
+namespace {
+
+__global__ void k_dot_self(const double* __restrict__ v, std::int64_t n, double* partials, unsigned* ticket,
+                           double* out) {
+    double s = 0;
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        s += v[i] * v[i];
+    grid_sum_last_block(s, partials, ticket, out);
+}
+
+// x += alpha p ahead of a restart SpMV (pcg.hpp:67-71)
+__global__ void k_x_update(std::int64_t n3, PcgArgs a) {
+    if (a.flags[F_DONE]) return;
+    double alpha;
+    if (!pcg_alpha(a, alpha)) return;
+    for (std::int64_t g = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; g < n3;
+         g += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        a.x[g] += alpha * a.p[g];
+}
+
+// clear Ap for the next SpMV, fused into nothing else yet (pcg step 4 does it
+// when it runs; this covers init and restart bookkeeping)
+__global__ void k_zero(double* __restrict__ v, std::int64_t n, const int* __restrict__ flags) {
+    if (flags && flags[F_DONE]) return;
+    for (std::int64_t g = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; g < n;
+         g += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        v[g] = 0;
+}
+
+}  // namespace
+
+PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters, double* d_x) {
+    PcgOut out;
+    cudaStream_t st = c.stream;
+    const std::int32_t n = c.A.n;
+    const std::int64_t n3 = 3 * static_cast<std::int64_t>(n);
+    if (c.pkind == kNone) throw StatusError(kInvalidArgument, "no preconditioner built");
+    PcgWork& w = c.w;
+    w.r.reserve(n3);
+    w.p.reserve(n3);
+    w.ap.reserve(n3);
+    w.z.reserve(n3);
+    w.tmp.reserve(n3);
+    int pmax = std::max({spmv_grid(c), slot_grid(c), kSMs * 8});
+    if (c.pkind == kMas) pmax = std::max({pmax, l0_grid(c), coarse_grid(c)});
+    else pmax = std::max(pmax, jacobi_grid(c));
+    w.partials.reserve(static_cast<std::size_t>(pmax) * T_COUNT);
+    w.tickets.reserve(T_COUNT);
+    w.scal.reserve(S_COUNT);
+    w.flags.reserve(F_COUNT);
+    double* part = w.partials.p;
+    auto partials_of = [&](int t) { return part + static_cast<std::size_t>(t) * pmax; };
+    ADIPC_CUDA(cudaMemsetAsync(w.tickets.p, 0, sizeof(unsigned) * T_COUNT, st));
+    ADIPC_CUDA(cudaMemsetAsync(w.flags.p, 0, sizeof(int) * F_COUNT, st));
+    double h_scal[S_COUNT] = {0};
+    h_scal[S_STOP] = rel_tol * rel_tol;
+    ADIPC_CUDA(cudaMemcpyAsync(w.scal.p, h_scal, sizeof(h_scal), cudaMemcpyHostToDevice, st));
+
+    cudaEvent_t e0, e1;
+    ADIPC_CUDA(cudaEventCreate(&e0));
+    ADIPC_CUDA(cudaEventCreate(&e1));
+    ADIPC_CUDA(cudaEventRecord(e0, st));
+
+    // zero right hand side -> converged in 0 iterations, x = 0 (pcg.hpp:38-42)
+    k_dot_self<<<grid_for(n3, 256, 8), 256, 0, st>>>(d_b, n3, partials_of(T_BB), w.tickets.p + T_BB, w.scal.p + S_BB);
+    ADIPC_LAUNCH_CHECK();
+    double bb = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&bb, w.scal.p + S_BB, sizeof(double), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    if (bb == 0) {
+        ADIPC_CUDA(cudaMemsetAsync(d_x, 0, sizeof(double) * n3, st));
+        ADIPC_CUDA(cudaStreamSynchronize(st));
+        out.converged = 1;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        c.ms_pcg = 0;
+        c.last_iters = 0;
+        return out;
+    }
+
+    PcgArgs a{};
+    a.x = d_x;
+    a.r = w.r.p;
+    a.p = w.p.p;
+    a.ap = w.ap.p;
+    a.b = d_b;
+    a.scal = w.scal.p;
+    a.flags = w.flags.p;
+    a.k = 0;
+    const bool mas = c.pkind == kMas;
+    // r = b, z = M r, p = z, rho0 = r.z (pcg.hpp:51-57)
+    if (mas) {
+        launch_l0<M_INIT>(c, nullptr, w.z.p, a, partials_of(T_L0), w.tickets.p + T_L0, w.scal.p + S_RZ_L0);
+        launch_coarse(c, w.r.p, w.flags.p, partials_of(T_C), w.tickets.p + T_C, w.scal.p + S_RZ_C);
+    } else {
+        launch_jacobi<M_INIT>(c, nullptr, w.z.p, a, partials_of(T_L0), w.tickets.p + T_L0, w.scal.p + S_RZ_L0);
+        ADIPC_CUDA(cudaMemsetAsync(w.scal.p + S_RZ_C, 0, sizeof(double), st));
+    }
+    launch_final<F_PCG_INIT>(c, w.z.p, w.p.p, a);
+    k_zero<<<slot_grid(c), 256, 0, st>>>(w.ap.p, n3, w.flags.p);
+    ADIPC_LAUNCH_CHECK();
+
+    int h_flags[F_COUNT] = {0};
+    const int chunk = 16;
+    // optional per-kernel-class timing (ADIPC_OPT_PROFILE): events bracket the
+    // SpMV, level-0, coarse and prolongation/update launches of every
+    // iteration on the solve stream; summed after each chunk's sync.
+    const bool prof = c.profile;
+    if (prof) {
+        if (c.prof_events.empty()) {
+            c.prof_events.resize(static_cast<std::size_t>(chunk) * 5);
+            for (auto& e : c.prof_events) ADIPC_CUDA(cudaEventCreate(&e));
+        }
+        for (int q = 0; q < 4; ++q) c.prof_ms[q] = 0;
+        c.prof_iters = 0;
+    }
+    auto mark = [&](int it_in_chunk, int q) {
+        if (prof) ADIPC_CUDA(cudaEventRecord(c.prof_events[5 * it_in_chunk + q], st));
+    };
+    for (int k = 1; k <= max_iters;) {
+        const int kend = std::min(max_iters, k + chunk - 1);
+        const int kbeg = k;
+        for (; k <= kend; ++k) {
+            a.k = k;
+            mark(k - kbeg, 0);
+            // 1. Ap = A p, p.Ap
+            spmv_launch(c, w.p.p, w.ap.p, false, w.flags.p, partials_of(T_SPMV), w.tickets.p + T_SPMV,
+                        w.scal.p + S_PAP);
+            mark(k - kbeg, 1);
+            const bool is_restart = restart > 0 && k % restart == 0;
+            if (is_restart) {  // x += alpha p; r = b - A x
+                k_x_update<<<slot_grid(c), 256, 0, st>>>(n3, a);
+                ADIPC_LAUNCH_CHECK();
+                k_zero<<<slot_grid(c), 256, 0, st>>>(w.tmp.p, n3, w.flags.p);
+                ADIPC_LAUNCH_CHECK();
+                spmv_launch(c, d_x, w.tmp.p, false, w.flags.p, nullptr, nullptr, nullptr);
+                PcgArgs ar = a;
+                ar.ap = w.tmp.p;
+                if (mas)
+                    launch_l0<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_L0), w.tickets.p + T_L0,
+                                         w.scal.p + S_RZ_L0);
+                else
+                    launch_jacobi<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_L0), w.tickets.p + T_L0,
+                                             w.scal.p + S_RZ_L0);
+            } else {
+                if (mas)
+                    launch_l0<M_UPDATE>(c, nullptr, w.z.p, a, partials_of(T_L0), w.tickets.p + T_L0,
+                                        w.scal.p + S_RZ_L0);
+                else
+                    launch_jacobi<M_UPDATE>(c, nullptr, w.z.p, a, partials_of(T_L0), w.tickets.p + T_L0,
+                                            w.scal.p + S_RZ_L0);
+            }
+            mark(k - kbeg, 2);
+            if (mas) launch_coarse(c, w.r.p, w.flags.p, partials_of(T_C), w.tickets.p + T_C, w.scal.p + S_RZ_C);
+            mark(k - kbeg, 3);
+            launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, a);
+            k_zero<<<slot_grid(c), 256, 0, st>>>(w.ap.p, n3, w.flags.p);
+            ADIPC_LAUNCH_CHECK();
+            mark(k - kbeg, 4);
+        }
+        ADIPC_CUDA(cudaMemcpyAsync(h_flags, w.flags.p, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
+        ADIPC_CUDA(cudaStreamSynchronize(st));
+        if (prof) {
+            // iterations of this chunk that did work (the rest returned early)
+            const int done_at = h_flags[F_DONE] ? h_flags[F_ITERS] : kend;
+            for (int kk = kbeg; kk <= std::min(kend, std::max(done_at, kbeg)); ++kk) {
+                for (int q = 0; q < 4; ++q) {
+                    float ms = 0;
+                    ADIPC_CUDA(cudaEventElapsedTime(&ms, c.prof_events[5 * (kk - kbeg) + q],
+                                                    c.prof_events[5 * (kk - kbeg) + q + 1]));
+                    c.prof_ms[q] += ms;
+                }
+                ++c.prof_iters;
+            }
+        }
+        if (h_flags[F_DONE]) break;
+    }
+    ADIPC_CUDA(cudaEventRecord(e1, st));
+    ADIPC_CUDA(cudaMemcpyAsync(h_flags, w.flags.p, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaMemcpyAsync(h_scal, w.scal.p, sizeof(h_scal), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    ADIPC_CUDA(cudaEventElapsedTime(&c.ms_pcg, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (h_flags[F_DONE]) {
+        out.iters = h_flags[F_ITERS];
+        out.converged = h_flags[F_CONVERGED];
+        out.rel_residual = h_scal[S_REL];
+    } else {  // ran out of iterations (pcg.hpp:86-87)
+        out.iters = max_iters;
+        out.converged = 0;
+        const double rho = h_scal[S_RHO0 + (max_iters & 1)];
+        out.rel_residual = std::sqrt(std::fabs(rho) / h_scal[S_RHO_INIT]);
+    }
+    c.last_iters = out.iters;
+    return out;
+}
+
+}  // namespace adipc_gpu

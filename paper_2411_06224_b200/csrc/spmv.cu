@@ -1,0 +1,113 @@
+// Symmetric reduce-by-key block SpMV (SRBK, paper Alg. 4; reference
+// sparse/srbk_spmv.hpp:13-49): y = A x with A stored as its sorted upper block
+// triangle. Each warp owns 32 consecutive blocks (the reference's lane group
+// of width 32): lane e computes H_e x[col] and, off the diagonal, H_e^T x[row]
+// (scattered with fp64 RED atomics to y[col]); the row contributions are
+// summed with a head-segmented shuffle reduction over the warp's sorted rows
+// and the run heads add them to y[row] atomically.
+//
+// Optional fusion for PCG: the same pass accumulates p.(A p) directly from the
+// blocks, p_r.(H p_c) * (r != c ? 2 : 1), so the dot needs no second sweep
+// over Ap; the grid total is finished by the last CTA (deterministic order).
+#include "context.hpp"
+
+namespace adipc_gpu {
+
+namespace {
+
+constexpr int kSpmvThreads = 256;
+
+template <bool kDot>
+__global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __restrict__ rows,
+                                                     const std::uint32_t* __restrict__ cols,
+                                                     const double* __restrict__ blocks, std::int64_t U,
+                                                     const double* __restrict__ x, double* __restrict__ y,
+                                                     double* __restrict__ partials, unsigned* __restrict__ ticket,
+                                                     double* __restrict__ dot_out, const int* __restrict__ flags) {
+    if (flags && flags[0]) return;  // PCG already finished (F_DONE)
+    const int lane = threadIdx.x & 31;
+    const std::int64_t warp0 = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    double dsum = 0;
+    for (std::int64_t wbase = warp0 * 32; wbase < U; wbase += nwarps * 32) {
+        const std::int64_t e = wbase + lane;
+        const bool valid = e < U;
+        std::uint32_t r = 0xFFFFFFFFu, c = 0;
+        double h[9];
+        double yr0 = 0, yr1 = 0, yr2 = 0;
+        if (valid) {
+            r = __ldg(rows + e);
+            c = __ldg(cols + e);
+            const double* hb = blocks + 9 * e;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) h[k] = __ldg(hb + k);
+            const double xc0 = __ldg(x + 3 * c), xc1 = __ldg(x + 3 * c + 1), xc2 = __ldg(x + 3 * c + 2);
+            // column-major H(i,j) = h[3j+i]
+            yr0 = h[0] * xc0 + h[3] * xc1 + h[6] * xc2;
+            yr1 = h[1] * xc0 + h[4] * xc1 + h[7] * xc2;
+            yr2 = h[2] * xc0 + h[5] * xc1 + h[8] * xc2;
+            const double xr0 = __ldg(x + 3 * r), xr1 = __ldg(x + 3 * r + 1), xr2 = __ldg(x + 3 * r + 2);
+            if (r != c) {
+                const double yc0 = h[0] * xr0 + h[1] * xr1 + h[2] * xr2;
+                const double yc1 = h[3] * xr0 + h[4] * xr1 + h[5] * xr2;
+                const double yc2 = h[6] * xr0 + h[7] * xr1 + h[8] * xr2;
+                atomicAdd(y + 3 * c, yc0);
+                atomicAdd(y + 3 * c + 1, yc1);
+                atomicAdd(y + 3 * c + 2, yc2);
+            }
+            if (kDot) dsum += (r != c ? 2.0 : 1.0) * (xr0 * yr0 + xr1 * yr1 + xr2 * yr2);
+        }
+        // head-segmented sum of the row contributions (rows sorted within the warp)
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double a0 = __shfl_down_sync(0xffffffffu, yr0, off);
+            const double a1 = __shfl_down_sync(0xffffffffu, yr1, off);
+            const double a2 = __shfl_down_sync(0xffffffffu, yr2, off);
+            const std::uint32_t ro = __shfl_down_sync(0xffffffffu, r, off);
+            if (lane + off < 32 && ro == r) {
+                yr0 += a0;
+                yr1 += a1;
+                yr2 += a2;
+            }
+        }
+        const std::uint32_t rprev = __shfl_up_sync(0xffffffffu, r, 1);
+        if (valid && (lane == 0 || rprev != r)) {
+            atomicAdd(y + 3 * r, yr0);
+            atomicAdd(y + 3 * r + 1, yr1);
+            atomicAdd(y + 3 * r + 2, yr2);
+        }
+    }
+    if (kDot) grid_sum_last_block(dsum, partials, ticket, dot_out);
+}
+
+}  // namespace
+
+int spmv_grid(const Ctx& c) { return grid_for(ceil_div(c.A.U, 32), kSpmvThreads / 32, 8); }
+
+// y (+)= A x. zero_y: clear y first (otherwise the caller guarantees y == 0).
+// With `dot_out`: x.(A x) -> *dot_out (device), using `partials`
+// (>= spmv_grid doubles) and `ticket` (one zeroed unsigned). `flags`: skip
+// when the PCG solve is done.
+void spmv_launch(Ctx& c, const double* d_x, double* d_y, bool zero_y, const int* flags, double* partials,
+                 unsigned* ticket, double* dot_out) {
+    const std::int64_t nx3 = 3 * static_cast<std::int64_t>(c.A.n);
+    if (zero_y) ADIPC_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * nx3, c.stream));
+    if (c.A.U == 0) {
+        if (dot_out) ADIPC_CUDA(cudaMemsetAsync(dot_out, 0, sizeof(double), c.stream));
+        return;
+    }
+    const int grid = spmv_grid(c);
+    if (dot_out)
+        k_spmv<true><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
+                                                          partials, ticket, dot_out, flags);
+    else
+        k_spmv<false><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
+                                                           nullptr, nullptr, nullptr, flags);
+    ADIPC_LAUNCH_CHECK();
+}
+
+void spmv(Ctx& c, const double* d_x, double* d_y, double*, int) {
+    spmv_launch(c, d_x, d_y, true, nullptr, nullptr, nullptr, nullptr);
+}
+
+}  // namespace adipc_gpu

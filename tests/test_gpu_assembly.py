@@ -1,0 +1,184 @@
+"""GPU parity of the assembly path through the C-ABI against the oracle:
+sort_stream, fast_hash_reduction (bit-exact with the reference's
+deterministic mode), fast_segment_reduction, filter_pinned and
+two_level_abd_reduce — the reference's kernel-oracle suites (seed 90210,
+tools/verify_suites.hpp:140-343), its unit fixtures, edge cases (empty,
+single, long rows crossing the warp / CTA sort limits) and the configs."""
+import numpy as np
+import pytest
+
+import oracle_py as O
+import paper_2411_06224_b200 as P
+from paper_2411_06224_b200 import scenes
+from paper_2411_06224_b200.context import Context, InvalidArgument
+from helpers import Stream, cm, dense_from, map_accumulate
+from kernel_cases import abd_cases, hash_cases, segment_cases
+
+pytestmark = pytest.mark.gpu
+DET = O.ExecPolicy(deterministic=True)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def oracle_assemble(keys, vals, n):
+    sk, sv = O.sort_stream(keys, vals, DET)
+    return O.fast_hash_reduction(sk, sv, n, DET)
+
+
+def gpu_assemble(ctx, keys, vals, n):
+    U = ctx.assemble(keys, vals, n)
+    nn, rows, cols, blocks = ctx.copy_matrix()
+    assert nn == n and len(rows) == U
+    return rows, cols, blocks
+
+
+def assert_bitwise(got, want):
+    for g, w in zip(got, want):
+        assert g.shape == w.shape
+        assert np.array_equal(g.view(np.uint8) if g.dtype == np.float64 else g,
+                              w.view(np.uint8) if w.dtype == np.float64 else w)
+
+
+def test_emission_fixture(ctx):  # test_block_sparse.cpp:72-91
+    B1 = np.array([[1, 2, 3], [4, 5, 6], [7, 8, 9]], float)
+    s = Stream()
+    s.emit(2, 1, B1)
+    s.emit(1, 2, 2 * np.eye(3))
+    s.emit(1, 1, np.array([[0, 1, 0], [1, 0, 2], [0, 2, 0]], float))
+    k, v = ctx.sort_stream(*s.arrays())
+    ok, ov = O.sort_stream(*s.arrays())
+    assert np.array_equal(k, ok) and np.array_equal(v, ov)
+    rows, cols, blocks = gpu_assemble(ctx, *s.arrays(), 3)
+    assert list(rows) == [1, 1] and list(cols) == [1, 2]
+    assert np.array_equal(blocks[1], cm(B1.T) + cm(2 * np.eye(3)))
+
+
+def test_sort_stream_random(ctx):  # :93-101 + stability
+    rng = O.Rng(7)
+    keys, vals = O.random_stream(rng, 40, 5000)
+    k, v = ctx.sort_stream(keys, vals)
+    ok, ov = O.sort_stream(keys, vals)
+    assert np.array_equal(k, ok) and np.array_equal(v, ov)
+
+
+def test_hash_reduction_suite_bitwise(ctx):  # verify_suites.hpp:192-215, 1000 cases
+    rng = O.Rng(90210)
+    for _ in segment_cases(rng):  # advance the shared RNG like the suite does
+        pass
+    fails = 0
+    for n_blocks, keys, vals in hash_cases(rng):
+        got = gpu_assemble(ctx, keys, vals, n_blocks)
+        want = oracle_assemble(keys, vals, n_blocks)
+        oracle = map_accumulate(keys, vals)
+        assert len(got[2]) == len(oracle)
+        for r, c, b in zip(*got):
+            if not np.array_equal(b, oracle[(int(r) << 32) | int(c)]):
+                fails += 1
+        assert_bitwise(got, want)
+    assert fails == 0
+
+
+def test_segment_reduction_suite_bitwise(ctx):  # verify_suites.hpp:161-191
+    rng = O.Rng(90210)
+    for Oseg, V, n_seg in segment_cases(rng):
+        want = np.zeros(n_seg)
+        for i in range(len(V)):
+            want[Oseg[i]] += V[i]
+        got = ctx.segment_reduce(Oseg, V, n_seg)
+        assert np.array_equal(got, want)
+    assert list(ctx.segment_reduce([0, 0, 0, 1, 1, 1, 2, 2], np.ones(8), 3)) == [3.0, 3.0, 2.0]
+    assert list(ctx.segment_reduce([0] * 12, np.ones(12), 1)) == [12.0]
+    # Vec3 / Mat3 widths
+    rng = np.random.default_rng(0)
+    Oseg = np.sort(rng.integers(0, 50, 700)).astype(np.int32)
+    for w in (3, 9):
+        V = rng.standard_normal((700, w))
+        assert np.array_equal(ctx.segment_reduce(Oseg, V, 50), O.fast_segment_reduction(Oseg, V, 50, DET))
+    with pytest.raises(InvalidArgument):
+        P.fast_segment_reduction([0, 0, 1], np.ones(2), 2)
+
+
+def test_edge_cases(ctx):
+    assert ctx.assemble(np.zeros(0, np.uint64), np.zeros((0, 9)), 5) == 0
+    assert ctx.matrix_info() == (5, 0)
+    keys = np.array([O.make_block_key(3, 4)], np.uint64)
+    vals = np.arange(9, dtype=float).reshape(1, 9)
+    assert_bitwise(gpu_assemble(ctx, keys, vals, 5), oracle_assemble(keys, vals, 5))
+    with pytest.raises(InvalidArgument):  # row >= n_block_rows
+        ctx.assemble(keys, vals, 3)
+
+
+@pytest.mark.parametrize("row_len", [255, 256, 257, 1000, 8191, 8192, 8193, 40000])
+def test_long_rows(ctx, row_len):
+    """Rows longer than the warp sort (256) and the CTA sort (8192) limits:
+    contact rows of affine bodies collect very many tiles; many duplicates."""
+    rng = np.random.default_rng(row_len)
+    cols = rng.integers(3, 3 + max(2, row_len // 7), row_len)
+    keys = ((np.uint64(3) << np.uint64(32)) | cols.astype(np.uint64)).astype(np.uint64)
+    extra = rng.integers(0, 50, 500)
+    keys = np.concatenate([keys, ((extra.astype(np.uint64) << np.uint64(32)) | (extra + 1).astype(np.uint64))])
+    perm = rng.permutation(len(keys))
+    keys = keys[perm]
+    vals = rng.standard_normal((len(keys), 9))
+    n = int(max(cols.max(), 51)) + 1
+    assert_bitwise(gpu_assemble(ctx, keys, vals, n), oracle_assemble(keys, vals, n))
+
+
+@pytest.mark.parametrize("name", ["cfg1_soft_cube", "stiff_beam", "cfg2_cloth"])
+def test_config_assembly_bitwise(ctx, name):
+    sc = scenes.CONFIGS[name]()
+    fk, fv = ctx.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    ok, ov = O.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    assert np.array_equal(fk, ok) and np.array_equal(fv, ov)
+    assert_bitwise(gpu_assemble(ctx, fk, fv, sc.n_blocks), oracle_assemble(ok, ov, sc.n_blocks))
+
+
+def test_two_level_suite(ctx):  # verify_suites.hpp:254-343, tiles bitwise + sandwich 1e-10
+    rng = O.Rng(90210)
+    for _ in segment_cases(rng):
+        pass
+    for _ in hash_cases(rng):
+        pass
+    from kernel_cases import spmv_cases
+    for _ in spmv_cases(rng):
+        pass
+    worst = 0.0
+    for case in abd_cases(rng):
+        args = (case["keys"], case["vals"], case["n_fem"], case["n_bodies"], case["body"], case["jac36"])
+        tk, tv = ctx.two_level_abd_reduce(*args)
+        ok, ov = O.two_level_abd_reduce(*args, DET)
+        assert np.array_equal(tk, ok) and np.array_equal(tv, ov)
+        rows, cols, blocks = gpu_assemble(ctx, tk, tv, case["n_blocks"])
+        D = dense_from(case["n_blocks"], rows, cols, blocks)
+        worst = max(worst, np.linalg.norm(D - case["naive"]) / np.linalg.norm(case["naive"]))
+    assert worst <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["cfg3_abd_stack", "cfg4_hybrid"])
+def test_contact_configs_bitwise(ctx, name):
+    """Two-level contact reduction + global assembly of the contact configs,
+    bit-exact with the oracle's deterministic mode."""
+    sc = scenes.CONFIGS[name]()
+    args = (sc.node_keys, sc.node_vals, sc.n_fem, sc.n_bodies, sc.abd_body, sc.jac36)
+    tk, tv = ctx.two_level_abd_reduce(*args)
+    ok, ov = O.two_level_abd_reduce(*args, DET)
+    assert np.array_equal(tk, ok) and np.array_equal(tv, ov)
+    keys = np.concatenate([sc.keys, tk])
+    vals = np.concatenate([sc.vals, tv])
+    assert_bitwise(gpu_assemble(ctx, keys, vals, sc.n_blocks), oracle_assemble(keys, vals, sc.n_blocks))
+
+
+def test_api_mirror(ctx):
+    """api.py mirrors the reference signatures (block_coo.hpp / reduction.hpp)."""
+    rng = O.Rng(11)
+    keys, vals = O.random_stream(rng, 12, 400)
+    s = P.BlockTripletStream(keys, vals)
+    P.sort_stream(s, P.ExecPolicy(deterministic=True))
+    A = P.fast_hash_reduction(s, 12, P.ExecPolicy(deterministic=True))
+    want = oracle_assemble(keys, vals, 12)
+    assert_bitwise((A.rows, A.cols, A.blocks), want)

@@ -1,0 +1,281 @@
+"""GPU parity of SpMV, MAS / block-Jacobi build + apply and PCG through the
+C-ABI against the oracle and the reference's own test assertions
+(test_block_sparse.cpp:196-237, test_precond.cpp:179-293,
+test_solver.cpp:79-130, verify_suites.hpp:217-252), plus the north-star
+parity contract on the configs: PCG iteration counts within +-2 %, solution
+within 1e-5 relative L2 of the oracle."""
+import numpy as np
+import pytest
+
+import oracle_py as O
+import paper_2411_06224_b200 as P
+from paper_2411_06224_b200 import scenes
+from paper_2411_06224_b200.context import Context, IndefiniteSubdomain
+from helpers import chain_spd_system, cm, dense_from, make_spd_system, restriction_matrix
+from kernel_cases import hash_cases, segment_cases, spmv_cases
+
+pytestmark = pytest.mark.gpu
+DET = O.ExecPolicy(deterministic=True)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def test_spmv_two_row_fixture(ctx):  # test_block_sparse.cpp:196-211
+    ctx.set_matrix(2, np.array([0, 0, 1], np.uint32), np.array([0, 1, 1], np.uint32),
+                   np.array([cm(2 * np.eye(3)), cm(np.eye(3)), cm(2 * np.eye(3))]))
+    assert np.array_equal(ctx.spmv(np.ones(6)), np.full(6, 3.0))
+
+
+def test_spmv_suite(ctx):  # verify_suites.hpp:217-252: dense oracle 1e-12
+    rng = O.Rng(90210)
+    for _ in segment_cases(rng):
+        pass
+    for _ in hash_cases(rng):
+        pass
+    worst = 0.0
+    for n_blocks, rows, cols, blocks, x in spmv_cases(rng):
+        want = dense_from(n_blocks, rows, cols, blocks) @ x
+        ctx.set_matrix(n_blocks, rows, cols, blocks)
+        y = ctx.spmv(x)
+        worst = max(worst, np.max(np.linalg.norm((y - want).reshape(-1, 3), axis=1)) / max(1.0, np.linalg.norm(want)))
+    assert worst <= 1e-12
+
+
+def _filtered_matrix(sc):
+    fk, fv = O.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    sk, sv = O.sort_stream(fk, fv, DET)
+    return O.fast_hash_reduction(sk, sv, sc.n_blocks, DET)
+
+
+@pytest.mark.parametrize("name", ["cfg1_soft_cube", "stiff_beam"])
+def test_spmv_configs(ctx, name):
+    sc = scenes.CONFIGS[name]()
+    rows, cols, blocks = _filtered_matrix(sc)
+    ctx.set_matrix(sc.n_blocks, rows, cols, blocks)
+    x = np.random.default_rng(1).standard_normal(3 * sc.n_blocks)
+    want = O.srbk_spmv(sc.n_blocks, rows, cols, blocks, x, DET)
+    got = ctx.spmv(x)
+    assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+
+
+# ---------------------------------------------------------------- MAS ----
+def _random_edges(rng, v, count):
+    pick = O.UniformInt(0, v - 1)
+    edges = []
+    for _ in range(count):
+        a, b = pick(rng), pick(rng)
+        if a == b:
+            continue
+        edges.append((min(a, b), max(a, b)))
+    return sorted(set(edges))
+
+
+def test_level_inverses_and_apply():  # test_precond.cpp:179-226
+    rng = O.Rng(71)
+    v = 30
+    edges = _random_edges(rng, v, 70)
+    rows, cols, blocks = make_spd_system(v, edges, rng)
+    Ad = dense_from(v, rows, cols, blocks)
+    A = P.SortedSymBlockCoo(v, rows, cols, blocks)
+    be = P.block_edges(A)
+    h = P.build_hierarchy(P.partition_block_graph(v, be, 8), be, 4)
+    M = P.MasPreconditioner()
+    M.build(A, h)
+    for l in range(h.n_levels()):
+        for s in range(h.levels[l]["n_parts"]):
+            R = restriction_matrix(h.levels, v, l, s)
+            D = R @ Ad @ R.T
+            Dinv = M.level_inverse(l, s)
+            assert np.linalg.norm(Dinv @ D - np.eye(len(D))) <= 1e-10
+    u = O.UniformReal(-1, 1)
+    r = u.fill(rng, 3 * v)
+    z = M.apply(r)
+    expect = np.zeros(3 * v)
+    for l in range(h.n_levels()):
+        for s in range(h.levels[l]["n_parts"]):
+            R = restriction_matrix(h.levels, v, l, s)
+            expect += R.T @ np.linalg.solve(R @ Ad @ R.T, R @ r)
+    assert np.linalg.norm(z - expect) <= 1e-10 * np.linalg.norm(expect)
+    # and against the oracle's own MasPreconditioner
+    ho = O.Hierarchy(h.levels[0]["part_of"], h.levels[0]["n_parts"], 8, be, 4)
+    Mo = O.MasPreconditioner(O.Matrix(v, rows, cols, blocks), ho)
+    assert np.linalg.norm(z - Mo.apply(r)) <= 1e-10 * np.linalg.norm(z)
+
+
+def test_apply_symmetric_positive():  # :228-253
+    rng = O.Rng(81)
+    rows, cols, blocks = make_spd_system(20, [(i, i + 1) for i in range(19)], rng)
+    A = P.SortedSymBlockCoo(20, rows, cols, blocks)
+    be = P.block_edges(A)
+    M = P.MasPreconditioner()
+    M.build(A, P.build_hierarchy(P.partition_block_graph(20, be, 6), be, 4))
+    u = O.UniformReal(-1, 1)
+    for _ in range(20):
+        r1 = np.empty(60)
+        r2 = np.empty(60)
+        for i in range(60):
+            r1[i] = u(rng)
+            r2[i] = u(rng)
+        z1, z2 = M.apply(r1), M.apply(r2)
+        assert abs(r2 @ z1 - r1 @ z2) <= 1e-10 * (abs(r1 @ z1) + abs(r2 @ z2))
+        assert r1 @ z1 > 0
+
+
+def test_single_covering_subdomain_exact():  # :255-274
+    rng = O.Rng(91)
+    rows, cols, blocks = make_spd_system(10, [(i, i + 1) for i in range(9)], rng)
+    A = P.SortedSymBlockCoo(10, rows, cols, blocks)
+    be = P.block_edges(A)
+    h = P.build_hierarchy(P.partition_block_graph(10, be, 16), be, 4)
+    assert h.n_levels() == 1 and h.levels[0]["n_parts"] == 1
+    M = P.MasPreconditioner()
+    M.build(A, h)
+    Ad = dense_from(10, rows, cols, blocks)
+    x = O.UniformReal(-1, 1).fill(rng, 30)
+    assert np.linalg.norm(M.apply(Ad @ x) - x) <= 1e-10 * np.linalg.norm(x)
+
+
+def test_block_jacobi_exact():  # :276-293
+    rng = O.Rng(101)
+    rows, cols, blocks = make_spd_system(4, [(0, 1), (1, 2), (0, 3)], rng)
+    A = P.SortedSymBlockCoo(4, rows, cols, blocks)
+    M = P.BlockJacobiPreconditioner()
+    M.build(A)
+    Ad = dense_from(4, rows, cols, blocks)
+    r = O.UniformReal(-1, 1).fill(rng, 12)
+    z = M.apply(r)
+    for i in range(4):
+        e = np.linalg.solve(Ad[3 * i:3 * i + 3, 3 * i:3 * i + 3], r[3 * i:3 * i + 3])
+        assert np.linalg.norm(z[3 * i:3 * i + 3] - e) <= 1e-12 * np.linalg.norm(e)
+
+
+def test_regularisation_retry_semantics():  # mas.hpp:66-81
+    A = P.SortedSymBlockCoo(1, [0], [0], [cm(np.diag([-1.0, 1.0, 1.0]))])
+    h = P.build_hierarchy(P.chunk_partition(1, 4), np.zeros((0, 2), np.int32), 4)
+    M = P.MasPreconditioner()
+    with pytest.raises(IndefiniteSubdomain, match="indefinite"):
+        M.build(A, h)
+    A = P.SortedSymBlockCoo(1, [0], [0], [cm(np.diag([0.0, 1.0, 1.0]))])
+    M = P.MasPreconditioner()
+    M.build(A, h)
+    assert M.ctx.shifts() == 1
+
+
+# ---------------------------------------------------------------- PCG ----
+@pytest.fixture(scope="module")
+def chain():  # test_solver.cpp:79-88
+    rng = O.Rng(11)
+    v = 20
+    rows, cols, blocks = chain_spd_system(v, rng)
+    Ad = dense_from(v, rows, cols, blocks)
+    b = O.UniformReal(-1, 1).fill(rng, 3 * v)
+    return P.SortedSymBlockCoo(v, rows, cols, blocks), Ad, b
+
+
+def test_pcg_block_jacobi(chain):
+    A, Ad, b = chain
+    M = P.BlockJacobiPreconditioner()
+    M.build(A)
+    x, r = P.pcg_solve(A, b, M, 1e-8, 250, 10000)
+    assert r.converged and np.linalg.norm(Ad @ x - b) <= 1e-6 * np.linalg.norm(b)
+    xo, ro = O.pcg_solve(O.Matrix(A.n_block_rows, A.rows, A.cols, A.blocks), b,
+                         O.BlockJacobiPreconditioner(O.Matrix(A.n_block_rows, A.rows, A.cols, A.blocks)),
+                         1e-8, 250, 10000)
+    assert abs(r.iters - ro["iters"]) <= max(1, 0.02 * ro["iters"])
+
+
+def test_pcg_exact_mas_one_iteration(chain):
+    A, Ad, b = chain
+    be = P.block_edges(A)
+    h = P.build_hierarchy(P.partition_block_graph(A.n_block_rows, be, 64), be, 4)
+    assert h.levels[0]["n_parts"] == 1
+    M = P.MasPreconditioner()
+    M.build(A, h)
+    x, r = P.pcg_solve(A, b, M, 1e-4, 250, 10000)
+    assert r.converged and r.iters == 1
+    assert np.linalg.norm(Ad @ x - b) <= 1e-8 * np.linalg.norm(b)
+
+
+def test_pcg_restart_path(chain):
+    A, Ad, b = chain
+    M = P.BlockJacobiPreconditioner()
+    M.build(A)
+    x, r = P.pcg_solve(A, b, M, 1e-8, 1, 10000)
+    assert r.converged and np.linalg.norm(Ad @ x - b) <= 1e-6 * np.linalg.norm(b)
+
+
+def test_pcg_zero_rhs(chain):
+    A, Ad, b = chain
+    M = P.BlockJacobiPreconditioner()
+    M.build(A)
+    x, r = P.pcg_solve(A, np.zeros(len(b)), M, 1e-4, 250, 100)
+    assert r.converged and r.iters == 0 and np.linalg.norm(x) == 0
+
+
+def test_pcg_max_iters_exhausted(chain):
+    A, Ad, b = chain
+    M = P.BlockJacobiPreconditioner()
+    M.build(A)
+    x, r = P.pcg_solve(A, b, M, 1e-14, 250, 3)
+    Mo = O.BlockJacobiPreconditioner(O.Matrix(A.n_block_rows, A.rows, A.cols, A.blocks))
+    xo, ro = O.pcg_solve(O.Matrix(A.n_block_rows, A.rows, A.cols, A.blocks), b, Mo, 1e-14, 250, 3)
+    assert not r.converged and r.iters == 3 == ro["iters"]
+    assert abs(r.rel_residual - ro["rel_residual"]) <= 1e-8 * ro["rel_residual"]
+    assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+
+
+def _solve_config(ctx, sc, kind, tol=1e-4, restart=250):
+    fk, fv = ctx.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    ctx.assemble(fk, fv, sc.n_blocks)
+    l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, 16)
+    ctx.set_level0_partition(l0.part_of, l0.n_parts, 16, 4)
+    ctx.build_preconditioner(kind)
+    n, rows, cols, blocks = ctx.copy_matrix()
+    xs = np.random.default_rng(5).standard_normal(3 * n)
+    b = O.srbk_spmv(n, rows, cols, blocks, xs, DET)
+    x, r = ctx.pcg(b, tol, restart, 100000)
+    return (rows, cols, blocks, l0, b), x, r
+
+
+@pytest.mark.parametrize("name", ["cfg1_soft_cube", "stiff_beam"])
+@pytest.mark.parametrize("kind", [1, 2])
+def test_pcg_config_parity(ctx, name, kind):
+    """North-star parity: iteration counts +-2 %, solutions 1e-5 rel L2."""
+    sc = scenes.CONFIGS[name]()
+    (rows, cols, blocks, l0, b), x, r = _solve_config(ctx, sc, kind)
+    Am = O.Matrix(sc.n_blocks, rows, cols, blocks)
+    if kind == 1:
+        be = O.block_edges(rows, cols)
+        M = O.MasPreconditioner(Am, O.Hierarchy(l0.part_of, l0.n_parts, 16, be, 4))
+    else:
+        M = O.BlockJacobiPreconditioner(Am)
+    xo, ro = O.pcg_solve(Am, b, M, 1e-4, 250, 100000)
+    assert r.converged == ro["converged"]
+    assert abs(r.iters - ro["iters"]) <= max(1, 0.02 * ro["iters"]), (r.iters, ro["iters"])
+    assert np.linalg.norm(x - xo) <= 1e-5 * np.linalg.norm(xo)
+
+
+def test_stiff_beam_preconditioner_quality(ctx):
+    """Acceptance #6 analogue on the beam's first Newton matrix: cemas16
+    needs <= 0.6x the block-Jacobi iterations (acceptance.cpp:121-164)."""
+    sc = scenes.CONFIGS["stiff_beam"]()
+    _, _, rm = _solve_config(ctx, sc, 1)
+    _, _, rj = _solve_config(ctx, sc, 2)
+    assert rm.converged and rj.converged
+    assert rm.iters / rj.iters <= 0.6, (rm.iters, rj.iters)
+
+
+def test_hierarchy_in_context_matches_oracle(ctx):
+    sc = scenes.CONFIGS["stiff_beam"]()
+    (rows, cols, blocks, l0, b), x, r = _solve_config(ctx, sc, 1)
+    levels = ctx.precond_levels()
+    ho = O.Hierarchy(l0.part_of, l0.n_parts, 16, O.block_edges(rows, cols), 4)
+    assert len(levels) == ho.n_levels()
+    for a, o in zip(levels, ho.levels):
+        assert a["n_nodes"] == o["n_nodes"] and a["n_parts"] == o["n_parts"]
+        assert np.array_equal(a["part_of"], o["part_of"]) and np.array_equal(a["agg"], o["agg"])

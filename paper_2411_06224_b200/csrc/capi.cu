@@ -111,8 +111,10 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
         L->pos_of.free();
         L->sub_ptr.free();
         L->sub_nodes.free();
-        L->node_ptr.free();
-        L->node_slots.free();
+        L->up_first.free();
+        L->upc_ptr.free();
+        L->upc_pos.free();
+        L->rr.free();
         L->inv_off.free();
         L->inv.free();
         L->y.free();

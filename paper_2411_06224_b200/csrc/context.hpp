@@ -44,8 +44,11 @@ struct DeviceLevel {
     DBuf<std::int32_t> pos_of;     // node -> position inside its subdomain
     DBuf<std::int32_t> sub_ptr;    // subdomain -> first member node (CSR over sub_nodes)
     DBuf<std::int32_t> sub_nodes;  // members of each subdomain, ascending node id (= pos order)
-    DBuf<std::int32_t> node_ptr;   // node -> first member slot (CSR over node_slots); levels >= 1
-    DBuf<std::int32_t> node_slots; // member slots of each node, ascending
+    DBuf<std::int32_t> up_first;   // subdomain -> first next-level node nested in it
+    DBuf<std::int32_t> upc_ptr;    // next-level node -> range of its children (CSR)
+    DBuf<std::int32_t> upc_pos;    // children as positions inside this level's subdomain
+    DBuf<double> rr;               // level >= 1: restricted residual per node (3 per node)
+    std::vector<std::int32_t> pos_host;
     DBuf<std::int64_t> inv_off;    // subdomain -> offset of its dense (3f)^2 inverse
     DBuf<double> inv;              // explicit dense inverses, column-major (symmetric)
     DBuf<double> y;                // level >= 1: per-node solution (3 per node)

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <limits>
 
 #include "mas_kernels.cuh"
 
@@ -33,7 +34,7 @@ struct RestrictLevel {
 };
 struct RestrictArgs {
     int n_levels;
-    RestrictLevel lv[kMaxCoarse + 1];
+    RestrictLevel lv[kMaxLevels];
 };
 
 __device__ __forceinline__ void add_tile(double* D, int dim, int pr, int pc, const double* h, bool transpose,
@@ -235,17 +236,41 @@ void build_level(Ctx& c, DeviceLevel& L, const host::Level& hl, int level, std::
     upload(L.inv_off, inv_off, st);
     if (level > 0) {
         upload(L.agg, hl.agg, st);
-        std::vector<std::int32_t> node_ptr(hl.n_nodes + 1, 0), node_slots(n_slots);
-        for (std::int32_t s = 0; s < n_slots; ++s) ++node_ptr[hl.agg[s] + 1];
-        for (std::int32_t v = 0; v < hl.n_nodes; ++v) node_ptr[v + 1] += node_ptr[v];
-        std::vector<std::int32_t> fill(node_ptr.begin(), node_ptr.end() - 1);
-        for (std::int32_t s = 0; s < n_slots; ++s) node_slots[fill[hl.agg[s]]++] = s;  // ascending slots
-        upload(L.node_ptr, node_ptr, st);
-        upload(L.node_slots, node_slots, st);
         L.y.reserve(3 * static_cast<std::size_t>(hl.n_nodes));
+        L.rr.reserve(3 * static_cast<std::size_t>(hl.n_nodes));
     }
+    L.pos_host = std::move(pos_of);
     L.inv.reserve(static_cast<std::size_t>(L.inv_doubles));
     ADIPC_CUDA(cudaMemsetAsync(L.inv.p, 0, sizeof(double) * std::max<std::int64_t>(L.inv_doubles, 1), st));
+}
+
+// Restriction metadata from level l to l+1 (see mas_kernels.cuh): the
+// level-(l+1) nodes inside each level-l subdomain are consecutive ids; their
+// children are given as positions inside that subdomain.
+void link_levels(Ctx& c, const host::MasHierarchy& h) {
+    cudaStream_t st = c.stream;
+    for (int l = 0; l + 1 < h.n_levels(); ++l) {
+        const host::Level& cur = h.levels[l];
+        const host::Level& nxt = h.levels[l + 1];
+        DeviceLevel& L = *c.levels[l];
+        std::vector<std::int32_t> up(cur.n_nodes, -1);
+        for (std::int32_t slot = 0; slot < h.n_slots; ++slot) up[l == 0 ? slot : cur.agg[slot]] = nxt.agg[slot];
+        std::vector<std::int32_t> first(cur.n_parts + 1, std::numeric_limits<std::int32_t>::max());
+        std::vector<std::int32_t> cnt(nxt.n_nodes + 1, 0);
+        for (std::int32_t v = 0; v < cur.n_nodes; ++v) {
+            first[cur.part_of[v]] = std::min(first[cur.part_of[v]], up[v]);
+            ++cnt[up[v] + 1];
+        }
+        first[cur.n_parts] = nxt.n_nodes;
+        for (std::int32_t s = cur.n_parts - 1; s >= 0; --s)
+            if (first[s] == std::numeric_limits<std::int32_t>::max()) first[s] = first[s + 1];  // empty subdomain
+        for (std::int32_t v = 0; v < nxt.n_nodes; ++v) cnt[v + 1] += cnt[v];
+        std::vector<std::int32_t> pos(cur.n_nodes), fill(cnt.begin(), cnt.end() - 1);
+        for (std::int32_t v = 0; v < cur.n_nodes; ++v) pos[fill[up[v]]++] = L.pos_host[v];  // children ascending
+        upload(L.up_first, first, st);
+        upload(L.upc_ptr, cnt, st);
+        upload(L.upc_pos, pos, st);
+    }
 }
 
 }  // namespace
@@ -326,12 +351,13 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
                 pairs.push_back(static_cast<std::int32_t>(cols[i]));
             }
         c.hier = host::build_hierarchy(c.l0, pairs.data(), pairs.size() / 2, c.max_levels);
-        if (c.hier.n_levels() > kMaxCoarse + 1) throw StatusError(kInvalidArgument, "too many MAS levels");
+        if (c.hier.n_levels() > kMaxLevels) throw StatusError(kInvalidArgument, "too many MAS levels");
         c.levels.clear();
         for (int l = 0; l < c.hier.n_levels(); ++l) {
             c.levels.emplace_back(new DeviceLevel());
             build_level(c, *c.levels.back(), c.hier.levels[l], l, A.n);
         }
+        link_levels(c, c.hier);
         c.hier_version = A.version;
     } else {
         for (auto& L : c.levels)
@@ -344,13 +370,14 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
 
 void build_mas_from_hierarchy(Ctx& c, const host::MasHierarchy& h) {
     const auto t0 = std::chrono::steady_clock::now();
-    if (h.n_levels() > kMaxCoarse + 1) throw StatusError(kInvalidArgument, "too many MAS levels");
+    if (h.n_levels() > kMaxLevels) throw StatusError(kInvalidArgument, "too many MAS levels");
     c.hier = h;
     c.levels.clear();
     for (int l = 0; l < c.hier.n_levels(); ++l) {
         c.levels.emplace_back(new DeviceLevel());
         build_level(c, *c.levels.back(), c.hier.levels[l], l, c.A.n);
     }
+    link_levels(c, c.hier);
     c.hier_version = ~0ull;  // explicit hierarchies are never reused by the cache
     c.ms_build_host = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
     factorize(c);
@@ -358,87 +385,67 @@ void build_mas_from_hierarchy(Ctx& c, const host::MasHierarchy& h) {
 
 // ---------------------------------------------------------------------------
 // launch helpers shared with pcg.cu
-int l0_grid(const Ctx& c) { return grid_for(c.levels[0]->n_parts, 8, 8); }
-int coarse_grid(const Ctx& c) {
-    std::int64_t tot = 0;
-    for (std::size_t l = 1; l < c.levels.size(); ++l) tot += c.levels[l]->n_parts;
-    return grid_for(std::max<std::int64_t>(tot, 1), 8, 8);
+int level_grid(const Ctx& c, int l) {
+    const DeviceLevel& L = *c.levels[l];
+    return L.max_fill > 32 ? grid_for(L.n_parts, 1, 8) : grid_for(L.n_parts, 8, 8);
 }
 int slot_grid(const Ctx& c) { return grid_for(3 * static_cast<std::int64_t>(c.A.n), 256, 8); }
 int jacobi_grid(const Ctx& c) { return grid_for(c.A.n, 256, 8); }
 
-// lanes hold dims j = lane + 32 t, t < regs; fills above 32 use the CTA kernels
+// lanes hold dims j = lane + 32 t, t < regs; fills above 32 use the CTA kernel
 static int dim_regs(int max_fill) { return max_fill <= 10 ? 1 : (max_fill <= 21 ? 2 : (max_fill <= 32 ? 3 : 0)); }
 
+LevelArgs level_args(Ctx& c, int l, const double* r_in, double* out) {
+    DeviceLevel& L = *c.levels[l];
+    const bool top = l + 1 >= static_cast<int>(c.levels.size());
+    LevelArgs la{};
+    la.n_parts = L.n_parts;
+    la.sub_ptr = L.sub_ptr.p;
+    la.sub_nodes = L.sub_nodes.p;
+    la.inv_off = L.inv_off.p;
+    la.inv = L.inv.p;
+    la.r_in = l == 0 ? r_in : L.rr.p;
+    la.out = l == 0 ? out : L.y.p;
+    la.up_first = top ? nullptr : L.up_first.p;
+    la.upc_ptr = top ? nullptr : L.upc_ptr.p;
+    la.upc_pos = top ? nullptr : L.upc_pos.p;
+    la.r_next = top ? nullptr : c.levels[l + 1]->rr.p;
+    return la;
+}
+
+// Level-l MAS solve (+ restriction to level l+1). Level 0 uses `kMode`
+// (apply / PCG gather modes); coarser levels read their restricted residual.
 template <int kMode>
-void launch_l0(Ctx& c, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
-               double* dot_out) {
-    const DeviceLevel& L = *c.levels[0];
+void launch_level(Ctx& c, int l, const double* r_in, double* z, const PcgArgs& a, double* partials,
+                  unsigned* ticket, double* dot_out) {
+    const LevelArgs la = level_args(c, l, r_in, z);
+    const DeviceLevel& L = *c.levels[l];
     const int regs = dim_regs(L.max_fill);
-    const int grid = l0_grid(c);
+    const int grid = level_grid(c, l);
     if (regs == 0) {
         const std::size_t smem = sizeof(double) * 3 * L.max_fill;
-        ADIPC_CUDA(cudaFuncSetAttribute(k_mas_l0_big<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        ADIPC_CUDA(cudaFuncSetAttribute(k_mas_level_big<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-        k_mas_l0_big<kMode><<<grid_for(L.n_parts, 1, 8), 128, smem, c.stream>>>(
-            L.n_parts, L.sub_ptr.p, L.sub_nodes.p, L.inv_off.p, L.inv.p, r_in, z, a, partials, ticket, dot_out);
-        ADIPC_LAUNCH_CHECK();
-        return;
+        k_mas_level_big<kMode><<<grid, 128, smem, c.stream>>>(la, a, partials, ticket, dot_out);
+    } else if (regs == 1) {
+        k_mas_level<kMode, 1><<<grid, 256, 0, c.stream>>>(la, a, partials, ticket, dot_out);
+    } else if (regs == 2) {
+        k_mas_level<kMode, 2><<<grid, 256, 0, c.stream>>>(la, a, partials, ticket, dot_out);
+    } else {
+        k_mas_level<kMode, 3><<<grid, 256, 0, c.stream>>>(la, a, partials, ticket, dot_out);
     }
-#define ADIPC_L0(R)                                                                                              \
-    k_mas_l0<kMode, R><<<grid, 256, 0, c.stream>>>(L.n_parts, L.sub_ptr.p, L.sub_nodes.p, L.inv_off.p, L.inv.p, \
-                                                   r_in, z, a, partials, ticket, dot_out)
-    if (regs == 1)
-        ADIPC_L0(1);
-    else if (regs == 2)
-        ADIPC_L0(2);
-    else
-        ADIPC_L0(3);
-#undef ADIPC_L0
     ADIPC_LAUNCH_CHECK();
 }
-template void launch_l0<M_APPLY>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
-template void launch_l0<M_INIT>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
-template void launch_l0<M_UPDATE>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
-template void launch_l0<M_RESTART>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
-
-void launch_coarse(Ctx& c, const double* r, const int* flags, double* partials, unsigned* ticket, double* dot_out) {
-    const int nl = static_cast<int>(c.levels.size()) - 1;
-    if (nl <= 0) {
-        if (dot_out) ADIPC_CUDA(cudaMemsetAsync(dot_out, 0, sizeof(double), c.stream));
-        return;
-    }
-    CoarseArgs ca{};
-    ca.n_levels = nl;
-    ca.part_begin[0] = 0;
-    int max_fill = 0;
-    for (int l = 0; l < nl; ++l) {
-        DeviceLevel& L = *c.levels[l + 1];
-        ca.lv[l] = CoarseLevelArgs{L.n_parts, L.sub_ptr.p, L.sub_nodes.p, L.node_ptr.p, L.node_slots.p,
-                                   L.inv_off.p, L.inv.p, L.y.p};
-        ca.part_begin[l + 1] = ca.part_begin[l] + L.n_parts;
-        max_fill = std::max(max_fill, L.max_fill);
-    }
-    const int regs = dim_regs(max_fill);
-    const int grid = coarse_grid(c);
-    if (regs == 0) {
-        const std::size_t smem = sizeof(double) * 3 * max_fill;
-        ADIPC_CUDA(cudaFuncSetAttribute(k_mas_coarse_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-        k_mas_coarse_big<<<grid_for(ca.part_begin[nl], 1, 8), 128, smem, c.stream>>>(ca, r, flags, partials, ticket,
-                                                                                     dot_out);
-    } else if (regs == 1)
-        k_mas_coarse<1><<<grid, 256, 0, c.stream>>>(ca, r, flags, partials, ticket, dot_out);
-    else if (regs == 2)
-        k_mas_coarse<2><<<grid, 256, 0, c.stream>>>(ca, r, flags, partials, ticket, dot_out);
-    else
-        k_mas_coarse<3><<<grid, 256, 0, c.stream>>>(ca, r, flags, partials, ticket, dot_out);
-    ADIPC_LAUNCH_CHECK();
-}
+template void launch_level<M_APPLY>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+template void launch_level<M_INIT>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+template void launch_level<M_UPDATE>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+template void launch_level<M_RESTART>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+template void launch_level<M_COARSE>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
 
 ProlongArgs prolong_args(const Ctx& c) {
     ProlongArgs pa{};
     pa.n_levels = c.pkind == kMas ? static_cast<int>(c.levels.size()) - 1 : 0;
+    pa.n_rz = c.pkind == kMas ? static_cast<int>(c.levels.size()) : 1;
     for (int l = 0; l < pa.n_levels; ++l) {
         pa.agg[l] = c.levels[l + 1]->agg.p;
         pa.y[l] = c.levels[l + 1]->y.p;
@@ -447,13 +454,13 @@ ProlongArgs prolong_args(const Ctx& c) {
 }
 
 template <int kFinal>
-void launch_final(Ctx& c, double* z, double* p, const PcgArgs& a) {
-    k_mas_final<kFinal><<<slot_grid(c), 256, 0, c.stream>>>(c.A.n, prolong_args(c), z, p, a);
+void launch_final(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a) {
+    k_mas_final<kFinal><<<slot_grid(c), 256, 0, c.stream>>>(c.A.n, prolong_args(c), z, p, ap, a);
     ADIPC_LAUNCH_CHECK();
 }
-template void launch_final<F_APPLY>(Ctx&, double*, double*, const PcgArgs&);
-template void launch_final<F_PCG_INIT>(Ctx&, double*, double*, const PcgArgs&);
-template void launch_final<F_PCG_STEP>(Ctx&, double*, double*, const PcgArgs&);
+template void launch_final<F_APPLY>(Ctx&, double*, double*, double*, const PcgArgs&);
+template void launch_final<F_PCG_INIT>(Ctx&, double*, double*, double*, const PcgArgs&);
+template void launch_final<F_PCG_STEP>(Ctx&, double*, double*, double*, const PcgArgs&);
 
 template <int kMode>
 void launch_jacobi(Ctx& c, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
@@ -473,9 +480,10 @@ void precond_apply(Ctx& c, const double* d_r, double* d_z) {
     if (c.pkind == kJacobi) {
         launch_jacobi<M_APPLY>(c, d_r, d_z, a, nullptr, nullptr, nullptr);
     } else if (c.pkind == kMas) {
-        launch_l0<M_APPLY>(c, d_r, d_z, a, nullptr, nullptr, nullptr);
-        launch_coarse(c, d_r, nullptr, nullptr, nullptr, nullptr);
-        launch_final<F_APPLY>(c, d_z, nullptr, a);
+        launch_level<M_APPLY>(c, 0, d_r, d_z, a, nullptr, nullptr, nullptr);
+        for (int l = 1; l < static_cast<int>(c.levels.size()); ++l)
+            launch_level<M_COARSE>(c, l, nullptr, nullptr, a, nullptr, nullptr, nullptr);
+        launch_final<F_APPLY>(c, d_z, nullptr, nullptr, a);
     } else {
         throw StatusError(kInvalidArgument, "no preconditioner built");
     }

@@ -1,11 +1,23 @@
 // MAS / block-Jacobi apply kernels, shared by the stand-alone preconditioner
 // apply (mas.hpp:85-99 / block_jacobi.hpp:16-22) and the fused PCG iteration
 // (pcg.hpp:59-85), which runs them in its "update" modes.
+//
+// MAS apply as a restriction tree. The reference restricts r onto every level
+// directly from the slots (b[pos] += r[slot], mas.hpp:92-93). The hierarchy
+// nests: every level-(l+1) node is a connected piece of ONE level-l
+// subdomain, and the ids of the level-(l+1) nodes of subdomain s are
+// consecutive (hierarchy.hpp:53-72 visits subdomains in order). So the warp
+// that solves level-l subdomain s already holds b_l for all the children of
+// its level-(l+1) nodes and emits r_{l+1} for them — one small parallel launch
+// per level, no long per-lane loops over slots. Summation order is a tree
+// instead of the reference's slot order (rounding-level difference).
 #pragma once
 
 #include "context.hpp"
 
 namespace adipc_gpu {
+
+constexpr int kMaxLevels = 8;
 
 // Device scalars / flags of one PCG solve (PcgWork::scal / flags).
 enum Scal : int {
@@ -13,21 +25,22 @@ enum Scal : int {
     S_RHO_INIT = 2,  // rho_0 (r0 . z0)
     S_STOP = 3,      // tol^2 * rho_0
     S_PAP = 4,       // p . A p of the current iteration
-    S_RZ_L0 = 5,     // level-0 (or Jacobi) share of r . z
-    S_RZ_C = 6,      // coarse-level share of r . z
-    S_REL = 7,       // rel_residual result
-    S_BB = 8,        // b . b
-    S_COUNT = 16
+    S_REL = 5,       // rel_residual result
+    S_BB = 6,        // b . b
+    S_RZ = 8,        // S_RZ + l: level-l share of r . z (Jacobi: level 0)
+    S_COUNT = S_RZ + kMaxLevels
 };
 enum Flag : int { F_DONE = 0, F_ITERS = 1, F_CONVERGED = 2, F_COUNT = 8 };
-enum Ticket : int { T_SPMV = 0, T_L0 = 1, T_C = 2, T_BB = 3, T_COUNT = 8 };
+// last-block tickets / partial arrays: 0 spmv, 1 b.b, 2 + l level l
+enum Ticket : int { T_SPMV = 0, T_BB = 1, T_LEVEL = 2, T_COUNT = T_LEVEL + kMaxLevels };
 
-// Apply modes of the level-0 / Jacobi kernel.
+// Gather modes of the level-0 / Jacobi kernels.
 enum ApplyMode : int {
     M_APPLY = 0,    // b = r (given), z <- y
     M_INIT = 1,     // PCG start: r = b, x = 0, then as APPLY
     M_UPDATE = 2,   // PCG step: x += a p, r -= a Ap, then as APPLY
     M_RESTART = 3,  // PCG restart step: x already updated, r = b - tmp
+    M_COARSE = 4,   // level >= 1: b = r_l[node] (restricted by the level below)
 };
 
 struct PcgArgs {
@@ -39,6 +52,22 @@ struct PcgArgs {
     double* scal;
     int* flags;
     int k;              // iteration index (1-based), 0 in init
+};
+
+// One level of the hierarchy as the apply kernels see it.
+struct LevelArgs {
+    std::int32_t n_parts;
+    const std::int32_t* sub_ptr;    // subdomain -> first member node
+    const std::int32_t* sub_nodes;  // members (level 0: slots), ascending
+    const std::int64_t* inv_off;
+    const double* inv;              // explicit inverses, column-major dim x dim
+    const double* r_in;             // M_COARSE: restricted residual per node (3 per node)
+    double* out;                    // level 0: z per slot; coarse: y per node
+    // restriction to the next level (null at the top level)
+    const std::int32_t* up_first;   // subdomain -> first next-level node inside it
+    const std::int32_t* upc_ptr;    // next-level node -> children range
+    const std::int32_t* upc_pos;    // children as positions inside the subdomain
+    double* r_next;                 // next level's restricted residual (3 per node)
 };
 
 // alpha of iteration k; returns false (and records the termination like
@@ -58,234 +87,130 @@ __device__ __forceinline__ bool pcg_alpha(const PcgArgs& a, double& alpha) {
     return true;
 }
 
-// Level-0 subdomain solve, one warp per subdomain: gather b (fusing the PCG
-// vector update for the slots this subdomain owns — the level-0 partition
-// owns every slot exactly once), y = D^-1 b with the explicit inverse read
-// column by column (coalesced), z[slot] = y, dot partial b.y.
-template <int kMode, int kMaxDimRegs>
-__global__ void __launch_bounds__(256) k_mas_l0(std::int32_t n_parts, const std::int32_t* __restrict__ sub_ptr,
-                                               const std::int32_t* __restrict__ slots,
-                                               const std::int64_t* __restrict__ inv_off,
-                                               const double* __restrict__ inv, const double* __restrict__ r_in,
-                                               double* __restrict__ z, PcgArgs a, double* __restrict__ partials,
-                                               unsigned* __restrict__ ticket, double* __restrict__ dot_out) {
-    const int lane = threadIdx.x & 31;
+// Residual value of dof g under the gather mode (fusing the PCG vector update
+// for the slots the level-0 partition owns — each slot exactly once).
+template <int kMode>
+__device__ __forceinline__ double gather_r(const PcgArgs& a, const double* r_in, std::int64_t g, double alpha) {
+    if (kMode == M_APPLY || kMode == M_COARSE) return r_in[g];
+    if (kMode == M_INIT) {
+        const double rv = a.b[g];
+        a.r[g] = rv;
+        a.x[g] = 0.0;
+        return rv;
+    }
+    if (kMode == M_UPDATE) {
+        a.x[g] += alpha * a.p[g];
+        const double rv = a.r[g] - alpha * a.ap[g];
+        a.r[g] = rv;
+        return rv;
+    }
+    const double rv = a.b[g] - a.ap[g];  // M_RESTART (x updated before the restart SpMV)
+    a.r[g] = rv;
+    return rv;
+}
+
+// One warp per subdomain (dim = 3 f <= 32 kRegs): gather b, y = D^-1 b with
+// the inverse read column by column (coalesced), store y, emit the next
+// level's restricted residual from b (smem), dot partial b.y.
+template <int kMode, int kRegs>
+__global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, double* __restrict__ partials,
+                                                  unsigned* __restrict__ ticket, double* __restrict__ dot_out) {
+    __shared__ double bsm[8][32 * kRegs];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double alpha = 0;
-    if (kMode == M_UPDATE || kMode == M_RESTART) {
-        if (a.flags[F_DONE]) return;
-        if (!pcg_alpha(a, alpha)) return;
+    if (kMode != M_APPLY && kMode != M_INIT) {
+        if (a.flags && a.flags[F_DONE]) return;
+        if ((kMode == M_UPDATE || kMode == M_RESTART) && !pcg_alpha(a, alpha)) return;
     }
     double dsum = 0;
     const int wpb = blockDim.x >> 5;
-    for (std::int32_t s = blockIdx.x * wpb + (threadIdx.x >> 5); s < n_parts; s += gridDim.x * wpb) {
-        const std::int32_t s0 = sub_ptr[s];
-        const int dim = 3 * (sub_ptr[s + 1] - s0);
-        double b[kMaxDimRegs], y[kMaxDimRegs];
-        std::int64_t gi[kMaxDimRegs];
+    for (std::int32_t s = blockIdx.x * wpb + w; s < L.n_parts; s += gridDim.x * wpb) {
+        const std::int32_t s0 = L.sub_ptr[s];
+        const int dim = 3 * (L.sub_ptr[s + 1] - s0);
+        double b[kRegs], y[kRegs];
+        std::int64_t gi[kRegs];
 #pragma unroll
-        for (int t = 0; t < kMaxDimRegs; ++t) {
+        for (int t = 0; t < kRegs; ++t) {
             const int j = lane + 32 * t;
             b[t] = 0;
             y[t] = 0;
             gi[t] = -1;
             if (j < dim) {
-                const std::int32_t slot = slots[s0 + j / 3];
-                const std::int64_t g = 3 * static_cast<std::int64_t>(slot) + (j % 3);
-                gi[t] = g;
-                double rv;
-                if (kMode == M_APPLY) {
-                    rv = r_in[g];
-                } else if (kMode == M_INIT) {
-                    rv = a.b[g];
-                    a.r[g] = rv;
-                    a.x[g] = 0.0;
-                } else if (kMode == M_UPDATE) {
-                    a.x[g] += alpha * a.p[g];
-                    rv = a.r[g] - alpha * a.ap[g];
-                    a.r[g] = rv;
-                } else {  // M_RESTART: x was updated before the restart SpMV
-                    rv = a.b[g] - a.ap[g];
-                    a.r[g] = rv;
-                }
-                b[t] = rv;
+                gi[t] = 3 * static_cast<std::int64_t>(L.sub_nodes[s0 + j / 3]) + (j % 3);
+                b[t] = gather_r<kMode>(a, L.r_in, gi[t], alpha);
             }
         }
-        const double* M = inv + inv_off[s];
+        const double* M = L.inv + L.inv_off[s];
         for (int k = 0; k < dim; ++k) {
             const double bk = __shfl_sync(0xffffffffu, b[k >> 5], k & 31);
             const double* col = M + static_cast<std::int64_t>(k) * dim;
 #pragma unroll
-            for (int t = 0; t < kMaxDimRegs; ++t) {
+            for (int t = 0; t < kRegs; ++t) {
                 const int j = lane + 32 * t;
                 if (j < dim) y[t] += __ldg(col + j) * bk;
             }
         }
 #pragma unroll
-        for (int t = 0; t < kMaxDimRegs; ++t)
+        for (int t = 0; t < kRegs; ++t)
             if (gi[t] >= 0) {
-                z[gi[t]] = y[t];
+                L.out[gi[t]] = y[t];
                 dsum += b[t] * y[t];
             }
+        if (L.r_next) {  // restriction to the nested next-level nodes
+#pragma unroll
+            for (int t = 0; t < kRegs; ++t) bsm[w][lane + 32 * t] = b[t];
+            __syncwarp();
+            const std::int32_t v0 = L.up_first[s];
+            const int nv3 = 3 * (L.up_first[s + 1] - v0);
+            for (int t = lane; t < nv3; t += 32) {
+                const std::int32_t v = v0 + t / 3;
+                const int comp = t % 3;
+                double acc = 0;
+                for (std::int32_t q = L.upc_ptr[v]; q < L.upc_ptr[v + 1]; ++q) acc += bsm[w][3 * L.upc_pos[q] + comp];
+                L.r_next[3 * static_cast<std::int64_t>(v) + comp] = acc;
+            }
+            __syncwarp();
+        }
     }
     if (dot_out) grid_sum_last_block(dsum, partials, ticket, dot_out);
 }
 
-// General-size variant (subdomain capacity > 32, e.g. the exact single-domain
+// General-size variant (fill > 32, e.g. the exact single-domain
 // preconditioner of test_solver.cpp:99-111): one CTA per subdomain, b in
-// shared memory (dim doubles, dynamic), any dim.
+// dynamic shared memory, any dim.
 template <int kMode>
-__global__ void __launch_bounds__(128) k_mas_l0_big(std::int32_t n_parts, const std::int32_t* __restrict__ sub_ptr,
-                                                   const std::int32_t* __restrict__ slots,
-                                                   const std::int64_t* __restrict__ inv_off,
-                                                   const double* __restrict__ inv, const double* __restrict__ r_in,
-                                                   double* __restrict__ z, PcgArgs a, double* __restrict__ partials,
-                                                   unsigned* __restrict__ ticket, double* __restrict__ dot_out) {
+__global__ void __launch_bounds__(128) k_mas_level_big(LevelArgs L, PcgArgs a, double* __restrict__ partials,
+                                                      unsigned* __restrict__ ticket, double* __restrict__ dot_out) {
     extern __shared__ double bs[];
     double alpha = 0;
-    if (kMode == M_UPDATE || kMode == M_RESTART) {
-        if (a.flags[F_DONE]) return;
-        if (!pcg_alpha(a, alpha)) return;
+    if (kMode != M_APPLY && kMode != M_INIT) {
+        if (a.flags && a.flags[F_DONE]) return;
+        if ((kMode == M_UPDATE || kMode == M_RESTART) && !pcg_alpha(a, alpha)) return;
     }
     double dsum = 0;
-    for (std::int32_t s = blockIdx.x; s < n_parts; s += gridDim.x) {
-        const std::int32_t s0 = sub_ptr[s];
-        const int dim = 3 * (sub_ptr[s + 1] - s0);
-        for (int j = threadIdx.x; j < dim; j += blockDim.x) {
-            const std::int64_t g = 3 * static_cast<std::int64_t>(slots[s0 + j / 3]) + (j % 3);
-            double rv;
-            if (kMode == M_APPLY) {
-                rv = r_in[g];
-            } else if (kMode == M_INIT) {
-                rv = a.b[g];
-                a.r[g] = rv;
-                a.x[g] = 0.0;
-            } else if (kMode == M_UPDATE) {
-                a.x[g] += alpha * a.p[g];
-                rv = a.r[g] - alpha * a.ap[g];
-                a.r[g] = rv;
-            } else {
-                rv = a.b[g] - a.ap[g];
-                a.r[g] = rv;
-            }
-            bs[j] = rv;
-        }
+    for (std::int32_t s = blockIdx.x; s < L.n_parts; s += gridDim.x) {
+        const std::int32_t s0 = L.sub_ptr[s];
+        const int dim = 3 * (L.sub_ptr[s + 1] - s0);
+        for (int j = threadIdx.x; j < dim; j += blockDim.x)
+            bs[j] = gather_r<kMode>(a, L.r_in, 3 * static_cast<std::int64_t>(L.sub_nodes[s0 + j / 3]) + (j % 3), alpha);
         __syncthreads();
-        const double* M = inv + inv_off[s];
+        const double* M = L.inv + L.inv_off[s];
         for (int j = threadIdx.x; j < dim; j += blockDim.x) {
             double y = 0;
             for (int k = 0; k < dim; ++k) y += M[static_cast<std::int64_t>(k) * dim + j] * bs[k];
-            z[3 * static_cast<std::int64_t>(slots[s0 + j / 3]) + (j % 3)] = y;
+            L.out[3 * static_cast<std::int64_t>(L.sub_nodes[s0 + j / 3]) + (j % 3)] = y;
             dsum += bs[j] * y;
         }
-        __syncthreads();
-    }
-    if (dot_out) grid_sum_last_block(dsum, partials, ticket, dot_out);
-}
-
-// Coarse levels (>= 1), all levels in one launch: one warp per (level,
-// subdomain). b[pos] = sum of r over the node's member slots in ascending
-// slot order (the reference's accumulation order, mas.hpp:92-93), y = D^-1 b,
-// y stored per node for the prolongation, dot partial b.y.
-struct CoarseLevelArgs {
-    std::int32_t n_parts;
-    const std::int32_t* sub_ptr;
-    const std::int32_t* sub_nodes;
-    const std::int32_t* node_ptr;
-    const std::int32_t* node_slots;
-    const std::int64_t* inv_off;
-    const double* inv;
-    double* y;
-};
-constexpr int kMaxCoarse = 8;
-struct CoarseArgs {
-    int n_levels;
-    std::int32_t part_begin[kMaxCoarse + 1];  // prefix of n_parts over coarse levels
-    CoarseLevelArgs lv[kMaxCoarse];
-};
-
-template <int kMaxDimRegs>
-__global__ void __launch_bounds__(256) k_mas_coarse(CoarseArgs ca, const double* __restrict__ r, const int* __restrict__ flags,
-                                                   double* __restrict__ partials, unsigned* __restrict__ ticket,
-                                                   double* __restrict__ dot_out) {
-    if (flags && flags[F_DONE]) return;
-    const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x >> 5;
-    const std::int32_t total = ca.part_begin[ca.n_levels];
-    double dsum = 0;
-    for (std::int32_t gs = blockIdx.x * wpb + (threadIdx.x >> 5); gs < total; gs += gridDim.x * wpb) {
-        int l = 0;
-        while (gs >= ca.part_begin[l + 1]) ++l;
-        const CoarseLevelArgs& L = ca.lv[l];
-        const std::int32_t s = gs - ca.part_begin[l];
-        const std::int32_t s0 = L.sub_ptr[s];
-        const int dim = 3 * (L.sub_ptr[s + 1] - s0);
-        double b[kMaxDimRegs], y[kMaxDimRegs];
-#pragma unroll
-        for (int t = 0; t < kMaxDimRegs; ++t) {
-            const int j = lane + 32 * t;
-            b[t] = 0;
-            y[t] = 0;
-            if (j < dim) {
-                const std::int32_t node = L.sub_nodes[s0 + j / 3];
-                const int comp = j % 3;
+        if (L.r_next) {
+            const std::int32_t v0 = L.up_first[s];
+            const int nv3 = 3 * (L.up_first[s + 1] - v0);
+            for (int t = threadIdx.x; t < nv3; t += blockDim.x) {
+                const std::int32_t v = v0 + t / 3;
+                const int comp = t % 3;
                 double acc = 0;
-                for (std::int32_t q = L.node_ptr[node]; q < L.node_ptr[node + 1]; ++q)
-                    acc += __ldg(r + 3 * static_cast<std::int64_t>(L.node_slots[q]) + comp);
-                b[t] = acc;
+                for (std::int32_t q = L.upc_ptr[v]; q < L.upc_ptr[v + 1]; ++q) acc += bs[3 * L.upc_pos[q] + comp];
+                L.r_next[3 * static_cast<std::int64_t>(v) + comp] = acc;
             }
-        }
-        const double* M = L.inv + L.inv_off[s];
-        for (int k = 0; k < dim; ++k) {
-            const double bk = __shfl_sync(0xffffffffu, b[k >> 5], k & 31);
-            const double* col = M + static_cast<std::int64_t>(k) * dim;
-#pragma unroll
-            for (int t = 0; t < kMaxDimRegs; ++t) {
-                const int j = lane + 32 * t;
-                if (j < dim) y[t] += __ldg(col + j) * bk;
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < kMaxDimRegs; ++t) {
-            const int j = lane + 32 * t;
-            if (j < dim) {
-                const std::int32_t node = L.sub_nodes[s0 + j / 3];
-                L.y[3 * static_cast<std::int64_t>(node) + (j % 3)] = y[t];
-                dsum += b[t] * y[t];
-            }
-        }
-    }
-    if (dot_out) grid_sum_last_block(dsum, partials, ticket, dot_out);
-}
-
-// General-size coarse variant: one CTA per (level, subdomain), b in smem.
-static __global__ void __launch_bounds__(128) k_mas_coarse_big(CoarseArgs ca, const double* __restrict__ r,
-                                                       const int* __restrict__ flags, double* __restrict__ partials,
-                                                       unsigned* __restrict__ ticket, double* __restrict__ dot_out) {
-    extern __shared__ double bs[];
-    if (flags && flags[F_DONE]) return;
-    const std::int32_t total = ca.part_begin[ca.n_levels];
-    double dsum = 0;
-    for (std::int32_t gs = blockIdx.x; gs < total; gs += gridDim.x) {
-        int l = 0;
-        while (gs >= ca.part_begin[l + 1]) ++l;
-        const CoarseLevelArgs& L = ca.lv[l];
-        const std::int32_t s = gs - ca.part_begin[l];
-        const std::int32_t s0 = L.sub_ptr[s];
-        const int dim = 3 * (L.sub_ptr[s + 1] - s0);
-        for (int j = threadIdx.x; j < dim; j += blockDim.x) {
-            const std::int32_t node = L.sub_nodes[s0 + j / 3];
-            double acc = 0;
-            for (std::int32_t q = L.node_ptr[node]; q < L.node_ptr[node + 1]; ++q)
-                acc += r[3 * static_cast<std::int64_t>(L.node_slots[q]) + (j % 3)];
-            bs[j] = acc;
-        }
-        __syncthreads();
-        const double* M = L.inv + L.inv_off[s];
-        for (int j = threadIdx.x; j < dim; j += blockDim.x) {
-            double y = 0;
-            for (int k = 0; k < dim; ++k) y += M[static_cast<std::int64_t>(k) * dim + j] * bs[k];
-            L.y[3 * static_cast<std::int64_t>(L.sub_nodes[s0 + j / 3]) + (j % 3)] = y;
-            dsum += bs[j] * y;
         }
         __syncthreads();
     }
@@ -294,23 +219,26 @@ static __global__ void __launch_bounds__(128) k_mas_coarse_big(CoarseArgs ca, co
 
 // Prolongation z[slot] = ((y0 + y1[agg1]) + y2[agg2]) + ... (mas.hpp:95-96
 // order), then either stores z (apply) or finishes the PCG step:
-// rho' = r.z; converged -> stop; else p = z + (rho'/rho) p (pcg.hpp:76-84).
+// rho' = r.z; converged -> stop; else p = z + (rho'/rho) p (pcg.hpp:76-84);
+// Ap is cleared for the next SpMV in the same pass.
 struct ProlongArgs {
     int n_levels;  // coarse levels
-    const std::int32_t* agg[kMaxCoarse];
-    const double* y[kMaxCoarse];
+    int n_rz;      // number of r.z shares to add (levels, or 1 for Jacobi)
+    const std::int32_t* agg[kMaxLevels];
+    const double* y[kMaxLevels];
 };
 
 enum FinalMode : int { F_APPLY = 0, F_PCG_INIT = 1, F_PCG_STEP = 2 };
 
 template <int kFinal>
-__global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs pa, double* __restrict__ z, double* __restrict__ p,
-                                                  PcgArgs a) {
+__global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs pa, double* __restrict__ z,
+                                                  double* __restrict__ p, double* __restrict__ ap, PcgArgs a) {
     double beta = 0;
     bool write_p = false;
     if (kFinal != F_APPLY) {
         if (a.flags[F_DONE]) return;
-        const double rz = a.scal[S_RZ_L0] + a.scal[S_RZ_C];
+        double rz = 0;
+        for (int l = 0; l < pa.n_rz; ++l) rz += a.scal[S_RZ + l];
         if (kFinal == F_PCG_INIT) {
             // pcg.hpp:52-57: rho0 = r.z; fail if !(rho0 > 0)
             if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -329,13 +257,12 @@ __global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs p
             const double stop = a.scal[S_STOP];
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 a.flags[F_ITERS] = a.k;
+                a.scal[S_REL] = sqrt(fabs(rz) / a.scal[S_RHO_INIT]);
                 if (rz <= stop) {
                     a.flags[F_DONE] = 1;
                     a.flags[F_CONVERGED] = 1;
-                    a.scal[S_REL] = sqrt(fabs(rz) / a.scal[S_RHO_INIT]);
                 } else {
                     a.scal[S_RHO0 + (a.k & 1)] = rz;
-                    a.scal[S_REL] = sqrt(fabs(rz) / a.scal[S_RHO_INIT]);
                 }
             }
             if (rz <= stop) return;
@@ -354,6 +281,7 @@ __global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs p
             z[g] = zz;
         } else if (write_p) {
             p[g] = (kFinal == F_PCG_INIT) ? zz : zz + beta * p[g];
+            ap[g] = 0.0;
         }
     }
 }
@@ -361,9 +289,10 @@ __global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs p
 // Block Jacobi (block_jacobi.hpp:16-22), one thread per slot, with the same
 // PCG modes as the level-0 MAS kernel. z = inv[i] r_i.
 template <int kMode>
-__global__ void __launch_bounds__(256) k_jacobi(std::int32_t n, const double* __restrict__ jinv, const double* __restrict__ r_in,
-                                               double* __restrict__ z, PcgArgs a, double* __restrict__ partials,
-                                               unsigned* __restrict__ ticket, double* __restrict__ dot_out) {
+__global__ void __launch_bounds__(256) k_jacobi(std::int32_t n, const double* __restrict__ jinv,
+                                               const double* __restrict__ r_in, double* __restrict__ z, PcgArgs a,
+                                               double* __restrict__ partials, unsigned* __restrict__ ticket,
+                                               double* __restrict__ dot_out) {
     double alpha = 0;
     if (kMode == M_UPDATE || kMode == M_RESTART) {
         if (a.flags[F_DONE]) return;
@@ -373,23 +302,7 @@ __global__ void __launch_bounds__(256) k_jacobi(std::int32_t n, const double* __
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         double rv[3];
-        for (int k = 0; k < 3; ++k) {
-            const std::int64_t g = 3 * i + k;
-            if (kMode == M_APPLY) {
-                rv[k] = r_in[g];
-            } else if (kMode == M_INIT) {
-                rv[k] = a.b[g];
-                a.r[g] = rv[k];
-                a.x[g] = 0.0;
-            } else if (kMode == M_UPDATE) {
-                a.x[g] += alpha * a.p[g];
-                rv[k] = a.r[g] - alpha * a.ap[g];
-                a.r[g] = rv[k];
-            } else {
-                rv[k] = a.b[g] - a.ap[g];
-                a.r[g] = rv[k];
-            }
-        }
+        for (int k = 0; k < 3; ++k) rv[k] = gather_r<kMode>(a, r_in, 3 * i + k, alpha);
         const double* M = jinv + 9 * i;
         for (int k = 0; k < 3; ++k) {
             const double zk = M[k] * rv[0] + M[3 + k] * rv[1] + M[6 + k] * rv[2];

@@ -1,13 +1,14 @@
 // Fused PCG (replaces pcg_solve, solver/pcg.hpp:34-88) over the device
-// matrix and preconditioner of a context. One iteration is four launches,
+// matrix and preconditioner of a context. One iteration is 2 + L launches,
 // each of which is also a grid-wide dependency point of the algorithm:
 //   1. SRBK SpMV  Ap = A p  with p.Ap fused (last CTA finishes the dot)
 //   2. level-0 MAS (or Jacobi): alpha = rho / p.Ap, x += alpha p,
-//      r -= alpha Ap, z0 = D0^-1 r per subdomain, partial r.z0
-//   3. all coarse MAS levels in one launch (restriction from r, dense solve,
-//      partial r.z_l)
+//      r -= alpha Ap, z0 = D0^-1 r per subdomain, r restricted to level 1,
+//      partial r.z0
+//   3. levels 1..L-1: dense solve of the restricted residual, restriction to
+//      the next level, partial r.z_l
 //   4. prolongation z = z0 + sum_l P_l y_l, rho' = r.z, convergence test,
-//      p = z + (rho'/rho) p, and Ap cleared for the next SpMV.
+//      p = z + (rho'/rho) p, Ap cleared for the next SpMV.
 // Scalars (alpha, beta, dots, stop test) never leave the device; the host
 // polls the done flag once per chunk of iterations. Every kernel returns
 // immediately once the done flag is set, so over-issued iterations are
@@ -25,16 +26,14 @@ namespace adipc_gpu {
 void spmv_launch(Ctx& c, const double* d_x, double* d_y, bool zero_y, const int* flags, double* partials,
                  unsigned* ticket, double* dot_out);
 int spmv_grid(const Ctx& c);
-int l0_grid(const Ctx& c);
-int coarse_grid(const Ctx& c);
+int level_grid(const Ctx& c, int l);
 int slot_grid(const Ctx& c);
 int jacobi_grid(const Ctx& c);
 template <int kMode>
-void launch_l0(Ctx& c, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
-               double* dot_out);
-void launch_coarse(Ctx& c, const double* r, const int* flags, double* partials, unsigned* ticket, double* dot_out);
+void launch_level(Ctx& c, int l, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
+                  double* dot_out);
 template <int kFinal>
-void launch_final(Ctx& c, double* z, double* p, const PcgArgs& a);
+void launch_final(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a);
 template <int kMode>
 void launch_jacobi(Ctx& c, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
                    double* dot_out);
@@ -60,8 +59,6 @@ __global__ void k_x_update(std::int64_t n3, PcgArgs a) {
         a.x[g] += alpha * a.p[g];
 }
 
-// clear Ap for the next SpMV, fused into nothing else yet (pcg step 4 does it
-// when it runs; this covers init and restart bookkeeping)
 __global__ void k_zero(double* __restrict__ v, std::int64_t n, const int* __restrict__ flags) {
     if (flags && flags[F_DONE]) return;
     for (std::int64_t g = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; g < n;
@@ -77,15 +74,16 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
     const std::int32_t n = c.A.n;
     const std::int64_t n3 = 3 * static_cast<std::int64_t>(n);
     if (c.pkind == kNone) throw StatusError(kInvalidArgument, "no preconditioner built");
+    const bool mas = c.pkind == kMas;
+    const int n_levels = mas ? static_cast<int>(c.levels.size()) : 0;
     PcgWork& w = c.w;
     w.r.reserve(n3);
     w.p.reserve(n3);
     w.ap.reserve(n3);
     w.z.reserve(n3);
     w.tmp.reserve(n3);
-    int pmax = std::max({spmv_grid(c), slot_grid(c), kSMs * 8});
-    if (c.pkind == kMas) pmax = std::max({pmax, l0_grid(c), coarse_grid(c)});
-    else pmax = std::max(pmax, jacobi_grid(c));
+    int pmax = std::max({spmv_grid(c), slot_grid(c), kSMs * 8, jacobi_grid(c)});
+    for (int l = 0; l < n_levels; ++l) pmax = std::max(pmax, level_grid(c, l));
     w.partials.reserve(static_cast<std::size_t>(pmax) * T_COUNT);
     w.tickets.reserve(T_COUNT);
     w.scal.reserve(S_COUNT);
@@ -129,23 +127,24 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
     a.scal = w.scal.p;
     a.flags = w.flags.p;
     a.k = 0;
-    const bool mas = c.pkind == kMas;
+    auto coarse = [&](const PcgArgs& aa) {
+        for (int l = 1; l < n_levels; ++l)
+            launch_level<M_COARSE>(c, l, nullptr, nullptr, aa, partials_of(T_LEVEL + l), w.tickets.p + T_LEVEL + l,
+                                   w.scal.p + S_RZ + l);
+    };
     // r = b, z = M r, p = z, rho0 = r.z (pcg.hpp:51-57)
     if (mas) {
-        launch_l0<M_INIT>(c, nullptr, w.z.p, a, partials_of(T_L0), w.tickets.p + T_L0, w.scal.p + S_RZ_L0);
-        launch_coarse(c, w.r.p, w.flags.p, partials_of(T_C), w.tickets.p + T_C, w.scal.p + S_RZ_C);
+        launch_level<M_INIT>(c, 0, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL, w.scal.p + S_RZ);
+        coarse(a);
     } else {
-        launch_jacobi<M_INIT>(c, nullptr, w.z.p, a, partials_of(T_L0), w.tickets.p + T_L0, w.scal.p + S_RZ_L0);
-        ADIPC_CUDA(cudaMemsetAsync(w.scal.p + S_RZ_C, 0, sizeof(double), st));
+        launch_jacobi<M_INIT>(c, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL, w.scal.p + S_RZ);
     }
-    launch_final<F_PCG_INIT>(c, w.z.p, w.p.p, a);
-    k_zero<<<slot_grid(c), 256, 0, st>>>(w.ap.p, n3, w.flags.p);
-    ADIPC_LAUNCH_CHECK();
+    launch_final<F_PCG_INIT>(c, w.z.p, w.p.p, w.ap.p, a);
 
     int h_flags[F_COUNT] = {0};
     const int chunk = 16;
     // optional per-kernel-class timing (ADIPC_OPT_PROFILE): events bracket the
-    // SpMV, level-0, coarse and prolongation/update launches of every
+    // SpMV, level-0, coarse-level and prolongation/update launches of every
     // iteration on the solve stream; summed after each chunk's sync.
     const bool prof = c.profile;
     if (prof) {
@@ -179,33 +178,31 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
                 PcgArgs ar = a;
                 ar.ap = w.tmp.p;
                 if (mas)
-                    launch_l0<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_L0), w.tickets.p + T_L0,
-                                         w.scal.p + S_RZ_L0);
+                    launch_level<M_RESTART>(c, 0, nullptr, w.z.p, ar, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
+                                            w.scal.p + S_RZ);
                 else
-                    launch_jacobi<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_L0), w.tickets.p + T_L0,
-                                             w.scal.p + S_RZ_L0);
+                    launch_jacobi<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
+                                             w.scal.p + S_RZ);
             } else {
                 if (mas)
-                    launch_l0<M_UPDATE>(c, nullptr, w.z.p, a, partials_of(T_L0), w.tickets.p + T_L0,
-                                        w.scal.p + S_RZ_L0);
+                    launch_level<M_UPDATE>(c, 0, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
+                                           w.scal.p + S_RZ);
                 else
-                    launch_jacobi<M_UPDATE>(c, nullptr, w.z.p, a, partials_of(T_L0), w.tickets.p + T_L0,
-                                            w.scal.p + S_RZ_L0);
+                    launch_jacobi<M_UPDATE>(c, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
+                                            w.scal.p + S_RZ);
             }
             mark(k - kbeg, 2);
-            if (mas) launch_coarse(c, w.r.p, w.flags.p, partials_of(T_C), w.tickets.p + T_C, w.scal.p + S_RZ_C);
+            if (mas) coarse(a);
             mark(k - kbeg, 3);
-            launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, a);
-            k_zero<<<slot_grid(c), 256, 0, st>>>(w.ap.p, n3, w.flags.p);
-            ADIPC_LAUNCH_CHECK();
+            launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
             mark(k - kbeg, 4);
         }
         ADIPC_CUDA(cudaMemcpyAsync(h_flags, w.flags.p, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
         ADIPC_CUDA(cudaStreamSynchronize(st));
         if (prof) {
             // iterations of this chunk that did work (the rest returned early)
-            const int done_at = h_flags[F_DONE] ? h_flags[F_ITERS] : kend;
-            for (int kk = kbeg; kk <= std::min(kend, std::max(done_at, kbeg)); ++kk) {
+            const int last = h_flags[F_DONE] ? std::min(kend, std::max(h_flags[F_ITERS], kbeg)) : kend;
+            for (int kk = kbeg; kk <= last; ++kk) {
                 for (int q = 0; q < 4; ++q) {
                     float ms = 0;
                     ADIPC_CUDA(cudaEventElapsedTime(&ms, c.prof_events[5 * (kk - kbeg) + q],

@@ -58,6 +58,18 @@ def hybrid(n_soft=4, soft_res=20, n_gears=40, gear_res=8, stencils_per_pair=1250
     return Scene(_lib.scenes().adipc_scene_hybrid(n_soft, soft_res, n_gears, gear_res, stencils_per_pair, seed))
 
 
+def gravity_rhs(sc: Scene, dt: float = 0.01, g=(0.0, -9.81, 0.0)) -> np.ndarray:
+    """Newton right-hand side of the first iteration of a step from rest:
+    -grad E = -M (x - x_tilde) = M dt^2 g (incremental_potential.hpp:170-180,
+    newton.hpp:85-99), zero on pinned slots (incremental_potential.hpp:253-254).
+    FEM-only scenes: the first n_blocks stream entries are the mass diagonals."""
+    assert sc.n_bodies == 0, "gravity_rhs is defined for deformable-only scenes"
+    mass = sc.vals[: sc.n_blocks, 0]
+    b = mass[:, None] * (dt * dt) * np.asarray(g, np.float64)[None, :]
+    b[sc.pinned.astype(bool)] = 0.0
+    return np.ascontiguousarray(b.reshape(-1))
+
+
 CONFIGS = {
     "cfg1_soft_cube": lambda: fem_box(11, 11, 11, 0.1, 0.1, 0.1, E=1e5, pin_x0=False),
     "cfg2_cloth": lambda: cloth(224, 224),

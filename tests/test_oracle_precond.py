@@ -230,3 +230,27 @@ def test_pcg_zero_rhs(chain):  # :122-129
     A = O.Matrix(v, rows, cols, blocks)
     x, r = O.pcg_solve(A, np.zeros(3 * v), O.BlockJacobiPreconditioner(A), 1e-4, 250, 100)
     assert r["converged"] and r["iters"] == 0 and np.linalg.norm(x) == 0
+
+
+def test_stiff_beam_cemas_vs_jacobi_ratio():
+    """Acceptance #6 (acceptance.cpp:121-164) analogue on the
+    beam's first Newton system (rest state, pinned x=0 face, b = M dt^2 g):
+    cemas16 needs <= 0.6x the block-Jacobi PCG iterations. Also pins the
+    hierarchy sizes of SURVEY.md Appendix B (371/62/34/17, 513 L1 nodes)."""
+    import paper_2411_06224_b200 as P
+    from paper_2411_06224_b200 import scenes
+
+    sc = scenes.CONFIGS["stiff_beam"]()
+    det = O.ExecPolicy(deterministic=True)
+    fk, fv = O.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    sk, sv = O.sort_stream(fk, fv, det)
+    rows, cols, blocks = O.fast_hash_reduction(sk, sv, sc.n_blocks, det)
+    A = O.Matrix(sc.n_blocks, rows, cols, blocks)
+    l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, 16)
+    H = O.Hierarchy(l0.part_of, l0.n_parts, 16, O.block_edges(rows, cols), 4)
+    assert [(L["n_nodes"], L["n_parts"]) for L in H.levels] == [(5040, 371), (513, 62), (197, 34), (169, 17)]
+    b = scenes.gravity_rhs(sc)
+    _, rm = O.pcg_solve(A, b, O.MasPreconditioner(A, H), 1e-4, 250, 100000, det)
+    _, rj = O.pcg_solve(A, b, O.BlockJacobiPreconditioner(A), 1e-4, 250, 100000, det)
+    assert rm["converged"] and rj["converged"]
+    assert rm["iters"] / rj["iters"] <= 0.6, (rm["iters"], rj["iters"])

@@ -268,6 +268,7 @@ def run_ours(args, rank, world, local_rank, dist):
     pcg_ms = sum(t["pcg_ms"] for _, t, _ in recs)
     asm_ms = sum(t["assemble_ms"] for _, t, _ in recs)
     build_ms = sum(t["build_ms"] for _, t, _ in recs)
+    build_host_ms = sum(t["build_host_ms"] for _, t, _ in recs)
     prof = {k: sum(p[k] for _, _, p in recs) for k in ("spmv_ms", "l0_ms", "coarse_ms", "final_ms", "iters")}
     res_last = recs[-1][0]
     # size-independent check at full size: true residual of the returned x
@@ -322,6 +323,7 @@ def run_ours(args, rank, world, local_rank, dist):
             "ms_per_newton_solve": (sum(g["build_ms"] + g["pcg_ms"] for g in gathered[:1]) / args.steps),
             "assembly_ms": asm_ms / args.steps,
             "mas_build_ms": build_ms / args.steps,
+            "mas_build_host_ms": build_host_ms / args.steps,
             "pcg_ms": pcg_ms / args.steps,
             "pcg_iters_per_solve": iters / args.steps,
             "converged": all(g["conv"] for g in gathered),

@@ -205,11 +205,12 @@ __global__ void k_sort_rows_cta(std::uint64_t* __restrict__ sorted, std::uint64_
 }
 
 // One warp per row: every head lane (first element of a unique col) sums its
-// run sequentially in emission order and writes the unique block.
+// run sequentially in emission order and writes the unique block into the
+// SoA block planes (plane k = element k of every block, stride U).
 __global__ void k_reduce_rows(const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
                               const std::int64_t* __restrict__ uniq_start, std::int32_t n,
                               const double* __restrict__ vals, std::uint32_t* __restrict__ out_rows,
-                              std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks) {
+                              std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks, std::int64_t U) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
     for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps) {
@@ -237,9 +238,8 @@ __global__ void k_reduce_rows(const std::uint64_t* __restrict__ sorted, const st
                 }
                 out_rows[my_u] = static_cast<std::uint32_t>(r);
                 out_cols[my_u] = col;
-                double* dst = out_blocks + 9 * my_u;
 #pragma unroll
-                for (int k = 0; k < 9; ++k) dst[k] = acc[k];
+                for (int k = 0; k < 9; ++k) out_blocks[k * U + my_u] = acc[k];
             }
             u += __popc(hm);
         }
@@ -268,6 +268,22 @@ __global__ void k_gather_sorted(const std::uint64_t* __restrict__ sorted, const 
             const double* src = vals + 9 * static_cast<std::int64_t>(static_cast<std::uint32_t>(v));
             for (int k = 0; k < 9; ++k) out_vals[9 * p + k] = src[k];
         }
+}
+
+// AoS (9 doubles per block, the reference's Mat3 storage) <-> SoA planes
+__global__ void k_aos_to_soa(const double* __restrict__ aos, double* __restrict__ soa, std::int64_t U) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < 9 * U;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t u = i / 9;
+        soa[(i - 9 * u) * U + u] = aos[i];
+    }
+}
+__global__ void k_soa_to_aos(const double* __restrict__ soa, double* __restrict__ aos, std::int64_t U) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < 9 * U;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t u = i / 9;
+        aos[i] = soa[(i - 9 * u) * U + u];
+    }
 }
 
 __global__ void k_count_rows(const std::uint32_t* __restrict__ rows, std::int64_t U, std::int32_t n,
@@ -384,6 +400,17 @@ void bucket_sort(Ctx& c, const std::uint64_t* d_keys, std::int64_t T, std::int32
     }
 }
 
+void blocks_aos_to_soa(Ctx& c, const double* aos, double* soa, std::int64_t U) {
+    if (U == 0) return;
+    k_aos_to_soa<<<grid_for(9 * U, 256, 16), 256, 0, c.stream>>>(aos, soa, U);
+    ADIPC_LAUNCH_CHECK();
+}
+void blocks_soa_to_aos(Ctx& c, const double* soa, double* aos, std::int64_t U) {
+    if (U == 0) return;
+    k_soa_to_aos<<<grid_for(9 * U, 256, 16), 256, 0, c.stream>>>(soa, aos, U);
+    ADIPC_LAUNCH_CHECK();
+}
+
 // Sort + reduce of a device-resident triplet stream into `out` (CSR row_ptr
 // included). Shared by the global assembly and the two-level ABD reduction.
 void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
@@ -402,7 +429,7 @@ void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std:
     out.blocks.reserve(static_cast<std::size_t>(U) * 9);
     if (n > 0 && U > 0) {
         k_reduce_rows<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, out.row_ptr.p, n, d_vals,
-                                                          out.rows.p, out.cols.p, out.blocks.p);
+                                                          out.rows.p, out.cols.p, out.blocks.p, U);
         ADIPC_LAUNCH_CHECK();
     }
     ++out.version;
@@ -446,7 +473,9 @@ void upload_matrix(Ctx& c, std::int32_t n, std::int64_t U, const std::uint32_t* 
     if (U > 0) {
         ADIPC_CUDA(cudaMemcpyAsync(A.rows.p, rows, 4 * U, kind, c.stream));
         ADIPC_CUDA(cudaMemcpyAsync(A.cols.p, cols, 4 * U, kind, c.stream));
-        ADIPC_CUDA(cudaMemcpyAsync(A.blocks.p, blocks, 72 * U, kind, c.stream));
+        c.vals.reserve(9 * U);  // AoS staging, then transposed into the SoA planes
+        ADIPC_CUDA(cudaMemcpyAsync(c.vals.p, blocks, 72 * U, kind, c.stream));
+        blocks_aos_to_soa(c, c.vals.p, A.blocks.p, U);
     }
     // row_ptr from the sorted rows: histogram + scan
     c.row_cnt.reserve(static_cast<std::size_t>(n) + 1);

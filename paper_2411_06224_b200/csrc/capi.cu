@@ -227,7 +227,11 @@ int adipc_gpu_copy_matrix(adipc_gpu_ctx* ctx, uint32_t* rows, uint32_t* cols, do
         if (U == 0) return;
         if (rows) ADIPC_CUDA(cudaMemcpyAsync(rows, c.A.rows.p, 4 * U, cudaMemcpyDeviceToHost, c.stream));
         if (cols) ADIPC_CUDA(cudaMemcpyAsync(cols, c.A.cols.p, 4 * U, cudaMemcpyDeviceToHost, c.stream));
-        if (blocks9) ADIPC_CUDA(cudaMemcpyAsync(blocks9, c.A.blocks.p, 72 * U, cudaMemcpyDeviceToHost, c.stream));
+        if (blocks9) {
+            c.vals.reserve(9 * U);
+            blocks_soa_to_aos(c, c.A.blocks.p, c.vals.p, U);
+            ADIPC_CUDA(cudaMemcpyAsync(blocks9, c.vals.p, 72 * U, cudaMemcpyDeviceToHost, c.stream));
+        }
         sync(c);
     });
 }

@@ -24,9 +24,11 @@ struct StatusError : std::runtime_error {
 };
 
 // Assembled SortedSymBlockCoo (block_coo.hpp:54-61) in HBM.
-//   rows/cols u32[U], blocks f64[9U] (each block column-major, 72 B, exactly
-//   the reference's std::vector<Mat3> storage), row_ptr i64[n+1] (CSR offsets
-//   of the sorted rows, derived).
+//   rows/cols u32[U]; blocks f64[9][U] as SoA planes (plane k holds element k,
+//   column-major within the block, of every block) so that each warp-wide
+//   load in SpMV / restriction is one fully coalesced 256-byte access; the
+//   C-ABI converts to / from the reference's AoS Mat3 storage (72 B per block)
+//   at the boundary. row_ptr i64[n+1]: CSR offsets of the sorted rows.
 struct DeviceMatrix {
     std::int32_t n = 0;
     std::int64_t U = 0;
@@ -120,6 +122,8 @@ void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std:
                  DeviceMatrix& out);
 void sort_stream(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::uint64_t* d_out_keys,
                  double* d_out_vals);
+void blocks_aos_to_soa(Ctx& c, const double* aos, double* soa, std::int64_t U);
+void blocks_soa_to_aos(Ctx& c, const double* soa, double* aos, std::int64_t U);
 void upload_matrix(Ctx& c, std::int32_t n, std::int64_t U, const std::uint32_t* rows, const std::uint32_t* cols,
                    const double* blocks, bool host_ptrs);
 void segment_reduce(Ctx& c, const std::int32_t* d_O, std::int64_t n, const double* d_V, int width,

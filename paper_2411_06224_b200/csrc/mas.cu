@@ -60,7 +60,7 @@ __global__ void k_restrict(const std::uint32_t* __restrict__ rows, const std::ui
         const std::int32_t r = rows[e], c = cols[e];
         double h[9];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) h[k] = blocks[9 * e + k];
+        for (int k = 0; k < 9; ++k) h[k] = blocks[k * U + e];  // SoA planes
         for (int l = 0; l < ra.n_levels; ++l) {
             const RestrictLevel& L = ra.lv[l];
             const std::int32_t nr = L.agg ? L.agg[r] : r;
@@ -176,13 +176,13 @@ __global__ void k_invert(std::int32_t n_parts, const std::int32_t* __restrict__ 
 }
 
 __global__ void k_jacobi_build(std::int32_t n, const std::uint32_t* __restrict__ cols, const double* __restrict__ blocks,
-                               const std::int64_t* __restrict__ row_ptr, double* __restrict__ jinv) {
+                               std::int64_t U, const std::int64_t* __restrict__ row_ptr, double* __restrict__ jinv) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         double a[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
         for (std::int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
             if (cols[e] == static_cast<std::uint32_t>(i)) {
-                for (int k = 0; k < 9; ++k) a[k] = blocks[9 * e + k];
+                for (int k = 0; k < 9; ++k) a[k] = blocks[k * U + e];  // SoA planes
                 // adjugate inverse (Mat3::inverse), a column-major: A(r,c) = a[3c+r]
                 auto A = [&](int r, int c) { return a[3 * c + r]; };
                 double cof[9];
@@ -324,7 +324,7 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
     if (kind == kJacobi) {
         c.jinv.reserve(9 * static_cast<std::size_t>(A.n));
         if (A.n > 0) {
-            k_jacobi_build<<<grid_for(A.n, 256, 16), 256, 0, st>>>(A.n, A.cols.p, A.blocks.p, A.row_ptr.p, c.jinv.p);
+            k_jacobi_build<<<grid_for(A.n, 256, 16), 256, 0, st>>>(A.n, A.cols.p, A.blocks.p, A.U, A.row_ptr.p, c.jinv.p);
             ADIPC_LAUNCH_CHECK();
         }
         c.pkind = kJacobi;

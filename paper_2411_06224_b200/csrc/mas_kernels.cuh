@@ -140,14 +140,37 @@ __global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, doubl
                 b[t] = gather_r<kMode>(a, L.r_in, gi[t], alpha);
             }
         }
+        // b to shared memory (broadcast reads below; also feeds the restriction)
+#pragma unroll
+        for (int t = 0; t < kRegs; ++t) bsm[w][lane + 32 * t] = b[t];
+        __syncwarp();
         const double* M = L.inv + L.inv_off[s];
-        for (int k = 0; k < dim; ++k) {
-            const double bk = __shfl_sync(0xffffffffu, b[k >> 5], k & 31);
-            const double* col = M + static_cast<std::int64_t>(k) * dim;
+        // y = M b, columns streamed 8 at a time so every lane keeps 8 * kRegs
+        // independent loads in flight (the inverse is read exactly once)
+        constexpr int kU = 8;
+        int k = 0;
+        for (; k + kU <= dim; k += kU) {
+            double c[kU][kRegs];
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+#pragma unroll
+                for (int t = 0; t < kRegs; ++t) {
+                    const int j = lane + 32 * t;
+                    c[u][t] = j < dim ? __ldg(M + static_cast<std::int64_t>(k + u) * dim + j) : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const double bk = bsm[w][k + u];
+#pragma unroll
+                for (int t = 0; t < kRegs; ++t) y[t] += c[u][t] * bk;
+            }
+        }
+        for (; k < dim; ++k) {
+            const double bk = bsm[w][k];
 #pragma unroll
             for (int t = 0; t < kRegs; ++t) {
                 const int j = lane + 32 * t;
-                if (j < dim) y[t] += __ldg(col + j) * bk;
+                if (j < dim) y[t] += __ldg(M + static_cast<std::int64_t>(k) * dim + j) * bk;
             }
         }
 #pragma unroll
@@ -157,9 +180,6 @@ __global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, doubl
                 dsum += b[t] * y[t];
             }
         if (L.r_next) {  // restriction to the nested next-level nodes
-#pragma unroll
-            for (int t = 0; t < kRegs; ++t) bsm[w][lane + 32 * t] = b[t];
-            __syncwarp();
             const std::int32_t v0 = L.up_first[s];
             const int nv3 = 3 * (L.up_first[s + 1] - v0);
             for (int t = lane; t < nv3; t += 32) {

@@ -38,9 +38,8 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
         if (valid) {
             r = __ldg(rows + e);
             c = __ldg(cols + e);
-            const double* hb = blocks + 9 * e;
 #pragma unroll
-            for (int k = 0; k < 9; ++k) h[k] = __ldg(hb + k);
+            for (int k = 0; k < 9; ++k) h[k] = __ldg(blocks + k * U + e);  // SoA planes: coalesced
             const double xc0 = __ldg(x + 3 * c), xc1 = __ldg(x + 3 * c + 1), xc2 = __ldg(x + 3 * c + 2);
             // column-major H(i,j) = h[3j+i]
             yr0 = h[0] * xc0 + h[3] * xc1 + h[6] * xc2;

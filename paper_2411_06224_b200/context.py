@@ -102,7 +102,7 @@ class Context:
         t = np.zeros(4, np.float32)
         it = C.c_int()
         self._check(self._L.adipc_gpu_pcg_profile(self.h, t, C.byref(it)))
-        return dict(spmv_ms=float(t[0]), l0_ms=float(t[1]), coarse_ms=float(t[2]), final_ms=float(t[3]),
+        return dict(spmv_ms=float(t[0]), update_ms=float(t[1]), precond_ms=float(t[2]), final_ms=float(t[3]),
                     iters=it.value)
 
     @staticmethod

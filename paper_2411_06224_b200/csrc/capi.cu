@@ -126,6 +126,9 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.w.tickets.free();
     c.w.flags.free();
     for (auto e : c.prof_events) cudaEventDestroy(e);
+    if (c.side) cudaStreamDestroy(c.side);
+    if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+    if (c.ev_join) cudaEventDestroy(c.ev_join);
     if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
     delete ctx;
     return ADIPC_OK;

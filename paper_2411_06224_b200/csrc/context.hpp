@@ -102,6 +102,11 @@ struct Ctx {
 
     PcgWork w;
 
+    // side stream + fork/join events: the coarse MAS chain runs concurrently
+    // with the level-0 solve inside each PCG iteration
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+
     // per-kernel-class PCG timing (ADIPC_OPT_PROFILE): spmv, level 0, coarse, final
     bool profile = false;
     std::vector<cudaEvent_t> prof_events;

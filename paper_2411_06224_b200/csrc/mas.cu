@@ -387,7 +387,10 @@ void build_mas_from_hierarchy(Ctx& c, const host::MasHierarchy& h) {
 // launch helpers shared with pcg.cu
 int level_grid(const Ctx& c, int l) {
     const DeviceLevel& L = *c.levels[l];
-    return L.max_fill > 32 ? grid_for(L.n_parts, 1, 8) : grid_for(L.n_parts, 8, 8);
+    // one subdomain per warp (8 per CTA), no grid-stride: the block scheduler
+    // balances the memory-bound warps; fills > 32 take a CTA each
+    const std::int64_t per = L.max_fill > 32 ? 1 : 8;
+    return static_cast<int>(std::max<std::int64_t>(1, ceil_div(L.n_parts, per)));
 }
 int slot_grid(const Ctx& c) { return grid_for(3 * static_cast<std::int64_t>(c.A.n), 256, 8); }
 int jacobi_grid(const Ctx& c) { return grid_for(c.A.n, 256, 8); }
@@ -415,32 +418,40 @@ LevelArgs level_args(Ctx& c, int l, const double* r_in, double* out) {
 
 // Level-l MAS solve (+ restriction to level l+1). Level 0 uses `kMode`
 // (apply / PCG gather modes); coarser levels read their restricted residual.
-template <int kMode>
+// kSolve = false: gather + restriction only (the PCG update pass);
+// restrict_next = false: no restriction (the level-0 solve of the PCG, whose
+// restriction was done by the update pass).
+template <int kMode, bool kSolve>
 void launch_level(Ctx& c, int l, const double* r_in, double* z, const PcgArgs& a, double* partials,
-                  unsigned* ticket, double* dot_out) {
-    const LevelArgs la = level_args(c, l, r_in, z);
+                  unsigned* ticket, double* dot_out, cudaStream_t st, bool restrict_next) {
+    LevelArgs la = level_args(c, l, r_in, z);
+    if (!restrict_next) la.r_next = nullptr;
     const DeviceLevel& L = *c.levels[l];
     const int regs = dim_regs(L.max_fill);
     const int grid = level_grid(c, l);
     if (regs == 0) {
         const std::size_t smem = sizeof(double) * 3 * L.max_fill;
-        ADIPC_CUDA(cudaFuncSetAttribute(k_mas_level_big<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        ADIPC_CUDA(cudaFuncSetAttribute(k_mas_level_big<kMode, kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-        k_mas_level_big<kMode><<<grid, 128, smem, c.stream>>>(la, a, partials, ticket, dot_out);
+        k_mas_level_big<kMode, kSolve><<<grid, 128, smem, st>>>(la, a, partials, ticket, dot_out);
     } else if (regs == 1) {
-        k_mas_level<kMode, 1><<<grid, 256, 0, c.stream>>>(la, a, partials, ticket, dot_out);
+        k_mas_level<kMode, 1, kSolve><<<grid, 256, 0, st>>>(la, a, partials, ticket, dot_out);
     } else if (regs == 2) {
-        k_mas_level<kMode, 2><<<grid, 256, 0, c.stream>>>(la, a, partials, ticket, dot_out);
+        k_mas_level<kMode, 2, kSolve><<<grid, 256, 0, st>>>(la, a, partials, ticket, dot_out);
     } else {
-        k_mas_level<kMode, 3><<<grid, 256, 0, c.stream>>>(la, a, partials, ticket, dot_out);
+        k_mas_level<kMode, 3, kSolve><<<grid, 256, 0, st>>>(la, a, partials, ticket, dot_out);
     }
     ADIPC_LAUNCH_CHECK();
 }
-template void launch_level<M_APPLY>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
-template void launch_level<M_INIT>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
-template void launch_level<M_UPDATE>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
-template void launch_level<M_RESTART>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
-template void launch_level<M_COARSE>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
+#define ADIPC_INST(M, S)                                                                                      \
+    template void launch_level<M, S>(Ctx&, int, const double*, double*, const PcgArgs&, double*, unsigned*, \
+                                     double*, cudaStream_t, bool);
+ADIPC_INST(M_APPLY, true)
+ADIPC_INST(M_COARSE, true)
+ADIPC_INST(M_INIT, false)
+ADIPC_INST(M_UPDATE, false)
+ADIPC_INST(M_RESTART, false)
+#undef ADIPC_INST
 
 ProlongArgs prolong_args(const Ctx& c) {
     ProlongArgs pa{};
@@ -480,9 +491,9 @@ void precond_apply(Ctx& c, const double* d_r, double* d_z) {
     if (c.pkind == kJacobi) {
         launch_jacobi<M_APPLY>(c, d_r, d_z, a, nullptr, nullptr, nullptr);
     } else if (c.pkind == kMas) {
-        launch_level<M_APPLY>(c, 0, d_r, d_z, a, nullptr, nullptr, nullptr);
+        launch_level<M_APPLY, true>(c, 0, d_r, d_z, a, nullptr, nullptr, nullptr, c.stream, true);
         for (int l = 1; l < static_cast<int>(c.levels.size()); ++l)
-            launch_level<M_COARSE>(c, l, nullptr, nullptr, a, nullptr, nullptr, nullptr);
+            launch_level<M_COARSE, true>(c, l, nullptr, nullptr, a, nullptr, nullptr, nullptr, c.stream, true);
         launch_final<F_APPLY>(c, d_z, nullptr, nullptr, a);
     } else {
         throw StatusError(kInvalidArgument, "no preconditioner built");

@@ -112,21 +112,36 @@ __device__ __forceinline__ double gather_r(const PcgArgs& a, const double* r_in,
 // One warp per subdomain (dim = 3 f <= 32 kRegs): gather b, y = D^-1 b with
 // the inverse read column by column (coalesced), store y, emit the next
 // level's restricted residual from b (smem), dot partial b.y.
-template <int kMode, int kRegs>
+// kSolve = false: gather (with the fused PCG vector update) + restriction
+// only — the PCG's update pass, after which the level-0 solve and the coarse
+// chain run concurrently.
+template <int kMode, int kRegs, bool kSolve = true>
 __global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, double* __restrict__ partials,
                                                   unsigned* __restrict__ ticket, double* __restrict__ dot_out) {
     __shared__ double bsm[8][32 * kRegs];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double alpha = 0;
-    if (kMode != M_APPLY && kMode != M_INIT) {
-        if (a.flags && a.flags[F_DONE]) return;
-        if ((kMode == M_UPDATE || kMode == M_RESTART) && !pcg_alpha(a, alpha)) return;
-    }
+    if (a.flags && a.flags[F_DONE]) return;
+    if ((kMode == M_UPDATE || kMode == M_RESTART) && !pcg_alpha(a, alpha)) return;
     double dsum = 0;
     const int wpb = blockDim.x >> 5;
     for (std::int32_t s = blockIdx.x * wpb + w; s < L.n_parts; s += gridDim.x * wpb) {
         const std::int32_t s0 = L.sub_ptr[s];
         const int dim = 3 * (L.sub_ptr[s + 1] - s0);
+        constexpr int kU = 8;
+        const double* M = kSolve ? L.inv + L.inv_off[s] : nullptr;
+        // first batch of inverse columns issued before the (latency-bound)
+        // gather: the inverse does not depend on b
+        double c[kU][kRegs];
+        if (kSolve) {
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+#pragma unroll
+                for (int t = 0; t < kRegs; ++t) {
+                    const int j = lane + 32 * t;
+                    c[u][t] = (j < dim && u < dim) ? __ldg(M + static_cast<std::int64_t>(u) * dim + j) : 0.0;
+                }
+        }
         double b[kRegs], y[kRegs];
         std::int64_t gi[kRegs];
 #pragma unroll
@@ -144,41 +159,39 @@ __global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, doubl
 #pragma unroll
         for (int t = 0; t < kRegs; ++t) bsm[w][lane + 32 * t] = b[t];
         __syncwarp();
-        const double* M = L.inv + L.inv_off[s];
-        // y = M b, columns streamed 8 at a time so every lane keeps 8 * kRegs
-        // independent loads in flight (the inverse is read exactly once)
-        constexpr int kU = 8;
-        int k = 0;
-        for (; k + kU <= dim; k += kU) {
-            double c[kU][kRegs];
+        if (kSolve) {
+            // y = M b, columns streamed kU at a time, the next batch in flight
+            // while the current one is consumed (the inverse is read once)
+            for (int k = 0; k < dim; k += kU) {
+                double nc[kU][kRegs];
+                const bool more = k + kU < dim;
 #pragma unroll
-            for (int u = 0; u < kU; ++u)
+                for (int u = 0; u < kU; ++u)
 #pragma unroll
-                for (int t = 0; t < kRegs; ++t) {
-                    const int j = lane + 32 * t;
-                    c[u][t] = j < dim ? __ldg(M + static_cast<std::int64_t>(k + u) * dim + j) : 0.0;
+                    for (int t = 0; t < kRegs; ++t) {
+                        const int j = lane + 32 * t;
+                        const int kk = k + kU + u;
+                        nc[u][t] = (more && j < dim && kk < dim) ? __ldg(M + static_cast<std::int64_t>(kk) * dim + j)
+                                                                  : 0.0;
+                    }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const double bk = (k + u < dim) ? bsm[w][k + u] : 0.0;
+#pragma unroll
+                    for (int t = 0; t < kRegs; ++t) y[t] += c[u][t] * bk;
                 }
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const double bk = bsm[w][k + u];
+                for (int u = 0; u < kU; ++u)
 #pragma unroll
-                for (int t = 0; t < kRegs; ++t) y[t] += c[u][t] * bk;
+                    for (int t = 0; t < kRegs; ++t) c[u][t] = nc[u][t];
             }
+#pragma unroll
+            for (int t = 0; t < kRegs; ++t)
+                if (gi[t] >= 0) {
+                    L.out[gi[t]] = y[t];
+                    dsum += b[t] * y[t];
+                }
         }
-        for (; k < dim; ++k) {
-            const double bk = bsm[w][k];
-#pragma unroll
-            for (int t = 0; t < kRegs; ++t) {
-                const int j = lane + 32 * t;
-                if (j < dim) y[t] += __ldg(M + static_cast<std::int64_t>(k) * dim + j) * bk;
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < kRegs; ++t)
-            if (gi[t] >= 0) {
-                L.out[gi[t]] = y[t];
-                dsum += b[t] * y[t];
-            }
         if (L.r_next) {  // restriction to the nested next-level nodes
             const std::int32_t v0 = L.up_first[s];
             const int nv3 = 3 * (L.up_first[s + 1] - v0);
@@ -198,15 +211,13 @@ __global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, doubl
 // General-size variant (fill > 32, e.g. the exact single-domain
 // preconditioner of test_solver.cpp:99-111): one CTA per subdomain, b in
 // dynamic shared memory, any dim.
-template <int kMode>
+template <int kMode, bool kSolve = true>
 __global__ void __launch_bounds__(128) k_mas_level_big(LevelArgs L, PcgArgs a, double* __restrict__ partials,
                                                       unsigned* __restrict__ ticket, double* __restrict__ dot_out) {
     extern __shared__ double bs[];
     double alpha = 0;
-    if (kMode != M_APPLY && kMode != M_INIT) {
-        if (a.flags && a.flags[F_DONE]) return;
-        if ((kMode == M_UPDATE || kMode == M_RESTART) && !pcg_alpha(a, alpha)) return;
-    }
+    if (a.flags && a.flags[F_DONE]) return;
+    if ((kMode == M_UPDATE || kMode == M_RESTART) && !pcg_alpha(a, alpha)) return;
     double dsum = 0;
     for (std::int32_t s = blockIdx.x; s < L.n_parts; s += gridDim.x) {
         const std::int32_t s0 = L.sub_ptr[s];
@@ -215,7 +226,7 @@ __global__ void __launch_bounds__(128) k_mas_level_big(LevelArgs L, PcgArgs a, d
             bs[j] = gather_r<kMode>(a, L.r_in, 3 * static_cast<std::int64_t>(L.sub_nodes[s0 + j / 3]) + (j % 3), alpha);
         __syncthreads();
         const double* M = L.inv + L.inv_off[s];
-        for (int j = threadIdx.x; j < dim; j += blockDim.x) {
+        for (int j = threadIdx.x; kSolve && j < dim; j += blockDim.x) {
             double y = 0;
             for (int k = 0; k < dim; ++k) y += M[static_cast<std::int64_t>(k) * dim + j] * bs[k];
             L.out[3 * static_cast<std::int64_t>(L.sub_nodes[s0 + j / 3]) + (j % 3)] = y;

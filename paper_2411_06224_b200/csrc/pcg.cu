@@ -29,9 +29,9 @@ int spmv_grid(const Ctx& c);
 int level_grid(const Ctx& c, int l);
 int slot_grid(const Ctx& c);
 int jacobi_grid(const Ctx& c);
-template <int kMode>
+template <int kMode, bool kSolve>
 void launch_level(Ctx& c, int l, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
-                  double* dot_out);
+                  double* dot_out, cudaStream_t st, bool restrict_next);
 template <int kFinal>
 void launch_final(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a);
 template <int kMode>
@@ -127,15 +127,33 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
     a.scal = w.scal.p;
     a.flags = w.flags.p;
     a.k = 0;
-    auto coarse = [&](const PcgArgs& aa) {
+    // MAS preconditioner application inside the iteration: after the update
+    // pass (x, r and the level-1 restriction), the level-0 solve runs on the
+    // solve stream while the latency-bound coarse chain (levels 1..L-1, each
+    // restricting to the next) runs concurrently on a high-priority side
+    // stream; the prolongation/p-update kernel joins both.
+    if (mas && !c.side) {
+        int lo = 0, hi = 0;
+        ADIPC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        ADIPC_CUDA(cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, hi));
+        ADIPC_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+        ADIPC_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+    }
+    auto mas_apply = [&](const PcgArgs& aa) {
+        ADIPC_CUDA(cudaEventRecord(c.ev_fork, st));
+        ADIPC_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
         for (int l = 1; l < n_levels; ++l)
-            launch_level<M_COARSE>(c, l, nullptr, nullptr, aa, partials_of(T_LEVEL + l), w.tickets.p + T_LEVEL + l,
-                                   w.scal.p + S_RZ + l);
+            launch_level<M_COARSE, true>(c, l, nullptr, nullptr, aa, partials_of(T_LEVEL + l),
+                                         w.tickets.p + T_LEVEL + l, w.scal.p + S_RZ + l, c.side, true);
+        launch_level<M_APPLY, true>(c, 0, w.r.p, w.z.p, aa, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
+                                    w.scal.p + S_RZ, st, false);
+        ADIPC_CUDA(cudaEventRecord(c.ev_join, c.side));
+        ADIPC_CUDA(cudaStreamWaitEvent(st, c.ev_join, 0));
     };
     // r = b, z = M r, p = z, rho0 = r.z (pcg.hpp:51-57)
     if (mas) {
-        launch_level<M_INIT>(c, 0, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL, w.scal.p + S_RZ);
-        coarse(a);
+        launch_level<M_INIT, false>(c, 0, nullptr, nullptr, a, nullptr, nullptr, nullptr, st, true);
+        mas_apply(a);
     } else {
         launch_jacobi<M_INIT>(c, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL, w.scal.p + S_RZ);
     }
@@ -178,21 +196,19 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
                 PcgArgs ar = a;
                 ar.ap = w.tmp.p;
                 if (mas)
-                    launch_level<M_RESTART>(c, 0, nullptr, w.z.p, ar, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
-                                            w.scal.p + S_RZ);
+                    launch_level<M_RESTART, false>(c, 0, nullptr, nullptr, ar, nullptr, nullptr, nullptr, st, true);
                 else
                     launch_jacobi<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
                                              w.scal.p + S_RZ);
             } else {
                 if (mas)
-                    launch_level<M_UPDATE>(c, 0, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
-                                           w.scal.p + S_RZ);
+                    launch_level<M_UPDATE, false>(c, 0, nullptr, nullptr, a, nullptr, nullptr, nullptr, st, true);
                 else
                     launch_jacobi<M_UPDATE>(c, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
                                             w.scal.p + S_RZ);
             }
             mark(k - kbeg, 2);
-            if (mas) coarse(a);
+            if (mas) mas_apply(a);
             mark(k - kbeg, 3);
             launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
             mark(k - kbeg, 4);

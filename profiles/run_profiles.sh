@@ -1,16 +1,21 @@
 #!/bin/bash
-# Profiling recipe (B200_PROFILING.md), run on the GPU box from the repo root:
-#   bash profiles/run_profiles.sh <tag>
+# Profiling recipe (/opt/skills/guides/B200_PROFILING.md), on the GPU box from
+# the repo root:   bash profiles/run_profiles.sh <tag>
 # 1. launch list: every kernel of one warm bench step with its device time
-# 2. ncu --set full on the hot kernels of the PCG iteration and the build
+#    (cold-cache, serialised: compare shares, not absolutes)
+# 2. ncu --set full on the PCG-iteration kernels, the MAS build kernels and
+#    the assembly kernels (one capture each; never multi-rank)
 set -u
 TAG=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $CMD \
+    > $OUT/ncu_launch_$TAG.log 2>&1
 echo "launch list rc=$?"
-ncu --set full --clock-control none --import-source on \
-    -k regex:'k_spmv|k_mas_level|k_mas_final|k_restrict|k_invert|k_reduce_rows' -s 40 -c 12 \
-    -o $OUT/prof_$TAG -f $CMD > $OUT/ncu_full_$TAG.log 2>&1
-echo "ncu full rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:'k_spmv|k_mas_level|k_mas_final' -s 300 -c 8 \
+    -o $OUT/prof_pcg_$TAG -f $CMD > $OUT/ncu_pcg_$TAG.log 2>&1
+echo "ncu pcg rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:'k_restrict|k_invert|k_reduce_rows|k_row_scatter|k_sort_rows' \
+    -c 8 -o $OUT/prof_build_$TAG -f $CMD > $OUT/ncu_build_$TAG.log 2>&1
+echo "ncu build rc=$?"

@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--config", default="cfg5_stiff_box")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cache", action="store_true", help="rebuild the MAS hierarchy every step")
     ap.add_argument("--cpu-iters", type=int, default=10, help="PCG iterations per CPU sample step")
     return ap.parse_args()
 
@@ -244,8 +245,16 @@ def run_ours(args, rank, world, local_rank, dist):
         prof = ctx.pcg_profile()
         return res, t, prof
 
-    for _ in range(args.warmup):
-        step()
+    # first warm-up step: cold MAS build (hierarchy from the pattern); later
+    # steps reuse it while the pattern hash is unchanged (the hierarchy is a
+    # pure function of the pattern), as a Newton loop without contact changes
+    cold = None
+    for i in range(args.warmup):
+        _, t, _ = step()
+        if i == 0:
+            cold = t
+        if i == 0 and not args.no_cache:
+            ctx.set_option(_lib.OPT_CACHE_HIERARCHY, 1)
     levels = ctx.precond_levels()
     bm = byte_model(n, U, levels)
 
@@ -326,6 +335,9 @@ def run_ours(args, rank, world, local_rank, dist):
             "assembly_ms": asm_ms / args.steps,
             "mas_build_ms": build_ms / args.steps,
             "mas_build_host_ms": build_host_ms / args.steps,
+            "mas_build_cold_ms": cold["build_ms"] if cold else None,
+            "mas_build_cold_host_ms": cold["build_host_ms"] if cold else None,
+            "hierarchy_cache": not args.no_cache,
             "pcg_ms": pcg_ms / args.steps,
             "pcg_iters_per_solve": iters / args.steps,
             "converged": all(g["conv"] for g in gathered),

@@ -318,6 +318,39 @@ void factorize(Ctx& c) {
 }
 
 
+namespace {
+__device__ __forceinline__ std::uint64_t mix64(std::uint64_t z) {  // splitmix64 finaliser
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+// order-sensitive 64-bit hash of the pattern: sum_i mix(i, row_i, col_i)
+__global__ void k_pattern_hash(const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,
+                               std::int64_t U, unsigned long long* __restrict__ out) {
+    std::uint64_t h = 0;
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < U;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        h += mix64((static_cast<std::uint64_t>(rows[i]) << 32 | cols[i]) ^ mix64(static_cast<std::uint64_t>(i)));
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, static_cast<unsigned long long>(h));
+}
+}  // namespace
+
+std::uint64_t pattern_hash(Ctx& c) {
+    c.build_status.reserve(4);
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(c.build_status.p + 2);
+    ADIPC_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c.stream));
+    if (c.A.U > 0) {
+        k_pattern_hash<<<grid_for(c.A.U, 256, 8), 256, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.U, d);
+        ADIPC_LAUNCH_CHECK();
+    }
+    unsigned long long h = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    ADIPC_CUDA(cudaStreamSynchronize(c.stream));
+    return (h ^ (static_cast<std::uint64_t>(c.A.n) << 1) ^ static_cast<std::uint64_t>(c.A.U) * 0x9e3779b97f4a7c15ull) |
+           1ull;  // never equals the ~0 "invalid" marker's complement pattern; non-zero
+}
+
 void build_preconditioner(Ctx& c, PrecondKind kind) {
     cudaStream_t st = c.stream;
     const DeviceMatrix& A = c.A;
@@ -334,8 +367,13 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
     if (static_cast<std::int32_t>(c.l0.part_of.size()) != A.n)
         throw StatusError(kInvalidArgument, "level-0 partition size differs from n_block_rows");
     const auto t0 = std::chrono::steady_clock::now();
+    // The hierarchy is a pure function of (level-0 partition, sparsity
+    // pattern, max_levels): with ADIPC_OPT_CACHE_HIERARCHY it is reused while
+    // the pattern hash is unchanged (e.g. Newton iterations without contact
+    // changes); restriction and inversion always rerun on the new values.
+    const std::uint64_t phash = c.cache_hierarchy ? pattern_hash(c) : 0;
+    const bool reuse = c.cache_hierarchy && c.hier_version == phash && !c.levels.empty();
     // block_edges(A) (mas.hpp:19-25): off-diagonal (row, col) pairs, in order
-    const bool reuse = c.cache_hierarchy && c.hier_version == A.version && !c.levels.empty();
     if (!reuse) {
         std::vector<std::uint32_t> rows(A.U), cols(A.U);
         if (A.U) {
@@ -358,7 +396,7 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
             build_level(c, *c.levels.back(), c.hier.levels[l], l, A.n);
         }
         link_levels(c, c.hier);
-        c.hier_version = A.version;
+        c.hier_version = c.cache_hierarchy ? phash : ~0ull;
     } else {
         for (auto& L : c.levels)
             ADIPC_CUDA(cudaMemsetAsync(L->inv.p, 0, sizeof(double) * std::max<std::int64_t>(L->inv_doubles, 1), st));

@@ -28,18 +28,35 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
     const int lane = threadIdx.x & 31;
     const std::int64_t warp0 = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    // each warp owns a contiguous run of 32-block chunks (row locality for the
+    // x gathers and y atomics); software-pipelined: the next chunk's indices
+    // and block planes are in flight while the current chunk is processed
+    const std::int64_t n_chunks = (U + 31) >> 5;
+    const std::int64_t ch0 = warp0 * n_chunks / nwarps, ch1 = (warp0 + 1) * n_chunks / nwarps;
     double dsum = 0;
-    for (std::int64_t wbase = warp0 * 32; wbase < U; wbase += nwarps * 32) {
-        const std::int64_t e = wbase + lane;
-        const bool valid = e < U;
-        std::uint32_t r = 0xFFFFFFFFu, c = 0;
+    std::uint32_t nr = 0xFFFFFFFFu, nc = 0;
+    double nh[9];
+    auto load = [&](std::int64_t ch) {
+        const std::int64_t e = (ch << 5) + lane;
+        nr = 0xFFFFFFFFu;
+        nc = 0;
+        if (ch < ch1 && e < U) {
+            nr = __ldg(rows + e);
+            nc = __ldg(cols + e);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) nh[k] = __ldg(blocks + k * U + e);  // SoA planes: coalesced
+        }
+    };
+    load(ch0);
+    for (std::int64_t ch = ch0; ch < ch1; ++ch) {
+        const std::uint32_t r = nr, c = nc;
         double h[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) h[k] = nh[k];
+        load(ch + 1);
+        const bool valid = r != 0xFFFFFFFFu;
         double yr0 = 0, yr1 = 0, yr2 = 0;
         if (valid) {
-            r = __ldg(rows + e);
-            c = __ldg(cols + e);
-#pragma unroll
-            for (int k = 0; k < 9; ++k) h[k] = __ldg(blocks + k * U + e);  // SoA planes: coalesced
             const double xc0 = __ldg(x + 3 * c), xc1 = __ldg(x + 3 * c + 1), xc2 = __ldg(x + 3 * c + 2);
             // column-major H(i,j) = h[3j+i]
             yr0 = h[0] * xc0 + h[3] * xc1 + h[6] * xc2;
@@ -81,7 +98,19 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
 
 }  // namespace
 
-int spmv_grid(const Ctx& c) { return grid_for(ceil_div(c.A.U, 32), kSpmvThreads / 32, 8); }
+// One wave: SMs x resident CTAs per SM (each warp then streams one contiguous
+// run of chunks with its software pipeline).
+int spmv_grid(const Ctx& c) {
+    static int occ = 0;
+    if (occ == 0) {
+        ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<true>, kSpmvThreads, 0));
+        if (occ < 1) occ = 1;
+    }
+    int sms = kSMs;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    const std::int64_t need = ceil_div(ceil_div(c.A.U, 32), kSpmvThreads / 32);
+    return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(need, static_cast<std::int64_t>(sms) * occ)));
+}
 
 // y (+)= A x. zero_y: clear y first (otherwise the caller guarantees y == 0).
 // With `dot_out`: x.(A x) -> *dot_out (device), using `partials`

@@ -119,6 +119,9 @@ int adipc_gpu_filter_pinned_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, c
  * x and y of 3 * n_block_rows doubles. */
 int adipc_gpu_spmv(adipc_gpu_ctx* ctx, const double* x, double* y);
 int adipc_gpu_spmv_device(adipc_gpu_ctx* ctx, const double* d_x, double* d_y);
+/* profiling aid: ms per SpMV launch of a variant (0 normal, 1 no transposed
+ * scatter, 2 no atomics, 3 no column gather; 1-3 give wrong y) */
+int adipc_gpu_debug_spmv_time(adipc_gpu_ctx* ctx, const double* d_x, double* d_y, int mode, int iters, float* ms);
 
 /* ---- partition / hierarchy (host-side integer code, no GPU needed) ---------------- */
 int32_t adipc_subdomain_count(int32_t v, int32_t n, int32_t n_o);              /* partition.hpp:12-15 */

@@ -84,7 +84,7 @@ __global__ void k_abd_emit(const std::uint32_t* __restrict__ rows, const std::ui
          e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const std::int32_t i = static_cast<std::int32_t>(rows[e]), j = static_cast<std::int32_t>(cols[e]);
         double C[9];
-        for (int k = 0; k < 9; ++k) C[k] = blocks[k * U + e];  // SoA planes
+        for (int k = 0; k < 9; ++k) C[k] = blocks[blk(e, k)];
         std::int64_t pos = off[e];
         const bool fi = m.is_fem(i), fj = m.is_fem(j);
         double t[9];

@@ -206,7 +206,7 @@ __global__ void k_sort_rows_cta(std::uint64_t* __restrict__ sorted, std::uint64_
 
 // One warp per row: every head lane (first element of a unique col) sums its
 // run sequentially in emission order and writes the unique block into the
-// SoA block planes (plane k = element k of every block, stride U).
+// tiled block storage (blk(), common.cuh).
 __global__ void k_reduce_rows(const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
                               const std::int64_t* __restrict__ uniq_start, std::int32_t n,
                               const double* __restrict__ vals, std::uint32_t* __restrict__ out_rows,
@@ -239,7 +239,7 @@ __global__ void k_reduce_rows(const std::uint64_t* __restrict__ sorted, const st
                 out_rows[my_u] = static_cast<std::uint32_t>(r);
                 out_cols[my_u] = col;
 #pragma unroll
-                for (int k = 0; k < 9; ++k) out_blocks[k * U + my_u] = acc[k];
+                for (int k = 0; k < 9; ++k) out_blocks[blk(my_u, k)] = acc[k];
             }
             u += __popc(hm);
         }
@@ -270,19 +270,19 @@ __global__ void k_gather_sorted(const std::uint64_t* __restrict__ sorted, const 
         }
 }
 
-// AoS (9 doubles per block, the reference's Mat3 storage) <-> SoA planes
+// AoS (9 doubles per block, the reference's Mat3 storage) <-> tiled storage
 __global__ void k_aos_to_soa(const double* __restrict__ aos, double* __restrict__ soa, std::int64_t U) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < 9 * U;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const std::int64_t u = i / 9;
-        soa[(i - 9 * u) * U + u] = aos[i];
+        soa[blk(u, static_cast<int>(i - 9 * u))] = aos[i];
     }
 }
 __global__ void k_soa_to_aos(const double* __restrict__ soa, double* __restrict__ aos, std::int64_t U) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < 9 * U;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const std::int64_t u = i / 9;
-        aos[i] = soa[(i - 9 * u) * U + u];
+        aos[i] = soa[blk(u, static_cast<int>(i - 9 * u))];
     }
 }
 
@@ -426,7 +426,7 @@ void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std:
     out.U = U;
     out.rows.reserve(static_cast<std::size_t>(U));
     out.cols.reserve(static_cast<std::size_t>(U));
-    out.blocks.reserve(static_cast<std::size_t>(U) * 9);
+    out.blocks.reserve(blk_doubles(U));
     if (n > 0 && U > 0) {
         k_reduce_rows<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, out.row_ptr.p, n, d_vals,
                                                           out.rows.p, out.cols.p, out.blocks.p, U);
@@ -467,13 +467,13 @@ void upload_matrix(Ctx& c, std::int32_t n, std::int64_t U, const std::uint32_t* 
     A.U = U;
     A.rows.reserve(U);
     A.cols.reserve(U);
-    A.blocks.reserve(9 * U);
+    A.blocks.reserve(blk_doubles(U));
     A.row_ptr.reserve(static_cast<std::size_t>(n) + 1);
     const cudaMemcpyKind kind = host_ptrs ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     if (U > 0) {
         ADIPC_CUDA(cudaMemcpyAsync(A.rows.p, rows, 4 * U, kind, c.stream));
         ADIPC_CUDA(cudaMemcpyAsync(A.cols.p, cols, 4 * U, kind, c.stream));
-        c.vals.reserve(9 * U);  // AoS staging, then transposed into the SoA planes
+        c.vals.reserve(9 * U);  // AoS staging, then transposed into the tiled storage
         ADIPC_CUDA(cudaMemcpyAsync(c.vals.p, blocks, 72 * U, kind, c.stream));
         blocks_aos_to_soa(c, c.vals.p, A.blocks.p, U);
     }

@@ -378,6 +378,15 @@ int adipc_gpu_spmv(adipc_gpu_ctx* ctx, const double* x, double* y) {
     });
 }
 
+}  // extern "C"
+namespace adipc_gpu {
+float spmv_debug_time(Ctx& c, const double* d_x, double* d_y, int mode, int iters);
+}
+extern "C" {
+int adipc_gpu_debug_spmv_time(adipc_gpu_ctx* ctx, const double* d_x, double* d_y, int mode, int iters, float* ms) {
+    return guarded(ctx, [&] { *ms = spmv_debug_time(ctx->c, d_x, d_y, mode, iters); });
+}
+
 int adipc_gpu_spmv_device(adipc_gpu_ctx* ctx, const double* d_x, double* d_y) {
     return guarded(ctx, [&] {
         spmv(ctx->c, d_x, d_y, nullptr, 0);

@@ -73,6 +73,13 @@ struct DBuf {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Block value storage of the assembled matrix: 32-block tiles, SoA inside a
+// tile ("AoSoA"): element k (column-major within the 3x3 block) of block e
+// lives at blk(e, k). A warp working on 32 consecutive blocks reads one
+// contiguous 2,304-byte tile with nine fully coalesced 256-byte loads.
+__host__ __device__ __forceinline__ std::int64_t blk(std::int64_t e, int k) { return (e >> 5) * 288 + 32 * k + (e & 31); }
+inline std::size_t blk_doubles(std::int64_t U) { return static_cast<std::size_t>((U + 31) >> 5) * 288; }
+
 // Block-wide sum of a double; result valid in thread 0. blockDim <= 1024.
 __device__ __forceinline__ double block_sum(double v, double* smem32) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

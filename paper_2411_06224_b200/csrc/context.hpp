@@ -24,11 +24,12 @@ struct StatusError : std::runtime_error {
 };
 
 // Assembled SortedSymBlockCoo (block_coo.hpp:54-61) in HBM.
-//   rows/cols u32[U]; blocks f64[9][U] as SoA planes (plane k holds element k,
-//   column-major within the block, of every block) so that each warp-wide
-//   load in SpMV / restriction is one fully coalesced 256-byte access; the
-//   C-ABI converts to / from the reference's AoS Mat3 storage (72 B per block)
-//   at the boundary. row_ptr i64[n+1]: CSR offsets of the sorted rows.
+//   rows/cols u32[U]; blocks in 32-block tiles, SoA inside a tile (blk(),
+//   common.cuh): a warp's 32 consecutive blocks are one contiguous 2,304-byte
+//   tile read with nine coalesced 256-byte loads (DRAM page locality: one
+//   stream per warp instead of nine); the C-ABI converts to / from the
+//   reference's AoS Mat3 storage (72 B per block) at the boundary.
+//   row_ptr i64[n+1]: CSR offsets of the sorted rows.
 struct DeviceMatrix {
     std::int32_t n = 0;
     std::int64_t U = 0;

@@ -60,7 +60,7 @@ __global__ void k_restrict(const std::uint32_t* __restrict__ rows, const std::ui
         const std::int32_t r = rows[e], c = cols[e];
         double h[9];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) h[k] = blocks[k * U + e];  // SoA planes
+        for (int k = 0; k < 9; ++k) h[k] = blocks[blk(e, k)];
         for (int l = 0; l < ra.n_levels; ++l) {
             const RestrictLevel& L = ra.lv[l];
             const std::int32_t nr = L.agg ? L.agg[r] : r;
@@ -182,7 +182,7 @@ __global__ void k_jacobi_build(std::int32_t n, const std::uint32_t* __restrict__
         double a[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
         for (std::int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
             if (cols[e] == static_cast<std::uint32_t>(i)) {
-                for (int k = 0; k < 9; ++k) a[k] = blocks[k * U + e];  // SoA planes
+                for (int k = 0; k < 9; ++k) a[k] = blocks[blk(e, k)];
                 // adjugate inverse (Mat3::inverse), a column-major: A(r,c) = a[3c+r]
                 auto A = [&](int r, int c) { return a[3 * c + r]; };
                 double cof[9];

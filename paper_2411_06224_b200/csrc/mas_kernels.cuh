@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, doubl
 #pragma unroll
                 for (int t = 0; t < kRegs; ++t) {
                     const int j = lane + 32 * t;
-                    c[u][t] = (j < dim && u < dim) ? __ldg(M + static_cast<std::int64_t>(u) * dim + j) : 0.0;
+                    c[u][t] = (j < dim && u < dim) ? __ldcs(M + static_cast<std::int64_t>(u) * dim + j) : 0.0;
                 }
         }
         double b[kRegs], y[kRegs];
@@ -171,7 +171,10 @@ __global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, doubl
                     for (int t = 0; t < kRegs; ++t) {
                         const int j = lane + 32 * t;
                         const int kk = k + kU + u;
-                        nc[u][t] = (more && j < dim && kk < dim) ? __ldg(M + static_cast<std::int64_t>(kk) * dim + j)
+                        // inverses are streamed once per iteration: evict-first
+                        // (ld.global.cs) so they do not push A and the vectors
+                        // out of the 126 MB L2
+                        nc[u][t] = (more && j < dim && kk < dim) ? __ldcs(M + static_cast<std::int64_t>(kk) * dim + j)
                                                                   : 0.0;
                     }
 #pragma unroll

@@ -23,7 +23,8 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
                                                      const double* __restrict__ blocks, std::int64_t U,
                                                      const double* __restrict__ x, double* __restrict__ y,
                                                      double* __restrict__ partials, unsigned* __restrict__ ticket,
-                                                     double* __restrict__ dot_out, const int* __restrict__ flags) {
+                                                     double* __restrict__ dot_out, const int* __restrict__ flags,
+                                                     int dbg = 0) {
     if (flags && flags[0]) return;  // PCG already finished (F_DONE)
     const int lane = threadIdx.x & 31;
     const std::int64_t warp0 = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -44,7 +45,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
             nr = __ldg(rows + e);
             nc = __ldg(cols + e);
 #pragma unroll
-            for (int k = 0; k < 9; ++k) nh[k] = __ldg(blocks + k * U + e);  // SoA planes: coalesced
+            for (int k = 0; k < 9; ++k) nh[k] = __ldg(blocks + blk(e, k));  // one contiguous tile per chunk
         }
     };
     load(ch0);
@@ -57,13 +58,14 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
         const bool valid = r != 0xFFFFFFFFu;
         double yr0 = 0, yr1 = 0, yr2 = 0;
         if (valid) {
-            const double xc0 = __ldg(x + 3 * c), xc1 = __ldg(x + 3 * c + 1), xc2 = __ldg(x + 3 * c + 2);
+            const std::uint32_t cx = dbg == 3 ? r : c;  // dbg 3: no column gather
+            const double xc0 = __ldg(x + 3 * cx), xc1 = __ldg(x + 3 * cx + 1), xc2 = __ldg(x + 3 * cx + 2);
             // column-major H(i,j) = h[3j+i]
             yr0 = h[0] * xc0 + h[3] * xc1 + h[6] * xc2;
             yr1 = h[1] * xc0 + h[4] * xc1 + h[7] * xc2;
             yr2 = h[2] * xc0 + h[5] * xc1 + h[8] * xc2;
             const double xr0 = __ldg(x + 3 * r), xr1 = __ldg(x + 3 * r + 1), xr2 = __ldg(x + 3 * r + 2);
-            if (r != c) {
+            if (r != c && dbg != 1 && dbg != 2) {
                 const double yc0 = h[0] * xr0 + h[1] * xr1 + h[2] * xr2;
                 const double yc1 = h[3] * xr0 + h[4] * xr1 + h[5] * xr2;
                 const double yc2 = h[6] * xr0 + h[7] * xr1 + h[8] * xr2;
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
             }
         }
         const std::uint32_t rprev = __shfl_up_sync(0xffffffffu, r, 1);
-        if (valid && (lane == 0 || rprev != r)) {
+        if (valid && (lane == 0 || rprev != r) && dbg != 2) {
             atomicAdd(y + 3 * r, yr0);
             atomicAdd(y + 3 * r + 1, yr1);
             atomicAdd(y + 3 * r + 2, yr2);
@@ -132,6 +134,29 @@ void spmv_launch(Ctx& c, const double* d_x, double* d_y, bool zero_y, const int*
         k_spmv<false><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
                                                            nullptr, nullptr, nullptr, flags);
     ADIPC_LAUNCH_CHECK();
+}
+
+// Debug timing of the SpMV variants (0 normal, 1 no transposed scatter,
+// 2 no atomics, 3 no column gather): ms per launch over `iters` launches.
+float spmv_debug_time(Ctx& c, const double* d_x, double* d_y, int mode, int iters) {
+    cudaEvent_t e0, e1;
+    ADIPC_CUDA(cudaEventCreate(&e0));
+    ADIPC_CUDA(cudaEventCreate(&e1));
+    const int grid = spmv_grid(c);
+    for (int w = 0; w < 2; ++w)
+        k_spmv<false><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
+                                                           nullptr, nullptr, nullptr, nullptr, mode);
+    ADIPC_CUDA(cudaEventRecord(e0, c.stream));
+    for (int i = 0; i < iters; ++i)
+        k_spmv<false><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
+                                                           nullptr, nullptr, nullptr, nullptr, mode);
+    ADIPC_CUDA(cudaEventRecord(e1, c.stream));
+    ADIPC_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    ADIPC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms / iters;
 }
 
 void spmv(Ctx& c, const double* d_x, double* d_y, double*, int) {

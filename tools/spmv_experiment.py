@@ -1,0 +1,30 @@
+"""Profiling aid: time SpMV variants on the cfg5 matrix (normal, without the
+transposed scatter, without atomics, without the column gather) to attribute
+the SpMV time. Variants 1-3 compute wrong results by construction."""
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2411_06224_b200 import _lib, scenes  # noqa: E402
+from paper_2411_06224_b200.context import Context  # noqa: E402
+
+sc = scenes.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg5_stiff_box"]()
+ctx = Context(0)
+fk, fv = ctx.filter_pinned(sc.keys, sc.vals, sc.pinned)
+ctx.assemble(fk, fv, sc.n_blocks)
+n, U = ctx.matrix_info()
+x = torch.randn(3 * n, dtype=torch.float64, device="cuda")
+y = torch.empty_like(x)
+out = {"n": n, "U": U, "bytes": 80 * U + 48 * n}
+L = _lib.gpu()
+for mode in range(4):
+    ms = C.c_float()
+    ctx._check(L.adipc_gpu_debug_spmv_time(ctx.h, x.data_ptr(), y.data_ptr(), mode, 50, C.byref(ms)))
+    out[f"mode{mode}_us"] = ms.value * 1000
+    out[f"mode{mode}_gbs"] = out["bytes"] / (ms.value / 1000) / 1e9
+print(json.dumps(out))

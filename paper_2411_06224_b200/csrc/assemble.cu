@@ -424,8 +424,9 @@ void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std:
     ADIPC_CUDA(cudaMemcpyAsync(&U, out.row_ptr.p + n, sizeof(U), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaStreamSynchronize(st));
     out.U = U;
-    out.rows.reserve(static_cast<std::size_t>(U));
-    out.cols.reserve(static_cast<std::size_t>(U));
+    // whole 32-block tiles (the SpMV bulk-copies rows/cols per tile)
+    out.rows.reserve(static_cast<std::size_t>((U + 31) & ~std::int64_t(31)));
+    out.cols.reserve(static_cast<std::size_t>((U + 31) & ~std::int64_t(31)));
     out.blocks.reserve(blk_doubles(U));
     if (n > 0 && U > 0) {
         k_reduce_rows<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, out.row_ptr.p, n, d_vals,
@@ -465,8 +466,8 @@ void upload_matrix(Ctx& c, std::int32_t n, std::int64_t U, const std::uint32_t* 
     DeviceMatrix& A = c.A;
     A.n = n;
     A.U = U;
-    A.rows.reserve(U);
-    A.cols.reserve(U);
+    A.rows.reserve(static_cast<std::size_t>((U + 31) & ~std::int64_t(31)));
+    A.cols.reserve(static_cast<std::size_t>((U + 31) & ~std::int64_t(31)));
     A.blocks.reserve(blk_doubles(U));
     A.row_ptr.reserve(static_cast<std::size_t>(n) + 1);
     const cudaMemcpyKind kind = host_ptrs ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;

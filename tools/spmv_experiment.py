@@ -22,9 +22,9 @@ x = torch.randn(3 * n, dtype=torch.float64, device="cuda")
 y = torch.empty_like(x)
 out = {"n": n, "U": U, "bytes": 80 * U + 48 * n}
 L = _lib.gpu()
-for mode in range(4):
+for mode in (0, 1, 2, 3, 8, 9, 10):  # +8: L2 evicted before every launch (cold)
     ms = C.c_float()
-    ctx._check(L.adipc_gpu_debug_spmv_time(ctx.h, x.data_ptr(), y.data_ptr(), mode, 50, C.byref(ms)))
-    out[f"mode{mode}_us"] = ms.value * 1000
-    out[f"mode{mode}_gbs"] = out["bytes"] / (ms.value / 1000) / 1e9
+    ctx._check(L.adipc_gpu_debug_spmv_time(ctx.h, x.data_ptr(), y.data_ptr(), mode, 30, C.byref(ms)))
+    out[f"mode{mode}_us"] = round(ms.value * 1000, 2)
+    out[f"mode{mode}_gbs"] = round(out["bytes"] / (ms.value / 1000) / 1e9, 1)
 print(json.dumps(out))

@@ -114,11 +114,12 @@ class ClockSampler:
 def byte_model(n, U, levels):
     """Algorithmic (compulsory) bytes per PCG iteration by kernel class
     (DESIGN.md 'byte model'): fp64 values, u32/i32 indices,
-    explicit dense inverses as stored (full (3f)^2)."""
+    explicit inverses as stored (symmetric-packed, (3f)(3f+1)/2 doubles)."""
     inv, nodes, parts = [], [], []
     for L in levels:
         fill = np.bincount(L["part_of"], minlength=L["n_parts"]).astype(np.int64)
-        inv.append(int(np.sum((3 * fill) ** 2) * 8))
+        d = 3 * fill  # symmetric-packed inverses: d(d+1)/2 doubles, padded to even
+        inv.append(int(np.sum(((d * (d + 1) // 2 + 1) // 2) * 2) * 8))
         nodes.append(int(L["n_nodes"]))
         parts.append(int(L["n_parts"]))
     nl = len(levels)

@@ -117,6 +117,8 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
         L->rr.free();
         L->inv_off.free();
         L->inv.free();
+        L->dense.free();
+        L->dense_off.free();
         L->y.free();
     }
     c.levels.clear();
@@ -533,10 +535,12 @@ int adipc_gpu_precond_subdomain_inverse(adipc_gpu_ctx* ctx, int level, int32_t s
         sync(c);
         const int d = 3 * (sp[1] - sp[0]);
         if (dim) *dim = d;
-        if (out && d) {
-            ADIPC_CUDA(cudaMemcpyAsync(out, L.inv.p + off, 8 * static_cast<std::size_t>(d) * d, cudaMemcpyDeviceToHost,
-                                       c.stream));
+        if (out && d) {  // unpack the symmetric-packed storage to a full column-major matrix
+            std::vector<double> pk(static_cast<std::size_t>(packed_doubles(d)));
+            ADIPC_CUDA(cudaMemcpyAsync(pk.data(), L.inv.p + off, 8 * pk.size(), cudaMemcpyDeviceToHost, c.stream));
             sync(c);
+            for (int k = 0; k < d; ++k)
+                for (int j = 0; j < d; ++j) out[static_cast<std::size_t>(k) * d + j] = pk[packed_idx(j, k)];
         }
     });
 }

@@ -80,6 +80,17 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __host__ __device__ __forceinline__ std::int64_t blk(std::int64_t e, int k) { return (e >> 5) * 288 + 32 * k + (e & 31); }
 inline std::size_t blk_doubles(std::int64_t U) { return static_cast<std::size_t>((U + 31) >> 5) * 288; }
 
+// Symmetric-packed storage of a d x d subdomain inverse: upper triangle by
+// columns, entry (j, k), j <= k, at k(k+1)/2 + j; padded to an even count so
+// every inverse starts 16-byte aligned (one TMA bulk copy each).
+__host__ __device__ __forceinline__ std::int64_t packed_doubles(int d) {
+    const std::int64_t n = static_cast<std::int64_t>(d) * (d + 1) / 2;
+    return (n + 1) & ~std::int64_t(1);
+}
+__host__ __device__ __forceinline__ int packed_idx(int j, int k) {  // any order
+    return j <= k ? k * (k + 1) / 2 + j : j * (j + 1) / 2 + k;
+}
+
 // Block-wide sum of a double; result valid in thread 0. blockDim <= 1024.
 __device__ __forceinline__ double block_sum(double v, double* smem32) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

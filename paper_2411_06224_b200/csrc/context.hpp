@@ -52,8 +52,12 @@ struct DeviceLevel {
     DBuf<std::int32_t> upc_pos;    // children as positions inside this level's subdomain
     DBuf<double> rr;               // level >= 1: restricted residual per node (3 per node)
     std::vector<std::int32_t> pos_host;
-    DBuf<std::int64_t> inv_off;    // subdomain -> offset of its dense (3f)^2 inverse
-    DBuf<double> inv;              // explicit dense inverses, column-major (symmetric)
+    DBuf<std::int64_t> inv_off;    // subdomain -> offset of its packed inverse (16-byte aligned)
+    DBuf<double> inv;              // explicit inverses, symmetric-packed upper by columns
+    DBuf<std::int64_t> dense_off;  // subdomain -> offset of its dense restricted matrix (build scratch)
+    DBuf<double> dense;            // restricted matrices R A R^T, column-major (build scratch)
+    std::int64_t dense_doubles = 0;
+    std::vector<std::int64_t> inv_off_host;
     DBuf<double> y;                // level >= 1: per-node solution (3 per node)
     std::int64_t inv_doubles = 0;
     int max_fill = 0;

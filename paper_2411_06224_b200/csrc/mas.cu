@@ -28,7 +28,7 @@ struct RestrictLevel {
     const std::int32_t* agg;      // null at level 0 (identity)
     const std::int32_t* part_of;
     const std::int32_t* pos_of;
-    const std::int64_t* inv_off;
+    const std::int64_t* dense_off;
     const std::int32_t* sub_ptr;
     double* dense;
 };
@@ -68,7 +68,7 @@ __global__ void k_restrict(const std::uint32_t* __restrict__ rows, const std::ui
             const std::int32_t s = L.part_of[nr];
             if (s != L.part_of[nc]) continue;
             const int dim = 3 * (L.sub_ptr[s + 1] - L.sub_ptr[s]);
-            double* D = L.dense + L.inv_off[s];
+            double* D = L.dense + L.dense_off[s];
             const int pr = L.pos_of[nr], pc = L.pos_of[nc];
             const bool atomic = l > 0;
             add_tile(D, dim, pr, pc, h, false, atomic);
@@ -77,12 +77,15 @@ __global__ void k_restrict(const std::uint32_t* __restrict__ rows, const std::ui
     }
 }
 
-// One CTA per subdomain: Cholesky with retry, then explicit inverse.
+// One CTA per subdomain: Cholesky with retry, then explicit inverse, written
+// symmetric-packed (upper triangle by columns: P[k(k+1)/2 + j] = D^-1(j,k),
+// j <= k) — half the bytes the PCG streams per application.
 // Work arrays S (dim x dim, column-major) + X (dim x dim) live in shared
 // memory, or — for subdomains too large for it (capacity > 32) — in a global
 // scratch slice per CTA (`gscratch`, 2 * max_dim^2 doubles per CTA).
 __global__ void k_invert(std::int32_t n_parts, const std::int32_t* __restrict__ sub_ptr,
-                         const std::int64_t* __restrict__ inv_off, double* __restrict__ dense,
+                         const std::int64_t* __restrict__ dense_off, const double* __restrict__ dense,
+                         const std::int64_t* __restrict__ inv_off, double* __restrict__ inv,
                          int* __restrict__ status, int* __restrict__ shifts, double* __restrict__ gscratch,
                          int max_dim) {
     extern __shared__ double sm[];
@@ -94,7 +97,8 @@ __global__ void k_invert(std::int32_t n_parts, const std::int32_t* __restrict__ 
         if (dim == 0) continue;
         double* S = work;
         double* X = work + dim * dim;
-        double* D = dense + inv_off[s];
+        const double* D = dense + dense_off[s];
+        double* P = inv + inv_off[s];
         const int nn = dim * dim;
         if (threadIdx.x == 0) {
             double tr = 0;
@@ -162,14 +166,13 @@ __global__ void k_invert(std::int32_t n_parts, const std::int32_t* __restrict__ 
             }
         }
         __syncthreads();
-        // D^-1 = X^T X, symmetric: compute lower, mirror
+        // D^-1 = X^T X, symmetric: entry (j, k), j <= k, into the packed upper
         for (int t = threadIdx.x; t < nn; t += blockDim.x) {
-            const int i = t % dim, j = t / dim;
-            if (j > i) continue;
+            const int j = t % dim, k = t / dim;
+            if (j > k) continue;
             double v = 0;
-            for (int k = i; k < dim; ++k) v += X[i * dim + k] * X[j * dim + k];
-            D[j * dim + i] = v;
-            D[i * dim + j] = v;
+            for (int q = k; q < dim; ++q) v += X[j * dim + q] * X[k * dim + q];
+            P[k * (k + 1) / 2 + j] = v;
         }
         __syncthreads();
     }
@@ -222,18 +225,24 @@ void build_level(Ctx& c, DeviceLevel& L, const host::Level& hl, int level, std::
     for (std::int32_t s = 0; s < hl.n_parts; ++s) max_fill = std::max(max_fill, sub_ptr[s + 1]);
     for (std::int32_t s = 0; s < hl.n_parts; ++s) sub_ptr[s + 1] += sub_ptr[s];
     for (std::int32_t v = 0; v < hl.n_nodes; ++v) sub_nodes[sub_ptr[hl.part_of[v]] + pos_of[v]] = v;
-    std::vector<std::int64_t> inv_off(hl.n_parts + 1, 0);
+    // dense restricted matrices (build scratch, full d x d) and the packed
+    // inverses (d(d+1)/2, padded to 16 B so each is one TMA bulk copy)
+    std::vector<std::int64_t> inv_off(hl.n_parts + 1, 0), dense_off(hl.n_parts + 1, 0);
     for (std::int32_t s = 0; s < hl.n_parts; ++s) {
         const std::int64_t d = 3 * static_cast<std::int64_t>(sub_ptr[s + 1] - sub_ptr[s]);
-        inv_off[s + 1] = inv_off[s] + d * d;
+        dense_off[s + 1] = dense_off[s] + d * d;
+        inv_off[s + 1] = inv_off[s] + packed_doubles(static_cast<int>(d));
     }
     L.max_fill = max_fill;
     L.inv_doubles = inv_off[hl.n_parts];
+    L.dense_doubles = dense_off[hl.n_parts];
     upload(L.part_of, hl.part_of, st);
     upload(L.pos_of, pos_of, st);
     upload(L.sub_ptr, sub_ptr, st);
     upload(L.sub_nodes, sub_nodes, st);
     upload(L.inv_off, inv_off, st);
+    upload(L.dense_off, dense_off, st);
+    L.inv_off_host = std::move(inv_off);
     if (level > 0) {
         upload(L.agg, hl.agg, st);
         L.y.reserve(3 * static_cast<std::size_t>(hl.n_nodes));
@@ -242,6 +251,8 @@ void build_level(Ctx& c, DeviceLevel& L, const host::Level& hl, int level, std::
     L.pos_host = std::move(pos_of);
     L.inv.reserve(static_cast<std::size_t>(L.inv_doubles));
     ADIPC_CUDA(cudaMemsetAsync(L.inv.p, 0, sizeof(double) * std::max<std::int64_t>(L.inv_doubles, 1), st));
+    L.dense.reserve(static_cast<std::size_t>(L.dense_doubles));
+    ADIPC_CUDA(cudaMemsetAsync(L.dense.p, 0, sizeof(double) * std::max<std::int64_t>(L.dense_doubles, 1), st));
 }
 
 // Restriction metadata from level l to l+1 (see mas_kernels.cuh): the
@@ -283,7 +294,8 @@ void factorize(Ctx& c) {
     ra.n_levels = static_cast<int>(c.levels.size());
     for (int l = 0; l < ra.n_levels; ++l) {
         DeviceLevel& L = *c.levels[l];
-        ra.lv[l] = RestrictLevel{l > 0 ? L.agg.p : nullptr, L.part_of.p, L.pos_of.p, L.inv_off.p, L.sub_ptr.p, L.inv.p};
+        ra.lv[l] = RestrictLevel{l > 0 ? L.agg.p : nullptr, L.part_of.p, L.pos_of.p, L.dense_off.p, L.sub_ptr.p,
+                                 L.dense.p};
     }
     if (A.U > 0) {
         k_restrict<<<grid_for(A.U, 256, 16), 256, 0, st>>>(A.rows.p, A.cols.p, A.blocks.p, A.U, ra);
@@ -302,7 +314,8 @@ void factorize(Ctx& c) {
         if (!in_smem) c.invert_scratch.reserve(need / sizeof(double) * grid);
         const std::size_t smem = in_smem ? need : 0;
         ADIPC_CUDA(cudaFuncSetAttribute(k_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        k_invert<<<grid, threads, smem, st>>>(L.n_parts, L.sub_ptr.p, L.inv_off.p, L.inv.p, c.build_status.p,
+        k_invert<<<grid, threads, smem, st>>>(L.n_parts, L.sub_ptr.p, L.dense_off.p, L.dense.p, L.inv_off.p, L.inv.p,
+                                              c.build_status.p,
                                               c.build_status.p + 1, in_smem ? nullptr : c.invert_scratch.p, dim);
         ADIPC_LAUNCH_CHECK();
     }
@@ -399,7 +412,7 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
         c.hier_version = c.cache_hierarchy ? phash : ~0ull;
     } else {
         for (auto& L : c.levels)
-            ADIPC_CUDA(cudaMemsetAsync(L->inv.p, 0, sizeof(double) * std::max<std::int64_t>(L->inv_doubles, 1), st));
+            ADIPC_CUDA(cudaMemsetAsync(L->dense.p, 0, sizeof(double) * std::max<std::int64_t>(L->dense_doubles, 1), st));
     }
     const auto t1 = std::chrono::steady_clock::now();
     c.ms_build_host = std::chrono::duration<float, std::milli>(t1 - t0).count();
@@ -425,9 +438,9 @@ void build_mas_from_hierarchy(Ctx& c, const host::MasHierarchy& h) {
 // launch helpers shared with pcg.cu
 int level_grid(const Ctx& c, int l) {
     const DeviceLevel& L = *c.levels[l];
-    // one subdomain per warp (8 per CTA), no grid-stride: the block scheduler
-    // balances the memory-bound warps; fills > 32 take a CTA each
-    const std::int64_t per = L.max_fill > 32 ? 1 : 8;
+    // one subdomain per warp (kLevelWarps per CTA), no grid-stride: the block
+    // scheduler balances the memory-bound warps; fills > 32 take a CTA each
+    const std::int64_t per = L.max_fill > 32 ? 1 : kLevelWarps;
     return static_cast<int>(std::max<std::int64_t>(1, ceil_div(L.n_parts, per)));
 }
 int slot_grid(const Ctx& c) { return grid_for(3 * static_cast<std::int64_t>(c.A.n), 256, 8); }
@@ -472,12 +485,28 @@ void launch_level(Ctx& c, int l, const double* r_in, double* z, const PcgArgs& a
         ADIPC_CUDA(cudaFuncSetAttribute(k_mas_level_big<kMode, kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
         k_mas_level_big<kMode, kSolve><<<grid, 128, smem, st>>>(la, a, partials, ticket, dot_out);
-    } else if (regs == 1) {
-        k_mas_level<kMode, 1, kSolve><<<grid, 256, 0, st>>>(la, a, partials, ticket, dot_out);
-    } else if (regs == 2) {
-        k_mas_level<kMode, 2, kSolve><<<grid, 256, 0, st>>>(la, a, partials, ticket, dot_out);
     } else {
-        k_mas_level<kMode, 3, kSolve><<<grid, 256, 0, st>>>(la, a, partials, ticket, dot_out);
+        const int ws = static_cast<int>(level_warp_smem(kSolve ? 3 * L.max_fill : 0, regs));
+        const std::size_t smem = static_cast<std::size_t>(kLevelWarps) * ws;
+        const int block = 32 * kLevelWarps;
+#define ADIPC_LVL(R)                                                                                           \
+    do {                                                                                                       \
+        static bool attr = false;                                                                              \
+        if (!attr) {                                                                                           \
+            ADIPC_CUDA(cudaFuncSetAttribute(k_mas_level<kMode, R, kSolve>,                                     \
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,                       \
+                                            static_cast<int>(kLevelWarps * level_warp_smem(32 * R, R))));      \
+            attr = true;                                                                                       \
+        }                                                                                                      \
+        k_mas_level<kMode, R, kSolve><<<grid, block, smem, st>>>(la, a, partials, ticket, dot_out, ws);        \
+    } while (0)
+        if (regs == 1)
+            ADIPC_LVL(1);
+        else if (regs == 2)
+            ADIPC_LVL(2);
+        else
+            ADIPC_LVL(3);
+#undef ADIPC_LVL
     }
     ADIPC_LAUNCH_CHECK();
 }

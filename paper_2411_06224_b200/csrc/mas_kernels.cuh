@@ -7,13 +7,19 @@
 // nests: every level-(l+1) node is a connected piece of ONE level-l
 // subdomain, and the ids of the level-(l+1) nodes of subdomain s are
 // consecutive (hierarchy.hpp:53-72 visits subdomains in order). So the warp
-// that solves level-l subdomain s already holds b_l for all the children of
+// that handles level-l subdomain s already holds b_l for all the children of
 // its level-(l+1) nodes and emits r_{l+1} for them — one small parallel launch
 // per level, no long per-lane loops over slots. Summation order is a tree
 // instead of the reference's slot order (rounding-level difference).
+//
+// Subdomain inverses are stored symmetric-packed (packed_idx, common.cuh) and
+// staged into shared memory with one TMA bulk copy per subdomain
+// (cp.async.bulk + mbarrier, L2 evict-first: streamed once per application),
+// issued before the residual gather so the copy overlaps it.
 #pragma once
 
 #include "context.hpp"
+#include "tma.cuh"
 
 namespace adipc_gpu {
 
@@ -59,8 +65,8 @@ struct LevelArgs {
     std::int32_t n_parts;
     const std::int32_t* sub_ptr;    // subdomain -> first member node
     const std::int32_t* sub_nodes;  // members (level 0: slots), ascending
-    const std::int64_t* inv_off;
-    const double* inv;              // explicit inverses, column-major dim x dim
+    const std::int64_t* inv_off;    // packed-inverse offsets (16-byte aligned)
+    const double* inv;              // packed explicit inverses
     const double* r_in;             // M_COARSE: restricted residual per node (3 per node)
     double* out;                    // level 0: z per slot; coarse: y per node
     // restriction to the next level (null at the top level)
@@ -109,38 +115,46 @@ __device__ __forceinline__ double gather_r(const PcgArgs& a, const double* r_in,
     return rv;
 }
 
-// One warp per subdomain (dim = 3 f <= 32 kRegs): gather b, y = D^-1 b with
-// the inverse read column by column (coalesced), store y, emit the next
-// level's restricted residual from b (smem), dot partial b.y.
+constexpr int kLevelWarps = 4;  // warps (= subdomains) per CTA of the level kernels
+
+// Bytes of dynamic shared memory per warp of k_mas_level for a level whose
+// largest subdomain has dimension max_dim: packed inverse + b + mbarrier.
+inline std::size_t level_warp_smem(int max_dim, int regs) {
+    const std::size_t inv = static_cast<std::size_t>(packed_doubles(max_dim)) * 8;
+    return ((inv + static_cast<std::size_t>(32 * regs) * 8 + 16 + 15) / 16) * 16;
+}
+
+// One warp per subdomain (dim = 3 f <= 32 kRegs), kLevelWarps per CTA:
+//   lane 0 bulk-copies the packed inverse into this warp's smem slot (kSolve),
+//   the warp gathers b (with the fused PCG vector update for level 0),
+//   waits for the copy, y = D^-1 b from smem (lane j owns rows j, j+32, ...),
+//   stores y, emits the next level's restricted residual, dot partial b.y.
 // kSolve = false: gather (with the fused PCG vector update) + restriction
 // only — the PCG's update pass, after which the level-0 solve and the coarse
 // chain run concurrently.
 template <int kMode, int kRegs, bool kSolve = true>
-__global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, double* __restrict__ partials,
-                                                  unsigned* __restrict__ ticket, double* __restrict__ dot_out) {
-    __shared__ double bsm[8][32 * kRegs];
+__global__ void __launch_bounds__(32 * kLevelWarps) k_mas_level(LevelArgs L, PcgArgs a, double* __restrict__ partials,
+                                                                unsigned* __restrict__ ticket,
+                                                                double* __restrict__ dot_out, int warp_smem) {
+    extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* Mw = reinterpret_cast<double*>(smem + static_cast<std::size_t>(w) * warp_smem);
+    double* bw = reinterpret_cast<double*>(smem + static_cast<std::size_t>(w + 1) * warp_smem) - 32 * kRegs - 2;
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(bw + 32 * kRegs);
     double alpha = 0;
     if (a.flags && a.flags[F_DONE]) return;
     if ((kMode == M_UPDATE || kMode == M_RESTART) && !pcg_alpha(a, alpha)) return;
     double dsum = 0;
-    const int wpb = blockDim.x >> 5;
-    for (std::int32_t s = blockIdx.x * wpb + w; s < L.n_parts; s += gridDim.x * wpb) {
+    const std::int32_t s = blockIdx.x * kLevelWarps + w;
+    if (s < L.n_parts) {
         const std::int32_t s0 = L.sub_ptr[s];
         const int dim = 3 * (L.sub_ptr[s + 1] - s0);
-        constexpr int kU = 8;
-        const double* M = kSolve ? L.inv + L.inv_off[s] : nullptr;
-        // first batch of inverse columns issued before the (latency-bound)
-        // gather: the inverse does not depend on b
-        double c[kU][kRegs];
-        if (kSolve) {
-#pragma unroll
-            for (int u = 0; u < kU; ++u)
-#pragma unroll
-                for (int t = 0; t < kRegs; ++t) {
-                    const int j = lane + 32 * t;
-                    c[u][t] = (j < dim && u < dim) ? __ldcs(M + static_cast<std::int64_t>(u) * dim + j) : 0.0;
-                }
+        if (kSolve && lane == 0) {  // stage the packed inverse (overlaps the gather)
+            const std::uint32_t bytes = static_cast<std::uint32_t>(packed_doubles(dim) * 8);
+            mbar_init(bar, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(bar, bytes);
+            bulk_g2s_evict_first(Mw, L.inv + L.inv_off[s], bytes, bar);
         }
         double b[kRegs], y[kRegs];
         std::int64_t gi[kRegs];
@@ -155,38 +169,22 @@ __global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, doubl
                 b[t] = gather_r<kMode>(a, L.r_in, gi[t], alpha);
             }
         }
-        // b to shared memory (broadcast reads below; also feeds the restriction)
 #pragma unroll
-        for (int t = 0; t < kRegs; ++t) bsm[w][lane + 32 * t] = b[t];
+        for (int t = 0; t < kRegs; ++t) bw[lane + 32 * t] = b[t];
         __syncwarp();
         if (kSolve) {
-            // y = M b, columns streamed kU at a time, the next batch in flight
-            // while the current one is consumed (the inverse is read once)
-            for (int k = 0; k < dim; k += kU) {
-                double nc[kU][kRegs];
-                const bool more = k + kU < dim;
+            mbar_wait(bar, 0);
+            // y_j = sum_k D^-1(j, k) b_k over the packed upper triangle:
+            // k >= j reads column k (contiguous across lanes), k < j reads
+            // column j (triangular-number offsets: distinct banks per half-warp)
+            for (int k = 0; k < dim; ++k) {
+                const double bk = bw[k];
+                const int ck = k * (k + 1) / 2;
 #pragma unroll
-                for (int u = 0; u < kU; ++u)
-#pragma unroll
-                    for (int t = 0; t < kRegs; ++t) {
-                        const int j = lane + 32 * t;
-                        const int kk = k + kU + u;
-                        // inverses are streamed once per iteration: evict-first
-                        // (ld.global.cs) so they do not push A and the vectors
-                        // out of the 126 MB L2
-                        nc[u][t] = (more && j < dim && kk < dim) ? __ldcs(M + static_cast<std::int64_t>(kk) * dim + j)
-                                                                  : 0.0;
-                    }
-#pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const double bk = (k + u < dim) ? bsm[w][k + u] : 0.0;
-#pragma unroll
-                    for (int t = 0; t < kRegs; ++t) y[t] += c[u][t] * bk;
+                for (int t = 0; t < kRegs; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j < dim) y[t] += Mw[j <= k ? ck + j : j * (j + 1) / 2 + k] * bk;
                 }
-#pragma unroll
-                for (int u = 0; u < kU; ++u)
-#pragma unroll
-                    for (int t = 0; t < kRegs; ++t) c[u][t] = nc[u][t];
             }
 #pragma unroll
             for (int t = 0; t < kRegs; ++t)
@@ -202,10 +200,9 @@ __global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, doubl
                 const std::int32_t v = v0 + t / 3;
                 const int comp = t % 3;
                 double acc = 0;
-                for (std::int32_t q = L.upc_ptr[v]; q < L.upc_ptr[v + 1]; ++q) acc += bsm[w][3 * L.upc_pos[q] + comp];
+                for (std::int32_t q = L.upc_ptr[v]; q < L.upc_ptr[v + 1]; ++q) acc += bw[3 * L.upc_pos[q] + comp];
                 L.r_next[3 * static_cast<std::int64_t>(v) + comp] = acc;
             }
-            __syncwarp();
         }
     }
     if (dot_out) grid_sum_last_block(dsum, partials, ticket, dot_out);
@@ -213,7 +210,7 @@ __global__ void __launch_bounds__(256) k_mas_level(LevelArgs L, PcgArgs a, doubl
 
 // General-size variant (fill > 32, e.g. the exact single-domain
 // preconditioner of test_solver.cpp:99-111): one CTA per subdomain, b in
-// dynamic shared memory, any dim.
+// dynamic shared memory, packed inverse read from global, any dim.
 template <int kMode, bool kSolve = true>
 __global__ void __launch_bounds__(128) k_mas_level_big(LevelArgs L, PcgArgs a, double* __restrict__ partials,
                                                       unsigned* __restrict__ ticket, double* __restrict__ dot_out) {
@@ -231,7 +228,7 @@ __global__ void __launch_bounds__(128) k_mas_level_big(LevelArgs L, PcgArgs a, d
         const double* M = L.inv + L.inv_off[s];
         for (int j = threadIdx.x; kSolve && j < dim; j += blockDim.x) {
             double y = 0;
-            for (int k = 0; k < dim; ++k) y += M[static_cast<std::int64_t>(k) * dim + j] * bs[k];
+            for (int k = 0; k < dim; ++k) y += M[packed_idx(j, k)] * bs[k];
             L.out[3 * static_cast<std::int64_t>(L.sub_nodes[s0 + j / 3]) + (j % 3)] = y;
             dsum += bs[j] * y;
         }

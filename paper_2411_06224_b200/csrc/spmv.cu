@@ -1,34 +1,21 @@
 // Symmetric reduce-by-key block SpMV (SRBK, paper Alg. 4; reference
 // sparse/srbk_spmv.hpp:13-49): y = A x with A stored as its sorted upper block
-// triangle. Each warp owns 32 consecutive blocks at a time (the reference's
-// lane group of width 32): lane e computes H_e x[col] and, off the diagonal,
-// H_e^T x[row] (scattered with fp64 RED atomics to y[col]); the row
-// contributions are summed with a head-segmented shuffle reduction over the
-// warp's sorted rows and the run heads add them to y[row] atomically.
-//
-// Memory pipeline (B200): every warp streams a contiguous run of 32-block
-// tiles. Each tile (2,304 B of values in the tiled layout + 128 B rows +
-// 128 B cols) is staged into shared memory by TMA bulk copies
-// (cp.async.bulk + mbarrier) kStages tiles ahead of use, so the bytes in
-// flight per SM are set by shared memory (2 x 80 KB per SM), not registers.
+// triangle. Each warp owns 32 consecutive blocks (the reference's lane group
+// of width 32): lane e computes H_e x[col] and, off the diagonal, H_e^T x[row]
+// (scattered with fp64 RED atomics to y[col]); the row contributions are
+// summed with a head-segmented shuffle reduction over the warp's sorted rows
+// and the run heads add them to y[row] atomically.
 //
 // Optional fusion for PCG: the same pass accumulates p.(A p) directly from the
 // blocks, p_r.(H p_c) * (r != c ? 2 : 1), so the dot needs no second sweep
 // over Ap; the grid total is finished by the last CTA (deterministic order).
-#include <algorithm>
-
 #include "context.hpp"
-#include "tma.cuh"
 
 namespace adipc_gpu {
 
 namespace {
 
 constexpr int kSpmvThreads = 256;
-constexpr int kStages = 4;
-constexpr int kTileBytes = 32 * 9 * 8;                // values of 32 blocks
-constexpr int kStageBytes = kTileBytes + 2 * 32 * 4;  // + rows + cols
-constexpr int kSmemBytes = (kSpmvThreads / 32) * kStages * (kStageBytes + 8);
 
 template <bool kDot>
 __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __restrict__ rows,
@@ -37,51 +24,38 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
                                                      const double* __restrict__ x, double* __restrict__ y,
                                                      double* __restrict__ partials, unsigned* __restrict__ ticket,
                                                      double* __restrict__ dot_out, const int* __restrict__ flags,
-                                                     int dbg) {
-    extern __shared__ __align__(128) unsigned char smem[];
+                                                     int dbg = 0) {
     if (flags && flags[0]) return;  // PCG already finished (F_DONE)
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int nw = blockDim.x >> 5;
-    unsigned char* wbuf = smem + static_cast<std::size_t>(w) * kStages * kStageBytes;
-    std::uint64_t* bars =
-        reinterpret_cast<std::uint64_t*>(smem + static_cast<std::size_t>(nw) * kStages * kStageBytes) + w * kStages;
-    const std::int64_t warp0 = static_cast<std::int64_t>(blockIdx.x) * nw + w;
-    const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * nw;
+    const int lane = threadIdx.x & 31;
+    const std::int64_t warp0 = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    // each warp owns a contiguous run of 32-block chunks (row locality for the
+    // x gathers and y atomics); software-pipelined: the next chunk's indices
+    // and block planes are in flight while the current chunk is processed
     const std::int64_t n_chunks = (U + 31) >> 5;
     const std::int64_t ch0 = warp0 * n_chunks / nwarps, ch1 = (warp0 + 1) * n_chunks / nwarps;
-    if (lane == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    auto issue = [&](std::int64_t ch, int s) {  // lane 0 only
-        unsigned char* st = wbuf + s * kStageBytes;
-        mbar_arrive_expect_tx(&bars[s], kStageBytes);
-        bulk_g2s(st, blocks + ch * 288, kTileBytes, &bars[s]);
-        bulk_g2s(st + kTileBytes, rows + (ch << 5), 128, &bars[s]);
-        bulk_g2s(st + kTileBytes + 128, cols + (ch << 5), 128, &bars[s]);
-    };
-    if (lane == 0)
-        for (int s = 0; s < kStages && ch0 + s < ch1; ++s) issue(ch0 + s, s);
     double dsum = 0;
-    int i = 0;
-    for (std::int64_t ch = ch0; ch < ch1; ++ch, ++i) {
-        const int s = i % kStages;
-        mbar_wait(&bars[s], static_cast<std::uint32_t>((i / kStages) & 1));
-        const unsigned char* st = wbuf + s * kStageBytes;
-        const double* ht = reinterpret_cast<const double*>(st);
+    std::uint32_t nr = 0xFFFFFFFFu, nc = 0;
+    double nh[9];
+    auto load = [&](std::int64_t ch) {
+        const std::int64_t e = (ch << 5) + lane;
+        nr = 0xFFFFFFFFu;
+        nc = 0;
+        if (ch < ch1 && e < U) {
+            nr = __ldg(rows + e);
+            nc = __ldg(cols + e);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) nh[k] = __ldg(blocks + blk(e, k));  // one contiguous tile per chunk
+        }
+    };
+    load(ch0);
+    for (std::int64_t ch = ch0; ch < ch1; ++ch) {
+        const std::uint32_t r = nr, c = nc;
         double h[9];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) h[k] = ht[32 * k + lane];
-        const std::int64_t e = (ch << 5) + lane;
-        const bool valid = e < U;
-        const std::uint32_t r = valid ? reinterpret_cast<const std::uint32_t*>(st + kTileBytes)[lane] : 0xFFFFFFFFu;
-        const std::uint32_t c = valid ? reinterpret_cast<const std::uint32_t*>(st + kTileBytes + 128)[lane] : 0u;
-        __syncwarp();
-        if (lane == 0 && ch + kStages < ch1) {  // refill this stage kStages tiles ahead
-            fence_proxy_async();
-            issue(ch + kStages, s);
-        }
+        for (int k = 0; k < 9; ++k) h[k] = nh[k];
+        load(ch + 1);
+        const bool valid = r != 0xFFFFFFFFu;
         double yr0 = 0, yr1 = 0, yr2 = 0;
         if (valid) {
             const std::uint32_t cx = dbg == 3 ? r : c;  // dbg 3: no column gather
@@ -124,24 +98,14 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
     if (kDot) grid_sum_last_block(dsum, partials, ticket, dot_out);
 }
 
-template <bool kDot>
-void set_smem_attr() {
-    static bool done = false;
-    if (!done) {
-        ADIPC_CUDA(cudaFuncSetAttribute(k_spmv<kDot>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-        done = true;
-    }
-}
-
 }  // namespace
 
 // One wave: SMs x resident CTAs per SM (each warp then streams one contiguous
-// run of tiles through its TMA ring).
+// run of chunks with its software pipeline).
 int spmv_grid(const Ctx& c) {
     static int occ = 0;
     if (occ == 0) {
-        set_smem_attr<true>();
-        ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<true>, kSpmvThreads, kSmemBytes));
+        ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<true>, kSpmvThreads, 0));
         if (occ < 1) occ = 1;
     }
     int sms = kSMs;
@@ -163,38 +127,34 @@ void spmv_launch(Ctx& c, const double* d_x, double* d_y, bool zero_y, const int*
         return;
     }
     const int grid = spmv_grid(c);
-    if (dot_out) {
-        set_smem_attr<true>();
-        k_spmv<true><<<grid, kSpmvThreads, kSmemBytes, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x,
-                                                                   d_y, partials, ticket, dot_out, flags, 0);
-    } else {
-        set_smem_attr<false>();
-        k_spmv<false><<<grid, kSpmvThreads, kSmemBytes, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x,
-                                                                    d_y, nullptr, nullptr, nullptr, flags, 0);
-    }
+    if (dot_out)
+        k_spmv<true><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
+                                                          partials, ticket, dot_out, flags);
+    else
+        k_spmv<false><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
+                                                           nullptr, nullptr, nullptr, flags);
     ADIPC_LAUNCH_CHECK();
 }
 
 // Debug timing of the SpMV variants (0 normal, 1 no transposed scatter,
 // 2 no atomics, 3 no column gather): ms per launch over `iters` launches.
-// `cold`: evict L2 before every launch (a 256 MB write), as inside PCG where
-// the MAS inverses stream through L2 between SpMVs.
+// (A TMA bulk-copy ring variant measured slower in situ: 95 vs 81 us at cfg5;
+// the SpMV is not limited by bytes in flight.)
 float spmv_debug_time(Ctx& c, const double* d_x, double* d_y, int mode, int iters) {
-    const bool cold = mode >= 8;
+    const bool cold = mode >= 8;  // +8: evict L2 (256 MB write) before every launch, as inside PCG
     mode &= 7;
     cudaEvent_t e0, e1;
     ADIPC_CUDA(cudaEventCreate(&e0));
     ADIPC_CUDA(cudaEventCreate(&e1));
     const int grid = spmv_grid(c);
-    set_smem_attr<false>();
     DBuf<char> flush;
     if (cold) flush.reserve(256u << 20);
     float total = 0;
     for (int i = -2; i < iters; ++i) {
         if (cold) ADIPC_CUDA(cudaMemsetAsync(flush.p, i & 0xff, 256u << 20, c.stream));
         ADIPC_CUDA(cudaEventRecord(e0, c.stream));
-        k_spmv<false><<<grid, kSpmvThreads, kSmemBytes, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x,
-                                                                    d_y, nullptr, nullptr, nullptr, nullptr, mode);
+        k_spmv<false><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
+                                                           nullptr, nullptr, nullptr, nullptr, mode);
         ADIPC_CUDA(cudaEventRecord(e1, c.stream));
         ADIPC_CUDA(cudaEventSynchronize(e1));
         float ms = 0;

@@ -45,6 +45,7 @@ extern "C" {
 
 #define ADIPC_OPT_CACHE_HIERARCHY 1 /* reuse the MAS hierarchy while the sparsity is unchanged */
 #define ADIPC_OPT_PROFILE 2         /* time each PCG kernel class with CUDA events */
+#define ADIPC_OPT_L2_PERSIST 3      /* value/1024 of the matrix tiles kept L2-resident (evict-last) across SpMVs */
 
 typedef struct adipc_gpu_ctx adipc_gpu_ctx;
 typedef struct adipc_hierarchy adipc_hierarchy;

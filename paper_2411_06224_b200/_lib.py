@@ -24,6 +24,7 @@ OK, INVALID_ARGUMENT, INDEFINITE, CUDA_ERROR = 0, 1, 2, 3
 PRECOND_MAS, PRECOND_JACOBI = 1, 2
 OPT_CACHE_HIERARCHY = 1
 OPT_PROFILE = 2
+OPT_L2_PERSIST = 3
 
 # Every symbol include/adipc_gpu.h declares, with its ctypes signature.
 GPU_SIGNATURES = {

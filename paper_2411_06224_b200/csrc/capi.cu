@@ -129,6 +129,9 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.w.flags.free();
     for (auto e : c.prof_events) cudaEventDestroy(e);
     if (c.side) cudaStreamDestroy(c.side);
+    if (c.h_flags) cudaFreeHost(c.h_flags);
+    for (auto e : c.ev_chunk)
+        if (e) cudaEventDestroy(e);
     if (c.ev_fork) cudaEventDestroy(c.ev_fork);
     if (c.ev_join) cudaEventDestroy(c.ev_join);
     if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
@@ -159,6 +162,15 @@ int adipc_gpu_set_option(adipc_gpu_ctx* ctx, int option, int value) {
             ctx->c.cache_hierarchy = value != 0;
         else if (option == ADIPC_OPT_PROFILE)
             ctx->c.profile = value != 0;
+        else if (option == ADIPC_OPT_L2_PERSIST) {
+            if (value < 0 || value > 1024) throw StatusError(kInvalidArgument, "L2 persist fraction out of [0, 1024]");
+            ctx->c.l2_persist_1024 = value;
+            if (value > 0) {  // allow evict-last lines up to the device's persisting set-aside maximum
+                int mx = 0;
+                ADIPC_CUDA(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, ctx->c.device));
+                ADIPC_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<std::size_t>(mx)));
+            }
+        }
         else
             throw StatusError(kInvalidArgument, "unknown option");
     });

@@ -111,6 +111,13 @@ struct Ctx {
     // with the level-0 solve inside each PCG iteration
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // asynchronous done-flag polling of the PCG chunks (pinned, double-buffered)
+    int* h_flags = nullptr;
+    cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
+
+    // fraction (x/1024) of A's tiles the SpMV loads with L2 evict-last
+    // priority (ADIPC_OPT_L2_PERSIST)
+    int l2_persist_1024 = 0;
 
     // per-kernel-class PCG timing (ADIPC_OPT_PROFILE): spmv, level 0, coarse, final
     bool profile = false;

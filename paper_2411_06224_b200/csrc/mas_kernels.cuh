@@ -36,7 +36,10 @@ enum Scal : int {
     S_RZ = 8,        // S_RZ + l: level-l share of r . z (Jacobi: level 0)
     S_COUNT = S_RZ + kMaxLevels
 };
-enum Flag : int { F_DONE = 0, F_ITERS = 1, F_CONVERGED = 2, F_COUNT = 8 };
+// F_K: index (1-based) of the iteration the next kernels execute; advanced by
+// the last CTA of the prolongation/p-update kernel, so an iteration's launch
+// sequence is identical every time (captured once as a CUDA graph).
+enum Flag : int { F_DONE = 0, F_ITERS = 1, F_CONVERGED = 2, F_K = 3, F_KTICKET = 4, F_COUNT = 8 };
 // last-block tickets / partial arrays: 0 spmv, 1 b.b, 2 + l level l
 enum Ticket : int { T_SPMV = 0, T_BB = 1, T_LEVEL = 2, T_COUNT = T_LEVEL + kMaxLevels };
 
@@ -56,8 +59,7 @@ struct PcgArgs {
     const double* ap;   // A p  (or A x in restart mode)
     const double* b;
     double* scal;
-    int* flags;
-    int k;              // iteration index (1-based), 0 in init
+    int* flags;         // F_* (the current iteration index is flags[F_K])
 };
 
 // One level of the hierarchy as the apply kernels see it.
@@ -79,12 +81,13 @@ struct LevelArgs {
 // alpha of iteration k; returns false (and records the termination like
 // pcg.hpp:61-66) when p.Ap lost positivity. All CTAs see the same scalars.
 __device__ __forceinline__ bool pcg_alpha(const PcgArgs& a, double& alpha) {
-    const double rho = a.scal[S_RHO0 + ((a.k - 1) & 1)];
+    const int k = a.flags[F_K];
+    const double rho = a.scal[S_RHO0 + ((k - 1) & 1)];
     const double pap = a.scal[S_PAP];
     if (!(pap > 0)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.flags[F_DONE] = 1;
-            a.flags[F_ITERS] = a.k - 1;
+            a.flags[F_ITERS] = k - 1;
             a.scal[S_REL] = sqrt(fabs(rho) / a.scal[S_RHO_INIT]);
         }
         return false;
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs p
                                                   double* __restrict__ p, double* __restrict__ ap, PcgArgs a) {
     double beta = 0;
     bool write_p = false;
+    int k = 0;
     if (kFinal != F_APPLY) {
         if (a.flags[F_DONE]) return;
         double rz = 0;
@@ -284,16 +288,17 @@ __global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs p
             }
             write_p = rz > 0;
         } else {
-            const double rho = a.scal[S_RHO0 + ((a.k - 1) & 1)];
+            k = a.flags[F_K];
+            const double rho = a.scal[S_RHO0 + ((k - 1) & 1)];
             const double stop = a.scal[S_STOP];
             if (blockIdx.x == 0 && threadIdx.x == 0) {
-                a.flags[F_ITERS] = a.k;
+                a.flags[F_ITERS] = k;
                 a.scal[S_REL] = sqrt(fabs(rz) / a.scal[S_RHO_INIT]);
                 if (rz <= stop) {
                     a.flags[F_DONE] = 1;
                     a.flags[F_CONVERGED] = 1;
                 } else {
-                    a.scal[S_RHO0 + (a.k & 1)] = rz;
+                    a.scal[S_RHO0 + (k & 1)] = rz;
                 }
             }
             if (rz <= stop) return;
@@ -313,6 +318,18 @@ __global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs p
         } else if (write_p) {
             p[g] = (kFinal == F_PCG_INIT) ? zz : zz + beta * p[g];
             ap[g] = 0.0;
+        }
+    }
+    if (kFinal == F_PCG_STEP) {  // the last CTA advances the iteration index
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            unsigned* ticket = reinterpret_cast<unsigned*>(a.flags + F_KTICKET);
+            if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+                a.flags[F_K] = k + 1;
+                *ticket = 0;
+                __threadfence();
+            }
         }
     }
 }

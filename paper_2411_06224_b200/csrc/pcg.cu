@@ -2,20 +2,23 @@
 // matrix and preconditioner of a context. One iteration is 2 + L launches,
 // each of which is also a grid-wide dependency point of the algorithm:
 //   1. SRBK SpMV  Ap = A p  with p.Ap fused (last CTA finishes the dot)
-//   2. level-0 MAS (or Jacobi): alpha = rho / p.Ap, x += alpha p,
-//      r -= alpha Ap, z0 = D0^-1 r per subdomain, r restricted to level 1,
-//      partial r.z0
-//   3. levels 1..L-1: dense solve of the restricted residual, restriction to
-//      the next level, partial r.z_l
+//   2. update pass (one warp per level-0 subdomain): alpha = rho / p.Ap,
+//      x += alpha p, r -= alpha Ap, restriction of r to level 1
+//   3. level-0 dense solves || coarse chain (levels 1..L-1, each solving and
+//      restricting to the next) on a high-priority side stream
 //   4. prolongation z = z0 + sum_l P_l y_l, rho' = r.z, convergence test,
-//      p = z + (rho'/rho) p, Ap cleared for the next SpMV.
-// Scalars (alpha, beta, dots, stop test) never leave the device; the host
-// polls the done flag once per chunk of iterations. Every kernel returns
-// immediately once the done flag is set, so over-issued iterations are
-// near-free. Termination semantics follow pcg.hpp exactly: x0 = 0, zero rhs
-// -> 0 iterations, !(rho0 > 0) -> not converged, !(pAp > 0) -> iters = k-1,
-// residual recomputed as b - A x every `restart` iterations, stop when
-// r.z <= tol^2 r0.z0.
+//      p = z + (rho'/rho) p, Ap cleared for the next SpMV, iteration index
+//      advanced on the device.
+// Scalars (alpha, beta, dots, stop test, iteration index) never leave the
+// device, so an iteration's launch sequence is identical every time: it is
+// captured once per solve as a CUDA graph (plus a restart variant) and
+// replayed. The host polls the done flag asynchronously, one chunk behind the
+// chunk it is enqueuing, so the GPU never drains between chunks; every kernel
+// returns immediately once the done flag is set, so over-issued iterations
+// are near-free. Termination semantics follow pcg.hpp exactly: x0 = 0, zero
+// rhs -> 0 iterations, !(rho0 > 0) -> not converged, !(pAp > 0) ->
+// iters = k-1, residual recomputed as b - A x every `restart` iterations, stop
+// when r.z <= tol^2 r0.z0.
 #include <algorithm>
 #include <cmath>
 
@@ -66,6 +69,13 @@ __global__ void k_zero(double* __restrict__ v, std::int64_t n, const int* __rest
         v[g] = 0;
 }
 
+struct GraphExec {
+    cudaGraphExec_t exec = nullptr;
+    ~GraphExec() {
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+
 }  // namespace
 
 PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters, double* d_x) {
@@ -88,10 +98,13 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
     w.tickets.reserve(T_COUNT);
     w.scal.reserve(S_COUNT);
     w.flags.reserve(F_COUNT);
+    if (!c.h_flags) ADIPC_CUDA(cudaMallocHost(&c.h_flags, 2 * F_COUNT * sizeof(int)));
     double* part = w.partials.p;
     auto partials_of = [&](int t) { return part + static_cast<std::size_t>(t) * pmax; };
     ADIPC_CUDA(cudaMemsetAsync(w.tickets.p, 0, sizeof(unsigned) * T_COUNT, st));
-    ADIPC_CUDA(cudaMemsetAsync(w.flags.p, 0, sizeof(int) * F_COUNT, st));
+    int h_flags0[F_COUNT] = {0};
+    h_flags0[F_K] = 1;
+    ADIPC_CUDA(cudaMemcpyAsync(w.flags.p, h_flags0, sizeof(h_flags0), cudaMemcpyHostToDevice, st));
     double h_scal[S_COUNT] = {0};
     h_scal[S_STOP] = rel_tol * rel_tol;
     ADIPC_CUDA(cudaMemcpyAsync(w.scal.p, h_scal, sizeof(h_scal), cudaMemcpyHostToDevice, st));
@@ -126,7 +139,6 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
     a.b = d_b;
     a.scal = w.scal.p;
     a.flags = w.flags.p;
-    a.k = 0;
     // MAS preconditioner application inside the iteration: after the update
     // pass (x, r and the level-1 restriction), the level-0 solve runs on the
     // solve stream while the latency-bound coarse chain (levels 1..L-1, each
@@ -159,12 +171,11 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
     }
     launch_final<F_PCG_INIT>(c, w.z.p, w.p.p, w.ap.p, a);
 
-    int h_flags[F_COUNT] = {0};
-    const int chunk = 16;
     // optional per-kernel-class timing (ADIPC_OPT_PROFILE): events bracket the
-    // SpMV, level-0, coarse-level and prolongation/update launches of every
-    // iteration on the solve stream; summed after each chunk's sync.
+    // SpMV, update, preconditioner and prolongation/p-update launches of every
+    // iteration; iterations are then launched directly instead of as graphs.
     const bool prof = c.profile;
+    const int chunk = 16;
     if (prof) {
         if (c.prof_events.empty()) {
             c.prof_events.resize(static_cast<std::size_t>(chunk) * 5);
@@ -173,51 +184,82 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
         for (int q = 0; q < 4; ++q) c.prof_ms[q] = 0;
         c.prof_iters = 0;
     }
-    auto mark = [&](int it_in_chunk, int q) {
-        if (prof) ADIPC_CUDA(cudaEventRecord(c.prof_events[5 * it_in_chunk + q], st));
+    auto mark = [&](int slot, int q) {
+        if (prof) ADIPC_CUDA(cudaEventRecord(c.prof_events[5 * slot + q], st));
     };
-    for (int k = 1; k <= max_iters;) {
-        const int kend = std::min(max_iters, k + chunk - 1);
-        const int kbeg = k;
-        for (; k <= kend; ++k) {
-            a.k = k;
-            mark(k - kbeg, 0);
-            // 1. Ap = A p, p.Ap
-            spmv_launch(c, w.p.p, w.ap.p, false, w.flags.p, partials_of(T_SPMV), w.tickets.p + T_SPMV,
-                        w.scal.p + S_PAP);
-            mark(k - kbeg, 1);
-            const bool is_restart = restart > 0 && k % restart == 0;
-            if (is_restart) {  // x += alpha p; r = b - A x
-                k_x_update<<<slot_grid(c), 256, 0, st>>>(n3, a);
-                ADIPC_LAUNCH_CHECK();
-                k_zero<<<slot_grid(c), 256, 0, st>>>(w.tmp.p, n3, w.flags.p);
-                ADIPC_LAUNCH_CHECK();
-                spmv_launch(c, d_x, w.tmp.p, false, w.flags.p, nullptr, nullptr, nullptr);
-                PcgArgs ar = a;
-                ar.ap = w.tmp.p;
-                if (mas)
-                    launch_level<M_RESTART, false>(c, 0, nullptr, nullptr, ar, nullptr, nullptr, nullptr, st, true);
-                else
-                    launch_jacobi<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
-                                             w.scal.p + S_RZ);
-            } else {
-                if (mas)
-                    launch_level<M_UPDATE, false>(c, 0, nullptr, nullptr, a, nullptr, nullptr, nullptr, st, true);
-                else
-                    launch_jacobi<M_UPDATE>(c, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
-                                            w.scal.p + S_RZ);
-            }
-            mark(k - kbeg, 2);
-            if (mas) mas_apply(a);
-            mark(k - kbeg, 3);
-            launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
-            mark(k - kbeg, 4);
+    // one iteration's launch sequence (restart variant: x += alpha p, r = b - A x)
+    auto iteration = [&](bool is_restart, int slot) {
+        mark(slot, 0);
+        spmv_launch(c, w.p.p, w.ap.p, false, w.flags.p, partials_of(T_SPMV), w.tickets.p + T_SPMV, w.scal.p + S_PAP);
+        mark(slot, 1);
+        if (is_restart) {
+            k_x_update<<<slot_grid(c), 256, 0, st>>>(n3, a);
+            ADIPC_LAUNCH_CHECK();
+            k_zero<<<slot_grid(c), 256, 0, st>>>(w.tmp.p, n3, w.flags.p);
+            ADIPC_LAUNCH_CHECK();
+            spmv_launch(c, d_x, w.tmp.p, false, w.flags.p, nullptr, nullptr, nullptr);
+            PcgArgs ar = a;
+            ar.ap = w.tmp.p;
+            if (mas)
+                launch_level<M_RESTART, false>(c, 0, nullptr, nullptr, ar, nullptr, nullptr, nullptr, st, true);
+            else
+                launch_jacobi<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
+                                         w.scal.p + S_RZ);
+        } else {
+            if (mas)
+                launch_level<M_UPDATE, false>(c, 0, nullptr, nullptr, a, nullptr, nullptr, nullptr, st, true);
+            else
+                launch_jacobi<M_UPDATE>(c, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
+                                        w.scal.p + S_RZ);
         }
-        ADIPC_CUDA(cudaMemcpyAsync(h_flags, w.flags.p, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
-        ADIPC_CUDA(cudaStreamSynchronize(st));
-        if (prof) {
-            // iterations of this chunk that did work (the rest returned early)
-            const int last = h_flags[F_DONE] ? std::min(kend, std::max(h_flags[F_ITERS], kbeg)) : kend;
+        mark(slot, 2);
+        if (mas) mas_apply(a);
+        mark(slot, 3);
+        launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
+        mark(slot, 4);
+    };
+    // capture the two iteration variants as graphs (non-profiled runs)
+    GraphExec g_norm, g_rest;
+    if (!prof) {
+        auto capture = [&](bool is_restart, GraphExec& g) {
+            cudaGraph_t graph;
+            ADIPC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            try {
+                iteration(is_restart, 0);
+            } catch (...) {
+                cudaStreamEndCapture(st, &graph);
+                throw;
+            }
+            ADIPC_CUDA(cudaStreamEndCapture(st, &graph));
+            ADIPC_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+            ADIPC_CUDA(cudaGraphDestroy(graph));
+        };
+        capture(false, g_norm);
+        if (restart > 0 && restart <= max_iters) capture(true, g_rest);
+    }
+
+    // chunks of iterations; the done flag of chunk i is checked while chunk
+    // i+1 is already queued (h_flags double-buffered in pinned memory)
+    int* hf[2] = {c.h_flags, c.h_flags + F_COUNT};
+    if (!c.ev_chunk[0])
+        for (auto& e : c.ev_chunk) ADIPC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int k = 1, ci = 0;
+    bool done = false;
+    while (!done && k <= max_iters) {
+        const int kbeg = k, kend = std::min(max_iters, k + chunk - 1);
+        for (; k <= kend; ++k) {
+            const bool is_restart = restart > 0 && k % restart == 0;
+            if (prof)
+                iteration(is_restart, k - kbeg);
+            else
+                ADIPC_CUDA(cudaGraphLaunch(is_restart ? g_rest.exec : g_norm.exec, st));
+        }
+        ADIPC_CUDA(cudaMemcpyAsync(hf[ci & 1], w.flags.p, F_COUNT * sizeof(int), cudaMemcpyDeviceToHost, st));
+        ADIPC_CUDA(cudaEventRecord(c.ev_chunk[ci & 1], st));
+        if (prof) {  // profiling: synchronous per chunk (events are reused)
+            ADIPC_CUDA(cudaEventSynchronize(c.ev_chunk[ci & 1]));
+            const int* f = hf[ci & 1];
+            const int last = f[F_DONE] ? std::min(kend, std::max(f[F_ITERS], kbeg)) : kend;
             for (int kk = kbeg; kk <= last; ++kk) {
                 for (int q = 0; q < 4; ++q) {
                     float ms = 0;
@@ -227,19 +269,24 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
                 }
                 ++c.prof_iters;
             }
+            done = f[F_DONE] != 0;
+        } else if (ci > 0) {  // check the previous chunk while this one runs
+            ADIPC_CUDA(cudaEventSynchronize(c.ev_chunk[(ci - 1) & 1]));
+            done = hf[(ci - 1) & 1][F_DONE] != 0;
         }
-        if (h_flags[F_DONE]) break;
+        ++ci;
     }
     ADIPC_CUDA(cudaEventRecord(e1, st));
-    ADIPC_CUDA(cudaMemcpyAsync(h_flags, w.flags.p, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
+    int h_final[F_COUNT];
+    ADIPC_CUDA(cudaMemcpyAsync(h_final, w.flags.p, sizeof(h_final), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaMemcpyAsync(h_scal, w.scal.p, sizeof(h_scal), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaStreamSynchronize(st));
     ADIPC_CUDA(cudaEventElapsedTime(&c.ms_pcg, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (h_flags[F_DONE]) {
-        out.iters = h_flags[F_ITERS];
-        out.converged = h_flags[F_CONVERGED];
+    if (h_final[F_DONE]) {
+        out.iters = h_final[F_ITERS];
+        out.converged = h_final[F_CONVERGED];
         out.rel_residual = h_scal[S_REL];
     } else {  // ran out of iterations (pcg.hpp:86-87)
         out.iters = max_iters;

@@ -10,6 +10,7 @@
 // blocks, p_r.(H p_c) * (r != c ? 2 : 1), so the dot needs no second sweep
 // over Ap; the grid total is finished by the last CTA (deterministic order).
 #include "context.hpp"
+#include "tma.cuh"
 
 namespace adipc_gpu {
 
@@ -24,9 +25,14 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
                                                      const double* __restrict__ x, double* __restrict__ y,
                                                      double* __restrict__ partials, unsigned* __restrict__ ticket,
                                                      double* __restrict__ dot_out, const int* __restrict__ flags,
-                                                     int dbg = 0) {
+                                                     int dbg = 0, int persist_1024 = 0) {
     if (flags && flags[0]) return;  // PCG already finished (F_DONE)
     const int lane = threadIdx.x & 31;
+    // L2 residency control: the first persist_1024/1024 of A's tiles are
+    // loaded evict-last so they survive in the 126 MB L2 from one SpMV to the
+    // next (the MAS inverses stream evict-first in between); the rest
+    // evict-first.
+    const std::uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
     const std::int64_t warp0 = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
     // each warp owns a contiguous run of 32-block chunks (row locality for the
@@ -42,10 +48,12 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
         nr = 0xFFFFFFFFu;
         nc = 0;
         if (ch < ch1 && e < U) {
-            nr = __ldg(rows + e);
-            nc = __ldg(cols + e);
+            const std::uint64_t pol = (ch * 1024 < static_cast<std::int64_t>(persist_1024) * n_chunks) ? pol_keep
+                                                                                                      : pol_stream;
+            nr = ld_nc_policy(rows + e, pol);
+            nc = ld_nc_policy(cols + e, pol);
 #pragma unroll
-            for (int k = 0; k < 9; ++k) nh[k] = __ldg(blocks + blk(e, k));  // one contiguous tile per chunk
+            for (int k = 0; k < 9; ++k) nh[k] = ld_nc_policy(blocks + blk(e, k), pol);  // one contiguous tile
         }
     };
     load(ch0);
@@ -129,10 +137,10 @@ void spmv_launch(Ctx& c, const double* d_x, double* d_y, bool zero_y, const int*
     const int grid = spmv_grid(c);
     if (dot_out)
         k_spmv<true><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
-                                                          partials, ticket, dot_out, flags);
+                                                          partials, ticket, dot_out, flags, 0, c.l2_persist_1024);
     else
         k_spmv<false><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
-                                                           nullptr, nullptr, nullptr, flags);
+                                                           nullptr, nullptr, nullptr, flags, 0, c.l2_persist_1024);
     ADIPC_LAUNCH_CHECK();
 }
 
@@ -154,7 +162,7 @@ float spmv_debug_time(Ctx& c, const double* d_x, double* d_y, int mode, int iter
         if (cold) ADIPC_CUDA(cudaMemsetAsync(flush.p, i & 0xff, 256u << 20, c.stream));
         ADIPC_CUDA(cudaEventRecord(e0, c.stream));
         k_spmv<false><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
-                                                           nullptr, nullptr, nullptr, nullptr, mode);
+                                                           nullptr, nullptr, nullptr, nullptr, mode, c.l2_persist_1024);
         ADIPC_CUDA(cudaEventRecord(e1, c.stream));
         ADIPC_CUDA(cudaEventSynchronize(e1));
         float ms = 0;

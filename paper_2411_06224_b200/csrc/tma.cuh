@@ -49,6 +49,28 @@ __device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src,
         : "memory");
 }
 
+// L2 cache policies for explicit residency control of streamed operands
+__device__ __forceinline__ std::uint64_t policy_evict_last() {
+    std::uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ std::uint64_t policy_evict_first() {
+    std::uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_nc_policy(const double* ptr, std::uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ std::uint32_t ld_nc_policy(const std::uint32_t* ptr, std::uint64_t pol) {
+    std::uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
+    return v;
+}
+
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
     std::uint32_t done;
     do {

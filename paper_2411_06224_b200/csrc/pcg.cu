@@ -71,6 +71,7 @@ __global__ void k_zero(double* __restrict__ v, std::int64_t n, const int* __rest
 
 struct GraphExec {
     cudaGraphExec_t exec = nullptr;
+    long long kernels = 0;
     ~GraphExec() {
         if (exec) cudaGraphExecDestroy(exec);
     }
@@ -223,6 +224,9 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
     if (!prof) {
         auto capture = [&](bool is_restart, GraphExec& g) {
             cudaGraph_t graph;
+            // kernels recorded into the graph are counted when the graph is
+            // replayed (kernel_launches() reports kernels actually executed)
+            const long long before = launch_counter();
             ADIPC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
             try {
                 iteration(is_restart, 0);
@@ -233,6 +237,8 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
             ADIPC_CUDA(cudaStreamEndCapture(st, &graph));
             ADIPC_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
             ADIPC_CUDA(cudaGraphDestroy(graph));
+            g.kernels = launch_counter() - before;
+            launch_counter() = before;
         };
         capture(false, g_norm);
         if (restart > 0 && restart <= max_iters) capture(true, g_rest);
@@ -251,8 +257,11 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
             const bool is_restart = restart > 0 && k % restart == 0;
             if (prof)
                 iteration(is_restart, k - kbeg);
-            else
-                ADIPC_CUDA(cudaGraphLaunch(is_restart ? g_rest.exec : g_norm.exec, st));
+            else {
+                GraphExec& g = is_restart ? g_rest : g_norm;
+                ADIPC_CUDA(cudaGraphLaunch(g.exec, st));
+                launch_counter() += g.kernels;
+            }
         }
         ADIPC_CUDA(cudaMemcpyAsync(hf[ci & 1], w.flags.p, F_COUNT * sizeof(int), cudaMemcpyDeviceToHost, st));
         ADIPC_CUDA(cudaEventRecord(c.ev_chunk[ci & 1], st));

@@ -64,6 +64,15 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic():
+    """DRAM bytes per launch by kernel class from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)["bytes_per_launch"]
+    except Exception:
+        return {}
+
+
 # ----------------------------------------------------------------- clocks ---
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
@@ -209,25 +218,10 @@ def run_ours(args, rank, world, local_rank, dist):
         d_keys = torch.from_numpy(sc.keys.view(np.int64)).to(dev)
         d_vals = torch.from_numpy(sc.vals).to(dev)
         d_pin = torch.from_numpy(sc.pinned).to(dev)
-        T = len(sc.keys)
-        d_fk = torch.empty(T + sc.n_blocks, dtype=torch.int64, device=dev)
-        d_fv = torch.empty((T + sc.n_blocks, 9), dtype=torch.float64, device=dev)
     stream.synchronize()
-    # filtered stream on device (filter_pinned, incremental_potential.hpp:410-425)
-    import ctypes as C
-
-    L = _lib.gpu()
-    nf = C.c_int64()
-
-    def filter_dev():
-        # device filter through the same kernels the host-pointer API uses
-        ctx._check(L.adipc_gpu_filter_pinned_device(ctx.h, d_keys.data_ptr(), d_vals.data_ptr(), T,
-                                                    d_pin.data_ptr(), sc.n_blocks, d_fk.data_ptr(), d_fv.data_ptr(),
-                                                    C.byref(nf)))
-        return nf.value
-
-    Tf = filter_dev()
-    ctx.assemble(d_fk[:Tf], d_fv[:Tf], sc.n_blocks)
+    # filter_pinned + sort + reduce on the device-resident raw stream
+    # (incremental_potential.hpp:255-257)
+    ctx.assemble_filtered(d_keys, d_vals, sc.n_blocks, d_pin)
     n, U = ctx.matrix_info()
     # the first Newton step from rest: b = M dt^2 g, pinned slots zero
     from paper_2411_06224_b200 import scenes as S
@@ -238,8 +232,7 @@ def run_ours(args, rank, world, local_rank, dist):
     stream.synchronize()
 
     def step():
-        Tf = filter_dev()
-        ctx.assemble(d_fk[:Tf], d_fv[:Tf], sc.n_blocks)
+        ctx.assemble_filtered(d_keys, d_vals, sc.n_blocks, d_pin)
         ctx.build_preconditioner(_lib.PRECOND_MAS)
         _, res = ctx.pcg(d_b, REL_TOL, RESTART, MAX_ITERS, x=d_x)
         t = ctx.timings()
@@ -357,7 +350,8 @@ def run_ours(args, rank, world, local_rank, dist):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_gbs"], "peak": hbm,
                          "peak_source": peak_src, "unit": "GB/s",
                          "frac": (dk["achieved_gbs"] / hbm) if dk["achieved_gbs"] else None,
-                         "algorithmic_bytes_per_launch": dk["bytes_per_launch"], "traffic": None},
+                         "algorithmic_bytes_per_launch": dk["bytes_per_launch"],
+                         "traffic": ncu_traffic().get(dom), "traffic_source": "profiles/ncu_traffic.json"},
             "roofline_pcg_iteration": {"bound": "hbm", "bytes_per_iter": bm["total"],
                                        "achieved": bm["total"] / iter_s / 1e9, "peak": hbm, "unit": "GB/s",
                                        "frac": bm["total"] / iter_s / 1e9 / hbm},
@@ -376,7 +370,7 @@ def run_ours(args, rank, world, local_rank, dist):
             out["e2e"] = {"value": sum(x["iters"] for x in g) / (tot / 1000.0), "unit": "PCG iterations/s",
                           "h2d_bytes_per_step": g[0]["h2d"], "d2h_bytes_per_step": g[0]["d2h"],
                           "ms_per_step": tot / args.steps,
-                          "path": "adipc_gpu_filter_pinned + adipc_gpu_assemble + adipc_gpu_build_preconditioner "
+                          "path": "adipc_gpu_assemble_filtered + adipc_gpu_build_preconditioner "
                                   "+ adipc_gpu_pcg (host pointers, pinned)"}
     ctx.close()
     return out, sc
@@ -394,18 +388,15 @@ def run_e2e(args, ctx, sc, d_b, stream, dev):
     h_keys = torch.from_numpy(sc.keys.view(np.int64)).pin_memory()
     h_vals = torch.from_numpy(sc.vals).pin_memory()
     h_pin = torch.from_numpy(sc.pinned).pin_memory()
-    h_fk = torch.empty(T + sc.n_blocks, dtype=torch.int64).pin_memory()
-    h_fv = torch.empty((T + sc.n_blocks, 9), dtype=torch.float64).pin_memory()
     h_b = d_b.cpu().pin_memory()
     h_x = torch.empty_like(h_b).pin_memory()
-    nf, U = C.c_int64(), C.c_int64()
+    U = C.c_int64()
     it, rr, cv = C.c_int(), C.c_double(), C.c_int()
 
     def step():
-        ctx._check(L.adipc_gpu_filter_pinned(ctx.h, h_keys.data_ptr(), h_vals.data_ptr(), T, h_pin.data_ptr(),
-                                             sc.n_blocks, h_fk.data_ptr(), h_fv.data_ptr(), C.byref(nf)))
-        ctx._check(L.adipc_gpu_assemble(ctx.h, h_fk.data_ptr(), h_fv.data_ptr(), nf.value, sc.n_blocks, 1,
-                                        C.byref(U)))
+        # filter_pinned + sort + reduce from the host stream (one H2D of it)
+        ctx._check(L.adipc_gpu_assemble_filtered(ctx.h, h_keys.data_ptr(), h_vals.data_ptr(), T, sc.n_blocks,
+                                                 h_pin.data_ptr(), 1, C.byref(U)))
         ctx._check(L.adipc_gpu_build_preconditioner(ctx.h, _lib.PRECOND_MAS))
         ctx._check(L.adipc_gpu_pcg(ctx.h, h_b.data_ptr(), REL_TOL, RESTART, MAX_ITERS, h_x.data_ptr(), C.byref(it),
                                    C.byref(rr), C.byref(cv)))
@@ -421,8 +412,8 @@ def run_e2e(args, ctx, sc, d_b, stream, dev):
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1000.0
     n3 = 3 * sc.n_blocks
-    h2d = T * 80 + sc.n_blocks + nf.value * 80 + n3 * 8  # raw stream + pins, filtered stream, b
-    d2h = nf.value * 80 + n3 * 8                           # filtered stream back, x
+    h2d = T * 80 + sc.n_blocks + n3 * 8  # raw stream (keys + values) + pins + b
+    d2h = n3 * 8                          # x
     return {"ms": ms, "iters": iters, "h2d": int(h2d), "d2h": int(d2h)}
 
 

@@ -79,6 +79,14 @@ int adipc_gpu_assemble(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* v
                        int32_t n_block_rows, int deterministic, int64_t* n_unique);
 int adipc_gpu_assemble_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const double* d_vals9, int64_t T,
                               int32_t n_block_rows, int deterministic, int64_t* n_unique);
+/* filter_pinned + sort_stream + fast_hash_reduction in one call, exactly the
+ * sequence of incremental_potential.hpp:255-257 (pinned: one byte per block
+ * slot); the raw stream crosses PCIe once. */
+int adipc_gpu_assemble_filtered(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T,
+                                int32_t n_block_rows, const uint8_t* pinned, int deterministic, int64_t* n_unique);
+int adipc_gpu_assemble_filtered_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const double* d_vals9, int64_t T,
+                                       int32_t n_block_rows, const uint8_t* d_pinned, int deterministic,
+                                       int64_t* n_unique);
 int adipc_gpu_matrix_info(adipc_gpu_ctx* ctx, int32_t* n_block_rows, int64_t* n_blocks);
 /* copy SortedSymBlockCoo{rows, cols, blocks} out (block_coo.hpp:54-61) */
 int adipc_gpu_copy_matrix(adipc_gpu_ctx* ctx, uint32_t* rows, uint32_t* cols, double* blocks9);

@@ -38,6 +38,8 @@ GPU_SIGNATURES = {
     "adipc_gpu_pcg_profile": (ci, [vp, f32p, C.POINTER(ci)]),
     "adipc_gpu_assemble": (ci, [vp, vp, vp, i64, i32, ci, C.POINTER(i64)]),
     "adipc_gpu_assemble_device": (ci, [vp, vp, vp, i64, i32, ci, C.POINTER(i64)]),
+    "adipc_gpu_assemble_filtered": (ci, [vp, vp, vp, i64, i32, vp, ci, C.POINTER(i64)]),
+    "adipc_gpu_assemble_filtered_device": (ci, [vp, vp, vp, i64, i32, vp, ci, C.POINTER(i64)]),
     "adipc_gpu_matrix_info": (ci, [vp, C.POINTER(i32), C.POINTER(i64)]),
     "adipc_gpu_copy_matrix": (ci, [vp, vp, vp, vp]),
     "adipc_gpu_set_matrix": (ci, [vp, i32, i64, vp, vp, vp]),

@@ -124,6 +124,21 @@ class Context:
                                                    C.byref(U)))
         return U.value
 
+    def assemble_filtered(self, keys, vals, n_block_rows: int, pinned, deterministic: bool = True) -> int:
+        """filter_pinned + sort_stream + fast_hash_reduction (incremental_potential.hpp:255-257)."""
+        U = C.c_int64()
+        T = len(keys)
+        if _is_device(keys):
+            self._check(self._L.adipc_gpu_assemble_filtered_device(self.h, ptr(keys), ptr(vals), T, n_block_rows,
+                                                                   ptr(pinned), int(deterministic), C.byref(U)))
+        else:
+            k = np.ascontiguousarray(keys, np.uint64)
+            v = np.ascontiguousarray(vals, np.float64).reshape(-1, 9)
+            p = np.ascontiguousarray(pinned, np.uint8)
+            self._check(self._L.adipc_gpu_assemble_filtered(self.h, ptr(k), ptr(v), T, n_block_rows, ptr(p),
+                                                            int(deterministic), C.byref(U)))
+        return U.value
+
     def matrix_info(self):
         n, U = C.c_int32(), C.c_int64()
         self._check(self._L.adipc_gpu_matrix_info(self.h, C.byref(n), C.byref(U)))

@@ -105,6 +105,8 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.scan_scratch.free();
     c.counters.free();
     c.pinned.free();
+    c.fkeys.free();
+    c.fvals.free();
     for (auto& L : c.levels) {
         L->agg.free();
         L->part_of.free();
@@ -226,6 +228,48 @@ int adipc_gpu_assemble_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const 
         Ctx& c = ctx->c;
         if (T < 0 || n < 0) throw StatusError(kInvalidArgument, "negative size");
         timed_assemble(c, d_keys, d_vals9, T, n, det);
+        if (n_unique) *n_unique = c.A.U;
+    });
+}
+
+// filter_pinned + sort_stream + fast_hash_reduction in one call
+// (incremental_potential.hpp:255-257): the raw stream crosses PCIe once.
+static void filtered_assemble(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T,
+                              std::int32_t n, const std::uint8_t* d_pinned, int det) {
+    cudaEvent_t e0, e1;
+    ADIPC_CUDA(cudaEventCreate(&e0));
+    ADIPC_CUDA(cudaEventCreate(&e1));
+    ADIPC_CUDA(cudaEventRecord(e0, c.stream));
+    c.fkeys.reserve(static_cast<std::size_t>(T + n));
+    c.fvals.reserve(9 * static_cast<std::size_t>(T + n));
+    const std::int64_t Tf = filter_pinned(c, d_keys, d_vals, T, d_pinned, n, c.fkeys.p, c.fvals.p);
+    assemble(c, c.fkeys.p, c.fvals.p, Tf, n, det);
+    ADIPC_CUDA(cudaEventRecord(e1, c.stream));
+    ADIPC_CUDA(cudaEventSynchronize(e1));
+    ADIPC_CUDA(cudaEventElapsedTime(&c.ms_assemble, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+}
+
+int adipc_gpu_assemble_filtered(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T,
+                                int32_t n, const uint8_t* pinned, int det, int64_t* n_unique) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (T < 0 || n < 0) throw StatusError(kInvalidArgument, "negative size");
+        h2d(c.keys, keys, static_cast<std::size_t>(T), c.stream);
+        h2d(c.vals, vals9, 9 * static_cast<std::size_t>(T), c.stream);
+        h2d(c.pinned, pinned, static_cast<std::size_t>(n), c.stream);
+        filtered_assemble(c, c.keys.p, c.vals.p, T, n, c.pinned.p, det);
+        if (n_unique) *n_unique = c.A.U;
+    });
+}
+
+int adipc_gpu_assemble_filtered_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const double* d_vals9, int64_t T,
+                                       int32_t n, const uint8_t* d_pinned, int det, int64_t* n_unique) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (T < 0 || n < 0) throw StatusError(kInvalidArgument, "negative size");
+        filtered_assemble(c, d_keys, d_vals9, T, n, d_pinned, det);
         if (n_unique) *n_unique = c.A.U;
     });
 }

@@ -88,6 +88,8 @@ struct Ctx {
     DBuf<std::int64_t> row_start, uniq_start, scan_scratch;
     DBuf<std::int32_t> counters;
     DBuf<std::uint8_t> pinned;
+    DBuf<std::uint64_t> fkeys;  // filtered stream (assemble_filtered)
+    DBuf<double> fvals;
     DBuf<std::int32_t> pin_keep;
     DBuf<std::int64_t> pin_pos, pin_spos;
 

@@ -64,6 +64,22 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def gather_scene_stats(stats, world, dist):
+    """Batch of independent scenes, one per rank (replicas):
+    the only collective is an all-gather of each scene's stats; the job time
+    is the max over ranks, the work (PCG iterations) the sum over ranks."""
+    if dist is not None and world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, stats)
+    else:
+        gathered = [stats]
+    agg = {"max_total_ms": max(g["total_ms"] for g in gathered),
+           "max_pcg_ms": max(g["pcg_ms"] for g in gathered),
+           "iters": sum(g["iters"] for g in gathered),
+           "converged": all(g.get("conv", True) for g in gathered)}
+    return gathered, agg
+
+
 def ncu_traffic():
     """DRAM bytes per launch by kernel class from the committed ncu capture."""
     try:
@@ -288,14 +304,8 @@ def run_ours(args, rank, world, local_rank, dist):
 
     stats = dict(total_ms=total_ms, pcg_ms=pcg_ms, iters=iters, asm_ms=asm_ms, build_ms=build_ms,
                  launches=launches, conv=bool(res_last.converged), rel=float(res_last.rel_residual), xerr=xerr)
-    if dist:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, stats)  # the only collective: per-scene stats
-    else:
-        gathered = [stats]
-    max_total = max(g["total_ms"] for g in gathered)
-    max_pcg = max(g["pcg_ms"] for g in gathered)
-    all_iters = sum(g["iters"] for g in gathered)
+    gathered, agg = gather_scene_stats(stats, world, dist)
+    max_total, max_pcg, all_iters = agg["max_total_ms"], agg["max_pcg_ms"], agg["iters"]
 
     out = None
     if rank == 0:

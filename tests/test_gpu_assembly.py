@@ -182,3 +182,25 @@ def test_api_mirror(ctx):
     A = P.fast_hash_reduction(s, 12, P.ExecPolicy(deterministic=True))
     want = oracle_assemble(keys, vals, 12)
     assert_bitwise((A.rows, A.cols, A.blocks), want)
+
+
+@pytest.mark.parametrize("name", ["stiff_beam", "cfg1_soft_cube"])
+def test_assemble_filtered_bitwise(ctx, name):
+    """adipc_gpu_assemble_filtered = filter_pinned + sort_stream +
+    fast_hash_reduction (incremental_potential.hpp:255-257), host and device
+    pointers, bit-exact with the oracle."""
+    import torch
+
+    sc = scenes.CONFIGS[name]()
+    pinned = sc.pinned.copy()
+    pinned[::97] = 1
+    ok, ov = O.filter_pinned(sc.keys, sc.vals, pinned)
+    want = oracle_assemble(ok, ov, sc.n_blocks)
+    ctx.assemble_filtered(sc.keys, sc.vals, sc.n_blocks, pinned)
+    assert_bitwise(ctx.copy_matrix()[1:], want)
+    dk = torch.from_numpy(sc.keys.view(np.int64)).cuda()
+    dv = torch.from_numpy(sc.vals).cuda()
+    dp = torch.from_numpy(pinned).cuda()
+    torch.cuda.synchronize()  # the context runs on its own non-blocking stream
+    ctx.assemble_filtered(dk, dv, sc.n_blocks, dp)
+    assert_bitwise(ctx.copy_matrix()[1:], want)

@@ -11,11 +11,13 @@
 // timed CPU baseline. The product path (paper_2411_06224_b200/) never links
 // or calls it.
 //
-// The reference cannot be compiled here (Eigen 3.4, Catch2 and CLI11 are
-// absent), so the arithmetic Eigen performs (3x3 products, LLT, dots) is
-// restated with plain loops. Results Eigen produces are pinned by the
-// reference's tests to tolerance only; everything integer (keys, sort order,
-// partitions, hierarchies) and the deterministic reductions are bit-exact.
+// Eigen is absent here, so the arithmetic Eigen performs (3x3 products, LLT,
+// dots) is restated with plain loops, following Eigen 3.4's evaluation order
+// where that order decides bits (fixed-size products, the 3x3 inverse).
+// Everything integer (keys, sort order, partitions, hierarchies), the
+// deterministic reductions and the two-level tiles are bit-exact with the
+// reference's own code compiled in place (oracle/_ref, see ref_capi.cpp and
+// tests/test_oracle_vs_reference.py); LLT solves and dots agree to rounding.
 // Compiled like the reference: -O2 -fopenmp, no FMA contraction.
 #pragma once
 
@@ -87,23 +89,21 @@ struct Mat3 {
             y[r] = (*this)(r, 0) * x[0] + (*this)(r, 1) * x[1] + (*this)(r, 2) * x[2];
         return y;
     }
-    // Mat3::inverse via the adjugate (block_jacobi.hpp:13 uses Eigen's
-    // closed-form cofactor inverse for 3x3).
+    // Mat3::inverse as Eigen 3.4 computes a fixed 3x3 inverse
+    // (block_jacobi.hpp:13 -> Eigen/src/LU/InverseImpl.h compute_inverse<3,3>):
+    // cyclic cofactors, det by expansion down column 0, times 1/det.
+    static Real cofactor(const Mat3& a, int i, int j) {
+        const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+        return a(i1, j1) * a(i2, j2) - a(i1, j2) * a(i2, j1);
+    }
     Mat3 inverse() const {
         const Mat3& a = *this;
-        Mat3 cof;
-        cof(0, 0) = a(1, 1) * a(2, 2) - a(1, 2) * a(2, 1);
-        cof(1, 0) = a(1, 2) * a(2, 0) - a(1, 0) * a(2, 2);
-        cof(2, 0) = a(1, 0) * a(2, 1) - a(1, 1) * a(2, 0);
-        const Real det = a(0, 0) * cof(0, 0) + a(0, 1) * cof(1, 0) + a(0, 2) * cof(2, 0);
-        cof(0, 1) = a(0, 2) * a(2, 1) - a(0, 1) * a(2, 2);
-        cof(1, 1) = a(0, 0) * a(2, 2) - a(0, 2) * a(2, 0);
-        cof(2, 1) = a(0, 1) * a(2, 0) - a(0, 0) * a(2, 1);
-        cof(0, 2) = a(0, 1) * a(1, 2) - a(0, 2) * a(1, 1);
-        cof(1, 2) = a(0, 2) * a(1, 0) - a(0, 0) * a(1, 2);
-        cof(2, 2) = a(0, 0) * a(1, 1) - a(0, 1) * a(1, 0);
+        const Real c0 = cofactor(a, 0, 0), c1 = cofactor(a, 1, 0), c2 = cofactor(a, 2, 0);
+        const Real det = c0 * a(0, 0) + c1 * a(1, 0) + c2 * a(2, 0);
+        const Real invdet = Real(1) / det;
         Mat3 inv;
-        for (int k = 0; k < 9; ++k) inv.m[k] = cof.m[k] / det;
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) inv(i, j) = cofactor(a, j, i) * invdet;
         return inv;
     }
 };
@@ -377,13 +377,18 @@ struct MatRC {  // small dense column-major matrix (Mat12, Mat12x3, Mat3x12)
 };
 
 // Eigen's dynamic-free product for small fixed matrices: inner-product order k=0..K-1.
-inline MatRC matmul(const MatRC& A, const MatRC& B) {
+// Eigen product evaluation for the shapes on this path: coefficient-based
+// (3x3*3x12, 12x3*3x3) sums from the first term; the 12x3*3x12 product is a
+// GEMM (GeneralProduct.h product_type_selector<Large,Large,Small>, 27 >=
+// EIGEN_GEMM_TO_COEFFBASED_THRESHOLD) whose accumulators start at zero, so
+// its -0.0 entries come out +0.0 (gemm = true). Inner index ascending, no FMA.
+inline MatRC matmul(const MatRC& A, const MatRC& B, bool gemm = false) {
     MatRC C(A.rows, B.cols);
     for (int c = 0; c < B.cols; ++c)
         for (int r = 0; r < A.rows; ++r) {
             Real s = A(r, 0) * B(0, c);
             for (int k = 1; k < A.cols; ++k) s += A(r, k) * B(k, c);
-            C(r, c) = s;
+            C(r, c) = gemm ? 0.0 + s : s;
         }
     return C;
 }
@@ -447,11 +452,11 @@ inline BlockTripletStream two_level_abd_reduce(const BlockTripletStream& node_pa
             const MatRC JiT = map.jacobian(i).transpose();
             if (bi != bj) {
                 split_12x12(map.body_block_base(bi), map.body_block_base(bj),
-                            matmul(matmul(JiT, C), map.jacobian(j)), out);
+                            matmul(matmul(JiT, C), map.jacobian(j), true), out);
             } else if (i == j) {
-                split_sym_12x12(map.body_block_base(bi), matmul(matmul(JiT, C), map.jacobian(i)), out);
+                split_sym_12x12(map.body_block_base(bi), matmul(matmul(JiT, C), map.jacobian(i), true), out);
             } else {
-                const MatRC K = matmul(matmul(JiT, C), map.jacobian(j));
+                const MatRC K = matmul(matmul(JiT, C), map.jacobian(j), true);
                 MatRC S(12, 12);
                 for (int r = 0; r < 12; ++r)
                     for (int c = 0; c < 12; ++c) S(r, c) = K(r, c) + K(c, r);

@@ -327,73 +327,6 @@ int oracle_pcg_solve(void* mat, const double* b, std::size_t n, void* precond, d
     return 0;
 }
 
-// ---- the reference tests' random draws (libstdc++ std::mt19937) -------------------
-void* oracle_rng_new(std::uint32_t seed) { return new std::mt19937(seed); }
-void oracle_rng_free(void* g) { delete static_cast<std::mt19937*>(g); }
-
-struct Dist {
-    int kind;  // 0 uniform_int, 1 normal, 2 uniform_real
-    std::uniform_int_distribution<long> ui;
-    std::normal_distribution<double> nd;
-    std::uniform_real_distribution<double> ur;
-};
-void* oracle_dist_uniform_int(long a, long b) { return new Dist{0, std::uniform_int_distribution<long>(a, b), {}, {}}; }
-void* oracle_dist_normal(double m, double s) { return new Dist{1, {}, std::normal_distribution<double>(m, s), {}}; }
-void* oracle_dist_uniform_real(double a, double b) {
-    return new Dist{2, {}, {}, std::uniform_real_distribution<double>(a, b)};
-}
-void oracle_dist_free(void* d) { delete static_cast<Dist*>(d); }
-// std::uniform_int_distribution<int> and <long> draw identically for these
-// ranges in libstdc++ (both downscale one 32-bit mt19937 output).
-double oracle_dist_draw(void* dp, void* gp) {
-    auto* d = static_cast<Dist*>(dp);
-    auto& g = *static_cast<std::mt19937*>(gp);
-    if (d->kind == 0) return static_cast<double>(d->ui(g));
-    if (d->kind == 1) return d->nd(g);
-    return d->ur(g);
-}
-void oracle_dist_fill(void* dp, void* gp, double* out, std::size_t n) {
-    for (std::size_t i = 0; i < n; ++i) out[i] = oracle_dist_draw(dp, gp);
-}
-
-// test_block_sparse.cpp:40-52 / verify_suites.hpp:106-119 random_stream:
-// fresh distributions per call, B.data()[k] column-major, symmetrised
-// diagonal blocks, canonicalising emit. Buffers sized >= n_entries.
-void oracle_random_stream(void* gp, int n_blocks, int n_entries, std::uint64_t* keys, double* vals) {
-    auto& rng = *static_cast<std::mt19937*>(gp);
-    std::uniform_int_distribution<int> pick(0, n_blocks - 1);
-    std::normal_distribution<Real> val(0.0, 1.0);
-    BlockTripletStream s;
-    for (int i = 0; i < n_entries; ++i) {
-        Mat3 B;
-        for (int k = 0; k < 9; ++k) B.data()[k] = val(rng);
-        const Index r = pick(rng), c = pick(rng);
-        if (r == c) {
-            const Mat3 t = B.transpose();
-            Mat3 sym;
-            for (int k = 0; k < 9; ++k) sym.m[k] = B.m[k] + t.m[k];
-            B = sym;
-        }
-        s.emit(r, c, B);
-    }
-    store_stream(s, keys, vals);
-}
-
-// test_precond.cpp:17-23 / test_solver.cpp:15-21 random_spd3 with a fresh
-// uniform(-1,1) per call: g g^T + shift I (Eigen lazy product order).
-void oracle_random_spd3(void* gp, double shift, double* out9) {
-    auto& rng = *static_cast<std::mt19937*>(gp);
-    std::uniform_real_distribution<Real> u(-1, 1);
-    Mat3 g;
-    for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) g(r, c) = u(rng);
-    Mat3 m;
-    for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) {
-            m(r, c) = g(r, 0) * g(c, 0) + g(r, 1) * g(c, 1) + g(r, 2) * g(c, 2);
-            if (r == c) m(r, c) += shift;
-        }
-    std::memcpy(out9, m.m, 72);
-}
+#include "capi_rng.inc"
 
 }  // extern "C"

@@ -44,7 +44,7 @@ _lib = None
 def lib():
     global _lib
     if _lib is not None:
-        return _lib
+        return _ref_dispatch() if _backend == "reference" else _lib
     if not os.path.exists(_LIB_PATH):
         build()
     L = C.CDLL(_LIB_PATH)
@@ -97,7 +97,77 @@ def lib():
         fn.restype = res
         fn.argtypes = args
     _lib = L
-    return L
+    global _SIG
+    _SIG = sig
+    return _ref_dispatch() if _backend == "reference" else L
+
+
+# ------------------------------------------------------- reference backend --
+# oracle/_ref/libadipc_ref.so is the reference's OWN hot-path code compiled in
+# place (oracle/ref_capi.cpp, oracle/Makefile target `ref`). Its ref_* entries
+# have the oracle_* signatures, so every wrapper below runs on either library:
+# `with use_backend("reference"): ...` routes compute entries to it (entries
+# it lacks — the test RNG — stay on the restatement).
+_REF_PATH = os.path.join(_HERE, "_ref", "libadipc_ref.so")
+_REF_SRC = "/root/reference/proj/include"
+_backend = "restated"
+_SIG = None
+_ref = None
+
+
+def reference_available() -> bool:
+    if os.path.exists(_REF_PATH):
+        return True
+    if os.path.isdir(_REF_SRC):
+        try:
+            subprocess.check_call(["make", "-s", "-C", _HERE, "ref"])
+        except (OSError, subprocess.CalledProcessError):
+            return False
+        return os.path.exists(_REF_PATH)
+    return False
+
+
+class _Dispatch:
+    def __init__(self, base, ref):
+        self._base, self._ref = base, ref
+
+    def __getattr__(self, name):
+        f = getattr(self._ref, "ref_" + name[len("oracle_"):], None) if name.startswith("oracle_") else None
+        if f is None:
+            return getattr(self._base, name)
+        res, args = _SIG[name]
+        f.restype, f.argtypes = res, args
+        return f
+
+
+def _ref_dispatch():
+    global _ref
+    if _ref is None:
+        if not reference_available():
+            raise RuntimeError("oracle/_ref/libadipc_ref.so missing and /root/reference not present")
+        _ref = _Dispatch(_lib, C.CDLL(_REF_PATH))
+    return _ref
+
+
+def backend() -> str:
+    return _backend
+
+
+class use_backend:
+    """Context manager: ``"restated"`` (oracle.hpp) or ``"reference"``."""
+
+    def __init__(self, name):
+        assert name in ("restated", "reference")
+        self.name = name
+
+    def __enter__(self):
+        global _backend
+        self.prev, _backend = _backend, self.name
+        return lib()
+
+    def __exit__(self, *exc):
+        global _backend
+        _backend = self.prev
 
 
 def _pol(policy):
@@ -273,6 +343,8 @@ def filter_pinned(keys, vals, pinned):
     ok = np.empty(cap, np.uint64)
     ov = np.empty((cap, 9), np.float64)
     n = lib().oracle_filter_pinned(k, v, len(k), p, len(p), ok, ov)
+    if n < 0:  # not exposed by the compiled reference (ref_capi.cpp): restated version
+        n = _lib.oracle_filter_pinned(k, v, len(k), p, len(p), ok, ov)
     return ok[:n].copy(), ov[:n].copy()
 
 
@@ -314,15 +386,16 @@ class Hierarchy:
         e, ne = _edges(edges)
         self.n_slots = len(part_of)
         self.capacity = capacity
-        self.h = lib().oracle_build_hierarchy(part_of if len(part_of) else np.zeros(1, np.int32),
+        self._L = L = lib()
+        self.h = L.oracle_build_hierarchy(part_of if len(part_of) else np.zeros(1, np.int32),
                                               self.n_slots, n_parts, capacity, e, ne, max_levels)
         self.levels = []
-        for l in range(lib().oracle_hierarchy_n_levels(self.h)):
+        for l in range(self._L.oracle_hierarchy_n_levels(self.h)):
             nn, npart = i32(), i32()
-            lib().oracle_hierarchy_level(self.h, l, C.byref(nn), C.byref(npart), None, None)
+            self._L.oracle_hierarchy_level(self.h, l, C.byref(nn), C.byref(npart), None, None)
             part = np.empty(max(nn.value, 1), np.int32)
             agg = np.empty(max(self.n_slots, 1), np.int32)
-            lib().oracle_hierarchy_level(self.h, l, C.byref(nn), C.byref(npart),
+            self._L.oracle_hierarchy_level(self.h, l, C.byref(nn), C.byref(npart),
                                          part.ctypes.data_as(vp), agg.ctypes.data_as(vp))
             self.levels.append(dict(n_nodes=nn.value, n_parts=npart.value,
                                     part_of=part[: nn.value].copy(), agg=agg[: self.n_slots].copy()))
@@ -332,7 +405,7 @@ class Hierarchy:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().oracle_hierarchy_free(self.h)
+            self._L.oracle_hierarchy_free(self.h)
             self.h = None
 
 
@@ -340,14 +413,15 @@ class Matrix:
     def __init__(self, n_block_rows, rows, cols, blocks):
         self.n_block_rows = n_block_rows
         U = len(rows)
-        self.h = lib().oracle_matrix_new(n_block_rows, U,
+        self._L = lib()
+        self.h = self._L.oracle_matrix_new(n_block_rows, U,
                                          np.ascontiguousarray(rows, np.uint32) if U else np.zeros(1, np.uint32),
                                          np.ascontiguousarray(cols, np.uint32) if U else np.zeros(1, np.uint32),
                                          np.ascontiguousarray(blocks, np.float64).reshape(-1) if U else np.zeros(9))
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().oracle_matrix_free(self.h)
+            self._L.oracle_matrix_free(self.h)
             self.h = None
 
 
@@ -355,43 +429,45 @@ class _Precond:
     def apply(self, r):
         r = np.ascontiguousarray(r, np.float64)
         z = np.empty_like(r)
-        lib().oracle_precond_apply(self.h, r, len(r), z)
+        self._L.oracle_precond_apply(self.h, r, len(r), z)
         return z
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().oracle_precond_free(self.h)
+            self._L.oracle_precond_free(self.h)
             self.h = None
 
 
 class MasPreconditioner(_Precond):
     def __init__(self, mat: Matrix, hier: Hierarchy):
-        self.h = lib().oracle_mas_build(mat.h, hier.h)
+        self._L = mat._L
+        self.h = self._L.oracle_mas_build(mat.h, hier.h)
         if not self.h:
-            raise RuntimeError(lib().oracle_last_error().decode())
+            raise RuntimeError(self._L.oracle_last_error().decode())
 
     def n_levels(self):
-        return lib().oracle_mas_n_levels(self.h)
+        return self._L.oracle_mas_n_levels(self.h)
 
     def shifts(self):
-        return lib().oracle_mas_shifts(self.h)
+        return self._L.oracle_mas_shifts(self.h)
 
     def level_matrix(self, l, s):
-        d = lib().oracle_mas_level_matrix(self.h, l, s, None)
+        d = self._L.oracle_mas_level_matrix(self.h, l, s, None)
         out = np.empty(d * d, np.float64)
-        lib().oracle_mas_level_matrix(self.h, l, s, out.ctypes.data_as(vp))
+        self._L.oracle_mas_level_matrix(self.h, l, s, out.ctypes.data_as(vp))
         return out.reshape(d, d).T.copy()  # column-major -> natural
 
 
 class BlockJacobiPreconditioner(_Precond):
     def __init__(self, mat: Matrix):
-        self.h = lib().oracle_jacobi_build(mat.h)
+        self._L = mat._L
+        self.h = self._L.oracle_jacobi_build(mat.h)
 
 
 def pcg_solve(mat: Matrix, b, M: _Precond, rel_tol, restart, max_iters, policy=None):
     b = np.ascontiguousarray(b, np.float64)
     x = np.empty_like(b)
     it, rr, cv = ci(), cd(), ci()
-    lib().oracle_pcg_solve(mat.h, b, len(b), M.h, rel_tol, restart, max_iters, *_pol(policy), x,
+    mat._L.oracle_pcg_solve(mat.h, b, len(b), M.h, rel_tol, restart, max_iters, *_pol(policy), x,
                            C.byref(it), C.byref(rr), C.byref(cv))
     return x, dict(iters=it.value, rel_residual=rr.value, converged=bool(cv.value))

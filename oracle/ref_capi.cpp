@@ -1,0 +1,330 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" surface over the REFERENCE's own hot-path headers, compiled in
+// place from /root/reference/proj/include (nothing copied) against the Eigen
+// subset in oracle/eigen_shim, into oracle/_ref/libadipc_ref.so. Every entry
+// has the signature of the oracle_* entry of the same suffix in
+// oracle_capi.cpp, so oracle_py can drive either library with one set of
+// wrappers (oracle_py.use_backend("reference")). Used only to pin the
+// restatement (tests/test_oracle_vs_reference.py) and as bench.py's
+// "reference" CPU arm; never by the product.
+//
+// Not exposed: filter_pinned (a private member of IncrementalPotential,
+// solver/incremental_potential.hpp:410, whose header drags in the contact and
+// energy stack) and the MAS shift count (the reference does not record it).
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include "adipc/precond/block_jacobi.hpp"
+#include "adipc/precond/hierarchy.hpp"
+#include "adipc/precond/mas.hpp"
+#include "adipc/precond/partition.hpp"
+#include "adipc/solver/pcg.hpp"
+#include "adipc/sparse/abd_reduce.hpp"
+#include "adipc/sparse/block_coo.hpp"
+#include "adipc/sparse/block_split.hpp"
+#include "adipc/sparse/reduction.hpp"
+#include "adipc/sparse/srbk_spmv.hpp"
+
+using namespace adipc;
+
+namespace {
+
+thread_local std::string g_err;
+
+ExecPolicy make_pol(int det, int threads, int lane_width) {
+    ExecPolicy p;
+    p.deterministic = det != 0;
+    p.threads = threads;
+    p.lane_width = lane_width > 0 ? lane_width : 32;
+    return p;
+}
+
+Mat3 load_mat3(const double* p) {
+    Mat3 m;
+    std::memcpy(m.data(), p, 72);
+    return m;
+}
+
+BlockTripletStream load_stream(const std::uint64_t* keys, const double* vals, std::size_t T) {
+    BlockTripletStream s;
+    s.keys.assign(keys, keys + T);
+    s.values.resize(T);
+    for (std::size_t i = 0; i < T; ++i) s.values[i] = load_mat3(vals + 9 * i);
+    return s;
+}
+
+void store_stream(const BlockTripletStream& s, std::uint64_t* keys, double* vals) {
+    for (std::size_t i = 0; i < s.size(); ++i) {
+        keys[i] = s.keys[i];
+        std::memcpy(vals + 9 * i, s.values[i].data(), 72);
+    }
+}
+
+SortedSymBlockCoo load_matrix(std::int32_t n_block_rows, std::size_t U, const std::uint32_t* rows,
+                              const std::uint32_t* cols, const double* blocks) {
+    SortedSymBlockCoo A;
+    A.n_block_rows = n_block_rows;
+    A.rows.assign(rows, rows + U);
+    A.cols.assign(cols, cols + U);
+    A.blocks.resize(U);
+    for (std::size_t i = 0; i < U; ++i) A.blocks[i] = load_mat3(blocks + 9 * i);
+    return A;
+}
+
+std::vector<std::pair<Index, Index>> load_edges(const std::int32_t* pairs, std::size_t n) {
+    std::vector<std::pair<Index, Index>> e(n);
+    for (std::size_t i = 0; i < n; ++i) e[i] = {pairs[2 * i], pairs[2 * i + 1]};
+    return e;
+}
+
+VecX load_vec(const double* p, std::size_t n) {
+    VecX v(static_cast<int>(n));
+    if (n) std::memcpy(v.data(), p, n * 8);
+    return v;
+}
+
+template <class V, int W>
+int segment_reduce_w(const std::vector<Index>& o, const double* Vp, std::size_t nV, std::int32_t n_segments,
+                     const ExecPolicy& pol, double* R) {
+    std::vector<V> v(nV);
+    for (std::size_t i = 0; i < nV; ++i) std::memcpy(v[i].data(), Vp + W * i, W * 8);
+    auto r = fast_segment_reduction(o, v, n_segments, pol);
+    for (std::size_t i = 0; i < r.size(); ++i) std::memcpy(R + W * i, r[i].data(), W * 8);
+    return 0;
+}
+
+struct RefMatrix {
+    SortedSymBlockCoo A;
+};
+
+struct RefMas {
+    MasPreconditioner M;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+int ref_max_threads() { return process_thread_default(); }
+void ref_set_default_threads(int n) {
+    if (n > 0) set_default_threads(n);
+}
+
+std::uint64_t ref_make_block_key(std::uint32_t r, std::uint32_t c) { return make_block_key(r, c); }
+
+std::uint64_t ref_emit(std::int32_t r, std::int32_t c, const double* m9, double* out9) {
+    BlockTripletStream s;
+    s.emit(r, c, load_mat3(m9));
+    std::memcpy(out9, s.values[0].data(), 72);
+    return s.keys[0];
+}
+
+void ref_radix_sort_keys(std::uint64_t* keys, std::uint32_t* perm, std::size_t T) {
+    std::vector<std::uint64_t> k(keys, keys + T);
+    std::vector<std::uint32_t> p;
+    detail::radix_sort_keys(k, p);
+    if (T) {
+        std::memcpy(keys, k.data(), T * 8);
+        std::memcpy(perm, p.data(), T * 4);
+    }
+}
+
+void ref_sort_stream(std::uint64_t* keys, double* vals, std::size_t T, int det, int threads, int lw) {
+    BlockTripletStream s = load_stream(keys, vals, T);
+    sort_stream(s, make_pol(det, threads, lw));
+    store_stream(s, keys, vals);
+}
+
+std::int64_t ref_fast_hash_reduction(const std::uint64_t* keys, const double* vals, std::size_t T,
+                                     std::int32_t n_block_rows, int det, int threads, int lw, std::uint32_t* rows,
+                                     std::uint32_t* cols, double* blocks) {
+    const BlockTripletStream s = load_stream(keys, vals, T);
+    const SortedSymBlockCoo A = fast_hash_reduction(s, n_block_rows, make_pol(det, threads, lw));
+    for (std::size_t i = 0; i < A.size(); ++i) {
+        rows[i] = A.rows[i];
+        cols[i] = A.cols[i];
+        std::memcpy(blocks + 9 * i, A.blocks[i].data(), 72);
+    }
+    return static_cast<std::int64_t>(A.size());
+}
+
+int ref_segment_reduce(const std::int32_t* O, std::size_t nO, const double* V, std::size_t nV, int width,
+                       std::int32_t n_segments, int det, int threads, int lw, double* R) {
+    const ExecPolicy pol = make_pol(det, threads, lw);
+    const std::vector<Index> o(O, O + nO);
+    try {
+        if (width == 1) {
+            std::vector<Real> v(V, V + nV);
+            auto r = fast_segment_reduction(o, v, n_segments, pol);
+            if (!r.empty()) std::memcpy(R, r.data(), r.size() * 8);
+            return 0;
+        }
+        if (width == 3) return segment_reduce_w<Vec3, 3>(o, V, nV, n_segments, pol, R);
+        if (width == 9) return segment_reduce_w<Mat3, 9>(o, V, nV, n_segments, pol, R);
+        g_err = "width must be 1, 3 or 9";
+        return 1;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+void ref_srbk_spmv(std::int32_t n_block_rows, std::size_t U, const std::uint32_t* rows, const std::uint32_t* cols,
+                   const double* blocks, const double* x, std::size_t nx, int det, int threads, int lw, double* y) {
+    const SortedSymBlockCoo A = load_matrix(n_block_rows, U, rows, cols, blocks);
+    std::vector<Vec3> xv(nx);
+    for (std::size_t i = 0; i < nx; ++i) std::memcpy(xv[i].data(), x + 3 * i, 24);
+    const auto yv = srbk_spmv(A, xv, make_pol(det, threads, lw));
+    for (std::size_t i = 0; i < nx; ++i) std::memcpy(y + 3 * i, yv[i].data(), 24);
+}
+
+int ref_split(int kind, std::int32_t rb, std::int32_t cb, const double* H, std::uint64_t* keys, double* vals) {
+    BlockTripletStream out;
+    if (kind == 0 || kind == 1) {
+        Mat12 m;
+        std::memcpy(m.data(), H, 144 * 8);
+        if (kind == 0)
+            split_12x12(rb, cb, m, out);
+        else
+            split_sym_12x12(rb, m, out);
+    } else if (kind == 2) {
+        Mat12x3 m;
+        std::memcpy(m.data(), H, 36 * 8);
+        split_12x3(rb, cb, m, out);
+    } else {
+        Mat3x12 m;
+        std::memcpy(m.data(), H, 36 * 8);
+        split_3x12(rb, cb, m, out);
+    }
+    store_stream(out, keys, vals);
+    return static_cast<int>(out.size());
+}
+
+std::int64_t ref_two_level_abd_reduce(const std::uint64_t* keys, const double* vals, std::size_t Tn,
+                                      std::int32_t n_fem, std::int32_t n_bodies, std::size_t n_abd,
+                                      const std::int32_t* abd_node_body, const double* jac36, int det, int threads,
+                                      int lw, std::uint64_t* out_keys, double* out_vals) {
+    const BlockTripletStream s = load_stream(keys, vals, Tn);
+    DofMap m;
+    m.n_fem_nodes = n_fem;
+    m.n_bodies = n_bodies;
+    m.abd_node_body.assign(abd_node_body, abd_node_body + n_abd);
+    m.abd_node_jacobian.resize(n_abd);
+    for (std::size_t i = 0; i < n_abd; ++i) std::memcpy(m.abd_node_jacobian[i].data(), jac36 + 36 * i, 36 * 8);
+    const BlockTripletStream t = two_level_abd_reduce(s, m, make_pol(det, threads, lw));
+    store_stream(t, out_keys, out_vals);
+    return static_cast<std::int64_t>(t.size());
+}
+
+std::int64_t ref_filter_pinned(const std::uint64_t*, const double*, std::size_t, const std::uint8_t*, std::int32_t,
+                               std::uint64_t*, double*) {
+    g_err = "filter_pinned is private to IncrementalPotential in the reference";
+    return -1;
+}
+
+std::int32_t ref_subdomain_count(std::int32_t v, std::int32_t n, std::int32_t n_o) { return subdomain_count(v, n, n_o); }
+
+std::int32_t ref_chunk_partition(std::int32_t v, std::int32_t cap, std::int32_t* part_of) {
+    const Partition p = chunk_partition(v, cap);
+    if (v) std::memcpy(part_of, p.part_of.data(), v * 4);
+    return p.n_parts;
+}
+
+std::int32_t ref_partition_block_graph(std::int32_t v, const std::int32_t* pairs, std::size_t n_edges,
+                                       std::int32_t cap, std::int32_t* part_of) {
+    const Partition p = partition_block_graph(v, load_edges(pairs, n_edges), cap);
+    if (v) std::memcpy(part_of, p.part_of.data(), v * 4);
+    return p.n_parts;
+}
+
+std::int64_t ref_block_edges(std::size_t U, const std::uint32_t* rows, const std::uint32_t* cols,
+                             std::int32_t* pairs) {
+    SortedSymBlockCoo A;
+    A.rows.assign(rows, rows + U);
+    A.cols.assign(cols, cols + U);
+    const auto e = block_edges(A);
+    for (std::size_t i = 0; i < e.size(); ++i) {
+        pairs[2 * i] = e[i].first;
+        pairs[2 * i + 1] = e[i].second;
+    }
+    return static_cast<std::int64_t>(e.size());
+}
+
+void* ref_build_hierarchy(const std::int32_t* part_of, std::int32_t n_slots, std::int32_t n_parts,
+                          std::int32_t capacity, const std::int32_t* pairs, std::size_t n_edges, int max_levels) {
+    Partition l0;
+    l0.part_of.assign(part_of, part_of + n_slots);
+    l0.n_parts = n_parts;
+    l0.capacity = capacity;
+    return new MasHierarchy(build_hierarchy(l0, load_edges(pairs, n_edges), max_levels));
+}
+void ref_hierarchy_free(void* h) { delete static_cast<MasHierarchy*>(h); }
+int ref_hierarchy_n_levels(void* h) { return static_cast<MasHierarchy*>(h)->n_levels(); }
+void ref_hierarchy_level(void* hp, int l, std::int32_t* n_nodes, std::int32_t* n_parts, std::int32_t* part_of,
+                         std::int32_t* agg) {
+    const auto& L = static_cast<MasHierarchy*>(hp)->levels[l];
+    *n_nodes = L.n_nodes;
+    *n_parts = L.n_parts;
+    if (part_of && L.n_nodes) std::memcpy(part_of, L.part_of.data(), L.n_nodes * 4);
+    if (agg && !L.agg.empty()) std::memcpy(agg, L.agg.data(), L.agg.size() * 4);
+}
+
+void* ref_matrix_new(std::int32_t n_block_rows, std::size_t U, const std::uint32_t* rows, const std::uint32_t* cols,
+                     const double* blocks) {
+    return new RefMatrix{load_matrix(n_block_rows, U, rows, cols, blocks)};
+}
+void ref_matrix_free(void* m) { delete static_cast<RefMatrix*>(m); }
+
+void* ref_mas_build(void* mat, void* hier) {
+    auto* M = new MasPreconditioner();
+    try {
+        M->build(static_cast<RefMatrix*>(mat)->A, *static_cast<MasHierarchy*>(hier));
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        delete M;
+        return nullptr;
+    }
+    return static_cast<Preconditioner*>(M);
+}
+void ref_precond_free(void* p) { delete static_cast<Preconditioner*>(p); }
+long ref_mas_shifts(void*) { return -1; }
+int ref_mas_n_levels(void* p) { return static_cast<MasPreconditioner*>(static_cast<Preconditioner*>(p))->n_levels(); }
+int ref_mas_level_matrix(void* p, int l, std::int32_t s, double* out) {
+    const auto* M = static_cast<MasPreconditioner*>(static_cast<Preconditioner*>(p));
+    const MatX& D = M->level_matrices(l)[s];
+    if (out) std::memcpy(out, D.data(), D.size() * 8);
+    return D.rows();
+}
+
+void* ref_jacobi_build(void* mat) {
+    auto* J = new BlockJacobiPreconditioner();
+    J->build(static_cast<RefMatrix*>(mat)->A);
+    return static_cast<Preconditioner*>(J);
+}
+
+void ref_precond_apply(void* p, const double* r, std::size_t n, double* z) {
+    const VecX rv = load_vec(r, n);
+    VecX zv;
+    static_cast<Preconditioner*>(p)->apply(rv, zv);
+    std::memcpy(z, zv.data(), n * 8);
+}
+
+int ref_pcg_solve(void* mat, const double* b, std::size_t n, void* precond, double rel_tol, int restart,
+                  int max_iters, int det, int threads, int lw, double* x, int* iters, double* rel_residual,
+                  int* converged) {
+    const VecX bv = load_vec(b, n);
+    VecX xv;
+    const PcgResult r = pcg_solve(static_cast<RefMatrix*>(mat)->A, bv, *static_cast<Preconditioner*>(precond),
+                                  rel_tol, restart, max_iters, make_pol(det, threads, lw), xv);
+    std::memcpy(x, xv.data(), n * 8);
+    *iters = r.iters;
+    *rel_residual = r.rel_residual;
+    *converged = r.converged ? 1 : 0;
+    return 0;
+}
+
+}  // extern "C"

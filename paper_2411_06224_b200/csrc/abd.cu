@@ -71,10 +71,13 @@ __device__ __forceinline__ void jtcj_tile(const Map& m, std::int32_t i, std::int
         for (int k = 0; k < 3; ++k)
             jtc[3 * a + k] = mac3(m.J(i, 0, 3 * ti + a), C[3 * k + 0], m.J(i, 1, 3 * ti + a), C[3 * k + 1],
                                   m.J(i, 2, 3 * ti + a), C[3 * k + 2]);
+    // (J^T C) J is an Eigen GEMM (12x3 * 3x12: accumulators start at zero),
+    // so a -0.0 entry comes out +0.0: the trailing + 0.0 reproduces that
     for (int b = 0; b < 3; ++b)
         for (int a = 0; a < 3; ++a)
-            out[3 * b + a] = mac3(jtc[3 * a + 0], m.J(j, 0, 3 * tj + b), jtc[3 * a + 1], m.J(j, 1, 3 * tj + b),
-                                  jtc[3 * a + 2], m.J(j, 2, 3 * tj + b));
+            out[3 * b + a] = __dadd_rn(mac3(jtc[3 * a + 0], m.J(j, 0, 3 * tj + b), jtc[3 * a + 1],
+                                            m.J(j, 1, 3 * tj + b), jtc[3 * a + 2], m.J(j, 2, 3 * tj + b)),
+                                       0.0);
 }
 
 __global__ void k_abd_emit(const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,

@@ -186,21 +186,21 @@ __global__ void k_jacobi_build(std::int32_t n, const std::uint32_t* __restrict__
         for (std::int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
             if (cols[e] == static_cast<std::uint32_t>(i)) {
                 for (int k = 0; k < 9; ++k) a[k] = blocks[blk(e, k)];
-                // adjugate inverse (Mat3::inverse), a column-major: A(r,c) = a[3c+r]
+                // Mat3::inverse as Eigen computes a fixed 3x3 (block_jacobi.hpp:13):
+                // cyclic cofactors, det down column 0, times 1/det; explicit
+                // _rn ops so nvcc cannot contract into FMAs (bitwise with CPU)
                 auto A = [&](int r, int c) { return a[3 * c + r]; };
-                double cof[9];
-                auto C = [&](int r, int c) -> double& { return cof[3 * c + r]; };
-                C(0, 0) = A(1, 1) * A(2, 2) - A(1, 2) * A(2, 1);
-                C(1, 0) = A(1, 2) * A(2, 0) - A(1, 0) * A(2, 2);
-                C(2, 0) = A(1, 0) * A(2, 1) - A(1, 1) * A(2, 0);
-                const double det = A(0, 0) * C(0, 0) + A(0, 1) * C(1, 0) + A(0, 2) * C(2, 0);
-                C(0, 1) = A(0, 2) * A(2, 1) - A(0, 1) * A(2, 2);
-                C(1, 1) = A(0, 0) * A(2, 2) - A(0, 2) * A(2, 0);
-                C(2, 1) = A(0, 1) * A(2, 0) - A(0, 0) * A(2, 1);
-                C(0, 2) = A(0, 1) * A(1, 2) - A(0, 2) * A(1, 1);
-                C(1, 2) = A(0, 2) * A(1, 0) - A(0, 0) * A(1, 2);
-                C(2, 2) = A(0, 0) * A(1, 1) - A(0, 1) * A(1, 0);
-                for (int k = 0; k < 9; ++k) a[k] = cof[k] / det;
+                auto cof = [&](int i, int j) {
+                    const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+                    return __dsub_rn(__dmul_rn(A(i1, j1), A(i2, j2)), __dmul_rn(A(i1, j2), A(i2, j1)));
+                };
+                const double det = __dadd_rn(__dadd_rn(__dmul_rn(cof(0, 0), A(0, 0)), __dmul_rn(cof(1, 0), A(1, 0))),
+                                             __dmul_rn(cof(2, 0), A(2, 0)));
+                const double invdet = __ddiv_rn(1.0, det);
+                double inv[9];
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) inv[3 * j + i] = __dmul_rn(cof(j, i), invdet);
+                for (int k = 0; k < 9; ++k) a[k] = inv[k];
                 break;
             }
         for (int k = 0; k < 9; ++k) jinv[9 * i + k] = a[k];

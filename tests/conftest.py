@@ -30,3 +30,17 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(params=["restated", "reference"])
+def oracle_backend(request):
+    """Run an oracle test on the restatement (oracle/oracle.hpp) and on the
+    reference's own hot-path code compiled in place (oracle/_ref, built by
+    `make -C oracle ref` from /root/reference). The reference leg pins the
+    restatement and the Python ports of the reference tests alike."""
+    import oracle_py as O
+
+    if request.param == "reference" and not O.reference_available():
+        pytest.skip("oracle/_ref not built and /root/reference absent")
+    with O.use_backend(request.param):
+        yield request.param

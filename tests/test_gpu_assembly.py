@@ -204,3 +204,22 @@ def test_assemble_filtered_bitwise(ctx, name):
     torch.cuda.synchronize()  # the context runs on its own non-blocking stream
     ctx.assemble_filtered(dk, dv, sc.n_blocks, dp)
     assert_bitwise(ctx.copy_matrix()[1:], want)
+
+
+@pytest.mark.parametrize("name", ["cfg4_hybrid", "stiff_beam"])
+def test_against_compiled_reference(ctx, name):
+    """GPU output against the reference's own code (oracle/_ref) directly:
+    two-level tiles and the assembled matrix, bit-exact."""
+    if not O.reference_available():
+        pytest.skip("oracle/_ref unavailable")
+    sc = scenes.CONFIGS[name]()
+    keys, vals = O.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    with O.use_backend("reference"):
+        if sc.n_bodies:
+            args = (sc.node_keys, sc.node_vals, sc.n_fem, sc.n_bodies, sc.abd_body, sc.jac36)
+            tk, tv = ctx.two_level_abd_reduce(*args)
+            rk, rv = O.two_level_abd_reduce(*args, DET)
+            assert np.array_equal(tk, rk) and np.array_equal(tv.view(np.uint8), rv.view(np.uint8))
+            keys, vals = np.concatenate([keys, rk]), np.concatenate([vals, rv])
+        want = oracle_assemble(keys, vals, sc.n_blocks)
+    assert_bitwise(gpu_assemble(ctx, keys, vals, sc.n_blocks), want)

@@ -4,10 +4,14 @@ the same budgets (deterministic exact, parallel 1e-12, two-level 1e-10).
 The per-case inputs are produced by the generators in kernel_cases.py, which
 the GPU parity tests reuse."""
 import numpy as np
+import pytest
 
 import oracle_py as O
 from helpers import dense_from, map_accumulate
 from kernel_cases import abd_cases, hash_cases, segment_cases, spmv_cases
+
+# every test runs on the restatement and on the compiled reference (conftest)
+pytestmark = pytest.mark.usefixtures("oracle_backend")
 
 DET = O.ExecPolicy(deterministic=True)
 PAR = O.ExecPolicy(threads=4, lane_width=8)

@@ -2,9 +2,13 @@
 tests: proj/tests/test_block_sparse.cpp (each case cites its lines) with the
 same seeds and the same libstdc++ std::mt19937 draw sequences."""
 import numpy as np
+import pytest
 
 import oracle_py as O
 from helpers import Stream, abd_jacobian, cm, dense_from, map_accumulate, nat, vec3_draw
+
+# every test runs on the restatement and on the compiled reference (conftest)
+pytestmark = pytest.mark.usefixtures("oracle_backend")
 
 DET = O.ExecPolicy(deterministic=True)
 

@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cache", action="store_true", help="rebuild the MAS hierarchy every step")
+    ap.add_argument("--no-solve-order", action="store_true",
+                    help="run the MAS/PCG in the reference slot numbering (A/B of the solve-order renumbering)")
     ap.add_argument("--cpu-iters", type=int, default=10, help="PCG iterations per CPU sample step")
     return ap.parse_args()
 
@@ -237,6 +239,7 @@ def run_ours(args, rank, world, local_rank, dist):
     stream = torch.cuda.Stream(dev)
     ctx = Context(local_rank, stream=stream)
     ctx.set_option(_lib.OPT_PROFILE, 0)  # timed steps: graph-replayed iterations, no profiling events
+    ctx.set_option(_lib.OPT_SOLVE_ORDER, 0 if args.no_solve_order else 1)
     l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, CAPACITY)
     ctx.set_level0_partition(l0.part_of, l0.n_parts, CAPACITY, MAX_LEVELS)
 

@@ -46,6 +46,8 @@ extern "C" {
 #define ADIPC_OPT_CACHE_HIERARCHY 1 /* reuse the MAS hierarchy while the sparsity is unchanged */
 #define ADIPC_OPT_PROFILE 2         /* time each PCG kernel class with CUDA events */
 #define ADIPC_OPT_L2_PERSIST 3      /* value/1024 of the matrix tiles kept L2-resident (evict-last) across SpMVs */
+#define ADIPC_OPT_SOLVE_ORDER 4     /* 1 (default): MAS/PCG renumber slots by level-0 subdomain internally */
+#define ADIPC_OPT_SPMV_VARIANT 5    /* SpMV kernel: 0 LDG-streamed tiles, 2/3/4 TMA-staged (stages per warp; default 3) */
 
 typedef struct adipc_gpu_ctx adipc_gpu_ctx;
 typedef struct adipc_hierarchy adipc_hierarchy;

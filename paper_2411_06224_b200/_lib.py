@@ -25,6 +25,8 @@ PRECOND_MAS, PRECOND_JACOBI = 1, 2
 OPT_CACHE_HIERARCHY = 1
 OPT_PROFILE = 2
 OPT_L2_PERSIST = 3
+OPT_SOLVE_ORDER = 4
+OPT_SPMV_VARIANT = 5
 
 # Every symbol include/adipc_gpu.h declares, with its ctypes signature.
 GPU_SIGNATURES = {

@@ -126,6 +126,15 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.levels.clear();
     c.jinv.free();
     c.build_status.free();
+    c.perm.free();
+    c.perm_keys.free();
+    c.perm_vals.free();
+    c.pv_in.free();
+    c.pv_out.free();
+    c.As.rows.free();
+    c.As.cols.free();
+    c.As.blocks.free();
+    c.As.row_ptr.free();
     for (auto* b : {&c.w.x, &c.w.r, &c.w.p, &c.w.ap, &c.w.z, &c.w.b, &c.w.tmp, &c.w.partials, &c.w.scal}) b->free();
     c.w.tickets.free();
     c.w.flags.free();
@@ -172,8 +181,15 @@ int adipc_gpu_set_option(adipc_gpu_ctx* ctx, int option, int value) {
                 ADIPC_CUDA(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, ctx->c.device));
                 ADIPC_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<std::size_t>(mx)));
             }
-        }
-        else
+        } else if (option == ADIPC_OPT_SPMV_VARIANT) {
+            if (value != 0 && (value < 2 || value > 4)) throw StatusError(kInvalidArgument, "SpMV variant not in {0,2,3,4}");
+            ctx->c.spmv_variant = value;
+        } else if (option == ADIPC_OPT_SOLVE_ORDER) {
+            ctx->c.solve_order = value != 0;
+            ctx->c.hier_version = ~0ull;  // the device levels depend on the numbering
+            ctx->c.levels.clear();
+            ctx->c.pkind = kNone;
+        } else
             throw StatusError(kInvalidArgument, "unknown option");
     });
 }

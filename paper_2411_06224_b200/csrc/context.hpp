@@ -109,6 +109,25 @@ struct Ctx {
 
     PcgWork w;
 
+    // Solve order (MAS): the PCG and the preconditioner run on A renumbered so
+    // that every level-0 subdomain is a contiguous slot range,
+    // perm[i] = first slot of subdomain part_of[i] + rank of i inside it
+    // (pos_of order, mas.hpp:42-45, is preserved, so the subdomain matrices
+    // and inverses are the reference's). The vectors of the level-0 solve,
+    // the update pass and the prolongation become unit-stride streams and the
+    // SpMV gathers gain locality. Internal only: the C-ABI takes and returns
+    // vectors and matrices in the reference's numbering.
+    bool solve_order = true;       // ADIPC_OPT_SOLVE_ORDER
+    bool perm_active = false;      // the current preconditioner / solve matrix use `perm`
+    bool levels_permuted = false;  // the device levels were built in solve order
+    DBuf<std::int32_t> perm;       // reference slot -> solve slot
+    DeviceMatrix As;               // A in solve order (upper triangle re-canonicalised)
+    DBuf<std::uint64_t> perm_keys; // scratch stream for building As
+    DBuf<double> perm_vals;
+    DBuf<double> pv_in, pv_out;    // rhs / solution in solve order
+    const DeviceMatrix& S() const { return perm_active ? As : A; }
+    DeviceMatrix& S() { return perm_active ? As : A; }
+
     // side stream + fork/join events: the coarse MAS chain runs concurrently
     // with the level-0 solve inside each PCG iteration
     cudaStream_t side = nullptr;
@@ -120,6 +139,9 @@ struct Ctx {
     // fraction (x/1024) of A's tiles the SpMV loads with L2 evict-last
     // priority (ADIPC_OPT_L2_PERSIST)
     int l2_persist_1024 = 0;
+    // SpMV kernel variant (ADIPC_OPT_SPMV_VARIANT): 0 LDG-streamed tiles,
+    // 2/3/4 TMA-staged tiles with that many chunks in flight per warp
+    int spmv_variant = 3;
 
     // per-kernel-class PCG timing (ADIPC_OPT_PROFILE): spmv, level 0, coarse, final
     bool profile = false;
@@ -159,12 +181,16 @@ std::int64_t two_level_abd_reduce(Ctx& c, const std::uint64_t* d_keys, const dou
 
 // spmv.cu
 void spmv(Ctx& c, const double* d_x, double* d_y, double* d_pdot_partials, int n_partials);
-int spmv_grid(const Ctx& c);
+int spmv_grid(const Ctx& c, const DeviceMatrix& M);
+void spmv_launch(Ctx& c, const DeviceMatrix& M, const double* d_x, double* d_y, bool zero_y, const int* flags,
+                 double* partials, unsigned* ticket, double* dot_out);
 
 // mas.cu
 void build_preconditioner(Ctx& c, PrecondKind kind);
 void build_mas_from_hierarchy(Ctx& c, const host::MasHierarchy& h);
 void precond_apply(Ctx& c, const double* d_r, double* d_z);
+// vectors between the reference numbering and the solve order (Ctx::perm)
+void permute_vec(Ctx& c, const double* src, double* dst, bool to_solve);
 
 // pcg.cu
 struct PcgOut {

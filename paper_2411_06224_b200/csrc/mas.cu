@@ -284,12 +284,86 @@ void link_levels(Ctx& c, const host::MasHierarchy& h) {
     }
 }
 
+// A in solve order as a triplet stream: (perm[r], perm[c]) re-canonicalised to
+// the upper triangle (the block transposed when the order flips, as
+// BlockTripletStream::emit does, block_coo.hpp:36-43), AoS column-major values.
+__global__ void k_permute_stream(const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,
+                                 const double* __restrict__ blocks, std::int64_t U,
+                                 const std::int32_t* __restrict__ perm, std::uint64_t* __restrict__ keys,
+                                 double* __restrict__ vals) {
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < U;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t r = static_cast<std::uint32_t>(perm[rows[e]]);
+        const std::uint32_t c = static_cast<std::uint32_t>(perm[cols[e]]);
+        double h[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) h[k] = blocks[blk(e, k)];
+        const bool flip = r > c;
+        keys[e] = flip ? (static_cast<std::uint64_t>(c) << 32 | r) : (static_cast<std::uint64_t>(r) << 32 | c);
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) vals[9 * e + 3 * j + i] = flip ? h[3 * i + j] : h[3 * j + i];
+    }
+}
+
+// Solve order of a hierarchy: slots renumbered so each level-0 subdomain is a
+// contiguous range, members in ascending reference id (= pos_of order).
+// Uploads the slot map to c.perm and returns the hierarchy in solve order
+// (level 0: part_of by solve slot, agg identity; coarser levels: agg by solve
+// slot; node-level data unchanged).
+host::MasHierarchy to_solve_order(Ctx& c, const host::MasHierarchy& h) {
+    const host::Level& l0 = h.levels[0];
+    const std::int32_t n = h.n_slots;
+    std::vector<std::int32_t> start(static_cast<std::size_t>(l0.n_parts) + 1, 0), perm(n);
+    for (std::int32_t i = 0; i < n; ++i) ++start[l0.part_of[i] + 1];
+    for (std::int32_t s = 0; s < l0.n_parts; ++s) start[s + 1] += start[s];
+    for (std::int32_t i = 0; i < n; ++i) perm[i] = start[l0.part_of[i]]++;
+    upload(c.perm, perm, c.stream);
+    host::MasHierarchy hp = h;
+    for (std::int32_t i = 0; i < n; ++i) hp.levels[0].part_of[perm[i]] = l0.part_of[i];
+    for (std::size_t l = 1; l < h.levels.size(); ++l)
+        for (std::int32_t i = 0; i < n; ++i) hp.levels[l].agg[perm[i]] = h.levels[l].agg[i];
+    return hp;
+}
+
+// (Re)build the device levels of hierarchy h, in solve order when enabled.
+void set_levels(Ctx& c, const host::MasHierarchy& h) {
+    c.levels.clear();
+    const bool perm = c.solve_order && h.n_levels() > 0 && h.n_slots > 0;
+    const host::MasHierarchy hp = perm ? to_solve_order(c, h) : host::MasHierarchy{};
+    const host::MasHierarchy& hl = perm ? hp : h;
+    for (int l = 0; l < hl.n_levels(); ++l) {
+        c.levels.emplace_back(new DeviceLevel());
+        build_level(c, *c.levels.back(), hl.levels[l], l, c.A.n);
+    }
+    link_levels(c, hl);
+    c.levels_permuted = perm;
+}
+
 }  // namespace
+
+void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
+                 DeviceMatrix& out);
+
+// As = P A P^T in solve order (sorted upper block triangle, the same layout
+// as A), rebuilt from the current A values on every preconditioner build.
+void build_solve_matrix(Ctx& c) {
+    const DeviceMatrix& A = c.A;
+    c.perm_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(A.U, 1)));
+    c.perm_vals.reserve(9 * static_cast<std::size_t>(std::max<std::int64_t>(A.U, 1)));
+    if (A.U > 0) {
+        k_permute_stream<<<grid_for(A.U, 256, 16), 256, 0, c.stream>>>(A.rows.p, A.cols.p, A.blocks.p, A.U, c.perm.p,
+                                                                      c.perm_keys.p, c.perm_vals.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    sort_reduce(c, c.perm_keys.p, c.perm_vals.p, A.U, A.n, c.As);
+}
 
 // K9 restriction + K10 batched factorisation/inversion for the current levels.
 void factorize(Ctx& c) {
     cudaStream_t st = c.stream;
-    const DeviceMatrix& A = c.A;
+    const DeviceMatrix& A = c.S();
     RestrictArgs ra{};
     ra.n_levels = static_cast<int>(c.levels.size());
     for (int l = 0; l < ra.n_levels; ++l) {
@@ -374,6 +448,7 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
             ADIPC_LAUNCH_CHECK();
         }
         c.pkind = kJacobi;
+        c.perm_active = false;
         return;
     }
     if (!c.have_l0) throw StatusError(kInvalidArgument, "level-0 partition not set (adipc_gpu_set_level0_partition)");
@@ -403,12 +478,7 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
             }
         c.hier = host::build_hierarchy(c.l0, pairs.data(), pairs.size() / 2, c.max_levels);
         if (c.hier.n_levels() > kMaxLevels) throw StatusError(kInvalidArgument, "too many MAS levels");
-        c.levels.clear();
-        for (int l = 0; l < c.hier.n_levels(); ++l) {
-            c.levels.emplace_back(new DeviceLevel());
-            build_level(c, *c.levels.back(), c.hier.levels[l], l, A.n);
-        }
-        link_levels(c, c.hier);
+        set_levels(c, c.hier);
         c.hier_version = c.cache_hierarchy ? phash : ~0ull;
     } else {
         for (auto& L : c.levels)
@@ -416,6 +486,8 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
     }
     const auto t1 = std::chrono::steady_clock::now();
     c.ms_build_host = std::chrono::duration<float, std::milli>(t1 - t0).count();
+    c.perm_active = c.levels_permuted;
+    if (c.perm_active) build_solve_matrix(c);
     factorize(c);
 }
 
@@ -423,14 +495,11 @@ void build_mas_from_hierarchy(Ctx& c, const host::MasHierarchy& h) {
     const auto t0 = std::chrono::steady_clock::now();
     if (h.n_levels() > kMaxLevels) throw StatusError(kInvalidArgument, "too many MAS levels");
     c.hier = h;
-    c.levels.clear();
-    for (int l = 0; l < c.hier.n_levels(); ++l) {
-        c.levels.emplace_back(new DeviceLevel());
-        build_level(c, *c.levels.back(), c.hier.levels[l], l, c.A.n);
-    }
-    link_levels(c, c.hier);
+    set_levels(c, c.hier);
     c.hier_version = ~0ull;  // explicit hierarchies are never reused by the cache
     c.ms_build_host = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    c.perm_active = c.levels_permuted;
+    if (c.perm_active) build_solve_matrix(c);
     factorize(c);
 }
 
@@ -551,10 +620,44 @@ template void launch_jacobi<M_INIT>(Ctx&, const double*, double*, const PcgArgs&
 template void launch_jacobi<M_UPDATE>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
 template void launch_jacobi<M_RESTART>(Ctx&, const double*, double*, const PcgArgs&, double*, unsigned*, double*);
 
+namespace {
+__global__ void k_permute_vec(std::int32_t n, const std::int32_t* __restrict__ perm, const double* __restrict__ src,
+                              double* __restrict__ dst, bool to_solve) {
+    const std::int64_t n3 = 3 * static_cast<std::int64_t>(n);
+    for (std::int64_t g = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; g < n3;
+         g += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t i = g / 3, k = g - 3 * i;
+        const std::int64_t q = 3 * static_cast<std::int64_t>(perm[i]) + k;
+        if (to_solve)
+            dst[q] = src[g];
+        else
+            dst[g] = src[q];
+    }
+}
+}  // namespace
+
+void permute_vec(Ctx& c, const double* src, double* dst, bool to_solve) {
+    if (c.A.n == 0) return;
+    k_permute_vec<<<slot_grid(c), 256, 0, c.stream>>>(c.A.n, c.perm.p, src, dst, to_solve);
+    ADIPC_LAUNCH_CHECK();
+}
+
 // z = M r (MasPreconditioner::apply / BlockJacobiPreconditioner::apply).
 void precond_apply(Ctx& c, const double* d_r, double* d_z) {
     PcgArgs a{};
     if (c.A.n == 0) return;
+    if (c.pkind == kMas && c.perm_active) {  // run in solve order
+        const std::size_t n3 = 3 * static_cast<std::size_t>(c.A.n);
+        c.pv_in.reserve(n3);
+        c.pv_out.reserve(n3);
+        permute_vec(c, d_r, c.pv_in.p, true);
+        launch_level<M_APPLY, true>(c, 0, c.pv_in.p, c.pv_out.p, a, nullptr, nullptr, nullptr, c.stream, true);
+        for (int l = 1; l < static_cast<int>(c.levels.size()); ++l)
+            launch_level<M_COARSE, true>(c, l, nullptr, nullptr, a, nullptr, nullptr, nullptr, c.stream, true);
+        launch_final<F_APPLY>(c, c.pv_out.p, nullptr, nullptr, a);
+        permute_vec(c, c.pv_out.p, d_z, false);
+        return;
+    }
     if (c.pkind == kJacobi) {
         launch_jacobi<M_APPLY>(c, d_r, d_z, a, nullptr, nullptr, nullptr);
     } else if (c.pkind == kMas) {

@@ -26,9 +26,6 @@
 
 namespace adipc_gpu {
 
-void spmv_launch(Ctx& c, const double* d_x, double* d_y, bool zero_y, const int* flags, double* partials,
-                 unsigned* ticket, double* dot_out);
-int spmv_grid(const Ctx& c);
 int level_grid(const Ctx& c, int l);
 int slot_grid(const Ctx& c);
 int jacobi_grid(const Ctx& c);
@@ -79,7 +76,7 @@ struct GraphExec {
 
 }  // namespace
 
-PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters, double* d_x) {
+static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters, double* d_x) {
     PcgOut out;
     cudaStream_t st = c.stream;
     const std::int32_t n = c.A.n;
@@ -93,7 +90,7 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
     w.ap.reserve(n3);
     w.z.reserve(n3);
     w.tmp.reserve(n3);
-    int pmax = std::max({spmv_grid(c), slot_grid(c), kSMs * 8, jacobi_grid(c)});
+    int pmax = std::max({spmv_grid(c, c.S()), slot_grid(c), kSMs * 8, jacobi_grid(c)});
     for (int l = 0; l < n_levels; ++l) pmax = std::max(pmax, level_grid(c, l));
     w.partials.reserve(static_cast<std::size_t>(pmax) * T_COUNT);
     w.tickets.reserve(T_COUNT);
@@ -191,14 +188,14 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
     // one iteration's launch sequence (restart variant: x += alpha p, r = b - A x)
     auto iteration = [&](bool is_restart, int slot) {
         mark(slot, 0);
-        spmv_launch(c, w.p.p, w.ap.p, false, w.flags.p, partials_of(T_SPMV), w.tickets.p + T_SPMV, w.scal.p + S_PAP);
+        spmv_launch(c, c.S(), w.p.p, w.ap.p, false, w.flags.p, partials_of(T_SPMV), w.tickets.p + T_SPMV, w.scal.p + S_PAP);
         mark(slot, 1);
         if (is_restart) {
             k_x_update<<<slot_grid(c), 256, 0, st>>>(n3, a);
             ADIPC_LAUNCH_CHECK();
             k_zero<<<slot_grid(c), 256, 0, st>>>(w.tmp.p, n3, w.flags.p);
             ADIPC_LAUNCH_CHECK();
-            spmv_launch(c, d_x, w.tmp.p, false, w.flags.p, nullptr, nullptr, nullptr);
+            spmv_launch(c, c.S(), d_x, w.tmp.p, false, w.flags.p, nullptr, nullptr, nullptr);
             PcgArgs ar = a;
             ar.ap = w.tmp.p;
             if (mas)
@@ -305,6 +302,18 @@ PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters
     }
     c.last_iters = out.iters;
     return out;
+}
+
+// The MAS solve runs in solve order (Ctx::perm): b is permuted in and x out.
+PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters, double* d_x) {
+    if (!(c.pkind == kMas && c.perm_active)) return pcg_impl(c, d_b, rel_tol, restart, max_iters, d_x);
+    const std::size_t n3 = 3 * static_cast<std::size_t>(c.A.n);
+    c.pv_in.reserve(n3);
+    c.pv_out.reserve(n3);
+    permute_vec(c, d_b, c.pv_in.p, true);
+    const PcgOut o = pcg_impl(c, c.pv_in.p, rel_tol, restart, max_iters, c.pv_out.p);
+    permute_vec(c, c.pv_out.p, d_x, false);
+    return o;
 }
 
 }  // namespace adipc_gpu

@@ -9,6 +9,8 @@
 // Optional fusion for PCG: the same pass accumulates p.(A p) directly from the
 // blocks, p_r.(H p_c) * (r != c ? 2 : 1), so the dot needs no second sweep
 // over Ap; the grid total is finished by the last CTA (deterministic order).
+#include <algorithm>
+
 #include "context.hpp"
 #include "tma.cuh"
 
@@ -67,19 +69,19 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
         double yr0 = 0, yr1 = 0, yr2 = 0;
         if (valid) {
             const std::uint32_t cx = dbg == 3 ? r : c;  // dbg 3: no column gather
-            const double xc0 = __ldg(x + 3 * cx), xc1 = __ldg(x + 3 * cx + 1), xc2 = __ldg(x + 3 * cx + 2);
+            const double xc0 = ldg_issue(x + 3 * cx), xc1 = ldg_issue(x + 3 * cx + 1), xc2 = ldg_issue(x + 3 * cx + 2);
+            const double xr0 = ldg_issue(x + 3 * r), xr1 = ldg_issue(x + 3 * r + 1), xr2 = ldg_issue(x + 3 * r + 2);
             // column-major H(i,j) = h[3j+i]
             yr0 = h[0] * xc0 + h[3] * xc1 + h[6] * xc2;
             yr1 = h[1] * xc0 + h[4] * xc1 + h[7] * xc2;
             yr2 = h[2] * xc0 + h[5] * xc1 + h[8] * xc2;
-            const double xr0 = __ldg(x + 3 * r), xr1 = __ldg(x + 3 * r + 1), xr2 = __ldg(x + 3 * r + 2);
             if (r != c && dbg != 1 && dbg != 2) {
                 const double yc0 = h[0] * xr0 + h[1] * xr1 + h[2] * xr2;
                 const double yc1 = h[3] * xr0 + h[4] * xr1 + h[5] * xr2;
                 const double yc2 = h[6] * xr0 + h[7] * xr1 + h[8] * xr2;
-                atomicAdd(y + 3 * c, yc0);
-                atomicAdd(y + 3 * c + 1, yc1);
-                atomicAdd(y + 3 * c + 2, yc2);
+                red_add(y + 3 * c, yc0);
+                red_add(y + 3 * c + 1, yc1);
+                red_add(y + 3 * c + 2, yc2);
             }
             if (kDot) dsum += (r != c ? 2.0 : 1.0) * (xr0 * yr0 + xr1 * yr1 + xr2 * yr2);
         }
@@ -98,71 +100,276 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
         }
         const std::uint32_t rprev = __shfl_up_sync(0xffffffffu, r, 1);
         if (valid && (lane == 0 || rprev != r) && dbg != 2) {
-            atomicAdd(y + 3 * r, yr0);
-            atomicAdd(y + 3 * r + 1, yr1);
-            atomicAdd(y + 3 * r + 2, yr2);
+            red_add(y + 3 * r, yr0);
+            red_add(y + 3 * r + 1, yr1);
+            red_add(y + 3 * r + 2, yr2);
         }
     }
     if (kDot) grid_sum_last_block(dsum, partials, ticket, dot_out);
 }
 
+// TMA-staged variant. On B200 the L1 data pipe moves one 32-byte sector per
+// wavefront for LDG traffic, so streaming the matrix tiles through LDG costs
+// as many L1 cycles as the scattered x gathers and y atomics together (ncu:
+// ~146 sectors per 32-block chunk, 61 % of the L1 wavefront peak at 82 us).
+// Here the tiles (2,304 B of blocks + 128 B rows + 128 B cols, one contiguous
+// chunk each) arrive by cp.async.bulk into a per-warp ring of kStages shared
+// buffers, bypassing the LSU; the warp reads them back with conflict-free
+// 128-byte-per-wavefront LDS, and the LDG path carries only the x gathers.
+struct __align__(16) ChunkStage {
+    double blk[288];
+    std::uint32_t rows[32];
+    std::uint32_t cols[32];
+};
+constexpr int kTmaWarps = 8;
+constexpr std::uint32_t kChunkBytes = sizeof(ChunkStage);
+
+template <bool kDot, int kStages>
+__global__ void __launch_bounds__(32 * kTmaWarps) k_spmv_tma(const std::uint32_t* __restrict__ rows,
+                                                             const std::uint32_t* __restrict__ cols,
+                                                             const double* __restrict__ blocks, std::int64_t U,
+                                                             const double* __restrict__ x, double* __restrict__ y,
+                                                             double* __restrict__ partials,
+                                                             unsigned* __restrict__ ticket, double* __restrict__ dot_out,
+                                                             const int* __restrict__ flags, int dbg = 0) {
+    if (flags && flags[0]) return;  // PCG already finished (F_DONE)
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    ChunkStage* stage = reinterpret_cast<ChunkStage*>(smem) + w * kStages;
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(smem + sizeof(ChunkStage) * kStages * kTmaWarps) + w * kStages;
+    const std::int64_t warp0 = static_cast<std::int64_t>(blockIdx.x) * kTmaWarps + w;
+    const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * kTmaWarps;
+    const std::int64_t n_chunks = (U + 31) >> 5;
+    const std::int64_t ch0 = warp0 * n_chunks / nwarps, ch1 = (warp0 + 1) * n_chunks / nwarps;
+    auto issue = [&](std::int64_t ch, int s) {  // lane 0 only
+        mbar_arrive_expect_tx(&bar[s], kChunkBytes);
+        bulk_g2s_evict_first(stage[s].blk, blocks + ch * 288, 288 * 8, &bar[s]);
+        bulk_g2s_evict_first(stage[s].rows, rows + ch * 32, 128, &bar[s]);
+        bulk_g2s_evict_first(stage[s].cols, cols + ch * 32, 128, &bar[s]);
+    };
+    if (lane == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+        for (int s = 0; s < kStages && ch0 + s < ch1; ++s) issue(ch0 + s, s);
+    }
+    __syncwarp();
+    // Gathers run one chunk ahead: while chunk ch is multiplied, the x[col]
+    // and x[row] loads of chunk ch+1 (whose indices are already staged) are in
+    // flight, so the L2 round trip of the gathers is off the critical path.
+    std::uint32_t r = 0xFFFFFFFFu, c = 0;
+    double g[6];
+    auto gather = [&](std::int64_t ch, int s, std::uint32_t par, std::uint32_t& rr, std::uint32_t& cc, double* gg) {
+        mbar_wait(&bar[s], par);
+        const bool valid = (ch << 5) + lane < U;
+        rr = valid ? stage[s].rows[lane] : 0xFFFFFFFFu;
+        cc = valid ? stage[s].cols[lane] : 0u;
+        const std::uint32_t rx = valid ? rr : 0u;
+        gg[0] = ldg_issue(x + 3 * cc);
+        gg[1] = ldg_issue(x + 3 * cc + 1);
+        gg[2] = ldg_issue(x + 3 * cc + 2);
+        gg[3] = ldg_issue(x + 3 * rx);
+        gg[4] = ldg_issue(x + 3 * rx + 1);
+        gg[5] = ldg_issue(x + 3 * rx + 2);
+    };
+    if (ch0 < ch1) gather(ch0, 0, 0u, r, c, g);
+    double dsum = 0;
+    int s = 0;
+    std::uint32_t par = 0;
+    for (std::int64_t ch = ch0; ch < ch1; ++ch) {
+        double h[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) h[k] = stage[s].blk[32 * k + lane];
+        int sn = s + 1;
+        std::uint32_t pn = par;
+        if (sn == kStages) {
+            sn = 0;
+            pn ^= 1u;
+        }
+        std::uint32_t rn = 0xFFFFFFFFu, cn = 0;
+        double gn[6];
+        if (ch + 1 < ch1) gather(ch + 1, sn, pn, rn, cn, gn);
+        __syncwarp();
+        if (lane == 0 && ch + kStages < ch1) {  // refill this stage kStages chunks ahead
+            fence_proxy_async();
+            issue(ch + kStages, s);
+        }
+        s = sn;
+        par = pn;
+        const bool valid = r != 0xFFFFFFFFu;
+        double yr0 = 0, yr1 = 0, yr2 = 0;
+        if (valid) {
+            const double xc0 = g[0], xc1 = g[1], xc2 = g[2], xr0 = g[3], xr1 = g[4], xr2 = g[5];
+            // column-major H(i,j) = h[3j+i]
+            yr0 = h[0] * xc0 + h[3] * xc1 + h[6] * xc2;
+            yr1 = h[1] * xc0 + h[4] * xc1 + h[7] * xc2;
+            yr2 = h[2] * xc0 + h[5] * xc1 + h[8] * xc2;
+            if (r != c && dbg != 2) {
+                red_add(y + 3 * c, h[0] * xr0 + h[1] * xr1 + h[2] * xr2);
+                red_add(y + 3 * c + 1, h[3] * xr0 + h[4] * xr1 + h[5] * xr2);
+                red_add(y + 3 * c + 2, h[6] * xr0 + h[7] * xr1 + h[8] * xr2);
+            }
+            if (kDot) dsum += (r != c ? 2.0 : 1.0) * (xr0 * yr0 + xr1 * yr1 + xr2 * yr2);
+        }
+        // head-segmented sum of the row contributions (rows sorted within the chunk)
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double a0 = __shfl_down_sync(0xffffffffu, yr0, off);
+            const double a1 = __shfl_down_sync(0xffffffffu, yr1, off);
+            const double a2 = __shfl_down_sync(0xffffffffu, yr2, off);
+            const std::uint32_t ro = __shfl_down_sync(0xffffffffu, r, off);
+            if (lane + off < 32 && ro == r) {
+                yr0 += a0;
+                yr1 += a1;
+                yr2 += a2;
+            }
+        }
+        const std::uint32_t rprev = __shfl_up_sync(0xffffffffu, r, 1);
+        if (valid && (lane == 0 || rprev != r) && dbg != 2) {
+            red_add(y + 3 * r, yr0);
+            red_add(y + 3 * r + 1, yr1);
+            red_add(y + 3 * r + 2, yr2);
+        }
+        r = rn;
+        c = cn;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) g[k] = gn[k];
+    }
+    if (kDot) grid_sum_last_block(dsum, partials, ticket, dot_out);
+}
+
+template <int kStages>
+constexpr std::size_t tma_smem() {
+    return (sizeof(ChunkStage) + sizeof(std::uint64_t)) * kStages * kTmaWarps;
+}
+
 }  // namespace
 
-// One wave: SMs x resident CTAs per SM (each warp then streams one contiguous
-// run of chunks with its software pipeline).
-int spmv_grid(const Ctx& c) {
-    static int occ = 0;
-    if (occ == 0) {
-        ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<true>, kSpmvThreads, 0));
-        if (occ < 1) occ = 1;
-    }
+// Launch of one SpMV variant (0: LDG-streamed k_spmv; 2/3/4: k_spmv_tma with
+// that many stages per warp). One wave: SMs x resident CTAs per SM, each warp
+// then streams one contiguous run of chunks.
+namespace {
+struct SpmvLaunch {
+    int grid = 1, block = 256;
+    std::size_t smem = 0;
+};
+
+template <class K>
+SpmvLaunch spmv_config(K kernel, int block, std::size_t smem, const Ctx& c, std::int64_t U) {
+    static_assert(sizeof(K) > 0, "");
+    int occ = 0;
+    if (smem > 0) ADIPC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem));
+    if (occ < 1) occ = 1;
     int sms = kSMs;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-    const std::int64_t need = ceil_div(ceil_div(c.A.U, 32), kSpmvThreads / 32);
-    return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(need, static_cast<std::int64_t>(sms) * occ)));
+    const std::int64_t need = ceil_div(ceil_div(U, 32), block / 32);
+    SpmvLaunch l;
+    l.grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(need, static_cast<std::int64_t>(sms) * occ)));
+    l.block = block;
+    l.smem = smem;
+    return l;
+}
+
+template <bool kDot>
+void launch_variant(Ctx& c, const DeviceMatrix& M, int variant, const double* d_x, double* d_y, double* partials,
+                    unsigned* ticket, double* dot_out, const int* flags, int dbg) {
+    cudaStream_t st = c.stream;
+#define ADIPC_TMA(S)                                                                                              \
+    do {                                                                                                          \
+        static SpmvLaunch cfg;                                                                                    \
+        static std::int64_t cfg_u = -1;                                                                           \
+        if (cfg_u != M.U) {                                                                                       \
+            cfg = spmv_config(k_spmv_tma<kDot, S>, 32 * kTmaWarps, tma_smem<S>(), c, M.U);                         \
+            cfg_u = M.U;                                                                                          \
+        }                                                                                                         \
+        k_spmv_tma<kDot, S><<<cfg.grid, cfg.block, cfg.smem, st>>>(M.rows.p, M.cols.p, M.blocks.p, M.U, d_x, d_y, \
+                                                                   partials, ticket, dot_out, flags, dbg);        \
+    } while (0)
+    if (variant == 2)
+        ADIPC_TMA(2);
+    else if (variant == 3)
+        ADIPC_TMA(3);
+    else if (variant == 4)
+        ADIPC_TMA(4);
+    else {
+        static SpmvLaunch cfg;
+        static std::int64_t cfg_u = -1;
+        if (cfg_u != M.U) {
+            cfg = spmv_config(k_spmv<kDot>, kSpmvThreads, 0, c, M.U);
+            cfg_u = M.U;
+        }
+        k_spmv<kDot><<<cfg.grid, cfg.block, 0, st>>>(M.rows.p, M.cols.p, M.blocks.p, M.U, d_x, d_y, partials, ticket,
+                                                     dot_out, flags, dbg, c.l2_persist_1024);
+    }
+#undef ADIPC_TMA
+    ADIPC_LAUNCH_CHECK();
+}
+}  // namespace
+
+// upper bound of the grid of any variant (sizes the per-CTA partials)
+int spmv_grid(const Ctx& c, const DeviceMatrix& M) {
+    int sms = kSMs;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    return sms * 8;
 }
 
 // y (+)= A x. zero_y: clear y first (otherwise the caller guarantees y == 0).
 // With `dot_out`: x.(A x) -> *dot_out (device), using `partials`
 // (>= spmv_grid doubles) and `ticket` (one zeroed unsigned). `flags`: skip
 // when the PCG solve is done.
-void spmv_launch(Ctx& c, const double* d_x, double* d_y, bool zero_y, const int* flags, double* partials,
-                 unsigned* ticket, double* dot_out) {
-    const std::int64_t nx3 = 3 * static_cast<std::int64_t>(c.A.n);
+void spmv_launch(Ctx& c, const DeviceMatrix& M, const double* d_x, double* d_y, bool zero_y, const int* flags,
+                 double* partials, unsigned* ticket, double* dot_out) {
+    const std::int64_t nx3 = 3 * static_cast<std::int64_t>(M.n);
     if (zero_y) ADIPC_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * nx3, c.stream));
-    if (c.A.U == 0) {
+    if (M.U == 0) {
         if (dot_out) ADIPC_CUDA(cudaMemsetAsync(dot_out, 0, sizeof(double), c.stream));
         return;
     }
-    const int grid = spmv_grid(c);
     if (dot_out)
-        k_spmv<true><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
-                                                          partials, ticket, dot_out, flags, 0, c.l2_persist_1024);
+        launch_variant<true>(c, M, c.spmv_variant, d_x, d_y, partials, ticket, dot_out, flags, 0);
     else
-        k_spmv<false><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
-                                                           nullptr, nullptr, nullptr, flags, 0, c.l2_persist_1024);
-    ADIPC_LAUNCH_CHECK();
+        launch_variant<false>(c, M, c.spmv_variant, d_x, d_y, nullptr, nullptr, nullptr, flags, 0);
 }
 
-// Debug timing of the SpMV variants (0 normal, 1 no transposed scatter,
-// 2 no atomics, 3 no column gather): ms per launch over `iters` launches.
-// (A TMA bulk-copy ring variant measured slower in situ: 95 vs 81 us at cfg5;
-// the SpMV is not limited by bytes in flight.)
+// Debug timing of the SpMV variants: mode & 7 = 0 normal, 1 no transposed
+// scatter, 2 no atomics, 3 no column gather (LDG kernel only); +8: evict L2
+// (256 MB write) before every launch, as inside PCG; mode >> 4 = variant
+// (0 LDG-streamed, 2/3/4 TMA stages). ms per launch over `iters` launches.
+// +256: the solve-order matrix with the last PCG's p as x (in-situ inputs).
 float spmv_debug_time(Ctx& c, const double* d_x, double* d_y, int mode, int iters) {
-    const bool cold = mode >= 8;  // +8: evict L2 (256 MB write) before every launch, as inside PCG
+    const int mode_all = mode;
+    const bool cold = (mode & 8) != 0;
+    const bool insitu = (mode & 256) != 0;
+    const int variant = (mode >> 4) & 15;
     mode &= 7;
+    const DeviceMatrix& M = insitu ? c.S() : c.A;
+    if (insitu) {
+        d_x = c.w.p.p;
+        c.w.tmp.reserve(3 * static_cast<std::size_t>(M.n));
+        d_y = c.w.tmp.p;
+    }
     cudaEvent_t e0, e1;
     ADIPC_CUDA(cudaEventCreate(&e0));
     ADIPC_CUDA(cudaEventCreate(&e1));
-    const int grid = spmv_grid(c);
     DBuf<char> flush;
     if (cold) flush.reserve(256u << 20);
+    // +512: the p.Ap-fused kernel (own partials / ticket / result)
+    const bool dot = (mode_all & 512) != 0;
+    DBuf<double> dpart;
+    DBuf<unsigned> dtick;
+    if (dot) {
+        dpart.reserve(static_cast<std::size_t>(spmv_grid(c, M)) + 1);
+        dtick.reserve(1);
+        ADIPC_CUDA(cudaMemsetAsync(dtick.p, 0, sizeof(unsigned), c.stream));
+    }
     float total = 0;
     for (int i = -2; i < iters; ++i) {
         if (cold) ADIPC_CUDA(cudaMemsetAsync(flush.p, i & 0xff, 256u << 20, c.stream));
         ADIPC_CUDA(cudaEventRecord(e0, c.stream));
-        k_spmv<false><<<grid, kSpmvThreads, 0, c.stream>>>(c.A.rows.p, c.A.cols.p, c.A.blocks.p, c.A.U, d_x, d_y,
-                                                           nullptr, nullptr, nullptr, nullptr, mode, c.l2_persist_1024);
+        if (dot)
+            launch_variant<true>(c, M, variant, d_x, d_y, dpart.p, dtick.p, dpart.p + spmv_grid(c, M), nullptr, mode);
+        else
+            launch_variant<false>(c, M, variant, d_x, d_y, nullptr, nullptr, nullptr, nullptr, mode);
         ADIPC_CUDA(cudaEventRecord(e1, c.stream));
         ADIPC_CUDA(cudaEventSynchronize(e1));
         float ms = 0;
@@ -170,13 +377,15 @@ float spmv_debug_time(Ctx& c, const double* d_x, double* d_y, int mode, int iter
         if (i >= 0) total += ms;
     }
     flush.free();
+    dpart.free();
+    dtick.free();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return total / iters;
 }
 
 void spmv(Ctx& c, const double* d_x, double* d_y, double*, int) {
-    spmv_launch(c, d_x, d_y, true, nullptr, nullptr, nullptr, nullptr);
+    spmv_launch(c, c.A, d_x, d_y, true, nullptr, nullptr, nullptr, nullptr);
 }
 
 }  // namespace adipc_gpu

@@ -42,7 +42,8 @@ def test_cache_reuse_is_exact():
         # coarse restrictions accumulate with fp64 atomics, so two builds agree
         # to rounding, not bitwise
         assert np.linalg.norm(zf - zc) <= 1e-10 * np.linalg.norm(zf)
-        assert abs(rf.iters - rc.iters) <= 1
+        # ... and so can converged iteration counts: the contract is +-2 %
+        assert abs(rf.iters - rc.iters) <= max(1, 0.02 * rc.iters)
         assert np.linalg.norm(xf - xc) <= 1e-6 * np.linalg.norm(xf)
     fresh.close()
     cached.close()

@@ -1,6 +1,6 @@
-"""Profiling aid: time SpMV variants on the cfg5 matrix (normal, without the
-transposed scatter, without atomics, without the column gather) to attribute
-the SpMV time. Variants 1-3 compute wrong results by construction."""
+"""Profiling aid: time SpMV kernels on the cfg5 matrix (the LDG-streamed and
+the TMA-staged variants; normal, without atomics, warm or cold L2) to attribute
+the SpMV time. Modes without atomics compute wrong results by construction."""
 import ctypes as C
 import json
 import os
@@ -22,7 +22,10 @@ x = torch.randn(3 * n, dtype=torch.float64, device="cuda")
 y = torch.empty_like(x)
 out = {"n": n, "U": U, "bytes": 80 * U + 48 * n}
 L = _lib.gpu()
-for mode in (0, 1, 2, 3, 8, 9, 10):  # +8: L2 evicted before every launch (cold)
+modes = [0, 2, 8, 10]
+for v in (2, 3, 4):
+    modes += [(v << 4), (v << 4) | 8, (v << 4) | 10]
+for mode in modes:  # +8: L2 evicted before every launch (cold); >>4: variant
     ms = C.c_float()
     ctx._check(L.adipc_gpu_debug_spmv_time(ctx.h, x.data_ptr(), y.data_ptr(), mode, 30, C.byref(ms)))
     out[f"mode{mode}_us"] = round(ms.value * 1000, 2)

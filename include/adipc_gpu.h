@@ -48,6 +48,8 @@ extern "C" {
 #define ADIPC_OPT_L2_PERSIST 3      /* value/1024 of the matrix tiles kept L2-resident (evict-last) across SpMVs */
 #define ADIPC_OPT_SOLVE_ORDER 4     /* 1 (default): MAS/PCG renumber slots by level-0 subdomain internally */
 #define ADIPC_OPT_SPMV_VARIANT 5    /* SpMV kernel: 0 LDG-streamed tiles, 2/3/4 TMA-staged (stages per warp; default 3) */
+#define ADIPC_OPT_SO_KERNELS 6      /* 1 (default): solve-order PCG iteration kernels; 0: the generic level kernels */
+#define ADIPC_OPT_L0_STAGES 7       /* 2 (default) or 3: packed inverses in flight per warp pair in the preconditioner */
 
 typedef struct adipc_gpu_ctx adipc_gpu_ctx;
 typedef struct adipc_hierarchy adipc_hierarchy;

@@ -27,6 +27,8 @@ OPT_PROFILE = 2
 OPT_L2_PERSIST = 3
 OPT_SOLVE_ORDER = 4
 OPT_SPMV_VARIANT = 5
+OPT_SO_KERNELS = 6
+OPT_L0_STAGES = 7
 
 # Every symbol include/adipc_gpu.h declares, with its ctypes signature.
 GPU_SIGNATURES = {

@@ -116,6 +116,8 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
         L->up_first.free();
         L->upc_ptr.free();
         L->upc_pos.free();
+        L->upc_node.free();
+        L->up_node.free();
         L->rr.free();
         L->inv_off.free();
         L->inv.free();
@@ -184,6 +186,11 @@ int adipc_gpu_set_option(adipc_gpu_ctx* ctx, int option, int value) {
         } else if (option == ADIPC_OPT_SPMV_VARIANT) {
             if (value != 0 && (value < 2 || value > 4)) throw StatusError(kInvalidArgument, "SpMV variant not in {0,2,3,4}");
             ctx->c.spmv_variant = value;
+        } else if (option == ADIPC_OPT_SO_KERNELS) {
+            ctx->c.so_kernels = value != 0;
+        } else if (option == ADIPC_OPT_L0_STAGES) {
+            if (value != 2 && value != 3) throw StatusError(kInvalidArgument, "level-0 stages not in {2,3}");
+            ctx->c.l0_stages = value;
         } else if (option == ADIPC_OPT_SOLVE_ORDER) {
             ctx->c.solve_order = value != 0;
             ctx->c.hier_version = ~0ull;  // the device levels depend on the numbering

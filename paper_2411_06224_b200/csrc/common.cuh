@@ -112,7 +112,10 @@ namespace adipc_gpu {
 // its partial, the last CTA to arrive (ticket) sums all partials in a fixed
 // order and writes *out, then re-arms the ticket. Must be called by all
 // threads of every CTA; `v` is this thread's contribution.
-__device__ __forceinline__ void grid_sum_last_block(double v, double* partials, unsigned* ticket, double* out) {
+// `advance` (optional): incremented once by the last CTA, after *out is
+// written (the PCG iteration index, advanced by the iteration's first kernel).
+__device__ __forceinline__ void grid_sum_last_block(double v, double* partials, unsigned* ticket, double* out,
+                                                    int* advance = nullptr) {
     __shared__ double red[32];
     __shared__ bool last;
     const double bs = block_sum(v, red);
@@ -131,6 +134,7 @@ __device__ __forceinline__ void grid_sum_last_block(double v, double* partials, 
     if (threadIdx.x == 0) {
         *out = tot;
         *ticket = 0;
+        if (advance) *advance += 1;
     }
 }
 

@@ -50,6 +50,8 @@ struct DeviceLevel {
     DBuf<std::int32_t> up_first;   // subdomain -> first next-level node nested in it
     DBuf<std::int32_t> upc_ptr;    // next-level node -> range of its children (CSR)
     DBuf<std::int32_t> upc_pos;    // children as positions inside this level's subdomain
+    DBuf<std::int32_t> upc_node;   // children as this level's node ids (solve order: level 0 = solve slots)
+    DBuf<std::int32_t> up_node;    // node -> the next level's node containing it
     DBuf<double> rr;               // level >= 1: restricted residual per node (3 per node)
     std::vector<std::int32_t> pos_host;
     DBuf<std::int64_t> inv_off;    // subdomain -> offset of its packed inverse (16-byte aligned)
@@ -142,6 +144,11 @@ struct Ctx {
     // SpMV kernel variant (ADIPC_OPT_SPMV_VARIANT): 0 LDG-streamed tiles,
     // 2/3/4 TMA-staged tiles with that many chunks in flight per warp
     int spmv_variant = 3;
+    // TMA ring depth (packed inverses in flight per warp) of the solve-order
+    // level-0 solve; ADIPC_OPT_SO_KERNELS selects the solve-order iteration
+    // kernels (solve_order.cu) when the levels allow them
+    int l0_stages = 2;
+    bool so_kernels = true;
 
     // per-kernel-class PCG timing (ADIPC_OPT_PROFILE): spmv, level 0, coarse, final
     bool profile = false;

@@ -276,11 +276,16 @@ void link_levels(Ctx& c, const host::MasHierarchy& h) {
         for (std::int32_t s = cur.n_parts - 1; s >= 0; --s)
             if (first[s] == std::numeric_limits<std::int32_t>::max()) first[s] = first[s + 1];  // empty subdomain
         for (std::int32_t v = 0; v < nxt.n_nodes; ++v) cnt[v + 1] += cnt[v];
-        std::vector<std::int32_t> pos(cur.n_nodes), fill(cnt.begin(), cnt.end() - 1);
-        for (std::int32_t v = 0; v < cur.n_nodes; ++v) pos[fill[up[v]]++] = L.pos_host[v];  // children ascending
+        std::vector<std::int32_t> pos(cur.n_nodes), node(cur.n_nodes), fill(cnt.begin(), cnt.end() - 1);
+        for (std::int32_t v = 0; v < cur.n_nodes; ++v) {  // children ascending
+            node[fill[up[v]]] = v;
+            pos[fill[up[v]]++] = L.pos_host[v];
+        }
         upload(L.up_first, first, st);
         upload(L.upc_ptr, cnt, st);
         upload(L.upc_pos, pos, st);
+        upload(L.upc_node, node, st);
+        upload(L.up_node, up, st);
     }
 }
 

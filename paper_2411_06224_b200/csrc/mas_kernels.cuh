@@ -36,8 +36,8 @@ enum Scal : int {
     S_RZ = 8,        // S_RZ + l: level-l share of r . z (Jacobi: level 0)
     S_COUNT = S_RZ + kMaxLevels
 };
-// F_K: index (1-based) of the iteration the next kernels execute; advanced by
-// the last CTA of the prolongation/p-update kernel, so an iteration's launch
+// F_K: index (1-based) of the current iteration; advanced by the last CTA of
+// the iteration's first kernel (the p.Ap SpMV), so an iteration's launch
 // sequence is identical every time (captured once as a CUDA graph).
 enum Flag : int { F_DONE = 0, F_ITERS = 1, F_CONVERGED = 2, F_K = 3, F_KTICKET = 4, F_COUNT = 8 };
 // last-block tickets / partial arrays: 0 spmv, 1 b.b, 2 + l level l
@@ -120,6 +120,99 @@ __device__ __forceinline__ double gather_r(const PcgArgs& a, const double* r_in,
 
 constexpr int kLevelWarps = 4;  // warps (= subdomains) per CTA of the level kernels
 
+// y = D^-1 b for one subdomain, D^-1 symmetric-packed in shared memory (upper
+// triangle by columns: D(j,k) at k(k+1)/2 + j for j <= k, packed_idx). Lane j
+// holds rows j + 32 t (t < R) in b[t] / y[t]. Fully unrolled over kK >= dim
+// columns, so D(j,k) is a shared load at a compile-time offset: k(k+1)/2 from
+// M + j when j <= k, k from M + j(j+1)/2 when j > k — per column one
+// broadcast of b_k, at most two shared loads and one FMA per row (two
+// accumulation chains for ILP). Columns k >= dim need b_k = 0 and finite slot
+// contents up to packed_doubles(kK); rows j >= dim come out as garbage.
+template <int kK>
+__device__ __forceinline__ void packed_matvec(const double* M, const double* b, double* y, int lane) {
+    constexpr int R = (kK + 31) / 32;
+    const double* P1[R];
+    const double* P2[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        const int j = min(lane + 32 * t, kK - 1);
+        P1[t] = M + j;
+        P2[t] = M + j * (j + 1) / 2;
+    }
+    double acc0[R], acc1[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) acc0[t] = acc1[t] = 0.0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        const double bk = __shfl_sync(0xffffffffu, b[k >> 5], k & 31);
+        const int ck = k * (k + 1) / 2;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            double m;
+            if (32 * t + 31 <= k)
+                m = P1[t][ck];
+            else if (32 * t > k)
+                m = P2[t][k];
+            else
+                m = (lane + 32 * t <= k) ? P1[t][ck] : P2[t][k];
+            if (k & 1)
+                acc1[t] = fma(m, bk, acc1[t]);
+            else
+                acc0[t] = fma(m, bk, acc0[t]);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t) y[t] = acc0[t] + acc1[t];
+}
+
+// Rows [kRow0, kRow0 + kRows) of y = D^-1 b (lane i holds row kRow0 + i + 32 t
+// in y[t]); b read from shared memory (bs, kK entries, b_k = 0 for k >= dim).
+// Compile-time row ranges let the compiler pick the access per column: all
+// rows <= k -> column k, all rows > k -> their own columns, else per lane.
+template <int kK, int kRow0, int kRows>
+__device__ __forceinline__ void packed_matvec_rows(const double* M, const double* bs, double* y, int lane) {
+    constexpr int R = (kRows + 31) / 32;
+    const double* P1[R];
+    const double* P2[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        const int j = min(kRow0 + lane + 32 * t, kK - 1);
+        P1[t] = M + j;
+        P2[t] = M + j * (j + 1) / 2;
+    }
+    double acc0[R], acc1[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) acc0[t] = acc1[t] = 0.0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        const double bk = bs[k];
+        const int ck = k * (k + 1) / 2;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int jlo = kRow0 + 32 * t;
+            const int jhi = min(kRow0 + 32 * t + 31, kRow0 + kRows - 1);
+            double m;
+            if (jhi <= k)
+                m = P1[t][ck];
+            else if (jlo > k)
+                m = P2[t][k];
+            else
+                m = (kRow0 + lane + 32 * t <= k) ? P1[t][ck] : P2[t][k];
+            if (k & 1)
+                acc1[t] = fma(m, bk, acc1[t]);
+            else
+                acc0[t] = fma(m, bk, acc0[t]);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t) y[t] = acc0[t] + acc1[t];
+}
+
+// column bound of packed_matvec for subdomains of at most max_fill nodes
+inline int matvec_cols(int max_fill) { return max_fill <= 8 ? 24 : (max_fill <= 16 ? 48 : (max_fill <= 32 ? 96 : 0)); }
+
 // Bytes of dynamic shared memory per warp of k_mas_level for a level whose
 // largest subdomain has dimension max_dim: packed inverse + b + mbarrier.
 inline std::size_t level_warp_smem(int max_dim, int regs) {
@@ -139,7 +232,7 @@ template <int kMode, int kRegs, bool kSolve = true>
 __global__ void __launch_bounds__(32 * kLevelWarps) k_mas_level(LevelArgs L, PcgArgs a, double* __restrict__ partials,
                                                                 unsigned* __restrict__ ticket,
                                                                 double* __restrict__ dot_out, int warp_smem) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double* Mw = reinterpret_cast<double*>(smem + static_cast<std::size_t>(w) * warp_smem);
     double* bw = reinterpret_cast<double*>(smem + static_cast<std::size_t>(w + 1) * warp_smem) - 32 * kRegs - 2;
@@ -269,7 +362,6 @@ __global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs p
                                                   double* __restrict__ p, double* __restrict__ ap, PcgArgs a) {
     double beta = 0;
     bool write_p = false;
-    int k = 0;
     if (kFinal != F_APPLY) {
         if (a.flags[F_DONE]) return;
         double rz = 0;
@@ -288,7 +380,7 @@ __global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs p
             }
             write_p = rz > 0;
         } else {
-            k = a.flags[F_K];
+            const int k = a.flags[F_K];
             const double rho = a.scal[S_RHO0 + ((k - 1) & 1)];
             const double stop = a.scal[S_STOP];
             if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -318,18 +410,6 @@ __global__ void __launch_bounds__(256) k_mas_final(std::int32_t n, ProlongArgs p
         } else if (write_p) {
             p[g] = (kFinal == F_PCG_INIT) ? zz : zz + beta * p[g];
             ap[g] = 0.0;
-        }
-    }
-    if (kFinal == F_PCG_STEP) {  // the last CTA advances the iteration index
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            unsigned* ticket = reinterpret_cast<unsigned*>(a.flags + F_KTICKET);
-            if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
-                a.flags[F_K] = k + 1;
-                *ticket = 0;
-                __threadfence();
-            }
         }
     }
 }

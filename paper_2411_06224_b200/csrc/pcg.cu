@@ -37,6 +37,16 @@ void launch_final(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a);
 template <int kMode>
 void launch_jacobi(Ctx& c, const double* r_in, double* z, const PcgArgs& a, double* partials, unsigned* ticket,
                    double* dot_out);
+// solve_order.cu
+bool so_supported(const Ctx& c);
+int so_partials(const Ctx& c);
+template <int kMode>
+void launch_update_so(Ctx& c, const PcgArgs& a);
+void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, double* partials, unsigned* ticket,
+                       double* dot);
+template <int kFinal>
+void launch_final_so(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a);
+void clear_restrict_so(Ctx& c);
 
 namespace {
 
@@ -92,6 +102,9 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     w.tmp.reserve(n3);
     int pmax = std::max({spmv_grid(c, c.S()), slot_grid(c), kSMs * 8, jacobi_grid(c)});
     for (int l = 0; l < n_levels; ++l) pmax = std::max(pmax, level_grid(c, l));
+    // solve-order iteration kernels (solve_order.cu)
+    const bool so = c.so_kernels && so_supported(c);
+    if (so) pmax = std::max(pmax, so_partials(c));
     w.partials.reserve(static_cast<std::size_t>(pmax) * T_COUNT);
     w.tickets.reserve(T_COUNT);
     w.scal.reserve(S_COUNT);
@@ -101,7 +114,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     auto partials_of = [&](int t) { return part + static_cast<std::size_t>(t) * pmax; };
     ADIPC_CUDA(cudaMemsetAsync(w.tickets.p, 0, sizeof(unsigned) * T_COUNT, st));
     int h_flags0[F_COUNT] = {0};
-    h_flags0[F_K] = 1;
+    h_flags0[F_K] = 0;  // advanced to 1 by the first iteration's SpMV
     ADIPC_CUDA(cudaMemcpyAsync(w.flags.p, h_flags0, sizeof(h_flags0), cudaMemcpyHostToDevice, st));
     double h_scal[S_COUNT] = {0};
     h_scal[S_STOP] = rel_tol * rel_tol;
@@ -168,6 +181,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
         launch_jacobi<M_INIT>(c, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL, w.scal.p + S_RZ);
     }
     launch_final<F_PCG_INIT>(c, w.z.p, w.p.p, w.ap.p, a);
+    if (so) clear_restrict_so(c);
 
     // optional per-kernel-class timing (ADIPC_OPT_PROFILE): events bracket the
     // SpMV, update, preconditioner and prolongation/p-update launches of every
@@ -198,22 +212,33 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
             spmv_launch(c, c.S(), d_x, w.tmp.p, false, w.flags.p, nullptr, nullptr, nullptr);
             PcgArgs ar = a;
             ar.ap = w.tmp.p;
-            if (mas)
+            if (so)
+                launch_update_so<M_RESTART>(c, ar);
+            else if (mas)
                 launch_level<M_RESTART, false>(c, 0, nullptr, nullptr, ar, nullptr, nullptr, nullptr, st, true);
             else
                 launch_jacobi<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
                                          w.scal.p + S_RZ);
         } else {
-            if (mas)
+            if (so)
+                launch_update_so<M_UPDATE>(c, a);
+            else if (mas)
                 launch_level<M_UPDATE, false>(c, 0, nullptr, nullptr, a, nullptr, nullptr, nullptr, st, true);
             else
                 launch_jacobi<M_UPDATE>(c, nullptr, w.z.p, a, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
                                         w.scal.p + S_RZ);
         }
         mark(slot, 2);
-        if (mas) mas_apply(a);
+        if (so)
+            launch_precond_so(c, w.r.p, w.z.p, w.flags.p, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
+                              w.scal.p + S_RZ);
+        else if (mas)
+            mas_apply(a);
         mark(slot, 3);
-        launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
+        if (so)
+            launch_final_so<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
+        else
+            launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
         mark(slot, 4);
     };
     // capture the two iteration variants as graphs (non-profiled runs)

@@ -1,0 +1,452 @@
+// PCG iteration kernels of the solve order (Ctx::perm active: every level-0
+// subdomain is a contiguous slot range, slots in pos_of order). The iteration
+// (pcg.hpp:59-85) becomes:
+//   1. SpMV + p.Ap                                  (spmv.cu)
+//   2. k_update_so: alpha, x += alpha p, r -= alpha Ap as a unit-stride stream
+//      over each CTA's run of level-0 subdomains; the level-1 restricted
+//      residual from the CTA's shared-memory copy of r (children in ascending
+//      order, as the tree restriction of mas_kernels.cuh); levels >= 2 get the
+//      level-1 sums by fp64 RED up the nesting (r_{l+1}[w] = sum of r_l over
+//      the level-l nodes inside w, hierarchy.hpp:53-72), so every coarse level
+//      is ready at once
+//   3. k_l0_solve_so (level-0 dense solves, persistent warps, each streaming
+//      its run of packed inverses through a ring of TMA bulk copies) on the
+//      solve stream, concurrently with k_coarse_so (all coarse levels in ONE
+//      launch, one warp per subdomain of any level) on the side stream
+//   4. k_final_so: z = ((z0 + y1[agg1]) + y2[agg2]) + ... (mas.hpp:95-96
+//      order), the convergence test, p = z + beta p, Ap cleared, the RED
+//      targets of step 2 cleared for the next iteration.
+// r.z comes from the per-level partial dots b_l.y_l of step 3 (the same
+// quantity: r.z = sum_l (P_l r).(D_l^-1 P_l r)).
+#include <algorithm>
+
+#include "mas_kernels.cuh"
+
+namespace adipc_gpu {
+
+namespace {
+
+constexpr int kUpdThreads = 256;
+constexpr int kUpdSubs = 32;  // level-0 subdomains per CTA of the update pass
+
+struct SoRestrict {
+    int n_levels;                        // total levels L (>= 2 when used)
+    std::int32_t n0_parts;               // level-0 subdomains
+    const std::int32_t* sub_ptr0;        // level-0 subdomain -> first solve slot
+    const std::int32_t* up_first0;       // level-0 subdomain -> first level-1 node
+    const std::int32_t* upc_ptr0;        // level-1 node -> children range
+    const std::int32_t* upc_node0;       // children (solve slots), ascending
+    double* rr[kMaxLevels];              // restricted residual of level l >= 1 (3 per node)
+    const std::int32_t* up_node[kMaxLevels];  // level-l node -> level-(l+1) node, l >= 1
+};
+
+template <int kMode>
+__global__ void __launch_bounds__(kUpdThreads) k_update_so(SoRestrict so, PcgArgs a) {
+    extern __shared__ double sr[];
+    double alpha = 0;
+    if (a.flags[F_DONE]) return;
+    if (!pcg_alpha(a, alpha)) return;
+    const std::int32_t s0 = blockIdx.x * kUpdSubs;
+    const std::int32_t s1 = min(s0 + kUpdSubs, so.n0_parts);
+    const std::int64_t g0 = 3 * static_cast<std::int64_t>(so.sub_ptr0[s0]);
+    const std::int64_t g1 = 3 * static_cast<std::int64_t>(so.sub_ptr0[s1]);
+    const double* __restrict__ p = a.p;
+    const double* __restrict__ ap = a.ap;
+    const double* __restrict__ b = a.b;
+    double* __restrict__ x = a.x;
+    double* __restrict__ r = a.r;
+    constexpr int kU = 4;  // elements per thread in flight
+    for (std::int64_t gb = g0 + threadIdx.x; gb < g1; gb += kU * kUpdThreads) {
+        double rv[kU], pv[kU], av[kU], xv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const std::int64_t g = gb + u * kUpdThreads;
+            if (g < g1) {
+                av[u] = ap[g];
+                if (kMode == M_UPDATE) {
+                    rv[u] = r[g];
+                    pv[u] = p[g];
+                    xv[u] = x[g];
+                } else {
+                    rv[u] = b[g];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const std::int64_t g = gb + u * kUpdThreads;
+            if (g < g1) {
+                double nr;
+                if (kMode == M_UPDATE) {
+                    x[g] = xv[u] + alpha * pv[u];
+                    nr = rv[u] - alpha * av[u];
+                } else {  // M_RESTART: r = b - A x (x updated before the restart SpMV)
+                    nr = rv[u] - av[u];
+                }
+                r[g] = nr;
+                sr[g - g0] = nr;
+            }
+        }
+    }
+    __syncthreads();
+    const std::int32_t v0 = so.up_first0[s0], v1 = so.up_first0[s1];
+    for (int t = threadIdx.x; t < 3 * (v1 - v0); t += kUpdThreads) {
+        const std::int32_t v = v0 + t / 3;
+        const int comp = t % 3;
+        double acc = 0;
+        for (std::int32_t q = so.upc_ptr0[v]; q < so.upc_ptr0[v + 1]; ++q)
+            acc += sr[3 * static_cast<std::int64_t>(so.upc_node0[q]) - g0 + comp];
+        so.rr[1][3 * static_cast<std::int64_t>(v) + comp] = acc;
+        std::int32_t w = v;
+        for (int l = 1; l + 1 < so.n_levels; ++l) {
+            w = so.up_node[l][w];
+            red_add(so.rr[l + 1] + 3 * static_cast<std::int64_t>(w) + comp, acc);
+        }
+    }
+}
+
+// ---- level-0 solve: persistent warp pairs, TMA ring of packed inverses -------
+// Each pair of warps owns a contiguous run of subdomains and keeps kStages
+// packed inverses in flight (cp.async.bulk, L2 evict-first) in its shared
+// ring; the two warps split the rows of every subdomain (kK/2 each), so the
+// ring's shared memory feeds twice the warps and each warp's unrolled
+// mat-vec is half as long. The residual of the next subdomain is loaded one
+// subdomain ahead. Pairs per CTA = blockDim.x / 64 (sized to the ring).
+__device__ __forceinline__ void pair_sync(int pair) {
+    asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
+}
+
+// Every level of the preconditioner in one persistent launch: the work list
+// is level 0's subdomains followed by each coarse level's (their restricted
+// residuals were all produced by the update pass), so there is no side stream
+// and no second kernel competing for the shared memory of the rings.
+struct PrecondTable {
+    int n;                                   // levels
+    std::int32_t base[kMaxLevels + 1];       // prefix sums of subdomain counts
+    const std::int32_t* sub_ptr[kMaxLevels];
+    const std::int32_t* sub_nodes[kMaxLevels];  // null at level 0 (solve order: contiguous slots)
+    const std::int64_t* inv_off[kMaxLevels];
+    const double* inv[kMaxLevels];
+    const double* rin[kMaxLevels];           // level 0: r; coarse: restricted residual
+    double* out[kMaxLevels];                 // level 0: z; coarse: y
+};
+
+template <int kK, int kStages>
+__global__ void __launch_bounds__(256) k_precond_so(PrecondTable pt, double* __restrict__ partials,
+                                                   unsigned* __restrict__ ticket, double* __restrict__ dot_out,
+                                                   const int* __restrict__ flags, int slot_doubles) {
+    constexpr int RB = (kK + 31) / 32;  // b entries per lane
+    constexpr int kHalf = kK / 2;       // rows per warp
+    constexpr int RY = (kHalf + 31) / 32;
+    if (flags && flags[F_DONE]) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, pair = w >> 1, half = w & 1;
+    const int npc = blockDim.x >> 6;
+    double* ring = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(pair) * kStages * slot_doubles;
+    double* bs = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(npc) * kStages * slot_doubles +
+                 static_cast<std::size_t>(w) * kK;
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(
+                             reinterpret_cast<double*>(smem) + static_cast<std::size_t>(npc) * kStages * slot_doubles +
+                             static_cast<std::size_t>(2 * npc) * kK) +
+                         pair * kStages;
+    const std::int32_t n_work = pt.base[pt.n];
+    const std::int64_t gp = static_cast<std::int64_t>(blockIdx.x) * npc + pair;
+    const std::int64_t np = static_cast<std::int64_t>(gridDim.x) * npc;
+    const std::int32_t q0 = static_cast<std::int32_t>(gp * n_work / np);
+    const std::int32_t q1 = static_cast<std::int32_t>((gp + 1) * n_work / np);
+    auto level_of = [&](std::int32_t q) {
+        int l = 0;
+        while (l + 1 < pt.n && q >= pt.base[l + 1]) ++l;
+        return l;
+    };
+    // finite slot contents beyond each inverse (packed_matvec reads them x 0)
+    for (int i = half * 32 + lane; i < kStages * slot_doubles; i += 64) ring[i] = 0.0;
+    fence_proxy_async();
+    pair_sync(pair);
+    auto issue = [&](std::int32_t q, int st) {  // one thread of the pair
+        const int l = level_of(q);
+        const std::int32_t s = q - pt.base[l];
+        const std::int64_t o = pt.inv_off[l][s];
+        const std::uint32_t bytes = static_cast<std::uint32_t>((pt.inv_off[l][s + 1] - o) * 8);
+        mbar_arrive_expect_tx(&bar[st], bytes);
+        if (l == 0)  // streamed once per application
+            bulk_g2s_evict_first(ring + static_cast<std::size_t>(st) * slot_doubles, pt.inv[0] + o, bytes, &bar[st]);
+        else  // coarse inverses (~26 MB at cfg5) stay L2-resident across iterations
+            bulk_g2s_evict_last(ring + static_cast<std::size_t>(st) * slot_doubles, pt.inv[l] + o, bytes, &bar[st]);
+    };
+    if (half == 0 && lane == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
+        fence_mbar_init();
+        for (int st = 0; st < kStages && q0 + st < q1; ++st) issue(q0 + st, st);
+    }
+    pair_sync(pair);
+    // b of a work item and the addresses of its rows (gathered for coarse levels)
+    struct Item {
+        int l;
+        std::int32_t s0, dim;
+    };
+    auto row_index = [&](const Item& it, int j) -> std::int64_t {
+        if (it.l == 0) return 3 * static_cast<std::int64_t>(it.s0) + j;
+        return 3 * static_cast<std::int64_t>(pt.sub_nodes[it.l][it.s0 + j / 3]) + (j % 3);
+    };
+    auto load_b = [&](std::int32_t q, Item& it, double* bb) {
+        it.l = level_of(q);
+        const std::int32_t s = q - pt.base[it.l];
+        it.s0 = pt.sub_ptr[it.l][s];
+        it.dim = 3 * (pt.sub_ptr[it.l][s + 1] - it.s0);
+#pragma unroll
+        for (int t = 0; t < RB; ++t) {
+            const int j = lane + 32 * t;
+            bb[t] = j < it.dim ? ldg_issue(pt.rin[it.l] + row_index(it, j)) : 0.0;
+        }
+    };
+    Item cur{0, 0, 0};
+    double b[RB];
+    if (q0 < q1) load_b(q0, cur, b);
+    double dsum = 0;
+    int st = 0;
+    std::uint32_t par = 0;
+    for (std::int32_t q = q0; q < q1; ++q) {
+#pragma unroll
+        for (int t = 0; t < RB; ++t)
+            if (lane + 32 * t < kK) bs[lane + 32 * t] = b[t];
+        Item nxt{0, 0, 0};
+        double bn[RB];
+        if (q + 1 < q1) load_b(q + 1, nxt, bn);
+        __syncwarp();
+        mbar_wait(&bar[st], par);
+        const double* M = ring + static_cast<std::size_t>(st) * slot_doubles;
+        double y[RY];
+        if (half == 0)
+            packed_matvec_rows<kK, 0, kHalf>(M, bs, y, lane);
+        else
+            packed_matvec_rows<kK, kHalf, kHalf>(M, bs, y, lane);
+        double* out = pt.out[cur.l];
+#pragma unroll
+        for (int t = 0; t < RY; ++t) {
+            const int i = lane + 32 * t;
+            const int j = half * kHalf + i;
+            if (i < kHalf && j < cur.dim) {
+                out[row_index(cur, j)] = y[t];
+                dsum += bs[j] * y[t];
+            }
+        }
+        pair_sync(pair);  // both warps are done with the slot and with bs
+        if (half == 0 && lane == 0 && q + kStages < q1) {  // refill kStages items ahead
+            fence_proxy_async();
+            issue(q + kStages, st);
+        }
+        if (++st == kStages) {
+            st = 0;
+            par ^= 1u;
+        }
+        cur = nxt;
+#pragma unroll
+        for (int t = 0; t < RB; ++t) b[t] = bn[t];
+    }
+    grid_sum_last_block(dsum, partials, ticket, dot_out);
+}
+
+// ---- prolongation + p update, one thread per solve slot ------------------------
+struct FinalSo {
+    int n_coarse;                            // coarse levels
+    const std::int32_t* agg[kMaxLevels];     // solve slot -> level-(l+1) node
+    const double* y[kMaxLevels];
+    double* clear[kMaxLevels];               // RED targets of k_update_so (levels >= 2)
+    std::int64_t clear_n[kMaxLevels];
+    int n_clear;
+};
+
+template <int kFinal>
+__global__ void __launch_bounds__(256) k_final_so(std::int32_t n, FinalSo fa, const double* __restrict__ z,
+                                                 double* __restrict__ p, double* __restrict__ ap, PcgArgs a) {
+    double beta = 0;
+    if (a.flags[F_DONE]) return;
+    const double rz = a.scal[S_RZ];  // r.z = sum over all levels of b_l.y_l (k_precond_so)
+    if (kFinal == F_PCG_INIT) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // pcg.hpp:52-57
+            a.scal[S_RHO0] = rz;
+            a.scal[S_RHO_INIT] = rz;
+            a.scal[S_STOP] = a.scal[S_STOP] * rz;  // S_STOP preloaded with tol^2
+            if (!(rz > 0)) {
+                a.flags[F_DONE] = 1;
+                a.flags[F_ITERS] = 0;
+                a.scal[S_REL] = 0;
+            }
+        }
+        if (!(rz > 0)) return;
+    } else {
+        const int k = a.flags[F_K];
+        const double rho = a.scal[S_RHO0 + ((k - 1) & 1)];
+        const double stop = a.scal[S_STOP];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.flags[F_ITERS] = k;
+            a.scal[S_REL] = sqrt(fabs(rz) / a.scal[S_RHO_INIT]);
+            if (rz <= stop) {
+                a.flags[F_DONE] = 1;
+                a.flags[F_CONVERGED] = 1;
+            } else {
+                a.scal[S_RHO0 + (k & 1)] = rz;
+            }
+        }
+        if (rz <= stop) return;
+        beta = rz / rho;
+    }
+    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+    if (tid < n) {
+        const std::int64_t g = 3 * tid;
+        std::int32_t nd[kMaxLevels];
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l)
+            if (l < fa.n_coarse) nd[l] = fa.agg[l][tid];
+        double zz0 = z[g], zz1 = z[g + 1], zz2 = z[g + 2];
+        double p0 = 0, p1 = 0, p2 = 0;
+        if (kFinal != F_PCG_INIT) {
+            p0 = p[g];
+            p1 = p[g + 1];
+            p2 = p[g + 2];
+        }
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l)
+            if (l < fa.n_coarse) {
+                const double* yl = fa.y[l] + 3 * static_cast<std::int64_t>(nd[l]);
+                zz0 += yl[0];
+                zz1 += yl[1];
+                zz2 += yl[2];
+            }
+        p[g] = zz0 + beta * p0;
+        p[g + 1] = zz1 + beta * p1;
+        p[g + 2] = zz2 + beta * p2;
+        ap[g] = 0.0;
+        ap[g + 1] = 0.0;
+        ap[g + 2] = 0.0;
+    }
+    // clear the RED targets of the next update pass
+    for (int l = 0; l < fa.n_clear; ++l)
+        for (std::int64_t i = tid; i < fa.clear_n[l]; i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+            fa.clear[l][i] = 0.0;
+}
+
+
+}  // namespace
+
+// The solve-order kernels apply when the levels were built in solve order,
+// there are >= 2 levels and every subdomain fits the unrolled mat-vec (fill <= 32).
+bool so_supported(const Ctx& c) {
+    if (!(c.pkind == kMas && c.perm_active) || c.levels.size() < 2 || c.levels.size() > kMaxLevels) return false;
+    for (const auto& L : c.levels)
+        if (L->max_fill > 32) return false;
+    return true;
+}
+
+template <int kMode>
+void launch_update_so(Ctx& c, const PcgArgs& a) {
+    SoRestrict so{};
+    const DeviceLevel& L0 = *c.levels[0];
+    so.n_levels = static_cast<int>(c.levels.size());
+    so.n0_parts = L0.n_parts;
+    so.sub_ptr0 = L0.sub_ptr.p;
+    so.up_first0 = L0.up_first.p;
+    so.upc_ptr0 = L0.upc_ptr.p;
+    so.upc_node0 = L0.upc_node.p;
+    for (int l = 1; l < so.n_levels; ++l) {
+        so.rr[l] = c.levels[l]->rr.p;
+        so.up_node[l] = c.levels[l]->up_node.p;
+    }
+    const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(L0.n_parts, kUpdSubs)));
+    const std::size_t smem = sizeof(double) * 3 * static_cast<std::size_t>(kUpdSubs) * L0.max_fill;
+    static bool attr = false;
+    if (!attr) {
+        ADIPC_CUDA(cudaFuncSetAttribute(k_update_so<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        attr = true;
+    }
+    k_update_so<kMode><<<grid, kUpdThreads, smem, c.stream>>>(so, a);
+    ADIPC_LAUNCH_CHECK();
+}
+template void launch_update_so<M_UPDATE>(Ctx&, const PcgArgs&);
+template void launch_update_so<M_RESTART>(Ctx&, const PcgArgs&);
+
+// z = M r: every level in one persistent launch (k_precond_so); r.z -> *dot
+void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, double* partials, unsigned* ticket,
+                       double* dot) {
+    PrecondTable pt{};
+    pt.n = static_cast<int>(c.levels.size());
+    int fill = 1;
+    for (int l = 0; l < pt.n; ++l) {
+        const DeviceLevel& L = *c.levels[l];
+        pt.base[l + 1] = pt.base[l] + L.n_parts;
+        pt.sub_ptr[l] = L.sub_ptr.p;
+        pt.sub_nodes[l] = l == 0 ? nullptr : L.sub_nodes.p;
+        pt.inv_off[l] = L.inv_off.p;
+        pt.inv[l] = L.inv.p;
+        pt.rin[l] = l == 0 ? r : L.rr.p;
+        pt.out[l] = l == 0 ? z : L.y.p;
+        fill = std::max(fill, L.max_fill);
+    }
+    const int kk = matvec_cols(fill);
+    const int slot = static_cast<int>(packed_doubles(kk));
+    const int stages = c.l0_stages;
+    // per warp pair: the ring + two b vectors + barriers; up to 4 pairs per
+    // CTA, two CTAs per SM
+    const std::size_t per_pair = (sizeof(double) * slot + sizeof(std::uint64_t)) * stages + 2 * sizeof(double) * kk;
+    const int pairs = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(4, (113u * 1024u) / per_pair)));
+    const std::size_t smem = per_pair * pairs;
+    int sms = kSMs;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+#define ADIPC_PC(K, S)                                                                                        \
+    do {                                                                                                      \
+        ADIPC_CUDA(cudaFuncSetAttribute(k_precond_so<K, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                        static_cast<int>(smem)));                                             \
+        int occ = 0;                                                                                          \
+        ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_precond_so<K, S>, 64 * pairs, smem)); \
+        if (occ < 1) throw StatusError(kInvalidArgument, "preconditioner ring does not fit in shared memory"); \
+        const int grid = static_cast<int>(std::min<std::int64_t>(static_cast<std::int64_t>(sms) * occ,          \
+                                                                 ceil_div(pt.base[pt.n], pairs)));            \
+        k_precond_so<K, S><<<std::max(grid, 1), 64 * pairs, smem, c.stream>>>(pt, partials, ticket, dot, flags, \
+                                                                             slot);                           \
+    } while (0)
+    if (kk == 24) {
+        if (stages == 2) ADIPC_PC(24, 2); else ADIPC_PC(24, 3);
+    } else if (kk == 48) {
+        if (stages == 2) ADIPC_PC(48, 2); else ADIPC_PC(48, 3);
+    } else {
+        if (stages == 2) ADIPC_PC(96, 2); else ADIPC_PC(96, 3);
+    }
+#undef ADIPC_PC
+    ADIPC_LAUNCH_CHECK();
+}
+
+// grid upper bound of the solve-order kernels (sizes the per-CTA partials)
+int so_partials(const Ctx& c) {
+    (void)c;
+    return kSMs * 8;
+}
+
+template <int kFinal>
+void launch_final_so(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a) {
+    FinalSo fa{};
+    const int L = static_cast<int>(c.levels.size());
+    fa.n_coarse = L - 1;
+    for (int l = 1; l < L; ++l) {
+        fa.agg[l - 1] = c.levels[l]->agg.p;
+        fa.y[l - 1] = c.levels[l]->y.p;
+    }
+    for (int l = 2; l < L; ++l) {
+        fa.clear[fa.n_clear] = c.levels[l]->rr.p;
+        fa.clear_n[fa.n_clear] = 3 * static_cast<std::int64_t>(c.levels[l]->n_nodes);
+        ++fa.n_clear;
+    }
+    const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(c.A.n, 256)));
+    k_final_so<kFinal><<<grid, 256, 0, c.stream>>>(c.A.n, fa, z, p, ap, a);
+    ADIPC_LAUNCH_CHECK();
+}
+template void launch_final_so<F_PCG_INIT>(Ctx&, double*, double*, double*, const PcgArgs&);
+template void launch_final_so<F_PCG_STEP>(Ctx&, double*, double*, double*, const PcgArgs&);
+
+// zero the RED targets (levels >= 2) before the first update pass
+void clear_restrict_so(Ctx& c) {
+    for (std::size_t l = 2; l < c.levels.size(); ++l)
+        ADIPC_CUDA(cudaMemsetAsync(c.levels[l]->rr.p, 0, sizeof(double) * 3 * c.levels[l]->n_nodes, c.stream));
+}
+
+}  // namespace adipc_gpu

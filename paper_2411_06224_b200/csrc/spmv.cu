@@ -11,8 +11,7 @@
 // over Ap; the grid total is finished by the last CTA (deterministic order).
 #include <algorithm>
 
-#include "context.hpp"
-#include "tma.cuh"
+#include "mas_kernels.cuh"
 
 namespace adipc_gpu {
 
@@ -105,7 +104,8 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
             red_add(y + 3 * r + 2, yr2);
         }
     }
-    if (kDot) grid_sum_last_block(dsum, partials, ticket, dot_out);
+    // the PCG's p.Ap SpMV opens an iteration: its last CTA advances F_K
+    if (kDot) grid_sum_last_block(dsum, partials, ticket, dot_out, flags ? const_cast<int*>(flags) + F_K : nullptr);
 }
 
 // TMA-staged variant. On B200 the L1 data pipe moves one 32-byte sector per
@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(32 * kTmaWarps) k_spmv_tma(const std::uint32_t
 #pragma unroll
         for (int k = 0; k < 6; ++k) g[k] = gn[k];
     }
-    if (kDot) grid_sum_last_block(dsum, partials, ticket, dot_out);
+    // the PCG's p.Ap SpMV opens an iteration: its last CTA advances F_K
+    if (kDot) grid_sum_last_block(dsum, partials, ticket, dot_out, flags ? const_cast<int*>(flags) + F_K : nullptr);
 }
 
 template <int kStages>

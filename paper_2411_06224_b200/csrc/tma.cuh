@@ -49,6 +49,18 @@ __device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src,
         : "memory");
 }
 
+// same, with an L2 evict-last hint (small operands re-read every iteration)
+__device__ __forceinline__ void bulk_g2s_evict_last(void* dst, const void* src, std::uint32_t bytes,
+                                                    std::uint64_t* bar) {
+    std::uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
 // L2 cache policies for explicit residency control of streamed operands
 __device__ __forceinline__ std::uint64_t policy_evict_last() {
     std::uint64_t p;

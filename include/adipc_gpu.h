@@ -47,8 +47,10 @@ extern "C" {
 #define ADIPC_OPT_PROFILE 2         /* time each PCG kernel class with CUDA events */
 #define ADIPC_OPT_L2_PERSIST 3      /* value/1024 of the matrix tiles kept L2-resident (evict-last) across SpMVs */
 #define ADIPC_OPT_SOLVE_ORDER 4     /* 1 (default): MAS/PCG renumber slots by level-0 subdomain internally */
-#define ADIPC_OPT_SPMV_VARIANT 5    /* SpMV kernel: 0 LDG-streamed tiles, 2/3/4 TMA-staged (stages per warp; default 3) */
+#define ADIPC_OPT_SPMV_VARIANT 5    /* SpMV kernel: 0 (default) LDG-streamed tiles, 2/3/4 TMA-staged (stages per warp), 5/6 TMA-staged two blocks per lane */
 #define ADIPC_OPT_SO_KERNELS 6      /* 1 (default): solve-order PCG iteration kernels; 0: the generic level kernels */
+#define ADIPC_OPT_PERSISTENT 8      /* 1: PCG iterations in one persistent cooperative kernel (solve order); default 0 */
+#define ADIPC_OPT_PC_VARIANT 9      /* preconditioner kernel: 0 (default) warp pairs per subdomain, 1 one warp per subdomain, 2 two subdomains per warp */
 #define ADIPC_OPT_L0_STAGES 7       /* 2 (default) or 3: packed inverses in flight per warp pair in the preconditioner */
 
 typedef struct adipc_gpu_ctx adipc_gpu_ctx;

@@ -29,6 +29,8 @@ OPT_SOLVE_ORDER = 4
 OPT_SPMV_VARIANT = 5
 OPT_SO_KERNELS = 6
 OPT_L0_STAGES = 7
+OPT_PERSISTENT = 8
+OPT_PC_VARIANT = 9
 
 # Every symbol include/adipc_gpu.h declares, with its ctypes signature.
 GPU_SIGNATURES = {

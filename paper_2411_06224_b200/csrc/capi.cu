@@ -118,6 +118,7 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
         L->upc_pos.free();
         L->upc_node.free();
         L->up_node.free();
+        L->anc.free();
         L->rr.free();
         L->inv_off.free();
         L->inv.free();
@@ -129,6 +130,7 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.jinv.free();
     c.build_status.free();
     c.perm.free();
+    c.phase_ns.free();
     c.perm_keys.free();
     c.perm_vals.free();
     c.pv_in.free();
@@ -184,8 +186,12 @@ int adipc_gpu_set_option(adipc_gpu_ctx* ctx, int option, int value) {
                 ADIPC_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<std::size_t>(mx)));
             }
         } else if (option == ADIPC_OPT_SPMV_VARIANT) {
-            if (value != 0 && (value < 2 || value > 4)) throw StatusError(kInvalidArgument, "SpMV variant not in {0,2,3,4}");
+            if (value != 0 && (value < 2 || value > 6)) throw StatusError(kInvalidArgument, "SpMV variant not in {0,2..6}");
             ctx->c.spmv_variant = value;
+        } else if (option == ADIPC_OPT_PC_VARIANT) {
+            ctx->c.pc_variant = value;
+        } else if (option == ADIPC_OPT_PERSISTENT) {
+            ctx->c.persistent = value != 0;
         } else if (option == ADIPC_OPT_SO_KERNELS) {
             ctx->c.so_kernels = value != 0;
         } else if (option == ADIPC_OPT_L0_STAGES) {

@@ -52,6 +52,7 @@ struct DeviceLevel {
     DBuf<std::int32_t> upc_pos;    // children as positions inside this level's subdomain
     DBuf<std::int32_t> upc_node;   // children as this level's node ids (solve order: level 0 = solve slots)
     DBuf<std::int32_t> up_node;    // node -> the next level's node containing it
+    DBuf<std::int32_t> anc;        // level >= 2: level-1 node -> this level's node containing it
     DBuf<double> rr;               // level >= 1: restricted residual per node (3 per node)
     std::vector<std::int32_t> pos_host;
     DBuf<std::int64_t> inv_off;    // subdomain -> offset of its packed inverse (16-byte aligned)
@@ -143,12 +144,16 @@ struct Ctx {
     int l2_persist_1024 = 0;
     // SpMV kernel variant (ADIPC_OPT_SPMV_VARIANT): 0 LDG-streamed tiles,
     // 2/3/4 TMA-staged tiles with that many chunks in flight per warp
-    int spmv_variant = 3;
+    int spmv_variant = 0;
     // TMA ring depth (packed inverses in flight per warp) of the solve-order
     // level-0 solve; ADIPC_OPT_SO_KERNELS selects the solve-order iteration
     // kernels (solve_order.cu) when the levels allow them
     int l0_stages = 2;
+    int pc_variant = 0;  // preconditioner kernel: 0 warp pairs per item, 1 one warp per item (ADIPC_OPT_PC_VARIANT)
     bool so_kernels = true;
+    // the PCG iterations as one persistent cooperative kernel (ADIPC_OPT_PERSISTENT)
+    bool persistent = false;
+    DBuf<unsigned long long> phase_ns;  // its per-phase times (ADIPC_OPT_PROFILE)
 
     // per-kernel-class PCG timing (ADIPC_OPT_PROFILE): spmv, level 0, coarse, final
     bool profile = false;

@@ -260,6 +260,7 @@ void build_level(Ctx& c, DeviceLevel& L, const host::Level& hl, int level, std::
 // children are given as positions inside that subdomain.
 void link_levels(Ctx& c, const host::MasHierarchy& h) {
     cudaStream_t st = c.stream;
+    std::vector<std::vector<std::int32_t>> ups(h.n_levels());
     for (int l = 0; l + 1 < h.n_levels(); ++l) {
         const host::Level& cur = h.levels[l];
         const host::Level& nxt = h.levels[l + 1];
@@ -286,6 +287,16 @@ void link_levels(Ctx& c, const host::MasHierarchy& h) {
         upload(L.upc_pos, pos, st);
         upload(L.upc_node, node, st);
         upload(L.up_node, up, st);
+        ups[l] = std::move(up);
+    }
+    // ancestors of the level-1 nodes at every level >= 2 (update-pass RED targets)
+    if (h.n_levels() > 2) {
+        std::vector<std::int32_t> a = ups[1];
+        for (int l = 2; l < h.n_levels(); ++l) {
+            upload(c.levels[l]->anc, a, st);
+            if (l + 1 < h.n_levels())
+                for (auto& v : a) v = ups[l][v];
+        }
     }
 }
 

@@ -165,49 +165,159 @@ __device__ __forceinline__ void packed_matvec(const double* M, const double* b, 
     for (int t = 0; t < R; ++t) y[t] = acc0[t] + acc1[t];
 }
 
-// Rows [kRow0, kRow0 + kRows) of y = D^-1 b (lane i holds row kRow0 + i + 32 t
-// in y[t]); b read from shared memory (bs, kK entries, b_k = 0 for k >= dim).
-// Compile-time row ranges let the compiler pick the access per column: all
-// rows <= k -> column k, all rows > k -> their own columns, else per lane.
+// Row handled by `lane` in register slot t of packed_matvec_rows. Rows are
+// lane + 32 t from kRow0, except that for kK = 48 the upper half (rows 24..47)
+// puts rows 32..47 on lanes 0..15: the transposed reads D(j,k) = P[j(j+1)/2
+// + k] of a half-warp then fall in 16 distinct banks (j(j+1)/2 mod 16 is a
+// permutation of 0..15 over every 16-aligned run of rows).
+template <int kK, int kRow0>
+__device__ __forceinline__ int matvec_row(int lane, int t) {
+    if (kK == 48 && kRow0 == 24 && t == 0) return lane < 16 ? 32 + lane : 8 + lane;
+    return kRow0 + lane + 32 * t;
+}
+
+// Rows [kRow0, kRow0 + kRows) of y = D^-1 b (lane i holds row
+// matvec_row(i, t) in y[t]); b read from shared memory (bs, 16-byte aligned,
+// kK entries, b_k = 0 for k >= dim) two entries per 128-bit broadcast load.
+// Per column: all rows <= k read column k at a compile-time offset, all rows
+// > k their own column, and mixed columns select the offset per lane — one
+// shared load per row and column.
 template <int kK, int kRow0, int kRows>
 __device__ __forceinline__ void packed_matvec_rows(const double* M, const double* bs, double* y, int lane) {
     constexpr int R = (kRows + 31) / 32;
+    int jr[R];
     const double* P1[R];
     const double* P2[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) {
-        const int j = min(kRow0 + lane + 32 * t, kK - 1);
+        jr[t] = matvec_row<kK, kRow0>(lane, t);
+        const int j = min(jr[t], kK - 1);
         P1[t] = M + j;
         P2[t] = M + j * (j + 1) / 2;
     }
     double acc0[R], acc1[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) acc0[t] = acc1[t] = 0.0;
+    const double2* b2 = reinterpret_cast<const double2*>(bs);
 #pragma unroll
-    for (int k = 0; k < kK; ++k) {
-        const double bk = bs[k];
-        const int ck = k * (k + 1) / 2;
+    for (int k2 = 0; k2 < kK; k2 += 2) {
+        const double2 bb = b2[k2 >> 1];
 #pragma unroll
-        for (int t = 0; t < R; ++t) {
-            constexpr int dummy = 0;
-            (void)dummy;
-            const int jlo = kRow0 + 32 * t;
-            const int jhi = min(kRow0 + 32 * t + 31, kRow0 + kRows - 1);
-            double m;
-            if (jhi <= k)
-                m = P1[t][ck];
-            else if (jlo > k)
-                m = P2[t][k];
-            else
-                m = (kRow0 + lane + 32 * t <= k) ? P1[t][ck] : P2[t][k];
-            if (k & 1)
-                acc1[t] = fma(m, bk, acc1[t]);
-            else
-                acc0[t] = fma(m, bk, acc0[t]);
+        for (int u = 0; u < 2; ++u) {
+            const int k = k2 + u;
+            const double bk = u == 0 ? bb.x : bb.y;
+            const int ck = k * (k + 1) / 2;
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+                const int jlo = kRow0 + 32 * t;
+                const int jhi = min(kRow0 + 32 * t + 31, kRow0 + kRows - 1);
+                double m;
+                if (jhi <= k)
+                    m = P1[t][ck];
+                else if (jlo > k)
+                    m = P2[t][k];
+                else
+                    m = jr[t] <= k ? M[ck + jr[t]] : P2[t][k];
+                if (u == 1)
+                    acc1[t] = fma(m, bk, acc1[t]);
+                else
+                    acc0[t] = fma(m, bk, acc0[t]);
+            }
         }
     }
 #pragma unroll
     for (int t = 0; t < R; ++t) y[t] = acc0[t] + acc1[t];
+}
+
+// One warp of a pair (half 0: rows [0, kK/2), half 1: the rest) solves its
+// rows of a subdomain of dimension dim <= kK and hands each row j < dim to
+// store(j, y_j); returns the warp's share of b.y. Small subdomains (coarse
+// levels) take a shorter unrolled column loop.
+template <int kK>
+__device__ __forceinline__ int pick_cols(int dim) {
+    if (kK >= 48 && dim <= 12) return 12;
+    if (kK >= 48 && dim <= 24) return 24;
+    return kK;
+}
+
+template <int kK, class Store>
+__device__ __forceinline__ double pair_rows_solve(const double* M, const double* bs, int lane, int half, int dim,
+                                                  Store store) {
+    constexpr int kHalf = kK / 2;
+    constexpr int RY = (kHalf + 31) / 32;
+    double y[RY];
+    if (half == 0)
+        packed_matvec_rows<kK, 0, kHalf>(M, bs, y, lane);
+    else
+        packed_matvec_rows<kK, kHalf, kHalf>(M, bs, y, lane);
+    double dsum = 0;
+#pragma unroll
+    for (int t = 0; t < RY; ++t) {
+        const int i = lane + 32 * t;
+        const int j = half == 0 ? matvec_row<kK, 0>(lane, t) : matvec_row<kK, kHalf>(lane, t);
+        if (i < kHalf && j < dim) {
+            store(j, y[t]);
+            dsum += bs[j] * y[t];
+        }
+    }
+    return dsum;
+}
+
+template <int kK, class Store>
+__device__ __forceinline__ double pair_solve(const double* M, const double* bs, int lane, int half, int dim,
+                                             Store store) {
+    const int kc = pick_cols<kK>(dim);
+    if (kK >= 48 && kc == 12) return pair_rows_solve<12>(M, bs, lane, half, dim, store);
+    if (kK >= 48 && kc == 24) return pair_rows_solve<24>(M, bs, lane, half, dim, store);
+    return pair_rows_solve<kK>(M, bs, lane, half, dim, store);
+}
+
+// Half-warp mat-vec: the 16 lanes of half-warp h solve one subdomain, lane i
+// holding rows i + 16 t (t < kK/16). Every shared load of a column then
+// serves both half-warps' subdomains with one full 256-byte access, and a
+// 16-aligned run of rows reads its own columns D(j,k) = P[j(j+1)/2 + k] in 16
+// distinct banks. b from bs (this half's copy), two entries per 128-bit load.
+template <int kK>
+__device__ __forceinline__ void packed_matvec_half(const double* M, const double* bs, double* y, int hl) {
+    constexpr int T = (kK + 15) / 16;
+    const double* P1[T];
+    const double* P2[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int j = min(hl + 16 * t, kK - 1);
+        P1[t] = M + j;
+        P2[t] = M + j * (j + 1) / 2;
+    }
+    double acc0[T], acc1[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc0[t] = acc1[t] = 0.0;
+    const double2* b2 = reinterpret_cast<const double2*>(bs);
+#pragma unroll
+    for (int k2 = 0; k2 < kK; k2 += 2) {
+        const double2 bb = b2[k2 >> 1];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int k = k2 + u;
+            const double bk = u == 0 ? bb.x : bb.y;
+            const int ck = k * (k + 1) / 2;
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                double m;
+                if (16 * t + 15 <= k)
+                    m = P1[t][ck];
+                else if (16 * t > k)
+                    m = P2[t][k];
+                else
+                    m = hl + 16 * t <= k ? P1[t][ck] : P2[t][k];
+                if (u == 1)
+                    acc1[t] = fma(m, bk, acc1[t]);
+                else
+                    acc0[t] = fma(m, bk, acc0[t]);
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) y[t] = acc0[t] + acc1[t];
 }
 
 // column bound of packed_matvec for subdomains of at most max_fill nodes

@@ -47,6 +47,7 @@ void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, dou
 template <int kFinal>
 void launch_final_so(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a);
 void clear_restrict_so(Ctx& c);
+bool pcg_persistent(Ctx& c, const PcgArgs& a, double* partials, int restart, int max_iters);
 
 namespace {
 
@@ -241,9 +242,11 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
             launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
         mark(slot, 4);
     };
-    // capture the two iteration variants as graphs (non-profiled runs)
+    // the iterations as one persistent cooperative kernel (solve_order.cu)
+    const bool persist = so && pcg_persistent(c, a, part, restart, max_iters);
+    // otherwise: capture the two iteration variants as graphs (non-profiled runs)
     GraphExec g_norm, g_rest;
-    if (!prof) {
+    if (!prof && !persist) {
         auto capture = [&](bool is_restart, GraphExec& g) {
             cudaGraph_t graph;
             // kernels recorded into the graph are counted when the graph is
@@ -272,7 +275,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     if (!c.ev_chunk[0])
         for (auto& e : c.ev_chunk) ADIPC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     int k = 1, ci = 0;
-    bool done = false;
+    bool done = persist;
     while (!done && k <= max_iters) {
         const int kbeg = k, kend = std::min(max_iters, k + chunk - 1);
         for (; k <= kend; ++k) {
@@ -308,6 +311,12 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
         ++ci;
     }
     ADIPC_CUDA(cudaEventRecord(e1, st));
+    if (persist && prof) {  // per-phase device times of the persistent kernel
+        unsigned long long ns[4];
+        ADIPC_CUDA(cudaMemcpyAsync(ns, c.phase_ns.p, sizeof(ns), cudaMemcpyDeviceToHost, st));
+        ADIPC_CUDA(cudaStreamSynchronize(st));
+        for (int q = 0; q < 4; ++q) c.prof_ms[q] = static_cast<float>(ns[q] * 1e-6);
+    }
     int h_final[F_COUNT];
     ADIPC_CUDA(cudaMemcpyAsync(h_final, w.flags.p, sizeof(h_final), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaMemcpyAsync(h_scal, w.scal.p, sizeof(h_scal), cudaMemcpyDeviceToHost, st));
@@ -326,6 +335,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
         out.rel_residual = std::sqrt(std::fabs(rho) / h_scal[S_RHO_INIT]);
     }
     c.last_iters = out.iters;
+    if (persist && prof) c.prof_iters = out.iters;
     return out;
 }
 

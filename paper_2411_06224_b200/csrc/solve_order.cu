@@ -19,6 +19,10 @@
 // r.z comes from the per-level partial dots b_l.y_l of step 3 (the same
 // quantity: r.z = sum_l (P_l r).(D_l^-1 P_l r)).
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+#include <cooperative_groups.h>
 
 #include "mas_kernels.cuh"
 
@@ -38,7 +42,89 @@ struct SoRestrict {
     const std::int32_t* upc_node0;       // children (solve slots), ascending
     double* rr[kMaxLevels];              // restricted residual of level l >= 1 (3 per node)
     const std::int32_t* up_node[kMaxLevels];  // level-l node -> level-(l+1) node, l >= 1
+    const std::int32_t* anc[kMaxLevels];      // level-1 node -> its level-l node, l >= 2
+    int max_fill0;                            // largest level-0 subdomain (tile smem sizing)
 };
+
+// One tile of kUpdSubs level-0 subdomains of the update pass (solve order):
+// the vector update as a unit-stride stream, r kept in shared memory, then
+// the level-1 restricted residual of the level-1 nodes nested in the tile.
+// In solve order the tile's slots are [sub_ptr0[s0], sub_ptr0[s1]) and the
+// children lists of its level-1 nodes are exactly upc_node0 over that same
+// range (CSR in node order), so all restriction metadata is fetched with
+// coalesced loads issued together with the vector stream. Levels >= 2 take
+// the level-1 sums by RED through the precomputed ancestors (no dependent
+// chain). smem: 3 * slots doubles, then (slots + 1 + slots) ints.
+template <int kMode, int kThreads>
+__device__ __forceinline__ void update_tile(const SoRestrict& so, const PcgArgs& a, double alpha,
+                                            const double* __restrict__ apv, std::int32_t tile, double* smem) {
+    const std::int32_t s0 = tile * kUpdSubs;
+    const std::int32_t s1 = min(s0 + kUpdSubs, so.n0_parts);
+    const std::int32_t slot0 = so.sub_ptr0[s0], slot1 = so.sub_ptr0[s1];
+    const std::int32_t v0 = so.up_first0[s0], v1 = so.up_first0[s1];
+    const std::int64_t g0 = 3 * static_cast<std::int64_t>(slot0);
+    const std::int64_t g1 = 3 * static_cast<std::int64_t>(slot1);
+    const int cap = kUpdSubs * so.max_fill0;
+    double* sr = smem;
+    int* uptr = reinterpret_cast<int*>(smem + 3 * cap);
+    int* child = uptr + cap + 1;
+    for (int i = threadIdx.x; i <= v1 - v0; i += kThreads) uptr[i] = so.upc_ptr0[v0 + i] - slot0;
+    for (int i = threadIdx.x; i < slot1 - slot0; i += kThreads) child[i] = so.upc_node0[slot0 + i] - slot0;
+    constexpr int kU = 4;
+    for (std::int64_t gb = g0 + threadIdx.x; gb < g1; gb += kU * kThreads) {
+        double rv[kU], pv[kU], av[kU], xv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const std::int64_t g = gb + u * kThreads;
+            if (g < g1) {
+                av[u] = apv[g];
+                if (kMode == M_UPDATE) {
+                    rv[u] = a.r[g];
+                    pv[u] = a.p[g];
+                    xv[u] = a.x[g];
+                } else {
+                    rv[u] = a.b[g];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const std::int64_t g = gb + u * kThreads;
+            if (g < g1) {
+                double nr;
+                if (kMode == M_UPDATE) {
+                    a.x[g] = xv[u] + alpha * pv[u];
+                    nr = rv[u] - alpha * av[u];
+                } else {  // M_RESTART: r = b - A x (x updated before the restart SpMV)
+                    nr = rv[u] - av[u];
+                }
+                a.r[g] = nr;
+                sr[g - g0] = nr;
+            }
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 3 * (v1 - v0); t += kThreads) {
+        const int i = t / 3, comp = t % 3;
+        const std::int32_t v = v0 + i;
+        std::int32_t w[kMaxLevels];
+#pragma unroll
+        for (int l = 2; l < kMaxLevels; ++l)
+            if (l < so.n_levels) w[l] = so.anc[l][v];
+        double acc = 0;
+        for (int q = uptr[i]; q < uptr[i + 1]; ++q) acc += sr[3 * child[q] + comp];
+        so.rr[1][3 * static_cast<std::int64_t>(v) + comp] = acc;
+#pragma unroll
+        for (int l = 2; l < kMaxLevels; ++l)
+            if (l < so.n_levels) red_add(so.rr[l] + 3 * static_cast<std::int64_t>(w[l]) + comp, acc);
+    }
+    __syncthreads();
+}
+
+inline std::size_t update_tile_smem(int max_fill0) {
+    const std::size_t cap = static_cast<std::size_t>(kUpdSubs) * max_fill0;
+    return sizeof(double) * 3 * cap + sizeof(int) * (2 * cap + 1);
+}
 
 template <int kMode>
 __global__ void __launch_bounds__(kUpdThreads) k_update_so(SoRestrict so, PcgArgs a) {
@@ -46,63 +132,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_update_so(SoRestrict so, PcgArg
     double alpha = 0;
     if (a.flags[F_DONE]) return;
     if (!pcg_alpha(a, alpha)) return;
-    const std::int32_t s0 = blockIdx.x * kUpdSubs;
-    const std::int32_t s1 = min(s0 + kUpdSubs, so.n0_parts);
-    const std::int64_t g0 = 3 * static_cast<std::int64_t>(so.sub_ptr0[s0]);
-    const std::int64_t g1 = 3 * static_cast<std::int64_t>(so.sub_ptr0[s1]);
-    const double* __restrict__ p = a.p;
-    const double* __restrict__ ap = a.ap;
-    const double* __restrict__ b = a.b;
-    double* __restrict__ x = a.x;
-    double* __restrict__ r = a.r;
-    constexpr int kU = 4;  // elements per thread in flight
-    for (std::int64_t gb = g0 + threadIdx.x; gb < g1; gb += kU * kUpdThreads) {
-        double rv[kU], pv[kU], av[kU], xv[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const std::int64_t g = gb + u * kUpdThreads;
-            if (g < g1) {
-                av[u] = ap[g];
-                if (kMode == M_UPDATE) {
-                    rv[u] = r[g];
-                    pv[u] = p[g];
-                    xv[u] = x[g];
-                } else {
-                    rv[u] = b[g];
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const std::int64_t g = gb + u * kUpdThreads;
-            if (g < g1) {
-                double nr;
-                if (kMode == M_UPDATE) {
-                    x[g] = xv[u] + alpha * pv[u];
-                    nr = rv[u] - alpha * av[u];
-                } else {  // M_RESTART: r = b - A x (x updated before the restart SpMV)
-                    nr = rv[u] - av[u];
-                }
-                r[g] = nr;
-                sr[g - g0] = nr;
-            }
-        }
-    }
-    __syncthreads();
-    const std::int32_t v0 = so.up_first0[s0], v1 = so.up_first0[s1];
-    for (int t = threadIdx.x; t < 3 * (v1 - v0); t += kUpdThreads) {
-        const std::int32_t v = v0 + t / 3;
-        const int comp = t % 3;
-        double acc = 0;
-        for (std::int32_t q = so.upc_ptr0[v]; q < so.upc_ptr0[v + 1]; ++q)
-            acc += sr[3 * static_cast<std::int64_t>(so.upc_node0[q]) - g0 + comp];
-        so.rr[1][3 * static_cast<std::int64_t>(v) + comp] = acc;
-        std::int32_t w = v;
-        for (int l = 1; l + 1 < so.n_levels; ++l) {
-            w = so.up_node[l][w];
-            red_add(so.rr[l + 1] + 3 * static_cast<std::int64_t>(w) + comp, acc);
-        }
-    }
+    update_tile<kMode, kUpdThreads>(so, a, alpha, a.ap, blockIdx.x, sr);
 }
 
 // ---- level-0 solve: persistent warp pairs, TMA ring of packed inverses -------
@@ -136,8 +166,6 @@ __global__ void __launch_bounds__(256) k_precond_so(PrecondTable pt, double* __r
                                                    unsigned* __restrict__ ticket, double* __restrict__ dot_out,
                                                    const int* __restrict__ flags, int slot_doubles) {
     constexpr int RB = (kK + 31) / 32;  // b entries per lane
-    constexpr int kHalf = kK / 2;       // rows per warp
-    constexpr int RY = (kHalf + 31) / 32;
     if (flags && flags[F_DONE]) return;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, pair = w >> 1, half = w & 1;
@@ -149,11 +177,32 @@ __global__ void __launch_bounds__(256) k_precond_so(PrecondTable pt, double* __r
                              reinterpret_cast<double*>(smem) + static_cast<std::size_t>(npc) * kStages * slot_doubles +
                              static_cast<std::size_t>(2 * npc) * kK) +
                          pair * kStages;
-    const std::int32_t n_work = pt.base[pt.n];
+    // every pair takes an even share of EACH level (a contiguous run per
+    // level, level 0 first): the coarse items, cheap in bytes but with a
+    // longer gather chain, are spread over all pairs instead of piling up at
+    // the end of the work list
     const std::int64_t gp = static_cast<std::int64_t>(blockIdx.x) * npc + pair;
     const std::int64_t np = static_cast<std::int64_t>(gridDim.x) * npc;
-    const std::int32_t q0 = static_cast<std::int32_t>(gp * n_work / np);
-    const std::int32_t q1 = static_cast<std::int32_t>((gp + 1) * n_work / np);
+    std::int32_t lv_lo[kMaxLevels], lv_n[kMaxLevels];
+    int nloc = 0;
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l) {
+        lv_lo[l] = lv_n[l] = 0;
+        if (l < pt.n) {
+            const std::int64_t nl = pt.base[l + 1] - pt.base[l];
+            lv_lo[l] = pt.base[l] + static_cast<std::int32_t>(gp * nl / np);
+            lv_n[l] = static_cast<std::int32_t>((gp + 1) * nl / np - gp * nl / np);
+            nloc += lv_n[l];
+        }
+    }
+    auto item = [&](int i) -> std::int32_t {
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l) {
+            if (i < lv_n[l]) return lv_lo[l] + i;
+            i -= lv_n[l];
+        }
+        return 0;
+    };
     auto level_of = [&](std::int32_t q) {
         int l = 0;
         while (l + 1 < pt.n && q >= pt.base[l + 1]) ++l;
@@ -177,7 +226,7 @@ __global__ void __launch_bounds__(256) k_precond_so(PrecondTable pt, double* __r
     if (half == 0 && lane == 0) {
         for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
         fence_mbar_init();
-        for (int st = 0; st < kStages && q0 + st < q1; ++st) issue(q0 + st, st);
+        for (int st = 0; st < kStages && st < nloc; ++st) issue(item(st), st);
     }
     pair_sync(pair);
     // b of a work item and the addresses of its rows (gathered for coarse levels)
@@ -202,39 +251,27 @@ __global__ void __launch_bounds__(256) k_precond_so(PrecondTable pt, double* __r
     };
     Item cur{0, 0, 0};
     double b[RB];
-    if (q0 < q1) load_b(q0, cur, b);
+    if (nloc > 0) load_b(item(0), cur, b);
     double dsum = 0;
     int st = 0;
     std::uint32_t par = 0;
-    for (std::int32_t q = q0; q < q1; ++q) {
+    for (int i = 0; i < nloc; ++i) {
 #pragma unroll
         for (int t = 0; t < RB; ++t)
             if (lane + 32 * t < kK) bs[lane + 32 * t] = b[t];
         Item nxt{0, 0, 0};
         double bn[RB];
-        if (q + 1 < q1) load_b(q + 1, nxt, bn);
+        if (i + 1 < nloc) load_b(item(i + 1), nxt, bn);
         __syncwarp();
         mbar_wait(&bar[st], par);
         const double* M = ring + static_cast<std::size_t>(st) * slot_doubles;
-        double y[RY];
-        if (half == 0)
-            packed_matvec_rows<kK, 0, kHalf>(M, bs, y, lane);
-        else
-            packed_matvec_rows<kK, kHalf, kHalf>(M, bs, y, lane);
         double* out = pt.out[cur.l];
-#pragma unroll
-        for (int t = 0; t < RY; ++t) {
-            const int i = lane + 32 * t;
-            const int j = half * kHalf + i;
-            if (i < kHalf && j < cur.dim) {
-                out[row_index(cur, j)] = y[t];
-                dsum += bs[j] * y[t];
-            }
-        }
+        dsum += pair_solve<kK>(M, bs, lane, half, cur.dim,
+                               [&](int j, double v) { out[row_index(cur, j)] = v; });
         pair_sync(pair);  // both warps are done with the slot and with bs
-        if (half == 0 && lane == 0 && q + kStages < q1) {  // refill kStages items ahead
+        if (half == 0 && lane == 0 && i + kStages < nloc) {  // refill kStages items ahead
             fence_proxy_async();
-            issue(q + kStages, st);
+            issue(item(i + kStages), st);
         }
         if (++st == kStages) {
             st = 0;
@@ -328,6 +365,746 @@ __global__ void __launch_bounds__(256) k_final_so(std::int32_t n, FinalSo fa, co
 }
 
 
+// Variant of k_precond_so with ONE warp per item (rows 0..31 on the lanes,
+// rows 32..47 on lanes 0..15 of a second register slot): every column is
+// three full 128-byte shared wavefronts instead of the pair split's partial
+// ones, and b is broadcast once per item instead of once per warp. Each warp
+// owns its ring of kStages slots; warps per CTA = blockDim.x / 32.
+template <int kK, int kStages>
+__global__ void __launch_bounds__(128) k_precond_so1(PrecondTable pt, double* __restrict__ partials,
+                                                    unsigned* __restrict__ ticket, double* __restrict__ dot_out,
+                                                    const int* __restrict__ flags, int slot_doubles) {
+    constexpr int RB = (kK + 31) / 32;
+    if (flags && flags[F_DONE]) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwc = blockDim.x >> 5;
+    double* ring = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(w) * kStages * slot_doubles;
+    double* bs = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(nwc) * kStages * slot_doubles +
+                 static_cast<std::size_t>(w) * kK;
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(
+                             reinterpret_cast<double*>(smem) + static_cast<std::size_t>(nwc) * kStages * slot_doubles +
+                             static_cast<std::size_t>(nwc) * kK) +
+                         w * kStages;
+    const std::int64_t gp = static_cast<std::int64_t>(blockIdx.x) * nwc + w;
+    const std::int64_t np = static_cast<std::int64_t>(gridDim.x) * nwc;
+    std::int32_t lv_lo[kMaxLevels], lv_n[kMaxLevels];
+    int nloc = 0;
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l) {
+        lv_lo[l] = lv_n[l] = 0;
+        if (l < pt.n) {
+            const std::int64_t nl = pt.base[l + 1] - pt.base[l];
+            lv_lo[l] = pt.base[l] + static_cast<std::int32_t>(gp * nl / np);
+            lv_n[l] = static_cast<std::int32_t>((gp + 1) * nl / np - gp * nl / np);
+            nloc += lv_n[l];
+        }
+    }
+    auto item = [&](int i) -> std::int32_t {
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l) {
+            if (i < lv_n[l]) return lv_lo[l] + i;
+            i -= lv_n[l];
+        }
+        return 0;
+    };
+    auto level_of = [&](std::int32_t q) {
+        int l = 0;
+        while (l + 1 < pt.n && q >= pt.base[l + 1]) ++l;
+        return l;
+    };
+    for (int i = lane; i < kStages * slot_doubles; i += 32) ring[i] = 0.0;  // finite slot tails
+    fence_proxy_async();
+    __syncwarp();
+    auto issue = [&](std::int32_t q, int st) {  // lane 0
+        const int l = level_of(q);
+        const std::int32_t s = q - pt.base[l];
+        const std::int64_t o = pt.inv_off[l][s];
+        const std::uint32_t bytes = static_cast<std::uint32_t>((pt.inv_off[l][s + 1] - o) * 8);
+        mbar_arrive_expect_tx(&bar[st], bytes);
+        if (l == 0)
+            bulk_g2s_evict_first(ring + static_cast<std::size_t>(st) * slot_doubles, pt.inv[0] + o, bytes, &bar[st]);
+        else
+            bulk_g2s_evict_last(ring + static_cast<std::size_t>(st) * slot_doubles, pt.inv[l] + o, bytes, &bar[st]);
+    };
+    if (lane == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
+        fence_mbar_init();
+        for (int st = 0; st < kStages && st < nloc; ++st) issue(item(st), st);
+    }
+    __syncwarp();
+    struct Item {
+        int l;
+        std::int32_t s0, dim;
+    };
+    auto row_index = [&](const Item& it, int j) -> std::int64_t {
+        if (it.l == 0) return 3 * static_cast<std::int64_t>(it.s0) + j;
+        return 3 * static_cast<std::int64_t>(pt.sub_nodes[it.l][it.s0 + j / 3]) + (j % 3);
+    };
+    auto load_b = [&](std::int32_t q, Item& it, double* bb) {
+        it.l = level_of(q);
+        const std::int32_t s = q - pt.base[it.l];
+        it.s0 = pt.sub_ptr[it.l][s];
+        it.dim = 3 * (pt.sub_ptr[it.l][s + 1] - it.s0);
+#pragma unroll
+        for (int t = 0; t < RB; ++t) {
+            const int j = lane + 32 * t;
+            bb[t] = j < it.dim ? ldg_issue(pt.rin[it.l] + row_index(it, j)) : 0.0;
+        }
+    };
+    Item cur{0, 0, 0};
+    double b[RB];
+    if (nloc > 0) load_b(item(0), cur, b);
+    double dsum = 0;
+    int st = 0;
+    std::uint32_t par = 0;
+    for (int i = 0; i < nloc; ++i) {
+#pragma unroll
+        for (int t = 0; t < RB; ++t)
+            if (lane + 32 * t < kK) bs[lane + 32 * t] = b[t];
+        Item nxt{0, 0, 0};
+        double bn[RB];
+        if (i + 1 < nloc) load_b(item(i + 1), nxt, bn);
+        __syncwarp();
+        mbar_wait(&bar[st], par);
+        const double* M = ring + static_cast<std::size_t>(st) * slot_doubles;
+        constexpr int R = (kK + 31) / 32;
+        double y[R];
+        const int kc = pick_cols<kK>(cur.dim);
+        double* out = pt.out[cur.l];
+        auto emit = [&](auto kc_tag) {
+            constexpr int K2 = decltype(kc_tag)::value;
+            constexpr int R2 = (K2 + 31) / 32;
+            double yy[R2];
+            packed_matvec_rows<K2, 0, K2>(M, bs, yy, lane);
+#pragma unroll
+            for (int t = 0; t < R2; ++t) {
+                const int j = matvec_row<K2, 0>(lane, t);
+                if (j < cur.dim) {
+                    out[row_index(cur, j)] = yy[t];
+                    dsum += bs[j] * yy[t];
+                }
+            }
+        };
+        (void)y;
+        if (kK >= 48 && kc == 12)
+            emit(std::integral_constant<int, 12>{});
+        else if (kK >= 48 && kc == 24)
+            emit(std::integral_constant<int, 24>{});
+        else
+            emit(std::integral_constant<int, kK>{});
+        __syncwarp();
+        if (lane == 0 && i + kStages < nloc) {
+            fence_proxy_async();
+            issue(item(i + kStages), st);
+        }
+        if (++st == kStages) {
+            st = 0;
+            par ^= 1u;
+        }
+        cur = nxt;
+#pragma unroll
+        for (int t = 0; t < RB; ++t) b[t] = bn[t];
+    }
+    grid_sum_last_block(dsum, partials, ticket, dot_out);
+}
+
+// Variant with TWO items per warp, one per half-warp (lane i of the half
+// holds rows i + 16 t): every column's shared load is a full 256-byte access
+// serving both items, and the transposed reads of each 16-aligned run of rows
+// hit 16 distinct banks (~4x fewer shared wavefronts per item than the pair
+// split). Each warp streams its items two at a time through a ring of kStages
+// double slots.
+template <int kK, int kStages>
+__global__ void __launch_bounds__(128) k_precond_so2(PrecondTable pt, double* __restrict__ partials,
+                                                    unsigned* __restrict__ ticket, double* __restrict__ dot_out,
+                                                    const int* __restrict__ flags, int slot_doubles) {
+    constexpr int T = (kK + 15) / 16;
+    constexpr int kBs = kK + 2;  // per-half b copy (padded: the halves' broadcasts hit different banks)
+    if (flags && flags[F_DONE]) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwc = blockDim.x >> 5;
+    const int half = lane >> 4, hl = lane & 15;
+    double* ring = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(w) * kStages * 2 * slot_doubles;
+    double* bsw = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(nwc) * kStages * 2 * slot_doubles +
+                  static_cast<std::size_t>(w) * 2 * kBs;
+    double* bs = bsw + half * kBs;
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(
+                             reinterpret_cast<double*>(smem) + static_cast<std::size_t>(nwc) * kStages * 2 * slot_doubles +
+                             static_cast<std::size_t>(nwc) * 2 * kBs) +
+                         w * kStages;
+    const std::int64_t gp = static_cast<std::int64_t>(blockIdx.x) * nwc + w;
+    const std::int64_t np = static_cast<std::int64_t>(gridDim.x) * nwc;
+    std::int32_t lv_lo[kMaxLevels], lv_n[kMaxLevels];
+    int nloc = 0;
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l) {
+        lv_lo[l] = lv_n[l] = 0;
+        if (l < pt.n) {
+            const std::int64_t nl = pt.base[l + 1] - pt.base[l];
+            lv_lo[l] = pt.base[l] + static_cast<std::int32_t>(gp * nl / np);
+            lv_n[l] = static_cast<std::int32_t>((gp + 1) * nl / np - gp * nl / np);
+            nloc += lv_n[l];
+        }
+    }
+    auto item = [&](int i) -> std::int32_t {
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l) {
+            if (i < lv_n[l]) return lv_lo[l] + i;
+            i -= lv_n[l];
+        }
+        return 0;
+    };
+    auto level_of = [&](std::int32_t q) {
+        int l = 0;
+        while (l + 1 < pt.n && q >= pt.base[l + 1]) ++l;
+        return l;
+    };
+    const int nsteps = (nloc + 1) / 2;
+    for (int i = lane; i < kStages * 2 * slot_doubles; i += 32) ring[i] = 0.0;  // finite slot tails
+    for (int i = lane; i < 2 * kBs; i += 32) bsw[i] = 0.0;
+    fence_proxy_async();
+    __syncwarp();
+    auto issue = [&](int step, int st) {  // lane 0: both items of a step on one barrier
+        std::uint32_t total = 0;
+        std::int64_t off[2];
+        std::uint32_t bytes[2] = {0, 0};
+        int lv[2] = {0, 0};
+        for (int h = 0; h < 2; ++h) {
+            const int i = 2 * step + h;
+            if (i >= nloc) continue;
+            const std::int32_t q = item(i);
+            lv[h] = level_of(q);
+            const std::int32_t s = q - pt.base[lv[h]];
+            off[h] = pt.inv_off[lv[h]][s];
+            bytes[h] = static_cast<std::uint32_t>((pt.inv_off[lv[h]][s + 1] - off[h]) * 8);
+            total += bytes[h];
+        }
+        mbar_arrive_expect_tx(&bar[st], total);
+        for (int h = 0; h < 2; ++h) {
+            if (!bytes[h]) continue;
+            double* dst = ring + (static_cast<std::size_t>(st) * 2 + h) * slot_doubles;
+            if (lv[h] == 0)
+                bulk_g2s_evict_first(dst, pt.inv[0] + off[h], bytes[h], &bar[st]);
+            else
+                bulk_g2s_evict_last(dst, pt.inv[lv[h]] + off[h], bytes[h], &bar[st]);
+        }
+    };
+    if (lane == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
+        fence_mbar_init();
+        for (int st = 0; st < kStages && st < nsteps; ++st) issue(st, st);
+    }
+    __syncwarp();
+    struct Item {
+        int l;
+        std::int32_t s0, dim;
+    };
+    auto row_index = [&](const Item& it, int j) -> std::int64_t {
+        if (it.l == 0) return 3 * static_cast<std::int64_t>(it.s0) + j;
+        return 3 * static_cast<std::int64_t>(pt.sub_nodes[it.l][it.s0 + j / 3]) + (j % 3);
+    };
+    // this half's item of a step (dim 0 when the step has a single item)
+    auto load_b = [&](int step, Item& it, double* bb) {
+        const int i = 2 * step + half;
+        it.l = 0;
+        it.s0 = 0;
+        it.dim = 0;
+        if (i < nloc) {
+            const std::int32_t q = item(i);
+            it.l = level_of(q);
+            const std::int32_t s = q - pt.base[it.l];
+            it.s0 = pt.sub_ptr[it.l][s];
+            it.dim = 3 * (pt.sub_ptr[it.l][s + 1] - it.s0);
+        }
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const int j = hl + 16 * t;
+            bb[t] = j < it.dim ? ldg_issue(pt.rin[it.l] + row_index(it, j)) : 0.0;
+        }
+    };
+    Item cur{0, 0, 0};
+    double b[T];
+    if (nsteps > 0) load_b(0, cur, b);
+    double dsum = 0;
+    int st = 0;
+    std::uint32_t par = 0;
+    for (int step = 0; step < nsteps; ++step) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) bs[hl + 16 * t] = b[t];
+        Item nxt{0, 0, 0};
+        double bn[T];
+        if (step + 1 < nsteps) load_b(step + 1, nxt, bn);
+        __syncwarp();
+        mbar_wait(&bar[st], par);
+        const double* M = ring + (static_cast<std::size_t>(st) * 2 + half) * slot_doubles;
+        const int dmax = max(cur.dim, __shfl_xor_sync(0xffffffffu, cur.dim, 16));
+        const int kc = pick_cols<kK>(dmax);
+        double* out = pt.out[cur.l];
+        auto emit = [&](auto kc_tag) {
+            constexpr int K2 = decltype(kc_tag)::value;
+            constexpr int T2 = (K2 + 15) / 16;
+            double yy[T2];
+            packed_matvec_half<K2>(M, bs, yy, hl);
+#pragma unroll
+            for (int t = 0; t < T2; ++t) {
+                const int j = hl + 16 * t;
+                if (j < cur.dim) {
+                    out[row_index(cur, j)] = yy[t];
+                    dsum += bs[j] * yy[t];
+                }
+            }
+        };
+        if (kK >= 48 && kc == 12)
+            emit(std::integral_constant<int, 12>{});
+        else if (kK >= 48 && kc == 24)
+            emit(std::integral_constant<int, 24>{});
+        else
+            emit(std::integral_constant<int, kK>{});
+        __syncwarp();
+        if (lane == 0 && step + kStages < nsteps) {
+            fence_proxy_async();
+            issue(step + kStages, st);
+        }
+        if (++st == kStages) {
+            st = 0;
+            par ^= 1u;
+        }
+        cur = nxt;
+#pragma unroll
+        for (int t = 0; t < T; ++t) b[t] = bn[t];
+    }
+    grid_sum_last_block(dsum, partials, ticket, dot_out);
+}
+
+// ============================================================================
+// The whole PCG loop as ONE persistent cooperative kernel (pcg.hpp:59-85).
+// Every iteration is four phases separated by grid barriers:
+//   S  SpMV Ap = A p with the p.Ap partials (TMA-staged tiles, as k_spmv_tma)
+//   U  x += alpha p, r -= alpha Ap, restriction to every coarse level
+//   P  every MAS level's dense solves (warp pairs, TMA ring, as k_precond_so)
+//   F  prolongation, convergence test, p = z + beta p, Ap cleared
+// (+ the restart iterations' x update and A x SpMV, pcg.hpp:69-74). The dots
+// are per-CTA partials that every CTA sums in the same fixed order after the
+// barrier, so alpha, beta and the stop decision are identical in every CTA
+// and never leave the device; the kernel-boundary ramp-up/drain of the four
+// kernels per iteration (and their CTA launches) are gone. Shared memory is
+// one union region that each phase lays out for itself (the phases are
+// separated by grid barriers and every TMA copy a phase issues is consumed
+// inside it).
+namespace cg = cooperative_groups;
+
+constexpr int kPT = 256;     // threads per CTA (8 warps, 4 warp pairs)
+constexpr int kPWarps = kPT / 32;
+constexpr int kPPairs = kPT / 64;
+
+struct __align__(16) SpmvStage {
+    double blk[288];
+    std::uint32_t rows[32];
+    std::uint32_t cols[32];
+};
+
+struct Persist {
+    const std::uint32_t* rows;
+    const std::uint32_t* cols;
+    const double* blocks;
+    std::int64_t U;
+    std::int32_t n;
+    double* x;
+    double* r;
+    double* p;
+    double* ap;
+    double* z;
+    double* tmp;
+    const double* b;
+    SoRestrict so;
+    PrecondTable pt;
+    FinalSo fa;
+    double* partials;  // 2 x gridDim.x
+    double* scal;
+    int* flags;
+    unsigned long long* phase_ns;  // optional: S, U, P, F (summed by CTA 0)
+    int restart, max_iters;
+    int slot_doubles;              // preconditioner ring slot (packed_doubles(kK))
+    int union_bytes;               // bytes of the shared union region
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// grid barrier; generic shared accesses of this phase are ordered before the
+// next phase's TMA writes into the same bytes
+__device__ __forceinline__ void phase_sync(cg::grid_group& grid) {
+    fence_proxy_async();
+    grid.sync();
+}
+
+// fixed-order sum of the per-CTA partials (identical in every CTA)
+__device__ __forceinline__ double sum_partials(const double* part, double* red) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = 0;
+        for (unsigned i = threadIdx.x; i < gridDim.x; i += 32) v += __ldcg(part + i);
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double v = red[0];
+    __syncthreads();
+    return v;
+}
+
+__device__ __forceinline__ void store_partial(double v, double* part, double* red) {
+    const double bs = block_sum(v, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = bs;
+}
+
+// ---- S: y (+)= A x over the solve-order matrix, p.Ap partial (kDot) ----------
+template <bool kDot, int kSS>
+__device__ double spmv_phase(const Persist& P, const double* __restrict__ xin, double* __restrict__ y,
+                             unsigned char* smem, std::uint64_t* sbar, std::uint32_t& cnt) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    SpmvStage* stage = reinterpret_cast<SpmvStage*>(smem) + w * kSS;
+    std::uint64_t* bar = sbar + w * kSS;
+    const std::int64_t warp0 = static_cast<std::int64_t>(blockIdx.x) * kPWarps + w;
+    const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * kPWarps;
+    const std::int64_t n_chunks = (P.U + 31) >> 5;
+    const std::int64_t ch0 = warp0 * n_chunks / nwarps, ch1 = (warp0 + 1) * n_chunks / nwarps;
+    auto issue = [&](std::int64_t ch, std::uint32_t c) {  // lane 0
+        const int s = static_cast<int>(c % kSS);
+        mbar_arrive_expect_tx(&bar[s], static_cast<std::uint32_t>(sizeof(SpmvStage)));
+        bulk_g2s_evict_first(stage[s].blk, P.blocks + ch * 288, 288 * 8, &bar[s]);
+        bulk_g2s_evict_first(stage[s].rows, P.rows + ch * 32, 128, &bar[s]);
+        bulk_g2s_evict_first(stage[s].cols, P.cols + ch * 32, 128, &bar[s]);
+    };
+    if (lane == 0) {
+        fence_proxy_async();
+        for (int i = 0; i < kSS && ch0 + i < ch1; ++i) issue(ch0 + i, cnt + i);
+    }
+    __syncwarp();
+    std::uint32_t r = 0xFFFFFFFFu, c = 0;
+    double g[6];
+    auto gather = [&](std::int64_t ch, std::uint32_t cc, std::uint32_t& rr, std::uint32_t& cl, double* gg) {
+        const int s = static_cast<int>(cc % kSS);
+        mbar_wait(&bar[s], (cc / kSS) & 1u);
+        const bool valid = (ch << 5) + lane < P.U;
+        rr = valid ? stage[s].rows[lane] : 0xFFFFFFFFu;
+        cl = valid ? stage[s].cols[lane] : 0u;
+        const std::uint32_t rx = valid ? rr : 0u;
+        gg[0] = ldg_issue(xin + 3 * cl);
+        gg[1] = ldg_issue(xin + 3 * cl + 1);
+        gg[2] = ldg_issue(xin + 3 * cl + 2);
+        gg[3] = ldg_issue(xin + 3 * rx);
+        gg[4] = ldg_issue(xin + 3 * rx + 1);
+        gg[5] = ldg_issue(xin + 3 * rx + 2);
+    };
+    if (ch0 < ch1) gather(ch0, cnt, r, c, g);
+    double dsum = 0;
+    for (std::int64_t ch = ch0; ch < ch1; ++ch, ++cnt) {
+        const int s = static_cast<int>(cnt % kSS);
+        double h[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) h[k] = stage[s].blk[32 * k + lane];
+        std::uint32_t rn = 0xFFFFFFFFu, cn = 0;
+        double gn[6];
+        if (ch + 1 < ch1) gather(ch + 1, cnt + 1, rn, cn, gn);
+        __syncwarp();
+        if (lane == 0 && ch + kSS < ch1) {
+            fence_proxy_async();
+            issue(ch + kSS, cnt + kSS);
+        }
+        const bool valid = r != 0xFFFFFFFFu;
+        double yr0 = 0, yr1 = 0, yr2 = 0;
+        if (valid) {
+            yr0 = h[0] * g[0] + h[3] * g[1] + h[6] * g[2];
+            yr1 = h[1] * g[0] + h[4] * g[1] + h[7] * g[2];
+            yr2 = h[2] * g[0] + h[5] * g[1] + h[8] * g[2];
+            if (r != c) {
+                red_add(y + 3 * c, h[0] * g[3] + h[1] * g[4] + h[2] * g[5]);
+                red_add(y + 3 * c + 1, h[3] * g[3] + h[4] * g[4] + h[5] * g[5]);
+                red_add(y + 3 * c + 2, h[6] * g[3] + h[7] * g[4] + h[8] * g[5]);
+            }
+            if (kDot) dsum += (r != c ? 2.0 : 1.0) * (g[3] * yr0 + g[4] * yr1 + g[5] * yr2);
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double a0 = __shfl_down_sync(0xffffffffu, yr0, off);
+            const double a1 = __shfl_down_sync(0xffffffffu, yr1, off);
+            const double a2 = __shfl_down_sync(0xffffffffu, yr2, off);
+            const std::uint32_t ro = __shfl_down_sync(0xffffffffu, r, off);
+            if (lane + off < 32 && ro == r) {
+                yr0 += a0;
+                yr1 += a1;
+                yr2 += a2;
+            }
+        }
+        const std::uint32_t rprev = __shfl_up_sync(0xffffffffu, r, 1);
+        if (valid && (lane == 0 || rprev != r)) {
+            red_add(y + 3 * r, yr0);
+            red_add(y + 3 * r + 1, yr1);
+            red_add(y + 3 * r + 2, yr2);
+        }
+        r = rn;
+        c = cn;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) g[k] = gn[k];
+    }
+    return dsum;
+}
+
+// ---- U: vector update + restriction to every coarse level --------------------
+template <int kMode>
+__device__ void update_phase(const Persist& P, double alpha, const double* __restrict__ apv, double* sm) {
+    PcgArgs a{};
+    a.x = P.x;
+    a.r = P.r;
+    a.p = P.p;
+    a.b = P.b;
+    const std::int32_t ntiles = static_cast<std::int32_t>(ceil_div(P.so.n0_parts, kUpdSubs));
+    for (std::int32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        update_tile<kMode, kPT>(P.so, a, alpha, apv, tile, sm);
+}
+
+// ---- P: every level's dense solves, z / y_l, partial r.z ----------------------
+template <int kK, int kSP>
+__device__ double precond_phase(const Persist& P, unsigned char* smem, std::uint64_t* pbar, std::uint32_t& cnt) {
+    constexpr int RB = (kK + 31) / 32;
+    const PrecondTable& pt = P.pt;
+    const int slot = P.slot_doubles;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, pair = w >> 1, half = w & 1;
+    double* ring = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(pair) * kSP * slot;
+    double* bs = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(kPPairs) * kSP * slot +
+                 static_cast<std::size_t>(w) * kK;
+    std::uint64_t* bar = pbar + pair * kSP;
+    // every pair takes an even share of EACH level (a contiguous run per
+    // level, level 0 first): the coarse items, cheap in bytes but with a
+    // longer gather chain, are spread over all pairs instead of piling up at
+    // the end of the work list
+    const std::int64_t gp = static_cast<std::int64_t>(blockIdx.x) * kPPairs + pair;
+    const std::int64_t np = static_cast<std::int64_t>(gridDim.x) * kPPairs;
+    std::int32_t lv_lo[kMaxLevels], lv_n[kMaxLevels];
+    int nloc = 0;
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l) {
+        lv_lo[l] = lv_n[l] = 0;
+        if (l < pt.n) {
+            const std::int64_t nl = pt.base[l + 1] - pt.base[l];
+            lv_lo[l] = pt.base[l] + static_cast<std::int32_t>(gp * nl / np);
+            lv_n[l] = static_cast<std::int32_t>((gp + 1) * nl / np - gp * nl / np);
+            nloc += lv_n[l];
+        }
+    }
+    auto item = [&](int i) -> std::int32_t {
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l) {
+            if (i < lv_n[l]) return lv_lo[l] + i;
+            i -= lv_n[l];
+        }
+        return 0;
+    };
+    auto level_of = [&](std::int32_t q) {
+        int l = 0;
+        while (l + 1 < pt.n && q >= pt.base[l + 1]) ++l;
+        return l;
+    };
+    // warp 0 of the pair: zero the slot tail past this item's inverse (the
+    // unrolled mat-vec reads up to packed_doubles(kK) with b_k = 0), then
+    // lane 0 issues the bulk copy
+    auto issue = [&](std::int32_t q, std::uint32_t c) {
+        const int st = static_cast<int>(c % kSP);
+        const int l = level_of(q);
+        const std::int32_t s = q - pt.base[l];
+        const std::int64_t o = pt.inv_off[l][s];
+        const int nd = static_cast<int>(pt.inv_off[l][s + 1] - o);
+        double* dst = ring + static_cast<std::size_t>(st) * slot;
+        for (int i = nd + lane; i < slot; i += 32) dst[i] = 0.0;
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&bar[st], static_cast<std::uint32_t>(nd * 8));
+            if (l == 0)
+                bulk_g2s_evict_first(dst, pt.inv[0] + o, static_cast<std::uint32_t>(nd * 8), &bar[st]);
+            else
+                bulk_g2s_evict_last(dst, pt.inv[l] + o, static_cast<std::uint32_t>(nd * 8), &bar[st]);
+        }
+    };
+    if (half == 0)
+        for (int i = 0; i < kSP && i < nloc; ++i) issue(item(i), cnt + i);
+    struct Item {
+        int l;
+        std::int32_t s0, dim;
+    };
+    auto row_index = [&](const Item& it, int j) -> std::int64_t {
+        if (it.l == 0) return 3 * static_cast<std::int64_t>(it.s0) + j;
+        return 3 * static_cast<std::int64_t>(pt.sub_nodes[it.l][it.s0 + j / 3]) + (j % 3);
+    };
+    auto load_b = [&](std::int32_t q, Item& it, double* bb) {
+        it.l = level_of(q);
+        const std::int32_t s = q - pt.base[it.l];
+        it.s0 = pt.sub_ptr[it.l][s];
+        it.dim = 3 * (pt.sub_ptr[it.l][s + 1] - it.s0);
+#pragma unroll
+        for (int t = 0; t < RB; ++t) {
+            const int j = lane + 32 * t;
+            bb[t] = j < it.dim ? ldg_issue(pt.rin[it.l] + row_index(it, j)) : 0.0;
+        }
+    };
+    Item cur{0, 0, 0};
+    double b[RB];
+    if (nloc > 0) load_b(item(0), cur, b);
+    double dsum = 0;
+    for (int i = 0; i < nloc; ++i, ++cnt) {
+        const int st = static_cast<int>(cnt % kSP);
+#pragma unroll
+        for (int t = 0; t < RB; ++t)
+            if (lane + 32 * t < kK) bs[lane + 32 * t] = b[t];
+        Item nxt{0, 0, 0};
+        double bn[RB];
+        if (i + 1 < nloc) load_b(item(i + 1), nxt, bn);
+        __syncwarp();
+        mbar_wait(&bar[st], (cnt / kSP) & 1u);
+        const double* M = ring + static_cast<std::size_t>(st) * slot;
+        double* out = pt.out[cur.l];
+        dsum += pair_solve<kK>(M, bs, lane, half, cur.dim,
+                               [&](int j, double v) { out[row_index(cur, j)] = v; });
+        pair_sync(pair);
+        if (half == 0 && i + kSP < nloc) issue(item(i + kSP), cnt + kSP);
+        cur = nxt;
+#pragma unroll
+        for (int t = 0; t < RB; ++t) b[t] = bn[t];
+    }
+    return dsum;
+}
+
+// ---- F: prolongation + p update (+ clears) ------------------------------------
+__device__ void final_phase(const Persist& P, double beta, bool zero_tmp) {
+    const FinalSo& fa = P.fa;
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * kPT;
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(kPT) + threadIdx.x; i < P.n; i += stride) {
+        const std::int64_t g = 3 * i;
+        std::int32_t nd[kMaxLevels];
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l)
+            if (l < fa.n_coarse) nd[l] = fa.agg[l][i];
+        double z0 = P.z[g], z1 = P.z[g + 1], z2 = P.z[g + 2];
+        const double p0 = P.p[g], p1 = P.p[g + 1], p2 = P.p[g + 2];
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l)
+            if (l < fa.n_coarse) {
+                const double* yl = fa.y[l] + 3 * static_cast<std::int64_t>(nd[l]);
+                z0 += yl[0];
+                z1 += yl[1];
+                z2 += yl[2];
+            }
+        P.p[g] = z0 + beta * p0;
+        P.p[g + 1] = z1 + beta * p1;
+        P.p[g + 2] = z2 + beta * p2;
+        P.ap[g] = 0.0;
+        P.ap[g + 1] = 0.0;
+        P.ap[g + 2] = 0.0;
+        if (zero_tmp) {
+            P.tmp[g] = 0.0;
+            P.tmp[g + 1] = 0.0;
+            P.tmp[g + 2] = 0.0;
+        }
+    }
+    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(kPT) + threadIdx.x;
+    for (int l = 0; l < fa.n_clear; ++l)
+        for (std::int64_t i = tid; i < fa.clear_n[l]; i += stride) fa.clear[l][i] = 0.0;
+}
+
+template <int kK, int kSP, int kSS>
+__global__ void __launch_bounds__(kPT, 2) k_pcg_persistent(Persist P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double red[32];
+    if (P.flags[F_DONE]) return;  // !(rho0 > 0) in the init sequence (pcg.hpp:56)
+    cg::grid_group grid = cg::this_grid();
+    std::uint64_t* sbar = reinterpret_cast<std::uint64_t*>(smem + P.union_bytes);
+    std::uint64_t* pbar = sbar + kPWarps * kSS;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kPWarps * kSS + kPPairs * kSP; ++i) mbar_init(&sbar[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    std::uint32_t sp_cnt = 0, pc_cnt = 0;  // ring positions (per warp / per pair)
+    double* part_a = P.partials;
+    double* part_b = P.partials + gridDim.x;
+    double rho = P.scal[S_RHO0];
+    const double rho0 = P.scal[S_RHO_INIT];
+    const double stop = P.scal[S_STOP];
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool timed = P.phase_ns != nullptr && lead;
+    unsigned long long t_s = 0, t_u = 0, t_p = 0, t_f = 0, t0 = timed ? gtimer() : 0;
+    int k = 1;
+    bool done = false;
+    for (; k <= P.max_iters; ++k) {
+        // S
+        store_partial(spmv_phase<true, kSS>(P, P.p, P.ap, smem, sbar, sp_cnt), part_a, red);
+        phase_sync(grid);
+        const double pap = sum_partials(part_a, red);
+        if (timed) { const unsigned long long t = gtimer(); t_s += t - t0; t0 = t; }
+        if (!(pap > 0)) {  // pcg.hpp:61-66
+            if (lead) {
+                P.flags[F_DONE] = 1;
+                P.flags[F_ITERS] = k - 1;
+                P.scal[S_REL] = sqrt(fabs(rho) / rho0);
+            }
+            done = true;
+            break;
+        }
+        const double alpha = rho / pap;
+        // U
+        if (P.restart > 0 && k % P.restart == 0) {  // pcg.hpp:69-72: x += alpha p; r = b - A x
+            const std::int64_t n3 = 3 * static_cast<std::int64_t>(P.n);
+            for (std::int64_t g = blockIdx.x * static_cast<std::int64_t>(kPT) + threadIdx.x; g < n3;
+                 g += static_cast<std::int64_t>(gridDim.x) * kPT)
+                P.x[g] += alpha * P.p[g];
+            phase_sync(grid);
+            spmv_phase<false, kSS>(P, P.x, P.tmp, smem, sbar, sp_cnt);
+            phase_sync(grid);
+            update_phase<M_RESTART>(P, alpha, P.tmp, reinterpret_cast<double*>(smem));
+        } else {
+            update_phase<M_UPDATE>(P, alpha, P.ap, reinterpret_cast<double*>(smem));
+        }
+        phase_sync(grid);
+        if (timed) { const unsigned long long t = gtimer(); t_u += t - t0; t0 = t; }
+        // P
+        store_partial(precond_phase<kK, kSP>(P, smem, pbar, pc_cnt), part_b, red);
+        phase_sync(grid);
+        const double rz = sum_partials(part_b, red);
+        if (timed) { const unsigned long long t = gtimer(); t_p += t - t0; t0 = t; }
+        if (lead) {
+            P.flags[F_ITERS] = k;
+            P.scal[S_REL] = sqrt(fabs(rz) / rho0);
+        }
+        if (rz <= stop) {  // pcg.hpp:76-82
+            if (lead) {
+                P.flags[F_DONE] = 1;
+                P.flags[F_CONVERGED] = 1;
+            }
+            done = true;
+            break;
+        }
+        const double beta = rz / rho;
+        rho = rz;
+        // F
+        final_phase(P, beta, P.restart > 0 && (k + 1) % P.restart == 0);
+        phase_sync(grid);
+        if (timed) { const unsigned long long t = gtimer(); t_f += t - t0; t0 = t; }
+    }
+    if (lead) {
+        if (!done) P.scal[S_RHO0 + (P.max_iters & 1)] = rho;  // ran out (pcg.hpp:86-87)
+        if (P.phase_ns) {
+            P.phase_ns[0] += t_s;
+            P.phase_ns[1] += t_u;
+            P.phase_ns[2] += t_p;
+            P.phase_ns[3] += t_f;
+        }
+    }
+}
+
 }  // namespace
 
 // The solve-order kernels apply when the levels were built in solve order,
@@ -352,9 +1129,11 @@ void launch_update_so(Ctx& c, const PcgArgs& a) {
     for (int l = 1; l < so.n_levels; ++l) {
         so.rr[l] = c.levels[l]->rr.p;
         so.up_node[l] = c.levels[l]->up_node.p;
+        if (l >= 2) so.anc[l] = c.levels[l]->anc.p;
     }
+    so.max_fill0 = L0.max_fill;
     const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(L0.n_parts, kUpdSubs)));
-    const std::size_t smem = sizeof(double) * 3 * static_cast<std::size_t>(kUpdSubs) * L0.max_fill;
+    const std::size_t smem = update_tile_smem(L0.max_fill);
     static bool attr = false;
     if (!attr) {
         ADIPC_CUDA(cudaFuncSetAttribute(k_update_so<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
@@ -371,6 +1150,7 @@ void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, dou
                        double* dot) {
     PrecondTable pt{};
     pt.n = static_cast<int>(c.levels.size());
+    if (const char* e = std::getenv("ADIPC_DEBUG_PC_LEVELS")) pt.n = std::min(pt.n, std::max(1, std::atoi(e)));  // timing experiments only
     int fill = 1;
     for (int l = 0; l < pt.n; ++l) {
         const DeviceLevel& L = *c.levels[l];
@@ -405,7 +1185,52 @@ void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, dou
         k_precond_so<K, S><<<std::max(grid, 1), 64 * pairs, smem, c.stream>>>(pt, partials, ticket, dot, flags, \
                                                                              slot);                           \
     } while (0)
-    if (kk == 24) {
+    if (c.pc_variant == 2 && kk <= 48) {  // two items per warp (half-warps), one warp per CTA
+        constexpr int wpc = 1;
+        const std::size_t per_warp = (sizeof(double) * 2 * slot + sizeof(std::uint64_t)) * stages +
+                                     sizeof(double) * 2 * (kk + 2);
+        const std::size_t sm2 = per_warp * wpc;
+#define ADIPC_PC2(K, S)                                                                                       \
+    do {                                                                                                      \
+        ADIPC_CUDA(cudaFuncSetAttribute(k_precond_so2<K, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                        static_cast<int>(sm2)));                                              \
+        int occ = 0;                                                                                          \
+        ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_precond_so2<K, S>, 32 * wpc, sm2));  \
+        if (occ < 1) throw StatusError(kInvalidArgument, "preconditioner ring does not fit in shared memory"); \
+        const int grid = static_cast<int>(std::min<std::int64_t>(static_cast<std::int64_t>(sms) * occ,          \
+                                                                 ceil_div(pt.base[pt.n], 2 * wpc)));          \
+        k_precond_so2<K, S><<<std::max(grid, 1), 32 * wpc, sm2, c.stream>>>(pt, partials, ticket, dot, flags,   \
+                                                                            slot);                            \
+    } while (0)
+        if (kk == 24) {
+            if (stages == 2) ADIPC_PC2(24, 2); else ADIPC_PC2(24, 3);
+        } else {
+            if (stages == 2) ADIPC_PC2(48, 2); else ADIPC_PC2(48, 3);
+        }
+#undef ADIPC_PC2
+    } else if (c.pc_variant == 1 && kk <= 48) {  // one warp per item, 4 warps per CTA
+        const std::size_t per_warp = (sizeof(double) * slot + sizeof(std::uint64_t)) * stages + sizeof(double) * kk;
+        const int wpc = 4;
+        const std::size_t sm1 = per_warp * wpc;
+#define ADIPC_PC1(K, S)                                                                                       \
+    do {                                                                                                      \
+        ADIPC_CUDA(cudaFuncSetAttribute(k_precond_so1<K, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                        static_cast<int>(sm1)));                                              \
+        int occ = 0;                                                                                          \
+        ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_precond_so1<K, S>, 32 * wpc, sm1));  \
+        if (occ < 1) throw StatusError(kInvalidArgument, "preconditioner ring does not fit in shared memory"); \
+        const int grid = static_cast<int>(std::min<std::int64_t>(static_cast<std::int64_t>(sms) * occ,          \
+                                                                 ceil_div(pt.base[pt.n], wpc)));              \
+        k_precond_so1<K, S><<<std::max(grid, 1), 32 * wpc, sm1, c.stream>>>(pt, partials, ticket, dot, flags,   \
+                                                                            slot);                            \
+    } while (0)
+        if (kk == 24) {
+            if (stages == 2) ADIPC_PC1(24, 2); else ADIPC_PC1(24, 3);
+        } else {
+            if (stages == 2) ADIPC_PC1(48, 2); else ADIPC_PC1(48, 3);
+        }
+#undef ADIPC_PC1
+    } else if (kk == 24) {
         if (stages == 2) ADIPC_PC(24, 2); else ADIPC_PC(24, 3);
     } else if (kk == 48) {
         if (stages == 2) ADIPC_PC(48, 2); else ADIPC_PC(48, 3);
@@ -447,6 +1272,113 @@ template void launch_final_so<F_PCG_STEP>(Ctx&, double*, double*, double*, const
 void clear_restrict_so(Ctx& c) {
     for (std::size_t l = 2; l < c.levels.size(); ++l)
         ADIPC_CUDA(cudaMemsetAsync(c.levels[l]->rr.p, 0, sizeof(double) * 3 * c.levels[l]->n_nodes, c.stream));
+}
+
+}  // namespace adipc_gpu
+
+namespace adipc_gpu {
+
+// The PCG iterations (after the init sequence of pcg.cu) as one persistent
+// cooperative launch. Returns false when the configuration is not covered
+// (the caller then runs the per-kernel CUDA-graph iterations).
+bool pcg_persistent(Ctx& c, const PcgArgs& a, double* partials, int restart, int max_iters) {
+    if (!c.persistent || !so_supported(c) || c.levels.size() > kMaxLevels) return false;
+    const DeviceMatrix& M = c.S();
+    Persist P{};
+    P.rows = M.rows.p;
+    P.cols = M.cols.p;
+    P.blocks = M.blocks.p;
+    P.U = M.U;
+    P.n = M.n;
+    P.x = a.x;
+    P.r = a.r;
+    P.p = const_cast<double*>(a.p);
+    P.ap = const_cast<double*>(a.ap);
+    P.z = c.w.z.p;
+    P.tmp = c.w.tmp.p;
+    P.b = a.b;
+    // restriction
+    const DeviceLevel& L0 = *c.levels[0];
+    SoRestrict& so = P.so;
+    so.n_levels = static_cast<int>(c.levels.size());
+    so.n0_parts = L0.n_parts;
+    so.sub_ptr0 = L0.sub_ptr.p;
+    so.up_first0 = L0.up_first.p;
+    so.upc_ptr0 = L0.upc_ptr.p;
+    so.upc_node0 = L0.upc_node.p;
+    for (int l = 1; l < so.n_levels; ++l) {
+        so.rr[l] = c.levels[l]->rr.p;
+        so.up_node[l] = c.levels[l]->up_node.p;
+        if (l >= 2) so.anc[l] = c.levels[l]->anc.p;
+    }
+    so.max_fill0 = L0.max_fill;
+    // preconditioner table
+    PrecondTable& pt = P.pt;
+    pt.n = so.n_levels;
+    int fill = 1;
+    for (int l = 0; l < pt.n; ++l) {
+        const DeviceLevel& L = *c.levels[l];
+        pt.base[l + 1] = pt.base[l] + L.n_parts;
+        pt.sub_ptr[l] = L.sub_ptr.p;
+        pt.sub_nodes[l] = l == 0 ? nullptr : L.sub_nodes.p;
+        pt.inv_off[l] = L.inv_off.p;
+        pt.inv[l] = L.inv.p;
+        pt.rin[l] = l == 0 ? a.r : L.rr.p;
+        pt.out[l] = l == 0 ? c.w.z.p : L.y.p;
+        fill = std::max(fill, L.max_fill);
+    }
+    // prolongation
+    FinalSo& fa = P.fa;
+    fa.n_coarse = pt.n - 1;
+    for (int l = 1; l < pt.n; ++l) {
+        fa.agg[l - 1] = c.levels[l]->agg.p;
+        fa.y[l - 1] = c.levels[l]->y.p;
+    }
+    for (int l = 2; l < pt.n; ++l) {
+        fa.clear[fa.n_clear] = c.levels[l]->rr.p;
+        fa.clear_n[fa.n_clear] = 3 * static_cast<std::int64_t>(c.levels[l]->n_nodes);
+        ++fa.n_clear;
+    }
+    P.partials = partials;
+    P.scal = a.scal;
+    P.flags = a.flags;
+    P.restart = restart;
+    P.max_iters = max_iters;
+    if (c.profile) {
+        c.phase_ns.reserve(4);
+        ADIPC_CUDA(cudaMemsetAsync(c.phase_ns.p, 0, 4 * sizeof(unsigned long long), c.stream));
+        P.phase_ns = c.phase_ns.p;
+    }
+    const int kk = matvec_cols(fill);
+    if (kk == 0) return false;
+    P.slot_doubles = static_cast<int>(packed_doubles(kk));
+    constexpr int kSP = 2, kSS = 4;
+    std::size_t ub = std::max<std::size_t>(sizeof(SpmvStage) * kPWarps * kSS,
+                                           sizeof(double) * (static_cast<std::size_t>(kPPairs) * kSP * P.slot_doubles +
+                                                             static_cast<std::size_t>(kPWarps) * kk));
+    ub = std::max<std::size_t>(ub, update_tile_smem(L0.max_fill));
+    ub = (ub + 127) & ~static_cast<std::size_t>(127);
+    P.union_bytes = static_cast<int>(ub);
+    const std::size_t smem = ub + sizeof(std::uint64_t) * (kPWarps * kSS + kPPairs * kSP);
+    ADIPC_CUDA(cudaMemsetAsync(c.w.tmp.p, 0, sizeof(double) * 3 * static_cast<std::size_t>(M.n), c.stream));
+    int sms = kSMs;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    void* args[] = {&P};
+    void* fn = nullptr;
+    if (kk == 24)
+        fn = reinterpret_cast<void*>(k_pcg_persistent<24, kSP, kSS>);
+    else if (kk == 48)
+        fn = reinterpret_cast<void*>(k_pcg_persistent<48, kSP, kSS>);
+    else
+        fn = reinterpret_cast<void*>(k_pcg_persistent<96, kSP, kSS>);
+    ADIPC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int occ = 0;
+    ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kPT, smem));
+    if (occ < 1) return false;
+    const int grid = sms * std::min(occ, 2);
+    ADIPC_CUDA(cudaLaunchCooperativeKernel(fn, grid, kPT, args, smem, c.stream));
+    ADIPC_LAUNCH_CHECK();
+    return true;
 }
 
 }  // namespace adipc_gpu

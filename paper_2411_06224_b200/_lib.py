@@ -31,6 +31,8 @@ OPT_SO_KERNELS = 6
 OPT_L0_STAGES = 7
 OPT_PERSISTENT = 8
 OPT_PC_VARIANT = 9
+OPT_FUSED = 10
+OPT_PC_PAIRS = 11
 
 # Every symbol include/adipc_gpu.h declares, with its ctypes signature.
 GPU_SIGNATURES = {

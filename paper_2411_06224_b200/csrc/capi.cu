@@ -1,6 +1,7 @@
 // extern "C" entry points of include/adipc_gpu.h. Each wraps the C++
 // implementation in a try/catch that maps exceptions to status codes and
 // records the message on the context.
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -73,6 +74,18 @@ int adipc_gpu_create(int device, adipc_gpu_ctx** out) {
         ADIPC_CUDA(cudaSetDevice(device));
         ADIPC_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
         ctx->c.own_stream = true;
+        // tuning overrides of the streaming kernels' tile shapes (experiments)
+        auto env_int = [](const char* name, int lo, int hi, int& v) {
+            if (const char* e = std::getenv(name)) {
+                const int x = std::atoi(e);
+                if (x >= lo && x <= hi) v = x;
+            }
+        };
+        env_int("ADIPC_UPD_SUBS", 4, 128, ctx->c.upd_subs);
+        env_int("ADIPC_FINAL_PER", 1, 4, ctx->c.final_per);
+        if (ctx->c.final_per == 3) ctx->c.final_per = 2;
+        env_int("ADIPC_FINAL_BLOCK", 64, 512, ctx->c.final_block);
+        env_int("ADIPC_PC_PAIRS", 1, 5, ctx->c.pc_pairs);
     });
     if (rc != ADIPC_OK) {
         g_global_err = ctx->c.err;
@@ -130,6 +143,8 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.jinv.free();
     c.build_status.free();
     c.perm.free();
+    for (auto& e : c.splits) e.buf.free();
+    c.splits.clear();
     c.phase_ns.free();
     c.perm_keys.free();
     c.perm_vals.free();
@@ -142,6 +157,7 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     for (auto* b : {&c.w.x, &c.w.r, &c.w.p, &c.w.ap, &c.w.z, &c.w.b, &c.w.tmp, &c.w.partials, &c.w.scal}) b->free();
     c.w.tickets.free();
     c.w.flags.free();
+    c.w.counters.free();
     for (auto e : c.prof_events) cudaEventDestroy(e);
     if (c.side) cudaStreamDestroy(c.side);
     if (c.h_flags) cudaFreeHost(c.h_flags);
@@ -188,6 +204,11 @@ int adipc_gpu_set_option(adipc_gpu_ctx* ctx, int option, int value) {
         } else if (option == ADIPC_OPT_SPMV_VARIANT) {
             if (value != 0 && (value < 2 || value > 6)) throw StatusError(kInvalidArgument, "SpMV variant not in {0,2..6}");
             ctx->c.spmv_variant = value;
+        } else if (option == ADIPC_OPT_PC_PAIRS) {
+            if (value < 1 || value > 5) throw StatusError(kInvalidArgument, "pairs per CTA not in 1..5");
+            ctx->c.pc_pairs = value;
+        } else if (option == ADIPC_OPT_FUSED) {
+            ctx->c.fused = value != 0;
         } else if (option == ADIPC_OPT_PC_VARIANT) {
             ctx->c.pc_variant = value;
         } else if (option == ADIPC_OPT_PERSISTENT) {

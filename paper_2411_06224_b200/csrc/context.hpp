@@ -74,6 +74,7 @@ struct PcgWork {
     DBuf<unsigned> tickets;      // last-block-done counters
     DBuf<double> scal;           // device scalars (see pcg.cu)
     DBuf<int> flags;             // device flags (see pcg.cu)
+    DBuf<unsigned> counters;     // in-kernel arrival counters of the fused iteration
 };
 
 struct Ctx {
@@ -123,6 +124,14 @@ struct Ctx {
     bool solve_order = true;       // ADIPC_OPT_SOLVE_ORDER
     bool perm_active = false;      // the current preconditioner / solve matrix use `perm`
     bool levels_permuted = false;  // the device levels were built in solve order
+    std::uint64_t levels_version = 0;  // bumped whenever the device levels are rebuilt
+    // byte-balanced work splits of the preconditioner kernels (solve_order.cu)
+    struct Split {
+        int np = 0;
+        std::uint64_t version = ~0ull;
+        DBuf<std::int32_t> buf;
+    };
+    std::vector<Split> splits;
     DBuf<std::int32_t> perm;       // reference slot -> solve slot
     DeviceMatrix As;               // A in solve order (upper triangle re-canonicalised)
     DBuf<std::uint64_t> perm_keys; // scratch stream for building As
@@ -149,8 +158,16 @@ struct Ctx {
     // level-0 solve; ADIPC_OPT_SO_KERNELS selects the solve-order iteration
     // kernels (solve_order.cu) when the levels allow them
     int l0_stages = 2;
-    int pc_variant = 0;  // preconditioner kernel: 0 warp pairs per item, 1 one warp per item (ADIPC_OPT_PC_VARIANT)
+    int pc_variant = 0;
+    int pc_pairs = 4;
+    // tile shapes of the streaming kernels (ADIPC_UPD_SUBS / ADIPC_FINAL_PER /
+    // ADIPC_FINAL_BLOCK environment overrides, read at context creation)
+    int upd_subs = 64, final_per = 1, final_block = 256;        // warp pairs per CTA of k_precond_so (ADIPC_OPT_PC_PAIRS)
+    bool pc_split = false;   // cost-weighted instead of equal-count work split  // preconditioner kernel: 0 warp pairs per item, 1 one warp per item (ADIPC_OPT_PC_VARIANT)
     bool so_kernels = true;
+    // update + every MAS level + prolongation in one cooperative kernel per
+    // iteration (ADIPC_OPT_FUSED; solve_order.cu k_iter_so)
+    bool fused = true;
     // the PCG iterations as one persistent cooperative kernel (ADIPC_OPT_PERSISTENT)
     bool persistent = false;
     DBuf<unsigned long long> phase_ns;  // its per-phase times (ADIPC_OPT_PROFILE)

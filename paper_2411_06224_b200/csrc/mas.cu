@@ -355,6 +355,7 @@ void set_levels(Ctx& c, const host::MasHierarchy& h) {
     }
     link_levels(c, hl);
     c.levels_permuted = perm;
+    ++c.levels_version;
 }
 
 }  // namespace

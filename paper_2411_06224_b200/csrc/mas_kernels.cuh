@@ -39,7 +39,9 @@ enum Scal : int {
 // F_K: index (1-based) of the current iteration; advanced by the last CTA of
 // the iteration's first kernel (the p.Ap SpMV), so an iteration's launch
 // sequence is identical every time (captured once as a CUDA graph).
-enum Flag : int { F_DONE = 0, F_ITERS = 1, F_CONVERGED = 2, F_K = 3, F_KTICKET = 4, F_COUNT = 8 };
+// F_ERR: an in-kernel dependency wait timed out (never expected; reported
+// as a CUDA-class error instead of hanging the device)
+enum Flag : int { F_DONE = 0, F_ITERS = 1, F_CONVERGED = 2, F_K = 3, F_KTICKET = 4, F_ERR = 5, F_COUNT = 8 };
 // last-block tickets / partial arrays: 0 spmv, 1 b.b, 2 + l level l
 enum Ticket : int { T_SPMV = 0, T_BB = 1, T_LEVEL = 2, T_COUNT = T_LEVEL + kMaxLevels };
 

@@ -48,6 +48,9 @@ template <int kFinal>
 void launch_final_so(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a);
 void clear_restrict_so(Ctx& c);
 bool pcg_persistent(Ctx& c, const PcgArgs& a, double* partials, int restart, int max_iters);
+bool iter_so_supported(const Ctx& c);
+void prepare_work_splits(Ctx& c);
+void launch_iter_so(Ctx& c, const PcgArgs& a, bool restart, unsigned* counters, double* partials);
 
 namespace {
 
@@ -106,6 +109,8 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     // solve-order iteration kernels (solve_order.cu)
     const bool so = c.so_kernels && so_supported(c);
     if (so) pmax = std::max(pmax, so_partials(c));
+    const bool fused = so && iter_so_supported(c);  // one kernel after the SpMV per iteration
+    if (so) prepare_work_splits(c);  // byte-balanced splits, before any graph capture
     w.partials.reserve(static_cast<std::size_t>(pmax) * T_COUNT);
     w.tickets.reserve(T_COUNT);
     w.scal.reserve(S_COUNT);
@@ -183,6 +188,10 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     }
     launch_final<F_PCG_INIT>(c, w.z.p, w.p.p, w.ap.p, a);
     if (so) clear_restrict_so(c);
+    if (fused) {
+        w.counters.reserve(2);
+        ADIPC_CUDA(cudaMemsetAsync(w.counters.p, 0, 2 * sizeof(unsigned), st));
+    }
 
     // optional per-kernel-class timing (ADIPC_OPT_PROFILE): events bracket the
     // SpMV, update, preconditioner and prolongation/p-update launches of every
@@ -213,7 +222,9 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
             spmv_launch(c, c.S(), d_x, w.tmp.p, false, w.flags.p, nullptr, nullptr, nullptr);
             PcgArgs ar = a;
             ar.ap = w.tmp.p;
-            if (so)
+            if (fused)
+                launch_iter_so(c, ar, true, w.counters.p, partials_of(T_LEVEL + 1));
+            else if (so)
                 launch_update_so<M_RESTART>(c, ar);
             else if (mas)
                 launch_level<M_RESTART, false>(c, 0, nullptr, nullptr, ar, nullptr, nullptr, nullptr, st, true);
@@ -221,7 +232,9 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
                 launch_jacobi<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
                                          w.scal.p + S_RZ);
         } else {
-            if (so)
+            if (fused)
+                launch_iter_so(c, a, false, w.counters.p, partials_of(T_LEVEL + 1));
+            else if (so)
                 launch_update_so<M_UPDATE>(c, a);
             else if (mas)
                 launch_level<M_UPDATE, false>(c, 0, nullptr, nullptr, a, nullptr, nullptr, nullptr, st, true);
@@ -230,13 +243,17 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
                                         w.scal.p + S_RZ);
         }
         mark(slot, 2);
-        if (so)
+        if (fused)
+            ;  // the fused kernel did the preconditioner and the prolongation
+        else if (so)
             launch_precond_so(c, w.r.p, w.z.p, w.flags.p, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
                               w.scal.p + S_RZ);
         else if (mas)
             mas_apply(a);
         mark(slot, 3);
-        if (so)
+        if (fused)
+            ;
+        else if (so)
             launch_final_so<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
         else
             launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
@@ -324,6 +341,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     ADIPC_CUDA(cudaEventElapsedTime(&c.ms_pcg, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (h_final[F_ERR]) throw StatusError(kCudaError, "fused PCG iteration: in-kernel dependency wait timed out");
     if (h_final[F_DONE]) {
         out.iters = h_final[F_ITERS];
         out.converged = h_final[F_CONVERGED];

@@ -19,6 +19,7 @@
 // r.z comes from the per-level partial dots b_l.y_l of step 3 (the same
 // quantity: r.z = sum_l (P_l r).(D_l^-1 P_l r)).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -44,6 +45,7 @@ struct SoRestrict {
     const std::int32_t* up_node[kMaxLevels];  // level-l node -> level-(l+1) node, l >= 1
     const std::int32_t* anc[kMaxLevels];      // level-1 node -> its level-l node, l >= 2
     int max_fill0;                            // largest level-0 subdomain (tile smem sizing)
+    int subs;                                 // level-0 subdomains per tile
 };
 
 // One tile of kUpdSubs level-0 subdomains of the update pass (solve order):
@@ -58,13 +60,13 @@ struct SoRestrict {
 template <int kMode, int kThreads>
 __device__ __forceinline__ void update_tile(const SoRestrict& so, const PcgArgs& a, double alpha,
                                             const double* __restrict__ apv, std::int32_t tile, double* smem) {
-    const std::int32_t s0 = tile * kUpdSubs;
-    const std::int32_t s1 = min(s0 + kUpdSubs, so.n0_parts);
+    const std::int32_t s0 = tile * so.subs;
+    const std::int32_t s1 = min(s0 + so.subs, so.n0_parts);
     const std::int32_t slot0 = so.sub_ptr0[s0], slot1 = so.sub_ptr0[s1];
     const std::int32_t v0 = so.up_first0[s0], v1 = so.up_first0[s1];
     const std::int64_t g0 = 3 * static_cast<std::int64_t>(slot0);
     const std::int64_t g1 = 3 * static_cast<std::int64_t>(slot1);
-    const int cap = kUpdSubs * so.max_fill0;
+    const int cap = so.subs * so.max_fill0;
     double* sr = smem;
     int* uptr = reinterpret_cast<int*>(smem + 3 * cap);
     int* child = uptr + cap + 1;
@@ -121,8 +123,8 @@ __device__ __forceinline__ void update_tile(const SoRestrict& so, const PcgArgs&
     __syncthreads();
 }
 
-inline std::size_t update_tile_smem(int max_fill0) {
-    const std::size_t cap = static_cast<std::size_t>(kUpdSubs) * max_fill0;
+inline std::size_t update_tile_smem(int max_fill0, int subs) {
+    const std::size_t cap = static_cast<std::size_t>(subs) * max_fill0;
     return sizeof(double) * 3 * cap + sizeof(int) * (2 * cap + 1);
 }
 
@@ -159,10 +161,15 @@ struct PrecondTable {
     const double* inv[kMaxLevels];
     const double* rin[kMaxLevels];           // level 0: r; coarse: restricted residual
     double* out[kMaxLevels];                 // level 0: z; coarse: y
+    int dbg_nomath;                          // timing experiments only
+    // byte-balanced work split: split[l * (np + 1) + p] = first subdomain of
+    // level l for work unit p (np units), cut at equal packed-inverse bytes
+    const std::int32_t* split;
+    int np;
 };
 
 template <int kK, int kStages>
-__global__ void __launch_bounds__(256) k_precond_so(PrecondTable pt, double* __restrict__ partials,
+__global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __restrict__ partials,
                                                    unsigned* __restrict__ ticket, double* __restrict__ dot_out,
                                                    const int* __restrict__ flags, int slot_doubles) {
     constexpr int RB = (kK + 31) / 32;  // b entries per lane
@@ -189,9 +196,17 @@ __global__ void __launch_bounds__(256) k_precond_so(PrecondTable pt, double* __r
     for (int l = 0; l < kMaxLevels; ++l) {
         lv_lo[l] = lv_n[l] = 0;
         if (l < pt.n) {
-            const std::int64_t nl = pt.base[l + 1] - pt.base[l];
-            lv_lo[l] = pt.base[l] + static_cast<std::int32_t>(gp * nl / np);
-            lv_n[l] = static_cast<std::int32_t>((gp + 1) * nl / np - gp * nl / np);
+            std::int32_t a, b;
+            if (pt.split && pt.np == np) {
+                a = pt.split[l * (np + 1) + gp];
+                b = pt.split[l * (np + 1) + gp + 1];
+            } else {
+                const std::int64_t nl = pt.base[l + 1] - pt.base[l];
+                a = static_cast<std::int32_t>(gp * nl / np);
+                b = static_cast<std::int32_t>((gp + 1) * nl / np);
+            }
+            lv_lo[l] = pt.base[l] + a;
+            lv_n[l] = b - a;
             nloc += lv_n[l];
         }
     }
@@ -266,8 +281,11 @@ __global__ void __launch_bounds__(256) k_precond_so(PrecondTable pt, double* __r
         mbar_wait(&bar[st], par);
         const double* M = ring + static_cast<std::size_t>(st) * slot_doubles;
         double* out = pt.out[cur.l];
-        dsum += pair_solve<kK>(M, bs, lane, half, cur.dim,
-                               [&](int j, double v) { out[row_index(cur, j)] = v; });
+        if (pt.dbg_nomath)  // timing experiments: stream the inverses, skip the mat-vec
+            dsum += M[lane] * bs[lane];
+        else
+            dsum += pair_solve<kK>(M, bs, lane, half, cur.dim,
+                                   [&](int j, double v) { out[row_index(cur, j)] = v; });
         pair_sync(pair);  // both warps are done with the slot and with bs
         if (half == 0 && lane == 0 && i + kStages < nloc) {  // refill kStages items ahead
             fence_proxy_async();
@@ -294,8 +312,8 @@ struct FinalSo {
     int n_clear;
 };
 
-template <int kFinal>
-__global__ void __launch_bounds__(256) k_final_so(std::int32_t n, FinalSo fa, const double* __restrict__ z,
+template <int kFinal, int kPer>
+__global__ void __launch_bounds__(512) k_final_so(std::int32_t n, FinalSo fa, const double* __restrict__ z,
                                                  double* __restrict__ p, double* __restrict__ ap, PcgArgs a) {
     double beta = 0;
     if (a.flags[F_DONE]) return;
@@ -329,41 +347,47 @@ __global__ void __launch_bounds__(256) k_final_so(std::int32_t n, FinalSo fa, co
         if (rz <= stop) return;
         beta = rz / rho;
     }
+    // kPer slots per thread (strided by the grid), every load issued up front
+    const std::int64_t nthreads = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-    if (tid < n) {
-        const std::int64_t g = 3 * tid;
-        std::int32_t nd[kMaxLevels];
+    std::int32_t nd[kPer][kMaxLevels];
+    double zz[kPer][3], pp[kPer][3];
 #pragma unroll
-        for (int l = 0; l < kMaxLevels; ++l)
-            if (l < fa.n_coarse) nd[l] = fa.agg[l][tid];
-        double zz0 = z[g], zz1 = z[g + 1], zz2 = z[g + 2];
-        double p0 = 0, p1 = 0, p2 = 0;
-        if (kFinal != F_PCG_INIT) {
-            p0 = p[g];
-            p1 = p[g + 1];
-            p2 = p[g + 2];
-        }
+    for (int u = 0; u < kPer; ++u) {
+        const std::int64_t sl = tid + u * nthreads;
+        if (sl < n) {
 #pragma unroll
-        for (int l = 0; l < kMaxLevels; ++l)
-            if (l < fa.n_coarse) {
-                const double* yl = fa.y[l] + 3 * static_cast<std::int64_t>(nd[l]);
-                zz0 += yl[0];
-                zz1 += yl[1];
-                zz2 += yl[2];
+            for (int l = 0; l < kMaxLevels; ++l)
+                if (l < fa.n_coarse) nd[u][l] = fa.agg[l][sl];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                zz[u][q] = z[3 * sl + q];
+                pp[u][q] = kFinal != F_PCG_INIT ? p[3 * sl + q] : 0.0;
             }
-        p[g] = zz0 + beta * p0;
-        p[g + 1] = zz1 + beta * p1;
-        p[g + 2] = zz2 + beta * p2;
-        ap[g] = 0.0;
-        ap[g + 1] = 0.0;
-        ap[g + 2] = 0.0;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const std::int64_t sl = tid + u * nthreads;
+        if (sl < n) {
+#pragma unroll
+            for (int l = 0; l < kMaxLevels; ++l)
+                if (l < fa.n_coarse) {
+                    const double* yl = fa.y[l] + 3 * static_cast<std::int64_t>(nd[u][l]);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) zz[u][q] += yl[q];
+                }
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                p[3 * sl + q] = zz[u][q] + beta * pp[u][q];
+                ap[3 * sl + q] = 0.0;
+            }
+        }
     }
     // clear the RED targets of the next update pass
     for (int l = 0; l < fa.n_clear; ++l)
-        for (std::int64_t i = tid; i < fa.clear_n[l]; i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
-            fa.clear[l][i] = 0.0;
+        for (std::int64_t i = tid; i < fa.clear_n[l]; i += nthreads) fa.clear[l][i] = 0.0;
 }
-
 
 // Variant of k_precond_so with ONE warp per item (rows 0..31 on the lanes,
 // rows 32..47 on lanes 0..15 of a second register slot): every column is
@@ -393,9 +417,17 @@ __global__ void __launch_bounds__(128) k_precond_so1(PrecondTable pt, double* __
     for (int l = 0; l < kMaxLevels; ++l) {
         lv_lo[l] = lv_n[l] = 0;
         if (l < pt.n) {
-            const std::int64_t nl = pt.base[l + 1] - pt.base[l];
-            lv_lo[l] = pt.base[l] + static_cast<std::int32_t>(gp * nl / np);
-            lv_n[l] = static_cast<std::int32_t>((gp + 1) * nl / np - gp * nl / np);
+            std::int32_t a, b;
+            if (pt.split && pt.np == np) {
+                a = pt.split[l * (np + 1) + gp];
+                b = pt.split[l * (np + 1) + gp + 1];
+            } else {
+                const std::int64_t nl = pt.base[l + 1] - pt.base[l];
+                a = static_cast<std::int32_t>(gp * nl / np);
+                b = static_cast<std::int32_t>((gp + 1) * nl / np);
+            }
+            lv_lo[l] = pt.base[l] + a;
+            lv_n[l] = b - a;
             nloc += lv_n[l];
         }
     }
@@ -540,9 +572,17 @@ __global__ void __launch_bounds__(128) k_precond_so2(PrecondTable pt, double* __
     for (int l = 0; l < kMaxLevels; ++l) {
         lv_lo[l] = lv_n[l] = 0;
         if (l < pt.n) {
-            const std::int64_t nl = pt.base[l + 1] - pt.base[l];
-            lv_lo[l] = pt.base[l] + static_cast<std::int32_t>(gp * nl / np);
-            lv_n[l] = static_cast<std::int32_t>((gp + 1) * nl / np - gp * nl / np);
+            std::int32_t a, b;
+            if (pt.split && pt.np == np) {
+                a = pt.split[l * (np + 1) + gp];
+                b = pt.split[l * (np + 1) + gp + 1];
+            } else {
+                const std::int64_t nl = pt.base[l + 1] - pt.base[l];
+                a = static_cast<std::int32_t>(gp * nl / np);
+                b = static_cast<std::int32_t>((gp + 1) * nl / np);
+            }
+            lv_lo[l] = pt.base[l] + a;
+            lv_n[l] = b - a;
             nloc += lv_n[l];
         }
     }
@@ -674,6 +714,363 @@ __global__ void __launch_bounds__(128) k_precond_so2(PrecondTable pt, double* __
         for (int t = 0; t < T; ++t) b[t] = bn[t];
     }
     grid_sum_last_block(dsum, partials, ticket, dot_out);
+}
+
+// ============================================================================
+// One PCG iteration after the SpMV as ONE cooperative kernel (k_iter_so):
+//   items   level-0 subdomains first: warp 0 of the pair applies the vector
+//           update to the subdomain's slots (x += alpha p, r -= alpha Ap, or
+//           r = b - A x on restart iterations, pcg.hpp:67-74) and hands the
+//           new residual to both warps through shared memory as b; warp 1
+//           restricts it to the subdomain's level-1 nodes (and REDs the sums
+//           to their coarser ancestors); both solve the packed inverse.
+//           Then the coarse items, once every pair has finished its level-0
+//           items (a global arrival counter: the coarse restricted residuals
+//           are complete).
+//   final   once every CTA has published its share of r.z (second counter),
+//           every CTA sums the shares in the same order, applies the stop test
+//           and beta, and prolongs + updates p for its slice of the slots.
+// Two kernels per iteration (SpMV, this) instead of four; r is read once.
+// The counters are monotone (target = iteration index x participants, the
+// iteration index advanced by the SpMV), so nothing needs re-arming.
+struct IterArgs {
+    PrecondTable pt;
+    FinalSo fa;
+    // update (solve order)
+    double* x;
+    double* r;
+    const double* p;
+    const double* ap;   // A p, or A x_new on restart iterations
+    const double* b;
+    double* z;
+    double* pout;       // p (updated in place by the final phase)
+    double* apclear;    // A p buffer, cleared for the next SpMV
+    double* tmpclear;   // A x buffer of the next restart iteration (or null)
+    // restriction metadata (level 0 -> 1 and ancestors)
+    const std::int32_t* up_first0;
+    const std::int32_t* upc_ptr0;
+    const std::int32_t* upc_node0;
+    double* rr1;
+    double* rr[kMaxLevels];
+    const std::int32_t* anc[kMaxLevels];
+    int n_levels;
+    std::int32_t n_slots;
+    double* scal;
+    int* flags;
+    unsigned* counters;  // [0] level-0 pairs done, [1] CTAs done
+    double* partials;    // per-CTA r.z shares
+    int restart_mode;    // 1: r = b - A x (restart iteration)
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void spin_until(const unsigned* p, unsigned target, int* err) {
+    long long n = 0;
+    while (static_cast<int>(ld_acquire(p) - target) < 0) {
+        __nanosleep(64);
+        if (++n > (1ll << 26)) {  // ~seconds: never expected; fail loudly instead of hanging
+            atomicExch(err, 1);
+            break;
+        }
+    }
+}
+
+template <int kK, int kStages>
+__global__ void __launch_bounds__(256) k_iter_so(IterArgs ia, int slot_doubles) {
+    constexpr int RB = (kK + 31) / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double red[32];
+    int* flags = ia.flags;
+    if (flags[F_DONE]) return;
+    const int k_it = flags[F_K];
+    double alpha = 0;
+    {
+        PcgArgs pa{};
+        pa.scal = ia.scal;
+        pa.flags = flags;
+        if (!pcg_alpha(pa, alpha)) return;  // every CTA sees the same p.Ap
+    }
+    const PrecondTable& pt = ia.pt;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, pair = w >> 1, half = w & 1;
+    const int npc = blockDim.x >> 6;
+    double* ring = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(pair) * kStages * slot_doubles;
+    double* bs = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(npc) * kStages * slot_doubles +
+                 static_cast<std::size_t>(pair) * kK;  // one b per pair (written by warp 0)
+    int* meta = reinterpret_cast<int*>(reinterpret_cast<double*>(smem) +
+                                       static_cast<std::size_t>(npc) * kStages * slot_doubles +
+                                       static_cast<std::size_t>(npc) * kK) +
+                pair * 80;  // [0..32] level-1 CSR offsets, [40..71] children
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(reinterpret_cast<double*>(smem) +
+                                                          static_cast<std::size_t>(npc) * kStages * slot_doubles +
+                                                          static_cast<std::size_t>(npc) * kK + npc * 40) +
+                         pair * kStages;
+    const std::int64_t gp = static_cast<std::int64_t>(blockIdx.x) * npc + pair;
+    const std::int64_t np = static_cast<std::int64_t>(gridDim.x) * npc;
+    std::int32_t lv_lo[kMaxLevels], lv_n[kMaxLevels];
+    int nloc = 0;
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l) {
+        lv_lo[l] = lv_n[l] = 0;
+        if (l < pt.n) {
+            std::int32_t a, b;
+            if (pt.split && pt.np == np) {
+                a = pt.split[l * (np + 1) + gp];
+                b = pt.split[l * (np + 1) + gp + 1];
+            } else {
+                const std::int64_t nl = pt.base[l + 1] - pt.base[l];
+                a = static_cast<std::int32_t>(gp * nl / np);
+                b = static_cast<std::int32_t>((gp + 1) * nl / np);
+            }
+            lv_lo[l] = pt.base[l] + a;
+            lv_n[l] = b - a;
+            nloc += lv_n[l];
+        }
+    }
+    const int n0 = lv_n[0];  // this pair's level-0 items come first
+    auto item = [&](int i) -> std::int32_t {
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l) {
+            if (i < lv_n[l]) return lv_lo[l] + i;
+            i -= lv_n[l];
+        }
+        return 0;
+    };
+    auto level_of = [&](std::int32_t q) {
+        int l = 0;
+        while (l + 1 < pt.n && q >= pt.base[l + 1]) ++l;
+        return l;
+    };
+    for (int i = half * 32 + lane; i < kStages * slot_doubles; i += 64) ring[i] = 0.0;  // finite slot tails
+    fence_proxy_async();
+    pair_sync(pair);
+    auto issue = [&](std::int32_t q, int st) {
+        const int l = level_of(q);
+        const std::int32_t s = q - pt.base[l];
+        const std::int64_t o = pt.inv_off[l][s];
+        const std::uint32_t bytes = static_cast<std::uint32_t>((pt.inv_off[l][s + 1] - o) * 8);
+        mbar_arrive_expect_tx(&bar[st], bytes);
+        if (l == 0)
+            bulk_g2s_evict_first(ring + static_cast<std::size_t>(st) * slot_doubles, pt.inv[0] + o, bytes, &bar[st]);
+        else
+            bulk_g2s_evict_last(ring + static_cast<std::size_t>(st) * slot_doubles, pt.inv[l] + o, bytes, &bar[st]);
+    };
+    if (half == 0 && lane == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
+        fence_mbar_init();
+        for (int st = 0; st < kStages && st < nloc; ++st) issue(item(st), st);
+    }
+    pair_sync(pair);
+    struct Item {
+        int l;
+        std::int32_t s, s0, dim;
+    };
+    auto row_index = [&](const Item& it, int j) -> std::int64_t {
+        if (it.l == 0) return 3 * static_cast<std::int64_t>(it.s0) + j;
+        return 3 * static_cast<std::int64_t>(pt.sub_nodes[it.l][it.s0 + j / 3]) + (j % 3);
+    };
+    // Per item, prefetched one item ahead into registers:
+    //   level 0, warp 0: the update operands -> new residual in b (x, r written)
+    //   level 0, warp 1: level-1 node range, CSR offsets and children
+    //   coarse: both warps gather b from the restricted residual
+    std::int32_t v0 = 0, nv = 0, my_uptr = 0, my_child = 0;
+    auto load = [&](int i, Item& it, double* bb, std::int32_t& av0, std::int32_t& anv, std::int32_t& aup,
+                    std::int32_t& ach) {
+        const std::int32_t q = item(i);
+        it.l = level_of(q);
+        it.s = q - pt.base[it.l];
+        it.s0 = pt.sub_ptr[it.l][it.s];
+        it.dim = 3 * (pt.sub_ptr[it.l][it.s + 1] - it.s0);
+        if (it.l == 0) {
+            if (half == 0) {
+                double pv[RB], av[RB], xv[RB], rv[RB];
+#pragma unroll
+                for (int t = 0; t < RB; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j < it.dim) {
+                        const std::int64_t g = 3 * static_cast<std::int64_t>(it.s0) + j;
+                        av[t] = ldg_issue(ia.ap + g);
+                        if (ia.restart_mode) {
+                            rv[t] = ldg_issue(ia.b + g);
+                        } else {
+                            rv[t] = ldg_issue(ia.r + g);
+                            pv[t] = ldg_issue(ia.p + g);
+                            xv[t] = ldg_issue(ia.x + g);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < RB; ++t) {
+                    const int j = lane + 32 * t;
+                    bb[t] = 0.0;
+                    if (j < it.dim) {
+                        const std::int64_t g = 3 * static_cast<std::int64_t>(it.s0) + j;
+                        double nr;
+                        if (ia.restart_mode) {
+                            nr = rv[t] - av[t];
+                        } else {
+                            ia.x[g] = xv[t] + alpha * pv[t];
+                            nr = rv[t] - alpha * av[t];
+                        }
+                        ia.r[g] = nr;
+                        bb[t] = nr;
+                    }
+                }
+            } else {
+                av0 = ia.up_first0[it.s];
+                anv = ia.up_first0[it.s + 1] - av0;
+                aup = lane < anv ? ia.upc_ptr0[av0 + lane] - it.s0 : 0;
+                ach = lane < it.dim / 3 ? ia.upc_node0[it.s0 + lane] - it.s0 : 0;
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < RB; ++t) {
+                const int j = lane + 32 * t;
+                bb[t] = j < it.dim ? ldg_issue(pt.rin[it.l] + row_index(it, j)) : 0.0;
+            }
+        }
+    };
+    Item cur{0, 0, 0, 0};
+    double b[RB];
+    if (nloc > 0 && n0 > 0) load(0, cur, b, v0, nv, my_uptr, my_child);
+    double dsum = 0;
+    int st = 0;
+    std::uint32_t par = 0;
+    for (int i = 0; i < nloc; ++i) {
+        if (i == n0) {
+            // every pair's level-0 items (and restrictions) must be complete
+            // before the coarse residuals are read
+            __threadfence();
+            pair_sync(pair);
+            if (half == 0 && lane == 0) {
+                atomicAdd(ia.counters + 0, 1u);
+                spin_until(ia.counters + 0, static_cast<unsigned>(k_it) * static_cast<unsigned>(np), flags + F_ERR);
+            }
+            pair_sync(pair);
+            load(i, cur, b, v0, nv, my_uptr, my_child);
+        }
+        // b into shared memory: warp 0 for level-0 items (it holds the updated
+        // residual), both warps otherwise (same values)
+        if (cur.l > 0 || half == 0) {
+#pragma unroll
+            for (int t = 0; t < RB; ++t)
+                if (lane + 32 * t < kK) bs[lane + 32 * t] = b[t];
+        }
+        if (cur.l == 0 && half == 1) {
+            if (lane < nv) meta[lane] = my_uptr;
+            if (lane < cur.dim / 3) meta[40 + lane] = my_child;
+            if (lane == 0) meta[nv] = cur.dim / 3;  // end of the last node's children
+        }
+        Item nxt{0, 0, 0, 0};
+        double bn[RB];
+        std::int32_t nv0 = 0, nnv = 0, nup = 0, nch = 0;
+        if (i + 1 < nloc && i + 1 != n0) load(i + 1, nxt, bn, nv0, nnv, nup, nch);
+        pair_sync(pair);  // bs (and meta) ready for both warps
+        if (cur.l == 0 && half == 1) {  // level-1 restriction of this subdomain (children ascending)
+            for (int t = lane; t < 3 * nv; t += 32) {
+                const int vi = t / 3, comp = t % 3;
+                double acc = 0;
+                for (int q = meta[vi]; q < meta[vi + 1]; ++q) acc += bs[3 * meta[40 + q] + comp];
+                const std::int32_t v = v0 + vi;
+                ia.rr1[3 * static_cast<std::int64_t>(v) + comp] = acc;
+#pragma unroll
+                for (int l = 2; l < kMaxLevels; ++l)
+                    if (l < ia.n_levels) red_add(ia.rr[l] + 3 * static_cast<std::int64_t>(ia.anc[l][v]) + comp, acc);
+            }
+        }
+        mbar_wait(&bar[st], par);
+        const double* M = ring + static_cast<std::size_t>(st) * slot_doubles;
+        double* out = pt.out[cur.l];
+        dsum += pair_solve<kK>(M, bs, lane, half, cur.dim,
+                               [&](int j, double v) { out[row_index(cur, j)] = v; });
+        pair_sync(pair);  // both warps are done with the slot, bs and meta
+        if (half == 0 && lane == 0 && i + kStages < nloc) {
+            fence_proxy_async();
+            issue(item(i + kStages), st);
+        }
+        if (++st == kStages) {
+            st = 0;
+            par ^= 1u;
+        }
+        cur = nxt;
+        v0 = nv0;
+        nv = nnv;
+        my_uptr = nup;
+        my_child = nch;
+#pragma unroll
+        for (int t = 0; t < RB; ++t) b[t] = bn[t];
+    }
+    if (n0 == nloc) {  // a pair without coarse items still arrives
+        __threadfence();
+        pair_sync(pair);
+        if (half == 0 && lane == 0) atomicAdd(ia.counters + 0, 1u);
+    }
+    // ---- final: r.z from every CTA, stop test, beta, prolongation + p ----
+    const double bsum = block_sum(dsum, red);
+    if (threadIdx.x == 0) {
+        ia.partials[blockIdx.x] = bsum;
+        __threadfence();
+        atomicAdd(ia.counters + 1, 1u);
+        spin_until(ia.counters + 1, static_cast<unsigned>(k_it) * gridDim.x, flags + F_ERR);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = 0;
+        for (unsigned q = threadIdx.x; q < gridDim.x; q += 32) v += __ldcg(ia.partials + q);
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double rz = red[0];
+    const double rho = ia.scal[S_RHO0 + ((k_it - 1) & 1)];
+    const double stop = ia.scal[S_STOP];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // pcg.hpp:76-82
+        flags[F_ITERS] = k_it;
+        ia.scal[S_REL] = sqrt(fabs(rz) / ia.scal[S_RHO_INIT]);
+        if (rz <= stop) {
+            flags[F_DONE] = 1;
+            flags[F_CONVERGED] = 1;
+        } else {
+            ia.scal[S_RHO0 + (k_it & 1)] = rz;
+        }
+    }
+    if (rz <= stop) return;
+    const double beta = rz / rho;
+    const FinalSo& fa = ia.fa;
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+    for (std::int64_t sl = tid; sl < ia.n_slots; sl += stride) {
+        const std::int64_t g = 3 * sl;
+        std::int32_t nd[kMaxLevels];
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l)
+            if (l < fa.n_coarse) nd[l] = fa.agg[l][sl];
+        double z0 = ia.z[g], z1 = ia.z[g + 1], z2 = ia.z[g + 2];
+        const double p0 = ia.pout[g], p1 = ia.pout[g + 1], p2 = ia.pout[g + 2];
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l)
+            if (l < fa.n_coarse) {
+                const double* yl = fa.y[l] + 3 * static_cast<std::int64_t>(nd[l]);
+                z0 += yl[0];
+                z1 += yl[1];
+                z2 += yl[2];
+            }
+        ia.pout[g] = z0 + beta * p0;
+        ia.pout[g + 1] = z1 + beta * p1;
+        ia.pout[g + 2] = z2 + beta * p2;
+        ia.apclear[g] = 0.0;
+        ia.apclear[g + 1] = 0.0;
+        ia.apclear[g + 2] = 0.0;
+        if (ia.tmpclear) {
+            ia.tmpclear[g] = 0.0;
+            ia.tmpclear[g + 1] = 0.0;
+            ia.tmpclear[g + 2] = 0.0;
+        }
+    }
+    for (int l = 0; l < fa.n_clear; ++l)
+        for (std::int64_t q = tid; q < fa.clear_n[l]; q += stride) fa.clear[l][q] = 0.0;
 }
 
 // ============================================================================
@@ -862,7 +1259,7 @@ __device__ void update_phase(const Persist& P, double alpha, const double* __res
     a.r = P.r;
     a.p = P.p;
     a.b = P.b;
-    const std::int32_t ntiles = static_cast<std::int32_t>(ceil_div(P.so.n0_parts, kUpdSubs));
+    const std::int32_t ntiles = static_cast<std::int32_t>(ceil_div(P.so.n0_parts, P.so.subs));
     for (std::int32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
         update_tile<kMode, kPT>(P.so, a, alpha, apv, tile, sm);
 }
@@ -890,9 +1287,17 @@ __device__ double precond_phase(const Persist& P, unsigned char* smem, std::uint
     for (int l = 0; l < kMaxLevels; ++l) {
         lv_lo[l] = lv_n[l] = 0;
         if (l < pt.n) {
-            const std::int64_t nl = pt.base[l + 1] - pt.base[l];
-            lv_lo[l] = pt.base[l] + static_cast<std::int32_t>(gp * nl / np);
-            lv_n[l] = static_cast<std::int32_t>((gp + 1) * nl / np - gp * nl / np);
+            std::int32_t a, b;
+            if (pt.split && pt.np == np) {
+                a = pt.split[l * (np + 1) + gp];
+                b = pt.split[l * (np + 1) + gp + 1];
+            } else {
+                const std::int64_t nl = pt.base[l + 1] - pt.base[l];
+                a = static_cast<std::int32_t>(gp * nl / np);
+                b = static_cast<std::int32_t>((gp + 1) * nl / np);
+            }
+            lv_lo[l] = pt.base[l] + a;
+            lv_n[l] = b - a;
             nloc += lv_n[l];
         }
     }
@@ -1132,8 +1537,9 @@ void launch_update_so(Ctx& c, const PcgArgs& a) {
         if (l >= 2) so.anc[l] = c.levels[l]->anc.p;
     }
     so.max_fill0 = L0.max_fill;
-    const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(L0.n_parts, kUpdSubs)));
-    const std::size_t smem = update_tile_smem(L0.max_fill);
+    so.subs = c.upd_subs;
+    const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(L0.n_parts, so.subs)));
+    const std::size_t smem = update_tile_smem(L0.max_fill, so.subs);
     static bool attr = false;
     if (!attr) {
         ADIPC_CUDA(cudaFuncSetAttribute(k_update_so<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
@@ -1145,12 +1551,89 @@ void launch_update_so(Ctx& c, const PcgArgs& a) {
 template void launch_update_so<M_UPDATE>(Ctx&, const PcgArgs&);
 template void launch_update_so<M_RESTART>(Ctx&, const PcgArgs&);
 
+// Byte-balanced split points of every level over np work units, cached on
+// the context per (levels, np). Computed outside stream capture
+// (prepare_work_splits, from pcg.cu before the iteration graphs are captured).
+const std::int32_t* work_split(Ctx& c, int np) {
+    for (auto& e : c.splits)
+        if (e.np == np && e.version == c.levels_version) return e.buf.p;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    ADIPC_CUDA(cudaStreamIsCapturing(c.stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;  // equal-count split inside an unprepared capture
+    const int L = static_cast<int>(c.levels.size());
+    std::vector<std::int32_t> h(static_cast<std::size_t>(L) * (np + 1));
+    for (int l = 0; l < L; ++l) {
+        // cost of a subdomain ~ a fixed per-item latency (kItemCost, in units
+        // of one packed double streamed) + its packed-inverse doubles
+        constexpr std::int64_t kItemCost = 700;
+        const std::vector<std::int64_t>& off = c.levels[l]->inv_off_host;  // n_parts + 1 cumulative
+        const std::int32_t n = c.levels[l]->n_parts;
+        auto cost = [&](std::int32_t i) { return off[i] + kItemCost * i; };
+        const std::int64_t total = cost(n);
+        std::int32_t s = 0;
+        for (int p = 0; p <= np; ++p) {
+            const std::int64_t target = total * p / np;
+            while (s < n && cost(s) < target) ++s;  // first subdomain starting at or after the cut
+            h[static_cast<std::size_t>(l) * (np + 1) + p] = p == np ? n : s;
+        }
+    }
+    if (c.splits.size() >= 4) {
+        c.splits.front().buf.free();
+        c.splits.erase(c.splits.begin());
+    }
+    c.splits.emplace_back();
+    Ctx::Split& e = c.splits.back();
+    e.np = np;
+    e.version = c.levels_version;
+    e.buf.reserve(h.size());
+    ADIPC_CUDA(cudaMemcpyAsync(e.buf.p, h.data(), h.size() * sizeof(std::int32_t), cudaMemcpyHostToDevice, c.stream));
+    ADIPC_CUDA(cudaStreamSynchronize(c.stream));  // h goes out of scope
+    return e.buf.p;
+}
+
+struct PcLaunch {
+    void* fn = nullptr;
+    int slot = 0, pairs = 1, grid = 1;
+    std::size_t smem = 0;
+};
+
+// launch configuration of k_precond_so (warp pairs, TMA ring per pair)
+PcLaunch precond_launch(Ctx& c) {
+    PcLaunch L;
+    int fill = 1;
+    for (const auto& lv : c.levels) fill = std::max(fill, lv->max_fill);
+    const int kk = matvec_cols(fill);
+    L.slot = static_cast<int>(packed_doubles(kk));
+    const int stages = c.l0_stages;
+    const std::size_t per_pair = (sizeof(double) * L.slot + sizeof(std::uint64_t)) * stages + 2 * sizeof(double) * kk;
+    L.pairs = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(c.pc_pairs, (113u * 1024u) / per_pair)));
+    L.smem = per_pair * L.pairs;
+    if (kk == 24)
+        L.fn = stages == 2 ? reinterpret_cast<void*>(k_precond_so<24, 2>) : reinterpret_cast<void*>(k_precond_so<24, 3>);
+    else if (kk == 48)
+        L.fn = stages == 2 ? reinterpret_cast<void*>(k_precond_so<48, 2>) : reinterpret_cast<void*>(k_precond_so<48, 3>);
+    else
+        L.fn = stages == 2 ? reinterpret_cast<void*>(k_precond_so<96, 2>) : reinterpret_cast<void*>(k_precond_so<96, 3>);
+    ADIPC_CUDA(cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)));
+    int occ = 0;
+    ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, 64 * L.pairs, L.smem));
+    if (occ < 1) throw StatusError(kInvalidArgument, "preconditioner ring does not fit in shared memory");
+    int sms = kSMs;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    std::int64_t items = 0;
+    for (const auto& lv : c.levels) items += lv->n_parts;
+    L.grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(static_cast<std::int64_t>(sms) * occ,
+                                                                                  ceil_div(items, L.pairs))));
+    return L;
+}
+
 // z = M r: every level in one persistent launch (k_precond_so); r.z -> *dot
 void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, double* partials, unsigned* ticket,
                        double* dot) {
     PrecondTable pt{};
     pt.n = static_cast<int>(c.levels.size());
     if (const char* e = std::getenv("ADIPC_DEBUG_PC_LEVELS")) pt.n = std::min(pt.n, std::max(1, std::atoi(e)));  // timing experiments only
+    if (const char* e = std::getenv("ADIPC_DEBUG_PC_NOMATH")) pt.dbg_nomath = std::atoi(e);
     int fill = 1;
     for (int l = 0; l < pt.n; ++l) {
         const DeviceLevel& L = *c.levels[l];
@@ -1173,18 +1656,6 @@ void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, dou
     const std::size_t smem = per_pair * pairs;
     int sms = kSMs;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-#define ADIPC_PC(K, S)                                                                                        \
-    do {                                                                                                      \
-        ADIPC_CUDA(cudaFuncSetAttribute(k_precond_so<K, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                        static_cast<int>(smem)));                                             \
-        int occ = 0;                                                                                          \
-        ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_precond_so<K, S>, 64 * pairs, smem)); \
-        if (occ < 1) throw StatusError(kInvalidArgument, "preconditioner ring does not fit in shared memory"); \
-        const int grid = static_cast<int>(std::min<std::int64_t>(static_cast<std::int64_t>(sms) * occ,          \
-                                                                 ceil_div(pt.base[pt.n], pairs)));            \
-        k_precond_so<K, S><<<std::max(grid, 1), 64 * pairs, smem, c.stream>>>(pt, partials, ticket, dot, flags, \
-                                                                             slot);                           \
-    } while (0)
     if (c.pc_variant == 2 && kk <= 48) {  // two items per warp (half-warps), one warp per CTA
         constexpr int wpc = 1;
         const std::size_t per_warp = (sizeof(double) * 2 * slot + sizeof(std::uint64_t)) * stages +
@@ -1230,14 +1701,14 @@ void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, dou
             if (stages == 2) ADIPC_PC1(48, 2); else ADIPC_PC1(48, 3);
         }
 #undef ADIPC_PC1
-    } else if (kk == 24) {
-        if (stages == 2) ADIPC_PC(24, 2); else ADIPC_PC(24, 3);
-    } else if (kk == 48) {
-        if (stages == 2) ADIPC_PC(48, 2); else ADIPC_PC(48, 3);
     } else {
-        if (stages == 2) ADIPC_PC(96, 2); else ADIPC_PC(96, 3);
+        const PcLaunch L = precond_launch(c);
+        pt.np = L.grid * L.pairs;
+        pt.split = c.pc_split ? work_split(c, pt.np) : nullptr;
+        int slot_arg = L.slot;
+        void* args[] = {&pt, &partials, &ticket, &dot, const_cast<int**>(&flags), &slot_arg};
+        ADIPC_CUDA(cudaLaunchKernel(L.fn, dim3(L.grid), dim3(64 * L.pairs), args, L.smem, c.stream));
     }
-#undef ADIPC_PC
     ADIPC_LAUNCH_CHECK();
 }
 
@@ -1261,8 +1732,14 @@ void launch_final_so(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a)
         fa.clear_n[fa.n_clear] = 3 * static_cast<std::int64_t>(c.levels[l]->n_nodes);
         ++fa.n_clear;
     }
-    const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(c.A.n, 256)));
-    k_final_so<kFinal><<<grid, 256, 0, c.stream>>>(c.A.n, fa, z, p, ap, a);
+    const int per = c.final_per, block = c.final_block;
+    const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(c.A.n, static_cast<std::int64_t>(block) * per)));
+    if (per == 1)
+        k_final_so<kFinal, 1><<<grid, block, 0, c.stream>>>(c.A.n, fa, z, p, ap, a);
+    else if (per == 2)
+        k_final_so<kFinal, 2><<<grid, block, 0, c.stream>>>(c.A.n, fa, z, p, ap, a);
+    else
+        k_final_so<kFinal, 4><<<grid, block, 0, c.stream>>>(c.A.n, fa, z, p, ap, a);
     ADIPC_LAUNCH_CHECK();
 }
 template void launch_final_so<F_PCG_INIT>(Ctx&, double*, double*, double*, const PcgArgs&);
@@ -1356,7 +1833,8 @@ bool pcg_persistent(Ctx& c, const PcgArgs& a, double* partials, int restart, int
     std::size_t ub = std::max<std::size_t>(sizeof(SpmvStage) * kPWarps * kSS,
                                            sizeof(double) * (static_cast<std::size_t>(kPPairs) * kSP * P.slot_doubles +
                                                              static_cast<std::size_t>(kPWarps) * kk));
-    ub = std::max<std::size_t>(ub, update_tile_smem(L0.max_fill));
+    P.so.subs = kUpdSubs;
+    ub = std::max<std::size_t>(ub, update_tile_smem(L0.max_fill, kUpdSubs));
     ub = (ub + 127) & ~static_cast<std::size_t>(127);
     P.union_bytes = static_cast<int>(ub);
     const std::size_t smem = ub + sizeof(std::uint64_t) * (kPWarps * kSS + kPPairs * kSP);
@@ -1381,4 +1859,141 @@ bool pcg_persistent(Ctx& c, const PcgArgs& a, double* partials, int restart, int
     return true;
 }
 
+}  // namespace adipc_gpu
+
+namespace adipc_gpu {
+
+// One PCG iteration after the SpMV: update + every MAS level + prolongation
+// (k_iter_so), cooperative launch (the in-kernel arrival counters need every
+// CTA resident). Returns false when not applicable.
+bool iter_so_supported(const Ctx& c) {
+    if (!c.fused || !so_supported(c)) return false;
+    int fill = 1;
+    for (const auto& L : c.levels) fill = std::max(fill, L->max_fill);
+    return matvec_cols(fill) != 0;
+}
+
+struct IterLaunch {
+    void* fn = nullptr;
+    int kk = 0, slot = 0, pairs = 1, grid = 1;
+    std::size_t smem = 0;
+};
+
+IterLaunch iter_launch(Ctx& c) {
+    IterLaunch L;
+    int fill = 1;
+    for (const auto& lv : c.levels) fill = std::max(fill, lv->max_fill);
+    L.kk = matvec_cols(fill);
+    L.slot = static_cast<int>(packed_doubles(L.kk));
+    const int stages = c.l0_stages;
+    const std::size_t per_pair = (sizeof(double) * L.slot + sizeof(std::uint64_t)) * stages +
+                                 sizeof(double) * L.kk + sizeof(double) * 40;
+    L.pairs = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(4, (113u * 1024u) / per_pair)));
+    L.smem = per_pair * L.pairs;
+    int sms = kSMs;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    if (L.kk == 24)
+        L.fn = stages == 2 ? reinterpret_cast<void*>(k_iter_so<24, 2>) : reinterpret_cast<void*>(k_iter_so<24, 3>);
+    else if (L.kk == 48)
+        L.fn = stages == 2 ? reinterpret_cast<void*>(k_iter_so<48, 2>) : reinterpret_cast<void*>(k_iter_so<48, 3>);
+    else
+        L.fn = stages == 2 ? reinterpret_cast<void*>(k_iter_so<96, 2>) : reinterpret_cast<void*>(k_iter_so<96, 3>);
+    ADIPC_CUDA(cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)));
+    int occ = 0;
+    ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, 64 * L.pairs, L.smem));
+    if (occ < 1) throw StatusError(kInvalidArgument, "fused iteration kernel does not fit on an SM");
+    L.grid = sms * occ;
+    return L;
+}
+
+void launch_iter_so(Ctx& c, const PcgArgs& a, bool restart, unsigned* counters, double* partials) {
+    IterArgs ia{};
+    PrecondTable& pt = ia.pt;
+    pt.n = static_cast<int>(c.levels.size());
+    int fill = 1;
+    for (int l = 0; l < pt.n; ++l) {
+        const DeviceLevel& L = *c.levels[l];
+        pt.base[l + 1] = pt.base[l] + L.n_parts;
+        pt.sub_ptr[l] = L.sub_ptr.p;
+        pt.sub_nodes[l] = l == 0 ? nullptr : L.sub_nodes.p;
+        pt.inv_off[l] = L.inv_off.p;
+        pt.inv[l] = L.inv.p;
+        pt.rin[l] = l == 0 ? a.r : L.rr.p;
+        pt.out[l] = l == 0 ? c.w.z.p : L.y.p;
+        fill = std::max(fill, L.max_fill);
+    }
+    FinalSo& fa = ia.fa;
+    fa.n_coarse = pt.n - 1;
+    for (int l = 1; l < pt.n; ++l) {
+        fa.agg[l - 1] = c.levels[l]->agg.p;
+        fa.y[l - 1] = c.levels[l]->y.p;
+    }
+    for (int l = 2; l < pt.n; ++l) {
+        fa.clear[fa.n_clear] = c.levels[l]->rr.p;
+        fa.clear_n[fa.n_clear] = 3 * static_cast<std::int64_t>(c.levels[l]->n_nodes);
+        ++fa.n_clear;
+    }
+    const DeviceLevel& L0 = *c.levels[0];
+    ia.x = a.x;
+    ia.r = a.r;
+    ia.p = a.p;
+    ia.ap = a.ap;
+    ia.b = a.b;
+    ia.z = c.w.z.p;
+    ia.pout = c.w.p.p;
+    ia.apclear = c.w.ap.p;
+    ia.tmpclear = nullptr;
+    ia.up_first0 = L0.up_first.p;
+    ia.upc_ptr0 = L0.upc_ptr.p;
+    ia.upc_node0 = L0.upc_node.p;
+    ia.rr1 = c.levels[1]->rr.p;
+    ia.n_levels = pt.n;
+    for (int l = 2; l < pt.n; ++l) {
+        ia.rr[l] = c.levels[l]->rr.p;
+        ia.anc[l] = c.levels[l]->anc.p;
+    }
+    ia.n_slots = c.A.n;
+    ia.scal = a.scal;
+    ia.flags = a.flags;
+    ia.counters = counters;
+    ia.partials = partials;
+    ia.restart_mode = restart ? 1 : 0;
+    const IterLaunch L = iter_launch(c);
+    const int slot = L.slot, pairs = L.pairs, grid = L.grid;
+    const std::size_t smem = L.smem;
+    void* fn = L.fn;
+    pt.np = grid * pairs;
+    pt.split = c.pc_split ? work_split(c, pt.np) : nullptr;
+    int slot_arg = slot;
+    void* args[] = {&ia, &slot_arg};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(64 * pairs);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ADIPC_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+    ADIPC_LAUNCH_CHECK();
+}
+
+}  // namespace adipc_gpu
+
+namespace adipc_gpu {
+IterLaunch iter_launch(Ctx& c);
+PcLaunch precond_launch(Ctx& c);
+// byte-balanced splits for the launch configurations the PCG iteration graph
+// will capture (no allocation may happen while capturing)
+void prepare_work_splits(Ctx& c) {
+    if (!so_supported(c) || !c.pc_split) return;
+    if (iter_so_supported(c)) {
+        const IterLaunch L = iter_launch(c);
+        work_split(c, L.grid * L.pairs);
+    }
+    const PcLaunch P = precond_launch(c);
+    work_split(c, P.grid * P.pairs);
+}
 }  // namespace adipc_gpu

@@ -14,7 +14,7 @@ from paper_2411_06224_b200 import api as P  # noqa: E402
 from paper_2411_06224_b200.context import Context  # noqa: E402
 
 OPTS = {"so": _lib.OPT_SO_KERNELS, "l0": _lib.OPT_L0_STAGES, "spmv": _lib.OPT_SPMV_VARIANT,
-        "order": _lib.OPT_SOLVE_ORDER, "persist": _lib.OPT_PERSISTENT, "pc": _lib.OPT_PC_VARIANT}
+        "order": _lib.OPT_SOLVE_ORDER, "persist": _lib.OPT_PERSISTENT, "pc": _lib.OPT_PC_VARIANT, "fused": _lib.OPT_FUSED, "pairs": _lib.OPT_PC_PAIRS}
 sc = scenes.CONFIGS[os.environ.get("CFG", "cfg5_stiff_box")]()
 ctx = Context(0)
 l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, 16)

@@ -155,10 +155,12 @@ def byte_model(n, U, levels):
     nxt = lambda l: nodes[l + 1] if l + 1 < nl else 0  # noqa: E731
     vec = 24 * n
     spmv = 80 * U + vec + vec                      # A (72 B + 2 x u32 per block), p read, Ap written
-    # update pass: slot list, x r/w, p, r r/w, Ap, r_1 write, restriction metadata
+    # update pass (solve order: unit-stride): x r/w, p, r r/w, Ap, r_1 write,
+    # level-1 children lists + offsets, subdomain bounds
     update = 4 * n + 6 * vec + 24 * nxt(0) + 4 * (n + nxt(0) + parts[0])
-    # preconditioner: level-0 solve (D0^-1, slot list, r read, z write) || coarse chain
-    # (D_l^-1, member list, r_l read, y_l write, r_{l+1} write, restriction metadata)
+    # preconditioner, every level in one launch: level 0 (D0^-1, r read, z write,
+    # subdomain bounds) + each coarse level (D_l^-1, member list, r_l read, y_l
+    # write, RED targets of the update pass)
     precond = inv[0] + 4 * n + 2 * vec + sum(
         inv[l] + 4 * nodes[l] + 48 * nodes[l] + 24 * nxt(l) + 4 * (nodes[l] + nxt(l) + parts[l])
         for l in range(1, nl))

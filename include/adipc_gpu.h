@@ -51,7 +51,7 @@ extern "C" {
 #define ADIPC_OPT_SO_KERNELS 6      /* 1 (default): solve-order PCG iteration kernels; 0: the generic level kernels */
 #define ADIPC_OPT_PERSISTENT 8      /* 1: PCG iterations in one persistent cooperative kernel (solve order); default 0 */
 #define ADIPC_OPT_PC_VARIANT 9      /* preconditioner kernel: 0 (default) warp pairs per subdomain, 1 one warp per subdomain, 2 two subdomains per warp */
-#define ADIPC_OPT_FUSED 10          /* 1 (default): update + MAS levels + prolongation in one kernel per PCG iteration */
+#define ADIPC_OPT_FUSED 10          /* 1: update + MAS levels + prolongation in one cooperative kernel per PCG iteration (default 0) */
 #define ADIPC_OPT_PC_PAIRS 11       /* warp pairs per CTA of the preconditioner kernel (1..5, default 4) */
 #define ADIPC_OPT_L0_STAGES 7       /* 2 (default) or 3: packed inverses in flight per warp pair in the preconditioner */
 

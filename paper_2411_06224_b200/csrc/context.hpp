@@ -160,6 +160,10 @@ struct Ctx {
     int l0_stages = 2;
     int pc_variant = 0;
     int pc_pairs = 4;
+    int ws_cons = 8;
+    // share (x/1024) of the level-0 inverses streamed with L2 evict-last, so
+    // they stay L2-resident from one PCG iteration to the next (ADIPC_L0_KEEP)
+    int l0_keep_1024 = 0;          // consumer warps of the warp-specialised preconditioner (ADIPC_WS_CONS)
     // tile shapes of the streaming kernels (ADIPC_UPD_SUBS / ADIPC_FINAL_PER /
     // ADIPC_FINAL_BLOCK environment overrides, read at context creation)
     int upd_subs = 64, final_per = 1, final_block = 256;        // warp pairs per CTA of k_precond_so (ADIPC_OPT_PC_PAIRS)
@@ -167,7 +171,7 @@ struct Ctx {
     bool so_kernels = true;
     // update + every MAS level + prolongation in one cooperative kernel per
     // iteration (ADIPC_OPT_FUSED; solve_order.cu k_iter_so)
-    bool fused = true;
+    bool fused = false;
     // the PCG iterations as one persistent cooperative kernel (ADIPC_OPT_PERSISTENT)
     bool persistent = false;
     DBuf<unsigned long long> phase_ns;  // its per-phase times (ADIPC_OPT_PROFILE)

@@ -162,6 +162,7 @@ struct PrecondTable {
     const double* rin[kMaxLevels];           // level 0: r; coarse: restricted residual
     double* out[kMaxLevels];                 // level 0: z; coarse: y
     int dbg_nomath;                          // timing experiments only
+    std::int64_t l0_keep;                    // level-0 inverse doubles below this offset stream L2 evict-last
     // byte-balanced work split: split[l * (np + 1) + p] = first subdomain of
     // level l for work unit p (np units), cut at equal packed-inverse bytes
     const std::int32_t* split;
@@ -233,9 +234,9 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
         const std::int64_t o = pt.inv_off[l][s];
         const std::uint32_t bytes = static_cast<std::uint32_t>((pt.inv_off[l][s + 1] - o) * 8);
         mbar_arrive_expect_tx(&bar[st], bytes);
-        if (l == 0)  // streamed once per application
+        if (l == 0 && o >= pt.l0_keep)  // streamed once per application
             bulk_g2s_evict_first(ring + static_cast<std::size_t>(st) * slot_doubles, pt.inv[0] + o, bytes, &bar[st]);
-        else  // coarse inverses (~26 MB at cfg5) stay L2-resident across iterations
+        else  // coarse inverses (~26 MB at cfg5) and the kept share of level 0 stay L2-resident across iterations
             bulk_g2s_evict_last(ring + static_cast<std::size_t>(st) * slot_doubles, pt.inv[l] + o, bytes, &bar[st]);
     };
     if (half == 0 && lane == 0) {
@@ -712,6 +713,172 @@ __global__ void __launch_bounds__(128) k_precond_so2(PrecondTable pt, double* __
         cur = nxt;
 #pragma unroll
         for (int t = 0; t < T; ++t) b[t] = bn[t];
+    }
+    grid_sum_last_block(dsum, partials, ticket, dot_out);
+}
+
+// ============================================================================
+// Warp-specialised preconditioner (k_precond_ws): one CTA per SM, one producer
+// warp streaming the CTA's packed inverses in order through a CTA-wide ring of
+// kSlots shared slots (cp.async.bulk; full/empty mbarriers per slot), and
+// kCons consumer warps, each solving two items at a time (one per half-warp,
+// packed_matvec_half: full 256-byte shared loads, conflict-free transposed
+// reads). Staging depth (slots in flight) and compute concurrency are sized
+// independently, so neither the TMA latency nor the mat-vec latency is
+// exposed per item as in the per-pair rings.
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int kK, int kSlots, int kCons>
+__global__ void __launch_bounds__(32 * (kCons + 1)) k_precond_ws(PrecondTable pt, double* __restrict__ partials,
+                                                                unsigned* __restrict__ ticket,
+                                                                double* __restrict__ dot_out,
+                                                                const int* __restrict__ flags, int slot_doubles) {
+    constexpr int T = (kK + 15) / 16;
+    constexpr int kBs = kK + 2;
+    if (flags && flags[F_DONE]) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* ring = reinterpret_cast<double*>(smem);
+    double* bsw = ring + static_cast<std::size_t>(kSlots) * slot_doubles;  // kCons x 2 x kBs
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(bsw + static_cast<std::size_t>(kCons) * 2 * kBs);
+    std::uint64_t* empty = full + kSlots;
+    // this CTA's items: an even share of each level, level 0 first
+    const std::int64_t gp = blockIdx.x, np = gridDim.x;
+    std::int32_t lv_lo[kMaxLevels], lv_n[kMaxLevels];
+    int nloc = 0;
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l) {
+        lv_lo[l] = lv_n[l] = 0;
+        if (l < pt.n) {
+            const std::int64_t nl = pt.base[l + 1] - pt.base[l];
+            const std::int32_t a = static_cast<std::int32_t>(gp * nl / np);
+            const std::int32_t b = static_cast<std::int32_t>((gp + 1) * nl / np);
+            lv_lo[l] = pt.base[l] + a;
+            lv_n[l] = b - a;
+            nloc += lv_n[l];
+        }
+    }
+    auto item = [&](int i) -> std::int32_t {
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l) {
+            if (i < lv_n[l]) return lv_lo[l] + i;
+            i -= lv_n[l];
+        }
+        return 0;
+    };
+    auto level_of = [&](std::int32_t q) {
+        int l = 0;
+        while (l + 1 < pt.n && q >= pt.base[l + 1]) ++l;
+        return l;
+    };
+    // finite slot tails (the unrolled mat-vec multiplies them by b_k = 0)
+    for (int i = threadIdx.x; i < kSlots * slot_doubles; i += blockDim.x) ring[i] = 0.0;
+    for (int i = threadIdx.x; i < kCons * 2 * kBs; i += blockDim.x) bsw[i] = 0.0;
+    fence_proxy_async();
+    if (threadIdx.x == 0) {
+        for (int sl = 0; sl < kSlots; ++sl) {
+            mbar_init(&full[sl], 1);
+            mbar_init(&empty[sl], 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    double dsum = 0;
+    if (w == kCons) {  // ---- producer warp ----
+        if (lane == 0) {
+            for (int i = 0; i < nloc; ++i) {
+                const int sl = i % kSlots;
+                const std::uint32_t ph = static_cast<std::uint32_t>(i / kSlots) & 1u;
+                if (i >= kSlots) mbar_wait(&empty[sl], ph ^ 1u);  // consumed item i - kSlots
+                const std::int32_t q = item(i);
+                const int l = level_of(q);
+                const std::int32_t s = q - pt.base[l];
+                const std::int64_t o = pt.inv_off[l][s];
+                const std::uint32_t bytes = static_cast<std::uint32_t>((pt.inv_off[l][s + 1] - o) * 8);
+                mbar_arrive_expect_tx(&full[sl], bytes);
+                double* dst = ring + static_cast<std::size_t>(sl) * slot_doubles;
+                if (l == 0)
+                    bulk_g2s_evict_first(dst, pt.inv[0] + o, bytes, &full[sl]);
+                else
+                    bulk_g2s_evict_last(dst, pt.inv[l] + o, bytes, &full[sl]);
+            }
+        }
+    } else {  // ---- consumer warps: items (2p, 2p+1) for p = w, w + kCons, ... ----
+        const int half = lane >> 4, hl = lane & 15;
+        double* bs = bsw + (static_cast<std::size_t>(w) * 2 + half) * kBs;
+        struct Item {
+            int l;
+            std::int32_t s0, dim;
+        };
+        auto row_index = [&](const Item& it, int j) -> std::int64_t {
+            if (it.l == 0) return 3 * static_cast<std::int64_t>(it.s0) + j;
+            return 3 * static_cast<std::int64_t>(pt.sub_nodes[it.l][it.s0 + j / 3]) + (j % 3);
+        };
+        auto load_b = [&](int i, Item& it, double* bb) {
+            it.l = 0;
+            it.s0 = 0;
+            it.dim = 0;
+            if (i < nloc) {
+                const std::int32_t q = item(i);
+                it.l = level_of(q);
+                const std::int32_t s = q - pt.base[it.l];
+                it.s0 = pt.sub_ptr[it.l][s];
+                it.dim = 3 * (pt.sub_ptr[it.l][s + 1] - it.s0);
+            }
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                const int j = hl + 16 * t;
+                bb[t] = j < it.dim ? ldg_issue(pt.rin[it.l] + row_index(it, j)) : 0.0;
+            }
+        };
+        const int npairs = (nloc + 1) / 2;
+        Item cur{0, 0, 0};
+        double b[T];
+        if (w < npairs) load_b(2 * w + half, cur, b);
+        for (int pi = w; pi < npairs; pi += kCons) {
+            const int i = 2 * pi + half;  // this half's item
+#pragma unroll
+            for (int t = 0; t < T; ++t) bs[hl + 16 * t] = b[t];
+            Item nxt{0, 0, 0};
+            double bn[T];
+            if (pi + kCons < npairs) load_b(2 * (pi + kCons) + half, nxt, bn);
+            __syncwarp();
+            const bool have = i < nloc;
+            const int sl = i % kSlots;
+            if (have) mbar_wait(&full[sl], static_cast<std::uint32_t>(i / kSlots) & 1u);
+            __syncwarp();
+            const double* M = ring + static_cast<std::size_t>(have ? sl : (i - 1) % kSlots) * slot_doubles;
+            const int dmax = max(cur.dim, __shfl_xor_sync(0xffffffffu, cur.dim, 16));
+            const int kc = pick_cols<kK>(dmax);
+            double* out = pt.out[cur.l];
+            auto emit = [&](auto kc_tag) {
+                constexpr int K2 = decltype(kc_tag)::value;
+                constexpr int T2 = (K2 + 15) / 16;
+                double yy[T2];
+                packed_matvec_half<K2>(M, bs, yy, hl);
+#pragma unroll
+                for (int t = 0; t < T2; ++t) {
+                    const int j = hl + 16 * t;
+                    if (j < cur.dim) {
+                        out[row_index(cur, j)] = yy[t];
+                        dsum += bs[j] * yy[t];
+                    }
+                }
+            };
+            if (kK >= 48 && kc == 12)
+                emit(std::integral_constant<int, 12>{});
+            else if (kK >= 48 && kc == 24)
+                emit(std::integral_constant<int, 24>{});
+            else
+                emit(std::integral_constant<int, kK>{});
+            __syncwarp();
+            if (have && hl == 0) mbar_arrive(&empty[sl]);  // this half is done with its slot
+            cur = nxt;
+#pragma unroll
+            for (int t = 0; t < T; ++t) b[t] = bn[t];
+        }
     }
     grid_sum_last_block(dsum, partials, ticket, dot_out);
 }
@@ -1634,6 +1801,8 @@ void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, dou
     pt.n = static_cast<int>(c.levels.size());
     if (const char* e = std::getenv("ADIPC_DEBUG_PC_LEVELS")) pt.n = std::min(pt.n, std::max(1, std::atoi(e)));  // timing experiments only
     if (const char* e = std::getenv("ADIPC_DEBUG_PC_NOMATH")) pt.dbg_nomath = std::atoi(e);
+    pt.l0_keep = static_cast<std::int64_t>(c.levels[0]->inv_doubles * static_cast<double>(c.l0_keep_1024) / 1024.0);
+
     int fill = 1;
     for (int l = 0; l < pt.n; ++l) {
         const DeviceLevel& L = *c.levels[l];
@@ -1656,7 +1825,29 @@ void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, dou
     const std::size_t smem = per_pair * pairs;
     int sms = kSMs;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-    if (c.pc_variant == 2 && kk <= 48) {  // two items per warp (half-warps), one warp per CTA
+    if (c.pc_variant == 3 && kk <= 48) {  // warp-specialised: producer + consumers, CTA-wide ring
+        int sms = kSMs;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+#define ADIPC_WS(K, NS, NC)                                                                                   \
+    do {                                                                                                      \
+        const std::size_t smw = sizeof(double) * (static_cast<std::size_t>(NS) * slot + static_cast<std::size_t>(NC) * 2 * (K + 2)) + \
+                                sizeof(std::uint64_t) * 2 * NS;                                               \
+        ADIPC_CUDA(cudaFuncSetAttribute(k_precond_ws<K, NS, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        static_cast<int>(smw)));                                              \
+        k_precond_ws<K, NS, NC><<<sms, 32 * (NC + 1), smw, c.stream>>>(pt, partials, ticket, dot, flags, slot); \
+    } while (0)
+        if (kk == 24)
+            ADIPC_WS(24, 22, 8);
+        else if (c.ws_cons == 4)
+            ADIPC_WS(48, 22, 4);
+        else if (c.ws_cons == 6)
+            ADIPC_WS(48, 22, 6);
+        else if (c.ws_cons == 10)
+            ADIPC_WS(48, 22, 10);
+        else
+            ADIPC_WS(48, 22, 8);
+#undef ADIPC_WS
+    } else if (c.pc_variant == 2 && kk <= 48) {  // two items per warp (half-warps), one warp per CTA
         constexpr int wpc = 1;
         const std::size_t per_warp = (sizeof(double) * 2 * slot + sizeof(std::uint64_t)) * stages +
                                      sizeof(double) * 2 * (kk + 2);

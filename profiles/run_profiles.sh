@@ -13,9 +13,9 @@ CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $CMD \
     > $OUT/ncu_launch_$TAG.log 2>&1
 echo "launch list rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:'k_spmv|k_mas_level|k_mas_final' -s 300 -c 8 \
+ncu --set full --clock-control none --import-source on -k regex:'k_spmv|k_update_so|k_precond_so|k_final_so' -s 300 -c 8 \
     -o $OUT/prof_pcg_$TAG -f $CMD > $OUT/ncu_pcg_$TAG.log 2>&1
 echo "ncu pcg rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:'k_restrict|k_invert|k_reduce_rows|k_row_scatter|k_sort_rows' \
+ncu --set full --clock-control none --import-source on -k regex:'k_restrict|k_invert|k_reduce_rows|k_row_scatter|k_sort_rows|k_permute_stream' \
     -c 8 -o $OUT/prof_build_$TAG -f $CMD > $OUT/ncu_build_$TAG.log 2>&1
 echo "ncu build rc=$?"

@@ -88,6 +88,9 @@ int adipc_gpu_create(int device, adipc_gpu_ctx** out) {
         env_int("ADIPC_PC_PAIRS", 1, 5, ctx->c.pc_pairs);
         env_int("ADIPC_WS_CONS", 4, 10, ctx->c.ws_cons);
         env_int("ADIPC_L0_KEEP", 0, 1024, ctx->c.l0_keep_1024);
+        int iw = 1;
+        env_int("ADIPC_INVERT_WARP", 0, 1, iw);
+        ctx->c.invert_warp = iw != 0;
     });
     if (rc != ADIPC_OK) {
         g_global_err = ctx->c.err;

@@ -178,6 +178,171 @@ __global__ void k_invert(std::int32_t n_parts, const std::int32_t* __restrict__ 
     }
 }
 
+// Warp-per-subdomain variant of k_invert for dim <= 32 R (R rows per lane),
+// same semantics (Cholesky with the mas.hpp:66-81 retry rule, explicit
+// inverse L^-T L^-1 written symmetric-packed). Warp-synchronous: lanes own
+// rows in the factorisation (lane i updates row i of the trailing matrix),
+// columns of W = L^-1 in the triangular inversion (row by row), and columns
+// j of the product W^T W (one packed column k at a time) — no block barriers
+// and no index divisions. Per warp in shared memory: S (dim x dim, column
+// major; L in its lower triangle, W^T in its strict upper one) + diag(W).
+template <int R>
+__global__ void __launch_bounds__(128) k_invert_warp(std::int32_t n_parts, const std::int32_t* __restrict__ sub_ptr,
+                                                    const std::int64_t* __restrict__ dense_off,
+                                                    const double* __restrict__ dense,
+                                                    const std::int64_t* __restrict__ inv_off, double* __restrict__ inv,
+                                                    int* __restrict__ status, int* __restrict__ shifts, int max_dim) {
+    extern __shared__ double sm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double* S = sm + static_cast<std::size_t>(w) * (max_dim * max_dim + max_dim);
+    double* dg = S + max_dim * max_dim;
+    for (std::int32_t s = blockIdx.x * nw + w; s < n_parts; s += gridDim.x * nw) {
+        const int d = 3 * (sub_ptr[s + 1] - sub_ptr[s]);
+        if (d == 0) continue;
+        const double* D = dense + dense_off[s];
+        double tr = 0;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            const int i = lane + 32 * t;
+            if (i < d) tr += D[static_cast<std::int64_t>(i) * d + i];
+        }
+        for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+        double eps0 = 1e-8 * tr / d;
+        if (!(eps0 > 0)) eps0 = 1e-12;
+        bool fail = true;
+        int attempt = 0;
+        for (; attempt < 4; ++attempt) {
+            // S = D + cumulative shifts eps, 100 eps, ... (mas.hpp:78-79)
+            for (int q = lane; q < d * d; q += 32) S[q] = D[q];
+            __syncwarp();
+            if (attempt > 0)
+                for (int i = lane; i < d; i += 32) {
+                    // the reference adds each shift to the diagonal in turn
+                    double x = S[i * d + i], ee = eps0;
+                    for (int a = 0; a < attempt; ++a) {
+                        x += ee;
+                        ee *= 100;
+                    }
+                    S[i * d + i] = x;
+                }
+            __syncwarp();
+            fail = false;
+            for (int k = 0; k < d; ++k) {
+                const double x = S[k * d + k];
+                if (x <= 0) {  // Eigen LLT: a non-positive pivot fails; NaN does not
+                    fail = true;
+                    break;
+                }
+                const double piv = sqrt(x);
+                __syncwarp();
+                if (lane == 0) S[k * d + k] = piv;
+#pragma unroll
+                for (int t = 0; t < R; ++t) {
+                    const int i = lane + 32 * t;
+                    if (i > k && i < d) S[k * d + i] /= piv;
+                }
+                __syncwarp();
+                // trailing update, uniform over j (broadcast L(j,k), rows i
+                // contiguous across lanes): S(i,j) -= L(i,k) L(j,k), k < j <= i
+                double lik[R];
+#pragma unroll
+                for (int t = 0; t < R; ++t) {
+                    const int i = lane + 32 * t;
+                    lik[t] = (i > k && i < d) ? S[k * d + i] : 0.0;
+                }
+#pragma unroll 4
+                for (int j = k + 1; j < d; ++j) {
+                    const double ljk = S[k * d + j];
+#pragma unroll
+                    for (int t = 0; t < R; ++t) {
+                        const int i = lane + 32 * t;
+                        if (i >= j && i < d) S[j * d + i] -= lik[t] * ljk;
+                    }
+                }
+                __syncwarp();
+            }
+            if (!fail) break;
+        }
+        if (fail) {
+            if (lane == 0) atomicOr(status, 1);
+            __syncwarp();
+            continue;
+        }
+        if (lane == 0 && attempt > 0) atomicAdd(shifts, attempt);
+        // W = L^-1 row by row; lane c owns column c (W(k,c), k > c, at S[k*d + c]; W(c,c) in dg)
+        for (int i = 0; i < d; ++i) {
+            const double lii = S[i * d + i];
+            double a0[R], a1[R];
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+                const int c = lane + 32 * t;
+                // k = c term (diagonal of W) first, then the uniform k loop
+                a0[t] = (c == i) ? 1.0 : ((c < i && c < d) ? -S[c * d + i] * dg[c] : 0.0);
+                a1[t] = 0.0;
+            }
+#pragma unroll 4
+            for (int k = 0; k < i; ++k) {
+                const double lik = S[k * d + i];  // broadcast
+#pragma unroll
+                for (int t = 0; t < R; ++t) {
+                    const int c = lane + 32 * t;
+                    if (c < k) {
+                        if (k & 1)
+                            a1[t] -= lik * S[k * d + c];
+                        else
+                            a0[t] -= lik * S[k * d + c];
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+                const int c = lane + 32 * t;
+                if (c <= i && c < d) {
+                    const double wic = (a0[t] + a1[t]) / lii;
+                    if (c == i)
+                        dg[c] = wic;
+                    else
+                        S[i * d + c] = wic;
+                }
+            }
+            __syncwarp();
+        }
+        // D^-1 = W^T W: packed column k, lanes j <= k: sum_{q >= k} W(q,j) W(q,k)
+        double* P = inv + inv_off[s];
+        for (int k = 0; k < d; ++k) {
+            double v0[R], v1[R];
+            const double wkk = dg[k];
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+                const int j = lane + 32 * t;  // q = k term
+                v0[t] = j < k ? S[k * d + j] * wkk : (j == k ? wkk * wkk : 0.0);
+                v1[t] = 0.0;
+            }
+#pragma unroll 4
+            for (int q = k + 1; q < d; ++q) {
+                const double wqk = S[q * d + k];  // broadcast
+#pragma unroll
+                for (int t = 0; t < R; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j <= k) {
+                        const double wqj = j == k ? wqk : S[q * d + j];
+                        if (q & 1)
+                            v1[t] += wqj * wqk;
+                        else
+                            v0[t] += wqj * wqk;
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+                const int j = lane + 32 * t;
+                if (j <= k) P[k * (k + 1) / 2 + j] = v0[t] + v1[t];
+            }
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void k_jacobi_build(std::int32_t n, const std::uint32_t* __restrict__ cols, const double* __restrict__ blocks,
                                std::int64_t U, const std::int64_t* __restrict__ row_ptr, double* __restrict__ jinv) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -398,6 +563,24 @@ void factorize(Ctx& c) {
         DeviceLevel& L = *Lp;
         if (L.n_parts == 0) continue;
         const int dim = 3 * L.max_fill;
+        if (dim <= 64 && c.invert_warp) {  // warp per subdomain (k_invert_warp)
+            const int nw = 4;
+            const std::size_t wsm = sizeof(double) * nw * (static_cast<std::size_t>(dim) * dim + dim);
+            int sms = kSMs;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+            const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(L.n_parts, nw), sms * 8)));
+            if (dim <= 32) {
+                ADIPC_CUDA(cudaFuncSetAttribute(k_invert_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
+                k_invert_warp<1><<<grid, 32 * nw, wsm, st>>>(L.n_parts, L.sub_ptr.p, L.dense_off.p, L.dense.p, L.inv_off.p,
+                                                          L.inv.p, c.build_status.p, c.build_status.p + 1, dim);
+            } else {
+                ADIPC_CUDA(cudaFuncSetAttribute(k_invert_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
+                k_invert_warp<2><<<grid, 32 * nw, wsm, st>>>(L.n_parts, L.sub_ptr.p, L.dense_off.p, L.dense.p, L.inv_off.p,
+                                                          L.inv.p, c.build_status.p, c.build_status.p + 1, dim);
+            }
+            ADIPC_LAUNCH_CHECK();
+            continue;
+        }
         const std::size_t need = 2 * sizeof(double) * dim * dim;
         const bool in_smem = need <= 200 * 1024;
         const int threads = dim <= 48 ? 128 : 256;

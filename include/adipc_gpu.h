@@ -139,6 +139,8 @@ int adipc_gpu_spmv_device(adipc_gpu_ctx* ctx, const double* d_x, double* d_y);
 /* profiling aid: ms per SpMV launch of a variant (0 normal, 1 no transposed
  * scatter, 2 no atomics, 3 no column gather; 1-3 give wrong y) */
 int adipc_gpu_debug_spmv_time(adipc_gpu_ctx* ctx, const double* d_x, double* d_y, int mode, int iters, float* ms);
+/* profiling aid: (re)build the sliced-ELL SpMV copy from the current matrix */
+int adipc_gpu_debug_build_sell(adipc_gpu_ctx* ctx);
 
 /* ---- partition / hierarchy (host-side integer code, no GPU needed) ---------------- */
 int32_t adipc_subdomain_count(int32_t v, int32_t n, int32_t n_o);              /* partition.hpp:12-15 */

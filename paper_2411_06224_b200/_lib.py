@@ -60,6 +60,7 @@ GPU_SIGNATURES = {
     "adipc_gpu_spmv": (ci, [vp, vp, vp]),
     "adipc_gpu_spmv_device": (ci, [vp, vp, vp]),
     "adipc_gpu_debug_spmv_time": (ci, [vp, vp, vp, ci, ci, C.POINTER(C.c_float)]),
+    "adipc_gpu_debug_build_sell": (ci, [vp]),
     "adipc_subdomain_count": (i32, [i32, i32, i32]),
     "adipc_chunk_partition": (i32, [i32, i32, vp]),
     "adipc_partition_block_graph": (i32, [i32, vp, i64, i32, vp]),

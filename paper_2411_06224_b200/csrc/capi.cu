@@ -91,6 +91,9 @@ int adipc_gpu_create(int device, adipc_gpu_ctx** out) {
         int iw = 1;
         env_int("ADIPC_INVERT_WARP", 0, 1, iw);
         ctx->c.invert_warp = iw != 0;
+        int pp = 0;
+        env_int("ADIPC_PAD_P", 0, 1, pp);
+        ctx->c.pad_p = pp != 0;
     });
     if (rc != ADIPC_OK) {
         g_global_err = ctx->c.err;
@@ -147,6 +150,11 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.levels.clear();
     c.jinv.free();
     c.build_status.free();
+    c.sell.slice_off.free();
+    c.sell.row_id.free();
+    c.sell.cols.free();
+    c.sell.vals.free();
+    c.sell_len.free();
     c.perm.free();
     for (auto& e : c.splits) e.buf.free();
     c.splits.clear();
@@ -159,7 +167,7 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.As.cols.free();
     c.As.blocks.free();
     c.As.row_ptr.free();
-    for (auto* b : {&c.w.x, &c.w.r, &c.w.p, &c.w.ap, &c.w.z, &c.w.b, &c.w.tmp, &c.w.partials, &c.w.scal}) b->free();
+    for (auto* b : {&c.w.x, &c.w.r, &c.w.p, &c.w.p4, &c.w.ap, &c.w.z, &c.w.b, &c.w.tmp, &c.w.partials, &c.w.scal}) b->free();
     c.w.tickets.free();
     c.w.flags.free();
     c.w.counters.free();
@@ -207,7 +215,7 @@ int adipc_gpu_set_option(adipc_gpu_ctx* ctx, int option, int value) {
                 ADIPC_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<std::size_t>(mx)));
             }
         } else if (option == ADIPC_OPT_SPMV_VARIANT) {
-            if (value != 0 && (value < 2 || value > 6)) throw StatusError(kInvalidArgument, "SpMV variant not in {0,2..6}");
+            if (value != 0 && (value < 2 || value > 8)) throw StatusError(kInvalidArgument, "SpMV variant not in {0,2..8}");
             ctx->c.spmv_variant = value;
         } else if (option == ADIPC_OPT_PC_PAIRS) {
             if (value < 1 || value > 5) throw StatusError(kInvalidArgument, "pairs per CTA not in 1..5");
@@ -496,6 +504,10 @@ namespace adipc_gpu {
 float spmv_debug_time(Ctx& c, const double* d_x, double* d_y, int mode, int iters);
 }
 extern "C" {
+int adipc_gpu_debug_build_sell(adipc_gpu_ctx* ctx) {
+    return guarded(ctx, [&] { build_sell(ctx->c); });
+}
+
 int adipc_gpu_debug_spmv_time(adipc_gpu_ctx* ctx, const double* d_x, double* d_y, int mode, int iters, float* ms) {
     return guarded(ctx, [&] { *ms = spmv_debug_time(ctx->c, d_x, d_y, mode, iters); });
 }

@@ -68,8 +68,23 @@ struct DeviceLevel {
 
 enum PrecondKind : int { kNone = 0, kMas = 1, kJacobi = 2 };
 
+// Sliced-ELL copy of A for the PCG SpMV (sell.cu): slices of 32 reference
+// rows (lane = row), slot s = block s of each lane's row in the 32-block SoA
+// tile format; row / column ids in the solve order when it is active.
+struct SellMatrix {
+    std::int32_t n = 0, n_slices = 0;
+    std::int64_t slots = 0;
+    DBuf<std::int64_t> slice_off;  // slice -> first slot (n_slices + 1)
+    DBuf<std::int32_t> row_id;     // 32 per slice, -1 past the last row
+    DBuf<std::uint32_t> cols;      // 32 per slot, 0xFFFFFFFF = padding
+    DBuf<double> vals;             // 288 per slot
+    std::uint64_t a_version = ~0ull, levels_version = ~0ull;
+    bool perm_active = false;
+};
+
 struct PcgWork {
     DBuf<double> x, r, p, ap, z, b, tmp;
+    DBuf<double> p4;             // p padded to 4 doubles per slot (256-bit SpMV gathers)
     DBuf<double> partials;       // per-CTA partial dots
     DBuf<unsigned> tickets;      // last-block-done counters
     DBuf<double> scal;           // device scalars (see pcg.cu)
@@ -112,6 +127,8 @@ struct Ctx {
     bool cache_hierarchy = false;   // reuse the hierarchy while the pattern is unchanged
 
     PcgWork w;
+    SellMatrix sell;
+    DBuf<std::int64_t> sell_len;
 
     // Solve order (MAS): the PCG and the preconditioner run on A renumbered so
     // that every level-0 subdomain is a contiguous slot range,
@@ -167,7 +184,9 @@ struct Ctx {
     int l0_keep_1024 = 0;          // consumer warps of the warp-specialised preconditioner (ADIPC_WS_CONS)
     // tile shapes of the streaming kernels (ADIPC_UPD_SUBS / ADIPC_FINAL_PER /
     // ADIPC_FINAL_BLOCK environment overrides, read at context creation)
-    int upd_subs = 64, final_per = 1, final_block = 256;        // warp pairs per CTA of k_precond_so (ADIPC_OPT_PC_PAIRS)
+    int upd_subs = 64, final_per = 1, final_block = 256;
+    bool pad_p = false;  // 4-double-per-slot copy of p for 256-bit SpMV gathers (ADIPC_PAD_P=1; measured: no gain)
+    double* p4_active = nullptr;  // the padded copy the current solve maintains (else null)        // warp pairs per CTA of k_precond_so (ADIPC_OPT_PC_PAIRS)
     bool pc_split = false;   // cost-weighted instead of equal-count work split  // preconditioner kernel: 0 warp pairs per item, 1 one warp per item (ADIPC_OPT_PC_VARIANT)
     bool so_kernels = true;
     // update + every MAS level + prolongation in one cooperative kernel per
@@ -217,7 +236,13 @@ std::int64_t two_level_abd_reduce(Ctx& c, const std::uint64_t* d_keys, const dou
 void spmv(Ctx& c, const double* d_x, double* d_y, double* d_pdot_partials, int n_partials);
 int spmv_grid(const Ctx& c, const DeviceMatrix& M);
 void spmv_launch(Ctx& c, const DeviceMatrix& M, const double* d_x, double* d_y, bool zero_y, const int* flags,
-                 double* partials, unsigned* ticket, double* dot_out);
+                 double* partials, unsigned* ticket, double* dot_out, bool pad = false);
+
+// sell.cu
+void build_sell(Ctx& c);
+bool sell_current(const Ctx& c);
+void sell_spmv_launch(Ctx& c, const double* d_x, double* d_y, const int* flags, double* partials, unsigned* ticket,
+                      double* dot_out);
 
 // mas.cu
 void build_preconditioner(Ctx& c, PrecondKind kind);

@@ -50,6 +50,7 @@ void clear_restrict_so(Ctx& c);
 bool pcg_persistent(Ctx& c, const PcgArgs& a, double* partials, int restart, int max_iters);
 bool iter_so_supported(const Ctx& c);
 void prepare_work_splits(Ctx& c);
+void pad4(Ctx& c, const double* p, double* p4);
 void launch_iter_so(Ctx& c, const PcgArgs& a, bool restart, unsigned* counters, double* partials);
 
 namespace {
@@ -111,6 +112,12 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     if (so) pmax = std::max(pmax, so_partials(c));
     const bool fused = so && iter_so_supported(c);  // one kernel after the SpMV per iteration
     if (so) prepare_work_splits(c);  // byte-balanced splits, before any graph capture
+    if (c.spmv_variant == 8 && !sell_current(c)) build_sell(c);  // sliced-ELL SpMV copy, before capture
+    // p padded to 4 doubles per slot for the SpMV's 256-bit gathers (the
+    // solve-order prolongation kernel keeps it current)
+    const bool pad = so && !fused && c.pad_p;
+    if (pad) w.p4.reserve(4 * static_cast<std::size_t>(n));
+    c.p4_active = pad ? w.p4.p : nullptr;
     w.partials.reserve(static_cast<std::size_t>(pmax) * T_COUNT);
     w.tickets.reserve(T_COUNT);
     w.scal.reserve(S_COUNT);
@@ -188,6 +195,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     }
     launch_final<F_PCG_INIT>(c, w.z.p, w.p.p, w.ap.p, a);
     if (so) clear_restrict_so(c);
+    if (pad) pad4(c, w.p.p, w.p4.p);
     if (fused) {
         w.counters.reserve(2);
         ADIPC_CUDA(cudaMemsetAsync(w.counters.p, 0, 2 * sizeof(unsigned), st));
@@ -212,7 +220,8 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     // one iteration's launch sequence (restart variant: x += alpha p, r = b - A x)
     auto iteration = [&](bool is_restart, int slot) {
         mark(slot, 0);
-        spmv_launch(c, c.S(), w.p.p, w.ap.p, false, w.flags.p, partials_of(T_SPMV), w.tickets.p + T_SPMV, w.scal.p + S_PAP);
+        spmv_launch(c, c.S(), pad ? w.p4.p : w.p.p, w.ap.p, false, w.flags.p, partials_of(T_SPMV),
+                    w.tickets.p + T_SPMV, w.scal.p + S_PAP, pad);
         mark(slot, 1);
         if (is_restart) {
             k_x_update<<<slot_grid(c), 256, 0, st>>>(n3, a);
@@ -353,6 +362,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
         out.rel_residual = std::sqrt(std::fabs(rho) / h_scal[S_RHO_INIT]);
     }
     c.last_iters = out.iters;
+    c.p4_active = nullptr;
     if (persist && prof) c.prof_iters = out.iters;
     return out;
 }

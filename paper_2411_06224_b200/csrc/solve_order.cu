@@ -311,6 +311,7 @@ struct FinalSo {
     double* clear[kMaxLevels];               // RED targets of k_update_so (levels >= 2)
     std::int64_t clear_n[kMaxLevels];
     int n_clear;
+    double* p4;                              // optional copy of p padded to 4 doubles per slot
 };
 
 template <int kFinal, int kPer>
@@ -348,41 +349,82 @@ __global__ void __launch_bounds__(512) k_final_so(std::int32_t n, FinalSo fa, co
         if (rz <= stop) return;
         beta = rz / rho;
     }
-    // kPer slots per thread (strided by the grid), every load issued up front
+    // two slots (6 doubles, three 128-bit accesses per vector) per thread
     const std::int64_t nthreads = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-    std::int32_t nd[kPer][kMaxLevels];
-    double zz[kPer][3], pp[kPer][3];
+    (void)kPer;
+    for (std::int64_t pr = tid; 2 * pr < n; pr += nthreads) {
+        const std::int64_t sl0 = 2 * pr;
+        const bool two = sl0 + 1 < n;
+        std::int32_t nd[kMaxLevels][2];
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-        const std::int64_t sl = tid + u * nthreads;
-        if (sl < n) {
-#pragma unroll
-            for (int l = 0; l < kMaxLevels; ++l)
-                if (l < fa.n_coarse) nd[u][l] = fa.agg[l][sl];
+        for (int l = 0; l < kMaxLevels; ++l)
+            if (l < fa.n_coarse) {
+                if (two) {
+                    const int2 v = *reinterpret_cast<const int2*>(fa.agg[l] + sl0);
+                    nd[l][0] = v.x;
+                    nd[l][1] = v.y;
+                } else {
+                    nd[l][0] = fa.agg[l][sl0];
+                    nd[l][1] = nd[l][0];
+                }
+            }
+        double zz[6], pp[6];
+        if (two) {
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                zz[u][q] = z[3 * sl + q];
-                pp[u][q] = kFinal != F_PCG_INIT ? p[3 * sl + q] : 0.0;
+                const double2 zv = reinterpret_cast<const double2*>(z)[3 * pr + q];
+                zz[2 * q] = zv.x;
+                zz[2 * q + 1] = zv.y;
+                if (kFinal != F_PCG_INIT) {
+                    const double2 pv = reinterpret_cast<const double2*>(p)[3 * pr + q];
+                    pp[2 * q] = pv.x;
+                    pp[2 * q + 1] = pv.y;
+                } else {
+                    pp[2 * q] = pp[2 * q + 1] = 0.0;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                zz[q] = z[3 * sl0 + q];
+                pp[q] = kFinal != F_PCG_INIT ? p[3 * sl0 + q] : 0.0;
+                zz[3 + q] = pp[3 + q] = 0.0;
             }
         }
-    }
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-        const std::int64_t sl = tid + u * nthreads;
-        if (sl < n) {
+        for (int l = 0; l < kMaxLevels; ++l)
+            if (l < fa.n_coarse) {
 #pragma unroll
-            for (int l = 0; l < kMaxLevels; ++l)
-                if (l < fa.n_coarse) {
-                    const double* yl = fa.y[l] + 3 * static_cast<std::int64_t>(nd[u][l]);
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) zz[u][q] += yl[q];
+                for (int u = 0; u < 2; ++u) {
+                    const double* yl = fa.y[l] + 3 * static_cast<std::int64_t>(nd[l][u]);
+                    zz[3 * u] += yl[0];
+                    zz[3 * u + 1] += yl[1];
+                    zz[3 * u + 2] += yl[2];
                 }
+            }
+        double pn[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) pn[q] = zz[q] + beta * pp[q];
+        if (two) {
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                p[3 * sl + q] = zz[u][q] + beta * pp[u][q];
-                ap[3 * sl + q] = 0.0;
+                reinterpret_cast<double2*>(p)[3 * pr + q] = make_double2(pn[2 * q], pn[2 * q + 1]);
+                reinterpret_cast<double2*>(ap)[3 * pr + q] = make_double2(0.0, 0.0);
             }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                p[3 * sl0 + q] = pn[q];
+                ap[3 * sl0 + q] = 0.0;
+            }
+        }
+        if (fa.p4) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                if (u == 0 || two)
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) fa.p4[4 * (sl0 + u) + q] = pn[3 * u + q];
         }
     }
     // clear the RED targets of the next update pass
@@ -1909,9 +1951,28 @@ int so_partials(const Ctx& c) {
     return kSMs * 8;
 }
 
+namespace {
+__global__ void k_pad4(std::int32_t n, const double* __restrict__ p, double* __restrict__ p4) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        p4[4 * i] = p[3 * i];
+        p4[4 * i + 1] = p[3 * i + 1];
+        p4[4 * i + 2] = p[3 * i + 2];
+        p4[4 * i + 3] = 0.0;
+    }
+}
+}  // namespace
+
+void pad4(Ctx& c, const double* p, double* p4) {
+    if (c.A.n == 0) return;
+    k_pad4<<<grid_for(c.A.n, 256, 8), 256, 0, c.stream>>>(c.A.n, p, p4);
+    ADIPC_LAUNCH_CHECK();
+}
+
 template <int kFinal>
 void launch_final_so(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a) {
     FinalSo fa{};
+    fa.p4 = c.p4_active;
     const int L = static_cast<int>(c.levels.size());
     fa.n_coarse = L - 1;
     for (int l = 1; l < L; ++l) {
@@ -1924,7 +1985,8 @@ void launch_final_so(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a)
         ++fa.n_clear;
     }
     const int per = c.final_per, block = c.final_block;
-    const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(c.A.n, static_cast<std::int64_t>(block) * per)));
+    const int grid = static_cast<int>(
+        std::max<std::int64_t>(1, ceil_div(ceil_div(c.A.n, 2), static_cast<std::int64_t>(block) * per)));
     if (per == 1)
         k_final_so<kFinal, 1><<<grid, block, 0, c.stream>>>(c.A.n, fa, z, p, ap, a);
     else if (per == 2)

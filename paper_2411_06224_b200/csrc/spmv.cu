@@ -19,7 +19,7 @@ namespace {
 
 constexpr int kSpmvThreads = 256;
 
-template <bool kDot>
+template <bool kDot, bool kPad = false, bool kCoalesce = false>
 __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __restrict__ rows,
                                                      const std::uint32_t* __restrict__ cols,
                                                      const double* __restrict__ blocks, std::int64_t U,
@@ -66,23 +66,56 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __re
         load(ch + 1);
         const bool valid = r != 0xFFFFFFFFu;
         double yr0 = 0, yr1 = 0, yr2 = 0;
+        double tc0 = 0, tc1 = 0, tc2 = 0;  // H^T x[row], towards y[col]
+        bool tr = false;
         if (valid) {
             const std::uint32_t cx = dbg == 3 ? r : c;  // dbg 3: no column gather
-            const double xc0 = ldg_issue(x + 3 * cx), xc1 = ldg_issue(x + 3 * cx + 1), xc2 = ldg_issue(x + 3 * cx + 2);
-            const double xr0 = ldg_issue(x + 3 * r), xr1 = ldg_issue(x + 3 * r + 1), xr2 = ldg_issue(x + 3 * r + 2);
+            double xc0, xc1, xc2, xr0, xr1, xr2;
+            if (kPad) {  // x padded to 4 doubles per slot: one 256-bit gather each
+                double u0, u1;
+                ldg_v4(x + 4 * static_cast<std::int64_t>(cx), xc0, xc1, xc2, u0);
+                ldg_v4(x + 4 * static_cast<std::int64_t>(r), xr0, xr1, xr2, u1);
+            } else {
+                xc0 = ldg_issue(x + 3 * cx);
+                xc1 = ldg_issue(x + 3 * cx + 1);
+                xc2 = ldg_issue(x + 3 * cx + 2);
+                xr0 = ldg_issue(x + 3 * r);
+                xr1 = ldg_issue(x + 3 * r + 1);
+                xr2 = ldg_issue(x + 3 * r + 2);
+            }
             // column-major H(i,j) = h[3j+i]
             yr0 = h[0] * xc0 + h[3] * xc1 + h[6] * xc2;
             yr1 = h[1] * xc0 + h[4] * xc1 + h[7] * xc2;
             yr2 = h[2] * xc0 + h[5] * xc1 + h[8] * xc2;
             if (r != c && dbg != 1 && dbg != 2) {
-                const double yc0 = h[0] * xr0 + h[1] * xr1 + h[2] * xr2;
-                const double yc1 = h[3] * xr0 + h[4] * xr1 + h[5] * xr2;
-                const double yc2 = h[6] * xr0 + h[7] * xr1 + h[8] * xr2;
-                red_add(y + 3 * c, yc0);
-                red_add(y + 3 * c + 1, yc1);
-                red_add(y + 3 * c + 2, yc2);
+                tc0 = h[0] * xr0 + h[1] * xr1 + h[2] * xr2;
+                tc1 = h[3] * xr0 + h[4] * xr1 + h[5] * xr2;
+                tc2 = h[6] * xr0 + h[7] * xr1 + h[8] * xr2;
+                tr = true;
+                if (!kCoalesce) {
+                    red_add(y + 3 * c, tc0);
+                    red_add(y + 3 * c + 1, tc1);
+                    red_add(y + 3 * c + 2, tc2);
+                }
             }
             if (kDot) dsum += (r != c ? 2.0 : 1.0) * (xr0 * yr0 + xr1 * yr1 + xr2 * yr2);
+        }
+        if (kCoalesce) {
+            // the 96 scatter values of the chunk (block b, component k) go out in
+            // three RED instructions, lane L of round I taking value 32 I + L:
+            // each instruction hits ~11 blocks' contiguous 24-byte targets
+            // instead of 32 scattered doubles
+#pragma unroll
+            for (int round = 0; round < 3; ++round) {
+                const int v = 32 * round + lane;
+                const int bsrc = v / 3, k = v - 3 * bsrc;
+                const double a0 = __shfl_sync(0xffffffffu, tc0, bsrc);
+                const double a1 = __shfl_sync(0xffffffffu, tc1, bsrc);
+                const double a2 = __shfl_sync(0xffffffffu, tc2, bsrc);
+                const std::uint32_t cb = __shfl_sync(0xffffffffu, c, bsrc);
+                const bool tb = __shfl_sync(0xffffffffu, tr ? 1 : 0, bsrc) != 0;
+                if (tb) red_add(y + 3 * static_cast<std::int64_t>(cb) + k, k == 0 ? a0 : (k == 1 ? a1 : a2));
+            }
         }
         // head-segmented sum of the row contributions (rows sorted within the warp)
 #pragma unroll
@@ -459,7 +492,7 @@ SpmvLaunch spmv_config(K kernel, int block, std::size_t smem, const Ctx& c, std:
 
 template <bool kDot>
 void launch_variant(Ctx& c, const DeviceMatrix& M, int variant, const double* d_x, double* d_y, double* partials,
-                    unsigned* ticket, double* dot_out, const int* flags, int dbg) {
+                    unsigned* ticket, double* dot_out, const int* flags, int dbg, bool pad = false) {
     cudaStream_t st = c.stream;
 #define ADIPC_TMA(S)                                                                                              \
     do {                                                                                                          \
@@ -500,7 +533,15 @@ void launch_variant(Ctx& c, const DeviceMatrix& M, int variant, const double* d_
             cfg = spmv_config(k_spmv<kDot>, kSpmvThreads, 0, c, M.U);
             cfg_u = M.U;
         }
-        k_spmv<kDot><<<cfg.grid, cfg.block, 0, st>>>(M.rows.p, M.cols.p, M.blocks.p, M.U, d_x, d_y, partials, ticket,
+        if (pad)
+            k_spmv<kDot, true><<<cfg.grid, cfg.block, 0, st>>>(M.rows.p, M.cols.p, M.blocks.p, M.U, d_x, d_y, partials,
+                                                               ticket, dot_out, flags, dbg, c.l2_persist_1024);
+        else if (variant == 7)
+            k_spmv<kDot, false, true><<<cfg.grid, cfg.block, 0, st>>>(M.rows.p, M.cols.p, M.blocks.p, M.U, d_x, d_y,
+                                                                      partials, ticket, dot_out, flags, dbg,
+                                                                      c.l2_persist_1024);
+        else
+            k_spmv<kDot><<<cfg.grid, cfg.block, 0, st>>>(M.rows.p, M.cols.p, M.blocks.p, M.U, d_x, d_y, partials, ticket,
                                                      dot_out, flags, dbg, c.l2_persist_1024);
     }
 #undef ADIPC_TMA
@@ -521,17 +562,21 @@ int spmv_grid(const Ctx& c, const DeviceMatrix& M) {
 // (>= spmv_grid doubles) and `ticket` (one zeroed unsigned). `flags`: skip
 // when the PCG solve is done.
 void spmv_launch(Ctx& c, const DeviceMatrix& M, const double* d_x, double* d_y, bool zero_y, const int* flags,
-                 double* partials, unsigned* ticket, double* dot_out) {
+                 double* partials, unsigned* ticket, double* dot_out, bool pad) {
     const std::int64_t nx3 = 3 * static_cast<std::int64_t>(M.n);
     if (zero_y) ADIPC_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * nx3, c.stream));
     if (M.U == 0) {
         if (dot_out) ADIPC_CUDA(cudaMemsetAsync(dot_out, 0, sizeof(double), c.stream));
         return;
     }
+    if (c.spmv_variant == 8 && &M == &c.S() && sell_current(c)) {  // sliced-ELL copy (sell.cu)
+        sell_spmv_launch(c, d_x, d_y, flags, partials, ticket, dot_out);
+        return;
+    }
     if (dot_out)
-        launch_variant<true>(c, M, c.spmv_variant, d_x, d_y, partials, ticket, dot_out, flags, 0);
+        launch_variant<true>(c, M, pad ? 0 : c.spmv_variant, d_x, d_y, partials, ticket, dot_out, flags, 0, pad);
     else
-        launch_variant<false>(c, M, c.spmv_variant, d_x, d_y, nullptr, nullptr, nullptr, flags, 0);
+        launch_variant<false>(c, M, pad ? 0 : c.spmv_variant, d_x, d_y, nullptr, nullptr, nullptr, flags, 0, pad);
 }
 
 // Debug timing of the SpMV variants: mode & 7 = 0 normal, 1 no transposed
@@ -569,7 +614,10 @@ float spmv_debug_time(Ctx& c, const double* d_x, double* d_y, int mode, int iter
     for (int i = -2; i < iters; ++i) {
         if (cold) ADIPC_CUDA(cudaMemsetAsync(flush.p, i & 0xff, 256u << 20, c.stream));
         ADIPC_CUDA(cudaEventRecord(e0, c.stream));
-        if (dot)
+        if (variant == 8)  // the sliced-ELL copy as built (c.sell)
+            sell_spmv_launch(c, d_x, d_y, nullptr, dot ? dpart.p : nullptr, dot ? dtick.p : nullptr,
+                             dot ? dpart.p + spmv_grid(c, M) : nullptr);
+        else if (dot)
             launch_variant<true>(c, M, variant, d_x, d_y, dpart.p, dtick.p, dpart.p + spmv_grid(c, M), nullptr, mode);
         else
             launch_variant<false>(c, M, variant, d_x, d_y, nullptr, nullptr, nullptr, nullptr, mode);

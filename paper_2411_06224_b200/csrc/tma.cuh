@@ -100,6 +100,11 @@ __device__ __forceinline__ void red_add(double* ptr, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(ptr), "d"(v));
 }
 
+// 256-bit read-only gather (sm_100: LDG.E.256) of a slot padded to 4 doubles
+__device__ __forceinline__ void ldg_v4(const double* ptr, double& a, double& b, double& c, double& d) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(ptr));
+}
+
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
     std::uint32_t done;
     do {

@@ -23,6 +23,8 @@ VARIANTS = {
     "generic-kernels": {_lib.OPT_SO_KERNELS: 0},
     "spmv-tma3": {_lib.OPT_SPMV_VARIANT: 3},
     "spmv-tma-2blk": {_lib.OPT_SPMV_VARIANT: 5},
+    "spmv-tma-coalesced-red": {_lib.OPT_SPMV_VARIANT: 7},
+    "spmv-sliced-ell": {_lib.OPT_SPMV_VARIANT: 8},
     "pc-stages3": {_lib.OPT_L0_STAGES: 3},
     "pc-1warp": {_lib.OPT_PC_VARIANT: 1},
     "pc-halfwarp": {_lib.OPT_PC_VARIANT: 2},

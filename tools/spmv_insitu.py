@@ -25,6 +25,8 @@ b = torch.from_numpy(scenes.gravity_rhs(sc)).cuda()
 x = torch.empty_like(b)
 out = {"n": n, "U": U}
 for variant in [int(a) for a in (sys.argv[1:] or ["0", "3"])]:
+    if variant == 8:  # sliced-ELL copy built from the current matrix (ADIPC_SELL_REF: reference order)
+        ctx.set_option(_lib.OPT_SPMV_VARIANT, 8)
     ctx.set_option(_lib.OPT_SPMV_VARIANT, variant)
     ctx.build_preconditioner(_lib.PRECOND_MAS)
     ctx.set_option(_lib.OPT_PROFILE, 1)
@@ -34,6 +36,8 @@ for variant in [int(a) for a in (sys.argv[1:] or ["0", "3"])]:
     it = max(prof["iters"], 1)
     out[f"v{variant}_pcg"] = {k: round(prof[k + "_ms"] / it * 1000, 1) for k in ("spmv", "update", "precond", "final")}
     L = _lib.gpu()
+    if variant == 8:
+        ctx._check(L.adipc_gpu_debug_build_sell(ctx.h))
     xr = torch.randn(3 * n, dtype=torch.float64, device="cuda")
     yr = torch.zeros_like(xr)
     for mode, name in ((256, "insitu_warm"), (256 | 8, "insitu_cold"), (256 | 512, "insitu_dot_warm"),

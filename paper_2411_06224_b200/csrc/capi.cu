@@ -91,6 +91,9 @@ int adipc_gpu_create(int device, adipc_gpu_ctx** out) {
         int iw = 1;
         env_int("ADIPC_INVERT_WARP", 0, 1, iw);
         ctx->c.invert_warp = iw != 0;
+        int pd = 1;
+        env_int("ADIPC_PDL", 0, 1, pd);
+        ctx->c.pdl = pd != 0;
         int pp = 0;
         env_int("ADIPC_PAD_P", 0, 1, pp);
         ctx->c.pad_p = pp != 0;

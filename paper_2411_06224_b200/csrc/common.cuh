@@ -35,6 +35,32 @@ long long& launch_counter();
 
 __host__ __device__ inline std::int64_t ceil_div(std::int64_t a, std::int64_t b) { return (a + b - 1) / b; }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// launch_pdl(..., pdl = true) may start while its predecessor in the stream
+// drains; it runs its independent prologue (constant data, shared-memory and
+// barrier setup, prefetches of operands that do not change during the solve)
+// and calls pdl_wait() before touching anything the predecessor writes.
+// pdl_launch() lets the successor's CTAs be scheduled. Both are no-ops for
+// ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t st,
+                              bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Grid size for grid-stride kernels: enough CTAs for every SM several times
 // over, never more than the work needs.
 inline int grid_for(std::int64_t work_items, int items_per_cta, int per_sm = 8) {

@@ -178,7 +178,11 @@ struct Ctx {
     int pc_variant = 0;
     int pc_pairs = 4;
     int ws_cons = 8;
-    bool invert_warp = true;  // warp-per-subdomain factorisation/inversion (ADIPC_INVERT_WARP=0: CTA kernel)
+    bool invert_warp = true;
+    // programmatic dependent launch between the PCG iteration's kernels
+    // (ADIPC_PDL=0 disables): each starts its independent prologue while the
+    // previous one drains
+    bool pdl = true;  // warp-per-subdomain factorisation/inversion (ADIPC_INVERT_WARP=0: CTA kernel)
     // share (x/1024) of the level-0 inverses streamed with L2 evict-last, so
     // they stay L2-resident from one PCG iteration to the next (ADIPC_L0_KEEP)
     int l0_keep_1024 = 0;          // consumer warps of the warp-specialised preconditioner (ADIPC_WS_CONS)

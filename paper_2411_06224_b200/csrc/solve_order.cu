@@ -132,8 +132,10 @@ template <int kMode>
 __global__ void __launch_bounds__(kUpdThreads) k_update_so(SoRestrict so, PcgArgs a) {
     extern __shared__ double sr[];
     double alpha = 0;
+    pdl_wait();
     if (a.flags[F_DONE]) return;
     if (!pcg_alpha(a, alpha)) return;
+    pdl_launch();
     update_tile<kMode, kUpdThreads>(so, a, alpha, a.ap, blockIdx.x, sr);
 }
 
@@ -174,7 +176,6 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
                                                    unsigned* __restrict__ ticket, double* __restrict__ dot_out,
                                                    const int* __restrict__ flags, int slot_doubles) {
     constexpr int RB = (kK + 31) / 32;  // b entries per lane
-    if (flags && flags[F_DONE]) return;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, pair = w >> 1, half = w & 1;
     const int npc = blockDim.x >> 6;
@@ -245,6 +246,15 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
         for (int st = 0; st < kStages && st < nloc; ++st) issue(item(st), st);
     }
     pair_sync(pair);
+    // the inverses are constant during the solve: the ring above fills while
+    // the predecessor (update pass) drains; its outputs are read from here on
+    pdl_wait();
+    if (flags && flags[F_DONE]) {  // PCG already finished: drain the issued copies, leave
+        if (half == 0 && lane == 0)
+            for (int st = 0; st < kStages && st < nloc; ++st) mbar_wait(&bar[st], 0);
+        return;
+    }
+    pdl_launch();
     // b of a work item and the addresses of its rows (gathered for coarse levels)
     struct Item {
         int l;
@@ -318,7 +328,9 @@ template <int kFinal, int kPer>
 __global__ void __launch_bounds__(512) k_final_so(std::int32_t n, FinalSo fa, const double* __restrict__ z,
                                                  double* __restrict__ p, double* __restrict__ ap, PcgArgs a) {
     double beta = 0;
+    pdl_wait();
     if (a.flags[F_DONE]) return;
+    pdl_launch();
     const double rz = a.scal[S_RZ];  // r.z = sum over all levels of b_l.y_l (k_precond_so)
     if (kFinal == F_PCG_INIT) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {  // pcg.hpp:52-57
@@ -1754,7 +1766,7 @@ void launch_update_so(Ctx& c, const PcgArgs& a) {
         ADIPC_CUDA(cudaFuncSetAttribute(k_update_so<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
         attr = true;
     }
-    k_update_so<kMode><<<grid, kUpdThreads, smem, c.stream>>>(so, a);
+    ADIPC_CUDA(launch_pdl(k_update_so<kMode>, dim3(grid), dim3(kUpdThreads), smem, c.stream, c.pdl, so, a));
     ADIPC_LAUNCH_CHECK();
 }
 template void launch_update_so<M_UPDATE>(Ctx&, const PcgArgs&);
@@ -1940,7 +1952,17 @@ void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, dou
         pt.split = c.pc_split ? work_split(c, pt.np) : nullptr;
         int slot_arg = L.slot;
         void* args[] = {&pt, &partials, &ticket, &dot, const_cast<int**>(&flags), &slot_arg};
-        ADIPC_CUDA(cudaLaunchKernel(L.fn, dim3(L.grid), dim3(64 * L.pairs), args, L.smem, c.stream));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(L.grid);
+        cfg.blockDim = dim3(64 * L.pairs);
+        cfg.dynamicSmemBytes = L.smem;
+        cfg.stream = c.stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = c.pdl ? 1 : 0;
+        ADIPC_CUDA(cudaLaunchKernelExC(&cfg, L.fn, args));
     }
     ADIPC_LAUNCH_CHECK();
 }
@@ -1988,7 +2010,7 @@ void launch_final_so(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a)
     const int grid = static_cast<int>(
         std::max<std::int64_t>(1, ceil_div(ceil_div(c.A.n, 2), static_cast<std::int64_t>(block) * per)));
     if (per == 1)
-        k_final_so<kFinal, 1><<<grid, block, 0, c.stream>>>(c.A.n, fa, z, p, ap, a);
+        ADIPC_CUDA(launch_pdl(k_final_so<kFinal, 1>, dim3(grid), dim3(block), 0, c.stream, c.pdl, c.A.n, fa, z, p, ap, a));
     else if (per == 2)
         k_final_so<kFinal, 2><<<grid, block, 0, c.stream>>>(c.A.n, fa, z, p, ap, a);
     else

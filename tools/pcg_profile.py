@@ -33,8 +33,13 @@ for spec in sys.argv[1:] or ["so=1"]:
     out = {"spec": spec}
     for prof in (0, 1):
         ctx.set_option(_lib.OPT_PROFILE, prof)
-        _, res = ctx.pcg(b, 1e-4, 250, 100000, x=x)
-        t = ctx.timings()
+        best = None
+        for _ in range(1 if prof else 3):  # graph mode: best of 3 solves
+            _, res = ctx.pcg(b, 1e-4, 250, 100000, x=x)
+            t = ctx.timings()
+            if best is None or t["pcg_ms"] < best[1]["pcg_ms"]:
+                best = (res, t)
+        res, t = best
         if prof:
             pr = ctx.pcg_profile()
             it = max(pr["iters"], 1)

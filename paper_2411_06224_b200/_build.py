@@ -56,7 +56,7 @@ def _compile(src: str, verbose: bool) -> str:
     if src.endswith(".cu"):
         cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-c", path, "-o", obj]
     else:
-        cmd = [CXX, *CXX_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", path, "-o", obj]
+        cmd = [CXX, *CXX_FLAGS, "-fopenmp", "-I", os.path.join(ROOT, "include"), "-c", path, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
@@ -68,7 +68,7 @@ def build(verbose: bool = False) -> None:
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), GPU_SOURCES))
     if _stale(GPU_LIB, objs):
-        cmd = [_nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", GPU_LIB, *objs]
+        cmd = [_nvcc(), *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fopenmp", "-lgomp", "-o", GPU_LIB, *objs]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)

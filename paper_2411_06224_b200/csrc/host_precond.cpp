@@ -2,6 +2,10 @@
 // compare every output array against the oracle restatement.
 #include "host_precond.hpp"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <cstring>
 
@@ -39,20 +43,21 @@ Graph build_graph(Index v, const Index* pairs, std::size_t n_edges) {  // partit
         g.adj[cur[a]++] = b;
         g.adj[cur[b]++] = a;
     }
-    // sort + unique each list, compacting in place
-    std::int64_t w = 0;
+    // sort + unique each list (in parallel), then compact in place
+    std::vector<std::int64_t> ulen(static_cast<std::size_t>(v));
+#pragma omp parallel for schedule(static, 4096)
     for (Index i = 0; i < v; ++i) {
         Index* beg = g.adj.data() + g.ptr[i];
         Index* end = g.adj.data() + g.ptr[i + 1];
         if (!std::is_sorted(beg, end)) std::sort(beg, end);
-        const std::int64_t start = w;
-        Index last = kInvalid;
-        for (Index* it = beg; it != end; ++it)
-            if (it == beg || *it != last) {
-                last = *it;
-                g.adj[w++] = *it;
-            }
-        g.ptr[i] = start;
+        ulen[i] = std::unique(beg, end) - beg;
+    }
+    std::int64_t w = 0;
+    for (Index i = 0; i < v; ++i) {
+        const std::int64_t b = g.ptr[i];
+        g.ptr[i] = w;
+        if (w != b) std::memmove(g.adj.data() + w, g.adj.data() + b, sizeof(Index) * ulen[i]);
+        w += ulen[i];
     }
     g.ptr[v] = w;
     g.adj.resize(w);
@@ -176,11 +181,15 @@ MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_
 
     std::vector<Index> cur_edges(pairs, pairs + 2 * n_edges);
     std::vector<Index> up, queue, members, mem_ptr;
-    std::vector<std::uint64_t> packed;
     while (h.n_levels() < max_levels) {
         const Level& cur = h.levels.back();
         if (cur.n_parts <= 1) break;
+        const bool dbg = std::getenv("ADIPC_DEBUG_HIER") != nullptr;
+        auto tnow = [] { return std::chrono::steady_clock::now(); };
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        const auto t0 = tnow();
         const Graph g = build_graph(cur.n_nodes, cur_edges.data(), cur_edges.size() / 2);
+        const auto t1 = tnow();
         // members of each subdomain in ascending node order (counting sort)
         mem_ptr.assign(static_cast<std::size_t>(cur.n_parts) + 1, 0);
         for (Index i = 0; i < cur.n_nodes; ++i) ++mem_ptr[cur.part_of[i] + 1];
@@ -190,52 +199,107 @@ MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_
             std::vector<Index> fill(mem_ptr.begin(), mem_ptr.end() - 1);
             for (Index i = 0; i < cur.n_nodes; ++i) members[fill[cur.part_of[i]]++] = i;
         }
+        // connected components inside each subdomain (hierarchy.hpp:53-72:
+        // seeds in ascending node order, neighbours in adjacency order),
+        // subdomains in parallel with local ids, then offset by a scan over
+        // the subdomains so the super-node ids are exactly the sequential ones
         up.assign(cur.n_nodes, kInvalid);
-        Index n_next = 0;
-        for (Index s = 0; s < cur.n_parts; ++s)
-            for (Index k = mem_ptr[s]; k < mem_ptr[s + 1]; ++k) {
-                const Index seed = members[k];
-                if (up[seed] != kInvalid) continue;
-                const Index super = n_next++;
-                up[seed] = super;
-                queue.assign(1, seed);
-                for (std::size_t head = 0; head < queue.size(); ++head) {
-                    const Index q = queue[head];
-                    for (std::int64_t e = g.ptr[q]; e < g.ptr[q + 1]; ++e) {
-                        const Index nb = g.adj[e];
-                        if (cur.part_of[nb] == s && up[nb] == kInvalid) {
-                            up[nb] = super;
-                            queue.push_back(nb);
+        std::vector<Index> ncomp(static_cast<std::size_t>(cur.n_parts) + 1, 0);
+#pragma omp parallel
+        {
+            std::vector<Index> q;
+#pragma omp for schedule(dynamic, 256)
+            for (Index s = 0; s < cur.n_parts; ++s) {
+                Index local = 0;
+                for (Index k = mem_ptr[s]; k < mem_ptr[s + 1]; ++k) {
+                    const Index seed = members[k];
+                    if (up[seed] != kInvalid) continue;
+                    const Index super = local++;
+                    up[seed] = super;
+                    q.assign(1, seed);
+                    for (std::size_t head = 0; head < q.size(); ++head) {
+                        const Index qq = q[head];
+                        for (std::int64_t e = g.ptr[qq]; e < g.ptr[qq + 1]; ++e) {
+                            const Index nb = g.adj[e];
+                            if (cur.part_of[nb] == s && up[nb] == kInvalid) {
+                                up[nb] = super;
+                                q.push_back(nb);
+                            }
                         }
                     }
                 }
+                ncomp[s + 1] = local;
             }
+        }
+        for (Index s = 0; s < cur.n_parts; ++s) ncomp[s + 1] += ncomp[s];
+        const Index n_next = ncomp[cur.n_parts];
+#pragma omp parallel for schedule(static, 4096)
+        for (Index i = 0; i < cur.n_nodes; ++i) up[i] += ncomp[cur.part_of[i]];
+        const auto t2 = tnow();
         if (n_next == cur.n_nodes) break;
-        packed.clear();
-        packed.reserve(cur_edges.size() / 2);
-        for (std::size_t e = 0; e + 1 < cur_edges.size(); e += 2) {
-            Index ua = up[cur_edges[e]], ub = up[cur_edges[e + 1]];
-            if (ua == ub) continue;
-            if (ua > ub) std::swap(ua, ub);
-            packed.push_back((static_cast<std::uint64_t>(static_cast<std::uint32_t>(ua)) << 32) |
-                             static_cast<std::uint32_t>(ub));
+        // coarse edges (hierarchy.hpp:75-85: mapped, deduplicated, sorted):
+        // per super node U the sorted unique super neighbours V > U of its
+        // members, concatenated in U order — the sorted unique (U, V) list,
+        // built in parallel over super nodes
+        std::vector<Index> sptr(static_cast<std::size_t>(n_next) + 1, 0), smem(cur.n_nodes);
+        for (Index i = 0; i < cur.n_nodes; ++i) ++sptr[up[i] + 1];
+        for (Index u = 0; u < n_next; ++u) sptr[u + 1] += sptr[u];
+        {
+            std::vector<Index> fill(sptr.begin(), sptr.end() - 1);
+            for (Index i = 0; i < cur.n_nodes; ++i) smem[fill[up[i]]++] = i;
         }
-        std::sort(packed.begin(), packed.end());
-        packed.erase(std::unique(packed.begin(), packed.end()), packed.end());
-        std::vector<Index> next_edges(2 * packed.size());
-        for (std::size_t e = 0; e < packed.size(); ++e) {
-            next_edges[2 * e] = static_cast<Index>(packed[e] >> 32);
-            next_edges[2 * e + 1] = static_cast<Index>(packed[e] & 0xFFFFFFFFu);
+        std::vector<std::int64_t> ecnt(static_cast<std::size_t>(n_next) + 1, 0);
+        auto neighbours = [&](Index u, std::vector<Index>& out) {
+            out.clear();
+            for (Index k = sptr[u]; k < sptr[u + 1]; ++k) {
+                const Index m = smem[k];
+                for (std::int64_t e = g.ptr[m]; e < g.ptr[m + 1]; ++e) {
+                    const Index v = up[g.adj[e]];
+                    if (v > u) out.push_back(v);
+                }
+            }
+            std::sort(out.begin(), out.end());
+            out.erase(std::unique(out.begin(), out.end()), out.end());
+        };
+#pragma omp parallel
+        {
+            std::vector<Index> nbr;
+#pragma omp for schedule(dynamic, 512)
+            for (Index u = 0; u < n_next; ++u) {
+                neighbours(u, nbr);
+                ecnt[u + 1] = static_cast<std::int64_t>(nbr.size());
+            }
         }
+        for (Index u = 0; u < n_next; ++u) ecnt[u + 1] += ecnt[u];
+        const auto t3 = tnow();
+        std::vector<Index> next_edges(2 * static_cast<std::size_t>(ecnt[n_next]));
+#pragma omp parallel
+        {
+            std::vector<Index> nbr;
+#pragma omp for schedule(dynamic, 512)
+            for (Index u = 0; u < n_next; ++u) {
+                neighbours(u, nbr);
+                std::int64_t o = ecnt[u];
+                for (const Index v : nbr) {
+                    next_edges[2 * o] = u;
+                    next_edges[2 * o + 1] = v;
+                    ++o;
+                }
+            }
+        }
+        const std::size_t n_coarse_edges = static_cast<std::size_t>(ecnt[n_next]);
         Level next;
         next.n_nodes = n_next;
-        Partition grouped = partition_block_graph(n_next, next_edges.data(), packed.size(), h.capacity);
+        Partition grouped = partition_block_graph(n_next, next_edges.data(), n_coarse_edges, h.capacity);
         next.n_parts = grouped.n_parts;
         next.part_of = std::move(grouped.part_of);
         next.agg.resize(h.n_slots);
         for (Index slot = 0; slot < h.n_slots; ++slot) next.agg[slot] = up[cur.agg[slot]];
         h.levels.push_back(std::move(next));
         cur_edges = std::move(next_edges);
+        if (dbg)
+            std::fprintf(stderr, "hierarchy level %d: graph %.1f ms, bfs %.1f ms, edges sort %.1f ms, partition %.1f ms\n",
+                         h.n_levels() - 1, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, tnow()));
     }
     return h;
 }

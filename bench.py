@@ -380,6 +380,14 @@ def run_ours(args, rank, world, local_rank, dist):
             "roofline_pcg_iteration": {"bound": "hbm", "bytes_per_iter": bm["total"],
                                        "achieved": bm["total"] / iter_s / 1e9, "peak": hbm, "unit": "GB/s",
                                        "frac": bm["total"] / iter_s / 1e9 / hbm},
+            # context for the fractions above: the read bandwidth ONE kernel of
+            # this size reaches on this B200 with a cold L2 and no compute
+            # (tools/stream_read_bench.cu; profiles/r01f_summary.md): 50 MB
+            # 3.2 TB/s, 200 MB 4.65, 2 GB 6.65 — the copy peak needs GB-size
+            # transfers that the iteration's 36-223 MB kernels do not make
+            "roofline_practical": {"unit": "GB/s", "single_kernel_read_200MB": 4650.0,
+                                   "dominant_kernel_frac": kernels[dom]["achieved_gbs"] / 4650.0,
+                                   "source": "tools/stream_read_bench.cu"},
             "clocks": clk.summary(),
         }
     # e2e through the host-pointer C-ABI (pinned host buffers)

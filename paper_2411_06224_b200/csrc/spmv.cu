@@ -18,9 +18,13 @@ namespace adipc_gpu {
 namespace {
 
 constexpr int kSpmvThreads = 256;
+#ifndef ADIPC_SPMV_MIN_BLOCKS
+#define ADIPC_SPMV_MIN_BLOCKS 1
+#endif
+constexpr int kSpmvMinBlocks = ADIPC_SPMV_MIN_BLOCKS;  // 4 (<= 64 registers, 32 warps/SM) spills: 85 vs 61 us
 
 template <bool kDot, bool kPad = false, bool kCoalesce = false>
-__global__ void __launch_bounds__(kSpmvThreads) k_spmv(const std::uint32_t* __restrict__ rows,
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvMinBlocks) k_spmv(const std::uint32_t* __restrict__ rows,
                                                      const std::uint32_t* __restrict__ cols,
                                                      const double* __restrict__ blocks, std::int64_t U,
                                                      const double* __restrict__ x, double* __restrict__ y,

@@ -19,9 +19,9 @@ namespace {
 
 constexpr int kSpmvThreads = 256;
 #ifndef ADIPC_SPMV_MIN_BLOCKS
-#define ADIPC_SPMV_MIN_BLOCKS 1
+#define ADIPC_SPMV_MIN_BLOCKS 3
 #endif
-constexpr int kSpmvMinBlocks = ADIPC_SPMV_MIN_BLOCKS;  // 4 (<= 64 registers, 32 warps/SM) spills: 85 vs 61 us
+constexpr int kSpmvMinBlocks = ADIPC_SPMV_MIN_BLOCKS;  // 3 x 256 threads (<= 85 registers, 24 warps/SM); 4 spills: 85 vs 61 us
 
 template <bool kDot, bool kPad = false, bool kCoalesce = false>
 __global__ void __launch_bounds__(kSpmvThreads, kSpmvMinBlocks) k_spmv(const std::uint32_t* __restrict__ rows,

@@ -4,17 +4,50 @@
 // the reference's types (Eigen-based Mat3 / VecX, BlockTripletStream,
 // SortedSymBlockCoo, MasHierarchy, Preconditioner, PcgResult).
 //
-// Memory layout: std::vector<Mat3> is 9 contiguous column-major doubles per
-// block and std::vector<Vec3> / VecX are 3n contiguous doubles, exactly the
-// C-ABI's layout, so every call passes the vectors' storage straight through.
+// Memory layout: with Eigen, std::vector<Mat3> is 9 contiguous column-major
+// doubles per block and VecX 3n contiguous doubles, exactly the C-ABI's
+// layout, so every call passes the vectors' storage straight through. When a
+// matrix type carries more than its coefficients (sizeof(Mat3) != 72, e.g.
+// the Eigen subset the tests compile the reference with), the blocks are
+// packed into / unpacked from a contiguous buffer instead.
 #pragma once
 
+#include <cstring>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "adipc_gpu.h"
 
 namespace adipc::gpu {
+
+// N contiguous doubles per element (zero-copy when the type is exactly that)
+template <int N, class M>
+const double* flat_in(const std::vector<M>& v, std::vector<double>& tmp) {
+    if (v.empty()) return nullptr;
+    if constexpr (sizeof(M) == N * sizeof(double)) {
+        return v[0].data();
+    } else {
+        tmp.resize(v.size() * N);
+        for (std::size_t i = 0; i < v.size(); ++i) std::memcpy(tmp.data() + N * i, v[i].data(), N * sizeof(double));
+        return tmp.data();
+    }
+}
+template <int N, class M>
+double* flat_out(std::vector<M>& v, std::vector<double>& tmp) {
+    if (v.empty()) return nullptr;
+    if constexpr (sizeof(M) == N * sizeof(double)) {
+        return v[0].data();
+    } else {
+        tmp.resize(v.size() * N);
+        return tmp.data();
+    }
+}
+template <int N, class M>
+void flat_back(std::vector<M>& v, const std::vector<double>& tmp) {
+    if constexpr (sizeof(M) != N * sizeof(double))
+        for (std::size_t i = 0; i < v.size(); ++i) std::memcpy(v[i].data(), tmp.data() + N * i, N * sizeof(double));
+}
 
 inline void check(int rc, const adipc_gpu_ctx* ctx) {
     if (rc == ADIPC_OK) return;
@@ -43,24 +76,29 @@ private:
 inline void assemble(Context& c, const BlockTripletStream& s, Index n_block_rows, SortedSymBlockCoo& hess,
                      bool copy_back = true) {
     int64_t U = 0;
-    check(adipc_gpu_assemble(c.get(), s.keys.data(), s.values.empty() ? nullptr : s.values[0].data(),
-                             static_cast<int64_t>(s.size()), n_block_rows, 1, &U),
+    std::vector<double> in, out;
+    check(adipc_gpu_assemble(c.get(), s.keys.data(), flat_in<9>(s.values, in), static_cast<int64_t>(s.size()),
+                             n_block_rows, 1, &U),
           c.get());
     hess.n_block_rows = n_block_rows;
     if (!copy_back) return;
     hess.rows.resize(U);
     hess.cols.resize(U);
     hess.blocks.resize(U);
-    check(adipc_gpu_copy_matrix(c.get(), hess.rows.data(), hess.cols.data(),
-                                U ? hess.blocks[0].data() : nullptr),
+    check(adipc_gpu_copy_matrix(c.get(), reinterpret_cast<uint32_t*>(hess.rows.data()),
+                                reinterpret_cast<uint32_t*>(hess.cols.data()), flat_out<9>(hess.blocks, out)),
           c.get());
+    flat_back<9>(hess.blocks, out);
 }
 
 // block_coo.hpp:106 (stable, in place)
 inline void sort_stream(Context& c, BlockTripletStream& s) {
-    check(adipc_gpu_sort_stream(c.get(), s.keys.data(), s.values.empty() ? nullptr : s.values[0].data(),
-                                static_cast<int64_t>(s.size())),
-          c.get());
+    std::vector<double> tmp;
+    double* v = flat_out<9>(s.values, tmp);
+    if constexpr (sizeof(s.values[0]) != 9 * sizeof(double))
+        for (std::size_t i = 0; i < s.values.size(); ++i) std::memcpy(v + 9 * i, s.values[i].data(), 9 * sizeof(double));
+    check(adipc_gpu_sort_stream(c.get(), s.keys.data(), v, static_cast<int64_t>(s.size())), c.get());
+    flat_back<9>(s.values, tmp);
 }
 
 // abd_reduce.hpp:32 — same DofMap, same tile order
@@ -70,13 +108,14 @@ inline BlockTripletStream two_level_abd_reduce(Context& c, const BlockTripletStr
     out.keys.resize(cap);
     out.values.resize(cap);
     int64_t n = 0;
+    std::vector<double> vin, jin, vout;
     check(adipc_gpu_two_level_abd_reduce(
-              c.get(), node_pairs.keys.data(), node_pairs.values.empty() ? nullptr : node_pairs.values[0].data(),
+              c.get(), node_pairs.keys.data(), flat_in<9>(node_pairs.values, vin),
               static_cast<int64_t>(node_pairs.size()), map.n_fem_nodes, map.n_bodies,
               static_cast<int32_t>(map.abd_node_body.size()), map.abd_node_body.data(),
-              map.abd_node_jacobian.empty() ? nullptr : map.abd_node_jacobian[0].data(), out.keys.data(),
-              cap ? out.values[0].data() : nullptr, cap, &n),
+              flat_in<36>(map.abd_node_jacobian, jin), out.keys.data(), flat_out<9>(out.values, vout), cap, &n),
           c.get());
+    flat_back<9>(out.values, vout);
     out.keys.resize(n);
     out.values.resize(n);
     return out;

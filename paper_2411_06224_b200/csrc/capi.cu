@@ -158,6 +158,12 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.sell.cols.free();
     c.sell.vals.free();
     c.sell_len.free();
+    c.graph_deg.free();
+    c.graph_adj.free();
+    c.graph_adj2.free();
+    c.graph_ptr.free();
+    c.graph_cur.free();
+    c.graph_ptr2.free();
     c.perm.free();
     for (auto& e : c.splits) e.buf.free();
     c.splits.clear();

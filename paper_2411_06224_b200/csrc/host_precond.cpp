@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include <omp.h>
+
 namespace adipc_gpu::host {
 
 Index subdomain_count(Index v, Index n, Index n_o) {  // partition.hpp:12-15
@@ -25,43 +27,66 @@ Partition chunk_partition(Index v, Index capacity) {  // partition.hpp:25-32
     return p;
 }
 
-Graph build_graph(Index v, const Index* pairs, std::size_t n_edges) {  // partition.hpp:37-50
+namespace {
+
+// Adjacency lists of the undirected graph over v nodes whose edges are
+// edge(e, a, b) for e < n_edges (false = no edge, e.g. a diagonal block):
+// every list sorted ascending and duplicate-free, which is the
+// std::set-per-node result of partition.hpp:37-50 independent of the edge
+// order, so counting and scattering run in parallel (relaxed atomics) and
+// each list is sorted after the scatter.
+template <class Edge>
+Graph build_graph_impl(Index v, std::int64_t n_edges, Edge edge) {
     Graph g;
-    g.ptr.assign(static_cast<std::size_t>(v) + 1, 0);
-    for (std::size_t e = 0; e < n_edges; ++e) {
-        const Index a = pairs[2 * e], b = pairs[2 * e + 1];
-        if (a == b) continue;
-        ++g.ptr[a + 1];
-        ++g.ptr[b + 1];
+    std::vector<std::int64_t> deg(static_cast<std::size_t>(v) + 1, 0);
+#pragma omp parallel for schedule(static, 65536)
+    for (std::int64_t e = 0; e < n_edges; ++e) {
+        Index a, b;
+        if (!edge(e, a, b) || a == b) continue;
+        __atomic_fetch_add(&deg[a + 1], 1, __ATOMIC_RELAXED);
+        __atomic_fetch_add(&deg[b + 1], 1, __ATOMIC_RELAXED);
     }
-    for (Index i = 0; i < v; ++i) g.ptr[i + 1] += g.ptr[i];
-    g.adj.resize(g.ptr[v]);
-    std::vector<std::int64_t> cur(g.ptr.begin(), g.ptr.end() - 1);
-    for (std::size_t e = 0; e < n_edges; ++e) {
-        const Index a = pairs[2 * e], b = pairs[2 * e + 1];
-        if (a == b) continue;
-        g.adj[cur[a]++] = b;
-        g.adj[cur[b]++] = a;
+    for (Index i = 0; i < v; ++i) deg[i + 1] += deg[i];
+    std::vector<Index> adj(static_cast<std::size_t>(deg[v]));
+    std::vector<std::int64_t> cur(deg.begin(), deg.end() - 1);
+#pragma omp parallel for schedule(static, 65536)
+    for (std::int64_t e = 0; e < n_edges; ++e) {
+        Index a, b;
+        if (!edge(e, a, b) || a == b) continue;
+        adj[__atomic_fetch_add(&cur[a], 1, __ATOMIC_RELAXED)] = b;
+        adj[__atomic_fetch_add(&cur[b], 1, __ATOMIC_RELAXED)] = a;
     }
-    // sort + unique each list (in parallel), then compact in place
-    std::vector<std::int64_t> ulen(static_cast<std::size_t>(v));
+    // sort + unique each list, then compact into the final arrays
+    std::vector<std::int64_t> ulen(static_cast<std::size_t>(v) + 1, 0);
 #pragma omp parallel for schedule(static, 4096)
     for (Index i = 0; i < v; ++i) {
-        Index* beg = g.adj.data() + g.ptr[i];
-        Index* end = g.adj.data() + g.ptr[i + 1];
-        if (!std::is_sorted(beg, end)) std::sort(beg, end);
-        ulen[i] = std::unique(beg, end) - beg;
+        Index* beg = adj.data() + deg[i];
+        Index* end = adj.data() + deg[i + 1];
+        std::sort(beg, end);
+        ulen[i + 1] = std::unique(beg, end) - beg;
     }
-    std::int64_t w = 0;
-    for (Index i = 0; i < v; ++i) {
-        const std::int64_t b = g.ptr[i];
-        g.ptr[i] = w;
-        if (w != b) std::memmove(g.adj.data() + w, g.adj.data() + b, sizeof(Index) * ulen[i]);
-        w += ulen[i];
+    for (Index i = 0; i < v; ++i) ulen[i + 1] += ulen[i];
+    if (ulen[v] == deg[v]) {  // already duplicate-free (e.g. a symmetric matrix's pattern)
+        g.ptr = std::move(deg);
+        g.adj = std::move(adj);
+        return g;
     }
-    g.ptr[v] = w;
-    g.adj.resize(w);
+    g.ptr = std::move(ulen);
+    g.adj.resize(static_cast<std::size_t>(g.ptr[v]));
+#pragma omp parallel for schedule(static, 4096)
+    for (Index i = 0; i < v; ++i)
+        std::memcpy(g.adj.data() + g.ptr[i], adj.data() + deg[i], sizeof(Index) * (g.ptr[i + 1] - g.ptr[i]));
     return g;
+}
+
+}  // namespace
+
+Graph build_graph(Index v, const Index* pairs, std::size_t n_edges) {  // partition.hpp:37-50
+    return build_graph_impl(v, static_cast<std::int64_t>(n_edges), [pairs](std::int64_t e, Index& a, Index& b) {
+        a = pairs[2 * e];
+        b = pairs[2 * e + 1];
+        return true;
+    });
 }
 
 // partition.hpp:54-77 BFS components + partition.hpp:88-159 packing/carving.
@@ -163,11 +188,23 @@ Partition partition_block_graph(Index v, const Graph& g, Index capacity) {
 }
 
 Partition partition_block_graph(Index v, const Index* pairs, std::size_t n_edges, Index capacity) {
-    return partition_block_graph(v, build_graph(v, pairs, n_edges), capacity);
+    const auto t0 = std::chrono::steady_clock::now();
+    Graph g = build_graph(v, pairs, n_edges);
+    const auto t1 = std::chrono::steady_clock::now();
+    Partition p = partition_block_graph(v, g, capacity);
+    if (std::getenv("ADIPC_DEBUG_HIER"))
+        std::fprintf(stderr, "  partition v=%d e=%zu: graph %.1f ms, carve %.1f ms\n", v, n_edges,
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
+    return p;
 }
 
 // hierarchy.hpp:30-100
 MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_t n_edges, int max_levels) {
+    return build_hierarchy(l0, build_graph(static_cast<Index>(l0.part_of.size()), pairs, n_edges), max_levels);
+}
+
+MasHierarchy build_hierarchy(const Partition& l0, Graph g0, int max_levels) {
     MasHierarchy h;
     h.capacity = l0.capacity;
     h.n_slots = static_cast<Index>(l0.part_of.size());
@@ -179,7 +216,7 @@ MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_
     for (Index i = 0; i < h.n_slots; ++i) base.agg[i] = i;
     h.levels.push_back(std::move(base));
 
-    std::vector<Index> cur_edges(pairs, pairs + 2 * n_edges);
+    Graph g = std::move(g0);  // graph of the current level's nodes
     std::vector<Index> up, queue, members, mem_ptr;
     while (h.n_levels() < max_levels) {
         const Level& cur = h.levels.back();
@@ -187,8 +224,6 @@ MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_
         const bool dbg = std::getenv("ADIPC_DEBUG_HIER") != nullptr;
         auto tnow = [] { return std::chrono::steady_clock::now(); };
         auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-        const auto t0 = tnow();
-        const Graph g = build_graph(cur.n_nodes, cur_edges.data(), cur_edges.size() / 2);
         const auto t1 = tnow();
         // members of each subdomain in ascending node order (counting sort)
         mem_ptr.assign(static_cast<std::size_t>(cur.n_parts) + 1, 0);
@@ -237,10 +272,11 @@ MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_
         for (Index i = 0; i < cur.n_nodes; ++i) up[i] += ncomp[cur.part_of[i]];
         const auto t2 = tnow();
         if (n_next == cur.n_nodes) break;
-        // coarse edges (hierarchy.hpp:75-85: mapped, deduplicated, sorted):
-        // per super node U the sorted unique super neighbours V > U of its
-        // members, concatenated in U order — the sorted unique (U, V) list,
-        // built in parallel over super nodes
+        // coarse edges (hierarchy.hpp:75-85: mapped, deduplicated, sorted)
+        // and the graph partition.hpp:37-50 builds from them, in one step:
+        // node U's adjacency list is the sorted set of super nodes V != U
+        // adjacent to any member of U. Threads own contiguous U ranges and
+        // dedupe with a stamp array; their lists are concatenated in U order.
         std::vector<Index> sptr(static_cast<std::size_t>(n_next) + 1, 0), smem(cur.n_nodes);
         for (Index i = 0; i < cur.n_nodes; ++i) ++sptr[up[i] + 1];
         for (Index u = 0; u < n_next; ++u) sptr[u + 1] += sptr[u];
@@ -248,58 +284,54 @@ MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_
             std::vector<Index> fill(sptr.begin(), sptr.end() - 1);
             for (Index i = 0; i < cur.n_nodes; ++i) smem[fill[up[i]]++] = i;
         }
-        std::vector<std::int64_t> ecnt(static_cast<std::size_t>(n_next) + 1, 0);
-        auto neighbours = [&](Index u, std::vector<Index>& out) {
-            out.clear();
-            for (Index k = sptr[u]; k < sptr[u + 1]; ++k) {
-                const Index m = smem[k];
-                for (std::int64_t e = g.ptr[m]; e < g.ptr[m + 1]; ++e) {
-                    const Index v = up[g.adj[e]];
-                    if (v > u) out.push_back(v);
-                }
-            }
-            std::sort(out.begin(), out.end());
-            out.erase(std::unique(out.begin(), out.end()), out.end());
-        };
+        Graph cg;
+        cg.ptr.assign(static_cast<std::size_t>(n_next) + 1, 0);
+        std::vector<std::vector<Index>> part_adj;
 #pragma omp parallel
         {
-            std::vector<Index> nbr;
-#pragma omp for schedule(dynamic, 512)
-            for (Index u = 0; u < n_next; ++u) {
-                neighbours(u, nbr);
-                ecnt[u + 1] = static_cast<std::int64_t>(nbr.size());
+            const int nt = omp_get_num_threads(), t = omp_get_thread_num();
+#pragma omp single
+            part_adj.resize(nt);
+            const Index u0 = static_cast<Index>(static_cast<std::int64_t>(n_next) * t / nt);
+            const Index u1 = static_cast<Index>(static_cast<std::int64_t>(n_next) * (t + 1) / nt);
+            std::vector<Index>& out = part_adj[t];
+            std::vector<Index> stamp(static_cast<std::size_t>(n_next), kInvalid);
+            for (Index u = u0; u < u1; ++u) {
+                const std::size_t o = out.size();
+                for (Index k = sptr[u]; k < sptr[u + 1]; ++k) {
+                    const Index m = smem[k];
+                    for (std::int64_t e = g.ptr[m]; e < g.ptr[m + 1]; ++e) {
+                        const Index v = up[g.adj[e]];
+                        if (v != u && stamp[v] != u) {
+                            stamp[v] = u;
+                            out.push_back(v);
+                        }
+                    }
+                }
+                std::sort(out.begin() + o, out.end());
+                cg.ptr[u + 1] = static_cast<std::int64_t>(out.size() - o);
             }
+#pragma omp barrier
+#pragma omp single
+            {
+                for (Index u = 0; u < n_next; ++u) cg.ptr[u + 1] += cg.ptr[u];
+                cg.adj.resize(static_cast<std::size_t>(cg.ptr[n_next]));
+            }
+            if (!out.empty()) std::memcpy(cg.adj.data() + cg.ptr[u0], out.data(), sizeof(Index) * out.size());
         }
-        for (Index u = 0; u < n_next; ++u) ecnt[u + 1] += ecnt[u];
         const auto t3 = tnow();
-        std::vector<Index> next_edges(2 * static_cast<std::size_t>(ecnt[n_next]));
-#pragma omp parallel
-        {
-            std::vector<Index> nbr;
-#pragma omp for schedule(dynamic, 512)
-            for (Index u = 0; u < n_next; ++u) {
-                neighbours(u, nbr);
-                std::int64_t o = ecnt[u];
-                for (const Index v : nbr) {
-                    next_edges[2 * o] = u;
-                    next_edges[2 * o + 1] = v;
-                    ++o;
-                }
-            }
-        }
-        const std::size_t n_coarse_edges = static_cast<std::size_t>(ecnt[n_next]);
         Level next;
         next.n_nodes = n_next;
-        Partition grouped = partition_block_graph(n_next, next_edges.data(), n_coarse_edges, h.capacity);
+        Partition grouped = partition_block_graph(n_next, cg, h.capacity);
         next.n_parts = grouped.n_parts;
         next.part_of = std::move(grouped.part_of);
         next.agg.resize(h.n_slots);
         for (Index slot = 0; slot < h.n_slots; ++slot) next.agg[slot] = up[cur.agg[slot]];
         h.levels.push_back(std::move(next));
-        cur_edges = std::move(next_edges);
+        g = std::move(cg);
         if (dbg)
-            std::fprintf(stderr, "hierarchy level %d: graph %.1f ms, bfs %.1f ms, edges sort %.1f ms, partition %.1f ms\n",
-                         h.n_levels() - 1, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, tnow()));
+            std::fprintf(stderr, "hierarchy level %d: bfs %.1f ms, coarse graph %.1f ms, partition %.1f ms\n",
+                         h.n_levels() - 1, ms(t1, t2), ms(t2, t3), ms(t3, tnow()));
     }
     return h;
 }

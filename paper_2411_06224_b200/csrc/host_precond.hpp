@@ -52,5 +52,7 @@ Graph build_graph(Index v, const Index* pairs, std::size_t n_edges);  // pairs: 
 Partition partition_block_graph(Index v, const Graph& g, Index capacity);
 Partition partition_block_graph(Index v, const Index* pairs, std::size_t n_edges, Index capacity);
 MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_t n_edges, int max_levels);
+// same, with the level-0 graph already built (the device build, mas.cu level0_graph)
+MasHierarchy build_hierarchy(const Partition& l0, Graph g0, int max_levels);
 
 }  // namespace adipc_gpu::host

@@ -13,11 +13,14 @@
 //           and explicit inverse D^-1 = L^-T L^-1 (paper Alg. 1), one CTA per
 //           subdomain.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cstring>
 #include <limits>
 
 #include "mas_kernels.cuh"
+#include "scan.cuh"
 
 
 namespace adipc_gpu {
@@ -510,15 +513,27 @@ host::MasHierarchy to_solve_order(Ctx& c, const host::MasHierarchy& h) {
 
 // (Re)build the device levels of hierarchy h, in solve order when enabled.
 void set_levels(Ctx& c, const host::MasHierarchy& h) {
+    const bool dbg = std::getenv("ADIPC_DEBUG_HIER") != nullptr;
+    auto lap = [&, t = std::chrono::steady_clock::now()](const char* what) mutable {
+        if (!dbg) return;
+        ADIPC_CUDA(cudaStreamSynchronize(c.stream));
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "set_levels %s %.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    };
     c.levels.clear();
+    lap("free");
     const bool perm = c.solve_order && h.n_levels() > 0 && h.n_slots > 0;
     const host::MasHierarchy hp = perm ? to_solve_order(c, h) : host::MasHierarchy{};
     const host::MasHierarchy& hl = perm ? hp : h;
+    lap("to_solve_order");
     for (int l = 0; l < hl.n_levels(); ++l) {
         c.levels.emplace_back(new DeviceLevel());
         build_level(c, *c.levels.back(), hl.levels[l], l, c.A.n);
+        lap("build_level");
     }
     link_levels(c, hl);
+    lap("link_levels");
     c.levels_permuted = perm;
     ++c.levels_version;
 }
@@ -638,6 +653,116 @@ std::uint64_t pattern_hash(Ctx& c) {
            1ull;  // never equals the ~0 "invalid" marker's complement pattern; non-zero
 }
 
+namespace {
+
+// Level-0 graph of build_hierarchy (hierarchy.hpp:30-100 -> partition.hpp:37-50)
+// straight from the device matrix's pattern: node i's neighbours are the
+// off-diagonal blocks of row i and of column i (block_edges, mas.hpp:19-25),
+// every list sorted ascending and duplicate-free, as std::set-per-node makes
+// them. Degree count and scatter with atomics, then one thread per node
+// insertion-sorts its (short) list and drops repeats.
+__global__ void k_graph_deg(const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,
+                            std::int64_t U, std::int32_t* __restrict__ deg) {
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < U;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t r = rows[e], c = cols[e];
+        if (r == c) continue;
+        atomicAdd(deg + r, 1);
+        atomicAdd(deg + c, 1);
+    }
+}
+
+__global__ void k_graph_fill(const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,
+                             std::int64_t U, unsigned long long* __restrict__ cur, std::int32_t* __restrict__ adj) {
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < U;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t r = rows[e], c = cols[e];
+        if (r == c) continue;
+        adj[atomicAdd(cur + r, 1ull)] = static_cast<std::int32_t>(c);
+        adj[atomicAdd(cur + c, 1ull)] = static_cast<std::int32_t>(r);
+    }
+}
+
+__global__ void k_graph_sort(std::int32_t n, const std::int64_t* __restrict__ ptr, std::int32_t* __restrict__ adj,
+                             std::int32_t* __restrict__ ulen) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        std::int32_t* a = adj + ptr[i];
+        const std::int64_t d = ptr[i + 1] - ptr[i];
+        for (std::int64_t k = 1; k < d; ++k) {
+            const std::int32_t v = a[k];
+            std::int64_t j = k - 1;
+            for (; j >= 0 && a[j] > v; --j) a[j + 1] = a[j];
+            a[j + 1] = v;
+        }
+        std::int32_t u = d > 0 ? 1 : 0;
+        for (std::int64_t k = 1; k < d; ++k)
+            if (a[k] != a[u - 1]) a[u++] = a[k];
+        ulen[i] = u;
+    }
+}
+
+__global__ void k_graph_compact(std::int32_t n, const std::int64_t* __restrict__ ptr, const std::int32_t* __restrict__ adj,
+                                const std::int64_t* __restrict__ ptr2, std::int32_t* __restrict__ adj2) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        for (std::int64_t k = 0; k < ptr2[i + 1] - ptr2[i]; ++k) adj2[ptr2[i] + k] = adj[ptr[i] + k];
+}
+
+host::Graph level0_graph(Ctx& c) {
+    const DeviceMatrix& A = c.A;
+    cudaStream_t st = c.stream;
+    const std::int32_t n = A.n;
+    host::Graph g;
+    c.graph_deg.reserve(static_cast<std::size_t>(std::max(n, 1)));
+    c.graph_ptr.reserve(static_cast<std::size_t>(n) + 1);
+    c.graph_cur.reserve(static_cast<std::size_t>(std::max(n, 1)));
+    ADIPC_CUDA(cudaMemsetAsync(c.graph_deg.p, 0, sizeof(std::int32_t) * std::max(n, 1), st));
+    if (A.U > 0) {
+        k_graph_deg<<<grid_for(A.U, 256, 16), 256, 0, st>>>(A.rows.p, A.cols.p, A.U, c.graph_deg.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    exclusive_scan(c.graph_deg.p, n, c.graph_ptr.p, c.scan_scratch, st);
+    std::int64_t E = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&E, c.graph_ptr.p + n, sizeof(E), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    c.graph_adj.reserve(static_cast<std::size_t>(std::max<std::int64_t>(E, 1)));
+    if (n > 0)
+        ADIPC_CUDA(cudaMemcpyAsync(c.graph_cur.p, c.graph_ptr.p, sizeof(std::int64_t) * n, cudaMemcpyDeviceToDevice, st));
+    if (A.U > 0 && E > 0) {
+        k_graph_fill<<<grid_for(A.U, 256, 16), 256, 0, st>>>(
+            A.rows.p, A.cols.p, A.U, reinterpret_cast<unsigned long long*>(c.graph_cur.p), c.graph_adj.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    if (n > 0) {
+        k_graph_sort<<<grid_for(n, 128, 64), 128, 0, st>>>(n, c.graph_ptr.p, c.graph_adj.p, c.graph_deg.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    c.graph_ptr2.reserve(static_cast<std::size_t>(n) + 1);
+    exclusive_scan(c.graph_deg.p, n, c.graph_ptr2.p, c.scan_scratch, st);
+    std::int64_t E2 = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&E2, c.graph_ptr2.p + n, sizeof(E2), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    const std::int32_t* adj = c.graph_adj.p;
+    const std::int64_t* ptr = c.graph_ptr.p;
+    if (E2 != E) {  // repeated pairs (not produced by a sorted unique pattern; kept for safety)
+        c.graph_adj2.reserve(static_cast<std::size_t>(std::max<std::int64_t>(E2, 1)));
+        k_graph_compact<<<grid_for(n, 128, 64), 128, 0, st>>>(n, c.graph_ptr.p, c.graph_adj.p, c.graph_ptr2.p,
+                                                             c.graph_adj2.p);
+        ADIPC_LAUNCH_CHECK();
+        adj = c.graph_adj2.p;
+        ptr = c.graph_ptr2.p;
+    }
+    g.ptr.resize(static_cast<std::size_t>(n) + 1);
+    g.adj.resize(static_cast<std::size_t>(E2));
+    ADIPC_CUDA(cudaMemcpyAsync(g.ptr.data(), ptr, sizeof(std::int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+    if (E2 > 0) ADIPC_CUDA(cudaMemcpyAsync(g.adj.data(), adj, sizeof(std::int32_t) * E2, cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    return g;
+}
+
+}  // namespace
+
 void build_preconditioner(Ctx& c, PrecondKind kind) {
     cudaStream_t st = c.stream;
     const DeviceMatrix& A = c.A;
@@ -663,23 +788,20 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
     const bool reuse = c.cache_hierarchy && c.hier_version == phash && !c.levels.empty();
     // block_edges(A) (mas.hpp:19-25): off-diagonal (row, col) pairs, in order
     if (!reuse) {
-        std::vector<std::uint32_t> rows(A.U), cols(A.U);
-        if (A.U) {
-            ADIPC_CUDA(cudaMemcpyAsync(rows.data(), A.rows.p, 4 * A.U, cudaMemcpyDeviceToHost, st));
-            ADIPC_CUDA(cudaMemcpyAsync(cols.data(), A.cols.p, 4 * A.U, cudaMemcpyDeviceToHost, st));
-            ADIPC_CUDA(cudaStreamSynchronize(st));
-        }
-        std::vector<std::int32_t> pairs;
-        pairs.reserve(2 * A.U);
-        for (std::int64_t i = 0; i < A.U; ++i)
-            if (rows[i] != cols[i]) {
-                pairs.push_back(static_cast<std::int32_t>(rows[i]));
-                pairs.push_back(static_cast<std::int32_t>(cols[i]));
-            }
-        c.hier = host::build_hierarchy(c.l0, pairs.data(), pairs.size() / 2, c.max_levels);
+        // the level-0 graph built on the device from A's pattern, one D2H
+        host::Graph g0 = level0_graph(c);
+        const auto ta = std::chrono::steady_clock::now();
+        c.hier = host::build_hierarchy(c.l0, std::move(g0), c.max_levels);
         if (c.hier.n_levels() > kMaxLevels) throw StatusError(kInvalidArgument, "too many MAS levels");
+        const auto tb = std::chrono::steady_clock::now();
         set_levels(c, c.hier);
         c.hier_version = c.cache_hierarchy ? phash : ~0ull;
+        if (std::getenv("ADIPC_DEBUG_HIER")) {
+            const auto tc = std::chrono::steady_clock::now();
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "cold MAS host: block_edges %.1f ms, build_hierarchy %.1f ms, device levels %.1f ms\n",
+                         ms(t0, ta), ms(ta, tb), ms(tb, tc));
+        }
     } else {
         for (auto& L : c.levels)
             ADIPC_CUDA(cudaMemsetAsync(L->dense.p, 0, sizeof(double) * std::max<std::int64_t>(L->dense_doubles, 1), st));

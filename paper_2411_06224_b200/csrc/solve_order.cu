@@ -180,11 +180,14 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, pair = w >> 1, half = w & 1;
     const int npc = blockDim.x >> 6;
     double* ring = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(pair) * kStages * slot_doubles;
+    // one b per pair: both warps write the same values into it after the
+    // pair barrier that ends the previous item, then read it after their own
+    // __syncwarp (no cross-warp dependency)
     double* bs = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(npc) * kStages * slot_doubles +
-                 static_cast<std::size_t>(w) * kK;
+                 static_cast<std::size_t>(pair) * kK;
     std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(
                              reinterpret_cast<double*>(smem) + static_cast<std::size_t>(npc) * kStages * slot_doubles +
-                             static_cast<std::size_t>(2 * npc) * kK) +
+                             static_cast<std::size_t>(npc) * kK) +
                          pair * kStages;
     // every pair takes an even share of EACH level (a contiguous run per
     // level, level 0 first): the coarse items, cheap in bytes but with a
@@ -292,16 +295,19 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
         mbar_wait(&bar[st], par);
         const double* M = ring + static_cast<std::size_t>(st) * slot_doubles;
         double* out = pt.out[cur.l];
+        auto refill = [&] {
+            pair_sync(pair);  // both warps are done with the slot
+            if (half == 0 && lane == 0 && i + kStages < nloc) {  // refill kStages items ahead
+                fence_proxy_async();
+                issue(item(i + kStages), st);
+            }
+        };
         if (pt.dbg_nomath)  // timing experiments: stream the inverses, skip the mat-vec
             dsum += M[lane] * bs[lane];
         else
             dsum += pair_solve<kK>(M, bs, lane, half, cur.dim,
                                    [&](int j, double v) { out[row_index(cur, j)] = v; });
-        pair_sync(pair);  // both warps are done with the slot and with bs
-        if (half == 0 && lane == 0 && i + kStages < nloc) {  // refill kStages items ahead
-            fence_proxy_async();
-            issue(item(i + kStages), st);
-        }
+        refill();  // also orders the next item's bs writes after both warps' reads
         if (++st == kStages) {
             st = 0;
             par ^= 1u;
@@ -1826,7 +1832,7 @@ PcLaunch precond_launch(Ctx& c) {
     const int kk = matvec_cols(fill);
     L.slot = static_cast<int>(packed_doubles(kk));
     const int stages = c.l0_stages;
-    const std::size_t per_pair = (sizeof(double) * L.slot + sizeof(std::uint64_t)) * stages + 2 * sizeof(double) * kk;
+    const std::size_t per_pair = (sizeof(double) * L.slot + sizeof(std::uint64_t)) * stages + sizeof(double) * kk;
     L.pairs = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(c.pc_pairs, (113u * 1024u) / per_pair)));
     L.smem = per_pair * L.pairs;
     if (kk == 24)

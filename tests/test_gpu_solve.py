@@ -301,3 +301,49 @@ def test_hierarchy_in_context_matches_oracle(ctx):
     for a, o in zip(levels, ho.levels):
         assert a["n_nodes"] == o["n_nodes"] and a["n_parts"] == o["n_parts"]
         assert np.array_equal(a["part_of"], o["part_of"]) and np.array_equal(a["agg"], o["agg"])
+
+
+def _full_stream(sc):
+    """The reference's full emission (incremental_potential.hpp:170-257):
+    element / body tiles, then the contact tiles of two_level_abd_reduce
+    (:392-393), then filter_pinned (:410-425)."""
+    keys, vals = sc.keys, sc.vals
+    if sc.n_bodies:
+        rk, rv = O.two_level_abd_reduce(sc.node_keys, sc.node_vals, sc.n_fem, sc.n_bodies, sc.abd_body, sc.jac36, DET)
+        keys, vals = np.concatenate([keys, rk]), np.concatenate([vals, rv])
+    return O.filter_pinned(keys, vals, sc.pinned)
+
+
+@pytest.mark.parametrize("name", ["cfg2_cloth", "cfg3_abd_stack", "cfg4_hybrid"])
+@pytest.mark.parametrize("kind", [1, 2])
+def test_pcg_shell_and_contact_configs(ctx, name, kind):
+    """PCG parity on the shell (cfg2) and affine-body / contact scenes (cfg3,
+    cfg4, assembled through the two-level reduction): iteration counts +-2 %,
+    solutions within 1e-5 relative L2 of the oracle. Gravity rhs for the
+    cloth, b = A x* (x* ~ N(0,1), seed 5) for the scenes with affine bodies.
+    Block-Jacobi PCG on cfg4 needs ~157 iterations and crosses the 1e-4 stop
+    threshold within rounding (GPU 156, oracle 157 iterations; CG on this
+    conditioning turns last-bit differences into ~3e-3 in x even at equal
+    iteration counts), so there the check is the solve quality itself: true
+    residual |b - A x| / |b| and error |x - x*| / |x*| within 1.25x of the
+    oracle's."""
+    sc = scenes.CONFIGS[name]()
+    fk, fv = _full_stream(sc)
+    ctx.assemble(fk, fv, sc.n_blocks)
+    n, rows, cols, blocks = ctx.copy_matrix()
+    l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, 16)
+    ctx.set_level0_partition(l0.part_of, l0.n_parts, 16, 4)
+    ctx.build_preconditioner(kind)
+    xstar = np.random.default_rng(5).standard_normal(3 * n)
+    b = scenes.gravity_rhs(sc) if sc.n_bodies == 0 else O.srbk_spmv(n, rows, cols, blocks, xstar, DET)
+    x, r = ctx.pcg(b, 1e-4, 250, 100000)
+    xo, ro = _oracle_solve(sc, rows, cols, blocks, l0, b, kind, DET)
+    assert r.converged and ro["converged"]
+    assert abs(r.iters - ro["iters"]) <= max(1, 0.02 * ro["iters"]), (r.iters, ro["iters"])
+    if name == "cfg4_hybrid" and kind == 2:
+        res = lambda v: np.linalg.norm(b - O.srbk_spmv(n, rows, cols, blocks, v, DET)) / np.linalg.norm(b)
+        err = lambda v: np.linalg.norm(v - xstar) / np.linalg.norm(xstar)
+        assert res(x) <= 1.25 * res(xo), (res(x), res(xo))
+        assert err(x) <= 1.25 * err(xo), (err(x), err(xo))
+    else:
+        assert np.linalg.norm(x - xo) <= 1e-5 * np.linalg.norm(xo)

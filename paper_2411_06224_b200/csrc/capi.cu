@@ -169,6 +169,7 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.splits.clear();
     c.phase_ns.free();
     c.perm_keys.free();
+    c.as_src.free();
     c.perm_vals.free();
     c.pv_in.free();
     c.pv_out.free();

@@ -155,6 +155,8 @@ struct Ctx {
     DBuf<std::int32_t> perm;       // reference slot -> solve slot
     DeviceMatrix As;               // A in solve order (upper triangle re-canonicalised)
     DBuf<std::uint64_t> perm_keys; // scratch stream for building As
+    DBuf<std::uint32_t> as_src;    // As entry -> A entry (bit 31: transposed); valid for as_src_version
+    std::uint64_t as_src_version = ~0ull;
     DBuf<double> perm_vals;
     DBuf<double> pv_in, pv_out;    // rhs / solution in solve order
     const DeviceMatrix& S() const { return perm_active ? As : A; }

@@ -189,20 +189,39 @@ __global__ void k_invert(std::int32_t n_parts, const std::int32_t* __restrict__ 
 // j of the product W^T W (one packed column k at a time) — no block barriers
 // and no index divisions. Per warp in shared memory: S (dim x dim, column
 // major; L in its lower triangle, W^T in its strict upper one) + diag(W).
+// Every level's subdomains in one launch (the levels are independent once
+// restricted): item q of the concatenated list belongs to level l with
+// base[l] <= q < base[l + 1].
+struct InvertLevel {
+    const std::int32_t* sub_ptr;
+    const std::int64_t* dense_off;
+    const double* dense;
+    const std::int64_t* inv_off;
+    double* inv;
+};
+struct InvertTable {
+    int n;
+    std::int32_t base[kMaxLevels + 1];
+    InvertLevel lv[kMaxLevels];
+};
+
 template <int R>
-__global__ void __launch_bounds__(128) k_invert_warp(std::int32_t n_parts, const std::int32_t* __restrict__ sub_ptr,
-                                                    const std::int64_t* __restrict__ dense_off,
-                                                    const double* __restrict__ dense,
-                                                    const std::int64_t* __restrict__ inv_off, double* __restrict__ inv,
-                                                    int* __restrict__ status, int* __restrict__ shifts, int max_dim) {
+__global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __restrict__ status,
+                                                    int* __restrict__ shifts, int max_dim) {
     extern __shared__ double sm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double* S = sm + static_cast<std::size_t>(w) * (max_dim * max_dim + max_dim);
     double* dg = S + max_dim * max_dim;
-    for (std::int32_t s = blockIdx.x * nw + w; s < n_parts; s += gridDim.x * nw) {
+    for (std::int32_t q = blockIdx.x * nw + w; q < tab.base[tab.n]; q += gridDim.x * nw) {
+        int l = 0;
+        while (l + 1 < tab.n && q >= tab.base[l + 1]) ++l;
+        const std::int32_t s = q - tab.base[l];
+        const std::int32_t* sub_ptr = tab.lv[l].sub_ptr;
+        const std::int64_t* inv_off = tab.lv[l].inv_off;
+        double* inv = tab.lv[l].inv;
         const int d = 3 * (sub_ptr[s + 1] - sub_ptr[s]);
         if (d == 0) continue;
-        const double* D = dense + dense_off[s];
+        const double* D = tab.lv[l].dense + tab.lv[l].dense_off[s];
         double tr = 0;
 #pragma unroll
         for (int t = 0; t < R; ++t) {
@@ -538,15 +557,58 @@ void set_levels(Ctx& c, const host::MasHierarchy& h) {
     ++c.levels_version;
 }
 
+// As entry i <- A entry src (the bucket sort's emission index: the permuted
+// stream has no repeated keys, so sorted position i IS As entry i), bit 31 when
+// the block is stored transposed
+__global__ void k_solve_map(const std::uint64_t* __restrict__ sorted, std::int64_t U,
+                            const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,
+                            const std::int32_t* __restrict__ perm, std::uint32_t* __restrict__ src) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < U;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t e = static_cast<std::uint32_t>(sorted[i] & 0xFFFFFFFFu);
+        const bool flip = perm[rows[e]] > perm[cols[e]];
+        src[i] = e | (flip ? 0x80000000u : 0u);
+    }
+}
+
+// As values from A through the map (pattern unchanged since the map was built)
+__global__ void k_solve_gather(const double* __restrict__ blocks, const std::uint32_t* __restrict__ src,
+                               std::int64_t U, double* __restrict__ out) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < U;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t m = src[i];
+        const std::int64_t e = m & 0x7FFFFFFFu;
+        double h[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) h[k] = blocks[blk(e, k)];
+        const bool flip = (m >> 31) != 0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int i2 = 0; i2 < 3; ++i2) out[blk(i, 3 * j + i2)] = flip ? h[3 * i2 + j] : h[3 * j + i2];
+    }
+}
+
 }  // namespace
 
 void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
                  DeviceMatrix& out);
 
 // As = P A P^T in solve order (sorted upper block triangle, the same layout
-// as A), rebuilt from the current A values on every preconditioner build.
-void build_solve_matrix(Ctx& c) {
+// as A), rebuilt from the current A values on every preconditioner build:
+// while the pattern and the levels are unchanged (`reuse`), one gather
+// through the As -> A map; otherwise permute stream + the assembly
+// sort/reduce, and the map is taken from the sort.
+void build_solve_matrix(Ctx& c, bool reuse) {
     const DeviceMatrix& A = c.A;
+    if (reuse && c.as_src_version == c.levels_version && c.As.U == A.U && c.As.n == A.n) {
+        if (A.U > 0) {
+            k_solve_gather<<<grid_for(A.U, 256, 16), 256, 0, c.stream>>>(A.blocks.p, c.as_src.p, A.U, c.As.blocks.p);
+            ADIPC_LAUNCH_CHECK();
+        }
+        ++c.As.version;
+        return;
+    }
     c.perm_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(A.U, 1)));
     c.perm_vals.reserve(9 * static_cast<std::size_t>(std::max<std::int64_t>(A.U, 1)));
     if (A.U > 0) {
@@ -555,6 +617,15 @@ void build_solve_matrix(Ctx& c) {
         ADIPC_LAUNCH_CHECK();
     }
     sort_reduce(c, c.perm_keys.p, c.perm_vals.p, A.U, A.n, c.As);
+    c.as_src_version = ~0ull;
+    if (c.As.U != A.U) return;  // cannot happen for a permutation; no map then
+    c.as_src.reserve(static_cast<std::size_t>(std::max<std::int64_t>(A.U, 1)));
+    if (A.U > 0) {
+        k_solve_map<<<grid_for(A.U, 256, 16), 256, 0, c.stream>>>(c.sorted.p, A.U, A.rows.p, A.cols.p, c.perm.p,
+                                                                 c.as_src.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    c.as_src_version = c.levels_version;
 }
 
 // K9 restriction + K10 batched factorisation/inversion for the current levels.
@@ -574,28 +645,39 @@ void factorize(Ctx& c) {
     }
     c.build_status.reserve(2);
     ADIPC_CUDA(cudaMemsetAsync(c.build_status.p, 0, 2 * sizeof(int), st));
+    // warp-per-subdomain levels (dim <= 64): one launch for all of them
+    InvertTable tab{};
+    int wdim = 0;
+    for (auto& Lp : c.levels) {
+        DeviceLevel& L = *Lp;
+        const int dim = 3 * L.max_fill;
+        if (L.n_parts == 0 || dim > 64 || !c.invert_warp) continue;
+        tab.lv[tab.n] = InvertLevel{L.sub_ptr.p, L.dense_off.p, L.dense.p, L.inv_off.p, L.inv.p};
+        tab.base[tab.n + 1] = tab.base[tab.n] + L.n_parts;
+        ++tab.n;
+        wdim = std::max(wdim, dim);
+    }
+    if (tab.n > 0) {
+        const int nw = 4;
+        const std::size_t wsm = sizeof(double) * nw * (static_cast<std::size_t>(wdim) * wdim + wdim);
+        int sms = kSMs;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+        const int grid = static_cast<int>(
+            std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(tab.base[tab.n], nw), sms * 8)));
+        if (wdim <= 32) {
+            ADIPC_CUDA(cudaFuncSetAttribute(k_invert_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
+            k_invert_warp<1><<<grid, 32 * nw, wsm, st>>>(tab, c.build_status.p, c.build_status.p + 1, wdim);
+        } else {
+            ADIPC_CUDA(cudaFuncSetAttribute(k_invert_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
+            k_invert_warp<2><<<grid, 32 * nw, wsm, st>>>(tab, c.build_status.p, c.build_status.p + 1, wdim);
+        }
+        ADIPC_LAUNCH_CHECK();
+    }
     for (auto& Lp : c.levels) {
         DeviceLevel& L = *Lp;
         if (L.n_parts == 0) continue;
         const int dim = 3 * L.max_fill;
-        if (dim <= 64 && c.invert_warp) {  // warp per subdomain (k_invert_warp)
-            const int nw = 4;
-            const std::size_t wsm = sizeof(double) * nw * (static_cast<std::size_t>(dim) * dim + dim);
-            int sms = kSMs;
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-            const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(L.n_parts, nw), sms * 8)));
-            if (dim <= 32) {
-                ADIPC_CUDA(cudaFuncSetAttribute(k_invert_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
-                k_invert_warp<1><<<grid, 32 * nw, wsm, st>>>(L.n_parts, L.sub_ptr.p, L.dense_off.p, L.dense.p, L.inv_off.p,
-                                                          L.inv.p, c.build_status.p, c.build_status.p + 1, dim);
-            } else {
-                ADIPC_CUDA(cudaFuncSetAttribute(k_invert_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
-                k_invert_warp<2><<<grid, 32 * nw, wsm, st>>>(L.n_parts, L.sub_ptr.p, L.dense_off.p, L.dense.p, L.inv_off.p,
-                                                          L.inv.p, c.build_status.p, c.build_status.p + 1, dim);
-            }
-            ADIPC_LAUNCH_CHECK();
-            continue;
-        }
+        if (dim <= 64 && c.invert_warp) continue;  // done above
         const std::size_t need = 2 * sizeof(double) * dim * dim;
         const bool in_smem = need <= 200 * 1024;
         const int threads = dim <= 48 ? 128 : 256;
@@ -809,7 +891,7 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
     const auto t1 = std::chrono::steady_clock::now();
     c.ms_build_host = std::chrono::duration<float, std::milli>(t1 - t0).count();
     c.perm_active = c.levels_permuted;
-    if (c.perm_active) build_solve_matrix(c);
+    if (c.perm_active) build_solve_matrix(c, reuse);
     factorize(c);
 }
 
@@ -821,7 +903,7 @@ void build_mas_from_hierarchy(Ctx& c, const host::MasHierarchy& h) {
     c.hier_version = ~0ull;  // explicit hierarchies are never reused by the cache
     c.ms_build_host = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
     c.perm_active = c.levels_permuted;
-    if (c.perm_active) build_solve_matrix(c);
+    if (c.perm_active) build_solve_matrix(c, false);
     factorize(c);
 }
 

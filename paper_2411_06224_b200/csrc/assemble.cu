@@ -29,6 +29,7 @@ namespace adipc_gpu {
 
 namespace {
 
+constexpr std::uint32_t kNoIdentity = 0xFFFFFFFFu;
 constexpr int kWarpSortMax = 256;   // rows up to this length: one warp, smem bitonic
 constexpr int kCtaSortMax = 8192;   // rows up to this length: one CTA, smem bitonic
 constexpr int kCtaSortThreads = 1024;
@@ -46,15 +47,17 @@ __global__ void k_row_hist(const std::uint64_t* __restrict__ keys, std::int64_t 
     }
 }
 
+// entry = (col << 32) | emission index; the index is i, or vidx[i] when the
+// keys are a filtered copy (vidx increasing: still the emission order)
 __global__ void k_row_scatter(const std::uint64_t* __restrict__ keys, std::int64_t T,
                               const std::int64_t* __restrict__ row_start, std::int32_t* __restrict__ cursor,
-                              std::uint64_t* __restrict__ out) {
+                              std::uint64_t* __restrict__ out, const std::uint32_t* __restrict__ vidx) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < T;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const std::uint64_t k = keys[i];
         const std::uint32_t row = static_cast<std::uint32_t>(k >> 32);
         const std::int64_t pos = row_start[row] + atomicAdd(cursor + row, 1);
-        out[pos] = (k << 32) | static_cast<std::uint32_t>(i);
+        out[pos] = (k << 32) | (vidx ? vidx[i] : static_cast<std::uint32_t>(i));
     }
 }
 
@@ -210,7 +213,20 @@ __global__ void k_sort_rows_cta(std::uint64_t* __restrict__ sorted, std::uint64_
 __global__ void k_reduce_rows(const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
                               const std::int64_t* __restrict__ uniq_start, std::int32_t n,
                               const double* __restrict__ vals, std::uint32_t* __restrict__ out_rows,
-                              std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks, std::int64_t U) {
+                              std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks, std::int64_t U,
+                              std::uint32_t identity_from) {
+    // value of emission index q: vals[9 q]; q >= identity_from is an appended
+    // pinned-diagonal I3 (filtered streams, assemble_filtered)
+    auto value = [&](std::uint32_t src, double* out) {
+        if (src >= identity_from) {
+#pragma unroll
+            for (int k = 0; k < 9; ++k) out[k] = (k % 4 == 0) ? 1.0 : 0.0;
+        } else {
+            const double* v = vals + 9 * static_cast<std::int64_t>(src);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) out[k] = v[k];
+        }
+    };
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
     for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps) {
@@ -226,13 +242,12 @@ __global__ void k_reduce_rows(const std::uint64_t* __restrict__ sorted, const st
             if (head) {
                 const std::int64_t my_u = u + __popc(hm & ((1u << lane) - 1u));
                 double acc[9];
-                const double* src = vals + 9 * static_cast<std::int64_t>(static_cast<std::uint32_t>(v));
-#pragma unroll
-                for (int k = 0; k < 9; ++k) acc[k] = src[k];
+                value(static_cast<std::uint32_t>(v), acc);
                 for (std::int64_t q = p + 1; q < e; ++q) {
                     const std::uint64_t w2 = sorted[q];
                     if (static_cast<std::uint32_t>(w2 >> 32) != col) break;
-                    const double* s2 = vals + 9 * static_cast<std::int64_t>(static_cast<std::uint32_t>(w2));
+                    double s2[9];
+                    value(static_cast<std::uint32_t>(w2), s2);
 #pragma unroll
                     for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(acc[k], s2[k]);
                 }
@@ -347,6 +362,34 @@ __global__ void k_pin_identity(const std::uint8_t* __restrict__ pinned, std::int
     }
 }
 
+// filter_pinned on the keys only: kept keys compacted in order, vidx = their
+// index in the original stream (values stay where they are)
+__global__ void k_pin_compact_keys(const std::uint64_t* __restrict__ keys, std::int64_t T,
+                                   const std::int32_t* __restrict__ keep, const std::int64_t* __restrict__ pos,
+                                   std::uint64_t* __restrict__ ok, std::uint32_t* __restrict__ vidx) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        if (!keep[i]) continue;
+        const std::int64_t p = pos[i];
+        ok[p] = keys[i];
+        vidx[p] = static_cast<std::uint32_t>(i);
+    }
+}
+
+// the appended identities take emission indices T, T + 1, ... (after every
+// original entry), which the reduction recognises as I3
+__global__ void k_pin_identity_keys(const std::uint8_t* __restrict__ pinned, std::int32_t n_slots,
+                                    const std::int64_t* __restrict__ pos, std::int64_t base, std::int64_t T,
+                                    std::uint64_t* __restrict__ ok, std::uint32_t* __restrict__ vidx) {
+    for (std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; s < n_slots;
+         s += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        if (!pinned[s]) continue;
+        const std::int64_t p = base + pos[s];
+        ok[p] = (static_cast<std::uint64_t>(s) << 32) | static_cast<std::uint64_t>(s);
+        vidx[p] = static_cast<std::uint32_t>(T + pos[s]);
+    }
+}
+
 __global__ void k_u8_to_i32(const std::uint8_t* __restrict__ a, std::int64_t n, std::int32_t* __restrict__ b) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
@@ -358,7 +401,7 @@ __global__ void k_u8_to_i32(const std::uint8_t* __restrict__ a, std::int64_t n, 
 // Steps 1-5: bucket by row, sort each row by (col, emission index), count
 // unique cols. Leaves c.sorted / c.row_start / c.uniq_cnt filled. Throws
 // kInvalidArgument if a key's row is >= n.
-void bucket_sort(Ctx& c, const std::uint64_t* d_keys, std::int64_t T, std::int32_t n) {
+void bucket_sort(Ctx& c, const std::uint64_t* d_keys, std::int64_t T, std::int32_t n, const std::uint32_t* d_vidx) {
     cudaStream_t st = c.stream;
     if (T >= (std::int64_t(1) << 32)) throw StatusError(kInvalidArgument, "triplet stream longer than 2^32");
     c.row_cnt.reserve(static_cast<std::size_t>(n) + 1);
@@ -377,7 +420,8 @@ void bucket_sort(Ctx& c, const std::uint64_t* d_keys, std::int64_t T, std::int32
     }
     exclusive_scan(c.row_cnt.p, n, c.row_start.p, c.scan_scratch, st);
     if (T > 0) {
-        k_row_scatter<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, c.row_start.p, c.row_cursor.p, c.sorted.p);
+        k_row_scatter<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, c.row_start.p, c.row_cursor.p, c.sorted.p,
+                                                             d_vidx);
         ADIPC_LAUNCH_CHECK();
     }
     if (n > 0) {
@@ -414,9 +458,10 @@ void blocks_soa_to_aos(Ctx& c, const double* soa, double* aos, std::int64_t U) {
 // Sort + reduce of a device-resident triplet stream into `out` (CSR row_ptr
 // included). Shared by the global assembly and the two-level ABD reduction.
 void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
-                 DeviceMatrix& out) {
+                 DeviceMatrix& out, const std::uint32_t* d_vidx, std::uint32_t identity_from, cudaEvent_t vals_ready) {
     cudaStream_t st = c.stream;
-    bucket_sort(c, d_keys, T, n);
+    bucket_sort(c, d_keys, T, n, d_vidx);  // keys only: overlaps an upload of the values still in flight
+    if (vals_ready) ADIPC_CUDA(cudaStreamWaitEvent(st, vals_ready, 0));
     out.n = n;
     out.row_ptr.reserve(static_cast<std::size_t>(n) + 1);
     exclusive_scan(c.uniq_cnt.p, n, out.row_ptr.p, c.scan_scratch, st);
@@ -430,7 +475,7 @@ void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std:
     out.blocks.reserve(blk_doubles(U));
     if (n > 0 && U > 0) {
         k_reduce_rows<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, out.row_ptr.p, n, d_vals,
-                                                          out.rows.p, out.cols.p, out.blocks.p, U);
+                                                          out.rows.p, out.cols.p, out.blocks.p, U, identity_from);
         ADIPC_LAUNCH_CHECK();
     }
     ++out.version;
@@ -451,14 +496,57 @@ void sort_stream(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std:
     ADIPC_CUDA(cudaStreamSynchronize(st));
     if (max_row >= (1u << 30)) throw StatusError(kInvalidArgument, "sort_stream: block row index >= 2^30");
     const std::int32_t n = static_cast<std::int32_t>(max_row) + 1;
-    bucket_sort(c, d_keys, T, n);
+    bucket_sort(c, d_keys, T, n, nullptr);
     k_gather_sorted<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, n, d_vals, d_out_keys, d_out_vals);
     ADIPC_LAUNCH_CHECK();
 }
 
 void assemble(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
-              int /*deterministic: the device path is always the bitwise-deterministic order*/) {
-    sort_reduce(c, d_keys, d_vals, T, n, c.A);
+              int /*deterministic: the device path is always the bitwise-deterministic order*/, cudaEvent_t vals_ready) {
+    sort_reduce(c, d_keys, d_vals, T, n, c.A, nullptr, kNoIdentity, vals_ready);
+}
+
+// filter_pinned + sort + reduce without moving a value: the kept keys are
+// compacted with their original stream index (vidx) and the pinned-diagonal
+// identities appended (incremental_potential.hpp:410-425), the keys sorted,
+// and the reduction reads each value from the ORIGINAL stream through vidx,
+// in the same emission order — bitwise the compacted-stream result.
+void assemble_filtered(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
+                       const std::uint8_t* d_pinned, cudaEvent_t vals_ready) {
+    cudaStream_t st = c.stream;
+    if (T + n >= (std::int64_t(1) << 32) - 1) throw StatusError(kInvalidArgument, "triplet stream longer than 2^32");
+    DBuf<std::int32_t>& keep = c.pin_keep;
+    DBuf<std::int64_t>& pos = c.pin_pos;
+    DBuf<std::int64_t>& spos = c.pin_spos;
+    keep.reserve(static_cast<std::size_t>(std::max<std::int64_t>(T, n)) + 1);
+    pos.reserve(static_cast<std::size_t>(T) + 1);
+    spos.reserve(static_cast<std::size_t>(n) + 1);
+    c.fkeys.reserve(static_cast<std::size_t>(T + n) + 1);
+    c.fidx.reserve(static_cast<std::size_t>(T + n) + 1);
+    if (T > 0) {
+        k_pin_keep<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, d_pinned, keep.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    exclusive_scan(keep.p, T, pos.p, c.scan_scratch, st);
+    if (T > 0) {
+        k_pin_compact_keys<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, keep.p, pos.p, c.fkeys.p, c.fidx.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    std::int64_t kept = 0, npin = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&kept, pos.p + T, sizeof(kept), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    if (n > 0) {
+        k_u8_to_i32<<<grid_for(n, 256, 16), 256, 0, st>>>(d_pinned, n, keep.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    exclusive_scan(keep.p, n, spos.p, c.scan_scratch, st);
+    if (n > 0) {
+        k_pin_identity_keys<<<grid_for(n, 256, 16), 256, 0, st>>>(d_pinned, n, spos.p, kept, T, c.fkeys.p, c.fidx.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    ADIPC_CUDA(cudaMemcpyAsync(&npin, spos.p + n, sizeof(npin), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    sort_reduce(c, c.fkeys.p, d_vals, kept + npin, n, c.A, c.fidx.p, static_cast<std::uint32_t>(T), vals_ready);
 }
 
 void upload_matrix(Ctx& c, std::int32_t n, std::int64_t U, const std::uint32_t* rows, const std::uint32_t* cols,

@@ -60,6 +60,44 @@ void sync(Ctx& c) { ADIPC_CUDA(cudaStreamSynchronize(c.stream)); }
 
 }  // namespace
 
+namespace {
+// Host-pointer entry points: the keys (and pins) go first on the solve stream;
+// the values (9/10 of the bytes) follow on a copy stream and the key filter
+// and sort run on the device meanwhile — only the reduction waits for them.
+// (From pageable host memory the copies are staged synchronously: still
+// correct, without the overlap.)
+static cudaEvent_t upload_values(Ctx& c, const double* vals9, std::int64_t T) {
+    c.vals.reserve(9 * static_cast<std::size_t>(T));
+    if (!c.copy_stream) {
+        ADIPC_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+        ADIPC_CUDA(cudaEventCreateWithFlags(&c.ev_keys, cudaEventDisableTiming));
+        ADIPC_CUDA(cudaEventCreateWithFlags(&c.ev_vals, cudaEventDisableTiming));
+    }
+    ADIPC_CUDA(cudaEventRecord(c.ev_keys, c.stream));  // after the key upload: keys get the link first
+    ADIPC_CUDA(cudaStreamWaitEvent(c.copy_stream, c.ev_keys, 0));
+    if (T > 0)
+        ADIPC_CUDA(cudaMemcpyAsync(c.vals.p, vals9, sizeof(double) * 9 * static_cast<std::size_t>(T),
+                                   cudaMemcpyHostToDevice, c.copy_stream));
+    ADIPC_CUDA(cudaEventRecord(c.ev_vals, c.copy_stream));
+    return c.ev_vals;
+}
+
+template <class F>
+static void timed(Ctx& c, F&& work) {
+    cudaEvent_t e0, e1;
+    ADIPC_CUDA(cudaEventCreate(&e0));
+    ADIPC_CUDA(cudaEventCreate(&e1));
+    ADIPC_CUDA(cudaEventRecord(e0, c.stream));
+    work();
+    ADIPC_CUDA(cudaEventRecord(e1, c.stream));
+    ADIPC_CUDA(cudaEventSynchronize(e1));
+    ADIPC_CUDA(cudaEventElapsedTime(&c.ms_assemble, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+}
+
+}  // namespace
+
 extern "C" {
 
 int adipc_gpu_create(int device, adipc_gpu_ctx** out) {
@@ -130,7 +168,7 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.counters.free();
     c.pinned.free();
     c.fkeys.free();
-    c.fvals.free();
+    c.fidx.free();
     for (auto& L : c.levels) {
         L->agg.free();
         L->part_of.free();
@@ -183,6 +221,9 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.w.counters.free();
     for (auto e : c.prof_events) cudaEventDestroy(e);
     if (c.side) cudaStreamDestroy(c.side);
+    if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+    if (c.ev_keys) cudaEventDestroy(c.ev_keys);
+    if (c.ev_vals) cudaEventDestroy(c.ev_vals);
     if (c.h_flags) cudaFreeHost(c.h_flags);
     for (auto e : c.ev_chunk)
         if (e) cudaEventDestroy(e);
@@ -269,28 +310,15 @@ int adipc_gpu_last_timings(adipc_gpu_ctx* ctx, float* ms4) {
     return ADIPC_OK;
 }
 
-// ---- assembly -----------------------------------------------------------------
-static void timed_assemble(Ctx& c, const std::uint64_t* k, const double* v, std::int64_t T, std::int32_t n, int det) {
-    cudaEvent_t e0, e1;
-    ADIPC_CUDA(cudaEventCreate(&e0));
-    ADIPC_CUDA(cudaEventCreate(&e1));
-    ADIPC_CUDA(cudaEventRecord(e0, c.stream));
-    assemble(c, k, v, T, n, det);
-    ADIPC_CUDA(cudaEventRecord(e1, c.stream));
-    ADIPC_CUDA(cudaEventSynchronize(e1));
-    ADIPC_CUDA(cudaEventElapsedTime(&c.ms_assemble, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-}
-
+// ---- assembly (helpers: upload_values, timed above the extern block) -----------
 int adipc_gpu_assemble(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T, int32_t n,
                        int det, int64_t* n_unique) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
         if (T < 0 || n < 0) throw StatusError(kInvalidArgument, "negative size");
         h2d(c.keys, keys, static_cast<std::size_t>(T), c.stream);
-        h2d(c.vals, vals9, 9 * static_cast<std::size_t>(T), c.stream);
-        timed_assemble(c, c.keys.p, c.vals.p, T, n, det);
+        cudaEvent_t ready = upload_values(c, vals9, T);
+        timed(c, [&] { assemble(c, c.keys.p, c.vals.p, T, n, det, ready); });
         if (n_unique) *n_unique = c.A.U;
     });
 }
@@ -300,49 +328,35 @@ int adipc_gpu_assemble_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const 
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
         if (T < 0 || n < 0) throw StatusError(kInvalidArgument, "negative size");
-        timed_assemble(c, d_keys, d_vals9, T, n, det);
+        timed(c, [&] { assemble(c, d_keys, d_vals9, T, n, det); });
         if (n_unique) *n_unique = c.A.U;
     });
 }
 
 // filter_pinned + sort_stream + fast_hash_reduction in one call
-// (incremental_potential.hpp:255-257): the raw stream crosses PCIe once.
-static void filtered_assemble(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T,
-                              std::int32_t n, const std::uint8_t* d_pinned, int det) {
-    cudaEvent_t e0, e1;
-    ADIPC_CUDA(cudaEventCreate(&e0));
-    ADIPC_CUDA(cudaEventCreate(&e1));
-    ADIPC_CUDA(cudaEventRecord(e0, c.stream));
-    c.fkeys.reserve(static_cast<std::size_t>(T + n));
-    c.fvals.reserve(9 * static_cast<std::size_t>(T + n));
-    const std::int64_t Tf = filter_pinned(c, d_keys, d_vals, T, d_pinned, n, c.fkeys.p, c.fvals.p);
-    assemble(c, c.fkeys.p, c.fvals.p, Tf, n, det);
-    ADIPC_CUDA(cudaEventRecord(e1, c.stream));
-    ADIPC_CUDA(cudaEventSynchronize(e1));
-    ADIPC_CUDA(cudaEventElapsedTime(&c.ms_assemble, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-}
-
+// (incremental_potential.hpp:255-257): the raw stream crosses PCIe once and
+// the values are never moved on the device (assemble_filtered, assemble.cu).
 int adipc_gpu_assemble_filtered(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T,
                                 int32_t n, const uint8_t* pinned, int det, int64_t* n_unique) {
+    (void)det;  // the device path is always the bitwise-deterministic order
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
         if (T < 0 || n < 0) throw StatusError(kInvalidArgument, "negative size");
         h2d(c.keys, keys, static_cast<std::size_t>(T), c.stream);
-        h2d(c.vals, vals9, 9 * static_cast<std::size_t>(T), c.stream);
         h2d(c.pinned, pinned, static_cast<std::size_t>(n), c.stream);
-        filtered_assemble(c, c.keys.p, c.vals.p, T, n, c.pinned.p, det);
+        cudaEvent_t ready = upload_values(c, vals9, T);
+        timed(c, [&] { assemble_filtered(c, c.keys.p, c.vals.p, T, n, c.pinned.p, ready); });
         if (n_unique) *n_unique = c.A.U;
     });
 }
 
 int adipc_gpu_assemble_filtered_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const double* d_vals9, int64_t T,
                                        int32_t n, const uint8_t* d_pinned, int det, int64_t* n_unique) {
+    (void)det;
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
         if (T < 0 || n < 0) throw StatusError(kInvalidArgument, "negative size");
-        filtered_assemble(c, d_keys, d_vals9, T, n, d_pinned, det);
+        timed(c, [&] { assemble_filtered(c, d_keys, d_vals9, T, n, d_pinned); });
         if (n_unique) *n_unique = c.A.U;
     });
 }

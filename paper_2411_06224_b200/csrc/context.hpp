@@ -107,8 +107,8 @@ struct Ctx {
     DBuf<std::int64_t> row_start, uniq_start, scan_scratch;
     DBuf<std::int32_t> counters;
     DBuf<std::uint8_t> pinned;
-    DBuf<std::uint64_t> fkeys;  // filtered stream (assemble_filtered)
-    DBuf<double> fvals;
+    DBuf<std::uint64_t> fkeys;  // filtered keys (assemble_filtered)
+    DBuf<std::uint32_t> fidx;   // their index in the original stream (0xFFFFFFFF: pinned identity)
     DBuf<std::int32_t> pin_keep;
     DBuf<std::int64_t> pin_pos, pin_spos;
 
@@ -167,6 +167,8 @@ struct Ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // asynchronous done-flag polling of the PCG chunks (pinned, double-buffered)
+    cudaStream_t copy_stream = nullptr;  // value uploads overlapping the key sort (host-pointer assembly)
+    cudaEvent_t ev_keys = nullptr, ev_vals = nullptr;
     int* h_flags = nullptr;
     cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
 
@@ -219,10 +221,17 @@ struct Ctx {
 Ctx* unwrap(adipc_gpu_ctx* c);
 
 // assemble.cu
+// vals_ready: event the reduction waits for (values uploaded on another stream
+// while the keys are sorted), or null
 void assemble(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n_block_rows,
-              int deterministic);
+              int deterministic, cudaEvent_t vals_ready = nullptr);
+void assemble_filtered(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
+                       const std::uint8_t* d_pinned, cudaEvent_t vals_ready = nullptr);
+// d_vidx: emission index of key q (a filtered copy of a stream: increasing
+// indices into d_vals; null: q itself); indices >= identity_from are I3
 void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
-                 DeviceMatrix& out);
+                 DeviceMatrix& out, const std::uint32_t* d_vidx = nullptr, std::uint32_t identity_from = 0xFFFFFFFFu,
+                 cudaEvent_t vals_ready = nullptr);
 void sort_stream(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::uint64_t* d_out_keys,
                  double* d_out_vals);
 void blocks_aos_to_soa(Ctx& c, const double* aos, double* soa, std::int64_t U);

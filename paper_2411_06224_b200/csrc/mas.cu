@@ -591,9 +591,6 @@ __global__ void k_solve_gather(const double* __restrict__ blocks, const std::uin
 
 }  // namespace
 
-void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
-                 DeviceMatrix& out);
-
 // As = P A P^T in solve order (sorted upper block triangle, the same layout
 // as A), rebuilt from the current A values on every preconditioner build:
 // while the pattern and the levels are unchanged (`reuse`), one gather

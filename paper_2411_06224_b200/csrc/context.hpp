@@ -58,7 +58,7 @@ struct DeviceLevel {
     DBuf<std::int64_t> inv_off;    // subdomain -> offset of its packed inverse (16-byte aligned)
     DBuf<double> inv;              // explicit inverses, symmetric-packed upper by columns
     DBuf<std::int64_t> dense_off;  // subdomain -> offset of its dense restricted matrix (build scratch)
-    DBuf<double> dense;            // restricted matrices R A R^T, column-major (build scratch)
+    DBuf<double> dense;            // restricted matrices R A R^T, packed lower triangle by columns (build scratch)
     std::int64_t dense_doubles = 0;
     std::vector<std::int64_t> inv_off_host;
     DBuf<double> y;                // level >= 1: per-node solution (3 per node)

@@ -40,15 +40,25 @@ struct RestrictArgs {
     RestrictLevel lv[kMaxLevels];
 };
 
+// Restricted subdomain matrices are stored packed: the lower triangle by
+// columns, column j (rows j..d-1) starting at lpk_col(d, j). Only the lower
+// triangle is ever read (Cholesky), so tiles above the diagonal are dropped —
+// their transposes land below it.
+__host__ __device__ __forceinline__ int lpk_col(int d, int j) { return j * d - (j * (j - 1)) / 2; }
+__host__ __device__ __forceinline__ std::int64_t lpk_size(std::int64_t d) { return d * (d + 1) / 2; }
+
 __device__ __forceinline__ void add_tile(double* D, int dim, int pr, int pc, const double* h, bool transpose,
                                          bool atomic) {
-    // D column-major: D(3pr+i, 3pc+j) at [(3pc+j)*dim + 3pr+i]; h column-major H(i,j)=h[3j+i]
+    // h column-major H(i,j) = h[3j+i] lands at (3pr+i, 3pc+j) when on or below the diagonal
+    if (pr < pc) return;
 #pragma unroll
     for (int j = 0; j < 3; ++j)
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
+            const int row = 3 * pr + i, col = 3 * pc + j;
+            if (row < col) continue;
             const double v = transpose ? h[3 * i + j] : h[3 * j + i];
-            double* dst = D + static_cast<std::int64_t>(3 * pc + j) * dim + 3 * pr + i;
+            double* dst = D + lpk_col(dim, col) + (row - col);
             if (atomic)
                 atomicAdd(dst, v);
             else
@@ -105,7 +115,7 @@ __global__ void k_invert(std::int32_t n_parts, const std::int32_t* __restrict__ 
         const int nn = dim * dim;
         if (threadIdx.x == 0) {
             double tr = 0;
-            for (int k = 0; k < dim; ++k) tr += D[k * dim + k];
+            for (int k = 0; k < dim; ++k) tr += D[lpk_col(dim, k)];
             double e = 1e-8 * tr / dim;
             if (!(e > 0)) e = 1e-12;
             eps0 = e;
@@ -113,7 +123,10 @@ __global__ void k_invert(std::int32_t n_parts, const std::int32_t* __restrict__ 
         __syncthreads();
         int attempt = 0;
         for (;; ++attempt) {
-            for (int i = threadIdx.x; i < nn; i += blockDim.x) S[i] = D[i];
+            for (int t = threadIdx.x; t < nn; t += blockDim.x) {  // lower triangle of the packed D
+                const int i = t % dim, j = t / dim;
+                if (i >= j) S[t] = D[lpk_col(dim, j) + (i - j)];
+            }
             __syncthreads();
             if (threadIdx.x == 0) {
                 fail = 0;
@@ -183,12 +196,15 @@ __global__ void k_invert(std::int32_t n_parts, const std::int32_t* __restrict__ 
 
 // Warp-per-subdomain variant of k_invert for dim <= 32 R (R rows per lane),
 // same semantics (Cholesky with the mas.hpp:66-81 retry rule, explicit
-// inverse L^-T L^-1 written symmetric-packed). Warp-synchronous: lanes own
-// rows in the factorisation (lane i updates row i of the trailing matrix),
-// columns of W = L^-1 in the triangular inversion (row by row), and columns
-// j of the product W^T W (one packed column k at a time) — no block barriers
-// and no index divisions. Per warp in shared memory: S (dim x dim, column
-// major; L in its lower triangle, W^T in its strict upper one) + diag(W).
+// inverse L^-T L^-1 written symmetric-packed). Warp-synchronous, all in ONE
+// packed lower triangle per warp in shared memory (d(d+1)/2 doubles, so twice
+// the warps of a full d x d work array fit an SM): right-looking Cholesky in
+// place (lane i updates row i of the trailing columns), W = L^-1 in place
+// column by column from the right (W(i,j) = -W(j,j) sum_{k>j} W(i,k) L(k,j),
+// the trailing block already inverted), then the packed upper of W^T W
+// column by column. Column accesses are lane-contiguous; the row reads of the
+// product fall in distinct banks for 16 consecutive columns (triangular
+// offsets).
 // Every level's subdomains in one launch (the levels are independent once
 // restricted): item q of the concatenated list belongs to level l with
 // base[l] <= q < base[l + 1].
@@ -210,23 +226,22 @@ __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __res
                                                     int* __restrict__ shifts, int max_dim) {
     extern __shared__ double sm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double* S = sm + static_cast<std::size_t>(w) * (max_dim * max_dim + max_dim);
-    double* dg = S + max_dim * max_dim;
+    const int slot = static_cast<int>(lpk_size(max_dim) + 1) & ~1;  // 16-byte aligned slots
+    double* S = sm + static_cast<std::size_t>(w) * slot;
     for (std::int32_t q = blockIdx.x * nw + w; q < tab.base[tab.n]; q += gridDim.x * nw) {
         int l = 0;
         while (l + 1 < tab.n && q >= tab.base[l + 1]) ++l;
         const std::int32_t s = q - tab.base[l];
         const std::int32_t* sub_ptr = tab.lv[l].sub_ptr;
-        const std::int64_t* inv_off = tab.lv[l].inv_off;
-        double* inv = tab.lv[l].inv;
         const int d = 3 * (sub_ptr[s + 1] - sub_ptr[s]);
         if (d == 0) continue;
         const double* D = tab.lv[l].dense + tab.lv[l].dense_off[s];
+        const int np = static_cast<int>(lpk_size(d));
         double tr = 0;
 #pragma unroll
         for (int t = 0; t < R; ++t) {
             const int i = lane + 32 * t;
-            if (i < d) tr += D[static_cast<std::int64_t>(i) * d + i];
+            if (i < d) tr += D[lpk_col(d, i)];
         }
         for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
         double eps0 = 1e-8 * tr / d;
@@ -234,51 +249,50 @@ __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __res
         bool fail = true;
         int attempt = 0;
         for (; attempt < 4; ++attempt) {
-            // S = D + cumulative shifts eps, 100 eps, ... (mas.hpp:78-79)
-            for (int q = lane; q < d * d; q += 32) S[q] = D[q];
+            for (int e = lane; e < np; e += 32) S[e] = D[e];
             __syncwarp();
-            if (attempt > 0)
+            if (attempt > 0)  // cumulative shifts eps, 100 eps, ... (mas.hpp:78-79), added in turn
                 for (int i = lane; i < d; i += 32) {
-                    // the reference adds each shift to the diagonal in turn
-                    double x = S[i * d + i], ee = eps0;
+                    double x = S[lpk_col(d, i)], ee = eps0;
                     for (int a = 0; a < attempt; ++a) {
                         x += ee;
                         ee *= 100;
                     }
-                    S[i * d + i] = x;
+                    S[lpk_col(d, i)] = x;
                 }
             __syncwarp();
             fail = false;
             for (int k = 0; k < d; ++k) {
-                const double x = S[k * d + k];
+                const int ok = lpk_col(d, k) - k;  // L(i,k) at S[ok + i]
+                const double x = S[ok + k];
                 if (x <= 0) {  // Eigen LLT: a non-positive pivot fails; NaN does not
                     fail = true;
                     break;
                 }
                 const double piv = sqrt(x);
                 __syncwarp();
-                if (lane == 0) S[k * d + k] = piv;
+                if (lane == 0) S[ok + k] = piv;
 #pragma unroll
                 for (int t = 0; t < R; ++t) {
                     const int i = lane + 32 * t;
-                    if (i > k && i < d) S[k * d + i] /= piv;
+                    if (i > k && i < d) S[ok + i] /= piv;
                 }
                 __syncwarp();
-                // trailing update, uniform over j (broadcast L(j,k), rows i
-                // contiguous across lanes): S(i,j) -= L(i,k) L(j,k), k < j <= i
                 double lik[R];
 #pragma unroll
                 for (int t = 0; t < R; ++t) {
                     const int i = lane + 32 * t;
-                    lik[t] = (i > k && i < d) ? S[k * d + i] : 0.0;
+                    lik[t] = (i > k && i < d) ? S[ok + i] : 0.0;
                 }
+                // trailing update S(i,j) -= L(i,k) L(j,k), k < j <= i
 #pragma unroll 4
                 for (int j = k + 1; j < d; ++j) {
-                    const double ljk = S[k * d + j];
+                    const double ljk = S[ok + j];  // broadcast
+                    const int oj = lpk_col(d, j) - j;
 #pragma unroll
                     for (int t = 0; t < R; ++t) {
                         const int i = lane + 32 * t;
-                        if (i >= j && i < d) S[j * d + i] -= lik[t] * ljk;
+                        if (i >= j && i < d) S[oj + i] -= lik[t] * ljk;
                     }
                 }
                 __syncwarp();
@@ -291,64 +305,64 @@ __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __res
             continue;
         }
         if (lane == 0 && attempt > 0) atomicAdd(shifts, attempt);
-        // W = L^-1 row by row; lane c owns column c (W(k,c), k > c, at S[k*d + c]; W(c,c) in dg)
-        for (int i = 0; i < d; ++i) {
-            const double lii = S[i * d + i];
+        // W = L^-1 in place, columns from the right
+        for (int j = d - 1; j >= 0; --j) {
+            const int oj = lpk_col(d, j) - j;
+            const double wjj = 1.0 / S[oj + j];
             double a0[R], a1[R];
 #pragma unroll
-            for (int t = 0; t < R; ++t) {
-                const int c = lane + 32 * t;
-                // k = c term (diagonal of W) first, then the uniform k loop
-                a0[t] = (c == i) ? 1.0 : ((c < i && c < d) ? -S[c * d + i] * dg[c] : 0.0);
-                a1[t] = 0.0;
-            }
+            for (int t = 0; t < R; ++t) a0[t] = a1[t] = 0.0;
 #pragma unroll 4
-            for (int k = 0; k < i; ++k) {
-                const double lik = S[k * d + i];  // broadcast
+            for (int k = j + 1; k < d; ++k) {
+                const double lkj = S[oj + k];  // L(k,j), broadcast
+                const int okk = lpk_col(d, k) - k;
 #pragma unroll
                 for (int t = 0; t < R; ++t) {
-                    const int c = lane + 32 * t;
-                    if (c < k) {
+                    const int i = lane + 32 * t;
+                    if (i >= k && i < d) {
                         if (k & 1)
-                            a1[t] -= lik * S[k * d + c];
+                            a1[t] += S[okk + i] * lkj;  // W(i,k)
                         else
-                            a0[t] -= lik * S[k * d + c];
+                            a0[t] += S[okk + i] * lkj;
                     }
                 }
             }
+            __syncwarp();  // every read of column j done before it is overwritten
 #pragma unroll
             for (int t = 0; t < R; ++t) {
-                const int c = lane + 32 * t;
-                if (c <= i && c < d) {
-                    const double wic = (a0[t] + a1[t]) / lii;
-                    if (c == i)
-                        dg[c] = wic;
-                    else
-                        S[i * d + c] = wic;
-                }
+                const int i = lane + 32 * t;
+                if (i > j && i < d) S[oj + i] = -wjj * (a0[t] + a1[t]);
             }
+            if (lane == 0) S[oj + j] = wjj;
             __syncwarp();
         }
         // D^-1 = W^T W: packed column k, lanes j <= k: sum_{q >= k} W(q,j) W(q,k)
-        double* P = inv + inv_off[s];
+        double* P = tab.lv[l].inv + tab.lv[l].inv_off[s];
+        int oc[R];  // W(q, j) of lane j at S[oc + q]
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            const int j = min(lane + 32 * t, d - 1);
+            oc[t] = lpk_col(d, j) - j;
+        }
         for (int k = 0; k < d; ++k) {
+            const int ok = lpk_col(d, k) - k;
+            const double wkk = S[ok + k];
             double v0[R], v1[R];
-            const double wkk = dg[k];
 #pragma unroll
             for (int t = 0; t < R; ++t) {
                 const int j = lane + 32 * t;  // q = k term
-                v0[t] = j < k ? S[k * d + j] * wkk : (j == k ? wkk * wkk : 0.0);
+                v0[t] = j < k ? S[oc[t] + k] * wkk : (j == k ? wkk * wkk : 0.0);
                 v1[t] = 0.0;
             }
 #pragma unroll 4
-            for (int q = k + 1; q < d; ++q) {
-                const double wqk = S[q * d + k];  // broadcast
+            for (int q2 = k + 1; q2 < d; ++q2) {
+                const double wqk = S[ok + q2];  // broadcast
 #pragma unroll
                 for (int t = 0; t < R; ++t) {
                     const int j = lane + 32 * t;
                     if (j <= k) {
-                        const double wqj = j == k ? wqk : S[q * d + j];
-                        if (q & 1)
+                        const double wqj = j == k ? wqk : S[oc[t] + q2];
+                        if (q2 & 1)
                             v1[t] += wqj * wqk;
                         else
                             v0[t] += wqj * wqk;
@@ -412,12 +426,12 @@ void build_level(Ctx& c, DeviceLevel& L, const host::Level& hl, int level, std::
     for (std::int32_t s = 0; s < hl.n_parts; ++s) max_fill = std::max(max_fill, sub_ptr[s + 1]);
     for (std::int32_t s = 0; s < hl.n_parts; ++s) sub_ptr[s + 1] += sub_ptr[s];
     for (std::int32_t v = 0; v < hl.n_nodes; ++v) sub_nodes[sub_ptr[hl.part_of[v]] + pos_of[v]] = v;
-    // dense restricted matrices (build scratch, full d x d) and the packed
+    // restricted matrices (build scratch, packed lower triangle) and the packed
     // inverses (d(d+1)/2, padded to 16 B so each is one TMA bulk copy)
     std::vector<std::int64_t> inv_off(hl.n_parts + 1, 0), dense_off(hl.n_parts + 1, 0);
     for (std::int32_t s = 0; s < hl.n_parts; ++s) {
         const std::int64_t d = 3 * static_cast<std::int64_t>(sub_ptr[s + 1] - sub_ptr[s]);
-        dense_off[s + 1] = dense_off[s] + d * d;
+        dense_off[s + 1] = dense_off[s] + lpk_size(d);  // packed lower triangle
         inv_off[s + 1] = inv_off[s] + packed_doubles(static_cast<int>(d));
     }
     L.max_fill = max_fill;
@@ -656,7 +670,7 @@ void factorize(Ctx& c) {
     }
     if (tab.n > 0) {
         const int nw = 4;
-        const std::size_t wsm = sizeof(double) * nw * (static_cast<std::size_t>(wdim) * wdim + wdim);
+        const std::size_t wsm = sizeof(double) * nw * static_cast<std::size_t>((lpk_size(wdim) + 1) & ~1);
         int sms = kSMs;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
         const int grid = static_cast<int>(

@@ -270,13 +270,17 @@ def run_ours(args, rank, world, local_rank, dist):
         prof = ctx.pcg_profile()
         return res, t, prof
 
-    # first warm-up step: cold MAS build (hierarchy from the pattern); later
-    # steps reuse it while the pattern hash is unchanged (the hierarchy is a
+    # first two warm-up steps: cold MAS builds (hierarchy from the pattern) —
+    # the first one also pays the process's one-time allocations and module
+    # loads, the second is a new-pattern rebuild in a running solver; later
+    # steps reuse the hierarchy while the pattern hash is unchanged (it is a
     # pure function of the pattern), as a Newton loop without contact changes
-    cold = None
+    cold = first = None
     for i in range(args.warmup):
         _, t, _ = step()
         if i == 0:
+            first = cold = t
+        if i == 1:
             cold = t
         if i == 0 and not args.no_cache:
             ctx.set_option(_lib.OPT_CACHE_HIERARCHY, 1)
@@ -360,6 +364,7 @@ def run_ours(args, rank, world, local_rank, dist):
             "mas_build_host_ms": build_host_ms / args.steps,
             "mas_build_cold_ms": cold["build_ms"] if cold else None,
             "mas_build_cold_host_ms": cold["build_host_ms"] if cold else None,
+            "mas_build_first_ms": first["build_ms"] if first else None,
             "hierarchy_cache": not args.no_cache,
             "pcg_ms": pcg_ms / args.steps,
             "pcg_iters_per_solve": iters / args.steps,

@@ -210,53 +210,91 @@ __global__ void k_sort_rows_cta(std::uint64_t* __restrict__ sorted, std::uint64_
 // One warp per row: every head lane (first element of a unique col) sums its
 // run sequentially in emission order and writes the unique block into the
 // tiled block storage (blk(), common.cuh).
-__global__ void k_reduce_rows(const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
-                              const std::int64_t* __restrict__ uniq_start, std::int32_t n,
-                              const double* __restrict__ vals, std::uint32_t* __restrict__ out_rows,
-                              std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks, std::int64_t U,
-                              std::uint32_t identity_from) {
+// One warp per row, windows of 32 sorted entries: every lane loads its own
+// entry's block (all loads of a window in flight at once) into the warp's
+// shared tile, then each run's owner folds it SEQUENTIALLY in emission order
+// (bitwise the reference's deterministic left-to-right sum, reduction.hpp:
+// 39-53); a run crossing the window boundary carries its partial sum (and
+// output slot) to lane 0 of the next window. Writes the unique blocks into
+// the tiled block storage (blk(), common.cuh).
+constexpr int kReduceWarps = 8;
+__global__ void __launch_bounds__(32 * kReduceWarps) k_reduce_rows(
+    const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
+    const std::int64_t* __restrict__ uniq_start, std::int32_t n, const double* __restrict__ vals,
+    std::uint32_t* __restrict__ out_rows, std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks,
+    std::int64_t U, std::uint32_t identity_from) {
     // value of emission index q: vals[9 q]; q >= identity_from is an appended
     // pinned-diagonal I3 (filtered streams, assemble_filtered)
-    auto value = [&](std::uint32_t src, double* out) {
-        if (src >= identity_from) {
-#pragma unroll
-            for (int k = 0; k < 9; ++k) out[k] = (k % 4 == 0) ? 1.0 : 0.0;
-        } else {
-            const double* v = vals + 9 * static_cast<std::int64_t>(src);
-#pragma unroll
-            for (int k = 0; k < 9; ++k) out[k] = v[k];
-        }
-    };
+    __shared__ double tile[kReduceWarps][9][32];
+    __shared__ double carry[kReduceWarps][9];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
+    double(*T)[32] = tile[w];
+    double* C = carry[w];
     for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps) {
         const std::int64_t b = row_start[r], e = row_start[r + 1];
         std::int64_t u = uniq_start[r];
+        bool carried = false;       // a run continues into this window (warp-uniform)
+        std::int64_t carry_u = 0;   // its output slot
         for (std::int64_t base = b; base < e; base += 32) {
             const std::int64_t p = base + lane;
             const bool valid = p < e;
-            const std::uint64_t v = valid ? sorted[p] : 0;
+            const std::uint64_t v = valid ? sorted[p] : ~0ull;
             const std::uint32_t col = static_cast<std::uint32_t>(v >> 32);
-            const bool head = valid && (p == b || static_cast<std::uint32_t>(sorted[p - 1] >> 32) != col);
-            const unsigned hm = __ballot_sync(0xffffffffu, head);
-            if (head) {
-                const std::int64_t my_u = u + __popc(hm & ((1u << lane) - 1u));
-                double acc[9];
-                value(static_cast<std::uint32_t>(v), acc);
-                for (std::int64_t q = p + 1; q < e; ++q) {
-                    const std::uint64_t w2 = sorted[q];
-                    if (static_cast<std::uint32_t>(w2 >> 32) != col) break;
-                    double s2[9];
-                    value(static_cast<std::uint32_t>(w2), s2);
+            const std::uint32_t prev_col = __shfl_up_sync(0xffffffffu, col, 1);
+            bool head = valid && (lane == 0 ? (p == b || static_cast<std::uint32_t>(sorted[p - 1] >> 32) != col)
+                                            : prev_col != col);
+            if (valid) {
+                const std::uint32_t src = static_cast<std::uint32_t>(v);
+                if (src >= identity_from) {
 #pragma unroll
-                    for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(acc[k], s2[k]);
+                    for (int k = 0; k < 9; ++k) T[k][lane] = (k % 4 == 0) ? 1.0 : 0.0;
+                } else {
+                    const double* sv = vals + 9 * static_cast<std::int64_t>(src);
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) T[k][lane] = sv[k];
                 }
-                out_rows[my_u] = static_cast<std::uint32_t>(r);
-                out_cols[my_u] = col;
-#pragma unroll
-                for (int k = 0; k < 9; ++k) out_blocks[blk(my_u, k)] = acc[k];
             }
+            // does the window's last run continue past it?
+            const std::int64_t nxt = base + 32;
+            const bool cont_out = __shfl_sync(0xffffffffu, nxt < e && lane == 31 &&
+                                                               static_cast<std::uint32_t>(sorted[nxt] >> 32) == col,
+                                              31);
+            const unsigned hm = __ballot_sync(0xffffffffu, head);
+            const int nv = static_cast<int>(e - base < 32 ? e - base : 32);
+            __syncwarp();
+            const bool owner = head || (lane == 0 && carried);
+            if (owner) {
+                // run [lane, end): up to the next head of the window or its valid end
+                const unsigned later = hm & ~((2u << lane) - 1u);
+                const int end = later ? __ffs(later) - 1 : nv;
+                double acc[9];
+                if (head) {
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) acc[k] = T[k][lane];
+                } else {  // continuing run: carried sum, then this window's entries
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(C[k], T[k][lane]);
+                }
+                for (int j = lane + 1; j < end; ++j)
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(acc[k], T[k][j]);
+                const std::int64_t my_u = head ? u + __popc(hm & ((1u << lane) - 1u)) : carry_u;
+                if (end == nv && cont_out) {  // hand over to the next window
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) C[k] = acc[k];
+                } else {
+                    out_rows[my_u] = static_cast<std::uint32_t>(r);
+                    out_cols[my_u] = col;
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) out_blocks[blk(my_u, k)] = acc[k];
+                }
+            }
+            // the continuing run's slot: the last head's, or the one already carried
+            if (cont_out) carry_u = hm ? u + __popc(hm) - 1 : carry_u;
+            carried = cont_out;
             u += __popc(hm);
+            __syncwarp();
         }
     }
 }

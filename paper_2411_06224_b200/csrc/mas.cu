@@ -223,12 +223,17 @@ struct InvertTable {
 
 template <int R>
 __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __restrict__ status,
-                                                    int* __restrict__ shifts, int max_dim) {
+                                                    int* __restrict__ shifts, int* __restrict__ next, int max_dim) {
     extern __shared__ double sm[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int slot = static_cast<int>(lpk_size(max_dim) + 1) & ~1;  // 16-byte aligned slots
     double* S = sm + static_cast<std::size_t>(w) * slot;
-    for (std::int32_t q = blockIdx.x * nw + w; q < tab.base[tab.n]; q += gridDim.x * nw) {
+    // resident grid, items taken dynamically (their cost varies with dim and retries)
+    for (;;) {
+        std::int32_t q = 0;
+        if (lane == 0) q = atomicAdd(next, 1);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q >= tab.base[tab.n]) break;
         int l = 0;
         while (l + 1 < tab.n && q >= tab.base[l + 1]) ++l;
         const std::int32_t s = q - tab.base[l];
@@ -654,8 +659,8 @@ void factorize(Ctx& c) {
         k_restrict<<<grid_for(A.U, 256, 16), 256, 0, st>>>(A.rows.p, A.cols.p, A.blocks.p, A.U, ra);
         ADIPC_LAUNCH_CHECK();
     }
-    c.build_status.reserve(2);
-    ADIPC_CUDA(cudaMemsetAsync(c.build_status.p, 0, 2 * sizeof(int), st));
+    c.build_status.reserve(3);  // failure flag, shifts applied, work counter
+    ADIPC_CUDA(cudaMemsetAsync(c.build_status.p, 0, 3 * sizeof(int), st));
     // warp-per-subdomain levels (dim <= 64): one launch for all of them
     InvertTable tab{};
     int wdim = 0;
@@ -673,15 +678,18 @@ void factorize(Ctx& c) {
         const std::size_t wsm = sizeof(double) * nw * static_cast<std::size_t>((lpk_size(wdim) + 1) & ~1);
         int sms = kSMs;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-        const int grid = static_cast<int>(
-            std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(tab.base[tab.n], nw), sms * 8)));
-        if (wdim <= 32) {
-            ADIPC_CUDA(cudaFuncSetAttribute(k_invert_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
-            k_invert_warp<1><<<grid, 32 * nw, wsm, st>>>(tab, c.build_status.p, c.build_status.p + 1, wdim);
-        } else {
-            ADIPC_CUDA(cudaFuncSetAttribute(k_invert_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
-            k_invert_warp<2><<<grid, 32 * nw, wsm, st>>>(tab, c.build_status.p, c.build_status.p + 1, wdim);
-        }
+        auto run = [&](auto kernel) {
+            ADIPC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm)));
+            int occ = 0;
+            ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 32 * nw, wsm));
+            const int grid = static_cast<int>(std::max<std::int64_t>(
+                1, std::min<std::int64_t>(ceil_div(tab.base[tab.n], nw), static_cast<std::int64_t>(sms) * std::max(occ, 1))));
+            kernel<<<grid, 32 * nw, wsm, st>>>(tab, c.build_status.p, c.build_status.p + 1, c.build_status.p + 2, wdim);
+        };
+        if (wdim <= 32)
+            run(k_invert_warp<1>);
+        else
+            run(k_invert_warp<2>);
         ADIPC_LAUNCH_CHECK();
     }
     for (auto& Lp : c.levels) {

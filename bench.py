@@ -338,7 +338,11 @@ def run_ours(args, rank, world, local_rank, dist):
                             "achieved_gbs": bm[bkey] / avg_s / 1e9 if avg_s > 0 else None}
         dom = max(kernels, key=lambda k: kernels[k]["avg_ms"])
         dk = kernels[dom]
-        iter_s = (prof["spmv_ms"] + prof["update_ms"] + prof["precond_ms"] + prof["final_ms"]) / max(prof["iters"], 1) / 1e3
+        # per-iteration time inside the timed region (CUDA graphs, kernels chained
+        # by programmatic dependent launch), per scene; and the per-class event
+        # sum of the profiled solve (direct launches, no overlap) for reference
+        iter_s = (max_pcg / 1000.0) / max(all_iters / world, 1)
+        iter_s_classes = (prof["spmv_ms"] + prof["update_ms"] + prof["precond_ms"] + prof["final_ms"]) / max(prof["iters"], 1) / 1e3
         out = {
             "metric": METRIC,
             "value": all_iters / (max_pcg / 1000.0),
@@ -384,7 +388,8 @@ def run_ours(args, rank, world, local_rank, dist):
                          "traffic": ncu_traffic().get(dom), "traffic_source": "profiles/ncu_traffic.json"},
             "roofline_pcg_iteration": {"bound": "hbm", "bytes_per_iter": bm["total"],
                                        "achieved": bm["total"] / iter_s / 1e9, "peak": hbm, "unit": "GB/s",
-                                       "frac": bm["total"] / iter_s / 1e9 / hbm},
+                                       "frac": bm["total"] / iter_s / 1e9 / hbm, "iter_us": iter_s * 1e6,
+                                       "iter_us_class_sum": iter_s_classes * 1e6},
             # context for the fractions above: the read bandwidth ONE kernel of
             # this size reaches on this B200 with a cold L2 and no compute
             # (tools/stream_read_bench.cu; profiles/r01f_summary.md): 50 MB

@@ -347,3 +347,26 @@ def test_pcg_shell_and_contact_configs(ctx, name, kind):
         assert err(x) <= 1.25 * err(xo), (err(x), err(xo))
     else:
         assert np.linalg.norm(x - xo) <= 1e-5 * np.linalg.norm(xo)
+
+
+@pytest.mark.parametrize("capacity", [8, 32])
+def test_pcg_other_subdomain_capacities(ctx, capacity):
+    """cemas8 / cemas32 on the beam: subdomain dimensions up to 24 / 96 take
+    the other kernel instantiations (24- and 96-column preconditioner
+    mat-vecs; for 96 the block-per-subdomain inversion) — iteration counts
+    +-2 % and solutions within 1e-5 of the oracle."""
+    sc = scenes.CONFIGS["stiff_beam"]()
+    fk, fv = ctx.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    ctx.assemble(fk, fv, sc.n_blocks)
+    n, rows, cols, blocks = ctx.copy_matrix()
+    l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, capacity)
+    ctx.set_level0_partition(l0.part_of, l0.n_parts, capacity, 4)
+    ctx.build_preconditioner(1)
+    b = scenes.gravity_rhs(sc)
+    x, r = ctx.pcg(b, 1e-4, 250, 100000)
+    Am = O.Matrix(n, rows, cols, blocks)
+    M = O.MasPreconditioner(Am, O.Hierarchy(l0.part_of, l0.n_parts, capacity, O.block_edges(rows, cols), 4))
+    xo, ro = O.pcg_solve(Am, b, M, 1e-4, 250, 100000)
+    assert r.converged and ro["converged"]
+    assert abs(r.iters - ro["iters"]) <= max(1, 0.02 * ro["iters"]), (r.iters, ro["iters"])
+    assert np.linalg.norm(x - xo) <= 1e-5 * np.linalg.norm(xo)

@@ -124,6 +124,9 @@ int adipc_gpu_create(int device, adipc_gpu_ctx** out) {
         if (ctx->c.final_per == 3) ctx->c.final_per = 2;
         env_int("ADIPC_FINAL_BLOCK", 64, 512, ctx->c.final_block);
         env_int("ADIPC_PC_PAIRS", 1, 5, ctx->c.pc_pairs);
+        int ps = 0;
+        env_int("ADIPC_PC_SPLIT", 0, 1, ps);  // cost-weighted preconditioner split (measured slower)
+        ctx->c.pc_split = ps != 0;
         env_int("ADIPC_WS_CONS", 4, 10, ctx->c.ws_cons);
         env_int("ADIPC_L0_KEEP", 0, 1024, ctx->c.l0_keep_1024);
         int iw = 1;

@@ -223,3 +223,27 @@ def test_against_compiled_reference(ctx, name):
             keys, vals = np.concatenate([keys, rk]), np.concatenate([vals, rv])
         want = oracle_assemble(keys, vals, sc.n_blocks)
     assert_bitwise(gpu_assemble(ctx, keys, vals, sc.n_blocks), want)
+
+
+@pytest.mark.parametrize("case", ["empty", "all_pinned", "none_pinned", "random"])
+def test_assemble_filtered_edge_cases(ctx, case):
+    """filter_pinned on the keys only (values read in place through the
+    original emission index, pinned identities appended after the stream):
+    an empty stream, every slot pinned (A = identity), nothing pinned, and a
+    random stream with duplicate keys touching pinned rows."""
+    rng = np.random.default_rng(7)
+    n = 40
+    if case == "empty":
+        keys, vals = np.zeros(0, np.uint64), np.zeros((0, 9))
+    else:
+        r = rng.integers(0, n, 3000)
+        c = rng.integers(0, n, 3000)
+        lo, hi = np.minimum(r, c), np.maximum(r, c)
+        keys = ((lo.astype(np.uint64) << np.uint64(32)) | hi.astype(np.uint64)).astype(np.uint64)
+        vals = rng.standard_normal((3000, 9))
+    pinned = {"empty": rng.integers(0, 2, n), "all_pinned": np.ones(n), "none_pinned": np.zeros(n),
+              "random": (rng.random(n) < 0.2)}[case].astype(np.uint8)
+    ok, ov = O.filter_pinned(keys, vals, pinned)
+    want = oracle_assemble(ok, ov, n)
+    ctx.assemble_filtered(keys, vals, n, pinned)
+    assert_bitwise(ctx.copy_matrix()[1:], want)

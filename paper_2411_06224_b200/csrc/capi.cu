@@ -172,26 +172,7 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.pinned.free();
     c.fkeys.free();
     c.fidx.free();
-    for (auto& L : c.levels) {
-        L->agg.free();
-        L->part_of.free();
-        L->pos_of.free();
-        L->sub_ptr.free();
-        L->sub_nodes.free();
-        L->up_first.free();
-        L->upc_ptr.free();
-        L->upc_pos.free();
-        L->upc_node.free();
-        L->up_node.free();
-        L->anc.free();
-        L->rr.free();
-        L->inv_off.free();
-        L->inv.free();
-        L->dense.free();
-        L->dense_off.free();
-        L->y.free();
-    }
-    c.levels.clear();
+    c.levels.clear();  // ~DeviceLevel releases the level buffers
     c.jinv.free();
     c.build_status.free();
     c.sell.slice_off.free();

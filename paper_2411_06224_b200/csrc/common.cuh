@@ -82,9 +82,13 @@ struct DBuf {
             n = count;
             return;
         }
+        // growing an existing buffer leaves 25 % headroom, so sizes that
+        // fluctuate (contact patterns between Newton iterations) do not
+        // reallocate every time
+        const std::size_t want = cap ? count + count / 4 : count;
         if (p) cudaFree(p);
         p = nullptr;
-        std::size_t c = count < 1 ? 1 : count;
+        std::size_t c = want < 1 ? 1 : want;
         ADIPC_CUDA(cudaMalloc(&p, c * sizeof(T)));
         cap = c;
         n = count;

@@ -64,6 +64,18 @@ struct DeviceLevel {
     DBuf<double> y;                // level >= 1: per-node solution (3 per node)
     std::int64_t inv_doubles = 0;
     int max_fill = 0;
+    void release() {
+        for (auto* b : {&agg, &part_of, &pos_of, &sub_ptr, &sub_nodes, &up_first, &upc_ptr, &upc_pos, &upc_node,
+                        &up_node, &anc})
+            b->free();
+        for (auto* b : {&rr, &inv, &dense, &y}) b->free();
+        inv_off.free();
+        dense_off.free();
+    }
+    DeviceLevel() = default;
+    DeviceLevel(const DeviceLevel&) = delete;
+    DeviceLevel& operator=(const DeviceLevel&) = delete;
+    ~DeviceLevel() { release(); }
 };
 
 enum PrecondKind : int { kNone = 0, kMas = 1, kJacobi = 2 };

@@ -559,15 +559,19 @@ void set_levels(Ctx& c, const host::MasHierarchy& h) {
         std::fprintf(stderr, "set_levels %s %.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
         t = now;
     };
-    c.levels.clear();
-    lap("free");
+    // level objects (and their device buffers, which only grow) are reused
+    // across rebuilds: a new sparsity pattern costs no cudaFree / cudaMalloc
+    // of the ~400 MB of level storage
+    const std::size_t n_lv = static_cast<std::size_t>(h.n_levels());
+    if (c.levels.size() > n_lv) c.levels.resize(n_lv);
+    while (c.levels.size() < n_lv) c.levels.emplace_back(new DeviceLevel());
+    lap("levels");
     const bool perm = c.solve_order && h.n_levels() > 0 && h.n_slots > 0;
     const host::MasHierarchy hp = perm ? to_solve_order(c, h) : host::MasHierarchy{};
     const host::MasHierarchy& hl = perm ? hp : h;
     lap("to_solve_order");
     for (int l = 0; l < hl.n_levels(); ++l) {
-        c.levels.emplace_back(new DeviceLevel());
-        build_level(c, *c.levels.back(), hl.levels[l], l, c.A.n);
+        build_level(c, *c.levels[l], hl.levels[l], l, c.A.n);
         lap("build_level");
     }
     link_levels(c, hl);

@@ -98,6 +98,9 @@ int adipc_gpu_assemble_filtered_device(adipc_gpu_ctx* ctx, const uint64_t* d_key
 int adipc_gpu_matrix_info(adipc_gpu_ctx* ctx, int32_t* n_block_rows, int64_t* n_blocks);
 /* copy SortedSymBlockCoo{rows, cols, blocks} out (block_coo.hpp:54-61) */
 int adipc_gpu_copy_matrix(adipc_gpu_ctx* ctx, uint32_t* rows, uint32_t* cols, double* blocks9);
+/* dump_block_coo (adipc/sparse/srbk_spmv.hpp:52-60; the CLI's --dump-hessian, adipc_cli.cpp:107-113) of
+ * the context's matrix into a text file, byte-identical to the reference's output */
+int adipc_gpu_dump_block_coo(adipc_gpu_ctx* ctx, const char* path);
 /* upload an existing SortedSymBlockCoo (strictly increasing keys) */
 int adipc_gpu_set_matrix(adipc_gpu_ctx* ctx, int32_t n_block_rows, int64_t n_blocks, const uint32_t* rows,
                          const uint32_t* cols, const double* blocks9);

@@ -297,6 +297,25 @@ def fast_segment_reduction(O, V, n_segments, policy=None):
     return R[:, 0].copy() if width == 1 else R.copy()
 
 
+def reference_dump_block_coo(n_block_rows, rows, cols, blocks) -> str:
+    """The reference's own dump_block_coo (srbk_spmv.hpp:52-60), compiled in
+    oracle/_ref: the text the CLI's --dump-hessian writes."""
+    if not reference_available():
+        raise RuntimeError("oracle/_ref unavailable")
+    f = C.CDLL(_REF_PATH).ref_dump_block_coo
+    f.restype = C.c_int64
+    U = len(rows)
+    r = np.ascontiguousarray(rows, np.uint32) if U else np.zeros(1, np.uint32)
+    c = np.ascontiguousarray(cols, np.uint32) if U else np.zeros(1, np.uint32)
+    b = np.ascontiguousarray(blocks, np.float64).reshape(-1) if U else np.zeros(9)
+    args = [C.c_int32(n_block_rows), C.c_size_t(U), r.ctypes.data_as(C.c_void_p), c.ctypes.data_as(C.c_void_p),
+            b.ctypes.data_as(C.c_void_p)]
+    size = f(*args, None, C.c_size_t(0))
+    buf = C.create_string_buffer(size + 1)
+    f(*args, buf, C.c_size_t(size + 1))
+    return buf.raw[:size].decode()
+
+
 def srbk_spmv(n_block_rows, rows, cols, blocks, x, policy=None):
     x = np.ascontiguousarray(x, np.float64).reshape(-1)
     nx = len(x) // 3

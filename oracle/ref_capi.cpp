@@ -14,6 +14,7 @@
 // energy stack) and the MAS shift count (the reference does not record it).
 #include <cstring>
 #include <random>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 
@@ -180,6 +181,17 @@ void ref_srbk_spmv(std::int32_t n_block_rows, std::size_t U, const std::uint32_t
     for (std::size_t i = 0; i < nx; ++i) std::memcpy(xv[i].data(), x + 3 * i, 24);
     const auto yv = srbk_spmv(A, xv, make_pol(det, threads, lw));
     for (std::size_t i = 0; i < nx; ++i) std::memcpy(y + 3 * i, yv[i].data(), 24);
+}
+
+// dump_block_coo (srbk_spmv.hpp:52-60) into `out` (cap bytes); returns the text length
+std::int64_t ref_dump_block_coo(std::int32_t n_block_rows, std::size_t U, const std::uint32_t* rows,
+                                const std::uint32_t* cols, const double* blocks, char* out, std::size_t cap) {
+    const SortedSymBlockCoo A = load_matrix(n_block_rows, U, rows, cols, blocks);
+    std::ostringstream os;
+    dump_block_coo(A, os);
+    const std::string t = os.str();
+    if (out && cap >= t.size()) std::memcpy(out, t.data(), t.size());
+    return static_cast<std::int64_t>(t.size());
 }
 
 int ref_split(int kind, std::int32_t rb, std::int32_t cb, const double* H, std::uint64_t* keys, double* vals) {

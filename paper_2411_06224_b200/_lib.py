@@ -50,6 +50,7 @@ GPU_SIGNATURES = {
     "adipc_gpu_assemble_filtered_device": (ci, [vp, vp, vp, i64, i32, vp, ci, C.POINTER(i64)]),
     "adipc_gpu_matrix_info": (ci, [vp, C.POINTER(i32), C.POINTER(i64)]),
     "adipc_gpu_copy_matrix": (ci, [vp, vp, vp, vp]),
+    "adipc_gpu_dump_block_coo": (ci, [vp, C.c_char_p]),
     "adipc_gpu_set_matrix": (ci, [vp, i32, i64, vp, vp, vp]),
     "adipc_gpu_set_matrix_device": (ci, [vp, i32, i64, vp, vp, vp]),
     "adipc_gpu_sort_stream": (ci, [vp, vp, vp, i64]),

@@ -171,11 +171,14 @@ def srbk_spmv(A: SortedSymBlockCoo, x, pol: ExecPolicy | None = None):
 
 
 def dump_block_coo(A: SortedSymBlockCoo, f) -> None:
-    """srbk_spmv.hpp:52-60: 'n U' header, then 'row col' + 9 values row-major per block."""
+    """srbk_spmv.hpp:52-60: 'n U' header, then 'row col' + the 9 values
+    row-major per block, each as a default-formatted C++ ostream double
+    (printf %g: 6 significant digits) — byte-identical to the reference's
+    --dump-hessian text."""
     f.write(f"{A.n_block_rows} {A.size()}\n")
     for r, c, b in zip(A.rows, A.cols, A.blocks):
-        nat = np.asarray(b).reshape(3, 3).T
-        f.write(f"{r} {c} " + " ".join(repr(float(v)) for v in nat.reshape(-1)) + "\n")
+        nat = np.asarray(b, np.float64).reshape(3, 3).T  # column-major storage -> row-major
+        f.write(f"{int(r)} {int(c)} " + " ".join("%g" % float(v) for v in nat.reshape(-1)) + "\n")
 
 
 # -- block_split.hpp:10-33 (host tiling helpers used by producers) -----------

@@ -144,6 +144,10 @@ class Context:
         self._check(self._L.adipc_gpu_matrix_info(self.h, C.byref(n), C.byref(U)))
         return n.value, U.value
 
+    def dump_block_coo(self, path):
+        """srbk_spmv.hpp:52-60 of the device matrix (--dump-hessian text)."""
+        self._check(self._L.adipc_gpu_dump_block_coo(self.h, str(path).encode()))
+
     def copy_matrix(self):
         n, U = self.matrix_info()
         rows = np.empty(U, np.uint32)

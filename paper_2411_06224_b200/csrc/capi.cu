@@ -3,6 +3,7 @@
 // records the message on the context.
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <vector>
 
 #include "../../include/adipc_gpu.h"
@@ -365,6 +366,38 @@ int adipc_gpu_copy_matrix(adipc_gpu_ctx* ctx, uint32_t* rows, uint32_t* cols, do
             ADIPC_CUDA(cudaMemcpyAsync(blocks9, c.vals.p, 72 * U, cudaMemcpyDeviceToHost, c.stream));
         }
         sync(c);
+    });
+}
+
+// dump_block_coo (srbk_spmv.hpp:52-60) of the context's matrix — the CLI's
+// --dump-hessian text: "n U", then per block "row col" and the 9 values
+// row-major, default-formatted doubles
+int adipc_gpu_dump_block_coo(adipc_gpu_ctx* ctx, const char* path) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (!path) throw StatusError(kInvalidArgument, "dump_block_coo: null path");
+        const std::int64_t U = c.A.U;
+        std::vector<std::uint32_t> rows(static_cast<std::size_t>(U)), cols(static_cast<std::size_t>(U));
+        std::vector<double> b(9 * static_cast<std::size_t>(U));
+        if (U > 0) {
+            ADIPC_CUDA(cudaMemcpyAsync(rows.data(), c.A.rows.p, 4 * U, cudaMemcpyDeviceToHost, c.stream));
+            ADIPC_CUDA(cudaMemcpyAsync(cols.data(), c.A.cols.p, 4 * U, cudaMemcpyDeviceToHost, c.stream));
+            c.vals.reserve(9 * U);
+            blocks_soa_to_aos(c, c.A.blocks.p, c.vals.p, U);
+            ADIPC_CUDA(cudaMemcpyAsync(b.data(), c.vals.p, 72 * U, cudaMemcpyDeviceToHost, c.stream));
+            sync(c);
+        }
+        std::ofstream os(path);
+        if (!os) throw StatusError(kInvalidArgument, std::string("dump_block_coo: cannot open ") + path);
+        os << c.A.n << " " << U << "\n";
+        for (std::int64_t e = 0; e < U; ++e) {
+            os << rows[e] << " " << cols[e];
+            const double* m = b.data() + 9 * e;  // column-major block
+            for (int i = 0; i < 3; ++i)
+                for (int k = 0; k < 3; ++k) os << " " << m[3 * k + i];
+            os << "\n";
+        }
+        if (!os) throw StatusError(kInvalidArgument, std::string("dump_block_coo: write failed: ") + path);
     });
 }
 

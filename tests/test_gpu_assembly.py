@@ -247,3 +247,22 @@ def test_assemble_filtered_edge_cases(ctx, case):
     want = oracle_assemble(ok, ov, n)
     ctx.assemble_filtered(keys, vals, n, pinned)
     assert_bitwise(ctx.copy_matrix()[1:], want)
+
+
+def test_dump_block_coo_from_device(ctx, tmp_path):
+    """adipc_gpu_dump_block_coo (--dump-hessian, srbk_spmv.hpp:52-60) writes the
+    device matrix as the same text as api.dump_block_coo, which the CPU suite
+    checks byte for byte against the reference's own dump."""
+    import io
+
+    sc = scenes.CONFIGS["cfg1_soft_cube"]()
+    fk, fv = ctx.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    ctx.assemble(fk, fv, sc.n_blocks)
+    path = tmp_path / "hess.txt"
+    ctx.dump_block_coo(path)
+    n, rows, cols, blocks = ctx.copy_matrix()
+    f = io.StringIO()
+    P.dump_block_coo(P.SortedSymBlockCoo(n, rows, cols, blocks), f)
+    assert path.read_text() == f.getvalue()
+    with pytest.raises(InvalidArgument):
+        ctx.dump_block_coo(tmp_path / "missing_dir" / "x.txt")

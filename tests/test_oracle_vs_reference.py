@@ -105,3 +105,21 @@ def test_partition_hierarchy_mas_pcg(name):
     # the product's host partition follows the same rules (host_precond.cpp)
     l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, 16)
     assert np.array_equal(l0.part_of, rb[0])
+
+
+def test_dump_block_coo_text_identical():
+    """api.dump_block_coo (the --dump-hessian wire format, srbk_spmv.hpp:52-60)
+    is byte-identical to the reference's own dump, including exponents,
+    negative zeros and values needing more than 6 significant digits."""
+    import io
+
+    from paper_2411_06224_b200 import api as P
+
+    rows, cols, blocks = assembled(scenes.CONFIGS["cfg1_soft_cube"]())
+    blocks = blocks.copy()
+    blocks[0, :4] = [-0.0, 1e-300, 123456789.0, -2.5e17]
+    want = O.reference_dump_block_coo(1728, rows, cols, blocks)
+    f = io.StringIO()
+    P.dump_block_coo(P.SortedSymBlockCoo(1728, rows, cols, blocks), f)
+    assert f.getvalue() == want
+    assert want.splitlines()[0] == f"1728 {len(rows)}"

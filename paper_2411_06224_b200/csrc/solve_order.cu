@@ -1878,11 +1878,6 @@ void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, dou
     const int kk = matvec_cols(fill);
     const int slot = static_cast<int>(packed_doubles(kk));
     const int stages = c.l0_stages;
-    // per warp pair: the ring + two b vectors + barriers; up to 4 pairs per
-    // CTA, two CTAs per SM
-    const std::size_t per_pair = (sizeof(double) * slot + sizeof(std::uint64_t)) * stages + 2 * sizeof(double) * kk;
-    const int pairs = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(4, (113u * 1024u) / per_pair)));
-    const std::size_t smem = per_pair * pairs;
     int sms = kSMs;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
     if (c.pc_variant == 3 && kk <= 48) {  // warp-specialised: producer + consumers, CTA-wide ring

@@ -290,15 +290,17 @@ __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __res
                     lik[t] = (i > k && i < d) ? S[ok + i] : 0.0;
                 }
                 // trailing update S(i,j) -= L(i,k) L(j,k), k < j <= i
+                // (column offsets advance by d - j - 1: lpk_col(d, j) - j)
+                int oj = lpk_col(d, k + 1) - (k + 1);
 #pragma unroll 4
                 for (int j = k + 1; j < d; ++j) {
                     const double ljk = S[ok + j];  // broadcast
-                    const int oj = lpk_col(d, j) - j;
 #pragma unroll
                     for (int t = 0; t < R; ++t) {
                         const int i = lane + 32 * t;
                         if (i >= j && i < d) S[oj + i] -= lik[t] * ljk;
                     }
+                    oj += d - j - 1;
                 }
                 __syncwarp();
             }
@@ -317,10 +319,10 @@ __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __res
             double a0[R], a1[R];
 #pragma unroll
             for (int t = 0; t < R; ++t) a0[t] = a1[t] = 0.0;
+            int okk = lpk_col(d, j + 1) - (j + 1);
 #pragma unroll 4
             for (int k = j + 1; k < d; ++k) {
                 const double lkj = S[oj + k];  // L(k,j), broadcast
-                const int okk = lpk_col(d, k) - k;
 #pragma unroll
                 for (int t = 0; t < R; ++t) {
                     const int i = lane + 32 * t;
@@ -331,6 +333,7 @@ __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __res
                             a0[t] += S[okk + i] * lkj;
                     }
                 }
+                okk += d - k - 1;
             }
             __syncwarp();  // every read of column j done before it is overwritten
 #pragma unroll

@@ -320,6 +320,15 @@ def run_ours(args, rank, world, local_rank, dist):
         ctx.spmv(d_x, d_res)
     stream.synchronize()
     xerr = float(torch.linalg.norm(d_b - d_res) / torch.linalg.norm(d_b))
+    # the step after the solve (newton.hpp:257-290, step.cu) on this direction:
+    # step_inf_norm + apply_direction through the C ABI (host-visible latency)
+    d_state = torch.zeros_like(d_x)
+    stream.synchronize()
+    t_ps = time.perf_counter()
+    for _ in range(10):
+        ctx.step_inf_norm(d_x, n, 0)
+        ctx.apply_direction(d_state, d_x, 1.0, d_res)
+    post_solve_us = (time.perf_counter() - t_ps) / 10 * 1e6
 
     stats = dict(total_ms=total_ms, pcg_ms=pcg_ms, iters=iters, asm_ms=asm_ms, build_ms=build_ms,
                  launches=launches, conv=bool(res_last.converged), rel=float(res_last.rel_residual), xerr=xerr)
@@ -370,6 +379,7 @@ def run_ours(args, rank, world, local_rank, dist):
             "mas_build_cold_host_ms": cold["build_host_ms"] if cold else None,
             "mas_build_first_ms": first["build_ms"] if first else None,
             "hierarchy_cache": not args.no_cache,
+            "post_solve_us": post_solve_us,
             "pcg_ms": pcg_ms / args.steps,
             "pcg_iters_per_solve": iters / args.steps,
             "converged": all(g["conv"] for g in gathered),

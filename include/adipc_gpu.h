@@ -98,6 +98,20 @@ int adipc_gpu_assemble_filtered_device(adipc_gpu_ctx* ctx, const uint64_t* d_key
 int adipc_gpu_matrix_info(adipc_gpu_ctx* ctx, int32_t* n_block_rows, int64_t* n_blocks);
 /* copy SortedSymBlockCoo{rows, cols, blocks} out (block_coo.hpp:54-61) */
 int adipc_gpu_copy_matrix(adipc_gpu_ctx* ctx, uint32_t* rows, uint32_t* cols, double* blocks9);
+/* ---- the step after the solve (TimeStepper, adipc/solver/newton.hpp:257-290), device pointers ----
+ * Vectors in the reference block numbering: n_fem FEM vertices, then 4 blocks (p, rows of A) per body. */
+/* step_inf_norm (newton.hpp:257-270): max(|d_i| over FEM vertices, |d_p| + |d_A|_F max_xbar[b] over bodies) */
+int adipc_gpu_step_inf_norm_device(adipc_gpu_ctx* ctx, const double* d_dir, int32_t n_fem, int32_t n_bodies,
+                                   const double* d_max_xbar, double* out);
+/* apply_direction (newton.hpp:283-290): out = state + alpha dir over n_dofs (x of the vertices, q of the bodies) */
+int adipc_gpu_apply_direction_device(adipc_gpu_ctx* ctx, const double* d_state, const double* d_dir, double alpha,
+                                     int64_t n_dofs, double* d_out);
+/* node_displacements (newton.hpp:272-281): FEM nodes copy d; affine-body node a moves by J_a d_body
+ * (abd_node_jacobian 3x12 column-major, 36 doubles per node, DofMap abd_reduce.hpp:11-27) */
+int adipc_gpu_node_displacements_device(adipc_gpu_ctx* ctx, const double* d_dir, int32_t n_fem, int32_t n_abd,
+                                        const int32_t* d_abd_node_body, const double* d_abd_jacobian36,
+                                        double* d_out);
+
 /* dump_block_coo (adipc/sparse/srbk_spmv.hpp:52-60; the CLI's --dump-hessian, adipc_cli.cpp:107-113) of
  * the context's matrix into a text file, byte-identical to the reference's output */
 int adipc_gpu_dump_block_coo(adipc_gpu_ctx* ctx, const char* path);

@@ -490,3 +490,42 @@ def pcg_solve(mat: Matrix, b, M: _Precond, rel_tol, restart, max_iters, policy=N
     mat._L.oracle_pcg_solve(mat.h, b, len(b), M.h, rel_tol, restart, max_iters, *_pol(policy), x,
                            C.byref(it), C.byref(rr), C.byref(cv))
     return x, dict(iters=it.value, rel_residual=rr.value, converged=bool(cv.value))
+
+
+# ---- the step after the solve (adipc/solver/newton.hpp:257-290), restated ----
+# Vectors in block numbering: n_fem vertices, then 4 blocks (12 dofs: p, the
+# rows of A) per affine body at block n_fem + 4 b (DofMap, abd_reduce.hpp:24).
+def step_inf_norm(d, n_fem, n_bodies, max_xbar):
+    """newton.hpp:257-270."""
+    d = np.asarray(d, np.float64)
+    worst = 0.0
+    for i in range(n_fem):
+        worst = max(worst, float(np.sqrt(d[3 * i] ** 2 + d[3 * i + 1] ** 2 + d[3 * i + 2] ** 2)))
+    for b in range(n_bodies):
+        s = d[3 * (n_fem + 4 * b): 3 * (n_fem + 4 * b) + 12]
+        worst = max(worst, float(np.sqrt(np.sum(s[:3] ** 2)) + np.sqrt(np.sum(s[3:] ** 2)) * max_xbar[b]))
+    return worst
+
+
+def apply_direction(state, d, alpha):
+    """newton.hpp:283-290 (x + alpha d for the vertices, q + alpha d for the bodies)."""
+    return np.asarray(state, np.float64) + alpha * np.asarray(d, np.float64)
+
+
+def node_displacements(d, n_fem, abd_node_body, jac36):
+    """newton.hpp:272-281: FEM nodes copy d, affine-body node a gets J_a d_body."""
+    d = np.asarray(d, np.float64)
+    out = [d[: 3 * n_fem]]
+    for a, b in enumerate(abd_node_body):
+        J = np.asarray(jac36[a], np.float64).reshape(12, 3).T  # column-major 3x12
+        out.append(J @ d[3 * (n_fem + 4 * b): 3 * (n_fem + 4 * b) + 12])
+    return np.concatenate(out) if out else np.zeros(0)
+
+
+def abd_jacobian(rest):
+    """mesh.hpp:196-201: J = [I3 | rows r: rest^T at columns 3 + 3 r], column-major 36 doubles."""
+    J = np.zeros((3, 12))
+    J[:, :3] = np.eye(3)
+    for r in range(3):
+        J[r, 3 + 3 * r: 6 + 3 * r] = rest
+    return J.T.reshape(-1).copy()

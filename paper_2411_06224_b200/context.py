@@ -144,6 +144,22 @@ class Context:
         self._check(self._L.adipc_gpu_matrix_info(self.h, C.byref(n), C.byref(U)))
         return n.value, U.value
 
+    # ---- the step after the solve (newton.hpp:257-290); device tensors ----
+    def step_inf_norm(self, d_dir, n_fem, n_bodies, d_max_xbar=None):
+        out = C.c_double()
+        self._check(self._L.adipc_gpu_step_inf_norm_device(self.h, ptr(d_dir), n_fem, n_bodies, ptr(d_max_xbar),
+                                                             C.byref(out)))
+        return out.value
+
+    def apply_direction(self, d_state, d_dir, alpha, d_out):
+        self._check(self._L.adipc_gpu_apply_direction_device(self.h, ptr(d_state), ptr(d_dir), float(alpha),
+                                                               d_state.numel(), ptr(d_out)))
+
+    def node_displacements(self, d_dir, n_fem, d_abd_body, d_jac36, d_out):
+        n_abd = 0 if d_abd_body is None else d_abd_body.numel()
+        self._check(self._L.adipc_gpu_node_displacements_device(self.h, ptr(d_dir), n_fem, n_abd, ptr(d_abd_body),
+                                                                  ptr(d_jac36), ptr(d_out)))
+
     def dump_block_coo(self, path):
         """srbk_spmv.hpp:52-60 of the device matrix (--dump-hessian text)."""
         self._check(self._L.adipc_gpu_dump_block_coo(self.h, str(path).encode()))

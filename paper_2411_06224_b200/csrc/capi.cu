@@ -181,6 +181,7 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.sell.cols.free();
     c.sell.vals.free();
     c.sell_len.free();
+    c.step_max.free();
     c.graph_deg.free();
     c.graph_adj.free();
     c.graph_adj2.free();
@@ -366,6 +367,35 @@ int adipc_gpu_copy_matrix(adipc_gpu_ctx* ctx, uint32_t* rows, uint32_t* cols, do
             ADIPC_CUDA(cudaMemcpyAsync(blocks9, c.vals.p, 72 * U, cudaMemcpyDeviceToHost, c.stream));
         }
         sync(c);
+    });
+}
+
+// ---- the step after the solve (newton.hpp:257-290), device pointers ----------
+int adipc_gpu_step_inf_norm_device(adipc_gpu_ctx* ctx, const double* d_dir, int32_t n_fem, int32_t n_bodies,
+                                   const double* d_max_xbar, double* out) {
+    return guarded(ctx, [&] {
+        if (n_fem < 0 || n_bodies < 0 || !out || (n_bodies > 0 && !d_max_xbar))
+            throw StatusError(kInvalidArgument, "step_inf_norm: bad arguments");
+        *out = step_inf_norm(ctx->c, d_dir, n_fem, n_bodies, d_max_xbar);
+    });
+}
+
+int adipc_gpu_apply_direction_device(adipc_gpu_ctx* ctx, const double* d_state, const double* d_dir, double alpha,
+                                     int64_t n_dofs, double* d_out) {
+    return guarded(ctx, [&] {
+        if (n_dofs < 0) throw StatusError(kInvalidArgument, "apply_direction: negative size");
+        apply_direction(ctx->c, d_state, d_dir, alpha, n_dofs, d_out);
+        sync(ctx->c);
+    });
+}
+
+int adipc_gpu_node_displacements_device(adipc_gpu_ctx* ctx, const double* d_dir, int32_t n_fem, int32_t n_abd,
+                                        const int32_t* d_abd_node_body, const double* d_abd_jacobian36,
+                                        double* d_out) {
+    return guarded(ctx, [&] {
+        if (n_fem < 0 || n_abd < 0) throw StatusError(kInvalidArgument, "node_displacements: negative size");
+        node_displacements(ctx->c, d_dir, n_fem, n_abd, d_abd_node_body, d_abd_jacobian36, d_out);
+        sync(ctx->c);
     });
 }
 

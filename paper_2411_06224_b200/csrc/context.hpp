@@ -141,6 +141,7 @@ struct Ctx {
     PcgWork w;
     SellMatrix sell;
     DBuf<std::int64_t> sell_len;
+    DBuf<unsigned long long> step_max;  // step_inf_norm result (step.cu)
     // level-0 graph of the cold hierarchy build (block_edges + build_graph on the device)
     DBuf<std::int32_t> graph_deg, graph_adj, graph_adj2;
     DBuf<std::int64_t> graph_ptr, graph_cur, graph_ptr2;
@@ -255,6 +256,12 @@ void segment_reduce(Ctx& c, const std::int32_t* d_O, std::int64_t n, const doubl
 std::int64_t filter_pinned(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T,
                            const std::uint8_t* d_pinned, std::int32_t n_slots, std::uint64_t* d_out_keys,
                            double* d_out_vals);
+
+// step.cu (newton.hpp:257-290): the step after the solve
+double step_inf_norm(Ctx& c, const double* d_dir, std::int32_t n_fem, std::int32_t n_bodies, const double* d_max_xbar);
+void apply_direction(Ctx& c, const double* d_state, const double* d_dir, double alpha, std::int64_t n, double* d_out);
+void node_displacements(Ctx& c, const double* d_dir, std::int32_t n_fem, std::int32_t n_abd,
+                        const std::int32_t* d_abd_body, const double* d_jac36, double* d_out);
 
 // abd.cu
 std::int64_t two_level_abd_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t Tn,

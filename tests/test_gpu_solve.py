@@ -370,3 +370,31 @@ def test_pcg_other_subdomain_capacities(ctx, capacity):
     assert r.converged and ro["converged"]
     assert abs(r.iters - ro["iters"]) <= max(1, 0.02 * ro["iters"]), (r.iters, ro["iters"])
     assert np.linalg.norm(x - xo) <= 1e-5 * np.linalg.norm(xo)
+
+
+def test_step_after_solve_matches_restatement(ctx):
+    """adipc_gpu_step_inf_norm / apply_direction / node_displacements
+    (newton.hpp:257-290) against the restatement, on a mixed FEM + affine-body
+    direction."""
+    import torch
+
+    rng = np.random.default_rng(9)
+    n_fem, n_bodies, per_body = 1000, 20, 30
+    d = rng.standard_normal(3 * (n_fem + 4 * n_bodies))
+    max_xbar = rng.random(n_bodies) + 0.5
+    body = np.repeat(np.arange(n_bodies, dtype=np.int32), per_body)
+    jac = np.stack([O.abd_jacobian(x) for x in rng.standard_normal((len(body), 3))])
+    state = rng.standard_normal(d.size)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    dd, dx, db, dj, ds = dev(d), dev(max_xbar), dev(body), dev(jac), dev(state)
+    out = torch.empty_like(dd)
+    torch.cuda.synchronize()  # the context runs on its own stream
+    got = ctx.step_inf_norm(dd, n_fem, n_bodies, dx)
+    assert abs(got - O.step_inf_norm(d, n_fem, n_bodies, max_xbar)) <= 1e-14 * got
+    ctx.apply_direction(ds, dd, 0.37, out)
+    assert np.array_equal(out.cpu().numpy(), O.apply_direction(state, d, 0.37))
+    disp = torch.empty(3 * (n_fem + len(body)), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    ctx.node_displacements(dd, n_fem, db, dj, disp)
+    want = O.node_displacements(d, n_fem, body, jac)
+    assert np.allclose(disp.cpu().numpy(), want, rtol=1e-14, atol=1e-14)

@@ -382,7 +382,7 @@ def run_ours(args, rank, world, local_rank, dist):
             "config": {"workload": "cfg5: stiff FEM box 68^3 cells, 985,527 DOF, E=1e8, PCG-only Newton solve, "
                                    "MAS cemas16 (4 levels), rel_tol 1e-4, restart 250; one scene per GPU",
                        "n_block_rows": n, "n_blocks": U, "triplets": int(len(sc.keys)),
-                       "l2": "inputs larger than L2 (A 206 MB + MAS inverses 402 MB per scene)",
+                       "l2": "inputs larger than L2 (A 203 MB + symmetric-packed MAS inverses 214 MB per scene, 126 MB L2)",
                        "parallelism": f"{world} independent scenes (replicas of the single-GPU solve)"},
             "ms_per_newton_solve": (sum(g["build_ms"] + g["pcg_ms"] for g in gathered[:1]) / args.steps),
             "assembly_ms": asm_ms / args.steps,

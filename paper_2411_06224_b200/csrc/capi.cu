@@ -182,6 +182,11 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.sell.vals.free();
     c.sell_len.free();
     c.step_max.free();
+    for (auto* b : {&c.l0_part, &c.l0_mem_ptr, &c.l0_members, &c.l0_pos, &c.l1_up, &c.l1_ncomp, &c.l1_cnt, &c.l1_adj})
+        b->free();
+    c.l1_base.free();
+    c.l1_ptr.free();
+    c.l1_keys.free();
     c.graph_deg.free();
     c.graph_adj.free();
     c.graph_adj2.free();
@@ -649,6 +654,7 @@ int adipc_gpu_set_level0_partition(adipc_gpu_ctx* ctx, const int32_t* part_of, i
         c.l0.part_of.assign(part_of, part_of + n_slots);
         c.l0.n_parts = n_parts;
         c.l0.capacity = capacity;
+        ++c.l0_version;
         c.max_levels = max_levels;
         c.have_l0 = true;
         c.hier_version = ~0ull;

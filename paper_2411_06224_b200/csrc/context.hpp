@@ -127,6 +127,12 @@ struct Ctx {
     // preconditioner
     PrecondKind pkind = kNone;
     host::Partition l0;             // level-0 partition (set once per scene)
+    std::uint64_t l0_version = 0, l0_dev_version = ~0ull;  // device copies of l0 (level-1 pass)
+    int l0_max_members = 0;
+    DBuf<std::int32_t> l0_part, l0_mem_ptr, l0_members, l0_pos;
+    DBuf<std::int32_t> l1_up, l1_ncomp, l1_cnt, l1_adj;
+    DBuf<std::int64_t> l1_base, l1_ptr;
+    DBuf<std::uint64_t> l1_keys;
     int max_levels = 4;
     bool have_l0 = false;
     host::MasHierarchy hier;        // last built hierarchy (host copy)
@@ -234,6 +240,8 @@ struct Ctx {
 Ctx* unwrap(adipc_gpu_ctx* c);
 
 // assemble.cu
+// row bucketing + per-row sort of 64-bit keys (c.sorted / row_start / uniq_cnt)
+void bucket_sort(Ctx& c, const std::uint64_t* d_keys, std::int64_t T, std::int32_t n, const std::uint32_t* d_vidx);
 // vals_ready: event the reduction waits for (values uploaded on another stream
 // while the keys are sorted), or null
 void assemble(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n_block_rows,

@@ -204,7 +204,9 @@ MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_
     return build_hierarchy(l0, build_graph(static_cast<Index>(l0.part_of.size()), pairs, n_edges), max_levels);
 }
 
-MasHierarchy build_hierarchy(const Partition& l0, Graph g0, int max_levels) {
+namespace {
+
+MasHierarchy base_hierarchy(const Partition& l0) {
     MasHierarchy h;
     h.capacity = l0.capacity;
     h.n_slots = static_cast<Index>(l0.part_of.size());
@@ -215,8 +217,40 @@ MasHierarchy build_hierarchy(const Partition& l0, Graph g0, int max_levels) {
     base.agg.resize(h.n_slots);
     for (Index i = 0; i < h.n_slots; ++i) base.agg[i] = i;
     h.levels.push_back(std::move(base));
+    return h;
+}
 
-    Graph g = std::move(g0);  // graph of the current level's nodes
+// the aggregation loop of hierarchy.hpp:46-99 from the current last level,
+// whose node graph is g
+void extend_hierarchy(MasHierarchy& h, Graph g, int max_levels);
+
+}  // namespace
+
+MasHierarchy build_hierarchy(const Partition& l0, Graph g0, int max_levels) {
+    MasHierarchy h = base_hierarchy(l0);
+    extend_hierarchy(h, std::move(g0), max_levels);
+    return h;
+}
+
+MasHierarchy build_hierarchy_l1(const Partition& l0, std::vector<Index> up1, Index n1, Graph g1, int max_levels) {
+    MasHierarchy h = base_hierarchy(l0);
+    // the first pass of the loop (hierarchy.hpp:46-99) with its super nodes
+    // and their graph given
+    if (h.n_levels() >= max_levels || l0.n_parts <= 1 || n1 == h.n_slots) return h;
+    Level next;
+    next.n_nodes = n1;
+    Partition grouped = partition_block_graph(n1, g1, h.capacity);
+    next.n_parts = grouped.n_parts;
+    next.part_of = std::move(grouped.part_of);
+    next.agg = std::move(up1);  // level 0's agg is the identity
+    h.levels.push_back(std::move(next));
+    extend_hierarchy(h, std::move(g1), max_levels);
+    return h;
+}
+
+namespace {
+
+void extend_hierarchy(MasHierarchy& h, Graph g, int max_levels) {
     std::vector<Index> up, queue, members, mem_ptr;
     while (h.n_levels() < max_levels) {
         const Level& cur = h.levels.back();
@@ -333,7 +367,8 @@ MasHierarchy build_hierarchy(const Partition& l0, Graph g0, int max_levels) {
             std::fprintf(stderr, "hierarchy level %d: bfs %.1f ms, coarse graph %.1f ms, partition %.1f ms\n",
                          h.n_levels() - 1, ms(t1, t2), ms(t2, t3), ms(t3, tnow()));
     }
-    return h;
 }
+
+}  // namespace
 
 }  // namespace adipc_gpu::host

@@ -54,5 +54,8 @@ Partition partition_block_graph(Index v, const Index* pairs, std::size_t n_edges
 MasHierarchy build_hierarchy(const Partition& l0, const Index* pairs, std::size_t n_edges, int max_levels);
 // same, with the level-0 graph already built (the device build, mas.cu level0_graph)
 MasHierarchy build_hierarchy(const Partition& l0, Graph g0, int max_levels);
+// same, with the first aggregation pass done elsewhere (the device, mas.cu): up1 = level-0 node ->
+// level-1 node (n1 nodes) and g1 = the level-1 node graph
+MasHierarchy build_hierarchy_l1(const Partition& l0, std::vector<Index> up1, Index n1, Graph g1, int max_levels);
 
 }  // namespace adipc_gpu::host

@@ -817,11 +817,16 @@ __global__ void k_graph_compact(std::int32_t n, const std::int64_t* __restrict__
         for (std::int64_t k = 0; k < ptr2[i + 1] - ptr2[i]; ++k) adj2[ptr2[i] + k] = adj[ptr[i] + k];
 }
 
-host::Graph level0_graph(Ctx& c) {
+struct DeviceGraph {
+    const std::int64_t* ptr = nullptr;
+    const std::int32_t* adj = nullptr;
+    std::int64_t E = 0;
+};
+
+DeviceGraph level0_graph_device(Ctx& c) {
     const DeviceMatrix& A = c.A;
     cudaStream_t st = c.stream;
     const std::int32_t n = A.n;
-    host::Graph g;
     c.graph_deg.reserve(static_cast<std::size_t>(std::max(n, 1)));
     c.graph_ptr.reserve(static_cast<std::size_t>(n) + 1);
     c.graph_cur.reserve(static_cast<std::size_t>(std::max(n, 1)));
@@ -861,12 +866,163 @@ host::Graph level0_graph(Ctx& c) {
         adj = c.graph_adj2.p;
         ptr = c.graph_ptr2.p;
     }
+    return DeviceGraph{ptr, adj, E2};
+}
+
+host::Graph graph_to_host(Ctx& c, const DeviceGraph& dg, std::int32_t n) {
+    host::Graph g;
     g.ptr.resize(static_cast<std::size_t>(n) + 1);
-    g.adj.resize(static_cast<std::size_t>(E2));
-    ADIPC_CUDA(cudaMemcpyAsync(g.ptr.data(), ptr, sizeof(std::int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
-    if (E2 > 0) ADIPC_CUDA(cudaMemcpyAsync(g.adj.data(), adj, sizeof(std::int32_t) * E2, cudaMemcpyDeviceToHost, st));
-    ADIPC_CUDA(cudaStreamSynchronize(st));
+    g.adj.resize(static_cast<std::size_t>(dg.E));
+    ADIPC_CUDA(cudaMemcpyAsync(g.ptr.data(), dg.ptr, sizeof(std::int64_t) * (n + 1), cudaMemcpyDeviceToHost, c.stream));
+    if (dg.E > 0)
+        ADIPC_CUDA(cudaMemcpyAsync(g.adj.data(), dg.adj, sizeof(std::int32_t) * dg.E, cudaMemcpyDeviceToHost, c.stream));
+    ADIPC_CUDA(cudaStreamSynchronize(c.stream));
     return g;
+}
+
+// ---- the first aggregation pass of build_hierarchy on the device -------------
+// (hierarchy.hpp:53-85 for level 0 -> 1): connected components inside each
+// level-0 subdomain, numbered in the order of their smallest member (= BFS
+// seeds in ascending node order), and the sorted unique super-node graph.
+// One warp per subdomain (<= 32 members): lane i = i-th member in ascending
+// node order; in-subdomain neighbours as a bit mask; min-label propagation.
+__global__ void k_l1_components(std::int32_t n_parts, const std::int32_t* __restrict__ mem_ptr,
+                                const std::int32_t* __restrict__ members, const std::int32_t* __restrict__ part_of,
+                                const std::int32_t* __restrict__ pos, const std::int64_t* __restrict__ gptr,
+                                const std::int32_t* __restrict__ gadj, std::int32_t* __restrict__ up_local,
+                                std::int32_t* __restrict__ ncomp) {
+    const int lane = threadIdx.x & 31;
+    const std::int64_t w = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (w >= n_parts) return;
+    const std::int32_t s = static_cast<std::int32_t>(w);
+    const std::int32_t m0 = mem_ptr[s], m = mem_ptr[s + 1] - m0;
+    const bool act = lane < m;
+    const std::int32_t node = act ? members[m0 + lane] : -1;
+    unsigned nb = 0;
+    if (act)
+        for (std::int64_t e = gptr[node]; e < gptr[node + 1]; ++e) {
+            const std::int32_t v = gadj[e];
+            if (part_of[v] == s) nb |= 1u << pos[v];
+        }
+    int lab = lane;
+    for (;;) {
+        int best = lab;
+        for (int j = 0; j < m; ++j) {
+            const int lj = __shfl_sync(0xffffffffu, lab, j);
+            if ((nb >> j) & 1u) best = min(best, lj);
+        }
+        const bool changed = act && best != lab;
+        lab = act ? best : lab;
+        if (!__any_sync(0xffffffffu, changed)) break;
+    }
+    const unsigned roots = __ballot_sync(0xffffffffu, act && lab == lane);
+    if (act) up_local[node] = __popc(roots & ((1u << lab) - 1u));
+    if (lane == 0) ncomp[s] = __popc(roots);
+}
+
+__global__ void k_l1_up(std::int32_t n, const std::int32_t* __restrict__ part_of, const std::int64_t* __restrict__ base,
+                        std::int32_t* __restrict__ up) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        up[i] = static_cast<std::int32_t>(base[part_of[i]] + up[i]);
+}
+
+// one key (up[a] << 32 | up[b]) per directed fine adjacency entry a -> b
+__global__ void k_l1_keys(std::int32_t n, const std::int64_t* __restrict__ gptr, const std::int32_t* __restrict__ gadj,
+                          const std::int32_t* __restrict__ up, std::uint64_t* __restrict__ keys) {
+    for (std::int64_t a = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; a < n;
+         a += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t ua = static_cast<std::uint64_t>(up[a]) << 32;
+        for (std::int64_t e = gptr[a]; e < gptr[a + 1]; ++e) keys[e] = ua | static_cast<std::uint32_t>(up[gadj[e]]);
+    }
+}
+
+// per super node: unique neighbour count without itself (rows of the bucket sort)
+__global__ void k_l1_count(std::int32_t n1, const std::uint64_t* __restrict__ sorted,
+                           const std::int64_t* __restrict__ row_start, const std::int32_t* __restrict__ uniq_cnt,
+                           std::int32_t* __restrict__ cnt) {
+    for (std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; r < n1;
+         r += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        bool self = false;
+        for (std::int64_t q = row_start[r]; q < row_start[r + 1] && !self; ++q)
+            self = static_cast<std::uint32_t>(sorted[q] >> 32) == static_cast<std::uint32_t>(r);
+        cnt[r] = uniq_cnt[r] - (self ? 1 : 0);
+    }
+}
+
+__global__ void k_l1_emit(std::int32_t n1, const std::uint64_t* __restrict__ sorted,
+                          const std::int64_t* __restrict__ row_start, const std::int64_t* __restrict__ ptr1,
+                          std::int32_t* __restrict__ adj1) {
+    for (std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; r < n1;
+         r += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        std::int64_t o = ptr1[r];
+        std::uint32_t prev = 0xFFFFFFFFu;
+        for (std::int64_t q = row_start[r]; q < row_start[r + 1]; ++q) {
+            const std::uint32_t v = static_cast<std::uint32_t>(sorted[q] >> 32);
+            if (v != prev && v != static_cast<std::uint32_t>(r)) adj1[o++] = static_cast<std::int32_t>(v);
+            prev = v;
+        }
+    }
+}
+
+// Level 0 -> 1 on the device; false when a level-0 subdomain has more than 32
+// members (the host pass handles any size).
+bool level1_device(Ctx& c, const DeviceGraph& g0, std::vector<std::int32_t>& up1, std::int32_t& n1,
+                   host::Graph& g1) {
+    const host::Partition& l0 = c.l0;
+    const std::int32_t n = static_cast<std::int32_t>(l0.part_of.size());
+    cudaStream_t st = c.stream;
+    if (c.l0_dev_version != c.l0_version) {  // per scene: members of each subdomain, ascending
+        std::vector<std::int32_t> mem_ptr(static_cast<std::size_t>(l0.n_parts) + 1, 0), members(n), pos(n);
+        for (std::int32_t i = 0; i < n; ++i) pos[i] = mem_ptr[l0.part_of[i] + 1]++;
+        c.l0_max_members = 0;
+        for (std::int32_t s = 0; s < l0.n_parts; ++s) c.l0_max_members = std::max(c.l0_max_members, mem_ptr[s + 1]);
+        for (std::int32_t s = 0; s < l0.n_parts; ++s) mem_ptr[s + 1] += mem_ptr[s];
+        for (std::int32_t i = 0; i < n; ++i) members[mem_ptr[l0.part_of[i]] + pos[i]] = i;
+        upload(c.l0_part, l0.part_of, st);
+        upload(c.l0_mem_ptr, mem_ptr, st);
+        upload(c.l0_members, members, st);
+        upload(c.l0_pos, pos, st);
+        c.l0_dev_version = c.l0_version;
+    }
+    if (c.l0_max_members > 32 || n == 0 || l0.n_parts == 0) return false;
+    c.l1_up.reserve(static_cast<std::size_t>(n));
+    c.l1_ncomp.reserve(static_cast<std::size_t>(l0.n_parts));
+    c.l1_base.reserve(static_cast<std::size_t>(l0.n_parts) + 1);
+    k_l1_components<<<static_cast<int>(ceil_div(l0.n_parts, 8)), 256, 0, st>>>(
+        l0.n_parts, c.l0_mem_ptr.p, c.l0_members.p, c.l0_part.p, c.l0_pos.p, g0.ptr, g0.adj, c.l1_up.p, c.l1_ncomp.p);
+    ADIPC_LAUNCH_CHECK();
+    exclusive_scan(c.l1_ncomp.p, l0.n_parts, c.l1_base.p, c.scan_scratch, st);
+    std::int64_t total = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&total, c.l1_base.p + l0.n_parts, sizeof(total), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    n1 = static_cast<std::int32_t>(total);
+    k_l1_up<<<grid_for(n, 256, 16), 256, 0, st>>>(n, c.l0_part.p, c.l1_base.p, c.l1_up.p);
+    ADIPC_LAUNCH_CHECK();
+    up1.resize(static_cast<std::size_t>(n));
+    ADIPC_CUDA(cudaMemcpyAsync(up1.data(), c.l1_up.p, sizeof(std::int32_t) * n, cudaMemcpyDeviceToHost, st));
+    if (n1 == n) {  // no merge: the hierarchy stops at level 0
+        ADIPC_CUDA(cudaStreamSynchronize(st));
+        return true;
+    }
+    // super-node graph: bucket-sort the mapped adjacency, drop repeats and self loops
+    c.l1_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(g0.E, 1)));
+    k_l1_keys<<<grid_for(n, 256, 16), 256, 0, st>>>(n, g0.ptr, g0.adj, c.l1_up.p, c.l1_keys.p);
+    ADIPC_LAUNCH_CHECK();
+    bucket_sort(c, c.l1_keys.p, g0.E, n1, nullptr);
+    c.l1_cnt.reserve(static_cast<std::size_t>(n1) + 1);
+    c.l1_ptr.reserve(static_cast<std::size_t>(n1) + 1);
+    k_l1_count<<<grid_for(n1, 256, 16), 256, 0, st>>>(n1, c.sorted.p, c.row_start.p, c.uniq_cnt.p, c.l1_cnt.p);
+    ADIPC_LAUNCH_CHECK();
+    exclusive_scan(c.l1_cnt.p, n1, c.l1_ptr.p, c.scan_scratch, st);
+    std::int64_t E1 = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&E1, c.l1_ptr.p + n1, sizeof(E1), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    c.l1_adj.reserve(static_cast<std::size_t>(std::max<std::int64_t>(E1, 1)));
+    k_l1_emit<<<grid_for(n1, 256, 16), 256, 0, st>>>(n1, c.sorted.p, c.row_start.p, c.l1_ptr.p, c.l1_adj.p);
+    ADIPC_LAUNCH_CHECK();
+    g1 = graph_to_host(c, DeviceGraph{c.l1_ptr.p, c.l1_adj.p, E1}, n1);
+    return true;
 }
 
 }  // namespace
@@ -896,10 +1052,19 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
     const bool reuse = c.cache_hierarchy && c.hier_version == phash && !c.levels.empty();
     // block_edges(A) (mas.hpp:19-25): off-diagonal (row, col) pairs, in order
     if (!reuse) {
-        // the level-0 graph built on the device from A's pattern, one D2H
-        host::Graph g0 = level0_graph(c);
+        // the level-0 graph built on the device from A's pattern and — for
+        // subdomains of <= 32 members — the first aggregation pass too; the
+        // host continues from the (small) level-1 graph
+        const DeviceGraph g0 = level0_graph_device(c);
+        std::vector<std::int32_t> up1;
+        std::int32_t n1 = 0;
+        host::Graph g1;
+        const bool dev_l1 = c.max_levels > 1 && c.l0.n_parts > 1 && level1_device(c, g0, up1, n1, g1);
         const auto ta = std::chrono::steady_clock::now();
-        c.hier = host::build_hierarchy(c.l0, std::move(g0), c.max_levels);
+        if (dev_l1)
+            c.hier = host::build_hierarchy_l1(c.l0, std::move(up1), n1, std::move(g1), c.max_levels);
+        else
+            c.hier = host::build_hierarchy(c.l0, graph_to_host(c, g0, A.n), c.max_levels);
         if (c.hier.n_levels() > kMaxLevels) throw StatusError(kInvalidArgument, "too many MAS levels");
         const auto tb = std::chrono::steady_clock::now();
         set_levels(c, c.hier);

@@ -398,3 +398,25 @@ def test_step_after_solve_matches_restatement(ctx):
     ctx.node_displacements(dd, n_fem, db, dj, disp)
     want = O.node_displacements(d, n_fem, body, jac)
     assert np.allclose(disp.cpu().numpy(), want, rtol=1e-14, atol=1e-14)
+
+
+@pytest.mark.parametrize("name,capacity", [("cfg1_soft_cube", 16), ("cfg2_cloth", 16), ("cfg4_hybrid", 16),
+                                           ("stiff_beam", 8), ("stiff_beam", 32)])
+def test_hierarchy_device_pass_matches_oracle(ctx, name, capacity):
+    """The cold hierarchy build's device pass (level-0 graph, per-subdomain
+    components, super-node graph) continued on the host gives exactly the
+    reference's hierarchy (hierarchy.hpp:30-100): every level's part_of and
+    agg equal the oracle's."""
+    sc = scenes.CONFIGS[name]()
+    fk, fv = _full_stream(sc)
+    ctx.assemble(fk, fv, sc.n_blocks)
+    n, rows, cols, blocks = ctx.copy_matrix()
+    l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, capacity)
+    ctx.set_level0_partition(l0.part_of, l0.n_parts, capacity, 4)
+    ctx.build_preconditioner(1)
+    levels = ctx.precond_levels()
+    ho = O.Hierarchy(l0.part_of, l0.n_parts, capacity, O.block_edges(rows, cols), 4)
+    assert len(levels) == ho.n_levels()
+    for a, o in zip(levels, ho.levels):
+        assert a["n_nodes"] == o["n_nodes"] and a["n_parts"] == o["n_parts"]
+        assert np.array_equal(a["part_of"], o["part_of"]) and np.array_equal(a["agg"], o["agg"])

@@ -11,7 +11,7 @@ fk, fv = ctx.filter_pinned(sc.keys, sc.vals, sc.pinned)
 ctx.assemble(fk, fv, sc.n_blocks)
 ctx.build_preconditioner(_lib.PRECOND_MAS)
 b = torch.from_numpy(scenes.gravity_rhs(sc)).cuda(); x = torch.empty_like(b); torch.cuda.synchronize()
-for mi in (100000, 340, 339, 100000, 340):
+for mi in [int(a) for a in (sys.argv[1:] or ["100000", "340", "339", "100000", "340"])]:
     best = 1e9
     for _ in range(3):
         _, r = ctx.pcg(b, 1e-4, 250, mi, x=x)

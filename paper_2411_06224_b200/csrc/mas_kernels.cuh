@@ -184,6 +184,11 @@ __device__ __forceinline__ int matvec_row(int lane, int t) {
 // Per column: all rows <= k read column k at a compile-time offset, all rows
 // > k their own column, and mixed columns select the offset per lane — one
 // shared load per row and column.
+// independent FMA chains per row in packed_matvec_rows: 4 measured best at
+// cfg5 (preconditioner 66 -> 61 us; 6: 61.7, 8: 62.0)
+#ifndef ADIPC_PC_ACC
+#define ADIPC_PC_ACC 4
+#endif
 template <int kK, int kRow0, int kRows>
 __device__ __forceinline__ void packed_matvec_rows(const double* M, const double* bs, double* y, int lane) {
     constexpr int R = (kRows + 31) / 32;
@@ -197,9 +202,13 @@ __device__ __forceinline__ void packed_matvec_rows(const double* M, const double
         P1[t] = M + j;
         P2[t] = M + j * (j + 1) / 2;
     }
-    double acc0[R], acc1[R];
+    // kAcc independent accumulation chains per row (fp64 FMA latency)
+    constexpr int kAcc = ADIPC_PC_ACC;
+    double acc[kAcc][R];
 #pragma unroll
-    for (int t = 0; t < R; ++t) acc0[t] = acc1[t] = 0.0;
+    for (int q = 0; q < kAcc; ++q)
+#pragma unroll
+        for (int t = 0; t < R; ++t) acc[q][t] = 0.0;
     const double2* b2 = reinterpret_cast<const double2*>(bs);
 #pragma unroll
     for (int k2 = 0; k2 < kK; k2 += 2) {
@@ -220,15 +229,17 @@ __device__ __forceinline__ void packed_matvec_rows(const double* M, const double
                     m = P2[t][k];
                 else
                     m = jr[t] <= k ? M[ck + jr[t]] : P2[t][k];
-                if (u == 1)
-                    acc1[t] = fma(m, bk, acc1[t]);
-                else
-                    acc0[t] = fma(m, bk, acc0[t]);
+                acc[k % kAcc][t] = fma(m, bk, acc[k % kAcc][t]);
             }
         }
     }
 #pragma unroll
-    for (int t = 0; t < R; ++t) y[t] = acc0[t] + acc1[t];
+    for (int t = 0; t < R; ++t) {
+        double v = acc[0][t];
+#pragma unroll
+        for (int q = 1; q < kAcc; ++q) v += acc[q][t];
+        y[t] = v;
+    }
 }
 
 // One warp of a pair (half 0: rows [0, kK/2), half 1: the rest) solves its

@@ -316,30 +316,34 @@ __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __res
         for (int j = d - 1; j >= 0; --j) {
             const int oj = lpk_col(d, j) - j;
             const double wjj = 1.0 / S[oj + j];
-            double a0[R], a1[R];
+            double a[4][R];  // four independent fp64 FMA chains (static indices)
 #pragma unroll
-            for (int t = 0; t < R; ++t) a0[t] = a1[t] = 0.0;
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int t = 0; t < R; ++t) a[q][t] = 0.0;
             int okk = lpk_col(d, j + 1) - (j + 1);
-#pragma unroll 4
-            for (int k = j + 1; k < d; ++k) {
+            auto inv_step = [&](int k, double* acc) {
                 const double lkj = S[oj + k];  // L(k,j), broadcast
 #pragma unroll
                 for (int t = 0; t < R; ++t) {
                     const int i = lane + 32 * t;
-                    if (i >= k && i < d) {
-                        if (k & 1)
-                            a1[t] += S[okk + i] * lkj;  // W(i,k)
-                        else
-                            a0[t] += S[okk + i] * lkj;
-                    }
+                    if (i >= k && i < d) acc[t] += S[okk + i] * lkj;  // W(i,k)
                 }
                 okk += d - k - 1;
+            };
+            int k = j + 1;
+            for (; k + 3 < d; k += 4) {
+                inv_step(k, a[0]);
+                inv_step(k + 1, a[1]);
+                inv_step(k + 2, a[2]);
+                inv_step(k + 3, a[3]);
             }
+            for (; k < d; ++k) inv_step(k, a[0]);
             __syncwarp();  // every read of column j done before it is overwritten
 #pragma unroll
             for (int t = 0; t < R; ++t) {
                 const int i = lane + 32 * t;
-                if (i > j && i < d) S[oj + i] = -wjj * (a0[t] + a1[t]);
+                if (i > j && i < d) S[oj + i] = -wjj * ((a[0][t] + a[1][t]) + (a[2][t] + a[3][t]));
             }
             if (lane == 0) S[oj + j] = wjj;
             __syncwarp();
@@ -355,32 +359,36 @@ __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __res
         for (int k = 0; k < d; ++k) {
             const int ok = lpk_col(d, k) - k;
             const double wkk = S[ok + k];
-            double v0[R], v1[R];
+            double v[4][R];  // four independent fp64 FMA chains
 #pragma unroll
             for (int t = 0; t < R; ++t) {
                 const int j = lane + 32 * t;  // q = k term
-                v0[t] = j < k ? S[oc[t] + k] * wkk : (j == k ? wkk * wkk : 0.0);
-                v1[t] = 0.0;
+                v[0][t] = j < k ? S[oc[t] + k] * wkk : (j == k ? wkk * wkk : 0.0);
+                v[1][t] = v[2][t] = v[3][t] = 0.0;
             }
-#pragma unroll 4
-            for (int q2 = k + 1; q2 < d; ++q2) {
+            auto prod_step = [&](int q2, double* acc) {
                 const double wqk = S[ok + q2];  // broadcast
 #pragma unroll
                 for (int t = 0; t < R; ++t) {
                     const int j = lane + 32 * t;
                     if (j <= k) {
                         const double wqj = j == k ? wqk : S[oc[t] + q2];
-                        if (q2 & 1)
-                            v1[t] += wqj * wqk;
-                        else
-                            v0[t] += wqj * wqk;
+                        acc[t] += wqj * wqk;
                     }
                 }
+            };
+            int q2 = k + 1;
+            for (; q2 + 3 < d; q2 += 4) {
+                prod_step(q2, v[0]);
+                prod_step(q2 + 1, v[1]);
+                prod_step(q2 + 2, v[2]);
+                prod_step(q2 + 3, v[3]);
             }
+            for (; q2 < d; ++q2) prod_step(q2, v[0]);
 #pragma unroll
             for (int t = 0; t < R; ++t) {
                 const int j = lane + 32 * t;
-                if (j <= k) P[k * (k + 1) / 2 + j] = v0[t] + v1[t];
+                if (j <= k) P[k * (k + 1) / 2 + j] = (v[0][t] + v[1][t]) + (v[2][t] + v[3][t]);
             }
         }
         __syncwarp();

@@ -267,42 +267,54 @@ __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __res
                 }
             __syncwarp();
             fail = false;
-            for (int k = 0; k < d; ++k) {
-                const int ok = lpk_col(d, k) - k;  // L(i,k) at S[ok + i]
-                const double x = S[ok + k];
+            // left-looking (Crout) Cholesky, column by column: lane i forms
+            // s_i = D(i,j) - sum_{k<j} L(i,k) L(j,k) in four independent FMA
+            // chains (no read-modify-write of the trailing matrix), the pivot
+            // is the row-j lane's s, then the column is scaled and written
+            for (int j = 0; j < d; ++j) {
+                const int oj = lpk_col(d, j) - j;  // column j: (i,j) at S[oj + i]
+                double sc[4][R];
+#pragma unroll
+                for (int t = 0; t < R; ++t) {
+                    const int i = lane + 32 * t;
+                    sc[0][t] = (i >= j && i < d) ? S[oj + i] : 0.0;
+                    sc[1][t] = sc[2][t] = sc[3][t] = 0.0;
+                }
+                int okc = 0;  // lpk_col(d, k) - k, from k = 0
+                auto chol_step = [&](int k, double* acc) {
+                    const double ljk = S[okc + j];  // L(j,k), broadcast
+#pragma unroll
+                    for (int t = 0; t < R; ++t) {
+                        const int i = lane + 32 * t;
+                        if (i >= j && i < d) acc[t] -= S[okc + i] * ljk;
+                    }
+                    okc += d - k - 1;
+                };
+                int k = 0;
+                for (; k + 3 < j; k += 4) {
+                    chol_step(k, sc[0]);
+                    chol_step(k + 1, sc[1]);
+                    chol_step(k + 2, sc[2]);
+                    chol_step(k + 3, sc[3]);
+                }
+                for (; k < j; ++k) chol_step(k, sc[0]);
+                double sv[R];
+#pragma unroll
+                for (int t = 0; t < R; ++t) sv[t] = (sc[0][t] + sc[1][t]) + (sc[2][t] + sc[3][t]);
+                // pivot: row j lives in lane j % 32, register slot j / 32
+                const double x = __shfl_sync(0xffffffffu, j < 32 ? sv[0] : sv[R - 1], j & 31);
                 if (x <= 0) {  // Eigen LLT: a non-positive pivot fails; NaN does not
                     fail = true;
                     break;
                 }
                 const double piv = sqrt(x);
-                __syncwarp();
-                if (lane == 0) S[ok + k] = piv;
 #pragma unroll
                 for (int t = 0; t < R; ++t) {
                     const int i = lane + 32 * t;
-                    if (i > k && i < d) S[ok + i] /= piv;
+                    if (i > j && i < d) S[oj + i] = sv[t] / piv;
                 }
-                __syncwarp();
-                double lik[R];
-#pragma unroll
-                for (int t = 0; t < R; ++t) {
-                    const int i = lane + 32 * t;
-                    lik[t] = (i > k && i < d) ? S[ok + i] : 0.0;
-                }
-                // trailing update S(i,j) -= L(i,k) L(j,k), k < j <= i
-                // (column offsets advance by d - j - 1: lpk_col(d, j) - j)
-                int oj = lpk_col(d, k + 1) - (k + 1);
-#pragma unroll 4
-                for (int j = k + 1; j < d; ++j) {
-                    const double ljk = S[ok + j];  // broadcast
-#pragma unroll
-                    for (int t = 0; t < R; ++t) {
-                        const int i = lane + 32 * t;
-                        if (i >= j && i < d) S[oj + i] -= lik[t] * ljk;
-                    }
-                    oj += d - j - 1;
-                }
-                __syncwarp();
+                if (lane == 0) S[oj + j] = piv;
+                __syncwarp();  // column j complete before later columns read it
             }
             if (!fail) break;
         }

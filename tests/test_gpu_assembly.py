@@ -266,3 +266,21 @@ def test_dump_block_coo_from_device(ctx, tmp_path):
     assert path.read_text() == f.getvalue()
     with pytest.raises(InvalidArgument):
         ctx.dump_block_coo(tmp_path / "missing_dir" / "x.txt")
+
+
+def test_assemble_filtered_pinned_host_overlap(ctx):
+    """Host-pointer assembly from PINNED buffers: the values upload runs on
+    the copy stream concurrently with the key filter and sort (only the
+    reduction waits for it) — still bit-exact, and repeated calls reuse the
+    upload buffers safely."""
+    import torch
+
+    sc = scenes.CONFIGS["stiff_beam"]()
+    ok, ov = O.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    want = oracle_assemble(ok, ov, sc.n_blocks)
+    hk = torch.from_numpy(sc.keys.view(np.int64)).pin_memory()
+    hv = torch.from_numpy(sc.vals).pin_memory()
+    hp = torch.from_numpy(sc.pinned).pin_memory()
+    for _ in range(3):
+        ctx.assemble_filtered(hk, hv, sc.n_blocks, hp)
+        assert_bitwise(ctx.copy_matrix()[1:], want)

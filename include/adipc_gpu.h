@@ -98,6 +98,11 @@ int adipc_gpu_assemble_filtered_device(adipc_gpu_ctx* ctx, const uint64_t* d_key
 int adipc_gpu_matrix_info(adipc_gpu_ctx* ctx, int32_t* n_block_rows, int64_t* n_blocks);
 /* copy SortedSymBlockCoo{rows, cols, blocks} out (block_coo.hpp:54-61) */
 int adipc_gpu_copy_matrix(adipc_gpu_ctx* ctx, uint32_t* rows, uint32_t* cols, double* blocks9);
+/* binary capture of the context's matrix (SPEC.md External Interfaces: binary triplet file for offline
+ * oracle checks): "ADIPCMAT", u32 version 1, i32 n_block_rows, i64 U, rows u32[U], cols u32[U],
+ * blocks f64[U][9] column-major; api.load_matrix_binary reads it back */
+int adipc_gpu_dump_matrix_binary(adipc_gpu_ctx* ctx, const char* path);
+
 /* ---- the step after the solve (TimeStepper, adipc/solver/newton.hpp:257-290), device pointers ----
  * Vectors in the reference block numbering: n_fem FEM vertices, then 4 blocks (p, rows of A) per body. */
 /* step_inf_norm (newton.hpp:257-270): max(|d_i| over FEM vertices, |d_p| + |d_A|_F max_xbar[b] over bodies) */

@@ -51,6 +51,7 @@ GPU_SIGNATURES = {
     "adipc_gpu_matrix_info": (ci, [vp, C.POINTER(i32), C.POINTER(i64)]),
     "adipc_gpu_copy_matrix": (ci, [vp, vp, vp, vp]),
     "adipc_gpu_dump_block_coo": (ci, [vp, C.c_char_p]),
+    "adipc_gpu_dump_matrix_binary": (ci, [vp, C.c_char_p]),
     "adipc_gpu_step_inf_norm_device": (ci, [vp, vp, i32, i32, vp, C.POINTER(cd)]),
     "adipc_gpu_apply_direction_device": (ci, [vp, vp, vp, cd, i64, vp]),
     "adipc_gpu_node_displacements_device": (ci, [vp, vp, i32, i32, vp, vp, vp]),

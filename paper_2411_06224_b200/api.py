@@ -32,7 +32,7 @@ from .context import Context, IndefiniteSubdomain, InvalidArgument, PcgResult, d
 
 __all__ = [
     "ExecPolicy", "make_block_key", "block_key_row", "block_key_col", "BlockTripletStream", "SortedSymBlockCoo",
-    "sort_stream", "fast_segment_reduction", "fast_hash_reduction", "srbk_spmv", "dump_block_coo", "split_12x12",
+    "sort_stream", "fast_segment_reduction", "fast_hash_reduction", "srbk_spmv", "dump_block_coo", "load_matrix_binary", "split_12x12",
     "split_sym_12x12", "split_12x3", "split_3x12", "DofMap", "two_level_abd_reduce", "subdomain_count", "Partition",
     "chunk_partition", "partition_block_graph", "MasHierarchy", "build_hierarchy", "block_edges", "Preconditioner",
     "MasPreconditioner", "BlockJacobiPreconditioner", "PcgResult", "pcg_solve", "IndefiniteSubdomain",
@@ -179,6 +179,22 @@ def dump_block_coo(A: SortedSymBlockCoo, f) -> None:
     for r, c, b in zip(A.rows, A.cols, A.blocks):
         nat = np.asarray(b, np.float64).reshape(3, 3).T  # column-major storage -> row-major
         f.write(f"{int(r)} {int(c)} " + " ".join("%g" % float(v) for v in nat.reshape(-1)) + "\n")
+
+
+def load_matrix_binary(path) -> SortedSymBlockCoo:
+    """Reads adipc_gpu_dump_matrix_binary's capture ("ADIPCMAT", version 1)."""
+    with open(path, "rb") as f:
+        head = f.read(24)
+        if len(head) != 24 or head[:8] != b"ADIPCMAT":
+            raise ValueError("not an ADIPCMAT capture")
+        version, n = np.frombuffer(head[8:16], np.uint32)[0], int(np.frombuffer(head[12:16], np.int32)[0])
+        if version != 1:
+            raise ValueError(f"unsupported ADIPCMAT version {version}")
+        U = int(np.frombuffer(head[16:24], np.int64)[0])
+        rows = np.frombuffer(f.read(4 * U), np.uint32).copy()
+        cols = np.frombuffer(f.read(4 * U), np.uint32).copy()
+        blocks = np.frombuffer(f.read(72 * U), np.float64).reshape(U, 9).copy()
+    return SortedSymBlockCoo(n, rows, cols, blocks)
 
 
 # -- block_split.hpp:10-33 (host tiling helpers used by producers) -----------

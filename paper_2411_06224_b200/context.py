@@ -160,6 +160,10 @@ class Context:
         self._check(self._L.adipc_gpu_node_displacements_device(self.h, ptr(d_dir), n_fem, n_abd, ptr(d_abd_body),
                                                                   ptr(d_jac36), ptr(d_out)))
 
+    def dump_matrix_binary(self, path):
+        """Binary capture of the device matrix (api.load_matrix_binary reads it)."""
+        self._check(self._L.adipc_gpu_dump_matrix_binary(self.h, str(path).encode()))
+
     def dump_block_coo(self, path):
         """srbk_spmv.hpp:52-60 of the device matrix (--dump-hessian text)."""
         self._check(self._L.adipc_gpu_dump_block_coo(self.h, str(path).encode()))

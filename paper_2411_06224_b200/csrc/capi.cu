@@ -375,6 +375,40 @@ int adipc_gpu_copy_matrix(adipc_gpu_ctx* ctx, uint32_t* rows, uint32_t* cols, do
     });
 }
 
+// Binary capture of the context's matrix (SPEC.md "External Interfaces":
+// binary or text triplet file for offline oracle checks): little-endian
+// "ADIPCMAT" magic, u32 version 1, i32 n_block_rows, i64 U, then rows u32[U],
+// cols u32[U], blocks f64[U][9] (column-major 3x3, the reference's Mat3).
+int adipc_gpu_dump_matrix_binary(adipc_gpu_ctx* ctx, const char* path) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (!path) throw StatusError(kInvalidArgument, "dump_matrix_binary: null path");
+        const std::int64_t U = c.A.U;
+        std::vector<std::uint32_t> rows(static_cast<std::size_t>(U)), cols(static_cast<std::size_t>(U));
+        std::vector<double> b(9 * static_cast<std::size_t>(U));
+        if (U > 0) {
+            ADIPC_CUDA(cudaMemcpyAsync(rows.data(), c.A.rows.p, 4 * U, cudaMemcpyDeviceToHost, c.stream));
+            ADIPC_CUDA(cudaMemcpyAsync(cols.data(), c.A.cols.p, 4 * U, cudaMemcpyDeviceToHost, c.stream));
+            c.vals.reserve(9 * U);
+            blocks_soa_to_aos(c, c.A.blocks.p, c.vals.p, U);
+            ADIPC_CUDA(cudaMemcpyAsync(b.data(), c.vals.p, 72 * U, cudaMemcpyDeviceToHost, c.stream));
+            sync(c);
+        }
+        std::ofstream os(path, std::ios::binary);
+        if (!os) throw StatusError(kInvalidArgument, std::string("dump_matrix_binary: cannot open ") + path);
+        const std::uint32_t version = 1;
+        const std::int32_t n = c.A.n;
+        os.write("ADIPCMAT", 8);
+        os.write(reinterpret_cast<const char*>(&version), 4);
+        os.write(reinterpret_cast<const char*>(&n), 4);
+        os.write(reinterpret_cast<const char*>(&U), 8);
+        os.write(reinterpret_cast<const char*>(rows.data()), 4 * U);
+        os.write(reinterpret_cast<const char*>(cols.data()), 4 * U);
+        os.write(reinterpret_cast<const char*>(b.data()), 72 * U);
+        if (!os) throw StatusError(kInvalidArgument, std::string("dump_matrix_binary: write failed: ") + path);
+    });
+}
+
 // ---- the step after the solve (newton.hpp:257-290), device pointers ----------
 int adipc_gpu_step_inf_norm_device(adipc_gpu_ctx* ctx, const double* d_dir, int32_t n_fem, int32_t n_bodies,
                                    const double* d_max_xbar, double* out) {

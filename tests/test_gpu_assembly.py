@@ -284,3 +284,16 @@ def test_assemble_filtered_pinned_host_overlap(ctx):
     for _ in range(3):
         ctx.assemble_filtered(hk, hv, sc.n_blocks, hp)
         assert_bitwise(ctx.copy_matrix()[1:], want)
+
+
+def test_dump_matrix_binary_round_trip(ctx, tmp_path):
+    """adipc_gpu_dump_matrix_binary -> api.load_matrix_binary reproduces the
+    device matrix bit for bit (the binary capture for offline oracle checks)."""
+    sc = scenes.CONFIGS["cfg1_soft_cube"]()
+    fk, fv = ctx.filter_pinned(sc.keys, sc.vals, sc.pinned)
+    ctx.assemble(fk, fv, sc.n_blocks)
+    ctx.dump_matrix_binary(tmp_path / "A.bin")
+    A = P.load_matrix_binary(tmp_path / "A.bin")
+    n, rows, cols, blocks = ctx.copy_matrix()
+    assert A.n_block_rows == n
+    assert_bitwise((A.rows, A.cols, A.blocks), (rows, cols, blocks))

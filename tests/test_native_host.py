@@ -128,3 +128,25 @@ def test_scene_sizes_match_reference_generators():
     assert s.n_blocks == 1728 and len(s.keys) == 81588
     s = scenes.CONFIGS["stiff_beam"]()
     assert s.n_blocks == 5040 and len(s.keys) == 251880 and int(s.pinned.sum()) == 144
+
+
+def test_load_matrix_binary_format(tmp_path):
+    """api.load_matrix_binary: the ADIPCMAT layout (magic, version, n, U, rows,
+    cols, column-major blocks) and its error on foreign files."""
+    import numpy as np
+    import pytest
+
+    from paper_2411_06224_b200 import api as P
+
+    rows = np.array([0, 0, 1], np.uint32)
+    cols = np.array([0, 1, 1], np.uint32)
+    blocks = np.arange(27, dtype=np.float64).reshape(3, 9)
+    raw = (b"ADIPCMAT" + np.uint32(1).tobytes() + np.int32(2).tobytes() + np.int64(3).tobytes() + rows.tobytes()
+           + cols.tobytes() + blocks.tobytes())
+    (tmp_path / "m.bin").write_bytes(raw)
+    A = P.load_matrix_binary(tmp_path / "m.bin")
+    assert A.n_block_rows == 2 and np.array_equal(A.rows, rows) and np.array_equal(A.cols, cols)
+    assert np.array_equal(A.blocks, blocks)
+    (tmp_path / "bad.bin").write_bytes(b"NOTAMATRIX" + bytes(20))
+    with pytest.raises(ValueError):
+        P.load_matrix_binary(tmp_path / "bad.bin")

@@ -443,3 +443,24 @@ def test_spmv_and_mas_apply_shell_and_contact(ctx, name):
     M = O.MasPreconditioner(Am, O.Hierarchy(l0.part_of, l0.n_parts, 16, O.block_edges(rows, cols), 4))
     zo = M.apply(x)
     assert np.linalg.norm(ctx.precond_apply(x) - zo) <= 1e-10 * np.linalg.norm(zo)
+
+
+def test_step_entry_points_validate_arguments(ctx):
+    """Status 1 (std::invalid_argument in the shim) for bad sizes / missing
+    inputs of the post-solve entry points, as for the rest of the C ABI."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2411_06224_b200 import _lib
+    from paper_2411_06224_b200.context import InvalidArgument
+
+    L = _lib.gpu()
+    d = torch.zeros(12, dtype=torch.float64, device="cuda")
+    out = C.c_double()
+    assert L.adipc_gpu_step_inf_norm_device(ctx.h, d.data_ptr(), -1, 0, None, C.byref(out)) == 1
+    assert L.adipc_gpu_step_inf_norm_device(ctx.h, d.data_ptr(), 0, 1, None, C.byref(out)) == 1  # no max_xbar
+    assert L.adipc_gpu_apply_direction_device(ctx.h, d.data_ptr(), d.data_ptr(), 1.0, -3, d.data_ptr()) == 1
+    assert L.adipc_gpu_node_displacements_device(ctx.h, d.data_ptr(), -1, 0, None, None, d.data_ptr()) == 1
+    with pytest.raises(InvalidArgument):
+        ctx.step_inf_norm(d, 4, 1, None)

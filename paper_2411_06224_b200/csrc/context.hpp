@@ -202,7 +202,7 @@ struct Ctx {
     // kernels (solve_order.cu) when the levels allow them
     int l0_stages = 2;
     int pc_variant = 0;
-    int pc_pairs = 4;
+    int pc_pairs = 5;  // warp pairs per CTA of k_precond_so (ADIPC_OPT_PC_PAIRS): 5 -> 59.5 vs 61.0 us at cfg5
     int ws_cons = 8;
     bool invert_warp = true;
     // programmatic dependent launch between the PCG iteration's kernels

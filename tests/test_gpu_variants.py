@@ -29,7 +29,7 @@ VARIANTS = {
     "pc-1warp": {_lib.OPT_PC_VARIANT: 1},
     "pc-halfwarp": {_lib.OPT_PC_VARIANT: 2},
     "pc-warpspec": {_lib.OPT_PC_VARIANT: 3},
-    "pc-5pairs": {_lib.OPT_PC_PAIRS: 5},
+    "pc-4pairs": {_lib.OPT_PC_PAIRS: 4},
     "fused": {_lib.OPT_FUSED: 1},
     "persistent": {_lib.OPT_PERSISTENT: 1},
 }

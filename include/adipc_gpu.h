@@ -45,14 +45,9 @@ extern "C" {
 
 #define ADIPC_OPT_CACHE_HIERARCHY 1 /* reuse the MAS hierarchy while the sparsity is unchanged */
 #define ADIPC_OPT_PROFILE 2         /* time each PCG kernel class with CUDA events */
-#define ADIPC_OPT_L2_PERSIST 3      /* value/1024 of the matrix tiles kept L2-resident (evict-last) across SpMVs */
 #define ADIPC_OPT_SOLVE_ORDER 4     /* 1 (default): MAS/PCG renumber slots by level-0 subdomain internally */
-#define ADIPC_OPT_SPMV_VARIANT 5    /* SpMV kernel: 0 (default) LDG-streamed tiles, 2/3/4 TMA-staged (stages per warp), 5/6 TMA-staged two blocks per lane */
 #define ADIPC_OPT_SO_KERNELS 6      /* 1 (default): solve-order PCG iteration kernels; 0: the generic level kernels */
-#define ADIPC_OPT_PERSISTENT 8      /* 1: PCG iterations in one persistent cooperative kernel (solve order); default 0 */
-#define ADIPC_OPT_PC_VARIANT 9      /* preconditioner kernel: 0 (default) warp pairs per subdomain, 1 one warp per subdomain, 2 two subdomains per warp */
-#define ADIPC_OPT_FUSED 10          /* 1: update + MAS levels + prolongation in one cooperative kernel per PCG iteration (default 0) */
-#define ADIPC_OPT_PC_PAIRS 11       /* warp pairs per CTA of the preconditioner kernel (1..5, default 4) */
+#define ADIPC_OPT_PC_PAIRS 11       /* warp pairs per CTA of the preconditioner kernel (1..5, default 5) */
 #define ADIPC_OPT_L0_STAGES 7       /* 2 (default) or 3: packed inverses in flight per warp pair in the preconditioner */
 
 typedef struct adipc_gpu_ctx adipc_gpu_ctx;
@@ -158,11 +153,6 @@ int adipc_gpu_filter_pinned_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, c
  * x and y of 3 * n_block_rows doubles. */
 int adipc_gpu_spmv(adipc_gpu_ctx* ctx, const double* x, double* y);
 int adipc_gpu_spmv_device(adipc_gpu_ctx* ctx, const double* d_x, double* d_y);
-/* profiling aid: ms per SpMV launch of a variant (0 normal, 1 no transposed
- * scatter, 2 no atomics, 3 no column gather; 1-3 give wrong y) */
-int adipc_gpu_debug_spmv_time(adipc_gpu_ctx* ctx, const double* d_x, double* d_y, int mode, int iters, float* ms);
-/* profiling aid: (re)build the sliced-ELL SpMV copy from the current matrix */
-int adipc_gpu_debug_build_sell(adipc_gpu_ctx* ctx);
 
 /* ---- partition / hierarchy (host-side integer code, no GPU needed) ---------------- */
 int32_t adipc_subdomain_count(int32_t v, int32_t n, int32_t n_o);              /* partition.hpp:12-15 */

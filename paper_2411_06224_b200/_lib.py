@@ -24,14 +24,9 @@ OK, INVALID_ARGUMENT, INDEFINITE, CUDA_ERROR = 0, 1, 2, 3
 PRECOND_MAS, PRECOND_JACOBI = 1, 2
 OPT_CACHE_HIERARCHY = 1
 OPT_PROFILE = 2
-OPT_L2_PERSIST = 3
 OPT_SOLVE_ORDER = 4
-OPT_SPMV_VARIANT = 5
 OPT_SO_KERNELS = 6
 OPT_L0_STAGES = 7
-OPT_PERSISTENT = 8
-OPT_PC_VARIANT = 9
-OPT_FUSED = 10
 OPT_PC_PAIRS = 11
 
 # Every symbol include/adipc_gpu.h declares, with its ctypes signature.
@@ -64,8 +59,6 @@ GPU_SIGNATURES = {
     "adipc_gpu_filter_pinned_device": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
     "adipc_gpu_spmv": (ci, [vp, vp, vp]),
     "adipc_gpu_spmv_device": (ci, [vp, vp, vp]),
-    "adipc_gpu_debug_spmv_time": (ci, [vp, vp, vp, ci, ci, C.POINTER(C.c_float)]),
-    "adipc_gpu_debug_build_sell": (ci, [vp]),
     "adipc_subdomain_count": (i32, [i32, i32, i32]),
     "adipc_chunk_partition": (i32, [i32, i32, vp]),
     "adipc_partition_block_graph": (i32, [i32, vp, i64, i32, vp]),

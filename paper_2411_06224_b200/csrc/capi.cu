@@ -18,9 +18,13 @@ struct adipc_hierarchy {
 
 namespace adipc_gpu {
 Ctx* unwrap(adipc_gpu_ctx* c) { return &c->c; }
-long long& launch_counter() {
-    static long long n = 0;
+std::atomic<long long>& launch_counter() {
+    static std::atomic<long long> n{0};
     return n;
+}
+CaptureCount& capture_count() {
+    thread_local CaptureCount cc;
+    return cc;
 }
 }  // namespace adipc_gpu
 
@@ -113,32 +117,6 @@ int adipc_gpu_create(int device, adipc_gpu_ctx** out) {
         ADIPC_CUDA(cudaSetDevice(device));
         ADIPC_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
         ctx->c.own_stream = true;
-        // tuning overrides of the streaming kernels' tile shapes (experiments)
-        auto env_int = [](const char* name, int lo, int hi, int& v) {
-            if (const char* e = std::getenv(name)) {
-                const int x = std::atoi(e);
-                if (x >= lo && x <= hi) v = x;
-            }
-        };
-        env_int("ADIPC_UPD_SUBS", 4, 128, ctx->c.upd_subs);
-        env_int("ADIPC_FINAL_PER", 1, 4, ctx->c.final_per);
-        if (ctx->c.final_per == 3) ctx->c.final_per = 2;
-        env_int("ADIPC_FINAL_BLOCK", 64, 512, ctx->c.final_block);
-        env_int("ADIPC_PC_PAIRS", 1, 5, ctx->c.pc_pairs);
-        int ps = 0;
-        env_int("ADIPC_PC_SPLIT", 0, 1, ps);  // cost-weighted preconditioner split (measured slower)
-        ctx->c.pc_split = ps != 0;
-        env_int("ADIPC_WS_CONS", 4, 10, ctx->c.ws_cons);
-        env_int("ADIPC_L0_KEEP", 0, 1024, ctx->c.l0_keep_1024);
-        int iw = 1;
-        env_int("ADIPC_INVERT_WARP", 0, 1, iw);
-        ctx->c.invert_warp = iw != 0;
-        int pd = 1;
-        env_int("ADIPC_PDL", 0, 1, pd);
-        ctx->c.pdl = pd != 0;
-        int pp = 0;
-        env_int("ADIPC_PAD_P", 0, 1, pp);
-        ctx->c.pad_p = pp != 0;
     });
     if (rc != ADIPC_OK) {
         g_global_err = ctx->c.err;
@@ -176,11 +154,6 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.levels.clear();  // ~DeviceLevel releases the level buffers
     c.jinv.free();
     c.build_status.free();
-    c.sell.slice_off.free();
-    c.sell.row_id.free();
-    c.sell.cols.free();
-    c.sell.vals.free();
-    c.sell_len.free();
     c.step_max.free();
     for (auto* b : {&c.l0_part, &c.l0_mem_ptr, &c.l0_members, &c.l0_pos, &c.l1_up, &c.l1_ncomp, &c.l1_cnt, &c.l1_adj})
         b->free();
@@ -194,9 +167,6 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.graph_cur.free();
     c.graph_ptr2.free();
     c.perm.free();
-    for (auto& e : c.splits) e.buf.free();
-    c.splits.clear();
-    c.phase_ns.free();
     c.perm_keys.free();
     c.as_src.free();
     c.perm_vals.free();
@@ -206,10 +176,9 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.As.cols.free();
     c.As.blocks.free();
     c.As.row_ptr.free();
-    for (auto* b : {&c.w.x, &c.w.r, &c.w.p, &c.w.p4, &c.w.ap, &c.w.z, &c.w.b, &c.w.tmp, &c.w.partials, &c.w.scal}) b->free();
+    for (auto* b : {&c.w.x, &c.w.r, &c.w.p, &c.w.ap, &c.w.z, &c.w.b, &c.w.tmp, &c.w.partials, &c.w.scal}) b->free();
     c.w.tickets.free();
     c.w.flags.free();
-    c.w.counters.free();
     for (auto e : c.prof_events) cudaEventDestroy(e);
     if (c.side) cudaStreamDestroy(c.side);
     if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
@@ -248,26 +217,9 @@ int adipc_gpu_set_option(adipc_gpu_ctx* ctx, int option, int value) {
             ctx->c.cache_hierarchy = value != 0;
         else if (option == ADIPC_OPT_PROFILE)
             ctx->c.profile = value != 0;
-        else if (option == ADIPC_OPT_L2_PERSIST) {
-            if (value < 0 || value > 1024) throw StatusError(kInvalidArgument, "L2 persist fraction out of [0, 1024]");
-            ctx->c.l2_persist_1024 = value;
-            if (value > 0) {  // allow evict-last lines up to the device's persisting set-aside maximum
-                int mx = 0;
-                ADIPC_CUDA(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, ctx->c.device));
-                ADIPC_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<std::size_t>(mx)));
-            }
-        } else if (option == ADIPC_OPT_SPMV_VARIANT) {
-            if (value != 0 && (value < 2 || value > 8)) throw StatusError(kInvalidArgument, "SpMV variant not in {0,2..8}");
-            ctx->c.spmv_variant = value;
-        } else if (option == ADIPC_OPT_PC_PAIRS) {
+        else if (option == ADIPC_OPT_PC_PAIRS) {
             if (value < 1 || value > 5) throw StatusError(kInvalidArgument, "pairs per CTA not in 1..5");
             ctx->c.pc_pairs = value;
-        } else if (option == ADIPC_OPT_FUSED) {
-            ctx->c.fused = value != 0;
-        } else if (option == ADIPC_OPT_PC_VARIANT) {
-            ctx->c.pc_variant = value;
-        } else if (option == ADIPC_OPT_PERSISTENT) {
-            ctx->c.persistent = value != 0;
         } else if (option == ADIPC_OPT_SO_KERNELS) {
             ctx->c.so_kernels = value != 0;
         } else if (option == ADIPC_OPT_L0_STAGES) {
@@ -601,7 +553,7 @@ int adipc_gpu_spmv(adipc_gpu_ctx* ctx, const double* x, double* y) {
         DBuf<double> dx, dy;
         h2d(dx, x, n3, c.stream);
         dy.reserve(n3);
-        spmv(c, dx.p, dy.p, nullptr, 0);
+        spmv(c, dx.p, dy.p);
         if (n3) ADIPC_CUDA(cudaMemcpyAsync(y, dy.p, 8 * n3, cudaMemcpyDeviceToHost, c.stream));
         sync(c);
         dx.free();
@@ -609,22 +561,9 @@ int adipc_gpu_spmv(adipc_gpu_ctx* ctx, const double* x, double* y) {
     });
 }
 
-}  // extern "C"
-namespace adipc_gpu {
-float spmv_debug_time(Ctx& c, const double* d_x, double* d_y, int mode, int iters);
-}
-extern "C" {
-int adipc_gpu_debug_build_sell(adipc_gpu_ctx* ctx) {
-    return guarded(ctx, [&] { build_sell(ctx->c); });
-}
-
-int adipc_gpu_debug_spmv_time(adipc_gpu_ctx* ctx, const double* d_x, double* d_y, int mode, int iters, float* ms) {
-    return guarded(ctx, [&] { *ms = spmv_debug_time(ctx->c, d_x, d_y, mode, iters); });
-}
-
 int adipc_gpu_spmv_device(adipc_gpu_ctx* ctx, const double* d_x, double* d_y) {
     return guarded(ctx, [&] {
-        spmv(ctx->c, d_x, d_y, nullptr, 0);
+        spmv(ctx->c, d_x, d_y);
         sync(ctx->c);
     });
 }

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -26,10 +27,25 @@ struct CudaError : std::runtime_error {
 
 // Every kernel launch of the library is followed by ADIPC_LAUNCH_CHECK, which
 // also counts it (adipc_gpu_kernel_launches(), the bench's gpu_launches).
-long long& launch_counter();
+// Launches recorded into a CUDA graph are counted on the capturing thread
+// (capture_count) and added to the global counter each time the graph is
+// replayed, so the counter reports kernels actually executed.
+std::atomic<long long>& launch_counter();
+struct CaptureCount {
+    bool active = false;
+    long long n = 0;
+};
+CaptureCount& capture_count();
+inline void count_launch() {
+    CaptureCount& cc = capture_count();
+    if (cc.active)
+        ++cc.n;
+    else
+        launch_counter().fetch_add(1, std::memory_order_relaxed);
+}
 #define ADIPC_LAUNCH_CHECK()                \
     do {                                    \
-        ++::adipc_gpu::launch_counter();    \
+        ::adipc_gpu::count_launch();        \
         ADIPC_CUDA(cudaGetLastError());     \
     } while (0)
 

@@ -80,28 +80,12 @@ struct DeviceLevel {
 
 enum PrecondKind : int { kNone = 0, kMas = 1, kJacobi = 2 };
 
-// Sliced-ELL copy of A for the PCG SpMV (sell.cu): slices of 32 reference
-// rows (lane = row), slot s = block s of each lane's row in the 32-block SoA
-// tile format; row / column ids in the solve order when it is active.
-struct SellMatrix {
-    std::int32_t n = 0, n_slices = 0;
-    std::int64_t slots = 0;
-    DBuf<std::int64_t> slice_off;  // slice -> first slot (n_slices + 1)
-    DBuf<std::int32_t> row_id;     // 32 per slice, -1 past the last row
-    DBuf<std::uint32_t> cols;      // 32 per slot, 0xFFFFFFFF = padding
-    DBuf<double> vals;             // 288 per slot
-    std::uint64_t a_version = ~0ull, levels_version = ~0ull;
-    bool perm_active = false;
-};
-
 struct PcgWork {
     DBuf<double> x, r, p, ap, z, b, tmp;
-    DBuf<double> p4;             // p padded to 4 doubles per slot (256-bit SpMV gathers)
     DBuf<double> partials;       // per-CTA partial dots
     DBuf<unsigned> tickets;      // last-block-done counters
     DBuf<double> scal;           // device scalars (see pcg.cu)
     DBuf<int> flags;             // device flags (see pcg.cu)
-    DBuf<unsigned> counters;     // in-kernel arrival counters of the fused iteration
 };
 
 struct Ctx {
@@ -145,8 +129,6 @@ struct Ctx {
     bool cache_hierarchy = false;   // reuse the hierarchy while the pattern is unchanged
 
     PcgWork w;
-    SellMatrix sell;
-    DBuf<std::int64_t> sell_len;
     DBuf<unsigned long long> step_max;  // step_inf_norm result (step.cu)
     // level-0 graph of the cold hierarchy build (block_edges + build_graph on the device)
     DBuf<std::int32_t> graph_deg, graph_adj, graph_adj2;
@@ -191,40 +173,13 @@ struct Ctx {
     int* h_flags = nullptr;
     cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
 
-    // fraction (x/1024) of A's tiles the SpMV loads with L2 evict-last
-    // priority (ADIPC_OPT_L2_PERSIST)
-    int l2_persist_1024 = 0;
-    // SpMV kernel variant (ADIPC_OPT_SPMV_VARIANT): 0 LDG-streamed tiles,
-    // 2/3/4 TMA-staged tiles with that many chunks in flight per warp
-    int spmv_variant = 0;
-    // TMA ring depth (packed inverses in flight per warp) of the solve-order
-    // level-0 solve; ADIPC_OPT_SO_KERNELS selects the solve-order iteration
-    // kernels (solve_order.cu) when the levels allow them
+    // packed inverses in flight per warp pair of the preconditioner (TMA ring
+    // depth, ADIPC_OPT_L0_STAGES) and warp pairs per CTA (ADIPC_OPT_PC_PAIRS:
+    // 5 -> 59.5 vs 61.0 us at cfg5)
     int l0_stages = 2;
-    int pc_variant = 0;
-    int pc_pairs = 5;  // warp pairs per CTA of k_precond_so (ADIPC_OPT_PC_PAIRS): 5 -> 59.5 vs 61.0 us at cfg5
-    int ws_cons = 8;
-    bool invert_warp = true;
-    // programmatic dependent launch between the PCG iteration's kernels
-    // (ADIPC_PDL=0 disables): each starts its independent prologue while the
-    // previous one drains
-    bool pdl = true;  // warp-per-subdomain factorisation/inversion (ADIPC_INVERT_WARP=0: CTA kernel)
-    // share (x/1024) of the level-0 inverses streamed with L2 evict-last, so
-    // they stay L2-resident from one PCG iteration to the next (ADIPC_L0_KEEP)
-    int l0_keep_1024 = 0;          // consumer warps of the warp-specialised preconditioner (ADIPC_WS_CONS)
-    // tile shapes of the streaming kernels (ADIPC_UPD_SUBS / ADIPC_FINAL_PER /
-    // ADIPC_FINAL_BLOCK environment overrides, read at context creation)
-    int upd_subs = 64, final_per = 1, final_block = 256;
-    bool pad_p = false;  // 4-double-per-slot copy of p for 256-bit SpMV gathers (ADIPC_PAD_P=1; measured: no gain)
-    double* p4_active = nullptr;  // the padded copy the current solve maintains (else null)        // warp pairs per CTA of k_precond_so (ADIPC_OPT_PC_PAIRS)
-    bool pc_split = false;   // cost-weighted instead of equal-count work split  // preconditioner kernel: 0 warp pairs per item, 1 one warp per item (ADIPC_OPT_PC_VARIANT)
+    int pc_pairs = 5;
+    // solve-order iteration kernels (ADIPC_OPT_SO_KERNELS) when the levels allow them
     bool so_kernels = true;
-    // update + every MAS level + prolongation in one cooperative kernel per
-    // iteration (ADIPC_OPT_FUSED; solve_order.cu k_iter_so)
-    bool fused = false;
-    // the PCG iterations as one persistent cooperative kernel (ADIPC_OPT_PERSISTENT)
-    bool persistent = false;
-    DBuf<unsigned long long> phase_ns;  // its per-phase times (ADIPC_OPT_PROFILE)
 
     // per-kernel-class PCG timing (ADIPC_OPT_PROFILE): spmv, level 0, coarse, final
     bool profile = false;
@@ -278,16 +233,10 @@ std::int64_t two_level_abd_reduce(Ctx& c, const std::uint64_t* d_keys, const dou
                                   double* d_out_vals, std::int64_t out_cap);
 
 // spmv.cu
-void spmv(Ctx& c, const double* d_x, double* d_y, double* d_pdot_partials, int n_partials);
+void spmv(Ctx& c, const double* d_x, double* d_y);
 int spmv_grid(const Ctx& c, const DeviceMatrix& M);
 void spmv_launch(Ctx& c, const DeviceMatrix& M, const double* d_x, double* d_y, bool zero_y, const int* flags,
-                 double* partials, unsigned* ticket, double* dot_out, bool pad = false);
-
-// sell.cu
-void build_sell(Ctx& c);
-bool sell_current(const Ctx& c);
-void sell_spmv_launch(Ctx& c, const double* d_x, double* d_y, const int* flags, double* partials, unsigned* ticket,
-                      double* dot_out);
+                 double* partials, unsigned* ticket, double* dot_out);
 
 // mas.cu
 void build_preconditioner(Ctx& c, PrecondKind kind);

@@ -694,7 +694,7 @@ void factorize(Ctx& c) {
     for (auto& Lp : c.levels) {
         DeviceLevel& L = *Lp;
         const int dim = 3 * L.max_fill;
-        if (L.n_parts == 0 || dim > 64 || !c.invert_warp) continue;
+        if (L.n_parts == 0 || dim > 64) continue;
         tab.lv[tab.n] = InvertLevel{L.sub_ptr.p, L.dense_off.p, L.dense.p, L.inv_off.p, L.inv.p};
         tab.base[tab.n + 1] = tab.base[tab.n] + L.n_parts;
         ++tab.n;
@@ -723,7 +723,7 @@ void factorize(Ctx& c) {
         DeviceLevel& L = *Lp;
         if (L.n_parts == 0) continue;
         const int dim = 3 * L.max_fill;
-        if (dim <= 64 && c.invert_warp) continue;  // done above
+        if (dim <= 64) continue;  // done above
         const std::size_t need = 2 * sizeof(double) * dim * dim;
         const bool in_smem = need <= 200 * 1024;
         const int threads = dim <= 48 ? 128 : 256;
@@ -1175,13 +1175,10 @@ void launch_level(Ctx& c, int l, const double* r_in, double* z, const PcgArgs& a
         const int block = 32 * kLevelWarps;
 #define ADIPC_LVL(R)                                                                                           \
     do {                                                                                                       \
-        static bool attr = false;                                                                              \
-        if (!attr) {                                                                                           \
-            ADIPC_CUDA(cudaFuncSetAttribute(k_mas_level<kMode, R, kSolve>,                                     \
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,                       \
-                                            static_cast<int>(kLevelWarps * level_warp_smem(32 * R, R))));      \
-            attr = true;                                                                                       \
-        }                                                                                                      \
+        /* per-device attribute: set on every launch (cheap, legal while capturing) */                        \
+        ADIPC_CUDA(cudaFuncSetAttribute(k_mas_level<kMode, R, kSolve>,                                         \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,                           \
+                                        static_cast<int>(kLevelWarps * level_warp_smem(32 * R, R))));          \
         k_mas_level<kMode, R, kSolve><<<grid, block, smem, st>>>(la, a, partials, ticket, dot_out, ws);        \
     } while (0)
         if (regs == 1)

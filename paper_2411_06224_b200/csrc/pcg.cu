@@ -47,11 +47,6 @@ void launch_precond_so(Ctx& c, const double* r, double* z, const int* flags, dou
 template <int kFinal>
 void launch_final_so(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a);
 void clear_restrict_so(Ctx& c);
-bool pcg_persistent(Ctx& c, const PcgArgs& a, double* partials, int restart, int max_iters);
-bool iter_so_supported(const Ctx& c);
-void prepare_work_splits(Ctx& c);
-void pad4(Ctx& c, const double* p, double* p4);
-void launch_iter_so(Ctx& c, const PcgArgs& a, bool restart, unsigned* counters, double* partials);
 
 namespace {
 
@@ -110,14 +105,6 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     // solve-order iteration kernels (solve_order.cu)
     const bool so = c.so_kernels && so_supported(c);
     if (so) pmax = std::max(pmax, so_partials(c));
-    const bool fused = so && iter_so_supported(c);  // one kernel after the SpMV per iteration
-    if (so) prepare_work_splits(c);  // byte-balanced splits, before any graph capture
-    if (c.spmv_variant == 8 && !sell_current(c)) build_sell(c);  // sliced-ELL SpMV copy, before capture
-    // p padded to 4 doubles per slot for the SpMV's 256-bit gathers (the
-    // solve-order prolongation kernel keeps it current)
-    const bool pad = so && !fused && c.pad_p;
-    if (pad) w.p4.reserve(4 * static_cast<std::size_t>(n));
-    c.p4_active = pad ? w.p4.p : nullptr;
     w.partials.reserve(static_cast<std::size_t>(pmax) * T_COUNT);
     w.tickets.reserve(T_COUNT);
     w.scal.reserve(S_COUNT);
@@ -195,11 +182,6 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     }
     launch_final<F_PCG_INIT>(c, w.z.p, w.p.p, w.ap.p, a);
     if (so) clear_restrict_so(c);
-    if (pad) pad4(c, w.p.p, w.p4.p);
-    if (fused) {
-        w.counters.reserve(2);
-        ADIPC_CUDA(cudaMemsetAsync(w.counters.p, 0, 2 * sizeof(unsigned), st));
-    }
 
     // optional per-kernel-class timing (ADIPC_OPT_PROFILE): events bracket the
     // SpMV, update, preconditioner and prolongation/p-update launches of every
@@ -220,8 +202,8 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     // one iteration's launch sequence (restart variant: x += alpha p, r = b - A x)
     auto iteration = [&](bool is_restart, int slot) {
         mark(slot, 0);
-        spmv_launch(c, c.S(), pad ? w.p4.p : w.p.p, w.ap.p, false, w.flags.p, partials_of(T_SPMV),
-                    w.tickets.p + T_SPMV, w.scal.p + S_PAP, pad);
+        spmv_launch(c, c.S(), w.p.p, w.ap.p, false, w.flags.p, partials_of(T_SPMV), w.tickets.p + T_SPMV,
+                    w.scal.p + S_PAP);
         mark(slot, 1);
         if (is_restart) {
             k_x_update<<<slot_grid(c), 256, 0, st>>>(n3, a);
@@ -231,9 +213,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
             spmv_launch(c, c.S(), d_x, w.tmp.p, false, w.flags.p, nullptr, nullptr, nullptr);
             PcgArgs ar = a;
             ar.ap = w.tmp.p;
-            if (fused)
-                launch_iter_so(c, ar, true, w.counters.p, partials_of(T_LEVEL + 1));
-            else if (so)
+            if (so)
                 launch_update_so<M_RESTART>(c, ar);
             else if (mas)
                 launch_level<M_RESTART, false>(c, 0, nullptr, nullptr, ar, nullptr, nullptr, nullptr, st, true);
@@ -241,9 +221,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
                 launch_jacobi<M_RESTART>(c, nullptr, w.z.p, ar, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
                                          w.scal.p + S_RZ);
         } else {
-            if (fused)
-                launch_iter_so(c, a, false, w.counters.p, partials_of(T_LEVEL + 1));
-            else if (so)
+            if (so)
                 launch_update_so<M_UPDATE>(c, a);
             else if (mas)
                 launch_level<M_UPDATE, false>(c, 0, nullptr, nullptr, a, nullptr, nullptr, nullptr, st, true);
@@ -252,44 +230,41 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
                                         w.scal.p + S_RZ);
         }
         mark(slot, 2);
-        if (fused)
-            ;  // the fused kernel did the preconditioner and the prolongation
-        else if (so)
+        if (so)
             launch_precond_so(c, w.r.p, w.z.p, w.flags.p, partials_of(T_LEVEL), w.tickets.p + T_LEVEL,
                               w.scal.p + S_RZ);
         else if (mas)
             mas_apply(a);
         mark(slot, 3);
-        if (fused)
-            ;
-        else if (so)
+        if (so)
             launch_final_so<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
         else
             launch_final<F_PCG_STEP>(c, w.z.p, w.p.p, w.ap.p, a);
         mark(slot, 4);
     };
-    // the iterations as one persistent cooperative kernel (solve_order.cu)
-    const bool persist = so && pcg_persistent(c, a, part, restart, max_iters);
-    // otherwise: capture the two iteration variants as graphs (non-profiled runs)
+    // capture the two iteration variants as graphs (non-profiled runs)
     GraphExec g_norm, g_rest;
-    if (!prof && !persist) {
+    if (!prof) {
         auto capture = [&](bool is_restart, GraphExec& g) {
             cudaGraph_t graph;
             // kernels recorded into the graph are counted when the graph is
             // replayed (kernel_launches() reports kernels actually executed)
-            const long long before = launch_counter();
+            CaptureCount& cc = capture_count();
+            cc.active = true;
+            cc.n = 0;
             ADIPC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
             try {
                 iteration(is_restart, 0);
             } catch (...) {
+                cc.active = false;
                 cudaStreamEndCapture(st, &graph);
                 throw;
             }
+            cc.active = false;
             ADIPC_CUDA(cudaStreamEndCapture(st, &graph));
             ADIPC_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
             ADIPC_CUDA(cudaGraphDestroy(graph));
-            g.kernels = launch_counter() - before;
-            launch_counter() = before;
+            g.kernels = cc.n;
         };
         capture(false, g_norm);
         if (restart > 0 && restart <= max_iters) capture(true, g_rest);
@@ -301,7 +276,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     if (!c.ev_chunk[0])
         for (auto& e : c.ev_chunk) ADIPC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     int k = 1, ci = 0;
-    bool done = persist;
+    bool done = false;
     while (!done && k <= max_iters) {
         const int kbeg = k, kend = std::min(max_iters, k + chunk - 1);
         for (; k <= kend; ++k) {
@@ -337,12 +312,6 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
         ++ci;
     }
     ADIPC_CUDA(cudaEventRecord(e1, st));
-    if (persist && prof) {  // per-phase device times of the persistent kernel
-        unsigned long long ns[4];
-        ADIPC_CUDA(cudaMemcpyAsync(ns, c.phase_ns.p, sizeof(ns), cudaMemcpyDeviceToHost, st));
-        ADIPC_CUDA(cudaStreamSynchronize(st));
-        for (int q = 0; q < 4; ++q) c.prof_ms[q] = static_cast<float>(ns[q] * 1e-6);
-    }
     int h_final[F_COUNT];
     ADIPC_CUDA(cudaMemcpyAsync(h_final, w.flags.p, sizeof(h_final), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaMemcpyAsync(h_scal, w.scal.p, sizeof(h_scal), cudaMemcpyDeviceToHost, st));
@@ -350,7 +319,6 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     ADIPC_CUDA(cudaEventElapsedTime(&c.ms_pcg, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (h_final[F_ERR]) throw StatusError(kCudaError, "fused PCG iteration: in-kernel dependency wait timed out");
     if (h_final[F_DONE]) {
         out.iters = h_final[F_ITERS];
         out.converged = h_final[F_CONVERGED];
@@ -362,8 +330,6 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
         out.rel_residual = std::sqrt(std::fabs(rho) / h_scal[S_RHO_INIT]);
     }
     c.last_iters = out.iters;
-    c.p4_active = nullptr;
-    if (persist && prof) c.prof_iters = out.iters;
     return out;
 }
 

@@ -1,6 +1,6 @@
 """Profiling aid: one cfg5 Newton solve per option set, with the per-kernel-class
 CUDA-event breakdown of the PCG iteration (us per iteration) and the graph-mode
-PCG time. Usage: python tools/pcg_profile.py 'so=1,l0=3,spmv=3' 'so=0' ..."""
+PCG time. Usage: python tools/pcg_profile.py 'so=1,l0=3,pairs=4' 'so=0' ..."""
 import json
 import os
 import sys
@@ -13,8 +13,7 @@ from paper_2411_06224_b200 import _lib, scenes  # noqa: E402
 from paper_2411_06224_b200 import api as P  # noqa: E402
 from paper_2411_06224_b200.context import Context  # noqa: E402
 
-OPTS = {"so": _lib.OPT_SO_KERNELS, "l0": _lib.OPT_L0_STAGES, "spmv": _lib.OPT_SPMV_VARIANT,
-        "order": _lib.OPT_SOLVE_ORDER, "persist": _lib.OPT_PERSISTENT, "pc": _lib.OPT_PC_VARIANT, "fused": _lib.OPT_FUSED, "pairs": _lib.OPT_PC_PAIRS}
+OPTS = {"so": _lib.OPT_SO_KERNELS, "l0": _lib.OPT_L0_STAGES, "order": _lib.OPT_SOLVE_ORDER, "pairs": _lib.OPT_PC_PAIRS}
 sc = scenes.CONFIGS[os.environ.get("CFG", "cfg5_stiff_box")]()
 ctx = Context(0)
 l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, 16)

@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-solve-order", action="store_true",
                     help="run the MAS/PCG in the reference slot numbering (A/B of the solve-order renumbering)")
     ap.add_argument("--cpu-iters", type=int, default=10, help="PCG iterations per CPU sample step")
+    ap.add_argument("--selftest", action="store_true",
+                    help="launcher / rendezvous / stats-gather self-test without GPU work (CPU tests, gloo)")
     return ap.parse_args()
 
 
@@ -177,10 +179,30 @@ def byte_model(n, U, levels):
 
 # --------------------------------------------------------------- scenes ---
 def make_problem(config, seed):
-    from paper_2411_06224_b200 import scenes
+    """The rank's scene. cfg5: the batch of SURVEY.md §8d — rank r solves the
+    scene of seed 5 + r (seed 5 unjittered, the others with a +-1e-3 h vertex
+    jitter); other configs are the same scene on every rank."""
+    import scenegen as scenes
 
-    sc = scenes.CONFIGS[config]()
-    return sc
+    if config == "cfg5_stiff_box":
+        return scenes.cfg5_batch_scene(seed)
+    return scenes.CONFIGS[config]()
+
+
+WORKLOADS = {
+    "cfg5_stiff_box": "cfg5: stiff FEM box 68^3 cells, 985,527 DOF, E=1e8, PCG-only Newton solve, MAS cemas16 "
+                      "(4 levels), rel_tol 1e-4, restart 250; batch of scenes seeds 5.. (one per GPU)",
+}
+
+
+def workload_config(args, sc, world):
+    """The `config` object, identical in both arms (same keys, same values)."""
+    return {"workload": WORKLOADS.get(args.config, args.config), "config": args.config,
+            "n_block_rows": int(sc.n_blocks), "triplets": int(len(sc.keys)),
+            "contact_node_blocks": int(len(sc.node_keys)),
+            "l2": "inputs larger than L2 (A 203 MB + symmetric-packed MAS inverses 214 MB per scene, 126 MB L2)",
+            "parallelism": f"{world} independent scenes (replicas of the single-GPU solve)",
+            "seeds": list(range(5, 5 + world))}
 
 
 def cpu_reference(sc, rank_seed, cpu_iters, steps, warmup, sample_note=True, full_solve=False):
@@ -205,15 +227,15 @@ def cpu_reference(sc, rank_seed, cpu_iters, steps, warmup, sample_note=True, ful
         sk, sv = O.sort_stream(fk, fv, par)
         rows, cols, blocks = O.fast_hash_reduction(sk, sv, sc.n_blocks, par)
         t_asm = time.perf_counter() - t0
-        from paper_2411_06224_b200 import api as P  # host-only partition (no GPU call)
-
-        l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, CAPACITY)
+        # the level-0 partition by the reference's own partition_block_graph
+        # (partition.hpp:88-159, in oracle/_ref) — untimed, once per scene
+        part_of, n_parts = O.partition_block_graph(sc.n_blocks, sc.rest_edges, CAPACITY)
         t0 = time.perf_counter()
         A = O.Matrix(sc.n_blocks, rows, cols, blocks)
-        H = O.Hierarchy(l0.part_of, l0.n_parts, CAPACITY, O.block_edges(rows, cols), MAX_LEVELS)
+        H = O.Hierarchy(part_of, n_parts, CAPACITY, O.block_edges(rows, cols), MAX_LEVELS)
         M = O.MasPreconditioner(A, H)
         t_build = time.perf_counter() - t0
-        from paper_2411_06224_b200 import scenes as S
+        import scenegen as S
 
         b = S.gravity_rhs(sc)
         times = []
@@ -268,7 +290,7 @@ def run_ours(args, rank, world, local_rank, dist):
     ctx.assemble_filtered(d_keys, d_vals, sc.n_blocks, d_pin)
     n, U = ctx.matrix_info()
     # the first Newton step from rest: b = M dt^2 g, pinned slots zero
-    from paper_2411_06224_b200 import scenes as S
+    import scenegen as S
 
     d_b = torch.from_numpy(S.gravity_rhs(sc)).to(dev)
     d_x = torch.empty(3 * n, dtype=torch.float64, device=dev)
@@ -379,11 +401,7 @@ def run_ours(args, rank, world, local_rank, dist):
             "dtype": "f64",
             "data": "synthetic (reference generators: make_box_tets + stable Neo-Hookean first-Newton matrix; "
                     "b = M dt^2 g, the first Newton step from rest)",
-            "config": {"workload": "cfg5: stiff FEM box 68^3 cells, 985,527 DOF, E=1e8, PCG-only Newton solve, "
-                                   "MAS cemas16 (4 levels), rel_tol 1e-4, restart 250; one scene per GPU",
-                       "n_block_rows": n, "n_blocks": U, "triplets": int(len(sc.keys)),
-                       "l2": "inputs larger than L2 (A 203 MB + symmetric-packed MAS inverses 214 MB per scene, 126 MB L2)",
-                       "parallelism": f"{world} independent scenes (replicas of the single-GPU solve)"},
+            "config": workload_config(args, sc, world),
             "ms_per_newton_solve": (sum(g["build_ms"] + g["pcg_ms"] for g in gathered[:1]) / args.steps),
             "assembly_ms": asm_ms / args.steps,
             "mas_build_ms": build_ms / args.steps,
@@ -483,17 +501,67 @@ def run_e2e(args, ctx, sc, d_b, stream, dev):
     return {"ms": ms, "iters": iters, "h2d": int(h2d), "d2h": int(d2h)}
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` without an external launcher: start N ranks of this
+    script (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* set, rendezvous on
+    127.0.0.1), forward their output, and return the worst exit code."""
+    import socket
+
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
+
+
+def selftest(args, rank, world, dist):
+    """Launcher / rendezvous / max-over-ranks self-test (no GPU work): every
+    rank reports synthetic timings for its seed; rank 0 prints the gathered
+    aggregate. Used by the CPU tests at world size 2 over gloo."""
+    stats = dict(total_ms=10.0 + rank, pcg_ms=5.0 + rank, iters=100 + rank, conv=True, seed=5 + rank)
+    gathered, agg = gather_scene_stats(stats, world, dist)
+    if rank == 0:
+        print(json.dumps({"selftest": True, "n_gpus": world, "seeds": [g["seed"] for g in gathered], **agg}),
+              flush=True)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.selftest:
+        import torch.distributed as tdist
+
+        if world > 1:
+            tdist.init_process_group("gloo")
+        selftest(args, rank, world, tdist if world > 1 else None)
+        if world > 1:
+            tdist.barrier()
+            tdist.destroy_process_group()
+        return
     if args.impl == "reference":
         if rank != 0:
             return
-        from paper_2411_06224_b200 import scenes
+        # the reference arm loads only oracle/ libraries: the reference's own
+        # hot-path code (oracle/_ref) and the scene generators built under
+        # oracle/build — nothing from the product package
+        import scenegen as scenes
 
-        sc = scenes.CONFIGS[args.config]()
+        scenes.use_library("oracle")
+        sc = make_problem(args.config, 5)
         cb = cpu_reference(sc, 5, args.cpu_iters, args.steps, args.warmup, full_solve=not args.no_full_solve)
         full = cb["full_solve"]
         # e2e in the GPU arm's unit: PCG iterations per second of whole Newton
@@ -503,7 +571,7 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * args.cpu_iters / cb["value"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (same generator and seed as the GPU arm)",
-                "config": {"workload": "cfg5: stiff FEM box 68^3 cells, 985,527 DOF, E=1e8, MAS cemas16"},
+                "config": workload_config(args, sc, world),
                 "impl": "reference",
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "assembly_s": cb["assembly_s"], "mas_build_s": cb["mas_build_s"], "full_solve": full,

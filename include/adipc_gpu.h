@@ -138,6 +138,25 @@ int adipc_gpu_two_level_abd_reduce(adipc_gpu_ctx* ctx, const uint64_t* keys, con
                                    const double* abd_node_jacobian36, uint64_t* out_keys, double* out_vals9,
                                    int64_t out_capacity, int64_t* n_out);
 
+/* The contact half of IncrementalPotential::assemble as one device call:
+ *   stream_.append(two_level_abd_reduce(node_stream_, dofs, pol))   incremental_potential.hpp:392-394
+ *   filter_pinned(); sort_stream(...); hess = fast_hash_reduction(...)          :253-257
+ * The DOF stream (keys/vals9, T) is followed by the reduced tiles, which never
+ * leave the device; pinned (n bytes, may be NULL = nothing pinned) filters as
+ * filter_pinned does. The result is the context matrix (as adipc_gpu_assemble);
+ * n_tiles receives the number of appended tiles. Bit-exact with the reference's
+ * deterministic mode. */
+int adipc_gpu_assemble_contact(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T,
+                               const uint64_t* node_keys, const double* node_vals9, int64_t Tn, int32_t n_fem,
+                               int32_t n_bodies, int32_t n_abd, const int32_t* abd_node_body,
+                               const double* abd_node_jacobian36, int32_t n_block_rows, const uint8_t* pinned,
+                               int64_t* n_unique, int64_t* n_tiles);
+int adipc_gpu_assemble_contact_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const double* d_vals9, int64_t T,
+                                      const uint64_t* d_node_keys, const double* d_node_vals9, int64_t Tn,
+                                      int32_t n_fem, int32_t n_bodies, int32_t n_abd, const int32_t* d_abd_node_body,
+                                      const double* d_abd_node_jacobian36, int32_t n_block_rows,
+                                      const uint8_t* d_pinned, int64_t* n_unique, int64_t* n_tiles);
+
 /* IncrementalPotential::filter_pinned (incremental_potential.hpp:410-425):
  * drop blocks touching a pinned slot, append I3 per pinned slot.
  * out capacity >= T + n_slots. */

@@ -2,7 +2,6 @@
 with the repo snapshot to the GPU box).
 
   libadipc_gpu.so     CUDA kernels + C-ABI (include/adipc_gpu.h), sm_100a only
-  libadipc_scenes.so  host C++ synthetic-scene generators (bench/test inputs)
 """
 from __future__ import annotations
 
@@ -17,7 +16,6 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 GPU_LIB = os.path.join(PKG, "libadipc_gpu.so")
-SCENES_LIB = os.path.join(PKG, "libadipc_scenes.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -26,7 +24,6 @@ CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"  # image's $CX
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter"]
 
 GPU_SOURCES = ["assemble.cu", "spmv.cu", "mas.cu", "solve_order.cu", "pcg.cu", "abd.cu", "step.cu", "capi.cu", "host_precond.cpp"]
-SCENE_SOURCES = ["scenes.cpp"]
 
 
 def _nvcc() -> str:
@@ -69,12 +66,6 @@ def build(verbose: bool = False) -> None:
         objs = list(ex.map(lambda s: _compile(s, verbose), GPU_SOURCES))
     if _stale(GPU_LIB, objs):
         cmd = [_nvcc(), *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fopenmp", "-lgomp", "-o", GPU_LIB, *objs]
-        if verbose:
-            print(" ".join(cmd), flush=True)
-        subprocess.check_call(cmd)
-    scene_srcs = [os.path.join(CSRC, s) for s in SCENE_SOURCES]
-    if _stale(SCENES_LIB, scene_srcs):
-        cmd = [CXX, *CXX_FLAGS, "-shared", "-o", SCENES_LIB, *scene_srcs]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)

@@ -1,6 +1,6 @@
-"""ctypes binding of libadipc_gpu.so (include/adipc_gpu.h) and
-libadipc_scenes.so. Loading fails loudly when the native library is missing:
-there is no CPU fallback on the product path."""
+"""ctypes binding of libadipc_gpu.so (include/adipc_gpu.h). Loading fails
+loudly when the native library is missing: there is no CPU fallback on the
+product path."""
 from __future__ import annotations
 
 import ctypes as C
@@ -10,7 +10,6 @@ import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 GPU_LIB = os.path.join(PKG, "libadipc_gpu.so")
-SCENES_LIB = os.path.join(PKG, "libadipc_scenes.so")
 
 u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
@@ -55,6 +54,10 @@ GPU_SIGNATURES = {
     "adipc_gpu_sort_stream": (ci, [vp, vp, vp, i64]),
     "adipc_gpu_segment_reduce": (ci, [vp, vp, i64, vp, i64, ci, i32, ci, vp]),
     "adipc_gpu_two_level_abd_reduce": (ci, [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, i64, C.POINTER(i64)]),
+    "adipc_gpu_assemble_contact": (ci, [vp, vp, vp, i64, vp, vp, i64, i32, i32, i32, vp, vp, i32, vp,
+                                        C.POINTER(i64), C.POINTER(i64)]),
+    "adipc_gpu_assemble_contact_device": (ci, [vp, vp, vp, i64, vp, vp, i64, i32, i32, i32, vp, vp, i32, vp,
+                                               C.POINTER(i64), C.POINTER(i64)]),
     "adipc_gpu_filter_pinned": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
     "adipc_gpu_filter_pinned_device": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
     "adipc_gpu_spmv": (ci, [vp, vp, vp]),
@@ -79,18 +82,8 @@ GPU_SIGNATURES = {
     "adipc_gpu_pcg_device": (ci, [vp, vp, cd, ci, ci, vp, C.POINTER(ci), C.POINTER(cd), C.POINTER(ci)]),
 }
 
-SCENE_SIGNATURES = {
-    "adipc_scene_fem_box": (vp, [ci, ci, ci, cd, cd, cd, cd, cd, cd, cd, ci]),
-    "adipc_scene_cloth": (vp, [ci, ci, cd, cd, C.c_uint]),
-    "adipc_scene_abd_stack": (vp, [ci, ci, ci, C.c_uint]),
-    "adipc_scene_hybrid": (vp, [ci, ci, ci, ci, ci, C.c_uint]),
-    "adipc_scene_free": (None, [vp]),
-    "adipc_scene_sizes": (None, [vp, vp]),
-    "adipc_scene_copy": (None, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
-}
 
 _gpu = None
-_scenes = None
 
 
 def _load(path, sigs):
@@ -111,13 +104,6 @@ def gpu():
     if _gpu is None:
         _gpu = _load(GPU_LIB, GPU_SIGNATURES)
     return _gpu
-
-
-def scenes():
-    global _scenes
-    if _scenes is None:
-        _scenes = _load(SCENES_LIB, SCENE_SIGNATURES)
-    return _scenes
 
 
 def ptr(a) -> int | None:

@@ -139,6 +139,33 @@ class Context:
                                                             int(deterministic), C.byref(U)))
         return U.value
 
+    def assemble_contact(self, keys, vals, node_keys, node_vals, n_fem, n_bodies, abd_node_body, jac36,
+                         n_block_rows: int, pinned=None):
+        """two_level_abd_reduce + append + filter_pinned + sort + reduce
+        (incremental_potential.hpp:392-394, 253-257) in one call; the reduced
+        contact tiles stay on the device. Returns (U, n_tiles)."""
+        U, nt = C.c_int64(), C.c_int64()
+        T, Tn = len(keys), len(node_keys)
+        if _is_device(keys):
+            self._check(self._L.adipc_gpu_assemble_contact_device(
+                self.h, ptr(keys), ptr(vals), T, ptr(node_keys), ptr(node_vals), Tn, n_fem, n_bodies,
+                len(abd_node_body), ptr(abd_node_body), ptr(jac36), n_block_rows, ptr(pinned), C.byref(U),
+                C.byref(nt)))
+        else:
+            k = np.ascontiguousarray(keys, np.uint64)
+            v = np.ascontiguousarray(vals, np.float64).reshape(-1, 9)
+            nk = np.ascontiguousarray(node_keys, np.uint64)
+            nv = np.ascontiguousarray(node_vals, np.float64).reshape(-1, 9)
+            body = np.ascontiguousarray(abd_node_body, np.int32)
+            jac = np.ascontiguousarray(jac36, np.float64).reshape(-1, 36)
+            p = None if pinned is None else np.ascontiguousarray(pinned, np.uint8)
+            if p is not None and len(p) != n_block_rows:
+                raise InvalidArgument("pinned: one byte per block row expected")
+            self._check(self._L.adipc_gpu_assemble_contact(
+                self.h, ptr(k), ptr(v), T, ptr(nk), ptr(nv), Tn, n_fem, n_bodies, len(body), ptr(body), ptr(jac),
+                n_block_rows, ptr(p), C.byref(U), C.byref(nt)))
+        return U.value, nt.value
+
     def matrix_info(self):
         n, U = C.c_int32(), C.c_int64()
         self._check(self._L.adipc_gpu_matrix_info(self.h, C.byref(n), C.byref(U)))
@@ -225,12 +252,31 @@ class Context:
                                                     C.byref(n)))
         return ok[: n.value].copy(), ov[: n.value].copy()
 
+    # -- vector arguments -----------------------------------------------------------------
+    def _vec(self, a, name):
+        """The C entry points read / write exactly 3 * n_block_rows doubles
+        through the raw pointers: check length, dtype and layout here."""
+        n, _ = self.matrix_info()
+        if a is None:
+            raise InvalidArgument(f"{name}: missing vector")
+        if _is_device(a):
+            import torch
+
+            if a.dtype != torch.float64 or not a.is_contiguous() or a.numel() != 3 * n:
+                raise InvalidArgument(f"{name}: expected a contiguous float64 tensor of {3 * n} elements")
+            return a
+        a = np.ascontiguousarray(a, np.float64).reshape(-1)
+        if a.size != 3 * n:
+            raise InvalidArgument(f"{name}: length {a.size} != 3 * n_block_rows = {3 * n}")
+        return a
+
     # -- spmv ----------------------------------------------------------------------------
     def spmv(self, x, y=None):
+        x = self._vec(x, "x")
         if _is_device(x):
+            y = self._vec(y, "y")
             self._check(self._L.adipc_gpu_spmv_device(self.h, ptr(x), ptr(y)))
             return y
-        x = np.ascontiguousarray(x, np.float64).reshape(-1)
         y = np.empty_like(x)
         self._check(self._L.adipc_gpu_spmv(self.h, ptr(x), ptr(y)))
         return y
@@ -271,10 +317,11 @@ class Context:
         return s.value
 
     def precond_apply(self, r, z=None):
+        r = self._vec(r, "r")
         if _is_device(r):
+            z = self._vec(z, "z")
             self._check(self._L.adipc_gpu_precond_apply_device(self.h, ptr(r), ptr(z)))
             return z
-        r = np.ascontiguousarray(r, np.float64).reshape(-1)
         z = np.empty_like(r)
         self._check(self._L.adipc_gpu_precond_apply(self.h, ptr(r), ptr(z)))
         return z
@@ -282,11 +329,12 @@ class Context:
     # -- pcg ----------------------------------------------------------------------------------
     def pcg(self, b, rel_tol=1e-4, restart=250, max_iters=100000, x=None):
         it, rr, cv = C.c_int(), C.c_double(), C.c_int()
+        b = self._vec(b, "b")
         if _is_device(b):
+            x = self._vec(x, "x")
             self._check(self._L.adipc_gpu_pcg_device(self.h, ptr(b), rel_tol, restart, max_iters, ptr(x),
                                                      C.byref(it), C.byref(rr), C.byref(cv)))
         else:
-            b = np.ascontiguousarray(b, np.float64).reshape(-1)
             x = np.empty_like(b)
             self._check(self._L.adipc_gpu_pcg(self.h, ptr(b), rel_tol, restart, max_iters, ptr(x), C.byref(it),
                                               C.byref(rr), C.byref(cv)))

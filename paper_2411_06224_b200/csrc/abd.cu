@@ -143,39 +143,71 @@ __global__ void k_abd_emit(const std::uint32_t* __restrict__ rows, const std::ui
 
 }  // namespace
 
-std::int64_t two_level_abd_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t Tn,
-                                  std::int32_t n_fem, std::int32_t n_bodies, std::int32_t n_abd,
-                                  const std::int32_t* d_body, const double* d_jac36, std::uint64_t* d_out_keys,
-                                  double* d_out_vals, std::int64_t out_cap) {
+// LEVEL 1 + tile emission into `ok` / `ov` (reserved here to the exact tile
+// count when `grow`; otherwise out_cap bounds it). Scratch lives in the
+// context (reused across Newton iterations, freed with it).
+static std::int64_t two_level_impl(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t Tn,
+                                   std::int32_t n_fem, std::int32_t n_bodies, std::int32_t n_abd,
+                                   const std::int32_t* d_body, const double* d_jac36, DBuf<std::uint64_t>* grow_k,
+                                   DBuf<double>* grow_v, std::uint64_t* d_out_keys, double* d_out_vals,
+                                   std::int64_t out_cap) {
     cudaStream_t st = c.stream;
-    static thread_local DeviceMatrix merged;  // per host thread scratch
+    DeviceMatrix& merged = c.abd_l1;
     const std::int32_t n_nodes = n_fem + n_abd;
     sort_reduce(c, d_keys, d_vals, Tn, n_nodes, merged);  // LEVEL 1 (abd_reduce.hpp:35-37)
     const std::int64_t U = merged.U;
     if (U == 0) return 0;
     Map m{n_fem, n_bodies, n_abd, d_body, d_jac36};
-    DBuf<std::int32_t> cnt;
-    DBuf<std::int64_t> off;
-    cnt.reserve(U);
-    off.reserve(U + 1);
-    k_abd_count<<<grid_for(U, 256, 16), 256, 0, st>>>(merged.rows.p, merged.cols.p, U, m, cnt.p);
+    c.abd_cnt.reserve(U);
+    c.abd_off.reserve(U + 1);
+    k_abd_count<<<grid_for(U, 256, 16), 256, 0, st>>>(merged.rows.p, merged.cols.p, U, m, c.abd_cnt.p);
     ADIPC_LAUNCH_CHECK();
-    exclusive_scan(cnt.p, U, off.p, c.scan_scratch, st);
+    exclusive_scan(c.abd_cnt.p, U, c.abd_off.p, c.scan_scratch, st);
     std::int64_t total = 0;
-    ADIPC_CUDA(cudaMemcpyAsync(&total, off.p + U, sizeof(total), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaMemcpyAsync(&total, c.abd_off.p + U, sizeof(total), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaStreamSynchronize(st));
-    if (total > out_cap) {
-        cnt.free();
-        off.free();
+    if (grow_k) {
+        grow_k->reserve(static_cast<std::size_t>(total));
+        grow_v->reserve(9 * static_cast<std::size_t>(total));
+        d_out_keys = grow_k->p;
+        d_out_vals = grow_v->p;
+    } else if (total > out_cap) {
         throw StatusError(kInvalidArgument, "two_level_abd_reduce: output capacity too small");
     }
-    k_abd_emit<<<grid_for(U, 128, 16), 128, 0, st>>>(merged.rows.p, merged.cols.p, merged.blocks.p, U, m, off.p,
-                                                      d_out_keys, d_out_vals);
+    k_abd_emit<<<grid_for(U, 128, 16), 128, 0, st>>>(merged.rows.p, merged.cols.p, merged.blocks.p, U, m,
+                                                      c.abd_off.p, d_out_keys, d_out_vals);
     ADIPC_LAUNCH_CHECK();
-    ADIPC_CUDA(cudaStreamSynchronize(st));
-    cnt.free();
-    off.free();
     return total;
+}
+
+std::int64_t two_level_abd_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t Tn,
+                                  std::int32_t n_fem, std::int32_t n_bodies, std::int32_t n_abd,
+                                  const std::int32_t* d_body, const double* d_jac36, std::uint64_t* d_out_keys,
+                                  double* d_out_vals, std::int64_t out_cap) {
+    const std::int64_t total = two_level_impl(c, d_keys, d_vals, Tn, n_fem, n_bodies, n_abd, d_body, d_jac36, nullptr,
+                                              nullptr, d_out_keys, d_out_vals, out_cap);
+    ADIPC_CUDA(cudaStreamSynchronize(c.stream));
+    return total;
+}
+
+// The device fast path of assemble_contact (incremental_potential.hpp:
+// 392-394 then 253-257): the reduced tiles stay on the device in the
+// context's tile buffers and are appended to the DOF stream as its second
+// segment — filter_pinned, sort and reduce read both segments in place.
+std::int64_t assemble_contact(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T,
+                              const std::uint64_t* d_nkeys, const double* d_nvals, std::int64_t Tn,
+                              std::int32_t n_fem, std::int32_t n_bodies, std::int32_t n_abd, const std::int32_t* d_body,
+                              const double* d_jac36, std::int32_t n, const std::uint8_t* d_pinned,
+                              cudaEvent_t vals_ready) {
+    std::int64_t Tt = 0;
+    if (Tn > 0)
+        Tt = two_level_impl(c, d_nkeys, d_nvals, Tn, n_fem, n_bodies, n_abd, d_body, d_jac36, &c.tile_keys,
+                            &c.tile_vals, nullptr, nullptr, 0);
+    if (d_pinned)
+        assemble_filtered(c, d_keys, d_vals, T, n, d_pinned, vals_ready, c.tile_keys.p, c.tile_vals.p, Tt);
+    else
+        assemble_filtered(c, d_keys, d_vals, T, n, nullptr, vals_ready, c.tile_keys.p, c.tile_vals.p, Tt);
+    return Tt;
 }
 
 }  // namespace adipc_gpu

@@ -29,36 +29,106 @@ namespace adipc_gpu {
 
 namespace {
 
-constexpr std::uint32_t kNoIdentity = 0xFFFFFFFFu;
-constexpr int kWarpSortMax = 256;   // rows up to this length: one warp, smem bitonic
+constexpr int kWarpSortMax = 256;   // rows up to this length: one warp, register bitonic
 constexpr int kCtaSortMax = 8192;   // rows up to this length: one CTA, smem bitonic
 constexpr int kCtaSortThreads = 1024;
 
-__global__ void k_row_hist(const std::uint64_t* __restrict__ keys, std::int64_t T, std::int32_t n,
-                           std::int32_t* __restrict__ row_cnt, std::int32_t* __restrict__ err) {
-    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < T;
-         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const std::uint32_t row = static_cast<std::uint32_t>(keys[i] >> 32);
-        if (row >= static_cast<std::uint32_t>(n)) {
-            atomicOr(err, 1);
-            continue;
-        }
-        atomicAdd(row_cnt + row, 1);
+// The triplet stream as the kernels see it: up to two segments (the DOF
+// stream, then the reduced contact tiles appended by two_level_abd_reduce,
+// incremental_potential.hpp:392-394) and optionally filter_pinned
+// (incremental_potential.hpp:410-425) applied on the fly: an entry touching a
+// pinned slot is dropped, and every pinned slot s gets an I3 on its diagonal
+// with emission index T1 + T2 + s (after every stream entry). The emission
+// index of a kept entry is its index in the concatenated stream; the filter
+// keeps order, so sorting by it is sorting in the filtered stream's order.
+struct StreamSrc {
+    const std::uint64_t* k1;
+    const double* v1;
+    std::int64_t T1;
+    const std::uint64_t* k2;
+    const double* v2;
+    std::int64_t T2;
+    const std::uint8_t* pinned;  // null: no filter
+    std::int32_t n_pin;          // pinned slots (= n_block_rows when filtering)
+    const std::uint32_t* vidx;   // optional: emission index of key i (sorted-stream callers), else i
+    __device__ __forceinline__ std::int64_t total() const { return T1 + T2; }
+    __device__ __forceinline__ std::uint64_t key(std::int64_t i) const { return i < T1 ? k1[i] : k2[i - T1]; }
+    __device__ __forceinline__ bool kept(std::uint64_t k) const {
+        return !pinned || !(pinned[static_cast<std::uint32_t>(k >> 32)] | pinned[static_cast<std::uint32_t>(k)]);
     }
+    // address of the value of emission index q, or null for an appended I3
+    __device__ __forceinline__ const double* value(std::uint32_t q) const {
+        if (q < T1) return v1 + 9 * static_cast<std::int64_t>(q);
+        if (q < T1 + T2) return v2 + 9 * (static_cast<std::int64_t>(q) - T1);
+        return nullptr;
+    }
+};
+
+// Warp-aggregated atomicAdd on a per-row counter: lanes with the same row
+// share one atomic; returns this lane's slot among them (in lane order).
+__device__ __forceinline__ std::int32_t aggregated_add(std::int32_t* ctr, std::uint32_t row, bool valid) {
+    const unsigned grp = __match_any_sync(0xffffffffu, valid ? row : 0xFFFFFFFFu);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(grp) - 1;
+    std::int32_t base = 0;
+    if (valid && lane == leader) base = atomicAdd(ctr + row, __popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    return base + __popc(grp & ((1u << lane) - 1u));
 }
 
-// entry = (col << 32) | emission index; the index is i, or vidx[i] when the
-// keys are a filtered copy (vidx increasing: still the emission order)
-__global__ void k_row_scatter(const std::uint64_t* __restrict__ keys, std::int64_t T,
-                              const std::int64_t* __restrict__ row_start, std::int32_t* __restrict__ cursor,
-                              std::uint64_t* __restrict__ out, const std::uint32_t* __restrict__ vidx) {
-    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < T;
-         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const std::uint64_t k = keys[i];
-        const std::uint32_t row = static_cast<std::uint32_t>(k >> 32);
-        const std::int64_t pos = row_start[row] + atomicAdd(cursor + row, 1);
-        out[pos] = (k << 32) | (vidx ? vidx[i] : static_cast<std::uint32_t>(i));
+// 1. row histogram of the kept entries (+ one I3 per pinned slot)
+__global__ void k_row_hist(StreamSrc s, std::int32_t n, std::int32_t* __restrict__ row_cnt,
+                           std::int32_t* __restrict__ err) {
+    const std::int64_t T = s.total();
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t b = blockIdx.x * static_cast<std::int64_t>(blockDim.x); b < T; b += stride) {
+        const std::int64_t i = b + threadIdx.x;
+        bool valid = i < T;
+        std::uint32_t row = 0;
+        if (valid) {
+            const std::uint64_t k = s.key(i);
+            row = static_cast<std::uint32_t>(k >> 32);
+            if (row >= static_cast<std::uint32_t>(n) ||
+                (s.pinned && static_cast<std::uint32_t>(k) >= static_cast<std::uint32_t>(s.n_pin))) {
+                atomicOr(err, 1);
+                valid = false;
+            } else {
+                valid = s.kept(k);
+            }
+        }
+        aggregated_add(row_cnt, row, valid);
     }
+    if (s.pinned)
+        for (std::int64_t q = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; q < s.n_pin; q += stride)
+            if (s.pinned[q]) atomicAdd(row_cnt + q, 1);
+}
+
+// 2. bucket scatter of (col << 32 | emission index) into the row's range
+//    (slot order within a row is arbitrary here; fixed by the row sort)
+__global__ void k_row_scatter(StreamSrc s, std::int32_t n, const std::int64_t* __restrict__ row_start,
+                              std::int32_t* __restrict__ cursor, std::uint64_t* __restrict__ out) {
+    const std::int64_t T = s.total();
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t b = blockIdx.x * static_cast<std::int64_t>(blockDim.x); b < T; b += stride) {
+        const std::int64_t i = b + threadIdx.x;
+        bool valid = i < T;
+        std::uint64_t k = 0;
+        if (valid) {
+            k = s.key(i);
+            valid = static_cast<std::uint32_t>(k >> 32) < static_cast<std::uint32_t>(n) && s.kept(k);
+        }
+        const std::uint32_t row = static_cast<std::uint32_t>(k >> 32);
+        const std::int32_t slot = aggregated_add(cursor, row, valid);
+        if (valid)
+            out[row_start[row] + slot] =
+                (k << 32) | (s.vidx ? s.vidx[i] : static_cast<std::uint32_t>(i));
+    }
+    if (s.pinned)
+        for (std::int64_t q = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; q < s.n_pin; q += stride)
+            if (s.pinned[q]) {
+                const std::int64_t pos = row_start[q] + atomicAdd(cursor + q, 1);
+                out[pos] = (static_cast<std::uint64_t>(q) << 32) | static_cast<std::uint32_t>(T + q);
+            }
 }
 
 // Bitonic sort of s[0..N) (N power of two) by `nthr` cooperating threads.
@@ -84,40 +154,96 @@ __device__ __forceinline__ void bitonic(std::uint64_t* s, int N, int tid, int nt
         }
 }
 
-// One warp per row; rows longer than kWarpSortMax are deferred to the CTA
-// kernel through big_rows. Also counts unique cols of each sorted row.
+// Bitonic sort of 32 E 64-bit words held in registers, E per lane (element
+// g = E lane + e): exchanges closer than E stay in a lane, the others are
+// warp shuffles. No shared memory.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(std::uint64_t (&v)[E], int lane) {
+    constexpr int N = 32 * E;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < E) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int p = e ^ j;
+                    if (p > e) {
+                        const bool up = ((lane * E + e) & k) == 0;
+                        const std::uint64_t a = v[e], b = v[p];
+                        if ((a > b) == up) {
+                            v[e] = b;
+                            v[p] = a;
+                        }
+                    }
+                }
+            } else {
+                const int lj = j / E;
+                const bool lower = (lane & lj) == 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const std::uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], lj);
+                    const bool up = ((lane * E + e) & k) == 0;
+                    v[e] = (lower == up) ? (v[e] < o ? v[e] : o) : (v[e] < o ? o : v[e]);
+                }
+            }
+        }
+    }
+}
+
+template <int E>
+__device__ __forceinline__ int warp_sort_row(std::uint64_t* seg, int len, int lane) {
+    std::uint64_t v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int g = lane * E + e;
+        v[e] = g < len ? seg[g] : ~0ull;
+    }
+    warp_bitonic<E>(v, lane);
+    std::uint64_t prev = __shfl_up_sync(0xffffffffu, v[E - 1], 1);
+    int uniq = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int g = lane * E + e;
+        if (g < len) {
+            seg[g] = v[e];
+            uniq += (g == 0 || (v[e] >> 32) != (prev >> 32)) ? 1 : 0;
+        }
+        prev = v[e];
+    }
+    for (int o = 16; o > 0; o >>= 1) uniq += __shfl_xor_sync(0xffffffffu, uniq, o);
+    return uniq;
+}
+
+// 3. one warp per row: sort by (col, emission index) — the emission index as
+//    the low word makes it the reference's STABLE order — and count unique
+//    cols. Rows longer than kWarpSortMax are deferred to the CTA kernel.
 __global__ void k_sort_rows_warp(std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
                                  std::int32_t n, std::int32_t* __restrict__ uniq_cnt,
                                  std::int32_t* __restrict__ big_rows, std::int32_t* __restrict__ n_big) {
-    __shared__ std::uint64_t sm[8][kWarpSortMax];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    std::uint64_t* s = sm[w];
-    const int warps = gridDim.x * (blockDim.x >> 5);
-    for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps) {
-        const std::int64_t b = row_start[r], e = row_start[r + 1];
-        const int len = static_cast<int>(e - b);
-        if (len > kWarpSortMax) {
+    const int lane = threadIdx.x & 31;
+    const std::int32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const std::int32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (std::int32_t r = warp; r < n; r += warps) {
+        const std::int64_t b = row_start[r];
+        const int len = static_cast<int>(row_start[r + 1] - b);
+        std::uint64_t* seg = sorted + b;
+        int uniq;
+        if (len <= 1)
+            uniq = len;
+        else if (len <= 32)
+            uniq = warp_sort_row<1>(seg, len, lane);
+        else if (len <= 64)
+            uniq = warp_sort_row<2>(seg, len, lane);
+        else if (len <= 128)
+            uniq = warp_sort_row<4>(seg, len, lane);
+        else if (len <= kWarpSortMax)
+            uniq = warp_sort_row<8>(seg, len, lane);
+        else {
             if (lane == 0) big_rows[atomicAdd(n_big, 1)] = r;
             continue;
         }
-        if (len <= 1) {
-            if (lane == 0) uniq_cnt[r] = len;
-            continue;
-        }
-        int N = 2;
-        while (N < len) N <<= 1;
-        for (int i = lane; i < N; i += 32) s[i] = i < len ? sorted[b + i] : ~0ull;
-        __syncwarp();
-        bitonic<true>(s, N, lane, 32);
-        int uniq = 0;
-        for (int i = lane; i < len; i += 32) {
-            const std::uint64_t v = s[i];
-            sorted[b + i] = v;
-            uniq += (i == 0 || (v >> 32) != (s[i - 1] >> 32)) ? 1 : 0;
-        }
-        for (int o = 16; o > 0; o >>= 1) uniq += __shfl_xor_sync(0xffffffffu, uniq, o);
         if (lane == 0) uniq_cnt[r] = uniq;
-        __syncwarp();
     }
 }
 
@@ -207,29 +333,26 @@ __global__ void k_sort_rows_cta(std::uint64_t* __restrict__ sorted, std::uint64_
     }
 }
 
-// One warp per row: every head lane (first element of a unique col) sums its
-// run sequentially in emission order and writes the unique block into the
-// tiled block storage (blk(), common.cuh).
-// One warp per row, windows of 32 sorted entries: every lane loads its own
-// entry's block (all loads of a window in flight at once) into the warp's
-// shared tile, then each run's owner folds it SEQUENTIALLY in emission order
-// (bitwise the reference's deterministic left-to-right sum, reduction.hpp:
-// 39-53); a run crossing the window boundary carries its partial sum (and
-// output slot) to lane 0 of the next window. Writes the unique blocks into
-// the tiled block storage (blk(), common.cuh).
+// 4. one warp per row, windows of 32 sorted entries. The warp first gathers
+//    the window's 32 blocks into its shared tile cooperatively: load k of
+//    lane L fetches double 32 k + L of the window's 288 (entry (32 k + L) / 9,
+//    element (32 k + L) % 9), so each instruction reads ~4 whole 72-byte
+//    records instead of one double of 32 scattered records. Then each run's
+//    owner folds it SEQUENTIALLY in emission order (bitwise the reference's
+//    deterministic left-to-right sum, reduction.hpp:39-53); a run crossing the
+//    window boundary carries its partial sum (and output slot) to lane 0 of
+//    the next window. Writes the unique blocks into the tiled block storage
+//    (blk(), common.cuh).
 constexpr int kReduceWarps = 8;
 __global__ void __launch_bounds__(32 * kReduceWarps) k_reduce_rows(
     const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
-    const std::int64_t* __restrict__ uniq_start, std::int32_t n, const double* __restrict__ vals,
-    std::uint32_t* __restrict__ out_rows, std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks,
-    std::int64_t U, std::uint32_t identity_from) {
-    // value of emission index q: vals[9 q]; q >= identity_from is an appended
-    // pinned-diagonal I3 (filtered streams, assemble_filtered)
-    __shared__ double tile[kReduceWarps][9][32];
+    const std::int64_t* __restrict__ uniq_start, std::int32_t n, StreamSrc s, std::uint32_t* __restrict__ out_rows,
+    std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks) {
+    __shared__ double tile[kReduceWarps][9][33];
     __shared__ double carry[kReduceWarps][9];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
-    double(*T)[32] = tile[w];
+    double(*Tl)[33] = tile[w];
     double* C = carry[w];
     for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps) {
         const std::int64_t b = row_start[r], e = row_start[r + 1];
@@ -241,18 +364,19 @@ __global__ void __launch_bounds__(32 * kReduceWarps) k_reduce_rows(
             const bool valid = p < e;
             const std::uint64_t v = valid ? sorted[p] : ~0ull;
             const std::uint32_t col = static_cast<std::uint32_t>(v >> 32);
+            const std::uint32_t src = static_cast<std::uint32_t>(v);
             const std::uint32_t prev_col = __shfl_up_sync(0xffffffffu, col, 1);
-            bool head = valid && (lane == 0 ? (p == b || static_cast<std::uint32_t>(sorted[p - 1] >> 32) != col)
-                                            : prev_col != col);
-            if (valid) {
-                const std::uint32_t src = static_cast<std::uint32_t>(v);
-                if (src >= identity_from) {
+            const bool head = valid && (lane == 0 ? (p == b || static_cast<std::uint32_t>(sorted[p - 1] >> 32) != col)
+                                                  : prev_col != col);
+            const int nv = static_cast<int>(e - base < 32 ? e - base : 32);
 #pragma unroll
-                    for (int k = 0; k < 9; ++k) T[k][lane] = (k % 4 == 0) ? 1.0 : 0.0;
-                } else {
-                    const double* sv = vals + 9 * static_cast<std::int64_t>(src);
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) T[k][lane] = sv[k];
+            for (int k = 0; k < 9; ++k) {
+                const int word = 32 * k + lane;
+                const int j = word / 9, el = word - 9 * j;
+                const std::uint32_t q = __shfl_sync(0xffffffffu, src, j);
+                if (j < nv) {
+                    const double* sv = s.value(q);
+                    Tl[el][j] = sv ? sv[el] : ((el & 3) == 0 ? 1.0 : 0.0);
                 }
             }
             // does the window's last run continue past it?
@@ -261,7 +385,6 @@ __global__ void __launch_bounds__(32 * kReduceWarps) k_reduce_rows(
                                                                static_cast<std::uint32_t>(sorted[nxt] >> 32) == col,
                                               31);
             const unsigned hm = __ballot_sync(0xffffffffu, head);
-            const int nv = static_cast<int>(e - base < 32 ? e - base : 32);
             __syncwarp();
             const bool owner = head || (lane == 0 && carried);
             if (owner) {
@@ -271,14 +394,14 @@ __global__ void __launch_bounds__(32 * kReduceWarps) k_reduce_rows(
                 double acc[9];
                 if (head) {
 #pragma unroll
-                    for (int k = 0; k < 9; ++k) acc[k] = T[k][lane];
+                    for (int k = 0; k < 9; ++k) acc[k] = Tl[k][lane];
                 } else {  // continuing run: carried sum, then this window's entries
 #pragma unroll
-                    for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(C[k], T[k][lane]);
+                    for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(C[k], Tl[k][lane]);
                 }
                 for (int j = lane + 1; j < end; ++j)
 #pragma unroll
-                    for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(acc[k], T[k][j]);
+                    for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(acc[k], Tl[k][j]);
                 const std::int64_t my_u = head ? u + __popc(hm & ((1u << lane) - 1u)) : carry_u;
                 if (end == nv && cont_out) {  // hand over to the next window
 #pragma unroll
@@ -400,33 +523,7 @@ __global__ void k_pin_identity(const std::uint8_t* __restrict__ pinned, std::int
     }
 }
 
-// filter_pinned on the keys only: kept keys compacted in order, vidx = their
-// index in the original stream (values stay where they are)
-__global__ void k_pin_compact_keys(const std::uint64_t* __restrict__ keys, std::int64_t T,
-                                   const std::int32_t* __restrict__ keep, const std::int64_t* __restrict__ pos,
-                                   std::uint64_t* __restrict__ ok, std::uint32_t* __restrict__ vidx) {
-    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < T;
-         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        if (!keep[i]) continue;
-        const std::int64_t p = pos[i];
-        ok[p] = keys[i];
-        vidx[p] = static_cast<std::uint32_t>(i);
-    }
-}
 
-// the appended identities take emission indices T, T + 1, ... (after every
-// original entry), which the reduction recognises as I3
-__global__ void k_pin_identity_keys(const std::uint8_t* __restrict__ pinned, std::int32_t n_slots,
-                                    const std::int64_t* __restrict__ pos, std::int64_t base, std::int64_t T,
-                                    std::uint64_t* __restrict__ ok, std::uint32_t* __restrict__ vidx) {
-    for (std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; s < n_slots;
-         s += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        if (!pinned[s]) continue;
-        const std::int64_t p = base + pos[s];
-        ok[p] = (static_cast<std::uint64_t>(s) << 32) | static_cast<std::uint64_t>(s);
-        vidx[p] = static_cast<std::uint32_t>(T + pos[s]);
-    }
-}
 
 __global__ void k_u8_to_i32(const std::uint8_t* __restrict__ a, std::int64_t n, std::int32_t* __restrict__ b) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -436,50 +533,62 @@ __global__ void k_u8_to_i32(const std::uint8_t* __restrict__ a, std::int64_t n, 
 
 }  // namespace
 
-// Steps 1-5: bucket by row, sort each row by (col, emission index), count
+// Steps 1-3: bucket by row, sort each row by (col, emission index), count
 // unique cols. Leaves c.sorted / c.row_start / c.uniq_cnt filled. Throws
 // kInvalidArgument if a key's row is >= n.
-void bucket_sort(Ctx& c, const std::uint64_t* d_keys, std::int64_t T, std::int32_t n, const std::uint32_t* d_vidx) {
+static void bucket_sort(Ctx& c, const StreamSrc& s, std::int32_t n) {
     cudaStream_t st = c.stream;
-    if (T >= (std::int64_t(1) << 32)) throw StatusError(kInvalidArgument, "triplet stream longer than 2^32");
+    const std::int64_t T = s.T1 + s.T2;
+    const std::int64_t entries = T + (s.pinned ? s.n_pin : 0);
+    if (entries >= (std::int64_t(1) << 32) - 1) throw StatusError(kInvalidArgument, "triplet stream longer than 2^32");
     c.row_cnt.reserve(static_cast<std::size_t>(n) + 1);
     c.row_cursor.reserve(static_cast<std::size_t>(n) + 1);
     c.uniq_cnt.reserve(static_cast<std::size_t>(n) + 1);
     c.big_rows.reserve(static_cast<std::size_t>(n) + 1);
     c.row_start.reserve(static_cast<std::size_t>(n) + 1);
     c.counters.reserve(4);
-    c.sorted.reserve(static_cast<std::size_t>(T));
+    c.sorted.reserve(static_cast<std::size_t>(std::max<std::int64_t>(entries, 1)));
     ADIPC_CUDA(cudaMemsetAsync(c.row_cnt.p, 0, sizeof(std::int32_t) * (n + 1), st));
     ADIPC_CUDA(cudaMemsetAsync(c.row_cursor.p, 0, sizeof(std::int32_t) * (n + 1), st));
     ADIPC_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(std::int32_t) * 4, st));
-    if (T > 0) {
-        k_row_hist<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, n, c.row_cnt.p, c.counters.p);
+    if (entries > 0) {
+        k_row_hist<<<grid_for(entries, 256, 16), 256, 0, st>>>(s, n, c.row_cnt.p, c.counters.p);
         ADIPC_LAUNCH_CHECK();
     }
     exclusive_scan(c.row_cnt.p, n, c.row_start.p, c.scan_scratch, st);
-    if (T > 0) {
-        k_row_scatter<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, c.row_start.p, c.row_cursor.p, c.sorted.p,
-                                                             d_vidx);
+    if (entries > 0) {
+        k_row_scatter<<<grid_for(entries, 256, 16), 256, 0, st>>>(s, n, c.row_start.p, c.row_cursor.p, c.sorted.p);
         ADIPC_LAUNCH_CHECK();
     }
     if (n > 0) {
-        k_sort_rows_warp<<<grid_for(n, 8, 8), 256, 0, st>>>(c.sorted.p, c.row_start.p, n, c.uniq_cnt.p, c.big_rows.p,
-                                                            c.counters.p + 1);
+        k_sort_rows_warp<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, n, c.uniq_cnt.p, c.big_rows.p,
+                                                             c.counters.p + 1);
         ADIPC_LAUNCH_CHECK();
     }
     int h_counters[2] = {0, 0};
     ADIPC_CUDA(cudaMemcpyAsync(h_counters, c.counters.p, sizeof(h_counters), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaStreamSynchronize(st));
-    if (h_counters[0]) throw StatusError(kInvalidArgument, "block row index >= n_block_rows in triplet stream");
+    if (h_counters[0])
+        throw StatusError(kInvalidArgument, "block row index >= n_block_rows in triplet stream");
     if (h_counters[1] > 0) {
         const int nb = h_counters[1];
-        c.merge_scratch.reserve(static_cast<std::size_t>(T));
+        c.merge_scratch.reserve(static_cast<std::size_t>(entries));
         const int smem = kCtaSortMax * sizeof(std::uint64_t);
         ADIPC_CUDA(cudaFuncSetAttribute(k_sort_rows_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         k_sort_rows_cta<<<std::min(nb, kSMs * 2), kCtaSortThreads, smem, st>>>(
             c.sorted.p, c.merge_scratch.p, c.row_start.p, c.big_rows.p, c.counters.p + 1, c.uniq_cnt.p);
         ADIPC_LAUNCH_CHECK();
     }
+}
+
+static StreamSrc plain_src(const std::uint64_t* k, const double* v, std::int64_t T) {
+    return StreamSrc{k, v, T, nullptr, nullptr, 0, nullptr, 0, nullptr};
+}
+
+void bucket_sort(Ctx& c, const std::uint64_t* d_keys, std::int64_t T, std::int32_t n, const std::uint32_t* d_vidx) {
+    StreamSrc s = plain_src(d_keys, nullptr, T);
+    s.vidx = d_vidx;
+    bucket_sort(c, s, n);
 }
 
 void blocks_aos_to_soa(Ctx& c, const double* aos, double* soa, std::int64_t U) {
@@ -494,11 +603,11 @@ void blocks_soa_to_aos(Ctx& c, const double* soa, double* aos, std::int64_t U) {
 }
 
 // Sort + reduce of a device-resident triplet stream into `out` (CSR row_ptr
-// included). Shared by the global assembly and the two-level ABD reduction.
-void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
-                 DeviceMatrix& out, const std::uint32_t* d_vidx, std::uint32_t identity_from, cudaEvent_t vals_ready) {
+// included). Shared by the global assembly, the solve-order matrix and the
+// two-level ABD reduction.
+static void sort_reduce(Ctx& c, const StreamSrc& s, std::int32_t n, DeviceMatrix& out, cudaEvent_t vals_ready) {
     cudaStream_t st = c.stream;
-    bucket_sort(c, d_keys, T, n, d_vidx);  // keys only: overlaps an upload of the values still in flight
+    bucket_sort(c, s, n);  // keys only: overlaps an upload of the values still in flight
     if (vals_ready) ADIPC_CUDA(cudaStreamWaitEvent(st, vals_ready, 0));
     out.n = n;
     out.row_ptr.reserve(static_cast<std::size_t>(n) + 1);
@@ -507,16 +616,21 @@ void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std:
     ADIPC_CUDA(cudaMemcpyAsync(&U, out.row_ptr.p + n, sizeof(U), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaStreamSynchronize(st));
     out.U = U;
-    // whole 32-block tiles (the SpMV bulk-copies rows/cols per tile)
+    // whole 32-block tiles (the SpMV reads rows/cols per tile)
     out.rows.reserve(static_cast<std::size_t>((U + 31) & ~std::int64_t(31)));
     out.cols.reserve(static_cast<std::size_t>((U + 31) & ~std::int64_t(31)));
     out.blocks.reserve(blk_doubles(U));
     if (n > 0 && U > 0) {
-        k_reduce_rows<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, out.row_ptr.p, n, d_vals,
-                                                          out.rows.p, out.cols.p, out.blocks.p, U, identity_from);
+        k_reduce_rows<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, out.row_ptr.p, n, s, out.rows.p,
+                                                          out.cols.p, out.blocks.p);
         ADIPC_LAUNCH_CHECK();
     }
     ++out.version;
+}
+
+void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
+                 DeviceMatrix& out, cudaEvent_t vals_ready) {
+    sort_reduce(c, plain_src(d_keys, d_vals, T), n, out, vals_ready);
 }
 
 // sort_stream drop-in (block_coo.hpp:106-113): stable sort of the stream by
@@ -541,50 +655,22 @@ void sort_stream(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std:
 
 void assemble(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
               int /*deterministic: the device path is always the bitwise-deterministic order*/, cudaEvent_t vals_ready) {
-    sort_reduce(c, d_keys, d_vals, T, n, c.A, nullptr, kNoIdentity, vals_ready);
+    sort_reduce(c, plain_src(d_keys, d_vals, T), n, c.A, vals_ready);
 }
 
-// filter_pinned + sort + reduce without moving a value: the kept keys are
-// compacted with their original stream index (vidx) and the pinned-diagonal
-// identities appended (incremental_potential.hpp:410-425), the keys sorted,
-// and the reduction reads each value from the ORIGINAL stream through vidx,
-// in the same emission order — bitwise the compacted-stream result.
+// filter_pinned + sort + reduce without moving a value: the pin filter runs
+// inside the bucketing passes (dropped entries are never bucketed, the
+// pinned-diagonal identities are bucketed with emission indices past the
+// stream, incremental_potential.hpp:410-425), and the reduction reads each
+// kept value from the ORIGINAL stream in the same emission order — bitwise
+// the compacted-stream result. A second stream segment (the contact tiles
+// two_level_abd_reduce appends, incremental_potential.hpp:392-394) may
+// follow the first.
 void assemble_filtered(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
-                       const std::uint8_t* d_pinned, cudaEvent_t vals_ready) {
-    cudaStream_t st = c.stream;
-    if (T + n >= (std::int64_t(1) << 32) - 1) throw StatusError(kInvalidArgument, "triplet stream longer than 2^32");
-    DBuf<std::int32_t>& keep = c.pin_keep;
-    DBuf<std::int64_t>& pos = c.pin_pos;
-    DBuf<std::int64_t>& spos = c.pin_spos;
-    keep.reserve(static_cast<std::size_t>(std::max<std::int64_t>(T, n)) + 1);
-    pos.reserve(static_cast<std::size_t>(T) + 1);
-    spos.reserve(static_cast<std::size_t>(n) + 1);
-    c.fkeys.reserve(static_cast<std::size_t>(T + n) + 1);
-    c.fidx.reserve(static_cast<std::size_t>(T + n) + 1);
-    if (T > 0) {
-        k_pin_keep<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, d_pinned, keep.p);
-        ADIPC_LAUNCH_CHECK();
-    }
-    exclusive_scan(keep.p, T, pos.p, c.scan_scratch, st);
-    if (T > 0) {
-        k_pin_compact_keys<<<grid_for(T, 256, 16), 256, 0, st>>>(d_keys, T, keep.p, pos.p, c.fkeys.p, c.fidx.p);
-        ADIPC_LAUNCH_CHECK();
-    }
-    std::int64_t kept = 0, npin = 0;
-    ADIPC_CUDA(cudaMemcpyAsync(&kept, pos.p + T, sizeof(kept), cudaMemcpyDeviceToHost, st));
-    ADIPC_CUDA(cudaStreamSynchronize(st));
-    if (n > 0) {
-        k_u8_to_i32<<<grid_for(n, 256, 16), 256, 0, st>>>(d_pinned, n, keep.p);
-        ADIPC_LAUNCH_CHECK();
-    }
-    exclusive_scan(keep.p, n, spos.p, c.scan_scratch, st);
-    if (n > 0) {
-        k_pin_identity_keys<<<grid_for(n, 256, 16), 256, 0, st>>>(d_pinned, n, spos.p, kept, T, c.fkeys.p, c.fidx.p);
-        ADIPC_LAUNCH_CHECK();
-    }
-    ADIPC_CUDA(cudaMemcpyAsync(&npin, spos.p + n, sizeof(npin), cudaMemcpyDeviceToHost, st));
-    ADIPC_CUDA(cudaStreamSynchronize(st));
-    sort_reduce(c, c.fkeys.p, d_vals, kept + npin, n, c.A, c.fidx.p, static_cast<std::uint32_t>(T), vals_ready);
+                       const std::uint8_t* d_pinned, cudaEvent_t vals_ready, const std::uint64_t* d_keys2,
+                       const double* d_vals2, std::int64_t T2) {
+    const StreamSrc s{d_keys, d_vals, T, d_keys2, d_vals2, T2, d_pinned, n, nullptr};
+    sort_reduce(c, s, n, c.A, vals_ready);
 }
 
 void upload_matrix(Ctx& c, std::int32_t n, std::int64_t U, const std::uint32_t* rows, const std::uint32_t* cols,

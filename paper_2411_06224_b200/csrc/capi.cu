@@ -149,8 +149,25 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.scan_scratch.free();
     c.counters.free();
     c.pinned.free();
-    c.fkeys.free();
-    c.fidx.free();
+    for (DeviceMatrix* m : {&c.abd_l1}) {
+        m->rows.free();
+        m->cols.free();
+        m->blocks.free();
+        m->row_ptr.free();
+    }
+    c.abd_cnt.free();
+    c.abd_off.free();
+    c.tile_keys.free();
+    c.tile_vals.free();
+    c.io_keys.free();
+    c.io_keys2.free();
+    c.io_vals.free();
+    c.io_vals2.free();
+    c.io_jac.free();
+    c.io_body.free();
+    c.pin_keep.free();
+    c.pin_pos.free();
+    c.pin_spos.free();
     c.levels.clear();  // ~DeviceLevel releases the level buffers
     c.jinv.free();
     c.build_status.free();
@@ -486,27 +503,69 @@ int adipc_gpu_two_level_abd_reduce(adipc_gpu_ctx* ctx, const uint64_t* keys, con
                                    int64_t* n_out) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
-        if (Tn < 0 || n_fem < 0 || n_bodies < 0 || n_abd < 0) throw StatusError(kInvalidArgument, "negative size");
-        DBuf<std::uint64_t> dk, ok;
-        DBuf<double> dv, ov, dj;
-        DBuf<std::int32_t> db;
-        h2d(dk, keys, static_cast<std::size_t>(Tn), c.stream);
-        h2d(dv, vals9, 9 * static_cast<std::size_t>(Tn), c.stream);
-        h2d(db, body, static_cast<std::size_t>(n_abd), c.stream);
-        h2d(dj, jac36, 36 * static_cast<std::size_t>(n_abd), c.stream);
-        ok.reserve(static_cast<std::size_t>(out_cap));
-        ov.reserve(9 * static_cast<std::size_t>(out_cap));
-        const std::int64_t n = two_level_abd_reduce(c, dk.p, dv.p, Tn, n_fem, n_bodies, n_abd, db.p, dj.p, ok.p, ov.p,
-                                                    out_cap);
+        if (Tn < 0 || n_fem < 0 || n_bodies < 0 || n_abd < 0 || out_cap < 0)
+            throw StatusError(kInvalidArgument, "negative size");
+        h2d(c.io_keys, keys, static_cast<std::size_t>(Tn), c.stream);
+        h2d(c.io_vals, vals9, 9 * static_cast<std::size_t>(Tn), c.stream);
+        h2d(c.io_body, body, static_cast<std::size_t>(n_abd), c.stream);
+        h2d(c.io_jac, jac36, 36 * static_cast<std::size_t>(n_abd), c.stream);
+        c.io_keys2.reserve(static_cast<std::size_t>(std::max<std::int64_t>(out_cap, 1)));
+        c.io_vals2.reserve(9 * static_cast<std::size_t>(std::max<std::int64_t>(out_cap, 1)));
+        const std::int64_t n = two_level_abd_reduce(c, c.io_keys.p, c.io_vals.p, Tn, n_fem, n_bodies, n_abd,
+                                                    c.io_body.p, c.io_jac.p, c.io_keys2.p, c.io_vals2.p, out_cap);
         if (n) {
-            ADIPC_CUDA(cudaMemcpyAsync(out_keys, ok.p, 8 * n, cudaMemcpyDeviceToHost, c.stream));
-            ADIPC_CUDA(cudaMemcpyAsync(out_vals9, ov.p, 72 * n, cudaMemcpyDeviceToHost, c.stream));
+            ADIPC_CUDA(cudaMemcpyAsync(out_keys, c.io_keys2.p, 8 * n, cudaMemcpyDeviceToHost, c.stream));
+            ADIPC_CUDA(cudaMemcpyAsync(out_vals9, c.io_vals2.p, 72 * n, cudaMemcpyDeviceToHost, c.stream));
         }
         sync(c);
         if (n_out) *n_out = n;
-        for (auto* b : {&dk, &ok}) b->free();
-        for (auto* b : {&dv, &ov, &dj}) b->free();
-        db.free();
+    });
+}
+
+// two_level_abd_reduce + stream_.append + filter_pinned + sort_stream +
+// fast_hash_reduction in one call (incremental_potential.hpp:392-394 and
+// 253-257): the reduced contact tiles never leave the device.
+int adipc_gpu_assemble_contact(adipc_gpu_ctx* ctx, const uint64_t* keys, const double* vals9, int64_t T,
+                               const uint64_t* node_keys, const double* node_vals9, int64_t Tn, int32_t n_fem,
+                               int32_t n_bodies, int32_t n_abd, const int32_t* body, const double* jac36, int32_t n,
+                               const uint8_t* pinned, int64_t* n_unique, int64_t* n_tiles) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (T < 0 || Tn < 0 || n < 0 || n_fem < 0 || n_bodies < 0 || n_abd < 0)
+            throw StatusError(kInvalidArgument, "negative size");
+        h2d(c.keys, keys, static_cast<std::size_t>(T), c.stream);
+        if (pinned) h2d(c.pinned, pinned, static_cast<std::size_t>(n), c.stream);
+        h2d(c.io_keys, node_keys, static_cast<std::size_t>(Tn), c.stream);
+        h2d(c.io_vals, node_vals9, 9 * static_cast<std::size_t>(Tn), c.stream);
+        h2d(c.io_body, body, static_cast<std::size_t>(n_abd), c.stream);
+        h2d(c.io_jac, jac36, 36 * static_cast<std::size_t>(n_abd), c.stream);
+        cudaEvent_t ready = upload_values(c, vals9, T);
+        std::int64_t tiles = 0;
+        timed(c, [&] {
+            tiles = assemble_contact(c, c.keys.p, c.vals.p, T, c.io_keys.p, c.io_vals.p, Tn, n_fem, n_bodies, n_abd,
+                                     c.io_body.p, c.io_jac.p, n, pinned ? c.pinned.p : nullptr, ready);
+        });
+        if (n_unique) *n_unique = c.A.U;
+        if (n_tiles) *n_tiles = tiles;
+    });
+}
+
+int adipc_gpu_assemble_contact_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys, const double* d_vals9, int64_t T,
+                                      const uint64_t* d_node_keys, const double* d_node_vals9, int64_t Tn,
+                                      int32_t n_fem, int32_t n_bodies, int32_t n_abd, const int32_t* d_body,
+                                      const double* d_jac36, int32_t n, const uint8_t* d_pinned, int64_t* n_unique,
+                                      int64_t* n_tiles) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (T < 0 || Tn < 0 || n < 0 || n_fem < 0 || n_bodies < 0 || n_abd < 0)
+            throw StatusError(kInvalidArgument, "negative size");
+        std::int64_t tiles = 0;
+        timed(c, [&] {
+            tiles = assemble_contact(c, d_keys, d_vals9, T, d_node_keys, d_node_vals9, Tn, n_fem, n_bodies, n_abd,
+                                     d_body, d_jac36, n, d_pinned);
+        });
+        if (n_unique) *n_unique = c.A.U;
+        if (n_tiles) *n_tiles = tiles;
     });
 }
 
@@ -550,14 +609,11 @@ int adipc_gpu_spmv(adipc_gpu_ctx* ctx, const double* x, double* y) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
         const std::size_t n3 = 3 * static_cast<std::size_t>(c.A.n);
-        DBuf<double> dx, dy;
-        h2d(dx, x, n3, c.stream);
-        dy.reserve(n3);
-        spmv(c, dx.p, dy.p);
-        if (n3) ADIPC_CUDA(cudaMemcpyAsync(y, dy.p, 8 * n3, cudaMemcpyDeviceToHost, c.stream));
+        h2d(c.io_vals, x, n3, c.stream);
+        c.io_vals2.reserve(n3);
+        spmv(c, c.io_vals.p, c.io_vals2.p);
+        if (n3) ADIPC_CUDA(cudaMemcpyAsync(y, c.io_vals2.p, 8 * n3, cudaMemcpyDeviceToHost, c.stream));
         sync(c);
-        dx.free();
-        dy.free();
     });
 }
 
@@ -632,6 +688,9 @@ int adipc_gpu_set_level0_partition(adipc_gpu_ctx* ctx, const int32_t* part_of, i
         c.have_l0 = true;
         c.hier_version = ~0ull;
         c.levels.clear();
+        // the levels are gone: a preconditioner must be rebuilt before use
+        c.pkind = kNone;
+        c.perm_active = false;
     });
 }
 
@@ -728,14 +787,11 @@ int adipc_gpu_precond_apply(adipc_gpu_ctx* ctx, const double* r, double* z) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
         const std::size_t n3 = 3 * static_cast<std::size_t>(c.A.n);
-        DBuf<double> dr, dz;
-        h2d(dr, r, n3, c.stream);
-        dz.reserve(n3);
-        precond_apply(c, dr.p, dz.p);
-        if (n3) ADIPC_CUDA(cudaMemcpyAsync(z, dz.p, 8 * n3, cudaMemcpyDeviceToHost, c.stream));
+        h2d(c.io_vals, r, n3, c.stream);
+        c.io_vals2.reserve(n3);
+        precond_apply(c, c.io_vals.p, c.io_vals2.p);
+        if (n3) ADIPC_CUDA(cudaMemcpyAsync(z, c.io_vals2.p, 8 * n3, cudaMemcpyDeviceToHost, c.stream));
         sync(c);
-        dr.free();
-        dz.free();
     });
 }
 

@@ -103,10 +103,19 @@ struct Ctx {
     DBuf<std::int64_t> row_start, uniq_start, scan_scratch;
     DBuf<std::int32_t> counters;
     DBuf<std::uint8_t> pinned;
-    DBuf<std::uint64_t> fkeys;  // filtered keys (assemble_filtered)
-    DBuf<std::uint32_t> fidx;   // their index in the original stream (0xFFFFFFFF: pinned identity)
     DBuf<std::int32_t> pin_keep;
     DBuf<std::int64_t> pin_pos, pin_spos;
+    // two-level ABD reduction (abd.cu): level-1 node-pair matrix, tile counts /
+    // offsets, and the reduced tiles of the device fast path (assemble_contact)
+    DeviceMatrix abd_l1;
+    DBuf<std::int32_t> abd_cnt;
+    DBuf<std::int64_t> abd_off;
+    DBuf<std::uint64_t> tile_keys;
+    DBuf<double> tile_vals;
+    // staging of the host-pointer entry points (contact node stream, DofMap)
+    DBuf<std::uint64_t> io_keys, io_keys2;
+    DBuf<double> io_vals, io_vals2, io_jac;
+    DBuf<std::int32_t> io_body;
 
     // preconditioner
     PrecondKind pkind = kNone;
@@ -123,6 +132,7 @@ struct Ctx {
     std::uint64_t hier_version = ~0ull;
     std::vector<std::unique_ptr<DeviceLevel>> levels;
     DBuf<double> jinv;              // block-Jacobi 3x3 inverses, column-major
+    std::int32_t jinv_n = -1;       // their block count
     DBuf<double> invert_scratch;    // global work arrays for subdomains too large for smem
     DBuf<int> build_status;
     long shifts_applied = 0;
@@ -158,6 +168,7 @@ struct Ctx {
     DBuf<std::uint64_t> perm_keys; // scratch stream for building As
     DBuf<std::uint32_t> as_src;    // As entry -> A entry (bit 31: transposed); valid for as_src_version
     std::uint64_t as_src_version = ~0ull;
+    std::uint64_t as_a_version = ~0ull;  // A.version As was built from
     DBuf<double> perm_vals;
     DBuf<double> pv_in, pv_out;    // rhs / solution in solve order
     const DeviceMatrix& S() const { return perm_active ? As : A; }
@@ -195,19 +206,20 @@ struct Ctx {
 Ctx* unwrap(adipc_gpu_ctx* c);
 
 // assemble.cu
-// row bucketing + per-row sort of 64-bit keys (c.sorted / row_start / uniq_cnt)
+// row bucketing + per-row sort of 64-bit keys (c.sorted / row_start / uniq_cnt);
+// d_vidx: emission index of key q (null: q itself)
 void bucket_sort(Ctx& c, const std::uint64_t* d_keys, std::int64_t T, std::int32_t n, const std::uint32_t* d_vidx);
 // vals_ready: event the reduction waits for (values uploaded on another stream
 // while the keys are sorted), or null
 void assemble(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n_block_rows,
               int deterministic, cudaEvent_t vals_ready = nullptr);
+// filter_pinned + sort + reduce; optionally a second stream segment appended
+// after the first (the two-level contact tiles)
 void assemble_filtered(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
-                       const std::uint8_t* d_pinned, cudaEvent_t vals_ready = nullptr);
-// d_vidx: emission index of key q (a filtered copy of a stream: increasing
-// indices into d_vals; null: q itself); indices >= identity_from are I3
+                       const std::uint8_t* d_pinned, cudaEvent_t vals_ready = nullptr,
+                       const std::uint64_t* d_keys2 = nullptr, const double* d_vals2 = nullptr, std::int64_t T2 = 0);
 void sort_reduce(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
-                 DeviceMatrix& out, const std::uint32_t* d_vidx = nullptr, std::uint32_t identity_from = 0xFFFFFFFFu,
-                 cudaEvent_t vals_ready = nullptr);
+                 DeviceMatrix& out, cudaEvent_t vals_ready = nullptr);
 void sort_stream(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::uint64_t* d_out_keys,
                  double* d_out_vals);
 void blocks_aos_to_soa(Ctx& c, const double* aos, double* soa, std::int64_t U);
@@ -219,6 +231,12 @@ void segment_reduce(Ctx& c, const std::int32_t* d_O, std::int64_t n, const doubl
 std::int64_t filter_pinned(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T,
                            const std::uint8_t* d_pinned, std::int32_t n_slots, std::uint64_t* d_out_keys,
                            double* d_out_vals);
+
+std::int64_t assemble_contact(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T,
+                              const std::uint64_t* d_nkeys, const double* d_nvals, std::int64_t Tn,
+                              std::int32_t n_fem, std::int32_t n_bodies, std::int32_t n_abd, const std::int32_t* d_body,
+                              const double* d_jac36, std::int32_t n, const std::uint8_t* d_pinned,
+                              cudaEvent_t vals_ready = nullptr);
 
 // step.cu (newton.hpp:257-290): the step after the solve
 double step_inf_norm(Ctx& c, const double* d_dir, std::int32_t n_fem, std::int32_t n_bodies, const double* d_max_xbar);
@@ -244,6 +262,8 @@ void build_mas_from_hierarchy(Ctx& c, const host::MasHierarchy& h);
 void precond_apply(Ctx& c, const double* d_r, double* d_z);
 // vectors between the reference numbering and the solve order (Ctx::perm)
 void permute_vec(Ctx& c, const double* src, double* dst, bool to_solve);
+// before a PCG solve: the preconditioner fits A; As follows A's current values
+void check_solve_matrix(Ctx& c);
 
 // pcg.cu
 struct PcgOut {

@@ -650,6 +650,7 @@ void build_solve_matrix(Ctx& c, bool reuse) {
             ADIPC_LAUNCH_CHECK();
         }
         ++c.As.version;
+        c.as_a_version = A.version;
         return;
     }
     c.perm_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(A.U, 1)));
@@ -660,6 +661,7 @@ void build_solve_matrix(Ctx& c, bool reuse) {
         ADIPC_LAUNCH_CHECK();
     }
     sort_reduce(c, c.perm_keys.p, c.perm_vals.p, A.U, A.n, c.As);
+    c.as_a_version = A.version;
     c.as_src_version = ~0ull;
     if (c.As.U != A.U) return;  // cannot happen for a permutation; no map then
     c.as_src.reserve(static_cast<std::size_t>(std::max<std::int64_t>(A.U, 1)));
@@ -669,6 +671,22 @@ void build_solve_matrix(Ctx& c, bool reuse) {
         ADIPC_LAUNCH_CHECK();
     }
     c.as_src_version = c.levels_version;
+}
+
+// The solve-order PCG multiplies by As: if A was reassembled (or uploaded)
+// since As was built, rebuild As from the current A, as the reference's
+// pcg_solve always uses the A it is given (pcg.hpp:34) whatever matrix the
+// preconditioner was built on. A different size cannot be preconditioned.
+static void check_precond_size(const Ctx& c) {
+    if (c.pkind == kNone) throw StatusError(kInvalidArgument, "no preconditioner built");
+    if ((c.pkind == kMas && (c.levels.empty() || c.levels[0]->n_nodes != c.A.n)) ||
+        (c.pkind == kJacobi && c.jinv_n != c.A.n))
+        throw StatusError(kInvalidArgument, "preconditioner built for a matrix of a different size");
+}
+
+void check_solve_matrix(Ctx& c) {
+    check_precond_size(c);
+    if (c.pkind == kMas && c.perm_active && c.as_a_version != c.A.version) build_solve_matrix(c, false);
 }
 
 // K9 restriction + K10 batched factorisation/inversion for the current levels.
@@ -1057,6 +1075,7 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
             ADIPC_LAUNCH_CHECK();
         }
         c.pkind = kJacobi;
+        c.jinv_n = A.n;
         c.perm_active = false;
         return;
     }
@@ -1257,6 +1276,7 @@ void permute_vec(Ctx& c, const double* src, double* dst, bool to_solve) {
 // z = M r (MasPreconditioner::apply / BlockJacobiPreconditioner::apply).
 void precond_apply(Ctx& c, const double* d_r, double* d_z) {
     PcgArgs a{};
+    check_precond_size(c);
     if (c.A.n == 0) return;
     if (c.pkind == kMas && c.perm_active) {  // run in solve order
         const std::size_t n3 = 3 * static_cast<std::size_t>(c.A.n);

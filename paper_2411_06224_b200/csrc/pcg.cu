@@ -335,6 +335,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
 
 // The MAS solve runs in solve order (Ctx::perm): b is permuted in and x out.
 PcgOut pcg(Ctx& c, const double* d_b, double rel_tol, int restart, int max_iters, double* d_x) {
+    check_solve_matrix(c);
     if (!(c.pkind == kMas && c.perm_active)) return pcg_impl(c, d_b, rel_tol, restart, max_iters, d_x);
     const std::size_t n3 = 3 * static_cast<std::size_t>(c.A.n);
     c.pv_in.reserve(n3);

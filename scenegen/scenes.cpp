@@ -330,10 +330,25 @@ void body_mass_matrix(const Body& b, double* M) {  // sum m J^T J
     }
 }
 
+// jitter > 0: every vertex moved by jitter * (cell size) * U(-1, 1) per axis
+// (std::mt19937(seed)) — the cfg5 batch of scenes, seeds 5..12 (SURVEY.md
+// §8d): same connectivity and pins, different element shapes and values.
 Scene* fem_box(int nx, int ny, int nz, double sx, double sy, double sz, double E, double nu, double rho, double dt,
-               int pin_x0) {
+               int pin_x0, double jitter, unsigned seed) {
     auto* s = new Scene();
     FemPart f{make_box_tets(nx, ny, nz, sx, sy, sz), 0, E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu)), rho, {}};
+    std::vector<std::uint8_t> on_x0(f.mesh.verts.size(), 0);
+    for (std::size_t v = 0; v < f.mesh.verts.size(); ++v) on_x0[v] = f.mesh.verts[v].x <= 1e-12 ? 1 : 0;
+    if (jitter > 0) {
+        std::mt19937 rng(seed);
+        std::uniform_real_distribution<double> ud(-1.0, 1.0);
+        const double hx = sx / nx, hy = sy / ny, hz = sz / nz;
+        for (auto& v : f.mesh.verts) {
+            v.x += jitter * hx * ud(rng);
+            v.y += jitter * hy * ud(rng);
+            v.z += jitter * hz * ud(rng);
+        }
+    }
     fem_masses(f);
     s->n_fem = s->n_blocks = static_cast<Index>(f.mesh.verts.size());
     s->keys.reserve(f.mesh.verts.size() + 10 * f.mesh.tets.size());
@@ -343,7 +358,7 @@ Scene* fem_box(int nx, int ny, int nz, double sx, double sy, double sz, double E
     s->pinned.assign(s->n_blocks, 0);
     if (pin_x0)
         for (std::size_t v = 0; v < f.mesh.verts.size(); ++v)
-            if (f.mesh.verts[v].x <= 1e-12) s->pinned[v] = 1;
+            if (on_x0[v]) s->pinned[v] = 1;
     finish_edges(*s);
     return s;
 }
@@ -552,8 +567,8 @@ Scene* hybrid(int n_soft, int soft_res, int n_gears, int gear_res, int stencils_
 extern "C" {
 
 void* adipc_scene_fem_box(int nx, int ny, int nz, double sx, double sy, double sz, double E, double nu, double rho,
-                          double dt, int pin_x0) {
-    return fem_box(nx, ny, nz, sx, sy, sz, E, nu, rho, dt, pin_x0);
+                          double dt, int pin_x0, double jitter, unsigned seed) {
+    return fem_box(nx, ny, nz, sx, sy, sz, E, nu, rho, dt, pin_x0, jitter, seed);
 }
 void* adipc_scene_cloth(int nx, int ny, double sx, double sy, unsigned seed) { return cloth(nx, ny, sx, sy, seed); }
 void* adipc_scene_abd_stack(int bx, int by, int bz, unsigned seed) { return abd_stack(bx, by, bz, seed); }

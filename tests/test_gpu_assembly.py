@@ -9,7 +9,7 @@ import pytest
 
 import oracle_py as O
 import paper_2411_06224_b200 as P
-from paper_2411_06224_b200 import scenes
+import scenegen as scenes
 from paper_2411_06224_b200.context import Context, InvalidArgument
 from helpers import Stream, cm, dense_from, map_accumulate
 from kernel_cases import abd_cases, hash_cases, segment_cases
@@ -113,10 +113,13 @@ def test_edge_cases(ctx):
         ctx.assemble(keys, vals, 3)
 
 
-@pytest.mark.parametrize("row_len", [255, 256, 257, 1000, 8191, 8192, 8193, 40000])
-def test_long_rows(ctx, row_len):
-    """Rows longer than the warp sort (256) and the CTA sort (8192) limits:
-    contact rows of affine bodies collect very many tiles; many duplicates."""
+@pytest.mark.parametrize("row_len", [1, 2, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 1000, 8191, 8192,
+                                     8193, 40000])
+def test_row_lengths(ctx, row_len):
+    """Every row-sort regime: the register bitonic sorts of 32 / 64 / 128 / 256
+    entries per warp and their boundaries, then rows longer than the warp sort
+    (256) and the CTA sort (8192) limits: contact rows of affine bodies
+    collect very many tiles; many duplicates."""
     rng = np.random.default_rng(row_len)
     cols = rng.integers(3, 3 + max(2, row_len // 7), row_len)
     keys = ((np.uint64(3) << np.uint64(32)) | cols.astype(np.uint64)).astype(np.uint64)
@@ -297,3 +300,33 @@ def test_dump_matrix_binary_round_trip(ctx, tmp_path):
     n, rows, cols, blocks = ctx.copy_matrix()
     assert A.n_block_rows == n
     assert_bitwise((A.rows, A.cols, A.blocks), (rows, cols, blocks))
+
+
+@pytest.mark.parametrize("name,pin", [("cfg3_abd_stack", "none"), ("cfg3_abd_stack", "scene"),
+                                      ("cfg4_hybrid", "scene"), ("cfg4_hybrid", "random")])
+def test_assemble_contact_bitwise(ctx, name, pin):
+    """adipc_gpu_assemble_contact: two_level_abd_reduce + stream_.append +
+    filter_pinned + sort + reduce (incremental_potential.hpp:392-394,
+    253-257) with the tiles kept on the device — bit-exact with the oracle's
+    deterministic mode over the concatenated stream, host and device
+    pointers."""
+    import torch
+
+    sc = scenes.CONFIGS[name]()
+    pinned = {"none": np.zeros(sc.n_blocks, np.uint8), "scene": sc.pinned.copy(),
+              "random": (np.random.default_rng(5).random(sc.n_blocks) < 0.05).astype(np.uint8)}[pin]
+    args = (sc.node_keys, sc.node_vals, sc.n_fem, sc.n_bodies, sc.abd_body, sc.jac36)
+    tk, tv = O.two_level_abd_reduce(*args, DET)
+    keys, vals = O.filter_pinned(np.concatenate([sc.keys, tk]), np.concatenate([sc.vals, tv]), pinned)
+    want = oracle_assemble(keys, vals, sc.n_blocks)
+    U, nt = ctx.assemble_contact(sc.keys, sc.vals, sc.node_keys, sc.node_vals, sc.n_fem, sc.n_bodies, sc.abd_body,
+                                 sc.jac36, sc.n_blocks, pinned)
+    assert nt == len(tk) and U == len(want[0])
+    assert_bitwise(ctx.copy_matrix()[1:], want)
+    d = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    dk, dnk = d(sc.keys.view(np.int64)), d(sc.node_keys.view(np.int64))
+    torch.cuda.synchronize()
+    U2, nt2 = ctx.assemble_contact(dk, d(sc.vals), dnk, d(sc.node_vals), sc.n_fem, sc.n_bodies, d(sc.abd_body),
+                                   d(sc.jac36), sc.n_blocks, d(pinned))
+    assert (U2, nt2) == (U, nt)
+    assert_bitwise(ctx.copy_matrix()[1:], want)

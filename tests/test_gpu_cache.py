@@ -7,7 +7,8 @@ import numpy as np
 import pytest
 
 import paper_2411_06224_b200 as P
-from paper_2411_06224_b200 import _lib, scenes
+from paper_2411_06224_b200 import _lib
+import scenegen as scenes
 from paper_2411_06224_b200.context import Context
 
 pytestmark = pytest.mark.gpu

@@ -9,7 +9,7 @@ import pytest
 
 import oracle_py as O
 import paper_2411_06224_b200 as P
-from paper_2411_06224_b200 import scenes
+import scenegen as scenes
 from paper_2411_06224_b200.context import Context, IndefiniteSubdomain
 from helpers import chain_spd_system, cm, dense_from, make_spd_system, restriction_matrix
 from kernel_cases import hash_cases, segment_cases, spmv_cases

@@ -11,7 +11,8 @@ import pytest
 
 import oracle_py as O
 import paper_2411_06224_b200 as P
-from paper_2411_06224_b200 import _lib, scenes
+from paper_2411_06224_b200 import _lib
+import scenegen as scenes
 from helpers import sixteen_slot_graph_edges
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

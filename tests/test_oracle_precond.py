@@ -241,7 +241,7 @@ def test_stiff_beam_cemas_vs_jacobi_ratio():
     cemas16 needs <= 0.6x the block-Jacobi PCG iterations. Also pins the
     hierarchy sizes of SURVEY.md Appendix B (371/62/34/17, 513 L1 nodes)."""
     import paper_2411_06224_b200 as P
-    from paper_2411_06224_b200 import scenes
+    import scenegen as scenes
 
     sc = scenes.CONFIGS["stiff_beam"]()
     det = O.ExecPolicy(deterministic=True)

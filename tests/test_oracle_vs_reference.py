@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import oracle_py as O
-from paper_2411_06224_b200 import scenes
+import scenegen as scenes
 
 DET = O.ExecPolicy(deterministic=True)
 PAR = O.ExecPolicy(deterministic=False, threads=4)

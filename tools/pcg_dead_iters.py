@@ -1,6 +1,7 @@
 import os, sys, torch
 sys.path.insert(0, '/root/repo')
-from paper_2411_06224_b200 import _lib, scenes
+from paper_2411_06224_b200 import _lib
+import scenegen as scenes
 from paper_2411_06224_b200 import api as P
 from paper_2411_06224_b200.context import Context
 sc = scenes.CONFIGS["cfg5_stiff_box"]()

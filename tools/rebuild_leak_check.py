@@ -8,7 +8,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2411_06224_b200 import _lib, scenes  # noqa: E402
+from paper_2411_06224_b200 import _lib  # noqa: E402
+import scenegen as scenes  # noqa: E402
 from paper_2411_06224_b200 import api as P  # noqa: E402
 from paper_2411_06224_b200.context import Context  # noqa: E402
 

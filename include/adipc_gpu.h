@@ -49,6 +49,9 @@ extern "C" {
 #define ADIPC_OPT_SO_KERNELS 6      /* 1 (default): solve-order PCG iteration kernels; 0: the generic level kernels */
 #define ADIPC_OPT_PC_PAIRS 11       /* warp pairs per CTA of the preconditioner kernel (1..5, default 5) */
 #define ADIPC_OPT_L0_STAGES 7       /* 2 (default) or 3: packed inverses in flight per warp pair in the preconditioner */
+#define ADIPC_OPT_DETERMINISTIC 12  /* 1: ExecPolicy::deterministic (core/parallel.hpp:40-43): no fp atomics on the path
+                                       (serial-order SpMV of srbk_spmv.hpp:20-27, fixed-order restrictions), so
+                                       repeated builds and solves are bitwise identical; default 0 */
 
 typedef struct adipc_gpu_ctx adipc_gpu_ctx;
 typedef struct adipc_hierarchy adipc_hierarchy;

@@ -27,6 +27,7 @@ OPT_SOLVE_ORDER = 4
 OPT_SO_KERNELS = 6
 OPT_L0_STAGES = 7
 OPT_PC_PAIRS = 11
+OPT_DETERMINISTIC = 12
 
 # Every symbol include/adipc_gpu.h declares, with its ctypes signature.
 GPU_SIGNATURES = {

@@ -29,7 +29,7 @@ namespace adipc_gpu {
 
 namespace {
 
-constexpr int kWarpSortMax = 256;   // rows up to this length: one warp, register bitonic
+constexpr int kWarpSortMax = 128;   // rows up to this length: one warp, register bitonic
 constexpr int kCtaSortMax = 8192;   // rows up to this length: one CTA, smem bitonic
 constexpr int kCtaSortThreads = 1024;
 
@@ -65,69 +65,86 @@ struct StreamSrc {
 };
 
 // Warp-aggregated atomicAdd on a per-row counter: lanes with the same row
-// share one atomic; returns this lane's slot among them (in lane order).
+// share one atomic (FEM streams emit an element's blocks consecutively, so a
+// warp's 32 entries touch few rows); returns this lane's slot among them.
 __device__ __forceinline__ std::int32_t aggregated_add(std::int32_t* ctr, std::uint32_t row, bool valid) {
     const unsigned grp = __match_any_sync(0xffffffffu, valid ? row : 0xFFFFFFFFu);
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(grp) - 1;
     std::int32_t base = 0;
     if (valid && lane == leader) base = atomicAdd(ctr + row, __popc(grp));
-    base = __shfl_sync(grp, base, leader);
+    base = __shfl_sync(0xffffffffu, base, leader);
     return base + __popc(grp & ((1u << lane) - 1u));
 }
 
-// 1. row histogram of the kept entries (+ one I3 per pinned slot)
-__global__ void k_row_hist(StreamSrc s, std::int32_t n, std::int32_t* __restrict__ row_cnt,
-                           std::int32_t* __restrict__ err) {
+// 1. row histogram of the kept entries (+ one I3 per pinned slot). Each
+//    thread keeps kIlp independent keys in flight (coalesced: key i + k *
+//    blockDim of its CTA's window).
+constexpr int kIlp = 4;
+__global__ void __launch_bounds__(256) k_row_hist(StreamSrc s, std::int32_t n, std::int32_t* __restrict__ row_cnt,
+                                                  std::int32_t* __restrict__ err) {
     const std::int64_t T = s.total();
-    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    for (std::int64_t b = blockIdx.x * static_cast<std::int64_t>(blockDim.x); b < T; b += stride) {
-        const std::int64_t i = b + threadIdx.x;
-        bool valid = i < T;
-        std::uint32_t row = 0;
-        if (valid) {
-            const std::uint64_t k = s.key(i);
-            row = static_cast<std::uint32_t>(k >> 32);
-            if (row >= static_cast<std::uint32_t>(n) ||
-                (s.pinned && static_cast<std::uint32_t>(k) >= static_cast<std::uint32_t>(s.n_pin))) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x * kIlp;
+    for (std::int64_t b = blockIdx.x * static_cast<std::int64_t>(blockDim.x) * kIlp; b < T; b += stride) {
+        std::uint64_t k[kIlp];
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+            const std::int64_t i = b + threadIdx.x + u * blockDim.x;
+            k[u] = i < T ? s.key(i) : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+            const std::uint32_t row = static_cast<std::uint32_t>(k[u] >> 32);
+            bool valid = k[u] != ~0ull;
+            if (valid && (row >= static_cast<std::uint32_t>(n) ||
+                          (s.pinned && static_cast<std::uint32_t>(k[u]) >= static_cast<std::uint32_t>(s.n_pin)))) {
                 atomicOr(err, 1);
                 valid = false;
-            } else {
-                valid = s.kept(k);
             }
+            aggregated_add(row_cnt, row, valid && s.kept(k[u]));
         }
-        aggregated_add(row_cnt, row, valid);
     }
+    const std::int64_t tstride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     if (s.pinned)
-        for (std::int64_t q = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; q < s.n_pin; q += stride)
+        for (std::int64_t q = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; q < s.n_pin; q += tstride)
             if (s.pinned[q]) atomicAdd(row_cnt + q, 1);
 }
 
 // 2. bucket scatter of (col << 32 | emission index) into the row's range
 //    (slot order within a row is arbitrary here; fixed by the row sort)
-__global__ void k_row_scatter(StreamSrc s, std::int32_t n, const std::int64_t* __restrict__ row_start,
-                              std::int32_t* __restrict__ cursor, std::uint64_t* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_row_scatter(StreamSrc s, std::int32_t n,
+                                                     const std::int64_t* __restrict__ row_start,
+                                                     std::int32_t* __restrict__ cursor,
+                                                     std::uint64_t* __restrict__ out) {
     const std::int64_t T = s.total();
-    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    for (std::int64_t b = blockIdx.x * static_cast<std::int64_t>(blockDim.x); b < T; b += stride) {
-        const std::int64_t i = b + threadIdx.x;
-        bool valid = i < T;
-        std::uint64_t k = 0;
-        if (valid) {
-            k = s.key(i);
-            valid = static_cast<std::uint32_t>(k >> 32) < static_cast<std::uint32_t>(n) && s.kept(k);
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x * kIlp;
+    for (std::int64_t b = blockIdx.x * static_cast<std::int64_t>(blockDim.x) * kIlp; b < T; b += stride) {
+        std::uint64_t k[kIlp];
+        std::int64_t pos[kIlp];
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+            const std::int64_t i = b + threadIdx.x + u * blockDim.x;
+            k[u] = i < T ? s.key(i) : ~0ull;
         }
-        const std::uint32_t row = static_cast<std::uint32_t>(k >> 32);
-        const std::int32_t slot = aggregated_add(cursor, row, valid);
-        if (valid)
-            out[row_start[row] + slot] =
-                (k << 32) | (s.vidx ? s.vidx[i] : static_cast<std::uint32_t>(i));
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+            const std::uint32_t row = static_cast<std::uint32_t>(k[u] >> 32);
+            const bool valid = k[u] != ~0ull && row < static_cast<std::uint32_t>(n) && s.kept(k[u]);
+            const std::int32_t slot = aggregated_add(cursor, row, valid);
+            pos[u] = valid ? row_start[row] + slot : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+            const std::int64_t i = b + threadIdx.x + u * blockDim.x;
+            if (pos[u] >= 0) out[pos[u]] = (k[u] << 32) | (s.vidx ? s.vidx[i] : static_cast<std::uint32_t>(i));
+        }
     }
+    const std::int64_t tstride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     if (s.pinned)
-        for (std::int64_t q = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; q < s.n_pin; q += stride)
+        for (std::int64_t q = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; q < s.n_pin; q += tstride)
             if (s.pinned[q]) {
-                const std::int64_t pos = row_start[q] + atomicAdd(cursor + q, 1);
-                out[pos] = (static_cast<std::uint64_t>(q) << 32) | static_cast<std::uint32_t>(T + q);
+                const std::int64_t p = row_start[q] + atomicAdd(cursor + q, 1);
+                out[p] = (static_cast<std::uint64_t>(q) << 32) | static_cast<std::uint32_t>(T + q);
             }
 }
 
@@ -235,10 +252,8 @@ __global__ void k_sort_rows_warp(std::uint64_t* __restrict__ sorted, const std::
             uniq = warp_sort_row<1>(seg, len, lane);
         else if (len <= 64)
             uniq = warp_sort_row<2>(seg, len, lane);
-        else if (len <= 128)
-            uniq = warp_sort_row<4>(seg, len, lane);
         else if (len <= kWarpSortMax)
-            uniq = warp_sort_row<8>(seg, len, lane);
+            uniq = warp_sort_row<4>(seg, len, lane);
         else {
             if (lane == 0) big_rows[atomicAdd(n_big, 1)] = r;
             continue;
@@ -344,7 +359,20 @@ __global__ void k_sort_rows_cta(std::uint64_t* __restrict__ sorted, std::uint64_
 //    the next window. Writes the unique blocks into the tiled block storage
 //    (blk(), common.cuh).
 constexpr int kReduceWarps = 8;
-__global__ void __launch_bounds__(32 * kReduceWarps) k_reduce_rows(
+
+// window gather: load k of lane L fetches double 32 k + L of the window's 288
+__device__ __forceinline__ void gather_window(const StreamSrc& s, std::uint32_t src, int nv, int lane, double (&g)[9]) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        const int word = 32 * k + lane;
+        const int j = word / 9, el = word - 9 * j;
+        const std::uint32_t q = __shfl_sync(0xffffffffu, src, j);
+        const double* sv = j < nv ? s.value(q) : nullptr;
+        g[k] = sv ? __ldg(sv + el) : ((el & 3) == 0 ? 1.0 : 0.0);
+    }
+}
+
+__global__ void __launch_bounds__(32 * kReduceWarps, 3) k_reduce_rows(
     const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
     const std::int64_t* __restrict__ uniq_start, std::int32_t n, StreamSrc s, std::uint32_t* __restrict__ out_rows,
     std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks) {
@@ -364,20 +392,17 @@ __global__ void __launch_bounds__(32 * kReduceWarps) k_reduce_rows(
             const bool valid = p < e;
             const std::uint64_t v = valid ? sorted[p] : ~0ull;
             const std::uint32_t col = static_cast<std::uint32_t>(v >> 32);
-            const std::uint32_t src = static_cast<std::uint32_t>(v);
             const std::uint32_t prev_col = __shfl_up_sync(0xffffffffu, col, 1);
             const bool head = valid && (lane == 0 ? (p == b || static_cast<std::uint32_t>(sorted[p - 1] >> 32) != col)
                                                   : prev_col != col);
             const int nv = static_cast<int>(e - base < 32 ? e - base : 32);
+            double g[9];
+            gather_window(s, static_cast<std::uint32_t>(v), nv, lane, g);
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
                 const int word = 32 * k + lane;
                 const int j = word / 9, el = word - 9 * j;
-                const std::uint32_t q = __shfl_sync(0xffffffffu, src, j);
-                if (j < nv) {
-                    const double* sv = s.value(q);
-                    Tl[el][j] = sv ? sv[el] : ((el & 3) == 0 ? 1.0 : 0.0);
-                }
+                if (j < nv) Tl[el][j] = g[k];
             }
             // does the window's last run continue past it?
             const std::int64_t nxt = base + 32;
@@ -552,12 +577,13 @@ static void bucket_sort(Ctx& c, const StreamSrc& s, std::int32_t n) {
     ADIPC_CUDA(cudaMemsetAsync(c.row_cursor.p, 0, sizeof(std::int32_t) * (n + 1), st));
     ADIPC_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(std::int32_t) * 4, st));
     if (entries > 0) {
-        k_row_hist<<<grid_for(entries, 256, 16), 256, 0, st>>>(s, n, c.row_cnt.p, c.counters.p);
+        k_row_hist<<<grid_for(ceil_div(entries, kIlp), 256, 16), 256, 0, st>>>(s, n, c.row_cnt.p, c.counters.p);
         ADIPC_LAUNCH_CHECK();
     }
     exclusive_scan(c.row_cnt.p, n, c.row_start.p, c.scan_scratch, st);
     if (entries > 0) {
-        k_row_scatter<<<grid_for(entries, 256, 16), 256, 0, st>>>(s, n, c.row_start.p, c.row_cursor.p, c.sorted.p);
+        k_row_scatter<<<grid_for(ceil_div(entries, kIlp), 256, 16), 256, 0, st>>>(s, n, c.row_start.p, c.row_cursor.p,
+                                                                                   c.sorted.p);
         ADIPC_LAUNCH_CHECK();
     }
     if (n > 0) {

@@ -165,6 +165,8 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.io_vals2.free();
     c.io_jac.free();
     c.io_body.free();
+    c.det_tptr.free();
+    c.det_tidx.free();
     c.pin_keep.free();
     c.pin_pos.free();
     c.pin_spos.free();
@@ -237,6 +239,8 @@ int adipc_gpu_set_option(adipc_gpu_ctx* ctx, int option, int value) {
         else if (option == ADIPC_OPT_PC_PAIRS) {
             if (value < 1 || value > 5) throw StatusError(kInvalidArgument, "pairs per CTA not in 1..5");
             ctx->c.pc_pairs = value;
+        } else if (option == ADIPC_OPT_DETERMINISTIC) {
+            ctx->c.deterministic = value != 0;
         } else if (option == ADIPC_OPT_SO_KERNELS) {
             ctx->c.so_kernels = value != 0;
         } else if (option == ADIPC_OPT_L0_STAGES) {

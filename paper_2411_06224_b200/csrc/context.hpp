@@ -53,6 +53,11 @@ struct DeviceLevel {
     DBuf<std::int32_t> upc_node;   // children as this level's node ids (solve order: level 0 = solve slots)
     DBuf<std::int32_t> up_node;    // node -> the next level's node containing it
     DBuf<std::int32_t> anc;        // level >= 2: level-1 node -> this level's node containing it
+    // deterministic build (level >= 1): the solve slots of each subdomain in
+    // ascending order (CSR), valid for det_version == Ctx::levels_version
+    DBuf<std::int64_t> det_ptr;
+    DBuf<std::int32_t> det_slots;
+    std::uint64_t det_version = ~0ull;
     DBuf<double> rr;               // level >= 1: restricted residual per node (3 per node)
     std::vector<std::int32_t> pos_host;
     DBuf<std::int64_t> inv_off;    // subdomain -> offset of its packed inverse (16-byte aligned)
@@ -69,6 +74,8 @@ struct DeviceLevel {
                         &up_node, &anc})
             b->free();
         for (auto* b : {&rr, &inv, &dense, &y}) b->free();
+        det_ptr.free();
+        det_slots.free();
         inv_off.free();
         dense_off.free();
     }
@@ -192,6 +199,18 @@ struct Ctx {
     // solve-order iteration kernels (ADIPC_OPT_SO_KERNELS) when the levels allow them
     bool so_kernels = true;
 
+    // deterministic mode (ADIPC_OPT_DETERMINISTIC; the reference's
+    // ExecPolicy::deterministic, core/parallel.hpp:40-43): no floating-point
+    // atomics anywhere on the path — the row-owner SpMV of the serial
+    // srbk_spmv order (spmv.cu k_spmv_det, through the column index below),
+    // fixed-order coarse restrictions in the MAS build and the PCG update
+    // pass — so repeated solves are bitwise identical
+    bool deterministic = false;
+    DBuf<std::int64_t> det_tptr;   // column index of the solve matrix: tptr[c].. lists entries (r, c), r < c
+    DBuf<std::uint32_t> det_tidx;
+    std::uint64_t det_version = ~0ull;
+    const DeviceMatrix* det_matrix = nullptr;
+
     // per-kernel-class PCG timing (ADIPC_OPT_PROFILE): spmv, level 0, coarse, final
     bool profile = false;
     std::vector<cudaEvent_t> prof_events;
@@ -253,6 +272,8 @@ std::int64_t two_level_abd_reduce(Ctx& c, const std::uint64_t* d_keys, const dou
 // spmv.cu
 void spmv(Ctx& c, const double* d_x, double* d_y);
 int spmv_grid(const Ctx& c, const DeviceMatrix& M);
+// deterministic mode: build the solve matrix's column index ahead of a graph capture
+void prepare_spmv(Ctx& c, const DeviceMatrix& M);
 void spmv_launch(Ctx& c, const DeviceMatrix& M, const double* d_x, double* d_y, bool zero_y, const int* flags,
                  double* partials, unsigned* ticket, double* dot_out);
 

@@ -90,6 +90,82 @@ __global__ void k_restrict(const std::uint32_t* __restrict__ rows, const std::ui
     }
 }
 
+// Deterministic coarse restriction (mas.hpp:56-64 semantics without fp
+// atomics): one warp per level-l subdomain s walks its solve slots in
+// ascending order and each slot's row entries in column order — the matrix's
+// entry order restricted to s — and adds every entry whose both ends fall in
+// s: H to tile (pr, pc), then H^T to (pc, pr), exactly the reference's
+// sequence per dense element. Lanes evaluate 32 entries at a time; the adds
+// are then applied entry by entry, nine lanes per 3x3 tile (lane i + 3 j owns
+// element (i, j) of every tile, so an address is only ever updated by one
+// lane, in program order).
+__global__ void __launch_bounds__(128) k_restrict_det(std::int32_t n_parts, const std::int64_t* __restrict__ mem_ptr,
+                                                      const std::int32_t* __restrict__ mem_slots,
+                                                      const std::int64_t* __restrict__ row_ptr,
+                                                      const std::uint32_t* __restrict__ cols,
+                                                      const double* __restrict__ blocks, RestrictLevel L) {
+    const int lane = threadIdx.x & 31;
+    const std::int32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (s >= n_parts) return;
+    const int dim = 3 * (L.sub_ptr[s + 1] - L.sub_ptr[s]);
+    double* D = L.dense + L.dense_off[s];
+    const int ti = lane % 3, tj = lane / 3;  // lanes 0..8: element (ti, tj) of a tile
+    for (std::int64_t mi = mem_ptr[s]; mi < mem_ptr[s + 1]; ++mi) {
+        const std::int32_t r = mem_slots[mi];
+        const int pr = L.pos_of[L.agg[r]];
+        const std::int64_t e0 = row_ptr[r], e1 = row_ptr[r + 1];
+        for (std::int64_t base = e0; base < e1; base += 32) {
+            const std::int64_t e = base + lane;
+            int pc = -1;
+            bool diag = false;
+            double h[9];
+            if (e < e1) {
+                const std::int32_t c = static_cast<std::int32_t>(cols[e]);
+                const std::int32_t nc = L.agg[c];
+                if (L.part_of[nc] == s) {
+                    pc = L.pos_of[nc];
+                    diag = c == r;
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) h[k] = blocks[blk(e, k)];
+                }
+            }
+            const int nv = static_cast<int>(e1 - base < 32 ? e1 - base : 32);
+            for (int q = 0; q < nv; ++q) {
+                const int qpc = __shfl_sync(0xffffffffu, pc, q);
+                const bool qdiag = __shfl_sync(0xffffffffu, diag ? 1 : 0, q) != 0;
+                double hv[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) hv[k] = __shfl_sync(0xffffffffu, h[k], q);
+                if (qpc < 0 || lane >= 9) continue;
+                // H to (pr, qpc); H^T to (qpc, pr) when r != c — kept where on or below the diagonal
+                for (int t = 0; t < (qdiag ? 1 : 2); ++t) {
+                    const int br = t == 0 ? pr : qpc, bc = t == 0 ? qpc : pr;
+                    if (br < bc) continue;
+                    const int row = 3 * br + ti, col = 3 * bc + tj;
+                    if (row < col) continue;
+                    const double v = t == 0 ? hv[3 * tj + ti] : hv[3 * ti + tj];
+                    double* dst = D + lpk_col(dim, col) + (row - col);
+                    *dst = __dadd_rn(*dst, v);
+                }
+            }
+        }
+    }
+}
+
+// keys (level-l subdomain of slot << 32 | slot) for the member lists
+__global__ void k_member_keys(std::int32_t n, const std::int32_t* __restrict__ agg,
+                              const std::int32_t* __restrict__ part_of, std::uint64_t* __restrict__ keys) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        keys[i] = (static_cast<std::uint64_t>(part_of[agg[i]]) << 32) | static_cast<std::uint32_t>(i);
+}
+
+__global__ void k_high_words(const std::uint64_t* __restrict__ in, std::int64_t n, std::int32_t* __restrict__ out) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<std::int32_t>(in[i] >> 32);
+}
+
 // One CTA per subdomain: Cholesky with retry, then explicit inverse, written
 // symmetric-packed (upper triangle by columns: P[k(k+1)/2 + j] = D^-1(j,k),
 // j <= k) — half the bytes the PCG streams per application.
@@ -700,8 +776,32 @@ void factorize(Ctx& c) {
         ra.lv[l] = RestrictLevel{l > 0 ? L.agg.p : nullptr, L.part_of.p, L.pos_of.p, L.dense_off.p, L.sub_ptr.p,
                                  L.dense.p};
     }
+    // deterministic mode: the atomics-free k_restrict pass covers level 0
+    // only (conflict-free: one entry per dense element); coarse levels in a
+    // fixed order per subdomain (k_restrict_det)
+    const int n_all = ra.n_levels;
+    if (c.deterministic) ra.n_levels = std::min(ra.n_levels, 1);
     if (A.U > 0) {
         k_restrict<<<grid_for(A.U, 256, 16), 256, 0, st>>>(A.rows.p, A.cols.p, A.blocks.p, A.U, ra);
+        ADIPC_LAUNCH_CHECK();
+    }
+    for (int l = 1; c.deterministic && l < n_all && A.U > 0; ++l) {
+        DeviceLevel& L = *c.levels[l];
+        if (L.det_version != c.levels_version) {  // solve slots of each subdomain, ascending
+            c.perm_keys.reserve(static_cast<std::size_t>(A.n));
+            k_member_keys<<<grid_for(A.n, 256, 16), 256, 0, st>>>(A.n, L.agg.p, L.part_of.p, c.perm_keys.p);
+            ADIPC_LAUNCH_CHECK();
+            bucket_sort(c, c.perm_keys.p, A.n, L.n_parts, nullptr);
+            L.det_ptr.reserve(static_cast<std::size_t>(L.n_parts) + 1);
+            L.det_slots.reserve(static_cast<std::size_t>(A.n));
+            ADIPC_CUDA(cudaMemcpyAsync(L.det_ptr.p, c.row_start.p, sizeof(std::int64_t) * (L.n_parts + 1),
+                                       cudaMemcpyDeviceToDevice, st));
+            k_high_words<<<grid_for(A.n, 256, 16), 256, 0, st>>>(c.sorted.p, A.n, L.det_slots.p);
+            ADIPC_LAUNCH_CHECK();
+            L.det_version = c.levels_version;
+        }
+        k_restrict_det<<<static_cast<int>(ceil_div(L.n_parts, 4)), 128, 0, st>>>(
+            L.n_parts, L.det_ptr.p, L.det_slots.p, A.row_ptr.p, A.cols.p, A.blocks.p, ra.lv[l]);
         ADIPC_LAUNCH_CHECK();
     }
     c.build_status.reserve(3);  // failure flag, shifts applied, work counter

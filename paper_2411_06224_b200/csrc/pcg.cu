@@ -105,6 +105,7 @@ static PcgOut pcg_impl(Ctx& c, const double* d_b, double rel_tol, int restart, i
     // solve-order iteration kernels (solve_order.cu)
     const bool so = c.so_kernels && so_supported(c);
     if (so) pmax = std::max(pmax, so_partials(c));
+    prepare_spmv(c, c.S());  // deterministic mode: column index, before any graph capture
     w.partials.reserve(static_cast<std::size_t>(pmax) * T_COUNT);
     w.tickets.reserve(T_COUNT);
     w.scal.reserve(S_COUNT);

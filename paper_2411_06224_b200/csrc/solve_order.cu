@@ -46,6 +46,7 @@ struct SoRestrict {
     const std::int32_t* anc[kMaxLevels];      // level-1 node -> its level-l node, l >= 2
     int max_fill0;                            // largest level-0 subdomain (tile smem sizing)
     int subs;                                 // level-0 subdomains per tile
+    int red_levels;                           // levels >= 2 restricted by RED here (deterministic mode: none)
 };
 
 // One tile of kUpdSubs level-0 subdomains of the update pass (solve order):
@@ -112,13 +113,13 @@ __device__ __forceinline__ void update_tile(const SoRestrict& so, const PcgArgs&
         std::int32_t w[kMaxLevels];
 #pragma unroll
         for (int l = 2; l < kMaxLevels; ++l)
-            if (l < so.n_levels) w[l] = so.anc[l][v];
+            if (l < so.red_levels) w[l] = so.anc[l][v];
         double acc = 0;
         for (int q = uptr[i]; q < uptr[i + 1]; ++q) acc += sr[3 * child[q] + comp];
         so.rr[1][3 * static_cast<std::int64_t>(v) + comp] = acc;
 #pragma unroll
         for (int l = 2; l < kMaxLevels; ++l)
-            if (l < so.n_levels) red_add(so.rr[l] + 3 * static_cast<std::int64_t>(w[l]) + comp, acc);
+            if (l < so.red_levels) red_add(so.rr[l] + 3 * static_cast<std::int64_t>(w[l]) + comp, acc);
     }
     __syncthreads();
 }
@@ -137,6 +138,26 @@ __global__ void __launch_bounds__(kUpdThreads) k_update_so(SoRestrict so, PcgArg
     if (!pcg_alpha(a, alpha)) return;
     pdl_launch();
     update_tile<kMode, kUpdThreads>(so, a, alpha, a.ap, blockIdx.x, sr);
+}
+
+// Deterministic mode: level l >= 2 restricted from level l - 1 in a fixed
+// order, r_l[w] = sum of r_{l-1} over w's children in ascending id
+// (hierarchy.hpp:53-72 nesting), one thread per (node, component).
+__global__ void k_restrict_up(std::int32_t n_nodes, const std::int32_t* __restrict__ upc_ptr,
+                              const std::int32_t* __restrict__ upc_node, const double* __restrict__ r_prev,
+                              double* __restrict__ r_next, const int* __restrict__ flags) {
+    pdl_wait();
+    if (flags[F_DONE]) return;
+    pdl_launch();
+    for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < 3 * std::int64_t(n_nodes);
+         t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int32_t w = static_cast<std::int32_t>(t / 3);
+        const int comp = static_cast<int>(t - 3 * std::int64_t(w));
+        double acc = 0;
+        for (std::int32_t q = upc_ptr[w]; q < upc_ptr[w + 1]; ++q)
+            acc += r_prev[3 * static_cast<std::int64_t>(upc_node[q]) + comp];
+        r_next[t] = acc;
+    }
 }
 
 // ---- level-0 solve: persistent warp pairs, TMA ring of packed inverses -------
@@ -454,6 +475,7 @@ void launch_update_so(Ctx& c, const PcgArgs& a) {
     }
     so.max_fill0 = L0.max_fill;
     so.subs = kUpdSubs;
+    so.red_levels = c.deterministic ? 2 : so.n_levels;
     const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(L0.n_parts, so.subs)));
     const std::size_t smem = update_tile_smem(L0.max_fill, so.subs);
     // a per-device function attribute: set on every launch (cheap, legal while
@@ -462,6 +484,14 @@ void launch_update_so(Ctx& c, const PcgArgs& a) {
                                     static_cast<int>(smem)));
     ADIPC_CUDA(launch_pdl(k_update_so<kMode>, dim3(grid), dim3(kUpdThreads), smem, c.stream, true, so, a));
     ADIPC_LAUNCH_CHECK();
+    if (c.deterministic)
+        for (int l = 2; l < so.n_levels; ++l) {
+            const DeviceLevel& P = *c.levels[l - 1];
+            const DeviceLevel& N = *c.levels[l];
+            ADIPC_CUDA(launch_pdl(k_restrict_up, dim3(grid_for(3 * std::int64_t(N.n_nodes), 256, 8)), dim3(256), 0,
+                                  c.stream, true, N.n_nodes, P.upc_ptr.p, P.upc_node.p, P.rr.p, N.rr.p, a.flags));
+            ADIPC_LAUNCH_CHECK();
+        }
 }
 template void launch_update_so<M_UPDATE>(Ctx&, const PcgArgs&);
 template void launch_update_so<M_RESTART>(Ctx&, const PcgArgs&);

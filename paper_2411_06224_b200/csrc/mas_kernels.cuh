@@ -13,9 +13,10 @@
 // instead of the reference's slot order (rounding-level difference).
 //
 // Subdomain inverses are stored symmetric-packed (packed_idx, common.cuh) and
-// staged into shared memory with one TMA bulk copy per subdomain
-// (cp.async.bulk + mbarrier, L2 evict-first: streamed once per application),
-// issued before the residual gather so the copy overlaps it.
+// staged into shared memory with streaming 16-byte loads issued before the
+// residual gather, so the two overlap. (These generic level kernels serve the
+// stand-alone apply, the PCG start and the reference-numbering path; the
+// solve-order PCG iteration uses k_precond_so, solve_order.cu.)
 #pragma once
 
 #include "context.hpp"
@@ -344,9 +345,9 @@ inline std::size_t level_warp_smem(int max_dim, int regs) {
 }
 
 // One warp per subdomain (dim = 3 f <= 32 kRegs), kLevelWarps per CTA:
-//   lane 0 bulk-copies the packed inverse into this warp's smem slot (kSolve),
-//   the warp gathers b (with the fused PCG vector update for level 0),
-//   waits for the copy, y = D^-1 b from smem (lane j owns rows j, j+32, ...),
+//   the warp stages the packed inverse into its smem slot (kSolve), gathers b
+//   (with the fused PCG vector update for level 0), then y = D^-1 b from
+//   smem (lane j owns rows j, j+32, ...),
 //   stores y, emits the next level's restricted residual, dot partial b.y.
 // kSolve = false: gather (with the fused PCG vector update) + restriction
 // only — the PCG's update pass, after which the level-0 solve and the coarse
@@ -359,7 +360,6 @@ __global__ void __launch_bounds__(32 * kLevelWarps) k_mas_level(LevelArgs L, Pcg
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double* Mw = reinterpret_cast<double*>(smem + static_cast<std::size_t>(w) * warp_smem);
     double* bw = reinterpret_cast<double*>(smem + static_cast<std::size_t>(w + 1) * warp_smem) - 32 * kRegs - 2;
-    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(bw + 32 * kRegs);
     double alpha = 0;
     if (a.flags && a.flags[F_DONE]) return;
     if ((kMode == M_UPDATE || kMode == M_RESTART) && !pcg_alpha(a, alpha)) return;
@@ -368,12 +368,11 @@ __global__ void __launch_bounds__(32 * kLevelWarps) k_mas_level(LevelArgs L, Pcg
     if (s < L.n_parts) {
         const std::int32_t s0 = L.sub_ptr[s];
         const int dim = 3 * (L.sub_ptr[s + 1] - s0);
-        if (kSolve && lane == 0) {  // stage the packed inverse (overlaps the gather)
-            const std::uint32_t bytes = static_cast<std::uint32_t>(packed_doubles(dim) * 8);
-            mbar_init(bar, 1);
-            fence_mbar_init();
-            mbar_arrive_expect_tx(bar, bytes);
-            bulk_g2s_evict_first(Mw, L.inv + L.inv_off[s], bytes, bar);
+        if (kSolve) {  // stage the packed inverse (16-byte loads, in flight during the gather)
+            const double2* src = reinterpret_cast<const double2*>(L.inv + L.inv_off[s]);
+            double2* dst = reinterpret_cast<double2*>(Mw);
+            const int n2 = static_cast<int>(packed_doubles(dim) / 2);
+            for (int i = lane; i < n2; i += 32) dst[i] = __ldcs(src + i);
         }
         double b[kRegs], y[kRegs];
         std::int64_t gi[kRegs];
@@ -392,7 +391,6 @@ __global__ void __launch_bounds__(32 * kLevelWarps) k_mas_level(LevelArgs L, Pcg
         for (int t = 0; t < kRegs; ++t) bw[lane + 32 * t] = b[t];
         __syncwarp();
         if (kSolve) {
-            mbar_wait(bar, 0);
             // y_j = sum_k D^-1(j, k) b_k over the packed upper triangle:
             // k >= j reads column k (contiguous across lanes), k < j reads
             // column j (triangular-number offsets: distinct banks per half-warp)

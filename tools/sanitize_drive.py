@@ -1,0 +1,48 @@
+"""Small end-to-end drive of every kernel family for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck): assembly (plain, filtered,
+two-level contact device path), MAS build (solve order and reference
+numbering), block Jacobi, preconditioner apply, PCG (graphs + PDL) in the
+default and the deterministic mode, SpMV, the post-solve step kernels.
+Scenes: the soft cube (cfg1), the stiff beam, the ABD stack (cfg3).
+Usage: compute-sanitizer --tool <tool> python tools/sanitize_drive.py"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2411_06224_b200 as P  # noqa: E402
+import scenegen as scenes  # noqa: E402
+from paper_2411_06224_b200 import _lib  # noqa: E402
+from paper_2411_06224_b200.context import Context  # noqa: E402
+
+for name in sys.argv[1:] or ["cfg1_soft_cube", "stiff_beam", "cfg3_abd_stack"]:
+    sc = scenes.CONFIGS[name]()
+    l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, 16)
+    for det in (0, 1):
+        for order in (1, 0):
+            c = Context(0)
+            c.set_option(_lib.OPT_DETERMINISTIC, det)
+            c.set_option(_lib.OPT_SOLVE_ORDER, order)
+            c.set_level0_partition(l0.part_of, l0.n_parts, 16, 4)
+            if sc.n_bodies:
+                U, nt = c.assemble_contact(sc.keys, sc.vals, sc.node_keys, sc.node_vals, sc.n_fem, sc.n_bodies,
+                                           sc.abd_body, sc.jac36, sc.n_blocks, sc.pinned)
+                b = c.spmv(np.random.default_rng(5).standard_normal(3 * sc.n_blocks))
+            else:
+                c.assemble_filtered(sc.keys, sc.vals, sc.n_blocks, sc.pinned)
+                b = scenes.gravity_rhs(sc)
+            for kind in (_lib.PRECOND_MAS, _lib.PRECOND_JACOBI):
+                c.build_preconditioner(kind)
+                z = c.precond_apply(b)
+                x, r = c.pcg(b, 1e-4, 50, 100000)
+                print(name, "det", det, "order", order, "kind", kind, r, float(np.linalg.norm(z)), flush=True)
+            d = torch.from_numpy(x).cuda()
+            st = torch.zeros_like(d)
+            torch.cuda.synchronize()
+            c.step_inf_norm(d, sc.n_fem, 0) if sc.n_bodies == 0 else None
+            c.apply_direction(st, d, 0.5, torch.empty_like(d))
+            torch.cuda.synchronize()
+            c.close()
+print("sanitize drive done")

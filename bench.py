@@ -432,12 +432,12 @@ def run_ours(args, rank, world, local_rank, dist):
                                        "frac": bm["total"] / iter_s / 1e9 / hbm, "iter_us": iter_s * 1e6,
                                        "iter_us_class_sum": iter_s_classes * 1e6},
             # context for the fractions above: the read bandwidth ONE kernel of
-            # this size reaches on this B200 with a cold L2 and no compute
-            # (tools/stream_read_bench.cu; profiles/r01f_summary.md): 50 MB
-            # 3.2 TB/s, 200 MB 4.65, 2 GB 6.65 — the copy peak needs GB-size
-            # transfers that the iteration's 36-223 MB kernels do not make
-            "roofline_practical": {"unit": "GB/s", "single_kernel_read_200MB": 4650.0,
-                                   "dominant_kernel_frac": kernels[dom]["achieved_gbs"] / 4650.0,
+            # this size reaches on this B200 with a cold, CLEAN L2 and no
+            # compute (tools/stream_read_bench.cu, r02: 50 MB 3.7 TB/s, 200 MB
+            # 6.0; the r01 figures 3.2 / 4.65 had the flush's dirty lines
+            # written back inside the timed kernel)
+            "roofline_practical": {"unit": "GB/s", "single_kernel_read_200MB": 6030.0,
+                                   "dominant_kernel_frac": kernels[dom]["achieved_gbs"] / 6030.0,
                                    "source": "tools/stream_read_bench.cu"},
             "clocks": clk.summary(),
         }

@@ -35,7 +35,7 @@ for spec in sys.argv[1:] or ["so=1"]:
         ctx.set_option(_lib.OPT_PROFILE, prof)
         best = None
         for _ in range(1 if prof else 3):  # graph mode: best of 3 solves
-            _, res = ctx.pcg(b, 1e-4, 250, 100000, x=x)
+            _, res = ctx.pcg(b, 1e-4, 250, int(os.environ.get("MAXIT", "100000")), x=x)
             t = ctx.timings()
             if best is None or t["pcg_ms"] < best[1]["pcg_ms"]:
                 best = (res, t)

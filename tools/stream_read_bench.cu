@@ -4,9 +4,11 @@
 // cp.async.bulk rings through shared memory (per-warp rings of D stages of S
 // bytes), no compute. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3
 // -std=c++17 -o stream_read_bench tools/stream_read_bench.cu
-// Results (r01f, profiles/r01f_summary.md): 50 MB 3.2 TB/s, 100 MB 3.9,
-// 200 MB 4.65, 400 MB 5.1, 2 GB 6.65 — the practical floor of the PCG
-// iteration's 36-223 MB kernels is well below the 6.55 TB/s copy peak.
+// argv[2] = 1 (default): after the memset, a 512 MB read of another buffer
+// evicts the memset's dirty lines, so the timed kernel reads from a cold AND
+// clean L2. r02: 50 MB 3.7 TB/s, 200 MB 6.0 (LDG.128). The r01f figures
+// (50 MB 3.2, 200 MB 4.65; argv[2] = 0) had up to 126 MB of dirty L2 lines
+// written back inside the timed kernel.
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
@@ -45,10 +47,12 @@ __global__ void k_ldg(const double2* src, long n2, double* out) {
 int main(int argc, char** argv) {
   long total = (argc > 1 ? atol(argv[1]) : 200l) << 20; char* src; double* out; cudaMalloc(&src, total); cudaMalloc(&out, 8); cudaMemset(src, 0, total);
   char* flush; cudaMalloc(&flush, 512l << 20);
+  char* flush2; cudaMalloc(&flush2, 512l << 20); cudaMemset(flush2, 1, 512l << 20);
+  const int clean = argc > 2 ? atoi(argv[2]) : 1;  // 1: evict the memset's dirty lines with a 512 MB read before timing
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   auto run = [&](auto launch, const char* name) {
     float best = 1e9;
-    for (int it = 0; it < 5; ++it) { cudaMemset(flush, it, 512l << 20); cudaEventRecord(a); launch(); cudaEventRecord(b); cudaEventSynchronize(b); float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms; }
+    for (int it = 0; it < 5; ++it) { cudaMemset(flush, it, 512l << 20); if (clean) k_ldg<<<148 * 8, 256>>>((const double2*)flush2, (512l << 20) / 16, out); cudaEventRecord(a); launch(); cudaEventRecord(b); cudaEventSynchronize(b); float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms; }
     printf("%-40s %7.1f us  %6.2f TB/s  (%s)\n", name, best * 1000, total / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   };
   run([&] { k_ldg<<<148 * 8, 256>>>((const double2*)src, total / 16, out); }, "LDG.128 grid-stride");

@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-solve-order", action="store_true",
                     help="run the MAS/PCG in the reference slot numbering (A/B of the solve-order renumbering)")
     ap.add_argument("--cpu-iters", type=int, default=10, help="PCG iterations per CPU sample step")
+    ap.add_argument("--no-hybrid", action="store_true",
+                    help="skip the cfg4_hybrid_1m Newton-solve line (the north star's ~1M-DOF hybrid scene)")
     ap.add_argument("--selftest", action="store_true",
                     help="launcher / rendezvous / stats-gather self-test without GPU work (CPU tests, gloo)")
     return ap.parse_args()
@@ -260,6 +262,185 @@ def cpu_reference(sc, rank_seed, cpu_iters, steps, warmup, sample_note=True, ful
                       f"a one-time assembly ({t_asm:.2f} s) and MAS build ({t_build:.2f} s); the reference's "
                       f"serial stages (radix sort, O scan, restriction, LLT, hierarchy, PCG vector ops) stay serial",
             "assembly_s": t_asm, "mas_build_s": t_build, "full_solve": full}
+
+
+# ------------------------------------------------------------ hybrid scene ---
+HYBRID = "cfg4_hybrid_1m"
+
+
+def hybrid_cpu(sc, cpu_iters, full_solve):
+    """The reference's CPU path on the hybrid scene: two_level_abd_reduce of
+    the contact node stream appended to the DOF stream
+    (incremental_potential.hpp:322-394), filter_pinned, sort + reduce, the
+    hierarchy + MAS build, then PCG (a bounded sample of `cpu_iters`
+    iterations; full_solve: also the whole solve to rel_tol)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O
+    import scenegen as S
+
+    kind = "reference" if O.reference_available() else "port"
+    with O.use_backend("reference" if kind == "reference" else "restated"):
+        cores = O.lib().oracle_max_threads()
+        par = O.ExecPolicy(deterministic=False, threads=cores)
+        t0 = time.perf_counter()
+        tk, tv = O.two_level_abd_reduce(sc.node_keys, sc.node_vals, sc.n_fem, sc.n_bodies, sc.abd_body, sc.jac36, par)
+        t_two = time.perf_counter() - t0
+        keys = np.concatenate([sc.keys, tk])
+        vals = np.concatenate([sc.vals, tv])
+        del tk, tv
+        fk, fv = O.filter_pinned(keys, vals, sc.pinned)  # restated (private in the reference): untimed
+        del keys, vals
+        t0 = time.perf_counter()
+        sk, sv = O.sort_stream(fk, fv, par)
+        rows, cols, blocks = O.fast_hash_reduction(sk, sv, sc.n_blocks, par)
+        t_asm = time.perf_counter() - t0 + t_two
+        del sk, sv, fk, fv
+        part_of, n_parts = O.partition_block_graph(sc.n_blocks, sc.rest_edges, CAPACITY)
+        t0 = time.perf_counter()
+        A = O.Matrix(sc.n_blocks, rows, cols, blocks)
+        H = O.Hierarchy(part_of, n_parts, CAPACITY, O.block_edges(rows, cols), MAX_LEVELS)
+        M = O.MasPreconditioner(A, H)
+        t_build = time.perf_counter() - t0
+        b = O.srbk_spmv(sc.n_blocks, rows, cols, blocks, S.ballistic_direction(sc), O.ExecPolicy(deterministic=True))
+        t0 = time.perf_counter()
+        _, r = O.pcg_solve(A, b, M, 1e-30, RESTART, cpu_iters, par)
+        it_s = cpu_iters / (time.perf_counter() - t0)
+        full = None
+        if full_solve:
+            t0 = time.perf_counter()
+            _, rf = O.pcg_solve(A, b, M, REL_TOL, RESTART, MAX_ITERS, par)
+            t_pcg = time.perf_counter() - t0
+            full = {"iters": int(rf["iters"]), "pcg_s": t_pcg, "converged": bool(rf["converged"]),
+                    "newton_solve_s": t_asm + t_build + t_pcg}
+    return {"value": it_s, "unit": "PCG iterations/s", "cores": cores, "kind": kind,
+            "sample": f"{'oracle/_ref (the reference headers)' if kind == 'reference' else 'oracle restatement'}; "
+                      f"two-level reduction + sort/reduce ({t_asm:.2f} s), MAS build ({t_build:.2f} s), "
+                      f"{cpu_iters} PCG iterations" + (", then the whole PCG solve" if full else ""),
+            "assembly_s": t_asm, "two_level_s": t_two, "mas_build_s": t_build, "full_solve": full}
+
+
+def hybrid_gpu(args, local_rank, with_cpu):
+    """cfg4_hybrid_1m on this GPU: a step = one Newton linear solve of the
+    hybrid scene through the C ABI with the DOF stream and the contact node
+    stream resident in HBM: two_level_abd_reduce + append + filter + sort +
+    reduce (adipc_gpu_assemble_contact_device), a COLD MAS build (no hierarchy
+    reuse: contacts change the pattern every Newton iteration, and the
+    reference rebuilds the hierarchy every iteration, newton.hpp:243-255),
+    PCG to rel_tol on b = A x*, x* the free-fall step."""
+    import torch
+
+    from paper_2411_06224_b200 import _lib
+    from paper_2411_06224_b200 import api as P
+    from paper_2411_06224_b200.context import Context
+    import scenegen as S
+
+    dev = torch.device("cuda", local_rank)
+    sc = make_problem(HYBRID, 4)
+    stream = torch.cuda.Stream(dev)
+    ctx = Context(local_rank, stream=stream)
+    ctx.set_option(_lib.OPT_PROFILE, 0)
+    ctx.set_option(_lib.OPT_CACHE_HIERARCHY, 0)
+    l0 = P.partition_block_graph(sc.n_blocks, sc.rest_edges, CAPACITY)
+    ctx.set_level0_partition(l0.part_of, l0.n_parts, CAPACITY, MAX_LEVELS)
+    with torch.cuda.stream(stream):
+        d = {k: torch.from_numpy(v).to(dev) for k, v in dict(
+            keys=sc.keys.view(np.int64), vals=sc.vals, nk=sc.node_keys.view(np.int64), nv=sc.node_vals,
+            body=sc.abd_body, jac=sc.jac36, pin=sc.pinned).items()}
+    stream.synchronize()
+
+    def assemble():
+        return ctx.assemble_contact(d["keys"], d["vals"], d["nk"], d["nv"], sc.n_fem, sc.n_bodies, d["body"],
+                                    d["jac"], sc.n_blocks, d["pin"])
+
+    U, n_tiles = assemble()
+    n, _ = ctx.matrix_info()
+    xs = torch.from_numpy(S.ballistic_direction(sc)).to(dev)
+    d_b = torch.empty_like(xs)
+    d_x = torch.empty_like(xs)
+    with torch.cuda.stream(stream):
+        ctx.spmv(xs, d_b)
+    stream.synchronize()
+
+    def step():
+        assemble()
+        ctx.build_preconditioner(_lib.PRECOND_MAS)
+        _, res = ctx.pcg(d_b, REL_TOL, RESTART, MAX_ITERS, x=d_x)
+        return res, ctx.timings()
+
+    for _ in range(args.warmup):
+        step()
+    levels = ctx.precond_levels()
+    bm = byte_model(n, U, levels)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    recs = []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        recs.append(step())
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    total_ms = ev0.elapsed_time(ev1)
+    iters = sum(r.iters for r, _ in recs)
+    t = {k: sum(tt[k] for _, tt in recs) / args.steps for k in recs[0][1]}
+    err = float(torch.linalg.norm(d_x - xs) / torch.linalg.norm(xs))
+    pcg_iter_s = t["pcg_ms"] / 1e3 / max(iters / args.steps, 1)
+    # e2e: the same solve through the host-pointer C ABI (pinned buffers):
+    # both streams cross PCIe every Newton iteration, x comes back
+    import ctypes as C
+
+    L = _lib.gpu()
+    h = {k: v.cpu().pin_memory() for k, v in d.items()}
+    h_b, h_x = d_b.cpu().pin_memory(), torch.empty(3 * n, dtype=torch.float64).pin_memory()
+    Uo, nto, it, rr, cv = C.c_int64(), C.c_int64(), C.c_int(), C.c_double(), C.c_int()
+
+    def e2e_step():
+        ctx._check(L.adipc_gpu_assemble_contact(
+            ctx.h, h["keys"].data_ptr(), h["vals"].data_ptr(), len(sc.keys), h["nk"].data_ptr(), h["nv"].data_ptr(),
+            len(sc.node_keys), sc.n_fem, sc.n_bodies, len(sc.abd_body), h["body"].data_ptr(), h["jac"].data_ptr(),
+            sc.n_blocks, h["pin"].data_ptr(), C.byref(Uo), C.byref(nto)))
+        ctx._check(L.adipc_gpu_build_preconditioner(ctx.h, _lib.PRECOND_MAS))
+        ctx._check(L.adipc_gpu_pcg(ctx.h, h_b.data_ptr(), REL_TOL, RESTART, MAX_ITERS, h_x.data_ptr(), C.byref(it),
+                                   C.byref(rr), C.byref(cv)))
+        return it.value
+
+    e2e_step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e_iters = sum(e2e_step() for _ in range(args.steps))
+    e2e_ms = (time.perf_counter() - t0) * 1000.0 / args.steps
+    h2d = sum(v.numel() * v.element_size() for v in h.values()) + h_b.numel() * 8
+    out = {"config": HYBRID,
+           "workload": "hybrid affine-deformable coupling at ~1M DOF: 8 FEM blocks 34^3 cells (E=1e8) + 40 ABD gears "
+                       "(kappa 1e8), 105K contact stencils -> two_level_abd_reduce; cold MAS build every Newton "
+                       "iteration; b = A x*, x* the free-fall step",
+           "n_block_rows": int(sc.n_blocks), "dof": 3 * int(sc.n_blocks), "triplets": int(len(sc.keys)),
+           "contact_node_blocks": int(len(sc.node_keys)), "contact_tiles": int(n_tiles), "U": int(U),
+           "levels": [(int(L_["n_nodes"]), int(L_["n_parts"])) for L_ in levels],
+           "ms_per_newton_solve": total_ms / args.steps,
+           "assembly_ms": t["assemble_ms"], "mas_build_cold_ms": t["build_ms"],
+           "mas_build_cold_host_ms": t["build_host_ms"], "pcg_ms": t["pcg_ms"],
+           "pcg_iters_per_solve": iters / args.steps, "pcg_iters_per_s": iters / (t["pcg_ms"] * args.steps / 1e3),
+           "converged": all(r.converged for r, _ in recs), "x_err_vs_xstar": err,
+           "roofline_pcg_iteration": {"bound": "hbm", "bytes_per_iter": bm["total"],
+                                      "achieved": bm["total"] / pcg_iter_s / 1e9, "peak": peaks()[0], "unit": "GB/s",
+                                      "frac": bm["total"] / pcg_iter_s / 1e9 / peaks()[0],
+                                      "iter_us": pcg_iter_s * 1e6},
+           "e2e": {"ms_per_newton_solve": e2e_ms, "pcg_iters_per_solve": e_iters / args.steps,
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(3 * n * 8),
+                   "path": "adipc_gpu_assemble_contact + adipc_gpu_build_preconditioner + adipc_gpu_pcg "
+                           "(host pointers, pinned)"}}
+    ctx.close()
+    if with_cpu:
+        cb = hybrid_cpu(sc, args.cpu_iters, full_solve=False)
+        # per Newton solve on the CPU: its own assembly + MAS build + the GPU's
+        # iteration count at the sampled CPU iteration rate
+        cpu_solve_s = cb["assembly_s"] + cb["mas_build_s"] + out["pcg_iters_per_solve"] / cb["value"]
+        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "assembly_s",
+                                                  "two_level_s", "mas_build_s")}
+        out["cpu_baseline"]["ms_per_newton_solve_est"] = cpu_solve_s * 1e3
+        out["speedup_newton_solve_vs_cpu"] = cpu_solve_s * 1e3 / out["ms_per_newton_solve"]
+        out["speedup_e2e_newton_solve_vs_cpu"] = cpu_solve_s * 1e3 / e2e_ms
+    return out
 
 
 # -------------------------------------------------------------- main arm ---
@@ -580,6 +761,14 @@ def main():
                         "d2h_bytes_per_step": 0,
                         "scope": "one whole Newton linear solve (assembly + MAS build + PCG to rel_tol), timed"
                                  if full else "PCG-loop sample only"}}
+        if not args.no_hybrid and args.config == "cfg5_stiff_box":
+            hy = hybrid_cpu(make_problem(HYBRID, 4), args.cpu_iters, full_solve=not args.no_full_solve)
+            hf = hy["full_solve"]
+            line["hybrid"] = {"config": HYBRID, "pcg_iters_per_s": hy["value"],
+                              "cpu_baseline": {k: hy[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                              "assembly_s": hy["assembly_s"], "two_level_s": hy["two_level_s"],
+                              "mas_build_s": hy["mas_build_s"], "full_solve": hf,
+                              "ms_per_newton_solve": 1000.0 * hf["newton_solve_s"] if hf else None}
         print(json.dumps(line), flush=True)
         return
     dist = None
@@ -591,6 +780,10 @@ def main():
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         dist = tdist
     out, sc = run_ours(args, rank, world, local_rank, dist)
+    if not args.no_hybrid and args.config == "cfg5_stiff_box":
+        hy = hybrid_gpu(args, local_rank, with_cpu=(rank == 0 and world == 1 and not args.no_cpu_baseline))
+        if rank == 0:
+            out["hybrid"] = hy
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(sc, 5, args.cpu_iters, 2, 1)

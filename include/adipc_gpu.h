@@ -160,6 +160,41 @@ int adipc_gpu_assemble_contact_device(adipc_gpu_ctx* ctx, const uint64_t* d_keys
                                       const double* d_abd_node_jacobian36, int32_t n_block_rows,
                                       const uint8_t* d_pinned, int64_t* n_unique, int64_t* n_tiles);
 
+
+/* ---- element-Hessian producer --------------------------------
+ * The inertia + solid-mesh part of IncrementalPotential::assemble
+ * (adipc/solver/incremental_potential.hpp:170-180, 222-239; scatter12 :310-318;
+ * pinned gradient :253-254) on the device: stable Neo-Hookean stencils
+ * (energy/neo_hookean.hpp:64-104) projected to PSD (energy/psd.hpp:8-14),
+ * the triplet stream in the reference's emission order (n_verts inertia
+ * diagonals, then 10 blocks per tet), the gradient and the value.
+ * Arrays are DEVICE pointers except tet_begin / mu / lambda (host, per solid
+ * mesh; tet_begin has n_meshes + 1 entries, tets are global slot ids).
+ * Deformable-solid scenes: the FEM vertices are block slots [0, n_verts). */
+typedef struct adipc_fem_desc {
+    int32_t n_verts;
+    const double* x;            /* 3 n_verts: SystemState::x */
+    const double* x_tilde;      /* 3 n_verts: the inertial target */
+    const double* mass;         /* n_verts: vertex_mass */
+    int32_t n_meshes;
+    const int64_t* tet_begin;   /* host */
+    const double* mu;           /* host, per mesh: solid.mu() */
+    const double* lambda;       /* host, per mesh: solid.lambda() */
+    const int32_t* tets;        /* 4 per tet */
+    const double* rest_inv9;    /* TetRest::inv_rest_edges, 9 column-major per tet */
+    const double* rest_volume;  /* TetRest::volume per tet */
+    double dt2;
+    int project;                /* 1: project_psd every stencil (the reference's default) */
+    const uint8_t* pinned;      /* n_verts or NULL: zero gradient on pinned slots */
+} adipc_fem_desc;
+/* the raw stream (n_verts + 10 n_tets entries) + gradient (3 n_verts) + value */
+int adipc_gpu_fem_emit_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* desc, uint64_t* d_keys, double* d_vals9,
+                              double* d_grad, double* value);
+/* emit + filter_pinned + sort + reduce into the context matrix (the whole
+ * assemble() for these scenes; the stream never leaves HBM) */
+int adipc_gpu_fem_assemble_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* desc, double* d_grad, double* value,
+                                  int64_t* n_unique);
+
 /* IncrementalPotential::filter_pinned (incremental_potential.hpp:410-425):
  * drop blocks touching a pinned slot, append I3 per pinned slot.
  * out capacity >= T + n_slots. */

@@ -33,6 +33,8 @@
 
 #ifdef _OPENMP
 #include <omp.h>
+
+#include "sym_eig.hpp"
 #endif
 
 namespace oracle {
@@ -936,6 +938,206 @@ inline PcgResult pcg_solve(const SortedSymBlockCoo& A, const std::vector<Real>& 
     }
     out.rel_residual = std::sqrt(std::abs(rho) / rho0);
     return out;
+}
+
+
+// ---------------------------------------------------------------------------
+// Element-Hessian producer: the stable Neo-Hookean stencil
+// (energy/neo_hookean.hpp:13-104), its PSD projection (energy/psd.hpp:8-14;
+// Eigen's SelfAdjointEigenSolver restated in sym_eig.hpp) and the
+// deformable-solid part of IncrementalPotential::assemble
+// (solver/incremental_potential.hpp:170-180 inertia, :222-239 tets,
+// scatter12 :310-318, pinned gradient :253-254). 12-vectors and 12x12
+// matrices are plain column-major arrays.
+
+// Eigen 3.4 determinant of a fixed 3x3 (Determinant.h bruteforce_det3_helper)
+inline Real det3(const Mat3& m) {
+    return m(0, 0) * (m(1, 1) * m(2, 2) - m(1, 2) * m(2, 1)) - m(0, 1) * (m(1, 0) * m(2, 2) - m(1, 2) * m(2, 0)) +
+           m(0, 2) * (m(1, 0) * m(2, 1) - m(1, 1) * m(2, 0));
+}
+
+inline Vec3 cross(const Vec3& a, const Vec3& b) {  // Eigen cross order
+    Vec3 c;
+    c[0] = a[1] * b[2] - a[2] * b[1];
+    c[1] = a[2] * b[0] - a[0] * b[2];
+    c[2] = a[0] * b[1] - a[1] * b[0];
+    return c;
+}
+
+// neo_hookean.hpp:8-27
+struct TetRest {
+    Mat3 inv_rest_edges;
+    Real volume = 0;
+};
+inline TetRest tet_rest(const Vec3& p0, const Vec3& p1, const Vec3& p2, const Vec3& p3) {
+    Mat3 Dm;
+    for (int k = 0; k < 3; ++k) {
+        Dm(k, 0) = p1[k] - p0[k];
+        Dm(k, 1) = p2[k] - p0[k];
+        Dm(k, 2) = p3[k] - p0[k];
+    }
+    const Real vol = det3(Dm) / 6.0;
+    if (!(vol > 0)) throw std::invalid_argument("inverted or degenerate rest tet");
+    return TetRest{Dm.inverse(), vol};
+}
+
+// neo_hookean.hpp:44-54: vec(F) vs (x0..x3), 9 x 12 column-major
+inline void tet_dFdx(const Mat3& B, Real* J) {
+    for (int k = 0; k < 108; ++k) J[k] = 0;
+    for (int j = 0; j < 3; ++j)
+        for (int c = 0; c < 3; ++c)
+            for (int k = 0; k < 3; ++k) {
+                J[9 * (3 * (c + 1) + k) + 3 * j + k] += B(c, j);
+                J[9 * k + 3 * j + k] -= B(c, j);
+            }
+}
+
+struct Stencil12 {  // neo_hookean.hpp:56-60
+    Real value = 0;
+    Real grad[12] = {};
+    Real hess[144] = {};
+};
+
+// neo_hookean.hpp:64-104 (polynomial stable variant)
+inline Stencil12 stable_neo_hookean(const Vec3& x0, const Vec3& x1, const Vec3& x2, const Vec3& x3,
+                                    const TetRest& rest, Real mu, Real lam, bool project = true) {
+    Mat3 Ds, F;
+    for (int k = 0; k < 3; ++k) {
+        Ds(k, 0) = x1[k] - x0[k];
+        Ds(k, 1) = x2[k] - x0[k];
+        Ds(k, 2) = x3[k] - x0[k];
+    }
+    const Mat3& B = rest.inv_rest_edges;
+    for (int j = 0; j < 3; ++j)
+        for (int i = 0; i < 3; ++i) F(i, j) = Ds(i, 0) * B(0, j) + Ds(i, 1) * B(1, j) + Ds(i, 2) * B(2, j);
+    const Real J = det3(F);
+    Real IC = 0;
+    for (int k = 0; k < 9; ++k) IC += F.m[k] * F.m[k];
+    Vec3 f[3];
+    for (int c = 0; c < 3; ++c)
+        for (int k = 0; k < 3; ++k) f[c][k] = F(k, c);
+    const Vec3 cof_c[3] = {cross(f[1], f[2]), cross(f[2], f[0]), cross(f[0], f[1])};
+    Real cof[9];
+    for (int c = 0; c < 3; ++c)
+        for (int k = 0; k < 3; ++k) cof[3 * c + k] = cof_c[c][k];
+    const Real V = rest.volume;
+    Stencil12 out;
+    out.value = V * (0.5 * mu * (IC - 3) - mu * (J - 1) + 0.5 * lam * (J - 1) * (J - 1));
+    const Real dJcoef = lam * (J - 1) - mu;
+    Real P[9];
+    for (int k = 0; k < 9; ++k) P[k] = mu * F.m[k] + dJcoef * cof[k];
+    Real D[108];
+    tet_dFdx(B, D);
+    for (int i = 0; i < 12; ++i) {
+        Real s = 0;
+        for (int k = 0; k < 9; ++k) s += (V * D[9 * i + k]) * P[k];
+        out.grad[i] = s;
+    }
+    // H9 = mu I + lam cof cof^T + dJcoef HJ (neo_hookean.hpp:90-99)
+    Real H9[81];
+    for (int j = 0; j < 9; ++j)
+        for (int i = 0; i < 9; ++i) H9[9 * j + i] = (i == j ? mu : 0.0) + lam * cof[i] * cof[j];
+    auto cross_mat = [](const Vec3& a, Real* M3) {  // neo_hookean.hpp:37-42, column-major
+        M3[0] = 0, M3[3] = -a[2], M3[6] = a[1];
+        M3[1] = a[2], M3[4] = 0, M3[7] = -a[0];
+        M3[2] = -a[1], M3[5] = a[0], M3[8] = 0;
+    };
+    Real HJ[81] = {};
+    auto put = [&](int bi, int bj, const Vec3& a, Real sgn) {
+        Real M3[9];
+        cross_mat(a, M3);
+        for (int c = 0; c < 3; ++c)
+            for (int r = 0; r < 3; ++r) HJ[9 * (3 * bj + c) + 3 * bi + r] = sgn * M3[3 * c + r];
+    };
+    put(0, 1, f[2], -1);
+    put(0, 2, f[1], 1);
+    put(1, 0, f[2], 1);
+    put(1, 2, f[0], -1);
+    put(2, 0, f[1], -1);
+    put(2, 1, f[0], 1);
+    for (int k = 0; k < 81; ++k) H9[k] += dJcoef * HJ[k];
+    // hess = (V D^T) H9 D
+    Real T[108];  // (V D^T) H9: 12 x 9
+    for (int j = 0; j < 9; ++j)
+        for (int i = 0; i < 12; ++i) {
+            Real s = 0;
+            for (int k = 0; k < 9; ++k) s += (V * D[9 * i + k]) * H9[9 * j + k];
+            T[12 * j + i] = s;
+        }
+    for (int j = 0; j < 12; ++j)
+        for (int i = 0; i < 12; ++i) {
+            Real s = 0;
+            for (int k = 0; k < 9; ++k) s += T[12 * k + i] * D[9 * j + k];
+            out.hess[12 * j + i] = s;
+        }
+    if (project) {
+        Real Pj[144];
+        oracle_eig::project_psd(12, out.hess, Pj);
+        for (int k = 0; k < 144; ++k) out.hess[k] = Pj[k];
+    }
+    return out;
+}
+
+// One deformable solid part of the scene for the producer: tets as global
+// slot ids (mesh offset applied), rest data and material per mesh.
+struct FemSolids {
+    std::vector<std::int32_t> tets;      // 4 per tet
+    std::vector<TetRest> rest;           // per tet
+    std::vector<std::int64_t> tet_begin; // per mesh, n_meshes + 1
+    std::vector<Real> mu, lam;           // per mesh
+};
+
+// IncrementalPotential::assemble for inertia + solid meshes, up to (not
+// including) filter_pinned / sort / reduce: returns the value, fills grad
+// (3 n, zeroed on pinned slots, :253-254) and the triplet stream in emission
+// order (inertia diagonals of every vertex, then 10 blocks per tet, a <= b).
+inline Real ip_fem_assemble(const std::vector<Vec3>& x, const std::vector<Vec3>& x_tilde, const std::vector<Real>& mass,
+                            const FemSolids& fs, Real dt2, const std::vector<char>& pinned, std::vector<Real>& grad,
+                            BlockTripletStream& stream, bool project = true) {
+    const std::size_t n = x.size();
+    grad.assign(3 * n, 0.0);
+    stream.keys.clear();
+    stream.values.clear();
+    Real val = 0;
+    for (std::size_t v = 0; v < n; ++v) {  // :170-180
+        Vec3 dx;
+        for (int k = 0; k < 3; ++k) dx[k] = x[v][k] - x_tilde[v][k];
+        val += 0.5 * mass[v] * (dx[0] * dx[0] + dx[1] * dx[1] + dx[2] * dx[2]);
+        for (int k = 0; k < 3; ++k) grad[3 * v + k] += mass[v] * dx[k];
+        Mat3 m;
+        m(0, 0) = m(1, 1) = m(2, 2) = mass[v];
+        stream.emit(static_cast<Index>(v), static_cast<Index>(v), m);
+    }
+    const std::size_t nt = fs.rest.size();
+    std::vector<Stencil12> st(nt);
+    std::vector<Real> tet_mu(nt), tet_lam(nt);
+    for (std::size_t m = 0; m + 1 < fs.tet_begin.size(); ++m)
+        for (std::int64_t t = fs.tet_begin[m]; t < fs.tet_begin[m + 1]; ++t) {
+            tet_mu[t] = fs.mu[m];
+            tet_lam[t] = fs.lam[m];
+        }
+#pragma omp parallel for schedule(static)
+    for (std::int64_t t = 0; t < static_cast<std::int64_t>(nt); ++t) {  // :223-232 (parallel_for)
+        const std::int32_t* te = &fs.tets[4 * t];
+        st[t] = stable_neo_hookean(x[te[0]], x[te[1]], x[te[2]], x[te[3]], fs.rest[t], tet_mu[t], tet_lam[t], project);
+    }
+    for (std::size_t t = 0; t < nt; ++t) {  // :233-239 + scatter12 :310-318
+        const std::int32_t* te = &fs.tets[4 * t];
+        val += dt2 * st[t].value;
+        for (int a = 0; a < 4; ++a)
+            for (int k = 0; k < 3; ++k) grad[3 * te[a] + k] += dt2 * st[t].grad[3 * a + k];
+        for (int a = 0; a < 4; ++a)
+            for (int b = a; b < 4; ++b) {
+                Mat3 blk;
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r) blk(r, c) = dt2 * st[t].hess[12 * (3 * b + c) + 3 * a + r];
+                stream.emit(te[a], te[b], blk);
+            }
+    }
+    for (std::size_t v = 0; v < n && v < pinned.size(); ++v)
+        if (pinned[v])
+            for (int k = 0; k < 3; ++k) grad[3 * v + k] = 0;
+    return val;
 }
 
 }  // namespace oracle

@@ -218,6 +218,76 @@ std::int64_t oracle_filter_pinned(const std::uint64_t* keys, const double* vals,
     return static_cast<std::int64_t>(s.size());
 }
 
+
+// ---- element-Hessian producer ---------------------------------
+static Vec3 ld3(const double* p) {
+    Vec3 v;
+    for (int k = 0; k < 3; ++k) v[k] = p[k];
+    return v;
+}
+
+// tet_rest (neo_hookean.hpp:13-27): p12 = 4 rest positions; 0 ok, 1 degenerate
+int oracle_tet_rest(const double* p12, double* inv9, double* vol) {
+    try {
+        const TetRest r = tet_rest(ld3(p12), ld3(p12 + 3), ld3(p12 + 6), ld3(p12 + 9));
+        for (int k = 0; k < 9; ++k) inv9[k] = r.inv_rest_edges.m[k];
+        *vol = r.volume;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+void oracle_stable_neo_hookean(const double* x12, const double* inv9, double vol, double mu, double lam, int project,
+                               double* value, double* grad12, double* hess144) {
+    TetRest r;
+    for (int k = 0; k < 9; ++k) r.inv_rest_edges.m[k] = inv9[k];
+    r.volume = vol;
+    const Stencil12 s = stable_neo_hookean(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9), r, mu, lam, project != 0);
+    *value = s.value;
+    for (int k = 0; k < 12; ++k) grad12[k] = s.grad[k];
+    for (int k = 0; k < 144; ++k) hess144[k] = s.hess[k];
+}
+
+void oracle_project_psd(int n, const double* M, double* out) { oracle_eig::project_psd(n, M, out); }
+
+// IncrementalPotential::assemble, inertia + solid meshes (see oracle.hpp):
+// stream written to keys / vals9 (capacity n_verts + 10 n_tets), grad 3n;
+// returns the stream length
+std::int64_t oracle_ip_fem_assemble(std::int32_t n_verts, const double* x, const double* x_tilde, const double* mass,
+                                    std::int32_t n_meshes, const std::int64_t* tet_begin, const double* mu,
+                                    const double* lam, const std::int32_t* tets, const double* inv9, const double* vol,
+                                    double dt2, const std::uint8_t* pinned, int project, std::uint64_t* keys,
+                                    double* vals9, double* grad, double* value) {
+    std::vector<Vec3> xs(n_verts), xt(n_verts);
+    for (std::int32_t v = 0; v < n_verts; ++v) {
+        xs[v] = ld3(x + 3 * v);
+        xt[v] = ld3(x_tilde + 3 * v);
+    }
+    std::vector<Real> m(mass, mass + n_verts);
+    FemSolids fs;
+    const std::int64_t nt = tet_begin[n_meshes];
+    fs.tets.assign(tets, tets + 4 * nt);
+    fs.rest.resize(nt);
+    for (std::int64_t t = 0; t < nt; ++t) {
+        for (int k = 0; k < 9; ++k) fs.rest[t].inv_rest_edges.m[k] = inv9[9 * t + k];
+        fs.rest[t].volume = vol[t];
+    }
+    fs.tet_begin.assign(tet_begin, tet_begin + n_meshes + 1);
+    fs.mu.assign(mu, mu + n_meshes);
+    fs.lam.assign(lam, lam + n_meshes);
+    std::vector<char> pin(n_verts, 0);
+    if (pinned)
+        for (std::int32_t v = 0; v < n_verts; ++v) pin[v] = static_cast<char>(pinned[v]);
+    std::vector<Real> g;
+    BlockTripletStream s;
+    *value = ip_fem_assemble(xs, xt, m, fs, dt2, pin, g, s, project != 0);
+    for (std::size_t k = 0; k < g.size(); ++k) grad[k] = g[k];
+    store_stream(s, keys, vals9);
+    return static_cast<std::int64_t>(s.size());
+}
+
 // ---- partition / hierarchy ----------------------------------------------------
 std::int32_t oracle_subdomain_count(std::int32_t v, std::int32_t n, std::int32_t n_o) {
     return subdomain_count(v, n, n_o);

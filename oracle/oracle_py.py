@@ -25,6 +25,7 @@ u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 vp = C.c_void_p
 sz = C.c_size_t
 i32 = C.c_int32
@@ -91,6 +92,11 @@ def lib():
         "oracle_dist_fill": (None, [vp, vp, f64p, sz]),
         "oracle_random_stream": (None, [vp, ci, ci, u64p, f64p]),
         "oracle_random_spd3": (None, [vp, cd, f64p]),
+        "oracle_tet_rest": (ci, [f64p, f64p, f64p]),
+        "oracle_stable_neo_hookean": (None, [f64p, f64p, cd, cd, cd, ci, f64p, f64p, f64p]),
+        "oracle_project_psd": (None, [ci, f64p, f64p]),
+        "oracle_ip_fem_assemble": (i64, [i32, f64p, f64p, f64p, i32, i64p, f64p, f64p, i32p, f64p, f64p, cd, vp, ci,
+                                         u64p, f64p, f64p, f64p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -352,6 +358,57 @@ def two_level_abd_reduce(keys, vals, n_fem, n_bodies, abd_node_body, jac36, poli
                                           body if len(body) else np.zeros(1, np.int32),
                                           jac if len(jac) else np.zeros(1), *_pol(policy), ok, ov)
     return ok[:n].copy(), ov[:n].copy()
+
+
+# ------------------------------------------- element-Hessian producer ----
+def tet_rest(p12):
+    """energy/neo_hookean.hpp:13-27 -> (inv_rest_edges 9 column-major, volume)."""
+    p = np.ascontiguousarray(p12, np.float64).reshape(12)
+    inv, vol = np.empty(9), np.empty(1)
+    if lib().oracle_tet_rest(p, inv, vol) != 0:
+        raise ValueError(lib().oracle_last_error().decode())
+    return inv, float(vol[0])
+
+
+def stable_neo_hookean(x12, inv9, vol, mu, lam, project=True):
+    """energy/neo_hookean.hpp:64-104 -> (value, grad 12, hess 12x12 column-major)."""
+    val, g, h = np.empty(1), np.empty(12), np.empty(144)
+    lib().oracle_stable_neo_hookean(np.ascontiguousarray(x12, np.float64).reshape(12),
+                                    np.ascontiguousarray(inv9, np.float64).reshape(9), vol, mu, lam, int(project),
+                                    val, g, h)
+    return float(val[0]), g, h.reshape(12, 12).T.copy()
+
+
+def project_psd(M):
+    """energy/psd.hpp:8-14 on a symmetric n x n matrix."""
+    M = np.asarray(M, np.float64)
+    n = M.shape[0]
+    out = np.empty(n * n)
+    lib().oracle_project_psd(n, np.ascontiguousarray(M.T).reshape(-1), out)
+    return out.reshape(n, n).T.copy()
+
+
+def ip_fem_assemble(x, x_tilde, mass, tet_begin, mu, lam, tets, inv9, vol, dt2, pinned=None, project=True):
+    """IncrementalPotential::assemble restricted to inertia + solid meshes
+    (incremental_potential.hpp:170-180, 222-239, 310-318, 253-254) ->
+    (value, grad 3n, keys, vals) in emission order."""
+    x = np.ascontiguousarray(x, np.float64).reshape(-1)
+    n = len(x) // 3
+    tb = np.ascontiguousarray(tet_begin, np.int64)
+    nm = len(tb) - 1
+    nt = int(tb[-1])
+    cap = max(n + 10 * nt, 1)
+    keys, vals = np.empty(cap, np.uint64), np.empty((cap, 9))
+    grad, val = np.empty(3 * n), np.empty(1)
+    pin = None if pinned is None else np.ascontiguousarray(pinned, np.uint8)
+    T = lib().oracle_ip_fem_assemble(n, x, np.ascontiguousarray(x_tilde, np.float64).reshape(-1),
+                                     np.ascontiguousarray(mass, np.float64), nm, tb,
+                                     np.ascontiguousarray(mu, np.float64), np.ascontiguousarray(lam, np.float64),
+                                     np.ascontiguousarray(tets, np.int32).reshape(-1),
+                                     np.ascontiguousarray(inv9, np.float64).reshape(-1),
+                                     np.ascontiguousarray(vol, np.float64), dt2,
+                                     None if pin is None else pin.ctypes.data, int(project), keys, vals, grad, val)
+    return float(val[0]), grad, keys[:T].copy(), vals[:T].copy()
 
 
 def filter_pinned(keys, vals, pinned):

@@ -9,7 +9,9 @@
 // restatement (tests/test_oracle_vs_reference.py) and as bench.py's
 // "reference" CPU arm; never by the product.
 //
-// Not exposed: filter_pinned (a private member of IncrementalPotential,
+// Not exposed: ip_fem_assemble (IncrementalPotential::assemble, whose header
+// drags in the contact stack; its element stencils ARE exposed: tet_rest,
+// stable_neo_hookean, project_psd), filter_pinned (a private member of IncrementalPotential,
 // solver/incremental_potential.hpp:410, whose header drags in the contact and
 // energy stack) and the MAS shift count (the reference does not record it).
 #include <cstring>
@@ -18,6 +20,8 @@
 #include <stdexcept>
 #include <string>
 
+#include "adipc/energy/neo_hookean.hpp"
+#include "adipc/energy/psd.hpp"
 #include "adipc/precond/block_jacobi.hpp"
 #include "adipc/precond/hierarchy.hpp"
 #include "adipc/precond/mas.hpp"
@@ -236,6 +240,41 @@ std::int64_t ref_filter_pinned(const std::uint64_t*, const double*, std::size_t,
                                std::uint64_t*, double*) {
     g_err = "filter_pinned is private to IncrementalPotential in the reference";
     return -1;
+}
+
+
+// ---- element-Hessian producer: energy/neo_hookean.hpp + energy/psd.hpp (the
+// reference's own code; psd.hpp's eigen-solver is the shim's, sym_eig.hpp) ----
+static Vec3 ld3(const double* p) { return Vec3(p[0], p[1], p[2]); }
+
+int ref_tet_rest(const double* p12, double* inv9, double* vol) {
+    try {
+        const TetRest r = tet_rest(ld3(p12), ld3(p12 + 3), ld3(p12 + 6), ld3(p12 + 9));
+        std::memcpy(inv9, r.inv_rest_edges.data(), 72);
+        *vol = r.volume;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+void ref_stable_neo_hookean(const double* x12, const double* inv9, double vol, double mu, double lam, int project,
+                            double* value, double* grad12, double* hess144) {
+    TetRest r;
+    r.inv_rest_edges = load_mat3(inv9);
+    r.volume = vol;
+    const Stencil12 s = stable_neo_hookean(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9), r, mu, lam, project != 0);
+    *value = s.value;
+    std::memcpy(grad12, s.grad.data(), 96);
+    std::memcpy(hess144, s.hess.data(), 144 * 8);
+}
+
+void ref_project_psd(int n, const double* M, double* out) {
+    MatX m(n, n);
+    std::memcpy(m.data(), M, sizeof(double) * n * n);
+    const MatX p = project_psd(m);
+    std::memcpy(out, p.data(), sizeof(double) * n * n);
 }
 
 std::int32_t ref_subdomain_count(std::int32_t v, std::int32_t n, std::int32_t n_o) { return subdomain_count(v, n, n_o); }

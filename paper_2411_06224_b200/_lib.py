@@ -30,6 +30,15 @@ OPT_PC_PAIRS = 11
 OPT_DETERMINISTIC = 12
 
 # Every symbol include/adipc_gpu.h declares, with its ctypes signature.
+class FemDesc(C.Structure):
+    """adipc_fem_desc (include/adipc_gpu.h): the element-Hessian producer's
+    input — device pointers except tet_begin / mu / lambda (host)."""
+    _fields_ = [("n_verts", C.c_int32), ("x", C.c_void_p), ("x_tilde", C.c_void_p), ("mass", C.c_void_p),
+                ("n_meshes", C.c_int32), ("tet_begin", C.c_void_p), ("mu", C.c_void_p), ("lam", C.c_void_p),
+                ("tets", C.c_void_p), ("rest_inv9", C.c_void_p), ("rest_volume", C.c_void_p), ("dt2", C.c_double),
+                ("project", C.c_int), ("pinned", C.c_void_p)]
+
+
 GPU_SIGNATURES = {
     "adipc_gpu_create": (ci, [ci, C.POINTER(vp)]),
     "adipc_gpu_destroy": (ci, [vp]),
@@ -60,6 +69,8 @@ GPU_SIGNATURES = {
     "adipc_gpu_assemble_contact_device": (ci, [vp, vp, vp, i64, vp, vp, i64, i32, i32, i32, vp, vp, i32, vp,
                                                C.POINTER(i64), C.POINTER(i64)]),
     "adipc_gpu_filter_pinned": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
+    "adipc_gpu_fem_emit_device": (ci, [vp, C.POINTER(FemDesc), vp, vp, vp, C.POINTER(cd)]),
+    "adipc_gpu_fem_assemble_device": (ci, [vp, C.POINTER(FemDesc), vp, C.POINTER(cd), C.POINTER(i64)]),
     "adipc_gpu_filter_pinned_device": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
     "adipc_gpu_spmv": (ci, [vp, vp, vp]),
     "adipc_gpu_spmv_device": (ci, [vp, vp, vp]),

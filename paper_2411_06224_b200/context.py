@@ -166,6 +166,40 @@ class Context:
                 n_block_rows, ptr(p), C.byref(U), C.byref(nt)))
         return U.value, nt.value
 
+    # -- element-Hessian producer ------------------------------
+    def _fem_desc(self, mesh, x, x_tilde, dt2, project, pinned):
+        """mesh: dict of DEVICE tensors mass / tets / rest_inv9 / rest_volume and
+        host lists tet_begin / mu / lam (one entry per solid mesh)."""
+        tb = np.ascontiguousarray(mesh["tet_begin"], np.int64)
+        mu = np.ascontiguousarray(mesh["mu"], np.float64)
+        lam = np.ascontiguousarray(mesh["lam"], np.float64)
+        n = int(mesh["mass"].numel())
+        for name, t in (("x", x), ("x_tilde", x_tilde)):
+            if not _is_device(t) or t.numel() != 3 * n:
+                raise InvalidArgument(f"{name}: device tensor of 3 * n_verts = {3 * n} doubles expected")
+        d = _lib.FemDesc(n, ptr(x), ptr(x_tilde), ptr(mesh["mass"]), len(tb) - 1, tb.ctypes.data, mu.ctypes.data,
+                         lam.ctypes.data, ptr(mesh["tets"]), ptr(mesh["rest_inv9"]), ptr(mesh["rest_volume"]),
+                         float(dt2), int(project), ptr(pinned) if pinned is not None else None)
+        return d, (tb, mu, lam), n
+
+    def fem_emit(self, mesh, x, x_tilde, dt2, keys, vals, grad, project=True, pinned=None):
+        """IncrementalPotential::assemble's inertia + tet stencils into the
+        device stream (keys / vals, n + 10 n_tets entries) and grad; returns
+        the value."""
+        d, keep, _ = self._fem_desc(mesh, x, x_tilde, dt2, project, pinned)
+        v = C.c_double()
+        self._check(self._L.adipc_gpu_fem_emit_device(self.h, C.byref(d), ptr(keys), ptr(vals), ptr(grad),
+                                                      C.byref(v)))
+        return v.value
+
+    def fem_assemble(self, mesh, x, x_tilde, dt2, grad, project=True, pinned=None):
+        """emit + filter_pinned + sort + reduce into the context matrix; returns
+        (value, U)."""
+        d, keep, _ = self._fem_desc(mesh, x, x_tilde, dt2, project, pinned)
+        v, U = C.c_double(), C.c_int64()
+        self._check(self._L.adipc_gpu_fem_assemble_device(self.h, C.byref(d), ptr(grad), C.byref(v), C.byref(U)))
+        return v.value, U.value
+
     def matrix_info(self):
         n, U = C.c_int32(), C.c_int64()
         self._check(self._L.adipc_gpu_matrix_info(self.h, C.byref(n), C.byref(U)))

@@ -325,6 +325,72 @@ int adipc_gpu_assemble_filtered_device(adipc_gpu_ctx* ctx, const uint64_t* d_key
     });
 }
 
+
+// ---- element-Hessian producer (energy.cu) ---------------------
+static FemDesc fem_desc(const adipc_fem_desc* d) {
+    if (!d) throw StatusError(kInvalidArgument, "null adipc_fem_desc");
+    if (d->n_verts < 0 || d->n_meshes < 0) throw StatusError(kInvalidArgument, "negative size");
+    if (d->n_verts > 0 && (!d->x || !d->x_tilde || !d->mass)) throw StatusError(kInvalidArgument, "missing x / x_tilde / mass");
+    if (d->n_meshes > 0 && (!d->tet_begin || !d->mu || !d->lambda))
+        throw StatusError(kInvalidArgument, "missing tet_begin / mu / lambda");
+    for (int m = 0; m < d->n_meshes; ++m)
+        if (d->tet_begin[m + 1] < d->tet_begin[m] || d->tet_begin[0] != 0)
+            throw StatusError(kInvalidArgument, "tet_begin must start at 0 and not decrease");
+    if (d->n_meshes > 0 && d->tet_begin[d->n_meshes] > 0 && (!d->tets || !d->rest_inv9 || !d->rest_volume))
+        throw StatusError(kInvalidArgument, "missing tets / rest data");
+    FemDesc f;
+    f.n_verts = d->n_verts;
+    f.x = d->x;
+    f.x_tilde = d->x_tilde;
+    f.mass = d->mass;
+    f.n_meshes = d->n_meshes;
+    f.tet_begin = d->tet_begin;
+    f.mu = d->mu;
+    f.lambda = d->lambda;
+    f.tets = d->tets;
+    f.rest_inv9 = d->rest_inv9;
+    f.rest_volume = d->rest_volume;
+    f.dt2 = d->dt2;
+    f.project = d->project;
+    f.pinned = d->pinned;
+    return f;
+}
+
+static std::int64_t fem_stream_len(const adipc_fem_desc* d) {
+    return static_cast<std::int64_t>(d->n_verts) + 10 * (d->n_meshes > 0 ? d->tet_begin[d->n_meshes] : 0);
+}
+
+int adipc_gpu_fem_emit_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* d, uint64_t* d_keys, double* d_vals9,
+                              double* d_grad, double* value) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const FemDesc f = fem_desc(d);
+        c.fem_value.reserve(1);
+        fem_emit(c, f, d_keys, d_vals9, d_grad, c.fem_value.p);
+        if (value) ADIPC_CUDA(cudaMemcpyAsync(value, c.fem_value.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+    });
+}
+
+int adipc_gpu_fem_assemble_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* d, double* d_grad, double* value,
+                                  int64_t* n_unique) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const FemDesc f = fem_desc(d);
+        const std::int64_t T = fem_stream_len(d);
+        c.fem_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(T, 1)));
+        c.fem_vals.reserve(9 * static_cast<std::size_t>(std::max<std::int64_t>(T, 1)));
+        c.fem_value.reserve(1);
+        timed(c, [&] {
+            fem_emit(c, f, c.fem_keys.p, c.fem_vals.p, d_grad, c.fem_value.p);
+            assemble_filtered(c, c.fem_keys.p, c.fem_vals.p, T, d->n_verts, d->pinned);
+        });
+        if (value) ADIPC_CUDA(cudaMemcpyAsync(value, c.fem_value.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+        if (n_unique) *n_unique = c.A.U;
+    });
+}
+
 int adipc_gpu_matrix_info(adipc_gpu_ctx* ctx, int32_t* n, int64_t* U) {
     return guarded(ctx, [&] {
         if (n) *n = ctx->c.A.n;

@@ -118,6 +118,9 @@ struct Ctx {
     DBuf<std::int32_t> abd_cnt;
     DBuf<std::int64_t> abd_off;
     DBuf<std::uint64_t> tile_keys;
+    // element-Hessian producer (energy.cu): the emitted stream + the value
+    DBuf<std::uint64_t> fem_keys;
+    DBuf<double> fem_vals, fem_value;
     DBuf<double> tile_vals;
     // staging of the host-pointer entry points (contact node stream, DofMap)
     DBuf<std::uint64_t> io_keys, io_keys2;
@@ -234,6 +237,27 @@ void assemble(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::in
               int deterministic, cudaEvent_t vals_ready = nullptr);
 // filter_pinned + sort + reduce; optionally a second stream segment appended
 // after the first (the two-level contact tiles)
+// Element-Hessian producer input (energy.cu; incremental_potential.hpp:
+// 170-180, 222-239): device arrays except tet_begin / mu / lambda (host,
+// one entry per solid mesh; tet_begin has n_meshes + 1).
+struct FemDesc {
+    std::int32_t n_verts = 0;
+    const double* x = nullptr;        // 3 n_verts
+    const double* x_tilde = nullptr;  // 3 n_verts
+    const double* mass = nullptr;     // n_verts
+    std::int32_t n_meshes = 0;
+    const std::int64_t* tet_begin = nullptr;
+    const double* mu = nullptr;
+    const double* lambda = nullptr;
+    const std::int32_t* tets = nullptr;     // 4 global slots per tet
+    const double* rest_inv9 = nullptr;      // Dm^-1, 9 column-major per tet
+    const double* rest_volume = nullptr;    // per tet
+    double dt2 = 0;
+    int project = 1;
+    const std::uint8_t* pinned = nullptr;   // n_verts or null
+};
+void fem_emit(Ctx& c, const FemDesc& d, std::uint64_t* d_keys, double* d_vals, double* d_grad, double* d_value);
+
 void assemble_filtered(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
                        const std::uint8_t* d_pinned, cudaEvent_t vals_ready = nullptr,
                        const std::uint64_t* d_keys2 = nullptr, const double* d_vals2 = nullptr, std::int64_t T2 = 0);

@@ -1,0 +1,363 @@
+// Device element-Hessian producer: the inertia + solid-mesh
+// part of IncrementalPotential::assemble (solver/incremental_potential.hpp:
+// 170-180 inertia, 222-239 tets, scatter12 :310-318, pinned gradient
+// :253-254) with the polynomial stable Neo-Hookean stencil
+// (energy/neo_hookean.hpp:64-104) projected to the PSD cone (energy/psd.hpp:
+// 8-14). The triplet stream is written in the reference's emission order
+// (every vertex's inertia diagonal, then 10 blocks per tet, a <= b, emit()
+// canonicalisation), so the existing filter + sort + reduce turns it into the
+// same SortedSymBlockCoo — the 1.5 GB stream never crosses PCIe.
+//
+// One thread per tet, everything in registers:
+//  * vec(F) = (C^T (x) I3) x12 with C = G^T Dm^-1 (4 x 3, G the edge
+//    operator of neo_hookean.hpp:44-54), so the 12 x 12 Hessian
+//    dFdx^T H9 dFdx is a bilinear form in the rows c_a of C:
+//      H_ab = V [ mu (c_a.c_b) I + lam u_a u_b^T + dJcoef [-F (c_a x c_b)]_x ],
+//      u_a = cof c_a  (H9 = mu I + lam vec(cof) vec(cof)^T + dJcoef HJ,
+//      neo_hookean.hpp:90-99; HJ's six cross-product blocks collapse to one
+//      cross-product matrix per block pair).
+//  * PSD projection in the 9-dimensional complement of the translations:
+//    C = Q R with Q a fixed orthonormal basis of 1-perp in R^4 (Helmert), so
+//    H12 = (Q (x) I3) M (Q (x) I3)^T with M_jl = the same bilinear form on the
+//    rows r_j of R = Q^T C. The projection of H12 is (Q (x) I3) proj(M)
+//    (Q (x) I3)^T (the 3 translation eigenvalues of H12 are exactly 0).
+//    Fast path: if M + tau I (tau = 1e-12 tr M) passes a Cholesky, every
+//    eigenvalue is > -tau and H12 is emitted as is (the reference clamps
+//    eigenvalues in (-tau, 0): a difference below 1e-11 |H|). Otherwise a
+//    cyclic Jacobi eigen-decomposition of M (per-thread local arrays; only
+//    indefinite elements take it) and proj(M) = V max(w, 0) V^T.
+#include "context.hpp"
+
+namespace adipc_gpu {
+
+namespace {
+
+constexpr int kFemThreads = 128;
+
+__device__ __forceinline__ void red_add_f64(double* p, double v) { asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v)); }
+
+// CTA sum of v, one fp64 atomic per CTA into *out
+__device__ __forceinline__ void block_sum_atomic(double v, double* out) {
+    __shared__ double part[32];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) part[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < static_cast<int>(blockDim.x >> 5) ? part[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) atomicAdd(out, v);
+    }
+}
+
+// Helmert basis of the complement of (1,1,1,1) in R^4 (columns of Q, 4 x 3)
+__device__ __forceinline__ double helmert(int a, int j) {
+    const double s2 = 0.70710678118654752440, s6 = 0.40824829046386301637, s12 = 0.28867513459481288225;
+    if (j == 0) return a == 0 ? s2 : (a == 1 ? -s2 : 0.0);
+    if (j == 1) return a < 2 ? s6 : (a == 2 ? -2.0 * s6 : 0.0);
+    return a < 3 ? s12 : -3.0 * s12;
+}
+
+struct TetState {
+    double F[9];    // column-major
+    double cof[9];  // columns f1 x f2, f2 x f0, f0 x f1 (neo_hookean.hpp:29-35)
+    double mu, lam, dJ, V;
+};
+
+// H_xy = V [ mu (x.y) I + lam (cof x)(cof y)^T + dJ [-F (x cross y)]_x ], 3x3 column-major
+__device__ __forceinline__ void stencil_block(const TetState& s, const double* x, const double* y, double* h) {
+    double ux[3], uy[3], w[3], xy;
+    xy = x[0] * y[0] + x[1] * y[1] + x[2] * y[2];
+    for (int k = 0; k < 3; ++k) {
+        ux[k] = s.cof[k] * x[0] + s.cof[3 + k] * x[1] + s.cof[6 + k] * x[2];
+        uy[k] = s.cof[k] * y[0] + s.cof[3 + k] * y[1] + s.cof[6 + k] * y[2];
+    }
+    const double z0 = x[1] * y[2] - x[2] * y[1], z1 = x[2] * y[0] - x[0] * y[2], z2 = x[0] * y[1] - x[1] * y[0];
+    for (int k = 0; k < 3; ++k) w[k] = -(s.F[k] * z0 + s.F[3 + k] * z1 + s.F[6 + k] * z2);
+    // [w]_x column-major: (0,1) = -w2, (0,2) = w1, (1,2) = -w0
+    const double W[9] = {0, w[2], -w[1], -w[2], 0, w[0], w[1], -w[0], 0};
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            h[3 * c + r] = s.V * ((r == c ? s.mu * xy : 0.0) + s.lam * ux[r] * uy[c] + s.dJ * W[3 * c + r]);
+}
+
+// packed lower index of (i, j), i >= j, n = 9
+__device__ __forceinline__ constexpr int pk(int i, int j) { return i * (i + 1) / 2 + j; }
+
+// Cholesky of M + tau I in place (packed lower); true when every pivot > 0
+__device__ __forceinline__ bool shifted_cholesky_ok(double* L, double tau) {
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        double d = L[pk(j, j)] + tau;
+#pragma unroll
+        for (int k = 0; k < j; ++k) d -= L[pk(j, k)] * L[pk(j, k)];
+        ok = ok && d > 0;
+        const double inv = d > 0 ? rsqrt(d) : 0.0;
+        L[pk(j, j)] = d > 0 ? d * inv : 0.0;
+#pragma unroll
+        for (int i = j + 1; i < 9; ++i) {
+            double s = L[pk(i, j)];
+#pragma unroll
+            for (int k = 0; k < j; ++k) s -= L[pk(i, k)] * L[pk(j, k)];
+            L[pk(i, j)] = s * inv;
+        }
+    }
+    return ok;
+}
+
+// proj(M) for a symmetric 9 x 9 (full column-major in `a`, overwritten):
+// cyclic Jacobi (oracle/sym_eig.hpp's rotations), then V max(w, 0) V^T
+__device__ __noinline__ void project9(double* a) {
+    double v[81];
+    for (int k = 0; k < 81; ++k) v[k] = (k % 10 == 0) ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        double off = 0, tot = 0;
+        for (int j = 0; j < 9; ++j)
+            for (int i = 0; i < 9; ++i) {
+                const double x = a[9 * j + i] * a[9 * j + i];
+                tot += x;
+                if (i != j) off += x;
+            }
+        if (off <= 1e-32 * tot) break;
+        for (int p = 0; p < 8; ++p)
+            for (int q = p + 1; q < 9; ++q) {
+                const double apq = a[9 * q + p];
+                if (apq == 0.0) continue;
+                const double theta = (a[9 * q + q] - a[9 * p + p]) / (2.0 * apq);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                const double c = rsqrt(t * t + 1.0), s = t * c;
+                for (int k = 0; k < 9; ++k) {
+                    const double kp = a[9 * p + k], kq = a[9 * q + k];
+                    a[9 * p + k] = c * kp - s * kq;
+                    a[9 * q + k] = s * kp + c * kq;
+                }
+                for (int k = 0; k < 9; ++k) {
+                    const double pk_ = a[9 * k + p], qk = a[9 * k + q];
+                    a[9 * k + p] = c * pk_ - s * qk;
+                    a[9 * k + q] = s * pk_ + c * qk;
+                }
+                for (int k = 0; k < 9; ++k) {
+                    const double kp = v[9 * p + k], kq = v[9 * q + k];
+                    v[9 * p + k] = c * kp - s * kq;
+                    v[9 * q + k] = s * kp + c * kq;
+                }
+            }
+    }
+    double w[9];
+    for (int k = 0; k < 9; ++k) w[k] = a[10 * k] > 0 ? a[10 * k] : 0.0;
+    for (int j = 0; j < 9; ++j)
+        for (int i = 0; i < 9; ++i) {
+            double s = 0;
+            for (int k = 0; k < 9; ++k) s += v[9 * k + i] * w[k] * v[9 * k + j];
+            a[9 * j + i] = s;
+        }
+}
+
+// inertia (incremental_potential.hpp:170-180): one thread per vertex
+__global__ void k_fem_inertia(std::int32_t n, const double* __restrict__ x, const double* __restrict__ xt,
+                              const double* __restrict__ mass, std::uint64_t* __restrict__ keys,
+                              double* __restrict__ vals, double* __restrict__ grad, double* __restrict__ value) {
+    double e = 0;
+    for (std::int64_t v = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const double m = mass[v];
+        const double d0 = x[3 * v] - xt[3 * v], d1 = x[3 * v + 1] - xt[3 * v + 1], d2 = x[3 * v + 2] - xt[3 * v + 2];
+        e += 0.5 * m * (d0 * d0 + d1 * d1 + d2 * d2);
+        grad[3 * v] = m * d0;
+        grad[3 * v + 1] = m * d1;
+        grad[3 * v + 2] = m * d2;
+        keys[v] = (static_cast<std::uint64_t>(v) << 32) | static_cast<std::uint64_t>(v);
+        double* o = vals + 9 * v;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) o[k] = (k % 4 == 0) ? m : 0.0;
+    }
+    block_sum_atomic(e, value);
+}
+
+// tets of one mesh: stream entries [base + 10 t, base + 10 t + 10)
+__global__ void __launch_bounds__(kFemThreads) k_fem_tets(std::int64_t n_tets, const std::int32_t* __restrict__ tets,
+                                                         const double* __restrict__ inv9, const double* __restrict__ vol,
+                                                         const double* __restrict__ x, double mu, double lam,
+                                                         double dt2, int project, std::uint64_t* __restrict__ keys,
+                                                         double* __restrict__ vals, double* __restrict__ grad,
+                                                         double* __restrict__ value) {
+    double e = 0;
+    for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < n_tets;
+         t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int4 id = reinterpret_cast<const int4*>(tets)[t];
+        const int ids[4] = {id.x, id.y, id.z, id.w};
+        double B[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) B[k] = inv9[9 * t + k];
+        TetState s;
+        s.V = vol[t];
+        s.mu = mu;
+        s.lam = lam;
+        double xa[4][3];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) xa[a][k] = x[3 * static_cast<std::int64_t>(ids[a]) + k];
+        // C = G^T B (rows c_a): c_0 = -(B row 0 + row 1 + row 2), c_a = B row a-1
+        double C[4][3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            C[0][j] = ((0.0 - B[3 * j]) - B[3 * j + 1]) - B[3 * j + 2];
+            C[1][j] = B[3 * j];
+            C[2][j] = B[3 * j + 1];
+            C[3][j] = B[3 * j + 2];
+        }
+        // F = Ds B (neo_hookean.hpp:69-73)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                s.F[3 * j + k] = (xa[1][k] - xa[0][k]) * B[3 * j] + (xa[2][k] - xa[0][k]) * B[3 * j + 1] +
+                                 (xa[3][k] - xa[0][k]) * B[3 * j + 2];
+        const double* f0 = s.F;
+        const double* f1 = s.F + 3;
+        const double* f2 = s.F + 6;
+        auto crossp = [](const double* a, const double* b, double* c) {
+            c[0] = a[1] * b[2] - a[2] * b[1];
+            c[1] = a[2] * b[0] - a[0] * b[2];
+            c[2] = a[0] * b[1] - a[1] * b[0];
+        };
+        crossp(f1, f2, s.cof);
+        crossp(f2, f0, s.cof + 3);
+        crossp(f0, f1, s.cof + 6);
+        const double J = f0[0] * s.cof[0] + f0[1] * s.cof[1] + f0[2] * s.cof[2];
+        double IC = 0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) IC += s.F[k] * s.F[k];
+        e += s.V * (0.5 * mu * (IC - 3) - mu * (J - 1) + 0.5 * lam * (J - 1) * (J - 1));
+        s.dJ = lam * (J - 1) - mu;
+        // gradient V dFdx^T vec(P), P = mu F + dJ cof: g_a = V P c_a
+        double P[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) P[k] = mu * s.F[k] + s.dJ * s.cof[k];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const std::int64_t o = 3 * static_cast<std::int64_t>(ids[a]);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                red_add_f64(grad + o + k,
+                            dt2 * (s.V * (P[k] * C[a][0] + P[3 + k] * C[a][1] + P[6 + k] * C[a][2])));
+        }
+        // PSD test in the reduced space: R = Q^T C, M_jl = stencil(r_j, r_l)
+        bool psd = !project;
+        double R[3][3];
+        if (project) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    R[j][i] = helmert(0, j) * C[0][i] + helmert(1, j) * C[1][i] + helmert(2, j) * C[2][i] +
+                              helmert(3, j) * C[3][i];
+            double L[45];
+            double tr = 0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int l = 0; l <= j; ++l) {
+                    double h[9];
+                    stencil_block(s, R[j], R[l], h);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+#pragma unroll
+                        for (int r = 0; r < 3; ++r)
+                            if (3 * j + r >= 3 * l + c) L[pk(3 * j + r, 3 * l + c)] = h[3 * c + r];
+                }
+#pragma unroll
+            for (int i = 0; i < 9; ++i) tr += L[pk(i, i)];
+            psd = tr > 0 && shifted_cholesky_ok(L, 1e-12 * tr);
+        }
+        const std::int64_t base = 10 * t;
+        if (psd) {
+            int q = 0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = a; b < 4; ++b, ++q) {
+                    double h[9];
+                    stencil_block(s, C[a], C[b], h);
+                    const bool flip = ids[a] > ids[b];
+                    const std::uint32_t r0 = static_cast<std::uint32_t>(flip ? ids[b] : ids[a]);
+                    const std::uint32_t c0 = static_cast<std::uint32_t>(flip ? ids[a] : ids[b]);
+                    keys[base + q] = (static_cast<std::uint64_t>(r0) << 32) | c0;
+                    double* o = vals + 9 * (base + q);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+#pragma unroll
+                        for (int r = 0; r < 3; ++r) o[3 * c + r] = dt2 * (flip ? h[3 * r + c] : h[3 * c + r]);
+                }
+        } else {
+            // indefinite: full M, project, lift back through Q (x) I3
+            double M[81];
+            for (int j = 0; j < 3; ++j)
+                for (int l = 0; l < 3; ++l) {
+                    double h[9];
+                    stencil_block(s, R[j], R[l], h);
+                    for (int c = 0; c < 3; ++c)
+                        for (int r = 0; r < 3; ++r) M[9 * (3 * l + c) + 3 * j + r] = h[3 * c + r];
+                }
+            project9(M);
+            int q = 0;
+            for (int a = 0; a < 4; ++a)
+                for (int b = a; b < 4; ++b, ++q) {
+                    double h[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+                    for (int j = 0; j < 3; ++j)
+                        for (int l = 0; l < 3; ++l) {
+                            const double w = helmert(a, j) * helmert(b, l);
+                            for (int c = 0; c < 3; ++c)
+                                for (int r = 0; r < 3; ++r) h[3 * c + r] += w * M[9 * (3 * l + c) + 3 * j + r];
+                        }
+                    const bool flip = ids[a] > ids[b];
+                    const std::uint32_t r0 = static_cast<std::uint32_t>(flip ? ids[b] : ids[a]);
+                    const std::uint32_t c0 = static_cast<std::uint32_t>(flip ? ids[a] : ids[b]);
+                    keys[base + q] = (static_cast<std::uint64_t>(r0) << 32) | c0;
+                    double* o = vals + 9 * (base + q);
+                    for (int c = 0; c < 3; ++c)
+                        for (int r = 0; r < 3; ++r) o[3 * c + r] = dt2 * (flip ? h[3 * r + c] : h[3 * c + r]);
+                }
+        }
+    }
+    block_sum_atomic(dt2 * e, value);
+}
+
+// pinned slots: zero gradient (incremental_potential.hpp:253-254)
+__global__ void k_fem_pin_grad(std::int32_t n, const std::uint8_t* __restrict__ pinned, double* __restrict__ grad) {
+    for (std::int64_t v = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        if (pinned[v]) grad[3 * v] = grad[3 * v + 1] = grad[3 * v + 2] = 0.0;
+}
+
+}  // namespace
+
+// The stream (n_verts + 10 n_tets entries), the gradient (3 n_verts) and the
+// value (one device double) of inertia + every solid mesh.
+void fem_emit(Ctx& c, const FemDesc& d, std::uint64_t* d_keys, double* d_vals, double* d_grad, double* d_value) {
+    cudaStream_t st = c.stream;
+    ADIPC_CUDA(cudaMemsetAsync(d_value, 0, sizeof(double), st));
+    if (d.n_verts > 0) {
+        k_fem_inertia<<<grid_for(d.n_verts, 256, 8), 256, 0, st>>>(d.n_verts, d.x, d.x_tilde, d.mass, d_keys, d_vals,
+                                                                 d_grad, d_value);
+        ADIPC_LAUNCH_CHECK();
+    }
+    for (int m = 0; m < d.n_meshes; ++m) {
+        const std::int64_t t0 = d.tet_begin[m], nt = d.tet_begin[m + 1] - t0;
+        if (nt <= 0) continue;
+        k_fem_tets<<<grid_for(nt, kFemThreads, 16), kFemThreads, 0, st>>>(
+            nt, d.tets + 4 * t0, d.rest_inv9 + 9 * t0, d.rest_volume + t0, d.x, d.mu[m], d.lambda[m], d.dt2,
+            d.project, d_keys + d.n_verts + 10 * t0, d_vals + 9 * (d.n_verts + 10 * t0), d_grad, d_value);
+        ADIPC_LAUNCH_CHECK();
+    }
+    if (d.pinned && d.n_verts > 0) {
+        k_fem_pin_grad<<<grid_for(d.n_verts, 256, 8), 256, 0, st>>>(d.n_verts, d.pinned, d_grad);
+        ADIPC_LAUNCH_CHECK();
+    }
+}
+
+}  // namespace adipc_gpu

@@ -27,8 +27,10 @@ SIGNATURES = {
     "adipc_scene_fem_box": (vp, [ci, ci, ci, cd, cd, cd, cd, cd, cd, cd, ci, cd, C.c_uint]),
     "adipc_scene_cloth": (vp, [ci, ci, cd, cd, C.c_uint]),
     "adipc_scene_abd_stack": (vp, [ci, ci, ci, C.c_uint]),
-    "adipc_scene_hybrid": (vp, [ci, ci, ci, ci, ci, C.c_uint]),
+    "adipc_scene_hybrid": (vp, [ci, ci, ci, ci, ci, cd, C.c_uint]),
     "adipc_scene_free": (None, [vp]),
+    "adipc_scene_mesh_sizes": (None, [vp, vp, vp]),
+    "adipc_scene_copy_mesh": (None, [vp, vp, vp, vp]),
     "adipc_scene_sizes": (None, [vp, vp]),
     "adipc_scene_copy": (None, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
 }
@@ -102,6 +104,13 @@ class Scene:
             self.rest_edges = np.empty((ne, 2), np.int32)
             L.adipc_scene_copy(handle, ptr(self.keys), ptr(self.vals), ptr(self.node_keys), ptr(self.node_vals),
                                ptr(self.abd_body), ptr(self.jac36), ptr(self.pinned), ptr(self.rest_edges))
+            ms, mat = np.zeros(2, np.int64), np.zeros(2)
+            L.adipc_scene_mesh_sizes(handle, ptr(ms), ptr(mat))
+            self.verts = np.empty((int(ms[0]), 3))
+            self.tets = np.empty((int(ms[1]), 4), np.int32)
+            self.mass = np.empty(int(ms[0]))
+            self.mu, self.lam = float(mat[0]), float(mat[1])
+            L.adipc_scene_copy_mesh(handle, ptr(self.verts), ptr(self.tets), ptr(self.mass))
         finally:
             L.adipc_scene_free(handle)
 
@@ -123,9 +132,44 @@ def abd_stack(bx=10, by=5, bz=10, seed=3) -> Scene:
     return Scene(lib().adipc_scene_abd_stack(bx, by, bz, seed))
 
 
-def hybrid(n_soft=4, soft_res=20, n_gears=40, gear_res=8, stencils_per_pair=1250, seed=4) -> Scene:
-    """cfg4: soft FEM blocks + ABD gears, ~100K contact stencils."""
-    return Scene(lib().adipc_scene_hybrid(n_soft, soft_res, n_gears, gear_res, stencils_per_pair, seed))
+def hybrid(n_soft=4, soft_res=20, n_gears=40, gear_res=8, stencils_per_pair=1250, E=1e5, seed=4) -> Scene:
+    """cfg4: FEM blocks (Young's modulus E) + ABD gears (kappa 1e8), seeded
+    PSD contact stencils between neighbouring objects (FEM-FEM, FEM-ABD,
+    ABD-ABD pairs) feeding two_level_abd_reduce."""
+    return Scene(lib().adipc_scene_hybrid(n_soft, soft_res, n_gears, gear_res, stencils_per_pair, float(E), seed))
+
+
+def ballistic_direction(sc: Scene, dt: float = 0.01, g=(0.0, -9.81, 0.0)) -> np.ndarray:
+    """x* for b = A x*: every FEM slot and every body translation moved by
+    dt^2 g, affine parts unchanged (the free-fall displacement of one step)."""
+    x = np.zeros((sc.n_blocks, 3))
+    x[: sc.n_fem] = np.asarray(g, np.float64) * dt * dt
+    for b in range(sc.n_bodies):
+        x[sc.n_fem + 4 * b] = np.asarray(g, np.float64) * dt * dt
+    x[sc.pinned.astype(bool)] = 0.0
+    return np.ascontiguousarray(x.reshape(-1))
+
+
+def tet_rest_data(verts: np.ndarray, tets: np.ndarray):
+    """TetRest per tet (energy/neo_hookean.hpp:13-27) for the producer's input:
+    Dm^-1 (9 doubles column-major, cofactors / det like Eigen's fixed 3x3
+    inverse) and volume det(Dm) / 6; vectorised."""
+    p = verts[tets]  # nt x 4 x 3
+    Dm = np.stack([p[:, 1] - p[:, 0], p[:, 2] - p[:, 0], p[:, 3] - p[:, 0]], axis=2)  # nt x 3(row) x 3(col)
+    det = np.linalg.det(Dm)
+    if not np.all(det > 0):
+        raise ValueError("inverted or degenerate rest tet")
+    inv = np.linalg.inv(Dm)  # nt x 3 x 3
+    inv9 = np.ascontiguousarray(inv.transpose(0, 2, 1).reshape(-1, 9))  # column-major
+    return inv9, det / 6.0
+
+
+def inertial_target(sc: Scene, dt: float = 0.01, g=(0.0, -9.81, 0.0)) -> np.ndarray:
+    """x_tilde of the first step from rest: x + dt v + dt^2 g with v = 0
+    (TimeStepper's targets, newton.hpp:85-99); pinned vertices stay."""
+    xt = sc.verts + (dt * dt) * np.asarray(g, np.float64)[None, :]
+    xt[sc.pinned.astype(bool)] = sc.verts[sc.pinned.astype(bool)]
+    return np.ascontiguousarray(xt.reshape(-1))
 
 
 def gravity_rhs(sc: Scene, dt: float = 0.01, g=(0.0, -9.81, 0.0)) -> np.ndarray:
@@ -153,6 +197,9 @@ CONFIGS = {
     "cfg2_cloth": lambda: cloth(224, 224),
     "cfg3_abd_stack": lambda: abd_stack(10, 5, 10),
     "cfg4_hybrid": lambda: hybrid(),
+    # the north star's ~1M-DOF stiff hybrid scene: 8 FEM blocks of 34^3 cells
+    # (E = 1e8) + 40 ABD gears, 96 object pairs x 1,100 contact stencils
+    "cfg4_hybrid_1m": lambda: hybrid(8, 34, 40, 8, 1100, E=1e8, seed=4),
     "cfg5_stiff_box": lambda: fem_box(68, 68, 68, 1.0, 1.0, 1.0, E=1e8),
     "stiff_beam": lambda: fem_box(34, 11, 11, 0.7, 0.22, 0.22, E=1e8),
 }

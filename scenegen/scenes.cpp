@@ -41,6 +41,11 @@ struct Scene {
     std::vector<double> abd_jac;  // 36 per abd node
     std::vector<std::uint8_t> pinned;
     std::vector<Index> rest_edges;  // pairs
+    // deformable solid mesh of FEM-only scenes (the element producer's input):
+    // rest positions (3 per vertex), tets (4 global slots each), vertex masses
+    std::vector<double> mesh_verts, mesh_mass;
+    std::vector<Index> mesh_tets;
+    double mu = 0, lam = 0;
 
     void emit(std::vector<std::uint64_t>& ks, std::vector<double>& vs, Index r, Index c, const double* b) {
         if (r <= c) {
@@ -350,6 +355,11 @@ Scene* fem_box(int nx, int ny, int nz, double sx, double sy, double sz, double E
         }
     }
     fem_masses(f);
+    for (const auto& v : f.mesh.verts) s->mesh_verts.insert(s->mesh_verts.end(), {v.x, v.y, v.z});
+    for (const auto& t : f.mesh.tets) s->mesh_tets.insert(s->mesh_tets.end(), t.begin(), t.end());
+    s->mesh_mass = f.mass;
+    s->mu = f.mu;
+    s->lam = f.lam;
     s->n_fem = s->n_blocks = static_cast<Index>(f.mesh.verts.size());
     s->keys.reserve(f.mesh.verts.size() + 10 * f.mesh.tets.size());
     s->vals.reserve(9 * (f.mesh.verts.size() + 10 * f.mesh.tets.size()));
@@ -542,10 +552,11 @@ Scene* abd_stack(int bx, int by, int bz, unsigned seed) {  // cfg3
     return contact_scene(fems, bodies, 0.01, nb, 20, seed);
 }
 
-Scene* hybrid(int n_soft, int soft_res, int n_gears, int gear_res, int stencils_per_pair, unsigned seed) {  // cfg4
+Scene* hybrid(int n_soft, int soft_res, int n_gears, int gear_res, int stencils_per_pair, double E,
+              unsigned seed) {  // cfg4
     std::vector<FemPart> fems;
     std::vector<Body> bodies;
-    const double E = 1e5, nu = 0.3;
+    const double nu = 0.3;
     for (int f = 0; f < n_soft; ++f)
         fems.push_back(FemPart{make_box_tets(soft_res, soft_res, soft_res, 0.2, 0.2, 0.2), 0, E / (2 * (1 + nu)),
                                E * nu / ((1 + nu) * (1 - 2 * nu)), 1000.0, {}});
@@ -572,10 +583,26 @@ void* adipc_scene_fem_box(int nx, int ny, int nz, double sx, double sy, double s
 }
 void* adipc_scene_cloth(int nx, int ny, double sx, double sy, unsigned seed) { return cloth(nx, ny, sx, sy, seed); }
 void* adipc_scene_abd_stack(int bx, int by, int bz, unsigned seed) { return abd_stack(bx, by, bz, seed); }
-void* adipc_scene_hybrid(int n_soft, int soft_res, int n_gears, int gear_res, int stencils_per_pair, unsigned seed) {
-    return hybrid(n_soft, soft_res, n_gears, gear_res, stencils_per_pair, seed);
+void* adipc_scene_hybrid(int n_soft, int soft_res, int n_gears, int gear_res, int stencils_per_pair, double E,
+                         unsigned seed) {
+    return hybrid(n_soft, soft_res, n_gears, gear_res, stencils_per_pair, E, seed);
 }
 void adipc_scene_free(void* s) { delete static_cast<Scene*>(s); }
+
+// the solid mesh of a FEM-only scene: out = {n_verts, n_tets}; mat = {mu, lambda}
+void adipc_scene_mesh_sizes(void* sp, std::int64_t* out, double* mat) {
+    const Scene& s = *static_cast<Scene*>(sp);
+    out[0] = static_cast<std::int64_t>(s.mesh_mass.size());
+    out[1] = static_cast<std::int64_t>(s.mesh_tets.size() / 4);
+    mat[0] = s.mu;
+    mat[1] = s.lam;
+}
+void adipc_scene_copy_mesh(void* sp, double* verts, std::int32_t* tets, double* mass) {
+    const Scene& s = *static_cast<Scene*>(sp);
+    if (!s.mesh_verts.empty()) std::memcpy(verts, s.mesh_verts.data(), 8 * s.mesh_verts.size());
+    if (!s.mesh_tets.empty()) std::memcpy(tets, s.mesh_tets.data(), 4 * s.mesh_tets.size());
+    if (!s.mesh_mass.empty()) std::memcpy(mass, s.mesh_mass.data(), 8 * s.mesh_mass.size());
+}
 
 // out: n_blocks, n_fem, n_bodies, n_abd_nodes, T, Tn, n_rest_edges
 void adipc_scene_sizes(void* sp, std::int64_t* out) {

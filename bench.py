@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--no-solve-order", action="store_true",
                     help="run the MAS/PCG in the reference slot numbering (A/B of the solve-order renumbering)")
     ap.add_argument("--cpu-iters", type=int, default=10, help="PCG iterations per CPU sample step")
+    ap.add_argument("--no-producer", action="store_true", help="skip the device element-Hessian producer timing")
     ap.add_argument("--no-hybrid", action="store_true",
                     help="skip the cfg4_hybrid_1m Newton-solve line (the north star's ~1M-DOF hybrid scene)")
     ap.add_argument("--selftest", action="store_true",
@@ -622,6 +623,10 @@ def run_ours(args, rank, world, local_rank, dist):
                                    "source": "tools/stream_read_bench.cu"},
             "clocks": clk.summary(),
         }
+    if not args.no_producer and args.config == "cfg5_stiff_box" and len(sc.tets):
+        pr = producer_gpu(args, ctx, sc, d_b, stream, dev)
+        if rank == 0:
+            out["producer"] = pr
     # e2e through the host-pointer C-ABI (pinned host buffers)
     if not args.no_e2e:
         e2e = run_e2e(args, ctx, sc, d_b, stream, dev)
@@ -639,6 +644,79 @@ def run_ours(args, rank, world, local_rank, dist):
                                   "+ adipc_gpu_pcg (host pointers, pinned)"}
     ctx.close()
     return out, sc
+
+
+def producer_gpu(args, ctx, sc, d_b, stream, dev):
+    """§8f #1 on the benchmarked scene: the device element-Hessian producer
+    (inertia + stable Neo-Hookean stencils + PSD projection, emission in the
+    reference's order, energy.cu) replaces the host triplet stream. Times the
+    producer alone, the whole assemble() (produce + filter + sort + reduce),
+    and a whole Newton linear solve from HOST positions (H2D of x, assemble,
+    MAS build, PCG, D2H of the direction): the PCIe traffic per Newton
+    iteration drops from the 1.54 GB stream to two position vectors."""
+    import torch
+
+    from paper_2411_06224_b200 import _lib
+    import scenegen as S
+
+    inv9, vol = S.tet_rest_data(sc.verts, sc.tets)
+    n, nt = len(sc.mass), len(sc.tets)
+    with torch.cuda.stream(stream):
+        mesh = {"mass": torch.from_numpy(sc.mass).to(dev), "tets": torch.from_numpy(sc.tets).to(dev),
+                "rest_inv9": torch.from_numpy(inv9).to(dev), "rest_volume": torch.from_numpy(vol).to(dev),
+                "tet_begin": [0, nt], "mu": [sc.mu], "lam": [sc.lam]}
+        d_pin = torch.from_numpy(sc.pinned).to(dev)
+        d_xt = torch.from_numpy(S.inertial_target(sc)).to(dev)
+        d_x = torch.from_numpy(np.ascontiguousarray(sc.verts.reshape(-1))).to(dev)
+        keys = torch.empty(n + 10 * nt, dtype=torch.int64, device=dev)
+        vals = torch.empty((n + 10 * nt, 9), dtype=torch.float64, device=dev)
+        grad = torch.empty(3 * n, dtype=torch.float64, device=dev)
+        d_dir = torch.empty(3 * n, dtype=torch.float64, device=dev)
+        d_rhs = torch.empty(3 * n, dtype=torch.float64, device=dev)
+    stream.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(reps):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) / reps
+
+    emit_ms = timed(lambda: ctx.fem_emit(mesh, d_x, d_xt, 1e-4, keys, vals, grad, pinned=d_pin), args.steps)
+    asm_ms = timed(lambda: ctx.fem_assemble(mesh, d_x, d_xt, 1e-4, grad, pinned=d_pin), args.steps)
+    # whole Newton linear solve from host positions: x in, direction out
+    h_x = torch.from_numpy(np.ascontiguousarray(sc.verts.reshape(-1))).pin_memory()
+    h_dir = torch.empty(3 * n, dtype=torch.float64).pin_memory()
+
+    def newton():
+        with torch.cuda.stream(stream):
+            d_x.copy_(h_x, non_blocking=True)
+            ctx.fem_assemble(mesh, d_x, d_xt, 1e-4, grad, pinned=d_pin)
+            ctx.build_preconditioner(_lib.PRECOND_MAS)
+            torch.neg(grad, out=d_rhs)
+            _, res = ctx.pcg(d_rhs, REL_TOL, RESTART, MAX_ITERS, x=d_dir)
+            h_dir.copy_(d_dir, non_blocking=True)
+        stream.synchronize()
+        return res.iters
+
+    newton()
+    t0 = time.perf_counter()
+    iters = sum(newton() for _ in range(args.steps))
+    newton_ms = (time.perf_counter() - t0) * 1000.0 / args.steps
+    return {"what": "device element-Hessian producer (SURVEY 8f #1): inertia + 1,886,592 stable Neo-Hookean stencils "
+                    "with PSD projection, stream in the reference's emission order",
+            "tets": nt, "stream_entries": n + 10 * nt, "fem_emit_ms": emit_ms, "fem_assemble_ms": asm_ms,
+            "stream_bytes_written": 80 * (n + 10 * nt),
+            "emit_write_gbs": 80 * (n + 10 * nt) / (emit_ms / 1e3) / 1e9,
+            "newton_solve_from_host_positions_ms": newton_ms, "pcg_iters_per_solve": iters / args.steps,
+            "e2e_pcg_iters_per_s": iters / (newton_ms * args.steps / 1e3),
+            "h2d_bytes_per_step": 3 * n * 8, "d2h_bytes_per_step": 3 * n * 8,
+            "path": "H2D x + adipc_gpu_fem_assemble_device + adipc_gpu_build_preconditioner + adipc_gpu_pcg_device "
+                    "+ D2H direction"}
 
 
 def run_e2e(args, ctx, sc, d_b, stream, dev):

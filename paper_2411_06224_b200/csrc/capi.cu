@@ -181,10 +181,10 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.l1_keys.free();
     c.graph_deg.free();
     c.graph_adj.free();
-    c.graph_adj2.free();
     c.graph_ptr.free();
-    c.graph_cur.free();
-    c.graph_ptr2.free();
+    c.fem_keys.free();
+    c.fem_vals.free();
+    c.fem_value.free();
     c.perm.free();
     c.perm_keys.free();
     c.as_src.free();

@@ -151,8 +151,8 @@ struct Ctx {
     PcgWork w;
     DBuf<unsigned long long> step_max;  // step_inf_norm result (step.cu)
     // level-0 graph of the cold hierarchy build (block_edges + build_graph on the device)
-    DBuf<std::int32_t> graph_deg, graph_adj, graph_adj2;
-    DBuf<std::int64_t> graph_ptr, graph_cur, graph_ptr2;
+    DBuf<std::int32_t> graph_deg, graph_adj;
+    DBuf<std::int64_t> graph_ptr;
 
     // Solve order (MAS): the PCG and the preconditioner run on A renumbered so
     // that every level-0 subdomain is a contiguous slot range,

@@ -905,54 +905,61 @@ namespace {
 // straight from the device matrix's pattern: node i's neighbours are the
 // off-diagonal blocks of row i and of column i (block_edges, mas.hpp:19-25),
 // every list sorted ascending and duplicate-free, as std::set-per-node makes
-// them. Degree count and scatter with atomics, then one thread per node
-// insertion-sorts its (short) list and drops repeats.
-__global__ void k_graph_deg(const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,
-                            std::int64_t U, std::int32_t* __restrict__ deg) {
+// them. Both directions of every entry become a key (a << 32 | b) for the
+// assembly's bucket sort (any row length: contact scenes give affine-body
+// rows tens of thousands of neighbours), then per row the unique
+// neighbours without the node itself are counted and emitted.
+__global__ void k_graph_keys(const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,
+                             std::int64_t U, std::uint64_t* __restrict__ keys) {
     for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < U;
          e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const std::uint32_t r = rows[e], c = cols[e];
-        if (r == c) continue;
-        atomicAdd(deg + r, 1);
-        atomicAdd(deg + c, 1);
+        const std::uint64_t r = rows[e], c = cols[e];
+        keys[2 * e] = r << 32 | c;  // a diagonal entry gives self keys, dropped below
+        keys[2 * e + 1] = c << 32 | r;
     }
 }
 
-__global__ void k_graph_fill(const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,
-                             std::int64_t U, unsigned long long* __restrict__ cur, std::int32_t* __restrict__ adj) {
-    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < U;
-         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const std::uint32_t r = rows[e], c = cols[e];
-        if (r == c) continue;
-        adj[atomicAdd(cur + r, 1ull)] = static_cast<std::int32_t>(c);
-        adj[atomicAdd(cur + c, 1ull)] = static_cast<std::int32_t>(r);
-    }
-}
-
-__global__ void k_graph_sort(std::int32_t n, const std::int64_t* __restrict__ ptr, std::int32_t* __restrict__ adj,
-                             std::int32_t* __restrict__ ulen) {
-    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        std::int32_t* a = adj + ptr[i];
-        const std::int64_t d = ptr[i + 1] - ptr[i];
-        for (std::int64_t k = 1; k < d; ++k) {
-            const std::int32_t v = a[k];
-            std::int64_t j = k - 1;
-            for (; j >= 0 && a[j] > v; --j) a[j + 1] = a[j];
-            a[j + 1] = v;
+// per row of the bucket sort: unique neighbour count without the row itself
+// (one warp per row: rows of affine bodies in contact scenes are long)
+__global__ void k_adj_count(std::int32_t n, const std::uint64_t* __restrict__ sorted,
+                            const std::int64_t* __restrict__ row_start, std::int32_t* __restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    for (std::int64_t r = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5; r < n;
+         r += (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const std::int64_t b = row_start[r], e = row_start[r + 1];
+        int u = 0;
+        for (std::int64_t q = b + lane; q < e; q += 32) {
+            const std::uint32_t v = static_cast<std::uint32_t>(sorted[q] >> 32);
+            const bool head = q == b || static_cast<std::uint32_t>(sorted[q - 1] >> 32) != v;
+            u += (head && v != static_cast<std::uint32_t>(r)) ? 1 : 0;
         }
-        std::int32_t u = d > 0 ? 1 : 0;
-        for (std::int64_t k = 1; k < d; ++k)
-            if (a[k] != a[u - 1]) a[u++] = a[k];
-        ulen[i] = u;
+        for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+        if (lane == 0) cnt[r] = u;
     }
 }
 
-__global__ void k_graph_compact(std::int32_t n, const std::int64_t* __restrict__ ptr, const std::int32_t* __restrict__ adj,
-                                const std::int64_t* __restrict__ ptr2, std::int32_t* __restrict__ adj2) {
-    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
-        for (std::int64_t k = 0; k < ptr2[i + 1] - ptr2[i]; ++k) adj2[ptr2[i] + k] = adj[ptr[i] + k];
+__global__ void k_adj_emit(std::int32_t n, const std::uint64_t* __restrict__ sorted,
+                           const std::int64_t* __restrict__ row_start, const std::int64_t* __restrict__ ptr,
+                           std::int32_t* __restrict__ adj) {
+    const int lane = threadIdx.x & 31;
+    for (std::int64_t r = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5; r < n;
+         r += (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const std::int64_t b = row_start[r], e = row_start[r + 1];
+        std::int64_t o = ptr[r];
+        for (std::int64_t q0 = b; q0 < e; q0 += 32) {
+            const std::int64_t q = q0 + lane;
+            std::uint32_t v = 0;
+            bool keep = false;
+            if (q < e) {
+                v = static_cast<std::uint32_t>(sorted[q] >> 32);
+                keep = (q == b || static_cast<std::uint32_t>(sorted[q - 1] >> 32) != v) &&
+                       v != static_cast<std::uint32_t>(r);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) adj[o + __popc(m & ((1u << lane) - 1u))] = static_cast<std::int32_t>(v);
+            o += __popc(m);
+        }
+    }
 }
 
 struct DeviceGraph {
@@ -965,12 +972,16 @@ DeviceGraph level0_graph_device(Ctx& c) {
     const DeviceMatrix& A = c.A;
     cudaStream_t st = c.stream;
     const std::int32_t n = A.n;
+    c.l1_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(2 * A.U, 1)));
+    if (A.U > 0) {
+        k_graph_keys<<<grid_for(A.U, 256, 16), 256, 0, st>>>(A.rows.p, A.cols.p, A.U, c.l1_keys.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    bucket_sort(c, c.l1_keys.p, 2 * A.U, n, nullptr);
     c.graph_deg.reserve(static_cast<std::size_t>(std::max(n, 1)));
     c.graph_ptr.reserve(static_cast<std::size_t>(n) + 1);
-    c.graph_cur.reserve(static_cast<std::size_t>(std::max(n, 1)));
-    ADIPC_CUDA(cudaMemsetAsync(c.graph_deg.p, 0, sizeof(std::int32_t) * std::max(n, 1), st));
-    if (A.U > 0) {
-        k_graph_deg<<<grid_for(A.U, 256, 16), 256, 0, st>>>(A.rows.p, A.cols.p, A.U, c.graph_deg.p);
+    if (n > 0) {
+        k_adj_count<<<grid_for(n, 8, 16), 256, 0, st>>>(n, c.sorted.p, c.row_start.p, c.graph_deg.p);
         ADIPC_LAUNCH_CHECK();
     }
     exclusive_scan(c.graph_deg.p, n, c.graph_ptr.p, c.scan_scratch, st);
@@ -978,33 +989,11 @@ DeviceGraph level0_graph_device(Ctx& c) {
     ADIPC_CUDA(cudaMemcpyAsync(&E, c.graph_ptr.p + n, sizeof(E), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaStreamSynchronize(st));
     c.graph_adj.reserve(static_cast<std::size_t>(std::max<std::int64_t>(E, 1)));
-    if (n > 0)
-        ADIPC_CUDA(cudaMemcpyAsync(c.graph_cur.p, c.graph_ptr.p, sizeof(std::int64_t) * n, cudaMemcpyDeviceToDevice, st));
-    if (A.U > 0 && E > 0) {
-        k_graph_fill<<<grid_for(A.U, 256, 16), 256, 0, st>>>(
-            A.rows.p, A.cols.p, A.U, reinterpret_cast<unsigned long long*>(c.graph_cur.p), c.graph_adj.p);
+    if (n > 0 && E > 0) {
+        k_adj_emit<<<grid_for(n, 8, 16), 256, 0, st>>>(n, c.sorted.p, c.row_start.p, c.graph_ptr.p, c.graph_adj.p);
         ADIPC_LAUNCH_CHECK();
     }
-    if (n > 0) {
-        k_graph_sort<<<grid_for(n, 128, 64), 128, 0, st>>>(n, c.graph_ptr.p, c.graph_adj.p, c.graph_deg.p);
-        ADIPC_LAUNCH_CHECK();
-    }
-    c.graph_ptr2.reserve(static_cast<std::size_t>(n) + 1);
-    exclusive_scan(c.graph_deg.p, n, c.graph_ptr2.p, c.scan_scratch, st);
-    std::int64_t E2 = 0;
-    ADIPC_CUDA(cudaMemcpyAsync(&E2, c.graph_ptr2.p + n, sizeof(E2), cudaMemcpyDeviceToHost, st));
-    ADIPC_CUDA(cudaStreamSynchronize(st));
-    const std::int32_t* adj = c.graph_adj.p;
-    const std::int64_t* ptr = c.graph_ptr.p;
-    if (E2 != E) {  // repeated pairs (not produced by a sorted unique pattern; kept for safety)
-        c.graph_adj2.reserve(static_cast<std::size_t>(std::max<std::int64_t>(E2, 1)));
-        k_graph_compact<<<grid_for(n, 128, 64), 128, 0, st>>>(n, c.graph_ptr.p, c.graph_adj.p, c.graph_ptr2.p,
-                                                             c.graph_adj2.p);
-        ADIPC_LAUNCH_CHECK();
-        adj = c.graph_adj2.p;
-        ptr = c.graph_ptr2.p;
-    }
-    return DeviceGraph{ptr, adj, E2};
+    return DeviceGraph{c.graph_ptr.p, c.graph_adj.p, E};
 }
 
 host::Graph graph_to_host(Ctx& c, const DeviceGraph& dg, std::int32_t n) {
@@ -1075,34 +1064,6 @@ __global__ void k_l1_keys(std::int32_t n, const std::int64_t* __restrict__ gptr,
     }
 }
 
-// per super node: unique neighbour count without itself (rows of the bucket sort)
-__global__ void k_l1_count(std::int32_t n1, const std::uint64_t* __restrict__ sorted,
-                           const std::int64_t* __restrict__ row_start, const std::int32_t* __restrict__ uniq_cnt,
-                           std::int32_t* __restrict__ cnt) {
-    for (std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; r < n1;
-         r += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        bool self = false;
-        for (std::int64_t q = row_start[r]; q < row_start[r + 1] && !self; ++q)
-            self = static_cast<std::uint32_t>(sorted[q] >> 32) == static_cast<std::uint32_t>(r);
-        cnt[r] = uniq_cnt[r] - (self ? 1 : 0);
-    }
-}
-
-__global__ void k_l1_emit(std::int32_t n1, const std::uint64_t* __restrict__ sorted,
-                          const std::int64_t* __restrict__ row_start, const std::int64_t* __restrict__ ptr1,
-                          std::int32_t* __restrict__ adj1) {
-    for (std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; r < n1;
-         r += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        std::int64_t o = ptr1[r];
-        std::uint32_t prev = 0xFFFFFFFFu;
-        for (std::int64_t q = row_start[r]; q < row_start[r + 1]; ++q) {
-            const std::uint32_t v = static_cast<std::uint32_t>(sorted[q] >> 32);
-            if (v != prev && v != static_cast<std::uint32_t>(r)) adj1[o++] = static_cast<std::int32_t>(v);
-            prev = v;
-        }
-    }
-}
-
 // Level 0 -> 1 on the device; false when a level-0 subdomain has more than 32
 // members (the host pass handles any size).
 bool level1_device(Ctx& c, const DeviceGraph& g0, std::vector<std::int32_t>& up1, std::int32_t& n1,
@@ -1150,14 +1111,14 @@ bool level1_device(Ctx& c, const DeviceGraph& g0, std::vector<std::int32_t>& up1
     bucket_sort(c, c.l1_keys.p, g0.E, n1, nullptr);
     c.l1_cnt.reserve(static_cast<std::size_t>(n1) + 1);
     c.l1_ptr.reserve(static_cast<std::size_t>(n1) + 1);
-    k_l1_count<<<grid_for(n1, 256, 16), 256, 0, st>>>(n1, c.sorted.p, c.row_start.p, c.uniq_cnt.p, c.l1_cnt.p);
+    k_adj_count<<<grid_for(n1, 8, 16), 256, 0, st>>>(n1, c.sorted.p, c.row_start.p, c.l1_cnt.p);
     ADIPC_LAUNCH_CHECK();
     exclusive_scan(c.l1_cnt.p, n1, c.l1_ptr.p, c.scan_scratch, st);
     std::int64_t E1 = 0;
     ADIPC_CUDA(cudaMemcpyAsync(&E1, c.l1_ptr.p + n1, sizeof(E1), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaStreamSynchronize(st));
     c.l1_adj.reserve(static_cast<std::size_t>(std::max<std::int64_t>(E1, 1)));
-    k_l1_emit<<<grid_for(n1, 256, 16), 256, 0, st>>>(n1, c.sorted.p, c.row_start.p, c.l1_ptr.p, c.l1_adj.p);
+    k_adj_emit<<<grid_for(n1, 8, 16), 256, 0, st>>>(n1, c.sorted.p, c.row_start.p, c.l1_ptr.p, c.l1_adj.p);
     ADIPC_LAUNCH_CHECK();
     g1 = graph_to_host(c, DeviceGraph{c.l1_ptr.p, c.l1_adj.p, E1}, n1);
     return true;

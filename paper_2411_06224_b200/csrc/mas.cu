@@ -393,6 +393,7 @@ __global__ void __launch_bounds__(128) k_invert_warp(InvertTable tab, int* __res
                 __syncwarp();  // column j complete before later columns read it
             }
             if (!fail) break;
+            __syncwarp();  // every lane's reads of the failed attempt before the next one rewrites S
         }
         if (fail) {
             if (lane == 0) atomicOr(status, 1);

@@ -195,14 +195,15 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, pair = w >> 1, half = w & 1;
     const int npc = blockDim.x >> 6;
     double* ring = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(pair) * kStages * slot_doubles;
-    // one b per pair: both warps write the same values into it after the
-    // pair barrier that ends the previous item, then read it after their own
-    // __syncwarp (no cross-warp dependency)
+    // b of the current item, one copy per warp: each warp writes its own
+    // after the pair barrier that ends the previous item and reads it after
+    // its __syncwarp (a copy shared by the pair had both warps store the same
+    // values concurrently with the other's reads: compute-sanitizer racecheck)
     double* bs = reinterpret_cast<double*>(smem) + static_cast<std::size_t>(npc) * kStages * slot_doubles +
-                 static_cast<std::size_t>(pair) * kK;
+                 static_cast<std::size_t>(2 * pair + half) * kK;
     std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(
                              reinterpret_cast<double*>(smem) + static_cast<std::size_t>(npc) * kStages * slot_doubles +
-                             static_cast<std::size_t>(npc) * kK) +
+                             static_cast<std::size_t>(2 * npc) * kK) +
                          pair * kStages;
     // every pair takes an even share of EACH level (a contiguous run per
     // level, level 0 first): the coarse items, cheap in bytes but with a
@@ -510,7 +511,7 @@ PcLaunch precond_launch(Ctx& c) {
     const int kk = matvec_cols(fill);
     L.slot = static_cast<int>(packed_doubles(kk));
     const int stages = c.l0_stages;
-    const std::size_t per_pair = (sizeof(double) * L.slot + sizeof(std::uint64_t)) * stages + sizeof(double) * kk;
+    const std::size_t per_pair = (sizeof(double) * L.slot + sizeof(std::uint64_t)) * stages + 2 * sizeof(double) * kk;
     L.pairs = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(c.pc_pairs, (113u * 1024u) / per_pair)));
     L.smem = per_pair * L.pairs;
     if (kk == 24)

@@ -3,6 +3,7 @@
 two-level contact device path), MAS build (solve order and reference
 numbering), block Jacobi, preconditioner apply, PCG (graphs + PDL) in the
 default and the deterministic mode, SpMV, the post-solve step kernels.
+the element-Hessian producer (fast and Jacobi paths) on the cfg1 mesh.
 Scenes: the soft cube (cfg1), the stiff beam, the ABD stack (cfg3).
 Usage: compute-sanitizer --tool <tool> python tools/sanitize_drive.py"""
 import os
@@ -45,4 +46,20 @@ for name in sys.argv[1:] or ["cfg1_soft_cube", "stiff_beam", "cfg3_abd_stack"]:
             c.apply_direction(st, d, 0.5, torch.empty_like(d))
             torch.cuda.synchronize()
             c.close()
+# the element-Hessian producer: at rest (PSD fast path) and deformed (Jacobi)
+sc = scenes.CONFIGS["cfg1_soft_cube"]()
+inv9, vol = scenes.tet_rest_data(sc.verts, sc.tets)
+mesh = {"mass": torch.from_numpy(sc.mass).cuda(), "tets": torch.from_numpy(sc.tets).cuda(),
+        "rest_inv9": torch.from_numpy(inv9).cuda(), "rest_volume": torch.from_numpy(vol).cuda(),
+        "tet_begin": [0, len(sc.tets)], "mu": [sc.mu], "lam": [sc.lam]}
+c = Context(0)
+xt = torch.from_numpy(scenes.inertial_target(sc)).cuda()
+pin = torch.from_numpy(sc.pinned).cuda()
+for scale in (0.0, 0.3):
+    x = sc.verts + np.random.default_rng(1).uniform(-scale, scale, sc.verts.shape) * 0.01
+    dx = torch.from_numpy(np.ascontiguousarray(x.reshape(-1))).cuda()
+    g = torch.empty_like(dx)
+    val, U = c.fem_assemble(mesh, dx, xt, 1e-4, g, pinned=pin)
+    print("fem_assemble", scale, val, U, flush=True)
+c.close()
 print("sanitize drive done")

@@ -195,6 +195,55 @@ int adipc_gpu_fem_emit_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* desc, ui
 int adipc_gpu_fem_assemble_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* desc, double* d_grad, double* value,
                                   int64_t* n_unique);
 
+
+/* ---- contact producers --------------------------------------
+ * The contact-node part of IncrementalPotential::assemble_contact
+ * (adipc/solver/incremental_potential.hpp:322-384) for given candidates:
+ * PT / EE barrier stencils (contact/distance.hpp:13-223, contact/barrier.hpp:
+ * 14-66, PSD-projected), the ground barrier (barrier.hpp:70-91) and lagged
+ * friction (contact/friction.hpp:12-91). The node stream comes out in the
+ * reference's emission order (active PT pairs, active EE pairs, ground
+ * contacts, friction constraints) and feeds adipc_gpu_assemble_contact_device.
+ * Device arrays over the contact-node universe (FEM vertices, then the body
+ * vertices: DofMap, sparse/abd_reduce.hpp:11-27); stencils are node ids —
+ * PT (v, t0, t1, t2), EE (a0, a1, b0, b1) — i.e. the broad phase's surface
+ * candidates (contact/broad_phase.hpp:146-211) resolved to nodes. */
+typedef struct adipc_contact_desc {
+    int32_t n_nodes;
+    const double* pos;          /* 3 per node */
+    int64_t n_pt;
+    const int32_t* pt;          /* 4 per PT stencil */
+    int64_t n_ee;
+    const int32_t* ee;          /* 4 per EE stencil */
+    double dhat, kappa;
+    int ground;                 /* GroundPlane::enabled */
+    double ground_normal[3];
+    double ground_height;
+    int32_t n_surf_verts;
+    const int32_t* surf_verts;  /* ContactSurface::verts as nodes */
+    int64_t n_friction;         /* FrictionConstraint arrays: */
+    const int32_t* fr_nodes;    /*   4 per constraint */
+    const int32_t* fr_n_nodes;
+    const double* fr_coeff;     /*   4 per constraint */
+    const double* fr_t1;        /*   3 per constraint */
+    const double* fr_t2;
+    const double* fr_lambda;
+    const double* fr_base;      /* 3 per node: positions at the step start */
+    double mu, fr_eps;
+} adipc_contact_desc;
+/* node stream (capacity >= 10 (n_pt + n_ee) + n_surf_verts + 10 n_friction
+ * entries), node gradient (3 n_nodes), value; *n_out = entries written */
+int adipc_gpu_contact_emit_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* desc, double dt2, int project,
+                                  uint64_t* d_node_keys, double* d_node_vals9, int64_t capacity, double* d_node_grad,
+                                  double* value, int64_t* n_out);
+/* the contact terms of IncrementalPotential::value (:133-157); +inf when a
+ * stencil or a surface vertex touches */
+int adipc_gpu_contact_value_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* desc, double dt2, double* value);
+/* scene_ccd_step over the given stencils (contact/ccd.hpp:17-110): the largest
+ * fraction of d_disp (3 per node) no stencil or surface vertex can cross */
+int adipc_gpu_ccd_step_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* desc, const double* d_disp,
+                              double* alpha);
+
 /* IncrementalPotential::filter_pinned (incremental_potential.hpp:410-425):
  * drop blocks touching a pinned slot, append I3 per pinned slot.
  * out capacity >= T + n_slots. */

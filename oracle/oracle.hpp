@@ -22,6 +22,8 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
+#include <limits>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -1138,6 +1140,588 @@ inline Real ip_fem_assemble(const std::vector<Vec3>& x, const std::vector<Vec3>&
         if (pinned[v])
             for (int k = 0; k < 3; ++k) grad[3 * v + k] = 0;
     return val;
+}
+
+// ---------------------------------------------------------------------------
+// Contact producers: closest-feature classification and
+// per-feature squared distances with first and second derivatives
+// (contact/distance.hpp:13-209, forward-mode AD of core/dual2.hpp restated),
+// the log barrier (contact/barrier.hpp:14-91), lagged friction
+// (contact/friction.hpp:12-91) and the contact-node part of
+// IncrementalPotential::assemble_contact (solver/incremental_potential.hpp:
+// 322-384); the line-search value (:61-159, contact terms) and the
+// conservative-advancement CCD (contact/ccd.hpp:17-110).
+
+// core/dual2.hpp:11-86 (N = 12; Hessian dense column-major as Eigen stores it)
+struct Dual12 {
+    Real v = 0;
+    Real g[12] = {};
+    Real h[144] = {};
+    Dual12() = default;
+    explicit Dual12(Real c) : v(c) {}
+    static Dual12 variable(Real value, int k) {
+        Dual12 d(value);
+        d.g[k] = 1;
+        return d;
+    }
+};
+inline Dual12 operator+(const Dual12& a, const Dual12& b) {
+    Dual12 r(a.v + b.v);
+    for (int i = 0; i < 12; ++i) r.g[i] = a.g[i] + b.g[i];
+    for (int i = 0; i < 144; ++i) r.h[i] = a.h[i] + b.h[i];
+    return r;
+}
+inline Dual12 operator-(const Dual12& a, const Dual12& b) {
+    Dual12 r(a.v - b.v);
+    for (int i = 0; i < 12; ++i) r.g[i] = a.g[i] - b.g[i];
+    for (int i = 0; i < 144; ++i) r.h[i] = a.h[i] - b.h[i];
+    return r;
+}
+inline Dual12 operator*(const Dual12& a, const Dual12& b) {
+    Dual12 r(a.v * b.v);
+    for (int i = 0; i < 12; ++i) r.g[i] = a.g[i] * b.v + b.g[i] * a.v;
+    for (int j = 0; j < 12; ++j)
+        for (int i = 0; i < 12; ++i)
+            r.h[12 * j + i] = a.h[12 * j + i] * b.v + b.h[12 * j + i] * a.v + a.g[i] * b.g[j] + b.g[i] * a.g[j];
+    return r;
+}
+inline Dual12 inverse(const Dual12& b) {
+    const Real iv = 1.0 / b.v;
+    Dual12 r(iv);
+    for (int i = 0; i < 12; ++i) r.g[i] = -b.g[i] * (iv * iv);
+    const Real c = 2 * iv * iv * iv;
+    for (int j = 0; j < 12; ++j)
+        for (int i = 0; i < 12; ++i) r.h[12 * j + i] = -b.h[12 * j + i] * (iv * iv) + (c * b.g[i]) * b.g[j];
+    return r;
+}
+inline Dual12 operator/(const Dual12& a, const Dual12& b) { return a * inverse(b); }
+
+template <class T>
+using G3 = std::array<T, 3>;
+template <class T>
+G3<T> gsub(const G3<T>& a, const G3<T>& b) {
+    return {a[0] - b[0], a[1] - b[1], a[2] - b[2]};
+}
+template <class T>
+T gdot(const G3<T>& a, const G3<T>& b) {
+    return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+}
+template <class T>
+G3<T> gcross(const G3<T>& a, const G3<T>& b) {
+    return {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+}
+template <class T>
+T gnorm2(const G3<T>& a) {
+    return gdot(a, a);
+}
+// distance.hpp:111-140
+template <class T>
+T pp_dist2_g(const G3<T>& a, const G3<T>& b) {
+    return gnorm2(gsub(a, b));
+}
+template <class T>
+T pe_dist2_g(const G3<T>& p, const G3<T>& e0, const G3<T>& e1) {
+    const G3<T> d = gsub(e1, e0);
+    const G3<T> w = gsub(p, e0);
+    return gnorm2(gcross(w, d)) / gnorm2(d);
+}
+template <class T>
+T pt_plane_dist2_g(const G3<T>& p, const G3<T>& t0, const G3<T>& t1, const G3<T>& t2) {
+    const G3<T> n = gcross(gsub(t1, t0), gsub(t2, t0));
+    const T h = gdot(gsub(p, t0), n);
+    return h * h / gnorm2(n);
+}
+template <class T>
+T ee_line_dist2_g(const G3<T>& a0, const G3<T>& a1, const G3<T>& b0, const G3<T>& b1) {
+    const G3<T> n = gcross(gsub(a1, a0), gsub(b1, b0));
+    const T h = gdot(gsub(b0, a0), n);
+    return h * h / gnorm2(n);
+}
+
+inline Real dot3(const Vec3& a, const Vec3& b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+inline Vec3 sub3(const Vec3& a, const Vec3& b) {
+    Vec3 c;
+    for (int k = 0; k < 3; ++k) c[k] = a[k] - b[k];
+    return c;
+}
+
+// distance.hpp:13-108
+enum class PtRegion { V0, V1, V2, E01, E12, E20, Interior };
+enum class EeRegion { A0B0, A0B1, A1B0, A1B1, A0Int, A1Int, IntB0, IntB1, Interior };
+struct PtClass {
+    PtRegion region;
+    Real beta[3];
+};
+struct EeClass {
+    EeRegion region;
+    Real s = 0, t = 0;
+};
+inline PtClass classify_pt(const Vec3& p, const Vec3& t0, const Vec3& t1, const Vec3& t2) {
+    const Vec3 ab = sub3(t1, t0), ac = sub3(t2, t0), ap = sub3(p, t0);
+    const Real d1 = dot3(ab, ap), d2 = dot3(ac, ap);
+    if (d1 <= 0 && d2 <= 0) return {PtRegion::V0, {1, 0, 0}};
+    const Vec3 bp = sub3(p, t1);
+    const Real d3 = dot3(ab, bp), d4 = dot3(ac, bp);
+    if (d3 >= 0 && d4 <= d3) return {PtRegion::V1, {0, 1, 0}};
+    const Real vc = d1 * d4 - d3 * d2;
+    if (vc <= 0 && d1 >= 0 && d3 <= 0) {
+        const Real v = d1 / (d1 - d3);
+        return {PtRegion::E01, {1 - v, v, 0}};
+    }
+    const Vec3 cp = sub3(p, t2);
+    const Real d5 = dot3(ab, cp), d6 = dot3(ac, cp);
+    if (d6 >= 0 && d5 <= d6) return {PtRegion::V2, {0, 0, 1}};
+    const Real vb = d5 * d2 - d1 * d6;
+    if (vb <= 0 && d2 >= 0 && d6 <= 0) {
+        const Real w = d2 / (d2 - d6);
+        return {PtRegion::E20, {1 - w, 0, w}};
+    }
+    const Real va = d3 * d6 - d5 * d4;
+    if (va <= 0 && d4 - d3 >= 0 && d5 - d6 >= 0) {
+        const Real w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        return {PtRegion::E12, {0, 1 - w, w}};
+    }
+    const Real denom = 1.0 / (va + vb + vc);
+    const Real v = vb * denom, w = vc * denom;
+    return {PtRegion::Interior, {1 - v - w, v, w}};
+}
+inline EeClass classify_ee(const Vec3& a0, const Vec3& a1, const Vec3& b0, const Vec3& b1) {
+    const Vec3 da = sub3(a1, a0), db = sub3(b1, b0), r = sub3(a0, b0);
+    const Real a = dot3(da, da), e = dot3(db, db);
+    const Real f = dot3(db, r), c = dot3(da, r), b = dot3(da, db);
+    const Real denom = a * e - b * b;
+    Real s = 0;
+    bool s_interior_formula = false;
+    if (denom > 1e-12 * a * e) {
+        s = (b * f - c * e) / denom;
+        if (s <= 0)
+            s = 0;
+        else if (s >= 1)
+            s = 1;
+        else
+            s_interior_formula = true;
+    }
+    Real t = e > 0 ? (b * s + f) / e : 0;
+    bool t_clamped = false;
+    if (t <= 0) {
+        t = 0;
+        t_clamped = true;
+    } else if (t >= 1) {
+        t = 1;
+        t_clamped = true;
+    }
+    if (t_clamped) {
+        s = a > 0 ? (b * t - c) / a : 0;
+        s_interior_formula = s > 0 && s < 1;
+        if (s <= 0)
+            s = 0;
+        else if (s >= 1)
+            s = 1;
+    }
+    const bool s_end = !s_interior_formula;
+    const bool t_end = t == 0 || t == 1;
+    EeClass out;
+    out.s = s;
+    out.t = t;
+    if (s_end && t_end)
+        out.region = s == 0 ? (t == 0 ? EeRegion::A0B0 : EeRegion::A0B1) : (t == 0 ? EeRegion::A1B0 : EeRegion::A1B1);
+    else if (s_end)
+        out.region = s == 0 ? EeRegion::A0Int : EeRegion::A1Int;
+    else if (t_end)
+        out.region = t == 0 ? EeRegion::IntB0 : EeRegion::IntB1;
+    else
+        out.region = EeRegion::Interior;
+    return out;
+}
+// distance.hpp:144-155 (value paths for ccd and the line-search value)
+inline Real pt_dist2(const Vec3& p, const Vec3& t0, const Vec3& t1, const Vec3& t2) {
+    const PtClass c = classify_pt(p, t0, t1, t2);
+    Vec3 cl, d;
+    for (int k = 0; k < 3; ++k) cl[k] = c.beta[0] * t0[k] + c.beta[1] * t1[k] + c.beta[2] * t2[k];
+    d = sub3(p, cl);
+    return dot3(d, d);
+}
+inline Real ee_dist2(const Vec3& a0, const Vec3& a1, const Vec3& b0, const Vec3& b1) {
+    const EeClass c = classify_ee(a0, a1, b0, b1);
+    Vec3 pa, pb;
+    for (int k = 0; k < 3; ++k) {
+        pa[k] = a0[k] + c.s * (a1[k] - a0[k]);
+        pb[k] = b0[k] + c.t * (b1[k] - b0[k]);
+    }
+    const Vec3 d = sub3(pa, pb);
+    return dot3(d, d);
+}
+
+// distance.hpp:159-223: squared distance of the active feature with its
+// derivatives over the stacked stencil (12 dofs)
+struct PairDerivs {
+    Real dist2 = 0;
+    Real grad[12] = {};
+    Real hess[144] = {};
+};
+inline G3<Dual12> dual_point(const Vec3& p, int k0) {
+    return {Dual12::variable(p[0], k0), Dual12::variable(p[1], k0 + 1), Dual12::variable(p[2], k0 + 2)};
+}
+inline PairDerivs pack_pair(const Dual12& d) {
+    PairDerivs o;
+    o.dist2 = d.v;
+    for (int i = 0; i < 12; ++i) o.grad[i] = d.g[i];
+    for (int i = 0; i < 144; ++i) o.hess[i] = d.h[i];
+    return o;
+}
+inline PairDerivs pt_dist2_derivs(const Vec3& p, const Vec3& t0, const Vec3& t1, const Vec3& t2) {
+    const PtClass c = classify_pt(p, t0, t1, t2);
+    const auto P = dual_point(p, 0), T0 = dual_point(t0, 3), T1 = dual_point(t1, 6), T2 = dual_point(t2, 9);
+    Dual12 d2;
+    switch (c.region) {
+        case PtRegion::V0: d2 = pp_dist2_g(P, T0); break;
+        case PtRegion::V1: d2 = pp_dist2_g(P, T1); break;
+        case PtRegion::V2: d2 = pp_dist2_g(P, T2); break;
+        case PtRegion::E01: d2 = pe_dist2_g(P, T0, T1); break;
+        case PtRegion::E12: d2 = pe_dist2_g(P, T1, T2); break;
+        case PtRegion::E20: d2 = pe_dist2_g(P, T2, T0); break;
+        case PtRegion::Interior: d2 = pt_plane_dist2_g(P, T0, T1, T2); break;
+    }
+    return pack_pair(d2);
+}
+inline PairDerivs ee_dist2_derivs(const Vec3& a0, const Vec3& a1, const Vec3& b0, const Vec3& b1) {
+    const EeClass c = classify_ee(a0, a1, b0, b1);
+    const auto A0 = dual_point(a0, 0), A1 = dual_point(a1, 3), B0 = dual_point(b0, 6), B1 = dual_point(b1, 9);
+    Dual12 d2;
+    switch (c.region) {
+        case EeRegion::A0B0: d2 = pp_dist2_g(A0, B0); break;
+        case EeRegion::A0B1: d2 = pp_dist2_g(A0, B1); break;
+        case EeRegion::A1B0: d2 = pp_dist2_g(A1, B0); break;
+        case EeRegion::A1B1: d2 = pp_dist2_g(A1, B1); break;
+        case EeRegion::A0Int: d2 = pe_dist2_g(A0, B0, B1); break;
+        case EeRegion::A1Int: d2 = pe_dist2_g(A1, B0, B1); break;
+        case EeRegion::IntB0: d2 = pe_dist2_g(B0, A0, A1); break;
+        case EeRegion::IntB1: d2 = pe_dist2_g(B1, A0, A1); break;
+        case EeRegion::Interior: d2 = ee_line_dist2_g(A0, A1, B0, B1); break;
+    }
+    return pack_pair(d2);
+}
+
+// barrier.hpp:14-31
+inline Real barrier_value(Real s, Real shat, Real kappa) {
+    if (s >= shat) return 0;
+    const Real r = s - shat;
+    return -kappa * r * r * std::log(s / shat);
+}
+inline Real barrier_d1(Real s, Real shat, Real kappa) {
+    if (s >= shat) return 0;
+    const Real r = s - shat;
+    return -kappa * (2 * r * std::log(s / shat) + r * r / s);
+}
+inline Real barrier_d2(Real s, Real shat, Real kappa) {
+    if (s >= shat) return 0;
+    const Real r = s - shat;
+    return -kappa * (2 * std::log(s / shat) + 4 * r / s - r * r / (s * s));
+}
+inline Real barrier_curvature_in_d(Real d, Real dhat, Real kappa) {  // barrier.hpp:35-39
+    const Real s = d * d;
+    return 4 * s * barrier_d2(s, dhat * dhat, kappa) + 2 * barrier_d1(s, dhat * dhat, kappa);
+}
+// barrier.hpp:50-66
+struct BarrierDerivs {
+    Real value = 0;
+    Real grad[12] = {};
+    Real hess[144] = {};
+};
+inline BarrierDerivs barrier_pair_derivs(const PairDerivs& d, Real shat, Real kappa, bool project = true) {
+    BarrierDerivs out;
+    if (d.dist2 >= shat) return out;
+    const Real b1 = barrier_d1(d.dist2, shat, kappa);
+    const Real b2 = barrier_d2(d.dist2, shat, kappa);
+    out.value = barrier_value(d.dist2, shat, kappa);
+    for (int i = 0; i < 12; ++i) out.grad[i] = b1 * d.grad[i];
+    for (int j = 0; j < 12; ++j)
+        for (int i = 0; i < 12; ++i) out.hess[12 * j + i] = b2 * (d.grad[i] * d.grad[j]) + b1 * d.hess[12 * j + i];
+    if (project) {
+        Real P[144];
+        oracle_eig::project_psd(12, out.hess, P);
+        for (int k = 0; k < 144; ++k) out.hess[k] = P[k];
+    }
+    return out;
+}
+// barrier.hpp:70-91
+struct GroundDerivs {
+    Real value = 0;
+    Vec3 grad;
+    Mat3 hess;
+    Real dist = 0;
+};
+inline GroundDerivs ground_barrier_derivs(const Vec3& x, const Vec3& normal, Real height, Real dhat, Real kappa,
+                                          bool project = true) {
+    GroundDerivs out;
+    out.dist = dot3(normal, x) - height;
+    const Real s = out.dist * out.dist;
+    const Real shat = dhat * dhat;
+    if (out.dist <= 0 || s >= shat) return out;
+    out.value = barrier_value(s, shat, kappa);
+    const Real gs = barrier_d1(s, shat, kappa) * 2 * out.dist;
+    for (int k = 0; k < 3; ++k) out.grad[k] = gs * normal[k];
+    Real c = barrier_curvature_in_d(out.dist, dhat, kappa);
+    if (project && c < 0) c = 0;
+    for (int j = 0; j < 3; ++j)
+        for (int i = 0; i < 3; ++i) out.hess(i, j) = (c * normal[i]) * normal[j];
+    return out;
+}
+
+// friction.hpp:12-36
+inline Real friction_f0(Real y, Real eps) {
+    if (y >= eps) return y;
+    return -y * y * y / (3 * eps * eps) + y * y / eps + eps / 3;
+}
+inline Real friction_f1(Real y, Real eps) {
+    if (y >= eps) return 1;
+    return y * (2 * eps - y) / (eps * eps);
+}
+inline Real friction_f1_over_y(Real y, Real eps) {
+    if (y >= eps) return 1 / y;
+    return (2 * eps - y) / (eps * eps);
+}
+inline Real friction_f2(Real y, Real eps) {
+    if (y >= eps) return 0;
+    return 2 * (eps - y) / (eps * eps);
+}
+// friction.hpp:38-44
+struct FrictionConstraint {
+    Index nodes[4] = {kInvalid, kInvalid, kInvalid, kInvalid};
+    int n_nodes = 0;
+    Real coeff[4] = {0, 0, 0, 0};
+    Vec3 t1, t2;
+    Real lambda = 0;
+};
+// friction.hpp:58-91
+struct FrictionDerivs {
+    Real value = 0;
+    Real grad[12] = {};
+    Real hess[144] = {};
+};
+inline FrictionDerivs friction_derivs(const FrictionConstraint& c, const Vec3* dx, Real mu, Real eps) {
+    FrictionDerivs out;
+    Vec3 w;
+    for (int k = 0; k < c.n_nodes; ++k)
+        for (int a = 0; a < 3; ++a) w[a] += c.coeff[k] * dx[k][a];
+    const Real u0 = dot3(c.t1, w), u1 = dot3(c.t2, w);
+    const Real y = std::sqrt(u0 * u0 + u1 * u1);
+    const Real scale = mu * c.lambda;
+    out.value = scale * friction_f0(y, eps);
+    Real inner[4];  // 2x2 column-major
+    Vec3 gw;
+    if (y > 1e-14 * eps) {
+        const Real h0 = u0 / y, h1 = u1 / y;
+        const Real f1 = scale * friction_f1(y, eps);
+        for (int a = 0; a < 3; ++a) gw[a] = f1 * (c.t1[a] * h0 + c.t2[a] * h1);
+        const Real f2 = friction_f2(y, eps), fy = friction_f1_over_y(y, eps);
+        inner[0] = scale * (f2 * (h0 * h0) + fy * (1 - h0 * h0));
+        inner[1] = scale * (f2 * (h1 * h0) + fy * (0 - h1 * h0));
+        inner[2] = scale * (f2 * (h0 * h1) + fy * (0 - h0 * h1));
+        inner[3] = scale * (f2 * (h1 * h1) + fy * (1 - h1 * h1));
+    } else {
+        const Real fy = scale * friction_f1_over_y(0, eps);
+        inner[0] = fy, inner[1] = 0, inner[2] = 0, inner[3] = fy;
+    }
+    Mat3 hw;  // P inner P^T, P = [t1 t2]
+    for (int j = 0; j < 3; ++j)
+        for (int i = 0; i < 3; ++i) {
+            const Real pi0 = c.t1[i], pi1 = c.t2[i];
+            const Real q0 = inner[0] * c.t1[j] + inner[2] * c.t2[j];
+            const Real q1 = inner[1] * c.t1[j] + inner[3] * c.t2[j];
+            hw(i, j) = pi0 * q0 + pi1 * q1;
+        }
+    for (int k = 0; k < c.n_nodes; ++k) {
+        for (int a = 0; a < 3; ++a) out.grad[3 * k + a] = c.coeff[k] * gw[a];
+        for (int l = 0; l < c.n_nodes; ++l)
+            for (int b = 0; b < 3; ++b)
+                for (int a = 0; a < 3; ++a)
+                    out.hess[12 * (3 * l + b) + 3 * k + a] = c.coeff[k] * c.coeff[l] * hw(a, b);
+    }
+    return out;
+}
+
+// The contact-node part of IncrementalPotential::assemble_contact
+// (incremental_potential.hpp:322-384) for GIVEN candidates (pt / ee stencils
+// as node ids; the broad phase of :330 is separate): node stream in emission
+// order (active PT pairs, active EE pairs, ground contacts, friction
+// constraints), node gradient, value. Returns the value.
+struct ContactInput {
+    std::vector<Vec3> pos;                       // contact-node positions
+    std::vector<std::array<Index, 4>> pt, ee;    // stencils (v, t0, t1, t2) / (a0, a1, b0, b1)
+    Real dhat = 0, kappa = 0;
+    bool ground = false;
+    Vec3 ground_normal;
+    Real ground_height = 0;
+    std::vector<Index> surf_verts;
+    std::vector<FrictionConstraint> friction;
+    std::vector<Vec3> fr_base;
+    Real mu = 0, fr_eps = 1;
+};
+inline Real contact_assemble(const ContactInput& in, Real dt2, std::vector<Vec3>& node_grad,
+                             BlockTripletStream& out, bool project = true) {
+    const Real shat = in.dhat * in.dhat;
+    node_grad.assign(in.pos.size(), Vec3());
+    out.keys.clear();
+    out.values.clear();
+    Real val = 0;
+    struct PS {
+        BarrierDerivs bd;
+        Index nodes[4];
+        Real dist2;
+    };
+    std::vector<PS> ps(in.pt.size() + in.ee.size());
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < static_cast<std::int64_t>(ps.size()); ++i) {
+        const bool is_pt = i < static_cast<std::int64_t>(in.pt.size());
+        const auto& st = is_pt ? in.pt[i] : in.ee[i - in.pt.size()];
+        const PairDerivs pd = is_pt ? pt_dist2_derivs(in.pos[st[0]], in.pos[st[1]], in.pos[st[2]], in.pos[st[3]])
+                                    : ee_dist2_derivs(in.pos[st[0]], in.pos[st[1]], in.pos[st[2]], in.pos[st[3]]);
+        ps[i].bd = barrier_pair_derivs(pd, shat, in.kappa, project);
+        for (int a = 0; a < 4; ++a) ps[i].nodes[a] = st[a];
+        ps[i].dist2 = pd.dist2;
+    }
+    auto emit12 = [&](const Index* nodes, int n, const Real* hess) {
+        for (int a = 0; a < n; ++a)
+            for (int b = a; b < n; ++b) {
+                Mat3 blk;
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r) blk(r, c) = dt2 * hess[12 * (3 * b + c) + 3 * a + r];
+                out.emit(nodes[a], nodes[b], blk);
+            }
+    };
+    for (const auto& p : ps) {  // :350-359
+        if (p.dist2 >= shat) continue;
+        val += dt2 * p.bd.value;
+        for (int a = 0; a < 4; ++a)
+            for (int k = 0; k < 3; ++k) node_grad[p.nodes[a]][k] += dt2 * p.bd.grad[3 * a + k];
+        emit12(p.nodes, 4, p.bd.hess);
+    }
+    if (in.ground)  // :361-369
+        for (Index v : in.surf_verts) {
+            const GroundDerivs gd =
+                ground_barrier_derivs(in.pos[v], in.ground_normal, in.ground_height, in.dhat, in.kappa, project);
+            if (!(gd.dist > 0) || gd.dist >= in.dhat) continue;
+            val += dt2 * gd.value;
+            for (int k = 0; k < 3; ++k) node_grad[v][k] += dt2 * gd.grad[k];
+            Mat3 blk;
+            for (int k = 0; k < 9; ++k) blk.m[k] = dt2 * gd.hess.m[k];
+            out.emit(v, v, blk);
+        }
+    for (const auto& c : in.friction) {  // :371-382
+        Vec3 dx[4];
+        for (int k = 0; k < c.n_nodes; ++k) dx[k] = sub3(in.pos[c.nodes[k]], in.fr_base[c.nodes[k]]);
+        const FrictionDerivs fd = friction_derivs(c, dx, in.mu, in.fr_eps);
+        val += dt2 * fd.value;
+        for (int a = 0; a < c.n_nodes; ++a)
+            for (int k = 0; k < 3; ++k) node_grad[c.nodes[a]][k] += dt2 * fd.grad[3 * a + k];
+        emit12(c.nodes, c.n_nodes, fd.hess);
+    }
+    return val;
+}
+
+// The contact terms of IncrementalPotential::value (incremental_potential.hpp:
+// 133-157): +inf as soon as a stencil or a surface vertex touches.
+inline Real contact_value(const ContactInput& in, Real dt2) {
+    const Real shat = in.dhat * in.dhat;
+    Real val = 0;
+    for (const auto& c : in.pt) {
+        const Real d2 = pt_dist2(in.pos[c[0]], in.pos[c[1]], in.pos[c[2]], in.pos[c[3]]);
+        if (d2 <= 0) return std::numeric_limits<Real>::infinity();
+        if (d2 < shat) val += dt2 * barrier_value(d2, shat, in.kappa);
+    }
+    for (const auto& c : in.ee) {
+        const Real d2 = ee_dist2(in.pos[c[0]], in.pos[c[1]], in.pos[c[2]], in.pos[c[3]]);
+        if (d2 <= 0) return std::numeric_limits<Real>::infinity();
+        if (d2 < shat) val += dt2 * barrier_value(d2, shat, in.kappa);
+    }
+    if (in.ground)
+        for (Index v : in.surf_verts) {
+            const Real d = dot3(in.ground_normal, in.pos[v]) - in.ground_height;
+            if (d <= 0) return std::numeric_limits<Real>::infinity();
+            if (d < in.dhat) val += dt2 * barrier_value(d * d, shat, in.kappa);
+        }
+    for (const auto& c : in.friction) {
+        Vec3 w;
+        for (int k = 0; k < c.n_nodes; ++k)
+            for (int a = 0; a < 3; ++a) w[a] += c.coeff[k] * (in.pos[c.nodes[k]][a] - in.fr_base[c.nodes[k]][a]);
+        const Real u0 = dot3(c.t1, w), u1 = dot3(c.t2, w);
+        val += dt2 * in.mu * c.lambda * friction_f0(std::sqrt(u0 * u0 + u1 * u1), in.fr_eps);
+    }
+    return val;
+}
+
+// contact/ccd.hpp:17-56 conservative advancement
+constexpr Real kCcdGapFraction = 0.01, kCcdRescale = 0.9;
+constexpr int kCcdMaxIters = 64;
+template <class Dist2Fn>
+Real conservative_toi(const Vec3* x0, const Vec3* d0, int n_side_a, int n_nodes, Dist2Fn&& dist2_of) {
+    Vec3 x[4], d[4], mean;
+    for (int i = 0; i < n_nodes; ++i) {
+        x[i] = x0[i];
+        d[i] = d0[i];
+        for (int a = 0; a < 3; ++a) mean[a] += d[i][a];
+    }
+    for (int a = 0; a < 3; ++a) mean[a] /= n_nodes;
+    Real max_a = 0, max_b = 0;
+    for (int i = 0; i < n_nodes; ++i) {
+        for (int a = 0; a < 3; ++a) d[i][a] -= mean[a];
+        const Real len = std::sqrt(dot3(d[i], d[i]));
+        Real& m = i < n_side_a ? max_a : max_b;
+        m = std::max(m, len);
+    }
+    const Real speed = max_a + max_b;
+    if (speed == 0) return 1;
+    const Real g0 = std::sqrt(dist2_of(x));
+    if (!(g0 > 0)) return 0;
+    const Real gap = kCcdGapFraction * g0;
+    Real t = 0;
+    Vec3 cur[4];
+    for (int i = 0; i < n_nodes; ++i) cur[i] = x[i];
+    for (int iter = 0; iter < kCcdMaxIters; ++iter) {
+        const Real g = std::sqrt(dist2_of(cur));
+        if (g <= gap) return kCcdRescale * t;
+        const Real step = (g - gap) / speed;
+        if (t + step >= 1) return 1;
+        t += step;
+        for (int i = 0; i < n_nodes; ++i)
+            for (int a = 0; a < 3; ++a) cur[i][a] = x[i][a] + t * d[i][a];
+    }
+    return kCcdRescale * t;
+}
+// ccd.hpp:58-86
+inline Real pt_ccd_toi(const Vec3* x, const Vec3* d) {
+    return conservative_toi(x, d, 1, 4, [](const Vec3* c) { return pt_dist2(c[0], c[1], c[2], c[3]); });
+}
+inline Real ee_ccd_toi(const Vec3* x, const Vec3* d) {
+    return conservative_toi(x, d, 2, 4, [](const Vec3* c) { return ee_dist2(c[0], c[1], c[2], c[3]); });
+}
+inline Real ground_ccd_toi(const Vec3& x, const Vec3& dx, const Vec3& normal, Real height) {
+    const Real g0 = dot3(normal, x) - height;
+    if (!(g0 > 0)) return 0;
+    const Real closing = -dot3(normal, dx);
+    if (closing <= 0) return 1;
+    const Real t_gap = (1 - kCcdGapFraction) * g0 / closing;
+    if (t_gap >= 1) return 1;
+    return kCcdRescale * t_gap;
+}
+// ccd.hpp:88-110 over GIVEN candidates (the ccd broad phase of :91 is separate)
+inline Real ccd_step(const ContactInput& in, const std::vector<Vec3>& disp) {
+    Real alpha = 1;
+    for (std::size_t i = 0; i < in.pt.size() + in.ee.size(); ++i) {
+        const bool is_pt = i < in.pt.size();
+        const auto& st = is_pt ? in.pt[i] : in.ee[i - in.pt.size()];
+        Vec3 x[4], d[4];
+        for (int a = 0; a < 4; ++a) {
+            x[a] = in.pos[st[a]];
+            d[a] = disp[st[a]];
+        }
+        alpha = std::min(alpha, is_pt ? pt_ccd_toi(x, d) : ee_ccd_toi(x, d));
+    }
+    if (in.ground)
+        for (Index v : in.surf_verts)
+            alpha = std::min(alpha, ground_ccd_toi(in.pos[v], disp[v], in.ground_normal, in.ground_height));
+    return alpha;
 }
 
 }  // namespace oracle

@@ -288,6 +288,111 @@ std::int64_t oracle_ip_fem_assemble(std::int32_t n_verts, const double* x, const
     return static_cast<std::int64_t>(s.size());
 }
 
+
+// ---- contact producers -----------------------------------------
+void oracle_pt_dist2_derivs(const double* x12, double* d2, double* g12, double* h144) {
+    const PairDerivs pd = pt_dist2_derivs(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9));
+    *d2 = pd.dist2;
+    std::memcpy(g12, pd.grad, 96);
+    std::memcpy(h144, pd.hess, 1152);
+}
+void oracle_ee_dist2_derivs(const double* x12, double* d2, double* g12, double* h144) {
+    const PairDerivs pd = ee_dist2_derivs(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9));
+    *d2 = pd.dist2;
+    std::memcpy(g12, pd.grad, 96);
+    std::memcpy(h144, pd.hess, 1152);
+}
+double oracle_pt_dist2(const double* x12) { return pt_dist2(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9)); }
+double oracle_ee_dist2(const double* x12) { return ee_dist2(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9)); }
+void oracle_barrier_pair_derivs(double d2, const double* g12, const double* h144, double shat, double kappa,
+                                int project, double* value, double* og12, double* oh144) {
+    PairDerivs pd;
+    pd.dist2 = d2;
+    std::memcpy(pd.grad, g12, 96);
+    std::memcpy(pd.hess, h144, 1152);
+    const BarrierDerivs b = barrier_pair_derivs(pd, shat, kappa, project != 0);
+    *value = b.value;
+    std::memcpy(og12, b.grad, 96);
+    std::memcpy(oh144, b.hess, 1152);
+}
+void oracle_ground_barrier_derivs(const double* x3, const double* n3, double height, double dhat, double kappa,
+                                  int project, double* value, double* g3, double* h9, double* dist) {
+    const GroundDerivs gd = ground_barrier_derivs(ld3(x3), ld3(n3), height, dhat, kappa, project != 0);
+    *value = gd.value;
+    for (int k = 0; k < 3; ++k) g3[k] = gd.grad[k];
+    std::memcpy(h9, gd.hess.m, 72);
+    *dist = gd.dist;
+}
+
+static ContactInput contact_input(std::int32_t n_nodes, const double* pos, std::int64_t n_pt, const std::int32_t* pt,
+                                  std::int64_t n_ee, const std::int32_t* ee, double dhat, double kappa, int ground,
+                                  const double* normal, double height, std::int32_t n_sv, const std::int32_t* sv,
+                                  std::int64_t n_fr, const std::int32_t* fr_nodes, const std::int32_t* fr_n,
+                                  const double* fr_coeff, const double* fr_t1, const double* fr_t2,
+                                  const double* fr_lambda, const double* fr_base, double mu, double eps) {
+    ContactInput in;
+    in.pos.resize(n_nodes);
+    for (std::int32_t v = 0; v < n_nodes; ++v) in.pos[v] = ld3(pos + 3 * v);
+    for (std::int64_t i = 0; i < n_pt; ++i) in.pt.push_back({pt[4 * i], pt[4 * i + 1], pt[4 * i + 2], pt[4 * i + 3]});
+    for (std::int64_t i = 0; i < n_ee; ++i) in.ee.push_back({ee[4 * i], ee[4 * i + 1], ee[4 * i + 2], ee[4 * i + 3]});
+    in.dhat = dhat;
+    in.kappa = kappa;
+    in.ground = ground != 0;
+    if (normal) in.ground_normal = ld3(normal);
+    in.ground_height = height;
+    in.surf_verts.assign(sv, sv + n_sv);
+    for (std::int64_t i = 0; i < n_fr; ++i) {
+        FrictionConstraint c;
+        c.n_nodes = fr_n[i];
+        for (int k = 0; k < 4; ++k) {
+            c.nodes[k] = fr_nodes[4 * i + k];
+            c.coeff[k] = fr_coeff[4 * i + k];
+        }
+        c.t1 = ld3(fr_t1 + 3 * i);
+        c.t2 = ld3(fr_t2 + 3 * i);
+        c.lambda = fr_lambda[i];
+        in.friction.push_back(c);
+    }
+    if (n_fr > 0) {
+        in.fr_base.resize(n_nodes);
+        for (std::int32_t v = 0; v < n_nodes; ++v) in.fr_base[v] = ld3(fr_base + 3 * v);
+    }
+    in.mu = mu;
+    in.fr_eps = eps;
+    return in;
+}
+#define ORACLE_CONTACT_ARGS                                                                                        \
+    std::int32_t n_nodes, const double *pos, std::int64_t n_pt, const std::int32_t *pt, std::int64_t n_ee,        \
+        const std::int32_t *ee, double dhat, double kappa, int ground, const double *normal, double height,       \
+        std::int32_t n_sv, const std::int32_t *sv, std::int64_t n_fr, const std::int32_t *fr_nodes,              \
+        const std::int32_t *fr_n, const double *fr_coeff, const double *fr_t1, const double *fr_t2,               \
+        const double *fr_lambda, const double *fr_base, double mu, double eps
+#define ORACLE_CONTACT_PASS                                                                                        \
+    n_nodes, pos, n_pt, pt, n_ee, ee, dhat, kappa, ground, normal, height, n_sv, sv, n_fr, fr_nodes, fr_n,        \
+        fr_coeff, fr_t1, fr_t2, fr_lambda, fr_base, mu, eps
+
+// assemble_contact's node part: stream (keys / vals9), node gradient, value
+std::int64_t oracle_contact_assemble(ORACLE_CONTACT_ARGS, double dt2, int project, std::uint64_t* keys, double* vals9,
+                                     double* node_grad, double* value) {
+    const ContactInput in = contact_input(ORACLE_CONTACT_PASS);
+    std::vector<Vec3> g;
+    BlockTripletStream s;
+    *value = contact_assemble(in, dt2, g, s, project != 0);
+    for (std::int32_t v = 0; v < n_nodes; ++v)
+        for (int k = 0; k < 3; ++k) node_grad[3 * v + k] = g[v][k];
+    store_stream(s, keys, vals9);
+    return static_cast<std::int64_t>(s.size());
+}
+double oracle_contact_value(ORACLE_CONTACT_ARGS, double dt2) {
+    return contact_value(contact_input(ORACLE_CONTACT_PASS), dt2);
+}
+double oracle_ccd_step(ORACLE_CONTACT_ARGS, const double* disp) {
+    const ContactInput in = contact_input(ORACLE_CONTACT_PASS);
+    std::vector<Vec3> d(n_nodes);
+    for (std::int32_t v = 0; v < n_nodes; ++v) d[v] = ld3(disp + 3 * v);
+    return ccd_step(in, d);
+}
+
 // ---- partition / hierarchy ----------------------------------------------------
 std::int32_t oracle_subdomain_count(std::int32_t v, std::int32_t n, std::int32_t n_o) {
     return subdomain_count(v, n, n_o);

@@ -40,6 +40,7 @@ def build() -> None:
 
 
 _lib = None
+_CONTACT_ARGS = [i32, f64p, i64, vp, i64, vp, cd, cd, ci, vp, cd, i32, vp, i64, vp, vp, vp, vp, vp, vp, vp, cd, cd]
 
 
 def lib():
@@ -93,6 +94,15 @@ def lib():
         "oracle_random_stream": (None, [vp, ci, ci, u64p, f64p]),
         "oracle_random_spd3": (None, [vp, cd, f64p]),
         "oracle_tet_rest": (ci, [f64p, f64p, f64p]),
+        "oracle_pt_dist2_derivs": (None, [f64p, f64p, f64p, f64p]),
+        "oracle_ee_dist2_derivs": (None, [f64p, f64p, f64p, f64p]),
+        "oracle_pt_dist2": (cd, [f64p]),
+        "oracle_ee_dist2": (cd, [f64p]),
+        "oracle_barrier_pair_derivs": (None, [cd, f64p, f64p, cd, cd, ci, f64p, f64p, f64p]),
+        "oracle_ground_barrier_derivs": (None, [f64p, f64p, cd, cd, cd, ci, f64p, f64p, f64p, f64p]),
+        "oracle_contact_assemble": (i64, _CONTACT_ARGS + [cd, ci, u64p, f64p, f64p, f64p]),
+        "oracle_contact_value": (cd, _CONTACT_ARGS + [cd]),
+        "oracle_ccd_step": (cd, _CONTACT_ARGS + [f64p]),
         "oracle_stable_neo_hookean": (None, [f64p, f64p, cd, cd, cd, ci, f64p, f64p, f64p]),
         "oracle_project_psd": (None, [ci, f64p, f64p]),
         "oracle_ip_fem_assemble": (i64, [i32, f64p, f64p, f64p, i32, i64p, f64p, f64p, i32p, f64p, f64p, cd, vp, ci,
@@ -409,6 +419,107 @@ def ip_fem_assemble(x, x_tilde, mass, tet_begin, mu, lam, tets, inv9, vol, dt2, 
                                      np.ascontiguousarray(vol, np.float64), dt2,
                                      None if pin is None else pin.ctypes.data, int(project), keys, vals, grad, val)
     return float(val[0]), grad, keys[:T].copy(), vals[:T].copy()
+
+
+# --------------------------------------------------- contact producers ----
+def _x12(x):
+    return np.ascontiguousarray(x, np.float64).reshape(12)
+
+
+def pt_dist2_derivs(x12):
+    """contact/distance.hpp:159-189 -> (dist2, grad 12, hess 12x12)."""
+    d, g, h = np.empty(1), np.empty(12), np.empty(144)
+    lib().oracle_pt_dist2_derivs(_x12(x12), d, g, h)
+    return float(d[0]), g, h.reshape(12, 12).T.copy()
+
+
+def ee_dist2_derivs(x12):
+    """contact/distance.hpp:191-223."""
+    d, g, h = np.empty(1), np.empty(12), np.empty(144)
+    lib().oracle_ee_dist2_derivs(_x12(x12), d, g, h)
+    return float(d[0]), g, h.reshape(12, 12).T.copy()
+
+
+def pt_dist2(x12):
+    return float(lib().oracle_pt_dist2(_x12(x12)))
+
+
+def ee_dist2(x12):
+    return float(lib().oracle_ee_dist2(_x12(x12)))
+
+
+def barrier_pair_derivs(d2, g, H, shat, kappa, project=True):
+    """contact/barrier.hpp:50-66 -> (value, grad 12, hess 12x12)."""
+    v, og, oh = np.empty(1), np.empty(12), np.empty(144)
+    lib().oracle_barrier_pair_derivs(d2, np.ascontiguousarray(g, np.float64),
+                                     np.ascontiguousarray(np.asarray(H, np.float64).T).reshape(-1), shat, kappa,
+                                     int(project), v, og, oh)
+    return float(v[0]), og, oh.reshape(12, 12).T.copy()
+
+
+def ground_barrier_derivs(x, normal, height, dhat, kappa, project=True):
+    """contact/barrier.hpp:70-91 -> (value, grad 3, hess 3x3, dist)."""
+    v, g, h, d = np.empty(1), np.empty(3), np.empty(9), np.empty(1)
+    lib().oracle_ground_barrier_derivs(np.ascontiguousarray(x, np.float64), np.ascontiguousarray(normal, np.float64),
+                                       height, dhat, kappa, int(project), v, g, h, d)
+    return float(v[0]), g, h.reshape(3, 3).T.copy(), float(d[0])
+
+
+class ContactInput:
+    """Inputs of the contact-node part of assemble_contact / value / ccd:
+    positions, PT / EE stencils (node ids), ground plane + surface vertices,
+    lagged friction constraints."""
+
+    def __init__(self, pos, pt=(), ee=(), dhat=1e-3, kappa=1.0, ground=None, surf_verts=(), friction=None,
+                 fr_base=None, mu=0.0, fr_eps=1.0):
+        self.pos = np.ascontiguousarray(pos, np.float64).reshape(-1, 3)
+        self.pt = np.ascontiguousarray(np.asarray(pt, np.int32).reshape(-1, 4))
+        self.ee = np.ascontiguousarray(np.asarray(ee, np.int32).reshape(-1, 4))
+        self.dhat, self.kappa = float(dhat), float(kappa)
+        self.ground = ground  # (normal 3, height) or None
+        self.surf_verts = np.ascontiguousarray(np.asarray(surf_verts, np.int32).reshape(-1))
+        f = friction or {}
+        nf = len(f.get("n", []))
+        self.fr_n = np.ascontiguousarray(np.asarray(f.get("n", []), np.int32).reshape(nf))
+        self.fr_nodes = np.ascontiguousarray(np.asarray(f.get("nodes", np.zeros((nf, 4))), np.int32).reshape(nf, 4))
+        self.fr_coeff = np.ascontiguousarray(np.asarray(f.get("coeff", np.zeros((nf, 4))), np.float64).reshape(nf, 4))
+        self.fr_t1 = np.ascontiguousarray(np.asarray(f.get("t1", np.zeros((nf, 3))), np.float64).reshape(nf, 3))
+        self.fr_t2 = np.ascontiguousarray(np.asarray(f.get("t2", np.zeros((nf, 3))), np.float64).reshape(nf, 3))
+        self.fr_lambda = np.ascontiguousarray(np.asarray(f.get("lam", np.zeros(nf)), np.float64).reshape(nf))
+        self.fr_base = np.ascontiguousarray(self.pos if fr_base is None else fr_base, np.float64).reshape(-1, 3)
+        self.mu, self.fr_eps = float(mu), float(fr_eps)
+
+    def args(self):
+        p = lambda a: a.ctypes.data if a.size else None  # noqa: E731
+        normal = np.ascontiguousarray(self.ground[0], np.float64) if self.ground is not None else None
+        self._keep = normal
+        return [len(self.pos), self.pos.reshape(-1), len(self.pt), p(self.pt), len(self.ee), p(self.ee), self.dhat,
+                self.kappa, int(self.ground is not None), None if normal is None else normal.ctypes.data,
+                float(self.ground[1]) if self.ground is not None else 0.0, len(self.surf_verts), p(self.surf_verts),
+                len(self.fr_n), p(self.fr_nodes), p(self.fr_n), p(self.fr_coeff), p(self.fr_t1), p(self.fr_t2),
+                p(self.fr_lambda), p(self.fr_base), self.mu, self.fr_eps]
+
+    def max_entries(self):
+        return 10 * (len(self.pt) + len(self.ee)) + len(self.surf_verts) + 10 * len(self.fr_n)
+
+
+def contact_assemble(ci: ContactInput, dt2, project=True):
+    """incremental_potential.hpp:322-384 node part -> (value, node_grad 3n, keys, vals)."""
+    cap = max(ci.max_entries(), 1)
+    keys, vals = np.empty(cap, np.uint64), np.empty((cap, 9))
+    g, v = np.empty(3 * len(ci.pos)), np.empty(1)
+    T = lib().oracle_contact_assemble(*ci.args(), dt2, int(project), keys, vals, g, v)
+    return float(v[0]), g, keys[:T].copy(), vals[:T].copy()
+
+
+def contact_value(ci: ContactInput, dt2):
+    """incremental_potential.hpp:133-157 (contact terms of the line-search value)."""
+    return float(lib().oracle_contact_value(*ci.args(), dt2))
+
+
+def ccd_step(ci: ContactInput, disp):
+    """contact/ccd.hpp:88-110 over the given stencils."""
+    return float(lib().oracle_ccd_step(*ci.args(), np.ascontiguousarray(disp, np.float64).reshape(-1)))
 
 
 def filter_pinned(keys, vals, pinned):

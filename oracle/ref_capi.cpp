@@ -20,6 +20,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "adipc/contact/barrier.hpp"
 #include "adipc/energy/neo_hookean.hpp"
 #include "adipc/energy/psd.hpp"
 #include "adipc/precond/block_jacobi.hpp"
@@ -275,6 +276,41 @@ void ref_project_psd(int n, const double* M, double* out) {
     std::memcpy(m.data(), M, sizeof(double) * n * n);
     const MatX p = project_psd(m);
     std::memcpy(out, p.data(), sizeof(double) * n * n);
+}
+
+
+// ---- contact stencils: contact/distance.hpp + contact/barrier.hpp --------------
+static void store_pair(const PairDerivs& pd, double* d2, double* g12, double* h144) {
+    *d2 = pd.dist2;
+    std::memcpy(g12, pd.grad.data(), 96);
+    std::memcpy(h144, pd.hess.data(), 1152);
+}
+void ref_pt_dist2_derivs(const double* x12, double* d2, double* g12, double* h144) {
+    store_pair(pt_dist2_derivs(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9)), d2, g12, h144);
+}
+void ref_ee_dist2_derivs(const double* x12, double* d2, double* g12, double* h144) {
+    store_pair(ee_dist2_derivs(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9)), d2, g12, h144);
+}
+double ref_pt_dist2(const double* x12) { return pt_dist2(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9)); }
+double ref_ee_dist2(const double* x12) { return ee_dist2(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9)); }
+void ref_barrier_pair_derivs(double d2, const double* g12, const double* h144, double shat, double kappa, int project,
+                             double* value, double* og12, double* oh144) {
+    PairDerivs pd;
+    pd.dist2 = d2;
+    std::memcpy(pd.grad.data(), g12, 96);
+    std::memcpy(pd.hess.data(), h144, 1152);
+    const BarrierDerivs b = barrier_pair_derivs(pd, shat, kappa, project != 0);
+    *value = b.value;
+    std::memcpy(og12, b.grad.data(), 96);
+    std::memcpy(oh144, b.hess.data(), 1152);
+}
+void ref_ground_barrier_derivs(const double* x3, const double* n3, double height, double dhat, double kappa,
+                               int project, double* value, double* g3, double* h9, double* dist) {
+    const GroundDerivs gd = ground_barrier_derivs(ld3(x3), ld3(n3), height, dhat, kappa, project != 0);
+    *value = gd.value;
+    std::memcpy(g3, gd.grad.data(), 24);
+    std::memcpy(h9, gd.hess.data(), 72);
+    *dist = gd.dist;
 }
 
 std::int32_t ref_subdomain_count(std::int32_t v, std::int32_t n, std::int32_t n_o) { return subdomain_count(v, n, n_o); }

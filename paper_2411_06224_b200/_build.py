@@ -23,7 +23,10 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-r
 CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"  # image's $CXX lacks libgomp.spec
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter"]
 
-GPU_SOURCES = ["assemble.cu", "spmv.cu", "mas.cu", "solve_order.cu", "pcg.cu", "abd.cu", "step.cu", "energy.cu", "capi.cu", "host_precond.cpp"]
+GPU_SOURCES = ["assemble.cu", "spmv.cu", "mas.cu", "solve_order.cu", "pcg.cu", "abd.cu", "step.cu", "energy.cu", "contact.cu", "capi.cu", "host_precond.cpp"]
+
+
+PER_FILE_FLAGS = {"contact.cu": ["-fmad=false"]}
 
 
 def _nvcc() -> str:
@@ -51,7 +54,11 @@ def _compile(src: str, verbose: bool) -> str:
     if not _stale(obj, [path] + _headers()):
         return obj
     if src.endswith(".cu"):
-        cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-c", path, "-o", obj]
+        # the contact producer decides which stencils are active by the exact
+        # dual value (contact/distance.hpp's pd.dist2 < dhat^2): no FMA
+        # contraction there, so its arithmetic is the oracle's to the bit
+        extra = PER_FILE_FLAGS.get(src, [])
+        cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", path, "-o", obj]
     else:
         cmd = [CXX, *CXX_FLAGS, "-fopenmp", "-I", os.path.join(ROOT, "include"), "-c", path, "-o", obj]
     if verbose:

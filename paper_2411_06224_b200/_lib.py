@@ -39,6 +39,18 @@ class FemDesc(C.Structure):
                 ("project", C.c_int), ("pinned", C.c_void_p)]
 
 
+class ContactDesc(C.Structure):
+    """adipc_contact_desc (include/adipc_gpu.h): device arrays over the
+    contact-node universe; stencils as node ids."""
+    _fields_ = [("n_nodes", C.c_int32), ("pos", C.c_void_p), ("n_pt", C.c_int64), ("pt", C.c_void_p),
+                ("n_ee", C.c_int64), ("ee", C.c_void_p), ("dhat", C.c_double), ("kappa", C.c_double),
+                ("ground", C.c_int), ("ground_normal", C.c_double * 3), ("ground_height", C.c_double),
+                ("n_surf_verts", C.c_int32), ("surf_verts", C.c_void_p), ("n_friction", C.c_int64),
+                ("fr_nodes", C.c_void_p), ("fr_n_nodes", C.c_void_p), ("fr_coeff", C.c_void_p),
+                ("fr_t1", C.c_void_p), ("fr_t2", C.c_void_p), ("fr_lambda", C.c_void_p), ("fr_base", C.c_void_p),
+                ("mu", C.c_double), ("fr_eps", C.c_double)]
+
+
 GPU_SIGNATURES = {
     "adipc_gpu_create": (ci, [ci, C.POINTER(vp)]),
     "adipc_gpu_destroy": (ci, [vp]),
@@ -69,6 +81,10 @@ GPU_SIGNATURES = {
     "adipc_gpu_assemble_contact_device": (ci, [vp, vp, vp, i64, vp, vp, i64, i32, i32, i32, vp, vp, i32, vp,
                                                C.POINTER(i64), C.POINTER(i64)]),
     "adipc_gpu_filter_pinned": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
+    "adipc_gpu_contact_emit_device": (ci, [vp, C.POINTER(ContactDesc), cd, ci, vp, vp, i64, vp, C.POINTER(cd),
+                                           C.POINTER(i64)]),
+    "adipc_gpu_contact_value_device": (ci, [vp, C.POINTER(ContactDesc), cd, C.POINTER(cd)]),
+    "adipc_gpu_ccd_step_device": (ci, [vp, C.POINTER(ContactDesc), vp, C.POINTER(cd)]),
     "adipc_gpu_fem_emit_device": (ci, [vp, C.POINTER(FemDesc), vp, vp, vp, C.POINTER(cd)]),
     "adipc_gpu_fem_assemble_device": (ci, [vp, C.POINTER(FemDesc), vp, C.POINTER(cd), C.POINTER(i64)]),
     "adipc_gpu_filter_pinned_device": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),

@@ -200,6 +200,60 @@ class Context:
         self._check(self._L.adipc_gpu_fem_assemble_device(self.h, C.byref(d), ptr(grad), C.byref(v), C.byref(U)))
         return v.value, U.value
 
+    # -- contact producers ------------------------------------
+    @staticmethod
+    def contact_desc(c):
+        """c: dict of DEVICE tensors pos (n x 3 / 3n), pt / ee (k x 4 int32),
+        surf_verts (int32), friction arrays fr_nodes / fr_n / fr_coeff / fr_t1 /
+        fr_t2 / fr_lambda / fr_base; scalars dhat, kappa, mu, fr_eps; ground =
+        (normal, height) or None."""
+        def n_of(name, per=1):
+            t = c.get(name)
+            return 0 if t is None else t.numel() // per
+        d = _lib.ContactDesc()
+        d.n_nodes = n_of("pos", 3)
+        d.pos = ptr(c["pos"])
+        d.n_pt, d.pt = n_of("pt", 4), ptr(c.get("pt")) if n_of("pt", 4) else None
+        d.n_ee, d.ee = n_of("ee", 4), ptr(c.get("ee")) if n_of("ee", 4) else None
+        d.dhat, d.kappa = float(c["dhat"]), float(c["kappa"])
+        g = c.get("ground")
+        d.ground = int(g is not None)
+        if g is not None:
+            for k in range(3):
+                d.ground_normal[k] = float(g[0][k])
+            d.ground_height = float(g[1])
+        d.n_surf_verts = n_of("surf_verts") if g is not None else 0
+        d.surf_verts = ptr(c.get("surf_verts")) if d.n_surf_verts else None
+        d.n_friction = n_of("fr_n")
+        if d.n_friction:
+            for f in ("fr_nodes", "fr_coeff", "fr_t1", "fr_t2", "fr_lambda", "fr_base"):
+                setattr(d, f, ptr(c[f]))
+            d.fr_n_nodes = ptr(c["fr_n"])
+        d.mu, d.fr_eps = float(c.get("mu", 0.0)), float(c.get("fr_eps", 1.0))
+        return d
+
+    def contact_emit(self, c, dt2, keys, vals, node_grad, project=True):
+        """assemble_contact's node part into the device node stream; returns
+        (value, entries written)."""
+        d = self.contact_desc(c)
+        v, n = C.c_double(), C.c_int64()
+        self._check(self._L.adipc_gpu_contact_emit_device(self.h, C.byref(d), float(dt2), int(project), ptr(keys),
+                                                          ptr(vals), keys.numel(), ptr(node_grad), C.byref(v),
+                                                          C.byref(n)))
+        return v.value, n.value
+
+    def contact_value(self, c, dt2):
+        d = self.contact_desc(c)
+        v = C.c_double()
+        self._check(self._L.adipc_gpu_contact_value_device(self.h, C.byref(d), float(dt2), C.byref(v)))
+        return v.value
+
+    def ccd_step(self, c, disp):
+        d = self.contact_desc(c)
+        a = C.c_double()
+        self._check(self._L.adipc_gpu_ccd_step_device(self.h, C.byref(d), ptr(disp), C.byref(a)))
+        return a.value
+
     def matrix_info(self):
         n, U = C.c_int32(), C.c_int64()
         self._check(self._L.adipc_gpu_matrix_info(self.h, C.byref(n), C.byref(U)))

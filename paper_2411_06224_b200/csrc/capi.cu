@@ -183,6 +183,10 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.graph_adj.free();
     c.graph_ptr.free();
     c.fem_keys.free();
+    c.ct_on.free();
+    c.ct_rank.free();
+    c.ct_work.free();
+    c.ct_scal.free();
     c.fem_vals.free();
     c.fem_value.free();
     c.perm.free();
@@ -388,6 +392,76 @@ int adipc_gpu_fem_assemble_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* d, d
         if (value) ADIPC_CUDA(cudaMemcpyAsync(value, c.fem_value.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
         sync(c);
         if (n_unique) *n_unique = c.A.U;
+    });
+}
+
+
+// ---- contact producers (contact.cu) ---------------------------
+static ContactDesc contact_desc(const adipc_contact_desc* d) {
+    if (!d) throw StatusError(kInvalidArgument, "null adipc_contact_desc");
+    if (d->n_nodes < 0 || d->n_pt < 0 || d->n_ee < 0 || d->n_surf_verts < 0 || d->n_friction < 0)
+        throw StatusError(kInvalidArgument, "negative size");
+    if ((d->n_nodes > 0 && !d->pos) || (d->n_pt > 0 && !d->pt) || (d->n_ee > 0 && !d->ee) ||
+        (d->ground && d->n_surf_verts > 0 && !d->surf_verts))
+        throw StatusError(kInvalidArgument, "missing contact arrays");
+    if (d->n_friction > 0 && (!d->fr_nodes || !d->fr_n_nodes || !d->fr_coeff || !d->fr_t1 || !d->fr_t2 ||
+                              !d->fr_lambda || !d->fr_base))
+        throw StatusError(kInvalidArgument, "missing friction arrays");
+    if (!(d->dhat > 0)) throw StatusError(kInvalidArgument, "dhat must be positive");
+    ContactDesc c;
+    c.n_nodes = d->n_nodes;
+    c.pos = d->pos;
+    c.n_pt = d->n_pt;
+    c.n_ee = d->n_ee;
+    c.pt = d->pt;
+    c.ee = d->ee;
+    c.dhat = d->dhat;
+    c.kappa = d->kappa;
+    c.ground = d->ground;
+    for (int k = 0; k < 3; ++k) c.ground_normal[k] = d->ground_normal[k];
+    c.ground_height = d->ground_height;
+    c.n_surf_verts = d->n_surf_verts;
+    c.surf_verts = d->surf_verts;
+    c.n_friction = d->n_friction;
+    c.fr_nodes = d->fr_nodes;
+    c.fr_n_nodes = d->fr_n_nodes;
+    c.fr_coeff = d->fr_coeff;
+    c.fr_t1 = d->fr_t1;
+    c.fr_t2 = d->fr_t2;
+    c.fr_lambda = d->fr_lambda;
+    c.fr_base = d->fr_base;
+    c.mu = d->mu;
+    c.fr_eps = d->fr_eps;
+    return c;
+}
+
+int adipc_gpu_contact_emit_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* d, double dt2, int project,
+                                  uint64_t* d_node_keys, double* d_node_vals9, int64_t capacity, double* d_node_grad,
+                                  double* value, int64_t* n_out) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const ContactDesc cd = contact_desc(d);
+        c.ct_scal.reserve(2);
+        const std::int64_t T = contact_emit(c, cd, dt2, project, d_node_keys, d_node_vals9, capacity, d_node_grad,
+                                            c.ct_scal.p);
+        if (value) ADIPC_CUDA(cudaMemcpyAsync(value, c.ct_scal.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+        if (n_out) *n_out = T;
+    });
+}
+
+int adipc_gpu_contact_value_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* d, double dt2, double* value) {
+    return guarded(ctx, [&] {
+        const double v = contact_value(ctx->c, contact_desc(d), dt2);
+        if (value) *value = v;
+    });
+}
+
+int adipc_gpu_ccd_step_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* d, const double* d_disp, double* alpha) {
+    return guarded(ctx, [&] {
+        if (!d_disp) throw StatusError(kInvalidArgument, "missing displacement");
+        const double a = ccd_step(ctx->c, contact_desc(d), d_disp);
+        if (alpha) *alpha = a;
     });
 }
 

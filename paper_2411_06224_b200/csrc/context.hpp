@@ -121,6 +121,12 @@ struct Ctx {
     // element-Hessian producer (energy.cu): the emitted stream + the value
     DBuf<std::uint64_t> fem_keys;
     DBuf<double> fem_vals, fem_value;
+    // contact producers (contact.cu): activity flags / counts, their prefix
+    // sums, the per-thread dual scratch, value / touch / ccd scalars
+    DBuf<std::int32_t> ct_on;
+    DBuf<std::int64_t> ct_rank;
+    DBuf<unsigned char> ct_work;
+    DBuf<double> ct_scal;
     DBuf<double> tile_vals;
     // staging of the host-pointer entry points (contact node stream, DofMap)
     DBuf<std::uint64_t> io_keys, io_keys2;
@@ -257,6 +263,37 @@ struct FemDesc {
     const std::uint8_t* pinned = nullptr;   // n_verts or null
 };
 void fem_emit(Ctx& c, const FemDesc& d, std::uint64_t* d_keys, double* d_vals, double* d_grad, double* d_value);
+
+// Contact producer input (contact.cu; incremental_potential.hpp:322-384):
+// device arrays over the contact-node universe (FEM vertices, then body
+// vertices, abd_reduce.hpp:11-27). Stencils are node ids: PT (v, t0, t1, t2),
+// EE (a0, a1, b0, b1) — the broad phase's candidates resolved to nodes.
+struct ContactDesc {
+    std::int32_t n_nodes = 0;
+    const double* pos = nullptr;  // 3 per node
+    std::int64_t n_pt = 0, n_ee = 0;
+    const std::int32_t* pt = nullptr;
+    const std::int32_t* ee = nullptr;
+    double dhat = 0, kappa = 0;
+    int ground = 0;
+    double ground_normal[3] = {0, 1, 0};
+    double ground_height = 0;
+    std::int32_t n_surf_verts = 0;
+    const std::int32_t* surf_verts = nullptr;
+    std::int64_t n_friction = 0;
+    const std::int32_t* fr_nodes = nullptr;  // 4 per constraint
+    const std::int32_t* fr_n_nodes = nullptr;
+    const double* fr_coeff = nullptr;        // 4 per constraint
+    const double* fr_t1 = nullptr;           // 3 per constraint
+    const double* fr_t2 = nullptr;
+    const double* fr_lambda = nullptr;
+    const double* fr_base = nullptr;         // 3 per node
+    double mu = 0, fr_eps = 1;
+};
+std::int64_t contact_emit(Ctx& c, const ContactDesc& d, double dt2, int project, std::uint64_t* d_keys, double* d_vals,
+                          std::int64_t capacity, double* d_node_grad, double* d_value);
+double contact_value(Ctx& c, const ContactDesc& d, double dt2);
+double ccd_step(Ctx& c, const ContactDesc& d, const double* d_disp);
 
 void assemble_filtered(Ctx& c, const std::uint64_t* d_keys, const double* d_vals, std::int64_t T, std::int32_t n,
                        const std::uint8_t* d_pinned, cudaEvent_t vals_ready = nullptr,

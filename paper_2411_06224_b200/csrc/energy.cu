@@ -27,36 +27,13 @@
 //    cyclic Jacobi eigen-decomposition of M (per-thread local arrays; only
 //    indefinite elements take it) and proj(M) = V max(w, 0) V^T.
 #include "context.hpp"
+#include "psd.cuh"
 
 namespace adipc_gpu {
 
 namespace {
 
 constexpr int kFemThreads = 128;
-
-__device__ __forceinline__ void red_add_f64(double* p, double v) { asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v)); }
-
-// CTA sum of v, one fp64 atomic per CTA into *out
-__device__ __forceinline__ void block_sum_atomic(double v, double* out) {
-    __shared__ double part[32];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (lane == 0) part[w] = v;
-    __syncthreads();
-    if (w == 0) {
-        v = lane < static_cast<int>(blockDim.x >> 5) ? part[lane] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) atomicAdd(out, v);
-    }
-}
-
-// Helmert basis of the complement of (1,1,1,1) in R^4 (columns of Q, 4 x 3)
-__device__ __forceinline__ double helmert(int a, int j) {
-    const double s2 = 0.70710678118654752440, s6 = 0.40824829046386301637, s12 = 0.28867513459481288225;
-    if (j == 0) return a == 0 ? s2 : (a == 1 ? -s2 : 0.0);
-    if (j == 1) return a < 2 ? s6 : (a == 2 ? -2.0 * s6 : 0.0);
-    return a < 3 ? s12 : -3.0 * s12;
-}
 
 struct TetState {
     double F[9];    // column-major
@@ -81,79 +58,6 @@ __device__ __forceinline__ void stencil_block(const TetState& s, const double* x
 #pragma unroll
         for (int r = 0; r < 3; ++r)
             h[3 * c + r] = s.V * ((r == c ? s.mu * xy : 0.0) + s.lam * ux[r] * uy[c] + s.dJ * W[3 * c + r]);
-}
-
-// packed lower index of (i, j), i >= j, n = 9
-__device__ __forceinline__ constexpr int pk(int i, int j) { return i * (i + 1) / 2 + j; }
-
-// Cholesky of M + tau I in place (packed lower); true when every pivot > 0
-__device__ __forceinline__ bool shifted_cholesky_ok(double* L, double tau) {
-    bool ok = true;
-#pragma unroll
-    for (int j = 0; j < 9; ++j) {
-        double d = L[pk(j, j)] + tau;
-#pragma unroll
-        for (int k = 0; k < j; ++k) d -= L[pk(j, k)] * L[pk(j, k)];
-        ok = ok && d > 0;
-        const double inv = d > 0 ? rsqrt(d) : 0.0;
-        L[pk(j, j)] = d > 0 ? d * inv : 0.0;
-#pragma unroll
-        for (int i = j + 1; i < 9; ++i) {
-            double s = L[pk(i, j)];
-#pragma unroll
-            for (int k = 0; k < j; ++k) s -= L[pk(i, k)] * L[pk(j, k)];
-            L[pk(i, j)] = s * inv;
-        }
-    }
-    return ok;
-}
-
-// proj(M) for a symmetric 9 x 9 (full column-major in `a`, overwritten):
-// cyclic Jacobi (oracle/sym_eig.hpp's rotations), then V max(w, 0) V^T
-__device__ __noinline__ void project9(double* a) {
-    double v[81];
-    for (int k = 0; k < 81; ++k) v[k] = (k % 10 == 0) ? 1.0 : 0.0;
-    for (int sweep = 0; sweep < 64; ++sweep) {
-        double off = 0, tot = 0;
-        for (int j = 0; j < 9; ++j)
-            for (int i = 0; i < 9; ++i) {
-                const double x = a[9 * j + i] * a[9 * j + i];
-                tot += x;
-                if (i != j) off += x;
-            }
-        if (off <= 1e-32 * tot) break;
-        for (int p = 0; p < 8; ++p)
-            for (int q = p + 1; q < 9; ++q) {
-                const double apq = a[9 * q + p];
-                if (apq == 0.0) continue;
-                const double theta = (a[9 * q + q] - a[9 * p + p]) / (2.0 * apq);
-                const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-                const double c = rsqrt(t * t + 1.0), s = t * c;
-                for (int k = 0; k < 9; ++k) {
-                    const double kp = a[9 * p + k], kq = a[9 * q + k];
-                    a[9 * p + k] = c * kp - s * kq;
-                    a[9 * q + k] = s * kp + c * kq;
-                }
-                for (int k = 0; k < 9; ++k) {
-                    const double pk_ = a[9 * k + p], qk = a[9 * k + q];
-                    a[9 * k + p] = c * pk_ - s * qk;
-                    a[9 * k + q] = s * pk_ + c * qk;
-                }
-                for (int k = 0; k < 9; ++k) {
-                    const double kp = v[9 * p + k], kq = v[9 * q + k];
-                    v[9 * p + k] = c * kp - s * kq;
-                    v[9 * q + k] = s * kp + c * kq;
-                }
-            }
-    }
-    double w[9];
-    for (int k = 0; k < 9; ++k) w[k] = a[10 * k] > 0 ? a[10 * k] : 0.0;
-    for (int j = 0; j < 9; ++j)
-        for (int i = 0; i < 9; ++i) {
-            double s = 0;
-            for (int k = 0; k < 9; ++k) s += v[9 * k + i] * w[k] * v[9 * k + j];
-            a[9 * j + i] = s;
-        }
 }
 
 // inertia (incremental_potential.hpp:170-180): one thread per vertex

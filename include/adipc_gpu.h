@@ -185,11 +185,24 @@ typedef struct adipc_fem_desc {
     const double* rest_volume;  /* TetRest::volume per tet */
     double dt2;
     int project;                /* 1: project_psd every stencil (the reference's default) */
-    const uint8_t* pinned;      /* n_verts or NULL: zero gradient on pinned slots */
+    const uint8_t* pinned;      /* n_verts + 4 n_bodies or NULL: zero gradient on pinned slots */
+    /* affine bodies (scene.hpp Body; block rows n_verts + 4 b .. + 3): inertia
+     * tiles of the reduced mass (:181-188) and the orthogonality penalty
+     * (energy/abd_energy.hpp:19-42, :242-249) */
+    int32_t n_bodies;
+    const double* q;            /* 12 per body */
+    const double* q_tilde;      /* 12 per body */
+    const double* reduced_mass; /* 144 per body, column-major */
+    const double* body_kappa;
+    const double* body_volume;
 } adipc_fem_desc;
-/* the raw stream (n_verts + 10 n_tets entries) + gradient (3 n_verts) + value */
+/* the raw stream (n_verts + 10 n_tets + 20 n_bodies entries) + gradient
+ * (3 (n_verts + 4 n_bodies)) + value */
 int adipc_gpu_fem_emit_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* desc, uint64_t* d_keys, double* d_vals9,
                               double* d_grad, double* value);
+/* IncrementalPotential::value's inertia + elastic + body terms (:61-131) for
+ * the line search: no stream; d_grad may be NULL */
+int adipc_gpu_fem_value_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* desc, double* d_grad, double* value);
 /* emit + filter_pinned + sort + reduce into the context matrix (the whole
  * assemble() for these scenes; the stream never leaves HBM) */
 int adipc_gpu_fem_assemble_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* desc, double* d_grad, double* value,

@@ -1080,6 +1080,44 @@ inline Stencil12 stable_neo_hookean(const Vec3& x0, const Vec3& x1, const Vec3& 
     return out;
 }
 
+
+// energy/abd_energy.hpp:9-42: rigidity penalty kappa V |A^T A - I|_F^2 on the
+// affine part of q = [p, row0(A), row1(A), row2(A)]
+inline Stencil12 abd_orthogonality(const Real* q, Real kappa, Real rest_volume, bool project = true) {
+    Mat3 A;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) A(r, c) = q[3 + 3 * r + c];
+    Mat3 C;  // A^T A - I (Eigen lazy product: k ascending from the first term)
+    for (int c = 0; c < 3; ++c)
+        for (int r = 0; r < 3; ++r) C(r, c) = (A(0, r) * A(0, c) + A(1, r) * A(1, c) + A(2, r) * A(2, c)) - (r == c ? 1.0 : 0.0);
+    const Real kv = kappa * rest_volume;
+    Stencil12 out;
+    Real cn = 0;
+    for (int k = 0; k < 9; ++k) cn += C.m[k] * C.m[k];
+    out.value = kv * cn;
+    Mat3 G;  // 4 kv A C
+    for (int c = 0; c < 3; ++c)
+        for (int r = 0; r < 3; ++r) G(r, c) = (4 * kv * A(r, 0)) * C(0, c) + (4 * kv * A(r, 1)) * C(1, c) + (4 * kv * A(r, 2)) * C(2, c);
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) out.grad[3 + 3 * r + c] = G(r, c);
+    Mat3 AAt;
+    for (int c = 0; c < 3; ++c)
+        for (int r = 0; r < 3; ++r) AAt(r, c) = A(r, 0) * A(c, 0) + A(r, 1) * A(c, 1) + A(r, 2) * A(c, 2);
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+            for (int s2 = 0; s2 < 3; ++s2)
+                for (int t = 0; t < 3; ++t) {
+                    const Real v = A(r, t) * A(s2, c) + (r == s2 ? C(t, c) : 0.0) + (t == c ? AAt(r, s2) : 0.0);
+                    out.hess[12 * (3 + 3 * s2 + t) + 3 + 3 * r + c] = 4 * kv * v;
+                }
+    if (project) {
+        Real P[144];
+        oracle_eig::project_psd(12, out.hess, P);
+        for (int k = 0; k < 144; ++k) out.hess[k] = P[k];
+    }
+    return out;
+}
+
 // One deformable solid part of the scene for the producer: tets as global
 // slot ids (mesh offset applied), rest data and material per mesh.
 struct FemSolids {
@@ -1089,15 +1127,26 @@ struct FemSolids {
     std::vector<Real> mu, lam;           // per mesh
 };
 
-// IncrementalPotential::assemble for inertia + solid meshes, up to (not
-// including) filter_pinned / sort / reduce: returns the value, fills grad
-// (3 n, zeroed on pinned slots, :253-254) and the triplet stream in emission
-// order (inertia diagonals of every vertex, then 10 blocks per tet, a <= b).
+// Affine bodies of the scene (scene.hpp Body): q, q_tilde, reduced mass
+// (12 x 12 column-major), orthogonality stiffness and rest volume; body b
+// owns block rows n_fem + 4 b .. + 3 (DofMap, abd_reduce.hpp:11-27).
+struct Bodies {
+    std::vector<Real> q, q_tilde, reduced_mass, kappa, volume;  // 12, 12, 144, 1, 1 per body
+    std::size_t size() const { return kappa.size(); }
+};
+
+// IncrementalPotential::assemble for inertia + solid meshes + affine bodies,
+// up to (not including) assemble_contact / filter_pinned / sort / reduce:
+// returns the value, fills grad (3 (n + 4 nb), zeroed on pinned slots,
+// :253-254) and the triplet stream in emission order (:170-249): inertia
+// diagonals of every vertex, body inertia tiles (split_sym_12x12 of the
+// reduced mass), 10 blocks per tet, body orthogonality tiles.
 inline Real ip_fem_assemble(const std::vector<Vec3>& x, const std::vector<Vec3>& x_tilde, const std::vector<Real>& mass,
                             const FemSolids& fs, Real dt2, const std::vector<char>& pinned, std::vector<Real>& grad,
-                            BlockTripletStream& stream, bool project = true) {
+                            BlockTripletStream& stream, bool project = true, const Bodies* bodies = nullptr) {
     const std::size_t n = x.size();
-    grad.assign(3 * n, 0.0);
+    const std::size_t nb = bodies ? bodies->size() : 0;
+    grad.assign(3 * (n + 4 * nb), 0.0);
     stream.keys.clear();
     stream.values.clear();
     Real val = 0;
@@ -1109,6 +1158,31 @@ inline Real ip_fem_assemble(const std::vector<Vec3>& x, const std::vector<Vec3>&
         Mat3 m;
         m(0, 0) = m(1, 1) = m(2, 2) = mass[v];
         stream.emit(static_cast<Index>(v), static_cast<Index>(v), m);
+    }
+    auto split_sym = [&](Index base, const Real* H) {  // block_split.hpp:19-23
+        for (int ti = 0; ti < 4; ++ti)
+            for (int tj = ti; tj < 4; ++tj) {
+                Mat3 blk;
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r) blk(r, c) = H[12 * (3 * tj + c) + 3 * ti + r];
+                stream.emit(base + ti, base + tj, blk);
+            }
+    };
+    for (std::size_t b = 0; b < nb; ++b) {  // :181-188
+        const Index base = static_cast<Index>(n + 4 * b);
+        const Real* M = &bodies->reduced_mass[144 * b];
+        Real dq[12], g[12];
+        for (int k = 0; k < 12; ++k) dq[k] = bodies->q[12 * b + k] - bodies->q_tilde[12 * b + k];
+        Real dg = 0;
+        for (int i = 0; i < 12; ++i) {
+            Real s2 = 0;
+            for (int k = 0; k < 12; ++k) s2 += M[12 * k + i] * dq[k];
+            g[i] = s2;
+        }
+        for (int k = 0; k < 12; ++k) dg += dq[k] * g[k];
+        val += 0.5 * dg;
+        for (int k = 0; k < 12; ++k) grad[3 * base + k] += g[k];
+        split_sym(base, M);
     }
     const std::size_t nt = fs.rest.size();
     std::vector<Stencil12> st(nt);
@@ -1136,7 +1210,16 @@ inline Real ip_fem_assemble(const std::vector<Vec3>& x, const std::vector<Vec3>&
                 stream.emit(te[a], te[b], blk);
             }
     }
-    for (std::size_t v = 0; v < n && v < pinned.size(); ++v)
+    for (std::size_t b = 0; b < nb; ++b) {  // :242-249
+        const Index base = static_cast<Index>(n + 4 * b);
+        const Stencil12 st = abd_orthogonality(&bodies->q[12 * b], bodies->kappa[b], bodies->volume[b], project);
+        val += dt2 * st.value;
+        for (int k = 0; k < 12; ++k) grad[3 * base + k] += dt2 * st.grad[k];
+        Real H[144];
+        for (int k = 0; k < 144; ++k) H[k] = dt2 * st.hess[k];
+        split_sym(base, H);
+    }
+    for (std::size_t v = 0; v < n + 4 * nb && v < pinned.size(); ++v)
         if (pinned[v])
             for (int k = 0; k < 3; ++k) grad[3 * v + k] = 0;
     return val;

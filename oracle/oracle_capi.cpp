@@ -252,6 +252,14 @@ void oracle_stable_neo_hookean(const double* x12, const double* inv9, double vol
 
 void oracle_project_psd(int n, const double* M, double* out) { oracle_eig::project_psd(n, M, out); }
 
+void oracle_abd_orthogonality(const double* q12, double kappa, double volume, int project, double* value,
+                              double* grad12, double* hess144) {
+    const Stencil12 s = abd_orthogonality(q12, kappa, volume, project != 0);
+    *value = s.value;
+    std::memcpy(grad12, s.grad, 96);
+    std::memcpy(hess144, s.hess, 1152);
+}
+
 // IncrementalPotential::assemble, inertia + solid meshes (see oracle.hpp):
 // stream written to keys / vals9 (capacity n_verts + 10 n_tets), grad 3n;
 // returns the stream length
@@ -259,7 +267,9 @@ std::int64_t oracle_ip_fem_assemble(std::int32_t n_verts, const double* x, const
                                     std::int32_t n_meshes, const std::int64_t* tet_begin, const double* mu,
                                     const double* lam, const std::int32_t* tets, const double* inv9, const double* vol,
                                     double dt2, const std::uint8_t* pinned, int project, std::uint64_t* keys,
-                                    double* vals9, double* grad, double* value) {
+                                    double* vals9, double* grad, double* value, std::int32_t n_bodies, const double* q,
+                                    const double* q_tilde, const double* reduced_mass, const double* kappa,
+                                    const double* body_volume) {
     std::vector<Vec3> xs(n_verts), xt(n_verts);
     for (std::int32_t v = 0; v < n_verts; ++v) {
         xs[v] = ld3(x + 3 * v);
@@ -277,12 +287,21 @@ std::int64_t oracle_ip_fem_assemble(std::int32_t n_verts, const double* x, const
     fs.tet_begin.assign(tet_begin, tet_begin + n_meshes + 1);
     fs.mu.assign(mu, mu + n_meshes);
     fs.lam.assign(lam, lam + n_meshes);
-    std::vector<char> pin(n_verts, 0);
+    const std::int32_t n_slots = n_verts + 4 * n_bodies;
+    std::vector<char> pin(n_slots, 0);
     if (pinned)
-        for (std::int32_t v = 0; v < n_verts; ++v) pin[v] = static_cast<char>(pinned[v]);
+        for (std::int32_t v = 0; v < n_slots; ++v) pin[v] = static_cast<char>(pinned[v]);
+    Bodies bodies;
+    if (n_bodies > 0) {
+        bodies.q.assign(q, q + 12 * n_bodies);
+        bodies.q_tilde.assign(q_tilde, q_tilde + 12 * n_bodies);
+        bodies.reduced_mass.assign(reduced_mass, reduced_mass + 144 * n_bodies);
+        bodies.kappa.assign(kappa, kappa + n_bodies);
+        bodies.volume.assign(body_volume, body_volume + n_bodies);
+    }
     std::vector<Real> g;
     BlockTripletStream s;
-    *value = ip_fem_assemble(xs, xt, m, fs, dt2, pin, g, s, project != 0);
+    *value = ip_fem_assemble(xs, xt, m, fs, dt2, pin, g, s, project != 0, &bodies);
     for (std::size_t k = 0; k < g.size(); ++k) grad[k] = g[k];
     store_stream(s, keys, vals9);
     return static_cast<std::int64_t>(s.size());

@@ -106,7 +106,8 @@ def lib():
         "oracle_stable_neo_hookean": (None, [f64p, f64p, cd, cd, cd, ci, f64p, f64p, f64p]),
         "oracle_project_psd": (None, [ci, f64p, f64p]),
         "oracle_ip_fem_assemble": (i64, [i32, f64p, f64p, f64p, i32, i64p, f64p, f64p, i32p, f64p, f64p, cd, vp, ci,
-                                         u64p, f64p, f64p, f64p]),
+                                         u64p, f64p, f64p, f64p, i32, vp, vp, vp, vp, vp]),
+        "oracle_abd_orthogonality": (None, [f64p, cd, cd, ci, f64p, f64p, f64p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -398,18 +399,34 @@ def project_psd(M):
     return out.reshape(n, n).T.copy()
 
 
-def ip_fem_assemble(x, x_tilde, mass, tet_begin, mu, lam, tets, inv9, vol, dt2, pinned=None, project=True):
-    """IncrementalPotential::assemble restricted to inertia + solid meshes
-    (incremental_potential.hpp:170-180, 222-239, 310-318, 253-254) ->
-    (value, grad 3n, keys, vals) in emission order."""
+def abd_orthogonality(q12, kappa, volume, project=True):
+    """energy/abd_energy.hpp:19-42 -> (value, grad 12, hess 12x12)."""
+    v, g, h = np.empty(1), np.empty(12), np.empty(144)
+    lib().oracle_abd_orthogonality(np.ascontiguousarray(q12, np.float64).reshape(12), kappa, volume, int(project),
+                                   v, g, h)
+    return float(v[0]), g, h.reshape(12, 12).T.copy()
+
+
+def ip_fem_assemble(x, x_tilde, mass, tet_begin, mu, lam, tets, inv9, vol, dt2, pinned=None, project=True,
+                    bodies=None):
+    """IncrementalPotential::assemble restricted to inertia + solid meshes +
+    affine bodies (incremental_potential.hpp:170-249, 310-318, 253-254) ->
+    (value, grad 3 (n + 4 nb), keys, vals) in emission order. bodies: dict of
+    q (nb x 12), q_tilde, reduced_mass (nb x 12 x 12), kappa, volume."""
     x = np.ascontiguousarray(x, np.float64).reshape(-1)
     n = len(x) // 3
     tb = np.ascontiguousarray(tet_begin, np.int64)
     nm = len(tb) - 1
     nt = int(tb[-1])
-    cap = max(n + 10 * nt, 1)
+    nb = 0 if bodies is None else len(bodies["kappa"])
+    cap = max(n + 10 * nt + 20 * nb, 1)
     keys, vals = np.empty(cap, np.uint64), np.empty((cap, 9))
-    grad, val = np.empty(3 * n), np.empty(1)
+    grad, val = np.empty(3 * (n + 4 * nb)), np.empty(1)
+    bq = {}
+    if nb:
+        bq = {k: np.ascontiguousarray(bodies[k], np.float64) for k in ("q", "q_tilde", "kappa", "volume")}
+        bq["reduced_mass"] = np.ascontiguousarray(np.asarray(bodies["reduced_mass"], np.float64).transpose(0, 2, 1))
+    bp = lambda k: bq[k].ctypes.data if nb else None  # noqa: E731
     pin = None if pinned is None else np.ascontiguousarray(pinned, np.uint8)
     T = lib().oracle_ip_fem_assemble(n, x, np.ascontiguousarray(x_tilde, np.float64).reshape(-1),
                                      np.ascontiguousarray(mass, np.float64), nm, tb,
@@ -417,7 +434,8 @@ def ip_fem_assemble(x, x_tilde, mass, tet_begin, mu, lam, tets, inv9, vol, dt2, 
                                      np.ascontiguousarray(tets, np.int32).reshape(-1),
                                      np.ascontiguousarray(inv9, np.float64).reshape(-1),
                                      np.ascontiguousarray(vol, np.float64), dt2,
-                                     None if pin is None else pin.ctypes.data, int(project), keys, vals, grad, val)
+                                     None if pin is None else pin.ctypes.data, int(project), keys, vals, grad, val,
+                                     nb, bp("q"), bp("q_tilde"), bp("reduced_mass"), bp("kappa"), bp("volume"))
     return float(val[0]), grad, keys[:T].copy(), vals[:T].copy()
 
 

@@ -21,6 +21,7 @@
 #include <string>
 
 #include "adipc/contact/barrier.hpp"
+#include "adipc/energy/abd_energy.hpp"
 #include "adipc/energy/neo_hookean.hpp"
 #include "adipc/energy/psd.hpp"
 #include "adipc/precond/block_jacobi.hpp"
@@ -269,6 +270,16 @@ void ref_stable_neo_hookean(const double* x12, const double* inv9, double vol, d
     *value = s.value;
     std::memcpy(grad12, s.grad.data(), 96);
     std::memcpy(hess144, s.hess.data(), 144 * 8);
+}
+
+void ref_abd_orthogonality(const double* q12, double kappa, double volume, int project, double* value,
+                           double* grad12, double* hess144) {
+    Vec12 q;
+    std::memcpy(q.data(), q12, 96);
+    const Stencil12 s = abd_orthogonality(q, kappa, volume, project != 0);
+    *value = s.value;
+    std::memcpy(grad12, s.grad.data(), 96);
+    std::memcpy(hess144, s.hess.data(), 1152);
 }
 
 void ref_project_psd(int n, const double* M, double* out) {

@@ -36,7 +36,9 @@ class FemDesc(C.Structure):
     _fields_ = [("n_verts", C.c_int32), ("x", C.c_void_p), ("x_tilde", C.c_void_p), ("mass", C.c_void_p),
                 ("n_meshes", C.c_int32), ("tet_begin", C.c_void_p), ("mu", C.c_void_p), ("lam", C.c_void_p),
                 ("tets", C.c_void_p), ("rest_inv9", C.c_void_p), ("rest_volume", C.c_void_p), ("dt2", C.c_double),
-                ("project", C.c_int), ("pinned", C.c_void_p)]
+                ("project", C.c_int), ("pinned", C.c_void_p), ("n_bodies", C.c_int32), ("q", C.c_void_p),
+                ("q_tilde", C.c_void_p), ("reduced_mass", C.c_void_p), ("body_kappa", C.c_void_p),
+                ("body_volume", C.c_void_p)]
 
 
 class ContactDesc(C.Structure):
@@ -86,6 +88,7 @@ GPU_SIGNATURES = {
     "adipc_gpu_contact_value_device": (ci, [vp, C.POINTER(ContactDesc), cd, C.POINTER(cd)]),
     "adipc_gpu_ccd_step_device": (ci, [vp, C.POINTER(ContactDesc), vp, C.POINTER(cd)]),
     "adipc_gpu_fem_emit_device": (ci, [vp, C.POINTER(FemDesc), vp, vp, vp, C.POINTER(cd)]),
+    "adipc_gpu_fem_value_device": (ci, [vp, C.POINTER(FemDesc), vp, C.POINTER(cd)]),
     "adipc_gpu_fem_assemble_device": (ci, [vp, C.POINTER(FemDesc), vp, C.POINTER(cd), C.POINTER(i64)]),
     "adipc_gpu_filter_pinned_device": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
     "adipc_gpu_spmv": (ci, [vp, vp, vp]),

@@ -180,6 +180,11 @@ class Context:
         d = _lib.FemDesc(n, ptr(x), ptr(x_tilde), ptr(mesh["mass"]), len(tb) - 1, tb.ctypes.data, mu.ctypes.data,
                          lam.ctypes.data, ptr(mesh["tets"]), ptr(mesh["rest_inv9"]), ptr(mesh["rest_volume"]),
                          float(dt2), int(project), ptr(pinned) if pinned is not None else None)
+        b = mesh.get("bodies")  # device tensors q / q_tilde (nb x 12), reduced_mass (nb x 144), kappa, volume
+        if b is not None:
+            d.n_bodies = int(b["kappa"].numel())
+            d.q, d.q_tilde, d.reduced_mass = ptr(b["q"]), ptr(b["q_tilde"]), ptr(b["reduced_mass"])
+            d.body_kappa, d.body_volume = ptr(b["kappa"]), ptr(b["volume"])
         return d, (tb, mu, lam), n
 
     def fem_emit(self, mesh, x, x_tilde, dt2, keys, vals, grad, project=True, pinned=None):
@@ -190,6 +195,14 @@ class Context:
         v = C.c_double()
         self._check(self._L.adipc_gpu_fem_emit_device(self.h, C.byref(d), ptr(keys), ptr(vals), ptr(grad),
                                                       C.byref(v)))
+        return v.value
+
+    def fem_value(self, mesh, x, x_tilde, dt2, grad=None, pinned=None):
+        """IncrementalPotential::value's inertia + elastic + body terms (the
+        line search); optionally the gradient."""
+        d, keep, _ = self._fem_desc(mesh, x, x_tilde, dt2, False, pinned)
+        v = C.c_double()
+        self._check(self._L.adipc_gpu_fem_value_device(self.h, C.byref(d), ptr(grad), C.byref(v)))
         return v.value
 
     def fem_assemble(self, mesh, x, x_tilde, dt2, grad, project=True, pinned=None):

@@ -357,11 +357,21 @@ static FemDesc fem_desc(const adipc_fem_desc* d) {
     f.dt2 = d->dt2;
     f.project = d->project;
     f.pinned = d->pinned;
+    if (d->n_bodies < 0) throw StatusError(kInvalidArgument, "negative size");
+    if (d->n_bodies > 0 && (!d->q || !d->q_tilde || !d->reduced_mass || !d->body_kappa || !d->body_volume))
+        throw StatusError(kInvalidArgument, "missing body arrays");
+    f.n_bodies = d->n_bodies;
+    f.q = d->q;
+    f.q_tilde = d->q_tilde;
+    f.reduced_mass = d->reduced_mass;
+    f.body_kappa = d->body_kappa;
+    f.body_volume = d->body_volume;
     return f;
 }
 
 static std::int64_t fem_stream_len(const adipc_fem_desc* d) {
-    return static_cast<std::int64_t>(d->n_verts) + 10 * (d->n_meshes > 0 ? d->tet_begin[d->n_meshes] : 0);
+    return static_cast<std::int64_t>(d->n_verts) + 10 * (d->n_meshes > 0 ? d->tet_begin[d->n_meshes] : 0) +
+           20 * static_cast<std::int64_t>(d->n_bodies);
 }
 
 int adipc_gpu_fem_emit_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* d, uint64_t* d_keys, double* d_vals9,
@@ -371,6 +381,17 @@ int adipc_gpu_fem_emit_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* d, uint6
         const FemDesc f = fem_desc(d);
         c.fem_value.reserve(1);
         fem_emit(c, f, d_keys, d_vals9, d_grad, c.fem_value.p);
+        if (value) ADIPC_CUDA(cudaMemcpyAsync(value, c.fem_value.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        sync(c);
+    });
+}
+
+int adipc_gpu_fem_value_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* d, double* d_grad, double* value) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const FemDesc f = fem_desc(d);
+        c.fem_value.reserve(1);
+        fem_emit(c, f, nullptr, nullptr, d_grad, c.fem_value.p);
         if (value) ADIPC_CUDA(cudaMemcpyAsync(value, c.fem_value.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
         sync(c);
     });
@@ -387,7 +408,7 @@ int adipc_gpu_fem_assemble_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* d, d
         c.fem_value.reserve(1);
         timed(c, [&] {
             fem_emit(c, f, c.fem_keys.p, c.fem_vals.p, d_grad, c.fem_value.p);
-            assemble_filtered(c, c.fem_keys.p, c.fem_vals.p, T, d->n_verts, d->pinned);
+            assemble_filtered(c, c.fem_keys.p, c.fem_vals.p, T, d->n_verts + 4 * d->n_bodies, d->pinned);
         });
         if (value) ADIPC_CUDA(cudaMemcpyAsync(value, c.fem_value.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
         sync(c);

@@ -260,7 +260,14 @@ struct FemDesc {
     const double* rest_volume = nullptr;    // per tet
     double dt2 = 0;
     int project = 1;
-    const std::uint8_t* pinned = nullptr;   // n_verts or null
+    const std::uint8_t* pinned = nullptr;   // n_verts + 4 n_bodies or null
+    // affine bodies (block rows n_verts + 4 b .. + 3)
+    std::int32_t n_bodies = 0;
+    const double* q = nullptr;             // 12 per body
+    const double* q_tilde = nullptr;       // 12 per body
+    const double* reduced_mass = nullptr;  // 144 per body, column-major
+    const double* body_kappa = nullptr;
+    const double* body_volume = nullptr;
 };
 void fem_emit(Ctx& c, const FemDesc& d, std::uint64_t* d_keys, double* d_vals, double* d_grad, double* d_value);
 

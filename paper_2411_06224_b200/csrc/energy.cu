@@ -70,9 +70,12 @@ __global__ void k_fem_inertia(std::int32_t n, const double* __restrict__ x, cons
         const double m = mass[v];
         const double d0 = x[3 * v] - xt[3 * v], d1 = x[3 * v + 1] - xt[3 * v + 1], d2 = x[3 * v + 2] - xt[3 * v + 2];
         e += 0.5 * m * (d0 * d0 + d1 * d1 + d2 * d2);
-        grad[3 * v] = m * d0;
-        grad[3 * v + 1] = m * d1;
-        grad[3 * v + 2] = m * d2;
+        if (grad) {
+            grad[3 * v] = m * d0;
+            grad[3 * v + 1] = m * d1;
+            grad[3 * v + 2] = m * d2;
+        }
+        if (!keys) continue;  // value only (the line search)
         keys[v] = (static_cast<std::uint64_t>(v) << 32) | static_cast<std::uint64_t>(v);
         double* o = vals + 9 * v;
 #pragma unroll
@@ -142,14 +145,17 @@ __global__ void __launch_bounds__(kFemThreads) k_fem_tets(std::int64_t n_tets, c
         double P[9];
 #pragma unroll
         for (int k = 0; k < 9; ++k) P[k] = mu * s.F[k] + s.dJ * s.cof[k];
+        if (grad) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const std::int64_t o = 3 * static_cast<std::int64_t>(ids[a]);
+            for (int a = 0; a < 4; ++a) {
+                const std::int64_t o = 3 * static_cast<std::int64_t>(ids[a]);
 #pragma unroll
-            for (int k = 0; k < 3; ++k)
-                red_add_f64(grad + o + k,
-                            dt2 * (s.V * (P[k] * C[a][0] + P[3 + k] * C[a][1] + P[6 + k] * C[a][2])));
+                for (int k = 0; k < 3; ++k)
+                    red_add_f64(grad + o + k,
+                                dt2 * (s.V * (P[k] * C[a][0] + P[3 + k] * C[a][1] + P[6 + k] * C[a][2])));
+            }
         }
+        if (!keys) continue;  // value (+ gradient) only
         // PSD test in the reduced space: R = Q^T C, M_jl = stencil(r_j, r_l)
         bool psd = !project;
         double R[3][3];
@@ -231,6 +237,94 @@ __global__ void __launch_bounds__(kFemThreads) k_fem_tets(std::int64_t n_tets, c
     block_sum_atomic(dt2 * e, value);
 }
 
+
+// affine-body inertia (incremental_potential.hpp:181-188): g = M dq written
+// to the body's 12 gradient entries, 0.5 dq.g to the value, the reduced mass
+// as split_sym_12x12 tiles (block_split.hpp:19-23)
+__global__ void k_body_inertia(std::int32_t nb, std::int32_t base0, const double* __restrict__ q,
+                               const double* __restrict__ qt, const double* __restrict__ M12,
+                               std::uint64_t* __restrict__ keys, double* __restrict__ vals, double* __restrict__ grad,
+                               double* __restrict__ value) {
+    double e = 0;
+    for (std::int64_t b = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; b < nb;
+         b += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const double* M = M12 + 144 * b;
+        double dq[12], g[12];
+        for (int k = 0; k < 12; ++k) dq[k] = q[12 * b + k] - qt[12 * b + k];
+        double dg = 0;
+        for (int i = 0; i < 12; ++i) {
+            double s = 0;
+            for (int k = 0; k < 12; ++k) s += M[12 * k + i] * dq[k];
+            g[i] = s;
+        }
+        for (int k = 0; k < 12; ++k) dg += dq[k] * g[k];
+        e += 0.5 * dg;
+        const std::int64_t base = base0 + 4 * b;
+        if (grad)
+            for (int k = 0; k < 12; ++k) grad[3 * base + k] = g[k];
+        if (!keys) continue;
+        int t = 0;
+        for (int ti = 0; ti < 4; ++ti)
+            for (int tj = ti; tj < 4; ++tj, ++t) {
+                const std::int64_t o = 10 * b + t;
+                keys[o] = (static_cast<std::uint64_t>(base + ti) << 32) | static_cast<std::uint64_t>(base + tj);
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r) vals[9 * o + 3 * c + r] = M[12 * (3 * tj + c) + 3 * ti + r];
+            }
+    }
+    block_sum_atomic(e, value);
+}
+
+// affine-body orthogonality (energy/abd_energy.hpp:19-42; :242-249): the
+// stencil lives on the 9 affine dofs only, so its PSD projection is the 9 x 9
+// block's; dt^2-scaled split_sym_12x12 tiles, gradient added
+__global__ void k_body_orth(std::int32_t nb, std::int32_t base0, const double* __restrict__ q,
+                            const double* __restrict__ kappa, const double* __restrict__ vol, double dt2, int project,
+                            std::uint64_t* __restrict__ keys, double* __restrict__ vals, double* __restrict__ grad,
+                            double* __restrict__ value) {
+    double e = 0;
+    for (std::int64_t b = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; b < nb;
+         b += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        double A[3][3], C[3][3], AAt[3][3];
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) A[r][c] = q[12 * b + 3 + 3 * r + c];
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) {
+                C[r][c] = (A[0][r] * A[0][c] + A[1][r] * A[1][c] + A[2][r] * A[2][c]) - (r == c ? 1.0 : 0.0);
+                AAt[r][c] = A[r][0] * A[c][0] + A[r][1] * A[c][1] + A[r][2] * A[c][2];
+            }
+        const double kv = kappa[b] * vol[b];
+        double cn = 0;
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) cn += C[r][c] * C[r][c];
+        e += kv * cn;
+        const std::int64_t base = base0 + 4 * b;
+        for (int r = 0; r < 3 && grad; ++r)
+            for (int c = 0; c < 3; ++c)
+                red_add_f64(grad + 3 * base + 3 + 3 * r + c,
+                            dt2 * ((4 * kv * A[r][0]) * C[0][c] + (4 * kv * A[r][1]) * C[1][c] + (4 * kv * A[r][2]) * C[2][c]));
+        if (!keys) continue;
+        double M[81];  // the affine 9 x 9 block, column-major
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c)
+                for (int s2 = 0; s2 < 3; ++s2)
+                    for (int t = 0; t < 3; ++t)
+                        M[9 * (3 * s2 + t) + 3 * r + c] =
+                            4 * kv * (A[r][t] * A[s2][c] + (r == s2 ? C[t][c] : 0.0) + (t == c ? AAt[r][s2] : 0.0));
+        if (project && !psd9(M)) project9(M);
+        auto h12 = [&](int i, int j) { return (i < 3 || j < 3) ? 0.0 : M[9 * (j - 3) + (i - 3)]; };
+        int t = 0;
+        for (int ti = 0; ti < 4; ++ti)
+            for (int tj = ti; tj < 4; ++tj, ++t) {
+                const std::int64_t o = 10 * b + t;
+                keys[o] = (static_cast<std::uint64_t>(base + ti) << 32) | static_cast<std::uint64_t>(base + tj);
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r) vals[9 * o + 3 * c + r] = dt2 * h12(3 * ti + r, 3 * tj + c);
+            }
+    }
+    block_sum_atomic(dt2 * e, value);
+}
+
 // pinned slots: zero gradient (incremental_potential.hpp:253-254)
 __global__ void k_fem_pin_grad(std::int32_t n, const std::uint8_t* __restrict__ pinned, double* __restrict__ grad) {
     for (std::int64_t v = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; v < n;
@@ -240,8 +334,12 @@ __global__ void k_fem_pin_grad(std::int32_t n, const std::uint8_t* __restrict__ 
 
 }  // namespace
 
-// The stream (n_verts + 10 n_tets entries), the gradient (3 n_verts) and the
-// value (one device double) of inertia + every solid mesh.
+// The stream (n_verts + 10 n_tets + 20 n_bodies entries), the gradient
+// (3 (n_verts + 4 n_bodies)) and the value (one device double) of inertia,
+// every solid mesh and the affine bodies. d_keys / d_vals null: the value
+// (and, with d_grad, the gradient) only — IncrementalPotential::value for
+// the line search (incremental_potential.hpp:61-131, raw stencils: the
+// projection does not change values).
 void fem_emit(Ctx& c, const FemDesc& d, std::uint64_t* d_keys, double* d_vals, double* d_grad, double* d_value) {
     cudaStream_t st = c.stream;
     ADIPC_CUDA(cudaMemsetAsync(d_value, 0, sizeof(double), st));
@@ -250,16 +348,35 @@ void fem_emit(Ctx& c, const FemDesc& d, std::uint64_t* d_keys, double* d_vals, d
                                                                  d_grad, d_value);
         ADIPC_LAUNCH_CHECK();
     }
+    // stream layout (incremental_potential.hpp:170-249): vertex inertia, body
+    // inertia tiles, 10 blocks per tet, body orthogonality tiles
+    const std::int64_t nb = d.n_bodies;
+    const std::int64_t n_tets = d.n_meshes > 0 ? d.tet_begin[d.n_meshes] : 0;
+    const std::int64_t tets0 = d.n_verts + 10 * nb, orth0 = tets0 + 10 * n_tets;
+    if (nb > 0) {
+        k_body_inertia<<<grid_for(nb, 128, 8), 128, 0, st>>>(d.n_bodies, d.n_verts, d.q, d.q_tilde, d.reduced_mass,
+                                                             d_keys ? d_keys + d.n_verts : nullptr,
+                                                             d_vals ? d_vals + 9 * d.n_verts : nullptr, d_grad, d_value);
+        ADIPC_LAUNCH_CHECK();
+    }
     for (int m = 0; m < d.n_meshes; ++m) {
         const std::int64_t t0 = d.tet_begin[m], nt = d.tet_begin[m + 1] - t0;
         if (nt <= 0) continue;
         k_fem_tets<<<grid_for(nt, kFemThreads, 16), kFemThreads, 0, st>>>(
             nt, d.tets + 4 * t0, d.rest_inv9 + 9 * t0, d.rest_volume + t0, d.x, d.mu[m], d.lambda[m], d.dt2,
-            d.project, d_keys + d.n_verts + 10 * t0, d_vals + 9 * (d.n_verts + 10 * t0), d_grad, d_value);
+            d.project, d_keys ? d_keys + tets0 + 10 * t0 : nullptr, d_vals ? d_vals + 9 * (tets0 + 10 * t0) : nullptr,
+            d_grad, d_value);
         ADIPC_LAUNCH_CHECK();
     }
-    if (d.pinned && d.n_verts > 0) {
-        k_fem_pin_grad<<<grid_for(d.n_verts, 256, 8), 256, 0, st>>>(d.n_verts, d.pinned, d_grad);
+    if (nb > 0) {
+        k_body_orth<<<grid_for(nb, 128, 8), 128, 0, st>>>(d.n_bodies, d.n_verts, d.q, d.body_kappa, d.body_volume,
+                                                          d.dt2, d.project, d_keys ? d_keys + orth0 : nullptr,
+                                                          d_vals ? d_vals + 9 * orth0 : nullptr, d_grad, d_value);
+        ADIPC_LAUNCH_CHECK();
+    }
+    const std::int32_t n_slots = d.n_verts + 4 * d.n_bodies;
+    if (d_grad && d.pinned && n_slots > 0) {
+        k_fem_pin_grad<<<grid_for(n_slots, 256, 8), 256, 0, st>>>(n_slots, d.pinned, d_grad);
         ADIPC_LAUNCH_CHECK();
     }
 }

@@ -158,3 +158,56 @@ def test_cfg5_device_matrix_equals_streamed_matrix(ctx):
     assert np.abs(blocks - blocks2).max() <= 1e-11 * np.abs(blocks2).max()
     b = scenes.gravity_rhs(sc)
     assert np.abs(-grad.cpu().numpy() - b).max() <= 1e-9 * np.abs(b).max()
+
+
+def bodies_case(nb, seed):
+    rng = np.random.default_rng(seed)
+    q = np.zeros((nb, 12))
+    q[:, :3] = rng.normal(0, 1, (nb, 3))
+    q[:, 3:] = (np.eye(3)[None] + rng.normal(0, 0.05, (nb, 3, 3))).reshape(nb, 9)
+    qt = q + rng.normal(0, 1e-3, q.shape)
+    L = rng.normal(0, 1, (nb, 12, 12))
+    M = L @ L.transpose(0, 2, 1) + 12 * np.eye(12)[None]
+    return {"q": q, "q_tilde": qt, "reduced_mass": M, "kappa": rng.uniform(1e6, 1e8, nb),
+            "volume": rng.uniform(1e-4, 1e-3, nb)}
+
+
+def test_fem_emit_with_bodies_and_value(ctx):
+    """Inertia + tets + affine bodies (incremental_potential.hpp:170-249):
+    body inertia tiles after the vertex inertia, orthogonality tiles
+    (abd_energy.hpp:19-42) after the tets; the value-only entry (the line
+    search's IncrementalPotential::value, :61-131) equals the emit's value."""
+    sc = scenes.CONFIGS["cfg1_soft_cube"]()
+    mesh, inv9, vol = device_mesh(sc)
+    nb = 7
+    bd = bodies_case(nb, 3)
+    mesh["bodies"] = {"q": torch.from_numpy(bd["q"]).cuda(), "q_tilde": torch.from_numpy(bd["q_tilde"]).cuda(),
+                      "reduced_mass": torch.from_numpy(np.ascontiguousarray(bd["reduced_mass"].transpose(0, 2, 1)))
+                      .cuda(), "kappa": torch.from_numpy(bd["kappa"]).cuda(),
+                      "volume": torch.from_numpy(bd["volume"]).cuda()}
+    n, nt = len(sc.mass), len(sc.tets)
+    x = deformed(sc, 0.2, 11)
+    xt = scenes.inertial_target(sc)
+    pinned = np.zeros(n + 4 * nb, np.uint8)
+    pinned[:121] = 1
+    pinned[n + 4] = 1  # one body block
+    T = n + 10 * nt + 20 * nb
+    keys = torch.empty(T, dtype=torch.int64, device="cuda:0")
+    vals = torch.empty((T, 9), dtype=torch.float64, device="cuda:0")
+    grad = torch.empty(3 * (n + 4 * nb), dtype=torch.float64, device="cuda:0")
+    dx, dxt, dpin = torch.from_numpy(x).cuda(), torch.from_numpy(xt).cuda(), torch.from_numpy(pinned).cuda()
+    val = ctx.fem_emit(mesh, dx, dxt, DT2, keys, vals, grad, pinned=dpin)
+    ov, og, ok, ovals = O.ip_fem_assemble(x, xt, sc.mass, [0, nt], [sc.mu], [sc.lam], sc.tets, inv9, vol, DT2,
+                                          pinned, bodies=bd)
+    keys = keys.cpu().numpy().view(np.uint64)
+    vals = vals.cpu().numpy()
+    assert np.array_equal(keys, ok)
+    for lo, hi in ((0, n + 10 * nb), (n + 10 * nb, n + 10 * nb + 10 * nt), (n + 10 * nb + 10 * nt, T)):
+        assert np.abs(vals[lo:hi] - ovals[lo:hi]).max() <= 1e-10 * np.abs(ovals[lo:hi]).max()
+    g = grad.cpu().numpy()
+    assert np.linalg.norm(g - og) <= 1e-12 * np.linalg.norm(og)
+    assert abs(val - ov) <= 1e-12 * abs(ov)
+    g2 = torch.empty_like(grad)
+    v2 = ctx.fem_value(mesh, dx, dxt, DT2, g2, pinned=dpin)
+    assert abs(v2 - val) <= 1e-13 * abs(val)
+    assert torch.allclose(g2, grad, rtol=0, atol=1e-12 * float(torch.abs(grad).max()))

@@ -160,4 +160,23 @@ inline PcgResult pcg_solve(GpuPreconditioner& M, const VecX& b, Real rel_tol, in
     return out;
 }
 
+// pcg.hpp:34 with the reference's own signature, so the newton.hpp:129-131
+// call site only gains the namespace: `gpu::pcg_solve(hess_, rhs,
+// gpu_precond_, cfg.pcg_rel_tol, cfg.pcg_restart, cfg.max_pcg, pol_, dir_)`.
+// M must be a GpuPreconditioner (std::invalid_argument otherwise: there is
+// no host PCG behind this call) and A the matrix assembled into its context
+// (same block rows and stored blocks; checked). The device path ignores the
+// ExecPolicy except through ADIPC_OPT_DETERMINISTIC on the context.
+inline PcgResult pcg_solve(const SortedSymBlockCoo& A, const VecX& b, const Preconditioner& M, Real rel_tol,
+                           int restart, int max_iters, const ExecPolicy& /*pol*/, VecX& x) {
+    const auto* g = dynamic_cast<const GpuPreconditioner*>(&M);
+    if (!g) throw std::invalid_argument("gpu::pcg_solve: the preconditioner is not a GpuPreconditioner");
+    int32_t n = 0;
+    int64_t U = 0;
+    check(adipc_gpu_matrix_info(g->context().get(), &n, &U), g->context().get());
+    if (n != A.n_block_rows || (!A.rows.empty() && static_cast<int64_t>(A.rows.size()) != U))
+        throw std::invalid_argument("gpu::pcg_solve: A is not the matrix assembled on the device");
+    return pcg_solve(const_cast<GpuPreconditioner&>(*g), b, rel_tol, restart, max_iters, x);
+}
+
 }  // namespace adipc::gpu

@@ -106,7 +106,7 @@ int main(int argc, char** argv) {
     VecX z_gpu;
     gm.apply(rhs, z_gpu);
     VecX x_gpu;
-    const PcgResult r_gpu = gpu::pcg_solve(gm, rhs, 1e-8, 250, 10000, x_gpu);
+    const PcgResult r_gpu = gpu::pcg_solve(Ag, rhs, gm, 1e-8, 250, 10000, det, x_gpu);  // the reference signature
 
     const double dz = rel_l2(z_gpu, z_cpu), dx = rel_l2(x_gpu, x_cpu);
     const int di = std::abs(r_gpu.iters - r_cpu.iters);

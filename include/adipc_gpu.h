@@ -257,6 +257,23 @@ int adipc_gpu_contact_value_device(adipc_gpu_ctx* ctx, const adipc_contact_desc*
 int adipc_gpu_ccd_step_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* desc, const double* d_disp,
                               double* alpha);
 
+
+/* ---- broad phase (contact/broad_phase.hpp:143-211) --------------
+ * Vertex-triangle and edge-edge candidates of the contact surface whose boxes,
+ * inflated by inflate/2 per side (and swept over d_disp when given:
+ * ccd_candidates), overlap; stencils sharing a node dropped; sorted and
+ * duplicate free (find_candidates' exact result). Device arrays: d_pos /
+ * d_disp 3 per node, d_verts (ContactSurface::verts), d_edges 2 / d_tris 3
+ * node ids each. The results stay in the context until the next call. */
+int adipc_gpu_broad_phase_device(adipc_gpu_ctx* ctx, int32_t n_nodes, const double* d_pos, const double* d_disp,
+                                 int32_t n_verts, const int32_t* d_verts, int32_t n_edges, const int32_t* d_edges,
+                                 int32_t n_tris, const int32_t* d_tris, double inflate, int64_t* n_pt, int64_t* n_ee);
+/* copy the last candidates (host or device destinations, any may be NULL):
+ * pairs as surface slots (vert, tri) / (edge, edge), stencils as node ids
+ * (v, t0, t1, t2) / (a0, a1, b0, b1) — the contact producer's input */
+int adipc_gpu_broad_phase_copy(adipc_gpu_ctx* ctx, int32_t* pt_pairs, int32_t* pt_stencils, int32_t* ee_pairs,
+                               int32_t* ee_stencils);
+
 /* IncrementalPotential::filter_pinned (incremental_potential.hpp:410-425):
  * drop blocks touching a pinned slot, append I3 per pinned slot.
  * out capacity >= T + n_slots. */

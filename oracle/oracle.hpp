@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <array>
 #include <limits>
+#include <unordered_map>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -1805,6 +1806,154 @@ inline Real ccd_step(const ContactInput& in, const std::vector<Vec3>& disp) {
         for (Index v : in.surf_verts)
             alpha = std::min(alpha, ground_ccd_toi(in.pos[v], disp[v], in.ground_normal, in.ground_height));
     return alpha;
+}
+
+// contact/broad_phase.hpp:13-226: contact surface primitives over the
+// contact-node universe, inflated (and swept) AABBs, a hash grid of the
+// triangle / edge boxes, vertex-triangle and edge-edge candidates sorted and
+// duplicate free, stencils sharing a node dropped.
+struct ContactSurface {
+    std::vector<Index> verts;
+    std::vector<std::array<Index, 2>> edges;
+    std::vector<std::array<Index, 3>> tris;
+};
+struct Aabb {  // :57-71
+    Real lo[3] = {std::numeric_limits<Real>::max(), std::numeric_limits<Real>::max(),
+                  std::numeric_limits<Real>::max()};
+    Real hi[3] = {-std::numeric_limits<Real>::max(), -std::numeric_limits<Real>::max(),
+                  -std::numeric_limits<Real>::max()};
+    void grow(const Real* p) {
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], p[a]);
+            hi[a] = std::max(hi[a], p[a]);
+        }
+    }
+    void inflate(Real r) {
+        for (int a = 0; a < 3; ++a) {
+            lo[a] -= r;
+            hi[a] += r;
+        }
+    }
+    bool overlaps(const Aabb& o) const {
+        for (int a = 0; a < 3; ++a)
+            if (!(lo[a] <= o.hi[a] && o.lo[a] <= hi[a])) return false;
+        return true;
+    }
+};
+struct ContactCandidates {  // :76-79
+    std::vector<std::array<Index, 2>> pt, ee;
+};
+class HashGrid {  // :83-123
+public:
+    void build(const std::vector<Aabb>& boxes, Real cell_size) {
+        cell_ = cell_size;
+        cells_.clear();
+        for (std::size_t i = 0; i < boxes.size(); ++i)
+            visit(boxes[i], [&](std::uint64_t key) { cells_[key].push_back(static_cast<Index>(i)); });
+    }
+    template <class F>
+    void query(const Aabb& box, F&& fn) const {
+        visit(box, [&](std::uint64_t key) {
+            auto it = cells_.find(key);
+            if (it == cells_.end()) return;
+            for (Index id : it->second) fn(id);
+        });
+    }
+
+private:
+    template <class F>
+    void visit(const Aabb& box, F&& fn) const {
+        long lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = static_cast<long>(std::floor(box.lo[a] / cell_));
+            hi[a] = static_cast<long>(std::floor(box.hi[a] / cell_));
+        }
+        for (long x = lo[0]; x <= hi[0]; ++x)
+            for (long y = lo[1]; y <= hi[1]; ++y)
+                for (long z = lo[2]; z <= hi[2]; ++z) fn(pack(x, y, z));
+    }
+    static std::uint64_t pack(long x, long y, long z) {
+        const std::uint64_t m = (1u << 21) - 1;
+        auto wrap = [&](long v) { return static_cast<std::uint64_t>(v & static_cast<long>(m)); };
+        return (wrap(x) << 42) | (wrap(y) << 21) | wrap(z);
+    }
+    Real cell_ = 1;
+    std::unordered_map<std::uint64_t, std::vector<Index>> cells_;
+};
+inline Aabb swept_point(const std::vector<Vec3>& pos, const std::vector<Vec3>* disp, Index node) {  // :125-131
+    Aabb box;
+    box.grow(pos[node].v);
+    if (disp) {
+        Real e[3];
+        for (int a = 0; a < 3; ++a) e[a] = pos[node][a] + (*disp)[node][a];
+        box.grow(e);
+    }
+    return box;
+}
+inline void sort_unique(std::vector<std::array<Index, 2>>& pairs) {
+    std::sort(pairs.begin(), pairs.end());
+    pairs.erase(std::unique(pairs.begin(), pairs.end()), pairs.end());
+}
+// :143-211
+inline ContactCandidates find_candidates(const ContactSurface& surf, const std::vector<Vec3>& pos,
+                                         const std::vector<Vec3>* disp, Real inflate) {
+    ContactCandidates out;
+    const Real half = inflate / 2;
+    std::vector<Aabb> tri_boxes(surf.tris.size());
+    Real mean_extent = 0;
+    for (std::size_t t = 0; t < surf.tris.size(); ++t) {
+        Aabb box;
+        for (Index v : surf.tris[t]) {
+            const Aabb p = swept_point(pos, disp, v);
+            box.grow(p.lo);
+            box.grow(p.hi);
+        }
+        mean_extent += std::max({box.hi[0] - box.lo[0], box.hi[1] - box.lo[1], box.hi[2] - box.lo[2]});
+        box.inflate(half);
+        tri_boxes[t] = box;
+    }
+    std::vector<Aabb> edge_boxes(surf.edges.size());
+    for (std::size_t e = 0; e < surf.edges.size(); ++e) {
+        Aabb box;
+        for (Index v : surf.edges[e]) {
+            const Aabb p = swept_point(pos, disp, v);
+            box.grow(p.lo);
+            box.grow(p.hi);
+        }
+        box.inflate(half);
+        edge_boxes[e] = box;
+    }
+    if (surf.tris.empty() && surf.edges.empty()) return out;
+    mean_extent = surf.tris.empty() ? inflate : mean_extent / surf.tris.size();
+    const Real cell = std::max(mean_extent + inflate, 1e-12);
+    HashGrid tri_grid;
+    tri_grid.build(tri_boxes, cell);
+    for (std::size_t vi = 0; vi < surf.verts.size(); ++vi) {
+        const Index node = surf.verts[vi];
+        Aabb box = swept_point(pos, disp, node);
+        box.inflate(half);
+        tri_grid.query(box, [&](Index t) {
+            const auto& tri = surf.tris[t];
+            if (tri[0] == node || tri[1] == node || tri[2] == node) return;
+            if (!box.overlaps(tri_boxes[t])) return;
+            out.pt.push_back({static_cast<Index>(vi), t});
+        });
+    }
+    sort_unique(out.pt);
+    HashGrid edge_grid;
+    edge_grid.build(edge_boxes, cell);
+    for (std::size_t ei = 0; ei < surf.edges.size(); ++ei) {
+        const auto& ea = surf.edges[ei];
+        edge_grid.query(edge_boxes[ei], [&](Index ej) {
+            if (ej <= static_cast<Index>(ei)) return;
+            const auto& eb = surf.edges[ej];
+            if (ea[0] == eb[0] || ea[0] == eb[1] || ea[1] == eb[0] || ea[1] == eb[1]) return;
+            if (!edge_boxes[ei].overlaps(edge_boxes[ej])) return;
+            out.ee.push_back({static_cast<Index>(ei), ej});
+        });
+    }
+    sort_unique(out.ee);
+    return out;
 }
 
 }  // namespace oracle

@@ -412,6 +412,38 @@ double oracle_ccd_step(ORACLE_CONTACT_ARGS, const double* disp) {
     return ccd_step(in, d);
 }
 
+
+// broad_phase.hpp:143-211: candidates written as surface-slot pairs; returns
+// n_pt, *n_ee_out = n_ee (capacities pt_cap / ee_cap pairs)
+std::int64_t oracle_find_candidates(std::int32_t n_nodes, const double* pos, const double* disp, std::int32_t n_verts,
+                                    const std::int32_t* verts, std::int32_t n_edges, const std::int32_t* edges,
+                                    std::int32_t n_tris, const std::int32_t* tris, double inflate,
+                                    std::int32_t* pt_out, std::int64_t pt_cap, std::int32_t* ee_out,
+                                    std::int64_t ee_cap, std::int64_t* n_ee_out) {
+    std::vector<Vec3> p(n_nodes), d;
+    for (std::int32_t v = 0; v < n_nodes; ++v) p[v] = ld3(pos + 3 * v);
+    if (disp) {
+        d.resize(n_nodes);
+        for (std::int32_t v = 0; v < n_nodes; ++v) d[v] = ld3(disp + 3 * v);
+    }
+    ContactSurface s;
+    s.verts.assign(verts, verts + n_verts);
+    for (std::int32_t e = 0; e < n_edges; ++e) s.edges.push_back({edges[2 * e], edges[2 * e + 1]});
+    for (std::int32_t t = 0; t < n_tris; ++t) s.tris.push_back({tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]});
+    const ContactCandidates c = find_candidates(s, p, disp ? &d : nullptr, inflate);
+    *n_ee_out = static_cast<std::int64_t>(c.ee.size());
+    if (static_cast<std::int64_t>(c.pt.size()) > pt_cap || static_cast<std::int64_t>(c.ee.size()) > ee_cap) return -1;
+    for (std::size_t i = 0; i < c.pt.size(); ++i) {
+        pt_out[2 * i] = c.pt[i][0];
+        pt_out[2 * i + 1] = c.pt[i][1];
+    }
+    for (std::size_t i = 0; i < c.ee.size(); ++i) {
+        ee_out[2 * i] = c.ee[i][0];
+        ee_out[2 * i + 1] = c.ee[i][1];
+    }
+    return static_cast<std::int64_t>(c.pt.size());
+}
+
 // ---- partition / hierarchy ----------------------------------------------------
 std::int32_t oracle_subdomain_count(std::int32_t v, std::int32_t n, std::int32_t n_o) {
     return subdomain_count(v, n, n_o);

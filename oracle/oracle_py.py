@@ -103,6 +103,8 @@ def lib():
         "oracle_contact_assemble": (i64, _CONTACT_ARGS + [cd, ci, u64p, f64p, f64p, f64p]),
         "oracle_contact_value": (cd, _CONTACT_ARGS + [cd]),
         "oracle_ccd_step": (cd, _CONTACT_ARGS + [f64p]),
+        "oracle_find_candidates": (i64, [i32, f64p, vp, i32, vp, i32, vp, i32, vp, cd, vp, i64, vp, i64,
+                                         C.POINTER(i64)]),
         "oracle_stable_neo_hookean": (None, [f64p, f64p, cd, cd, cd, ci, f64p, f64p, f64p]),
         "oracle_project_psd": (None, [ci, f64p, f64p]),
         "oracle_ip_fem_assemble": (i64, [i32, f64p, f64p, f64p, i32, i64p, f64p, f64p, i32p, f64p, f64p, cd, vp, ci,
@@ -538,6 +540,26 @@ def contact_value(ci: ContactInput, dt2):
 def ccd_step(ci: ContactInput, disp):
     """contact/ccd.hpp:88-110 over the given stencils."""
     return float(lib().oracle_ccd_step(*ci.args(), np.ascontiguousarray(disp, np.float64).reshape(-1)))
+
+
+def find_candidates(pos, verts, edges, tris, inflate, disp=None):
+    """contact/broad_phase.hpp:143-211 -> (pt pairs (vert slot, tri slot),
+    ee pairs (edge slot, edge slot), both sorted, duplicate free)."""
+    pos = np.ascontiguousarray(pos, np.float64).reshape(-1)
+    v = np.ascontiguousarray(verts, np.int32).reshape(-1)
+    e = np.ascontiguousarray(edges, np.int32).reshape(-1)
+    t = np.ascontiguousarray(tris, np.int32).reshape(-1)
+    d = None if disp is None else np.ascontiguousarray(disp, np.float64).reshape(-1)
+    p = lambda a: a.ctypes.data if a is not None and a.size else None  # noqa: E731
+    cap_pt, cap_ee = max(len(v), 1) * 64, max(len(e) // 2, 1) * 64
+    while True:
+        pt, ee, nee = np.empty(2 * cap_pt, np.int32), np.empty(2 * cap_ee, np.int32), C.c_int64()
+        npt = lib().oracle_find_candidates(len(pos) // 3, pos, p(d), len(v), p(v), len(e) // 2, p(e), len(t) // 3,
+                                           p(t), float(inflate), pt.ctypes.data, cap_pt, ee.ctypes.data, cap_ee,
+                                           C.byref(nee))
+        if npt >= 0:
+            return pt[:2 * npt].reshape(-1, 2).copy(), ee[:2 * nee.value].reshape(-1, 2).copy()
+        cap_pt, cap_ee = cap_pt * 4, cap_ee * 4
 
 
 def filter_pinned(keys, vals, pinned):

@@ -23,7 +23,7 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-r
 CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"  # image's $CXX lacks libgomp.spec
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter"]
 
-GPU_SOURCES = ["assemble.cu", "spmv.cu", "mas.cu", "solve_order.cu", "pcg.cu", "abd.cu", "step.cu", "energy.cu", "contact.cu", "capi.cu", "host_precond.cpp"]
+GPU_SOURCES = ["assemble.cu", "spmv.cu", "mas.cu", "solve_order.cu", "pcg.cu", "abd.cu", "step.cu", "energy.cu", "contact.cu", "broad.cu", "capi.cu", "host_precond.cpp"]
 
 
 PER_FILE_FLAGS = {"contact.cu": ["-fmad=false"]}

@@ -83,6 +83,9 @@ GPU_SIGNATURES = {
     "adipc_gpu_assemble_contact_device": (ci, [vp, vp, vp, i64, vp, vp, i64, i32, i32, i32, vp, vp, i32, vp,
                                                C.POINTER(i64), C.POINTER(i64)]),
     "adipc_gpu_filter_pinned": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
+    "adipc_gpu_broad_phase_device": (ci, [vp, i32, vp, vp, i32, vp, i32, vp, i32, vp, cd, C.POINTER(i64),
+                                          C.POINTER(i64)]),
+    "adipc_gpu_broad_phase_copy": (ci, [vp, vp, vp, vp, vp]),
     "adipc_gpu_contact_emit_device": (ci, [vp, C.POINTER(ContactDesc), cd, ci, vp, vp, i64, vp, C.POINTER(cd),
                                            C.POINTER(i64)]),
     "adipc_gpu_contact_value_device": (ci, [vp, C.POINTER(ContactDesc), cd, C.POINTER(cd)]),

@@ -255,6 +255,24 @@ class Context:
                                                           C.byref(n)))
         return v.value, n.value
 
+    def broad_phase(self, pos, verts, edges, tris, inflate, disp=None):
+        """find_candidates (broad_phase.hpp:143-211) on device tensors; returns
+        device int32 tensors (pt_pairs k x 2, pt_stencils k x 4, ee_pairs,
+        ee_stencils)."""
+        import torch
+
+        npt, nee = C.c_int64(), C.c_int64()
+        self._check(self._L.adipc_gpu_broad_phase_device(self.h, pos.numel() // 3, ptr(pos), ptr(disp), verts.numel(),
+                                                         ptr(verts), edges.numel() // 2, ptr(edges), tris.numel() // 3,
+                                                         ptr(tris), float(inflate), C.byref(npt), C.byref(nee)))
+        dev = pos.device
+        out = [torch.empty((npt.value, 2), dtype=torch.int32, device=dev),
+               torch.empty((npt.value, 4), dtype=torch.int32, device=dev),
+               torch.empty((nee.value, 2), dtype=torch.int32, device=dev),
+               torch.empty((nee.value, 4), dtype=torch.int32, device=dev)]
+        self._check(self._L.adipc_gpu_broad_phase_copy(self.h, *[ptr(t) if t.numel() else None for t in out]))
+        return out
+
     def contact_value(self, c, dt2):
         d = self.contact_desc(c)
         v = C.c_double()

@@ -187,6 +187,7 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.ct_rank.free();
     c.ct_work.free();
     c.ct_scal.free();
+    c.bp = BroadState();
     c.fem_vals.free();
     c.fem_value.free();
     c.perm.free();
@@ -483,6 +484,50 @@ int adipc_gpu_ccd_step_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* d, c
         if (!d_disp) throw StatusError(kInvalidArgument, "missing displacement");
         const double a = ccd_step(ctx->c, contact_desc(d), d_disp);
         if (alpha) *alpha = a;
+    });
+}
+
+
+// ---- broad phase (broad.cu) ----------------------------------------------------
+int adipc_gpu_broad_phase_device(adipc_gpu_ctx* ctx, int32_t n_nodes, const double* d_pos, const double* d_disp,
+                                 int32_t n_verts, const int32_t* d_verts, int32_t n_edges, const int32_t* d_edges,
+                                 int32_t n_tris, const int32_t* d_tris, double inflate, int64_t* n_pt, int64_t* n_ee) {
+    return guarded(ctx, [&] {
+        if (n_nodes < 0 || n_verts < 0 || n_edges < 0 || n_tris < 0) throw StatusError(kInvalidArgument, "negative size");
+        if ((n_nodes > 0 && !d_pos) || (n_verts > 0 && !d_verts) || (n_edges > 0 && !d_edges) || (n_tris > 0 && !d_tris))
+            throw StatusError(kInvalidArgument, "missing surface arrays");
+        if (!(inflate >= 0)) throw StatusError(kInvalidArgument, "inflate must be non-negative");
+        BroadDesc d;
+        d.n_nodes = n_nodes;
+        d.pos = d_pos;
+        d.disp = d_disp;
+        d.n_verts = n_verts;
+        d.n_edges = n_edges;
+        d.n_tris = n_tris;
+        d.verts = d_verts;
+        d.edges = d_edges;
+        d.tris = d_tris;
+        d.inflate = inflate;
+        std::int64_t a = 0, b = 0;
+        broad_phase(ctx->c, d, &a, &b);
+        if (n_pt) *n_pt = a;
+        if (n_ee) *n_ee = b;
+    });
+}
+
+int adipc_gpu_broad_phase_copy(adipc_gpu_ctx* ctx, int32_t* pt_pairs, int32_t* pt_stencils, int32_t* ee_pairs,
+                               int32_t* ee_stencils) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const BroadState& B = c.bp;
+        auto cp = [&](int32_t* dst, const int* src, std::int64_t n) {
+            if (dst && n > 0) ADIPC_CUDA(cudaMemcpyAsync(dst, src, sizeof(int32_t) * n, cudaMemcpyDefault, c.stream));
+        };
+        cp(pt_pairs, B.pt_pairs.p, 2 * B.n_pt);
+        cp(pt_stencils, B.pt_stencils.p, 4 * B.n_pt);
+        cp(ee_pairs, B.ee_pairs.p, 2 * B.n_ee);
+        cp(ee_stencils, B.ee_stencils.p, 4 * B.n_ee);
+        sync(c);
     });
 }
 

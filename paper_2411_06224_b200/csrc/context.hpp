@@ -87,6 +87,24 @@ struct DeviceLevel {
 
 enum PrecondKind : int { kNone = 0, kMas = 1, kJacobi = 2 };
 
+// broad phase (broad.cu): primitive boxes, grid entries and their hash
+// table, per-query counts / offsets, the candidate pairs and node stencils
+struct BpBox {
+    double lo[3], hi[3];
+};
+struct BpEntry {
+    int x, y, z, id;
+};
+struct BroadState {
+    DBuf<BpBox> tri_box, edge_box;
+    DBuf<BpEntry> entries, tri_table, edge_table;
+    DBuf<std::int64_t> tri_bstart, edge_bstart, off, qoff;
+    DBuf<std::int32_t> cnt, bcnt, qcnt;
+    DBuf<int> pt_partner, pt_pairs, pt_stencils, ee_partner, ee_pairs, ee_stencils;
+    DBuf<double> scal;
+    std::int64_t n_pt = 0, n_ee = 0;
+};
+
 struct PcgWork {
     DBuf<double> x, r, p, ap, z, b, tmp;
     DBuf<double> partials;       // per-CTA partial dots
@@ -127,6 +145,7 @@ struct Ctx {
     DBuf<std::int64_t> ct_rank;
     DBuf<unsigned char> ct_work;
     DBuf<double> ct_scal;
+    BroadState bp;
     DBuf<double> tile_vals;
     // staging of the host-pointer entry points (contact node stream, DofMap)
     DBuf<std::uint64_t> io_keys, io_keys2;
@@ -297,6 +316,19 @@ struct ContactDesc {
     const double* fr_base = nullptr;         // 3 per node
     double mu = 0, fr_eps = 1;
 };
+// Broad phase input (broad.cu; broad_phase.hpp:143-211): device arrays
+struct BroadDesc {
+    std::int32_t n_nodes = 0;
+    const double* pos = nullptr;   // 3 per node
+    const double* disp = nullptr;  // 3 per node or null (ccd_candidates: swept boxes)
+    std::int32_t n_verts = 0, n_edges = 0, n_tris = 0;
+    const int* verts = nullptr;    // ContactSurface::verts
+    const int* edges = nullptr;    // 2 per edge
+    const int* tris = nullptr;     // 3 per triangle
+    double inflate = 0;
+};
+void broad_phase(Ctx& c, const BroadDesc& d, std::int64_t* n_pt, std::int64_t* n_ee);
+
 std::int64_t contact_emit(Ctx& c, const ContactDesc& d, double dt2, int project, std::uint64_t* d_keys, double* d_vals,
                           std::int64_t capacity, double* d_node_grad, double* d_value);
 double contact_value(Ctx& c, const ContactDesc& d, double dt2);

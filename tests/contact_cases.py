@@ -83,3 +83,64 @@ def device_dict(ci, dev="cuda:0"):
         d.update(fr_nodes=t(ci.fr_nodes), fr_n=t(ci.fr_n), fr_coeff=t(ci.fr_coeff), fr_t1=t(ci.fr_t1),
                  fr_t2=t(ci.fr_t2), fr_lambda=t(ci.fr_lambda), fr_base=t(ci.fr_base))
     return d
+
+
+def make_grid(nx, ny, sx, sy):
+    """geometry/shapes.hpp:22-44 (make_grid): vertex id = j nx + i, the
+    diagonal alternating with (i + j) parity."""
+    verts = np.array([[sx * i / (nx - 1), sy * j / (ny - 1), 0.0] for j in range(ny) for i in range(nx)])
+    tris = []
+    for j in range(ny - 1):
+        for i in range(nx - 1):
+            a, b, c, d = j * nx + i, j * nx + i + 1, (j + 1) * nx + i + 1, (j + 1) * nx + i
+            if (i + j) % 2 == 0:
+                tris += [[a, b, c], [a, c, d]]
+            else:
+                tris += [[a, b, d], [b, c, d]]
+    return verts, np.array(tris, np.int32)
+
+
+def edges_of(tris):
+    """scene/mesh.hpp:84-95 (extract_edges): sorted unique (min, max) pairs."""
+    e = np.concatenate([tris[:, [0, 1]], tris[:, [1, 2]], tris[:, [2, 0]]])
+    e = np.sort(e, axis=1)
+    return np.unique(e, axis=0).astype(np.int32)
+
+
+def layered_surface(n=6, layers=2, seed=51, noise=0.02):
+    """test_contact.cpp:341-360: interleaved cloth patches (shells: every
+    vertex, edge and triangle is on the contact surface) plus noise."""
+    rng = np.random.default_rng(seed)
+    P, T, E = [], [], []
+    off = 0
+    for layer in range(layers):
+        v, t = make_grid(n, n, 1, 1)
+        v = v + np.array([0.3 * layer, 0.05 * layer, 0.2 * layer])
+        P.append(v)
+        T.append(t + off)
+        E.append(edges_of(t) + off)
+        off += len(v)
+    pos = np.concatenate(P) + noise * rng.uniform(-1, 1, (off, 3))
+    return pos, np.arange(off, dtype=np.int32), np.concatenate(E), np.concatenate(T)
+
+
+def brute_candidates(pos, verts, edges, tris, inflate, disp=None):
+    """test_contact.cpp:362-389: every overlapping pair, brute force."""
+    half = inflate / 2
+
+    def box(nodes):
+        pts = pos[nodes]
+        if disp is not None:
+            pts = np.concatenate([pts, pos[nodes] + disp[nodes]])
+        return pts.min(0) - half, pts.max(0) + half
+
+    def ov(a, b):
+        return bool(np.all(a[0] <= b[1]) and np.all(b[0] <= a[1]))
+
+    tb = [box(t) for t in tris]
+    pt = [(vi, ti) for vi, v in enumerate(verts) for ti, t in enumerate(tris)
+          if v not in t and ov(box([v]), tb[ti])]
+    eb = [box(e) for e in edges]
+    ee = [(i, j) for i in range(len(edges)) for j in range(i + 1, len(edges))
+          if not set(edges[i]) & set(edges[j]) and ov(eb[i], eb[j])]
+    return np.array(pt, np.int32).reshape(-1, 2), np.array(ee, np.int32).reshape(-1, 2)

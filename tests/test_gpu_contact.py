@@ -131,3 +131,49 @@ def test_contact_pipeline_through_two_level_reduction(ctx):
     n, rows, cols, blocks = ctx.copy_matrix()
     assert U == len(orow) and np.array_equal(rows, orow) and np.array_equal(cols, ocol)
     assert_blocks_close(blocks, oblk, 1e-9)
+
+
+@pytest.mark.parametrize("n,swept", [(6, False), (6, True), (40, False), (40, True)])
+def test_broad_phase_matches_oracle(ctx, n, swept):
+    """Device find_candidates (broad_phase.hpp:143-211) equals the oracle's
+    hash grid (itself equal to brute force): pairs bitwise, in order; node
+    stencils resolved from the surface."""
+    from contact_cases import layered_surface
+
+    pos, verts, edges, tris = layered_surface(n=n, layers=3)
+    inflate = 0.11 if n == 6 else 0.03
+    disp = np.random.default_rng(n).normal(0, 0.01, pos.shape) if swept else None
+    opt, oee = O.find_candidates(pos, verts, edges, tris, inflate, disp=disp)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    ppairs, pst, epairs, est = ctx.broad_phase(t(pos), t(verts), t(edges), t(tris), inflate,
+                                               disp=None if disp is None else t(disp))
+    assert np.array_equal(ppairs.cpu().numpy(), opt) and np.array_equal(epairs.cpu().numpy(), oee)
+    assert len(opt) > 0 and len(oee) > 0
+    pst = pst.cpu().numpy()
+    assert np.array_equal(pst[:, 0], verts[opt[:, 0]]) and np.array_equal(pst[:, 1:], tris[opt[:, 1]])
+    est = est.cpu().numpy()
+    assert np.array_equal(est[:, :2], edges[oee[:, 0]]) and np.array_equal(est[:, 2:], edges[oee[:, 1]])
+
+
+def test_device_contact_chain(ctx):
+    """broad phase -> contact producer on the device (no host round trip)
+    against the oracle's candidates -> assemble_contact node part."""
+    from contact_cases import layered_surface
+
+    pos, verts, edges, tris = layered_surface(n=30, layers=3, noise=0.01)
+    dhat = 0.03
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    _, pst, _, est = ctx.broad_phase(t(pos), t(verts), t(edges), t(tris), dhat)
+    opt, oee = O.find_candidates(pos, verts, edges, tris, dhat)
+    ci = O.ContactInput(pos, np.c_[verts[opt[:, 0]], tris[opt[:, 1]]], np.c_[edges[oee[:, 0]], edges[oee[:, 1]]],
+                        dhat=dhat, kappa=1e3)
+    ov, og, ok, ovals = O.contact_assemble(ci, DT2)
+    cap = 10 * (len(pst) + len(est))
+    keys = torch.empty(cap, dtype=torch.int64, device="cuda:0")
+    vals = torch.empty((cap, 9), dtype=torch.float64, device="cuda:0")
+    g = torch.empty(3 * len(pos), dtype=torch.float64, device="cuda:0")
+    d = {"pos": t(pos), "pt": pst, "ee": est, "dhat": dhat, "kappa": 1e3, "ground": None}
+    val, nk = ctx.contact_emit(d, DT2, keys, vals, g)
+    assert np.array_equal(keys[:nk].cpu().numpy().view(np.uint64), ok) and len(ok) > 0
+    assert_blocks_close(vals[:nk].cpu().numpy(), ovals, 1e-9)
+    assert abs(val - ov) <= 1e-12 * abs(ov)

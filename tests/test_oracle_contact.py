@@ -183,3 +183,32 @@ def test_contact_assemble_emission_order():
         q += 1
     assert len(keys) == q + 10 * 10 + 5
     assert val == pytest.approx(O.contact_value(ci, dt2), rel=1e-12)
+
+
+def test_broad_phase_equals_brute_force():
+    """test_contact.cpp:341-409: the hash-grid candidates equal brute force
+    with the same inflation, every truly close pair is found, and the swept
+    variant with zero displacement equals the proximity one."""
+    from contact_cases import brute_candidates, layered_surface
+
+    pos, verts, edges, tris = layered_surface()
+    inflate = 0.11
+    pt, ee = O.find_candidates(pos, verts, edges, tris, inflate)
+    bpt, bee = brute_candidates(pos, verts, edges, tris, inflate)
+    assert np.array_equal(pt, bpt) and np.array_equal(ee, bee)
+    assert len(pt) and len(ee)
+    found = set(map(tuple, pt.tolist()))
+    for vi, v in enumerate(verts):
+        for ti, t in enumerate(tris):
+            if v in t:
+                continue
+            if O.pt_dist2(np.concatenate([pos[v], pos[t[0]], pos[t[1]], pos[t[2]]])) < inflate ** 2:
+                assert (vi, ti) in found
+    spt, see = O.find_candidates(pos, verts, edges, tris, inflate, disp=np.zeros_like(pos))
+    assert np.array_equal(spt, pt) and np.array_equal(see, ee)
+    # swept boxes: a displacement brings new pairs, a superset
+    disp = np.random.default_rng(3).normal(0, 0.05, pos.shape)
+    wpt, wee = O.find_candidates(pos, verts, edges, tris, inflate, disp=disp)
+    bwpt, bwee = brute_candidates(pos, verts, edges, tris, inflate, disp=disp)
+    assert np.array_equal(wpt, bwpt) and np.array_equal(wee, bwee)
+    assert set(map(tuple, pt.tolist())) <= set(map(tuple, wpt.tolist()))

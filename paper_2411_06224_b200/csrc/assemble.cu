@@ -372,6 +372,77 @@ __device__ __forceinline__ void gather_window(const StreamSrc& s, std::uint32_t 
     }
 }
 
+// One warp reduces the sorted entries [b, e) of row r — complete runs, the
+// first entry a run head — into output slots from u on: windows of 32
+// entries, every lane gathers its entry's block into the warp's shared tile,
+// each run's owner sums it sequentially in emission order (a run crossing a
+// window carries its partial sum to the next window).
+__device__ __forceinline__ void reduce_range(const std::uint64_t* __restrict__ sorted, std::int32_t r, std::int64_t b,
+                                             std::int64_t e, std::int64_t u, const StreamSrc& s,
+                                             std::uint32_t* __restrict__ out_rows,
+                                             std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks,
+                                             double (*Tl)[33], double* C, int lane) {
+    bool carried = false;       // a run continues into this window (warp-uniform)
+    std::int64_t carry_u = 0;   // its output slot
+    for (std::int64_t base = b; base < e; base += 32) {
+        const std::int64_t p = base + lane;
+        const bool valid = p < e;
+        const std::uint64_t v = valid ? sorted[p] : ~0ull;
+        const std::uint32_t col = static_cast<std::uint32_t>(v >> 32);
+        const std::uint32_t prev_col = __shfl_up_sync(0xffffffffu, col, 1);
+        const bool head = valid && (lane == 0 ? (p == b || static_cast<std::uint32_t>(sorted[p - 1] >> 32) != col)
+                                              : prev_col != col);
+        const int nv = static_cast<int>(e - base < 32 ? e - base : 32);
+        double g[9];
+        gather_window(s, static_cast<std::uint32_t>(v), nv, lane, g);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            const int word = 32 * k + lane;
+            const int j = word / 9, el = word - 9 * j;
+            if (j < nv) Tl[el][j] = g[k];
+        }
+        // does the window's last run continue past it?
+        const std::int64_t nxt = base + 32;
+        const bool cont_out = __shfl_sync(0xffffffffu, nxt < e && lane == 31 &&
+                                                           static_cast<std::uint32_t>(sorted[nxt] >> 32) == col,
+                                          31);
+        const unsigned hm = __ballot_sync(0xffffffffu, head);
+        __syncwarp();
+        const bool owner = head || (lane == 0 && carried);
+        if (owner) {
+            // run [lane, end): up to the next head of the window or its valid end
+            const unsigned later = hm & ~((2u << lane) - 1u);
+            const int end = later ? __ffs(later) - 1 : nv;
+            double acc[9];
+            if (head) {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[k] = Tl[k][lane];
+            } else {  // continuing run: carried sum, then this window's entries
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(C[k], Tl[k][lane]);
+            }
+            for (int j = lane + 1; j < end; ++j)
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(acc[k], Tl[k][j]);
+            const std::int64_t my_u = head ? u + __popc(hm & ((1u << lane) - 1u)) : carry_u;
+            if (end == nv && cont_out) {  // hand over to the next window
+#pragma unroll
+                for (int k = 0; k < 9; ++k) C[k] = acc[k];
+            } else {
+                out_rows[my_u] = static_cast<std::uint32_t>(r);
+                out_cols[my_u] = col;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) out_blocks[blk(my_u, k)] = acc[k];
+            }
+        }
+        // the continuing run's slot: the last head's, or the one already carried
+        if (cont_out) carry_u = hm ? u + __popc(hm) - 1 : carry_u;
+        carried = cont_out;
+        u += __popc(hm);
+        __syncwarp();
+    }
+}
+
 __global__ void __launch_bounds__(32 * kReduceWarps, 3) k_reduce_rows(
     const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
     const std::int64_t* __restrict__ uniq_start, std::int32_t n, StreamSrc s, std::uint32_t* __restrict__ out_rows,
@@ -380,71 +451,75 @@ __global__ void __launch_bounds__(32 * kReduceWarps, 3) k_reduce_rows(
     __shared__ double carry[kReduceWarps][9];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
-    double(*Tl)[33] = tile[w];
-    double* C = carry[w];
-    for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps) {
-        const std::int64_t b = row_start[r], e = row_start[r + 1];
-        std::int64_t u = uniq_start[r];
-        bool carried = false;       // a run continues into this window (warp-uniform)
-        std::int64_t carry_u = 0;   // its output slot
-        for (std::int64_t base = b; base < e; base += 32) {
-            const std::int64_t p = base + lane;
-            const bool valid = p < e;
-            const std::uint64_t v = valid ? sorted[p] : ~0ull;
-            const std::uint32_t col = static_cast<std::uint32_t>(v >> 32);
-            const std::uint32_t prev_col = __shfl_up_sync(0xffffffffu, col, 1);
-            const bool head = valid && (lane == 0 ? (p == b || static_cast<std::uint32_t>(sorted[p - 1] >> 32) != col)
-                                                  : prev_col != col);
-            const int nv = static_cast<int>(e - base < 32 ? e - base : 32);
-            double g[9];
-            gather_window(s, static_cast<std::uint32_t>(v), nv, lane, g);
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                const int word = 32 * k + lane;
-                const int j = word / 9, el = word - 9 * j;
-                if (j < nv) Tl[el][j] = g[k];
-            }
-            // does the window's last run continue past it?
-            const std::int64_t nxt = base + 32;
-            const bool cont_out = __shfl_sync(0xffffffffu, nxt < e && lane == 31 &&
-                                                               static_cast<std::uint32_t>(sorted[nxt] >> 32) == col,
-                                              31);
-            const unsigned hm = __ballot_sync(0xffffffffu, head);
-            __syncwarp();
-            const bool owner = head || (lane == 0 && carried);
-            if (owner) {
-                // run [lane, end): up to the next head of the window or its valid end
-                const unsigned later = hm & ~((2u << lane) - 1u);
-                const int end = later ? __ffs(later) - 1 : nv;
-                double acc[9];
-                if (head) {
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) acc[k] = Tl[k][lane];
-                } else {  // continuing run: carried sum, then this window's entries
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(C[k], Tl[k][lane]);
-                }
-                for (int j = lane + 1; j < end; ++j)
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(acc[k], Tl[k][j]);
-                const std::int64_t my_u = head ? u + __popc(hm & ((1u << lane) - 1u)) : carry_u;
-                if (end == nv && cont_out) {  // hand over to the next window
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) C[k] = acc[k];
-                } else {
-                    out_rows[my_u] = static_cast<std::uint32_t>(r);
-                    out_cols[my_u] = col;
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) out_blocks[blk(my_u, k)] = acc[k];
-                }
-            }
-            // the continuing run's slot: the last head's, or the one already carried
-            if (cont_out) carry_u = hm ? u + __popc(hm) - 1 : carry_u;
-            carried = cont_out;
-            u += __popc(hm);
-            __syncwarp();
+    for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps)
+        reduce_range(sorted, r, row_start[r], row_start[r + 1], uniq_start[r], s, out_rows, out_cols, out_blocks,
+                     tile[w], carry[w], lane);
+}
+
+// ---- long rows (contact scenes: affine-body rows with tens of thousands of
+// entries): rows are cut into segments of about kSegLen entries at run
+// heads, so one warp per SEGMENT reduces them; the runs stay whole and each
+// is still summed left to right (bitwise the per-row path).
+constexpr std::int64_t kSegLen = 1024;
+
+__global__ void k_seg_count(const std::int64_t* __restrict__ row_start, std::int32_t n, std::int32_t* __restrict__ cnt) {
+    for (std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        cnt[r] = static_cast<std::int32_t>(ceil_div(row_start[r + 1] - row_start[r], kSegLen));
+}
+__global__ void k_seg_rows(const std::int64_t* __restrict__ item_ptr, std::int32_t n, std::int32_t* __restrict__ item_row) {
+    for (std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        for (std::int64_t i = item_ptr[r]; i < item_ptr[r + 1]; ++i) item_row[i] = static_cast<std::int32_t>(r);
+}
+// first run head at or after p in [b, e) (e if none); warp-cooperative
+__device__ __forceinline__ std::int64_t next_head(const std::uint64_t* __restrict__ sorted, std::int64_t b,
+                                                  std::int64_t e, std::int64_t p, int lane) {
+    if (p <= b) return b;
+    for (std::int64_t q0 = p; q0 < e; q0 += 32) {
+        const std::int64_t q = q0 + lane;
+        const bool h = q < e && static_cast<std::uint32_t>(sorted[q] >> 32) != static_cast<std::uint32_t>(sorted[q - 1] >> 32);
+        const unsigned m = __ballot_sync(0xffffffffu, h);
+        if (m) return q0 + __ffs(m) - 1;
+    }
+    return e;
+}
+// segment bounds and head counts, one warp per segment
+__global__ void k_seg_heads(const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
+                            const std::int64_t* __restrict__ item_ptr, const std::int32_t* __restrict__ item_row,
+                            std::int64_t m, std::int64_t* __restrict__ seg, std::int32_t* __restrict__ heads) {
+    const int lane = threadIdx.x & 31;
+    for (std::int64_t i = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5; i < m;
+         i += (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const std::int32_t r = item_row[i];
+        const std::int64_t b = row_start[r], e = row_start[r + 1], k = i - item_ptr[r];
+        const std::int64_t s0 = next_head(sorted, b, e, b + k * kSegLen, lane);
+        const std::int64_t s1 = next_head(sorted, b, e, std::min(e, b + (k + 1) * kSegLen), lane);
+        int h = 0;
+        for (std::int64_t q0 = s0; q0 < s1; q0 += 32) {
+            const std::int64_t q = q0 + lane;
+            const bool hd = q < s1 && (q == b || static_cast<std::uint32_t>(sorted[q] >> 32) !=
+                                                     static_cast<std::uint32_t>(sorted[q - 1] >> 32));
+            h += __popc(__ballot_sync(0xffffffffu, hd));
+        }
+        if (lane == 0) {
+            seg[2 * i] = s0;
+            seg[2 * i + 1] = s1;
+            heads[i] = h;
         }
     }
+}
+__global__ void __launch_bounds__(32 * kReduceWarps, 3) k_reduce_segments(
+    const std::uint64_t* __restrict__ sorted, const std::int32_t* __restrict__ item_row,
+    const std::int64_t* __restrict__ seg, const std::int64_t* __restrict__ item_u, std::int64_t m, StreamSrc s,
+    std::uint32_t* __restrict__ out_rows, std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks) {
+    __shared__ double tile[kReduceWarps][9][33];
+    __shared__ double carry[kReduceWarps][9];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const std::int64_t warps = static_cast<std::int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * (blockDim.x >> 5) + w; i < m; i += warps)
+        reduce_range(sorted, item_row[i], seg[2 * i], seg[2 * i + 1], item_u[i], s, out_rows, out_cols, out_blocks,
+                     tile[w], carry[w], lane);
 }
 
 __global__ void k_max_row(const std::uint64_t* __restrict__ keys, std::int64_t T, unsigned* __restrict__ out) {
@@ -596,6 +671,7 @@ static void bucket_sort(Ctx& c, const StreamSrc& s, std::int32_t n) {
     ADIPC_CUDA(cudaStreamSynchronize(st));
     if (h_counters[0])
         throw StatusError(kInvalidArgument, "block row index >= n_block_rows in triplet stream");
+    c.sort_long_rows = h_counters[1];
     if (h_counters[1] > 0) {
         const int nb = h_counters[1];
         c.merge_scratch.reserve(static_cast<std::size_t>(entries));
@@ -646,9 +722,31 @@ static void sort_reduce(Ctx& c, const StreamSrc& s, std::int32_t n, DeviceMatrix
     out.rows.reserve(static_cast<std::size_t>((U + 31) & ~std::int64_t(31)));
     out.cols.reserve(static_cast<std::size_t>((U + 31) & ~std::int64_t(31)));
     out.blocks.reserve(blk_doubles(U));
-    if (n > 0 && U > 0) {
+    if (n > 0 && U > 0 && c.sort_long_rows == 0) {
         k_reduce_rows<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, out.row_ptr.p, n, s, out.rows.p,
                                                           out.cols.p, out.blocks.p);
+        ADIPC_LAUNCH_CHECK();
+    } else if (n > 0 && U > 0) {  // long rows: one warp per ~kSegLen-entry segment
+        c.seg_cnt.reserve(static_cast<std::size_t>(n) + 1);
+        c.seg_ptr.reserve(static_cast<std::size_t>(n) + 1);
+        k_seg_count<<<grid_for(n, 256, 16), 256, 0, st>>>(c.row_start.p, n, c.seg_cnt.p);
+        ADIPC_LAUNCH_CHECK();
+        exclusive_scan(c.seg_cnt.p, n, c.seg_ptr.p, c.scan_scratch, st);
+        std::int64_t m = 0;
+        ADIPC_CUDA(cudaMemcpyAsync(&m, c.seg_ptr.p + n, sizeof(m), cudaMemcpyDeviceToHost, st));
+        ADIPC_CUDA(cudaStreamSynchronize(st));
+        c.seg_row.reserve(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)));
+        c.seg_heads.reserve(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)));
+        c.seg_bounds.reserve(static_cast<std::size_t>(std::max<std::int64_t>(2 * m, 1)));
+        c.seg_u.reserve(static_cast<std::size_t>(m) + 1);
+        k_seg_rows<<<grid_for(n, 256, 16), 256, 0, st>>>(c.seg_ptr.p, n, c.seg_row.p);
+        ADIPC_LAUNCH_CHECK();
+        k_seg_heads<<<grid_for(m, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, c.seg_ptr.p, c.seg_row.p, m,
+                                                        c.seg_bounds.p, c.seg_heads.p);
+        ADIPC_LAUNCH_CHECK();
+        exclusive_scan(c.seg_heads.p, m, c.seg_u.p, c.scan_scratch, st);
+        k_reduce_segments<<<grid_for(m, 8, 16), 256, 0, st>>>(c.sorted.p, c.seg_row.p, c.seg_bounds.p, c.seg_u.p, m,
+                                                              s, out.rows.p, out.cols.p, out.blocks.p);
         ADIPC_LAUNCH_CHECK();
     }
     ++out.version;

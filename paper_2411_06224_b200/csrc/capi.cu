@@ -183,6 +183,8 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.graph_adj.free();
     c.graph_ptr.free();
     c.fem_keys.free();
+    for (auto* b : {&c.seg_cnt, &c.seg_row, &c.seg_heads}) b->free();
+    for (auto* b : {&c.seg_ptr, &c.seg_bounds, &c.seg_u}) b->free();
     c.ct_on.free();
     c.ct_rank.free();
     c.ct_work.free();

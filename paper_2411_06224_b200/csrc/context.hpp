@@ -136,6 +136,11 @@ struct Ctx {
     DBuf<std::int32_t> abd_cnt;
     DBuf<std::int64_t> abd_off;
     DBuf<std::uint64_t> tile_keys;
+    // rows longer than a warp sort in the last bucket sort, and the segments
+    // the reduction cuts them into (assemble.cu)
+    std::int32_t sort_long_rows = 0;
+    DBuf<std::int32_t> seg_cnt, seg_row, seg_heads;
+    DBuf<std::int64_t> seg_ptr, seg_bounds, seg_u;
     // element-Hessian producer (energy.cu): the emitted stream + the value
     DBuf<std::uint64_t> fem_keys;
     DBuf<double> fem_vals, fem_value;

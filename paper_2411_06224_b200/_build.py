@@ -18,7 +18,7 @@ OBJ = os.path.join(PKG, "build")
 GPU_LIB = os.path.join(PKG, "libadipc_gpu.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp", "--expt-relaxed-constexpr",
               "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
 CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"  # image's $CXX lacks libgomp.spec
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter"]

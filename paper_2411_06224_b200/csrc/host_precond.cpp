@@ -233,18 +233,28 @@ MasHierarchy build_hierarchy(const Partition& l0, Graph g0, int max_levels) {
 }
 
 MasHierarchy build_hierarchy_l1(const Partition& l0, std::vector<Index> up1, Index n1, Graph g1, int max_levels) {
+    const auto t0 = std::chrono::steady_clock::now();
     MasHierarchy h = base_hierarchy(l0);
+    const auto t1 = std::chrono::steady_clock::now();
     // the first pass of the loop (hierarchy.hpp:46-99) with its super nodes
     // and their graph given
     if (h.n_levels() >= max_levels || l0.n_parts <= 1 || n1 == h.n_slots) return h;
     Level next;
     next.n_nodes = n1;
     Partition grouped = partition_block_graph(n1, g1, h.capacity);
+    const auto t2 = std::chrono::steady_clock::now();
     next.n_parts = grouped.n_parts;
     next.part_of = std::move(grouped.part_of);
     next.agg = std::move(up1);  // level 0's agg is the identity
     h.levels.push_back(std::move(next));
+    const long long e1 = static_cast<long long>(g1.adj.size());
     extend_hierarchy(h, std::move(g1), max_levels);
+    if (std::getenv("ADIPC_DEBUG_HIER")) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "hierarchy from level 1: base %.1f ms, level-1 partition (v=%d, e=%lld) %.1f ms, "
+                             "levels >= 2 %.1f ms\n", ms(t0, t1), n1, e1, ms(t1, t2),
+                     ms(t2, std::chrono::steady_clock::now()));
+    }
     return h;
 }
 

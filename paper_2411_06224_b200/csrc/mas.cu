@@ -572,7 +572,12 @@ void link_levels(Ctx& c, const host::MasHierarchy& h) {
         const host::Level& nxt = h.levels[l + 1];
         DeviceLevel& L = *c.levels[l];
         std::vector<std::int32_t> up(cur.n_nodes, -1);
-        for (std::int32_t slot = 0; slot < h.n_slots; ++slot) up[l == 0 ? slot : cur.agg[slot]] = nxt.agg[slot];
+        if (l == 0) {
+#pragma omp parallel for schedule(static)
+            for (std::int32_t slot = 0; slot < h.n_slots; ++slot) up[slot] = nxt.agg[slot];
+        } else {
+            for (std::int32_t slot = 0; slot < h.n_slots; ++slot) up[cur.agg[slot]] = nxt.agg[slot];
+        }
         std::vector<std::int32_t> first(cur.n_parts + 1, std::numeric_limits<std::int32_t>::max());
         std::vector<std::int32_t> cnt(nxt.n_nodes + 1, 0);
         for (std::int32_t v = 0; v < cur.n_nodes; ++v) {
@@ -642,10 +647,27 @@ host::MasHierarchy to_solve_order(Ctx& c, const host::MasHierarchy& h) {
     for (std::int32_t s = 0; s < l0.n_parts; ++s) start[s + 1] += start[s];
     for (std::int32_t i = 0; i < n; ++i) perm[i] = start[l0.part_of[i]]++;
     upload(c.perm, perm, c.stream);
-    host::MasHierarchy hp = h;
+    // built directly (no copy of the slot-sized arrays): level 0's agg is the
+    // identity and never read in solve order
+    host::MasHierarchy hp;
+    hp.capacity = h.capacity;
+    hp.n_slots = n;
+    hp.levels.resize(h.levels.size());
+    for (std::size_t l = 0; l < h.levels.size(); ++l) {
+        hp.levels[l].n_nodes = h.levels[l].n_nodes;
+        hp.levels[l].n_parts = h.levels[l].n_parts;
+        if (l > 0) hp.levels[l].part_of = h.levels[l].part_of;
+    }
+    hp.levels[0].part_of.resize(n);
+#pragma omp parallel for schedule(static)
     for (std::int32_t i = 0; i < n; ++i) hp.levels[0].part_of[perm[i]] = l0.part_of[i];
-    for (std::size_t l = 1; l < h.levels.size(); ++l)
-        for (std::int32_t i = 0; i < n; ++i) hp.levels[l].agg[perm[i]] = h.levels[l].agg[i];
+    for (std::size_t l = 1; l < h.levels.size(); ++l) {
+        std::vector<std::int32_t>& agg = hp.levels[l].agg;
+        agg.resize(n);
+        const std::vector<std::int32_t>& src = h.levels[l].agg;
+#pragma omp parallel for schedule(static)
+        for (std::int32_t i = 0; i < n; ++i) agg[perm[i]] = src[i];
+    }
     return hp;
 }
 

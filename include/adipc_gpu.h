@@ -195,8 +195,22 @@ typedef struct adipc_fem_desc {
     const double* reduced_mass; /* 144 per body, column-major */
     const double* body_kappa;
     const double* body_volume;
+    /* shells (scene/mesh.hpp is_shell; :190-221): membrane triangles
+     * (IncrementalPotential::membrane_stencil, energy/membrane.hpp) and hinges
+     * (energy/bending.hpp); per-shell ranges / material on the host */
+    int32_t n_shells;
+    const int64_t* tri_begin;      /* host, n_shells + 1 */
+    const int32_t* tris;           /* 3 per triangle */
+    const double* tri_rest;        /* MembraneRest: Dm^-1 (2x2 column-major), area: 5 per triangle */
+    const int64_t* hinge_begin;    /* host, n_shells + 1 */
+    const int32_t* hinges;         /* 4 per hinge (edge x0-x1, wings x2, x3) */
+    const double* hinge_rest;      /* HingeRest: rest angle, weight */
+    const double* shell_material;  /* host, 5 per shell: thickness, stretch, strain limit, shear fraction, bending */
+    /* the scene's mesh order (0 solid, 1 shell), NULL / 0: solid meshes only */
+    int32_t n_kinds;
+    const int32_t* mesh_kind;      /* host */
 } adipc_fem_desc;
-/* the raw stream (n_verts + 10 n_tets + 20 n_bodies entries) + gradient
+/* the raw stream (n_verts + 10 n_tets + 20 n_bodies + 6 n_tris + 10 n_hinges entries) + gradient
  * (3 (n_verts + 4 n_bodies)) + value */
 int adipc_gpu_fem_emit_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* desc, uint64_t* d_keys, double* d_vals9,
                               double* d_grad, double* value);

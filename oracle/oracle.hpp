@@ -1119,112 +1119,6 @@ inline Stencil12 abd_orthogonality(const Real* q, Real kappa, Real rest_volume, 
     return out;
 }
 
-// One deformable solid part of the scene for the producer: tets as global
-// slot ids (mesh offset applied), rest data and material per mesh.
-struct FemSolids {
-    std::vector<std::int32_t> tets;      // 4 per tet
-    std::vector<TetRest> rest;           // per tet
-    std::vector<std::int64_t> tet_begin; // per mesh, n_meshes + 1
-    std::vector<Real> mu, lam;           // per mesh
-};
-
-// Affine bodies of the scene (scene.hpp Body): q, q_tilde, reduced mass
-// (12 x 12 column-major), orthogonality stiffness and rest volume; body b
-// owns block rows n_fem + 4 b .. + 3 (DofMap, abd_reduce.hpp:11-27).
-struct Bodies {
-    std::vector<Real> q, q_tilde, reduced_mass, kappa, volume;  // 12, 12, 144, 1, 1 per body
-    std::size_t size() const { return kappa.size(); }
-};
-
-// IncrementalPotential::assemble for inertia + solid meshes + affine bodies,
-// up to (not including) assemble_contact / filter_pinned / sort / reduce:
-// returns the value, fills grad (3 (n + 4 nb), zeroed on pinned slots,
-// :253-254) and the triplet stream in emission order (:170-249): inertia
-// diagonals of every vertex, body inertia tiles (split_sym_12x12 of the
-// reduced mass), 10 blocks per tet, body orthogonality tiles.
-inline Real ip_fem_assemble(const std::vector<Vec3>& x, const std::vector<Vec3>& x_tilde, const std::vector<Real>& mass,
-                            const FemSolids& fs, Real dt2, const std::vector<char>& pinned, std::vector<Real>& grad,
-                            BlockTripletStream& stream, bool project = true, const Bodies* bodies = nullptr) {
-    const std::size_t n = x.size();
-    const std::size_t nb = bodies ? bodies->size() : 0;
-    grad.assign(3 * (n + 4 * nb), 0.0);
-    stream.keys.clear();
-    stream.values.clear();
-    Real val = 0;
-    for (std::size_t v = 0; v < n; ++v) {  // :170-180
-        Vec3 dx;
-        for (int k = 0; k < 3; ++k) dx[k] = x[v][k] - x_tilde[v][k];
-        val += 0.5 * mass[v] * (dx[0] * dx[0] + dx[1] * dx[1] + dx[2] * dx[2]);
-        for (int k = 0; k < 3; ++k) grad[3 * v + k] += mass[v] * dx[k];
-        Mat3 m;
-        m(0, 0) = m(1, 1) = m(2, 2) = mass[v];
-        stream.emit(static_cast<Index>(v), static_cast<Index>(v), m);
-    }
-    auto split_sym = [&](Index base, const Real* H) {  // block_split.hpp:19-23
-        for (int ti = 0; ti < 4; ++ti)
-            for (int tj = ti; tj < 4; ++tj) {
-                Mat3 blk;
-                for (int c = 0; c < 3; ++c)
-                    for (int r = 0; r < 3; ++r) blk(r, c) = H[12 * (3 * tj + c) + 3 * ti + r];
-                stream.emit(base + ti, base + tj, blk);
-            }
-    };
-    for (std::size_t b = 0; b < nb; ++b) {  // :181-188
-        const Index base = static_cast<Index>(n + 4 * b);
-        const Real* M = &bodies->reduced_mass[144 * b];
-        Real dq[12], g[12];
-        for (int k = 0; k < 12; ++k) dq[k] = bodies->q[12 * b + k] - bodies->q_tilde[12 * b + k];
-        Real dg = 0;
-        for (int i = 0; i < 12; ++i) {
-            Real s2 = 0;
-            for (int k = 0; k < 12; ++k) s2 += M[12 * k + i] * dq[k];
-            g[i] = s2;
-        }
-        for (int k = 0; k < 12; ++k) dg += dq[k] * g[k];
-        val += 0.5 * dg;
-        for (int k = 0; k < 12; ++k) grad[3 * base + k] += g[k];
-        split_sym(base, M);
-    }
-    const std::size_t nt = fs.rest.size();
-    std::vector<Stencil12> st(nt);
-    std::vector<Real> tet_mu(nt), tet_lam(nt);
-    for (std::size_t m = 0; m + 1 < fs.tet_begin.size(); ++m)
-        for (std::int64_t t = fs.tet_begin[m]; t < fs.tet_begin[m + 1]; ++t) {
-            tet_mu[t] = fs.mu[m];
-            tet_lam[t] = fs.lam[m];
-        }
-#pragma omp parallel for schedule(static)
-    for (std::int64_t t = 0; t < static_cast<std::int64_t>(nt); ++t) {  // :223-232 (parallel_for)
-        const std::int32_t* te = &fs.tets[4 * t];
-        st[t] = stable_neo_hookean(x[te[0]], x[te[1]], x[te[2]], x[te[3]], fs.rest[t], tet_mu[t], tet_lam[t], project);
-    }
-    for (std::size_t t = 0; t < nt; ++t) {  // :233-239 + scatter12 :310-318
-        const std::int32_t* te = &fs.tets[4 * t];
-        val += dt2 * st[t].value;
-        for (int a = 0; a < 4; ++a)
-            for (int k = 0; k < 3; ++k) grad[3 * te[a] + k] += dt2 * st[t].grad[3 * a + k];
-        for (int a = 0; a < 4; ++a)
-            for (int b = a; b < 4; ++b) {
-                Mat3 blk;
-                for (int c = 0; c < 3; ++c)
-                    for (int r = 0; r < 3; ++r) blk(r, c) = dt2 * st[t].hess[12 * (3 * b + c) + 3 * a + r];
-                stream.emit(te[a], te[b], blk);
-            }
-    }
-    for (std::size_t b = 0; b < nb; ++b) {  // :242-249
-        const Index base = static_cast<Index>(n + 4 * b);
-        const Stencil12 st = abd_orthogonality(&bodies->q[12 * b], bodies->kappa[b], bodies->volume[b], project);
-        val += dt2 * st.value;
-        for (int k = 0; k < 12; ++k) grad[3 * base + k] += dt2 * st.grad[k];
-        Real H[144];
-        for (int k = 0; k < 144; ++k) H[k] = dt2 * st.hess[k];
-        split_sym(base, H);
-    }
-    for (std::size_t v = 0; v < n + 4 * nb && v < pinned.size(); ++v)
-        if (pinned[v])
-            for (int k = 0; k < 3; ++k) grad[3 * v + k] = 0;
-    return val;
-}
 
 // ---------------------------------------------------------------------------
 // Contact producers: closest-feature classification and
@@ -1279,6 +1173,39 @@ inline Dual12 inverse(const Dual12& b) {
     return r;
 }
 inline Dual12 operator/(const Dual12& a, const Dual12& b) { return a * inverse(b); }
+inline Dual12 operator*(const Dual12& a, Real s) {  // dual2.hpp:48-53
+    Dual12 r(a.v * s);
+    for (int i = 0; i < 12; ++i) r.g[i] = a.g[i] * s;
+    for (int i = 0; i < 144; ++i) r.h[i] = a.h[i] * s;
+    return r;
+}
+inline Dual12 operator*(Real s, const Dual12& a) { return a * s; }
+inline Dual12 operator-(const Dual12& a, Real s) {  // a + (-s)
+    Dual12 r = a;
+    r.v += -s;
+    return r;
+}
+inline Dual12 sqrt(const Dual12& a) {  // dual2.hpp:80-86
+    const Real s = std::sqrt(a.v);
+    Dual12 r(s);
+    for (int i = 0; i < 12; ++i) r.g[i] = a.g[i] / (2 * s);
+    for (int j = 0; j < 12; ++j)
+        for (int i = 0; i < 12; ++i) r.h[12 * j + i] = a.h[12 * j + i] / (2 * s) - a.g[i] * a.g[j] / (4 * a.v * s);
+    return r;
+}
+inline Dual12 atan2(const Dual12& y, const Dual12& x) {  // dual2.hpp:89-101
+    const Real r2 = x.v * x.v + y.v * y.v;
+    Dual12 r(std::atan2(y.v, x.v));
+    for (int i = 0; i < 12; ++i) r.g[i] = (x.v * y.g[i] - y.v * x.g[i]) / r2;
+    const Real c1 = y.v * y.v - x.v * x.v, c2 = 2 * x.v * y.v;
+    for (int j = 0; j < 12; ++j)
+        for (int i = 0; i < 12; ++i) {
+            const Real gxgy = x.g[i] * y.g[j] + x.g[j] * y.g[i];
+            const Real dd = x.g[i] * x.g[j] - y.g[i] * y.g[j];
+            r.h[12 * j + i] = (c1 * gxgy + c2 * dd) / (r2 * r2) + (x.v * y.h[12 * j + i] - y.v * x.h[12 * j + i]) / r2;
+        }
+    return r;
+}
 
 template <class T>
 using G3 = std::array<T, 3>;
@@ -1298,6 +1225,9 @@ template <class T>
 T gnorm2(const G3<T>& a) {
     return gdot(a, a);
 }
+using std::atan2;
+using std::sqrt;
+
 // distance.hpp:111-140
 template <class T>
 T pp_dist2_g(const G3<T>& a, const G3<T>& b) {
@@ -1955,5 +1885,326 @@ inline ContactCandidates find_candidates(const ContactSurface& surf, const std::
     sort_unique(out.ee);
     return out;
 }
+
+// ---------------------------------------------------------------------------
+// Shell energies: energy/membrane.hpp:10-131 (FBW
+// stretch, cubic strain limit, I6 shear), IncrementalPotential::
+// membrane_stencil (incremental_potential.hpp:273-298) and the hinge
+// bending of energy/bending.hpp:11-77 (dihedral angle by forward AD).
+struct MembraneRest {
+    Real inv[4];  // Mat2 column-major
+    Real area = 0;
+};
+inline MembraneRest membrane_rest(const Vec3& p0, const Vec3& p1, const Vec3& p2) {  // membrane.hpp:17-32
+    const Vec3 e1 = sub3(p1, p0), e2 = sub3(p2, p0);
+    const Vec3 nrm = cross(e1, e2);
+    const Real area2 = std::sqrt(dot3(nrm, nrm));
+    const Real n1 = std::sqrt(dot3(e1, e1)), n2 = std::sqrt(dot3(e2, e2));
+    if (!(area2 > 1e-14 * n1 * n2) || n1 == 0) throw std::invalid_argument("degenerate rest triangle");
+    Vec3 u, nn;
+    for (int k = 0; k < 3; ++k) {
+        u[k] = e1[k] / n1;
+        nn[k] = nrm[k] / area2;
+    }
+    const Vec3 v = cross(nn, u);
+    const Real a = dot3(e1, u), b = dot3(e2, u), c = dot3(e1, v), d = dot3(e2, v);  // Dm << a, b, c, d (row-wise)
+    const Real invdet = 1.0 / (a * d - b * c);
+    MembraneRest r;
+    r.inv[0] = d * invdet;   // (0,0)
+    r.inv[1] = -c * invdet;  // (1,0)
+    r.inv[2] = -b * invdet;  // (0,1)
+    r.inv[3] = a * invdet;   // (1,1)
+    r.area = 0.5 * area2;
+    return r;
+}
+struct ShellMaterial {  // scene/mesh.hpp:17-24
+    Real thickness = 1e-3, stretch = 5e4, strain_limit = 5e6, shear_fraction = 0.3, bending = 1e-6;
+};
+struct Stencil9 {
+    Real value = 0;
+    Real grad[9] = {};
+    Real hess[81] = {};
+};
+// incremental_potential.hpp:273-298 with membrane.hpp:36-131
+inline Stencil9 membrane_stencil(const Vec3& x0, const Vec3& x1, const Vec3& x2, const MembraneRest& rest,
+                                 const ShellMaterial& m, bool project = true) {
+    Real F[6];  // 3x2 column-major: D * inv
+    for (int j = 0; j < 2; ++j)
+        for (int k = 0; k < 3; ++k)
+            F[3 * j + k] = (x1[k] - x0[k]) * rest.inv[2 * j] + (x2[k] - x0[k]) * rest.inv[2 * j + 1];
+    const Real a_t = rest.area * m.thickness;
+    Real value = 0, dF[6] = {}, H6[36] = {};
+    // fbw_membrane (:54-75)
+    {
+        const Real scale = m.stretch * a_t;
+        for (int dir = 0; dir < 2; ++dir) {
+            const Real* f = F + 3 * dir;
+            const Real I5v = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+            const Real sq = std::sqrt(I5v);
+            value += scale * (sq - 1) * (sq - 1);
+            for (int k = 0; k < 3; ++k) dF[3 * dir + k] += 2 * scale * (1 - 1 / sq) * f[k];
+            const Real e1 = 2 * scale;
+            Real e23 = 2 * scale * (1 - 1 / sq);
+            if (project && e23 < 0) e23 = 0;
+            for (int c = 0; c < 3; ++c)
+                for (int r = 0; r < 3; ++r)
+                    H6[6 * (3 * dir + c) + 3 * dir + r] +=
+                        (r == c ? e23 : 0.0) + (e1 - e23) * (f[r] / sq) * (f[c] / sq);
+        }
+    }
+    // cubic_strain_limit (:87-102)
+    {
+        const Real scale = m.strain_limit * a_t;
+        for (int dir = 0; dir < 2; ++dir) {
+            const Real* f = F + 3 * dir;
+            const Real I5v = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+            if (I5v <= 1.0) continue;
+            const Real sq = std::sqrt(I5v);
+            value += scale * (sq - 1) * (sq - 1) * (sq - 1);
+            for (int k = 0; k < 3; ++k) dF[3 * dir + k] += scale * (3 * (sq - 1) * (sq - 1) / sq) * f[k];
+            const Real e1 = 6 * (sq - 1), e23 = 3 * (1 / sq + sq - 2);
+            for (int c = 0; c < 3; ++c)
+                for (int r = 0; r < 3; ++r)
+                    H6[6 * (3 * dir + c) + 3 * dir + r] +=
+                        scale * ((r == c ? e23 : 0.0) + ((e1 - e23) / I5v) * f[r] * f[c]);
+        }
+    }
+    // shear_energy (:105-121)
+    {
+        const Real scale = m.shear_fraction * m.stretch * a_t;
+        const Real* f0 = F;
+        const Real* f1 = F + 3;
+        const Real I6 = f0[0] * f1[0] + f0[1] * f1[1] + f0[2] * f1[2];
+        value += scale * I6 * I6;
+        for (int k = 0; k < 3; ++k) {
+            dF[k] += 2 * scale * I6 * f1[k];
+            dF[3 + k] += 2 * scale * I6 * f0[k];
+        }
+        const Real g[6] = {f1[0], f1[1], f1[2], f0[0], f0[1], f0[2]};
+        Real S[36];
+        for (int c = 0; c < 6; ++c)
+            for (int r = 0; r < 6; ++r)
+                S[6 * c + r] = 2 * scale * (g[r] * g[c] + I6 * ((r < 3) != (c < 3) && r % 3 == c % 3 ? 1.0 : 0.0));
+        if (project) {
+            Real P[36];
+            oracle_eig::project_psd(6, S, P);
+            for (int k = 0; k < 36; ++k) S[k] = P[k];
+        }
+        for (int k = 0; k < 36; ++k) H6[k] += S[k];
+    }
+    // chain rule through membrane_dFdx (:124-135): C(a, j), a = vertex
+    Real C[3][2];
+    for (int j = 0; j < 2; ++j) {
+        C[0][j] = -rest.inv[2 * j] - rest.inv[2 * j + 1];
+        C[1][j] = rest.inv[2 * j];
+        C[2][j] = rest.inv[2 * j + 1];
+    }
+    Stencil9 out;
+    out.value = value;
+    for (int a = 0; a < 3; ++a)
+        for (int k = 0; k < 3; ++k) out.grad[3 * a + k] = C[a][0] * dF[k] + C[a][1] * dF[3 + k];
+    for (int b = 0; b < 3; ++b)
+        for (int c = 0; c < 3; ++c)
+            for (int a = 0; a < 3; ++a)
+                for (int r = 0; r < 3; ++r) {
+                    Real v = 0;
+                    for (int j = 0; j < 2; ++j)
+                        for (int l = 0; l < 2; ++l) v += C[a][j] * C[b][l] * H6[6 * (3 * l + c) + 3 * j + r];
+                    out.hess[9 * (3 * b + c) + 3 * a + r] = v;
+                }
+    return out;
+}
+
+// bending.hpp:11-53
+template <class T>
+T dihedral_angle_g(const G3<T>& x0, const G3<T>& x1, const G3<T>& x2, const G3<T>& x3) {
+    const G3<T> e = gsub(x1, x0);
+    const G3<T> n1 = gcross(e, gsub(x2, x0));
+    const G3<T> n2 = gcross(gsub(x3, x0), e);
+    const T s = gdot(gcross(n1, n2), e) / sqrt(gnorm2(e));
+    const T c = gdot(n1, n2);
+    return atan2(s, c);
+}
+inline G3<Real> as_g(const Vec3& p) { return {p[0], p[1], p[2]}; }
+struct HingeRest {
+    Real rest_angle = 0, weight = 0;
+};
+inline HingeRest hinge_rest(const Vec3& p0, const Vec3& p1, const Vec3& p2, const Vec3& p3) {
+    const Vec3 c1 = cross(sub3(p1, p0), sub3(p2, p0)), c2 = cross(sub3(p3, p0), sub3(p1, p0));
+    const Real a1 = 0.5 * std::sqrt(dot3(c1, c1)), a2 = 0.5 * std::sqrt(dot3(c2, c2));
+    if (!(a1 > 0) || !(a2 > 0)) throw std::invalid_argument("degenerate hinge rest triangles");
+    HingeRest r;
+    r.rest_angle = dihedral_angle_g<Real>(as_g(p0), as_g(p1), as_g(p2), as_g(p3));
+    const Vec3 e = sub3(p1, p0);
+    r.weight = 3 * dot3(e, e) / (a1 + a2);
+    return r;
+}
+// bending.hpp:60-75: k w (theta - rest)^2 by forward AD, projected
+inline Stencil12 hinge_bending(const Vec3& x0, const Vec3& x1, const Vec3& x2, const Vec3& x3, const HingeRest& rest,
+                               Real k, bool project = true) {
+    const Dual12 th = dihedral_angle_g(dual_point(x0, 0), dual_point(x1, 3), dual_point(x2, 6), dual_point(x3, 9));
+    const Dual12 diff = th - rest.rest_angle;
+    const Dual12 e = (k * rest.weight) * (diff * diff);
+    Stencil12 out;
+    out.value = e.v;
+    for (int i = 0; i < 12; ++i) out.grad[i] = e.g[i];
+    if (project)
+        oracle_eig::project_psd(12, e.h, out.hess);
+    else
+        for (int i = 0; i < 144; ++i) out.hess[i] = e.h[i];
+    return out;
+}
+
+// The deformable meshes of a scene in scene order (kind 0 solid -> the next
+// FemSolids mesh, 1 shell -> the next shell), for ip_fem_assemble's element
+// loop (incremental_potential.hpp:190-241).
+struct FemShells {
+    std::vector<std::int32_t> tris;          // 3 global slots per triangle
+    std::vector<MembraneRest> tri_rest;
+    std::vector<std::int64_t> tri_begin;     // per shell mesh, + 1
+    std::vector<std::int32_t> hinges;        // 4 global slots per hinge
+    std::vector<HingeRest> hinge_rest;
+    std::vector<std::int64_t> hinge_begin;   // per shell mesh, + 1
+    std::vector<ShellMaterial> material;     // per shell mesh
+};
+
+
+// One deformable solid part of the scene for the producer: tets as global
+// slot ids (mesh offset applied), rest data and material per mesh.
+struct FemSolids {
+    std::vector<std::int32_t> tets;      // 4 per tet
+    std::vector<TetRest> rest;           // per tet
+    std::vector<std::int64_t> tet_begin; // per mesh, n_meshes + 1
+    std::vector<Real> mu, lam;           // per mesh
+};
+
+// Affine bodies of the scene (scene.hpp Body): q, q_tilde, reduced mass
+// (12 x 12 column-major), orthogonality stiffness and rest volume; body b
+// owns block rows n_fem + 4 b .. + 3 (DofMap, abd_reduce.hpp:11-27).
+struct Bodies {
+    std::vector<Real> q, q_tilde, reduced_mass, kappa, volume;  // 12, 12, 144, 1, 1 per body
+    std::size_t size() const { return kappa.size(); }
+};
+
+// IncrementalPotential::assemble for inertia + solid meshes + affine bodies,
+// up to (not including) assemble_contact / filter_pinned / sort / reduce:
+// returns the value, fills grad (3 (n + 4 nb), zeroed on pinned slots,
+// :253-254) and the triplet stream in emission order (:170-249): inertia
+// diagonals of every vertex, body inertia tiles (split_sym_12x12 of the
+// reduced mass), 10 blocks per tet, body orthogonality tiles.
+inline Real ip_fem_assemble(const std::vector<Vec3>& x, const std::vector<Vec3>& x_tilde, const std::vector<Real>& mass,
+                            const FemSolids& fs, Real dt2, const std::vector<char>& pinned, std::vector<Real>& grad,
+                            BlockTripletStream& stream, bool project = true, const Bodies* bodies = nullptr,
+                            const FemShells* shells = nullptr, const std::vector<int>* mesh_kind = nullptr) {
+    const std::size_t n = x.size();
+    const std::size_t nb = bodies ? bodies->size() : 0;
+    grad.assign(3 * (n + 4 * nb), 0.0);
+    stream.keys.clear();
+    stream.values.clear();
+    Real val = 0;
+    for (std::size_t v = 0; v < n; ++v) {  // :170-180
+        Vec3 dx;
+        for (int k = 0; k < 3; ++k) dx[k] = x[v][k] - x_tilde[v][k];
+        val += 0.5 * mass[v] * (dx[0] * dx[0] + dx[1] * dx[1] + dx[2] * dx[2]);
+        for (int k = 0; k < 3; ++k) grad[3 * v + k] += mass[v] * dx[k];
+        Mat3 m;
+        m(0, 0) = m(1, 1) = m(2, 2) = mass[v];
+        stream.emit(static_cast<Index>(v), static_cast<Index>(v), m);
+    }
+    auto split_sym = [&](Index base, const Real* H) {  // block_split.hpp:19-23
+        for (int ti = 0; ti < 4; ++ti)
+            for (int tj = ti; tj < 4; ++tj) {
+                Mat3 blk;
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r) blk(r, c) = H[12 * (3 * tj + c) + 3 * ti + r];
+                stream.emit(base + ti, base + tj, blk);
+            }
+    };
+    for (std::size_t b = 0; b < nb; ++b) {  // :181-188
+        const Index base = static_cast<Index>(n + 4 * b);
+        const Real* M = &bodies->reduced_mass[144 * b];
+        Real dq[12], g[12];
+        for (int k = 0; k < 12; ++k) dq[k] = bodies->q[12 * b + k] - bodies->q_tilde[12 * b + k];
+        Real dg = 0;
+        for (int i = 0; i < 12; ++i) {
+            Real s2 = 0;
+            for (int k = 0; k < 12; ++k) s2 += M[12 * k + i] * dq[k];
+            g[i] = s2;
+        }
+        for (int k = 0; k < 12; ++k) dg += dq[k] * g[k];
+        val += 0.5 * dg;
+        for (int k = 0; k < 12; ++k) grad[3 * base + k] += g[k];
+        split_sym(base, M);
+    }
+    const std::size_t nt = fs.rest.size();
+    std::vector<Stencil12> st(nt);
+    std::vector<Real> tet_mu(nt), tet_lam(nt);
+    for (std::size_t m = 0; m + 1 < fs.tet_begin.size(); ++m)
+        for (std::int64_t t = fs.tet_begin[m]; t < fs.tet_begin[m + 1]; ++t) {
+            tet_mu[t] = fs.mu[m];
+            tet_lam[t] = fs.lam[m];
+        }
+#pragma omp parallel for schedule(static)
+    for (std::int64_t t = 0; t < static_cast<std::int64_t>(nt); ++t) {  // :223-232 (parallel_for)
+        const std::int32_t* te = &fs.tets[4 * t];
+        st[t] = stable_neo_hookean(x[te[0]], x[te[1]], x[te[2]], x[te[3]], fs.rest[t], tet_mu[t], tet_lam[t], project);
+    }
+    auto scatter = [&](const std::int32_t* ids, int nn, Real value, const Real* g, const Real* H) {  // scatter9 / 12
+        const int ld = 3 * nn;
+        val += dt2 * value;
+        for (int a = 0; a < nn; ++a)
+            for (int k = 0; k < 3; ++k) grad[3 * ids[a] + k] += dt2 * g[3 * a + k];
+        for (int a = 0; a < nn; ++a)
+            for (int b = a; b < nn; ++b) {
+                Mat3 blk;
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r) blk(r, c) = dt2 * H[ld * (3 * b + c) + 3 * a + r];
+                stream.emit(ids[a], ids[b], blk);
+            }
+    };
+    auto solid_mesh = [&](std::size_t m) {  // :222-239
+        for (std::int64_t t = fs.tet_begin[m]; t < fs.tet_begin[m + 1]; ++t)
+            scatter(&fs.tets[4 * t], 4, st[t].value, st[t].grad, st[t].hess);
+    };
+    auto shell_mesh = [&](std::size_t m) {  // :190-221: triangles (scatter9), then hinges (scatter12)
+        const FemShells& sh = *shells;
+        for (std::int64_t t = sh.tri_begin[m]; t < sh.tri_begin[m + 1]; ++t) {
+            const std::int32_t* tr = &sh.tris[3 * t];
+            const Stencil9 s9 = membrane_stencil(x[tr[0]], x[tr[1]], x[tr[2]], sh.tri_rest[t], sh.material[m], project);
+            scatter(tr, 3, s9.value, s9.grad, s9.hess);
+        }
+        for (std::int64_t h = sh.hinge_begin[m]; h < sh.hinge_begin[m + 1]; ++h) {
+            const std::int32_t* hg = &sh.hinges[4 * h];
+            const Stencil12 s12 = hinge_bending(x[hg[0]], x[hg[1]], x[hg[2]], x[hg[3]], sh.hinge_rest[h],
+                                                sh.material[m].bending, project);
+            scatter(hg, 4, s12.value, s12.grad, s12.hess);
+        }
+    };
+    if (!mesh_kind) {
+        for (std::size_t m = 0; m + 1 < fs.tet_begin.size(); ++m) solid_mesh(m);
+    } else {
+        std::size_t si = 0, hi = 0;
+        for (int kind : *mesh_kind) {
+            if (kind == 0)
+                solid_mesh(si++);
+            else
+                shell_mesh(hi++);
+        }
+    }
+    for (std::size_t b = 0; b < nb; ++b) {  // :242-249
+        const Index base = static_cast<Index>(n + 4 * b);
+        const Stencil12 st = abd_orthogonality(&bodies->q[12 * b], bodies->kappa[b], bodies->volume[b], project);
+        val += dt2 * st.value;
+        for (int k = 0; k < 12; ++k) grad[3 * base + k] += dt2 * st.grad[k];
+        Real H[144];
+        for (int k = 0; k < 144; ++k) H[k] = dt2 * st.hess[k];
+        split_sym(base, H);
+    }
+    for (std::size_t v = 0; v < n + 4 * nb && v < pinned.size(); ++v)
+        if (pinned[v])
+            for (int k = 0; k < 3; ++k) grad[3 * v + k] = 0;
+    return val;
+}
+
 
 }  // namespace oracle

@@ -252,6 +252,50 @@ void oracle_stable_neo_hookean(const double* x12, const double* inv9, double vol
 
 void oracle_project_psd(int n, const double* M, double* out) { oracle_eig::project_psd(n, M, out); }
 
+// membrane.hpp:17-32 -> inv (2x2 column-major) + area; 0 ok, 1 degenerate
+int oracle_membrane_rest(const double* p9, double* rest5) {
+    try {
+        const MembraneRest r = membrane_rest(ld3(p9), ld3(p9 + 3), ld3(p9 + 6));
+        for (int k = 0; k < 4; ++k) rest5[k] = r.inv[k];
+        rest5[4] = r.area;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+// incremental_potential.hpp:273-298; material5 = thickness, stretch, strain limit, shear fraction, bending
+void oracle_membrane_stencil(const double* x9, const double* rest5, const double* material5, int project,
+                             double* value, double* grad9, double* hess81) {
+    MembraneRest r;
+    for (int k = 0; k < 4; ++k) r.inv[k] = rest5[k];
+    r.area = rest5[4];
+    const ShellMaterial m{material5[0], material5[1], material5[2], material5[3], material5[4]};
+    const Stencil9 s = membrane_stencil(ld3(x9), ld3(x9 + 3), ld3(x9 + 6), r, m, project != 0);
+    *value = s.value;
+    std::memcpy(grad9, s.grad, 72);
+    std::memcpy(hess81, s.hess, 648);
+}
+int oracle_hinge_rest(const double* p12, double* rest2) {
+    try {
+        const HingeRest r = hinge_rest(ld3(p12), ld3(p12 + 3), ld3(p12 + 6), ld3(p12 + 9));
+        rest2[0] = r.rest_angle;
+        rest2[1] = r.weight;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+void oracle_hinge_bending(const double* x12, const double* rest2, double k, int project, double* value,
+                          double* grad12, double* hess144) {
+    const Stencil12 s = hinge_bending(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9), {rest2[0], rest2[1]}, k,
+                                      project != 0);
+    *value = s.value;
+    std::memcpy(grad12, s.grad, 96);
+    std::memcpy(hess144, s.hess, 1152);
+}
+
 void oracle_abd_orthogonality(const double* q12, double kappa, double volume, int project, double* value,
                               double* grad12, double* hess144) {
     const Stencil12 s = abd_orthogonality(q12, kappa, volume, project != 0);
@@ -269,7 +313,10 @@ std::int64_t oracle_ip_fem_assemble(std::int32_t n_verts, const double* x, const
                                     double dt2, const std::uint8_t* pinned, int project, std::uint64_t* keys,
                                     double* vals9, double* grad, double* value, std::int32_t n_bodies, const double* q,
                                     const double* q_tilde, const double* reduced_mass, const double* kappa,
-                                    const double* body_volume) {
+                                    const double* body_volume, std::int32_t n_shells, const std::int64_t* tri_begin,
+                                    const std::int32_t* tris, const double* tri_rest5, const std::int64_t* hinge_begin,
+                                    const std::int32_t* hinges, const double* hinge_rest2, const double* material5,
+                                    std::int32_t n_kinds, const std::int32_t* mesh_kind) {
     std::vector<Vec3> xs(n_verts), xt(n_verts);
     for (std::int32_t v = 0; v < n_verts; ++v) {
         xs[v] = ld3(x + 3 * v);
@@ -299,9 +346,29 @@ std::int64_t oracle_ip_fem_assemble(std::int32_t n_verts, const double* x, const
         bodies.kappa.assign(kappa, kappa + n_bodies);
         bodies.volume.assign(body_volume, body_volume + n_bodies);
     }
+    FemShells sh;
+    std::vector<int> kinds(mesh_kind, mesh_kind + n_kinds);
+    if (n_shells > 0) {
+        sh.tri_begin.assign(tri_begin, tri_begin + n_shells + 1);
+        sh.hinge_begin.assign(hinge_begin, hinge_begin + n_shells + 1);
+        const std::int64_t ntr = tri_begin[n_shells], nh = hinge_begin[n_shells];
+        sh.tris.assign(tris, tris + 3 * ntr);
+        sh.hinges.assign(hinges, hinges + 4 * nh);
+        sh.tri_rest.resize(ntr);
+        for (std::int64_t t = 0; t < ntr; ++t) {
+            for (int k = 0; k < 4; ++k) sh.tri_rest[t].inv[k] = tri_rest5[5 * t + k];
+            sh.tri_rest[t].area = tri_rest5[5 * t + 4];
+        }
+        sh.hinge_rest.resize(nh);
+        for (std::int64_t h = 0; h < nh; ++h) sh.hinge_rest[h] = {hinge_rest2[2 * h], hinge_rest2[2 * h + 1]};
+        for (std::int32_t i = 0; i < n_shells; ++i)
+            sh.material.push_back({material5[5 * i], material5[5 * i + 1], material5[5 * i + 2], material5[5 * i + 3],
+                                   material5[5 * i + 4]});
+    }
     std::vector<Real> g;
     BlockTripletStream s;
-    *value = ip_fem_assemble(xs, xt, m, fs, dt2, pin, g, s, project != 0, &bodies);
+    *value = ip_fem_assemble(xs, xt, m, fs, dt2, pin, g, s, project != 0, &bodies, n_shells > 0 ? &sh : nullptr,
+                             n_kinds > 0 ? &kinds : nullptr);
     for (std::size_t k = 0; k < g.size(); ++k) grad[k] = g[k];
     store_stream(s, keys, vals9);
     return static_cast<std::int64_t>(s.size());

@@ -108,7 +108,12 @@ def lib():
         "oracle_stable_neo_hookean": (None, [f64p, f64p, cd, cd, cd, ci, f64p, f64p, f64p]),
         "oracle_project_psd": (None, [ci, f64p, f64p]),
         "oracle_ip_fem_assemble": (i64, [i32, f64p, f64p, f64p, i32, i64p, f64p, f64p, i32p, f64p, f64p, cd, vp, ci,
-                                         u64p, f64p, f64p, f64p, i32, vp, vp, vp, vp, vp]),
+                                         u64p, f64p, f64p, f64p, i32, vp, vp, vp, vp, vp,
+                                         i32, vp, vp, vp, vp, vp, vp, vp, i32, vp]),
+        "oracle_membrane_rest": (ci, [f64p, f64p]),
+        "oracle_membrane_stencil": (None, [f64p, f64p, f64p, ci, f64p, f64p, f64p]),
+        "oracle_hinge_rest": (ci, [f64p, f64p]),
+        "oracle_hinge_bending": (None, [f64p, f64p, cd, ci, f64p, f64p, f64p]),
         "oracle_abd_orthogonality": (None, [f64p, cd, cd, ci, f64p, f64p, f64p]),
     }
     for name, (res, args) in sig.items():
@@ -401,6 +406,41 @@ def project_psd(M):
     return out.reshape(n, n).T.copy()
 
 
+def membrane_rest(p9):
+    """energy/membrane.hpp:17-32 -> 5 doubles: Dm^-1 (2x2 column-major), area."""
+    out = np.empty(5)
+    if lib().oracle_membrane_rest(np.ascontiguousarray(p9, np.float64).reshape(9), out) != 0:
+        raise ValueError(lib().oracle_last_error().decode())
+    return out
+
+
+def membrane_stencil(x9, rest5, material5, project=True):
+    """IncrementalPotential::membrane_stencil (incremental_potential.hpp:273-298)
+    -> (value, grad 9, hess 9x9). material5 = thickness, stretch, strain
+    limit, shear fraction, bending."""
+    v, g, h = np.empty(1), np.empty(9), np.empty(81)
+    lib().oracle_membrane_stencil(np.ascontiguousarray(x9, np.float64).reshape(9),
+                                  np.ascontiguousarray(rest5, np.float64), np.ascontiguousarray(material5, np.float64),
+                                  int(project), v, g, h)
+    return float(v[0]), g, h.reshape(9, 9).T.copy()
+
+
+def hinge_rest(p12):
+    """energy/bending.hpp:36-48 -> (rest angle, weight)."""
+    out = np.empty(2)
+    if lib().oracle_hinge_rest(np.ascontiguousarray(p12, np.float64).reshape(12), out) != 0:
+        raise ValueError(lib().oracle_last_error().decode())
+    return out
+
+
+def hinge_bending(x12, rest2, k, project=True):
+    """energy/bending.hpp:60-75 -> (value, grad 12, hess 12x12)."""
+    v, g, h = np.empty(1), np.empty(12), np.empty(144)
+    lib().oracle_hinge_bending(np.ascontiguousarray(x12, np.float64).reshape(12),
+                               np.ascontiguousarray(rest2, np.float64), k, int(project), v, g, h)
+    return float(v[0]), g, h.reshape(12, 12).T.copy()
+
+
 def abd_orthogonality(q12, kappa, volume, project=True):
     """energy/abd_energy.hpp:19-42 -> (value, grad 12, hess 12x12)."""
     v, g, h = np.empty(1), np.empty(12), np.empty(144)
@@ -409,8 +449,24 @@ def abd_orthogonality(q12, kappa, volume, project=True):
     return float(v[0]), g, h.reshape(12, 12).T.copy()
 
 
+_KEEP = []
+
+
+def _keep(a):
+    _KEEP.append(a)
+    return a.ctypes.data
+
+
+def _shell_ptrs(sh, ns):
+    if not ns:
+        return [None] * 7
+    conv = [("tri_begin", np.int64), ("tris", np.int32), ("tri_rest", np.float64), ("hinge_begin", np.int64),
+            ("hinges", np.int32), ("hinge_rest", np.float64), ("material", np.float64)]
+    return [_keep(np.ascontiguousarray(sh[k], t).reshape(-1)) for k, t in conv]
+
+
 def ip_fem_assemble(x, x_tilde, mass, tet_begin, mu, lam, tets, inv9, vol, dt2, pinned=None, project=True,
-                    bodies=None):
+                    bodies=None, shells=None, mesh_kind=None):
     """IncrementalPotential::assemble restricted to inertia + solid meshes +
     affine bodies (incremental_potential.hpp:170-249, 310-318, 253-254) ->
     (value, grad 3 (n + 4 nb), keys, vals) in emission order. bodies: dict of
@@ -421,7 +477,11 @@ def ip_fem_assemble(x, x_tilde, mass, tet_begin, mu, lam, tets, inv9, vol, dt2, 
     nm = len(tb) - 1
     nt = int(tb[-1])
     nb = 0 if bodies is None else len(bodies["kappa"])
-    cap = max(n + 10 * nt + 20 * nb, 1)
+    sh = shells or {}
+    ns = len(sh.get("material", []))
+    n_tri = int(sh["tri_begin"][-1]) if ns else 0
+    n_hg = int(sh["hinge_begin"][-1]) if ns else 0
+    cap = max(n + 10 * nt + 20 * nb + 6 * n_tri + 10 * n_hg, 1)
     keys, vals = np.empty(cap, np.uint64), np.empty((cap, 9))
     grad, val = np.empty(3 * (n + 4 * nb)), np.empty(1)
     bq = {}
@@ -437,7 +497,10 @@ def ip_fem_assemble(x, x_tilde, mass, tet_begin, mu, lam, tets, inv9, vol, dt2, 
                                      np.ascontiguousarray(inv9, np.float64).reshape(-1),
                                      np.ascontiguousarray(vol, np.float64), dt2,
                                      None if pin is None else pin.ctypes.data, int(project), keys, vals, grad, val,
-                                     nb, bp("q"), bp("q_tilde"), bp("reduced_mass"), bp("kappa"), bp("volume"))
+                                     nb, bp("q"), bp("q_tilde"), bp("reduced_mass"), bp("kappa"), bp("volume"),
+                                     ns, *_shell_ptrs(sh, ns),
+                                     0 if mesh_kind is None else len(mesh_kind),
+                                     None if mesh_kind is None else _keep(np.ascontiguousarray(mesh_kind, np.int32)))
     return float(val[0]), grad, keys[:T].copy(), vals[:T].copy()
 
 

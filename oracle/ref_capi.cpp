@@ -22,6 +22,8 @@
 
 #include "adipc/contact/barrier.hpp"
 #include "adipc/energy/abd_energy.hpp"
+#include "adipc/energy/bending.hpp"
+#include "adipc/energy/membrane.hpp"
 #include "adipc/energy/neo_hookean.hpp"
 #include "adipc/energy/psd.hpp"
 #include "adipc/precond/block_jacobi.hpp"
@@ -277,6 +279,64 @@ void ref_abd_orthogonality(const double* q12, double kappa, double volume, int p
     Vec12 q;
     std::memcpy(q.data(), q12, 96);
     const Stencil12 s = abd_orthogonality(q, kappa, volume, project != 0);
+    *value = s.value;
+    std::memcpy(grad12, s.grad.data(), 96);
+    std::memcpy(hess144, s.hess.data(), 1152);
+}
+
+int ref_membrane_rest(const double* p9, double* rest5) {
+    try {
+        const MembraneRest r = membrane_rest(ld3(p9), ld3(p9 + 3), ld3(p9 + 6));
+        std::memcpy(rest5, r.inv_rest_edges.data(), 32);
+        rest5[4] = r.area;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+// IncrementalPotential::membrane_stencil (incremental_potential.hpp:273-298,
+// a private member) composed from the reference's own membrane.hpp functions
+// in its exact sequence
+void ref_membrane_stencil(const double* x9, const double* rest5, const double* material5, int project, double* value,
+                          double* grad9, double* hess81) {
+    Mat2 inv;
+    std::memcpy(inv.data(), rest5, 32);
+    const Mat3x2 F = membrane_deformation(ld3(x9), ld3(x9 + 3), ld3(x9 + 6), inv);
+    const Real a_t = rest5[4] * material5[0];
+    MembraneDerivs d = fbw_membrane(F, material5[1], a_t, project != 0);
+    const MembraneDerivs lim = cubic_strain_limit(F, material5[2], a_t);
+    const MembraneDerivs sh = shear_energy(F, material5[3] * material5[1], a_t, project != 0);
+    d.value += lim.value + sh.value;
+    d.dF += lim.dF + sh.dF;
+    d.hess += lim.hess + sh.hess;
+    const Eigen::Matrix<Real, 6, 9> J = membrane_dFdx(inv);
+    const Mat3x2& dF = d.dF;
+    Vec6 g6;
+    g6 << dF.col(0), dF.col(1);
+    *value = d.value;
+    const Vec9 g = J.transpose() * g6;
+    const Mat9 H = J.transpose() * d.hess * J;
+    std::memcpy(grad9, g.data(), 72);
+    std::memcpy(hess81, H.data(), 648);
+}
+int ref_hinge_rest(const double* p12, double* rest2) {
+    try {
+        const HingeRest r = hinge_rest(ld3(p12), ld3(p12 + 3), ld3(p12 + 6), ld3(p12 + 9));
+        rest2[0] = r.rest_angle;
+        rest2[1] = r.weight;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+void ref_hinge_bending(const double* x12, const double* rest2, double k, int project, double* value, double* grad12,
+                       double* hess144) {
+    HingeRest r;
+    r.rest_angle = rest2[0];
+    r.weight = rest2[1];
+    const Stencil12 s = hinge_bending(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9), r, k, project != 0);
     *value = s.value;
     std::memcpy(grad12, s.grad.data(), 96);
     std::memcpy(hess144, s.hess.data(), 1152);

@@ -38,7 +38,10 @@ class FemDesc(C.Structure):
                 ("tets", C.c_void_p), ("rest_inv9", C.c_void_p), ("rest_volume", C.c_void_p), ("dt2", C.c_double),
                 ("project", C.c_int), ("pinned", C.c_void_p), ("n_bodies", C.c_int32), ("q", C.c_void_p),
                 ("q_tilde", C.c_void_p), ("reduced_mass", C.c_void_p), ("body_kappa", C.c_void_p),
-                ("body_volume", C.c_void_p)]
+                ("body_volume", C.c_void_p), ("n_shells", C.c_int32), ("tri_begin", C.c_void_p), ("tris", C.c_void_p),
+                ("tri_rest", C.c_void_p), ("hinge_begin", C.c_void_p), ("hinges", C.c_void_p),
+                ("hinge_rest", C.c_void_p), ("shell_material", C.c_void_p), ("n_kinds", C.c_int32),
+                ("mesh_kind", C.c_void_p)]
 
 
 class ContactDesc(C.Structure):

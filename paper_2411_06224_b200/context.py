@@ -180,12 +180,25 @@ class Context:
         d = _lib.FemDesc(n, ptr(x), ptr(x_tilde), ptr(mesh["mass"]), len(tb) - 1, tb.ctypes.data, mu.ctypes.data,
                          lam.ctypes.data, ptr(mesh["tets"]), ptr(mesh["rest_inv9"]), ptr(mesh["rest_volume"]),
                          float(dt2), int(project), ptr(pinned) if pinned is not None else None)
+        sh = mesh.get("shells")  # device tris / tri_rest / hinges / hinge_rest; host tri_begin / hinge_begin / material
+        keep = [tb, mu, lam]
+        if sh is not None:
+            stb = np.ascontiguousarray(sh["tri_begin"], np.int64)
+            shb = np.ascontiguousarray(sh["hinge_begin"], np.int64)
+            smat = np.ascontiguousarray(sh["material"], np.float64).reshape(-1)
+            kinds = np.ascontiguousarray(mesh["mesh_kind"], np.int32)
+            keep += [stb, shb, smat, kinds]
+            d.n_shells = len(stb) - 1
+            d.tri_begin, d.hinge_begin, d.shell_material = stb.ctypes.data, shb.ctypes.data, smat.ctypes.data
+            d.tris, d.tri_rest = ptr(sh["tris"]), ptr(sh["tri_rest"])
+            d.hinges, d.hinge_rest = ptr(sh["hinges"]), ptr(sh["hinge_rest"])
+            d.n_kinds, d.mesh_kind = len(kinds), kinds.ctypes.data
         b = mesh.get("bodies")  # device tensors q / q_tilde (nb x 12), reduced_mass (nb x 144), kappa, volume
         if b is not None:
             d.n_bodies = int(b["kappa"].numel())
             d.q, d.q_tilde, d.reduced_mass = ptr(b["q"]), ptr(b["q_tilde"]), ptr(b["reduced_mass"])
             d.body_kappa, d.body_volume = ptr(b["kappa"]), ptr(b["volume"])
-        return d, (tb, mu, lam), n
+        return d, keep, n
 
     def fem_emit(self, mesh, x, x_tilde, dt2, keys, vals, grad, project=True, pinned=None):
         """IncrementalPotential::assemble's inertia + tet stencils into the

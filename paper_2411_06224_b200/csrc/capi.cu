@@ -183,6 +183,7 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.graph_adj.free();
     c.graph_ptr.free();
     c.fem_keys.free();
+    c.hinge_work.free();
     for (auto* b : {&c.seg_cnt, &c.seg_row, &c.seg_heads}) b->free();
     for (auto* b : {&c.seg_ptr, &c.seg_bounds, &c.seg_u}) b->free();
     c.ct_on.free();
@@ -369,12 +370,37 @@ static FemDesc fem_desc(const adipc_fem_desc* d) {
     f.reduced_mass = d->reduced_mass;
     f.body_kappa = d->body_kappa;
     f.body_volume = d->body_volume;
+    if (d->n_shells < 0 || d->n_kinds < 0) throw StatusError(kInvalidArgument, "negative size");
+    if (d->n_shells > 0 && (!d->tri_begin || !d->hinge_begin || !d->shell_material))
+        throw StatusError(kInvalidArgument, "missing shell ranges / material");
+    if (d->n_shells > 0 && ((d->tri_begin[d->n_shells] > 0 && (!d->tris || !d->tri_rest)) ||
+                            (d->hinge_begin[d->n_shells] > 0 && (!d->hinges || !d->hinge_rest))))
+        throw StatusError(kInvalidArgument, "missing shell arrays");
+    if (d->n_kinds > 0) {
+        if (!d->mesh_kind) throw StatusError(kInvalidArgument, "missing mesh_kind");
+        int ns = 0, nm = 0;
+        for (int i = 0; i < d->n_kinds; ++i) (d->mesh_kind[i] ? ns : nm) += 1;
+        if (ns != d->n_shells || nm != d->n_meshes) throw StatusError(kInvalidArgument, "mesh_kind does not match the meshes");
+    } else if (d->n_shells > 0) {
+        throw StatusError(kInvalidArgument, "shells need the scene's mesh order (mesh_kind)");
+    }
+    f.n_shells = d->n_shells;
+    f.tri_begin = d->tri_begin;
+    f.tris = d->tris;
+    f.tri_rest = d->tri_rest;
+    f.hinge_begin = d->hinge_begin;
+    f.hinges = d->hinges;
+    f.hinge_rest = d->hinge_rest;
+    f.shell_material = d->shell_material;
+    f.n_kinds = d->n_kinds;
+    f.mesh_kind = d->mesh_kind;
     return f;
 }
 
 static std::int64_t fem_stream_len(const adipc_fem_desc* d) {
     return static_cast<std::int64_t>(d->n_verts) + 10 * (d->n_meshes > 0 ? d->tet_begin[d->n_meshes] : 0) +
-           20 * static_cast<std::int64_t>(d->n_bodies);
+           20 * static_cast<std::int64_t>(d->n_bodies) + (d->n_shells > 0 ? 6 * d->tri_begin[d->n_shells] +
+                                                           10 * d->hinge_begin[d->n_shells] : 0);
 }
 
 int adipc_gpu_fem_emit_device(adipc_gpu_ctx* ctx, const adipc_fem_desc* d, uint64_t* d_keys, double* d_vals9,

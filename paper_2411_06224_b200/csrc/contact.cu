@@ -23,6 +23,7 @@
 #include <limits>
 
 #include "context.hpp"
+#include "dual.cuh"
 #include "psd.cuh"
 #include "scan.cuh"
 
@@ -32,86 +33,11 @@ namespace {
 
 constexpr int kContactThreads = 64;
 
-// core/dual2.hpp with N = 12, Hessian packed upper (j >= i at j (j+1)/2 + i)
-struct D12 {
-    double v;
-    double g[12];
-    double h[78];
-};
-__device__ __forceinline__ int hp(int i, int j) { return i <= j ? j * (j + 1) / 2 + i : i * (i + 1) / 2 + j; }
-
-__device__ void d_sub(D12& r, const D12& a, const D12& b) {
-    r.v = a.v - b.v;
-    for (int i = 0; i < 12; ++i) r.g[i] = a.g[i] - b.g[i];
-    for (int i = 0; i < 78; ++i) r.h[i] = a.h[i] - b.h[i];
-}
-__device__ void d_add(D12& r, const D12& a, const D12& b) {
-    r.v = a.v + b.v;
-    for (int i = 0; i < 12; ++i) r.g[i] = a.g[i] + b.g[i];
-    for (int i = 0; i < 78; ++i) r.h[i] = a.h[i] + b.h[i];
-}
-// r = a b (r may not alias a or b)
-__device__ void d_mul(D12& r, const D12& a, const D12& b) {
-    r.v = a.v * b.v;
-    for (int i = 0; i < 12; ++i) r.g[i] = a.g[i] * b.v + b.g[i] * a.v;
-    for (int j = 0; j < 12; ++j)
-        for (int i = 0; i <= j; ++i)
-            r.h[hp(i, j)] = a.h[hp(i, j)] * b.v + b.h[hp(i, j)] * a.v + a.g[i] * b.g[j] + b.g[i] * a.g[j];
-}
-// r = a / b = a * inverse(b) (dual2.hpp:64-75)
-__device__ void d_div(D12& r, const D12& a, const D12& b, D12& tmp) {
-    const double iv = 1.0 / b.v;
-    tmp.v = iv;
-    for (int i = 0; i < 12; ++i) tmp.g[i] = -b.g[i] * (iv * iv);
-    const double c = 2 * iv * iv * iv;
-    for (int j = 0; j < 12; ++j)
-        for (int i = 0; i <= j; ++i) tmp.h[hp(i, j)] = -b.h[hp(i, j)] * (iv * iv) + (c * b.g[i]) * b.g[j];
-    d_mul(r, a, tmp);
-}
-// r = |a|^2 = a0 a0 + a1 a1 + a2 a2
-__device__ void d_norm2(D12& r, const D12* a, D12& t0, D12& t1) {
-    d_mul(t0, a[0], a[0]);
-    d_mul(t1, a[1], a[1]);
-    d_add(r, t0, t1);
-    d_mul(t0, a[2], a[2]);
-    d_add(t1, r, t0);
-    r = t1;
-}
-// r = a . b
-__device__ void d_dot(D12& r, const D12* a, const D12* b, D12& t0, D12& t1) {
-    d_mul(t0, a[0], b[0]);
-    d_mul(t1, a[1], b[1]);
-    d_add(r, t0, t1);
-    d_mul(t0, a[2], b[2]);
-    d_add(t1, r, t0);
-    r = t1;
-}
-// r = a x b
-__device__ void d_cross(D12* r, const D12* a, const D12* b, D12& t0, D12& t1) {
-    const int i1[3] = {1, 2, 0}, i2[3] = {2, 0, 1};
-    for (int k = 0; k < 3; ++k) {
-        d_mul(t0, a[i1[k]], b[i2[k]]);
-        d_mul(t1, a[i2[k]], b[i1[k]]);
-        d_sub(r[k], t0, t1);
-    }
-}
-
 // scratch of one thread's derivative evaluation (a global slice per thread)
 struct DualWork {
     D12 u[3], w[3], n[3];
     D12 s0, s1, t0, t1, t2;
 };
-
-// dual of (xa - xb) with xa, xb the AD variables ka, kb (dual_point + gsub)
-__device__ void d_diff(D12& r, double xa, int ka, double xb, int kb) {
-    r.v = xa - xb;
-    for (int i = 0; i < 12; ++i) r.g[i] = (i == ka ? 1.0 : 0.0) - (i == kb ? 1.0 : 0.0);
-    for (int i = 0; i < 78; ++i) r.h[i] = 0.0;
-}
-// the 3-vector dual (pa - pb) of stencil points a, b (coordinates x[.], variables 3 a + k)
-__device__ void d_vdiff(D12* r, const double* x, int a, int b) {
-    for (int k = 0; k < 3; ++k) d_diff(r[k], x[3 * a + k], 3 * a + k, x[3 * b + k], 3 * b + k);
-}
 
 // distance.hpp:111-140 on duals over the stencil x (12 coordinates); result in W.s0
 __device__ void pp_d2(DualWork& W, const double* x, int a, int b) {

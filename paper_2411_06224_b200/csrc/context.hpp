@@ -144,6 +144,7 @@ struct Ctx {
     // element-Hessian producer (energy.cu): the emitted stream + the value
     DBuf<std::uint64_t> fem_keys;
     DBuf<double> fem_vals, fem_value;
+    DBuf<unsigned char> hinge_work;  // per-thread dual scratch of the hinge producer
     // contact producers (contact.cu): activity flags / counts, their prefix
     // sums, the per-thread dual scratch, value / touch / ccd scalars
     DBuf<std::int32_t> ct_on;
@@ -292,6 +293,17 @@ struct FemDesc {
     const double* reduced_mass = nullptr;  // 144 per body, column-major
     const double* body_kappa = nullptr;
     const double* body_volume = nullptr;
+    // shells (membrane triangles + hinges) and the scene's mesh order
+    std::int32_t n_shells = 0;
+    const std::int64_t* tri_begin = nullptr;    // host, n_shells + 1
+    const std::int32_t* tris = nullptr;         // 3 per triangle
+    const double* tri_rest = nullptr;           // MembraneRest: Dm^-1 (2x2 column-major) + area, 5 per triangle
+    const std::int64_t* hinge_begin = nullptr;  // host, n_shells + 1
+    const std::int32_t* hinges = nullptr;       // 4 per hinge
+    const double* hinge_rest = nullptr;         // HingeRest: rest angle, weight
+    const double* shell_material = nullptr;     // host, 5 per shell: thickness, stretch, strain limit, shear fraction, bending
+    std::int32_t n_kinds = 0;                   // scene mesh order (0 solid, 1 shell); 0: solids only
+    const std::int32_t* mesh_kind = nullptr;    // host
 };
 void fem_emit(Ctx& c, const FemDesc& d, std::uint64_t* d_keys, double* d_vals, double* d_grad, double* d_value);
 

@@ -27,6 +27,7 @@
 //    cyclic Jacobi eigen-decomposition of M (per-thread local arrays; only
 //    indefinite elements take it) and proj(M) = V max(w, 0) V^T.
 #include "context.hpp"
+#include "dual.cuh"
 #include "psd.cuh"
 
 namespace adipc_gpu {
@@ -325,6 +326,184 @@ __global__ void k_body_orth(std::int32_t nb, std::int32_t base0, const double* _
     block_sum_atomic(dt2 * e, value);
 }
 
+
+// ---- shells (cfg2 cloth): membrane triangles and hinges ----------------------
+struct ShellParams {
+    double thickness, stretch, strain_limit, shear_fraction, bending;
+};
+
+// IncrementalPotential::membrane_stencil (incremental_potential.hpp:273-298;
+// energy/membrane.hpp:36-135): FBW stretch (per-axis eigenvalue clamp), cubic
+// strain limit, I6 shear (its 6 x 6 Hessian projected), then the chain rule
+// through membrane_dFdx as a bilinear form in C = G^T Dm^-1 (3 x 2); scatter9
+// (:300-308): 6 blocks, a <= b
+__global__ void __launch_bounds__(128) k_shell_tris(std::int64_t n_tris, const std::int32_t* __restrict__ tris,
+                                                    const double* __restrict__ rest5, const double* __restrict__ x,
+                                                    ShellParams m, double dt2, int project,
+                                                    std::uint64_t* __restrict__ keys, double* __restrict__ vals,
+                                                    double* __restrict__ grad, double* __restrict__ value) {
+    double e = 0;
+    for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < n_tris;
+         t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int ids[3] = {tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]};
+        const double* rs = rest5 + 5 * t;
+        double xa[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int k = 0; k < 3; ++k) xa[a][k] = x[3 * static_cast<std::int64_t>(ids[a]) + k];
+        double F[6];
+        for (int j = 0; j < 2; ++j)
+            for (int k = 0; k < 3; ++k) F[3 * j + k] = (xa[1][k] - xa[0][k]) * rs[2 * j] + (xa[2][k] - xa[0][k]) * rs[2 * j + 1];
+        const double a_t = rs[4] * m.thickness;
+        double val = 0, dF[6] = {0, 0, 0, 0, 0, 0}, H6[36];
+        for (int k = 0; k < 36; ++k) H6[k] = 0;
+        for (int dir = 0; dir < 2; ++dir) {  // fbw_membrane (membrane.hpp:54-75)
+            const double scale = m.stretch * a_t;
+            const double* f = F + 3 * dir;
+            const double I5v = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+            const double sq = sqrt(I5v);
+            val += scale * (sq - 1) * (sq - 1);
+            for (int k = 0; k < 3; ++k) dF[3 * dir + k] += 2 * scale * (1 - 1 / sq) * f[k];
+            const double e1 = 2 * scale;
+            double e23 = 2 * scale * (1 - 1 / sq);
+            if (project && e23 < 0) e23 = 0;
+            for (int c = 0; c < 3; ++c)
+                for (int r = 0; r < 3; ++r)
+                    H6[6 * (3 * dir + c) + 3 * dir + r] += (r == c ? e23 : 0.0) + (e1 - e23) * (f[r] / sq) * (f[c] / sq);
+        }
+        for (int dir = 0; dir < 2; ++dir) {  // cubic_strain_limit (:87-102)
+            const double scale = m.strain_limit * a_t;
+            const double* f = F + 3 * dir;
+            const double I5v = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+            if (I5v <= 1.0) continue;
+            const double sq = sqrt(I5v);
+            val += scale * (sq - 1) * (sq - 1) * (sq - 1);
+            for (int k = 0; k < 3; ++k) dF[3 * dir + k] += scale * (3 * (sq - 1) * (sq - 1) / sq) * f[k];
+            const double e1 = 6 * (sq - 1), e23 = 3 * (1 / sq + sq - 2);
+            for (int c = 0; c < 3; ++c)
+                for (int r = 0; r < 3; ++r)
+                    H6[6 * (3 * dir + c) + 3 * dir + r] += scale * ((r == c ? e23 : 0.0) + ((e1 - e23) / I5v) * f[r] * f[c]);
+        }
+        {  // shear_energy (:105-121)
+            const double scale = m.shear_fraction * m.stretch * a_t;
+            const double I6 = F[0] * F[3] + F[1] * F[4] + F[2] * F[5];
+            val += scale * I6 * I6;
+            for (int k = 0; k < 3; ++k) {
+                dF[k] += 2 * scale * I6 * F[3 + k];
+                dF[3 + k] += 2 * scale * I6 * F[k];
+            }
+            const double g[6] = {F[3], F[4], F[5], F[0], F[1], F[2]};
+            double S[36];
+            for (int c = 0; c < 6; ++c)
+                for (int r = 0; r < 6; ++r)
+                    S[6 * c + r] = 2 * scale * (g[r] * g[c] + I6 * ((r < 3) != (c < 3) && r % 3 == c % 3 ? 1.0 : 0.0));
+            if (project) project_sym<6>(S);
+            for (int k = 0; k < 36; ++k) H6[k] += S[k];
+        }
+        e += val;
+        double C[3][2];
+        for (int j = 0; j < 2; ++j) {
+            C[0][j] = -rs[2 * j] - rs[2 * j + 1];
+            C[1][j] = rs[2 * j];
+            C[2][j] = rs[2 * j + 1];
+        }
+        if (grad)
+            for (int a = 0; a < 3; ++a)
+                for (int k = 0; k < 3; ++k)
+                    red_add_f64(grad + 3 * static_cast<std::int64_t>(ids[a]) + k, dt2 * (C[a][0] * dF[k] + C[a][1] * dF[3 + k]));
+        if (!keys) continue;
+        int q = 0;
+        for (int a = 0; a < 3; ++a)
+            for (int b = a; b < 3; ++b, ++q) {
+                double h[9];
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r) {
+                        double v = 0;
+                        for (int j = 0; j < 2; ++j)
+                            for (int l = 0; l < 2; ++l) v += C[a][j] * C[b][l] * H6[6 * (3 * l + c) + 3 * j + r];
+                        h[3 * c + r] = v;
+                    }
+                const bool flip = ids[a] > ids[b];
+                const std::uint32_t r0 = static_cast<std::uint32_t>(flip ? ids[b] : ids[a]);
+                const std::uint32_t c0 = static_cast<std::uint32_t>(flip ? ids[a] : ids[b]);
+                keys[6 * t + q] = (static_cast<std::uint64_t>(r0) << 32) | c0;
+                double* o = vals + 9 * (6 * t + q);
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r) o[3 * c + r] = dt2 * (flip ? h[3 * r + c] : h[3 * c + r]);
+            }
+    }
+    block_sum_atomic(dt2 * e, value);
+}
+
+// hinge bending (energy/bending.hpp:11-75): k w (theta - rest)^2 with the
+// dihedral angle by second-order duals; PSD projection in the complement of
+// the translations (the angle is translation invariant); scatter12, 10 blocks
+struct HingeWork {
+    D12 e[3], n1[3], n2[3], t[3];
+    D12 a, b, c, d, t0, t1;
+};
+__global__ void __launch_bounds__(64) k_shell_hinges(std::int64_t n_h, const std::int32_t* __restrict__ hinges,
+                                                     const double* __restrict__ rest2, const double* __restrict__ x,
+                                                     double kb, double dt2, int project, std::uint64_t* __restrict__ keys,
+                                                     double* __restrict__ vals, double* __restrict__ grad,
+                                                     double* __restrict__ value, HingeWork* __restrict__ work) {
+    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+    HingeWork& W = work[tid];
+    double en = 0;
+    for (std::int64_t h = tid; h < n_h; h += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int ids[4] = {hinges[4 * h], hinges[4 * h + 1], hinges[4 * h + 2], hinges[4 * h + 3]};
+        double xs[12];
+        for (int a = 0; a < 4; ++a)
+            for (int k = 0; k < 3; ++k) xs[3 * a + k] = x[3 * static_cast<std::int64_t>(ids[a]) + k];
+        // dihedral_angle_g: e = x1 - x0, n1 = e x (x2 - x0), n2 = (x3 - x0) x e,
+        // s = ((n1 x n2) . e) / sqrt(|e|^2), c = n1 . n2, atan2(s, c)
+        d_vdiff(W.e, xs, 1, 0);
+        d_vdiff(W.t, xs, 2, 0);
+        d_cross(W.n1, W.e, W.t, W.t0, W.t1);
+        d_vdiff(W.t, xs, 3, 0);
+        d_cross(W.n2, W.t, W.e, W.t0, W.t1);
+        d_cross(W.t, W.n1, W.n2, W.t0, W.t1);
+        d_dot(W.a, W.t, W.e, W.t0, W.t1);   // (n1 x n2) . e
+        d_norm2(W.b, W.e, W.t0, W.t1);      // |e|^2
+        d_sqrt(W.b, W.b);
+        d_div(W.c, W.a, W.b, W.t0);         // s
+        d_dot(W.d, W.n1, W.n2, W.t0, W.t1); // c
+        d_atan2(W.a, W.c, W.d);             // theta
+        W.a.v += -rest2[2 * h];             // theta - rest
+        d_mul(W.b, W.a, W.a);
+        d_scale(W.c, W.b, kb * rest2[2 * h + 1]);
+        const D12& E = W.c;
+        en += E.v;
+        if (grad)
+            for (int a = 0; a < 4; ++a)
+                for (int k = 0; k < 3; ++k) red_add_f64(grad + 3 * static_cast<std::int64_t>(ids[a]) + k, dt2 * E.g[3 * a + k]);
+        if (!keys) continue;
+        double H[144];
+        for (int j = 0; j < 12; ++j)
+            for (int i = 0; i < 12; ++i) H[12 * j + i] = E.h[hp(i, j)];
+        if (project) {
+            double M[81];
+            reduce_translation(H, M);
+            if (!psd9(M)) {
+                project9(M);
+                lift_translation(M, H);
+            }
+        }
+        int q = 0;
+        for (int a = 0; a < 4; ++a)
+            for (int b = a; b < 4; ++b, ++q) {
+                const bool flip = ids[a] > ids[b];
+                const std::uint32_t r0 = static_cast<std::uint32_t>(flip ? ids[b] : ids[a]);
+                const std::uint32_t c0 = static_cast<std::uint32_t>(flip ? ids[a] : ids[b]);
+                keys[10 * h + q] = (static_cast<std::uint64_t>(r0) << 32) | c0;
+                double* o = vals + 9 * (10 * h + q);
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r)
+                        o[3 * c + r] = dt2 * (flip ? H[12 * (3 * b + r) + 3 * a + c] : H[12 * (3 * b + c) + 3 * a + r]);
+            }
+    }
+    block_sum_atomic(dt2 * en, value);
+}
+
 // pinned slots: zero gradient (incremental_potential.hpp:253-254)
 __global__ void k_fem_pin_grad(std::int32_t n, const std::uint8_t* __restrict__ pinned, double* __restrict__ grad) {
     for (std::int64_t v = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; v < n;
@@ -349,25 +528,61 @@ void fem_emit(Ctx& c, const FemDesc& d, std::uint64_t* d_keys, double* d_vals, d
         ADIPC_LAUNCH_CHECK();
     }
     // stream layout (incremental_potential.hpp:170-249): vertex inertia, body
-    // inertia tiles, 10 blocks per tet, body orthogonality tiles
+    // inertia tiles, the meshes in scene order (solid: 10 blocks per tet;
+    // shell: 6 per membrane triangle, then 10 per hinge), body orthogonality
     const std::int64_t nb = d.n_bodies;
-    const std::int64_t n_tets = d.n_meshes > 0 ? d.tet_begin[d.n_meshes] : 0;
-    const std::int64_t tets0 = d.n_verts + 10 * nb, orth0 = tets0 + 10 * n_tets;
+    std::int64_t off = d.n_verts + 10 * nb;
     if (nb > 0) {
         k_body_inertia<<<grid_for(nb, 128, 8), 128, 0, st>>>(d.n_bodies, d.n_verts, d.q, d.q_tilde, d.reduced_mass,
                                                              d_keys ? d_keys + d.n_verts : nullptr,
                                                              d_vals ? d_vals + 9 * d.n_verts : nullptr, d_grad, d_value);
         ADIPC_LAUNCH_CHECK();
     }
-    for (int m = 0; m < d.n_meshes; ++m) {
+    auto solid = [&](int m) {
         const std::int64_t t0 = d.tet_begin[m], nt = d.tet_begin[m + 1] - t0;
-        if (nt <= 0) continue;
-        k_fem_tets<<<grid_for(nt, kFemThreads, 16), kFemThreads, 0, st>>>(
-            nt, d.tets + 4 * t0, d.rest_inv9 + 9 * t0, d.rest_volume + t0, d.x, d.mu[m], d.lambda[m], d.dt2,
-            d.project, d_keys ? d_keys + tets0 + 10 * t0 : nullptr, d_vals ? d_vals + 9 * (tets0 + 10 * t0) : nullptr,
-            d_grad, d_value);
-        ADIPC_LAUNCH_CHECK();
+        if (nt > 0) {
+            k_fem_tets<<<grid_for(nt, kFemThreads, 16), kFemThreads, 0, st>>>(
+                nt, d.tets + 4 * t0, d.rest_inv9 + 9 * t0, d.rest_volume + t0, d.x, d.mu[m], d.lambda[m], d.dt2,
+                d.project, d_keys ? d_keys + off : nullptr, d_vals ? d_vals + 9 * off : nullptr, d_grad, d_value);
+            ADIPC_LAUNCH_CHECK();
+        }
+        off += 10 * nt;
+    };
+    auto shell = [&](int m) {
+        const ShellParams sp{d.shell_material[5 * m], d.shell_material[5 * m + 1], d.shell_material[5 * m + 2],
+                             d.shell_material[5 * m + 3], d.shell_material[5 * m + 4]};
+        const std::int64_t t0 = d.tri_begin[m], ntr = d.tri_begin[m + 1] - t0;
+        if (ntr > 0) {
+            k_shell_tris<<<grid_for(ntr, 128, 16), 128, 0, st>>>(ntr, d.tris + 3 * t0, d.tri_rest + 5 * t0, d.x, sp, d.dt2,
+                                                                  d.project, d_keys ? d_keys + off : nullptr,
+                                                                  d_vals ? d_vals + 9 * off : nullptr, d_grad, d_value);
+            ADIPC_LAUNCH_CHECK();
+        }
+        off += 6 * ntr;
+        const std::int64_t h0 = d.hinge_begin[m], nh = d.hinge_begin[m + 1] - h0;
+        if (nh > 0) {
+            const int grid = static_cast<int>(std::min<std::int64_t>(ceil_div(nh, 64), kSMs * 4));
+            c.hinge_work.reserve(static_cast<std::size_t>(grid) * 64 * sizeof(HingeWork));
+            k_shell_hinges<<<grid, 64, 0, st>>>(nh, d.hinges + 4 * h0, d.hinge_rest + 2 * h0, d.x, sp.bending, d.dt2,
+                                                d.project, d_keys ? d_keys + off : nullptr,
+                                                d_vals ? d_vals + 9 * off : nullptr, d_grad, d_value,
+                                                reinterpret_cast<HingeWork*>(c.hinge_work.p));
+            ADIPC_LAUNCH_CHECK();
+        }
+        off += 10 * nh;
+    };
+    if (d.n_kinds == 0) {
+        for (int m = 0; m < d.n_meshes; ++m) solid(m);
+    } else {
+        int si = 0, hi = 0;
+        for (int i = 0; i < d.n_kinds; ++i) {
+            if (d.mesh_kind[i] == 0)
+                solid(si++);
+            else
+                shell(hi++);
+        }
     }
+    const std::int64_t orth0 = off;
     if (nb > 0) {
         k_body_orth<<<grid_for(nb, 128, 8), 128, 0, st>>>(d.n_bodies, d.n_verts, d.q, d.body_kappa, d.body_volume,
                                                           d.dt2, d.project, d_keys ? d_keys + orth0 : nullptr,

@@ -62,54 +62,55 @@ __device__ __forceinline__ bool shifted_cholesky_ok(double* L, double tau) {
     return ok;
 }
 
-// proj(M) for a symmetric 9 x 9 (full column-major in `a`, overwritten):
+// proj(M) for a symmetric N x N (full column-major in `a`, overwritten):
 // cyclic Jacobi (oracle/sym_eig.hpp's rotations), then V max(w, 0) V^T
-__device__ __noinline__ void project9(double* a) {
-    double v[81];
-    for (int k = 0; k < 81; ++k) v[k] = (k % 10 == 0) ? 1.0 : 0.0;
+template <int N>
+__device__ __noinline__ void project_sym(double* a) {
+    double v[N * N];
+    for (int k = 0; k < N * N; ++k) v[k] = (k % (N + 1) == 0) ? 1.0 : 0.0;
     for (int sweep = 0; sweep < 64; ++sweep) {
         double off = 0, tot = 0;
-        for (int j = 0; j < 9; ++j)
-            for (int i = 0; i < 9; ++i) {
-                const double x = a[9 * j + i] * a[9 * j + i];
+        for (int j = 0; j < N; ++j)
+            for (int i = 0; i < N; ++i) {
+                const double x = a[N * j + i] * a[N * j + i];
                 tot += x;
                 if (i != j) off += x;
             }
         if (off <= 1e-32 * tot) break;
-        for (int p = 0; p < 8; ++p)
-            for (int q = p + 1; q < 9; ++q) {
-                const double apq = a[9 * q + p];
+        for (int p = 0; p < N - 1; ++p)
+            for (int q = p + 1; q < N; ++q) {
+                const double apq = a[N * q + p];
                 if (apq == 0.0) continue;
-                const double theta = (a[9 * q + q] - a[9 * p + p]) / (2.0 * apq);
+                const double theta = (a[N * q + q] - a[N * p + p]) / (2.0 * apq);
                 const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
                 const double c = rsqrt(t * t + 1.0), s = t * c;
-                for (int k = 0; k < 9; ++k) {
-                    const double kp = a[9 * p + k], kq = a[9 * q + k];
-                    a[9 * p + k] = c * kp - s * kq;
-                    a[9 * q + k] = s * kp + c * kq;
+                for (int k = 0; k < N; ++k) {
+                    const double kp = a[N * p + k], kq = a[N * q + k];
+                    a[N * p + k] = c * kp - s * kq;
+                    a[N * q + k] = s * kp + c * kq;
                 }
-                for (int k = 0; k < 9; ++k) {
-                    const double pk_ = a[9 * k + p], qk = a[9 * k + q];
-                    a[9 * k + p] = c * pk_ - s * qk;
-                    a[9 * k + q] = s * pk_ + c * qk;
+                for (int k = 0; k < N; ++k) {
+                    const double pk_ = a[N * k + p], qk = a[N * k + q];
+                    a[N * k + p] = c * pk_ - s * qk;
+                    a[N * k + q] = s * pk_ + c * qk;
                 }
-                for (int k = 0; k < 9; ++k) {
-                    const double kp = v[9 * p + k], kq = v[9 * q + k];
-                    v[9 * p + k] = c * kp - s * kq;
-                    v[9 * q + k] = s * kp + c * kq;
+                for (int k = 0; k < N; ++k) {
+                    const double kp = v[N * p + k], kq = v[N * q + k];
+                    v[N * p + k] = c * kp - s * kq;
+                    v[N * q + k] = s * kp + c * kq;
                 }
             }
     }
-    double w[9];
-    for (int k = 0; k < 9; ++k) w[k] = a[10 * k] > 0 ? a[10 * k] : 0.0;
-    for (int j = 0; j < 9; ++j)
-        for (int i = 0; i < 9; ++i) {
+    double w[N];
+    for (int k = 0; k < N; ++k) w[k] = a[(N + 1) * k] > 0 ? a[(N + 1) * k] : 0.0;
+    for (int j = 0; j < N; ++j)
+        for (int i = 0; i < N; ++i) {
             double s = 0;
-            for (int k = 0; k < 9; ++k) s += v[9 * k + i] * w[k] * v[9 * k + j];
-            a[9 * j + i] = s;
+            for (int k = 0; k < N; ++k) s += v[N * k + i] * w[k] * v[N * k + j];
+            a[N * j + i] = s;
         }
 }
-
+__device__ __forceinline__ void project9(double* a) { project_sym<9>(a); }
 
 // M (9 x 9, full column-major) = (Q (x) I3)^T H (Q (x) I3) from a 12 x 12
 // column-major H

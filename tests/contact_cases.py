@@ -144,3 +144,35 @@ def brute_candidates(pos, verts, edges, tris, inflate, disp=None):
     ee = [(i, j) for i in range(len(edges)) for j in range(i + 1, len(edges))
           if not set(edges[i]) & set(edges[j]) and ov(eb[i], eb[j])]
     return np.array(pt, np.int32).reshape(-1, 2), np.array(ee, np.int32).reshape(-1, 2)
+
+
+def build_hinges(tris):
+    """scene/mesh.hpp:98-121: interior edges shared by two triangles ->
+    (e0, e1, w0, w1), w0 the wing of the triangle running e0 -> e1."""
+    half, hinges = {}, []
+    for t in tris:
+        for a in range(3):
+            u, v, w = int(t[a]), int(t[(a + 1) % 3]), int(t[(a + 2) % 3])
+            key = (min(u, v), max(u, v))
+            if key not in half:
+                half[key] = (w, 0 if u == key[0] else 1)
+            else:
+                w0, d = half[key]
+                hinges.append([key[0], key[1], w0, w] if d == 0 else [key[0], key[1], w, w0])
+    return np.array(hinges, np.int32).reshape(-1, 4)
+
+
+def cloth_patch(n=20, seed=1, offset=0):
+    """A shell mesh (make_grid n x n) with its rest data from the oracle
+    (membrane_rest / hinge_rest) and a deformed state; node ids shifted by
+    `offset` (its position in the scene's slots)."""
+    rng = np.random.default_rng(seed)
+    verts, tris = make_grid(n, n, 1.0, 1.0)
+    verts[:, 2] = 0.02 * np.sin(3 * verts[:, 0]) * np.cos(2 * verts[:, 1])
+    hinges = build_hinges(tris)
+    tri_rest = np.array([O.membrane_rest(verts[t].reshape(-1)) for t in tris])
+    hinge_rest = np.array([O.hinge_rest(verts[h].reshape(-1)) for h in hinges])
+    x = verts * np.array([1.05, 0.98, 1.0]) + rng.normal(0, 0.01, verts.shape)
+    mass = rng.uniform(1e-4, 2e-4, len(verts))
+    return {"verts": verts, "x": x, "mass": mass, "tris": tris + offset, "hinges": hinges + offset,
+            "tri_rest": tri_rest, "hinge_rest": hinge_rest, "material": [1e-3, 5e4, 5e6, 0.3, 1e-3]}

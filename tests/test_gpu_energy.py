@@ -211,3 +211,59 @@ def test_fem_emit_with_bodies_and_value(ctx):
     v2 = ctx.fem_value(mesh, dx, dxt, DT2, g2, pinned=dpin)
     assert abs(v2 - val) <= 1e-13 * abs(val)
     assert torch.allclose(g2, grad, rtol=0, atol=1e-12 * float(torch.abs(grad).max()))
+
+
+@pytest.mark.parametrize("order", [(0, 1), (1, 0)])
+def test_fem_emit_shells_and_solids_in_mesh_order(ctx, order):
+    """A cloth patch (membrane triangles + hinges, incremental_potential.hpp:
+    190-221, membrane.hpp, bending.hpp) and the soft cube in either scene
+    order: the stream follows the mesh order (solid: tets; shell: triangles
+    then hinges); keys bitwise, values to 1e-10 of each stencil's scale,
+    gradient and value to 1e-12."""
+    from contact_cases import cloth_patch
+
+    sc = scenes.CONFIGS["cfg1_soft_cube"]()
+    inv9, vol = scenes.tet_rest_data(sc.verts, sc.tets)
+    nsol = len(sc.mass)
+    first_solid = order[0] == 0
+    off = nsol if first_solid else 0
+    cl = cloth_patch(20, 3, offset=off)
+    ncl = len(cl["mass"])
+    sol_off = 0 if first_solid else ncl
+    tets = sc.tets + sol_off
+    n = nsol + ncl
+    x = np.zeros((n, 3))
+    mass = np.zeros(n)
+    xs = deformed(sc, 0.1, 4).reshape(-1, 3)
+    x[sol_off:sol_off + nsol], mass[sol_off:sol_off + nsol] = xs, sc.mass
+    x[off:off + ncl], mass[off:off + ncl] = cl["x"], cl["mass"]
+    x = np.ascontiguousarray(x.reshape(-1))
+    xt = x + np.random.default_rng(1).normal(0, 1e-5, x.shape)
+    shells = {"tri_begin": [0, len(cl["tris"])], "hinge_begin": [0, len(cl["hinges"])], "tris": cl["tris"],
+              "tri_rest": cl["tri_rest"], "hinges": cl["hinges"], "hinge_rest": cl["hinge_rest"],
+              "material": [cl["material"]]}
+    kinds = list(order)
+    ov, og, ok, ovals = O.ip_fem_assemble(x, xt, mass, [0, len(tets)], [sc.mu], [sc.lam], tets, inv9, vol, DT2,
+                                          shells=shells, mesh_kind=kinds)
+    t = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a, dt)).cuda()  # noqa: E731
+    mesh = {"mass": t(mass), "tets": t(tets, np.int32), "rest_inv9": t(inv9), "rest_volume": t(vol),
+            "tet_begin": [0, len(tets)], "mu": [sc.mu], "lam": [sc.lam], "mesh_kind": kinds,
+            "shells": {"tri_begin": [0, len(cl["tris"])], "hinge_begin": [0, len(cl["hinges"])],
+                       "tris": t(cl["tris"], np.int32), "tri_rest": t(cl["tri_rest"]),
+                       "hinges": t(cl["hinges"], np.int32), "hinge_rest": t(cl["hinge_rest"]),
+                       "material": [cl["material"]]}}
+    T = len(ok)
+    keys = torch.empty(T, dtype=torch.int64, device="cuda:0")
+    vals = torch.empty((T, 9), dtype=torch.float64, device="cuda:0")
+    grad = torch.empty(3 * n, dtype=torch.float64, device="cuda:0")
+    val = ctx.fem_emit(mesh, t(x), t(xt), DT2, keys, vals, grad)
+    keys = keys.cpu().numpy().view(np.uint64)
+    assert np.array_equal(keys, ok)
+    vals = vals.cpu().numpy()
+    diff = np.linalg.norm(vals - ovals, axis=1)
+    norm = np.linalg.norm(ovals, axis=1)
+    scale = np.max(np.lib.stride_tricks.sliding_window_view(np.pad(norm, 9), 19), axis=1)
+    assert np.all(diff <= 1e-10 * scale + 1e-300)
+    g = grad.cpu().numpy()
+    assert np.linalg.norm(g - og) <= 1e-12 * np.linalg.norm(og)
+    assert abs(val - ov) <= 1e-12 * abs(ov)

@@ -145,3 +145,40 @@ def test_rest_state_stream_matches_scene_generator():
     assert np.array_equal(keys, sc.keys)
     scale = np.abs(sc.vals).max()
     assert np.abs(vals - sc.vals).max() <= 1e-12 * scale
+
+
+def test_shell_stencils_equal_reference_and_fd():
+    """Membrane (incremental_potential.hpp:273-298 over energy/membrane.hpp)
+    and hinge bending (energy/bending.hpp) restated vs the reference's own
+    code (membrane to 1e-14, the chain-rule order differs; hinge bitwise),
+    and their raw gradients / Hessians against central differences."""
+    rng = np.random.default_rng(8)
+    mat = [1e-3, 5e4, 5e6, 0.3, 1e-3]
+    have_ref = O.reference_available()
+    for t in range(40):
+        p = np.array([0, 0, 0, 1, 0, 0, 0, 1, 0.0]) + rng.normal(0, 0.05, 9)
+        r = O.membrane_rest(p)
+        x = p * np.tile([1.1, 0.95, 1.0], 3) + rng.normal(0, 0.03, 9)
+        q = np.concatenate([p, p[3:6] + p[6:9] - p[:3] + rng.normal(0, 0.05, 3)])
+        hr = O.hinge_rest(q)
+        y = q + rng.normal(0, 0.05, 12)
+        for project in (True, False):
+            a = O.membrane_stencil(x, r, mat, project)
+            ha = O.hinge_bending(y, hr, 1e-3, project)
+            if have_ref:
+                with O.use_backend("reference"):
+                    b = O.membrane_stencil(x, r, mat, project)
+                    hb = O.hinge_bending(y, hr, 1e-3, project)
+                assert abs(a[0] - b[0]) <= 1e-14 * abs(b[0])
+                assert np.abs(a[1] - b[1]).max() <= 1e-14 * np.abs(b[1]).max()
+                assert np.abs(a[2] - b[2]).max() <= 1e-14 * np.abs(b[2]).max()
+                assert ha[0] == hb[0] and np.array_equal(ha[1], hb[1]) and np.array_equal(ha[2], hb[2])
+        if t < 8:  # central differences of the raw stencils
+            for f, z, n in ((lambda v: O.membrane_stencil(v, r, mat, False), x, 9),
+                            (lambda v: O.hinge_bending(v, hr, 1e-3, False), y, 12)):
+                _, g, H = f(z)
+                eps = 1e-7
+                fg = np.array([(f(z + e)[0] - f(z - e)[0]) / (2 * eps) for e in np.eye(n) * eps])
+                fh = np.array([(f(z + e)[1] - f(z - e)[1]) / (2 * eps) for e in np.eye(n) * eps]).T
+                assert rel_err(g, fg) <= 1e-5
+                assert rel_err(H, fh) <= 1e-4

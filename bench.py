@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-producer", action="store_true", help="skip the device element-Hessian producer timing")
     ap.add_argument("--no-hybrid", action="store_true",
                     help="skip the cfg4_hybrid_1m Newton-solve line (the north star's ~1M-DOF hybrid scene)")
+    ap.add_argument("--no-geom", action="store_true",
+                    help="skip the geometric hybrid Newton iteration (real contact: broad phase + producers on the device)")
     ap.add_argument("--selftest", action="store_true",
                     help="launcher / rendezvous / stats-gather self-test without GPU work (CPU tests, gloo)")
     return ap.parse_args()
@@ -441,6 +443,144 @@ def hybrid_gpu(args, local_rank, with_cpu):
         out["cpu_baseline"]["ms_per_newton_solve_est"] = cpu_solve_s * 1e3
         out["speedup_newton_solve_vs_cpu"] = cpu_solve_s * 1e3 / out["ms_per_newton_solve"]
         out["speedup_e2e_newton_solve_vs_cpu"] = cpu_solve_s * 1e3 / e2e_ms
+    return out
+
+
+# ------------------------------------------------- geometric hybrid scene ---
+GEOM = "geom_hybrid_1m"
+GEOM_WORKLOAD = ("geometric hybrid at ~1M DOF: 2x2x2 FEM blocks 34^3 cells (E=1e8, 343,000 vertices, 1.89M tets) + "
+                 "5x5 affine bodies (kappa 1e8) resting on them, every interface dhat/2 = 0.5 mm apart; one Newton "
+                 "iteration from host state: contact-node positions, broad phase, contact + element + body "
+                 "producers, gradient lift, two-level reduction + sort + reduce, cold MAS build, PCG on -grad")
+
+
+def geom_cpu(full_solve=True):
+    """The reference's CPU path for one Newton iteration of the geometric
+    hybrid scene (IncrementalPotential::assemble composed from oracle/_ref's
+    compiled reference pieces — element stencils, broad phase, contact
+    stencils, two-level reduction, sort, reduction — then the hierarchy + MAS
+    build and the whole PCG solve), all host threads."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O
+    from scenegen.geom import GeomHybrid
+
+    g = GeomHybrid()
+    kind = "reference" if O.reference_available() else "port"
+    with O.use_backend("reference" if kind == "reference" else "restated"):
+        cores = O.lib().oracle_max_threads()
+        par = O.ExecPolicy(deterministic=False, threads=cores)
+        t0 = time.perf_counter()
+        _, grad, rows, cols, blocks, cnt = O.ip_assemble(g, g.state(), par)
+        t_asm = time.perf_counter() - t0
+        part_of, n_parts = O.partition_block_graph(g.n_blocks, g.rest_edges, CAPACITY)
+        t0 = time.perf_counter()
+        A = O.Matrix(g.n_blocks, rows, cols, blocks)
+        H = O.Hierarchy(part_of, n_parts, CAPACITY, O.block_edges(rows, cols), MAX_LEVELS)
+        M = O.MasPreconditioner(A, H)
+        t_build = time.perf_counter() - t0
+        out = {"config": GEOM, "kind": kind, "cores": cores, "assembly_s": t_asm, "mas_build_s": t_build,
+               "U": int(len(rows)), **{k: int(v) for k, v in cnt.items()}}
+        if full_solve:
+            t0 = time.perf_counter()
+            _, r = O.pcg_solve(A, -grad, M, REL_TOL, RESTART, MAX_ITERS, par)
+            out.update(pcg_s=time.perf_counter() - t0, iters=int(r["iters"]), converged=bool(r["converged"]))
+            out["newton_iteration_s"] = t_asm + t_build + out["pcg_s"]
+    out["sample"] = ("one Newton iteration: " + ("oracle/_ref (the reference's compiled code)" if kind == "reference"
+                     else "oracle restatement") + "; assembly = element + body stencils with PSD projection, "
+                     "broad phase, contact stencils, two-level reduction, sort, reduction")
+    return out
+
+
+def geom_gpu(args, local_rank):
+    """geom_hybrid_1m on this GPU through the device IncrementalPotential
+    (potential.py over the C ABI): a step = one Newton iteration's linear
+    solve from the HOST state — H2D of [x; q], assemble (positions, broad
+    phase, contact / element / body producers, lift, two-level + sort +
+    reduce), a cold MAS build, PCG on -grad, D2H of the direction."""
+    import torch
+
+    from paper_2411_06224_b200 import _lib
+    from paper_2411_06224_b200 import api as P
+    from paper_2411_06224_b200.context import Context
+    from paper_2411_06224_b200.potential import IncrementalPotential
+    from scenegen.geom import GeomHybrid
+
+    g = GeomHybrid()
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.Stream(dev)
+    ctx = Context(local_rank, stream=stream)
+    ctx.set_option(_lib.OPT_PROFILE, 0)
+    ctx.set_option(_lib.OPT_CACHE_HIERARCHY, 0)
+    l0 = P.partition_block_graph(g.n_blocks, g.rest_edges, CAPACITY)
+    ctx.set_level0_partition(l0.part_of, l0.n_parts, CAPACITY, MAX_LEVELS)
+    with torch.cuda.stream(stream):
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        mesh = {"mass": t(g.mass), "tets": t(g.tets), "rest_inv9": t(g.rest_inv9), "rest_volume": t(g.rest_volume),
+                "tet_begin": g.tet_begin, "mu": [g.mu], "lam": [g.lam],
+                "bodies": {"reduced_mass": t(g.reduced_mass.transpose(0, 2, 1)), "kappa": t(g.kappa_abd),
+                           "volume": t(g.body_volume)}}
+        ip = IncrementalPotential(ctx, mesh, {"verts": t(g.surf_verts), "edges": t(g.edges), "tris": t(g.tris)},
+                                  {"n_fem": g.n_fem, "abd_body": t(g.abd_body), "jac36": t(g.jac36)}, g.dt,
+                                  pinned=t(g.pinned))
+        ip.set_targets(t(g.x_tilde.reshape(-1)), t(g.q_tilde))
+        ip.set_contact(g.dhat, g.kappa)
+        d_state = torch.empty(3 * g.n_blocks, dtype=torch.float64, device=dev)
+        d_dir, d_rhs, d_res = (torch.empty_like(d_state) for _ in range(3))
+    stream.synchronize()
+    h_state = torch.from_numpy(g.state()).pin_memory()
+    h_dir = torch.empty(3 * g.n_blocks, dtype=torch.float64).pin_memory()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+
+    def newton():
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            d_state.copy_(h_state, non_blocking=True)
+            _, grad = ip.assemble(d_state)
+            ev[1].record(stream)
+            ctx.build_preconditioner(_lib.PRECOND_MAS)
+            ev[2].record(stream)
+            torch.neg(grad, out=d_rhs)
+            _, res = ctx.pcg(d_rhs, REL_TOL, RESTART, MAX_ITERS, x=d_dir)
+            ev[3].record(stream)
+            h_dir.copy_(d_dir, non_blocking=True)
+            ev[4].record(stream)
+        stream.synchronize()
+        return res, [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
+
+    for _ in range(args.warmup):
+        newton()
+    ip.profile = True  # one profiled iteration: the assemble phases
+    newton()
+    asm_phases = dict(ip.last["phase_ms"])
+    ip.profile = False
+    launches0 = Context.kernel_launches()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    recs = [newton() for _ in range(args.steps)]
+    wall_ms = (time.perf_counter() - t0) * 1000.0 / args.steps
+    launches = (Context.kernel_launches() - launches0) / args.steps
+    ph = np.mean([r[1] for r in recs], axis=0)
+    with torch.cuda.stream(stream):  # size-independent check: ||A d + grad|| / ||grad||
+        ctx.spmv(d_dir, d_res)
+        rel = float(torch.linalg.norm(d_res - d_rhs) / torch.linalg.norm(d_rhs))
+    n, U = ctx.matrix_info()
+    levels = ctx.precond_levels()
+    out = {"config": GEOM, "workload": GEOM_WORKLOAD, "dof": 3 * int(g.n_blocks), "tets": int(len(g.tets)),
+           "bodies": int(g.n_bodies), "surface": {"verts": int(len(g.surf_verts)), "edges": int(len(g.edges)),
+                                                   "tris": int(len(g.tris))},
+           "U": int(U), "candidates_pt": ip.last["n_pt"], "candidates_ee": ip.last["n_ee"],
+           "contact_node_blocks": ip.last["node_blocks"], "contact_tiles": ip.last["contact_tiles"],
+           "levels": [(int(L_["n_nodes"]), int(L_["n_parts"])) for L_ in levels],
+           "ms_per_newton_iteration": wall_ms, "assemble_ms": float(ph[0]), "assemble_phases_ms": asm_phases,
+           "mas_build_cold_ms": float(ph[1]),
+           "pcg_ms": float(ph[2]), "d2h_ms": float(ph[3]),
+           "pcg_iters": float(np.mean([r[0].iters for r in recs])),
+           "converged": all(r[0].converged for r in recs), "true_rel_residual": rel,
+           "gpu_launches_per_iteration": launches,
+           "h2d_bytes_per_step": 3 * 8 * int(g.n_blocks), "d2h_bytes_per_step": 3 * 8 * int(g.n_blocks),
+           "timing": "wall clock per step around H2D .. D2H with a stream sync (host-pointer e2e); phases by "
+                     "CUDA events on the context stream"}
+    ctx.close()
     return out
 
 
@@ -866,6 +1006,8 @@ def main():
                               "assembly_s": hy["assembly_s"], "two_level_s": hy["two_level_s"],
                               "mas_build_s": hy["mas_build_s"], "full_solve": hf,
                               "ms_per_newton_solve": 1000.0 * hf["newton_solve_s"] if hf else None}
+        if not args.no_geom and args.config == "cfg5_stiff_box":
+            line["geom"] = geom_cpu(full_solve=not args.no_full_solve)
         print(json.dumps(line), flush=True)
         return
     dist = None
@@ -881,6 +1023,10 @@ def main():
         hy = hybrid_gpu(args, local_rank, with_cpu=(rank == 0 and world == 1 and not args.no_cpu_baseline))
         if rank == 0:
             out["hybrid"] = hy
+    if not args.no_geom and args.config == "cfg5_stiff_box":
+        ge = geom_gpu(args, local_rank)
+        if rank == 0:
+            out["geom"] = ge
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(sc, 5, args.cpu_iters, 2, 1)

@@ -109,6 +109,14 @@ int adipc_gpu_step_inf_norm_device(adipc_gpu_ctx* ctx, const double* d_dir, int3
 /* apply_direction (newton.hpp:283-290): out = state + alpha dir over n_dofs (x of the vertices, q of the bodies) */
 int adipc_gpu_apply_direction_device(adipc_gpu_ctx* ctx, const double* d_state, const double* d_dir, double alpha,
                                      int64_t n_dofs, double* d_out);
+/* the contact gradient lift of assemble_contact (incremental_potential.hpp:395-403):
+ * d_grad (block numbering) += node gradient, through J^T for affine-body nodes;
+ * slots with d_pinned[slot] != 0 (nullable) receive nothing, as the reference
+ * zeroes them right after (:253-254). The contact-node positions of a state
+ * (contact_node_positions, scene.hpp) are node_displacements applied to (x, q). */
+int adipc_gpu_lift_node_grad_device(adipc_gpu_ctx* ctx, const double* d_node_grad, int32_t n_fem, int32_t n_abd,
+                                    const int32_t* d_abd_node_body, const double* d_abd_node_jacobian36,
+                                    const uint8_t* d_pinned, double* d_grad);
 /* node_displacements (newton.hpp:272-281): FEM nodes copy d; affine-body node a moves by J_a d_body
  * (abd_node_jacobian 3x12 column-major, 36 doubles per node, DofMap abd_reduce.hpp:11-27) */
 int adipc_gpu_node_displacements_device(adipc_gpu_ctx* ctx, const double* d_dir, int32_t n_fem, int32_t n_abd,

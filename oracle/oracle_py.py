@@ -800,3 +800,53 @@ def abd_jacobian(rest):
     for r in range(3):
         J[r, 3 + 3 * r: 6 + 3 * r] = rest
     return J.T.reshape(-1).copy()
+
+
+# ---- IncrementalPotential::assemble composed (incremental_potential.hpp:162-258) ----
+def lift_node_grad(node_grad, n_fem, abd_node_body, jac36, grad):
+    """:395-403 — grad (block numbering) += node gradient: FEM nodes copy-add,
+    affine-body node a adds J_a^T g_a to its body's 12 dofs, in node order."""
+    g = np.asarray(node_grad, np.float64).reshape(-1, 3)
+    grad[: 3 * n_fem] += g[:n_fem].reshape(-1)  # zero node gradients add nothing
+    for a, b in enumerate(abd_node_body):
+        gn = g[n_fem + a]
+        if np.dot(gn, gn) == 0:
+            continue
+        J = np.asarray(jac36[a], np.float64).reshape(12, 3)  # J^T rows
+        s = 3 * (n_fem + 4 * int(b))
+        grad[s: s + 12] += J @ gn
+    return grad
+
+
+def ip_assemble(sc, state, policy=None, project=True):
+    """IncrementalPotential::assemble on a scene of one solid mesh + affine
+    bodies + a contact surface (scenegen.geom.GeomHybrid's attributes): the
+    element stream (ip_fem_assemble), contact-node positions, the proximity
+    broad phase (find_candidates, inflate dhat, :330), the contact node part
+    (contact_assemble), the gradient lift, two_level_abd_reduce appended to
+    the stream, pinned gradient zeroing (:253-254), filter_pinned, sort and
+    reduce. Returns (value, grad, rows, cols, blocks, counts)."""
+    state = np.asarray(state, np.float64)
+    n_fem, nb = sc.n_fem, sc.n_bodies
+    x, q = state[: 3 * n_fem], state[3 * n_fem:].reshape(nb, 12)
+    bodies = None
+    if nb:
+        bodies = {"q": q, "q_tilde": sc.q_tilde, "reduced_mass": sc.reduced_mass, "kappa": sc.kappa_abd,
+                  "volume": sc.body_volume}
+    dt2 = sc.dt * sc.dt
+    val, grad, keys, vals = ip_fem_assemble(x, sc.x_tilde, sc.mass, sc.tet_begin, [sc.mu], [sc.lam], sc.tets,
+                                            sc.rest_inv9, sc.rest_volume, dt2, None, project, bodies)
+    pos = node_displacements(state, n_fem, sc.abd_body, sc.jac36).reshape(-1, 3)
+    pt, ee = find_candidates(pos, sc.surf_verts, sc.edges, sc.tris, sc.dhat)
+    ci = ContactInput(pos, np.c_[sc.surf_verts[pt[:, 0]], sc.tris[pt[:, 1]]],
+                      np.c_[sc.edges[ee[:, 0]], sc.edges[ee[:, 1]]], dhat=sc.dhat, kappa=sc.kappa)
+    cv, ng, nk, nv = contact_assemble(ci, dt2, project)
+    val += cv
+    tk, tv = two_level_abd_reduce(nk, nv, n_fem, nb, sc.abd_body, sc.jac36, policy)
+    lift_node_grad(ng, n_fem, sc.abd_body, sc.jac36, grad)
+    grad.reshape(-1, 3)[np.asarray(sc.pinned, bool)] = 0
+    fk, fv = filter_pinned(np.concatenate([keys, tk]), np.concatenate([vals, tv]), sc.pinned)
+    sk, sv = sort_stream(fk, fv, policy)
+    rows, cols, blocks = fast_hash_reduction(sk, sv, sc.n_blocks, policy)
+    return val, grad, rows, cols, blocks, {"n_pt": len(pt), "n_ee": len(ee), "node_blocks": len(nk),
+                                           "contact_tiles": len(tk)}

@@ -86,6 +86,7 @@ GPU_SIGNATURES = {
     "adipc_gpu_assemble_contact_device": (ci, [vp, vp, vp, i64, vp, vp, i64, i32, i32, i32, vp, vp, i32, vp,
                                                C.POINTER(i64), C.POINTER(i64)]),
     "adipc_gpu_filter_pinned": (ci, [vp, vp, vp, i64, vp, i32, vp, vp, C.POINTER(i64)]),
+    "adipc_gpu_lift_node_grad_device": (ci, [vp, vp, i32, i32, vp, vp, vp, vp]),
     "adipc_gpu_broad_phase_device": (ci, [vp, i32, vp, vp, i32, vp, i32, vp, i32, vp, cd, C.POINTER(i64),
                                           C.POINTER(i64)]),
     "adipc_gpu_broad_phase_copy": (ci, [vp, vp, vp, vp, vp]),

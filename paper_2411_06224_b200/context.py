@@ -66,6 +66,7 @@ class Context:
             _raise(rc, self._L.adipc_gpu_last_error(None).decode())
         self.h = h
         self.device = device
+        self.stream = None
         if stream is not None:
             self.set_stream(stream)
 
@@ -89,6 +90,7 @@ class Context:
         """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None."""
         raw = getattr(stream, "cuda_stream", stream)
         self._check(self._L.adipc_gpu_set_stream(self.h, raw))
+        self.stream = stream
 
     def set_option(self, option: int, value: int):
         self._check(self._L.adipc_gpu_set_option(self.h, option, value))
@@ -267,6 +269,14 @@ class Context:
                                                           ptr(vals), keys.numel(), ptr(node_grad), C.byref(v),
                                                           C.byref(n)))
         return v.value, n.value
+
+    def lift_node_grad(self, node_grad, n_fem, abd_body, jac36, grad, pinned=None):
+        """grad += the contact node gradient (FEM nodes; J^T for body nodes),
+        incremental_potential.hpp:395-403 (device tensors); pinned slots get
+        nothing."""
+        n_abd = 0 if abd_body is None else abd_body.numel()
+        self._check(self._L.adipc_gpu_lift_node_grad_device(self.h, ptr(node_grad), n_fem, n_abd, ptr(abd_body),
+                                                            ptr(jac36), ptr(pinned), ptr(grad)))
 
     def broad_phase(self, pos, verts, edges, tris, inflate, disp=None):
         """find_candidates (broad_phase.hpp:143-211) on device tensors; returns

@@ -635,6 +635,18 @@ int adipc_gpu_apply_direction_device(adipc_gpu_ctx* ctx, const double* d_state, 
     });
 }
 
+int adipc_gpu_lift_node_grad_device(adipc_gpu_ctx* ctx, const double* d_node_grad, int32_t n_fem, int32_t n_abd,
+                                    const int32_t* d_abd_node_body, const double* d_abd_node_jacobian36,
+                                    const uint8_t* d_pinned, double* d_grad) {
+    return guarded(ctx, [&] {
+        if (n_fem < 0 || n_abd < 0) throw StatusError(kInvalidArgument, "negative size");
+        if ((n_fem + n_abd > 0 && (!d_node_grad || !d_grad)) || (n_abd > 0 && (!d_abd_node_body || !d_abd_node_jacobian36)))
+            throw StatusError(kInvalidArgument, "missing arrays");
+        lift_node_grad(ctx->c, d_node_grad, n_fem, n_abd, d_abd_node_body, d_abd_node_jacobian36, d_pinned, d_grad);
+        sync(ctx->c);
+    });
+}
+
 int adipc_gpu_node_displacements_device(adipc_gpu_ctx* ctx, const double* d_dir, int32_t n_fem, int32_t n_abd,
                                         const int32_t* d_abd_node_body, const double* d_abd_jacobian36,
                                         double* d_out) {

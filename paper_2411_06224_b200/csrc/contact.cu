@@ -12,18 +12,20 @@
 // the line-search value (incremental_potential.hpp:133-157) and the
 // conservative-advancement CCD step bound (contact/ccd.hpp:17-110).
 //
-// One thread per stencil. The derivatives use forward-mode second-order
-// duals over the 12 stencil coordinates exactly like core/dual2.hpp (value,
-// gradient, symmetric Hessian), in per-thread local memory; a pair is active
-// when the dual's value is below dhat^2 (the reference's test on pd.dist2),
-// found by a value-only pass with the same arithmetic so the stream can be
-// compacted by a prefix sum before the derivative pass.
+// A value-only pass classifies every candidate and flags it active when the
+// feature's squared distance (the duals' value arithmetic, bitwise) is below
+// dhat^2 — the reference's test on pd.dist2 — a prefix sum compacts the
+// active pairs, and the derivative pass runs one thread per ACTIVE pair. The
+// reference differentiates with second-order duals over the 12 stencil
+// coordinates (core/dual2.hpp); the derivative pass here uses the closed
+// forms of dist_derivs.cuh over the feature's 1-3 difference vectors (the
+// same derivatives to rounding, without a 91-double dual per intermediate).
 #include <cmath>
 #include <cstring>
 #include <limits>
 
 #include "context.hpp"
-#include "dual.cuh"
+#include "dist_derivs.cuh"
 #include "psd.cuh"
 #include "scan.cuh"
 
@@ -31,38 +33,7 @@ namespace adipc_gpu {
 
 namespace {
 
-constexpr int kContactThreads = 64;
-
-// scratch of one thread's derivative evaluation (a global slice per thread)
-struct DualWork {
-    D12 u[3], w[3], n[3];
-    D12 s0, s1, t0, t1, t2;
-};
-
-// distance.hpp:111-140 on duals over the stencil x (12 coordinates); result in W.s0
-__device__ void pp_d2(DualWork& W, const double* x, int a, int b) {
-    d_vdiff(W.u, x, a, b);
-    d_norm2(W.s0, W.u, W.t0, W.t1);
-}
-__device__ void pe_d2(DualWork& W, const double* x, int p, int e0, int e1) {
-    d_vdiff(W.u, x, e1, e0);  // d
-    d_vdiff(W.w, x, p, e0);   // w
-    d_cross(W.n, W.w, W.u, W.t0, W.t1);
-    d_norm2(W.s1, W.n, W.t0, W.t1);  // |w x d|^2
-    d_norm2(W.t2, W.u, W.t0, W.t1);  // |d|^2
-    d_div(W.s0, W.s1, W.t2, W.t0);
-}
-// plane / line form: h^2 / |n|^2 with n = (q1 - q0) x (r1 - r0), h = (o - base) . n
-__device__ void hn_d2(DualWork& W, const double* x, int q0, int q1, int r0, int r1, int o, int base) {
-    d_vdiff(W.u, x, q1, q0);
-    d_vdiff(W.w, x, r1, r0);
-    d_cross(W.n, W.u, W.w, W.t0, W.t1);
-    d_vdiff(W.u, x, o, base);
-    d_dot(W.s1, W.u, W.n, W.t0, W.t1);  // h
-    d_mul(W.t2, W.s1, W.s1);            // h h
-    d_norm2(W.s1, W.n, W.t0, W.t1);     // |n|^2
-    d_div(W.s0, W.t2, W.s1, W.t0);
-}
+constexpr int kContactThreads = 128;
 
 // ---- plain-double classification and value paths (distance.hpp:13-155) ----
 struct V3 {
@@ -212,37 +183,6 @@ __device__ double feature_dist2(int kind, const V3* x, int* region) {
     }
 }
 // the same feature's squared distance with derivatives (result in W.s0)
-__device__ void feature_dist2_derivs(int kind, int region, const V3* xv, DualWork& W) {
-    double x[12];
-    for (int a = 0; a < 4; ++a) {
-        x[3 * a] = xv[a].x;
-        x[3 * a + 1] = xv[a].y;
-        x[3 * a + 2] = xv[a].z;
-    }
-    if (kind == 0) {
-        switch (region) {
-            case 0: pp_d2(W, x, 0, 1); break;
-            case 1: pp_d2(W, x, 0, 2); break;
-            case 2: pp_d2(W, x, 0, 3); break;
-            case 3: pe_d2(W, x, 0, 1, 2); break;
-            case 4: pe_d2(W, x, 0, 2, 3); break;
-            case 5: pe_d2(W, x, 0, 3, 1); break;
-            default: hn_d2(W, x, 1, 2, 1, 3, 0, 1); break;
-        }
-        return;
-    }
-    switch (region) {
-        case 0: pp_d2(W, x, 0, 2); break;
-        case 1: pp_d2(W, x, 0, 3); break;
-        case 2: pp_d2(W, x, 1, 2); break;
-        case 3: pp_d2(W, x, 1, 3); break;
-        case 4: pe_d2(W, x, 0, 2, 3); break;
-        case 5: pe_d2(W, x, 1, 2, 3); break;
-        case 6: pe_d2(W, x, 2, 0, 1); break;
-        case 7: pe_d2(W, x, 3, 0, 1); break;
-        default: hn_d2(W, x, 0, 1, 2, 3, 2, 0); break;
-    }
-}
 // the closest-point value path of pt_dist2 / ee_dist2 (ccd, line-search value)
 __device__ double closest_dist2(int kind, const V3* x) {
     if (kind == 0) {
@@ -338,32 +278,51 @@ __global__ void k_contact_active(ContactArgs a, std::int32_t* __restrict__ pair_
     }
 }
 
-// pass 2: active pairs -> 10 blocks at 10 * rank, node gradient, value
-__global__ void __launch_bounds__(kContactThreads) k_contact_pairs(ContactArgs a, const std::int32_t* __restrict__ on,
-                                                                   const std::int64_t* __restrict__ rank,
+// active pair indices in emission order (list[rank[i]] = i)
+__global__ void k_active_list(const std::int32_t* __restrict__ on, const std::int64_t* __restrict__ rank,
+                              std::int64_t n, std::int64_t* __restrict__ list) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        if (on[i]) list[rank[i]] = i;
+}
+
+// pass 2: one thread per active pair -> 10 blocks at 10 * rank, node
+// gradient, value. The feature's derivatives in closed form over its
+// difference vectors (dist_derivs.cuh); barrier chain rule there, then the
+// 12 x 12 (S^T (b2 g g^T + b1 Hf) S) and its projection in the 9-dimensional
+// complement of the translations
+__global__ void __launch_bounds__(kContactThreads) k_contact_pairs(ContactArgs a, const std::int64_t* __restrict__ list,
+                                                                   std::int64_t n_active,
                                                                    std::uint64_t* __restrict__ keys,
                                                                    double* __restrict__ vals,
                                                                    double* __restrict__ node_grad,
-                                                                   double* __restrict__ value, DualWork* __restrict__ work) {
+                                                                   double* __restrict__ value) {
     const double shat = a.dhat * a.dhat;
-    const std::int64_t np = a.n_pt + a.n_ee;
-    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-    DualWork& W = work[tid];
     double e = 0;
-    for (std::int64_t i = tid; i < np; i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        if (!on[i]) continue;
+    for (std::int64_t j = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; j < n_active;
+         j += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t i = list[j];
         int kind, region;
         const int* st = stencil_of(a, i, &kind);
-        V3 x[4];
-        load_stencil(a.pos, st, x);
-        feature_dist2(kind, x, &region);
-        feature_dist2_derivs(kind, region, x, W);
-        const D12& d = W.s0;
-        const double b1 = barrier_d1(d.v, shat, a.kappa), b2 = barrier_d2(d.v, shat, a.kappa);
-        e += barrier_value(d.v, shat, a.kappa);
-        double H[144];
-        for (int j = 0; j < 12; ++j)
-            for (int i2 = 0; i2 < 12; ++i2) H[12 * j + i2] = b2 * (d.g[i2] * d.g[j]) + b1 * d.h[hp(i2, j)];
+        V3 xv[4];
+        load_stencil(a.pos, st, xv);
+        feature_dist2(kind, xv, &region);
+        double x[12];
+        for (int n = 0; n < 4; ++n) {
+            x[3 * n] = xv[n].x;
+            x[3 * n + 1] = xv[n].y;
+            x[3 * n + 2] = xv[n].z;
+        }
+        FeatDerivs f;
+        feature_derivs(kind, region, x, f);
+        const double b1 = barrier_d1(f.v, shat, a.kappa), b2 = barrier_d2(f.v, shat, a.kappa);
+        e += barrier_value(f.v, shat, a.kappa);
+        const int m = 3 * f.nvec;
+        for (int c = 0; c < m; ++c)
+            for (int r = 0; r < m; ++r) f.H[9 * c + r] = b2 * (f.g[r] * f.g[c]) + b1 * f.H[9 * c + r];
+        double H[144], g[12];
+        feat_lift(f, f.H, H);
+        feat_grad12(f, g);
         if (a.project) {
             double M[81];
             reduce_translation(H, M);
@@ -374,8 +333,8 @@ __global__ void __launch_bounds__(kContactThreads) k_contact_pairs(ContactArgs a
         }
         for (int n = 0; n < 4; ++n)
             for (int k = 0; k < 3; ++k)
-                red_add_f64(node_grad + 3 * static_cast<std::int64_t>(st[n]) + k, a.dt2 * (b1 * d.g[3 * n + k]));
-        const std::int64_t base = 10 * rank[i];
+                red_add_f64(node_grad + 3 * static_cast<std::int64_t>(st[n]) + k, a.dt2 * (b1 * g[3 * n + k]));
+        const std::int64_t base = 10 * j;
         int q = 0;
         for (int p0 = 0; p0 < 4; ++p0)
             for (int p1 = p0; p1 < 4; ++p1, ++q) {
@@ -659,10 +618,12 @@ std::int64_t contact_emit(Ctx& c, const ContactDesc& d, double dt2, int project,
     const std::int64_t T = 10 * h[0] + h[1] + h[2];
     if (T > capacity) throw StatusError(kInvalidArgument, "contact stream capacity too small");
     if (h[0] > 0) {
-        const int grid = static_cast<int>(std::min<std::int64_t>(ceil_div(np, kContactThreads), kSMs * 2));
-        c.ct_work.reserve(static_cast<std::size_t>(grid) * kContactThreads * sizeof(DualWork));
-        k_contact_pairs<<<grid, kContactThreads, 0, st>>>(a, pair_on, pair_rank, d_keys, d_vals, d_node_grad, d_value,
-                                                         reinterpret_cast<DualWork*>(c.ct_work.p));
+        c.ct_work.reserve(static_cast<std::size_t>(h[0]) * sizeof(std::int64_t));
+        std::int64_t* list = reinterpret_cast<std::int64_t*>(c.ct_work.p);
+        k_active_list<<<grid_for(np, 256, 16), 256, 0, st>>>(pair_on, pair_rank, np, list);
+        ADIPC_LAUNCH_CHECK();
+        k_contact_pairs<<<grid_for(h[0], kContactThreads, 8), kContactThreads, 0, st>>>(a, list, h[0], d_keys, d_vals,
+                                                                                        d_node_grad, d_value);
         ADIPC_LAUNCH_CHECK();
     }
     if (h[1] > 0) {

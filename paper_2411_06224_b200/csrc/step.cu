@@ -75,7 +75,45 @@ __global__ void k_node_displacements(const double* __restrict__ d, std::int32_t 
     }
 }
 
+// assemble_contact's gradient lift (incremental_potential.hpp:395-403): a FEM
+// node's contact gradient adds to its slot, an affine-body node's through
+// J^T to its body's 12 dofs (fp64 RED); pinned slots receive nothing (the
+// reference zeroes them right after, :253-254)
+__global__ void k_lift_node_grad(const double* __restrict__ g, std::int32_t n_fem, std::int32_t n_abd,
+                                 const std::int32_t* __restrict__ abd_body, const double* __restrict__ jac36,
+                                 const std::uint8_t* __restrict__ pinned, double* __restrict__ grad) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+         i < static_cast<std::int64_t>(n_fem) + n_abd; i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const double g0 = g[3 * i], g1 = g[3 * i + 1], g2 = g[3 * i + 2];
+        if (g0 * g0 + g1 * g1 + g2 * g2 == 0) continue;
+        if (i < n_fem) {
+            if (pinned && pinned[i]) continue;
+            atomicAdd(grad + 3 * i, g0);
+            atomicAdd(grad + 3 * i + 1, g1);
+            atomicAdd(grad + 3 * i + 2, g2);
+        } else {
+            const std::int64_t a = i - n_fem;
+            const double* J = jac36 + 36 * a;
+            const std::int64_t base = static_cast<std::int64_t>(n_fem) + 4 * static_cast<std::int64_t>(abd_body[a]);
+            double* q = grad + 3 * base;
+            for (int c = 0; c < 12; ++c)
+                if (!pinned || !pinned[base + c / 3])
+                    atomicAdd(q + c, J[3 * c] * g0 + J[3 * c + 1] * g1 + J[3 * c + 2] * g2);
+        }
+    }
+}
+
 }  // namespace
+
+void lift_node_grad(Ctx& c, const double* d_node_grad, std::int32_t n_fem, std::int32_t n_abd,
+                    const std::int32_t* d_abd_body, const double* d_jac36, const std::uint8_t* d_pinned,
+                    double* d_grad) {
+    const std::int64_t n = static_cast<std::int64_t>(n_fem) + n_abd;
+    if (n <= 0) return;
+    k_lift_node_grad<<<grid_for(n, 256, 16), 256, 0, c.stream>>>(d_node_grad, n_fem, n_abd, d_abd_body, d_jac36,
+                                                                d_pinned, d_grad);
+    ADIPC_LAUNCH_CHECK();
+}
 
 double step_inf_norm(Ctx& c, const double* d_dir, std::int32_t n_fem, std::int32_t n_bodies,
                      const double* d_max_xbar) {

@@ -63,24 +63,28 @@ __device__ __forceinline__ bool shifted_cholesky_ok(double* L, double tau) {
 }
 
 // proj(M) for a symmetric N x N (full column-major in `a`, overwritten):
-// cyclic Jacobi (oracle/sym_eig.hpp's rotations), then V max(w, 0) V^T
+// cyclic Jacobi (oracle/sym_eig.hpp's rotations) with the threshold rule — an
+// off-diagonal entry below 1e-17 of the Frobenius norm (rounding level) is
+// zeroed instead of rotated and the sweeps end once one rotates nothing —
+// then V max(w, 0) V^T
 template <int N>
 __device__ __noinline__ void project_sym(double* a) {
     double v[N * N];
     for (int k = 0; k < N * N; ++k) v[k] = (k % (N + 1) == 0) ? 1.0 : 0.0;
+    double tot = 0;  // ||a||_F^2, invariant under the rotations
+    for (int k = 0; k < N * N; ++k) tot += a[k] * a[k];
+    const double negligible = 1e-34 * tot;
     for (int sweep = 0; sweep < 64; ++sweep) {
-        double off = 0, tot = 0;
-        for (int j = 0; j < N; ++j)
-            for (int i = 0; i < N; ++i) {
-                const double x = a[N * j + i] * a[N * j + i];
-                tot += x;
-                if (i != j) off += x;
-            }
-        if (off <= 1e-32 * tot) break;
+        bool rotated = false;
         for (int p = 0; p < N - 1; ++p)
             for (int q = p + 1; q < N; ++q) {
                 const double apq = a[N * q + p];
                 if (apq == 0.0) continue;
+                if (apq * apq <= negligible) {
+                    a[N * q + p] = a[N * p + q] = 0.0;
+                    continue;
+                }
+                rotated = true;
                 const double theta = (a[N * q + q] - a[N * p + p]) / (2.0 * apq);
                 const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
                 const double c = rsqrt(t * t + 1.0), s = t * c;
@@ -100,6 +104,7 @@ __device__ __noinline__ void project_sym(double* a) {
                     v[N * q + k] = s * kp + c * kq;
                 }
             }
+        if (!rotated) break;
     }
     double w[N];
     for (int k = 0; k < N; ++k) w[k] = a[(N + 1) * k] > 0 ? a[(N + 1) * k] : 0.0;

@@ -105,8 +105,10 @@ def test_ccd_step_matches_oracle(ctx, scene):
 
 def test_newton_linear_solve_matches_oracle(ctx, scene):
     """One Newton iteration's linear solve: device assemble -> cold MAS ->
-    PCG on -grad, against the oracle's assemble -> Hierarchy + MAS -> PCG
-    (iterations within 2 %, direction within 1e-5)."""
+    PCG on -grad, against the oracle's assemble -> Hierarchy + MAS -> PCG:
+    iterations within 2 % at the bench tolerance (1e-4), and the direction
+    within 1e-6 when both solve to 1e-10 (at 1e-4 the two stopping points
+    differ by the contact-stiff system's conditioning times the tolerance)."""
     g = scene
     ip, t = device_potential(ctx, g)
     state = g.state()
@@ -123,4 +125,7 @@ def test_newton_linear_solve_matches_oracle(ctx, scene):
     xo, ro = O.pcg_solve(A, -og, O.MasPreconditioner(A, H), 1e-4, 250, 100000, DET)
     assert res.converged and ro["converged"]
     assert abs(res.iters - ro["iters"]) <= max(1, 0.02 * ro["iters"])
-    assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-5 * np.linalg.norm(xo)
+    _, res = ctx.pcg(b, 1e-10, 250, 100000, x=x)
+    xo, ro = O.pcg_solve(A, -og, O.MasPreconditioner(A, H), 1e-10, 250, 100000, DET)
+    assert res.converged and ro["converged"]
+    assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-6 * np.linalg.norm(xo)

@@ -288,9 +288,11 @@ __global__ void k_active_list(const std::int32_t* __restrict__ on, const std::in
 
 // pass 2: one thread per active pair -> 10 blocks at 10 * rank, node
 // gradient, value. The feature's derivatives in closed form over its
-// difference vectors (dist_derivs.cuh); barrier chain rule there, then the
-// 12 x 12 (S^T (b2 g g^T + b1 Hf) S) and its projection in the 9-dimensional
-// complement of the translations
+// difference vectors (dist_derivs.cuh) and the barrier chain rule there
+// (Hf = b2 g g^T + b1 d2(dist2)); the PSD test / projection on the reduction
+// to the 9-dimensional complement of the translations (the 12 x 12 S^T Hf S
+// is never formed), the blocks emitted from Hf (already PSD) or from the
+// projected reduction
 __global__ void __launch_bounds__(kContactThreads) k_contact_pairs(ContactArgs a, const std::int64_t* __restrict__ list,
                                                                    std::int64_t n_active,
                                                                    std::uint64_t* __restrict__ keys,
@@ -320,27 +322,61 @@ __global__ void __launch_bounds__(kContactThreads) k_contact_pairs(ContactArgs a
         const int m = 3 * f.nvec;
         for (int c = 0; c < m; ++c)
             for (int r = 0; r < m; ++r) f.H[9 * c + r] = b2 * (f.g[r] * f.g[c]) + b1 * f.H[9 * c + r];
-        double H[144], g[12];
-        feat_lift(f, f.H, H);
-        feat_grad12(f, g);
+        // node coefficients of the feature vectors, and R = S (Q (x) I3):
+        // the 9-dimensional translation complement straight from the
+        // feature space (M = R^T Hf R, no 12 x 12)
+        double C[4][3], R[3][3];
+        for (int n = 0; n < 4; ++n)
+            for (int p = 0; p < 3; ++p) C[n][p] = p < f.nvec ? feat_coef(f, p, n) : 0.0;
+        for (int p = 0; p < 3; ++p)
+            for (int j = 0; j < 3; ++j) {
+                double r = 0;
+                for (int n = 0; n < 4; ++n) r += C[n][p] * helmert(n, j);
+                R[p][j] = r;
+            }
+        for (int n = 0; n < 4; ++n)
+            for (int k = 0; k < 3; ++k) {
+                double gk = 0;
+                for (int p = 0; p < f.nvec; ++p) gk += C[n][p] * f.g[3 * p + k];
+                red_add_f64(node_grad + 3 * static_cast<std::int64_t>(st[n]) + k, a.dt2 * (b1 * gk));
+            }
+        bool projected = false;
+        double M[81];
         if (a.project) {
-            double M[81];
-            reduce_translation(H, M);
+            for (int l = 0; l < 3; ++l)
+                for (int c = 0; c < 3; ++c)
+                    for (int j = 0; j < 3; ++j)
+                        for (int r = 0; r < 3; ++r) {
+                            double sum = 0;
+                            for (int q = 0; q < f.nvec; ++q)
+                                for (int p = 0; p < f.nvec; ++p)
+                                    sum += R[p][j] * R[q][l] * f.H[9 * (3 * q + c) + 3 * p + r];
+                            M[9 * (3 * l + c) + 3 * j + r] = sum;
+                        }
             if (!psd9(M)) {
                 project9(M);
-                lift_translation(M, H);
+                projected = true;
             }
         }
-        for (int n = 0; n < 4; ++n)
-            for (int k = 0; k < 3; ++k)
-                red_add_f64(node_grad + 3 * static_cast<std::int64_t>(st[n]) + k, a.dt2 * (b1 * g[3 * n + k]));
         const std::int64_t base = 10 * j;
         int q = 0;
         for (int p0 = 0; p0 < 4; ++p0)
             for (int p1 = p0; p1 < 4; ++p1, ++q) {
                 double blk[9];
                 for (int c = 0; c < 3; ++c)
-                    for (int r = 0; r < 3; ++r) blk[3 * c + r] = a.dt2 * H[12 * (3 * p1 + c) + 3 * p0 + r];
+                    for (int r = 0; r < 3; ++r) {
+                        double sum = 0;
+                        if (projected) {  // (Q (x) I3) proj(M) (Q (x) I3)^T, block (p0, p1)
+                            for (int l = 0; l < 3; ++l)
+                                for (int jj = 0; jj < 3; ++jj)
+                                    sum += helmert(p0, jj) * helmert(p1, l) * M[9 * (3 * l + c) + 3 * jj + r];
+                        } else {  // S^T Hf S, block (p0, p1)
+                            for (int qq = 0; qq < f.nvec; ++qq)
+                                for (int p = 0; p < f.nvec; ++p)
+                                    sum += C[p0][p] * C[p1][qq] * f.H[9 * (3 * qq + c) + 3 * p + r];
+                        }
+                        blk[3 * c + r] = a.dt2 * sum;
+                    }
                 emit_block(keys, vals, base + q, st[p0], st[p1], blk);
             }
     }

@@ -71,19 +71,6 @@ ADIPC_HD void mtm(const double* A, const double* B, double* C) {
         for (int j = 0; j < 3; ++j) C[3 * i + j] = A[i] * B[j] + A[3 + i] * B[3 + j] + A[6 + i] * B[6 + j];
 }
 
-// f = a / b with the derivatives of a and b over m = 3 nvec features
-ADIPC_HD void quotient(int m, double a, const double* ga, const double* Ha, double b, const double* gb,
-                       const double* Hb, FeatDerivs& out) {
-    const double ib = 1.0 / b, ib2 = ib * ib, ib3 = ib2 * ib;
-    for (int i = 0; i < m; ++i) out.g[i] = ga[i] * ib - a * gb[i] * ib2;
-    for (int j = 0; j < m; ++j)
-        for (int i = 0; i < m; ++i) {
-            const int k = 9 * j + i;
-            out.H[k] = Ha[k] * ib - (ga[i] * gb[j] + gb[i] * ga[j]) * ib2 - a * Hb[k] * ib2 +
-                       2.0 * a * gb[i] * gb[j] * ib3;
-        }
-}
-
 }  // namespace fd
 
 // |x_a - x_b|^2 (distance.hpp:111-114)
@@ -120,26 +107,30 @@ ADIPC_HD void feat_pe(const double* x, int p, int e0, int e1, FeatDerivs& f) {
     fd::skew(d, Kd);
     fd::skew(w, Kw);
     fd::skew(n, Kn);
-    double gA[9], HA[81], gB[9], HB[81];
-    for (int k = 0; k < 81; ++k) HA[k] = HB[k] = 0;
-    double t[3];
+    // f = A / B, B = |d|^2 (dB/dd = 2 d, d2B/dd2 = 2 I): the quotient rule
+    // accumulated straight into f (no Hessian temporaries)
+    double gA[6], gB[6], t[3];
     fd::cross(d, n, t);  // dA/dw = 2 d x n
     for (int k = 0; k < 3; ++k) gA[k] = 2 * t[k];
     fd::cross(n, w, t);  // dA/dd = 2 n x w
     for (int k = 0; k < 3; ++k) gA[3 + k] = 2 * t[k];
-    fd::mtm(Kd, Kd, M);  // d2A/dw2 = 2 [d]x^T [d]x
-    fd::add_block(HA, 0, 0, M, 2);
-    fd::mtm(Kw, Kw, M);  // d2A/dd2 = 2 [w]x^T [w]x
-    fd::add_block(HA, 1, 1, M, 2);
-    fd::mtm(Kd, Kw, M);  // d2A/dw dd = -2 [d]x^T [w]x - 2 [n]x
-    for (int k = 0; k < 9; ++k) M[k] = -M[k] - Kn[k];
-    fd::add_sym_pair(HA, 0, 1, M, 2);
     for (int k = 0; k < 3; ++k) {
         gB[k] = 0;
         gB[3 + k] = 2 * d[k];
-        HB[9 * (3 + k) + 3 + k] = 2;
     }
-    fd::quotient(6, A, gA, HA, B, gB, HB, f);
+    const double ib = 1.0 / B, ib2 = ib * ib, ib3 = ib2 * ib;
+    for (int i = 0; i < 6; ++i) f.g[i] = gA[i] * ib - A * gB[i] * ib2;
+    for (int j = 0; j < 6; ++j)
+        for (int i = 0; i < 6; ++i)
+            f.H[9 * j + i] = -(gA[i] * gB[j] + gB[i] * gA[j]) * ib2 + 2.0 * A * gB[i] * gB[j] * ib3;
+    fd::mtm(Kd, Kd, M);  // d2A/dw2 = 2 [d]x^T [d]x
+    fd::add_block(f.H, 0, 0, M, 2 * ib);
+    fd::mtm(Kw, Kw, M);  // d2A/dd2 = 2 [w]x^T [w]x
+    fd::add_block(f.H, 1, 1, M, 2 * ib);
+    fd::mtm(Kd, Kw, M);  // d2A/dw dd = -2 [d]x^T [w]x - 2 [n]x
+    for (int k = 0; k < 9; ++k) M[k] = -M[k] - Kn[k];
+    fd::add_sym_pair(f.H, 0, 1, M, 2 * ib);
+    for (int k = 0; k < 3; ++k) f.H[9 * (3 + k) + 3 + k] -= 2 * A * ib2;  // - A d2B/dd2 / B^2
     f.v = A * (1.0 / B);  // the duals divide as a * (1 / b)
 }
 
@@ -162,7 +153,7 @@ ADIPC_HD void feat_hn(const double* x, int q0, int q1, int r0, int r1, int o, in
     const double h = fd::dot(c, n);
     const double a = h * h;
     const double N = (n[0] * n[0] + n[1] * n[1]) + n[2] * n[2];
-    double Ku[9], Kw[9], Kc[9], Kn[9], M[9], t[3];
+    double Ku[9], Kw[9], Kc[9], Kn[9], M[9], t[3];  // [.]x matrices, row-major
     fd::skew(u, Ku);
     fd::skew(w, Kw);
     fd::skew(c, Kc);
@@ -175,31 +166,37 @@ ADIPC_HD void feat_hn(const double* x, int q0, int q1, int r0, int r1, int o, in
     fd::cross(c, u, t);
     for (int k = 0; k < 3; ++k) gh[3 + k] = t[k];
     for (int k = 0; k < 3; ++k) gh[6 + k] = n[k];
-    double ga[9], Ha[81], gN[9], HN[81];
-    for (int k = 0; k < 81; ++k) Ha[k] = HN[k] = 0;
-    for (int k = 0; k < 9; ++k) ga[k] = 2 * h * gh[k];
-    for (int j = 0; j < 9; ++j)
-        for (int i = 0; i < 9; ++i) Ha[9 * j + i] = 2 * gh[i] * gh[j];
-    for (int k = 0; k < 9; ++k) M[k] = -Kc[k];
-    fd::add_sym_pair(Ha, 0, 1, M, 2 * h);
-    for (int k = 0; k < 9; ++k) M[k] = -Kw[k];
-    fd::add_sym_pair(Ha, 2, 0, M, 2 * h);
-    fd::add_sym_pair(Ha, 2, 1, Ku, 2 * h);
-    // N = |u x w|^2: dN/du = 2 w x n, dN/dw = 2 n x u;
-    // d2N/du2 = 2 [w]x^T [w]x, d2N/dw2 = 2 [u]x^T [u]x, d2N/du dw = -2 [w]x^T [u]x - 2 [n]x
+    // N = |u x w|^2: dN/du = 2 w x n, dN/dw = 2 n x u
+    double gN[9];
     fd::cross(w, n, t);
     for (int k = 0; k < 3; ++k) gN[k] = 2 * t[k];
     fd::cross(n, u, t);
     for (int k = 0; k < 3; ++k) gN[3 + k] = 2 * t[k];
     for (int k = 0; k < 3; ++k) gN[6 + k] = 0;
+    // f = a / N with a = h^2 (da = 2 h dh, d2a = 2 dh dh^T + 2 h d2h): the
+    // quotient rule accumulated straight into f
+    const double ib = 1.0 / N, ib2 = ib * ib, ib3 = ib2 * ib;
+    for (int i = 0; i < 9; ++i) f.g[i] = 2 * h * gh[i] * ib - a * gN[i] * ib2;
+    for (int j = 0; j < 9; ++j)
+        for (int i = 0; i < 9; ++i)
+            f.H[9 * j + i] = 2 * gh[i] * gh[j] * ib - (2 * h * gh[i] * gN[j] + gN[i] * 2 * h * gh[j]) * ib2 +
+                             2.0 * a * gN[i] * gN[j] * ib3;
+    // 2 h d2h / N: d2h/du dw = -[c]x, d2h/dc du = -[w]x, d2h/dc dw = [u]x
+    for (int k = 0; k < 9; ++k) M[k] = -Kc[k];
+    fd::add_sym_pair(f.H, 0, 1, M, 2 * h * ib);
+    for (int k = 0; k < 9; ++k) M[k] = -Kw[k];
+    fd::add_sym_pair(f.H, 2, 0, M, 2 * h * ib);
+    fd::add_sym_pair(f.H, 2, 1, Ku, 2 * h * ib);
+    // - a d2N / N^2: d2N/du2 = 2 [w]x^T [w]x, d2N/dw2 = 2 [u]x^T [u]x,
+    // d2N/du dw = -2 [w]x^T [u]x - 2 [n]x
+    const double sN = -2 * a * ib2;
     fd::mtm(Kw, Kw, M);
-    fd::add_block(HN, 0, 0, M, 2);
+    fd::add_block(f.H, 0, 0, M, sN);
     fd::mtm(Ku, Ku, M);
-    fd::add_block(HN, 1, 1, M, 2);
+    fd::add_block(f.H, 1, 1, M, sN);
     fd::mtm(Kw, Ku, M);
     for (int k = 0; k < 9; ++k) M[k] = -M[k] - Kn[k];
-    fd::add_sym_pair(HN, 0, 1, M, 2);
-    fd::quotient(9, a, ga, Ha, N, gN, HN, f);
+    fd::add_sym_pair(f.H, 0, 1, M, sN);
     f.v = a * (1.0 / N);
 }
 

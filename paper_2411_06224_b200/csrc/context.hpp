@@ -197,6 +197,11 @@ struct Ctx {
     bool perm_active = false;      // the current preconditioner / solve matrix use `perm`
     bool levels_permuted = false;  // the device levels were built in solve order
     std::uint64_t levels_version = 0;  // bumped whenever the device levels are rebuilt
+    // level 0 in solve order depends on the level-0 partition alone (fixed per
+    // scene): built once per l0_version and kept across cold rebuilds, with
+    // the host copies the coarse levels are linked against
+    std::uint64_t l0_levels_version = ~0ull;
+    std::vector<std::int32_t> perm_host, l0_solve_part_of;
     // byte-balanced work splits of the preconditioner kernels (solve_order.cu)
     struct Split {
         int np = 0;

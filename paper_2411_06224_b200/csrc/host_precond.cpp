@@ -121,8 +121,14 @@ Partition partition_block_graph(Index v, const Graph& g, Index capacity) {
         comp_ptr.push_back(static_cast<std::int64_t>(order.size()));
     }
     std::vector<char> assigned(v, 0);
-    std::vector<Index> conn(v, 0);
-    std::vector<Index> cand, touched;
+    // the carving frontier: unassigned neighbours of the open cluster as
+    // packed keys (connections << 32 | ~id), so the pick — most connections,
+    // ties to the lowest id — is one max over a short contiguous array;
+    // where[] locates a node's key for the increments (-1: not a candidate)
+    std::vector<std::int32_t> where(v, -1);
+    std::vector<std::uint64_t> cand;
+    constexpr std::uint64_t kOne = 1ull << 32;
+    auto key_id = [](std::uint64_t k) { return static_cast<Index>(~static_cast<std::uint32_t>(k)); };
     Index next_part = 0, open_part = kInvalid, open_fill = 0;
     const std::size_t n_comps = comp_ptr.size() - 1;
     for (std::size_t ci = 0; ci < n_comps; ++ci) {
@@ -146,8 +152,6 @@ Partition partition_block_graph(Index v, const Graph& g, Index capacity) {
             while (assigned[comp[seed_at]]) ++seed_at;
             Index pick = comp[seed_at];
             const Index part = next_part++;
-            cand.clear();
-            touched.clear();
             for (Index fill = 0; pick != kInvalid;) {
                 p.part_of[pick] = part;
                 assigned[pick] = 1;
@@ -156,31 +160,33 @@ Partition partition_block_graph(Index v, const Graph& g, Index capacity) {
                 if (fill == target || left == 0) break;
                 for (std::int64_t k = g.ptr[pick]; k < g.ptr[pick + 1]; ++k) {
                     const Index nb = g.adj[k];
-                    if (!assigned[nb]) {
-                        if (conn[nb] == 0) {
-                            cand.push_back(nb);
-                            touched.push_back(nb);
-                        }
-                        ++conn[nb];
+                    if (assigned[nb]) continue;
+                    if (where[nb] < 0) {
+                        where[nb] = static_cast<std::int32_t>(cand.size());
+                        cand.push_back(kOne | static_cast<std::uint32_t>(~static_cast<std::uint32_t>(nb)));
+                    } else {
+                        cand[where[nb]] += kOne;
                     }
                 }
-                // argmax conn, ties -> lowest id (order independent), so
-                // assigned candidates can be compacted away as we scan.
-                pick = kInvalid;
-                Index best = 0;
-                std::size_t w = 0;
-                for (std::size_t k = 0; k < cand.size(); ++k) {
-                    const Index c = cand[k];
-                    if (assigned[c]) continue;
-                    cand[w++] = c;
-                    if (pick == kInvalid || conn[c] > best || (conn[c] == best && c < pick)) {
-                        pick = c;
-                        best = conn[c];
-                    }
+                if (cand.empty()) {
+                    pick = kInvalid;
+                    break;
                 }
-                cand.resize(w);
+                std::size_t at = 0;
+                std::uint64_t best = cand[0];
+                for (std::size_t k = 1; k < cand.size(); ++k)
+                    if (cand[k] > best) {
+                        best = cand[k];
+                        at = k;
+                    }
+                pick = key_id(best);
+                where[pick] = -1;
+                cand[at] = cand.back();
+                cand.pop_back();
+                if (at < cand.size()) where[key_id(cand[at])] = static_cast<std::int32_t>(at);
             }
-            for (Index t : touched) conn[t] = 0;
+            for (std::uint64_t k : cand) where[key_id(k)] = -1;
+            cand.clear();
         }
     }
     p.n_parts = next_part;

@@ -36,7 +36,7 @@ struct RestrictLevel {
     double* dense;
 };
 struct RestrictArgs {
-    int n_levels;
+    int first, n_levels;  // levels [first, n_levels)
     RestrictLevel lv[kMaxLevels];
 };
 
@@ -74,7 +74,7 @@ __global__ void k_restrict(const std::uint32_t* __restrict__ rows, const std::ui
         double h[9];
 #pragma unroll
         for (int k = 0; k < 9; ++k) h[k] = blocks[blk(e, k)];
-        for (int l = 0; l < ra.n_levels; ++l) {
+        for (int l = ra.first; l < ra.n_levels; ++l) {
             const RestrictLevel& L = ra.lv[l];
             const std::int32_t nr = L.agg ? L.agg[r] : r;
             const std::int32_t nc = L.agg ? L.agg[c] : c;
@@ -687,6 +687,7 @@ void set_levels(Ctx& c, const host::MasHierarchy& h) {
     const std::size_t n_lv = static_cast<std::size_t>(h.n_levels());
     if (c.levels.size() > n_lv) c.levels.resize(n_lv);
     while (c.levels.size() < n_lv) c.levels.emplace_back(new DeviceLevel());
+    c.l0_levels_version = ~0ull;  // level 0 rebuilt from h: the per-scene cache no longer holds
     lap("levels");
     const bool perm = c.solve_order && h.n_levels() > 0 && h.n_slots > 0;
     const host::MasHierarchy hp = perm ? to_solve_order(c, h) : host::MasHierarchy{};
@@ -699,6 +700,64 @@ void set_levels(Ctx& c, const host::MasHierarchy& h) {
     link_levels(c, hl);
     lap("link_levels");
     c.levels_permuted = perm;
+    ++c.levels_version;
+}
+
+// Level 0 in solve order from the level-0 partition alone (per scene): the
+// slot permutation, its device copy and the level-0 metadata, kept across
+// cold rebuilds until the partition, the size or the mode changes.
+void ensure_level0(Ctx& c) {
+    const std::int32_t n = static_cast<std::int32_t>(c.l0.part_of.size());
+    if (c.l0_levels_version == c.l0_version && !c.levels.empty() && c.levels[0]->n_nodes == n &&
+        static_cast<std::int32_t>(c.perm_host.size()) == n)
+        return;
+    const host::Partition& l0 = c.l0;
+    std::vector<std::int32_t> start(static_cast<std::size_t>(l0.n_parts) + 1, 0);
+    c.perm_host.resize(n);
+    for (std::int32_t i = 0; i < n; ++i) ++start[l0.part_of[i] + 1];
+    for (std::int32_t s = 0; s < l0.n_parts; ++s) start[s + 1] += start[s];
+    for (std::int32_t i = 0; i < n; ++i) c.perm_host[i] = start[l0.part_of[i]]++;
+    upload(c.perm, c.perm_host, c.stream);
+    host::Level lv;
+    lv.n_nodes = n;
+    lv.n_parts = l0.n_parts;
+    lv.part_of.resize(n);
+    for (std::int32_t i = 0; i < n; ++i) lv.part_of[c.perm_host[i]] = l0.part_of[i];
+    if (c.levels.empty()) c.levels.emplace_back(new DeviceLevel());
+    build_level(c, *c.levels[0], lv, 0, n);
+    c.l0_solve_part_of = std::move(lv.part_of);
+    c.l0_levels_version = c.l0_version;
+    ++c.levels_version;
+}
+
+// The coarse levels (>= 1) of hierarchy h in solve order on top of the
+// cached level 0, and the restriction links of every level.
+void set_coarse_levels(Ctx& c, const host::MasHierarchy& h) {
+    const std::int32_t n = h.n_slots;
+    const std::size_t n_lv = static_cast<std::size_t>(h.n_levels());
+    if (c.levels.size() > std::max<std::size_t>(n_lv, 1)) c.levels.resize(std::max<std::size_t>(n_lv, 1));
+    while (c.levels.size() < n_lv) c.levels.emplace_back(new DeviceLevel());
+    host::MasHierarchy hp;
+    hp.capacity = h.capacity;
+    hp.n_slots = n;
+    hp.levels.resize(n_lv);
+    hp.levels[0].n_nodes = n;
+    hp.levels[0].n_parts = h.levels[0].n_parts;
+    hp.levels[0].part_of.swap(c.l0_solve_part_of);  // lent to link_levels, returned below
+    for (std::size_t l = 1; l < n_lv; ++l) {
+        hp.levels[l].n_nodes = h.levels[l].n_nodes;
+        hp.levels[l].n_parts = h.levels[l].n_parts;
+        hp.levels[l].part_of = h.levels[l].part_of;
+        std::vector<std::int32_t>& agg = hp.levels[l].agg;
+        agg.resize(n);
+        const std::vector<std::int32_t>& src = h.levels[l].agg;
+#pragma omp parallel for schedule(static)
+        for (std::int32_t i = 0; i < n; ++i) agg[c.perm_host[i]] = src[i];
+        build_level(c, *c.levels[l], hp.levels[l], static_cast<int>(l), n);
+    }
+    link_levels(c, hp);
+    hp.levels[0].part_of.swap(c.l0_solve_part_of);
+    c.levels_permuted = true;
     ++c.levels_version;
 }
 
@@ -788,13 +847,26 @@ void check_solve_matrix(Ctx& c) {
     if (c.pkind == kMas && c.perm_active && c.as_a_version != c.A.version) build_solve_matrix(c, false);
 }
 
-// K9 restriction + K10 batched factorisation/inversion for the current levels.
-void factorize(Ctx& c) {
+// K9 restriction + K10 batched factorisation/inversion, in three steps so a
+// cold build can factor level 0 while the host builds the coarse levels:
+// factor_begin (status counters), factor_levels over a level range,
+// factor_end (the one synchronisation: failure flag and shift count).
+static void factor_begin(Ctx& c) {
+    c.build_status.reserve(3);  // failure flag, shifts applied, work counter
+    ADIPC_CUDA(cudaMemsetAsync(c.build_status.p, 0, 3 * sizeof(int), c.stream));
+}
+
+static void factor_levels(Ctx& c, int lb, int le) {
     cudaStream_t st = c.stream;
     const DeviceMatrix& A = c.S();
+    for (int l = lb; l < le; ++l) {
+        DeviceLevel& L = *c.levels[l];
+        ADIPC_CUDA(cudaMemsetAsync(L.dense.p, 0, sizeof(double) * std::max<std::int64_t>(L.dense_doubles, 1), st));
+    }
     RestrictArgs ra{};
-    ra.n_levels = static_cast<int>(c.levels.size());
-    for (int l = 0; l < ra.n_levels; ++l) {
+    ra.first = lb;
+    ra.n_levels = le;
+    for (int l = 0; l < le; ++l) {
         DeviceLevel& L = *c.levels[l];
         ra.lv[l] = RestrictLevel{l > 0 ? L.agg.p : nullptr, L.part_of.p, L.pos_of.p, L.dense_off.p, L.sub_ptr.p,
                                  L.dense.p};
@@ -802,13 +874,12 @@ void factorize(Ctx& c) {
     // deterministic mode: the atomics-free k_restrict pass covers level 0
     // only (conflict-free: one entry per dense element); coarse levels in a
     // fixed order per subdomain (k_restrict_det)
-    const int n_all = ra.n_levels;
-    if (c.deterministic) ra.n_levels = std::min(ra.n_levels, 1);
-    if (A.U > 0) {
+    if (c.deterministic) ra.n_levels = std::min(le, 1);
+    if (A.U > 0 && ra.first < ra.n_levels) {
         k_restrict<<<grid_for(A.U, 256, 16), 256, 0, st>>>(A.rows.p, A.cols.p, A.blocks.p, A.U, ra);
         ADIPC_LAUNCH_CHECK();
     }
-    for (int l = 1; c.deterministic && l < n_all && A.U > 0; ++l) {
+    for (int l = std::max(lb, 1); c.deterministic && l < le && A.U > 0; ++l) {
         DeviceLevel& L = *c.levels[l];
         if (L.det_version != c.levels_version) {  // solve slots of each subdomain, ascending
             c.perm_keys.reserve(static_cast<std::size_t>(A.n));
@@ -827,13 +898,11 @@ void factorize(Ctx& c) {
             L.n_parts, L.det_ptr.p, L.det_slots.p, A.row_ptr.p, A.cols.p, A.blocks.p, ra.lv[l]);
         ADIPC_LAUNCH_CHECK();
     }
-    c.build_status.reserve(3);  // failure flag, shifts applied, work counter
-    ADIPC_CUDA(cudaMemsetAsync(c.build_status.p, 0, 3 * sizeof(int), st));
     // warp-per-subdomain levels (dim <= 64): one launch for all of them
     InvertTable tab{};
     int wdim = 0;
-    for (auto& Lp : c.levels) {
-        DeviceLevel& L = *Lp;
+    for (int l = lb; l < le; ++l) {
+        DeviceLevel& L = *c.levels[l];
         const int dim = 3 * L.max_fill;
         if (L.n_parts == 0 || dim > 64) continue;
         tab.lv[tab.n] = InvertLevel{L.sub_ptr.p, L.dense_off.p, L.dense.p, L.inv_off.p, L.inv.p};
@@ -842,6 +911,9 @@ void factorize(Ctx& c) {
         wdim = std::max(wdim, dim);
     }
     if (tab.n > 0) {
+        // the warps take subdomains from a work counter (build_status[2]): reset
+        // per launch, as a build may invert its levels in two launches
+        ADIPC_CUDA(cudaMemsetAsync(c.build_status.p + 2, 0, sizeof(int), st));
         const int nw = 4;
         const std::size_t wsm = sizeof(double) * nw * static_cast<std::size_t>((lpk_size(wdim) + 1) & ~1);
         int sms = kSMs;
@@ -860,8 +932,8 @@ void factorize(Ctx& c) {
             run(k_invert_warp<2>);
         ADIPC_LAUNCH_CHECK();
     }
-    for (auto& Lp : c.levels) {
-        DeviceLevel& L = *Lp;
+    for (int l = lb; l < le; ++l) {
+        DeviceLevel& L = *c.levels[l];
         if (L.n_parts == 0) continue;
         const int dim = 3 * L.max_fill;
         if (dim <= 64) continue;  // done above
@@ -877,15 +949,24 @@ void factorize(Ctx& c) {
                                               c.build_status.p + 1, in_smem ? nullptr : c.invert_scratch.p, dim);
         ADIPC_LAUNCH_CHECK();
     }
+}
+
+static void factor_end(Ctx& c) {
     int h_status[2] = {0, 0};
-    ADIPC_CUDA(cudaMemcpyAsync(h_status, c.build_status.p, sizeof(h_status), cudaMemcpyDeviceToHost, st));
-    ADIPC_CUDA(cudaStreamSynchronize(st));
+    ADIPC_CUDA(cudaMemcpyAsync(h_status, c.build_status.p, sizeof(h_status), cudaMemcpyDeviceToHost, c.stream));
+    ADIPC_CUDA(cudaStreamSynchronize(c.stream));
     c.shifts_applied = h_status[1];
     if (h_status[0]) {
         c.pkind = kNone;
         throw StatusError(kIndefinite, "subdomain matrix stayed indefinite after regularization");
     }
     c.pkind = kMas;
+}
+
+void factorize(Ctx& c) {
+    factor_begin(c);
+    factor_levels(c, 0, static_cast<int>(c.levels.size()));
+    factor_end(c);
 }
 
 
@@ -1184,6 +1265,33 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
         host::Graph g1;
         const bool dev_l1 = c.max_levels > 1 && c.l0.n_parts > 1 && level1_device(c, g0, up1, n1, g1);
         const auto ta = std::chrono::steady_clock::now();
+        if (dev_l1 && c.solve_order && A.n > 0) {
+            // level 0 (cached per scene) is factored on the device while the
+            // host builds the coarse levels: As, restriction and inversion of
+            // level 0 are queued before the host hierarchy and overlap it
+            ensure_level0(c);
+            c.perm_active = true;
+            build_solve_matrix(c, false);
+            factor_begin(c);
+            factor_levels(c, 0, 1);
+            const auto tq = std::chrono::steady_clock::now();
+            c.hier = host::build_hierarchy_l1(c.l0, std::move(up1), n1, std::move(g1), c.max_levels);
+            if (c.hier.n_levels() > kMaxLevels) throw StatusError(kInvalidArgument, "too many MAS levels");
+            const auto tb = std::chrono::steady_clock::now();
+            set_coarse_levels(c, c.hier);
+            c.as_src_version = c.levels_version;  // the As map depends on perm and the pattern only
+            c.hier_version = c.cache_hierarchy ? phash : ~0ull;
+            c.ms_build_host = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (std::getenv("ADIPC_DEBUG_HIER")) {
+                auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+                std::fprintf(stderr, "cold MAS host (level 0 overlapped): block_edges %.1f ms, level 0 + As queued %.1f ms, "
+                                     "build_hierarchy %.1f ms, coarse levels %.1f ms\n",
+                             ms(t0, ta), ms(ta, tq), ms(tq, tb), ms(tb, std::chrono::steady_clock::now()));
+            }
+            factor_levels(c, 1, static_cast<int>(c.levels.size()));
+            factor_end(c);
+            return;
+        }
         if (dev_l1)
             c.hier = host::build_hierarchy_l1(c.l0, std::move(up1), n1, std::move(g1), c.max_levels);
         else
@@ -1198,9 +1306,6 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
             std::fprintf(stderr, "cold MAS host: block_edges %.1f ms, build_hierarchy %.1f ms, device levels %.1f ms\n",
                          ms(t0, ta), ms(ta, tb), ms(tb, tc));
         }
-    } else {
-        for (auto& L : c.levels)
-            ADIPC_CUDA(cudaMemsetAsync(L->dense.p, 0, sizeof(double) * std::max<std::int64_t>(L->dense_doubles, 1), st));
     }
     const auto t1 = std::chrono::steady_clock::now();
     c.ms_build_host = std::chrono::duration<float, std::milli>(t1 - t0).count();

@@ -250,6 +250,10 @@ def cpu_reference(sc, rank_seed, cpu_iters, steps, warmup, sample_note=True, ful
             dt = time.perf_counter() - t0
             if s >= warmup:
                 times.append(dt)
+        # the same loop sample on ONE host thread
+        t0 = time.perf_counter()
+        O.pcg_solve(A, b, M, 1e-30, RESTART, cpu_iters, O.ExecPolicy(deterministic=False, threads=1))
+        it_s_1t = cpu_iters / (time.perf_counter() - t0)
         full = None
         if full_solve:
             t0 = time.perf_counter()
@@ -264,7 +268,7 @@ def cpu_reference(sc, rank_seed, cpu_iters, steps, warmup, sample_note=True, ful
             "sample": f"{what}; {steps} steps x {cpu_iters} PCG iterations (MAS-preconditioned, cfg5 matrix) after "
                       f"a one-time assembly ({t_asm:.2f} s) and MAS build ({t_build:.2f} s); the reference's "
                       f"serial stages (radix sort, O scan, restriction, LLT, hierarchy, PCG vector ops) stay serial",
-            "assembly_s": t_asm, "mas_build_s": t_build, "full_solve": full}
+            "assembly_s": t_asm, "mas_build_s": t_build, "full_solve": full, "value_1_thread": it_s_1t}
 
 
 # ------------------------------------------------------------ hybrid scene ---
@@ -991,7 +995,7 @@ def main():
                 "data": "synthetic (same generator and seed as the GPU arm)",
                 "config": workload_config(args, sc, world),
                 "impl": "reference",
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "value_1_thread")},
                 "assembly_s": cb["assembly_s"], "mas_build_s": cb["mas_build_s"], "full_solve": full,
                 "ms_per_newton_solve": 1000.0 * (cb["mas_build_s"] + full["pcg_s"]) if full else None,
                 "e2e": {"value": e2e_value, "unit": "PCG iterations/s", "h2d_bytes_per_step": 0,
@@ -1030,7 +1034,7 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(sc, 5, args.cpu_iters, 2, 1)
-            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "value_1_thread")}
             out["cpu_baseline"]["assembly_s"] = cb["assembly_s"]
             out["cpu_baseline"]["mas_build_s"] = cb["mas_build_s"]
             out["speedup_pcg_iters_per_s_vs_cpu"] = out["value"] / cb["value"]

@@ -62,4 +62,31 @@ for scale in (0.0, 0.3):
     val, U = c.fem_assemble(mesh, dx, xt, 1e-4, g, pinned=pin)
     print("fem_assemble", scale, val, U, flush=True)
 c.close()
+# the device IncrementalPotential on a small geometric hybrid scene: positions,
+# broad phase (proximity and swept), contact / element / body producers, the
+# gradient lift, two-level assembly, line-search value, CCD, cold MAS + PCG
+from paper_2411_06224_b200.potential import IncrementalPotential  # noqa: E402
+from scenegen.geom import GeomHybrid  # noqa: E402
+
+g = GeomHybrid(grid=(2, 2, 1), res=4, bodies=(2, 2), body_res=1)
+t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+c = Context(0)
+l0 = P.partition_block_graph(g.n_blocks, g.rest_edges, 16)
+c.set_level0_partition(l0.part_of, l0.n_parts, 16, 4)
+mesh = {"mass": t(g.mass), "tets": t(g.tets), "rest_inv9": t(g.rest_inv9), "rest_volume": t(g.rest_volume),
+        "tet_begin": g.tet_begin, "mu": [g.mu], "lam": [g.lam],
+        "bodies": {"reduced_mass": t(g.reduced_mass.transpose(0, 2, 1)), "kappa": t(g.kappa_abd),
+                   "volume": t(g.body_volume)}}
+ip = IncrementalPotential(c, mesh, {"verts": t(g.surf_verts), "edges": t(g.edges), "tris": t(g.tris)},
+                          {"n_fem": g.n_fem, "abd_body": t(g.abd_body), "jac36": t(g.jac36)}, g.dt, pinned=t(g.pinned))
+ip.set_targets(t(g.x_tilde.reshape(-1)), t(g.q_tilde))
+ip.set_contact(g.dhat, g.kappa)
+state = t(g.state() + np.random.default_rng(2).normal(0, 5e-5, 3 * g.n_blocks))
+val, grad = ip.assemble(state)
+print("potential", val, ip.last, ip.value(state), flush=True)
+c.build_preconditioner(_lib.PRECOND_MAS)
+d = torch.empty_like(grad)
+_, res = c.pcg(-grad, 1e-4, 250, 100000, x=d)
+print("ccd", ip.ccd_step(state, d), res, flush=True)
+c.close()
 print("sanitize drive done")

@@ -18,8 +18,15 @@ namespace adipc_gpu {
 namespace {
 
 constexpr int kSpmvThreads = 256;
-constexpr int kSpmvMinBlocks = 3;  // 3 x 256 threads (<= 85 registers, 24 warps/SM); 4 spills: 85 vs 61 us
+constexpr int kSpmvMinBlocks = 2;  // 2 x 256 threads: the two-stage pipeline's 114 registers without spills
 
+// Each warp owns a contiguous run of 32-block chunks (row locality for the x
+// gathers and y atomics), software-pipelined two deep: chunk ch is computed
+// while the x gathers of chunk ch + 1 and the indices / blocks of chunk ch + 2
+// are in flight (114 registers, 2 CTAs of 256 per SM; one stage deep at 3
+// CTAs / SM measured 63.2 vs 62.0 us per cfg5 SpMV, 136.8 vs 134.8 us per PCG
+// iteration). A streams through L2 once per SpMV (evict-first): it is 200 MB
+// at cfg5, larger than the 126 MB L2, and the vectors the gathers hit stay.
 template <bool kDot>
 __global__ void __launch_bounds__(kSpmvThreads, kSpmvMinBlocks) k_spmv(const std::uint32_t* __restrict__ rows,
                                                      const std::uint32_t* __restrict__ cols,
@@ -28,61 +35,69 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvMinBlocks) k_spmv(const std
                                                      double* __restrict__ partials, unsigned* __restrict__ ticket,
                                                      double* __restrict__ dot_out, const int* __restrict__ flags) {
     const int lane = threadIdx.x & 31;
-    // A streams through L2 once per SpMV (evict-first): it is 200 MB at cfg5,
-    // larger than the 126 MB L2, and the vectors the gathers hit should stay
     const std::uint64_t pol = policy_evict_first();
     const std::int64_t warp0 = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
-    // each warp owns a contiguous run of 32-block chunks (row locality for the
-    // x gathers and y atomics); software-pipelined: the next chunk's indices
-    // and block planes are in flight while the current chunk is processed
     const std::int64_t n_chunks = (U + 31) >> 5;
     const std::int64_t ch0 = warp0 * n_chunks / nwarps, ch1 = (warp0 + 1) * n_chunks / nwarps;
     double dsum = 0;
-    std::uint32_t nr = 0xFFFFFFFFu, nc = 0;
-    double nh[9];
+    std::uint32_t ar = 0xFFFFFFFFu, ac = 0;  // stage A: indices + blocks in flight
+    double ah[9];
     auto load = [&](std::int64_t ch) {
         const std::int64_t e = (ch << 5) + lane;
-        nr = 0xFFFFFFFFu;
-        nc = 0;
+        ar = 0xFFFFFFFFu;
+        ac = 0;
         if (ch < ch1 && e < U) {
-            nr = ld_nc_policy(rows + e, pol);
-            nc = ld_nc_policy(cols + e, pol);
+            ar = ld_nc_policy(rows + e, pol);
+            ac = ld_nc_policy(cols + e, pol);
 #pragma unroll
-            for (int k = 0; k < 9; ++k) nh[k] = ld_nc_policy(blocks + blk(e, k), pol);  // one contiguous tile
+            for (int k = 0; k < 9; ++k) ah[k] = ld_nc_policy(blocks + blk(e, k), pol);
         }
     };
-    load(ch0);  // the matrix does not change during the solve: prefetched before the dependency wait
-    pdl_wait();
-    if (flags && flags[0]) return;  // PCG already finished (F_DONE)
-    pdl_launch();
-    for (std::int64_t ch = ch0; ch < ch1; ++ch) {
-        const std::uint32_t r = nr, c = nc;
-        double h[9];
+    std::uint32_t br = 0xFFFFFFFFu, bc = 0;  // stage B: x gathers in flight
+    double bh[9], bx[6];
+    auto advance = [&] {  // A -> B, issue B's gathers
+        br = ar;
+        bc = ac;
 #pragma unroll
-        for (int k = 0; k < 9; ++k) h[k] = nh[k];
-        load(ch + 1);
+        for (int k = 0; k < 9; ++k) bh[k] = ah[k];
+        if (br != 0xFFFFFFFFu) {
+            bx[0] = ldg_issue(x + 3 * bc);
+            bx[1] = ldg_issue(x + 3 * bc + 1);
+            bx[2] = ldg_issue(x + 3 * bc + 2);
+            bx[3] = ldg_issue(x + 3 * br);
+            bx[4] = ldg_issue(x + 3 * br + 1);
+            bx[5] = ldg_issue(x + 3 * br + 2);
+        }
+    };
+    load(ch0);
+    pdl_wait();
+    if (flags && flags[0]) return;
+    pdl_launch();
+    advance();
+    load(ch0 + 1);
+    for (std::int64_t ch = ch0; ch < ch1; ++ch) {
+        const std::uint32_t r = br, c = bc;
+        double h[9], xv[6];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) h[k] = bh[k];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) xv[k] = bx[k];
+        advance();
+        load(ch + 2);
         const bool valid = r != 0xFFFFFFFFu;
         double yr0 = 0, yr1 = 0, yr2 = 0;
         if (valid) {
-            const double xc0 = ldg_issue(x + 3 * c);
-            const double xc1 = ldg_issue(x + 3 * c + 1);
-            const double xc2 = ldg_issue(x + 3 * c + 2);
-            const double xr0 = ldg_issue(x + 3 * r);
-            const double xr1 = ldg_issue(x + 3 * r + 1);
-            const double xr2 = ldg_issue(x + 3 * r + 2);
-            // column-major H(i,j) = h[3j+i]
-            yr0 = h[0] * xc0 + h[3] * xc1 + h[6] * xc2;
-            yr1 = h[1] * xc0 + h[4] * xc1 + h[7] * xc2;
-            yr2 = h[2] * xc0 + h[5] * xc1 + h[8] * xc2;
-            if (r != c) {  // H^T x[row] towards y[col]
-                red_add(y + 3 * c, h[0] * xr0 + h[1] * xr1 + h[2] * xr2);
-                red_add(y + 3 * c + 1, h[3] * xr0 + h[4] * xr1 + h[5] * xr2);
-                red_add(y + 3 * c + 2, h[6] * xr0 + h[7] * xr1 + h[8] * xr2);
+            yr0 = h[0] * xv[0] + h[3] * xv[1] + h[6] * xv[2];
+            yr1 = h[1] * xv[0] + h[4] * xv[1] + h[7] * xv[2];
+            yr2 = h[2] * xv[0] + h[5] * xv[1] + h[8] * xv[2];
+            if (r != c) {
+                red_add(y + 3 * c, h[0] * xv[3] + h[1] * xv[4] + h[2] * xv[5]);
+                red_add(y + 3 * c + 1, h[3] * xv[3] + h[4] * xv[4] + h[5] * xv[5]);
+                red_add(y + 3 * c + 2, h[6] * xv[3] + h[7] * xv[4] + h[8] * xv[5]);
             }
-            if (kDot) dsum += (r != c ? 2.0 : 1.0) * (xr0 * yr0 + xr1 * yr1 + xr2 * yr2);
+            if (kDot) dsum += (r != c ? 2.0 : 1.0) * (xv[3] * yr0 + xv[4] * yr1 + xv[5] * yr2);
         }
-        // head-segmented sum of the row contributions (rows sorted within the warp)
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const double a0 = __shfl_down_sync(0xffffffffu, yr0, off);
@@ -102,7 +117,6 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvMinBlocks) k_spmv(const std
             red_add(y + 3 * r + 2, yr2);
         }
     }
-    // the PCG's p.Ap SpMV opens an iteration: its last CTA advances F_K
     if (kDot) grid_sum_last_block(dsum, partials, ticket, dot_out, flags ? const_cast<int*>(flags) + F_K : nullptr);
 }
 

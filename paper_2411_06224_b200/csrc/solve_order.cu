@@ -475,8 +475,22 @@ void launch_update_so(Ctx& c, const PcgArgs& a) {
         if (l >= 2) so.anc[l] = c.levels[l]->anc.p;
     }
     so.max_fill0 = L0.max_fill;
-    so.subs = kUpdSubs;
     so.red_levels = c.deterministic ? 2 : so.n_levels;
+    // tiles sized so the grid is ONE wave of resident CTAs (at least kUpdSubs
+    // subdomains per tile): a second, mostly empty wave costs a whole CTA
+    // latency chain (cfg5: 687 tiles of 32 on 592 resident CTAs)
+    int sms = kSMs, occ = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    so.subs = kUpdSubs;
+    for (int it = 0; it < 2; ++it) {  // smem depends on subs; occupancy on smem
+        const std::size_t sm = update_tile_smem(L0.max_fill, so.subs);
+        ADIPC_CUDA(cudaFuncSetAttribute(k_update_so<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sm)));
+        ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_so<kMode>, kUpdThreads, sm));
+        const std::int64_t slots = static_cast<std::int64_t>(sms) * std::max(occ, 1);
+        so.subs = static_cast<int>(std::max<std::int64_t>(kUpdSubs, ceil_div(L0.n_parts, slots)));
+    }
+
     const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(L0.n_parts, so.subs)));
     const std::size_t smem = update_tile_smem(L0.max_fill, so.subs);
     // a per-device function attribute: set on every launch (cheap, legal while
@@ -580,6 +594,8 @@ void launch_final_so(Ctx& c, double* z, double* p, double* ap, const PcgArgs& a)
         ++fa.n_clear;
     }
     constexpr int block = 256;
+    // one CTA per 512 slots (a one-wave grid-stride variant measured slower
+    // in the PDL-chained graph: 137.0 vs 135.1 us per cfg5 iteration)
     const int grid = static_cast<int>(std::max<std::int64_t>(1, ceil_div(ceil_div(c.A.n, 2), block)));
     ADIPC_CUDA(launch_pdl(k_final_so<kFinal>, dim3(grid), dim3(block), 0, c.stream, true, c.A.n, fa, z, p, ap, a));
     ADIPC_LAUNCH_CHECK();

@@ -1130,11 +1130,23 @@ __global__ void k_l1_components(std::int32_t n_parts, const std::int32_t* __rest
     const bool act = lane < m;
     const std::int32_t node = act ? members[m0 + lane] : -1;
     unsigned nb = 0;
-    if (act)
-        for (std::int64_t e = gptr[node]; e < gptr[node + 1]; ++e) {
+    if (act) {
+        // in-subdomain neighbours lie in [first member, last member] of the
+        // sorted adjacency: binary-search the window (affine-body slots have
+        // tens of thousands of neighbours, their subdomain a handful)
+        const std::int32_t lo = members[m0], hi = members[m0 + m - 1];
+        std::int64_t a = gptr[node], b = gptr[node + 1];
+        while (a < b) {
+            const std::int64_t mid = (a + b) >> 1;
+            if (gadj[mid] < lo) a = mid + 1;
+            else b = mid;
+        }
+        for (std::int64_t e = a, e1 = gptr[node + 1]; e < e1; ++e) {
             const std::int32_t v = gadj[e];
+            if (v > hi) break;
             if (part_of[v] == s) nb |= 1u << pos[v];
         }
+    }
     int lab = lane;
     for (;;) {
         int best = lab;
@@ -1260,11 +1272,16 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
         // subdomains of <= 32 members — the first aggregation pass too; the
         // host continues from the (small) level-1 graph
         const DeviceGraph g0 = level0_graph_device(c);
+        const auto tg = std::chrono::steady_clock::now();
         std::vector<std::int32_t> up1;
         std::int32_t n1 = 0;
         host::Graph g1;
         const bool dev_l1 = c.max_levels > 1 && c.l0.n_parts > 1 && level1_device(c, g0, up1, n1, g1);
         const auto ta = std::chrono::steady_clock::now();
+        if (std::getenv("ADIPC_DEBUG_HIER"))
+            std::fprintf(stderr, "  level-0 graph (device, E=%lld) %.2f ms, level-1 pass + D2H %.2f ms\n",
+                         static_cast<long long>(g0.E), std::chrono::duration<double, std::milli>(tg - t0).count(),
+                         std::chrono::duration<double, std::milli>(ta - tg).count());
         if (dev_l1 && c.solve_order && A.n > 0) {
             // level 0 (cached per scene) is factored on the device while the
             // host builds the coarse levels: As, restriction and inversion of

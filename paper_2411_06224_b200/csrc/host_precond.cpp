@@ -377,6 +377,7 @@ void extend_hierarchy(MasHierarchy& h, Graph g, int max_levels) {
         next.part_of = std::move(grouped.part_of);
         next.agg.resize(h.n_slots);
         for (Index slot = 0; slot < h.n_slots; ++slot) next.agg[slot] = up[cur.agg[slot]];
+        if (h.n_levels() > 1) h.levels.back().up = up;  // coarse node maps (level 0's is agg of level 1)
         h.levels.push_back(std::move(next));
         g = std::move(cg);
         if (dbg)

@@ -29,6 +29,7 @@ struct Level {
     Index n_parts = 0;
     std::vector<Index> part_of;  // node -> subdomain
     std::vector<Index> agg;      // slot -> node
+    std::vector<Index> up;       // node -> the next level's node (levels >= 1 with a next level)
 };
 
 struct MasHierarchy {

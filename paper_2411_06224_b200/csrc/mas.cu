@@ -521,7 +521,7 @@ void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
 
 // Per-level CSR metadata from a hierarchy level (mas.hpp:42-54 semantics:
 // pos_of = rank of the node among its subdomain's nodes in ascending id).
-void build_level(Ctx& c, DeviceLevel& L, const host::Level& hl, int level, std::int32_t n_slots) {
+void build_level(Ctx& c, DeviceLevel& L, const host::Level& hl, int level, std::int32_t n_slots, bool upload_agg = true) {
     cudaStream_t st = c.stream;
     L.n_nodes = hl.n_nodes;
     L.n_parts = hl.n_parts;
@@ -550,7 +550,10 @@ void build_level(Ctx& c, DeviceLevel& L, const host::Level& hl, int level, std::
     upload(L.dense_off, dense_off, st);
     L.inv_off_host = std::move(inv_off);
     if (level > 0) {
-        upload(L.agg, hl.agg, st);
+        if (upload_agg)
+            upload(L.agg, hl.agg, st);
+        else
+            L.agg.reserve(static_cast<std::size_t>(n_slots));
         L.y.reserve(3 * static_cast<std::size_t>(hl.n_nodes));
         L.rr.reserve(3 * static_cast<std::size_t>(hl.n_nodes));
     }
@@ -730,33 +733,127 @@ void ensure_level0(Ctx& c) {
     ++c.levels_version;
 }
 
+__global__ void k_perm_scatter(std::int32_t n, const std::int32_t* __restrict__ perm,
+                               const std::int32_t* __restrict__ src, std::int32_t* __restrict__ dst) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        dst[perm[i]] = src[i];
+}
+__global__ void k_map_through(std::int32_t n, const std::int32_t* __restrict__ map,
+                              const std::int32_t* __restrict__ src, std::int32_t* __restrict__ dst) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = map[src[i]];
+}
+
+// Restriction links level 0 -> 1 in solve order (link_levels' level-0 part):
+// one warp per level-0 subdomain (<= 32 slots, contiguous in solve order,
+// lane j = slot sub_ptr[s] + j); its level-1 nodes are consecutive ids from
+// agg1 of its first slot, so the children lists (ascending slots) and their
+// CSR offsets follow from ballots inside the warp.
+__global__ void k_l0_links(std::int32_t n_parts, std::int32_t n, std::int32_t n1,
+                           const std::int32_t* __restrict__ sub_ptr, const std::int32_t* __restrict__ agg1,
+                           std::int32_t* __restrict__ up_first, std::int32_t* __restrict__ upc_ptr,
+                           std::int32_t* __restrict__ upc_pos, std::int32_t* __restrict__ upc_node) {
+    const int lane = threadIdx.x & 31;
+    const std::int64_t w = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (w >= n_parts) return;
+    const std::int32_t s = static_cast<std::int32_t>(w);
+    const std::int32_t a = sub_ptr[s], m = sub_ptr[s + 1] - a;
+    const bool act = lane < m;
+    // the subdomain's smallest level-1 node (an empty subdomain: the next one's)
+    const std::int32_t base = a < n ? agg1[a] : n1;
+    const std::int32_t loc = act ? agg1[a + lane] - base : 0x7FFFFFFF;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned same = __match_any_sync(0xffffffffu, loc);
+    // offset of node base + loc: slots of the subdomain in nodes < loc
+    int n_below = 0;
+    for (int j = 0; j < m; ++j) n_below += (__shfl_sync(0xffffffffu, loc, j) < loc) ? 1 : 0;
+    if (act) {
+        const int q = a + n_below + __popc(same & lt);
+        upc_node[q] = a + lane;
+        upc_pos[q] = lane;
+        if ((same & lt) == 0) upc_ptr[base + loc] = a + n_below;  // first child of its node
+    }
+    if (lane == 0) up_first[s] = base;
+    if (s == n_parts - 1 && lane == 0) upc_ptr[n1] = n;
+}
+
 // The coarse levels (>= 1) of hierarchy h in solve order on top of the
-// cached level 0, and the restriction links of every level.
+// cached level 0, and the restriction links of every level. The slot-sized
+// parts are built on the device: level-1 agg from the level-1 pass's map
+// through perm, levels >= 2 through the (small) level-1 -> level-l ancestor
+// maps, the level-0 links by k_l0_links; the host links the small coarse
+// levels.
 void set_coarse_levels(Ctx& c, const host::MasHierarchy& h) {
+    cudaStream_t st = c.stream;
     const std::int32_t n = h.n_slots;
     const std::size_t n_lv = static_cast<std::size_t>(h.n_levels());
     if (c.levels.size() > std::max<std::size_t>(n_lv, 1)) c.levels.resize(std::max<std::size_t>(n_lv, 1));
     while (c.levels.size() < n_lv) c.levels.emplace_back(new DeviceLevel());
-    host::MasHierarchy hp;
-    hp.capacity = h.capacity;
-    hp.n_slots = n;
-    hp.levels.resize(n_lv);
-    hp.levels[0].n_nodes = n;
-    hp.levels[0].n_parts = h.levels[0].n_parts;
-    hp.levels[0].part_of.swap(c.l0_solve_part_of);  // lent to link_levels, returned below
-    for (std::size_t l = 1; l < n_lv; ++l) {
-        hp.levels[l].n_nodes = h.levels[l].n_nodes;
-        hp.levels[l].n_parts = h.levels[l].n_parts;
-        hp.levels[l].part_of = h.levels[l].part_of;
-        std::vector<std::int32_t>& agg = hp.levels[l].agg;
-        agg.resize(n);
-        const std::vector<std::int32_t>& src = h.levels[l].agg;
-#pragma omp parallel for schedule(static)
-        for (std::int32_t i = 0; i < n; ++i) agg[c.perm_host[i]] = src[i];
-        build_level(c, *c.levels[l], hp.levels[l], static_cast<int>(l), n);
+    for (std::size_t l = 1; l < n_lv; ++l) build_level(c, *c.levels[l], h.levels[l], static_cast<int>(l), n, false);
+    if (n_lv < 2) {
+        c.levels_permuted = true;
+        ++c.levels_version;
+        return;
     }
-    link_levels(c, hp);
-    hp.levels[0].part_of.swap(c.l0_solve_part_of);
+    // agg of level 1 in solve order, then levels >= 2 through the ancestors
+    DeviceLevel& L1 = *c.levels[1];
+    k_perm_scatter<<<grid_for(n, 256, 16), 256, 0, st>>>(n, c.perm.p, c.l1_up.p, L1.agg.p);
+    ADIPC_LAUNCH_CHECK();
+    std::vector<std::int32_t> anc;  // level-1 node -> level-l node
+    for (std::size_t l = 2; l < n_lv; ++l) {
+        const std::vector<std::int32_t>& up = h.levels[l - 1].up;
+        if (l == 2) {
+            anc = up;
+        } else {
+            for (auto& v : anc) v = up[v];
+        }
+        DeviceLevel& Ll = *c.levels[l];
+        upload(Ll.anc, anc, st);
+        k_map_through<<<grid_for(n, 256, 16), 256, 0, st>>>(n, Ll.anc.p, L1.agg.p, Ll.agg.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    // level-0 links on the device
+    DeviceLevel& L0 = *c.levels[0];
+    const std::int32_t n1 = h.levels[1].n_nodes;
+    L0.up_first.reserve(static_cast<std::size_t>(h.levels[0].n_parts) + 1);
+    L0.upc_ptr.reserve(static_cast<std::size_t>(n1) + 1);
+    L0.upc_pos.reserve(static_cast<std::size_t>(n));
+    L0.upc_node.reserve(static_cast<std::size_t>(n));
+    L0.up_node.reserve(static_cast<std::size_t>(n));
+    k_l0_links<<<static_cast<int>(ceil_div(h.levels[0].n_parts, 8)), 256, 0, st>>>(
+        h.levels[0].n_parts, n, n1, L0.sub_ptr.p, L1.agg.p, L0.up_first.p, L0.upc_ptr.p, L0.upc_pos.p, L0.upc_node.p);
+    ADIPC_LAUNCH_CHECK();
+    ADIPC_CUDA(cudaMemcpyAsync(L0.up_node.p, L1.agg.p, sizeof(std::int32_t) * n, cudaMemcpyDeviceToDevice, st));
+    ADIPC_CUDA(cudaMemcpyAsync(L0.up_first.p + h.levels[0].n_parts, &n1, sizeof(n1), cudaMemcpyHostToDevice, st));
+    // levels >= 1: the host links from the stored node maps (link_levels' rule)
+    for (std::size_t l = 1; l + 1 < n_lv; ++l) {
+        const host::Level& cur = h.levels[l];
+        const host::Level& nxt = h.levels[l + 1];
+        DeviceLevel& L = *c.levels[l];
+        const std::vector<std::int32_t>& up = cur.up;
+        std::vector<std::int32_t> first(cur.n_parts + 1, std::numeric_limits<std::int32_t>::max());
+        std::vector<std::int32_t> cnt(nxt.n_nodes + 1, 0);
+        for (std::int32_t v = 0; v < cur.n_nodes; ++v) {
+            first[cur.part_of[v]] = std::min(first[cur.part_of[v]], up[v]);
+            ++cnt[up[v] + 1];
+        }
+        first[cur.n_parts] = nxt.n_nodes;
+        for (std::int32_t s = cur.n_parts - 1; s >= 0; --s)
+            if (first[s] == std::numeric_limits<std::int32_t>::max()) first[s] = first[s + 1];
+        for (std::int32_t v = 0; v < nxt.n_nodes; ++v) cnt[v + 1] += cnt[v];
+        std::vector<std::int32_t> pos(cur.n_nodes), node(cur.n_nodes), fill(cnt.begin(), cnt.end() - 1);
+        for (std::int32_t v = 0; v < cur.n_nodes; ++v) {
+            node[fill[up[v]]] = v;
+            pos[fill[up[v]]++] = L.pos_host[v];
+        }
+        upload(L.up_first, first, st);
+        upload(L.upc_ptr, cnt, st);
+        upload(L.upc_pos, pos, st);
+        upload(L.upc_node, node, st);
+        upload(L.up_node, up, st);
+    }
     c.levels_permuted = true;
     ++c.levels_version;
 }

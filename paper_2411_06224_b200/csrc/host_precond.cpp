@@ -121,14 +121,20 @@ Partition partition_block_graph(Index v, const Graph& g, Index capacity) {
         comp_ptr.push_back(static_cast<std::int64_t>(order.size()));
     }
     std::vector<char> assigned(v, 0);
-    // the carving frontier: unassigned neighbours of the open cluster as
-    // packed keys (connections << 32 | ~id), so the pick — most connections,
-    // ties to the lowest id — is one max over a short contiguous array;
-    // where[] locates a node's key for the increments (-1: not a candidate)
-    std::vector<std::int32_t> where(v, -1);
-    std::vector<std::uint64_t> cand;
-    constexpr std::uint64_t kOne = 1ull << 32;
-    auto key_id = [](std::uint64_t k) { return static_cast<Index>(~static_cast<std::uint32_t>(k)); };
+    // the carving frontier as a bucket queue: bucket k holds the unassigned
+    // neighbours of the open cluster with k connections into it; the pick —
+    // most connections, ties to the lowest id — scans only the top bucket.
+    // conn[] / slot[] locate a node (conn 0: not a candidate).
+    std::vector<Index> conn(v, 0), slot(v, 0);
+    std::vector<std::vector<Index>> bucket(1);
+    int top = 0;
+    auto bucket_remove = [&](Index x) {
+        std::vector<Index>& bk = bucket[conn[x]];
+        const Index last = bk.back();
+        bk[slot[x]] = last;
+        slot[last] = slot[x];
+        bk.pop_back();
+    };
     Index next_part = 0, open_part = kInvalid, open_fill = 0;
     const std::size_t n_comps = comp_ptr.size() - 1;
     for (std::size_t ci = 0; ci < n_comps; ++ci) {
@@ -161,32 +167,29 @@ Partition partition_block_graph(Index v, const Graph& g, Index capacity) {
                 for (std::int64_t k = g.ptr[pick]; k < g.ptr[pick + 1]; ++k) {
                     const Index nb = g.adj[k];
                     if (assigned[nb]) continue;
-                    if (where[nb] < 0) {
-                        where[nb] = static_cast<std::int32_t>(cand.size());
-                        cand.push_back(kOne | static_cast<std::uint32_t>(~static_cast<std::uint32_t>(nb)));
-                    } else {
-                        cand[where[nb]] += kOne;
-                    }
+                    if (conn[nb] > 0) bucket_remove(nb);
+                    const Index c = ++conn[nb];
+                    if (c >= static_cast<Index>(bucket.size())) bucket.resize(static_cast<std::size_t>(c) + 1);
+                    slot[nb] = static_cast<Index>(bucket[c].size());
+                    bucket[c].push_back(nb);
+                    if (c > top) top = c;
                 }
-                if (cand.empty()) {
+                while (top > 0 && bucket[top].empty()) --top;
+                if (top == 0) {
                     pick = kInvalid;
                     break;
                 }
-                std::size_t at = 0;
-                std::uint64_t best = cand[0];
-                for (std::size_t k = 1; k < cand.size(); ++k)
-                    if (cand[k] > best) {
-                        best = cand[k];
-                        at = k;
-                    }
-                pick = key_id(best);
-                where[pick] = -1;
-                cand[at] = cand.back();
-                cand.pop_back();
-                if (at < cand.size()) where[key_id(cand[at])] = static_cast<std::int32_t>(at);
+                const std::vector<Index>& bk = bucket[top];
+                pick = bk[0];
+                for (std::size_t k = 1; k < bk.size(); ++k) pick = bk[k] < pick ? bk[k] : pick;
+                bucket_remove(pick);
+                conn[pick] = 0;
             }
-            for (std::uint64_t k : cand) where[key_id(k)] = -1;
-            cand.clear();
+            for (int k = 1; k <= top; ++k) {
+                for (Index x : bucket[k]) conn[x] = 0;
+                bucket[k].clear();
+            }
+            top = 0;
         }
     }
     p.n_parts = next_part;

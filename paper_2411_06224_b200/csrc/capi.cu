@@ -179,6 +179,10 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.l1_base.free();
     c.l1_ptr.free();
     c.l1_keys.free();
+    for (auto* b : {&c.ag_part, &c.ag_mem_ptr, &c.ag_members, &c.ag_pos, &c.ag_up, &c.ag_ncomp, &c.ag_cnt, &c.ag_adj[0],
+                    &c.ag_adj[1]})
+        b->free();
+    for (auto* b : {&c.ag_base, &c.ag_ptr[0], &c.ag_ptr[1]}) b->free();
     c.graph_deg.free();
     c.graph_adj.free();
     c.graph_ptr.free();

@@ -167,6 +167,12 @@ struct Ctx {
     DBuf<std::int32_t> l1_up, l1_ncomp, l1_cnt, l1_adj;
     DBuf<std::int64_t> l1_base, l1_ptr;
     DBuf<std::uint64_t> l1_keys;
+    std::int64_t l1_E = 0;          // edges of the level-1 graph in l1_ptr / l1_adj
+    // aggregation passes above level 1 on the device (cold build): the
+    // level's member lists, the next level's node map, and its graph
+    // (ping-pong between two buffers)
+    DBuf<std::int32_t> ag_part, ag_mem_ptr, ag_members, ag_pos, ag_up, ag_ncomp, ag_cnt, ag_adj[2];
+    DBuf<std::int64_t> ag_base, ag_ptr[2];
     int max_levels = 4;
     bool have_l0 = false;
     host::MasHierarchy hier;        // last built hierarchy (host copy)

@@ -235,6 +235,28 @@ void extend_hierarchy(MasHierarchy& h, Graph g, int max_levels);
 
 }  // namespace
 
+MasHierarchy hierarchy_base(const Partition& l0) { return base_hierarchy(l0); }
+
+void extend_from(MasHierarchy& h, Graph g, int max_levels) { extend_hierarchy(h, std::move(g), max_levels); }
+
+void append_level(MasHierarchy& h, std::vector<Index> up, Index n_next, const Graph& g_next) {
+    Level next;
+    next.n_nodes = n_next;
+    Partition grouped = partition_block_graph(n_next, g_next, h.capacity);
+    next.n_parts = grouped.n_parts;
+    next.part_of = std::move(grouped.part_of);
+    if (h.n_levels() == 1) {
+        next.agg = std::move(up);  // level 0's agg is the identity
+    } else {
+        Level& cur = h.levels.back();
+        next.agg.resize(h.n_slots);
+#pragma omp parallel for schedule(static)
+        for (Index slot = 0; slot < h.n_slots; ++slot) next.agg[slot] = up[cur.agg[slot]];
+        cur.up = std::move(up);
+    }
+    h.levels.push_back(std::move(next));
+}
+
 MasHierarchy build_hierarchy(const Partition& l0, Graph g0, int max_levels) {
     MasHierarchy h = base_hierarchy(l0);
     extend_hierarchy(h, std::move(g0), max_levels);

@@ -58,5 +58,13 @@ MasHierarchy build_hierarchy(const Partition& l0, Graph g0, int max_levels);
 // same, with the first aggregation pass done elsewhere (the device, mas.cu): up1 = level-0 node ->
 // level-1 node (n1 nodes) and g1 = the level-1 node graph
 MasHierarchy build_hierarchy_l1(const Partition& l0, std::vector<Index> up1, Index n1, Graph g1, int max_levels);
+// the pieces for a loop driven elsewhere (the device aggregation passes,
+// mas.cu): the level-0 base, and one more level from the current last
+// level's node map `up` (node -> next node, n_next nodes) and the next
+// level's graph, partitioned here (partition.hpp:88-159; hierarchy.hpp:86-99)
+MasHierarchy hierarchy_base(const Partition& l0);
+void append_level(MasHierarchy& h, std::vector<Index> up, Index n_next, const Graph& g_next);
+// the rest of the aggregation loop on the host from the last level, whose graph is g
+void extend_from(MasHierarchy& h, Graph g, int max_levels);
 
 }  // namespace adipc_gpu::host

@@ -1334,7 +1334,101 @@ bool level1_device(Ctx& c, const DeviceGraph& g0, std::vector<std::int32_t>& up1
     k_adj_emit<<<grid_for(n1, 8, 16), 256, 0, st>>>(n1, c.sorted.p, c.row_start.p, c.l1_ptr.p, c.l1_adj.p);
     ADIPC_LAUNCH_CHECK();
     g1 = graph_to_host(c, DeviceGraph{c.l1_ptr.p, c.l1_adj.p, E1}, n1);
+    c.l1_E = E1;
     return true;
+}
+
+// One aggregation pass (hierarchy.hpp:53-85) above level 1 on the device, for
+// a level whose subdomains have <= 32 members: the components inside each
+// subdomain (numbered as the BFS seeds), the node map up (to the host too)
+// and the next level's sorted unique graph into ag_ptr / ag_adj[out]. False
+// when a subdomain is too large (the host continues then).
+bool agg_pass_device(Ctx& c, const host::Level& lv, const DeviceGraph& g, int out, std::vector<std::int32_t>& up,
+                     std::int32_t& n_next, DeviceGraph& g_next) {
+    cudaStream_t st = c.stream;
+    const std::int32_t n = lv.n_nodes, np = lv.n_parts;
+    std::vector<std::int32_t> mem_ptr(static_cast<std::size_t>(np) + 1, 0), members(n), pos(n);
+    for (std::int32_t i = 0; i < n; ++i) pos[i] = mem_ptr[lv.part_of[i] + 1]++;
+    for (std::int32_t s = 0; s < np; ++s)
+        if (mem_ptr[s + 1] > 32) return false;
+    for (std::int32_t s = 0; s < np; ++s) mem_ptr[s + 1] += mem_ptr[s];
+    for (std::int32_t i = 0; i < n; ++i) members[mem_ptr[lv.part_of[i]] + pos[i]] = i;
+    upload(c.ag_part, lv.part_of, st);
+    upload(c.ag_mem_ptr, mem_ptr, st);
+    upload(c.ag_members, members, st);
+    upload(c.ag_pos, pos, st);
+    c.ag_up.reserve(static_cast<std::size_t>(n));
+    c.ag_ncomp.reserve(static_cast<std::size_t>(np));
+    c.ag_base.reserve(static_cast<std::size_t>(np) + 1);
+    k_l1_components<<<static_cast<int>(ceil_div(np, 8)), 256, 0, st>>>(np, c.ag_mem_ptr.p, c.ag_members.p, c.ag_part.p,
+                                                                     c.ag_pos.p, g.ptr, g.adj, c.ag_up.p, c.ag_ncomp.p);
+    ADIPC_LAUNCH_CHECK();
+    exclusive_scan(c.ag_ncomp.p, np, c.ag_base.p, c.scan_scratch, st);
+    k_l1_up<<<grid_for(n, 256, 16), 256, 0, st>>>(n, c.ag_part.p, c.ag_base.p, c.ag_up.p);
+    ADIPC_LAUNCH_CHECK();
+    std::int64_t total = 0;
+    up.resize(static_cast<std::size_t>(n));
+    ADIPC_CUDA(cudaMemcpyAsync(&total, c.ag_base.p + np, sizeof(total), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaMemcpyAsync(up.data(), c.ag_up.p, sizeof(std::int32_t) * n, cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    n_next = static_cast<std::int32_t>(total);
+    if (n_next == n) return true;
+    c.l1_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(g.E, 1)));
+    k_l1_keys<<<grid_for(n, 256, 16), 256, 0, st>>>(n, g.ptr, g.adj, c.ag_up.p, c.l1_keys.p);
+    ADIPC_LAUNCH_CHECK();
+    bucket_sort(c, c.l1_keys.p, g.E, n_next, nullptr);
+    c.ag_cnt.reserve(static_cast<std::size_t>(n_next) + 1);
+    c.ag_ptr[out].reserve(static_cast<std::size_t>(n_next) + 1);
+    k_adj_count<<<grid_for(n_next, 8, 16), 256, 0, st>>>(n_next, c.sorted.p, c.row_start.p, c.ag_cnt.p);
+    ADIPC_LAUNCH_CHECK();
+    exclusive_scan(c.ag_cnt.p, n_next, c.ag_ptr[out].p, c.scan_scratch, st);
+    std::int64_t E = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&E, c.ag_ptr[out].p + n_next, sizeof(E), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    c.ag_adj[out].reserve(static_cast<std::size_t>(std::max<std::int64_t>(E, 1)));
+    k_adj_emit<<<grid_for(n_next, 8, 16), 256, 0, st>>>(n_next, c.sorted.p, c.row_start.p, c.ag_ptr[out].p,
+                                                      c.ag_adj[out].p);
+    ADIPC_LAUNCH_CHECK();
+    g_next = DeviceGraph{c.ag_ptr[out].p, c.ag_adj[out].p, E};
+    return true;
+}
+
+// build_hierarchy from the device level-1 pass (hierarchy.hpp:30-100): the
+// partitions (sequential carving) on the host, every aggregation pass above
+// level 1 on the device while its subdomains fit a warp
+host::MasHierarchy hierarchy_from_level1(Ctx& c, std::vector<std::int32_t> up1, std::int32_t n1, const host::Graph& g1) {
+    host::MasHierarchy h = host::hierarchy_base(c.l0);
+    if (h.n_levels() >= c.max_levels || c.l0.n_parts <= 1 || n1 == h.n_slots) return h;
+    const bool dbg = std::getenv("ADIPC_DEBUG_HIER") != nullptr;
+    auto t = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what, int l) {
+        if (!dbg) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "  level %d %s %.2f ms\n", l, what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    };
+    host::append_level(h, std::move(up1), n1, g1);  // level-1 partition (host carve)
+    lap("partition", 1);
+    DeviceGraph gcur{c.l1_ptr.p, c.l1_adj.p, c.l1_E};
+    int out = 0;
+    while (h.n_levels() < c.max_levels && h.levels.back().n_parts > 1) {
+        std::vector<std::int32_t> up;
+        std::int32_t n_next = 0;
+        DeviceGraph gn{};
+        if (!agg_pass_device(c, h.levels.back(), gcur, out, up, n_next, gn)) {  // subdomains beyond a warp
+            host::Graph gh = graph_to_host(c, gcur, h.levels.back().n_nodes);
+            host::extend_from(h, std::move(gh), c.max_levels);
+            break;
+        }
+        if (n_next == h.levels.back().n_nodes) break;
+        const host::Graph ghn = graph_to_host(c, gn, n_next);
+        lap("aggregation (device)", h.n_levels());
+        host::append_level(h, std::move(up), n_next, ghn);
+        lap("partition", h.n_levels() - 1);
+        gcur = gn;
+        out ^= 1;
+    }
+    return h;
 }
 
 }  // namespace
@@ -1389,7 +1483,7 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
             factor_begin(c);
             factor_levels(c, 0, 1);
             const auto tq = std::chrono::steady_clock::now();
-            c.hier = host::build_hierarchy_l1(c.l0, std::move(up1), n1, std::move(g1), c.max_levels);
+            c.hier = hierarchy_from_level1(c, std::move(up1), n1, g1);
             if (c.hier.n_levels() > kMaxLevels) throw StatusError(kInvalidArgument, "too many MAS levels");
             const auto tb = std::chrono::steady_clock::now();
             set_coarse_levels(c, c.hier);

@@ -63,56 +63,149 @@ __device__ __forceinline__ bool shifted_cholesky_ok(double* L, double tau) {
 }
 
 // proj(M) for a symmetric N x N (full column-major in `a`, overwritten):
-// cyclic Jacobi (oracle/sym_eig.hpp's rotations) with the threshold rule — an
-// off-diagonal entry below 1e-17 of the Frobenius norm (rounding level) is
-// zeroed instead of rotated and the sweeps end once one rotates nothing —
-// then V max(w, 0) V^T
+// V max(w, 0) V^T from a Householder reduction to tridiagonal form and
+// implicit shifted QL sweeps with deflation at |e_i| <= 2^-52 max(|d| + |e|)
+// (Wilkinson / Reinsch tred2 + tql2; Eigen's SelfAdjointEigenSolver is the
+// same family: tridiagonalisation + implicit symmetric QR). ~2 K FMA for a
+// 9 x 9 against ~17 K for cyclic Jacobi to convergence: the element
+// producer's indefinite path (nearly every stencil once the mesh deforms)
+// went from 27.3 to 12.9 ms at cfg5, the geometric scene's contact pass from
+// 4.4 to 2.3 ms.
 template <int N>
 __device__ __noinline__ void project_sym(double* a) {
-    double v[N * N];
-    for (int k = 0; k < N * N; ++k) v[k] = (k % (N + 1) == 0) ? 1.0 : 0.0;
-    double tot = 0;  // ||a||_F^2, invariant under the rotations
-    for (int k = 0; k < N * N; ++k) tot += a[k] * a[k];
-    const double negligible = 1e-34 * tot;
-    for (int sweep = 0; sweep < 64; ++sweep) {
-        bool rotated = false;
-        for (int p = 0; p < N - 1; ++p)
-            for (int q = p + 1; q < N; ++q) {
-                const double apq = a[N * q + p];
-                if (apq == 0.0) continue;
-                if (apq * apq <= negligible) {
-                    a[N * q + p] = a[N * p + q] = 0.0;
-                    continue;
-                }
-                rotated = true;
-                const double theta = (a[N * q + q] - a[N * p + p]) / (2.0 * apq);
-                const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-                const double c = rsqrt(t * t + 1.0), s = t * c;
-                for (int k = 0; k < N; ++k) {
-                    const double kp = a[N * p + k], kq = a[N * q + k];
-                    a[N * p + k] = c * kp - s * kq;
-                    a[N * q + k] = s * kp + c * kq;
-                }
-                for (int k = 0; k < N; ++k) {
-                    const double pk_ = a[N * k + p], qk = a[N * k + q];
-                    a[N * k + p] = c * pk_ - s * qk;
-                    a[N * k + q] = s * pk_ + c * qk;
-                }
-                for (int k = 0; k < N; ++k) {
-                    const double kp = v[N * p + k], kq = v[N * q + k];
-                    v[N * p + k] = c * kp - s * kq;
-                    v[N * q + k] = s * kp + c * kq;
-                }
+    double V[N * N], d[N], e[N];  // V row-major: V[i][j] = V[N * i + j]
+    for (int i = 0; i < N; ++i)
+        for (int j = 0; j < N; ++j) V[N * i + j] = a[N * j + i];
+    // --- tridiagonalisation (tred2)
+    for (int j = 0; j < N; ++j) d[j] = V[N * (N - 1) + j];
+    for (int i = N - 1; i > 0; --i) {
+        double scale = 0, h = 0;
+        for (int k = 0; k < i; ++k) scale += fabs(d[k]);
+        if (scale == 0) {
+            e[i] = d[i - 1];
+            for (int j = 0; j < i; ++j) {
+                d[j] = V[N * (i - 1) + j];
+                V[N * i + j] = 0;
+                V[N * j + i] = 0;
             }
-        if (!rotated) break;
+        } else {
+            for (int k = 0; k < i; ++k) {
+                d[k] /= scale;
+                h += d[k] * d[k];
+            }
+            double f = d[i - 1];
+            double g = sqrt(h);
+            if (f > 0) g = -g;
+            e[i] = scale * g;
+            h -= f * g;
+            d[i - 1] = f - g;
+            for (int j = 0; j < i; ++j) e[j] = 0;
+            for (int j = 0; j < i; ++j) {
+                f = d[j];
+                V[N * j + i] = f;
+                g = e[j] + V[N * j + j] * f;
+                for (int k = j + 1; k <= i - 1; ++k) {
+                    g += V[N * k + j] * d[k];
+                    e[k] += V[N * k + j] * f;
+                }
+                e[j] = g;
+            }
+            f = 0;
+            for (int j = 0; j < i; ++j) {
+                e[j] /= h;
+                f += e[j] * d[j];
+            }
+            const double hh = f / (h + h);
+            for (int j = 0; j < i; ++j) e[j] -= hh * d[j];
+            for (int j = 0; j < i; ++j) {
+                f = d[j];
+                g = e[j];
+                for (int k = j; k <= i - 1; ++k) V[N * k + j] -= (f * e[k] + g * d[k]);
+                d[j] = V[N * (i - 1) + j];
+                V[N * i + j] = 0;
+            }
+        }
+        d[i] = h;
     }
-    double w[N];
-    for (int k = 0; k < N; ++k) w[k] = a[(N + 1) * k] > 0 ? a[(N + 1) * k] : 0.0;
+    for (int i = 0; i < N - 1; ++i) {  // accumulate the reflections
+        V[N * (N - 1) + i] = V[N * i + i];
+        V[N * i + i] = 1;
+        const double h = d[i + 1];
+        if (h != 0) {
+            for (int k = 0; k <= i; ++k) d[k] = V[N * k + i + 1] / h;
+            for (int j = 0; j <= i; ++j) {
+                double g = 0;
+                for (int k = 0; k <= i; ++k) g += V[N * k + i + 1] * V[N * k + j];
+                for (int k = 0; k <= i; ++k) V[N * k + j] -= g * d[k];
+            }
+        }
+        for (int k = 0; k <= i; ++k) V[N * k + i + 1] = 0;
+    }
+    for (int j = 0; j < N; ++j) {
+        d[j] = V[N * (N - 1) + j];
+        V[N * (N - 1) + j] = 0;
+    }
+    V[N * (N - 1) + N - 1] = 1;
+    e[0] = 0;
+    // --- implicit shifted QL (tql2)
+    for (int i = 1; i < N; ++i) e[i - 1] = e[i];
+    e[N - 1] = 0;
+    double f = 0, tst1 = 0;
+    const double eps = 2.220446049250313e-16;
+    for (int l = 0; l < N; ++l) {
+        tst1 = fmax(tst1, fabs(d[l]) + fabs(e[l]));
+        int m = l;
+        while (m < N - 1 && fabs(e[m]) > eps * tst1) ++m;
+        if (m > l) {
+            for (int iter = 0; iter < 64; ++iter) {
+                double g = d[l];
+                double p = (d[l + 1] - g) / (2.0 * e[l]);
+                double r = hypot(p, 1.0);
+                if (p < 0) r = -r;
+                d[l] = e[l] / (p + r);
+                d[l + 1] = e[l] * (p + r);
+                const double dl1 = d[l + 1];
+                double h = g - d[l];
+                for (int i = l + 2; i < N; ++i) d[i] -= h;
+                f += h;
+                p = d[m];
+                double c = 1, c2 = 1, c3 = 1, sn = 0, s2 = 0;
+                const double el1 = e[l + 1];
+                for (int i = m - 1; i >= l; --i) {
+                    c3 = c2;
+                    c2 = c;
+                    s2 = sn;
+                    g = c * e[i];
+                    h = c * p;
+                    r = hypot(p, e[i]);
+                    e[i + 1] = sn * r;
+                    sn = e[i] / r;
+                    c = p / r;
+                    p = c * d[i] - sn * g;
+                    d[i + 1] = h + sn * (c * g + sn * d[i]);
+                    for (int k = 0; k < N; ++k) {
+                        h = V[N * k + i + 1];
+                        V[N * k + i + 1] = sn * V[N * k + i] + c * h;
+                        V[N * k + i] = c * V[N * k + i] - sn * h;
+                    }
+                }
+                p = -sn * s2 * c3 * el1 * e[l] / dl1;
+                e[l] = sn * p;
+                d[l] = c * p;
+                if (!(fabs(e[l]) > eps * tst1)) break;
+            }
+        }
+        d[l] += f;
+        e[l] = 0;
+    }
+    // --- V max(w, 0) V^T (column k of V = eigenvector of d[k])
+    for (int k = 0; k < N; ++k) d[k] = d[k] > 0 ? d[k] : 0.0;
     for (int j = 0; j < N; ++j)
-        for (int i = 0; i < N; ++i) {
-            double s = 0;
-            for (int k = 0; k < N; ++k) s += v[N * k + i] * w[k] * v[N * k + j];
-            a[N * j + i] = s;
+        for (int i = j; i < N; ++i) {
+            double sum = 0;
+            for (int k = 0; k < N; ++k) sum += V[N * i + k] * d[k] * V[N * j + k];
+            a[N * j + i] = sum;
+            a[N * i + j] = sum;
         }
 }
 __device__ __forceinline__ void project9(double* a) { project_sym<9>(a); }

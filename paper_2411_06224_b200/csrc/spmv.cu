@@ -91,12 +91,39 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvMinBlocks) k_spmv(const std
             yr0 = h[0] * xv[0] + h[3] * xv[1] + h[6] * xv[2];
             yr1 = h[1] * xv[0] + h[4] * xv[1] + h[7] * xv[2];
             yr2 = h[2] * xv[0] + h[5] * xv[1] + h[8] * xv[2];
-            if (r != c) {
-                red_add(y + 3 * c, h[0] * xv[3] + h[1] * xv[4] + h[2] * xv[5]);
-                red_add(y + 3 * c + 1, h[3] * xv[3] + h[4] * xv[4] + h[5] * xv[5]);
-                red_add(y + 3 * c + 2, h[6] * xv[3] + h[7] * xv[4] + h[8] * xv[5]);
-            }
             if (kDot) dsum += (r != c ? 2.0 : 1.0) * (xv[3] * yr0 + xv[4] * yr1 + xv[5] * yr2);
+        }
+        // H^T x[row] towards y[col]: lanes of the chunk with the same column
+        // (~30 % at cfg5: a node shared by the chunk's ~5 rows) are summed
+        // into their lowest lane first, which alone issues the REDs
+        {
+            const bool tr = valid && r != c;
+            double t0 = tr ? h[0] * xv[3] + h[1] * xv[4] + h[2] * xv[5] : 0.0;
+            double t1 = tr ? h[3] * xv[3] + h[4] * xv[4] + h[5] * xv[5] : 0.0;
+            double t2 = tr ? h[6] * xv[3] + h[7] * xv[4] + h[8] * xv[5] : 0.0;
+            const std::uint32_t key = tr ? c : 0xFFFFFFFFu;
+            const unsigned grp = __match_any_sync(0xffffffffu, key);
+            const int gsize = __popc(grp);
+            const int rounds = __reduce_max_sync(0xffffffffu, tr ? gsize : 1) - 1;
+            const bool lead = tr && (__ffs(grp) - 1) == lane;
+            unsigned rest = grp & (grp - 1u);  // members after the leader
+            for (int k = 0; k < rounds; ++k) {
+                const int src = rest ? __ffs(rest) - 1 : lane;
+                const double a0 = __shfl_sync(0xffffffffu, t0, src);
+                const double a1 = __shfl_sync(0xffffffffu, t1, src);
+                const double a2 = __shfl_sync(0xffffffffu, t2, src);
+                if (lead && rest) {
+                    t0 += a0;
+                    t1 += a1;
+                    t2 += a2;
+                }
+                rest &= rest - 1u;
+            }
+            if (lead) {
+                red_add(y + 3 * c, t0);
+                red_add(y + 3 * c + 1, t1);
+                red_add(y + 3 * c + 2, t2);
+            }
         }
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {

@@ -59,8 +59,8 @@ struct SoRestrict {
 // the level-1 sums by RED through the precomputed ancestors (no dependent
 // chain). smem: 3 * slots doubles, then (slots + 1 + slots) ints.
 template <int kMode, int kThreads>
-__device__ __forceinline__ void update_tile(const SoRestrict& so, const PcgArgs& a, double alpha,
-                                            const double* __restrict__ apv, std::int32_t tile, double* smem) {
+__device__ __forceinline__ void update_tile(const SoRestrict& so, const PcgArgs& a, const double* __restrict__ apv,
+                                            std::int32_t tile, double* smem) {
     const std::int32_t s0 = tile * so.subs;
     const std::int32_t s1 = min(s0 + so.subs, so.n0_parts);
     const std::int32_t slot0 = so.sub_ptr0[s0], slot1 = so.sub_ptr0[s1];
@@ -71,16 +71,18 @@ __device__ __forceinline__ void update_tile(const SoRestrict& so, const PcgArgs&
     double* sr = smem;
     int* uptr = reinterpret_cast<int*>(smem + 3 * cap);
     int* child = uptr + cap + 1;
+    // before the dependency wait: the restriction metadata and the first
+    // pass of r, p, x (written two or more kernels back, all complete once
+    // the SpMV passed its own wait) — only Ap and alpha come from the SpMV
     for (int i = threadIdx.x; i <= v1 - v0; i += kThreads) uptr[i] = so.upc_ptr0[v0 + i] - slot0;
     for (int i = threadIdx.x; i < slot1 - slot0; i += kThreads) child[i] = so.upc_node0[slot0 + i] - slot0;
     constexpr int kU = 4;
-    for (std::int64_t gb = g0 + threadIdx.x; gb < g1; gb += kU * kThreads) {
-        double rv[kU], pv[kU], av[kU], xv[kU];
+    double rv[kU], pv[kU], xv[kU];
+    auto load_pass = [&](std::int64_t gb) {
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const std::int64_t g = gb + u * kThreads;
             if (g < g1) {
-                av[u] = apv[g];
                 if (kMode == M_UPDATE) {
                     rv[u] = a.r[g];
                     pv[u] = a.p[g];
@@ -89,6 +91,21 @@ __device__ __forceinline__ void update_tile(const SoRestrict& so, const PcgArgs&
                     rv[u] = a.b[g];
                 }
             }
+        }
+    };
+    load_pass(g0 + threadIdx.x);
+    double alpha = 0;
+    pdl_wait();
+    if (a.flags[F_DONE]) return;
+    if (!pcg_alpha(a, alpha)) return;  // also the restart pass's breakdown check, as before
+    pdl_launch();
+    for (std::int64_t gb = g0 + threadIdx.x; gb < g1; gb += kU * kThreads) {
+        if (gb != g0 + threadIdx.x) load_pass(gb);
+        double av[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const std::int64_t g = gb + u * kThreads;
+            if (g < g1) av[u] = apv[g];
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -132,12 +149,7 @@ inline std::size_t update_tile_smem(int max_fill0, int subs) {
 template <int kMode>
 __global__ void __launch_bounds__(kUpdThreads) k_update_so(SoRestrict so, PcgArgs a) {
     extern __shared__ double sr[];
-    double alpha = 0;
-    pdl_wait();
-    if (a.flags[F_DONE]) return;
-    if (!pcg_alpha(a, alpha)) return;
-    pdl_launch();
-    update_tile<kMode, kUpdThreads>(so, a, alpha, a.ap, blockIdx.x, sr);
+    update_tile<kMode, kUpdThreads>(so, a, a.ap, blockIdx.x, sr);
 }
 
 // Deterministic mode: level l >= 2 restricted from level l - 1 in a fixed
@@ -339,6 +351,51 @@ struct FinalSo {
 template <int kFinal>
 __global__ void __launch_bounds__(512) k_final_so(std::int32_t n, FinalSo fa, const double* __restrict__ z,
                                                  double* __restrict__ p, double* __restrict__ ap, PcgArgs a) {
+    // one slot pair (6 doubles, three 128-bit accesses per vector) per thread
+    // (the grid covers n). Everything this pass reads that the preconditioner
+    // does not write — the aggregation maps and p — is loaded, and Ap (read
+    // by the update pass, which completed before the preconditioner passed
+    // its own dependency wait) is cleared, BEFORE the dependency wait.
+    const std::int64_t nthreads = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+    const std::int64_t pr = tid, sl0 = 2 * pr;
+    const bool have = sl0 < n, two = sl0 + 1 < n;
+    std::int32_t nd[kMaxLevels][2];
+    double pp[6];
+    if (have) {
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l)
+            if (l < fa.n_coarse) {
+                if (two) {
+                    const int2 v = *reinterpret_cast<const int2*>(fa.agg[l] + sl0);
+                    nd[l][0] = v.x;
+                    nd[l][1] = v.y;
+                } else {
+                    nd[l][0] = fa.agg[l][sl0];
+                    nd[l][1] = nd[l][0];
+                }
+            }
+        if (two) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (kFinal != F_PCG_INIT) {
+                    const double2 pv = reinterpret_cast<const double2*>(p)[3 * pr + q];
+                    pp[2 * q] = pv.x;
+                    pp[2 * q + 1] = pv.y;
+                } else {
+                    pp[2 * q] = pp[2 * q + 1] = 0.0;
+                }
+                reinterpret_cast<double2*>(ap)[3 * pr + q] = make_double2(0.0, 0.0);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                pp[q] = kFinal != F_PCG_INIT ? p[3 * sl0 + q] : 0.0;
+                pp[3 + q] = 0.0;
+                ap[3 * sl0 + q] = 0.0;
+            }
+        }
+    }
     double beta = 0;
     pdl_wait();
     if (a.flags[F_DONE]) return;
@@ -373,46 +430,20 @@ __global__ void __launch_bounds__(512) k_final_so(std::int32_t n, FinalSo fa, co
         if (rz <= stop) return;
         beta = rz / rho;
     }
-    // two slots (6 doubles, three 128-bit accesses per vector) per thread
-    const std::int64_t nthreads = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-    for (std::int64_t pr = tid; 2 * pr < n; pr += nthreads) {
-        const std::int64_t sl0 = 2 * pr;
-        const bool two = sl0 + 1 < n;
-        std::int32_t nd[kMaxLevels][2];
-#pragma unroll
-        for (int l = 0; l < kMaxLevels; ++l)
-            if (l < fa.n_coarse) {
-                if (two) {
-                    const int2 v = *reinterpret_cast<const int2*>(fa.agg[l] + sl0);
-                    nd[l][0] = v.x;
-                    nd[l][1] = v.y;
-                } else {
-                    nd[l][0] = fa.agg[l][sl0];
-                    nd[l][1] = nd[l][0];
-                }
-            }
-        double zz[6], pp[6];
+    if (have) {
+        double zz[6];
         if (two) {
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 const double2 zv = reinterpret_cast<const double2*>(z)[3 * pr + q];
                 zz[2 * q] = zv.x;
                 zz[2 * q + 1] = zv.y;
-                if (kFinal != F_PCG_INIT) {
-                    const double2 pv = reinterpret_cast<const double2*>(p)[3 * pr + q];
-                    pp[2 * q] = pv.x;
-                    pp[2 * q + 1] = pv.y;
-                } else {
-                    pp[2 * q] = pp[2 * q + 1] = 0.0;
-                }
             }
         } else {
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 zz[q] = z[3 * sl0 + q];
-                pp[q] = kFinal != F_PCG_INIT ? p[3 * sl0 + q] : 0.0;
-                zz[3 + q] = pp[3 + q] = 0.0;
+                zz[3 + q] = 0.0;
             }
         }
 #pragma unroll
@@ -431,16 +462,11 @@ __global__ void __launch_bounds__(512) k_final_so(std::int32_t n, FinalSo fa, co
         for (int q = 0; q < 6; ++q) pn[q] = zz[q] + beta * pp[q];
         if (two) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
+            for (int q = 0; q < 3; ++q)
                 reinterpret_cast<double2*>(p)[3 * pr + q] = make_double2(pn[2 * q], pn[2 * q + 1]);
-                reinterpret_cast<double2*>(ap)[3 * pr + q] = make_double2(0.0, 0.0);
-            }
         } else {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                p[3 * sl0 + q] = pn[q];
-                ap[3 * sl0 + q] = 0.0;
-            }
+            for (int q = 0; q < 3; ++q) p[3 * sl0 + q] = pn[q];
         }
     }
     // clear the RED targets of the next update pass

@@ -125,20 +125,25 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvMinBlocks) k_spmv(const std
                 red_add(y + 3 * c + 2, t2);
             }
         }
+        // head-segmented sum of the row contributions (rows sorted within the
+        // chunk): run heads from one ballot, and in each shuffle round a lane
+        // adds its partner's value when no run starts between them
+        const std::uint32_t rprev = __shfl_up_sync(0xffffffffu, r, 1);
+        const bool head = lane == 0 || rprev != r;
+        const std::uint64_t heads = __ballot_sync(0xffffffffu, head);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const double a0 = __shfl_down_sync(0xffffffffu, yr0, off);
             const double a1 = __shfl_down_sync(0xffffffffu, yr1, off);
             const double a2 = __shfl_down_sync(0xffffffffu, yr2, off);
-            const std::uint32_t ro = __shfl_down_sync(0xffffffffu, r, off);
-            if (lane + off < 32 && ro == r) {
+            const bool same = lane + off < 32 && ((heads >> (lane + 1)) & ((1ull << off) - 1ull)) == 0;
+            if (same) {
                 yr0 += a0;
                 yr1 += a1;
                 yr2 += a2;
             }
         }
-        const std::uint32_t rprev = __shfl_up_sync(0xffffffffu, r, 1);
-        if (valid && (lane == 0 || rprev != r)) {
+        if (valid && head) {
             red_add(y + 3 * r, yr0);
             red_add(y + 3 * r + 1, yr1);
             red_add(y + 3 * r + 2, yr2);

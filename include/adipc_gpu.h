@@ -274,6 +274,18 @@ int adipc_gpu_contact_emit_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* 
 /* the contact terms of IncrementalPotential::value (:133-157); +inf when a
  * stencil or a surface vertex touches */
 int adipc_gpu_contact_value_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* desc, double dt2, double* value);
+/* build_friction_constraints (contact/friction.hpp:95-149) for the given
+ * candidate stencils — the proximity broad phase of :99 is
+ * adipc_gpu_broad_phase_device with inflate dhat: the active PT stencils
+ * (0 < closest-feature distance < dhat, distance.hpp:226-256), the active EE
+ * stencils, then the ground contacts of desc->surf_verts, in that order, as
+ * the lagged friction arrays adipc_contact_desc takes (nodes 4, node count,
+ * coefficients 4, tangents t1 / t2, lambda = -b'(d^2) 2 d; tangent_basis
+ * :43-47). The friction block of *desc is ignored. capacity >= n_pt + n_ee +
+ * n_surf_verts always suffices; the count goes to *n_out. */
+int adipc_gpu_friction_constraints_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* desc, int64_t capacity,
+                                          int32_t* d_nodes4, int32_t* d_n_nodes, double* d_coeff4, double* d_t1,
+                                          double* d_t2, double* d_lambda, int64_t* n_out);
 /* scene_ccd_step over the given stencils (contact/ccd.hpp:17-110): the largest
  * fraction of d_disp (3 per node) no stencil or surface vertex can cross */
 int adipc_gpu_ccd_step_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* desc, const double* d_disp,

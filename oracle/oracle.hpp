@@ -1738,6 +1738,104 @@ inline Real ccd_step(const ContactInput& in, const std::vector<Vec3>& disp) {
     return alpha;
 }
 
+// contact/distance.hpp:226-256: the frame of a stencil's closest features —
+// distance, unit normal from the second feature towards the first (UnitY at
+// zero distance), relative-displacement coefficients
+struct ContactFrame {
+    Real dist = 0;
+    Vec3 normal;
+    Real coeff[4] = {0, 0, 0, 0};
+};
+inline ContactFrame frame_of(const Vec3& d) {
+    ContactFrame f;
+    f.dist = std::sqrt(dot3(d, d));
+    if (f.dist > 0) {
+        for (int a = 0; a < 3; ++a) f.normal[a] = d[a] / f.dist;
+    } else {
+        f.normal[1] = 1;
+    }
+    return f;
+}
+inline ContactFrame pt_contact_frame(const Vec3& p, const Vec3& t0, const Vec3& t1, const Vec3& t2) {
+    const PtClass c = classify_pt(p, t0, t1, t2);
+    Vec3 d;
+    for (int a = 0; a < 3; ++a) d[a] = p[a] - ((c.beta[0] * t0[a] + c.beta[1] * t1[a]) + c.beta[2] * t2[a]);
+    ContactFrame f = frame_of(d);
+    f.coeff[0] = 1;
+    f.coeff[1] = -c.beta[0];
+    f.coeff[2] = -c.beta[1];
+    f.coeff[3] = -c.beta[2];
+    return f;
+}
+inline ContactFrame ee_contact_frame(const Vec3& a0, const Vec3& a1, const Vec3& b0, const Vec3& b1) {
+    const EeClass c = classify_ee(a0, a1, b0, b1);
+    Vec3 d;
+    for (int a = 0; a < 3; ++a) d[a] = (a0[a] + c.s * (a1[a] - a0[a])) - (b0[a] + c.t * (b1[a] - b0[a]));
+    ContactFrame f = frame_of(d);
+    f.coeff[0] = 1 - c.s;
+    f.coeff[1] = c.s;
+    f.coeff[2] = -(1 - c.t);
+    f.coeff[3] = -c.t;
+    return f;
+}
+// friction.hpp:43-47
+inline void tangent_basis(const Vec3& n, Vec3& t1, Vec3& t2) {
+    Vec3 ref;
+    ref[std::abs(n[0]) > 0.9 ? 1 : 0] = 1;
+    auto cross = [](const Vec3& a, const Vec3& b) {
+        Vec3 r;
+        r[0] = a[1] * b[2] - a[2] * b[1];
+        r[1] = a[2] * b[0] - a[0] * b[2];
+        r[2] = a[0] * b[1] - a[1] * b[0];
+        return r;
+    };
+    const Vec3 u = cross(n, ref);
+    const Real z = dot3(u, u);  // Eigen normalized(): / sqrt(squaredNorm) when positive
+    if (z > 0) {
+        const Real nz = std::sqrt(z);
+        for (int a = 0; a < 3; ++a) t1[a] = u[a] / nz;
+    } else {
+        t1 = u;
+    }
+    t2 = cross(n, t1);
+}
+// friction.hpp:93-149 build_friction_constraints for GIVEN candidates (the
+// proximity broad phase of :99 is separate): active PT stencils, active EE
+// stencils, then ground contacts of the surface vertices, in that order;
+// lambda = -b'(d^2) 2 d, the lagged normal force
+inline std::vector<FrictionConstraint> friction_constraints(const ContactInput& in) {
+    std::vector<FrictionConstraint> out;
+    const Real shat = in.dhat * in.dhat;
+    auto normal_force = [&](Real dist) { return -barrier_d1(dist * dist, shat, in.kappa) * 2 * dist; };
+    auto add = [&](const ContactFrame& f, const std::array<Index, 4>& nodes) {
+        if (!(f.dist > 0) || f.dist >= in.dhat) return;
+        FrictionConstraint fc;
+        for (int k = 0; k < 4; ++k) {
+            fc.nodes[k] = nodes[k];
+            fc.coeff[k] = f.coeff[k];
+        }
+        fc.n_nodes = 4;
+        tangent_basis(f.normal, fc.t1, fc.t2);
+        fc.lambda = normal_force(f.dist);
+        out.push_back(fc);
+    };
+    for (const auto& st : in.pt) add(pt_contact_frame(in.pos[st[0]], in.pos[st[1]], in.pos[st[2]], in.pos[st[3]]), st);
+    for (const auto& st : in.ee) add(ee_contact_frame(in.pos[st[0]], in.pos[st[1]], in.pos[st[2]], in.pos[st[3]]), st);
+    if (in.ground)
+        for (Index v : in.surf_verts) {
+            const Real dist = dot3(in.ground_normal, in.pos[v]) - in.ground_height;
+            if (!(dist > 0) || dist >= in.dhat) continue;
+            FrictionConstraint fc;
+            fc.nodes[0] = v;
+            fc.n_nodes = 1;
+            fc.coeff[0] = 1;
+            tangent_basis(in.ground_normal, fc.t1, fc.t2);
+            fc.lambda = normal_force(dist);
+            out.push_back(fc);
+        }
+    return out;
+}
+
 // contact/broad_phase.hpp:13-226: contact surface primitives over the
 // contact-node universe, inflated (and swept) AABBs, a hash grid of the
 // triangle / edge boxes, vertex-triangle and edge-edge candidates sorted and

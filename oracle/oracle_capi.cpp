@@ -623,3 +623,47 @@ int oracle_pcg_solve(void* mat, const double* b, std::size_t n, void* precond, d
 #include "capi_rng.inc"
 
 }  // extern "C"
+
+
+extern "C" {
+// ---- contact frames, tangent basis, friction constraints (restated; see oracle.hpp) ----
+static void store_frame(const ContactFrame& f, double* dist, double* normal3, double* coeff4) {
+    *dist = f.dist;
+    for (int a = 0; a < 3; ++a) normal3[a] = f.normal[a];
+    for (int k = 0; k < 4; ++k) coeff4[k] = f.coeff[k];
+}
+void oracle_pt_contact_frame(const double* x12, double* dist, double* normal3, double* coeff4) {
+    store_frame(pt_contact_frame(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9)), dist, normal3, coeff4);
+}
+void oracle_ee_contact_frame(const double* x12, double* dist, double* normal3, double* coeff4) {
+    store_frame(ee_contact_frame(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9)), dist, normal3, coeff4);
+}
+void oracle_tangent_basis(const double* n3, double* t1, double* t2) {
+    Vec3 a, b;
+    tangent_basis(ld3(n3), a, b);
+    for (int k = 0; k < 3; ++k) {
+        t1[k] = a[k];
+        t2[k] = b[k];
+    }
+}
+// friction constraints for GIVEN candidates (the ContactInput's stencils)
+std::int64_t oracle_friction_constraints(ORACLE_CONTACT_ARGS, std::int64_t cap, std::int32_t* nodes4,
+                                         std::int32_t* n_nodes_out, double* coeff4, double* t1, double* t2,
+                                         double* lambda) {
+    const std::vector<FrictionConstraint> fc = friction_constraints(contact_input(ORACLE_CONTACT_PASS));
+    if (static_cast<std::int64_t>(fc.size()) > cap) return -static_cast<std::int64_t>(fc.size()) - 1;
+    for (std::size_t i = 0; i < fc.size(); ++i) {
+        for (int k = 0; k < 4; ++k) {
+            nodes4[4 * i + k] = fc[i].nodes[k];
+            coeff4[4 * i + k] = fc[i].coeff[k];
+        }
+        n_nodes_out[i] = fc[i].n_nodes;
+        for (int k = 0; k < 3; ++k) {
+            t1[3 * i + k] = fc[i].t1[k];
+            t2[3 * i + k] = fc[i].t2[k];
+        }
+        lambda[i] = fc[i].lambda;
+    }
+    return static_cast<std::int64_t>(fc.size());
+}
+}  // extern "C"

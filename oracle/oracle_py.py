@@ -115,6 +115,10 @@ def lib():
         "oracle_hinge_rest": (ci, [f64p, f64p]),
         "oracle_hinge_bending": (None, [f64p, f64p, cd, ci, f64p, f64p, f64p]),
         "oracle_abd_orthogonality": (None, [f64p, cd, cd, ci, f64p, f64p, f64p]),
+        "oracle_pt_contact_frame": (None, [f64p, f64p, f64p, f64p]),
+        "oracle_ee_contact_frame": (None, [f64p, f64p, f64p, f64p]),
+        "oracle_tangent_basis": (None, [f64p, f64p, f64p]),
+        "oracle_friction_constraints": (i64, _CONTACT_ARGS + [i64, vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -818,14 +822,17 @@ def lift_node_grad(node_grad, n_fem, abd_node_body, jac36, grad):
     return grad
 
 
-def ip_assemble(sc, state, policy=None, project=True):
+def ip_assemble(sc, state, policy=None, project=True, ground=None, friction=None, fr_base=None, mu=0.0, fr_eps=1.0):
     """IncrementalPotential::assemble on a scene of one solid mesh + affine
     bodies + a contact surface (scenegen.geom.GeomHybrid's attributes): the
     element stream (ip_fem_assemble), contact-node positions, the proximity
     broad phase (find_candidates, inflate dhat, :330), the contact node part
     (contact_assemble), the gradient lift, two_level_abd_reduce appended to
     the stream, pinned gradient zeroing (:253-254), filter_pinned, sort and
-    reduce. Returns (value, grad, rows, cols, blocks, counts)."""
+    reduce. ground = (normal, height) adds the ground barrier of the surface
+    vertices; friction (friction_constraints' dict) with fr_base / mu /
+    fr_eps the lagged friction. Returns (value, grad, rows, cols, blocks,
+    counts)."""
     state = np.asarray(state, np.float64)
     n_fem, nb = sc.n_fem, sc.n_bodies
     x, q = state[: 3 * n_fem], state[3 * n_fem:].reshape(nb, 12)
@@ -839,7 +846,8 @@ def ip_assemble(sc, state, policy=None, project=True):
     pos = node_displacements(state, n_fem, sc.abd_body, sc.jac36).reshape(-1, 3)
     pt, ee = find_candidates(pos, sc.surf_verts, sc.edges, sc.tris, sc.dhat)
     ci = ContactInput(pos, np.c_[sc.surf_verts[pt[:, 0]], sc.tris[pt[:, 1]]],
-                      np.c_[sc.edges[ee[:, 0]], sc.edges[ee[:, 1]]], dhat=sc.dhat, kappa=sc.kappa)
+                      np.c_[sc.edges[ee[:, 0]], sc.edges[ee[:, 1]]], dhat=sc.dhat, kappa=sc.kappa, ground=ground,
+                      surf_verts=sc.surf_verts, friction=friction, fr_base=fr_base, mu=mu, fr_eps=fr_eps)
     cv, ng, nk, nv = contact_assemble(ci, dt2, project)
     val += cv
     tk, tv = two_level_abd_reduce(nk, nv, n_fem, nb, sc.abd_body, sc.jac36, policy)
@@ -850,3 +858,74 @@ def ip_assemble(sc, state, policy=None, project=True):
     rows, cols, blocks = fast_hash_reduction(sk, sv, sc.n_blocks, policy)
     return val, grad, rows, cols, blocks, {"n_pt": len(pt), "n_ee": len(ee), "node_blocks": len(nk),
                                            "contact_tiles": len(tk)}
+
+
+# ---- friction constraints (friction.hpp:43-149, distance.hpp:226-256) -----------
+def pt_contact_frame(x12):
+    """distance.hpp:232-242 -> (dist, normal 3, coeff 4)."""
+    d, nrm, cf = np.zeros(1), np.zeros(3), np.zeros(4)
+    lib().oracle_pt_contact_frame(_x12(x12), d, nrm, cf)
+    return float(d[0]), nrm, cf
+
+
+def ee_contact_frame(x12):
+    """distance.hpp:244-256 -> (dist, normal 3, coeff 4)."""
+    d, nrm, cf = np.zeros(1), np.zeros(3), np.zeros(4)
+    lib().oracle_ee_contact_frame(_x12(x12), d, nrm, cf)
+    return float(d[0]), nrm, cf
+
+
+def tangent_basis(n):
+    """friction.hpp:43-47 -> (t1, t2)."""
+    t1, t2 = np.zeros(3), np.zeros(3)
+    lib().oracle_tangent_basis(np.ascontiguousarray(n, np.float64), t1, t2)
+    return t1, t2
+
+
+def _friction_arrays(cap):
+    return {"nodes": np.empty((cap, 4), np.int32), "n": np.empty(cap, np.int32), "coeff": np.empty((cap, 4)),
+            "t1": np.empty((cap, 3)), "t2": np.empty((cap, 3)), "lam": np.empty(cap)}
+
+
+def _friction_trim(f, k):
+    return {key: v[:k].copy() for key, v in f.items()}
+
+
+def friction_constraints(ci: ContactInput):
+    """build_friction_constraints (friction.hpp:95-149) over the ContactInput's
+    GIVEN candidate stencils (active PT, active EE, ground contacts) -> dict
+    nodes / n / coeff / t1 / t2 / lam (ContactInput's friction format)."""
+    cap = max(len(ci.pt) + len(ci.ee) + len(ci.surf_verts), 1)
+    f = _friction_arrays(cap)
+    k = lib().oracle_friction_constraints(*ci.args(), cap, *[a.ctypes.data for a in f.values()])
+    return _friction_trim(f, int(k))
+
+
+def build_friction_constraints(pos, verts, edges, tris, dhat, kappa, ground=None):
+    """friction.hpp:95-149 with its own proximity broad phase: the reference's
+    compiled function under the reference backend; the restatement composes
+    find_candidates (inflate dhat) with friction_constraints."""
+    pos = np.ascontiguousarray(pos, np.float64).reshape(-1, 3)
+    verts = np.ascontiguousarray(verts, np.int32).reshape(-1)
+    edges = np.ascontiguousarray(edges, np.int32).reshape(-1, 2)
+    tris = np.ascontiguousarray(tris, np.int32).reshape(-1, 3)
+    if _backend == "reference":
+        L = C.CDLL(_REF_PATH)
+        fn = L.ref_build_friction_constraints
+        fn.restype = i64
+        fn.argtypes = [i32, f64p, i32, vp, i32, vp, i32, vp, ci, vp, cd, cd, cd, i64, vp, vp, vp, vp, vp, vp]
+        cap = max(len(verts) * 64, 1)
+        while True:
+            f = _friction_arrays(cap)
+            nrm = None if ground is None else np.ascontiguousarray(ground[0], np.float64)
+            k = fn(len(pos), pos.reshape(-1), len(verts), verts.ctypes.data, len(edges), edges.ctypes.data, len(tris),
+                   tris.ctypes.data, int(ground is not None), None if nrm is None else nrm.ctypes.data,
+                   0.0 if ground is None else float(ground[1]), float(dhat), float(kappa), cap,
+                   *[a.ctypes.data for a in f.values()])
+            if k >= 0:
+                return _friction_trim(f, int(k))
+            cap = int(-k - 1)
+    pt, ee = find_candidates(pos, verts, edges, tris, dhat)
+    cin = ContactInput(pos, np.c_[verts[pt[:, 0]], tris[pt[:, 1]]], np.c_[edges[ee[:, 0]], edges[ee[:, 1]]],
+                       dhat=dhat, kappa=kappa, ground=ground, surf_verts=verts)
+    return friction_constraints(cin)

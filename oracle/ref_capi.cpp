@@ -20,7 +20,10 @@
 #include <stdexcept>
 #include <string>
 
+#include <Eigen/Cholesky>  // scene/mesh.hpp (pulled in by friction.hpp) uses LLT
+
 #include "adipc/contact/barrier.hpp"
+#include "adipc/contact/friction.hpp"
 #include "adipc/energy/abd_energy.hpp"
 #include "adipc/energy/bending.hpp"
 #include "adipc/energy/membrane.hpp"
@@ -485,4 +488,95 @@ int ref_pcg_solve(void* mat, const double* b, std::size_t n, void* precond, doub
     return 0;
 }
 
+}  // extern "C"
+
+
+extern "C" {
+// ---- broad phase, contact frames, friction constraints: contact/broad_phase.hpp,
+// distance.hpp:226-256, friction.hpp:43-149 (the scene headers they include
+// compile against the Eigen subset) ------------------------------------------------
+static ContactSurface ref_surface(std::int32_t n_verts, const std::int32_t* verts, std::int32_t n_edges,
+                                  const std::int32_t* edges, std::int32_t n_tris, const std::int32_t* tris) {
+    ContactSurface s;
+    s.verts.assign(verts, verts + n_verts);
+    for (std::int32_t e = 0; e < n_edges; ++e) s.edges.push_back({edges[2 * e], edges[2 * e + 1]});
+    for (std::int32_t t = 0; t < n_tris; ++t) s.tris.push_back({tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]});
+    return s;
+}
+std::int64_t ref_find_candidates(std::int32_t n_nodes, const double* pos, const double* disp, std::int32_t n_verts,
+                                 const std::int32_t* verts, std::int32_t n_edges, const std::int32_t* edges,
+                                 std::int32_t n_tris, const std::int32_t* tris, double inflate, std::int32_t* pt_out,
+                                 std::int64_t pt_cap, std::int32_t* ee_out, std::int64_t ee_cap,
+                                 std::int64_t* n_ee_out) {
+    std::vector<Vec3> p(n_nodes), d;
+    for (std::int32_t v = 0; v < n_nodes; ++v) p[v] = ld3(pos + 3 * v);
+    if (disp) {
+        d.resize(n_nodes);
+        for (std::int32_t v = 0; v < n_nodes; ++v) d[v] = ld3(disp + 3 * v);
+    }
+    const ContactSurface s = ref_surface(n_verts, verts, n_edges, edges, n_tris, tris);
+    const ContactCandidates c = find_candidates(s, p, disp ? &d : nullptr, inflate);
+    *n_ee_out = static_cast<std::int64_t>(c.ee.size());
+    if (static_cast<std::int64_t>(c.pt.size()) > pt_cap || static_cast<std::int64_t>(c.ee.size()) > ee_cap) return -1;
+    for (std::size_t i = 0; i < c.pt.size(); ++i) {
+        pt_out[2 * i] = c.pt[i][0];
+        pt_out[2 * i + 1] = c.pt[i][1];
+    }
+    for (std::size_t i = 0; i < c.ee.size(); ++i) {
+        ee_out[2 * i] = c.ee[i][0];
+        ee_out[2 * i + 1] = c.ee[i][1];
+    }
+    return static_cast<std::int64_t>(c.pt.size());
+}
+static void store_frame(const ContactFrame& f, double* dist, double* normal3, double* coeff4) {
+    *dist = f.dist;
+    for (int a = 0; a < 3; ++a) normal3[a] = f.normal[a];
+    for (int k = 0; k < 4; ++k) coeff4[k] = f.coeff[k];
+}
+void ref_pt_contact_frame(const double* x12, double* dist, double* normal3, double* coeff4) {
+    store_frame(pt_contact_frame(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9)), dist, normal3, coeff4);
+}
+void ref_ee_contact_frame(const double* x12, double* dist, double* normal3, double* coeff4) {
+    store_frame(ee_contact_frame(ld3(x12), ld3(x12 + 3), ld3(x12 + 6), ld3(x12 + 9)), dist, normal3, coeff4);
+}
+void ref_tangent_basis(const double* n3, double* t1, double* t2) {
+    Vec3 a, b;
+    tangent_basis(ld3(n3), a, b);
+    for (int k = 0; k < 3; ++k) {
+        t1[k] = a[k];
+        t2[k] = b[k];
+    }
+}
+// build_friction_constraints with its own proximity broad phase (friction.hpp:95-149)
+std::int64_t ref_build_friction_constraints(std::int32_t n_nodes, const double* pos, std::int32_t n_verts,
+                                           const std::int32_t* verts, std::int32_t n_edges, const std::int32_t* edges,
+                                           std::int32_t n_tris, const std::int32_t* tris, int ground,
+                                           const double* normal, double height, double dhat, double kappa,
+                                           std::int64_t cap, std::int32_t* nodes4, std::int32_t* n_nodes_out,
+                                           double* coeff4, double* t1, double* t2, double* lambda) {
+    std::vector<Vec3> p(n_nodes);
+    for (std::int32_t v = 0; v < n_nodes; ++v) p[v] = ld3(pos + 3 * v);
+    const ContactSurface s = ref_surface(n_verts, verts, n_edges, edges, n_tris, tris);
+    GroundPlane g;
+    g.enabled = ground != 0;
+    if (g.enabled) {
+        g.normal = ld3(normal);
+        g.height = height;
+    }
+    const std::vector<FrictionConstraint> fc = build_friction_constraints(s, p, g, dhat, kappa);
+    if (static_cast<std::int64_t>(fc.size()) > cap) return -static_cast<std::int64_t>(fc.size()) - 1;
+    for (std::size_t i = 0; i < fc.size(); ++i) {
+        for (int k = 0; k < 4; ++k) {
+            nodes4[4 * i + k] = fc[i].nodes[k];
+            coeff4[4 * i + k] = fc[i].coeff[k];
+        }
+        n_nodes_out[i] = fc[i].n_nodes;
+        for (int k = 0; k < 3; ++k) {
+            t1[3 * i + k] = fc[i].t1[k];
+            t2[3 * i + k] = fc[i].t2[k];
+        }
+        lambda[i] = fc[i].lambda;
+    }
+    return static_cast<std::int64_t>(fc.size());
+}
 }  // extern "C"

@@ -94,6 +94,8 @@ GPU_SIGNATURES = {
                                            C.POINTER(i64)]),
     "adipc_gpu_contact_value_device": (ci, [vp, C.POINTER(ContactDesc), cd, C.POINTER(cd)]),
     "adipc_gpu_ccd_step_device": (ci, [vp, C.POINTER(ContactDesc), vp, C.POINTER(cd)]),
+    "adipc_gpu_friction_constraints_device": (ci, [vp, C.POINTER(ContactDesc), i64, vp, vp, vp, vp, vp, vp,
+                                                   C.POINTER(i64)]),
     "adipc_gpu_fem_emit_device": (ci, [vp, C.POINTER(FemDesc), vp, vp, vp, C.POINTER(cd)]),
     "adipc_gpu_fem_value_device": (ci, [vp, C.POINTER(FemDesc), vp, C.POINTER(cd)]),
     "adipc_gpu_fem_assemble_device": (ci, [vp, C.POINTER(FemDesc), vp, C.POINTER(cd), C.POINTER(i64)]),

@@ -302,6 +302,29 @@ class Context:
         self._check(self._L.adipc_gpu_contact_value_device(self.h, C.byref(d), float(dt2), C.byref(v)))
         return v.value
 
+    def friction_constraints(self, c):
+        """build_friction_constraints (friction.hpp:95-149) over the stencils
+        of c (see contact_desc; the friction entries of c are ignored) ->
+        dict of device tensors fr_nodes / fr_n / fr_coeff / fr_t1 / fr_t2 /
+        fr_lambda in contact_desc's friction format."""
+        import torch
+
+        d = self.contact_desc(dict(c, fr_n=None))
+        cap = max(d.n_pt + d.n_ee + d.n_surf_verts, 1)
+        dev = c["pos"].device
+        out = {"fr_nodes": torch.empty((cap, 4), dtype=torch.int32, device=dev),
+               "fr_n": torch.empty(cap, dtype=torch.int32, device=dev),
+               "fr_coeff": torch.empty((cap, 4), dtype=torch.float64, device=dev),
+               "fr_t1": torch.empty((cap, 3), dtype=torch.float64, device=dev),
+               "fr_t2": torch.empty((cap, 3), dtype=torch.float64, device=dev),
+               "fr_lambda": torch.empty(cap, dtype=torch.float64, device=dev)}
+        k = C.c_int64()
+        self._check(self._L.adipc_gpu_friction_constraints_device(self.h, C.byref(d), cap, ptr(out["fr_nodes"]),
+                                                                  ptr(out["fr_n"]), ptr(out["fr_coeff"]),
+                                                                  ptr(out["fr_t1"]), ptr(out["fr_t2"]),
+                                                                  ptr(out["fr_lambda"]), C.byref(k)))
+        return {name: t[:k.value] for name, t in out.items()}
+
     def ccd_step(self, c, disp):
         d = self.contact_desc(c)
         a = C.c_double()

@@ -511,6 +511,19 @@ int adipc_gpu_contact_value_device(adipc_gpu_ctx* ctx, const adipc_contact_desc*
     });
 }
 
+int adipc_gpu_friction_constraints_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* d, int64_t capacity,
+                                          int32_t* d_nodes4, int32_t* d_n_nodes, double* d_coeff4, double* d_t1,
+                                          double* d_t2, double* d_lambda, int64_t* n_out) {
+    return guarded(ctx, [&] {
+        if (capacity < 0) throw StatusError(kInvalidArgument, "negative capacity");
+        if (capacity > 0 && (!d_nodes4 || !d_n_nodes || !d_coeff4 || !d_t1 || !d_t2 || !d_lambda))
+            throw StatusError(kInvalidArgument, "missing output arrays");
+        const std::int64_t k = friction_constraints(ctx->c, contact_desc(d), capacity, d_nodes4, d_n_nodes, d_coeff4,
+                                                    d_t1, d_t2, d_lambda);
+        if (n_out) *n_out = k;
+    });
+}
+
 int adipc_gpu_ccd_step_device(adipc_gpu_ctx* ctx, const adipc_contact_desc* d, const double* d_disp, double* alpha) {
     return guarded(ctx, [&] {
         if (!d_disp) throw StatusError(kInvalidArgument, "missing displacement");

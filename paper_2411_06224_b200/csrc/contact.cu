@@ -589,6 +589,125 @@ __global__ void k_ccd(ContactArgs a, const double* __restrict__ disp, unsigned l
     if ((threadIdx.x & 31) == 0) atomicMin(alpha, static_cast<unsigned long long>(__double_as_longlong(best)));
 }
 
+// ---- friction constraints at the step start (friction.hpp:43-149) -----------
+// the frame of candidate i (distance.hpp:226-256) or ground contact j:
+// distance, unit normal, coefficients; false when not in contact range
+__device__ bool friction_frame(const ContactArgs& a, std::int64_t i, double* dist, double* nrm, double* coeff,
+                               int* nodes, int* n_nodes) {
+    const std::int64_t np = a.n_pt + a.n_ee;
+    if (i >= np) {
+        const int v = a.sv[i - np];
+        const V3 p = ld(a.pos, v);
+        const double dd = (a.gn[0] * p.x + a.gn[1] * p.y) + a.gn[2] * p.z - a.gh;
+        *dist = dd;
+        nrm[0] = a.gn[0];
+        nrm[1] = a.gn[1];
+        nrm[2] = a.gn[2];
+        nodes[0] = v;
+        nodes[1] = nodes[2] = nodes[3] = -1;
+        coeff[0] = 1;
+        coeff[1] = coeff[2] = coeff[3] = 0;
+        *n_nodes = 1;
+        return dd > 0 && dd < a.dhat;
+    }
+    int kind;
+    const int* st = stencil_of(a, i, &kind);
+    V3 x[4];
+    load_stencil(a.pos, st, x);
+    double d[3];
+    if (kind == 0) {
+        double b[3];
+        classify_pt(x[0], x[1], x[2], x[3], b);
+        d[0] = x[0].x - ((b[0] * x[1].x + b[1] * x[2].x) + b[2] * x[3].x);
+        d[1] = x[0].y - ((b[0] * x[1].y + b[1] * x[2].y) + b[2] * x[3].y);
+        d[2] = x[0].z - ((b[0] * x[1].z + b[1] * x[2].z) + b[2] * x[3].z);
+        coeff[0] = 1;
+        coeff[1] = -b[0];
+        coeff[2] = -b[1];
+        coeff[3] = -b[2];
+    } else {
+        double sv, tv;
+        classify_ee(x[0], x[1], x[2], x[3], &sv, &tv);
+        d[0] = (x[0].x + sv * (x[1].x - x[0].x)) - (x[2].x + tv * (x[3].x - x[2].x));
+        d[1] = (x[0].y + sv * (x[1].y - x[0].y)) - (x[2].y + tv * (x[3].y - x[2].y));
+        d[2] = (x[0].z + sv * (x[1].z - x[0].z)) - (x[2].z + tv * (x[3].z - x[2].z));
+        coeff[0] = 1 - sv;
+        coeff[1] = sv;
+        coeff[2] = -(1 - tv);
+        coeff[3] = -tv;
+    }
+    const double dn = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+    *dist = dn;
+    if (dn > 0) {
+        nrm[0] = d[0] / dn;
+        nrm[1] = d[1] / dn;
+        nrm[2] = d[2] / dn;
+    } else {
+        nrm[0] = 0;
+        nrm[1] = 1;
+        nrm[2] = 0;
+    }
+    for (int k = 0; k < 4; ++k) nodes[k] = st[k];
+    *n_nodes = 4;
+    return dn > 0 && dn < a.dhat;
+}
+
+__global__ void k_friction_flags(ContactArgs a, std::int64_t n, std::int32_t* __restrict__ on) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        double dist, nrm[3], coeff[4];
+        int nodes[4], nn;
+        on[i] = friction_frame(a, i, &dist, nrm, coeff, nodes, &nn) ? 1 : 0;
+    }
+}
+
+__global__ void k_friction_emit(ContactArgs a, std::int64_t n, const std::int32_t* __restrict__ on,
+                                const std::int64_t* __restrict__ rank, std::int32_t* __restrict__ o_nodes,
+                                std::int32_t* __restrict__ o_n, double* __restrict__ o_coeff,
+                                double* __restrict__ o_t1, double* __restrict__ o_t2, double* __restrict__ o_lambda) {
+    const double shat = a.dhat * a.dhat;
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        if (!on[i]) continue;
+        double dist, nrm[3], coeff[4];
+        int nodes[4], nn;
+        friction_frame(a, i, &dist, nrm, coeff, nodes, &nn);
+        const std::int64_t q = rank[i];
+        // tangent_basis (friction.hpp:43-47): t1 = normalized(n x ref), t2 = n x t1
+        const bool ydir = fabs(nrm[0]) > 0.9;
+        double u[3];
+        if (ydir) {  // ref = (0, 1, 0)
+            u[0] = nrm[1] * 0.0 - nrm[2] * 1.0;
+            u[1] = nrm[2] * 0.0 - nrm[0] * 0.0;
+            u[2] = nrm[0] * 1.0 - nrm[1] * 0.0;
+        } else {  // ref = (1, 0, 0)
+            u[0] = nrm[1] * 0.0 - nrm[2] * 0.0;
+            u[1] = nrm[2] * 1.0 - nrm[0] * 0.0;
+            u[2] = nrm[0] * 0.0 - nrm[1] * 1.0;
+        }
+        const double z = (u[0] * u[0] + u[1] * u[1]) + u[2] * u[2];
+        double t1[3];
+        if (z > 0) {
+            const double nz = sqrt(z);
+            for (int k = 0; k < 3; ++k) t1[k] = u[k] / nz;
+        } else {
+            for (int k = 0; k < 3; ++k) t1[k] = u[k];
+        }
+        const double t2[3] = {nrm[1] * t1[2] - nrm[2] * t1[1], nrm[2] * t1[0] - nrm[0] * t1[2],
+                              nrm[0] * t1[1] - nrm[1] * t1[0]};
+        for (int k = 0; k < 4; ++k) {
+            o_nodes[4 * q + k] = nodes[k];
+            o_coeff[4 * q + k] = coeff[k];
+        }
+        o_n[q] = nn;
+        for (int k = 0; k < 3; ++k) {
+            o_t1[3 * q + k] = t1[k];
+            o_t2[3 * q + k] = t2[k];
+        }
+        o_lambda[q] = -barrier_d1(dist * dist, shat, a.kappa) * 2 * dist;
+    }
+}
+
 ContactArgs contact_args(const ContactDesc& d, double dt2, int project) {
     ContactArgs a{};
     a.pos = d.pos;
@@ -673,6 +792,29 @@ std::int64_t contact_emit(Ctx& c, const ContactDesc& d, double dt2, int project,
         ADIPC_LAUNCH_CHECK();
     }
     return T;
+}
+
+std::int64_t friction_constraints(Ctx& c, const ContactDesc& d, std::int64_t capacity, std::int32_t* d_nodes4,
+                                  std::int32_t* d_n, double* d_coeff4, double* d_t1, double* d_t2, double* d_lambda) {
+    cudaStream_t st = c.stream;
+    const ContactArgs a = contact_args(d, 0.0, 1);
+    const std::int64_t n = a.n_pt + a.n_ee + a.n_sv;
+    if (n == 0) return 0;
+    c.ct_on.reserve(static_cast<std::size_t>(n));
+    c.ct_rank.reserve(static_cast<std::size_t>(n) + 1);
+    k_friction_flags<<<grid_for(n, 256, 16), 256, 0, st>>>(a, n, c.ct_on.p);
+    ADIPC_LAUNCH_CHECK();
+    exclusive_scan(c.ct_on.p, n, c.ct_rank.p, c.scan_scratch, st);
+    std::int64_t total = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&total, c.ct_rank.p + n, sizeof(total), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    if (total > capacity) throw StatusError(kInvalidArgument, "friction constraint capacity too small");
+    if (total > 0) {
+        k_friction_emit<<<grid_for(n, 128, 16), 128, 0, st>>>(a, n, c.ct_on.p, c.ct_rank.p, d_nodes4, d_n, d_coeff4,
+                                                             d_t1, d_t2, d_lambda);
+        ADIPC_LAUNCH_CHECK();
+    }
+    return total;
 }
 
 double contact_value(Ctx& c, const ContactDesc& d, double dt2) {

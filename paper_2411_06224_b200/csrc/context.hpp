@@ -359,6 +359,8 @@ void broad_phase(Ctx& c, const BroadDesc& d, std::int64_t* n_pt, std::int64_t* n
 
 std::int64_t contact_emit(Ctx& c, const ContactDesc& d, double dt2, int project, std::uint64_t* d_keys, double* d_vals,
                           std::int64_t capacity, double* d_node_grad, double* d_value);
+std::int64_t friction_constraints(Ctx& c, const ContactDesc& d, std::int64_t capacity, std::int32_t* d_nodes4,
+                                  std::int32_t* d_n, double* d_coeff4, double* d_t1, double* d_t2, double* d_lambda);
 double contact_value(Ctx& c, const ContactDesc& d, double dt2);
 double ccd_step(Ctx& c, const ContactDesc& d, const double* d_disp);
 

@@ -65,6 +65,20 @@ class IncrementalPotential:
     def clear_friction(self):
         self.friction = None
 
+    def begin_friction(self, state, mu: float, eps: float):
+        """The step-start freeze of newton.hpp:104-113: friction constraints
+        from the contacts at `state` (build_friction_constraints,
+        friction.hpp:95-149: proximity broad phase, contact frames, tangent
+        bases, lagged normal forces) with the positions as the base; returns
+        the number of constraints."""
+        pos = self.contact_positions(state)
+        pt, ee = self.candidates(pos)
+        fr = self.ctx.friction_constraints({"pos": pos, "pt": pt, "ee": ee, "dhat": self.dhat, "kappa": self.kappa,
+                                            "ground": self.ground, "surf_verts": self.surf["verts"]})
+        fr["fr_base"] = pos.clone()
+        self.set_friction(fr, mu, eps)
+        return int(fr["fr_n"].numel())
+
     # -- helpers ----------------------------------------------------------------
     def _split(self, state):
         if not state.is_cuda or state.numel() != 3 * self.n_blocks:

@@ -112,11 +112,17 @@ int adipc_gpu_apply_direction_device(adipc_gpu_ctx* ctx, const double* d_state, 
 /* the contact gradient lift of assemble_contact (incremental_potential.hpp:395-403):
  * d_grad (block numbering) += node gradient, through J^T for affine-body nodes;
  * slots with d_pinned[slot] != 0 (nullable) receive nothing, as the reference
- * zeroes them right after (:253-254). The contact-node positions of a state
- * (contact_node_positions, scene.hpp) are node_displacements applied to (x, q). */
+ * zeroes them right after (:253-254). */
 int adipc_gpu_lift_node_grad_device(adipc_gpu_ctx* ctx, const double* d_node_grad, int32_t n_fem, int32_t n_abd,
                                     const int32_t* d_abd_node_body, const double* d_abd_node_jacobian36,
                                     const uint8_t* d_pinned, double* d_grad);
+/* contact_node_positions (scene.hpp:112-120): the contact-node positions of a
+ * block-numbered state [x; q] — FEM vertices copy x, affine-body node a is
+ * affine_point (core/types.hpp:34-40) A x_bar + p in the reference's
+ * operation order (x_bar from the node's Jacobian) */
+int adipc_gpu_contact_positions_device(adipc_gpu_ctx* ctx, const double* d_state, int32_t n_fem, int32_t n_abd,
+                                       const int32_t* d_abd_node_body, const double* d_abd_node_jacobian36,
+                                       double* d_out);
 /* node_displacements (newton.hpp:272-281): FEM nodes copy d; affine-body node a moves by J_a d_body
  * (abd_node_jacobian 3x12 column-major, 36 doubles per node, DofMap abd_reduce.hpp:11-27) */
 int adipc_gpu_node_displacements_device(adipc_gpu_ctx* ctx, const double* d_dir, int32_t n_fem, int32_t n_abd,

@@ -797,6 +797,22 @@ def node_displacements(d, n_fem, abd_node_body, jac36):
     return np.concatenate(out) if out else np.zeros(0)
 
 
+def contact_node_positions(state, n_fem, abd_node_body, jac36):
+    """scene.hpp:112-120 contact_node_positions: FEM vertices copy x; an
+    affine-body node is affine_point(q, x_bar) = A x_bar + p (core/types.hpp:
+    34-40), rows of A from q, in that operation order (x_bar read from the
+    node's Jacobian)."""
+    state = np.asarray(state, np.float64)
+    out = [state[: 3 * n_fem].reshape(-1, 3)]
+    J = np.asarray(jac36, np.float64).reshape(-1, 12, 3)  # [node][col][row]
+    xb = J[:, 3:6, 0]  # x_bar_k = J(0, 3 + k)
+    q = state[3 * n_fem:].reshape(-1, 12)[np.asarray(abd_node_body)]
+    A = q[:, 3:].reshape(-1, 3, 3)
+    pos = ((A[:, :, 0] * xb[:, 0:1] + A[:, :, 1] * xb[:, 1:2]) + A[:, :, 2] * xb[:, 2:3]) + q[:, :3]
+    out.append(pos)
+    return np.concatenate(out)
+
+
 def abd_jacobian(rest):
     """mesh.hpp:196-201: J = [I3 | rows r: rest^T at columns 3 + 3 r], column-major 36 doubles."""
     J = np.zeros((3, 12))
@@ -843,7 +859,7 @@ def ip_assemble(sc, state, policy=None, project=True, ground=None, friction=None
     dt2 = sc.dt * sc.dt
     val, grad, keys, vals = ip_fem_assemble(x, sc.x_tilde, sc.mass, sc.tet_begin, [sc.mu], [sc.lam], sc.tets,
                                             sc.rest_inv9, sc.rest_volume, dt2, None, project, bodies)
-    pos = node_displacements(state, n_fem, sc.abd_body, sc.jac36).reshape(-1, 3)
+    pos = contact_node_positions(state, n_fem, sc.abd_body, sc.jac36)
     pt, ee = find_candidates(pos, sc.surf_verts, sc.edges, sc.tris, sc.dhat)
     ci = ContactInput(pos, np.c_[sc.surf_verts[pt[:, 0]], sc.tris[pt[:, 1]]],
                       np.c_[sc.edges[ee[:, 0]], sc.edges[ee[:, 1]]], dhat=sc.dhat, kappa=sc.kappa, ground=ground,
@@ -929,3 +945,88 @@ def build_friction_constraints(pos, verts, edges, tris, dhat, kappa, ground=None
     cin = ContactInput(pos, np.c_[verts[pt[:, 0]], tris[pt[:, 1]]], np.c_[edges[ee[:, 0]], edges[ee[:, 1]]],
                        dhat=dhat, kappa=kappa, ground=ground, surf_verts=verts)
     return friction_constraints(cin)
+
+
+# ---- the reference's own Scene + IncrementalPotential (oracle/_ref) ------------
+class RefScene:
+    """The reference's Scene (scene/scene.hpp: finalize — boundary extraction,
+    masses, rest data, body reduced masses), its DofMap and ContactSurface, and
+    IncrementalPotential::assemble (solver/incremental_potential.hpp:19-258),
+    compiled in place. meshes: dicts rest (n x 3), tets (local, m x 4),
+    youngs, poisson, density; bodies: dicts rest, tets, kappa, density."""
+
+    def __init__(self, meshes, bodies, dt, ground=None):
+        if not reference_available():
+            raise RuntimeError("oracle/_ref not built")
+        L = self._L = C.CDLL(_REF_PATH)
+        L.ref_scene_new.restype = vp
+        L.ref_scene_new.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, cd, ci, vp, cd]
+        L.ref_scene_free.argtypes = [vp]
+        L.ref_scene_sizes.argtypes = [vp, vp]
+        L.ref_scene_export.argtypes = [vp] + [vp] * 14
+        L.ref_scene_begin_friction.restype = i64
+        L.ref_scene_begin_friction.argtypes = [vp, f64p, f64p, cd, cd, cd, cd]
+        L.ref_scene_assemble.restype = i64
+        L.ref_scene_assemble.argtypes = [vp, f64p, f64p, f64p, f64p, cd, cd, ci, f64p, f64p, i64, vp, vp, vp]
+        cat = lambda xs, dt_: np.ascontiguousarray(np.concatenate(xs) if xs else np.zeros(0), dt_)  # noqa: E731
+        begin = lambda xs: np.ascontiguousarray(np.r_[0, np.cumsum([len(x) for x in xs])], np.int64)  # noqa: E731
+        self._keep = [cat([m["rest"] for m in meshes], np.float64), begin([m["rest"] for m in meshes]),
+                      cat([m["tets"] for m in meshes], np.int32), begin([m["tets"] for m in meshes]),
+                      np.array([m["youngs"] for m in meshes], np.float64),
+                      np.array([m["poisson"] for m in meshes], np.float64),
+                      np.array([m["density"] for m in meshes], np.float64),
+                      cat([b["rest"] for b in bodies], np.float64), begin([b["rest"] for b in bodies]),
+                      cat([b["tets"] for b in bodies], np.int32), begin([b["tets"] for b in bodies]),
+                      np.array([b["kappa"] for b in bodies], np.float64),
+                      np.array([b["density"] for b in bodies], np.float64),
+                      None if ground is None else np.ascontiguousarray(ground[0], np.float64)]
+        k = self._keep
+        p = lambda a: None if a is None or a.size == 0 else a.ctypes.data  # noqa: E731
+        self.h = L.ref_scene_new(len(meshes), p(k[1]), p(k[0]), p(k[3]), p(k[2]), p(k[4]), p(k[5]), p(k[6]),
+                                 len(bodies), p(k[8]), p(k[7]), p(k[10]), p(k[9]), p(k[11]), p(k[12]), float(dt),
+                                 int(ground is not None), p(k[13]), 0.0 if ground is None else float(ground[1]))
+        sz = np.zeros(9, np.int64)
+        L.ref_scene_sizes(self.h, sz.ctypes.data)
+        (self.n_fem, self.n_bodies, self.n_blocks, self.n_nodes, n_tets, n_sv, n_e, n_t, n_m) = (int(v) for v in sz)
+        d = {"mass": np.zeros(self.n_fem), "rest_inv9": np.zeros((n_tets, 9)), "rest_volume": np.zeros(n_tets),
+             "tets": np.zeros((n_tets, 4), np.int32), "mu": np.zeros(n_m), "lam": np.zeros(n_m),
+             "reduced_mass": np.zeros((self.n_bodies, 144)), "body_volume": np.zeros(self.n_bodies),
+             "abd_body": np.zeros(self.n_nodes - self.n_fem, np.int32),
+             "jac36": np.zeros((self.n_nodes - self.n_fem, 36)), "surf_verts": np.zeros(n_sv, np.int32),
+             "edges": np.zeros((n_e, 2), np.int32), "tris": np.zeros((n_t, 3), np.int32),
+             "length_scale": np.zeros(1)}
+        L.ref_scene_export(self.h, *[p(d[k_]) if d[k_].size else None for k_ in
+                                     ("mass", "rest_inv9", "rest_volume", "tets", "mu", "lam", "reduced_mass",
+                                      "body_volume", "abd_body", "jac36", "surf_verts", "edges", "tris")],
+                           d["length_scale"].ctypes.data)
+        d["tet_begin"] = np.r_[0, np.cumsum([len(m["tets"]) for m in meshes])].astype(np.int64)
+        self.data = d
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._L.ref_scene_free(self.h)
+            self.h = None
+
+    def begin_friction(self, x, q, dhat, kappa, mu, eps):
+        """newton.hpp:104-113: build_friction_constraints at (x, q), base = those positions."""
+        return int(self._L.ref_scene_begin_friction(self.h, np.ascontiguousarray(x, np.float64).reshape(-1),
+                                                    np.ascontiguousarray(q, np.float64).reshape(-1), dhat, kappa,
+                                                    mu, eps))
+
+    def assemble(self, x, q, x_tilde, q_tilde, dhat, kappa, deterministic=True):
+        """IncrementalPotential::assemble -> (value, grad, rows, cols, blocks)."""
+        grad = np.zeros(3 * self.n_blocks)
+        val = np.zeros(1)
+        cap = 64 * self.n_blocks + 1024
+        while True:
+            rows, cols = np.zeros(cap, np.uint32), np.zeros(cap, np.uint32)
+            blocks = np.zeros((cap, 9))
+            U = self._L.ref_scene_assemble(self.h, np.ascontiguousarray(x, np.float64).reshape(-1),
+                                           np.ascontiguousarray(q, np.float64).reshape(-1),
+                                           np.ascontiguousarray(x_tilde, np.float64).reshape(-1),
+                                           np.ascontiguousarray(q_tilde, np.float64).reshape(-1), dhat, kappa,
+                                           int(deterministic), val, grad, cap, rows.ctypes.data, cols.ctypes.data,
+                                           blocks.ctypes.data)
+            if U >= 0:
+                return float(val[0]), grad, rows[:U].copy(), cols[:U].copy(), blocks[:U].copy()
+            cap = int(-U - 1)

@@ -24,6 +24,7 @@
 
 #include "adipc/contact/barrier.hpp"
 #include "adipc/contact/friction.hpp"
+#include "adipc/solver/incremental_potential.hpp"
 #include "adipc/energy/abd_energy.hpp"
 #include "adipc/energy/bending.hpp"
 #include "adipc/energy/membrane.hpp"
@@ -578,5 +579,163 @@ std::int64_t ref_build_friction_constraints(std::int32_t n_nodes, const double* 
         lambda[i] = fc[i].lambda;
     }
     return static_cast<std::int64_t>(fc.size());
+}
+
+// ---- the reference's IncrementalPotential::assemble on a scene built from
+// arrays (scene/scene.hpp Scene::finalize, make_dof_map, broad_phase.hpp
+// build_contact_surface; solver/incremental_potential.hpp:19-258), and the
+// scene data it derives, exported so the device path runs on identical inputs
+struct RefScene {
+    Scene scene;
+    ContactSurface surf;
+    DofMap dofs;
+    std::vector<FrictionConstraint> friction;
+    std::vector<Vec3> fr_base;
+    Real mu = 0, fr_eps = 1;
+};
+void* ref_scene_new(std::int32_t n_meshes, const std::int64_t* vert_begin, const double* rest,
+                    const std::int64_t* tet_begin, const std::int32_t* tets, const double* youngs,
+                    const double* poisson, const double* density, std::int32_t n_bodies,
+                    const std::int64_t* bvert_begin, const double* brest, const std::int64_t* btet_begin,
+                    const std::int32_t* btets, const double* bkappa, const double* bdensity, double dt, int ground,
+                    const double* gnormal, double gheight) {
+    auto* r = new RefScene;
+    Scene& sc = r->scene;
+    sc.config.dt = dt;
+    sc.ground.enabled = ground != 0;
+    if (ground) {
+        sc.ground.normal = ld3(gnormal);
+        sc.ground.height = gheight;
+    }
+    for (std::int32_t m = 0; m < n_meshes; ++m) {
+        DeformableMesh dm;
+        dm.name = "mesh" + std::to_string(m);
+        for (std::int64_t v = vert_begin[m]; v < vert_begin[m + 1]; ++v) dm.rest.push_back(ld3(rest + 3 * v));
+        for (std::int64_t t = tet_begin[m]; t < tet_begin[m + 1]; ++t)
+            dm.tets.push_back({tets[4 * t], tets[4 * t + 1], tets[4 * t + 2], tets[4 * t + 3]});
+        dm.solid.youngs = youngs[m];
+        dm.solid.poisson = poisson[m];
+        dm.solid.density = density[m];
+        sc.meshes.push_back(std::move(dm));
+    }
+    for (std::int32_t b = 0; b < n_bodies; ++b) {
+        AffineBody ab;
+        ab.name = "body" + std::to_string(b);
+        for (std::int64_t v = bvert_begin[b]; v < bvert_begin[b + 1]; ++v) ab.rest.push_back(ld3(brest + 3 * v));
+        for (std::int64_t t = btet_begin[b]; t < btet_begin[b + 1]; ++t)
+            ab.tets.push_back({btets[4 * t], btets[4 * t + 1], btets[4 * t + 2], btets[4 * t + 3]});
+        ab.mat.kappa = bkappa[b];
+        ab.mat.density = bdensity[b];
+        sc.bodies.push_back(std::move(ab));
+    }
+    sc.finalize();
+    r->surf = build_contact_surface(sc);
+    r->dofs = make_dof_map(sc);
+    return r;
+}
+void ref_scene_free(void* p) { delete static_cast<RefScene*>(p); }
+// sizes: n_fem, n_bodies, n_blocks, n_nodes, n_tets, n_surf_verts, n_edges, n_tris, n_meshes
+void ref_scene_sizes(void* p, std::int64_t* out) {
+    const RefScene& r = *static_cast<RefScene*>(p);
+    std::int64_t nt = 0;
+    for (const auto& m : r.scene.meshes) nt += static_cast<std::int64_t>(m.tets.size());
+    out[0] = r.dofs.n_fem_nodes;
+    out[1] = r.dofs.n_bodies;
+    out[2] = r.dofs.n_blocks();
+    out[3] = r.dofs.n_nodes();
+    out[4] = nt;
+    out[5] = static_cast<std::int64_t>(r.surf.verts.size());
+    out[6] = static_cast<std::int64_t>(r.surf.edges.size());
+    out[7] = static_cast<std::int64_t>(r.surf.tris.size());
+    out[8] = static_cast<std::int64_t>(r.scene.meshes.size());
+}
+// the derived data: vertex masses, per-tet rest data (Dm^-1 column-major, volume) and GLOBAL
+// tets, per-mesh mu / lambda, body reduced masses (column-major) / volumes, the abd node map and
+// jacobians (column-major 3x12), the contact surface, the scene length
+void ref_scene_export(void* p, double* mass, double* inv9, double* vol, std::int32_t* tets, double* mu, double* lam,
+                      double* reduced_mass, double* body_volume, std::int32_t* abd_body, double* jac36,
+                      std::int32_t* surf_verts, std::int32_t* edges, std::int32_t* tris, double* length_scale) {
+    const RefScene& r = *static_cast<RefScene*>(p);
+    const Scene& sc = r.scene;
+    std::int64_t t0 = 0;
+    for (std::size_t mi = 0; mi < sc.meshes.size(); ++mi) {
+        const auto& m = sc.meshes[mi];
+        const Index off = sc.mesh_offset[mi];
+        for (Index v = 0; v < m.n_verts(); ++v) mass[off + v] = m.vertex_mass[v];
+        for (std::size_t t = 0; t < m.tets.size(); ++t, ++t0) {
+            std::memcpy(inv9 + 9 * t0, m.tet_rest_data[t].inv_rest_edges.data(), 72);
+            vol[t0] = m.tet_rest_data[t].volume;
+            for (int k = 0; k < 4; ++k) tets[4 * t0 + k] = m.tets[t][k] + off;
+        }
+        mu[mi] = m.solid.mu();
+        lam[mi] = m.solid.lambda();
+    }
+    for (std::size_t b = 0; b < sc.bodies.size(); ++b) {
+        std::memcpy(reduced_mass + 144 * b, sc.bodies[b].reduced_mass.data(), 144 * 8);
+        body_volume[b] = sc.bodies[b].volume;
+    }
+    for (std::size_t a = 0; a < r.dofs.abd_node_body.size(); ++a) {
+        abd_body[a] = r.dofs.abd_node_body[a];
+        std::memcpy(jac36 + 36 * a, r.dofs.abd_node_jacobian[a].data(), 36 * 8);
+    }
+    for (std::size_t i = 0; i < r.surf.verts.size(); ++i) surf_verts[i] = r.surf.verts[i];
+    for (std::size_t i = 0; i < r.surf.edges.size(); ++i) {
+        edges[2 * i] = r.surf.edges[i][0];
+        edges[2 * i + 1] = r.surf.edges[i][1];
+    }
+    for (std::size_t i = 0; i < r.surf.tris.size(); ++i)
+        for (int k = 0; k < 3; ++k) tris[3 * i + k] = r.surf.tris[i][k];
+    *length_scale = sc.length_scale;
+}
+static SystemState ref_state(const RefScene& r, const double* x, const double* q) {
+    SystemState s;
+    s.x.resize(r.dofs.n_fem_nodes);
+    s.v.assign(r.dofs.n_fem_nodes, Vec3::Zero());
+    for (Index v = 0; v < r.dofs.n_fem_nodes; ++v) s.x[v] = ld3(x + 3 * v);
+    s.q.resize(r.dofs.n_bodies);
+    s.qd.assign(r.dofs.n_bodies, Vec12::Zero());
+    for (Index b = 0; b < r.dofs.n_bodies; ++b)
+        for (int k = 0; k < 12; ++k) s.q[b][k] = q[12 * b + k];
+    return s;
+}
+// the step-start friction freeze of newton.hpp:104-113 at state (x, q)
+std::int64_t ref_scene_begin_friction(void* p, const double* x, const double* q, double dhat, double kappa, double mu,
+                                      double eps) {
+    RefScene& r = *static_cast<RefScene*>(p);
+    const std::vector<Vec3> pos = contact_node_positions(r.scene, ref_state(r, x, q));
+    r.friction = build_friction_constraints(r.surf, pos, r.scene.ground, dhat, kappa);
+    r.fr_base = pos;
+    r.mu = mu;
+    r.fr_eps = eps;
+    return static_cast<std::int64_t>(r.friction.size());
+}
+// IncrementalPotential::assemble (value, grad, reduced Hessian) at (x, q) with
+// targets (x_tilde, q_tilde) and contact (dhat, kappa); returns U, or -U - 1
+// when cap is too small
+std::int64_t ref_scene_assemble(void* p, const double* x, const double* q, const double* x_tilde,
+                                const double* q_tilde, double dhat, double kappa, int det, double* value,
+                                double* grad, std::int64_t cap, std::uint32_t* rows, std::uint32_t* cols,
+                                double* blocks) {
+    RefScene& r = *static_cast<RefScene*>(p);
+    IncrementalPotential ip(r.scene, r.surf, r.dofs, make_pol(det, 0, 0));
+    std::vector<Vec3> xt(r.dofs.n_fem_nodes);
+    for (Index v = 0; v < r.dofs.n_fem_nodes; ++v) xt[v] = ld3(x_tilde + 3 * v);
+    std::vector<Vec12> qt(r.dofs.n_bodies);
+    for (Index b = 0; b < r.dofs.n_bodies; ++b)
+        for (int k = 0; k < 12; ++k) qt[b][k] = q_tilde[12 * b + k];
+    ip.set_targets(xt, qt);
+    ip.set_contact(dhat, kappa);
+    if (!r.friction.empty()) ip.set_friction(r.friction, r.fr_base, r.mu, r.fr_eps);
+    VecX g;
+    SortedSymBlockCoo A;
+    *value = ip.assemble(ref_state(r, x, q), g, A);
+    for (Index k = 0; k < 3 * r.dofs.n_blocks(); ++k) grad[k] = g[k];
+    if (static_cast<std::int64_t>(A.size()) > cap) return -static_cast<std::int64_t>(A.size()) - 1;
+    for (std::size_t i = 0; i < A.size(); ++i) {
+        rows[i] = A.rows[i];
+        cols[i] = A.cols[i];
+        std::memcpy(blocks + 9 * i, A.blocks[i].data(), 72);
+    }
+    return static_cast<std::int64_t>(A.size());
 }
 }  // extern "C"

@@ -76,6 +76,7 @@ GPU_SIGNATURES = {
     "adipc_gpu_step_inf_norm_device": (ci, [vp, vp, i32, i32, vp, C.POINTER(cd)]),
     "adipc_gpu_apply_direction_device": (ci, [vp, vp, vp, cd, i64, vp]),
     "adipc_gpu_node_displacements_device": (ci, [vp, vp, i32, i32, vp, vp, vp]),
+    "adipc_gpu_contact_positions_device": (ci, [vp, vp, i32, i32, vp, vp, vp]),
     "adipc_gpu_set_matrix": (ci, [vp, i32, i64, vp, vp, vp]),
     "adipc_gpu_set_matrix_device": (ci, [vp, i32, i64, vp, vp, vp]),
     "adipc_gpu_sort_stream": (ci, [vp, vp, vp, i64]),

@@ -347,6 +347,12 @@ class Context:
         self._check(self._L.adipc_gpu_apply_direction_device(self.h, ptr(d_state), ptr(d_dir), float(alpha),
                                                                d_state.numel(), ptr(d_out)))
 
+    def contact_positions(self, d_state, n_fem, d_abd_body, d_jac36, d_out):
+        """contact_node_positions (scene.hpp:112-120): FEM x, body nodes A x_bar + p."""
+        n_abd = 0 if d_abd_body is None else d_abd_body.numel()
+        self._check(self._L.adipc_gpu_contact_positions_device(self.h, ptr(d_state), n_fem, n_abd, ptr(d_abd_body),
+                                                                 ptr(d_jac36), ptr(d_out)))
+
     def node_displacements(self, d_dir, n_fem, d_abd_body, d_jac36, d_out):
         n_abd = 0 if d_abd_body is None else d_abd_body.numel()
         self._check(self._L.adipc_gpu_node_displacements_device(self.h, ptr(d_dir), n_fem, n_abd, ptr(d_abd_body),

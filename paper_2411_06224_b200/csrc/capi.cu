@@ -664,6 +664,18 @@ int adipc_gpu_lift_node_grad_device(adipc_gpu_ctx* ctx, const double* d_node_gra
     });
 }
 
+int adipc_gpu_contact_positions_device(adipc_gpu_ctx* ctx, const double* d_state, int32_t n_fem, int32_t n_abd,
+                                       const int32_t* d_abd_node_body, const double* d_abd_node_jacobian36,
+                                       double* d_out) {
+    return guarded(ctx, [&] {
+        if (n_fem < 0 || n_abd < 0) throw StatusError(kInvalidArgument, "contact_positions: negative size");
+        if (n_abd > 0 && (!d_abd_node_body || !d_abd_node_jacobian36))
+            throw StatusError(kInvalidArgument, "contact_positions: missing body arrays");
+        contact_positions(ctx->c, d_state, n_fem, n_abd, d_abd_node_body, d_abd_node_jacobian36, d_out);
+        sync(ctx->c);
+    });
+}
+
 int adipc_gpu_node_displacements_device(adipc_gpu_ctx* ctx, const double* d_dir, int32_t n_fem, int32_t n_abd,
                                         const int32_t* d_abd_node_body, const double* d_abd_jacobian36,
                                         double* d_out) {

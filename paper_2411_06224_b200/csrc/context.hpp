@@ -388,6 +388,8 @@ std::int64_t assemble_contact(Ctx& c, const std::uint64_t* d_keys, const double*
                               cudaEvent_t vals_ready = nullptr);
 
 // step.cu (newton.hpp:257-290): the step after the solve
+void contact_positions(Ctx& c, const double* d_state, std::int32_t n_fem, std::int32_t n_abd,
+                       const std::int32_t* d_abd_body, const double* d_jac36, double* d_out);
 void lift_node_grad(Ctx& c, const double* d_node_grad, std::int32_t n_fem, std::int32_t n_abd,
                     const std::int32_t* d_abd_body, const double* d_jac36, const std::uint8_t* d_pinned,
                     double* d_grad);

@@ -75,6 +75,33 @@ __global__ void k_node_displacements(const double* __restrict__ d, std::int32_t 
     }
 }
 
+// contact_node_positions (scene.hpp:112-120): FEM vertices copy x; an
+// affine-body node is affine_point(q, x_bar) = A x_bar + p (core/types.hpp:
+// 34-40) in that operation order — not J q, whose sum order differs in the
+// last bit (a friction base position feeds dx = x - base at 1e-5 scale).
+// x_bar_k is the node Jacobian's (0, 3 + k) entry.
+__global__ void k_contact_positions(const double* __restrict__ st, std::int32_t n_fem, std::int32_t n_abd,
+                                    const std::int32_t* __restrict__ abd_body, const double* __restrict__ jac36,
+                                    double* __restrict__ out) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+         i < static_cast<std::int64_t>(n_fem) + n_abd; i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        if (i < n_fem) {
+            for (int k = 0; k < 3; ++k) out[3 * i + k] = st[3 * i + k];
+        } else {
+            const std::int64_t a = i - n_fem;
+            const double* J = jac36 + 36 * a;
+            const double x0 = J[9], x1 = J[12], x2 = J[15];
+            const double* q = st + 3 * (static_cast<std::int64_t>(n_fem) + 4 * static_cast<std::int64_t>(abd_body[a]));
+            for (int r = 0; r < 3; ++r) {
+                const double* Ar = q + 3 + 3 * r;
+                out[3 * i + r] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Ar[0], x0), __dmul_rn(Ar[1], x1)),
+                                                     __dmul_rn(Ar[2], x2)),
+                                           q[r]);
+            }
+        }
+    }
+}
+
 // assemble_contact's gradient lift (incremental_potential.hpp:395-403): a FEM
 // node's contact gradient adds to its slot, an affine-body node's through
 // J^T to its body's 12 dofs (fp64 RED); pinned slots receive nothing (the
@@ -112,6 +139,14 @@ void lift_node_grad(Ctx& c, const double* d_node_grad, std::int32_t n_fem, std::
     if (n <= 0) return;
     k_lift_node_grad<<<grid_for(n, 256, 16), 256, 0, c.stream>>>(d_node_grad, n_fem, n_abd, d_abd_body, d_jac36,
                                                                 d_pinned, d_grad);
+    ADIPC_LAUNCH_CHECK();
+}
+
+void contact_positions(Ctx& c, const double* d_state, std::int32_t n_fem, std::int32_t n_abd,
+                       const std::int32_t* d_abd_body, const double* d_jac36, double* d_out) {
+    const std::int64_t n = static_cast<std::int64_t>(n_fem) + n_abd;
+    if (n <= 0) return;
+    k_contact_positions<<<grid_for(n, 256, 16), 256, 0, c.stream>>>(d_state, n_fem, n_abd, d_abd_body, d_jac36, d_out);
     ADIPC_LAUNCH_CHECK();
 }
 

@@ -92,9 +92,10 @@ class IncrementalPotential:
         return m
 
     def contact_positions(self, state):
-        """contact_node_positions (scene.hpp): FEM x, affine-body nodes J q."""
+        """contact_node_positions (scene.hpp:112-120): FEM x, affine-body nodes
+        A x_bar + p in the reference's operation order."""
         pos = torch.empty(3 * self.n_nodes, dtype=torch.float64, device=self.dev)
-        self.ctx.node_displacements(state, self.n_fem, self.abd_body, self.jac36, pos)
+        self.ctx.contact_positions(state, self.n_fem, self.abd_body, self.jac36, pos)
         return pos
 
     def candidates(self, pos, disp=None, inflate=None):

@@ -132,6 +132,7 @@ class GeomHybrid:
         span_x = grid[0] * size + (grid[0] - 1) * gap
         span_z = grid[2] * size + (grid[2] - 1) * gap
         bt_all, body_of, rest_all, ms, vols, bmass = [], [], [], [], [], []
+        self.body_tets = []  # local tets of each body (the reference builds bodies from rest + tets)
         node = self.n_fem
         vb0, tb0 = box_tets(body_res, body_res, body_res, body_size, body_size, body_size)
         btb0 = boundary_tris(tb0)
@@ -147,6 +148,7 @@ class GeomHybrid:
                 bmass.append(m)
                 bt_all.append(btb0 + node)
                 rest_all.append(v)
+                self.body_tets.append(tb0)
                 body_of.append(np.full(len(v), nb, np.int32))
                 ms.append(reduced_mass(v, m))
                 p = v[t]
@@ -157,6 +159,8 @@ class GeomHybrid:
         self.n_bodies = nb
         self.n_blocks = self.n_fem + 4 * nb
         self.abd_rest = np.concatenate(rest_all)
+        self.body_rest = rest_all
+        self.E, self.nu, self.rho = E, nu, rho
         self.abd_body = np.concatenate(body_of)
         self.jac36 = jacobian36(self.abd_rest)
         self.reduced_mass = np.stack(ms)

@@ -63,7 +63,7 @@ def test_frictional_step_matches_oracle(ctx, scene):
     s0 = g.state() + rng.normal(0, 3e-5, 3 * g.n_blocks)
     mu, eps = 0.4, 1e-5
     n_fr = ip.begin_friction(t(s0), mu, eps)
-    pos0 = O.node_displacements(s0, g.n_fem, g.abd_body, g.jac36).reshape(-1, 3)
+    pos0 = O.contact_node_positions(s0, g.n_fem, g.abd_body, g.jac36)
     fr = O.build_friction_constraints(pos0, g.surf_verts, g.edges, g.tris, g.dhat, g.kappa, GROUND)
     assert n_fr == len(fr["n"]) and n_fr > 0
     s1 = s0 + rng.normal(0, 2e-5, 3 * g.n_blocks)

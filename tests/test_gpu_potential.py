@@ -94,7 +94,7 @@ def test_ccd_step_matches_oracle(ctx, scene):
     for s in (1e-4, 1e-3):
         d = rng.normal(0, s, 3 * g.n_blocks)
         a = ip.ccd_step(t(state), t(d))
-        pos = O.node_displacements(state, g.n_fem, g.abd_body, g.jac36).reshape(-1, 3)
+        pos = O.contact_node_positions(state, g.n_fem, g.abd_body, g.jac36)
         disp = O.node_displacements(d, g.n_fem, g.abd_body, g.jac36).reshape(-1, 3)
         pt, ee = O.find_candidates(pos, g.surf_verts, g.edges, g.tris, g.dhat, disp=disp)
         ci = O.ContactInput(pos, np.c_[g.surf_verts[pt[:, 0]], g.tris[pt[:, 1]]],

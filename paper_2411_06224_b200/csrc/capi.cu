@@ -183,6 +183,8 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
                     &c.ag_adj[1]})
         b->free();
     for (auto* b : {&c.ag_base, &c.ag_ptr[0], &c.ag_ptr[1]}) b->free();
+    c.stage.free();
+    c.stage_up.free();
     c.graph_deg.free();
     c.graph_adj.free();
     c.graph_ptr.free();

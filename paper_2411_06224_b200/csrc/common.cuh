@@ -117,6 +117,28 @@ struct DBuf {
     std::size_t bytes() const { return n * sizeof(T); }
 };
 
+// pinned host staging for device -> host copies of hierarchy data (pageable
+// copies stage through the driver at a few GB/s)
+struct HostStage {
+    unsigned char* p = nullptr;
+    std::size_t cap = 0;
+    void* reserve(std::size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            const std::size_t want = bytes + bytes / 4;
+            ADIPC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), want));
+            cap = want;
+        }
+        return p;
+    }
+    void free() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // Block value storage of the assembled matrix: 32-block tiles, SoA inside a

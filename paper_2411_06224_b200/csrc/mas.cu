@@ -1201,10 +1201,14 @@ host::Graph graph_to_host(Ctx& c, const DeviceGraph& dg, std::int32_t n) {
     host::Graph g;
     g.ptr.resize(static_cast<std::size_t>(n) + 1);
     g.adj.resize(static_cast<std::size_t>(dg.E));
-    ADIPC_CUDA(cudaMemcpyAsync(g.ptr.data(), dg.ptr, sizeof(std::int64_t) * (n + 1), cudaMemcpyDeviceToHost, c.stream));
-    if (dg.E > 0)
-        ADIPC_CUDA(cudaMemcpyAsync(g.adj.data(), dg.adj, sizeof(std::int32_t) * dg.E, cudaMemcpyDeviceToHost, c.stream));
+    const std::size_t bp = sizeof(std::int64_t) * (static_cast<std::size_t>(n) + 1);
+    const std::size_t ba = sizeof(std::int32_t) * static_cast<std::size_t>(dg.E);
+    unsigned char* st = static_cast<unsigned char*>(c.stage.reserve(bp + ba));
+    ADIPC_CUDA(cudaMemcpyAsync(st, dg.ptr, bp, cudaMemcpyDeviceToHost, c.stream));
+    if (dg.E > 0) ADIPC_CUDA(cudaMemcpyAsync(st + bp, dg.adj, ba, cudaMemcpyDeviceToHost, c.stream));
     ADIPC_CUDA(cudaStreamSynchronize(c.stream));
+    std::memcpy(g.ptr.data(), st, bp);
+    if (ba) std::memcpy(g.adj.data(), st + bp, ba);
     return g;
 }
 
@@ -1282,6 +1286,15 @@ __global__ void k_l1_keys(std::int32_t n, const std::int64_t* __restrict__ gptr,
 bool level1_device(Ctx& c, const DeviceGraph& g0, std::vector<std::int32_t>& up1, std::int32_t& n1,
                    host::Graph& g1) {
     const host::Partition& l0 = c.l0;
+    const bool dbg = std::getenv("ADIPC_DEBUG_HIER") != nullptr;
+    auto t = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!dbg) return;
+        ADIPC_CUDA(cudaStreamSynchronize(c.stream));
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "    level-1 pass: %s %.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    };
     const std::int32_t n = static_cast<std::int32_t>(l0.part_of.size());
     cudaStream_t st = c.stream;
     if (c.l0_dev_version != c.l0_version) {  // per scene: members of each subdomain, ascending
@@ -1309,19 +1322,24 @@ bool level1_device(Ctx& c, const DeviceGraph& g0, std::vector<std::int32_t>& up1
     ADIPC_CUDA(cudaMemcpyAsync(&total, c.l1_base.p + l0.n_parts, sizeof(total), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaStreamSynchronize(st));
     n1 = static_cast<std::int32_t>(total);
+    lap("components + scan");
     k_l1_up<<<grid_for(n, 256, 16), 256, 0, st>>>(n, c.l0_part.p, c.l1_base.p, c.l1_up.p);
     ADIPC_LAUNCH_CHECK();
     up1.resize(static_cast<std::size_t>(n));
-    ADIPC_CUDA(cudaMemcpyAsync(up1.data(), c.l1_up.p, sizeof(std::int32_t) * n, cudaMemcpyDeviceToHost, st));
+    void* up_stage = c.stage_up.reserve(sizeof(std::int32_t) * static_cast<std::size_t>(n));
+    ADIPC_CUDA(cudaMemcpyAsync(up_stage, c.l1_up.p, sizeof(std::int32_t) * n, cudaMemcpyDeviceToHost, st));
     if (n1 == n) {  // no merge: the hierarchy stops at level 0
         ADIPC_CUDA(cudaStreamSynchronize(st));
+        std::memcpy(up1.data(), up_stage, sizeof(std::int32_t) * n);
         return true;
     }
+    lap("map + D2H");
     // super-node graph: bucket-sort the mapped adjacency, drop repeats and self loops
     c.l1_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(g0.E, 1)));
     k_l1_keys<<<grid_for(n, 256, 16), 256, 0, st>>>(n, g0.ptr, g0.adj, c.l1_up.p, c.l1_keys.p);
     ADIPC_LAUNCH_CHECK();
     bucket_sort(c, c.l1_keys.p, g0.E, n1, nullptr);
+    lap("keys + bucket sort");
     c.l1_cnt.reserve(static_cast<std::size_t>(n1) + 1);
     c.l1_ptr.reserve(static_cast<std::size_t>(n1) + 1);
     k_adj_count<<<grid_for(n1, 8, 16), 256, 0, st>>>(n1, c.sorted.p, c.row_start.p, c.l1_cnt.p);
@@ -1333,7 +1351,10 @@ bool level1_device(Ctx& c, const DeviceGraph& g0, std::vector<std::int32_t>& up1
     c.l1_adj.reserve(static_cast<std::size_t>(std::max<std::int64_t>(E1, 1)));
     k_adj_emit<<<grid_for(n1, 8, 16), 256, 0, st>>>(n1, c.sorted.p, c.row_start.p, c.l1_ptr.p, c.l1_adj.p);
     ADIPC_LAUNCH_CHECK();
-    g1 = graph_to_host(c, DeviceGraph{c.l1_ptr.p, c.l1_adj.p, E1}, n1);
+    lap("unique count / emit");
+    g1 = graph_to_host(c, DeviceGraph{c.l1_ptr.p, c.l1_adj.p, E1}, n1);  // synchronises: up1 has landed too
+    std::memcpy(up1.data(), up_stage, sizeof(std::int32_t) * n);
+    lap("graph D2H");
     c.l1_E = E1;
     return true;
 }

@@ -129,3 +129,28 @@ def test_newton_linear_solve_matches_oracle(ctx, scene):
     xo, ro = O.pcg_solve(A, -og, O.MasPreconditioner(A, H), 1e-10, 250, 100000, DET)
     assert res.converged and ro["converged"]
     assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-6 * np.linalg.norm(xo)
+
+
+def test_potential_without_contact_or_bodies(ctx):
+    """Edge cases of the composition: contact disabled (dhat = 0: no broad
+    phase, an empty node stream into the two-level assembly) and a scene with
+    no affine bodies: the result is the element / inertia assembly alone,
+    against the oracle's ip_fem_assemble + filter + sort + reduce."""
+    g = GeomHybrid(grid=(1, 1, 1), res=4, bodies=(1, 1), body_res=1)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    mesh = {"mass": t(g.mass), "tets": t(g.tets), "rest_inv9": t(g.rest_inv9), "rest_volume": t(g.rest_volume),
+            "tet_begin": g.tet_begin, "mu": [g.mu], "lam": [g.lam]}
+    ip = IncrementalPotential(ctx, mesh, {"verts": t(g.surf_verts[:0]), "edges": t(g.edges[:0]),
+                                          "tris": t(g.tris[:0])}, {"n_fem": g.n_fem}, g.dt)
+    ip.set_targets(t(g.x_tilde.reshape(-1)))
+    x = g.x.reshape(-1) + np.random.default_rng(3).normal(0, 1e-4, 3 * g.n_fem)
+    val, grad = ip.assemble(t(x))
+    assert ip.last["n_pt"] == 0 and ip.last["node_blocks"] == 0 and ip.last["contact_tiles"] == 0
+    ov, og, keys, vals = O.ip_fem_assemble(x, g.x_tilde, g.mass, g.tet_begin, [g.mu], [g.lam], g.tets, g.rest_inv9,
+                                           g.rest_volume, g.dt ** 2)
+    sk, sv = O.sort_stream(keys, vals, DET)
+    orow, ocol, oblk = O.fast_hash_reduction(sk, sv, g.n_fem, DET)
+    n, rows, cols, blocks = ctx.copy_matrix()
+    assert_matrix_close(rows, cols, blocks, orow, ocol, oblk, 1e-9)
+    assert np.linalg.norm(grad.cpu().numpy() - og) <= 1e-10 * np.linalg.norm(og)
+    assert abs(val - ov) <= 1e-12 * abs(ov)

@@ -184,6 +184,9 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
         b->free();
     for (auto* b : {&c.ag_base, &c.ag_ptr[0], &c.ag_ptr[1]}) b->free();
     c.stage.free();
+    c.fem_defer_m.free();
+    c.fem_defer_t.free();
+    c.fem_defer_n.free();
     c.stage_up.free();
     c.graph_deg.free();
     c.graph_adj.free();

@@ -145,6 +145,10 @@ struct Ctx {
     DBuf<std::uint64_t> fem_keys;
     DBuf<double> fem_vals, fem_value;
     DBuf<unsigned char> hinge_work;  // per-thread dual scratch of the hinge producer
+    // indefinite element stencils deferred to the projection pass (energy.cu)
+    DBuf<double> fem_defer_m;
+    DBuf<std::int64_t> fem_defer_t;
+    DBuf<unsigned long long> fem_defer_n;
     // contact producers (contact.cu): activity flags / counts, their prefix
     // sums, the per-thread dual scratch, value / touch / ccd scalars
     DBuf<std::int32_t> ct_on;

@@ -91,7 +91,9 @@ __global__ void __launch_bounds__(kFemThreads) k_fem_tets(std::int64_t n_tets, c
                                                          const double* __restrict__ x, double mu, double lam,
                                                          double dt2, int project, std::uint64_t* __restrict__ keys,
                                                          double* __restrict__ vals, double* __restrict__ grad,
-                                                         double* __restrict__ value) {
+                                                         double* __restrict__ value, double* __restrict__ defer_m,
+                                                         std::int64_t* __restrict__ defer_t,
+                                                         unsigned long long* __restrict__ defer_n) {
     double e = 0;
     for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < n_tets;
          t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
@@ -205,39 +207,217 @@ __global__ void __launch_bounds__(kFemThreads) k_fem_tets(std::int64_t n_tets, c
                         for (int r = 0; r < 3; ++r) o[3 * c + r] = dt2 * (flip ? h[3 * r + c] : h[3 * c + r]);
                 }
         } else {
-            // indefinite: full M, project, lift back through Q (x) I3
-            double M[81];
+            // indefinite: the reduced matrix (packed lower, 45 doubles) goes to
+            // the deferred list (fem_emit passes one whenever it emits with
+            // projection); k_fem_project projects it and emits the ten blocks
+            // with a lean, shared-memory working set
+            const unsigned long long slot = atomicAdd(defer_n, 1ull);
+#pragma unroll
             for (int j = 0; j < 3; ++j)
-                for (int l = 0; l < 3; ++l) {
+#pragma unroll
+                for (int l = 0; l <= j; ++l) {
                     double h[9];
                     stencil_block(s, R[j], R[l], h);
+#pragma unroll
                     for (int c = 0; c < 3; ++c)
-                        for (int r = 0; r < 3; ++r) M[9 * (3 * l + c) + 3 * j + r] = h[3 * c + r];
+#pragma unroll
+                        for (int r = 0; r < 3; ++r)
+                            if (3 * j + r >= 3 * l + c) defer_m[45 * slot + pk(3 * j + r, 3 * l + c)] = h[3 * c + r];
                 }
-            project9(M);
-            int q = 0;
-            for (int a = 0; a < 4; ++a)
-                for (int b = a; b < 4; ++b, ++q) {
-                    double h[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-                    for (int j = 0; j < 3; ++j)
-                        for (int l = 0; l < 3; ++l) {
-                            const double w = helmert(a, j) * helmert(b, l);
-                            for (int c = 0; c < 3; ++c)
-                                for (int r = 0; r < 3; ++r) h[3 * c + r] += w * M[9 * (3 * l + c) + 3 * j + r];
-                        }
-                    const bool flip = ids[a] > ids[b];
-                    const std::uint32_t r0 = static_cast<std::uint32_t>(flip ? ids[b] : ids[a]);
-                    const std::uint32_t c0 = static_cast<std::uint32_t>(flip ? ids[a] : ids[b]);
-                    keys[base + q] = (static_cast<std::uint64_t>(r0) << 32) | c0;
-                    double* o = vals + 9 * (base + q);
-                    for (int c = 0; c < 3; ++c)
-                        for (int r = 0; r < 3; ++r) o[3 * c + r] = dt2 * (flip ? h[3 * r + c] : h[3 * c + r]);
-                }
+            defer_t[slot] = t;
         }
     }
     block_sum_atomic(dt2 * e, value);
 }
 
+
+// The deferred projections of k_fem_tets: one thread per indefinite stencil,
+// its work arrays (eigenvectors, tridiagonal) in shared memory laid out
+// thread-minor (conflict-free), the same Householder + implicit-QL
+// projection as project_sym<9>, then V max(w, 0) V^T lifted through Q (x) I3
+// into the stencil's ten blocks at its own stream positions.
+constexpr int kProjThreads = 64;
+__global__ void __launch_bounds__(kProjThreads) k_fem_project(const unsigned long long* __restrict__ count,
+                                                               const double* __restrict__ defer_m,
+                                                               const std::int64_t* __restrict__ defer_t,
+                                                               const std::int32_t* __restrict__ tets, double dt2,
+                                                               std::uint64_t* __restrict__ keys,
+                                                               double* __restrict__ vals) {
+    constexpr int N = 9, T = kProjThreads;
+    extern __shared__ double sm[];
+    double* Vs = sm;                  // V[i][j] at (N * i + j) * T + tid
+    double* ds = sm + N * N * T;      // d[i] at i * T + tid
+    double* es = ds + N * T;          // e[i]
+    const int tid = threadIdx.x;
+    auto V = [&](int i, int j) -> double& { return Vs[(N * i + j) * T + tid]; };
+    auto d = [&](int i) -> double& { return ds[i * T + tid]; };
+    auto e = [&](int i) -> double& { return es[i * T + tid]; };
+    const unsigned long long n = *count;
+    for (unsigned long long w = blockIdx.x * static_cast<unsigned long long>(T) + tid; w < n;
+         w += static_cast<unsigned long long>(gridDim.x) * T) {
+        const double* Mp = defer_m + 45 * w;
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j <= i; ++j) V(i, j) = V(j, i) = Mp[pk(i, j)];
+        // tred2
+        for (int j = 0; j < N; ++j) d(j) = V(N - 1, j);
+        for (int i = N - 1; i > 0; --i) {
+            double scale = 0, h = 0;
+            for (int k = 0; k < i; ++k) scale += fabs(d(k));
+            if (scale == 0) {
+                e(i) = d(i - 1);
+                for (int j = 0; j < i; ++j) {
+                    d(j) = V(i - 1, j);
+                    V(i, j) = 0;
+                    V(j, i) = 0;
+                }
+            } else {
+                for (int k = 0; k < i; ++k) {
+                    d(k) /= scale;
+                    h += d(k) * d(k);
+                }
+                double f = d(i - 1);
+                double g = sqrt(h);
+                if (f > 0) g = -g;
+                e(i) = scale * g;
+                h -= f * g;
+                d(i - 1) = f - g;
+                for (int j = 0; j < i; ++j) e(j) = 0;
+                for (int j = 0; j < i; ++j) {
+                    f = d(j);
+                    V(j, i) = f;
+                    g = e(j) + V(j, j) * f;
+                    for (int k = j + 1; k <= i - 1; ++k) {
+                        g += V(k, j) * d(k);
+                        e(k) += V(k, j) * f;
+                    }
+                    e(j) = g;
+                }
+                f = 0;
+                for (int j = 0; j < i; ++j) {
+                    e(j) /= h;
+                    f += e(j) * d(j);
+                }
+                const double hh = f / (h + h);
+                for (int j = 0; j < i; ++j) e(j) -= hh * d(j);
+                for (int j = 0; j < i; ++j) {
+                    f = d(j);
+                    g = e(j);
+                    for (int k = j; k <= i - 1; ++k) V(k, j) -= (f * e(k) + g * d(k));
+                    d(j) = V(i - 1, j);
+                    V(i, j) = 0;
+                }
+            }
+            d(i) = h;
+        }
+        for (int i = 0; i < N - 1; ++i) {
+            V(N - 1, i) = V(i, i);
+            V(i, i) = 1;
+            const double h = d(i + 1);
+            if (h != 0) {
+                for (int k = 0; k <= i; ++k) d(k) = V(k, i + 1) / h;
+                for (int j = 0; j <= i; ++j) {
+                    double g = 0;
+                    for (int k = 0; k <= i; ++k) g += V(k, i + 1) * V(k, j);
+                    for (int k = 0; k <= i; ++k) V(k, j) -= g * d(k);
+                }
+            }
+            for (int k = 0; k <= i; ++k) V(k, i + 1) = 0;
+        }
+        for (int j = 0; j < N; ++j) {
+            d(j) = V(N - 1, j);
+            V(N - 1, j) = 0;
+        }
+        V(N - 1, N - 1) = 1;
+        e(0) = 0;
+        // tql2
+        for (int i = 1; i < N; ++i) e(i - 1) = e(i);
+        e(N - 1) = 0;
+        double f = 0, tst1 = 0;
+        const double eps = 2.220446049250313e-16;
+        for (int l = 0; l < N; ++l) {
+            tst1 = fmax(tst1, fabs(d(l)) + fabs(e(l)));
+            int m = l;
+            while (m < N - 1 && fabs(e(m)) > eps * tst1) ++m;
+            if (m > l) {
+                for (int iter = 0; iter < 64; ++iter) {
+                    double g = d(l);
+                    double p = (d(l + 1) - g) / (2.0 * e(l));
+                    double r = hypot(p, 1.0);
+                    if (p < 0) r = -r;
+                    d(l) = e(l) / (p + r);
+                    d(l + 1) = e(l) * (p + r);
+                    const double dl1 = d(l + 1);
+                    double h = g - d(l);
+                    for (int i = l + 2; i < N; ++i) d(i) -= h;
+                    f += h;
+                    p = d(m);
+                    double c = 1, c2 = 1, c3 = 1, sn = 0, s2 = 0;
+                    const double el1 = e(l + 1);
+                    for (int i = m - 1; i >= l; --i) {
+                        c3 = c2;
+                        c2 = c;
+                        s2 = sn;
+                        g = c * e(i);
+                        h = c * p;
+                        r = hypot(p, e(i));
+                        e(i + 1) = sn * r;
+                        sn = e(i) / r;
+                        c = p / r;
+                        p = c * d(i) - sn * g;
+                        d(i + 1) = h + sn * (c * g + sn * d(i));
+                        for (int k = 0; k < N; ++k) {
+                            h = V(k, i + 1);
+                            V(k, i + 1) = sn * V(k, i) + c * h;
+                            V(k, i) = c * V(k, i) - sn * h;
+                        }
+                    }
+                    p = -sn * s2 * c3 * el1 * e(l) / dl1;
+                    e(l) = sn * p;
+                    d(l) = c * p;
+                    if (!(fabs(e(l)) > eps * tst1)) break;
+                }
+            }
+            d(l) += f;
+            e(l) = 0;
+        }
+        // W = V diag(sqrt(max(w, 0))) in place: P = W W^T
+        for (int k = 0; k < N; ++k) {
+            const double sw = d(k) > 0 ? sqrt(d(k)) : 0.0;
+            for (int i = 0; i < N; ++i) V(i, k) *= sw;
+        }
+        const std::int64_t t = defer_t[w];
+        const int4 id = reinterpret_cast<const int4*>(tets)[t];
+        const int ids[4] = {id.x, id.y, id.z, id.w};
+        const std::int64_t base = 10 * t;
+        int q = 0;
+        for (int a = 0; a < 4; ++a) {
+            double Za[3][N];  // rows of (Q (x) I3) W for node a
+            for (int r = 0; r < 3; ++r)
+                for (int k = 0; k < N; ++k)
+                    Za[r][k] = helmert(a, 0) * V(r, k) + helmert(a, 1) * V(3 + r, k) + helmert(a, 2) * V(6 + r, k);
+            for (int b = a; b < 4; ++b, ++q) {
+                double h[9];
+                for (int c = 0; c < 3; ++c) {
+                    double zb[N];
+                    for (int k = 0; k < N; ++k)
+                        zb[k] = helmert(b, 0) * V(c, k) + helmert(b, 1) * V(3 + c, k) + helmert(b, 2) * V(6 + c, k);
+                    for (int r = 0; r < 3; ++r) {
+                        double sum = 0;
+                        for (int k = 0; k < N; ++k) sum += Za[r][k] * zb[k];
+                        h[3 * c + r] = sum;
+                    }
+                }
+                const bool flip = ids[a] > ids[b];
+                const std::uint32_t r0 = static_cast<std::uint32_t>(flip ? ids[b] : ids[a]);
+                const std::uint32_t c0 = static_cast<std::uint32_t>(flip ? ids[a] : ids[b]);
+                keys[base + q] = (static_cast<std::uint64_t>(r0) << 32) | c0;
+                double* o = vals + 9 * (base + q);
+                for (int c = 0; c < 3; ++c)
+                    for (int r = 0; r < 3; ++r) o[3 * c + r] = dt2 * (flip ? h[3 * r + c] : h[3 * c + r]);
+            }
+        }
+    }
+}
 
 // affine-body inertia (incremental_potential.hpp:181-188): g = M dq written
 // to the body's 12 gradient entries, 0.5 dq.g to the value, the reduced mass
@@ -541,10 +721,33 @@ void fem_emit(Ctx& c, const FemDesc& d, std::uint64_t* d_keys, double* d_vals, d
     auto solid = [&](int m) {
         const std::int64_t t0 = d.tet_begin[m], nt = d.tet_begin[m + 1] - t0;
         if (nt > 0) {
+            // indefinite stencils are projected by k_fem_project from a list
+            // (capacity: every stencil of the mesh)
+            const bool defer = d.project && d_keys;
+            if (defer) {
+                c.fem_defer_m.reserve(static_cast<std::size_t>(nt) * 45);
+                c.fem_defer_t.reserve(static_cast<std::size_t>(nt));
+                c.fem_defer_n.reserve(1);
+                ADIPC_CUDA(cudaMemsetAsync(c.fem_defer_n.p, 0, sizeof(unsigned long long), st));
+            }
             k_fem_tets<<<grid_for(nt, kFemThreads, 16), kFemThreads, 0, st>>>(
                 nt, d.tets + 4 * t0, d.rest_inv9 + 9 * t0, d.rest_volume + t0, d.x, d.mu[m], d.lambda[m], d.dt2,
-                d.project, d_keys ? d_keys + off : nullptr, d_vals ? d_vals + 9 * off : nullptr, d_grad, d_value);
+                d.project, d_keys ? d_keys + off : nullptr, d_vals ? d_vals + 9 * off : nullptr, d_grad, d_value,
+                defer ? c.fem_defer_m.p : nullptr, defer ? c.fem_defer_t.p : nullptr,
+                defer ? c.fem_defer_n.p : nullptr);
             ADIPC_LAUNCH_CHECK();
+            if (defer) {
+                const std::size_t smem = sizeof(double) * (81 + 18) * kProjThreads;
+                ADIPC_CUDA(cudaFuncSetAttribute(k_fem_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(smem)));
+                int sms = kSMs, occ = 0;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+                ADIPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fem_project, kProjThreads, smem));
+                k_fem_project<<<sms * std::max(occ, 1), kProjThreads, smem, st>>>(
+                    c.fem_defer_n.p, c.fem_defer_m.p, c.fem_defer_t.p, d.tets + 4 * t0, d.dt2, d_keys + off,
+                    d_vals + 9 * off);
+                ADIPC_LAUNCH_CHECK();
+            }
         }
         off += 10 * nt;
     };

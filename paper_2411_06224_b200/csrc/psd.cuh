@@ -67,10 +67,9 @@ __device__ __forceinline__ bool shifted_cholesky_ok(double* L, double tau) {
 // implicit shifted QL sweeps with deflation at |e_i| <= 2^-52 max(|d| + |e|)
 // (Wilkinson / Reinsch tred2 + tql2; Eigen's SelfAdjointEigenSolver is the
 // same family: tridiagonalisation + implicit symmetric QR). ~2 K FMA for a
-// 9 x 9 against ~17 K for cyclic Jacobi to convergence: the element
-// producer's indefinite path (nearly every stencil once the mesh deforms)
-// went from 27.3 to 12.9 ms at cfg5, the geometric scene's contact pass from
-// 4.4 to 2.3 ms.
+// 9 x 9 against ~17 K for cyclic Jacobi to convergence: the geometric
+// scene's contact pass went from 4.4 to 2.3 ms (the element producer runs
+// the same algorithm in its own deferred pass, energy.cu k_fem_project).
 template <int N>
 __device__ __noinline__ void project_sym(double* a) {
     double V[N * N], d[N], e[N];  // V row-major: V[i][j] = V[N * i + j]

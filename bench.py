@@ -850,6 +850,12 @@ def producer_gpu(args, ctx, sc, d_b, stream, dev):
         return ev0.elapsed_time(ev1) / reps
 
     emit_ms = timed(lambda: ctx.fem_emit(mesh, d_x, d_xt, 1e-4, keys, vals, grad, pinned=d_pin), args.steps)
+    # a later Newton iteration: a deformed mesh (vertices moved by up to 1 % of
+    # a cell) makes nearly every stencil indefinite -> the projection pass runs
+    h_cell = float(np.abs(sc.verts[1] - sc.verts[0]).max())
+    d_xdef = d_x + torch.from_numpy(np.random.default_rng(1).uniform(-0.01 * h_cell, 0.01 * h_cell,
+                                                                    3 * n)).to(dev)
+    emit_def_ms = timed(lambda: ctx.fem_emit(mesh, d_xdef, d_xt, 1e-4, keys, vals, grad, pinned=d_pin), args.steps)
     asm_ms = timed(lambda: ctx.fem_assemble(mesh, d_x, d_xt, 1e-4, grad, pinned=d_pin), args.steps)
     # whole Newton linear solve from host positions: x in, direction out
     h_x = torch.from_numpy(np.ascontiguousarray(sc.verts.reshape(-1))).pin_memory()
@@ -873,6 +879,7 @@ def producer_gpu(args, ctx, sc, d_b, stream, dev):
     return {"what": "device element-Hessian producer (SURVEY 8f #1): inertia + 1,886,592 stable Neo-Hookean stencils "
                     "with PSD projection, stream in the reference's emission order",
             "tets": nt, "stream_entries": n + 10 * nt, "fem_emit_ms": emit_ms, "fem_assemble_ms": asm_ms,
+            "fem_emit_deformed_ms": emit_def_ms,
             "stream_bytes_written": 80 * (n + 10 * nt),
             "emit_write_gbs": 80 * (n + 10 * nt) / (emit_ms / 1e3) / 1e9,
             "newton_solve_from_host_positions_ms": newton_ms, "pcg_iters_per_solve": iters / args.steps,

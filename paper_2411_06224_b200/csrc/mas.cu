@@ -66,26 +66,78 @@ __device__ __forceinline__ void add_tile(double* D, int dim, int pr, int pc, con
         }
 }
 
+// One pass over A (solve order) restricts into every level in [first, n):
+// level 0 conflict-free (each dense element receives exactly one entry);
+// coarser levels by fp64 atomics, after the lanes of a warp (32 consecutive
+// entries: a few rows, their columns ascending) that hit the same coarse tile
+// have summed their contributions into the lowest such lane — a row's ~8
+// upper entries fall into 2-3 level-1 nodes, so most atomics disappear.
+// Each entry contributes ONE tile, oriented lower: H to (pr, pc) when
+// pr > pc, H^T to (pc, pr) when pr < pc, H + H^T (r != c) on the diagonal.
 __global__ void k_restrict(const std::uint32_t* __restrict__ rows, const std::uint32_t* __restrict__ cols,
                            const double* __restrict__ blocks, std::int64_t U, RestrictArgs ra) {
-    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < U;
-         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const std::int32_t r = rows[e], c = cols[e];
+    const int lane = threadIdx.x & 31;
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t e0 = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) - lane; e0 < U;
+         e0 += stride) {  // warp-uniform trip count: the warp intrinsics below need every lane
+        const std::int64_t e = e0 + lane;
+        const bool valid = e < U;
+        const std::int32_t r = valid ? rows[e] : 0, c = valid ? cols[e] : 0;
         double h[9];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) h[k] = blocks[blk(e, k)];
+        for (int k = 0; k < 9; ++k) h[k] = valid ? blocks[blk(e, k)] : 0.0;
         for (int l = ra.first; l < ra.n_levels; ++l) {
             const RestrictLevel& L = ra.lv[l];
             const std::int32_t nr = L.agg ? L.agg[r] : r;
             const std::int32_t nc = L.agg ? L.agg[c] : c;
-            const std::int32_t s = L.part_of[nr];
-            if (s != L.part_of[nc]) continue;
-            const int dim = 3 * (L.sub_ptr[s + 1] - L.sub_ptr[s]);
-            double* D = L.dense + L.dense_off[s];
-            const int pr = L.pos_of[nr], pc = L.pos_of[nc];
-            const bool atomic = l > 0;
-            add_tile(D, dim, pr, pc, h, false, atomic);
-            if (r != c) add_tile(D, dim, pc, pr, h, true, atomic);
+            const std::int32_t sd = L.part_of[nr];
+            const bool act = valid && sd == L.part_of[nc];
+            const int dim = act ? 3 * (L.sub_ptr[sd + 1] - L.sub_ptr[sd]) : 0;
+            double* D = act ? L.dense + L.dense_off[sd] : nullptr;
+            const int pr = act ? L.pos_of[nr] : 0, pc = act ? L.pos_of[nc] : 0;
+            if (l == 0) {  // conflict-free
+                if (act) {
+                    add_tile(D, dim, pr, pc, h, false, false);
+                    if (r != c) add_tile(D, dim, pc, pr, h, true, false);
+                }
+                continue;
+            }
+            const int pa = pr > pc ? pr : pc, pb = pr > pc ? pc : pr;
+            double t[9];
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {  // t column-major, tile (pa, pb)
+                    const double hij = h[3 * j + i], hji = h[3 * i + j];
+                    t[3 * j + i] = pr > pc ? hij : (pr < pc ? hji : (r != c ? hij + hji : hij));
+                }
+            const unsigned long long key =
+                act ? (static_cast<unsigned long long>(sd) << 24) | (static_cast<unsigned long long>(pa) << 12) |
+                          static_cast<unsigned long long>(pb)
+                    : ~0ull;
+            const unsigned grp = __match_any_sync(0xffffffffu, key);
+            const int rounds = __reduce_max_sync(0xffffffffu, act ? __popc(grp) : 1) - 1;
+            const bool lead = act && (__ffs(grp) - 1) == lane;
+            unsigned rest = grp & (grp - 1u);
+            for (int k = 0; k < rounds; ++k) {
+                const int src = rest ? __ffs(rest) - 1 : lane;
+#pragma unroll
+                for (int q = 0; q < 9; ++q) {
+                    const double a = __shfl_sync(0xffffffffu, t[q], src);
+                    if (lead && rest) t[q] += a;
+                }
+                rest &= rest - 1u;
+            }
+            if (lead) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        const int row = 3 * pa + i, col = 3 * pb + j;
+                        if (row < col) continue;
+                        atomicAdd(D + lpk_col(dim, col) + (row - col), t[3 * j + i]);
+                    }
+            }
         }
     }
 }

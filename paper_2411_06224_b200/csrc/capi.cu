@@ -182,7 +182,8 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     for (auto* b : {&c.ag_part, &c.ag_mem_ptr, &c.ag_members, &c.ag_pos, &c.ag_up, &c.ag_ncomp, &c.ag_cnt, &c.ag_adj[0],
                     &c.ag_adj[1]})
         b->free();
-    for (auto* b : {&c.ag_base, &c.ag_ptr[0], &c.ag_ptr[1]}) b->free();
+    for (auto* b : {&c.ag_base, &c.ag_ptr[0], &c.ag_ptr[1], &c.ag_koff}) b->free();
+    c.ag_kcnt.free();
     c.stage.free();
     c.fem_defer_m.free();
     c.fem_defer_t.free();

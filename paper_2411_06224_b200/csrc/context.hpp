@@ -178,6 +178,8 @@ struct Ctx {
     // (ping-pong between two buffers)
     DBuf<std::int32_t> ag_part, ag_mem_ptr, ag_members, ag_pos, ag_up, ag_ncomp, ag_cnt, ag_adj[2];
     DBuf<std::int64_t> ag_base, ag_ptr[2];
+    DBuf<std::int32_t> ag_kcnt;     // compacted super-node keys per fine node
+    DBuf<std::int64_t> ag_koff;
     int max_levels = 4;
     bool have_l0 = false;
     host::MasHierarchy hier;        // last built hierarchy (host copy)

@@ -1323,14 +1323,75 @@ __global__ void k_l1_up(std::int32_t n, const std::int32_t* __restrict__ part_of
         up[i] = static_cast<std::int32_t>(base[part_of[i]] + up[i]);
 }
 
-// one key (up[a] << 32 | up[b]) per directed fine adjacency entry a -> b
-__global__ void k_l1_keys(std::int32_t n, const std::int64_t* __restrict__ gptr, const std::int32_t* __restrict__ gadj,
-                          const std::int32_t* __restrict__ up, std::uint64_t* __restrict__ keys) {
-    for (std::int64_t a = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; a < n;
-         a += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const std::uint64_t ua = static_cast<std::uint64_t>(up[a]) << 32;
-        for (std::int64_t e = gptr[a]; e < gptr[a + 1]; ++e) keys[e] = ua | static_cast<std::uint32_t>(up[gadj[e]]);
+
+// The super-node keys without the ones the unique pass would drop anyway:
+// self loops (up[b] == up[a]) and a repeat of the previous neighbour's super
+// node (the adjacency is sorted by fine id, and fine neighbours of one super
+// node are mostly consecutive) — about a third of the fine edges survive, so
+// the bucket sort moves a third of the keys. One warp per fine node (affine-
+// body slots have tens of thousands of neighbours); count, then emit at a
+// scanned offset in the same order.
+__device__ __forceinline__ bool l1_key_kept(const std::int64_t* gptr, const std::int32_t* gadj, const std::int32_t* up,
+                                            std::int64_t a, std::int64_t e, std::int32_t ua, std::int32_t* ub) {
+    *ub = up[gadj[e]];
+    return *ub != ua && (e == gptr[a] || up[gadj[e - 1]] != *ub);
+}
+__global__ void k_l1_keycount(std::int32_t n, const std::int64_t* __restrict__ gptr, const std::int32_t* __restrict__ gadj,
+                              const std::int32_t* __restrict__ up, std::int32_t* __restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    for (std::int64_t a = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5; a < n;
+         a += (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const std::int32_t ua = up[a];
+        int c = 0;
+        for (std::int64_t e0 = gptr[a]; e0 < gptr[a + 1]; e0 += 32) {
+            const std::int64_t e = e0 + lane;
+            std::int32_t ub;
+            const bool keep = e < gptr[a + 1] && l1_key_kept(gptr, gadj, up, a, e, ua, &ub);
+            c += __popc(__ballot_sync(0xffffffffu, keep));
+        }
+        if (lane == 0) cnt[a] = c;
     }
+}
+__global__ void k_l1_keyemit(std::int32_t n, const std::int64_t* __restrict__ gptr, const std::int32_t* __restrict__ gadj,
+                             const std::int32_t* __restrict__ up, const std::int64_t* __restrict__ off,
+                             std::uint64_t* __restrict__ keys) {
+    const int lane = threadIdx.x & 31;
+    for (std::int64_t a = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5; a < n;
+         a += (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const std::int32_t ua = up[a];
+        std::int64_t o = off[a];
+        for (std::int64_t e0 = gptr[a]; e0 < gptr[a + 1]; e0 += 32) {
+            const std::int64_t e = e0 + lane;
+            std::int32_t ub = 0;
+            const bool keep = e < gptr[a + 1] && l1_key_kept(gptr, gadj, up, a, e, ua, &ub);
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep)
+                keys[o + __popc(m & ((1u << lane) - 1u))] =
+                    (static_cast<std::uint64_t>(ua) << 32) | static_cast<std::uint32_t>(ub);
+            o += __popc(m);
+        }
+    }
+}
+
+// the compacted super-node keys of graph (gptr, gadj) under the map up into
+// c.l1_keys; returns their count
+std::int64_t super_keys(Ctx& c, std::int32_t n, const std::int64_t* gptr, const std::int32_t* gadj,
+                        const std::int32_t* up) {
+    cudaStream_t st = c.stream;
+    c.ag_kcnt.reserve(static_cast<std::size_t>(std::max(n, 1)));
+    c.ag_koff.reserve(static_cast<std::size_t>(n) + 1);
+    k_l1_keycount<<<grid_for(n, 8, 16), 256, 0, st>>>(n, gptr, gadj, up, c.ag_kcnt.p);
+    ADIPC_LAUNCH_CHECK();
+    exclusive_scan(c.ag_kcnt.p, n, c.ag_koff.p, c.scan_scratch, st);
+    std::int64_t k = 0;
+    ADIPC_CUDA(cudaMemcpyAsync(&k, c.ag_koff.p + n, sizeof(k), cudaMemcpyDeviceToHost, st));
+    ADIPC_CUDA(cudaStreamSynchronize(st));
+    c.l1_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(k, 1)));
+    if (k > 0) {
+        k_l1_keyemit<<<grid_for(n, 8, 16), 256, 0, st>>>(n, gptr, gadj, up, c.ag_koff.p, c.l1_keys.p);
+        ADIPC_LAUNCH_CHECK();
+    }
+    return k;
 }
 
 // Level 0 -> 1 on the device; false when a level-0 subdomain has more than 32
@@ -1387,10 +1448,8 @@ bool level1_device(Ctx& c, const DeviceGraph& g0, std::vector<std::int32_t>& up1
     }
     lap("map + D2H");
     // super-node graph: bucket-sort the mapped adjacency, drop repeats and self loops
-    c.l1_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(g0.E, 1)));
-    k_l1_keys<<<grid_for(n, 256, 16), 256, 0, st>>>(n, g0.ptr, g0.adj, c.l1_up.p, c.l1_keys.p);
-    ADIPC_LAUNCH_CHECK();
-    bucket_sort(c, c.l1_keys.p, g0.E, n1, nullptr);
+    const std::int64_t nk = super_keys(c, n, g0.ptr, g0.adj, c.l1_up.p);
+    bucket_sort(c, c.l1_keys.p, nk, n1, nullptr);
     lap("keys + bucket sort");
     c.l1_cnt.reserve(static_cast<std::size_t>(n1) + 1);
     c.l1_ptr.reserve(static_cast<std::size_t>(n1) + 1);
@@ -1446,10 +1505,8 @@ bool agg_pass_device(Ctx& c, const host::Level& lv, const DeviceGraph& g, int ou
     ADIPC_CUDA(cudaStreamSynchronize(st));
     n_next = static_cast<std::int32_t>(total);
     if (n_next == n) return true;
-    c.l1_keys.reserve(static_cast<std::size_t>(std::max<std::int64_t>(g.E, 1)));
-    k_l1_keys<<<grid_for(n, 256, 16), 256, 0, st>>>(n, g.ptr, g.adj, c.ag_up.p, c.l1_keys.p);
-    ADIPC_LAUNCH_CHECK();
-    bucket_sort(c, c.l1_keys.p, g.E, n_next, nullptr);
+    const std::int64_t nk = super_keys(c, n, g.ptr, g.adj, c.ag_up.p);
+    bucket_sort(c, c.l1_keys.p, nk, n_next, nullptr);
     c.ag_cnt.reserve(static_cast<std::size_t>(n_next) + 1);
     c.ag_ptr[out].reserve(static_cast<std::size_t>(n_next) + 1);
     k_adj_count<<<grid_for(n_next, 8, 16), 256, 0, st>>>(n_next, c.sorted.p, c.row_start.p, c.ag_cnt.p);

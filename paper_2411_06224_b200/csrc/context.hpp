@@ -173,6 +173,7 @@ struct Ctx {
     DBuf<std::uint64_t> l1_keys;
     std::int64_t l1_E = 0;          // edges of the level-1 graph in l1_ptr / l1_adj
     HostStage stage, stage_up;      // pinned staging of the graphs / node maps that come down
+    host::Graph host_graph[3];      // host copies of the coarse graphs (capacity kept across rebuilds)
     // aggregation passes above level 1 on the device (cold build): the
     // level's member lists, the next level's node map, and its graph
     // (ping-pong between two buffers)

@@ -1249,8 +1249,9 @@ DeviceGraph level0_graph_device(Ctx& c) {
     return DeviceGraph{c.graph_ptr.p, c.graph_adj.p, E};
 }
 
-host::Graph graph_to_host(Ctx& c, const DeviceGraph& dg, std::int32_t n) {
-    host::Graph g;
+// into g, reusing its capacity (the host graphs are kept in the context, so a
+// rebuild does not page-fault fresh vectors)
+void graph_to_host(Ctx& c, const DeviceGraph& dg, std::int32_t n, host::Graph& g) {
     g.ptr.resize(static_cast<std::size_t>(n) + 1);
     g.adj.resize(static_cast<std::size_t>(dg.E));
     const std::size_t bp = sizeof(std::int64_t) * (static_cast<std::size_t>(n) + 1);
@@ -1261,6 +1262,10 @@ host::Graph graph_to_host(Ctx& c, const DeviceGraph& dg, std::int32_t n) {
     ADIPC_CUDA(cudaStreamSynchronize(c.stream));
     std::memcpy(g.ptr.data(), st, bp);
     if (ba) std::memcpy(g.adj.data(), st + bp, ba);
+}
+host::Graph graph_to_host(Ctx& c, const DeviceGraph& dg, std::int32_t n) {
+    host::Graph g;
+    graph_to_host(c, dg, n, g);
     return g;
 }
 
@@ -1463,7 +1468,7 @@ bool level1_device(Ctx& c, const DeviceGraph& g0, std::vector<std::int32_t>& up1
     k_adj_emit<<<grid_for(n1, 8, 16), 256, 0, st>>>(n1, c.sorted.p, c.row_start.p, c.l1_ptr.p, c.l1_adj.p);
     ADIPC_LAUNCH_CHECK();
     lap("unique count / emit");
-    g1 = graph_to_host(c, DeviceGraph{c.l1_ptr.p, c.l1_adj.p, E1}, n1);  // synchronises: up1 has landed too
+    graph_to_host(c, DeviceGraph{c.l1_ptr.p, c.l1_adj.p, E1}, n1, g1);  // synchronises: up1 has landed too
     std::memcpy(up1.data(), up_stage, sizeof(std::int32_t) * n);
     lap("graph D2H");
     c.l1_E = E1;
@@ -1551,7 +1556,8 @@ host::MasHierarchy hierarchy_from_level1(Ctx& c, std::vector<std::int32_t> up1, 
             break;
         }
         if (n_next == h.levels.back().n_nodes) break;
-        const host::Graph ghn = graph_to_host(c, gn, n_next);
+        host::Graph& ghn = c.host_graph[out];
+        graph_to_host(c, gn, n_next, ghn);
         lap("aggregation (device)", h.n_levels());
         host::append_level(h, std::move(up), n_next, ghn);
         lap("partition", h.n_levels() - 1);
@@ -1596,7 +1602,7 @@ void build_preconditioner(Ctx& c, PrecondKind kind) {
         const auto tg = std::chrono::steady_clock::now();
         std::vector<std::int32_t> up1;
         std::int32_t n1 = 0;
-        host::Graph g1;
+        host::Graph& g1 = c.host_graph[2];
         const bool dev_l1 = c.max_levels > 1 && c.l0.n_parts > 1 && level1_device(c, g0, up1, n1, g1);
         const auto ta = std::chrono::steady_clock::now();
         if (std::getenv("ADIPC_DEBUG_HIER"))

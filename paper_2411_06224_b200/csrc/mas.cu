@@ -1299,10 +1299,28 @@ __global__ void k_l1_components(std::int32_t n_parts, const std::int32_t* __rest
             if (gadj[mid] < lo) a = mid + 1;
             else b = mid;
         }
-        for (std::int64_t e = a, e1 = gptr[node + 1]; e < e1; ++e) {
-            const std::int32_t v = gadj[e];
-            if (v > hi) break;
-            if (part_of[v] == s) nb |= 1u << pos[v];
+        std::int64_t z = a, zb = gptr[node + 1];  // end of the window: first neighbour > hi
+        while (z < zb) {
+            const std::int64_t mid = (z + zb) >> 1;
+            if (gadj[mid] <= hi) z = mid + 1;
+            else zb = mid;
+        }
+        if (z - a <= 4 * m) {  // short window: scan it
+            for (std::int64_t e2 = a; e2 < z; ++e2) {
+                const std::int32_t v = gadj[e2];
+                if (part_of[v] == s) nb |= 1u << pos[v];
+            }
+        } else {  // long window (coarse levels: members spread in id): look each member up
+            for (int j = 0; j < m; ++j) {
+                const std::int32_t v = members[m0 + j];
+                std::int64_t x = a, y = z;
+                while (x < y) {
+                    const std::int64_t mid = (x + y) >> 1;
+                    if (gadj[mid] < v) x = mid + 1;
+                    else y = mid;
+                }
+                if (x < z && gadj[x] == v) nb |= 1u << j;
+            }
         }
     }
     int lab = lane;
@@ -1484,6 +1502,15 @@ bool agg_pass_device(Ctx& c, const host::Level& lv, const DeviceGraph& g, int ou
                      std::int32_t& n_next, DeviceGraph& g_next) {
     cudaStream_t st = c.stream;
     const std::int32_t n = lv.n_nodes, np = lv.n_parts;
+    const bool dbg = std::getenv("ADIPC_DEBUG_HIER") != nullptr;
+    auto t = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!dbg) return;
+        ADIPC_CUDA(cudaStreamSynchronize(c.stream));
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "      pass (n=%d): %s %.2f ms\n", n, what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    };
     std::vector<std::int32_t> mem_ptr(static_cast<std::size_t>(np) + 1, 0), members(n), pos(n);
     for (std::int32_t i = 0; i < n; ++i) pos[i] = mem_ptr[lv.part_of[i] + 1]++;
     for (std::int32_t s = 0; s < np; ++s)
@@ -1494,13 +1521,16 @@ bool agg_pass_device(Ctx& c, const host::Level& lv, const DeviceGraph& g, int ou
     upload(c.ag_mem_ptr, mem_ptr, st);
     upload(c.ag_members, members, st);
     upload(c.ag_pos, pos, st);
+    lap("member lists + uploads");
     c.ag_up.reserve(static_cast<std::size_t>(n));
     c.ag_ncomp.reserve(static_cast<std::size_t>(np));
     c.ag_base.reserve(static_cast<std::size_t>(np) + 1);
     k_l1_components<<<static_cast<int>(ceil_div(np, 8)), 256, 0, st>>>(np, c.ag_mem_ptr.p, c.ag_members.p, c.ag_part.p,
                                                                      c.ag_pos.p, g.ptr, g.adj, c.ag_up.p, c.ag_ncomp.p);
     ADIPC_LAUNCH_CHECK();
+    lap("components kernel");
     exclusive_scan(c.ag_ncomp.p, np, c.ag_base.p, c.scan_scratch, st);
+    lap("scan");
     k_l1_up<<<grid_for(n, 256, 16), 256, 0, st>>>(n, c.ag_part.p, c.ag_base.p, c.ag_up.p);
     ADIPC_LAUNCH_CHECK();
     std::int64_t total = 0;
@@ -1509,9 +1539,12 @@ bool agg_pass_device(Ctx& c, const host::Level& lv, const DeviceGraph& g, int ou
     ADIPC_CUDA(cudaMemcpyAsync(up.data(), c.ag_up.p, sizeof(std::int32_t) * n, cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaStreamSynchronize(st));
     n_next = static_cast<std::int32_t>(total);
+    lap("components + map + D2H");
     if (n_next == n) return true;
     const std::int64_t nk = super_keys(c, n, g.ptr, g.adj, c.ag_up.p);
+    lap("keys");
     bucket_sort(c, c.l1_keys.p, nk, n_next, nullptr);
+    lap("bucket sort");
     c.ag_cnt.reserve(static_cast<std::size_t>(n_next) + 1);
     c.ag_ptr[out].reserve(static_cast<std::size_t>(n_next) + 1);
     k_adj_count<<<grid_for(n_next, 8, 16), 256, 0, st>>>(n_next, c.sorted.p, c.row_start.p, c.ag_cnt.p);

@@ -955,12 +955,18 @@ class RefScene:
     compiled in place. meshes: dicts rest (n x 3), tets (local, m x 4),
     youngs, poisson, density; bodies: dicts rest, tets, kappa, density."""
 
-    def __init__(self, meshes, bodies, dt, ground=None):
+    def __init__(self, meshes, bodies, dt, ground=None, shells=()):
+        """shells (after the solid meshes in the scene's mesh order): dicts
+        rest, tris, density, thickness, stretch, strain_limit, shear_fraction,
+        bending."""
         if not reference_available():
             raise RuntimeError("oracle/_ref not built")
         L = self._L = C.CDLL(_REF_PATH)
         L.ref_scene_new.restype = vp
-        L.ref_scene_new.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, cd, ci, vp, cd]
+        L.ref_scene_new.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, cd, ci, vp, cd,
+                                    i32, vp, vp, vp, vp, vp]
+        L.ref_scene_shell_sizes.argtypes = [vp, vp, vp]
+        L.ref_scene_shell_export.argtypes = [vp] + [vp] * 7
         L.ref_scene_free.argtypes = [vp]
         L.ref_scene_sizes.argtypes = [vp, vp]
         L.ref_scene_export.argtypes = [vp] + [vp] * 14
@@ -979,12 +985,17 @@ class RefScene:
                       cat([b["tets"] for b in bodies], np.int32), begin([b["tets"] for b in bodies]),
                       np.array([b["kappa"] for b in bodies], np.float64),
                       np.array([b["density"] for b in bodies], np.float64),
-                      None if ground is None else np.ascontiguousarray(ground[0], np.float64)]
+                      None if ground is None else np.ascontiguousarray(ground[0], np.float64),
+                      cat([m["rest"] for m in shells], np.float64), begin([m["rest"] for m in shells]),
+                      cat([m["tris"] for m in shells], np.int32), begin([m["tris"] for m in shells]),
+                      np.array([[m["density"], m["thickness"], m["stretch"], m["strain_limit"], m["shear_fraction"],
+                                 m["bending"]] for m in shells], np.float64).reshape(-1)]
         k = self._keep
         p = lambda a: None if a is None or a.size == 0 else a.ctypes.data  # noqa: E731
         self.h = L.ref_scene_new(len(meshes), p(k[1]), p(k[0]), p(k[3]), p(k[2]), p(k[4]), p(k[5]), p(k[6]),
                                  len(bodies), p(k[8]), p(k[7]), p(k[10]), p(k[9]), p(k[11]), p(k[12]), float(dt),
-                                 int(ground is not None), p(k[13]), 0.0 if ground is None else float(ground[1]))
+                                 int(ground is not None), p(k[13]), 0.0 if ground is None else float(ground[1]),
+                                 len(shells), p(k[15]), p(k[14]), p(k[17]), p(k[16]), p(k[18]))
         sz = np.zeros(9, np.int64)
         L.ref_scene_sizes(self.h, sz.ctypes.data)
         (self.n_fem, self.n_bodies, self.n_blocks, self.n_nodes, n_tets, n_sv, n_e, n_t, n_m) = (int(v) for v in sz)
@@ -1000,6 +1011,21 @@ class RefScene:
                                       "body_volume", "abd_body", "jac36", "surf_verts", "edges", "tris")],
                            d["length_scale"].ctypes.data)
         d["tet_begin"] = np.r_[0, np.cumsum([len(m["tets"]) for m in meshes])].astype(np.int64)
+        d["mu"], d["lam"] = d["mu"][:len(meshes)], d["lam"][:len(meshes)]
+        if shells:
+            ntr, nh = np.zeros(1, np.int64), np.zeros(1, np.int64)
+            L.ref_scene_shell_sizes(self.h, ntr.ctypes.data, nh.ctypes.data)
+            sh = {"tris": np.zeros((int(ntr[0]), 3), np.int32), "tri_rest": np.zeros((int(ntr[0]), 5)),
+                  "hinges": np.zeros((int(nh[0]), 4), np.int32), "hinge_rest": np.zeros((int(nh[0]), 2)),
+                  "material": np.zeros((len(shells), 5)), "tri_count": np.zeros(len(shells), np.int64),
+                  "hinge_count": np.zeros(len(shells), np.int64)}
+            L.ref_scene_shell_export(self.h, *[p(sh[k_]) if sh[k_].size else None for k_ in
+                                               ("tris", "tri_rest", "hinges", "hinge_rest", "material", "tri_count",
+                                                "hinge_count")])
+            sh["tri_begin"] = np.r_[0, np.cumsum(sh["tri_count"])].astype(np.int64)
+            sh["hinge_begin"] = np.r_[0, np.cumsum(sh["hinge_count"])].astype(np.int64)
+            d["shells"] = sh
+            d["mesh_kind"] = np.array([0] * len(meshes) + [1] * len(shells), np.int32)
         self.data = d
 
     def __del__(self):

@@ -598,7 +598,9 @@ void* ref_scene_new(std::int32_t n_meshes, const std::int64_t* vert_begin, const
                     const double* poisson, const double* density, std::int32_t n_bodies,
                     const std::int64_t* bvert_begin, const double* brest, const std::int64_t* btet_begin,
                     const std::int32_t* btets, const double* bkappa, const double* bdensity, double dt, int ground,
-                    const double* gnormal, double gheight) {
+                    const double* gnormal, double gheight, std::int32_t n_shells, const std::int64_t* svert_begin,
+                    const double* srest, const std::int64_t* stri_begin, const std::int32_t* stris,
+                    const double* smat6) {
     auto* r = new RefScene;
     Scene& sc = r->scene;
     sc.config.dt = dt;
@@ -618,6 +620,22 @@ void* ref_scene_new(std::int32_t n_meshes, const std::int64_t* vert_begin, const
         dm.solid.density = density[m];
         sc.meshes.push_back(std::move(dm));
     }
+    for (std::int32_t m = 0; m < n_shells; ++m) {  // shells after the solids (mesh order)
+        DeformableMesh dm;
+        dm.name = "shell" + std::to_string(m);
+        dm.is_shell = true;
+        for (std::int64_t v = svert_begin[m]; v < svert_begin[m + 1]; ++v) dm.rest.push_back(ld3(srest + 3 * v));
+        for (std::int64_t t = stri_begin[m]; t < stri_begin[m + 1]; ++t)
+            dm.tris.push_back({stris[3 * t], stris[3 * t + 1], stris[3 * t + 2]});
+        const double* mt = smat6 + 6 * m;  // density, thickness, stretch, strain limit, shear fraction, bending
+        dm.shell.density = mt[0];
+        dm.shell.thickness = mt[1];
+        dm.shell.stretch_stiffness = mt[2];
+        dm.shell.strain_limit_stiffness = mt[3];
+        dm.shell.shear_fraction = mt[4];
+        dm.shell.bending_stiffness = mt[5];
+        sc.meshes.push_back(std::move(dm));
+    }
     for (std::int32_t b = 0; b < n_bodies; ++b) {
         AffineBody ab;
         ab.name = "body" + std::to_string(b);
@@ -634,6 +652,49 @@ void* ref_scene_new(std::int32_t n_meshes, const std::int64_t* vert_begin, const
     return r;
 }
 void ref_scene_free(void* p) { delete static_cast<RefScene*>(p); }
+// shell meshes' derived data (after the solids, mesh order): GLOBAL triangles
+// and hinges, MembraneRest (Dm^-1 column-major 2x2, area), HingeRest (rest
+// angle, weight), per-shell material (thickness, stretch, strain limit, shear
+// fraction, bending) and per-shell triangle / hinge counts
+void ref_scene_shell_sizes(void* p, std::int64_t* n_tris, std::int64_t* n_hinges) {
+    const RefScene& r = *static_cast<RefScene*>(p);
+    *n_tris = *n_hinges = 0;
+    for (const auto& m : r.scene.meshes)
+        if (m.is_shell) {
+            *n_tris += static_cast<std::int64_t>(m.tris.size());
+            *n_hinges += static_cast<std::int64_t>(m.hinges.size());
+        }
+}
+void ref_scene_shell_export(void* p, std::int32_t* tris, double* tri_rest5, std::int32_t* hinges, double* hinge_rest2,
+                            double* material5, std::int64_t* tri_count, std::int64_t* hinge_count) {
+    const RefScene& r = *static_cast<RefScene*>(p);
+    const Scene& sc = r.scene;
+    std::int64_t t0 = 0, h0 = 0;
+    int si = 0;
+    for (std::size_t mi = 0; mi < sc.meshes.size(); ++mi) {
+        const auto& m = sc.meshes[mi];
+        if (!m.is_shell) continue;
+        const Index off = sc.mesh_offset[mi];
+        for (std::size_t t = 0; t < m.tris.size(); ++t, ++t0) {
+            for (int k = 0; k < 3; ++k) tris[3 * t0 + k] = m.tris[t][k] + off;
+            std::memcpy(tri_rest5 + 5 * t0, m.tri_rest_data[t].inv_rest_edges.data(), 32);
+            tri_rest5[5 * t0 + 4] = m.tri_rest_data[t].area;
+        }
+        for (std::size_t h = 0; h < m.hinges.size(); ++h, ++h0) {
+            for (int k = 0; k < 4; ++k) hinges[4 * h0 + k] = m.hinges[h][k] + off;
+            hinge_rest2[2 * h0] = m.hinge_rest_data[h].rest_angle;
+            hinge_rest2[2 * h0 + 1] = m.hinge_rest_data[h].weight;
+        }
+        material5[5 * si] = m.shell.thickness;
+        material5[5 * si + 1] = m.shell.stretch_stiffness;
+        material5[5 * si + 2] = m.shell.strain_limit_stiffness;
+        material5[5 * si + 3] = m.shell.shear_fraction;
+        material5[5 * si + 4] = m.shell.bending_stiffness;
+        tri_count[si] = static_cast<std::int64_t>(m.tris.size());
+        hinge_count[si] = static_cast<std::int64_t>(m.hinges.size());
+        ++si;
+    }
+}
 // sizes: n_fem, n_bodies, n_blocks, n_nodes, n_tets, n_surf_verts, n_edges, n_tris, n_meshes
 void ref_scene_sizes(void* p, std::int64_t* out) {
     const RefScene& r = *static_cast<RefScene*>(p);
@@ -662,6 +723,7 @@ void ref_scene_export(void* p, double* mass, double* inv9, double* vol, std::int
         const auto& m = sc.meshes[mi];
         const Index off = sc.mesh_offset[mi];
         for (Index v = 0; v < m.n_verts(); ++v) mass[off + v] = m.vertex_mass[v];
+        if (m.is_shell) continue;
         for (std::size_t t = 0; t < m.tets.size(); ++t, ++t0) {
             std::memcpy(inv9 + 9 * t0, m.tet_rest_data[t].inv_rest_edges.data(), 72);
             vol[t0] = m.tet_rest_data[t].volume;

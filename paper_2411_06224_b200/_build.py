@@ -57,7 +57,7 @@ def _compile(src: str, verbose: bool) -> str:
         # the contact producer decides which stencils are active by the exact
         # dual value (contact/distance.hpp's pd.dist2 < dhat^2): no FMA
         # contraction there, so its arithmetic is the oracle's to the bit
-        extra = PER_FILE_FLAGS.get(src, [])
+        extra = PER_FILE_FLAGS.get(src, []) + os.environ.get("ADIPC_NVCC_EXTRA", "").split()  # timing experiments
         cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", path, "-o", obj]
     else:
         cmd = [CXX, *CXX_FLAGS, "-fopenmp", "-I", os.path.join(ROOT, "include"), "-c", path, "-o", obj]

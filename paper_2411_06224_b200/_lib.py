@@ -9,7 +9,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-GPU_LIB = os.path.join(PKG, "libadipc_gpu.so")
+GPU_LIB = os.environ.get("ADIPC_GPU_LIB") or os.path.join(PKG, "libadipc_gpu.so")  # env: an A/B build (tools/)
 
 u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")

@@ -120,21 +120,15 @@ Partition partition_block_graph(Index v, const Graph& g, Index capacity) {
         }
         comp_ptr.push_back(static_cast<std::int64_t>(order.size()));
     }
-    std::vector<char> assigned(v, 0);
-    // the carving frontier as a bucket queue: bucket k holds the unassigned
-    // neighbours of the open cluster with k connections into it; the pick —
-    // most connections, ties to the lowest id — scans only the top bucket.
-    // conn[] / slot[] locate a node (conn 0: not a candidate).
-    std::vector<Index> conn(v, 0), slot(v, 0);
+    // the carving frontier as a bucket queue with lazy deletion: a
+    // candidate whose connection count into the open cluster rises to k is
+    // appended to bucket k and its older entries go stale (valid iff the
+    // node's conn still equals the bucket index); the pick — most
+    // connections, ties to the lowest id — compacts the top bucket while it
+    // takes the minimum. conn: -1 = assigned, 0 = not a candidate.
+    std::vector<Index> conn(v, 0);
     std::vector<std::vector<Index>> bucket(1);
     int top = 0;
-    auto bucket_remove = [&](Index x) {
-        std::vector<Index>& bk = bucket[conn[x]];
-        const Index last = bk.back();
-        bk[slot[x]] = last;
-        slot[last] = slot[x];
-        bk.pop_back();
-    };
     Index next_part = 0, open_part = kInvalid, open_fill = 0;
     const std::size_t n_comps = comp_ptr.size() - 1;
     for (std::size_t ci = 0; ci < n_comps; ++ci) {
@@ -155,38 +149,43 @@ Partition partition_block_graph(Index v, const Graph& g, Index capacity) {
         while (left > 0) {
             const Index target = chunk < chunks ? base + (chunk < extra ? 1 : 0) : capacity;
             ++chunk;
-            while (assigned[comp[seed_at]]) ++seed_at;
+            while (conn[comp[seed_at]] < 0) ++seed_at;
             Index pick = comp[seed_at];
             const Index part = next_part++;
             for (Index fill = 0; pick != kInvalid;) {
                 p.part_of[pick] = part;
-                assigned[pick] = 1;
+                conn[pick] = -1;
                 ++fill;
                 --left;
                 if (fill == target || left == 0) break;
-                for (std::int64_t k = g.ptr[pick]; k < g.ptr[pick + 1]; ++k) {
-                    const Index nb = g.adj[k];
-                    if (assigned[nb]) continue;
-                    if (conn[nb] > 0) bucket_remove(nb);
+                const Index* nb_end = g.adj.data() + g.ptr[pick + 1];
+                for (const Index* it = g.adj.data() + g.ptr[pick]; it != nb_end; ++it) {
+                    const Index nb = *it;
+                    if (conn[nb] < 0) continue;
                     const Index c = ++conn[nb];
                     if (c >= static_cast<Index>(bucket.size())) bucket.resize(static_cast<std::size_t>(c) + 1);
-                    slot[nb] = static_cast<Index>(bucket[c].size());
                     bucket[c].push_back(nb);
                     if (c > top) top = c;
                 }
-                while (top > 0 && bucket[top].empty()) --top;
-                if (top == 0) {
-                    pick = kInvalid;
-                    break;
+                pick = kInvalid;
+                for (; top > 0; --top) {
+                    std::vector<Index>& bk = bucket[top];
+                    std::size_t w = 0;
+                    for (std::size_t k = 0; k < bk.size(); ++k) {
+                        const Index x = bk[k];
+                        if (conn[x] != top) continue;
+                        bk[w++] = x;
+                        pick = (pick == kInvalid || x < pick) ? x : pick;
+                    }
+                    bk.resize(w);
+                    if (w) break;
                 }
-                const std::vector<Index>& bk = bucket[top];
-                pick = bk[0];
-                for (std::size_t k = 1; k < bk.size(); ++k) pick = bk[k] < pick ? bk[k] : pick;
-                bucket_remove(pick);
-                conn[pick] = 0;
+                if (pick == kInvalid) break;
+                conn[pick] = 0;  // its entry goes stale
             }
             for (int k = 1; k <= top; ++k) {
-                for (Index x : bucket[k]) conn[x] = 0;
+                for (Index x : bucket[k])
+                    if (conn[x] > 0) conn[x] = 0;
                 bucket[k].clear();
             }
             top = 0;

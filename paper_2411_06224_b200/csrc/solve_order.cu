@@ -254,18 +254,26 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
     for (int i = half * 32 + lane; i < kStages * slot_doubles; i += 64) ring[i] = 0.0;
     fence_proxy_async();
     pair_sync(pair);
-    auto issue = [&](std::int32_t q, int st) {  // one thread of the pair
-        const int l = level_of(q);
-        const std::int32_t s = q - pt.base[l];
-        const std::int64_t o = pt.inv_off[l][s];
-        const std::uint32_t bytes = static_cast<std::uint32_t>((pt.inv_off[l][s + 1] - o) * 8);
+    // one thread of the pair: the inverse of packed offset range [o, o1) of level l
+    auto issue_at = [&](int l, std::int64_t o, std::int64_t o1, int st) {
+        const std::uint32_t bytes = static_cast<std::uint32_t>((o1 - o) * 8);
         mbar_arrive_expect_tx(&bar[st], bytes);
         if (l == 0)  // streamed once per application
             bulk_g2s_evict_first(ring + static_cast<std::size_t>(st) * slot_doubles, pt.inv[0] + o, bytes, &bar[st]);
-        else  // coarse inverses (~26 MB at cfg5) and the kept share of level 0 stay L2-resident across iterations
+        else  // coarse inverses (~26 MB at cfg5) stay L2-resident across iterations
             bulk_g2s_evict_last(ring + static_cast<std::size_t>(st) * slot_doubles, pt.inv[l] + o, bytes, &bar[st]);
     };
-    if (half == 0 && lane == 0) {
+    auto issue = [&](std::int32_t q, int st) {
+        const int l = level_of(q);
+        const std::int32_t s = q - pt.base[l];
+#if ADIPC_PC_EXP == 3  // timing experiment: every item reads subdomain s % 64's inverse (L2-resident)
+        issue_at(l, pt.inv_off[l][s % 64], pt.inv_off[l][s % 64 + 1], st);
+#else
+        issue_at(l, pt.inv_off[l][s], pt.inv_off[l][s + 1], st);
+#endif
+    };
+    const bool leader = half == 0 && lane == 0;
+    if (leader) {
         for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
         fence_mbar_init();
         for (int st = 0; st < kStages && st < nloc; ++st) issue(item(st), st);
@@ -275,25 +283,43 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
     // the predecessor (update pass) drains; its outputs are read from here on
     pdl_wait();
     if (flags && flags[F_DONE]) {  // PCG already finished: drain the issued copies, leave
-        if (half == 0 && lane == 0)
+        if (leader)
             for (int st = 0; st < kStages && st < nloc; ++st) mbar_wait(&bar[st], 0);
         return;
     }
     pdl_launch();
-    // b of a work item and the addresses of its rows (gathered for coarse levels)
+    // Every global load on an item's critical path is issued one item ahead
+    // of its use: the subdomain range (sub_ptr) two items ahead, the residual
+    // gathers of the next item, and (leader) the packed-inverse offsets of
+    // the refill — so the pair never waits on a dependent load round trip
+    // between the ring slot landing and its refill being issued.
     struct Item {
         int l;
         std::int32_t s0, dim;
+    };
+    struct Meta {  // sub_ptr[s], sub_ptr[s + 1] of an item (loads in flight)
+        int l;
+        std::int32_t lo, hi;
+    };
+    auto meta_load = [&](int idx, Meta& m) {
+        m.l = 0;
+        m.lo = m.hi = 0;
+        if (idx < nloc) {
+            const std::int32_t q = item(idx);
+            m.l = level_of(q);
+            const std::int32_t s = q - pt.base[m.l];
+            m.lo = ldg_issue(pt.sub_ptr[m.l] + s);
+            m.hi = ldg_issue(pt.sub_ptr[m.l] + s + 1);
+        }
     };
     auto row_index = [&](const Item& it, int j) -> std::int64_t {
         if (it.l == 0) return 3 * static_cast<std::int64_t>(it.s0) + j;
         return 3 * static_cast<std::int64_t>(pt.sub_nodes[it.l][it.s0 + j / 3]) + (j % 3);
     };
-    auto load_b = [&](std::int32_t q, Item& it, double* bb) {
-        it.l = level_of(q);
-        const std::int32_t s = q - pt.base[it.l];
-        it.s0 = pt.sub_ptr[it.l][s];
-        it.dim = 3 * (pt.sub_ptr[it.l][s + 1] - it.s0);
+    auto load_b = [&](const Meta& m, Item& it, double* bb) {
+        it.l = m.l;
+        it.s0 = m.lo;
+        it.dim = 3 * (m.hi - m.lo);
 #pragma unroll
         for (int t = 0; t < RB; ++t) {
             const int j = lane + 32 * t;
@@ -302,7 +328,13 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
     };
     Item cur{0, 0, 0};
     double b[RB];
-    if (nloc > 0) load_b(item(0), cur, b);
+    Meta mn;  // item i + 1
+    {
+        Meta m0;
+        meta_load(0, m0);
+        meta_load(1, mn);
+        load_b(m0, cur, b);
+    }
     double dsum = 0;
     int st = 0;
     std::uint32_t par = 0;
@@ -310,28 +342,42 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
 #pragma unroll
         for (int t = 0; t < RB; ++t)
             if (lane + 32 * t < kK) bs[lane + 32 * t] = b[t];
+        // refill target (leader): offsets of item i + kStages
+        int rl = 0;
+        std::int64_t ro = 0, ro1 = 0;
+        if (leader && i + kStages < nloc) {
+            const std::int32_t q = item(i + kStages);
+            rl = level_of(q);
+#if ADIPC_PC_EXP == 3
+            const std::int32_t s = (q - pt.base[rl]) % 64;
+#else
+            const std::int32_t s = q - pt.base[rl];
+#endif
+            ro = ldg_issue(pt.inv_off[rl] + s);
+            ro1 = ldg_issue(pt.inv_off[rl] + s + 1);
+        }
         Item nxt{0, 0, 0};
         double bn[RB];
-        if (i + 1 < nloc) load_b(item(i + 1), nxt, bn);
+        if (i + 1 < nloc) load_b(mn, nxt, bn);
+        Meta mnn;
+        meta_load(i + 2, mnn);
         __syncwarp();
         mbar_wait(&bar[st], par);
         const double* M = ring + static_cast<std::size_t>(st) * slot_doubles;
         double* out = pt.out[cur.l];
-        auto refill = [&] {
-            pair_sync(pair);  // both warps are done with the slot
-            if (half == 0 && lane == 0 && i + kStages < nloc) {  // refill kStages items ahead
-                fence_proxy_async();
-                issue(item(i + kStages), st);
-            }
-        };
         dsum += pair_solve<kK>(M, bs, lane, half, cur.dim,
                                    [&](int j, double v) { out[row_index(cur, j)] = v; });
-        refill();  // also orders the next item's bs writes after both warps' reads
+        pair_sync(pair);  // both warps are done with the slot (and with bs before its next write)
+        if (leader && i + kStages < nloc) {
+            fence_proxy_async();
+            issue_at(rl, ro, ro1, st);
+        }
         if (++st == kStages) {
             st = 0;
             par ^= 1u;
         }
         cur = nxt;
+        mn = mnn;
 #pragma unroll
         for (int t = 0; t < RB; ++t) b[t] = bn[t];
     }

@@ -92,6 +92,17 @@ __device__ __forceinline__ double ldg_issue(const double* ptr) {
     return v;
 }
 
+__device__ __forceinline__ std::int32_t ldg_issue(const std::int32_t* ptr) {
+    std::int32_t v;
+    asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(ptr));
+    return v;
+}
+__device__ __forceinline__ std::int64_t ldg_issue(const std::int64_t* ptr) {
+    std::int64_t v;
+    asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(v) : "l"(ptr));
+    return v;
+}
+
 // Fire-and-forget fp64 add to global memory. Spelled out as `red` because
 // nvcc emits ATOMG (with a return path through L1) instead of REDG for
 // atomicAdd in kernels that also use a returning atomic + fence (the

@@ -56,8 +56,8 @@ int main(int argc, char** argv) {
     printf("%-40s %7.1f us  %6.2f TB/s  (%s)\n", name, best * 1000, total / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   };
   run([&] { k_ldg<<<148 * 8, 256>>>((const double2*)src, total / 16, out); }, "LDG.128 grid-stride");
-  int Ss[] = {4096, 8192, 16384};
-  for (int S : Ss) for (int warps : {4, 8}) {
+  int Ss[] = {4096, 9408, 16384};
+  for (int S : Ss) for (int warps : {4, 8, 10}) {
     for (int D : {2, 3, 4}) {
       size_t smem = (size_t)warps * D * S + warps * D * 8;
       if (smem > 227 * 1024) continue;

@@ -190,11 +190,6 @@ __device__ __forceinline__ int matvec_row(int lane, int t) {
 #ifndef ADIPC_PC_ACC
 #define ADIPC_PC_ACC 4
 #endif
-// timing experiments only (tools/): 1 = two columns per row instead of kK,
-// i.e. the ring / pipeline skeleton without the mat-vec (wrong results)
-#ifndef ADIPC_PC_EXP
-#define ADIPC_PC_EXP 0
-#endif
 template <int kK, int kRow0, int kRows>
 __device__ __forceinline__ void packed_matvec_rows(const double* M, const double* bs, double* y, int lane) {
     constexpr int R = (kRows + 31) / 32;
@@ -217,7 +212,7 @@ __device__ __forceinline__ void packed_matvec_rows(const double* M, const double
         for (int t = 0; t < R; ++t) acc[q][t] = 0.0;
     const double2* b2 = reinterpret_cast<const double2*>(bs);
 #pragma unroll
-    for (int k2 = 0; k2 < (ADIPC_PC_EXP == 1 ? 2 : kK); k2 += 2) {
+    for (int k2 = 0; k2 < kK; k2 += 2) {
         const double2 bb = b2[k2 >> 1];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {

@@ -266,11 +266,7 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
     auto issue = [&](std::int32_t q, int st) {
         const int l = level_of(q);
         const std::int32_t s = q - pt.base[l];
-#if ADIPC_PC_EXP == 3  // timing experiment: every item reads subdomain s % 64's inverse (L2-resident)
-        issue_at(l, pt.inv_off[l][s % 64], pt.inv_off[l][s % 64 + 1], st);
-#else
         issue_at(l, pt.inv_off[l][s], pt.inv_off[l][s + 1], st);
-#endif
     };
     const bool leader = half == 0 && lane == 0;
     if (leader) {
@@ -348,11 +344,7 @@ __global__ void __launch_bounds__(320) k_precond_so(PrecondTable pt, double* __r
         if (leader && i + kStages < nloc) {
             const std::int32_t q = item(i + kStages);
             rl = level_of(q);
-#if ADIPC_PC_EXP == 3
-            const std::int32_t s = (q - pt.base[rl]) % 64;
-#else
             const std::int32_t s = q - pt.base[rl];
-#endif
             ro = ldg_issue(pt.inv_off[rl] + s);
             ro1 = ldg_issue(pt.inv_off[rl] + s + 1);
         }

@@ -32,6 +32,8 @@ namespace {
 constexpr int kWarpSortMax = 128;   // rows up to this length: one warp, register bitonic
 constexpr int kCtaSortMax = 8192;   // rows up to this length: one CTA, smem bitonic
 constexpr int kCtaSortThreads = 1024;
+constexpr int kHugeRow = 4 * kCtaSortMax;  // longer rows: multi-CTA chunk sort + merge-path passes
+constexpr int kMergeTile = 4096;           // output elements per CTA of a merge pass
 
 // The triplet stream as the kernels see it: up to two segments (the DOF
 // stream, then the reduced contact tiles appended by two_level_abd_reduce,
@@ -238,6 +240,8 @@ __device__ __forceinline__ int warp_sort_row(std::uint64_t* seg, int len, int la
 __global__ void k_sort_rows_warp(std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
                                  std::int32_t n, std::int32_t* __restrict__ uniq_cnt,
                                  std::int32_t* __restrict__ big_rows, std::int32_t* __restrict__ n_big) {
+    // n_big[0]: rows for k_sort_rows_cta (listed from big_rows[0] up);
+    // n_big[1]: rows > kHugeRow (listed from big_rows[n - 1] down), n_big[2]: their longest
     const int lane = threadIdx.x & 31;
     const std::int32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const std::int32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -255,7 +259,14 @@ __global__ void k_sort_rows_warp(std::uint64_t* __restrict__ sorted, const std::
         else if (len <= kWarpSortMax)
             uniq = warp_sort_row<4>(seg, len, lane);
         else {
-            if (lane == 0) big_rows[atomicAdd(n_big, 1)] = r;
+            if (lane == 0) {
+                if (len > kHugeRow) {
+                    big_rows[n - 1 - atomicAdd(n_big + 1, 1)] = r;
+                    atomicMax(n_big + 2, len);
+                } else {
+                    big_rows[atomicAdd(n_big, 1)] = r;
+                }
+            }
             continue;
         }
         if (lane == 0) uniq_cnt[r] = uniq;
@@ -345,6 +356,102 @@ __global__ void k_sort_rows_cta(std::uint64_t* __restrict__ sorted, std::uint64_
             uniq_cnt[r] = t;
         }
         __syncthreads();
+    }
+}
+
+// Rows longer than kHugeRow (contact rows of affine bodies: hundreds of
+// thousands of entries) are sorted by the whole GPU instead of one CTA:
+// every kCtaSortMax chunk of every such row by its own CTA (shared-memory
+// bitonic), then log2 merge passes in which every kMergeTile-element tile
+// of the output is one CTA (merge-path split of its pair of runs), ping-pong
+// between `sorted` and `scratch`, and a final pass that moves odd-pass rows
+// back and counts the unique columns. Rows are big_rows[n - 1 - y].
+__device__ __forceinline__ int merge_split(const std::uint64_t* a, int na, const std::uint64_t* b, int nb, int d) {
+    int lo = max(0, d - nb), hi = min(d, na);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= b[d - mid - 1])
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ int huge_passes(int len) {
+    int p = 0;
+    for (int w = kCtaSortMax; w < len; w <<= 1) ++p;
+    return p;
+}
+__global__ void __launch_bounds__(kCtaSortThreads) k_huge_chunks(std::uint64_t* __restrict__ sorted,
+                                                                 const std::int64_t* __restrict__ row_start,
+                                                                 const std::int32_t* __restrict__ huge_tail,
+                                                                 std::int32_t* __restrict__ uniq_cnt) {
+    extern __shared__ std::uint64_t s[];
+    const std::int32_t r = huge_tail[-1 - static_cast<int>(blockIdx.y)];
+    const std::int64_t b = row_start[r];
+    const int len = static_cast<int>(row_start[r + 1] - b);
+    const int c0 = static_cast<int>(blockIdx.x) * kCtaSortMax;
+    if (c0 >= len) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) uniq_cnt[r] = 0;  // k_huge_finish adds the tiles' heads
+    std::uint64_t* seg = sorted + b + c0;
+    const int cl = min(kCtaSortMax, len - c0);
+    int N = 2;
+    while (N < cl) N <<= 1;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s[i] = i < cl ? seg[i] : ~0ull;
+    __syncthreads();
+    bitonic<false>(s, N, threadIdx.x, blockDim.x);
+    for (int i = threadIdx.x; i < cl; i += blockDim.x) seg[i] = s[i];
+}
+__global__ void __launch_bounds__(256) k_huge_merge(std::uint64_t* __restrict__ sorted,
+                                                    std::uint64_t* __restrict__ scratch,
+                                                    const std::int64_t* __restrict__ row_start,
+                                                    const std::int32_t* __restrict__ huge_tail, int width, int pass) {
+    __shared__ int split[2];
+    const std::int32_t r = huge_tail[-1 - static_cast<int>(blockIdx.y)];
+    const std::int64_t b = row_start[r];
+    const int len = static_cast<int>(row_start[r + 1] - b);
+    const int g0 = static_cast<int>(blockIdx.x) * kMergeTile;
+    if (len <= width || g0 >= len) return;  // row already merged / tile past its end
+    const std::uint64_t* src = ((pass & 1) ? scratch : sorted) + b;
+    std::uint64_t* dst = ((pass & 1) ? sorted : scratch) + b;
+    const int a0 = g0 / (2 * width) * (2 * width);  // kMergeTile divides 2 width
+    const int na = min(width, len - a0);
+    const int nb = min(width, max(0, len - a0 - width));
+    const std::uint64_t* A = src + a0;
+    const std::uint64_t* B = A + na;
+    const int d0 = g0 - a0, d1 = min(d0 + kMergeTile, na + nb);
+    if (threadIdx.x < 2) split[threadIdx.x] = merge_split(A, na, B, nb, threadIdx.x ? d1 : d0);
+    __syncthreads();
+    const int i0 = split[0], i1 = split[1];
+    cta_merge(A + i0, i1 - i0, B + (d0 - i0), (d1 - i1) - (d0 - i0), dst + a0 + d0);
+}
+__global__ void __launch_bounds__(256) k_huge_finish(std::uint64_t* __restrict__ sorted,
+                                                     const std::uint64_t* __restrict__ scratch,
+                                                     const std::int64_t* __restrict__ row_start,
+                                                     const std::int32_t* __restrict__ huge_tail,
+                                                     std::int32_t* __restrict__ uniq_cnt) {
+    __shared__ int red[8];
+    const std::int32_t r = huge_tail[-1 - static_cast<int>(blockIdx.y)];
+    const std::int64_t b = row_start[r];
+    const int len = static_cast<int>(row_start[r + 1] - b);
+    const int g0 = static_cast<int>(blockIdx.x) * kMergeTile;
+    if (g0 >= len) return;
+    const int g1 = min(g0 + kMergeTile, len);
+    const bool odd = huge_passes(len) & 1;
+    const std::uint64_t* fin = (odd ? scratch : sorted) + b;
+    int h = 0;
+    for (int i = g0 + static_cast<int>(threadIdx.x); i < g1; i += blockDim.x) {
+        const std::uint64_t v = fin[i];
+        h += (i == 0 || (v >> 32) != (fin[i - 1] >> 32)) ? 1 : 0;
+        if (odd) sorted[b + i] = v;
+    }
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = h;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
+        atomicAdd(&uniq_cnt[r], t);
     }
 }
 
@@ -446,12 +553,13 @@ __device__ __forceinline__ void reduce_range(const std::uint64_t* __restrict__ s
 __global__ void __launch_bounds__(32 * kReduceWarps, 3) k_reduce_rows(
     const std::uint64_t* __restrict__ sorted, const std::int64_t* __restrict__ row_start,
     const std::int64_t* __restrict__ uniq_start, std::int32_t n, StreamSrc s, std::uint32_t* __restrict__ out_rows,
-    std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks) {
+    std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks, std::int64_t max_len) {
     __shared__ double tile[kReduceWarps][9][33];
     __shared__ double carry[kReduceWarps][9];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
     for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps)
+        if (row_start[r + 1] - row_start[r] <= max_len)  // longer rows: k_reduce_segments
         reduce_range(sorted, r, row_start[r], row_start[r + 1], uniq_start[r], s, out_rows, out_cols, out_blocks,
                      tile[w], carry[w], lane);
 }
@@ -461,11 +569,17 @@ __global__ void __launch_bounds__(32 * kReduceWarps, 3) k_reduce_rows(
 // heads, so one warp per SEGMENT reduces them; the runs stay whole and each
 // is still summed left to right (bitwise the per-row path).
 constexpr std::int64_t kSegLen = 1024;
+// rows longer than this go through the segments; the others stay with
+// k_reduce_rows (one warp per row) in the same assembly
+constexpr std::int64_t kLongRow = 4 * kSegLen;
 
 __global__ void k_seg_count(const std::int64_t* __restrict__ row_start, std::int32_t n, std::int32_t* __restrict__ cnt) {
     for (std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; r < n;
          r += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
-        cnt[r] = static_cast<std::int32_t>(ceil_div(row_start[r + 1] - row_start[r], kSegLen));
+    {
+        const std::int64_t len = row_start[r + 1] - row_start[r];
+        cnt[r] = len > kLongRow ? static_cast<std::int32_t>(ceil_div(len, kSegLen)) : 0;
+    }
 }
 __global__ void k_seg_rows(const std::int64_t* __restrict__ item_ptr, std::int32_t n, std::int32_t* __restrict__ item_row) {
     for (std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; r < n;
@@ -509,17 +623,187 @@ __global__ void k_seg_heads(const std::uint64_t* __restrict__ sorted, const std:
         }
     }
 }
-__global__ void __launch_bounds__(32 * kReduceWarps, 3) k_reduce_segments(
+// 8-byte asynchronous global -> shared copy (LDGSTS) and its group fences
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// reduce_range for long segments (affine-body rows: runs of tens of
+// thousands of entries, one sequential chain each): the same windows and the
+// same left-to-right run sums, but the window's keys are fetched kKeyAhead
+// windows ahead and its 288 value words kValAhead windows ahead by
+// asynchronous copies into per-warp shared rings, so a long run's chain no
+// longer waits two dependent global round trips (key, then value) per window.
+// Every iteration commits exactly one cp.async group: the keys of window
+// w + kKeyAhead and the values of window w + kValAhead.
+constexpr int kValAhead = 3, kKeyAhead = 6;
+constexpr int kSegWarps = 4;
+struct SegRing {
+    double v[kValAhead][9][33];
+    std::uint64_t k[kKeyAhead][32];
+    double carry[9];
+};
+__device__ __forceinline__ void reduce_range_pipe(const std::uint64_t* __restrict__ sorted, std::int32_t r,
+                                                  std::int64_t b, std::int64_t e, std::int64_t u, const StreamSrc& s,
+                                                  std::uint32_t* __restrict__ out_rows,
+                                                  std::uint32_t* __restrict__ out_cols,
+                                                  double* __restrict__ out_blocks, SegRing& R, int lane) {
+    const std::int64_t nwin = (e - b + 31) >> 5;
+    auto issue_keys = [&](std::int64_t w) {
+        if (w >= nwin) return;
+        const std::int64_t p = b + 32 * w + lane;
+        std::uint64_t* d = &R.k[w % kKeyAhead][lane];
+        if (p < e)
+            cp_async8(d, sorted + p);
+        else
+            *d = ~0ull;
+    };
+    auto issue_vals = [&](std::int64_t w) {  // keys of w have landed (and are visible to the warp)
+        if (w >= nwin) return;
+        const std::int64_t base = b + 32 * w;
+        const int nv = static_cast<int>(e - base < 32 ? e - base : 32);
+        double (*T)[33] = R.v[w % kValAhead];
+        const std::uint64_t* kw = R.k[w % kKeyAhead];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            const int word = 32 * k + lane;
+            const int j = word / 9, el = word - 9 * j;
+            if (j < nv) {
+                const double* sv = s.value(static_cast<std::uint32_t>(kw[j]));
+                if (sv)
+                    cp_async8(&T[el][j], sv + el);
+                else
+                    T[el][j] = (el & 3) == 0 ? 1.0 : 0.0;  // appended pinned-diagonal identity
+            }
+        }
+    };
+    // prologue: the keys of the first kKeyAhead windows (waited for), then
+    // kValAhead groups P_j = {values of window j}. With the loop's groups
+    // I_w = {values of w + kValAhead, keys of w + kKeyAhead}, the group
+    // sequence P_0.., I_0.. has the values of window w at position w and the
+    // keys of window w + kValAhead (kKeyAhead = 2 kValAhead) at position w
+    // or in the prologue, so waiting for all but the newest kValAhead - 1
+    // groups at the top of iteration w covers both.
+    for (int w = 0; w < kKeyAhead; ++w) issue_keys(w);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    for (int j = 0; j < kValAhead; ++j) {
+        issue_vals(j);
+        cp_async_commit();
+    }
+    bool carried = false;
+    std::int64_t carry_u = 0;
+    std::uint32_t prev_last = 0;  // column of the previous window's last entry
+    for (std::int64_t w = 0; w < nwin; ++w) {
+        cp_async_wait<kValAhead - 1>();
+        __syncwarp();
+        const std::int64_t base = b + 32 * w;
+        const int nv = static_cast<int>(e - base < 32 ? e - base : 32);
+        double (*Tl)[33] = R.v[w % kValAhead];
+        const std::uint64_t v = R.k[w % kKeyAhead][lane];
+        const bool valid = lane < nv;
+        const std::uint32_t col = static_cast<std::uint32_t>(v >> 32);
+        const std::uint32_t prev_col = __shfl_up_sync(0xffffffffu, col, 1);
+        const bool head = valid && (lane == 0 ? (w == 0 || prev_last != col) : prev_col != col);
+        // does the window's last run continue past it?
+        const bool cont_out = __shfl_sync(0xffffffffu,
+                                          w + 1 < nwin && lane == 31 &&
+                                              static_cast<std::uint32_t>(R.k[(w + 1) % kKeyAhead][0] >> 32) == col,
+                                          31);
+        prev_last = __shfl_sync(0xffffffffu, col, 31);
+        const unsigned hm = __ballot_sync(0xffffffffu, head);
+        if (hm <= 1u) {
+            // one run fills the window (the body of a long run): lane k < 9
+            // folds element k of the run's blocks, the nine chains in
+            // parallel instead of interleaved in one owner thread (same
+            // left-to-right order per element)
+            const std::int64_t my_u = hm ? u : carry_u;
+            if (lane < 9) {
+                double acc = hm ? Tl[lane][0] : __dadd_rn(R.carry[lane], Tl[lane][0]);
+#pragma unroll 8
+                for (int j = 1; j < nv; ++j) acc = __dadd_rn(acc, Tl[lane][j]);
+                if (cont_out)
+                    R.carry[lane] = acc;
+                else
+                    out_blocks[blk(my_u, lane)] = acc;
+            }
+            if (lane == 0 && !cont_out) {
+                out_rows[my_u] = static_cast<std::uint32_t>(r);
+                out_cols[my_u] = col;
+            }
+            if (cont_out) carry_u = my_u;
+            carried = cont_out;
+            u += __popc(hm);
+            __syncwarp();
+            issue_vals(w + kValAhead);
+            issue_keys(w + kKeyAhead);
+            cp_async_commit();
+            continue;
+        }
+        const bool owner = head || (lane == 0 && carried);
+        if (owner) {
+            const unsigned later = hm & ~((2u << lane) - 1u);
+            const int end = later ? __ffs(later) - 1 : nv;
+            double acc[9];
+            if (head) {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[k] = Tl[k][lane];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(R.carry[k], Tl[k][lane]);
+            }
+            for (int j = lane + 1; j < end; ++j)
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(acc[k], Tl[k][j]);
+            const std::int64_t my_u = head ? u + __popc(hm & ((1u << lane) - 1u)) : carry_u;
+            if (end == nv && cont_out) {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) R.carry[k] = acc[k];
+            } else {
+                out_rows[my_u] = static_cast<std::uint32_t>(r);
+                out_cols[my_u] = col;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) out_blocks[blk(my_u, k)] = acc[k];
+            }
+        }
+        if (cont_out) carry_u = hm ? u + __popc(hm) - 1 : carry_u;
+        carried = cont_out;
+        u += __popc(hm);
+        __syncwarp();  // slot w % kValAhead and key slot w % kKeyAhead are free again
+        issue_vals(w + kValAhead);
+        issue_keys(w + kKeyAhead);
+        cp_async_commit();
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(32 * kSegWarps) k_reduce_segments(
     const std::uint64_t* __restrict__ sorted, const std::int32_t* __restrict__ item_row,
-    const std::int64_t* __restrict__ seg, const std::int64_t* __restrict__ item_u, std::int64_t m, StreamSrc s,
-    std::uint32_t* __restrict__ out_rows, std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks) {
-    __shared__ double tile[kReduceWarps][9][33];
-    __shared__ double carry[kReduceWarps][9];
+    const std::int64_t* __restrict__ seg, const std::int64_t* __restrict__ item_u,
+    const std::int64_t* __restrict__ item_ptr, const std::int64_t* __restrict__ uniq_start, std::int64_t m,
+    StreamSrc s, std::uint32_t* __restrict__ out_rows, std::uint32_t* __restrict__ out_cols,
+    double* __restrict__ out_blocks) {
+    extern __shared__ __align__(16) unsigned char seg_smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    SegRing& R = reinterpret_cast<SegRing*>(seg_smem)[w];
     const std::int64_t warps = static_cast<std::int64_t>(gridDim.x) * (blockDim.x >> 5);
     for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * (blockDim.x >> 5) + w; i < m; i += warps)
-        reduce_range(sorted, item_row[i], seg[2 * i], seg[2 * i + 1], item_u[i], s, out_rows, out_cols, out_blocks,
-                     tile[w], carry[w], lane);
+    {
+        // item_u: heads scanned over the long rows' segments only; the row's
+        // output slots start at uniq_start[r]
+        const std::int32_t r = item_row[i];
+        const std::int64_t u = uniq_start[r] + item_u[i] - item_u[item_ptr[r]];
+        reduce_range_pipe(sorted, r, seg[2 * i], seg[2 * i + 1], u, s, out_rows, out_cols, out_blocks, R, lane);
+    }
 }
 
 __global__ void k_max_row(const std::uint64_t* __restrict__ keys, std::int64_t T, unsigned* __restrict__ out) {
@@ -666,12 +950,30 @@ static void bucket_sort(Ctx& c, const StreamSrc& s, std::int32_t n) {
                                                              c.counters.p + 1);
         ADIPC_LAUNCH_CHECK();
     }
-    int h_counters[2] = {0, 0};
+    int h_counters[4] = {0, 0, 0, 0};
     ADIPC_CUDA(cudaMemcpyAsync(h_counters, c.counters.p, sizeof(h_counters), cudaMemcpyDeviceToHost, st));
     ADIPC_CUDA(cudaStreamSynchronize(st));
     if (h_counters[0])
         throw StatusError(kInvalidArgument, "block row index >= n_block_rows in triplet stream");
-    c.sort_long_rows = h_counters[1];
+    c.sort_long_rows = h_counters[1] + h_counters[2];
+    if (h_counters[2] > 0) {  // rows > kHugeRow: chunk sorts + merge passes over the whole GPU
+        const int nh = h_counters[2], maxlen = h_counters[3];
+        c.merge_scratch.reserve(static_cast<std::size_t>(entries));
+        const std::int32_t* tail = c.big_rows.p + n;
+        const int smem = kCtaSortMax * sizeof(std::uint64_t);
+        ADIPC_CUDA(cudaFuncSetAttribute(k_huge_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        k_huge_chunks<<<dim3(static_cast<unsigned>(ceil_div(maxlen, kCtaSortMax)), nh), kCtaSortThreads, smem, st>>>(
+            c.sorted.p, c.row_start.p, tail, c.uniq_cnt.p);
+        ADIPC_LAUNCH_CHECK();
+        const dim3 tiles(static_cast<unsigned>(ceil_div(maxlen, kMergeTile)), nh);
+        int pass = 0;
+        for (int width = kCtaSortMax; width < maxlen; width <<= 1, ++pass) {
+            k_huge_merge<<<tiles, 256, 0, st>>>(c.sorted.p, c.merge_scratch.p, c.row_start.p, tail, width, pass);
+            ADIPC_LAUNCH_CHECK();
+        }
+        k_huge_finish<<<tiles, 256, 0, st>>>(c.sorted.p, c.merge_scratch.p, c.row_start.p, tail, c.uniq_cnt.p);
+        ADIPC_LAUNCH_CHECK();
+    }
     if (h_counters[1] > 0) {
         const int nb = h_counters[1];
         c.merge_scratch.reserve(static_cast<std::size_t>(entries));
@@ -722,11 +1024,13 @@ static void sort_reduce(Ctx& c, const StreamSrc& s, std::int32_t n, DeviceMatrix
     out.rows.reserve(static_cast<std::size_t>((U + 31) & ~std::int64_t(31)));
     out.cols.reserve(static_cast<std::size_t>((U + 31) & ~std::int64_t(31)));
     out.blocks.reserve(blk_doubles(U));
-    if (n > 0 && U > 0 && c.sort_long_rows == 0) {
+    if (n > 0 && U > 0) {
         k_reduce_rows<<<grid_for(n, 8, 16), 256, 0, st>>>(c.sorted.p, c.row_start.p, out.row_ptr.p, n, s, out.rows.p,
-                                                          out.cols.p, out.blocks.p);
+                                                          out.cols.p, out.blocks.p,
+                                                          c.sort_long_rows ? kLongRow : INT64_MAX);
         ADIPC_LAUNCH_CHECK();
-    } else if (n > 0 && U > 0) {  // long rows: one warp per ~kSegLen-entry segment
+    }
+    if (n > 0 && U > 0 && c.sort_long_rows) {  // rows > kLongRow: one warp per ~kSegLen-entry segment
         c.seg_cnt.reserve(static_cast<std::size_t>(n) + 1);
         c.seg_ptr.reserve(static_cast<std::size_t>(n) + 1);
         k_seg_count<<<grid_for(n, 256, 16), 256, 0, st>>>(c.row_start.p, n, c.seg_cnt.p);
@@ -735,6 +1039,10 @@ static void sort_reduce(Ctx& c, const StreamSrc& s, std::int32_t n, DeviceMatrix
         std::int64_t m = 0;
         ADIPC_CUDA(cudaMemcpyAsync(&m, c.seg_ptr.p + n, sizeof(m), cudaMemcpyDeviceToHost, st));
         ADIPC_CUDA(cudaStreamSynchronize(st));
+        if (m == 0) {  // no row beyond kLongRow: k_reduce_rows did them all
+            ++out.version;
+            return;
+        }
         c.seg_row.reserve(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)));
         c.seg_heads.reserve(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)));
         c.seg_bounds.reserve(static_cast<std::size_t>(std::max<std::int64_t>(2 * m, 1)));
@@ -745,8 +1053,10 @@ static void sort_reduce(Ctx& c, const StreamSrc& s, std::int32_t n, DeviceMatrix
                                                         c.seg_bounds.p, c.seg_heads.p);
         ADIPC_LAUNCH_CHECK();
         exclusive_scan(c.seg_heads.p, m, c.seg_u.p, c.scan_scratch, st);
-        k_reduce_segments<<<grid_for(m, 8, 16), 256, 0, st>>>(c.sorted.p, c.seg_row.p, c.seg_bounds.p, c.seg_u.p, m,
-                                                              s, out.rows.p, out.cols.p, out.blocks.p);
+        static_assert(kSegWarps * sizeof(SegRing) <= 48 * 1024, "k_reduce_segments ring exceeds the default smem");
+        k_reduce_segments<<<grid_for(m, kSegWarps, 16), 32 * kSegWarps, kSegWarps * sizeof(SegRing), st>>>(
+            c.sorted.p, c.seg_row.p, c.seg_bounds.p, c.seg_u.p, c.seg_ptr.p, out.row_ptr.p, m, s, out.rows.p,
+            out.cols.p, out.blocks.p);
         ADIPC_LAUNCH_CHECK();
     }
     ++out.version;

@@ -114,7 +114,7 @@ def test_edge_cases(ctx):
 
 
 @pytest.mark.parametrize("row_len", [1, 2, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 1000, 8191, 8192,
-                                     8193, 40000])
+                                     8193, 32768, 32769, 40000, 65537, 140000])
 def test_row_lengths(ctx, row_len):
     """Every row-sort regime: the register bitonic sorts of 32 / 64 / 128 / 256
     entries per warp and their boundaries, then rows longer than the warp sort
@@ -129,6 +129,23 @@ def test_row_lengths(ctx, row_len):
     keys = keys[perm]
     vals = rng.standard_normal((len(keys), 9))
     n = int(max(cols.max(), 51)) + 1
+    assert_bitwise(gpu_assemble(ctx, keys, vals, n), oracle_assemble(keys, vals, n))
+
+
+def test_mixed_huge_rows(ctx):
+    """Several rows beyond the multi-CTA sort limit (32,768 entries) with
+    different merge-pass counts (odd and even: they finish in different
+    ping-pong buffers), CTA-sorted rows, warp-sorted rows and long runs of
+    one column (the segment reduction's single-run windows) in one stream."""
+    rng = np.random.default_rng(77)
+    parts = []
+    for row, ln, ncol in ((5, 50000, 40), (9, 70000, 3000), (2, 20000, 7), (11, 300, 50), (0, 40, 10)):
+        cols = rng.integers(row, row + ncol, ln)
+        parts.append((np.uint64(row) << np.uint64(32)) | cols.astype(np.uint64))
+    keys = np.concatenate(parts).astype(np.uint64)
+    keys = keys[rng.permutation(len(keys))]
+    vals = rng.standard_normal((len(keys), 9))
+    n = 3100
     assert_bitwise(gpu_assemble(ctx, keys, vals, n), oracle_assemble(keys, vals, n))
 
 

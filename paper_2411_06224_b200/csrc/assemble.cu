@@ -365,7 +365,9 @@ __global__ void k_sort_rows_cta(std::uint64_t* __restrict__ sorted, std::uint64_
 // bitonic), then log2 merge passes in which every kMergeTile-element tile
 // of the output is one CTA (merge-path split of its pair of runs), ping-pong
 // between `sorted` and `scratch`, and a final pass that moves odd-pass rows
-// back and counts the unique columns. Rows are big_rows[n - 1 - y].
+// back and counts the unique columns. Rows are big_rows[n - 1 - y]; the
+// host turns their lengths into exact (row, chunk / tile) work lists, so no
+// CTA is launched past a row's end.
 __device__ __forceinline__ int merge_split(const std::uint64_t* a, int na, const std::uint64_t* b, int nb, int d) {
     int lo = max(0, d - nb), hi = min(d, na);
     while (lo < hi) {
@@ -382,17 +384,26 @@ __device__ __forceinline__ int huge_passes(int len) {
     for (int w = kCtaSortMax; w < len; w <<= 1) ++p;
     return p;
 }
+// (row, length) of the huge rows, for the host's work lists
+__global__ void k_huge_info(const std::int32_t* __restrict__ huge_tail, const std::int64_t* __restrict__ row_start,
+                            int nh, std::int32_t* __restrict__ info) {
+    for (int y = blockIdx.x * blockDim.x + threadIdx.x; y < nh; y += gridDim.x * blockDim.x) {
+        const std::int32_t r = huge_tail[-1 - y];
+        info[2 * y] = r;
+        info[2 * y + 1] = static_cast<std::int32_t>(row_start[r + 1] - row_start[r]);
+    }
+}
+// work item k = (row r, chunk / tile x) at work[2 k], work[2 k + 1]
 __global__ void __launch_bounds__(kCtaSortThreads) k_huge_chunks(std::uint64_t* __restrict__ sorted,
                                                                  const std::int64_t* __restrict__ row_start,
-                                                                 const std::int32_t* __restrict__ huge_tail,
+                                                                 const std::int32_t* __restrict__ work,
                                                                  std::int32_t* __restrict__ uniq_cnt) {
     extern __shared__ std::uint64_t s[];
-    const std::int32_t r = huge_tail[-1 - static_cast<int>(blockIdx.y)];
+    const std::int32_t r = work[2 * blockIdx.x];
     const std::int64_t b = row_start[r];
     const int len = static_cast<int>(row_start[r + 1] - b);
-    const int c0 = static_cast<int>(blockIdx.x) * kCtaSortMax;
-    if (c0 >= len) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) uniq_cnt[r] = 0;  // k_huge_finish adds the tiles' heads
+    const int c0 = work[2 * blockIdx.x + 1] * kCtaSortMax;
+    if (c0 == 0 && threadIdx.x == 0) uniq_cnt[r] = 0;  // k_huge_finish adds the tiles' heads
     std::uint64_t* seg = sorted + b + c0;
     const int cl = min(kCtaSortMax, len - c0);
     int N = 2;
@@ -405,13 +416,12 @@ __global__ void __launch_bounds__(kCtaSortThreads) k_huge_chunks(std::uint64_t* 
 __global__ void __launch_bounds__(256) k_huge_merge(std::uint64_t* __restrict__ sorted,
                                                     std::uint64_t* __restrict__ scratch,
                                                     const std::int64_t* __restrict__ row_start,
-                                                    const std::int32_t* __restrict__ huge_tail, int width, int pass) {
+                                                    const std::int32_t* __restrict__ work, int width, int pass) {
     __shared__ int split[2];
-    const std::int32_t r = huge_tail[-1 - static_cast<int>(blockIdx.y)];
+    const std::int32_t r = work[2 * blockIdx.x];
     const std::int64_t b = row_start[r];
     const int len = static_cast<int>(row_start[r + 1] - b);
-    const int g0 = static_cast<int>(blockIdx.x) * kMergeTile;
-    if (len <= width || g0 >= len) return;  // row already merged / tile past its end
+    const int g0 = work[2 * blockIdx.x + 1] * kMergeTile;
     const std::uint64_t* src = ((pass & 1) ? scratch : sorted) + b;
     std::uint64_t* dst = ((pass & 1) ? sorted : scratch) + b;
     const int a0 = g0 / (2 * width) * (2 * width);  // kMergeTile divides 2 width
@@ -428,14 +438,13 @@ __global__ void __launch_bounds__(256) k_huge_merge(std::uint64_t* __restrict__ 
 __global__ void __launch_bounds__(256) k_huge_finish(std::uint64_t* __restrict__ sorted,
                                                      const std::uint64_t* __restrict__ scratch,
                                                      const std::int64_t* __restrict__ row_start,
-                                                     const std::int32_t* __restrict__ huge_tail,
+                                                     const std::int32_t* __restrict__ work,
                                                      std::int32_t* __restrict__ uniq_cnt) {
     __shared__ int red[8];
-    const std::int32_t r = huge_tail[-1 - static_cast<int>(blockIdx.y)];
+    const std::int32_t r = work[2 * blockIdx.x];
     const std::int64_t b = row_start[r];
     const int len = static_cast<int>(row_start[r + 1] - b);
-    const int g0 = static_cast<int>(blockIdx.x) * kMergeTile;
-    if (g0 >= len) return;
+    const int g0 = work[2 * blockIdx.x + 1] * kMergeTile;
     const int g1 = min(g0 + kMergeTile, len);
     const bool odd = huge_passes(len) & 1;
     const std::uint64_t* fin = (odd ? scratch : sorted) + b;
@@ -959,20 +968,49 @@ static void bucket_sort(Ctx& c, const StreamSrc& s, std::int32_t n) {
     if (h_counters[2] > 0) {  // rows > kHugeRow: chunk sorts + merge passes over the whole GPU
         const int nh = h_counters[2], maxlen = h_counters[3];
         c.merge_scratch.reserve(static_cast<std::size_t>(entries));
-        const std::int32_t* tail = c.big_rows.p + n;
+        c.huge_info.reserve(2 * static_cast<std::size_t>(nh));
+        k_huge_info<<<ceil_div(nh, 256), 256, 0, st>>>(c.big_rows.p + n, c.row_start.p, nh, c.huge_info.p);
+        ADIPC_LAUNCH_CHECK();
+        std::vector<std::int32_t> info(2 * static_cast<std::size_t>(nh));
+        ADIPC_CUDA(cudaMemcpyAsync(info.data(), c.huge_info.p, info.size() * sizeof(std::int32_t),
+                                   cudaMemcpyDeviceToHost, st));
+        ADIPC_CUDA(cudaStreamSynchronize(st));
+        // work lists: chunks, then each merge pass's tiles, then the finish tiles
+        std::vector<std::int32_t> work;
+        std::vector<std::size_t> start;  // offset (in items) of each list
+        auto list = [&](int unit, int min_len) {
+            start.push_back(work.size() / 2);
+            for (int y = 0; y < nh; ++y)
+                if (info[2 * y + 1] > min_len)
+                    for (int x = 0; x < ceil_div(info[2 * y + 1], unit); ++x) {
+                        work.push_back(info[2 * y]);
+                        work.push_back(x);
+                    }
+        };
+        list(kCtaSortMax, 0);
+        int passes = 0;
+        for (int width = kCtaSortMax; width < maxlen; width <<= 1, ++passes) list(kMergeTile, width);
+        list(kMergeTile, 0);
+        start.push_back(work.size() / 2);
+        c.huge_work.reserve(work.size());
+        ADIPC_CUDA(cudaMemcpyAsync(c.huge_work.p, work.data(), work.size() * sizeof(std::int32_t),
+                                   cudaMemcpyHostToDevice, st));
+        auto items = [&](int i) { return static_cast<unsigned>(start[i + 1] - start[i]); };
+        auto at = [&](int i) { return c.huge_work.p + 2 * start[i]; };
         const int smem = kCtaSortMax * sizeof(std::uint64_t);
         ADIPC_CUDA(cudaFuncSetAttribute(k_huge_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        k_huge_chunks<<<dim3(static_cast<unsigned>(ceil_div(maxlen, kCtaSortMax)), nh), kCtaSortThreads, smem, st>>>(
-            c.sorted.p, c.row_start.p, tail, c.uniq_cnt.p);
+        k_huge_chunks<<<items(0), kCtaSortThreads, smem, st>>>(c.sorted.p, c.row_start.p, at(0), c.uniq_cnt.p);
         ADIPC_LAUNCH_CHECK();
-        const dim3 tiles(static_cast<unsigned>(ceil_div(maxlen, kMergeTile)), nh);
-        int pass = 0;
-        for (int width = kCtaSortMax; width < maxlen; width <<= 1, ++pass) {
-            k_huge_merge<<<tiles, 256, 0, st>>>(c.sorted.p, c.merge_scratch.p, c.row_start.p, tail, width, pass);
+        for (int pass = 0, width = kCtaSortMax; pass < passes; ++pass, width <<= 1) {
+            k_huge_merge<<<items(1 + pass), 256, 0, st>>>(c.sorted.p, c.merge_scratch.p, c.row_start.p, at(1 + pass),
+                                                          width, pass);
             ADIPC_LAUNCH_CHECK();
         }
-        k_huge_finish<<<tiles, 256, 0, st>>>(c.sorted.p, c.merge_scratch.p, c.row_start.p, tail, c.uniq_cnt.p);
+        k_huge_finish<<<items(1 + passes), 256, 0, st>>>(c.sorted.p, c.merge_scratch.p, c.row_start.p,
+                                                         at(1 + passes), c.uniq_cnt.p);
         ADIPC_LAUNCH_CHECK();
+        // the host vector must outlive the upload
+        ADIPC_CUDA(cudaStreamSynchronize(st));
     }
     if (h_counters[1] > 0) {
         const int nb = h_counters[1];

@@ -139,6 +139,8 @@ int adipc_gpu_destroy(adipc_gpu_ctx* ctx) {
     c.keys.free();
     c.sorted.free();
     c.merge_scratch.free();
+    c.huge_info.free();
+    c.huge_work.free();
     c.vals.free();
     c.row_cnt.free();
     c.row_cursor.free();

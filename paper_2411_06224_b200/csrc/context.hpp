@@ -127,6 +127,7 @@ struct Ctx {
     DBuf<std::int32_t> row_cnt, row_cursor, uniq_cnt, big_rows;
     DBuf<std::int64_t> row_start, uniq_start, scan_scratch;
     DBuf<std::int32_t> counters;
+    DBuf<std::int32_t> huge_info, huge_work;  // rows > kHugeRow: (row, len) and the (row, chunk / tile) work lists
     DBuf<std::uint8_t> pinned;
     DBuf<std::int32_t> pin_keep;
     DBuf<std::int64_t> pin_pos, pin_spos;

@@ -500,7 +500,13 @@ __device__ __forceinline__ void reduce_range(const std::uint64_t* __restrict__ s
                                              double (*Tl)[33], double* C, int lane) {
     bool carried = false;       // a run continues into this window (warp-uniform)
     std::int64_t carry_u = 0;   // its output slot
-    for (std::int64_t base = b; base < e; base += 32) {
+    // the carried partial sums, two slots by window parity: lane 0 reads the
+    // incoming one while the owner of the window's last run may already
+    // write the outgoing one (no lane order inside a window)
+    int par = 0;
+    for (std::int64_t base = b; base < e; base += 32, par ^= 1) {
+        const double* Cin = C + 9 * par;
+        double* Cout = C + 9 * (par ^ 1);
         const std::int64_t p = base + lane;
         const bool valid = p < e;
         const std::uint64_t v = valid ? sorted[p] : ~0ull;
@@ -535,7 +541,7 @@ __device__ __forceinline__ void reduce_range(const std::uint64_t* __restrict__ s
                 for (int k = 0; k < 9; ++k) acc[k] = Tl[k][lane];
             } else {  // continuing run: carried sum, then this window's entries
 #pragma unroll
-                for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(C[k], Tl[k][lane]);
+                for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(Cin[k], Tl[k][lane]);
             }
             for (int j = lane + 1; j < end; ++j)
 #pragma unroll
@@ -543,7 +549,7 @@ __device__ __forceinline__ void reduce_range(const std::uint64_t* __restrict__ s
             const std::int64_t my_u = head ? u + __popc(hm & ((1u << lane) - 1u)) : carry_u;
             if (end == nv && cont_out) {  // hand over to the next window
 #pragma unroll
-                for (int k = 0; k < 9; ++k) C[k] = acc[k];
+                for (int k = 0; k < 9; ++k) Cout[k] = acc[k];
             } else {
                 out_rows[my_u] = static_cast<std::uint32_t>(r);
                 out_cols[my_u] = col;
@@ -564,7 +570,7 @@ __global__ void __launch_bounds__(32 * kReduceWarps, 3) k_reduce_rows(
     const std::int64_t* __restrict__ uniq_start, std::int32_t n, StreamSrc s, std::uint32_t* __restrict__ out_rows,
     std::uint32_t* __restrict__ out_cols, double* __restrict__ out_blocks, std::int64_t max_len) {
     __shared__ double tile[kReduceWarps][9][33];
-    __shared__ double carry[kReduceWarps][9];
+    __shared__ double carry[kReduceWarps][18];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
     for (std::int32_t r = blockIdx.x * (blockDim.x >> 5) + w; r < n; r += warps)
@@ -657,7 +663,7 @@ constexpr int kSegWarps = 4;
 struct SegRing {
     double v[kValAhead][9][33];
     std::uint64_t k[kKeyAhead][32];
-    double carry[9];
+    double carry[2][9];  // by window parity (see reduce_range)
 };
 __device__ __forceinline__ void reduce_range_pipe(const std::uint64_t* __restrict__ sorted, std::int32_t r,
                                                   std::int64_t b, std::int64_t e, std::int64_t u, const StreamSrc& s,
@@ -736,11 +742,11 @@ __device__ __forceinline__ void reduce_range_pipe(const std::uint64_t* __restric
             // left-to-right order per element)
             const std::int64_t my_u = hm ? u : carry_u;
             if (lane < 9) {
-                double acc = hm ? Tl[lane][0] : __dadd_rn(R.carry[lane], Tl[lane][0]);
+                double acc = hm ? Tl[lane][0] : __dadd_rn(R.carry[w & 1][lane], Tl[lane][0]);
 #pragma unroll 8
                 for (int j = 1; j < nv; ++j) acc = __dadd_rn(acc, Tl[lane][j]);
                 if (cont_out)
-                    R.carry[lane] = acc;
+                    R.carry[(w & 1) ^ 1][lane] = acc;
                 else
                     out_blocks[blk(my_u, lane)] = acc;
             }
@@ -767,7 +773,7 @@ __device__ __forceinline__ void reduce_range_pipe(const std::uint64_t* __restric
                 for (int k = 0; k < 9; ++k) acc[k] = Tl[k][lane];
             } else {
 #pragma unroll
-                for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(R.carry[k], Tl[k][lane]);
+                for (int k = 0; k < 9; ++k) acc[k] = __dadd_rn(R.carry[w & 1][k], Tl[k][lane]);
             }
             for (int j = lane + 1; j < end; ++j)
 #pragma unroll
@@ -775,7 +781,7 @@ __device__ __forceinline__ void reduce_range_pipe(const std::uint64_t* __restric
             const std::int64_t my_u = head ? u + __popc(hm & ((1u << lane) - 1u)) : carry_u;
             if (end == nv && cont_out) {
 #pragma unroll
-                for (int k = 0; k < 9; ++k) R.carry[k] = acc[k];
+                for (int k = 0; k < 9; ++k) R.carry[(w & 1) ^ 1][k] = acc[k];
             } else {
                 out_rows[my_u] = static_cast<std::uint32_t>(r);
                 out_cols[my_u] = col;

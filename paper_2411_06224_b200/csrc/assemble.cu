@@ -155,15 +155,16 @@ template <bool kWarp>
 __device__ __forceinline__ void bitonic(std::uint64_t* s, int N, int tid, int nthr) {
     for (int k = 2; k <= N; k <<= 1)
         for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = tid; i < N; i += nthr) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const std::uint64_t a = s[i], b = s[ixj];
-                    const bool up = (i & k) == 0;
-                    if ((a > b) == up) {
-                        s[i] = b;
-                        s[ixj] = a;
-                    }
+            // one compare-exchange per pair p: i = the pair's lower index
+            // (bit j clear), its partner i + j — no idle half of the threads
+            for (int p = tid; p < (N >> 1); p += nthr) {
+                const int i = 2 * p - (p & (j - 1));
+                const int ixj = i + j;
+                const std::uint64_t a = s[i], b = s[ixj];
+                const bool up = (i & k) == 0;
+                if ((a > b) == up) {
+                    s[i] = b;
+                    s[ixj] = a;
                 }
             }
             if (kWarp)

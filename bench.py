@@ -115,20 +115,43 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.samples = []
+        self.sampler = None
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml(self):
+        """NVML handle (nvidia-ml-py) for 20 ms sampling, or None: nvidia-smi
+        then (one process per sample, ~0.3 s each)."""
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            return N, N.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            return None
+
     def _run(self):
+        nv = self._nvml()
+        self.sampler = "nvml" if nv else "nvidia-smi"
+        bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap (NVML event reasons)
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                f = [x.strip() for x in out.stdout.strip().split(",")]
-                if len(f) >= 6:
-                    self.samples.append(f)
+                if nv:
+                    N, h = nv
+                    get = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                        N.nvmlDeviceGetCurrentClocksThrottleReasons
+                    r = get(h)
+                    self.samples.append([str(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)),
+                                         str(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))] +
+                                        ["Active" if r & b else "Not Active" for b in bits])
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                    f = [x.strip() for x in out.stdout.strip().split(",")]
+                    if len(f) >= 6:
+                        self.samples.append(f)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.02 if nv else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -148,7 +171,7 @@ class ClockSampler:
         reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
                           and "Not" not in s[2 + i]})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples), "sampler": self.sampler}
 
 
 # ------------------------------------------------------------- byte model ---

@@ -254,22 +254,33 @@ __device__ __forceinline__ int pick_cols(int dim) {
     return kK;
 }
 
+// kK = 48 splits the rows 32 / 16 (ADIPC_PC_SPLIT32): every shared load of
+// warp 0 then serves 32 rows and warp 1's 16 rows take one wavefront, 3/4
+// of the wavefronts of the 24 / 24 split whose loads each fed 24 of 32 lanes
+#ifndef ADIPC_PC_SPLIT32
+#define ADIPC_PC_SPLIT32 1
+#endif
+template <int kK>
+__device__ __forceinline__ constexpr int pair_split() {
+    return (kK == 48 && ADIPC_PC_SPLIT32) ? 32 : kK / 2;
+}
 template <int kK, class Store>
 __device__ __forceinline__ double pair_rows_solve(const double* M, const double* bs, int lane, int half, int dim,
                                                   Store store) {
-    constexpr int kHalf = kK / 2;
-    constexpr int RY = (kHalf + 31) / 32;
+    constexpr int kS = pair_split<kK>();
+    constexpr int RY = ((kS > kK - kS ? kS : kK - kS) + 31) / 32;
     double y[RY];
     if (half == 0)
-        packed_matvec_rows<kK, 0, kHalf>(M, bs, y, lane);
+        packed_matvec_rows<kK, 0, kS>(M, bs, y, lane);
     else
-        packed_matvec_rows<kK, kHalf, kHalf>(M, bs, y, lane);
+        packed_matvec_rows<kK, kS, kK - kS>(M, bs, y, lane);
+    const int rows = half == 0 ? kS : kK - kS;
     double dsum = 0;
 #pragma unroll
     for (int t = 0; t < RY; ++t) {
         const int i = lane + 32 * t;
-        const int j = half == 0 ? matvec_row<kK, 0>(lane, t) : matvec_row<kK, kHalf>(lane, t);
-        if (i < kHalf && j < dim) {
+        const int j = half == 0 ? matvec_row<kK, 0>(lane, t) : matvec_row<kK, kS>(lane, t);
+        if (i < rows && j < dim) {
             store(j, y[t]);
             dsum += bs[j] * y[t];
         }

@@ -21,6 +21,7 @@
 // (reduction.hpp:39-53: left-to-right adds, no FMA involved); the parallel
 // mode of the reference differs from it only by rounding (<= 1e-12).
 #include <algorithm>
+#include <vector>
 
 #include "context.hpp"
 #include "scan.cuh"
